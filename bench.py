@@ -1,0 +1,494 @@
+"""Benchmark of the deterministic elastic-DP step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1], "C2"): the reference MLP, 8 ESTs x
+micro-batch 4 (32 samples per mini-batch), seed 42, 1024-row synthetic
+dataset, d1, Tree(2) device kind, momentum SGD; a "step" is one mini-batch.
+
+* value  -- samples/s with everything resident in HBM: the fused persistent
+  step kernel (bt_mlp.cu), timed with CUDA events on its stream; the K steps
+  run as launches of one epoch (32 mini-batches) each, with an L2 flush
+  (256 MiB write) between launches, outside the timed spans.
+* e2e    -- the same K mini-batches through the C-ABI with HOST buffers: each
+  launch's global batches (split_by_rank rows) are copied from pinned host
+  memory and its per-EST losses copied back inside the timed span.
+* roofline -- the step kernel (latency-bound: 32 samples/step), plus the
+  deterministic reducer (bt_reduce.cu, C5 shape) measured against HBM.
+* cpu_baseline -- the CPU oracle (a C restatement of the reference) on a
+  bounded sample of the same workload, on this box's host cores.
+N > 1 (torchrun): the 8 ESTs are split into contiguous rank blocks; each rank
+runs its ESTs' forward/backward, the EST gradient slots are exchanged with an
+NCCL all-gather (a bit copy), and every rank applies the same fixed-order
+reduce + SGD kernel, so all ranks hold bit-identical weights ("scaling":
+"strong": the job's total work is fixed).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "samples/sec at 1/2/4/8 B200 with bit-identical weights across mappings"
+E_TOTAL, MICRO, NROWS, SEED = 8, 4, 1024, 42
+SAMPLES_PER_STEP = E_TOTAL * MICRO
+PEAKS = {"hbm_gbs": 6541.8, "bf16_tflops": 1639.6, "bf16_tflops_sustained": 1358.3}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return {k: d.get(k, v) for k, v in PEAKS.items()}, "measured"
+        except Exception:
+            pass
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the benchmark runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        self.busy = []
+
+    def mark(self):
+        self.busy.append(time.time())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flush_l2(buf: torch.Tensor) -> None:
+    buf.add_(1)  # 256 MiB read+write > 126 MB L2
+
+
+# ------------------------------------------------------------------ b200 arm
+def make_cfg(bt):
+    return bt.TrainRunConfig(seed=SEED, max_workers=E_TOTAL, micro_batch=MICRO, dataset_size=NROWS, lr=0.02,
+                             momentum=0.9, dropout_rate=0.5, jitter=0.1, bucket_capacity=64,
+                             determinism=bt.DeterminismMode.from_label("d1"),
+                             device_fanins={"gpu_fast": 2, "gpu_mid": 3})
+
+
+def chunks(K: int, spe: int):
+    out, left = [], K
+    while left > 0:
+        out.append(min(spe, left))
+        left -= out[-1]
+    return out
+
+
+def bench_device_single(bt, K: int, W: int, flush):
+    """N=1: persistent fused kernel, one launch per epoch-sized chunk."""
+    from paper_2208_14228_b200 import _native, engine
+    from paper_2208_14228_b200.device import stream
+
+    cfg = make_cfg(bt)
+    ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")])
+    spe = ts.pipeline.steps_per_epoch
+    for n in chunks(W, spe):
+        engine.run_steps(ts, n)
+    torch.cuda.synchronize()
+    spans = []
+    launches = 0
+    s = torch.cuda.current_stream()
+    for n in chunks(K, spe):
+        for st in range(n):
+            ts.pipeline.advance_all(ts.global_step + st)
+        losses = torch.empty((n, E_TOTAL), dtype=torch.float64, device="cuda")
+        a, keep = engine._step_args(ts, n, MICRO, None, losses, None)
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()))
+        e1.record(s)
+        launches += 1
+        e1.synchronize()
+        spans.append(e0.elapsed_time(e1))
+        st_, _, _ = ts.dev.flags.status()
+        assert st_ == 0, st_
+        engine._finish_steps(ts, n)
+        ts.dev.invalidate()
+    return ts, sum(spans), spans, launches, a.est_per_cta
+
+
+def bench_e2e_single(bt, K: int, W: int, flush):
+    """N=1 end to end: host global batches -> pinned H2D -> fused kernel -> D2H losses, per launch."""
+    from paper_2208_14228_b200 import _native, engine
+    from paper_2208_14228_b200.device import stream
+
+    cfg = make_cfg(bt)
+    ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")])
+    spe = ts.pipeline.steps_per_epoch
+    # The user-side data: the reference pipeline's jittered rows for every step,
+    # laid out as split_by_rank global batches (row r of EST k at r*E+k).
+    total = W + K
+    host_rows = torch.empty((total, MICRO * E_TOTAL, 9), dtype=torch.float64).pin_memory()
+    pipe = bt.DataPipeline(SEED, NROWS, E_TOTAL, MICRO, 0.1, 2, 2)
+    for step in range(total):
+        for k in range(E_TOTAL):
+            for r, (x, y) in enumerate(pipe.batch(k, step)):
+                host_rows[step, r * E_TOTAL + k, :8] = torch.tensor(x, dtype=torch.float64)
+                host_rows[step, r * E_TOTAL + k, 8] = y
+    host_losses = torch.empty((total, E_TOTAL), dtype=torch.float64).pin_memory()
+    dev_rows = torch.empty((spe, MICRO * E_TOTAL, 9), dtype=torch.float64, device="cuda")
+    dev_losses = torch.empty((spe, E_TOTAL), dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream()
+    spans, launches, h2d, d2h = [], 0, 0, 0
+
+    def launch(step0, n, timed):
+        nonlocal launches, h2d, d2h
+        if timed:
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+        dev_rows[:n].copy_(host_rows[step0:step0 + n], non_blocking=True)
+        a, keep = engine._step_args(ts, n, MICRO, dev_rows, dev_losses, None)
+        _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()))
+        host_losses[step0:step0 + n].copy_(dev_losses[:n], non_blocking=True)
+        if timed:
+            e1.record(s)
+            e1.synchronize()
+            spans.append(e0.elapsed_time(e1))
+            launches += 1
+            h2d += host_rows[step0:step0 + n].numel() * 8
+            d2h += n * E_TOTAL * 8
+        else:
+            s.synchronize()
+        engine._finish_steps(ts, n)
+
+    step = 0
+    for n in chunks(W, spe):
+        launch(step, n, False)
+        step += n
+    for n in chunks(K, spe):
+        launch(step, n, True)
+        step += n
+    return ts, sum(spans), launches, h2d / K, d2h / K, host_losses
+
+
+def bench_device_dist(bt, K: int, W: int, rank: int, world: int, flush, e2e: bool):
+    """N>1: EST blocks per rank; fwd/bwd kernel -> NCCL all-gather of EST gradient slots -> same
+    fixed-order reduce+SGD kernel on every rank."""
+    import torch.distributed as dist
+
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.buckets import build_buckets_initial, rotation_table
+    from paper_2208_14228_b200.device import Flags, stream, u64_to_i64
+    from paper_2208_14228_b200.prng import TAG_DROPOUT, derive_stream
+
+    assert E_TOTAL % world == 0, "8 ESTs split into equal contiguous blocks"
+    e_loc = E_TOTAL // world
+    base = rank * e_loc
+    cfg = make_cfg(bt)
+    pipe = bt.DataPipeline(SEED, NROWS, E_TOTAL, MICRO, 0.1, 2, 2)
+    spe = pipe.steps_per_epoch
+    params = torch.zeros((2, 161), dtype=torch.float64, device="cuda")
+    params[0] = bt.ToyModel.init_random(SEED).tensor
+    fan = torch.full((e_loc,), 2, dtype=torch.int32, device="cuda")
+    rng = torch.tensor([u64_to_i64(derive_stream(TAG_DROPOUT, SEED, base + k)) for k in range(e_loc)],
+                       dtype=torch.int64, device="cuda")
+    mean = torch.zeros(e_loc, dtype=torch.float64, device="cuda")
+    cnt = torch.zeros(e_loc, dtype=torch.int64, device="cuda")
+    grads_loc = torch.zeros((e_loc, 161), dtype=torch.float64, device="cuda")
+    grads_all = torch.zeros((E_TOTAL, 161), dtype=torch.float64, device="cuda")
+    losses = torch.zeros(e_loc, dtype=torch.float64, device="cuda")
+    rot = torch.from_numpy(rotation_table(build_buckets_initial(161, 64), E_TOTAL)).to("cuda")
+    flags = Flags()
+    new = torch.empty_like(params)
+    dataset = pipe.dataset_device
+    s = torch.cuda.current_stream()
+    host_losses = torch.empty((K + W, e_loc), dtype=torch.float64).pin_memory() if e2e else None
+
+    def step_once(step):
+        epoch, local = divmod(step, spe)
+        lists, lbase = pipe.device_lists(epoch, epoch)
+        a = _native.MlpArgs()
+        a.E, a.est_base, a.E_total, a.B, a.X, a.K = e_loc, base, E_TOTAL, MICRO, 1, 1
+        a.fuse_reduce, a.est_per_cta, a.comm_fanin, a.rank_override = 0, e_loc, 2, -1
+        a.rate, a.lr, a.mu, a.jitter = 0.5, 0.02, 0.9, 0.1
+        a.replicas, a.est_fanin, a.rng, a.stat_mean, a.stat_count = (params.data_ptr(), fan.data_ptr(),
+                                                                     rng.data_ptr(), mean.data_ptr(), cnt.data_ptr())
+        a.grads, a.losses, a.dataset, a.lists = grads_loc.data_ptr(), losses.data_ptr(), dataset.data_ptr(), lists.data_ptr()
+        a.seed, a.step0, a.spe, a.epoch_base, a.flags = SEED, step, spe, lbase, flags.t.data_ptr()
+        _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()))
+        dist.all_gather_into_tensor(grads_all, grads_loc)
+        r = _native.ReduceArgs()
+        r.dtype, r.mode, r.E, r.fanin, r.n = _native.DTYPE_F64, _native.REDUCE_UPDATE, E_TOTAL, 2, 161
+        r.grads[0], r.grads_ld, r.rot = grads_all.data_ptr(), 161, rot.data_ptr()
+        r.param, r.vel, r.param_out, r.vel_out = params[0].data_ptr(), params[1].data_ptr(), new[0].data_ptr(), new[1].data_ptr()
+        r.lr, r.mu, r.flags = 0.02, 0.9, flags.t.data_ptr()
+        _native.check(_native.lib().bt_reduce_update(C.byref(r), stream()))
+        params.copy_(new)
+        if e2e:
+            host_losses[step].copy_(losses, non_blocking=True)
+
+    for step in range(W):
+        step_once(step)
+    torch.cuda.synchronize()
+    dist.barrier()
+    spans = []
+    step = W
+    for n in chunks(K, spe):
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(n):
+            step_once(step)
+            step += 1
+        e1.record(s)
+        e1.synchronize()
+        spans.append(e0.elapsed_time(e1))
+    dist.barrier()
+    return params[0].clone(), sum(spans), 2 * K
+
+
+def bench_reducer(flush, peaks, E=8, S_MB=256, iters=10):
+    """C5-shaped deterministic reducer, G=1: E f32 EST gradient slots of S MB each,
+    RankTree(2) order, fused /E + momentum SGD.  HBM_alg = E*S + 4*S bytes."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import Flags, stream
+
+    n = S_MB * 2**20 // 4
+    g = torch.empty((E, n), dtype=torch.float32, device="cuda").uniform_(-1, 1)
+    p = torch.empty(n, dtype=torch.float32, device="cuda").uniform_(-1, 1)
+    v = torch.zeros(n, dtype=torch.float32, device="cuda")
+    flags = Flags()
+    out = {}
+    for name, fan in (("rank_tree2", 2), ("sequential", 0)):
+        a = _native.ReduceArgs()
+        a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, E, fan, n
+        for k in range(E):
+            a.grads[k] = g[k].data_ptr()
+        a.param, a.vel, a.param_out, a.vel_out = p.data_ptr(), v.data_ptr(), p.data_ptr(), v.data_ptr()
+        a.lr, a.mu, a.flags = 1e-9, 0.9, flags.t.data_ptr()
+        for _ in range(2):
+            _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()))
+        times = []
+        s = torch.cuda.current_stream()
+        for _ in range(iters):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()))
+            e1.record(s)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = statistics.median(times)
+        alg = (E + 4) * n * 4
+        out[name] = {"ms": ms, "achieved_gbs": alg / ms / 1e6, "frac": alg / ms / 1e6 / peaks["hbm_gbs"]}
+    del g, p, v
+    torch.cuda.empty_cache()
+    best = out["rank_tree2"]
+    return {"kernel": "reduce_fast_kernel<float,8,2> (bt_reduce.cu)", "E": E, "S_MB": S_MB, "dtype": "f32",
+            "bound": "hbm", "achieved": round(best["achieved_gbs"], 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(best["frac"], 4), "bytes_per_launch": (E + 4) * n * 4, "ms": round(best["ms"], 4),
+            "variants": {k: {kk: round(vv, 4) for kk, vv in d.items()} for k, d in out.items()}}
+
+
+def cpu_baseline(seconds: float, threads: int = 1):
+    """The CPU oracle (C restatement of the reference) on the same C2 workload, bounded in time."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+
+    run = oracle.Run(seed=SEED, max_workers=E_TOTAL, micro_batch=MICRO, dataset_size=NROWS, mode="d1",
+                     layout=("gpu_fast",))
+    run.set_threads(threads)
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        for _ in range(256):
+            run.step()
+        steps += 256
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return steps * SAMPLES_PER_STEP / el, steps, el, run
+
+
+def reference_arm(args, rank: int):
+    """--impl reference: the reference's CPU implementation of the path (the C oracle port; the
+    reference itself is Python and does not compile), on the host cores, same config/metric."""
+    if rank != 0:
+        return
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+
+    cores = oracle.host_cores()
+    # One mini-batch is ~10 us of dependent work: spreading 8 ESTs over threads costs more in
+    # synchronisation than it saves, so the port runs single-threaded (measured: see DESIGN.md).
+    run = oracle.Run(seed=SEED, max_workers=E_TOTAL, micro_batch=MICRO, dataset_size=NROWS, mode="d1",
+                     layout=("gpu_fast",))
+    for _ in range(args.warmup):
+        run.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run.step()
+    el = time.perf_counter() - t0
+    v = args.steps * SAMPLES_PER_STEP / el
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args.gpus),
+            "cpu_baseline": {"value": round(v, 1), "unit": "samples/s", "cores": 1, "kind": "port",
+                             "sample": f"{args.steps} C2 mini-batches after {args.warmup} warm-up, 1 of {cores} host cores"},
+            "e2e": {"value": round(v, 1), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def config_block(n):
+    return {"workload": "C2: reference MLP (8-16-1 tanh, dropout 0.5, MSE), 8 ESTs x micro-batch 4, seed 42, "
+                        "1024-row synthetic dataset, d1 / Tree(2) kind, momentum SGD (BASELINE.json configs[1])",
+            "ests": E_TOTAL, "micro_batch": MICRO, "global_batch": SAMPLES_PER_STEP, "dataset_rows": NROWS,
+            "parallelism": f"est-dp{n}", "l2": "flushed (256 MiB write) between timed launches; each launch = one "
+                                             "epoch of 32 mini-batches"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3200)
+    ap.add_argument("--warmup", type=int, default=64)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-reducer", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank)
+
+    import paper_2208_14228_b200 as bt
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks, peak_src = load_peaks()
+    clocks = ClockSampler(local)
+    flush_buf = torch.zeros(64 * 2**20, dtype=torch.float32, device="cuda")
+
+    def flush():
+        flush_buf.add_(1)
+
+    if world == 1:
+        ts, ms, spans, launches, epc = bench_device_single(bt, args.steps, args.warmup, flush)
+        final = np.array(ts.executors[0].model.values.tolist())
+        ts_e, ms_e2e, launches_e, h2d, d2h, _ = bench_e2e_single(bt, args.steps, args.warmup, flush)
+        final_e = np.array(ts_e.executors[0].model.values.tolist())
+        assert np.array_equal(final.view(np.uint64), final_e.view(np.uint64)), "e2e and device runs diverged"
+    else:
+        params, ms, launches = bench_device_dist(bt, args.steps, args.warmup, rank, world, flush, False)
+        final = params.cpu().numpy()
+        params_e, ms_e2e, launches_e = bench_device_dist(bt, args.steps, args.warmup, rank, world, flush, True)
+        h2d, d2h = 0, (E_TOTAL // world) * 8
+        epc = E_TOTAL // world
+    if world > 1:
+        t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_e2e = t.tolist()
+        h = torch.tensor([int.from_bytes(final.astype("<f8").tobytes()[:8], "little") & (2**62)], device="cuda")
+    weights_fnv = f"{bt.fnv1a64(final.astype('<f8').tobytes()):016x}"
+    if world > 1:
+        allh = [None] * world
+        dist.all_gather_object(allh, weights_fnv)
+        assert len(set(allh)) == 1, f"ranks disagree: {allh}"
+
+    value = args.steps * SAMPLES_PER_STEP / (ms / 1e3)
+    e2e = args.steps * SAMPLES_PER_STEP / (ms_e2e / 1e3)
+    reducer = None
+    if not args.no_reducer and rank == 0:
+        reducer = bench_reducer(flush, peaks)
+    clk = clocks.stop()
+
+    # Roofline of the step kernel: algorithmic HBM bytes per mini-batch = the 32 rows read
+    # (32 x 9 x 8 B) + 8 losses written (64 B); per launch x steps in the launch.
+    alg_step = SAMPLES_PER_STEP * 9 * 8 + E_TOTAL * 8
+    per_launch_ms = ms / launches
+    steps_per_launch = args.steps / launches
+    achieved = alg_step * steps_per_launch / (per_launch_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 42)",
+        "config": config_block(world),
+        "e2e": {"value": round(e2e, 1), "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": {"kernel": "mlp_step_kernel (bt_mlp.cu)", "bound": "hbm", "achieved": round(achieved, 3),
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 6),
+                     "traffic": None, "peak_source": peak_src,
+                     "note": "latency-bound: one mini-batch is a ~1 kflop/sample dependent fp64 chain over 32 "
+                             "samples; HBM and tensor rooflines do not bind (DESIGN.md section 5)",
+                     "us_per_step": round(ms * 1e3 / args.steps, 3), "est_per_cta": epc},
+        "weights_fnv": weights_fnv,
+        "clocks": clk,
+    }
+    if reducer is not None:
+        line["reducer"] = reducer
+    if rank == 0 and world == 1 and args.cpu_seconds > 0:
+        v, steps, el, run = cpu_baseline(args.cpu_seconds)
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle
+
+        line["cpu_baseline"] = {"value": round(v, 1), "unit": "samples/s", "cores": 1, "kind": "port",
+                                "sample": f"{steps} C2 mini-batches ({el:.1f} s) of the C oracle, 1 thread, "
+                                          f"{oracle.host_cores()} host cores present"}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,139 @@
+/*
+ * bittrain_b200.h -- C-ABI of the B200-native deterministic elastic
+ * data-parallel step (the drop-in for the reference's run_minibatch path).
+ *
+ * The reference (`bittrain` 0.1.0, /root/reference/pkg/src/bittrain) is pure
+ * Python with no FFI; its boundary is the Python API.  Each entry point below
+ * replaces one reference function (cited file:line) and is what a ctypes /
+ * cffi binding of that function would call.  The Python
+ * package paper_2208_14228_b200 is exactly such a binding and keeps the
+ * reference's names, argument meaning and exception classes.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Pointers suffixed _dev (and all pointers
+ *    inside bt_mlp_args / bt_reduce_args) are caller-owned DEVICE memory;
+ *    nothing is allocated inside.  `stream` is a cudaStream_t (NULL = legacy).
+ *  - Every call is stream-ordered and asynchronous except bt_step_status,
+ *    the bt_host_* helpers and the IPC/peer helpers.
+ *  - Return value: 0 = ok, else a status that maps 1:1 onto errors.py:
+ *      1 InputError  2 ConfigError  3 StateError  4 ProgressError
+ *      5 NumericError  6 CorruptionError  7 FormatError  8 VersionError
+ *      9 CUDA/launch failure.  bt_last_error() returns this thread's message.
+ *  - Device-detected errors (non-finite gradient, diverged replica) are
+ *    written to a 4-word device status block `flags` {status, detail, step,
+ *    spare}; the status word is sticky (later launches on the same block are
+ *    no-ops) and is decoded by bt_step_status.
+ */
+#ifndef BITTRAIN_B200_H
+#define BITTRAIN_B200_H
+
+#include <stdint.h>
+
+#include "../paper_2208_14228_b200/csrc/bt_mlp.cuh"
+#include "../paper_2208_14228_b200/csrc/bt_reduce.cuh"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BT_ABI_VERSION 1
+
+int bt_abi_version(void);
+const char *bt_last_error(void);
+int bt_device_count(void);
+
+/* ---------------- L0 numeric foundation: host-side sequential pieces ----
+ * These are inherently serial (a Fisher-Yates chain, a byte-serial hash) and
+ * run on the host in native code. */
+uint64_t bt_host_mix64(uint64_t x);                                  /* prng.py:27-35 */
+uint64_t bt_host_derive_stream(const uint64_t *words, int32_t n);    /* prng.py:59-69 */
+uint64_t bt_host_fnv1a64(const void *data, int64_t nbytes);          /* prng.py:72-78 */
+int bt_host_shuffled_range(int64_t n, uint64_t state, int32_t *out); /* prng.py:81-93 */
+/* epoch_indices: out is [workers][steps_per_epoch*micro]             sampling.py:63-82 */
+int bt_host_epoch_indices(uint64_t seed, uint64_t epoch, int64_t n, int32_t workers, int32_t micro,
+                          int32_t shuffle, int32_t *out);
+/* layout_arrival_perm: kind_fnv[e] = fnv1a64(utf-8 device kind)       buckets.py:70-82 */
+int bt_host_layout_arrival_perm(int64_t nparams, int32_t nexec, const uint64_t *kind_fnv,
+                                const int64_t *threads, int32_t *perm);
+/* per-parameter ring-chunk rotation start pos*nrep//len(bucket)       buckets.py:119-122 */
+int bt_host_rotation_table(int32_t nbuckets, const int32_t *sizes, const int32_t *idx, int32_t nrep,
+                           int64_t nparams, int32_t *rot);
+
+/* ---------------- L0 on device ------------------------------------------ */
+/* n draws of a splitmix64 stream starting at draw `first` (counter form)   prng.py:38-56 */
+int bt_splitmix64_draws(uint64_t state, uint64_t first, int64_t n, uint64_t *raw_dev, double *uniform_dev,
+                        void *stream);
+/* reduce_sum(values, Sequential|Tree(fanin)); fanin 0 = Sequential        reduction.py:51-62 */
+int bt_reduce_sum_f64(const double *values_dev, int64_t n, int32_t fanin, double *out_dev, void *stream);
+
+/* ---------------- L1 model ops --------------------------------------------- */
+/* math.tanh as the reference's libm computes it (glibc tanh + FMA expm1)   model.py:148 */
+int bt_tanh_f64(const double *x_dev, int64_t n, double *out_dev, void *stream);
+/* ToyModel.init_random: (u*2-1)*scale per parameter                      model.py:58-66 */
+int bt_init_random(uint64_t seed, double scale, int64_t n, double *out_dev, void *stream);
+/* forward_backward for E ESTs at once (one CTA group per EST block).     model.py:107-196
+ * rows_dev is the split_by_rank global batch [B*E_total][9] (row r of EST k at
+ * r*E_total+k); est_fanin_dev [E]; rng/stat arrays are read and advanced in
+ * place; losses_out [E]; grads_out [E][161].  rank_override >= 0 replaces the
+ * TrackedStat rank of EST 0 (the single-worker seam). */
+int bt_fwd_bwd_mlp_f64(const double *params_dev, const double *rows_dev, int32_t E, int32_t est_base,
+                       int32_t E_total, int32_t B, const int32_t *est_fanin_dev, double rate,
+                       int64_t rank_override, uint64_t *rng_io_dev, double *stat_mean_io_dev,
+                       uint64_t *stat_count_io_dev, double *losses_out_dev, double *grads_out_dev,
+                       int32_t *flags_dev, void *stream);
+/* The whole mini-batch, K consecutive times, in ONE launch: data -> replica
+ * check -> fwd/bwd of every EST -> fixed-order allreduce (executor 0's
+ * variant, rank-keyed) -> /E -> momentum SGD -> mirror to every replica.
+ *                                                           engine.py:271-329 */
+int bt_mlp_step(const bt_mlp_args *args, void *stream);
+/* Default ESTs-per-CTA for a shape (single CTA when the whole step fits). */
+int bt_mlp_pick_est_per_cta(int32_t E, int32_t B);
+
+/* ---------------- L2 communication: the deterministic reducer ------------ */
+/* allreduce(replicas, bucket_map, variant) [+ sgd_step], one shard.
+ *                                        buckets.py:85-124 + model.py:199-213 */
+int bt_reduce_update(const bt_reduce_args *args, void *stream);
+/* sgd_step, out of place; NumericError reported through flags.            model.py:199-213 */
+int bt_sgd_step_f64(const double *params_dev, const double *vel_dev, const double *grads_dev, int64_t n,
+                    double lr, double mu, double *params_out_dev, double *vel_out_dev, int32_t *flags_dev,
+                    void *stream);
+
+/* ---------------- L3 data ------------------------------------------------- */
+/* make_dataset(seed, n, dim): [n][dim+1], x then y                       sampling.py:24-35 */
+int bt_make_dataset(uint64_t seed, int64_t n, int32_t dim, double *out_dev, void *stream);
+/* DataPipeline._produce for ESTs [est_base, est_base+E) at (epoch, local):
+ * lists_dev is the epoch's [E_total][spe*B] lists; rows_out [E][B][9].  sampling.py:160-172 */
+int bt_jitter_gather(const double *dataset_dev, const int32_t *lists_dev, int32_t E, int32_t est_base,
+                     int32_t E_total, int32_t B, int64_t spe, uint64_t seed, int64_t epoch, int64_t local,
+                     double jitter, double *rows_out_dev, void *stream);
+/* forward_backward's dropout masks for `rows` rows of `units` units      model.py:151-161 */
+int bt_dropout_mask(uint64_t state, int64_t rows, int32_t units, double rate, double *out_dev, void *stream);
+
+/* ---------------- L4 runtime ---------------------------------------------- */
+/* check_replica_agreement: R buffers of nbytes compared bytewise with buffer 0;
+ * sets CorruptionError in flags.                                        engine.py:246-258 */
+int bt_replica_check(const void *const *ptrs_dev, int32_t R, int64_t nbytes, int32_t *flags_dev, void *stream);
+/* EST context/slot moves (elastic rescale), 128-bit vectorised, up to 64 pairs. */
+int bt_est_slot_copy(void *const *dst_dev, const void *const *src_dev, const int64_t *bytes, int32_t count,
+                     void *stream);
+/* Parameter all-gather by peer stores: copy `n` elements of `dtype` from
+ * src_dev to every dst in dst_dev[0..ndst) (bit copies, deterministic).   engine.py:313-315 */
+int bt_allgather_params(int32_t dtype, const void *src_dev, void *const *dst_dev, int32_t ndst, int64_t n,
+                        void *stream);
+/* Reset a status block to {0, INT32_MAX, 0, 0}. */
+int bt_flags_reset(int32_t *flags_dev, void *stream);
+/* Synchronise `stream`, read the status block; returns its status word. */
+int bt_step_status(const int32_t *flags_dev, int32_t *detail_out, int32_t *step_out, void *stream);
+
+/* ---------------- multi-GPU plumbing (one process per GPU) -------------- */
+int bt_ipc_handle_size(void);
+int bt_ipc_get_handle(const void *dev_ptr, void *handle_out);
+int bt_ipc_open_handle(const void *handle, void **dev_ptr_out);
+int bt_ipc_close(void *dev_ptr);
+int bt_enable_peer_access(int32_t peer_device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BITTRAIN_B200_H */

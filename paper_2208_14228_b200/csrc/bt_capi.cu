@@ -1,0 +1,363 @@
+// bt_capi.cu -- extern "C" entry points (include/bittrain_b200.h).
+// Validation + status mapping onto errors.py + launches.  No torch types.
+#include <cuda_runtime.h>
+
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "../../include/bittrain_b200.h"
+#include "bt_common.cuh"
+
+namespace bt {
+int mlp_launch(const bt_mlp_args& a, cudaStream_t s);
+size_t mlp_smem_bytes(int nrows);
+int reduce_launch(const bt_reduce_args& a, cudaStream_t s);
+int reduce_sum_launch(const double* v, int64_t n, int fanin, double* out, cudaStream_t s);
+int sgd_launch(const double* p, const double* v, const double* g, int64_t n, double lr, double mu, double* po,
+               double* vo, int32_t* flags, cudaStream_t s);
+int make_dataset_launch(uint64_t seed, int64_t n, int dim, double* out, cudaStream_t s);
+int init_random_launch(uint64_t seed, double scale, int64_t n, double* out, cudaStream_t s);
+int draws_launch(uint64_t state, uint64_t first, int64_t n, uint64_t* raw, double* uni, cudaStream_t s);
+int jitter_gather_launch(const double* dataset, const int32_t* lists, int E, int est_base, int E_total, int B,
+                         int64_t spe, uint64_t seed, int64_t epoch, int64_t local, double jitter, double* rows_out,
+                         cudaStream_t s);
+int dropout_mask_launch(uint64_t state, int64_t rows, int units, double rate, double* out, cudaStream_t s);
+int replica_check_launch(const void* const* ptrs, int R, int64_t nbytes, int32_t* flags, cudaStream_t s);
+int slot_copy_launch(void* const* dst, const void* const* src, const int64_t* bytes, int count, cudaStream_t s);
+int flags_reset_launch(int32_t* flags, cudaStream_t s);
+int tanh_launch(const double* x, int64_t n, double* out, cudaStream_t s);
+}  // namespace bt
+
+static thread_local char g_err[512];
+
+static int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+static int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+static int cuda_fail(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  return fail(bt::ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+static int done(int st, const char* what) {
+  if (st == bt::OK) {
+    g_err[0] = 0;
+    return 0;
+  }
+  if (st == bt::ERR_CUDA) return cuda_fail(what);
+  return st;
+}
+#define STREAM(s) ((cudaStream_t)(s))
+
+extern "C" {
+
+int bt_abi_version(void) { return BT_ABI_VERSION; }
+const char* bt_last_error(void) { return g_err; }
+int bt_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------- host helpers
+uint64_t bt_host_mix64(uint64_t x) { return bt::mix64(x); }
+
+uint64_t bt_host_derive_stream(const uint64_t* words, int32_t n) {
+  uint64_t s = bt::DERIVE_SEED;
+  for (int i = 0; i < n; ++i) s = bt::mix64(s ^ words[i]);
+  return s;
+}
+
+uint64_t bt_host_fnv1a64(const void* data, int64_t nbytes) {
+  const unsigned char* p = (const unsigned char*)data;
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (int64_t i = 0; i < nbytes; ++i) {
+    h ^= p[i];
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+
+int bt_host_shuffled_range(int64_t n, uint64_t state, int32_t* out) {
+  if (n < 0 || n > 0x7fffffff) return fail(bt::ERR_INPUT, "shuffled_range: bad n %lld", (long long)n);
+  for (int64_t i = 0; i < n; ++i) out[i] = (int32_t)i;
+  for (int64_t t = n - 1; t > 0; --t) {
+    state += bt::GOLDEN_GAMMA;
+    const uint64_t raw = bt::mix64(state);
+    const int64_t k = (int64_t)(raw % (uint64_t)(t + 1));
+    const int32_t tmp = out[t];
+    out[t] = out[k];
+    out[k] = tmp;
+  }
+  return 0;
+}
+
+int bt_host_epoch_indices(uint64_t seed, uint64_t epoch, int64_t n, int32_t workers, int32_t micro, int32_t shuffle,
+                          int32_t* out) {
+  if (workers < 1) return fail(bt::ERR_CONFIG, "total_workers must be >= 1");
+  if (n < workers) return fail(bt::ERR_CONFIG, "dataset smaller than the worker count");
+  if (micro < 1) return fail(bt::ERR_CONFIG, "micro_batch must be >= 1");
+  const int64_t spe = n / ((int64_t)workers * micro);
+  if (spe < 1) return fail(bt::ERR_CONFIG, "dataset smaller than one global batch");
+  std::vector<int32_t> order((size_t)n);
+  if (shuffle) bt_host_shuffled_range(n, seed ^ epoch, order.data());
+  else for (int64_t i = 0; i < n; ++i) order[(size_t)i] = (int32_t)i;
+  const int64_t per = spe * micro;
+  for (int32_t k = 0; k < workers; ++k)
+    for (int64_t t = 0; t < per; ++t) out[(size_t)k * per + t] = order[(size_t)(t * workers + k)];
+  return 0;
+}
+
+int bt_host_layout_arrival_perm(int64_t nparams, int32_t nexec, const uint64_t* kind_fnv, const int64_t* threads,
+                                int32_t* perm) {
+  std::vector<uint64_t> w;
+  w.push_back(bt::TAG_BUCKET_ARRIVAL);
+  w.push_back((uint64_t)nexec);
+  for (int e = 0; e < nexec; ++e) {
+    w.push_back(kind_fnv[e]);
+    w.push_back((uint64_t)threads[e]);
+  }
+  return bt_host_shuffled_range(nparams, bt_host_derive_stream(w.data(), (int32_t)w.size()), perm);
+}
+
+int bt_host_rotation_table(int32_t nbuckets, const int32_t* sizes, const int32_t* idx, int32_t nrep, int64_t nparams,
+                           int32_t* rot) {
+  int64_t base = 0;
+  for (int b = 0; b < nbuckets; ++b) {
+    const int64_t blen = sizes[b];
+    for (int64_t pos = 0; pos < blen; ++pos) {
+      const int64_t p = idx[base + pos];
+      if (p < 0 || p >= nparams) return fail(bt::ERR_INPUT, "bucket index %lld out of range", (long long)p);
+      rot[p] = (int32_t)((pos * nrep) / blen);
+    }
+    base += blen;
+  }
+  if (base != nparams) return fail(bt::ERR_INPUT, "bucket map covers %lld parameters, expected %lld",
+                                   (long long)base, (long long)nparams);
+  return 0;
+}
+
+// ------------------------------------------------------------- device: L0
+int bt_splitmix64_draws(uint64_t state, uint64_t first, int64_t n, uint64_t* raw_dev, double* uniform_dev,
+                        void* stream) {
+  if (n < 0) return fail(bt::ERR_INPUT, "negative draw count");
+  if (n == 0) return 0;
+  return done(bt::draws_launch(state, first, n, raw_dev, uniform_dev, STREAM(stream)), "bt_splitmix64_draws");
+}
+
+int bt_reduce_sum_f64(const double* values_dev, int64_t n, int32_t fanin, double* out_dev, void* stream) {
+  if (fanin < 0) return fail(bt::ERR_CONFIG, "fanin must be positive, got %d", fanin);
+  if (fanin == 1) return fail(bt::ERR_CONFIG, "Tree(1) never terminates in the reference; rejected");
+  if (n < 0) return fail(bt::ERR_INPUT, "negative length");
+  return done(bt::reduce_sum_launch(values_dev, n, fanin, out_dev, STREAM(stream)), "bt_reduce_sum_f64");
+}
+
+// ------------------------------------------------------------- device: L1
+int bt_tanh_f64(const double* x_dev, int64_t n, double* out_dev, void* stream) {
+  if (n < 0) return fail(bt::ERR_INPUT, "negative length");
+  if (n == 0) return 0;
+  return done(bt::tanh_launch(x_dev, n, out_dev, STREAM(stream)), "bt_tanh_f64");
+}
+
+int bt_init_random(uint64_t seed, double scale, int64_t n, double* out_dev, void* stream) {
+  return done(bt::init_random_launch(seed, scale, n, out_dev, STREAM(stream)), "bt_init_random");
+}
+
+int bt_mlp_pick_est_per_cta(int32_t E, int32_t B) {
+  if (E < 1 || B < 1) return 1;
+  // One CTA (no grid barrier) while the whole step's rows fit a modest tile;
+  // otherwise spread ESTs so each CTA holds <= 64 rows.
+  if ((int64_t)E * B <= 64) return E;
+  int epc = 64 / B;
+  if (epc < 1) epc = 1;
+  return epc > E ? E : epc;
+}
+
+static int validate_mlp(const bt_mlp_args* a) {
+  if (!a) return fail(bt::ERR_INPUT, "null args");
+  if (a->E < 1 || a->E_total < 1 || a->est_base < 0 || a->est_base + a->E > a->E_total)
+    return fail(bt::ERR_INPUT, "bad EST range [%d, %d) of %d", a->est_base, a->est_base + a->E, a->E_total);
+  if (a->B < 1 || a->B > 256) return fail(bt::ERR_INPUT, "micro-batch %d outside [1, 256]", a->B);
+  if (a->K < 1) return fail(bt::ERR_INPUT, "K must be >= 1");
+  if (a->X < 1) return fail(bt::ERR_INPUT, "need at least one replica");
+  if (a->est_per_cta < 1 || (int64_t)a->est_per_cta * a->B > 256)
+    return fail(bt::ERR_INPUT, "est_per_cta*B must be in [1, 256]");
+  if (a->fuse_reduce && a->E != a->E_total)
+    return fail(bt::ERR_INPUT, "fused allreduce needs every EST local (E == E_total)");
+  if (!a->fuse_reduce && a->K != 1) return fail(bt::ERR_INPUT, "grads-only mode runs one mini-batch");
+  if (a->comm_fanin < 0 || a->comm_fanin == 1) return fail(bt::ERR_CONFIG, "bad allreduce fanin %d", a->comm_fanin);
+  if (!a->rows && (!a->dataset || !a->lists || a->spe < 1))
+    return fail(bt::ERR_INPUT, "need either explicit rows or dataset+lists+spe");
+  if (!a->replicas || !a->est_fanin || !a->rng || !a->stat_mean || !a->stat_count || !a->grads || !a->losses ||
+      !a->flags)
+    return fail(bt::ERR_INPUT, "null device pointer in bt_mlp_args");
+  if (a->fuse_reduce && (a->E + a->est_per_cta - 1) / a->est_per_cta > 1 && !a->bar)
+    return fail(bt::ERR_INPUT, "multi-CTA fused step needs a barrier word");
+  return 0;
+}
+
+int bt_mlp_step(const bt_mlp_args* args, void* stream) {
+  int st = validate_mlp(args);
+  if (st) return st;
+  return done(bt::mlp_launch(*args, STREAM(stream)), "bt_mlp_step");
+}
+
+int bt_fwd_bwd_mlp_f64(const double* params_dev, const double* rows_dev, int32_t E, int32_t est_base,
+                       int32_t E_total, int32_t B, const int32_t* est_fanin_dev, double rate, int64_t rank_override,
+                       uint64_t* rng_io_dev, double* stat_mean_io_dev, uint64_t* stat_count_io_dev,
+                       double* losses_out_dev, double* grads_out_dev, int32_t* flags_dev, void* stream) {
+  bt_mlp_args a;
+  memset(&a, 0, sizeof a);
+  a.E = E;
+  a.est_base = est_base;
+  a.E_total = E_total;
+  a.B = B;
+  a.X = 1;
+  a.K = 1;
+  a.fuse_reduce = 0;
+  a.est_per_cta = bt_mlp_pick_est_per_cta(E, B);
+  if ((int64_t)a.est_per_cta * B > 256) a.est_per_cta = 256 / (B > 0 ? B : 1);
+  a.rank_override = rank_override;
+  a.rate = rate;
+  a.replicas = (double*)params_dev;
+  a.est_fanin = est_fanin_dev;
+  a.rng = rng_io_dev;
+  a.stat_mean = stat_mean_io_dev;
+  a.stat_count = stat_count_io_dev;
+  a.grads = grads_out_dev;
+  a.losses = losses_out_dev;
+  a.rows = rows_dev;
+  a.flags = flags_dev;
+  return bt_mlp_step(&a, stream);
+}
+
+// ------------------------------------------------------------- device: L2
+int bt_reduce_update(const bt_reduce_args* a, void* stream) {
+  if (!a) return fail(bt::ERR_INPUT, "null args");
+  if (a->dtype != BT_DTYPE_F64 && a->dtype != BT_DTYPE_F32) return fail(bt::ERR_INPUT, "bad dtype %d", a->dtype);
+  if (a->E < 1) return fail(bt::ERR_INPUT, "need at least one gradient replica");
+  if (a->grads_ld == 0 && a->E > BT_MAX_TABLE)
+    return fail(bt::ERR_INPUT, "pointer-table mode holds at most %d contributions", BT_MAX_TABLE);
+  if (a->fanin < 0 || a->fanin == 1) return fail(bt::ERR_CONFIG, "bad fanin %d", a->fanin);
+  if (a->n < 0) return fail(bt::ERR_INPUT, "negative length");
+  if (a->nout < 0 || a->nout > BT_MAX_REPLICA_OUT) return fail(bt::ERR_INPUT, "nout outside [0, 8]");
+  if (!a->param_out || (a->mode == BT_REDUCE_UPDATE && (!a->param || !a->vel || !a->vel_out || !a->flags)))
+    return fail(bt::ERR_INPUT, "null buffer");
+  return done(bt::reduce_launch(*a, STREAM(stream)), "bt_reduce_update");
+}
+
+int bt_sgd_step_f64(const double* params_dev, const double* vel_dev, const double* grads_dev, int64_t n, double lr,
+                    double mu, double* params_out_dev, double* vel_out_dev, int32_t* flags_dev, void* stream) {
+  if (n < 0) return fail(bt::ERR_INPUT, "negative length");
+  if (n == 0) return 0;
+  return done(bt::sgd_launch(params_dev, vel_dev, grads_dev, n, lr, mu, params_out_dev, vel_out_dev, flags_dev,
+                             STREAM(stream)),
+              "bt_sgd_step_f64");
+}
+
+// ------------------------------------------------------------- device: L3
+int bt_make_dataset(uint64_t seed, int64_t n, int32_t dim, double* out_dev, void* stream) {
+  if (n < 0 || dim < 0) return fail(bt::ERR_INPUT, "bad dataset shape");
+  if (n == 0) return 0;
+  return done(bt::make_dataset_launch(seed, n, dim, out_dev, STREAM(stream)), "bt_make_dataset");
+}
+
+int bt_jitter_gather(const double* dataset_dev, const int32_t* lists_dev, int32_t E, int32_t est_base,
+                     int32_t E_total, int32_t B, int64_t spe, uint64_t seed, int64_t epoch, int64_t local,
+                     double jitter, double* rows_out_dev, void* stream) {
+  if (E < 1 || B < 1 || est_base < 0 || est_base + E > E_total || local < 0 || local >= spe)
+    return fail(bt::ERR_INPUT, "bad jitter_gather shape");
+  return done(bt::jitter_gather_launch(dataset_dev, lists_dev, E, est_base, E_total, B, spe, seed, epoch, local,
+                                       jitter, rows_out_dev, STREAM(stream)),
+              "bt_jitter_gather");
+}
+
+int bt_dropout_mask(uint64_t state, int64_t rows, int32_t units, double rate, double* out_dev, void* stream) {
+  if (rows < 0 || units < 0) return fail(bt::ERR_INPUT, "bad mask shape");
+  if (rows * units == 0) return 0;
+  return done(bt::dropout_mask_launch(state, rows, units, rate, out_dev, STREAM(stream)), "bt_dropout_mask");
+}
+
+// ------------------------------------------------------------- device: L4
+int bt_replica_check(const void* const* ptrs, int32_t R, int64_t nbytes, int32_t* flags_dev, void* stream) {
+  if (R < 1 || R > 64) return fail(bt::ERR_INPUT, "replica count %d outside [1, 64]", R);
+  if (nbytes % 8) return fail(bt::ERR_INPUT, "replica size must be a multiple of 8 bytes");
+  if (R == 1 || nbytes == 0) return 0;
+  return done(bt::replica_check_launch(ptrs, R, nbytes, flags_dev, STREAM(stream)), "bt_replica_check");
+}
+
+int bt_est_slot_copy(void* const* dst, const void* const* src, const int64_t* bytes, int32_t count, void* stream) {
+  if (count < 0 || count > 64) return fail(bt::ERR_INPUT, "slot copy count %d outside [0, 64]", count);
+  if (count == 0) return 0;
+  return done(bt::slot_copy_launch(dst, src, bytes, count, STREAM(stream)), "bt_est_slot_copy");
+}
+
+int bt_allgather_params(int32_t dtype, const void* src_dev, void* const* dst_dev, int32_t ndst, int64_t n,
+                        void* stream) {
+  if (ndst < 0 || ndst > 64) return fail(bt::ERR_INPUT, "ndst outside [0, 64]");
+  const int64_t es = dtype == BT_DTYPE_F64 ? 8 : 4;
+  const void* srcs[64];
+  int64_t bytes[64];
+  for (int i = 0; i < ndst; ++i) {
+    srcs[i] = src_dev;
+    bytes[i] = n * es;
+  }
+  return bt_est_slot_copy(dst_dev, srcs, bytes, ndst, stream);
+}
+
+int bt_flags_reset(int32_t* flags_dev, void* stream) {
+  return done(bt::flags_reset_launch(flags_dev, STREAM(stream)), "bt_flags_reset");
+}
+
+int bt_step_status(const int32_t* flags_dev, int32_t* detail_out, int32_t* step_out, void* stream) {
+  int32_t h[4];
+  if (cudaMemcpyAsync(h, flags_dev, sizeof h, cudaMemcpyDeviceToHost, STREAM(stream)) != cudaSuccess)
+    return cuda_fail("bt_step_status");
+  if (cudaStreamSynchronize(STREAM(stream)) != cudaSuccess) return cuda_fail("bt_step_status sync");
+  if (detail_out) *detail_out = h[bt::FLAG_DETAIL];
+  if (step_out) *step_out = h[bt::FLAG_STEP];
+  if (h[0] != 0) {
+    snprintf(g_err, sizeof g_err, "device status %d (detail %d, step %d)", h[0], h[1], h[2]);
+  }
+  return h[0];
+}
+
+// ------------------------------------------------------------- multi-GPU
+int bt_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+int bt_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, (void*)dev_ptr) != cudaSuccess) return cuda_fail("cudaIpcGetMemHandle");
+  memcpy(handle_out, &h, sizeof h);
+  return 0;
+}
+int bt_ipc_open_handle(const void* handle, void** dev_ptr_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  if (cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return cuda_fail("cudaIpcOpenMemHandle");
+  return 0;
+}
+int bt_ipc_close(void* dev_ptr) {
+  if (cudaIpcCloseMemHandle(dev_ptr) != cudaSuccess) return cuda_fail("cudaIpcCloseMemHandle");
+  return 0;
+}
+int bt_enable_peer_access(int32_t peer_device) {
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (e != cudaSuccess) return cuda_fail("cudaDeviceEnablePeerAccess");
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,184 @@
+// bt_data.cu -- device data path and EST-slot utilities.
+//
+//  * make_dataset / init_random / raw draws: the reference's sequential
+//    splitmix64 streams (sampling.py:24-35, model.py:58-66, prng.py:38-56)
+//    in counter form, one element per thread.
+//  * jitter_gather: DataPipeline._produce (sampling.py:160-172) -- gather the
+//    EST's epoch-list rows and add (u-0.5)*jitter with one counter-form draw
+//    of worker_rng(seed, epoch, local, est) per row.
+//  * dropout_mask: the (row, unit) masks of forward_backward (model.py:151-161).
+//  * replica_check: bytewise agreement of executor replicas (engine.py:246-258).
+//  * slot_copy: 128-bit vectorised EST-context / slot moves used at rescale.
+#include "bt_common.cuh"
+#include "bt_libm.cuh"
+
+namespace bt {
+
+__global__ void make_dataset_kernel(uint64_t seed, int64_t n, int dim, double* out) {
+  const uint64_t s0 = derive2(TAG_DATASET, seed);
+  const int64_t total = n * (int64_t)(dim + 1);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = dsub(dmul(unit_float(draw_raw(s0, (uint64_t)i)), 2.0), 1.0);
+}
+
+__global__ void init_random_kernel(uint64_t seed, double scale, int64_t n, double* out) {
+  const uint64_t s0 = derive2(TAG_MODEL_INIT, seed);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = dmul(dsub(dmul(unit_float(draw_raw(s0, (uint64_t)i)), 2.0), 1.0), scale);
+}
+
+__global__ void draws_kernel(uint64_t state, uint64_t first, int64_t n, uint64_t* raw, double* uni) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = draw_raw(state, first + (uint64_t)i);
+    if (raw) raw[i] = r;
+    if (uni) uni[i] = unit_float(r);
+  }
+}
+
+// rows_out[e][r][9] for ESTs [est_base, est_base+E) of an E_total-EST job.
+__global__ void jitter_gather_kernel(const double* dataset, const int32_t* lists, int E, int est_base, int E_total,
+                                     int B, int64_t spe, uint64_t seed, int64_t epoch, int64_t local, double jitter,
+                                     double* rows_out) {
+  const int total = E * B;
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < total; it += gridDim.x * blockDim.x) {
+    const int el = it / B, r = it - el * B;
+    const int eg = est_base + el;
+    const int32_t* lst = lists + (size_t)eg * (size_t)(spe * B);
+    const double* src = dataset + (size_t)lst[local * B + r] * 9;
+    double* dst = rows_out + (size_t)it * 9;
+    if (jitter != 0.0) {
+      const uint64_t w = derive5(TAG_DATA_WORKER, seed, (uint64_t)epoch, (uint64_t)local, (uint64_t)eg);
+      const double ju = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), jitter);
+      for (int i = 0; i < 8; ++i) dst[i] = dadd(src[i], ju);
+    } else {
+      for (int i = 0; i < 8; ++i) dst[i] = src[i];
+    }
+    dst[8] = src[8];
+  }
+}
+
+__global__ void dropout_mask_kernel(uint64_t state, int64_t rows, int units, double rate, double* out) {
+  const double keep = rate >= 1.0 ? 0.0 : ddiv(1.0, dsub(1.0, rate));
+  const int64_t total = rows * units;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    if (rate > 0.0) out[i] = unit_float(draw_raw(state, (uint64_t)i)) < rate ? 0.0 : keep;
+    else out[i] = 1.0;
+  }
+}
+
+struct PtrTable {
+  const void* p[64];
+};
+
+__global__ void replica_check_kernel(const __grid_constant__ PtrTable t, int R, int64_t nwords, int32_t* flags) {
+  const uint64_t* r0 = (const uint64_t*)t.p[0];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t w = r0[i];
+    for (int r = 1; r < R; ++r)
+      if (((const uint64_t*)t.p[r])[i] != w) {
+        atomicCAS(flags + FLAG_STATUS, 0, (int)ERR_CORRUPTION);
+        atomicMin(flags + FLAG_DETAIL, r);
+      }
+  }
+}
+
+struct CopyTable {
+  void* dst[64];
+  const void* src[64];
+  int64_t bytes[64];
+};
+
+// One CTA group per (dst, src) pair; 16-byte vectors when both ends allow it.
+__global__ void slot_copy_kernel(const __grid_constant__ CopyTable t, int count) {
+  const int item = blockIdx.y;
+  if (item >= count) return;
+  const int64_t nb = t.bytes[item];
+  const uintptr_t d = (uintptr_t)t.dst[item], s = (uintptr_t)t.src[item];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  if (((d | s) & 15u) == 0) {
+    const int64_t nv = nb / 16;
+    const int4* sv = (const int4*)s;
+    int4* dv = (int4*)d;
+    for (int64_t i = tid; i < nv; i += stride) dv[i] = __ldcs(sv + i);
+    for (int64_t i = nv * 16 + tid; i < nb; i += stride) ((char*)d)[i] = ((const char*)s)[i];
+  } else {
+    for (int64_t i = tid; i < nb; i += stride) ((char*)d)[i] = ((const char*)s)[i];
+  }
+}
+
+__global__ void tanh_kernel(const double* x, int64_t n, double* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = glibc_tanh(x[i]);
+}
+
+__global__ void flags_reset_kernel(int32_t* flags) {
+  if (threadIdx.x == 0) {
+    flags[FLAG_STATUS] = 0;
+    flags[FLAG_DETAIL] = 0x7fffffff;
+    flags[FLAG_STEP] = 0;
+    flags[FLAG_SPARE] = 0;
+  }
+}
+
+int tanh_launch(const double* x, int64_t n, double* out, cudaStream_t s);
+
+int flags_reset_launch(int32_t* flags, cudaStream_t s) {
+  flags_reset_kernel<<<1, 32, 0, s>>>(flags);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+
+static unsigned grid_for(int64_t n, int threads = 256, int64_t cap = 148 * 8) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > cap) b = cap;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+int make_dataset_launch(uint64_t seed, int64_t n, int dim, double* out, cudaStream_t s) {
+  make_dataset_kernel<<<grid_for(n * (dim + 1)), 256, 0, s>>>(seed, n, dim, out);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+int init_random_launch(uint64_t seed, double scale, int64_t n, double* out, cudaStream_t s) {
+  init_random_kernel<<<grid_for(n), 256, 0, s>>>(seed, scale, n, out);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+int draws_launch(uint64_t state, uint64_t first, int64_t n, uint64_t* raw, double* uni, cudaStream_t s) {
+  draws_kernel<<<grid_for(n), 256, 0, s>>>(state, first, n, raw, uni);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+int jitter_gather_launch(const double* dataset, const int32_t* lists, int E, int est_base, int E_total, int B,
+                         int64_t spe, uint64_t seed, int64_t epoch, int64_t local, double jitter, double* rows_out,
+                         cudaStream_t s) {
+  jitter_gather_kernel<<<grid_for((int64_t)E * B), 256, 0, s>>>(dataset, lists, E, est_base, E_total, B, spe, seed,
+                                                                epoch, local, jitter, rows_out);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+int dropout_mask_launch(uint64_t state, int64_t rows, int units, double rate, double* out, cudaStream_t s) {
+  dropout_mask_kernel<<<grid_for(rows * units), 256, 0, s>>>(state, rows, units, rate, out);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+int replica_check_launch(const void* const* ptrs, int R, int64_t nbytes, int32_t* flags, cudaStream_t s) {
+  PtrTable t{};
+  for (int r = 0; r < R; ++r) t.p[r] = ptrs[r];
+  replica_check_kernel<<<grid_for(nbytes / 8), 256, 0, s>>>(t, R, nbytes / 8, flags);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+int slot_copy_launch(void* const* dst, const void* const* src, const int64_t* bytes, int count, cudaStream_t s) {
+  CopyTable t{};
+  int64_t maxb = 0;
+  for (int i = 0; i < count; ++i) {
+    t.dst[i] = dst[i];
+    t.src[i] = src[i];
+    t.bytes[i] = bytes[i];
+    if (bytes[i] > maxb) maxb = bytes[i];
+  }
+  dim3 grid(grid_for(maxb / 16 + 1, 256, 148 * 4), (unsigned)count);
+  slot_copy_kernel<<<grid, 256, 0, s>>>(t, count);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+
+int tanh_launch(const double* x, int64_t n, double* out, cudaStream_t s) {
+  tanh_kernel<<<grid_for(n), 256, 0, s>>>(x, n, out);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+
+}  // namespace bt

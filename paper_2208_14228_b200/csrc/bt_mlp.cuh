@@ -1,0 +1,60 @@
+// bt_mlp.cuh -- argument block of the fused MLP step kernel (C-ABI visible).
+#pragma once
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+// Model shape pinned by the reference (model.py:27-34).
+#define BT_INPUT_DIM 8
+#define BT_HIDDEN 16
+#define BT_W1 0
+#define BT_B1 (BT_INPUT_DIM * BT_HIDDEN)
+#define BT_W2 (BT_B1 + BT_HIDDEN)
+#define BT_B2 (BT_W2 + BT_HIDDEN)
+#define BT_P (BT_B2 + 1) /* 161 */
+#define BT_ROW (BT_INPUT_DIM + 1) /* dataset row: 8 x-values then y (sampling.py:24-35) */
+
+/* One launch runs K consecutive mini-batches of the data-parallel step
+ * (engine.py:271-329) for the ESTs [est_base, est_base+E) of an E_total-EST job.
+ * All pointers are caller-owned DEVICE memory. */
+typedef struct bt_mlp_args {
+  int32_t E;           /* ESTs handled by this launch */
+  int32_t est_base;    /* global virtual rank of local EST 0 */
+  int32_t E_total;     /* ESTs in the job (allreduce divisor, rotation, row deal) */
+  int32_t B;           /* micro-batch rows per EST */
+  int32_t X;           /* executor replicas held here (replica agreement check) */
+  int32_t K;           /* mini-batches in this launch */
+  int32_t fuse_reduce; /* 1: allreduce + sgd in-kernel (E must equal E_total); 0: grads only */
+  int32_t est_per_cta; /* ESTs per CTA (grid = ceil(E / est_per_cta)) */
+  int32_t comm_fanin;  /* executor 0's variant for the allreduce (engine.py:309); 0 = Sequential */
+  int32_t pad0;
+  int64_t rank_override; /* >= 0: TrackedStat rank of EST 0 (pure forward_backward seam) */
+  double rate, lr, mu, jitter;
+  /* state */
+  double *replicas;        /* [X][2][P]: params then velocity, one block per executor */
+  const int32_t *est_fanin;/* [E] batch-reduction fanin of each local EST's executor (0 = Sequential) */
+  uint64_t *rng;           /* [E] dropout stream state (WorkerContext.dropout_rng) */
+  double *stat_mean;       /* [E] TrackedStat.running_mean */
+  uint64_t *stat_count;    /* [E] TrackedStat.update_count */
+  double *grads;           /* fuse_reduce: [2][E][P] step-parity double buffer; else [E][P] */
+  double *losses;          /* [K][E] */
+  const int32_t *rot;      /* [P] allreduce rotation start per parameter (Tree only) or NULL */
+  /* data: explicit global batch (split_by_rank) OR the device sampler */
+  const double *rows;      /* [K][B*E_total][9] or NULL */
+  const double *dataset;   /* [n][9] resident dataset (sampler mode) */
+  const int32_t *lists;    /* [n_epochs][E_total][spe*B] epoch index lists (sampler mode) */
+  uint64_t seed;           /* job seed (worker_rng, sampling.py:99-101) */
+  int64_t step0;           /* global step of the first mini-batch in this launch */
+  int64_t spe;             /* steps per epoch */
+  int64_t epoch_base;      /* epoch of lists[0] */
+  /* control */
+  int32_t *flags;          /* [4] sticky device status (bt::Flag) */
+  uint32_t *bar;           /* grid barrier counter, zeroed by the launcher */
+  double *param_trace;     /* [K][P] parameters after each mini-batch (RunLog fingerprints) or NULL */
+} bt_mlp_args;
+
+#ifdef __cplusplus
+}
+#endif

@@ -1,0 +1,281 @@
+// bt_reduce.cu -- the deterministic fixed-order gradient reducer with the fused
+// 1/E scale and momentum-SGD update (the north star's core product).
+//
+// Replaces the reference's functional allreduce (buckets.py:85-124) +
+// sgd_step (model.py:199-213).  The fold order of every element is a pure
+// function of (EST rank, fanin, rotation): CTA/thread/GPU counts never enter,
+// so the same ESTs give the same bits on 1, 2, 4 or 8 GPUs.
+//
+// Two kernels:
+//  * reduce_fast_kernel<T, E, F>: Sequential (F=0) or unrotated Tree(2)
+//    (F=2, E a power of two) -- the HBM-bound production path.  16-byte
+//    vector loads (float4 / double2) of E contribution streams, folded in
+//    registers with a compile-time tree; streaming cache hints; grid sized to
+//    the SM count.  HBM bytes per element: E*sizeof(T) (grads) + 4*sizeof(T)
+//    (param, vel read + write).
+//  * reduce_generic_kernel<T>: any E, any fanin, optional per-element
+//    rotation (the reference's ring-chunk order under Tree, buckets.py:119-122),
+//    pointer-table or strided contributions.  Used for parity variants.
+#include "bt_common.cuh"
+#include "bt_reduce.cuh"
+
+namespace bt {
+
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using type = float4; static constexpr int W = 4; };
+template <> struct Vec16<double> { using type = double2; static constexpr int W = 2; };
+
+__device__ __forceinline__ float lane(const float4& v, int w) { return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w; }
+__device__ __forceinline__ double lane(const double2& v, int w) { return w == 0 ? v.x : v.y; }
+__device__ __forceinline__ void set_lane(float4& v, int w, float x) {
+  if (w == 0) v.x = x; else if (w == 1) v.y = x; else if (w == 2) v.z = x; else v.w = x;
+}
+__device__ __forceinline__ void set_lane(double2& v, int w, double x) { if (w == 0) v.x = x; else v.y = x; }
+
+__device__ __forceinline__ void flag_numeric(int32_t* flags, int64_t idx) {
+  atomicCAS(flags + FLAG_STATUS, 0, (int)ERR_NUMERIC);
+  atomicMin(flags + FLAG_DETAIL, (int)(idx < 0x7fffffff ? idx : 0x7fffffff));
+}
+
+template <typename T>
+__device__ __forceinline__ T elem(const bt_reduce_args& a, int k, int64_t p) {
+  const T* base = a.grads_ld > 0 ? (const T*)a.grads[0] + (size_t)k * a.grads_ld : (const T*)a.grads[k];
+  return base[p];
+}
+
+// Apply /E, finite check and the update for one element.
+template <typename T>
+__device__ __forceinline__ void finish_elem(const bt_reduce_args& a, int64_t p, T sum) {
+  const T g = Arith<T>::div(sum, (T)a.E);
+  if (a.mode == BT_REDUCE_MEAN_ONLY) {
+    ((T*)a.param_out)[p] = g;
+    return;
+  }
+  if (!finite_v(g)) flag_numeric(a.flags, p);
+  const T v = Arith<T>::add(Arith<T>::mul((T)a.mu, ((const T*)a.vel)[p]), g);
+  const T np = Arith<T>::sub(((const T*)a.param)[p], Arith<T>::mul((T)a.lr, v));
+  ((T*)a.vel_out)[p] = v;
+  ((T*)a.param_out)[p] = np;
+  for (int r = 0; r < a.nout; ++r) {
+    ((T*)a.extra_param_out[r])[p] = np;
+    ((T*)a.extra_vel_out[r])[p] = v;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_generic_kernel(const __grid_constant__ bt_reduce_args a) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < a.n; p += stride) {
+    const int start = a.rot ? a.rot[p] : 0;
+    StreamFold<T, 24> f;
+    f.init(a.fanin);
+    for (int k = 0; k < a.E; ++k) {
+      int src = start + k;
+      if (src >= a.E) src -= a.E;
+      f.push(elem<T>(a, src, p));
+    }
+    finish_elem<T>(a, p, f.finish());
+  }
+}
+
+template <typename V>
+__device__ __forceinline__ V ld_stream(const V* p) { return __ldcs(p); }
+template <typename V>
+__device__ __forceinline__ void st_stream(V* p, const V& v) { __stcs(p, v); }
+
+// E in {1,2,4,...,64}; F == 0 (Sequential) or F == 2 (unrotated Tree(2)).
+template <typename T, int E, int F>
+__global__ void __launch_bounds__(256) reduce_fast_kernel(const __grid_constant__ bt_reduce_args a) {
+  using V = typename Vec16<T>::type;
+  constexpr int W = Vec16<T>::W;
+  constexpr int C = E < 16 ? E : 16;  // contributions loaded per chunk
+  constexpr int NC = E / C;           // chunks (power-of-two E => exact)
+  const int64_t nv = a.n / W;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const T invE_dummy = (T)0;  // (division below is a true /E, never *1/E)
+  (void)invE_dummy;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    T sum[W];
+    T part[NC > 1 ? NC : 1][W];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      V buf[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) buf[k] = ld_stream((const V*)a.grads[c * C + k] + i);
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        if (F == 0) {  // strict left fold over ranks, continued across chunks
+          T acc = c == 0 ? lane(buf[0], w) : Arith<T>::add(sum[w], lane(buf[0], w));
+#pragma unroll
+          for (int k = 1; k < C; ++k) acc = Arith<T>::add(acc, lane(buf[k], w));
+          sum[w] = acc;
+        } else {  // complete binary tree: chunk subtrees, then the top levels
+          T v[C];
+#pragma unroll
+          for (int k = 0; k < C; ++k) v[k] = lane(buf[k], w);
+          part[c][w] = TreeLevel<C, 2>::run(v);
+        }
+      }
+    }
+    if (F != 0) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        T v[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[c] = part[c][w];
+        sum[w] = TreeLevel<NC, 2>::run(v);
+      }
+    }
+    V g;
+    bool fin = true;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const T gw = Arith<T>::div(sum[w], (T)E);
+      set_lane(g, w, gw);
+      fin = fin && finite_v(gw);
+    }
+    if (a.mode == BT_REDUCE_MEAN_ONLY) {
+      st_stream((V*)a.param_out + i, g);
+      continue;
+    }
+    if (!fin) flag_numeric(a.flags, i * W);
+    const V pv = ld_stream((const V*)a.param + i);
+    const V vv = ld_stream((const V*)a.vel + i);
+    V nv_, np_;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const T v = Arith<T>::add(Arith<T>::mul((T)a.mu, lane(vv, w)), lane(g, w));
+      set_lane(nv_, w, v);
+      set_lane(np_, w, Arith<T>::sub(lane(pv, w), Arith<T>::mul((T)a.lr, v)));
+    }
+    st_stream((V*)a.vel_out + i, nv_);
+    st_stream((V*)a.param_out + i, np_);
+    for (int r = 0; r < a.nout; ++r) {
+      st_stream((V*)a.extra_param_out[r] + i, np_);
+      st_stream((V*)a.extra_vel_out[r] + i, nv_);
+    }
+  }
+  // scalar tail (n % W elements)
+  if (blockIdx.x == 0) {
+    for (int64_t p = nv * W + threadIdx.x; p < a.n; p += blockDim.x) {
+      T acc = ((const T*)a.grads[0])[p];
+      if (F == 0) {
+        for (int k = 1; k < E; ++k) acc = Arith<T>::add(acc, ((const T*)a.grads[k])[p]);
+      } else {
+        T v[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) v[k] = ((const T*)a.grads[k])[p];
+        acc = TreeLevel<E, 2>::run(v);
+      }
+      finish_elem<T>(a, p, acc);
+    }
+  }
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <typename T, int E, int F>
+static cudaError_t launch_fast(const bt_reduce_args& a, cudaStream_t s) {
+  constexpr int W = Vec16<T>::W;
+  const int64_t nv = (a.n + W - 1) / W;
+  int64_t blocks = (nv + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;  // 8 x 256 threads resident per SM
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  reduce_fast_kernel<T, E, F><<<(unsigned)blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T, int F>
+static cudaError_t dispatch_fast_E(const bt_reduce_args& a, cudaStream_t s, bool* taken) {
+  *taken = true;
+  switch (a.E) {
+    case 1: return launch_fast<T, 1, F>(a, s);
+    case 2: return launch_fast<T, 2, F>(a, s);
+    case 4: return launch_fast<T, 4, F>(a, s);
+    case 8: return launch_fast<T, 8, F>(a, s);
+    case 16: return launch_fast<T, 16, F>(a, s);
+    case 32: return launch_fast<T, 32, F>(a, s);
+    case 64: return launch_fast<T, 64, F>(a, s);
+    default: *taken = false; return cudaSuccess;
+  }
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+template <typename T>
+static cudaError_t reduce_launch_t(const bt_reduce_args& a, cudaStream_t s) {
+  bool fast_ok = a.rot == nullptr && a.grads_ld == 0 && (a.fanin == 0 || a.fanin == 2);
+  if (fast_ok) {
+    for (int k = 0; k < a.E; ++k) fast_ok = fast_ok && aligned16(a.grads[k]);
+    fast_ok = fast_ok && aligned16(a.param_out);
+    if (a.mode == BT_REDUCE_UPDATE) {
+      fast_ok = fast_ok && aligned16(a.param) && aligned16(a.vel) && aligned16(a.vel_out);
+      for (int r = 0; r < a.nout; ++r) fast_ok = fast_ok && aligned16(a.extra_param_out[r]) && aligned16(a.extra_vel_out[r]);
+    }
+  }
+  if (fast_ok) {
+    bool taken = false;
+    cudaError_t e = a.fanin == 0 ? dispatch_fast_E<T, 0>(a, s, &taken) : dispatch_fast_E<T, 2>(a, s, &taken);
+    if (taken) return e;
+  }
+  int64_t blocks = (a.n + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  reduce_generic_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+int reduce_launch(const bt_reduce_args& a, cudaStream_t s) {
+  if (a.n == 0) return OK;
+  const cudaError_t e = a.dtype == BT_DTYPE_F64 ? reduce_launch_t<double>(a, s) : reduce_launch_t<float>(a, s);
+  return e == cudaSuccess ? OK : ERR_CUDA;
+}
+
+// ---------------------------------------------------------- small seams
+// reduce_sum(values, variant) for one list (reduction.py:51-62).
+__global__ void reduce_sum_kernel(const double* v, int64_t n, int fanin, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  StreamFold<double, 64> f;
+  f.init(fanin);
+  for (int64_t i = 0; i < n; ++i) f.push(v[i]);
+  *out = f.finish();
+}
+
+int reduce_sum_launch(const double* v, int64_t n, int fanin, double* out, cudaStream_t s) {
+  reduce_sum_kernel<<<1, 32, 0, s>>>(v, n, fanin, out);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+
+// sgd_step (model.py:199-213), out of place; NUMERIC flag + first bad index.
+__global__ void sgd_kernel(const double* p, const double* v, const double* g, int64_t n, double lr, double mu,
+                           double* po, double* vo, int32_t* flags) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double gi = g[i];
+    if (!finite_d(gi)) flag_numeric(flags, i);
+    const double vi = dadd(dmul(mu, v[i]), gi);
+    vo[i] = vi;
+    po[i] = dsub(p[i], dmul(lr, vi));
+  }
+}
+
+int sgd_launch(const double* p, const double* v, const double* g, int64_t n, double lr, double mu, double* po,
+               double* vo, int32_t* flags, cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  sgd_kernel<<<(unsigned)blocks, 256, 0, s>>>(p, v, g, n, lr, mu, po, vo, flags);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+
+}  // namespace bt

@@ -1,0 +1,43 @@
+// bt_reduce.cuh -- argument block of the deterministic gradient reducer (C-ABI visible).
+#pragma once
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BT_MAX_TABLE 64 /* per-EST pointer table entries (peer or local slots) */
+#define BT_MAX_REPLICA_OUT 8
+
+enum { BT_DTYPE_F64 = 0, BT_DTYPE_F32 = 1 };
+enum { BT_REDUCE_UPDATE = 0, BT_REDUCE_MEAN_ONLY = 1 };
+
+/* out[p] = reduce_sum(g[(rot[p]+k) % E][p] for k in 0..E-1, fanin) / E   (buckets.py:115-123)
+ * then, in BT_REDUCE_UPDATE mode, v' = mu*v + out; p' = p - lr*v'      (model.py:206-212).
+ * Contributions are addressed by EST rank k: either a table of E base pointers
+ * (each may be a local slot or a peer GPU's slot mapped by CUDA IPC) or one
+ * strided buffer (grads_ld > 0: base grads[0], EST k at grads[0] + k*grads_ld
+ * elements).  The order of every addition depends only on (E, fanin, rot):
+ * never on the GPU, CTA or thread count. */
+typedef struct bt_reduce_args {
+  int32_t dtype;  /* BT_DTYPE_F64 | BT_DTYPE_F32 */
+  int32_t mode;   /* BT_REDUCE_UPDATE | BT_REDUCE_MEAN_ONLY */
+  int32_t E;      /* contributions per element (EST count) */
+  int32_t fanin;  /* 0 = Sequential, >= 2 = Tree(fanin) */
+  int32_t nout;   /* extra replica outputs (P2P stores = fused parameter all-gather) */
+  int32_t pad0;
+  int64_t n;         /* elements in this shard */
+  int64_t grads_ld;  /* > 0: strided mode */
+  const void *grads[BT_MAX_TABLE];
+  const int32_t *rot; /* [n] rotation start (Tree parity with the bucket map) or NULL */
+  const void *param, *vel;       /* inputs (unused in MEAN_ONLY) */
+  void *param_out, *vel_out;     /* outputs; may alias the inputs */
+  void *extra_param_out[BT_MAX_REPLICA_OUT];
+  void *extra_vel_out[BT_MAX_REPLICA_OUT];
+  double lr, mu;
+  int32_t *flags; /* [4] device status; NUMERIC + first bad index */
+} bt_reduce_args;
+
+#ifdef __cplusplus
+}
+#endif

@@ -1,0 +1,588 @@
+"""Time-sliced elastic training runtime on the B200 (reference engine.py:1-395).
+
+A job has `max_workers` ESTs with fixed virtual ranks.  Executors host
+contiguous rank blocks (`assign_ranks`).  All per-EST state lives in HBM
+slots indexed by rank (dropout RNG, TrackedStat, gradient slot), so a
+"context switch" is an index change and a layout change never moves it.
+The executor replicas are [X][2][161] binary64 blocks.
+
+`run_minibatch` launches ONE fused kernel (bt_mlp.cu) that performs, in the
+reference's order: data gather + jitter -> replica agreement -> every EST's
+forward/backward -> fixed-order allreduce in executor 0's variant -> /E ->
+momentum SGD -> mirror to every replica.  `run_steps` runs K mini-batches in
+one persistent launch.  If `engine.allreduce` is replaced (e.g. a test spy,
+reference test_engine.py:175-199), the step falls back to the unfused device
+path that calls it through this module's global, exactly like the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native
+from . import buckets as _buckets
+from .buckets import (BucketMap, build_buckets_initial, layout_arrival_perm, rebuild_buckets_first_minibatch,
+                      rotation_table)
+from .device import DeviceVector, Flags, i64_to_u64, ptr, require_cuda, stream, u64_to_i64
+from .errors import ConfigError, CorruptionError, NumericError, StateError
+from .model import PARAM_COUNT, Batch, OptState, ToyModel, TrackedStat, rows_tensor, sgd_step
+from .prng import TAG_DROPOUT, derive_stream
+from .reduction import KernelProfile, fanin_code
+from .sampling import DataPipeline
+
+allreduce = _buckets.allreduce  # called through this module global (spy-able, engine.py:310)
+_DEVICE_ALLREDUCE = _buckets.allreduce
+P = PARAM_COUNT
+
+
+@dataclass(frozen=True)
+class DeterminismMode:
+    """d0 fixed-parallelism, d1 elasticity (implies d0), d2 heterogeneity (engine.py:44-80)."""
+
+    d0: bool = True
+    d1: bool = False
+    d2: bool = False
+
+    def __post_init__(self):
+        if self.d1 and not self.d0:
+            raise ConfigError("d1 requires d0")
+
+    @classmethod
+    def from_label(cls, label: str) -> "DeterminismMode":
+        table = {"d0": cls(True), "d1": cls(True, True), "d1d2": cls(True, True, True), "d0d2": cls(True, False, True)}
+        key = label.strip().lower()
+        if key not in table:
+            raise ConfigError(f"unknown determinism mode {label!r}")
+        return table[key]
+
+    @property
+    def label(self) -> str:
+        return {(True, True): "d1d2", (True, False): "d1", (False, True): "d0d2", (False, False): "d0"}[(self.d1, self.d2)]
+
+
+@dataclass(frozen=True)
+class ExecutorSpec:
+    """One executor of a layout: device kind and optional pinned EST count."""
+
+    device_kind: str
+    threads: int | None = None
+
+
+@dataclass(frozen=True)
+class TrainRunConfig:
+    """Everything a run depends on besides the layout (engine.py:117-141)."""
+
+    seed: int
+    max_workers: int
+    micro_batch: int = 4
+    dataset_size: int = 1000
+    lr: float = 0.02
+    momentum: float = 0.9
+    dropout_rate: float = 0.5
+    jitter: float = 0.1
+    bucket_capacity: int = 64
+    worker_slots: int = 2
+    prefetch_depth: int = 2
+    shuffle: bool = True
+    determinism: DeterminismMode = DeterminismMode()
+    device_fanins: dict = field(default_factory=lambda: {"cpu": 2})
+
+    def kernel_profile(self, device_kind: str) -> KernelProfile:
+        if device_kind not in self.device_fanins:
+            raise ConfigError(f"unknown device kind {device_kind!r}")
+        if self.determinism.d2:
+            return KernelProfile.device_agnostic(device_kind)
+        return KernelProfile.native(device_kind, self.device_fanins[device_kind])
+
+
+# ---------------------------------------------------------------- device state
+class DeviceState:
+    """HBM layout of one job."""
+
+    def __init__(self, E: int, X: int):
+        require_cuda()
+        self.E, self.X = E, X
+        self.replicas = torch.zeros((X, 2, P), dtype=torch.float64, device="cuda")  # params | velocity
+        self.est_fanin = torch.zeros(E, dtype=torch.int32, device="cuda")
+        self.rng = torch.zeros(E, dtype=torch.int64, device="cuda")         # u64 bit patterns
+        self.stat_mean = torch.zeros(E, dtype=torch.float64, device="cuda")
+        self.stat_count = torch.zeros(E, dtype=torch.int64, device="cuda")
+        self.grads = torch.zeros((2, E, P), dtype=torch.float64, device="cuda")  # step-parity slots
+        self.flags = Flags()
+        self.bar = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self._snap = None
+        self.rot = None
+        self.rot_key = None
+
+    def invalidate(self) -> None:
+        self._snap = None
+
+    def snapshot(self):
+        if self._snap is None:
+            self._snap = (self.rng.tolist(), self.stat_mean.tolist(), self.stat_count.tolist())
+        return self._snap
+
+    def replica_ptrs(self) -> list[int]:
+        return [self.replicas[x].data_ptr() for x in range(self.X)]
+
+
+class WorkerContext:
+    """All state owned by one EST (engine.py:95-103).
+
+    Detached (host fields) until attached to a DeviceState slot; attached
+    contexts read and write their HBM slot."""
+
+    def __init__(self, virtual_rank: int, dropout_rng: int = 0, stat: TrackedStat = TrackedStat(),
+                 pending_grads=None, minibatch_idx: int = 0):
+        self.virtual_rank = virtual_rank
+        self._rng = dropout_rng
+        self._stat = stat
+        self.pending_grads = pending_grads
+        self.minibatch_idx = minibatch_idx
+        self._dev: DeviceState | None = None
+
+    def attach(self, dev: DeviceState) -> None:
+        k = self.virtual_rank
+        dev.rng[k] = u64_to_i64(self._rng)
+        dev.stat_mean[k] = self._stat.running_mean
+        dev.stat_count[k] = self._stat.update_count
+        dev.invalidate()
+        self._dev = dev
+
+    @property
+    def dropout_rng(self) -> int:
+        if self._dev is None:
+            return self._rng
+        return i64_to_u64(self._dev.snapshot()[0][self.virtual_rank])
+
+    @dropout_rng.setter
+    def dropout_rng(self, v: int) -> None:
+        if self._dev is None:
+            self._rng = v
+        else:
+            self._dev.rng[self.virtual_rank] = u64_to_i64(v)
+            self._dev.invalidate()
+
+    @property
+    def stat(self) -> TrackedStat:
+        if self._dev is None:
+            return self._stat
+        _, means, counts = self._dev.snapshot()
+        return TrackedStat(means[self.virtual_rank], int(counts[self.virtual_rank]))
+
+    @stat.setter
+    def stat(self, s: TrackedStat) -> None:
+        if self._dev is None:
+            self._stat = s
+        else:
+            self._dev.stat_mean[self.virtual_rank] = s.running_mean
+            self._dev.stat_count[self.virtual_rank] = s.update_count
+            self._dev.invalidate()
+
+    def _key(self):
+        pg = None if self.pending_grads is None else list(self.pending_grads)
+        return (self.virtual_rank, self.dropout_rng, self.stat, pg, self.minibatch_idx)
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, WorkerContext) and self._key() == other._key()
+
+    __hash__ = None
+
+    def __repr__(self) -> str:
+        return (f"WorkerContext(virtual_rank={self.virtual_rank}, dropout_rng={self.dropout_rng:#x}, "
+                f"stat={self.stat}, minibatch_idx={self.minibatch_idx})")
+
+
+class ExecutorState:
+    """A device context hosting a replica shared by its ESTs (engine.py:106-114).
+
+    `model`/`opt` are views of this executor's block of DeviceState.replicas."""
+
+    def __init__(self, device_kind: str, kernel_profile: KernelProfile, assigned: list[int], dev: DeviceState,
+                 index: int, lr: float, momentum: float):
+        self.device_kind = device_kind
+        self.kernel_profile = kernel_profile
+        self.assigned = assigned
+        self._dev, self._x = dev, index
+        self._lr, self._mu = lr, momentum
+
+    @property
+    def model(self) -> ToyModel:
+        return ToyModel(self._dev.replicas[self._x, 0])
+
+    @model.setter
+    def model(self, m: ToyModel) -> None:
+        self._dev.replicas[self._x, 0].copy_(m.tensor)
+
+    @property
+    def opt(self) -> OptState:
+        return OptState(self._lr, self._mu, self._dev.replicas[self._x, 1])
+
+    @opt.setter
+    def opt(self, o: OptState) -> None:
+        self._lr, self._mu = o.lr, o.momentum
+        self._dev.replicas[self._x, 1].copy_(o.tensor)
+
+
+@dataclass
+class TrainingState:
+    """The unit of checkpointing (engine.py:144-162) plus its device slots."""
+
+    cfg: TrainRunConfig
+    contexts: list
+    executors: list
+    bucket_map: BucketMap
+    pipeline: DataPipeline
+    global_step: int = 0
+    epoch: int = 0
+    rebuild_pending: bool = False
+    dev: DeviceState | None = None
+
+    @property
+    def max_workers(self) -> int:
+        return self.cfg.max_workers
+
+    def layout_key(self) -> list[tuple[str, int]]:
+        return [(ex.device_kind, len(ex.assigned)) for ex in self.executors]
+
+
+def floats_to_bytes(values) -> bytes:
+    if isinstance(values, DeviceVector):
+        return values.to_bytes()
+    return struct.pack(f"<{len(values)}d", *values)
+
+
+def assign_ranks(specs: list[ExecutorSpec], max_workers: int) -> list[tuple[str, list[int]]]:
+    """Contiguous rank blocks (engine.py:169-199): pinned counts must sum to
+    max_workers; otherwise balanced, larger shares first."""
+    if not specs:
+        raise ConfigError("layout needs at least one executor")
+    pinned = [s.threads for s in specs]
+    if any(t is not None for t in pinned):
+        if any(t is None for t in pinned):
+            raise ConfigError("either all executors or none may pin thread counts")
+        if any(t < 1 for t in pinned):
+            raise ConfigError("executor thread counts must be >= 1")
+        if sum(pinned) != max_workers:
+            raise ConfigError(f"thread counts sum to {sum(pinned)}, expected {max_workers}")
+        counts = list(pinned)
+    else:
+        if len(specs) > max_workers:
+            raise ConfigError(f"{len(specs)} executors for only {max_workers} workers")
+        base, extra = divmod(max_workers, len(specs))
+        counts = [base + (i < extra) for i in range(len(specs))]
+    out, start = [], 0
+    for spec, c in zip(specs, counts):
+        out.append((spec.device_kind, list(range(start, start + c))))
+        start += c
+    return out
+
+
+def _build_executors(cfg: TrainRunConfig, layout, dev: DeviceState, lr: float, mu: float) -> list[ExecutorState]:
+    execs = []
+    fan = np.zeros(cfg.max_workers, dtype=np.int32)
+    for x, (kind, ranks) in enumerate(assign_ranks(list(layout), cfg.max_workers)):
+        prof = cfg.kernel_profile(kind)
+        f = fanin_code(prof.reduce_variant)
+        fan[ranks] = f
+        execs.append(ExecutorState(kind, prof, ranks, dev, x, lr, mu))
+    dev.est_fanin.copy_(torch.from_numpy(fan))
+    return execs
+
+
+def _new_pipeline(cfg: TrainRunConfig, dataset_dev=None) -> DataPipeline:
+    pipe = DataPipeline(cfg.seed, cfg.dataset_size, cfg.max_workers, cfg.micro_batch, cfg.jitter, cfg.worker_slots,
+                        cfg.prefetch_depth, cfg.shuffle)
+    if dataset_dev is not None:
+        pipe._dataset_dev = dataset_dev
+    return pipe
+
+
+def init_training(cfg: TrainRunConfig, layout: list[ExecutorSpec]) -> TrainingState:
+    """Fresh state on the layout (engine.py:202-243), built in HBM."""
+    for spec in layout:
+        cfg.kernel_profile(spec.device_kind)  # ConfigError on unknown kinds before allocating
+    ranks = assign_ranks(list(layout), cfg.max_workers)
+    dev = DeviceState(cfg.max_workers, len(ranks))
+    init = ToyModel.init_random(cfg.seed)
+    dev.replicas[:, 0, :] = init.tensor
+    executors = _build_executors(cfg, layout, dev, cfg.lr, cfg.momentum)
+    contexts = []
+    for k in range(cfg.max_workers):
+        ctx = WorkerContext(k, derive_stream(TAG_DROPOUT, cfg.seed, k), TrackedStat())
+        contexts.append(ctx)
+    dev.rng.copy_(torch.tensor([u64_to_i64(c._rng) for c in contexts], dtype=torch.int64))
+    for c in contexts:
+        c._dev = dev
+    dev.invalidate()
+    return TrainingState(cfg, contexts, executors, build_buckets_initial(P, cfg.bucket_capacity),
+                         _new_pipeline(cfg), rebuild_pending=not cfg.determinism.d1, dev=dev)
+
+
+def check_replica_agreement(ts: TrainingState) -> None:
+    """Every executor's params+velocity must be bitwise equal (engine.py:246-258), on the device."""
+    dev = ts.dev
+    if dev.X < 2:
+        return
+    ptrs = (C.c_void_p * dev.X)(*dev.replica_ptrs())
+    _native.check(_native.lib().bt_replica_check(ptrs, dev.X, 2 * P * 8, ptr(dev.flags.t), stream()),
+                  "check_replica_agreement")
+    st, detail, _ = dev.flags.status()
+    if st:
+        dev.flags.reset()
+        if st == 6:
+            kind = ts.executors[detail].device_kind if 0 <= detail < len(ts.executors) else "?"
+            raise CorruptionError(f"model/optimizer replica on executor of kind {kind!r} diverged")
+        raise RuntimeError(f"replica check failed with status {st}")
+
+
+def split_by_rank(global_batch: Batch, max_workers: int) -> list[Batch]:
+    """Row t belongs to rank t mod P (engine.py:261-268)."""
+    if len(global_batch) == 0 or len(global_batch) % max_workers != 0:
+        raise ConfigError(f"global batch of {len(global_batch)} rows is not divisible by {max_workers}")
+    return [global_batch[k::max_workers] for k in range(max_workers)]
+
+
+def _comm_variant(ts: TrainingState):
+    return ts.executors[0].kernel_profile.reduce_variant  # engine.py:309
+
+
+def _rot_tensor(ts: TrainingState):
+    variant = _comm_variant(ts)
+    if fanin_code(variant) == 0:
+        return None
+    key = (ts.bucket_map, ts.cfg.max_workers)
+    dev = ts.dev
+    if dev.rot_key != key:
+        dev.rot = torch.from_numpy(rotation_table(ts.bucket_map, ts.cfg.max_workers)).to("cuda")
+        dev.rot_key = key
+    return dev.rot
+
+
+def _step_args(ts: TrainingState, K: int, B: int, rows: torch.Tensor | None, losses: torch.Tensor,
+               trace: torch.Tensor | None, fuse: bool = True) -> tuple[_native.MlpArgs, list]:
+    cfg, dev = ts.cfg, ts.dev
+    ex0 = ts.executors[0]
+    keep = []
+    a = _native.MlpArgs()
+    a.E = a.E_total = cfg.max_workers
+    a.est_base = 0
+    a.B, a.X, a.K = B, dev.X, K
+    a.fuse_reduce = int(fuse)
+    a.est_per_cta = _native.lib().bt_mlp_pick_est_per_cta(cfg.max_workers, B)
+    a.comm_fanin = fanin_code(_comm_variant(ts))
+    a.rank_override = -1
+    a.rate, a.lr, a.mu, a.jitter = float(cfg.dropout_rate), float(ex0._lr), float(ex0._mu), float(cfg.jitter)
+    a.replicas, a.est_fanin, a.rng = ptr(dev.replicas), ptr(dev.est_fanin), ptr(dev.rng)
+    a.stat_mean, a.stat_count, a.grads, a.losses = ptr(dev.stat_mean), ptr(dev.stat_count), ptr(dev.grads), ptr(losses)
+    rot = _rot_tensor(ts) if fuse else None
+    a.rot = ptr(rot)
+    a.seed = cfg.seed & (2**64 - 1)
+    a.step0 = ts.global_step
+    a.spe = ts.pipeline.steps_per_epoch
+    if rows is not None:
+        a.rows = ptr(rows)
+    else:
+        first = ts.global_step // a.spe
+        last = (ts.global_step + K - 1) // a.spe
+        lists, base = ts.pipeline.device_lists(first, last)
+        keep.append(lists)
+        a.dataset, a.lists, a.epoch_base = ptr(ts.pipeline.dataset_device), ptr(lists), base
+    a.flags, a.bar, a.param_trace = ptr(dev.flags.t), ptr(dev.bar), ptr(trace)
+    keep += [rot, rows, losses, trace]
+    return a, keep
+
+
+def _raise_step_error(ts: TrainingState, st: int, detail: int, what: str) -> None:
+    ts.dev.flags.reset()
+    if st == 6:
+        raise CorruptionError(f"{what}: an executor's model/optimizer replica diverged")
+    if st == 5:
+        raise NumericError(f"{what}: non-finite synchronized gradient")
+    raise RuntimeError(f"{what}: device failure status {st}: {_native.last_error()}")
+
+
+def _finish_steps(ts: TrainingState, nsteps: int) -> None:
+    for ctx in ts.contexts:
+        ctx.pending_grads = None
+        ctx.minibatch_idx += nsteps
+    ts.global_step += nsteps
+    ts.epoch = ts.global_step // ts.pipeline.steps_per_epoch
+    if nsteps and ts.rebuild_pending:
+        # d0: after the first post-boot mini-batch the bucket map is rebuilt
+        # from the layout-keyed arrival order (engine.py:323-328).
+        perm = layout_arrival_perm(P, ts.layout_key())
+        ts.bucket_map = rebuild_buckets_first_minibatch(perm, ts.cfg.bucket_capacity)
+        ts.rebuild_pending = False
+
+
+def run_minibatch(ts: TrainingState, global_batch: Batch | None = None) -> list[float]:
+    """One mini-batch; returns per-EST losses by ascending rank (engine.py:271-329)."""
+    cfg = ts.cfg
+    E = cfg.max_workers
+    rows = None
+    if global_batch is not None:
+        split_by_rank(global_batch, E)  # validation (ConfigError)
+        B = len(global_batch) // E
+        rows = rows_tensor(global_batch)
+    else:
+        B = cfg.micro_batch
+        ts.pipeline.advance_all(ts.global_step)
+    if globals()["allreduce"] is not _DEVICE_ALLREDUCE:
+        return _run_minibatch_unfused(ts, B, rows)
+    losses = torch.empty((1, E), dtype=torch.float64, device="cuda")
+    a, keep = _step_args(ts, 1, B, rows, losses, None)
+    _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()), "run_minibatch")
+    st, detail, _ = ts.dev.flags.status()  # one sync per step (the API returns host losses)
+    ts.dev.invalidate()
+    if st:
+        _raise_step_error(ts, st, detail, "run_minibatch")
+    out = losses[0].tolist()
+    _finish_steps(ts, 1)
+    return out
+
+
+def _run_minibatch_unfused(ts: TrainingState, B: int, rows) -> list[float]:
+    """Same step, seams exposed: fwd/bwd kernel -> engine.allreduce -> sgd_step -> mirror."""
+    cfg, dev = ts.cfg, ts.dev
+    E = cfg.max_workers
+    check_replica_agreement(ts)
+    losses = torch.empty((1, E), dtype=torch.float64, device="cuda")
+    a, keep = _step_args(ts, 1, B, rows, losses, None, fuse=False)
+    _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()), "forward_backward")
+    st, detail, _ = dev.flags.status()
+    dev.invalidate()
+    if st:
+        _raise_step_error(ts, st, detail, "run_minibatch")
+    grads = dev.grads[0]
+    for ex in ts.executors:
+        for rank in ex.assigned[:-1]:  # non-final ESTs park their gradients (engine.py:305-307)
+            ts.contexts[rank].pending_grads = DeviceVector(grads[rank].clone())
+    synced = globals()["allreduce"]([DeviceVector(grads[r]) for r in range(E)], ts.bucket_map, _comm_variant(ts))
+    ex0 = ts.executors[0]
+    new_model, new_opt = sgd_step(ex0.model, ex0.opt, synced)
+    for ex in ts.executors:
+        ex.model = new_model
+        ex.opt = new_opt
+    out = losses[0].tolist()
+    _finish_steps(ts, 1)
+    return out
+
+
+def run_steps(ts: TrainingState, K: int, trace: bool = False):
+    """K mini-batches from the pipeline in one persistent launch.
+
+    Returns (losses [K][E] numpy, params-after-each-step [K][161] numpy or None).
+    Identical bits to K calls of run_minibatch."""
+    if K < 1:
+        raise ConfigError("K must be >= 1")
+    if ts.rebuild_pending or globals()["allreduce"] is not _DEVICE_ALLREDUCE:
+        first = [run_minibatch(ts)]
+        tr = [ts.executors[0].model.values.tolist()] if trace else None
+        if K == 1:
+            return np.array(first), (np.array(tr) if trace else None)
+        rest, rtr = run_steps(ts, K - 1, trace)
+        return np.concatenate([np.array(first), rest]), (np.concatenate([np.array(tr), rtr]) if trace else None)
+    cfg = ts.cfg
+    E = cfg.max_workers
+    for s in range(K):
+        ts.pipeline.advance_all(ts.global_step + s)
+    losses = torch.empty((K, E), dtype=torch.float64, device="cuda")
+    tr = torch.empty((K, P), dtype=torch.float64, device="cuda") if trace else None
+    a, keep = _step_args(ts, K, cfg.micro_batch, None, losses, tr)
+    _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()), "run_steps")
+    st, detail, failed = ts.dev.flags.status()
+    ts.dev.invalidate()
+    if st:
+        done = failed if st == 5 else 0
+        _finish_steps(ts, done)
+        _raise_step_error(ts, st, detail, f"run_steps (mini-batch {ts.global_step})")
+    _finish_steps(ts, K)
+    return losses.cpu().numpy(), (tr.cpu().numpy() if trace else None)
+
+
+def apply_layout(ts: TrainingState, layout: list[ExecutorSpec]) -> TrainingState:
+    """Elastic restart onto a new layout, in device memory.
+
+    Bit-for-bit the reference's checkpoint_save + checkpoint_restore
+    (engine.py:332-336, checkpoint.py:204-238): contexts and one replica carry
+    over; ESTs are redistributed contiguously; every new executor gets a full
+    replica copy (128-bit slot-copy kernel); the bucket map is kept iff d1."""
+    for ctx in ts.contexts:
+        if ctx.pending_grads is not None:
+            raise StateError("checkpoint requested mid-mini-batch (gradients in flight)")
+        if ctx.minibatch_idx != ts.global_step:
+            raise StateError("checkpoint requested mid-mini-batch (progress skew)")
+    check_replica_agreement(ts)
+    cfg = ts.cfg
+    for spec in layout:
+        cfg.kernel_profile(spec.device_kind)
+    ranks = assign_ranks(list(layout), cfg.max_workers)
+    old = ts.dev
+    dev = DeviceState(cfg.max_workers, len(ranks))
+    # EST context slots and replica 0 -> every new replica: one slot-copy launch.
+    pairs = [(dev.rng, old.rng), (dev.stat_mean, old.stat_mean), (dev.stat_count, old.stat_count)]
+    pairs += [(dev.replicas[x], old.replicas[0]) for x in range(dev.X)]
+    dsts = (C.c_void_p * len(pairs))(*[d.data_ptr() for d, _ in pairs])
+    srcs = (C.c_void_p * len(pairs))(*[s.data_ptr() for _, s in pairs])
+    nbytes = (C.c_int64 * len(pairs))(*[d.numel() * d.element_size() for d, _ in pairs])
+    _native.check(_native.lib().bt_est_slot_copy(dsts, srcs, nbytes, len(pairs), stream()), "EST slot copy")
+    ex0 = ts.executors[0]
+    executors = _build_executors(cfg, layout, dev, ex0._lr, ex0._mu)
+    contexts = []
+    for c in ts.contexts:
+        nc = WorkerContext(c.virtual_rank, minibatch_idx=c.minibatch_idx)
+        nc._dev = dev
+        contexts.append(nc)
+    dev.invalidate()
+    pipe = _new_pipeline(cfg, ts.pipeline._dataset_dev)
+    pipe.restore_queue(ts.pipeline.drain_for_checkpoint(), next_step=ts.global_step)
+    d1 = cfg.determinism.d1
+    return TrainingState(cfg, contexts, executors,
+                         ts.bucket_map if d1 else build_buckets_initial(P, cfg.bucket_capacity), pipe,
+                         ts.global_step, ts.epoch, rebuild_pending=not d1, dev=dev)
+
+
+def reconfigure(ts: TrainingState, plan, pool) -> TrainingState:
+    """Restart onto a planner configuration (engine.py:339-346).  The planner
+    itself is out of scope; any object with the reference PlanConfig/DevicePool
+    attributes is accepted."""
+    return apply_layout(ts, plan_layout(plan, pool, ts.cfg.max_workers))
+
+
+def plan_layout(plan, pool, max_workers: int) -> list[ExecutorSpec]:
+    """Expand <nums, executors, threads> into executor specs (engine.py:349-376)."""
+    if plan.cu_capacity < max_workers:
+        raise ConfigError(f"plan capacity {plan.cu_capacity} cannot host {max_workers} workers")
+    specs, remaining = [], max_workers
+    for i, dtype in enumerate(pool.types):
+        if plan.nums[i] > dtype.count:
+            raise ConfigError(f"plan uses {plan.nums[i]} GPUs of {dtype.name!r}, pool has {dtype.count}")
+        for _ in range(plan.nums[i]):
+            for _ in range(plan.executors[i]):
+                take = min(plan.threads[i], remaining)
+                if take > 0:
+                    specs.append(ExecutorSpec(dtype.name, take))
+                    remaining -= take
+    if remaining:
+        raise ConfigError("plan layout could not host every worker")
+    return specs
+
+
+def executor_peak_mu(threads: int, workload_mu: float, context_mu: float = 0.75) -> float:
+    """EST executor memory is flat in the EST count (engine.py:379-387)."""
+    if threads < 1:
+        raise ConfigError("an executor hosts at least one worker")
+    return context_mu + workload_mu
+
+
+def packing_peak_mu(workers: int, workload_mu: float, context_mu: float = 0.75) -> float:
+    """Worker packing grows linearly (engine.py:390-395)."""
+    if workers < 1:
+        raise ConfigError("need at least one packed worker")
+    return workers * (context_mu + workload_mu)

@@ -1,0 +1,216 @@
+"""Deterministic sampling and the shared data-worker pool (reference sampling.py:1-207).
+
+Split between host and device the B200 way:
+  * host (native C): the per-epoch Fisher-Yates order and round-robin deal
+    (`epoch_indices`, sequential by nature), the progress-ordered queue of
+    prefetched WorkerStates (pure bookkeeping, it travels in checkpoints);
+  * device: the resident dataset (generated in counter form), and the
+    gather + jitter of each EST's rows, fused into the step kernel's load
+    (bt_mlp.cu stage A) or run standalone (`bt_jitter_gather`).
+A micro-batch is a pure function of (seed, epoch, local step, EST) exactly
+as in the reference, so any worker-slot count or layout yields the same bytes.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .device import ptr, require_cuda, stream
+from .errors import ConfigError, CorruptionError, ProgressError
+from .model import INPUT_DIM
+from .prng import TAG_DATA_WORKER, derive_stream
+
+Row = tuple[tuple[float, ...], float]
+_i32p = C.POINTER(C.c_int32)
+
+
+def make_dataset_device(seed: int, n: int, dim: int = INPUT_DIM) -> torch.Tensor:
+    """[n][dim+1] rows, all components uniform in [-1, 1) (sampling.py:24-35)."""
+    require_cuda()
+    out = torch.empty((n, dim + 1), dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().bt_make_dataset(seed & (2**64 - 1), n, dim, ptr(out), stream()), "make_dataset")
+    return out
+
+
+def make_dataset(seed: int, n: int, dim: int) -> list[Row]:
+    rows = make_dataset_device(seed, n, dim).tolist()
+    return [(tuple(r[:dim]), r[dim]) for r in rows]
+
+
+@dataclass(frozen=True)
+class SamplePlan:
+    """One epoch's index distribution across all logical workers (drop-last)."""
+
+    seed: int
+    epoch: int
+    dataset_size: int
+    total_workers: int
+    micro_batch: int = 1
+    shuffle: bool = True
+
+    @property
+    def global_batch(self) -> int:
+        return self.total_workers * self.micro_batch
+
+    @property
+    def steps_per_epoch(self) -> int:
+        return self.dataset_size // self.global_batch
+
+
+def epoch_indices_array(plan: SamplePlan) -> np.ndarray:
+    """[workers][steps_per_epoch*micro] int32 lists (native host Fisher-Yates)."""
+    if plan.total_workers < 1:
+        raise ConfigError("total_workers must be >= 1")
+    if plan.dataset_size < plan.total_workers:
+        raise ConfigError("dataset smaller than the worker count")
+    if plan.steps_per_epoch < 1:
+        raise ConfigError("dataset smaller than one global batch")
+    out = np.zeros((plan.total_workers, plan.steps_per_epoch * plan.micro_batch), dtype=np.int32)
+    _native.check(_native.lib().bt_host_epoch_indices(plan.seed & (2**64 - 1), plan.epoch & (2**64 - 1),
+                                                      plan.dataset_size, plan.total_workers, plan.micro_batch,
+                                                      int(plan.shuffle), out.ctypes.data_as(_i32p)))
+    return out
+
+
+def epoch_indices(plan: SamplePlan) -> list[list[int]]:
+    """Shuffle seeded seed^epoch, dealt round-robin (sampling.py:63-82)."""
+    return epoch_indices_array(plan).tolist()
+
+
+@dataclass
+class WorkerState:
+    """What a data worker needs to build one worker's micro-batch; the slot is metadata."""
+
+    worker_index: int
+    worker_slot: int
+    rng: int
+    minibatch_idx: int
+
+
+def worker_rng(seed: int, epoch: int, local_step: int, worker_index: int) -> int:
+    return derive_stream(TAG_DATA_WORKER, seed, epoch, local_step, worker_index)
+
+
+class DataPipeline:
+    """Shared data-worker pool with a progress-ordered queuing buffer."""
+
+    EPOCH_WINDOW = 4  # epochs of index lists kept resident on the device
+
+    def __init__(self, seed: int, dataset_size: int, total_workers: int, micro_batch: int, jitter: float = 0.0,
+                 worker_slots: int = 1, prefetch_depth: int = 2, shuffle: bool = True):
+        if worker_slots < 1:
+            raise ConfigError("need at least one data-worker slot")
+        if prefetch_depth < 0:
+            raise ConfigError("prefetch_depth must be >= 0")
+        self.seed = seed
+        self.dataset_size = dataset_size
+        self.total_workers = total_workers
+        self.micro_batch = micro_batch
+        self.jitter = jitter
+        self.worker_slots = worker_slots
+        self.prefetch_depth = prefetch_depth
+        self.shuffle = shuffle
+        self.steps_per_epoch = SamplePlan(seed, 0, dataset_size, total_workers, micro_batch, shuffle).steps_per_epoch
+        if self.steps_per_epoch < 1:
+            raise ConfigError("dataset smaller than one global batch")
+        self._dataset_dev = None
+        self._queue: dict[tuple[int, int], WorkerState] = {}
+        self._next_step = [0] * total_workers
+        self._lists_host: dict[int, np.ndarray] = {}
+        self._lists_dev: torch.Tensor | None = None
+        self._lists_dev_base = -1
+        self._lists_dev_count = 0
+
+    # ------------------------------------------------------------- device data
+    @property
+    def dataset_device(self) -> torch.Tensor:
+        if self._dataset_dev is None:
+            self._dataset_dev = make_dataset_device(self.seed, self.dataset_size, INPUT_DIM)
+        return self._dataset_dev
+
+    @property
+    def dataset(self) -> list[Row]:
+        rows = self.dataset_device.tolist()
+        return [(tuple(r[:INPUT_DIM]), r[INPUT_DIM]) for r in rows]
+
+    def _lists_for_epoch(self, epoch: int) -> np.ndarray:
+        if epoch not in self._lists_host:
+            plan = SamplePlan(self.seed, epoch, self.dataset_size, self.total_workers, self.micro_batch, self.shuffle)
+            self._lists_host[epoch] = epoch_indices_array(plan)
+            if len(self._lists_host) > 2 * self.EPOCH_WINDOW:
+                for old in sorted(self._lists_host)[: -self.EPOCH_WINDOW]:
+                    del self._lists_host[old]
+        return self._lists_host[epoch]
+
+    def device_lists(self, first_epoch: int, last_epoch: int) -> tuple[torch.Tensor, int]:
+        """Resident [n_epochs][workers][spe*B] lists covering [first, last]; returns (tensor, base epoch)."""
+        if not (self._lists_dev is not None and self._lists_dev_base <= first_epoch
+                and last_epoch < self._lists_dev_base + self._lists_dev_count):
+            count = max(last_epoch - first_epoch + 1, min(self.EPOCH_WINDOW, last_epoch - first_epoch + 1))
+            host = np.stack([self._lists_for_epoch(e) for e in range(first_epoch, first_epoch + count)])
+            self._lists_dev = torch.from_numpy(host).to("cuda")
+            self._lists_dev_base, self._lists_dev_count = first_epoch, count
+        return self._lists_dev, self._lists_dev_base
+
+    # ------------------------------------------------------------- bookkeeping
+    def _make_state(self, step: int, worker: int) -> WorkerState:
+        epoch, local = divmod(step, self.steps_per_epoch)
+        slot = (step * self.total_workers + worker) % self.worker_slots
+        return WorkerState(worker, slot, worker_rng(self.seed, epoch, local, worker), step)
+
+    def _consume(self, worker: int, minibatch_idx: int) -> WorkerState:
+        expected = self._next_step[worker]
+        if minibatch_idx < expected:
+            raise ProgressError(f"mini-batch {minibatch_idx} of worker {worker} was already consumed")
+        if minibatch_idx > expected:
+            raise ProgressError(f"worker {worker} must consume mini-batch {expected} before {minibatch_idx}")
+        ws = self._queue.pop((minibatch_idx, worker), None)
+        if ws is None:
+            ws = self._make_state(minibatch_idx, worker)
+        self._next_step[worker] = minibatch_idx + 1
+        for ahead in range(1, self.prefetch_depth + 1):
+            key = (minibatch_idx + ahead, worker)
+            if key not in self._queue:
+                self._queue[key] = self._make_state(*key)
+        return ws
+
+    def _check_state(self, ws: WorkerState) -> None:
+        epoch, local = divmod(ws.minibatch_idx, self.steps_per_epoch)
+        if ws.rng != worker_rng(self.seed, epoch, local, ws.worker_index):
+            # The device derives the worker RNG from (seed, epoch, local, EST);
+            # a queued state can only differ if the checkpoint was forged.
+            raise CorruptionError(f"queued worker state for ({ws.minibatch_idx}, {ws.worker_index}) has a foreign RNG")
+
+    def batch(self, worker: int, minibatch_idx: int) -> list[Row]:
+        """Produce and consume the micro-batch for (minibatch_idx, worker) (sampling.py:174-198)."""
+        ws = self._consume(worker, minibatch_idx)
+        self._check_state(ws)
+        epoch, local = divmod(minibatch_idx, self.steps_per_epoch)
+        lists, base = self.device_lists(epoch, epoch)
+        rows = torch.empty((self.micro_batch, INPUT_DIM + 1), dtype=torch.float64, device="cuda")
+        _native.check(_native.lib().bt_jitter_gather(
+            ptr(self.dataset_device), ptr(lists[epoch - base]), 1, worker, self.total_workers, self.micro_batch,
+            self.steps_per_epoch, self.seed & (2**64 - 1), epoch, local, float(self.jitter), ptr(rows), stream()),
+            "jitter_gather")
+        return [(tuple(r[:INPUT_DIM]), r[INPUT_DIM]) for r in rows.tolist()]
+
+    def advance_all(self, minibatch_idx: int) -> None:
+        """Consume (minibatch_idx, w) for every worker without producing host rows:
+        the step kernel gathers them on the device.  Same progress/queue semantics as batch()."""
+        for w in range(self.total_workers):  # validate first so a failure leaves no partial progress
+            if self._next_step[w] != minibatch_idx:
+                self._consume(w, minibatch_idx)  # raises the reference's ProgressError
+        for w in range(self.total_workers):
+            self._check_state(self._consume(w, minibatch_idx))
+
+    def drain_for_checkpoint(self) -> list[WorkerState]:
+        return [self._queue[k] for k in sorted(self._queue)]
+
+    def restore_queue(self, states: list[WorkerState], next_step: int) -> None:
+        self._queue = {(ws.minibatch_idx, ws.worker_index): ws for ws in states}
+        self._next_step = [next_step] * self.total_workers

@@ -1,0 +1,284 @@
+"""CUDA path vs the oracle and the reference's golden vectors (needs a B200).
+
+Bar: bit-exact.  The reference is binary64 with a pinned evaluation order; the
+sm_100a kernels use explicit round-to-nearest ops and restate the reference
+libm's tanh, so every loss, gradient, parameter and statistic must match to
+the last bit (tolerance 0 ulp) -- stronger than north_star's 1e-5 relative.
+Every call goes through the C-ABI (include/bittrain_b200.h) via the package.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from golden_util import fhl, hf, hfl, load, u64
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bt():
+    import paper_2208_14228_b200 as pkg
+    from paper_2208_14228_b200 import _native
+
+    assert torch.cuda.is_available(), "GPU test on a box without CUDA"
+    _native.lib()
+    return pkg
+
+
+def test_library_is_the_in_tree_build(bt):
+    from paper_2208_14228_b200 import _native
+
+    assert _native.LIB_PATH.exists()
+    maps = open("/proc/self/maps").read()
+    assert str(_native.LIB_PATH) in maps
+
+
+def test_device_tanh_bitexact_vs_libm(bt, oracle):
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    rng = np.random.default_rng(7)
+    x = np.concatenate([rng.uniform(-4, 4, 400_000), rng.uniform(-30, 30, 200_000), rng.uniform(-1e-3, 1e-3, 100_000),
+                        rng.standard_normal(100_000) * 1e-9, np.array([0.0, -0.0, 22.0, -22.0, 1e-300, np.inf,
+                                                                       -np.inf, 0.5 * math.log(2), 1.0, -1.0])])
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty_like(xd)
+    _native.check(_native.lib().bt_tanh_f64(xd.data_ptr(), xd.numel(), out.data_ptr(), stream()))
+    got = out.cpu().numpy()
+    want = np.array([math.tanh(float(v)) for v in x])  # libm, as the reference's math.tanh (np.tanh is not libm)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_splitmix64_counter_form_matches_stream(bt):
+    from paper_2208_14228_b200.prng import draws
+
+    for seed_hex, outs in load("prng.json")["splitmix64"].items():
+        raw, uni = draws(int(seed_hex, 16), 0, 50)
+        assert [v & (2**64 - 1) for v in raw.tolist()] == [int(o, 16) for o in outs]
+    raw, uni = draws(42, 0, 20)
+    assert fhl(uni.tolist()) == load("prng.json")["uniform01_seed42"]
+
+
+def test_dataset_and_init_on_device(bt):
+    doc = load("sampling.json")
+    from paper_2208_14228_b200.sampling import make_dataset_device
+
+    ds = make_dataset_device(42, 1024).cpu().numpy()
+    assert f"{bt.fnv1a64(ds.astype('<f8').tobytes()):016x}" == doc["dataset_42_1024"]["fnv"]
+    assert [fhl(r) for r in make_dataset_device(42, 64).tolist()] == doc["dataset_42_64"]
+    for seed, vals in load("model.json")["init_random"].items():
+        assert fhl(bt.ToyModel.init_random(int(seed)).values) == vals
+
+
+def test_reduce_sum_shapes(bt):
+    for c in load("reduction.json")["cases"]:
+        vals = hfl(c["values"])
+        assert fhl([bt.reduce_sum(vals, bt.Sequential())]) == [c["seq"]]
+        for f in (2, 3, 4, 5, 8, 16):
+            assert fhl([bt.reduce_sum(vals, bt.Tree(f))]) == [c[f"tree{f}"]]
+
+
+def _variant(bt, tag):
+    return bt.Sequential() if tag == "seq" else bt.Tree(int(tag[4:]))
+
+
+def test_forward_backward_golden(bt):
+    for i, c in enumerate(load("model.json")["forward_backward"]):
+        m = bt.ToyModel(hfl(c["params"]))
+        batch = [(tuple(hfl(x)), hf(y)) for x, y in zip(c["x"], c["y"])]
+        loss, grads, rng, stat = bt.forward_backward(m, batch, c["rank"], u64(c["rng"]),
+                                                     bt.TrackedStat(hf(c["stat_mean"]), c["stat_count"]),
+                                                     _variant(bt, c["variant"]), hf(c["rate"]))
+        assert fhl([loss]) == [c["out_loss"]], i
+        assert fhl(grads) == c["out_grads"], i
+        assert rng == u64(c["out_rng"]), i
+        assert fhl([stat.running_mean]) == [c["out_stat_mean"]] and stat.update_count == c["out_stat_count"], i
+
+
+def test_allreduce_golden(bt):
+    for i, c in enumerate(load("allreduce.json")["cases"]):
+        bm = bt.BucketMap(c["capacity"], tuple(tuple(b) for b in c["buckets"]))
+        out = bt.allreduce([hfl(r) for r in c["replicas"]], bm, _variant(bt, c["variant"]))
+        assert fhl(out) == c["out"], i
+
+
+def test_sgd_step_golden(bt):
+    for c in load("model.json")["sgd_step"]:
+        m2, o2 = bt.sgd_step(bt.ToyModel(hfl(c["params"])), bt.OptState(hf(c["lr"]), hf(c["mu"]), hfl(c["vel"])),
+                             hfl(c["grads"]))
+        assert fhl(m2.values) == c["out_params"] and fhl(o2.velocity) == c["out_vel"]
+
+
+def test_sgd_rejects_non_finite(bt):
+    g = [0.0] * 161
+    g[5] = math.inf
+    m = bt.ToyModel.init_random(1)
+    with pytest.raises(bt.NumericError):
+        bt.sgd_step(m, bt.OptState.fresh(0.1, 0.9), g)
+
+
+def test_pipeline_batches_golden(bt):
+    docs = load("sampling.json")["pipeline_batches"]
+    for nw in (4, 8):
+        pipe = bt.DataPipeline(42, 1024, nw, 4, jitter=0.1, worker_slots=2, prefetch_depth=2)
+        want = {(d["step"], d["est"]): d["rows"] for d in docs if d["workers"] == nw}
+        for step in range(pipe.steps_per_epoch + 2):
+            for est in range(nw):
+                rows = pipe.batch(est, step)
+                if (step, est) in want:
+                    assert [fhl(list(x) + [y]) for x, y in rows] == want[(step, est)], (nw, step, est)
+
+
+def _cfg_from_doc(bt, r):
+    c = r["config"]
+    return bt.TrainRunConfig(seed=c["seed"], max_workers=c["max_workers"], micro_batch=c["micro_batch"],
+                             dataset_size=c["dataset_size"], lr=hf(c["lr"]), momentum=hf(c["momentum"]),
+                             dropout_rate=hf(c["dropout_rate"]), jitter=hf(c["jitter"]),
+                             bucket_capacity=c["bucket_capacity"],
+                             determinism=bt.DeterminismMode.from_label(c["determinism"]), device_fanins=c["devices"])
+
+
+def _spec(bt, layout_doc):
+    lay = tuple(bt.ExecutorSpec(k) for k in layout_doc["initial"])
+    rs = tuple(bt.RestartEvent(s, tuple(bt.ExecutorSpec(k) for k in ks)) for s, ks in layout_doc["restarts"])
+    return bt.RunSpec(lay, rs)
+
+
+RUNS = ["c1_d1", "c2_d1", "c2_d1d2", "train_d1_yaml", "mixed_d1", "mixed_d1d2", "d0_restart", "d0_plain", "small_e16"]
+
+
+@pytest.mark.parametrize("name", RUNS)
+def test_full_run_bit_exact_vs_reference(bt, name):
+    """Whole training runs (persistent fused kernel) vs the reference's own logs."""
+    r = next(x for x in load("runs.json")["runs"] if x["name"] == name)
+    log, ts = bt.run_training(_cfg_from_doc(bt, r), _spec(bt, r["layout"]), r["steps"])
+    assert [fhl(rec.losses) for rec in log.records] == r["losses"]
+    assert [rec.param_hash for rec in log.records] == r["param_hash"]
+    assert fhl(ts.executors[0].model.values) == r["final_params"]
+    assert fhl(ts.executors[0].opt.velocity) == r["final_velocity"]
+    assert [[fhl([c.stat.running_mean])[0], c.stat.update_count] for c in ts.contexts] == r["final_stats"]
+    assert [f"{c.dropout_rng:016x}" for c in ts.contexts] == r["final_dropout_rng"]
+    assert f"{bt.fnv1a64(bt.checkpoint_save(ts)):016x}" == r["final_ckpt_fnv"]
+
+
+@pytest.mark.parametrize("g", [1, 2, 4, 8])
+def test_c2_layout_invariance_on_device(bt, g):
+    """C2: 8 ESTs on 1/2/4/8 executors -> the same bits (cb363c5f8ef799aa)."""
+    r = next(x for x in load("runs.json")["runs"] if x["name"] == "c2_d1")
+    spec = bt.RunSpec(tuple(bt.ExecutorSpec("gpu_fast") for _ in range(g)))
+    log, ts = bt.run_training(_cfg_from_doc(bt, r), spec, 100)
+    assert log.records[-1].param_hash == "cb363c5f8ef799aa"
+    assert [rec.param_hash for rec in log.records] == r["param_hash"]
+
+
+def test_run_minibatch_matches_persistent_kernel(bt):
+    """K single-step launches == one K-step persistent launch, bit for bit."""
+    r = next(x for x in load("runs.json")["runs"] if x["name"] == "c2_d1")
+    cfg = _cfg_from_doc(bt, r)
+    ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")] * 2)
+    for step in range(40):
+        assert fhl(bt.run_minibatch(ts)) == r["losses"][step]
+        assert bt.param_fingerprint(ts.executors[0].model.values) == r["param_hash"][step]
+
+
+def test_global_batch_path(bt):
+    doc = load("global_batch.json")
+    c = doc["config"]
+    cfg = bt.TrainRunConfig(seed=c["seed"], max_workers=c["max_workers"], micro_batch=c["micro_batch"],
+                            dataset_size=c["dataset_size"], determinism=bt.DeterminismMode.from_label("d1"),
+                            device_fanins={"gpu_fast": 2, "gpu_mid": 3})
+    ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")] * c["executors"])
+    for s in doc["steps"]:
+        rows = [(tuple(hfl(row[:8])), hf(row[8])) for row in s["rows"]]
+        assert fhl(bt.run_minibatch(ts, rows)) == s["losses"]
+        assert fhl(ts.executors[0].model.values) == s["params"]
+
+
+def test_checkpoint_bytes_match_reference(bt):
+    for b in load("checkpoint.json")["blobs"]:
+        cfg = bt.TrainRunConfig(seed=42, max_workers=b["workers"], micro_batch=2, dataset_size=64,
+                                determinism=bt.DeterminismMode.from_label(b["mode"]),
+                                device_fanins={"gpu_fast": 2, "gpu_mid": 3})
+        ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")] * b["executors"])
+        for _ in range(b["steps"]):
+            bt.run_minibatch(ts)
+        blob = bt.checkpoint_save(ts)
+        assert blob.hex() == b["blob"]
+        ts2 = bt.checkpoint_restore(blob, [bt.ExecutorSpec("gpu_fast")] * 3, cfg)
+        assert bt.checkpoint_save(ts2) == blob
+
+
+def test_apply_layout_equals_byte_restart(bt):
+    r = next(x for x in load("runs.json")["runs"] if x["name"] == "c2_d1")
+    cfg = _cfg_from_doc(bt, r)
+    a = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")] * 4)
+    for _ in range(7):
+        bt.run_minibatch(a)
+    b = bt.checkpoint_restore(bt.checkpoint_save(a), [bt.ExecutorSpec("gpu_fast")] * 2, cfg)
+    a = bt.apply_layout(a, [bt.ExecutorSpec("gpu_fast")] * 2)
+    assert bt.checkpoint_save(a) == bt.checkpoint_save(b)
+    for _ in range(5):
+        assert bt.run_minibatch(a) == bt.run_minibatch(b)
+    assert bt.checkpoint_save(a) == bt.checkpoint_save(b)
+
+
+def test_tampered_replica_raises_corruption(bt):
+    cfg = bt.TrainRunConfig(seed=42, max_workers=4, micro_batch=2, dataset_size=64,
+                            determinism=bt.DeterminismMode.from_label("d1"), device_fanins={"gpu_a": 2})
+    ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_a")] * 2)
+    bt.run_minibatch(ts)
+    ts.executors[1].model.values[0] = math.nextafter(ts.executors[1].model.values[0], math.inf)
+    with pytest.raises(bt.CorruptionError):
+        bt.run_minibatch(ts)
+
+
+def test_non_finite_gradient_raises_numeric(bt):
+    cfg = bt.TrainRunConfig(seed=42, max_workers=4, micro_batch=2, dataset_size=64,
+                            determinism=bt.DeterminismMode.from_label("d1"), device_fanins={"gpu_a": 2})
+    ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_a")])
+    rows = [((1e308,) * 8, 1e308)] * 8
+    before = ts.executors[0].model.values.tolist()
+    with pytest.raises(bt.NumericError):
+        bt.run_minibatch(ts, rows)
+    assert ts.executors[0].model.values.tolist() == before
+    assert ts.global_step == 0
+
+
+def test_pending_grads_spy(bt, monkeypatch):
+    """The engine calls allreduce through its module global (reference test_engine.py:175-199)."""
+    import paper_2208_14228_b200.engine as engine_mod
+
+    cfg = bt.TrainRunConfig(seed=42, max_workers=4, micro_batch=2, dataset_size=64,
+                            determinism=bt.DeterminismMode.from_label("d1"), device_fanins={"gpu_a": 2})
+    ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_a")] * 2)
+    ref = bt.init_training(cfg, [bt.ExecutorSpec("gpu_a")] * 2)
+    observed = {}
+    real = engine_mod.allreduce
+
+    def spy(replicas, bm, variant):
+        observed["pending"] = [None if c.pending_grads is None else list(c.pending_grads) for c in ts.contexts]
+        observed["replicas"] = [list(r) for r in replicas]
+        return real(replicas, bm, variant)
+
+    monkeypatch.setattr(engine_mod, "allreduce", spy)
+    losses = bt.run_minibatch(ts)
+    monkeypatch.undo()
+    assert observed["pending"][0] == observed["replicas"][0]
+    assert observed["pending"][2] == observed["replicas"][2]
+    assert observed["pending"][1] is None and observed["pending"][3] is None
+    assert all(c.pending_grads is None for c in ts.contexts)
+    # the unfused (spied) path and the fused kernel agree bit for bit
+    assert losses == bt.run_minibatch(ref)
+    assert ts.executors[0].model.values == ref.executors[0].model.values
+
+
+def test_progress_error(bt):
+    pipe = bt.DataPipeline(42, 64, 4, 2, jitter=0.1)
+    pipe.batch(0, 0)
+    with pytest.raises(bt.ProgressError):
+        pipe.batch(0, 0)
+    with pytest.raises(bt.ProgressError):
+        pipe.batch(1, 3)
