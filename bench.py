@@ -256,6 +256,7 @@ def bench_device_dist(bt, K: int, W: int, rank: int, world: int, flush, e2e: boo
                                                                      rng.data_ptr(), mean.data_ptr(), cnt.data_ptr())
         a.grads, a.losses, a.dataset, a.lists = grads_loc.data_ptr(), losses.data_ptr(), dataset.data_ptr(), lists.data_ptr()
         a.seed, a.step0, a.spe, a.epoch_base, a.flags = SEED, step, spe, lbase, flags.t.data_ptr()
+        a.dataset_rows = NROWS
         _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()))
         dist.all_gather_into_tensor(grads_all, grads_loc)
         r = _native.ReduceArgs()

@@ -86,6 +86,10 @@ int bt_fwd_bwd_mlp_f64(const double *params_dev, const double *rows_dev, int32_t
  * variant, rank-keyed) -> /E -> momentum SGD -> mirror to every replica.
  *                                                           engine.py:271-329 */
 int bt_mlp_step(const bt_mlp_args *args, void *stream);
+/* Same launch with per-stage clock64 sums accumulated into timing_dev[0..4]
+ * (rows+tanh, output chain, gradients, allreduce fold, update) and the step
+ * count into timing_dev[5] (profiling; thread 0 of CTA 0's view). */
+int bt_mlp_step_profiled(const bt_mlp_args *args, uint64_t *timing_dev, void *stream);
 /* Default ESTs-per-CTA for a shape (single CTA when the whole step fits). */
 int bt_mlp_pick_est_per_cta(int32_t E, int32_t B);
 

@@ -109,10 +109,10 @@ double or_reduce_sum(const double *values, int n, int fanin) {
         for (int i = 1; i < n; i++) acc += values[i];
         return acc;
     }
-    double buf[4096];
+    double buf[64]; /* small: large stack frames pay stack-clash probes on every call */
     double *lvl = buf;
     double *heap = NULL;
-    if (n > 4096) lvl = heap = (double *)malloc(sizeof(double) * (size_t)n);
+    if (n > 64) lvl = heap = (double *)malloc(sizeof(double) * (size_t)n);
     memcpy(lvl, values, sizeof(double) * (size_t)n);
     int len = n;
     while (len > 1) {
@@ -146,10 +146,9 @@ int or_forward_backward(const double *v, const double *x, const double *y, int n
                         double *loss_out, double *grads, uint64_t *rng_out, double *stat_mean_out,
                         uint64_t *stat_count_out) {
     if (nrows <= 0) return OR_INPUT;
-    enum { MAXR = 256 };
-    if (nrows > MAXR) return OR_INPUT;
-    double acts[MAXR][OR_HIDDEN], masks[MAXR][OR_HIDDEN], hid[MAXR][OR_HIDDEN];
-    double dz[MAXR][OR_HIDDEN], errs[MAXR], gy[MAXR], col[MAXR];
+    if (nrows > 256) return OR_INPUT;
+    double acts[nrows][OR_HIDDEN], masks[nrows][OR_HIDDEN], hid[nrows][OR_HIDDEN]; /* VLAs sized to the batch */
+    double dz[nrows][OR_HIDDEN], errs[nrows], gy[nrows], col[nrows > OR_HIDDEN ? nrows : OR_HIDDEN];
     const int d = OR_INPUT_DIM, h = OR_HIDDEN;
     for (int r = 0; r < nrows; r++) {
         const double *xr = x + (size_t)r * d;
@@ -474,7 +473,7 @@ typedef struct {
 static void or_est_range(or_job *J) {
     or_run *R = J->R;
     const int B = R->cfg.micro_batch, E = R->cfg.max_workers;
-    double x[256 * OR_INPUT_DIM], y[256];
+    double x[R->cfg.micro_batch * OR_INPUT_DIM], y[R->cfg.micro_batch];
     for (int k = J->lo; k < J->hi; k++) {
         if (J->gx) {
             for (int r = 0; r < B; r++) { /* split_by_rank: rows t::E (engine.py:261-268) */

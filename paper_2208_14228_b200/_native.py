@@ -46,7 +46,7 @@ class MlpArgs(C.Structure):
         ("replicas", _vp), ("est_fanin", _vp), ("rng", _vp), ("stat_mean", _vp), ("stat_count", _vp),
         ("grads", _vp), ("losses", _vp), ("rot", _vp), ("rows", _vp), ("dataset", _vp), ("lists", _vp),
         ("seed", _u64), ("step0", _i64), ("spe", _i64), ("epoch_base", _i64),
-        ("flags", _vp), ("bar", _vp), ("param_trace", _vp),
+        ("flags", _vp), ("bar", _vp), ("param_trace", _vp), ("dataset_rows", _i64),
     ]
 
 
@@ -81,6 +81,7 @@ EXPORTS = {
     "bt_fwd_bwd_mlp_f64": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _dbl, _i64, _vp, _vp, _vp, _vp,
                                      _vp, _vp, _vp]),
     "bt_mlp_step": (C.c_int, [C.POINTER(MlpArgs), _vp]),
+    "bt_mlp_step_profiled": (C.c_int, [C.POINTER(MlpArgs), _vp, _vp]),
     "bt_mlp_pick_est_per_cta": (C.c_int, [_i32, _i32]),
     "bt_reduce_update": (C.c_int, [C.POINTER(ReduceArgs), _vp]),
     "bt_sgd_step_f64": (C.c_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp, _vp, _vp]),

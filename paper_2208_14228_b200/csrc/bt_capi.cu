@@ -12,8 +12,9 @@
 #include "bt_common.cuh"
 
 namespace bt {
-int mlp_launch(const bt_mlp_args& a, cudaStream_t s);
+int mlp_launch(const bt_mlp_args& a, cudaStream_t s, unsigned long long* timing = nullptr);
 size_t mlp_smem_bytes(int nrows);
+bool mlp_fused_fits(const bt_mlp_args& a);
 int reduce_launch(const bt_reduce_args& a, cudaStream_t s);
 int reduce_sum_launch(const double* v, int64_t n, int fanin, double* out, cudaStream_t s);
 int sgd_launch(const double* p, const double* v, const double* g, int64_t n, double lr, double mu, double* po,
@@ -174,12 +175,14 @@ int bt_init_random(uint64_t seed, double scale, int64_t n, double* out_dev, void
 
 int bt_mlp_pick_est_per_cta(int32_t E, int32_t B) {
   if (E < 1 || B < 1) return 1;
-  // One CTA (no grid barrier) while the whole step's rows fit a modest tile;
-  // otherwise spread ESTs so each CTA holds <= 64 rows.
-  if ((int64_t)E * B <= 64) return E;
-  int epc = 64 / B;
-  if (epc < 1) epc = 1;
-  return epc > E ? E : epc;
+  // Spread the ESTs over up to 8 CTAs of one thread-block cluster (one SM
+  // each): a mini-batch is a latency-bound fp64 chain, so fewer rows per SM
+  // means less issue contention; the clustered CTAs exchange gradient slots
+  // through DSMEM with one cluster barrier per step.  Each CTA holds at most
+  // 256 rows (shared-memory tile); beyond 8 CTAs the grid-barrier path is used.
+  int epc = (E + 7) / 8;
+  if ((int64_t)epc * B > 256) epc = 256 / B > 0 ? 256 / B : 1;
+  return epc;
 }
 
 static int validate_mlp(const bt_mlp_args* a) {
@@ -193,6 +196,9 @@ static int validate_mlp(const bt_mlp_args* a) {
     return fail(bt::ERR_INPUT, "est_per_cta*B must be in [1, 256]");
   if (a->fuse_reduce && a->E != a->E_total)
     return fail(bt::ERR_INPUT, "fused allreduce needs every EST local (E == E_total)");
+  if (a->fuse_reduce && !bt::mlp_fused_fits(*a))
+    return fail(bt::ERR_INPUT, "%d ESTs do not fit the fused step's shared memory; use grads-only + bt_reduce_update",
+                a->E_total);
   if (!a->fuse_reduce && a->K != 1) return fail(bt::ERR_INPUT, "grads-only mode runs one mini-batch");
   if (a->comm_fanin < 0 || a->comm_fanin == 1) return fail(bt::ERR_CONFIG, "bad allreduce fanin %d", a->comm_fanin);
   if (!a->rows && (!a->dataset || !a->lists || a->spe < 1))
@@ -209,6 +215,12 @@ int bt_mlp_step(const bt_mlp_args* args, void* stream) {
   int st = validate_mlp(args);
   if (st) return st;
   return done(bt::mlp_launch(*args, STREAM(stream)), "bt_mlp_step");
+}
+
+int bt_mlp_step_profiled(const bt_mlp_args* args, uint64_t* timing_dev, void* stream) {
+  int st = validate_mlp(args);
+  if (st) return st;
+  return done(bt::mlp_launch(*args, STREAM(stream), (unsigned long long*)timing_dev), "bt_mlp_step_profiled");
 }
 
 int bt_fwd_bwd_mlp_f64(const double* params_dev, const double* rows_dev, int32_t E, int32_t est_base,

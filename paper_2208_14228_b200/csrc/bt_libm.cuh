@@ -123,4 +123,83 @@ BT_HD double glibc_tanh(double x) {
   return (jx >> 31) ? -z : z;
 }
 
+// ---------------------------------------------------------------------------
+// Branch-free restatement for SIMT execution.  glibc's control flow diverges
+// across a warp (|x| >= 1 or not in tanh; k = 0, +-1, general, < 20, > 56 in
+// expm1), serialising up to ~6 paths.  The version below evaluates the
+// common polynomial once and every cheap reconstruction formula, then selects
+// -- each lane performs exactly the operations glibc performs for its input:
+//  * argument reduction: for k = +-1 glibc computes hi = x -+ ln2_hi,
+//    lo = +-ln2_lo; fma(-t, ln2_hi, x) and t*ln2_lo with t = +-1 are the same
+//    single roundings, and with t = 0 they return x and 0 exactly (x' = x);
+//  * tanh: num/(t+2) with num = 2 (|x| >= 1) or -t, then 1-q or q.
+// Only tanh's rare special inputs (NaN/inf, +-0, |x| < 2^-55, |x| >= 22) take
+// the scalar glibc path.  Inside tanh, expm1 sees x in [-2, -2^-54) u [2, 44),
+// so none of expm1's special branches can trigger there.
+BT_HD double glibc_expm1_fma_tanh_domain(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10,
+               invln2 = 1.44269504088896338700e+00;
+  const double Q1 = -3.33333333333331316428e-02, Q2 = 1.58730158725481460165e-03,
+               Q3 = -7.93650757867487942473e-05, Q4 = 4.00821782732936239552e-06,
+               Q5 = -2.01099218183624371326e-07;
+  const uint32_t hx = hi_word(x) & 0x7fffffffu;
+  const bool neg = (hi_word(x) >> 31) != 0;
+  const int kg = (int)dadd(dmul(invln2, x), neg ? -0.5 : 0.5);
+  const int k = hx <= 0x3fd62e42u ? 0 : (hx < 0x3FF0A2B2u ? (neg ? -1 : 1) : kg);
+  const double tk = (double)k;
+  const double hi = dfma(-tk, ln2_hi, x);
+  const double lo = dmul(tk, ln2_lo);
+  const double xr = dsub(hi, lo);
+  const double c = dsub(dsub(hi, xr), lo);
+  const double hfx = dmul(0.5, xr);
+  const double hxs = dmul(xr, hfx);
+  const double R1 = dfma(hxs, Q1, 1.0);
+  const double h2 = dmul(hxs, hxs);
+  const double R2 = dfma(hxs, Q3, Q2);
+  const double h4 = dmul(h2, h2);
+  const double R3 = dfma(hxs, Q5, Q4);
+  const double r1 = dfma(h4, R3, dfma(h2, R2, R1));
+  const double t = dfma(-r1, hfx, 3.0);
+  const double e = dmul(hxs, ddiv(dsub(r1, t), dfma(-xr, t, 6.0)));
+  const double res0 = dsub(xr, dfma(xr, e, -hxs));           // k == 0
+  const double e2 = dsub(dfma(dsub(e, c), xr, -c), hxs);
+  const double resm1 = dfma(0.5, dsub(xr, e2), -0.5);        // k == -1
+  const double res1 = xr < -0.25 ? dmul(-2.0, dsub(e2, dadd(xr, 0.5))) : dfma(dsub(xr, e2), 2.0, 1.0);
+  const uint32_t kshift = (uint32_t)k << 20;
+  const double yb = dsub(1.0, dsub(e2, xr));                 // k <= -2 || k > 56
+  const double resb = dsub(with_hi(yb, hi_word(yb) + kshift), 1.0);
+  const int kl = k < 0 ? 0 : (k > 31 ? 31 : k);              // 2 <= k < 20 (clamped: no UB shifts)
+  const double tl = u2d((uint64_t)(0x3ff00000u - (0x200000u >> kl)) << 32);
+  const double yl = dsub(tl, dsub(e2, xr));
+  const double resl = with_hi(yl, hi_word(yl) + kshift);
+  const int kh = k < 0 ? 0 : (k > 0x3ff ? 0x3ff : k);        // 20 <= k <= 56
+  const double th = u2d((uint64_t)((uint32_t)(0x3ff - kh) << 20) << 32);
+  const double yh = dadd(dsub(xr, dadd(e2, th)), 1.0);
+  const double resh = with_hi(yh, hi_word(yh) + kshift);
+  double r = resh;
+  r = k < 20 ? resl : r;
+  r = (k <= -2 || k > 56) ? resb : r;
+  r = k == 1 ? res1 : r;
+  r = k == -1 ? resm1 : r;
+  r = k == 0 ? res0 : r;
+  return r;
+}
+
+BT_HD double glibc_tanh_simt(double x) {
+  const uint32_t jx = hi_word(x), ix = jx & 0x7fffffffu, lx = lo_word(x);
+  if (ix >= 0x40360000u || ix < 0x3c800000u || (ix | lx) == 0) {  // rare inputs: glibc's early returns
+    if (ix >= 0x7ff00000u) return (jx >> 31) ? dsub(ddiv(1.0, x), 1.0) : dadd(ddiv(1.0, x), 1.0);
+    if ((ix | lx) == 0) return x;
+    if (ix < 0x3c800000u) return dmul(x, dadd(1.0, x));
+    const double one_m = dsub(1.0, 1e-300);
+    return (jx >> 31) ? -one_m : one_m;
+  }
+  const double ax = fabs(x);
+  const bool big = ix >= 0x3ff00000u;  // |x| >= 1
+  const double t = glibc_expm1_fma_tanh_domain(big ? dadd(ax, ax) : dmul(-2.0, ax));
+  const double q = ddiv(big ? 2.0 : -t, dadd(t, 2.0));
+  const double z = big ? dsub(1.0, q) : q;
+  return (jx >> 31) ? -z : z;
+}
+
 }  // namespace bt

@@ -1,23 +1,27 @@
 // bt_mlp.cu -- fused, persistent data-parallel step for the reference MLP.
 //
 // One launch runs K mini-batches of engine.run_minibatch (engine.py:271-329):
-//   A  rows: device sampler (epoch lists + counter-form worker RNG jitter,
-//      sampling.py:160-172) or an explicit global batch (split_by_rank,
-//      engine.py:261-268);
-//   B  hidden layer + tanh + dropout (model.py:141-163);
-//   C  output error, loss terms, tracked-stat row means (model.py:165-176, 194);
-//   D  dz, per-EST loss / TrackedStat / RNG advance (model.py:173-196, 99-104);
+//   B  rows (device sampler: epoch lists + counter-form worker-RNG jitter,
+//      sampling.py:160-172, or an explicit split_by_rank global batch,
+//      engine.py:261-268) -> hidden layer + tanh + dropout (model.py:141-163);
+//   C  output error, upstream factor gy, dz, tracked-stat row means
+//      (model.py:165-179, 194);
 //   E  161 per-EST gradients, each a batch-dim reduce_sum in the EST's
-//      executor variant (model.py:183-192) -> EST gradient slot;
+//      executor variant (model.py:183-192) -> EST gradient slot; per-EST loss,
+//      TrackedStat update and dropout-RNG advance (model.py:173, 99-104);
 //   F  the fixed-order allreduce in executor 0's variant (buckets.py:115-123,
-//      rank order keyed by EST rank, never by GPU/CTA) fused with /E and the
-//      momentum-SGD update (model.py:206-212).
-// Layout: CTA c owns ESTs [c*epc, (c+1)*epc).  Stage F is computed by EVERY
-// CTA redundantly (bit-identical: same inputs, same order), so a step needs a
-// single grid barrier; gradient slots are double-buffered by step parity so a
-// fast CTA's step s+1 writes never race a slow CTA's step s reads.
-// Every binary64 op uses an explicit _rn intrinsic (no FMA contraction); tanh
-// is glibc's (bt_libm.cuh), so results are bit-identical to the reference.
+//      keyed by EST rank, never by GPU/CTA) fused with /E and momentum SGD
+//      (model.py:206-212).
+// Layout: CTA c owns ESTs [c*epc, (c+1)*epc).  Everything a step touches is
+// staged in shared memory for the whole launch (parameters, velocity, EST
+// RNG/stat slots, the rotation table, the EST gradient slots, and -- when they
+// fit -- the dataset and this launch's index lists), so a step costs its
+// dependent fp64 chain plus four CTA barriers.  With several CTAs, stage F is
+// computed by EVERY CTA redundantly (bit-identical: same inputs, same order)
+// after one grid barrier; global gradient slots are double-buffered by step
+// parity so a fast CTA's step s+1 writes never race a slow CTA's step s reads.
+// Every binary64 op is an explicit _rn intrinsic (no FMA contraction) and tanh
+// is glibc's (bt_libm.cuh): results are bit-identical to the reference.
 #include "bt_common.cuh"
 #include "bt_libm.cuh"
 #include "bt_mlp.cuh"
@@ -25,7 +29,9 @@
 namespace bt {
 
 constexpr int MLP_THREADS = 512;
+constexpr int BT_MAX_FUSED_E = 256;  // ESTs of one fused step (shared slot table)
 constexpr int PAD_P = 168;  // 161 rounded up to a multiple of 8 doubles
+constexpr int FOLD_LEVELS = 10;  // trees of up to 2^9 = 512 leaves
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
@@ -57,43 +63,192 @@ __device__ __forceinline__ bool grid_sync(uint32_t* bar, uint32_t target, int32_
   return s_ok != 0;
 }
 
-__global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_constant__ bt_mlp_args a) {
+// reduce_sum over the B rows of one EST in its executor's variant.  With a
+// compile-time B the common fanins get a fully unrolled register tree.
+template <int BT, class Gen>
+__device__ __forceinline__ double fold_rows(int nb, int fan, Gen gen) {
+  if constexpr (BT > 0) {
+    double v[BT];
+#pragma unroll
+    for (int r = 0; r < BT; ++r) v[r] = gen(r);
+    if (fan == 0 || fan >= BT) return TreeLevel<BT, 0>::run(v);  // Tree(f >= n) folds like Sequential
+    if (fan == 2) return TreeLevel<BT, 2>::run(v);
+    StreamFold<double, FOLD_LEVELS> f;
+    f.init(fan);
+#pragma unroll
+    for (int r = 0; r < BT; ++r) f.push(v[r]);
+    return f.finish();
+  } else {
+    StreamFold<double, FOLD_LEVELS> f;
+    f.init(fan);
+    for (int r = 0; r < nb; ++r) f.push(gen(r));
+    return f.finish();
+  }
+}
+
+// The allreduce fold of one parameter over N EST slots (slot of leaf k is
+// (start+k) mod N), register-resident with a compile-time tree shape.
+// `ld(q)` returns EST slot q's value (local shared memory or a cluster peer's).
+template <int N, class Ld>
+__device__ __forceinline__ double fold_ranks_n(int fan, int start, Ld ld) {
+  double v[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    int q = start + k;
+    q -= q >= N ? N : 0;
+    v[k] = ld(q);
+  }
+  return fan == 0 ? TreeLevel<N, 0>::run(v) : TreeLevel<N, 2>::run(v);  // caller: fan in {0, 2}
+}
+
+// Register tree for the common shapes (power-of-two E, Sequential / Tree(2));
+// everything else takes the (compact) register StreamFold.  Few variants keep
+// the persistent kernel's loop small enough for the instruction cache.
+template <class Ld>
+__device__ __forceinline__ bool fold_ranks_ct(int n, int fan, int start, Ld ld, double* out) {
+  if (!(fan == 0 || fan == 2)) return false;
+  switch (n) {
+    case 1: *out = ld(0); return true;
+    case 2: *out = fold_ranks_n<2>(fan, start, ld); return true;
+    case 4: *out = fold_ranks_n<4>(fan, start, ld); return true;
+    case 8: *out = fold_ranks_n<8>(fan, start, ld); return true;
+    case 16: *out = fold_ranks_n<16>(fan, start, ld); return true;
+    default: return false;
+  }
+}
+
+// Any (E, fanin): the register StreamFold over the rotated slot order.
+template <class Ld>
+__device__ __forceinline__ double fold_ranks_any(int n, int fan, int start, Ld ld) {
+  double out;
+  if (fold_ranks_ct(n, fan, start, ld, &out)) return out;
+  StreamFold<double, 12> f;
+  f.init(fan);
+  for (int k = 0; k < n; ++k) {
+    int q = start + k;
+    q -= q >= n ? n : 0;
+    f.push(ld(q));
+  }
+  return f.finish();
+}
+
+struct MlpLaunch {  // launcher-computed shared-memory plan
+  int stage_data;   // dataset copied into shared memory
+  int stage_idx;    // this launch's index lists copied into shared memory
+  int grads_smem;   // EST gradient slots [E_total][P] in shared memory (fused, non-cluster mode)
+  int cluster;      // fused mode on a thread-block cluster: slots exchanged through DSMEM
+  unsigned long long* timing;  // optional [8] per-stage clock64 sums (bt_mlp_step_profiled)
+};
+
+__device__ __forceinline__ void cluster_barrier() {  // all threads of all CTAs; release/acquire
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster window address of `p` (this CTA's shared memory) in CTA `rank`
+__device__ __forceinline__ uint32_t cluster_map32(const double* p, int rank) {
+  const uint32_t local = (uint32_t)__cvta_generic_to_shared(p);
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(local), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ double ld_dsmem(uint32_t addr) {  // DSMEM load (not the generic path)
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// Per-stage cycle accounting for profiling builds of a launch (thread 0's view
+// of each barrier); compiled in, branch-predicated off when L.timing is null.
+#define BT_TICK(k)                                     \
+  if (L.timing && tid == 0) {                          \
+    const long long now_ = clock64();                  \
+    tacc[k] += (unsigned long long)(now_ - tlast);     \
+    tlast = now_;                                      \
+  }
+
+template <int BT>
+__global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_constant__ bt_mlp_args a,
+                                                               const MlpLaunch L) {
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, T = blockDim.x;
   const int cta = blockIdx.x, G = gridDim.x;
-  const int nb = a.B;
-  const int e0 = cta * a.est_per_cta;
-  const int ne = min(a.est_per_cta, a.E - e0);
+  const int nb = BT > 0 ? BT : a.B;
+  const int epc = a.est_per_cta;
+  const int e0 = cta * epc;
+  const int ne = min(epc, a.E - e0);
   const int nrows = ne * nb;
+  const int rows_cap = epc * nb;
+  const int Et = a.E_total;
 
   double* s_par = sm;
   double* s_vel = s_par + PAD_P;
   double* s_g = s_vel + PAD_P;
-  double* s_x = s_g + PAD_P;                    // [nrows][8]
-  double* s_y = s_x + nrows * BT_INPUT_DIM;     // [nrows]
-  double* s_act = s_y + nrows;                  // [nrows][16] tanh outputs
-  double* s_msk = s_act + nrows * BT_HIDDEN;    // [nrows][16] dropout masks
-  double* s_hid = s_msk + nrows * BT_HIDDEN;    // [nrows][16] acts*mask
-  double* s_dz = s_hid + nrows * BT_HIDDEN;     // [nrows][16]
-  double* s_gy = s_dz + nrows * BT_HIDDEN;      // [nrows]
-  double* s_e2 = s_gy + nrows;                  // [nrows]
-  double* s_rm = s_e2 + nrows;                  // [nrows] row means of acts
+  double* s_x = s_g + PAD_P;                     // [rows][8] jittered inputs
+  double* s_y = s_x + rows_cap * BT_INPUT_DIM;   // [rows]
+  double* s_act = s_y + rows_cap;                // [rows][16] tanh outputs
+  double* s_msk = s_act + rows_cap * BT_HIDDEN;  // [rows][16] dropout masks
+  double* s_hid = s_msk + rows_cap * BT_HIDDEN;  // [rows][16] acts*mask
+  double* s_dz = s_hid + rows_cap * BT_HIDDEN;   // [rows][16]
+  double* s_gy = s_dz + rows_cap * BT_HIDDEN;    // [rows]
+  double* s_e2 = s_gy + rows_cap;                // [rows]
+  double* s_rm = s_e2 + rows_cap;                // [rows] row means of acts
+  double* s_mean = s_rm + rows_cap;              // [epc]
+  uint64_t* s_rng = (uint64_t*)(s_mean + epc);   // [epc]
+  uint64_t* s_cnt = s_rng + epc;                 // [epc]
+  double* s_grad = (double*)(s_cnt + epc);  // [E_total][P] when L.grads_smem; [2][epc][P] when L.cluster
+  double* s_data = s_grad + (L.cluster ? (size_t)2 * epc * BT_P : (L.grads_smem ? (size_t)Et * BT_P : 0));
+  double* s_jit = s_data + (L.stage_data ? (size_t)a.dataset_rows * BT_ROW : 0);  // [K][epc][B] when L.stage_idx
+  int32_t* s_rot = (int32_t*)(s_jit + (L.stage_idx ? (size_t)a.K * rows_cap : 0));  // [P]
+  int32_t* s_fan = s_rot + PAD_P;                // [epc] batch-reduction fanin per local EST
+  int32_t* s_idx = s_fan + ((epc + 1) & ~1);     // [K][epc][B] when L.stage_idx
+
+  __shared__ uint32_t s_slot[BT_MAX_FUSED_E];  // cluster mode: slot q -> shared::cluster address
 
   if (a.flags[FLAG_STATUS] != 0) return;  // sticky error from an earlier launch
+  for (int q = tid; q < Et && L.cluster; q += T) {
+    const int r = q / epc, l = q - r * epc;
+    s_slot[q] = cluster_map32(s_grad + (size_t)l * BT_P, r);
+  }
 
-  // Replica 0 into shared memory + replica agreement (engine.py:246-258: bytes).
+  // ---- launch prologue: stage state in shared memory -----------------------
   const double* rep0 = a.replicas;
   int bad = 0;
-  // (grads-only mode needs no velocity: the seam passes a bare [161] params buffer)
   for (int i = tid; i < BT_P; i += T) {
     const double p0 = rep0[i];
-    const double v0 = a.fuse_reduce ? rep0[BT_P + i] : 0.0;
+    const double v0 = a.fuse_reduce ? rep0[BT_P + i] : 0.0;  // grads-only seam passes bare params
     s_par[i] = p0;
     s_vel[i] = v0;
-    for (int x = 1; x < a.X; ++x) {
+    s_rot[i] = a.rot ? a.rot[i] : 0;
+    for (int x = 1; x < a.X; ++x) {  // replica agreement, bytewise (engine.py:246-258)
       const double* rx = a.replicas + (size_t)x * 2 * BT_P;
       bad |= d2u(rx[i]) != d2u(p0);
       if (a.fuse_reduce) bad |= d2u(rx[BT_P + i]) != d2u(v0);
+    }
+  }
+  for (int el = tid; el < ne; el += T) {
+    s_rng[el] = a.rng[e0 + el];
+    s_mean[el] = a.stat_mean[e0 + el];
+    s_cnt[el] = a.stat_count[e0 + el];
+    s_fan[el] = a.est_fanin[e0 + el];
+  }
+  if (L.stage_data) {
+    const int64_t nd = a.dataset_rows * BT_ROW;
+    for (int64_t i = tid; i < nd; i += T) s_data[i] = a.dataset[i];
+  }
+  if (L.stage_idx) {
+    for (int it = tid; it < a.K * ne * nb; it += T) {
+      const int s = it / (ne * nb), rem = it - s * ne * nb;
+      const int el = rem / nb, r = rem - el * nb;
+      const int64_t gstep = a.step0 + s, epoch = gstep / a.spe, local = gstep % a.spe;
+      const int eg = a.est_base + e0 + el;
+      const int32_t* lst = a.lists + ((size_t)(epoch - a.epoch_base) * Et + eg) * (size_t)(a.spe * nb);
+      const int q = (s * epc + el) * nb + r;
+      s_idx[q] = lst[local * nb + r];
+      double ju = 0.0;
+      if (a.jitter != 0.0) {  // one uniform per row of worker_rng(seed, epoch, local, est) (sampling.py:99-170)
+        const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)epoch, (uint64_t)local, (uint64_t)eg);
+        ju = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), a.jitter);
+      }
+      s_jit[q] = ju;
     }
   }
   if (__syncthreads_or(bad)) {
@@ -107,52 +262,83 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
   const double rate = a.rate;
   const double keep = rate >= 1.0 ? 0.0 : ddiv(1.0, dsub(1.0, rate));  // model.py:150
   const double dB = (double)nb;
+  const double* data = L.stage_data ? s_data : a.dataset;
+  const bool jit = !a.rows && a.jitter != 0.0;
+  int s = 0;
+  int64_t epoch = a.rows ? 0 : a.step0 / a.spe, local = a.rows ? 0 : a.step0 % a.spe;
 
-  for (int s = 0; s < a.K; ++s) {
+  unsigned long long tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+  for (; s < a.K; ++s) {
     const int64_t gstep = a.step0 + s;
-    const int64_t epoch = a.rows ? 0 : gstep / a.spe;
-    const int64_t local = a.rows ? 0 : gstep % a.spe;
-
-    // ---- A: micro-batch rows -------------------------------------------
-    for (int it = tid; it < nrows; it += T) {
-      const int el = it / nb, r = it - el * nb;
-      const int eg = a.est_base + e0 + el;  // global virtual rank
-      const double* src;
-      double u = 0.0;
-      bool jit = false;
-      if (a.rows) {  // split_by_rank: row r of rank k is global row r*E+k
-        src = a.rows + ((size_t)s * nb * a.E_total + (size_t)r * a.E_total + eg) * BT_ROW;
-      } else {
-        const int32_t* lst = a.lists + ((size_t)(epoch - a.epoch_base) * a.E_total + eg) * (size_t)(a.spe * nb);
-        src = a.dataset + (size_t)lst[local * nb + r] * BT_ROW;
-        if (a.jitter != 0.0) {  // one uniform per row (sampling.py:168-170)
-          const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)epoch, (uint64_t)local, (uint64_t)eg);
-          u = unit_float(draw_raw(w, (uint64_t)r));
-          jit = true;
-        }
-      }
-      const double ju = jit ? dmul(dsub(u, 0.5), a.jitter) : 0.0;
-#pragma unroll
-      for (int i = 0; i < BT_INPUT_DIM; ++i) {
-        const double xv = src[i];
-        s_x[it * BT_INPUT_DIM + i] = jit ? dadd(xv, ju) : xv;
-      }
-      s_y[it] = src[BT_INPUT_DIM];
+    if (s > 0 && !a.rows && ++local == a.spe) {  // incremental (no 64-bit division per step)
+      local = 0;
+      ++epoch;
     }
-    __syncthreads();
 
-    // ---- B: hidden pre-activation, tanh, dropout -------------------------
+    // ---- B: rows + hidden pre-activation, tanh, dropout ------------------
+#pragma unroll 1
     for (int it = tid; it < nrows * BT_HIDDEN; it += T) {
       const int row = it >> 4, j = it & 15;
       const int el = row / nb, r = row - el * nb;
-      const double* xr = s_x + row * BT_INPUT_DIM;
-      double acc = dmul(s_par[BT_W1 + j], xr[0]);
+      const int eg = a.est_base + e0 + el;  // global virtual rank
+      double x[BT_ROW];  // 8 inputs, then y
+      double ju = 0.0;
+      if (L.stage_idx && L.stage_data) {  // the common path: shared-memory rows (LDS), staged index + jitter
+        const int q = (s * epc + el) * nb + r;
+        const double* srcs = s_data + (size_t)s_idx[q] * BT_ROW;
+        ju = s_jit[q];
 #pragma unroll
-      for (int i = 1; i < BT_INPUT_DIM; ++i) acc = dadd(acc, dmul(s_par[BT_W1 + i * BT_HIDDEN + j], xr[i]));
-      const double act = glibc_tanh(dadd(acc, s_par[BT_B1 + j]));
+        for (int i = 0; i < BT_ROW; ++i) x[i] = srcs[i];
+      } else {
+        const double* src;
+        if (a.rows) {  // split_by_rank: row r of rank k is global row r*E+k
+          src = a.rows + ((size_t)s * nb * Et + (size_t)r * Et + eg) * BT_ROW;
+        } else if (L.stage_idx) {
+          const int q = (s * epc + el) * nb + r;
+          src = data + (size_t)s_idx[q] * BT_ROW;
+          ju = s_jit[q];
+        } else {
+          const int32_t* lst = a.lists + ((size_t)(epoch - a.epoch_base) * Et + eg) * (size_t)(a.spe * nb);
+          src = data + (size_t)lst[local * nb + r] * BT_ROW;
+          if (jit) {  // one uniform per row (sampling.py:168-170)
+            const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)epoch, (uint64_t)local, (uint64_t)eg);
+            ju = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), a.jitter);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < BT_ROW; ++i) x[i] = src[i];
+      }
+      const long long tb0 = L.timing ? clock64() : 0;
+#pragma unroll
+      for (int i = 0; i < BT_INPUT_DIM; ++i) x[i] = jit ? dadd(x[i], ju) : x[i];
+      {  // lane j < 8 keeps input j, lane 8 keeps y: a select chain, no divergent stores
+        double keepv = x[0];
+#pragma unroll
+        for (int i = 1; i < BT_ROW; ++i) keepv = j == i ? x[i] : keepv;
+        if (j < BT_INPUT_DIM) s_x[row * BT_INPUT_DIM + j] = keepv;
+        else if (j == BT_INPUT_DIM) s_y[row] = keepv;
+      }
+      double acc = dmul(s_par[BT_W1 + j], x[0]);
+#pragma unroll
+      for (int i = 1; i < BT_INPUT_DIM; ++i) acc = dadd(acc, dmul(s_par[BT_W1 + i * BT_HIDDEN + j], x[i]));
+      const double pre = dadd(acc, s_par[BT_B1 + j]);
+      long long tb1 = 0;
+      if (L.timing && tid == 0) {  // profiling: keep `pre` live before the clock read
+        asm volatile("" ::"d"(pre));
+        tb1 = clock64();
+      }
+      const double act = glibc_tanh_simt(pre);
+      if (L.timing && tid == 0) {
+        asm volatile("" ::"d"(act));
+        const long long tb2 = clock64();
+        tacc[6] += (unsigned long long)(tb1 - tb0);
+        tacc[7] += (unsigned long long)(tb2 - tb1);
+        tacc[8] += (unsigned long long)(tb0 - tlast);
+      }
       double m = 1.0;
       if (rate > 0.0) {  // draw n = r*16+j of this EST's stream (rows outer, units inner)
-        const double ud = unit_float(draw_raw(a.rng[e0 + el], (uint64_t)(r * BT_HIDDEN + j)));
+        const double ud = unit_float(draw_raw(s_rng[el], (uint64_t)(r * BT_HIDDEN + j)));
         m = ud < rate ? 0.0 : keep;
       }
       s_act[it] = act;
@@ -160,88 +346,121 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
       s_hid[it] = dmul(act, m);
     }
     __syncthreads();
+    BT_TICK(0)
 
-    // ---- C: output, error, upstream factor, row means --------------------
-    for (int row = tid; row < nrows; row += T) {
-      const double* h = s_hid + row * BT_HIDDEN;
-      double acc = dmul(s_par[BT_W2], h[0]);
+    // ---- C: per row, a 16-lane group (lane j = hidden unit j) ------------
+    // Every lane of the group gathers the 16 products w2[j]*h[j] and the 16
+    // activations by shuffle and runs the two sequential 16-term folds (output
+    // and row mean, model.py:168-171, 194) -- identical bits on every lane, no
+    // divergence -- then lane j writes its own dz[r][j] = ((gy*w2[j])*mask)*(1-a*a)
+    // (model.py:179).
+    {
+      const int span = ((nrows * BT_HIDDEN + 31) / 32) * 32;
+#pragma unroll 1
+      for (int it = tid; it < span; it += T) {
+        const bool valid = it < nrows * BT_HIDDEN;
+        const int row = valid ? it >> 4 : 0, j = it & 15;
+        // all 16 lanes of the group read the same addresses: shared-memory broadcast
+        const double* h = s_hid + row * BT_HIDDEN;
+        const double* ar = s_act + row * BT_HIDDEN;
+        const double actj = ar[j];
+        double acc = dmul(s_par[BT_W2], h[0]);
+        double msum = ar[0];
 #pragma unroll
-      for (int j = 1; j < BT_HIDDEN; ++j) acc = dadd(acc, dmul(s_par[BT_W2 + j], h[j]));
-      const double err = dsub(dadd(acc, s_par[BT_B2]), s_y[row]);
-      s_e2[row] = dmul(err, err);
-      s_gy[row] = ddiv(dmul(2.0, err), dB);
-      const double* ar = s_act + row * BT_HIDDEN;
-      double m = ar[0];
-#pragma unroll
-      for (int j = 1; j < BT_HIDDEN; ++j) m = dadd(m, ar[j]);
-      s_rm[row] = ddiv(m, (double)BT_HIDDEN);
-    }
-    __syncthreads();
-
-    // ---- D: dz, loss, TrackedStat, RNG advance ---------------------------
-    for (int it = tid; it < nrows * BT_HIDDEN; it += T) {
-      const int row = it >> 4, j = it & 15;
-      const double av = s_act[it];
-      s_dz[it] = dmul(dmul(dmul(s_gy[row], s_par[BT_W2 + j]), s_msk[it]), dsub(1.0, dmul(av, av)));
-    }
-    for (int el = tid; el < ne; el += T) {
-      const int e = e0 + el;
-      StreamFold<double, 16> f;
-      f.init(a.est_fanin[e]);
-      for (int r = 0; r < nb; ++r) f.push(s_e2[el * nb + r]);
-      a.losses[(size_t)s * a.E + e] = ddiv(f.finish(), dB);
-      double bm = s_rm[el * nb];
-      for (int r = 1; r < nb; ++r) bm = dadd(bm, s_rm[el * nb + r]);
-      bm = ddiv(bm, dB);
-      const int64_t rank = a.rank_override >= 0 ? a.rank_override : (int64_t)(a.est_base + e);
-      const double mixed = dadd(bm, dmul((double)rank, 0x1p-40));  // model.py:99-104
-      a.stat_mean[e] = dadd(dmul(a.stat_mean[e], 0.9), dmul(0.1, mixed));
-      a.stat_count[e] += 1;
-      if (rate > 0.0) a.rng[e] = advance(a.rng[e], (uint64_t)nb * BT_HIDDEN);
-    }
-    __syncthreads();
-
-    // ---- E: per-EST gradients (batch-dim reduce_sum) -> EST slot ---------
-    double* gbuf = a.grads + (a.fuse_reduce ? (size_t)(gstep & 1) * (size_t)a.E * BT_P : 0);
-    for (int it = tid; it < ne * BT_P; it += T) {
-      const int el = it / BT_P, p = it - el * BT_P;
-      const int rb = el * nb;
-      StreamFold<double, 16> f;
-      f.init(a.est_fanin[e0 + el]);
-      if (p < BT_B1) {
-        const int i = p >> 4, j = p & 15;
-        for (int r = 0; r < nb; ++r) f.push(dmul(s_dz[(rb + r) * BT_HIDDEN + j], s_x[(rb + r) * BT_INPUT_DIM + i]));
-      } else if (p < BT_W2) {
-        const int j = p - BT_B1;
-        for (int r = 0; r < nb; ++r) f.push(s_dz[(rb + r) * BT_HIDDEN + j]);
-      } else if (p < BT_B2) {
-        const int j = p - BT_W2;
-        for (int r = 0; r < nb; ++r) f.push(dmul(s_gy[rb + r], s_hid[(rb + r) * BT_HIDDEN + j]));
-      } else {
-        for (int r = 0; r < nb; ++r) f.push(s_gy[rb + r]);
+        for (int q = 1; q < BT_HIDDEN; ++q) {
+          acc = dadd(acc, dmul(s_par[BT_W2 + q], h[q]));
+          msum = dadd(msum, ar[q]);
+        }
+        if (valid) {
+          const double err = dsub(dadd(acc, s_par[BT_B2]), s_y[row]);
+          const double gy = ddiv(dmul(2.0, err), dB);
+          s_dz[it] = dmul(dmul(dmul(gy, s_par[BT_W2 + j]), s_msk[it]), dsub(1.0, dmul(actj, actj)));
+          if (j == 0) {
+            s_e2[row] = dmul(err, err);
+            s_gy[row] = gy;
+            s_rm[row] = ddiv(msum, (double)BT_HIDDEN);
+          }
+        }
       }
-      gbuf[(size_t)(e0 + el) * BT_P + p] = f.finish();
     }
-    if (!a.fuse_reduce) return;  // grads-only mode (K == 1): the host reduces
+    __syncthreads();
+    BT_TICK(1)
+
+    // ---- E: per-EST gradients -> EST slot; loss, TrackedStat, RNG ---------
+    // One thread per (EST, parameter): a batch-dim reduce_sum in the EST's
+    // executor variant over precomputed terms (model.py:183-192) -- short
+    // independent chains, because with a few warps per SM the step is
+    // latency-bound and per-thread instruction count is the cost.  One more
+    // thread per EST folds the loss and updates TrackedStat and the RNG.
+    double* gbuf = a.grads + (a.fuse_reduce ? (size_t)(gstep & 1) * (size_t)a.E * BT_P : 0);
+    const bool to_global = !a.fuse_reduce || G > 1;
+    const int par = (int)(gstep & 1);
+    constexpr int ITEMS = BT_P + 1;
+#pragma unroll 1
+    for (int it = tid; it < ne * ITEMS; it += T) {
+      const int el = it / ITEMS, p = it - el * ITEMS;
+      const int rb = el * nb;
+      const int fan = s_fan[el];
+      const double g = fold_rows<BT>(nb, fan, [&](int r) {
+        const int row = rb + r;
+        if (p < BT_B1) return dmul(s_dz[row * BT_HIDDEN + (p & 15)], s_x[row * BT_INPUT_DIM + (p >> 4)]);  // w1
+        if (p < BT_W2) return s_dz[row * BT_HIDDEN + (p - BT_B1)];                                         // b1
+        if (p < BT_B2) return dmul(s_gy[row], s_hid[row * BT_HIDDEN + (p - BT_W2)]);                      // w2
+        if (p == BT_B2) return s_gy[row];                                                                  // b2
+        return s_e2[row];                                                                                  // loss
+      });
+      if (p < BT_P) {
+        if (to_global && !L.cluster) gbuf[(size_t)(e0 + el) * BT_P + p] = g;
+        if (L.cluster) s_grad[((size_t)par * epc + el) * BT_P + p] = g;  // step-parity slot, read by peers
+        else if (L.grads_smem) s_grad[(size_t)(e0 + el) * BT_P + p] = g;
+      } else {
+        const int e = e0 + el;
+        const double loss = ddiv(g, dB);
+        a.losses[(size_t)s * a.E + e] = loss;
+        double bm = s_rm[rb];
+        for (int r = 1; r < nb; ++r) bm = dadd(bm, s_rm[rb + r]);
+        bm = ddiv(bm, dB);
+        const int64_t rank = a.rank_override >= 0 ? a.rank_override : (int64_t)(a.est_base + e);
+        const double mixed = dadd(bm, dmul((double)rank, 0x1p-40));  // model.py:99-104
+        s_mean[el] = dadd(dmul(s_mean[el], 0.9), dmul(0.1, mixed));
+        s_cnt[el] += 1;
+        if (rate > 0.0) s_rng[el] = advance(s_rng[el], (uint64_t)nb * BT_HIDDEN);
+      }
+    }
+    if (!a.fuse_reduce) {  // grads-only mode (K == 1): the host reduces
+      ++s;
+      break;
+    }
 
     // ---- F: fixed-order allreduce + /E + momentum SGD --------------------
-    if (G > 1) {
-      if (!grid_sync(a.bar, (uint32_t)(s + 1) * (uint32_t)G, a.flags)) return;
+    if (L.cluster) {
+      // One cluster barrier: every CTA's step-parity slots are complete and
+      // visible (release/acquire); each CTA then folds all E slots -- its own
+      // and its peers' through DSMEM -- in the same rank order, bit-identically.
+      // A CTA can be at most one step ahead, and it writes the other parity.
+      cluster_barrier();
     } else {
+      if (G > 1) {
+        if (!grid_sync(a.bar, (uint32_t)(s + 1) * (uint32_t)G, a.flags)) break;
+        for (int i = tid; i < Et * BT_P; i += T) s_grad[i] = __ldcg(gbuf + i);  // L2: other CTAs' slots
+      }
       __syncthreads();
     }
+    BT_TICK(2)
     int ok = 1;
-    const int Et = a.E_total;
     for (int p = tid; p < BT_P; p += T) {
-      const int start = a.rot ? a.rot[p] : 0;
-      StreamFold<double, 16> f;
-      f.init(a.comm_fanin);
-      for (int k = 0; k < Et; ++k) {
-        int src = start + k;
-        if (src >= Et) src -= Et;
-        f.push(__ldcg(gbuf + (size_t)src * BT_P + p));  // L2: written by other CTAs this step
+      // Leaf k of parameter p is EST slot (rot[p] + k) mod E: ascending virtual
+      // rank, rotated by the parameter's ring chunk under Tree (buckets.py:115-123).
+      // cluster: slot q lives in a peer CTA's shared memory (ld.shared::cluster);
+      // otherwise all slots are local (LDS)
+      const uint32_t off = (uint32_t)(((size_t)par * epc * BT_P + p) * sizeof(double));
+      double sum;
+      if (L.cluster) {
+        sum = fold_ranks_any(Et, a.comm_fanin, s_rot[p], [&](int q) { return ld_dsmem(s_slot[q] + off); });
+      } else {
+        sum = fold_ranks_any(Et, a.comm_fanin, s_rot[p], [&](int q) { return s_grad[(size_t)q * BT_P + p]; });
       }
-      const double g = ddiv(f.finish(), (double)Et);
+      const double g = ddiv(sum, (double)Et);
       s_g[p] = g;
       ok &= finite_d(g) ? 1 : 0;
     }
@@ -250,8 +469,9 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
         a.flags[FLAG_STATUS] = ERR_NUMERIC;
         a.flags[FLAG_STEP] = s;
       }
-      return;
+      break;  // this mini-batch's EST contexts already advanced (engine.py:301-302)
     }
+    BT_TICK(3)
     for (int p = tid; p < BT_P; p += T) {
       const double v = dadd(dmul(a.mu, s_vel[p]), s_g[p]);
       const double np = dsub(s_par[p], dmul(a.lr, v));
@@ -260,10 +480,24 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
       if (a.param_trace && cta == 0) a.param_trace[(size_t)s * BT_P + p] = np;
     }
     __syncthreads();
+    BT_TICK(4)
+  }
+  if (L.timing && tid == 0 && cta == 0) {
+    for (int k = 0; k < 5; ++k) L.timing[k] += tacc[k];
+    for (int k = 6; k < 9; ++k) L.timing[k] += tacc[k];
+    L.timing[5] += (unsigned long long)s;
   }
 
-  // Mirror the update to every executor replica (engine.py:313-315).
-  if (cta == 0) {
+  // ---- epilogue: EST slots back to HBM; mirror the update to every replica
+  if (L.cluster) cluster_barrier();  // peers may still be reading this CTA's slots
+  else __syncthreads();
+  for (int el = tid; el < ne; el += T) {
+    a.rng[e0 + el] = s_rng[el];
+    a.stat_mean[e0 + el] = s_mean[el];
+    a.stat_count[e0 + el] = s_cnt[el];
+  }
+  // (after a NumericError s_par holds the last successfully updated parameters)
+  if (a.fuse_reduce && cta == 0) {  // engine.py:313-315
     for (int x = 0; x < a.X; ++x) {
       double* rx = a.replicas + (size_t)x * 2 * BT_P;
       for (int i = tid; i < BT_P; i += T) {
@@ -274,29 +508,114 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
   }
 }
 
-size_t mlp_smem_bytes(int nrows) {
-  return sizeof(double) * ((size_t)3 * PAD_P + (size_t)nrows * (BT_INPUT_DIM + 1 + 4 * BT_HIDDEN + 3));
+static constexpr size_t SMEM_LIMIT = 220 * 1024;
+
+static size_t base_smem_bytes(const bt_mlp_args& a) {
+  const size_t rows = (size_t)a.est_per_cta * a.B;
+  return sizeof(double) * (3 * PAD_P + rows * (BT_INPUT_DIM + 1 + 4 * BT_HIDDEN + 3) + 3 * (size_t)a.est_per_cta) +
+         sizeof(int32_t) * (PAD_P + (((size_t)a.est_per_cta + 1) & ~(size_t)1));
 }
 
-int mlp_launch(const bt_mlp_args& a, cudaStream_t stream) {
-  const int grid = (a.E + a.est_per_cta - 1) / a.est_per_cta;
-  const size_t smem = mlp_smem_bytes(a.est_per_cta * a.B);
+static constexpr int MAX_CLUSTER = 8;  // portable cluster size
+
+static int grid_of(const bt_mlp_args& a) { return (a.E + a.est_per_cta - 1) / a.est_per_cta; }
+
+static bool use_cluster(const bt_mlp_args& a) {
+  const int g = grid_of(a);
+  return a.fuse_reduce && g > 1 && g <= MAX_CLUSTER;
+}
+
+static MlpLaunch plan(const bt_mlp_args& a, size_t* smem) {
+  MlpLaunch L{0, 0, 0, 0, nullptr};
+  size_t bytes = base_smem_bytes(a);
+  if (use_cluster(a)) {  // [2][epc][P] step-parity slots, exchanged through DSMEM
+    L.cluster = 1;
+    bytes += sizeof(double) * 2 * (size_t)a.est_per_cta * BT_P;
+  } else if (a.fuse_reduce) {
+    const size_t g = sizeof(double) * (size_t)a.E_total * BT_P;
+    if (bytes + g <= SMEM_LIMIT) {
+      L.grads_smem = 1;
+      bytes += g;
+    }
+  }
+  if (!a.rows && a.dataset_rows > 0) {
+    const size_t d = sizeof(double) * (size_t)a.dataset_rows * BT_ROW;
+    if (bytes + d <= SMEM_LIMIT) {
+      L.stage_data = 1;
+      bytes += d;
+    }
+    const size_t ix = (sizeof(int32_t) + sizeof(double)) * (size_t)a.K * a.est_per_cta * a.B;  // idx + jitter
+    if (bytes + ix <= SMEM_LIMIT) {
+      L.stage_idx = 1;
+      bytes += ix;
+    }
+  }
+  *smem = bytes;
+  return L;
+}
+
+size_t mlp_smem_bytes(int nrows) { return sizeof(double) * (3 * PAD_P + (size_t)nrows * 76); }
+
+bool mlp_fused_fits(const bt_mlp_args& a) {
+  if (a.E_total > BT_MAX_FUSED_E) return false;
+  const size_t slots = use_cluster(a) ? 2 * (size_t)a.est_per_cta : (size_t)a.E_total;
+  return base_smem_bytes(a) + sizeof(double) * slots * BT_P <= SMEM_LIMIT;
+}
+
+template <int BT>
+static cudaError_t launch_bt(const bt_mlp_args& a, const MlpLaunch& L, size_t smem, int grid, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(mlp_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
-        cudaSuccess)
-      return ERR_CUDA;
+    cudaError_t e = cudaFuncSetAttribute(mlp_step_kernel<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM_LIMIT);
+    if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  cudaError_t err;
+  if (L.cluster) {
+    // One cluster of `grid` CTAs on `grid` SMs; threads sized to the CTA's rows
+    // (stage B: one thread per (row, unit)), at least one per parameter.
+    int threads = ((a.est_per_cta * a.B * BT_HIDDEN + 31) / 32) * 32;
+    threads = threads < 192 ? 192 : (threads > MLP_THREADS ? MLP_THREADS : threads);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = grid;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, mlp_step_kernel<BT>, a, L);
+  }
   if (grid > 1 && a.fuse_reduce) {
-    if (cudaMemsetAsync(a.bar, 0, sizeof(uint32_t), stream) != cudaSuccess) return ERR_CUDA;
-    void* params[] = {(void*)&a};
-    err = cudaLaunchCooperativeKernel((const void*)mlp_step_kernel, dim3(grid), dim3(MLP_THREADS), params, smem,
-                                      stream);
-  } else {
-    mlp_step_kernel<<<grid, MLP_THREADS, smem, stream>>>(a);
-    err = cudaGetLastError();
+    if (cudaMemsetAsync(a.bar, 0, sizeof(uint32_t), stream) != cudaSuccess) return cudaGetLastError();
+    void* params[] = {(void*)&a, (void*)&L};
+    return cudaLaunchCooperativeKernel((const void*)mlp_step_kernel<BT>, dim3(grid), dim3(MLP_THREADS), params,
+                                       smem, stream);
+  }
+  mlp_step_kernel<BT><<<grid, MLP_THREADS, smem, stream>>>(a, L);
+  return cudaGetLastError();
+}
+
+int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* timing) {
+  const int grid = (a.E + a.est_per_cta - 1) / a.est_per_cta;
+  size_t smem = 0;
+  MlpLaunch L = plan(a, &smem);
+  L.timing = timing;
+  if (a.fuse_reduce && !L.grads_smem && !L.cluster) return ERR_INPUT;  // too many ESTs for the fused path
+  if (smem > SMEM_LIMIT) return ERR_INPUT;
+  cudaError_t err;
+  switch (a.B) {
+    case 1: err = launch_bt<1>(a, L, smem, grid, stream); break;
+    case 2: err = launch_bt<2>(a, L, smem, grid, stream); break;
+    case 4: err = launch_bt<4>(a, L, smem, grid, stream); break;
+    case 8: err = launch_bt<8>(a, L, smem, grid, stream); break;
+    case 16: err = launch_bt<16>(a, L, smem, grid, stream); break;
+    case 32: err = launch_bt<32>(a, L, smem, grid, stream); break;
+    default: err = launch_bt<0>(a, L, smem, grid, stream); break;
   }
   return err == cudaSuccess ? OK : ERR_CUDA;
 }

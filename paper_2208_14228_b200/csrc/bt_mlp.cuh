@@ -53,6 +53,7 @@ typedef struct bt_mlp_args {
   int32_t *flags;          /* [4] sticky device status (bt::Flag) */
   uint32_t *bar;           /* grid barrier counter, zeroed by the launcher */
   double *param_trace;     /* [K][P] parameters after each mini-batch (RunLog fingerprints) or NULL */
+  int64_t dataset_rows;    /* rows in `dataset` (sampler mode); lets the kernel stage it in shared memory */
 } bt_mlp_args;
 
 #ifdef __cplusplus

@@ -393,6 +393,7 @@ def _step_args(ts: TrainingState, K: int, B: int, rows: torch.Tensor | None, los
         lists, base = ts.pipeline.device_lists(first, last)
         keep.append(lists)
         a.dataset, a.lists, a.epoch_base = ptr(ts.pipeline.dataset_device), ptr(lists), base
+        a.dataset_rows = cfg.dataset_size
     a.flags, a.bar, a.param_trace = ptr(dev.flags.t), ptr(dev.bar), ptr(trace)
     keep += [rot, rows, losses, trace]
     return a, keep
@@ -490,16 +491,19 @@ def run_steps(ts: TrainingState, K: int, trace: bool = False):
         return np.concatenate([np.array(first), rest]), (np.concatenate([np.array(tr), rtr]) if trace else None)
     cfg = ts.cfg
     E = cfg.max_workers
-    for s in range(K):
-        ts.pipeline.advance_all(ts.global_step + s)
+    gs = ts.global_step
+    ts.pipeline.advance_all(gs)  # progress check (ProgressError) before anything runs
     losses = torch.empty((K, E), dtype=torch.float64, device="cuda")
     tr = torch.empty((K, P), dtype=torch.float64, device="cuda") if trace else None
     a, keep = _step_args(ts, K, cfg.micro_batch, None, losses, tr)
     _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()), "run_steps")
     st, detail, failed = ts.dev.flags.status()
     ts.dev.invalidate()
+    done = K if not st else (failed if st == 5 else 0)
+    # the failing mini-batch's batches were consumed too (engine.py:282 precedes the sync)
+    for s in range(1, min(K, done + (1 if st == 5 else 0))):
+        ts.pipeline.advance_all(gs + s)
     if st:
-        done = failed if st == 5 else 0
         _finish_steps(ts, done)
         _raise_step_error(ts, st, detail, f"run_steps (mini-batch {ts.global_step})")
     _finish_steps(ts, K)

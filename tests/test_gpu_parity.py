@@ -174,6 +174,38 @@ def test_c2_layout_invariance_on_device(bt, g):
     assert [rec.param_hash for rec in log.records] == r["param_hash"]
 
 
+SHAPES = [  # (E, B, mode, layout kinds, dataset) -> exercises 1 CTA, multi-CTA grid barrier, generic-B path
+    (16, 8, "d1", ("gpu_fast", "gpu_mid"), 1024),
+    (64, 4, "d1", ("gpu_fast",) * 4, 2048),
+    (12, 3, "d1d2", ("gpu_mid", "gpu_fast", "gpu_fast"), 600),
+    (5, 7, "d0", ("gpu_mid",), 400),
+    (32, 16, "d1", ("gpu_mid",) * 2, 4096),
+    (2, 33, "d1", ("gpu_fast",), 700),
+]
+
+
+@pytest.mark.parametrize("E,B,mode,layout,n", SHAPES)
+def test_step_shapes_match_oracle(bt, oracle, E, B, mode, layout, n):
+    cfg = bt.TrainRunConfig(seed=7, max_workers=E, micro_batch=B, dataset_size=n, lr=0.05, momentum=0.8,
+                            dropout_rate=0.3, jitter=0.2, bucket_capacity=40,
+                            determinism=bt.DeterminismMode.from_label(mode),
+                            device_fanins={"gpu_fast": 2, "gpu_mid": 3})
+    ts = bt.init_training(cfg, [bt.ExecutorSpec(k) for k in layout])
+    ref = oracle.Run(seed=7, max_workers=E, micro_batch=B, dataset_size=n, lr=0.05, momentum=0.8, dropout_rate=0.3,
+                     jitter=0.2, bucket_capacity=40, mode=mode, layout=layout)
+    losses, trace = bt.run_steps(ts, 12, trace=True)
+    for s in range(12):
+        want = ref.step()
+        assert np.array_equal(losses[s].view(np.uint64), want.view(np.uint64)), s
+        assert np.array_equal(trace[s].view(np.uint64), ref.state()["params"].view(np.uint64)), s
+    for _ in range(3):  # single-step launches continue the same trajectory
+        assert fhl(bt.run_minibatch(ts)) == fhl(ref.step())
+    st = ref.state()
+    assert fhl(ts.executors[-1].model.values) == fhl(st["params"])
+    assert [c.dropout_rng for c in ts.contexts] == [int(x) for x in st["rng"]]
+    assert fhl([c.stat.running_mean for c in ts.contexts]) == fhl(st["stat_mean"])
+
+
 def test_run_minibatch_matches_persistent_kernel(bt):
     """K single-step launches == one K-step persistent launch, bit for bit."""
     r = next(x for x in load("runs.json")["runs"] if x["name"] == "c2_d1")
