@@ -103,8 +103,14 @@ class ClockSampler:
                 "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def flush_l2(buf: torch.Tensor) -> None:
-    buf.add_(1)  # 256 MiB read+write > 126 MB L2
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch, from the committed
+    `ncu --set full` capture summarised in profiles/ (tools/summarize_ncu.py)."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text()).get(kernel)
+    except (OSError, ValueError):
+        return None
 
 
 # ------------------------------------------------------------------ b200 arm
@@ -327,6 +333,7 @@ def bench_reducer(flush, peaks, E=8, S_MB=256, iters=10):
     torch.cuda.empty_cache()
     best = out["rank_tree2"]
     return {"kernel": "reduce_fast_kernel<float,8,2> (bt_reduce.cu)", "E": E, "S_MB": S_MB, "dtype": "f32",
+            "traffic": ncu_traffic("reduce_fast_kernel"),
             "bound": "hbm", "achieved": round(best["achieved_gbs"], 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(best["frac"], 4), "bytes_per_launch": (E + 4) * n * 4, "ms": round(best["ms"], 4),
             "variants": {k: {kk: round(vv, 4) for kk, vv in d.items()} for k, d in out.items()}}
@@ -467,7 +474,7 @@ def main():
         "gpu_launches": launches,
         "roofline": {"kernel": "mlp_step_kernel (bt_mlp.cu)", "bound": "hbm", "achieved": round(achieved, 3),
                      "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 6),
-                     "traffic": None, "peak_source": peak_src,
+                     "traffic": ncu_traffic("mlp_step_kernel"), "peak_source": peak_src,
                      "note": "latency-bound: one mini-batch is a ~1 kflop/sample dependent fp64 chain over 32 "
                              "samples; HBM and tensor rooflines do not bind (DESIGN.md section 5)",
                      "us_per_step": round(ms * 1e3 / args.steps, 3), "est_per_cta": epc},

@@ -1,0 +1,92 @@
+"""Summarise ncu outputs from gpurun_out/ into profiles/ (committed evidence).
+
+    python tools/summarize_ncu.py <round-tag>
+"""
+import csv
+import json
+import subprocess
+import sys
+from collections import defaultdict
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+OUT = ROOT / "gpurun_out"
+PROF = ROOT / "profiles"
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+
+
+def launches():
+    path = OUT / "launches.csv"
+    if not path.exists():
+        return None
+    rows = [r for r in csv.reader(open(path)) if r]
+    hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[hdr_i]
+    k_i, v_i, m_i = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in rows[hdr_i + 1:]:
+        if len(r) <= v_i or r[m_i] != "gpu__time_duration.sum":
+            continue
+        name = r[k_i].split("(")[0]
+        agg[name][0] += 1
+        agg[name][1] += float(r[v_i].replace(",", ""))
+    tot = sum(v[1] for v in agg.values())
+    lines = [f"# ncu launch list ({path.name}): gpu__time_duration.sum per kernel, --clock-control none",
+             f"# cold-cache, serialised launches: compare SHARES, not absolute times", "",
+             f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'share':>7s}"]
+    for name, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        lines.append(f"{name[:70]:70s} {n:8d} {t / 1e3:12.1f} {t / tot * 100:6.1f}%")
+    (PROF / f"{tag}_launches.txt").write_text("\n".join(lines) + "\n")
+    return agg
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    vals = rows[2:]
+    return [{h: (v, u) for h, u, v in zip(hdr, units, r)} for r in vals]
+
+
+KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread", "launch__block_size",
+        "launch__grid_size", "launch__cluster_dim_x", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "sm__icc_request_hit_rate.pct",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__shared_mem_per_block_dynamic"]
+
+
+def summarize(rep, name):
+    if not rep.exists():
+        return None
+    recs = raw(rep)
+    lines = [f"# ncu --set full summary of {rep.name}", ""]
+    traffic = []
+    for d in recs:
+        for k in KEYS:
+            if k in d:
+                v, u = d[k]
+                lines.append(f"{k:70s} {v} {u}")
+        try:
+            def tob(key):
+                v, u = d[key]
+                v = float(v.replace(",", ""))
+                return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+            traffic.append(tob("dram__bytes_read.sum") + tob("dram__bytes_write.sum"))
+        except (KeyError, ValueError):
+            pass
+        lines.append("")
+    (PROF / f"{tag}_{name}.txt").write_text("\n".join(lines) + "\n")
+    return traffic
+
+
+PROF.mkdir(exist_ok=True)
+launches()
+t_mlp = summarize(OUT / "prof_mlp_r1.ncu-rep", "ncu_mlp_step")
+t_red = summarize(OUT / "prof_reduce_r1.ncu-rep", "ncu_reducer")
+traffic = {"mlp_step_kernel": t_mlp[0] if t_mlp else None, "reduce_fast_kernel": t_red[0] if t_red else None,
+           "source": f"profiles/{tag}_ncu_*.txt (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"}
+(PROF / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+print(json.dumps(traffic))
