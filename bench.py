@@ -219,80 +219,42 @@ def bench_e2e_single(bt, K: int, W: int, flush):
 
 
 def bench_device_dist(bt, K: int, W: int, rank: int, world: int, flush, e2e: bool):
-    """N>1: EST blocks per rank; fwd/bwd kernel -> NCCL all-gather of EST gradient slots -> same
-    fixed-order reduce+SGD kernel on every rank."""
+    """N>1: EST blocks per rank (paper_2208_14228_b200.dist.DistributedTrainer): grads-only step
+    kernel -> NCCL all-gather of EST gradient slots (a bit copy) -> the same fixed-order reduce+SGD
+    kernel on every rank.  e2e: each epoch's index lists are re-uploaded from host memory and every
+    mini-batch's losses are read back inside the timed span."""
     import torch.distributed as dist
 
-    from paper_2208_14228_b200 import _native
-    from paper_2208_14228_b200.buckets import build_buckets_initial, rotation_table
-    from paper_2208_14228_b200.device import Flags, stream, u64_to_i64
-    from paper_2208_14228_b200.prng import TAG_DROPOUT, derive_stream
+    from paper_2208_14228_b200.dist import DistributedTrainer
 
-    assert E_TOTAL % world == 0, "8 ESTs split into equal contiguous blocks"
-    e_loc = E_TOTAL // world
-    base = rank * e_loc
-    cfg = make_cfg(bt)
-    pipe = bt.DataPipeline(SEED, NROWS, E_TOTAL, MICRO, 0.1, 2, 2)
-    spe = pipe.steps_per_epoch
-    params = torch.zeros((2, 161), dtype=torch.float64, device="cuda")
-    params[0] = bt.ToyModel.init_random(SEED).tensor
-    fan = torch.full((e_loc,), 2, dtype=torch.int32, device="cuda")
-    rng = torch.tensor([u64_to_i64(derive_stream(TAG_DROPOUT, SEED, base + k)) for k in range(e_loc)],
-                       dtype=torch.int64, device="cuda")
-    mean = torch.zeros(e_loc, dtype=torch.float64, device="cuda")
-    cnt = torch.zeros(e_loc, dtype=torch.int64, device="cuda")
-    grads_loc = torch.zeros((e_loc, 161), dtype=torch.float64, device="cuda")
-    grads_all = torch.zeros((E_TOTAL, 161), dtype=torch.float64, device="cuda")
-    losses = torch.zeros(e_loc, dtype=torch.float64, device="cuda")
-    rot = torch.from_numpy(rotation_table(build_buckets_initial(161, 64), E_TOTAL)).to("cuda")
-    flags = Flags()
-    new = torch.empty_like(params)
-    dataset = pipe.dataset_device
-    s = torch.cuda.current_stream()
-    host_losses = torch.empty((K + W, e_loc), dtype=torch.float64).pin_memory() if e2e else None
-
-    def step_once(step):
-        epoch, local = divmod(step, spe)
-        lists, lbase = pipe.device_lists(epoch, epoch)
-        a = _native.MlpArgs()
-        a.E, a.est_base, a.E_total, a.B, a.X, a.K = e_loc, base, E_TOTAL, MICRO, 1, 1
-        a.fuse_reduce, a.est_per_cta, a.comm_fanin, a.rank_override = 0, e_loc, 2, -1
-        a.rate, a.lr, a.mu, a.jitter = 0.5, 0.02, 0.9, 0.1
-        a.replicas, a.est_fanin, a.rng, a.stat_mean, a.stat_count = (params.data_ptr(), fan.data_ptr(),
-                                                                     rng.data_ptr(), mean.data_ptr(), cnt.data_ptr())
-        a.grads, a.losses, a.dataset, a.lists = grads_loc.data_ptr(), losses.data_ptr(), dataset.data_ptr(), lists.data_ptr()
-        a.seed, a.step0, a.spe, a.epoch_base, a.flags = SEED, step, spe, lbase, flags.t.data_ptr()
-        a.dataset_rows = NROWS
-        _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()))
-        dist.all_gather_into_tensor(grads_all, grads_loc)
-        r = _native.ReduceArgs()
-        r.dtype, r.mode, r.E, r.fanin, r.n = _native.DTYPE_F64, _native.REDUCE_UPDATE, E_TOTAL, 2, 161
-        r.grads[0], r.grads_ld, r.rot = grads_all.data_ptr(), 161, rot.data_ptr()
-        r.param, r.vel, r.param_out, r.vel_out = params[0].data_ptr(), params[1].data_ptr(), new[0].data_ptr(), new[1].data_ptr()
-        r.lr, r.mu, r.flags = 0.02, 0.9, flags.t.data_ptr()
-        _native.check(_native.lib().bt_reduce_update(C.byref(r), stream()))
-        params.copy_(new)
-        if e2e:
-            host_losses[step].copy_(losses, non_blocking=True)
-
-    for step in range(W):
-        step_once(step)
+    tr = DistributedTrainer(seed=SEED, max_workers=E_TOTAL, micro_batch=MICRO, dataset_size=NROWS)
+    spe = tr.pipe.steps_per_epoch
+    host_losses = torch.empty((K + W, tr.count), dtype=torch.float64).pin_memory()
+    for _ in range(W):
+        tr.step()
     torch.cuda.synchronize()
     dist.barrier()
-    spans = []
-    step = W
+    s = torch.cuda.current_stream()
+    spans, h2d = [], 0
     for n in chunks(K, spe):
+        if e2e:
+            tr.pipe._lists_dev = None  # force the epoch's lists through host memory again
         flush()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
         for _ in range(n):
-            step_once(step)
-            step += 1
+            step = tr.step_idx
+            losses = tr.step()
+            if e2e:
+                host_losses[step].copy_(losses, non_blocking=True)
         e1.record(s)
         e1.synchronize()
         spans.append(e0.elapsed_time(e1))
+        if e2e:
+            h2d += tr.pipe._lists_dev.numel() * 4
+    tr.check()
     dist.barrier()
-    return params[0].clone(), sum(spans), 2 * K
+    return tr.params[0].clone(), sum(spans), 2 * K, h2d / K, tr.count * 8
 
 
 def bench_reducer(flush, peaks, E=8, S_MB=256, iters=10):
@@ -436,16 +398,15 @@ def main():
         final_e = np.array(ts_e.executors[0].model.values.tolist())
         assert np.array_equal(final.view(np.uint64), final_e.view(np.uint64)), "e2e and device runs diverged"
     else:
-        params, ms, launches = bench_device_dist(bt, args.steps, args.warmup, rank, world, flush, False)
+        params, ms, launches, _, _ = bench_device_dist(bt, args.steps, args.warmup, rank, world, flush, False)
         final = params.cpu().numpy()
-        params_e, ms_e2e, launches_e = bench_device_dist(bt, args.steps, args.warmup, rank, world, flush, True)
-        h2d, d2h = 0, (E_TOTAL // world) * 8
+        params_e, ms_e2e, launches_e, h2d, d2h = bench_device_dist(bt, args.steps, args.warmup, rank, world, flush,
+                                                                   True)
         epc = E_TOTAL // world
     if world > 1:
         t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, ms_e2e = t.tolist()
-        h = torch.tensor([int.from_bytes(final.astype("<f8").tobytes()[:8], "little") & (2**62)], device="cuda")
     weights_fnv = f"{bt.fnv1a64(final.astype('<f8').tobytes()):016x}"
     if world > 1:
         allh = [None] * world

@@ -314,3 +314,31 @@ def test_progress_error(bt):
         pipe.batch(0, 0)
     with pytest.raises(bt.ProgressError):
         pipe.batch(1, 3)
+
+
+def test_distributed_trainer_single_rank_matches_reference(bt):
+    """The N>1 code path (grads-only kernel -> all-gather -> fixed-order reduce kernel) run as a
+    world-size-1 NCCL group reproduces the reference's C2 trajectory bit for bit."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2208_14228_b200.dist import DistributedTrainer
+
+    r = next(x for x in load("runs.json")["runs"] if x["name"] == "c2_d1")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        tr = DistributedTrainer(seed=42, max_workers=8, micro_batch=4, dataset_size=1024)
+        for step in range(40):
+            losses = tr.step()
+            assert fhl(losses.tolist()) == r["losses"][step], step
+            assert bt.param_fingerprint(tr.params[0].cpu().numpy().tobytes()) == r["param_hash"][step], step
+        tr.check()
+    finally:
+        dist.destroy_process_group()
