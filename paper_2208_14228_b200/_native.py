@@ -23,7 +23,7 @@ BT_P = 161
 BT_MAX_TABLE = 64
 BT_MAX_REPLICA_OUT = 8
 DTYPE_F64, DTYPE_F32 = 0, 1
-REDUCE_UPDATE, REDUCE_MEAN_ONLY = 0, 1
+REDUCE_UPDATE, REDUCE_MEAN_ONLY, REDUCE_SUM_ONLY = 0, 1, 2
 
 STATUS_TO_ERROR = {
     1: errors.InputError,
@@ -54,7 +54,7 @@ class ReduceArgs(C.Structure):
     """bt_reduce_args (paper_2208_14228_b200/csrc/bt_reduce.cuh)."""
 
     _fields_ = [
-        ("dtype", _i32), ("mode", _i32), ("E", _i32), ("fanin", _i32), ("nout", _i32), ("pad0", _i32),
+        ("dtype", _i32), ("mode", _i32), ("E", _i32), ("fanin", _i32), ("nout", _i32), ("divisor", _i32),
         ("n", _i64), ("grads_ld", _i64), ("grads", _vp * BT_MAX_TABLE), ("rot", _vp),
         ("param", _vp), ("vel", _vp), ("param_out", _vp), ("vel_out", _vp),
         ("extra_param_out", _vp * BT_MAX_REPLICA_OUT), ("extra_vel_out", _vp * BT_MAX_REPLICA_OUT),

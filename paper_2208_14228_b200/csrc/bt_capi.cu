@@ -262,6 +262,8 @@ int bt_reduce_update(const bt_reduce_args* a, void* stream) {
   if (a->fanin < 0 || a->fanin == 1) return fail(bt::ERR_CONFIG, "bad fanin %d", a->fanin);
   if (a->n < 0) return fail(bt::ERR_INPUT, "negative length");
   if (a->nout < 0 || a->nout > BT_MAX_REPLICA_OUT) return fail(bt::ERR_INPUT, "nout outside [0, 8]");
+  if (a->mode < BT_REDUCE_UPDATE || a->mode > BT_REDUCE_SUM_ONLY) return fail(bt::ERR_INPUT, "bad mode %d", a->mode);
+  if (a->divisor < 0) return fail(bt::ERR_INPUT, "negative divisor");
   if (!a->param_out || (a->mode == BT_REDUCE_UPDATE && (!a->param || !a->vel || !a->vel_out || !a->flags)))
     return fail(bt::ERR_INPUT, "null buffer");
   return done(bt::reduce_launch(*a, STREAM(stream)), "bt_reduce_update");

@@ -46,7 +46,11 @@ __device__ __forceinline__ T elem(const bt_reduce_args& a, int k, int64_t p) {
 // Apply /E, finite check and the update for one element.
 template <typename T>
 __device__ __forceinline__ void finish_elem(const bt_reduce_args& a, int64_t p, T sum) {
-  const T g = Arith<T>::div(sum, (T)a.E);
+  if (a.mode == BT_REDUCE_SUM_ONLY) {
+    ((T*)a.param_out)[p] = sum;
+    return;
+  }
+  const T g = Arith<T>::div(sum, (T)(a.divisor > 0 ? a.divisor : a.E));
   if (a.mode == BT_REDUCE_MEAN_ONLY) {
     ((T*)a.param_out)[p] = g;
     return;
@@ -126,11 +130,19 @@ __global__ void __launch_bounds__(256) reduce_fast_kernel(const __grid_constant_
         sum[w] = TreeLevel<NC, 2>::run(v);
       }
     }
+    if (a.mode == BT_REDUCE_SUM_ONLY) {  // per-GPU subtree partial (hierarchical path)
+      V sv;
+#pragma unroll
+      for (int w = 0; w < W; ++w) set_lane(sv, w, sum[w]);
+      st_stream((V*)a.param_out + i, sv);
+      continue;
+    }
     V g;
     bool fin = true;
+    const T div = (T)(a.divisor > 0 ? a.divisor : E);
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      const T gw = Arith<T>::div(sum[w], (T)E);
+      const T gw = Arith<T>::div(sum[w], div);
       set_lane(g, w, gw);
       fin = fin && finite_v(gw);
     }
@@ -218,7 +230,7 @@ static cudaError_t reduce_launch_t(const bt_reduce_args& a, cudaStream_t s) {
   if (fast_ok) {
     for (int k = 0; k < a.E; ++k) fast_ok = fast_ok && aligned16(a.grads[k]);
     fast_ok = fast_ok && aligned16(a.param_out);
-    if (a.mode == BT_REDUCE_UPDATE) {
+    if (a.mode == BT_REDUCE_UPDATE) {  // (SUM_ONLY / MEAN_ONLY only write param_out)
       fast_ok = fast_ok && aligned16(a.param) && aligned16(a.vel) && aligned16(a.vel_out);
       for (int r = 0; r < a.nout; ++r) fast_ok = fast_ok && aligned16(a.extra_param_out[r]) && aligned16(a.extra_vel_out[r]);
     }

@@ -10,10 +10,13 @@ extern "C" {
 #define BT_MAX_REPLICA_OUT 8
 
 enum { BT_DTYPE_F64 = 0, BT_DTYPE_F32 = 1 };
-enum { BT_REDUCE_UPDATE = 0, BT_REDUCE_MEAN_ONLY = 1 };
+enum { BT_REDUCE_UPDATE = 0, BT_REDUCE_MEAN_ONLY = 1, BT_REDUCE_SUM_ONLY = 2 };
 
 /* out[p] = reduce_sum(g[(rot[p]+k) % E][p] for k in 0..E-1, fanin) / E   (buckets.py:115-123)
  * then, in BT_REDUCE_UPDATE mode, v' = mu*v + out; p' = p - lr*v'      (model.py:206-212).
+ * BT_REDUCE_SUM_ONLY writes the raw fold (no division): the per-GPU subtree of
+ * the hierarchical RankTree(2) path, whose top level is then folded over the G
+ * partials in rank order with divisor = E.
  * Contributions are addressed by EST rank k: either a table of E base pointers
  * (each may be a local slot or a peer GPU's slot mapped by CUDA IPC) or one
  * strided buffer (grads_ld > 0: base grads[0], EST k at grads[0] + k*grads_ld
@@ -25,7 +28,7 @@ typedef struct bt_reduce_args {
   int32_t E;      /* contributions per element (EST count) */
   int32_t fanin;  /* 0 = Sequential, >= 2 = Tree(fanin) */
   int32_t nout;   /* extra replica outputs (P2P stores = fused parameter all-gather) */
-  int32_t pad0;
+  int32_t divisor;   /* 0: divide by E; > 0: divide by this (hierarchical top level: the job's E) */
   int64_t n;         /* elements in this shard */
   int64_t grads_ld;  /* > 0: strided mode */
   const void *grads[BT_MAX_TABLE];
