@@ -131,10 +131,15 @@ int bt_step_status(const int32_t *flags_dev, int32_t *detail_out, int32_t *step_
 
 /* ---------------- multi-GPU plumbing (one process per GPU) -------------- */
 int bt_ipc_handle_size(void);
-int bt_ipc_get_handle(const void *dev_ptr, void *handle_out);
+/* handle of the allocation containing dev_ptr, plus dev_ptr's byte offset in it */
+int bt_ipc_get_handle(const void *dev_ptr, void *handle_out, int64_t *offset_out);
 int bt_ipc_open_handle(const void *handle, void **dev_ptr_out);
 int bt_ipc_close(void *dev_ptr);
 int bt_enable_peer_access(int32_t peer_device);
+/* stream-ordered signalling between GPUs: write a word when the stream gets
+ * here (local or peer memory); make a stream wait until a word is >= value */
+int bt_stream_write_u32(void *dev_ptr, uint32_t value, void *stream);
+int bt_stream_wait_u32_geq(void *dev_ptr, uint32_t value, void *stream);
 
 #ifdef __cplusplus
 }

@@ -94,7 +94,9 @@ EXPORTS = {
     "bt_flags_reset": (C.c_int, [_vp, _vp]),
     "bt_step_status": (C.c_int, [_vp, _i32p, _i32p, _vp]),
     "bt_ipc_handle_size": (C.c_int, []),
-    "bt_ipc_get_handle": (C.c_int, [_vp, _vp]),
+    "bt_ipc_get_handle": (C.c_int, [_vp, _vp, _i64p]),
+    "bt_stream_write_u32": (C.c_int, [_vp, C.c_uint32, _vp]),
+    "bt_stream_wait_u32_geq": (C.c_int, [_vp, C.c_uint32, _vp]),
     "bt_ipc_open_handle": (C.c_int, [_vp, C.POINTER(_vp)]),
     "bt_ipc_close": (C.c_int, [_vp]),
     "bt_enable_peer_access": (C.c_int, [_i32]),

@@ -346,11 +346,54 @@ int bt_step_status(const int32_t* flags_dev, int32_t* detail_out, int32_t* step_
 }
 
 // ------------------------------------------------------------- multi-GPU
+}  // extern "C"
+
+// Driver entry points through the runtime (no link-time dependency on libcuda,
+// so the library still loads on a GPU-less build host).
+typedef int (*PFN_getAddressRange)(unsigned long long*, size_t*, unsigned long long);
+typedef int (*PFN_streamWriteValue32)(void*, unsigned long long, unsigned int, unsigned int);
+typedef int (*PFN_streamWaitValue32)(void*, unsigned long long, unsigned int, unsigned int);
+template <typename F>
+static F driver_fn(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return (F)fn;
+}
+
+extern "C" {
+
 int bt_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
-int bt_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+int bt_ipc_get_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out) {
+  // An IPC handle names a whole cudaMalloc allocation; caching allocators hand
+  // out sub-ranges, so return the handle of the base plus the byte offset.
+  static PFN_getAddressRange range = driver_fn<PFN_getAddressRange>("cuMemGetAddressRange");
+  unsigned long long base = (unsigned long long)dev_ptr;
+  size_t size = 0;
+  if (range && range(&base, &size, (unsigned long long)dev_ptr) != 0) return fail(bt::ERR_CUDA, "cuMemGetAddressRange");
   cudaIpcMemHandle_t h;
-  if (cudaIpcGetMemHandle(&h, (void*)dev_ptr) != cudaSuccess) return cuda_fail("cudaIpcGetMemHandle");
+  if (cudaIpcGetMemHandle(&h, (void*)base) != cudaSuccess) return cuda_fail("cudaIpcGetMemHandle");
   memcpy(handle_out, &h, sizeof h);
+  if (offset_out) *offset_out = (int64_t)((unsigned long long)dev_ptr - base);
+  return 0;
+}
+
+// Stream-ordered cross-GPU signalling (no host barrier, no spinning kernel):
+// write a 32-bit word (local or peer/IPC memory) when the stream reaches this
+// point, and block a stream until a word is >= value.
+int bt_stream_write_u32(void* dev_ptr, uint32_t value, void* stream) {
+  static PFN_streamWriteValue32 fn = driver_fn<PFN_streamWriteValue32>("cuStreamWriteValue32");
+  if (!fn) return fail(bt::ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  if (fn(stream, (unsigned long long)dev_ptr, value, 0 /*CU_STREAM_WRITE_VALUE_DEFAULT*/) != 0)
+    return fail(bt::ERR_CUDA, "cuStreamWriteValue32 failed");
+  return 0;
+}
+int bt_stream_wait_u32_geq(void* dev_ptr, uint32_t value, void* stream) {
+  static PFN_streamWaitValue32 fn = driver_fn<PFN_streamWaitValue32>("cuStreamWaitValue32");
+  if (!fn) return fail(bt::ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  if (fn(stream, (unsigned long long)dev_ptr, value, 0 /*CU_STREAM_WAIT_VALUE_GEQ*/) != 0)
+    return fail(bt::ERR_CUDA, "cuStreamWaitValue32 failed");
   return 0;
 }
 int bt_ipc_open_handle(const void* handle, void** dev_ptr_out) {

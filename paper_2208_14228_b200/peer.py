@@ -1,0 +1,149 @@
+"""The G-rank reducer across processes: CUDA IPC peer pointers + stream memory ops.
+
+One process per GPU.  Each rank exports IPC handles of its EST gradient slots,
+subtree partial, parameter/velocity replica and two 32-bit signal words, and
+maps every peer's.  A step is then (hier.GroupReducer's schedule, per rank):
+
+  phase 1  subtree partial of the rank's own slots        (RankTree(2) only)
+  signal   write own sig[0] = step  (cuStreamWriteValue32, ordered after phase 1)
+  wait     every peer's sig[0] >= step  (cuStreamWaitValue32 -- the GPU front
+           end blocks the stream; no host barrier, no spinning kernel)
+  phase 2  owner of shard g: peer LOADS of the G partials (or all E slots for
+           owner-computes) over NVLink, fixed rank-order fold, /E, momentum SGD,
+           peer STORES of the updated shard into every replica
+  signal   own sig[1] = step; wait every peer's sig[1] >= step
+
+so the reduce-scatter, update and parameter all-gather are one kernel per rank
+that moves data over NVLink itself, ordered purely on the device.  The control
+plane (exchanging handles once) uses torch.distributed (NCCL or gloo).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+import torch.distributed as dist
+
+from . import _native
+from .hier import GroupReducer, RankBuffers, _pow2, shard_bounds  # noqa: F401  (shared schedule/shards)
+from .device import Flags
+from .errors import ConfigError
+
+
+def _export(t: torch.Tensor) -> tuple[bytes, int]:
+    n = _native.lib().bt_ipc_handle_size()
+    buf = (C.c_char * n)()
+    off = C.c_int64()
+    _native.check(_native.lib().bt_ipc_get_handle(t.data_ptr(), buf, C.byref(off)), "ipc export")
+    return bytes(buf), off.value
+
+
+class _Opened:
+    """Open each distinct peer allocation once; unmap on close."""
+
+    def __init__(self):
+        self.bases: dict[bytes, int] = {}
+
+    def ptr(self, handle: bytes, offset: int) -> int:
+        if handle not in self.bases:
+            p = C.c_void_p()
+            _native.check(_native.lib().bt_ipc_open_handle(handle, C.byref(p)), "ipc open")
+            self.bases[handle] = p.value
+        return self.bases[handle] + offset
+
+    def close(self):
+        for base in self.bases.values():
+            _native.lib().bt_ipc_close(base)
+        self.bases.clear()
+
+
+class PeerGroupReducer:
+    """This rank's side of a G-rank deterministic reduce over CUDA IPC (see module doc)."""
+
+    NAMES = ("grads", "partial", "param", "vel", "sig")
+
+    def __init__(self, local: RankBuffers, E: int, variant: str = "rank_tree2", rot: torch.Tensor | None = None,
+                 lr: float = 0.02, mu: float = 0.9, group=None):
+        self.group = group
+        self.rank, self.G = dist.get_rank(group), dist.get_world_size(group)
+        self.local, self.E, self.variant, self.rot, self.lr, self.mu = local, E, variant, rot, lr, mu
+        if E % self.G:
+            raise ConfigError("E must split into equal contiguous rank blocks")
+        self.E_loc = E // self.G
+        if variant == "rank_tree2" and not (_pow2(self.E_loc) and _pow2(self.G)):
+            raise ConfigError("hierarchical RankTree(2) needs power-of-two E/G and G")
+        if variant != "rank_tree2" and E > _native.BT_MAX_TABLE:
+            raise ConfigError(f"owner-computes reads at most {_native.BT_MAX_TABLE} slots per element")
+        if local.partial is None:
+            local.partial = torch.empty_like(local.param)
+        self.sig = torch.zeros(2, dtype=torch.int32, device=local.param.device)
+        self.n, self.es = local.param.numel(), local.param.element_size()
+        self.dtype = _native.DTYPE_F64 if local.param.dtype == torch.float64 else _native.DTYPE_F32
+        self.shards = shard_bounds(self.n, self.G, 16 // self.es)
+        mine = {k: _export(getattr(self, k) if k == "sig" else getattr(local, k)) for k in self.NAMES}
+        table = [None] * self.G
+        dist.all_gather_object(table, mine, group=group)
+        self.opened = _Opened()
+        self.ptrs = []
+        for q in range(self.G):
+            if q == self.rank:
+                self.ptrs.append({k: (self.sig if k == "sig" else getattr(local, k)).data_ptr() for k in self.NAMES})
+            else:
+                self.ptrs.append({k: self.opened.ptr(*table[q][k]) for k in self.NAMES})
+        self.flags = Flags()
+        self.step_no = 0
+
+    def _signal_and_wait(self, word: int) -> None:
+        s = self.local.stream.cuda_stream
+        me = self.ptrs[self.rank]["sig"] + 4 * word
+        _native.check(_native.lib().bt_stream_write_u32(me, self.step_no, s), "signal")
+        for q in range(self.G):
+            if q != self.rank:
+                _native.check(_native.lib().bt_stream_wait_u32_geq(self.ptrs[q]["sig"] + 4 * word, self.step_no, s),
+                              "wait")
+
+    def step(self) -> None:
+        self.step_no += 1
+        loc, s = self.local, self.local.stream.cuda_stream
+        row = self.n * self.es  # bytes per EST slot row
+        if self.variant == "rank_tree2":
+            a = _native.ReduceArgs()
+            a.dtype, a.mode, a.E, a.fanin, a.n = self.dtype, _native.REDUCE_SUM_ONLY, self.E_loc, 2, self.n
+            for k in range(self.E_loc):
+                a.grads[k] = loc.grads[k].data_ptr()
+            a.param_out = loc.partial.data_ptr()
+            _native.check(_native.lib().bt_reduce_update(C.byref(a), s), "subtree")
+        self._signal_and_wait(0)
+        lo, hi = self.shards[self.rank]
+        if hi > lo:
+            off = lo * self.es
+            a = _native.ReduceArgs()
+            a.dtype, a.mode, a.n = self.dtype, _native.REDUCE_UPDATE, hi - lo
+            if self.variant == "rank_tree2":
+                a.E, a.fanin, a.divisor = self.G, 2, self.E
+                for q in range(self.G):
+                    a.grads[q] = self.ptrs[q]["partial"] + off
+            else:
+                a.E, a.fanin = self.E, 0 if self.variant == "sequential" else 2
+                for k in range(self.E):
+                    a.grads[k] = self.ptrs[k // self.E_loc]["grads"] + (k % self.E_loc) * row + off
+                if self.rot is not None:
+                    a.rot = self.rot.data_ptr() + lo * 4
+            a.param = a.param_out = self.ptrs[self.rank]["param"] + off
+            a.vel = a.vel_out = self.ptrs[self.rank]["vel"] + off
+            others = [q for q in range(self.G) if q != self.rank]
+            a.nout = len(others)
+            for i, q in enumerate(others):
+                a.extra_param_out[i] = self.ptrs[q]["param"] + off
+                a.extra_vel_out[i] = self.ptrs[q]["vel"] + off
+            a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
+            _native.check(_native.lib().bt_reduce_update(C.byref(a), s), "owner")
+        self._signal_and_wait(1)
+
+    def check(self) -> None:
+        self.flags.raise_if_set("peer group reduce")
+
+    def close(self) -> None:
+        torch.cuda.synchronize()
+        self.opened.close()

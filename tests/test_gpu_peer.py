@@ -1,0 +1,103 @@
+"""Multi-process G-rank reducer over CUDA IPC + stream memory ops (paper_2208_14228_b200.peer).
+
+Two processes share the one B200 of this run (IPC works across processes on
+the same device); each maps the other's slots, partial, replica and signal
+words, and the reduce-scatter / update / all-gather move data through those
+peer pointers with device-side ordering only.  Both replicas must equal the
+single-GPU reducer bit for bit, over several steps.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, variant, q):
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root))
+    import torch.distributed as dist
+
+    from paper_2208_14228_b200.hier import RankBuffers
+    from paper_2208_14228_b200.peer import PeerGroupReducer
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _run(rank, world, variant, q, dist, RankBuffers, PeerGroupReducer)
+    except Exception:  # report instead of leaving the parent waiting on the queue
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(rank, world, variant, q, dist, RankBuffers, PeerGroupReducer):
+    if True:
+        E, n = 8, 20_003
+        rng = np.random.default_rng(11)
+        grads = (rng.uniform(-1, 1, (E, n)) * 10.0 ** rng.integers(-12, 13, (E, n))).astype(np.float32)
+        p0 = rng.uniform(-1, 1, n).astype(np.float32)
+        E_loc = E // world
+        torch.cuda.set_device(0)
+        loc = RankBuffers(torch.from_numpy(grads[rank * E_loc:(rank + 1) * E_loc].copy()).cuda(),
+                          torch.from_numpy(p0.copy()).cuda(), torch.zeros(n, dtype=torch.float32, device="cuda"),
+                          torch.cuda.Stream())
+        red = PeerGroupReducer(loc, E, variant, None, 0.05, 0.9)
+        for _ in range(3):
+            red.step()
+        torch.cuda.synchronize()
+        red.check()
+        dist.barrier()
+        q.put((rank, loc.param.cpu().numpy().tobytes(), loc.vel.cpu().numpy().tobytes()))
+        dist.barrier()
+        red.close()
+
+
+@pytest.mark.parametrize("variant", ["rank_tree2", "sequential"])
+def test_two_process_ipc_reducer(oracle, variant):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, variant, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        res = {}
+        for _ in procs:
+            r, pb, vb = q.get(timeout=120)
+            assert pb != "error", vb
+            res[r] = (pb, vb)
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs)
+    E, n = 8, 20_003
+    rng = np.random.default_rng(11)
+    grads = (rng.uniform(-1, 1, (E, n)) * 10.0 ** rng.integers(-12, 13, (E, n))).astype(np.float32)
+    p = rng.uniform(-1, 1, n).astype(np.float32)
+    v = np.zeros(n, np.float32)
+    for _ in range(3):
+        p, v = oracle.reduce_update(grads, None, "tree2" if variant == "rank_tree2" else "seq", p, v, 0.05, 0.9)
+    for r in (0, 1):
+        assert res[r][0] == p.tobytes() and res[r][1] == v.tobytes()
