@@ -77,7 +77,12 @@ class DistributedTrainer:
     """C2-style job sharded over the ranks of the default process group (one GPU each)."""
 
     def __init__(self, seed=42, max_workers=8, micro_batch=4, dataset_size=1024, lr=0.02, momentum=0.9,
-                 dropout_rate=0.5, jitter=0.1, bucket_capacity=64, fanin=2, comm_fanin=2, group=None):
+                 dropout_rate=0.5, jitter=0.1, bucket_capacity=64, fanin=2, comm_fanin=2, group=None,
+                 exchange: str = "allgather"):
+        """exchange: "allgather" -- NCCL all-gather of the EST slots, then the reduce kernel on every
+        rank; "ipc" -- no collective at all: each rank owns a parameter shard and its reduce kernel
+        reads every rank's slots and writes every rank's replica through CUDA IPC peer pointers,
+        ordered by stream memory operations (paper_2208_14228_b200.peer)."""
         require_cuda()
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.E, self.B = max_workers, micro_batch
@@ -101,6 +106,21 @@ class DistributedTrainer:
         self.pipe = DataPipeline(seed, dataset_size, self.E, micro_batch, jitter, 2, 2)
         self.flags = Flags()
         self.step_idx = 0
+        self.exchange = exchange
+        self.peer = None
+        if exchange == "ipc":
+            from .hier import RankBuffers
+            from .peer import PeerGroupReducer
+
+            if comm_fanin not in (0, 2):
+                raise ConfigError("the IPC reducer supports Sequential and Tree(2) allreduce variants")
+            if self.E % self.world:
+                raise ConfigError("the IPC reducer needs equal EST blocks per rank")
+            self.peer = PeerGroupReducer(
+                RankBuffers(self.grads_loc, self.params[0], self.params[1], torch.cuda.current_stream()), self.E,
+                "sequential" if comm_fanin == 0 else "tree2_rotated", self.rot, lr, momentum, group)
+        elif exchange != "allgather":
+            raise ConfigError(f"unknown exchange {exchange!r}")
 
     def step(self) -> torch.Tensor:
         """One mini-batch; returns this rank's per-EST losses (device tensor)."""
@@ -120,6 +140,10 @@ class DistributedTrainer:
         a.seed, a.step0, a.spe, a.epoch_base = self.seed & (2**64 - 1), self.step_idx, spe, lbase
         a.flags = self.flags.t.data_ptr()
         _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()), "forward_backward")
+        if self.peer is not None:  # fused reduce-scatter + SGD + all-gather over peer memory
+            self.peer.step()
+            self.step_idx += 1
+            return self.losses
         self.xchg.allgather(self.grads_loc, self.grads_all)
         r = _native.ReduceArgs()
         r.dtype, r.mode, r.E, r.fanin, r.n = _native.DTYPE_F64, _native.REDUCE_UPDATE, self.E, self.comm_fanin, PARAM_COUNT
@@ -134,6 +158,8 @@ class DistributedTrainer:
         return self.losses
 
     def check(self) -> None:
+        if self.peer is not None:
+            self.peer.check()
         st, detail, _ = self.flags.status()
         if st == 5:
             raise NumericError(f"non-finite synchronized gradient at parameter {detail}")

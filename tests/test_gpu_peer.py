@@ -101,3 +101,70 @@ def test_two_process_ipc_reducer(oracle, variant):
         p, v = oracle.reduce_update(grads, None, "tree2" if variant == "rank_tree2" else "seq", p, v, 0.05, 0.9)
     for r in (0, 1):
         assert res[r][0] == p.tobytes() and res[r][1] == v.tobytes()
+
+
+def _trainer_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root))
+    import torch.distributed as dist
+
+    from paper_2208_14228_b200.dist import DistributedTrainer
+    from paper_2208_14228_b200.runlog import param_fingerprint
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        tr = DistributedTrainer(seed=42, max_workers=8, micro_batch=4, dataset_size=1024, exchange="ipc")
+        hashes, losses = [], []
+        for _ in range(40):
+            losses.append(tr.step().cpu().numpy().tobytes())
+            hashes.append(param_fingerprint(tr.params[0].cpu().numpy().tobytes()))
+        tr.check()
+        dist.barrier()
+        q.put((rank, hashes, losses))
+        dist.barrier()
+        tr.peer.close()
+    except Exception:
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_trainer_over_ipc_matches_reference():
+    """C2 with 4 ESTs per process, 2 processes, EST slots and replicas shared through CUDA IPC:
+    the reference's own per-step param fingerprints and losses, on both ranks."""
+    import struct
+
+    import torch.multiprocessing as mp
+
+    from golden_util import load
+
+    r = next(x for x in load("runs.json")["runs"] if x["name"] == "c2_d1")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_trainer_worker, args=(k, 2, port, q)) for k in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        res = {}
+        for _ in procs:
+            k, hashes, losses = q.get(timeout=180)
+            assert hashes != "error", losses
+            res[k] = (hashes, losses)
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for k in (0, 1):
+        assert res[k][0] == r["param_hash"][:40]
+        for step, blob in enumerate(res[k][1]):
+            got = [struct.pack("<d", v).hex() for v in struct.unpack(f"<{len(blob) // 8}d", blob)]
+            assert got == r["losses"][step][4 * k: 4 * k + 4], (k, step)
