@@ -218,16 +218,18 @@ def bench_e2e_single(bt, K: int, W: int, flush):
     return ts, sum(spans), launches, h2d / K, d2h / K, host_losses
 
 
-def bench_device_dist(bt, K: int, W: int, rank: int, world: int, flush, e2e: bool):
+def bench_device_dist(bt, K: int, W: int, rank: int, world: int, flush, e2e: bool, exchange: str):
     """N>1: EST blocks per rank (paper_2208_14228_b200.dist.DistributedTrainer): grads-only step
-    kernel -> NCCL all-gather of EST gradient slots (a bit copy) -> the same fixed-order reduce+SGD
-    kernel on every rank.  e2e: each epoch's index lists are re-uploaded from host memory and every
-    mini-batch's losses are read back inside the timed span."""
+    kernel, then either (ipc) each rank's owner kernel reads all EST slots of its parameter shard and
+    writes every replica through CUDA IPC peer pointers, ordered by stream memory ops, or (allgather)
+    an NCCL all-gather of the slots (a bit copy) and the same fixed-order reduce+SGD on every rank.
+    e2e: each epoch's index lists are re-uploaded from host memory and every mini-batch's losses are
+    read back inside the timed span."""
     import torch.distributed as dist
 
     from paper_2208_14228_b200.dist import DistributedTrainer
 
-    tr = DistributedTrainer(seed=SEED, max_workers=E_TOTAL, micro_batch=MICRO, dataset_size=NROWS)
+    tr = DistributedTrainer(seed=SEED, max_workers=E_TOTAL, micro_batch=MICRO, dataset_size=NROWS, exchange=exchange)
     spe = tr.pipe.steps_per_epoch
     host_losses = torch.empty((K + W, tr.count), dtype=torch.float64).pin_memory()
     for _ in range(W):
@@ -367,6 +369,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-reducer", action="store_true")
+    ap.add_argument("--exchange", default="ipc", choices=["ipc", "allgather"],
+                    help="N>1: peer-memory reducer over CUDA IPC, or NCCL all-gather of EST slots")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -398,10 +402,18 @@ def main():
         final_e = np.array(ts_e.executors[0].model.values.tolist())
         assert np.array_equal(final.view(np.uint64), final_e.view(np.uint64)), "e2e and device runs diverged"
     else:
-        params, ms, launches, _, _ = bench_device_dist(bt, args.steps, args.warmup, rank, world, flush, False)
+        exchange = args.exchange
+        try:
+            params, ms, launches, _, _ = bench_device_dist(bt, args.steps, args.warmup, rank, world, flush, False,
+                                                           exchange)
+        except Exception as exc:  # e.g. no peer access between these GPUs: the NCCL all-gather path
+            print(f"bench: exchange={exchange} failed ({exc}); using allgather", file=sys.stderr)
+            exchange = "allgather"
+            params, ms, launches, _, _ = bench_device_dist(bt, args.steps, args.warmup, rank, world, flush, False,
+                                                           exchange)
         final = params.cpu().numpy()
         params_e, ms_e2e, launches_e, h2d, d2h = bench_device_dist(bt, args.steps, args.warmup, rank, world, flush,
-                                                                   True)
+                                                                   True, exchange)
         epc = E_TOTAL // world
     if world > 1:
         t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device="cuda")
@@ -439,9 +451,11 @@ def main():
                      "note": "latency-bound: one mini-batch is a ~1 kflop/sample dependent fp64 chain over 32 "
                              "samples; HBM and tensor rooflines do not bind (DESIGN.md section 5)",
                      "us_per_step": round(ms * 1e3 / args.steps, 3), "est_per_cta": epc},
-        "weights_fnv": weights_fnv,
+        "weights_fnv": weights_fnv,  # FNV-1a of the final weights: equal for every N (bit-identical mappings)
         "clocks": clk,
     }
+    if world > 1:
+        line["config"]["exchange"] = exchange
     if reducer is not None:
         line["reducer"] = reducer
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
