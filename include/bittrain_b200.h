@@ -90,6 +90,9 @@ int bt_mlp_step(const bt_mlp_args *args, void *stream);
  * (rows+tanh, output chain, gradients, allreduce fold, update) and the step
  * count into timing_dev[5] (profiling; thread 0 of CTA 0's view). */
 int bt_mlp_step_profiled(const bt_mlp_args *args, uint64_t *timing_dev, void *stream);
+/* 1 when the fused (fuse_reduce = 1) step fits on chip for these args (E_total
+ * slots in shared memory), else 0: use grads-only + bt_reduce_update. */
+int bt_mlp_fused_fits(const bt_mlp_args *args);
 /* Default ESTs-per-CTA for a shape (single CTA when the whole step fits). */
 int bt_mlp_pick_est_per_cta(int32_t E, int32_t B);
 

@@ -509,6 +509,7 @@ int or_run_step(or_run *R, const double *gx, const double *gy, double *losses_ou
     }
     int nt = R->nthreads > 1 ? R->nthreads : 1;
     if (nt > E) nt = E;
+    if (nt > 64) nt = 64;
     or_job jobs[64];
     pthread_t th[64];
     for (int t = 0; t < nt; t++) {

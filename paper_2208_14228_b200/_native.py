@@ -82,6 +82,7 @@ EXPORTS = {
                                      _vp, _vp, _vp]),
     "bt_mlp_step": (C.c_int, [C.POINTER(MlpArgs), _vp]),
     "bt_mlp_step_profiled": (C.c_int, [C.POINTER(MlpArgs), _vp, _vp]),
+    "bt_mlp_fused_fits": (C.c_int, [C.POINTER(MlpArgs)]),
     "bt_mlp_pick_est_per_cta": (C.c_int, [_i32, _i32]),
     "bt_reduce_update": (C.c_int, [C.POINTER(ReduceArgs), _vp]),
     "bt_sgd_step_f64": (C.c_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp, _vp, _vp]),

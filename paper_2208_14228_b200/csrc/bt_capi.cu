@@ -211,6 +211,8 @@ static int validate_mlp(const bt_mlp_args* a) {
   return 0;
 }
 
+int bt_mlp_fused_fits(const bt_mlp_args* args) { return args && bt::mlp_fused_fits(*args) ? 1 : 0; }
+
 int bt_mlp_step(const bt_mlp_args* args, void* stream) {
   int st = validate_mlp(args);
   if (st) return st;

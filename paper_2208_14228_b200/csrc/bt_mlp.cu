@@ -29,7 +29,8 @@
 namespace bt {
 
 constexpr int MLP_THREADS = 512;
-constexpr int BT_MAX_FUSED_E = 256;  // ESTs of one fused step (shared slot table)
+constexpr int BT_MAX_FUSED_E = 256;  // ESTs of one fused step
+constexpr int MAX_CLUSTER_CTAS = 8;  // portable thread-block cluster size
 constexpr int PAD_P = 168;  // 161 rounded up to a multiple of 8 doubles
 constexpr int FOLD_LEVELS = 10;  // trees of up to 2^9 = 512 leaves
 
@@ -113,6 +114,8 @@ __device__ __forceinline__ bool fold_ranks_ct(int n, int fan, int start, Ld ld, 
     case 4: *out = fold_ranks_n<4>(fan, start, ld); return true;
     case 8: *out = fold_ranks_n<8>(fan, start, ld); return true;
     case 16: *out = fold_ranks_n<16>(fan, start, ld); return true;
+    case 32: *out = fold_ranks_n<32>(fan, start, ld); return true;
+    case 64: *out = fold_ranks_n<64>(fan, start, ld); return true;
     default: return false;
   }
 }
@@ -150,10 +153,8 @@ __device__ __forceinline__ uint32_t cluster_map32(const double* p, int rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(local), "r"(rank));
   return out;
 }
-__device__ __forceinline__ double ld_dsmem(uint32_t addr) {  // DSMEM load (not the generic path)
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-  return v;
+__device__ __forceinline__ void st_dsmem(uint32_t addr, double v) {  // DSMEM store (fire and forget)
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
 
 // Per-stage cycle accounting for profiling builds of a launch (thread 0's view
@@ -195,19 +196,16 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
   uint64_t* s_rng = (uint64_t*)(s_mean + epc);   // [epc]
   uint64_t* s_cnt = s_rng + epc;                 // [epc]
   double* s_grad = (double*)(s_cnt + epc);  // [E_total][P] when L.grads_smem; [2][epc][P] when L.cluster
-  double* s_data = s_grad + (L.cluster ? (size_t)2 * epc * BT_P : (L.grads_smem ? (size_t)Et * BT_P : 0));
+  double* s_data = s_grad + (L.cluster ? (size_t)2 * Et * BT_P : (L.grads_smem ? (size_t)Et * BT_P : 0));
   double* s_jit = s_data + (L.stage_data ? (size_t)a.dataset_rows * BT_ROW : 0);  // [K][epc][B] when L.stage_idx
   int32_t* s_rot = (int32_t*)(s_jit + (L.stage_idx ? (size_t)a.K * rows_cap : 0));  // [P]
   int32_t* s_fan = s_rot + PAD_P;                // [epc] batch-reduction fanin per local EST
   int32_t* s_idx = s_fan + ((epc + 1) & ~1);     // [K][epc][B] when L.stage_idx
 
-  __shared__ uint32_t s_slot[BT_MAX_FUSED_E];  // cluster mode: slot q -> shared::cluster address
+  __shared__ uint32_t s_peer[MAX_CLUSTER_CTAS];  // cluster mode: CTA r's slot array (shared::cluster)
 
   if (a.flags[FLAG_STATUS] != 0) return;  // sticky error from an earlier launch
-  for (int q = tid; q < Et && L.cluster; q += T) {
-    const int r = q / epc, l = q - r * epc;
-    s_slot[q] = cluster_map32(s_grad + (size_t)l * BT_P, r);
-  }
+  for (int r = tid; r < G && L.cluster; r += T) s_peer[r] = cluster_map32(s_grad, r);
 
   // ---- launch prologue: stage state in shared memory -----------------------
   const double* rep0 = a.replicas;
@@ -261,7 +259,8 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
 
   const double rate = a.rate;
   const double keep = rate >= 1.0 ? 0.0 : ddiv(1.0, dsub(1.0, rate));  // model.py:150
-  const double dB = (double)nb;
+  // true divisions of the reference (model.py:173,176,194, buckets.py:123); exact multiplies for powers of two
+  const IntDivisor divB = IntDivisor::of(nb), divH = IntDivisor::of(BT_HIDDEN), divE = IntDivisor::of(Et);
   const double* data = L.stage_data ? s_data : a.dataset;
   const bool jit = !a.rows && a.jitter != 0.0;
   int s = 0;
@@ -373,12 +372,12 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
         }
         if (valid) {
           const double err = dsub(dadd(acc, s_par[BT_B2]), s_y[row]);
-          const double gy = ddiv(dmul(2.0, err), dB);
+          const double gy = divB.apply(dmul(2.0, err));
           s_dz[it] = dmul(dmul(dmul(gy, s_par[BT_W2 + j]), s_msk[it]), dsub(1.0, dmul(actj, actj)));
           if (j == 0) {
             s_e2[row] = dmul(err, err);
             s_gy[row] = gy;
-            s_rm[row] = ddiv(msum, (double)BT_HIDDEN);
+            s_rm[row] = divH.apply(msum);
           }
         }
       }
@@ -411,15 +410,18 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
       });
       if (p < BT_P) {
         if (to_global && !L.cluster) gbuf[(size_t)(e0 + el) * BT_P + p] = g;
-        if (L.cluster) s_grad[((size_t)par * epc + el) * BT_P + p] = g;  // step-parity slot, read by peers
+        if (L.cluster) {  // push this EST's slot into every CTA's copy of the step-parity slot array
+          const uint32_t off = (uint32_t)((((size_t)par * Et + e0 + el) * BT_P + p) * sizeof(double));
+          for (int r = 0; r < G; ++r) st_dsmem(s_peer[r] + off, g);
+        }
         else if (L.grads_smem) s_grad[(size_t)(e0 + el) * BT_P + p] = g;
       } else {
         const int e = e0 + el;
-        const double loss = ddiv(g, dB);
+        const double loss = divB.apply(g);
         a.losses[(size_t)s * a.E + e] = loss;
         double bm = s_rm[rb];
         for (int r = 1; r < nb; ++r) bm = dadd(bm, s_rm[rb + r]);
-        bm = ddiv(bm, dB);
+        bm = divB.apply(bm);
         const int64_t rank = a.rank_override >= 0 ? a.rank_override : (int64_t)(a.est_base + e);
         const double mixed = dadd(bm, dmul((double)rank, 0x1p-40));  // model.py:99-104
         s_mean[el] = dadd(dmul(s_mean[el], 0.9), dmul(0.1, mixed));
@@ -451,16 +453,10 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
     for (int p = tid; p < BT_P; p += T) {
       // Leaf k of parameter p is EST slot (rot[p] + k) mod E: ascending virtual
       // rank, rotated by the parameter's ring chunk under Tree (buckets.py:115-123).
-      // cluster: slot q lives in a peer CTA's shared memory (ld.shared::cluster);
-      // otherwise all slots are local (LDS)
-      const uint32_t off = (uint32_t)(((size_t)par * epc * BT_P + p) * sizeof(double));
-      double sum;
-      if (L.cluster) {
-        sum = fold_ranks_any(Et, a.comm_fanin, s_rot[p], [&](int q) { return ld_dsmem(s_slot[q] + off); });
-      } else {
-        sum = fold_ranks_any(Et, a.comm_fanin, s_rot[p], [&](int q) { return s_grad[(size_t)q * BT_P + p]; });
-      }
-      const double g = ddiv(sum, (double)Et);
+      // every slot is local: cluster peers pushed theirs before the barrier
+      const double* col = s_grad + (L.cluster ? (size_t)par * Et * BT_P : 0) + p;
+      const double sum = fold_ranks_any(Et, a.comm_fanin, s_rot[p], [&](int q) { return col[(size_t)q * BT_P]; });
+      const double g = divE.apply(sum);
       s_g[p] = g;
       ok &= finite_d(g) ? 1 : 0;
     }
@@ -522,15 +518,16 @@ static int grid_of(const bt_mlp_args& a) { return (a.E + a.est_per_cta - 1) / a.
 
 static bool use_cluster(const bt_mlp_args& a) {
   const int g = grid_of(a);
-  return a.fuse_reduce && g > 1 && g <= MAX_CLUSTER;
+  return a.fuse_reduce && g > 1 && g <= MAX_CLUSTER &&
+         base_smem_bytes(a) + sizeof(double) * 2 * (size_t)a.E_total * BT_P <= SMEM_LIMIT;
 }
 
 static MlpLaunch plan(const bt_mlp_args& a, size_t* smem) {
   MlpLaunch L{0, 0, 0, 0, nullptr};
   size_t bytes = base_smem_bytes(a);
-  if (use_cluster(a)) {  // [2][epc][P] step-parity slots, exchanged through DSMEM
+  if (use_cluster(a)) {  // every CTA holds all [2][E][P] step-parity slots; peers push theirs via DSMEM
     L.cluster = 1;
-    bytes += sizeof(double) * 2 * (size_t)a.est_per_cta * BT_P;
+    bytes += sizeof(double) * 2 * (size_t)a.E_total * BT_P;
   } else if (a.fuse_reduce) {
     const size_t g = sizeof(double) * (size_t)a.E_total * BT_P;
     if (bytes + g <= SMEM_LIMIT) {
@@ -558,7 +555,7 @@ size_t mlp_smem_bytes(int nrows) { return sizeof(double) * (3 * PAD_P + (size_t)
 
 bool mlp_fused_fits(const bt_mlp_args& a) {
   if (a.E_total > BT_MAX_FUSED_E) return false;
-  const size_t slots = use_cluster(a) ? 2 * (size_t)a.est_per_cta : (size_t)a.E_total;
+  const size_t slots = use_cluster(a) ? 2 * (size_t)a.E_total : (size_t)a.E_total;
   return base_smem_bytes(a) + sizeof(double) * slots * BT_P <= SMEM_LIMIT;
 }
 

@@ -399,6 +399,16 @@ def _step_args(ts: TrainingState, K: int, B: int, rows: torch.Tensor | None, los
     return a, keep
 
 
+def _fused_fits(cfg, B: int | None = None) -> bool:
+    """Whether one fused launch holds the whole step on chip (bt_mlp_fused_fits)."""
+    a = _native.MlpArgs()
+    a.E = a.E_total = cfg.max_workers
+    a.B = cfg.micro_batch if B is None else B
+    a.K, a.fuse_reduce = 1, 1
+    a.est_per_cta = _native.lib().bt_mlp_pick_est_per_cta(a.E, a.B)
+    return bool(_native.lib().bt_mlp_fused_fits(C.byref(a)))
+
+
 def _raise_step_error(ts: TrainingState, st: int, detail: int, what: str) -> None:
     ts.dev.flags.reset()
     if st == 6:
@@ -434,7 +444,8 @@ def run_minibatch(ts: TrainingState, global_batch: Batch | None = None) -> list[
     else:
         B = cfg.micro_batch
         ts.pipeline.advance_all(ts.global_step)
-    if globals()["allreduce"] is not _DEVICE_ALLREDUCE:
+    if globals()["allreduce"] is not _DEVICE_ALLREDUCE or not _fused_fits(cfg, B):
+        # spied allreduce seam, or too many ESTs for on-chip slots: kernels per seam
         return _run_minibatch_unfused(ts, B, rows)
     losses = torch.empty((1, E), dtype=torch.float64, device="cuda")
     a, keep = _step_args(ts, 1, B, rows, losses, None)
@@ -482,13 +493,19 @@ def run_steps(ts: TrainingState, K: int, trace: bool = False):
     Identical bits to K calls of run_minibatch."""
     if K < 1:
         raise ConfigError("K must be >= 1")
-    if ts.rebuild_pending or globals()["allreduce"] is not _DEVICE_ALLREDUCE:
-        first = [run_minibatch(ts)]
-        tr = [ts.executors[0].model.values.tolist()] if trace else None
-        if K == 1:
-            return np.array(first), (np.array(tr) if trace else None)
-        rest, rtr = run_steps(ts, K - 1, trace)
-        return np.concatenate([np.array(first), rest]), (np.concatenate([np.array(tr), rtr]) if trace else None)
+    if ts.rebuild_pending or globals()["allreduce"] is not _DEVICE_ALLREDUCE or not _fused_fits(ts.cfg):
+        # one mini-batch at a time: the d0 rebuild after step 0, a spied seam,
+        # or a job too large for the fused launch (run_minibatch goes unfused)
+        out, tr = [run_minibatch(ts)], ([ts.executors[0].model.values.tolist()] if trace else None)
+        while len(out) < K and (ts.rebuild_pending or globals()["allreduce"] is not _DEVICE_ALLREDUCE
+                                or not _fused_fits(ts.cfg)):
+            out.append(run_minibatch(ts))
+            if trace:
+                tr.append(ts.executors[0].model.values.tolist())
+        if len(out) == K:
+            return np.array(out), (np.array(tr) if trace else None)
+        rest, rtr = run_steps(ts, K - len(out), trace)
+        return np.concatenate([np.array(out), rest]), (np.concatenate([np.array(tr), rtr]) if trace else None)
     cfg = ts.cfg
     E = cfg.max_workers
     gs = ts.global_step

@@ -347,8 +347,72 @@ def gen_global_batch():
                                                         "dataset_size": 64, "executors": 2}})
 
 
+def gen_ladder():
+    """The S1-S5 reproducibility ladder (scenarios.py:118-169) as the reference's
+    own scenario tests configure it (test_scenarios.py:16-29): per mode, each
+    level's two runs (per-step losses + param hashes) and the bitdiff verdict;
+    plus the staged kind-change run and seeded random restart schedules."""
+    from bittrain.runlog import bitdiff
+
+    kinds = {"gpu_a": 2, "gpu_b": 3}
+    steps = 16
+
+    def cfg_for(mode):
+        return engine.TrainRunConfig(seed=11, max_workers=4, micro_batch=4, dataset_size=64,
+                                     determinism=engine.DeterminismMode.from_label(mode), device_fanins=kinds)
+
+    def spec_doc(sp):
+        return {"layout": [e.device_kind for e in sp.layout],
+                "restarts": [[r.after_step, [e.device_kind for e in r.layout]] for r in sp.restarts]}
+
+    def run_pair(c, sp_a, sp_b):
+        la, ta = scenarios.run_training(c, sp_a, steps)
+        lb, tb = scenarios.run_training(c, sp_b, steps)
+        d = bitdiff(la, lb)
+        return {"run_a": spec_doc(sp_a), "run_b": spec_doc(sp_b),
+                "hash_a": [r.param_hash for r in la.records], "hash_b": [r.param_hash for r in lb.records],
+                "losses_b": [fhl(r.losses) for r in lb.records],
+                "final_equal": ta.executors[0].model.values == tb.executors[0].model.values,
+                "divergence": None if d is None else {"step": d.step, "field": d.field, "worker": d.worker}}
+
+    c0 = cfg_for("d1")
+    doc = {"steps": steps, "kinds": kinds,
+           "config": {"seed": 11, "max_workers": 4, "micro_batch": 4, "dataset_size": 64, "lr": fh(c0.lr),
+                      "momentum": fh(c0.momentum), "dropout_rate": fh(c0.dropout_rate), "jitter": fh(c0.jitter),
+                      "bucket_capacity": c0.bucket_capacity},
+           "matrix": {}}
+    for mode in ("d0", "d1", "d1d2"):
+        c = cfg_for(mode)
+        levels = []
+        for sc in scenarios.default_matrix("gpu_a", "gpu_b", steps):
+            levels.append({"level": sc.level, **run_pair(c, sc.run_a, sc.run_b)})
+        rep = scenarios.run_matrix(c, scenarios.default_matrix("gpu_a", "gpu_b", steps), steps)
+        assert [r.bitwise_equal for r in rep.results] == [lv["divergence"] is None and lv["final_equal"]
+                                                          for lv in levels]
+        doc["matrix"][mode] = {"levels": levels, "guaranteed": sorted(scenarios.guaranteed_levels(mode)),
+                               "failed_guarantees": rep.failed_guarantees()}
+    # test_scenarios.py:89-112: homogeneous shrink then a kind change
+    ref4 = spec(["gpu_a"] * 4)
+    staged = spec(["gpu_a"] * 4, [(6, ["gpu_a"] * 2), (11, ["gpu_a", "gpu_b"])])
+    doc["staged"] = {m: run_pair(cfg_for(m), ref4, staged) for m in ("d1", "d1d2")}
+    # test_scenarios.py:131-159: seeded random layouts and restart schedules
+    rng = random.Random(2718)
+    rand = []
+    for mode, ks in (("d1", ["gpu_a"]), ("d1d2", ["gpu_a", "gpu_b"])):
+        for _ in range(3):
+            lay = [rng.choice(ks) for _ in range(rng.randint(1, 4))]
+            rs = [(s, [rng.choice(ks) for _ in range(rng.randint(1, 4))])
+                  for s in sorted(rng.sample(range(2, steps - 1), rng.randint(0, 2)))]
+            rand.append({"mode": mode, **run_pair(cfg_for(mode), spec([ks[0]] * 4), spec(lay, rs))})
+    doc["random"] = rand
+    dump("ladder.json", doc)
+
+
 if __name__ == "__main__":
     assert os.path.isdir(REF_SRC), "needs the read-only reference at /root/reference"
+    if sys.argv[1:] == ["ladder"]:
+        gen_ladder()
+        sys.exit(0)
     gen_prng()
     gen_reduction()
     gen_model()
@@ -357,3 +421,4 @@ if __name__ == "__main__":
     gen_runs()
     gen_checkpoint()
     gen_global_batch()
+    gen_ladder()

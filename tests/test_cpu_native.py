@@ -118,6 +118,19 @@ def test_native_host_helpers_golden():
     assert out == 0xE220A8397B1DCDAF
 
 
+def test_fused_launch_planning():
+    """Which jobs take the one-launch fused step vs the per-seam kernels (host-only query)."""
+    from types import SimpleNamespace
+
+    from paper_2208_14228_b200.engine import _fused_fits
+
+    def fits(E, B):
+        return _fused_fits(SimpleNamespace(max_workers=E, micro_batch=B))
+
+    assert fits(8, 4) and fits(64, 4) and fits(96, 2) and fits(2, 33)
+    assert not fits(300, 4) and not fits(257, 1)
+
+
 def test_rotation_table_matches_oracle(oracle):
     import paper_2208_14228_b200 as bt
     from paper_2208_14228_b200.buckets import rotation_table

@@ -146,6 +146,34 @@ def test_full_runs_bit_exact(oracle, name):
     assert [format(int(x), "016x") for x in st["rng"]] == r["final_dropout_rng"]
 
 
+def _ladder_hashes(oracle, doc, mode, sp):
+    c = doc["config"]
+    run = oracle.Run(seed=c["seed"], max_workers=c["max_workers"], micro_batch=c["micro_batch"],
+                     dataset_size=c["dataset_size"], lr=hf(c["lr"]), momentum=hf(c["momentum"]),
+                     dropout_rate=hf(c["dropout_rate"]), jitter=hf(c["jitter"]),
+                     bucket_capacity=c["bucket_capacity"], mode=mode, devices=doc["kinds"],
+                     layout=tuple(sp["layout"]))
+    restarts = {s: lay for s, lay in sp["restarts"]}
+    hashes, losses = [], []
+    for step in range(doc["steps"]):
+        losses.append(fhl(run.step()))
+        hashes.append(format(oracle.fnv1a64(run.state()["params"].astype("<f8").tobytes()), "016x"))
+        if step + 1 in restarts:
+            run.relayout(tuple(restarts[step + 1]))
+    return hashes, losses
+
+
+def test_ladder_runs_bit_exact(oracle):
+    """Every run of the reference's S1-S5 ladder, staged and random schedules (ladder.json)."""
+    doc = load("ladder.json")
+    pairs = [(m, lv) for m, v in doc["matrix"].items() for lv in v["levels"]]
+    pairs += list(doc["staged"].items()) + [(r["mode"], r) for r in doc["random"]]
+    for mode, p in pairs:
+        assert _ladder_hashes(oracle, doc, mode, p["run_a"])[0] == p["hash_a"]
+        hb, lb = _ladder_hashes(oracle, doc, mode, p["run_b"])
+        assert hb == p["hash_b"] and lb == p["losses_b"]
+
+
 def test_oracle_threads_do_not_change_bits(oracle):
     r = next(x for x in load("runs.json")["runs"] if x["name"] == "c2_d1")
     run = _run_from_doc(oracle, r)

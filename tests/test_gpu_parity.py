@@ -181,6 +181,8 @@ SHAPES = [  # (E, B, mode, layout kinds, dataset) -> exercises 1 CTA, multi-CTA 
     (5, 7, "d0", ("gpu_mid",), 400),
     (32, 16, "d1", ("gpu_mid",) * 2, 4096),
     (2, 33, "d1", ("gpu_fast",), 700),
+    (96, 2, "d1d2", ("gpu_mid", "gpu_fast"), 1000),  # slots too big for a cluster: grid-barrier launch
+    (300, 4, "d1", ("gpu_fast",) * 3, 2400),  # slots too big for chip: grads kernel + reducer + sgd
 ]
 
 

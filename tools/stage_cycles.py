@@ -11,7 +11,9 @@ from paper_2208_14228_b200 import _native, engine  # noqa: E402
 from paper_2208_14228_b200.device import stream  # noqa: E402
 
 SHAPES = [tuple(int(v) for v in a.split(',')) for a in sys.argv[1:]] or [(8, 4, 32), (8, 4, 32), (16, 8, 32), (64, 4, 32)]
-for E, B, K in SHAPES:
+for shape in SHAPES:
+    E, B, K = shape[:3]
+    EPC = shape[3] if len(shape) > 3 else None
     cfg = bt.TrainRunConfig(seed=42, max_workers=E, micro_batch=B, dataset_size=max(1024, E * B * 32), lr=0.02,
                             momentum=0.9, dropout_rate=0.5, jitter=0.1, bucket_capacity=64,
                             determinism=bt.DeterminismMode.from_label("d1"), device_fanins={"gpu_fast": 2})
@@ -22,6 +24,8 @@ for E, B, K in SHAPES:
         ts.pipeline.advance_all(ts.global_step + st)
     losses = torch.empty((K, E), dtype=torch.float64, device="cuda")
     a, keep = engine._step_args(ts, K, B, None, losses, None)
+    if EPC:
+        a.est_per_cta = EPC
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     _native.check(_native.lib().bt_mlp_step_profiled(C.byref(a), timing.data_ptr(), stream()))
