@@ -41,7 +41,7 @@ class MlpArgs(C.Structure):
 
     _fields_ = [
         ("E", _i32), ("est_base", _i32), ("E_total", _i32), ("B", _i32), ("X", _i32), ("K", _i32),
-        ("fuse_reduce", _i32), ("est_per_cta", _i32), ("comm_fanin", _i32), ("pad0", _i32),
+        ("fuse_reduce", _i32), ("est_per_cta", _i32), ("comm_fanin", _i32), ("est_fanin_uniform", _i32),
         ("rank_override", _i64), ("rate", _dbl), ("lr", _dbl), ("mu", _dbl), ("jitter", _dbl),
         ("replicas", _vp), ("est_fanin", _vp), ("rng", _vp), ("stat_mean", _vp), ("stat_count", _vp),
         ("grads", _vp), ("losses", _vp), ("rot", _vp), ("rows", _vp), ("dataset", _vp), ("lists", _vp),

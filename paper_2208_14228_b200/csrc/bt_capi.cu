@@ -201,6 +201,8 @@ static int validate_mlp(const bt_mlp_args* a) {
                 a->E_total);
   if (!a->fuse_reduce && a->K != 1) return fail(bt::ERR_INPUT, "grads-only mode runs one mini-batch");
   if (a->comm_fanin < 0 || a->comm_fanin == 1) return fail(bt::ERR_CONFIG, "bad allreduce fanin %d", a->comm_fanin);
+  if (a->est_fanin_uniform < 0 || a->est_fanin_uniform == 2)
+    return fail(bt::ERR_CONFIG, "bad est_fanin_uniform %d", a->est_fanin_uniform);
   if (!a->rows && (!a->dataset || !a->lists || a->spe < 1))
     return fail(bt::ERR_INPUT, "need either explicit rows or dataset+lists+spe");
   if (!a->replicas || !a->est_fanin || !a->rng || !a->stat_mean || !a->stat_count || !a->grads || !a->losses ||

@@ -5,7 +5,7 @@
 //      sampling.py:160-172, or an explicit split_by_rank global batch,
 //      engine.py:261-268) -> hidden layer + tanh + dropout (model.py:141-163);
 //   C  output error, upstream factor gy, dz, tracked-stat row means
-//      (model.py:165-179, 194);
+//      (model.py:165-179, 194) -- fused into B: a row's 16 lanes sit in one warp;
 //   E  161 per-EST gradients, each a batch-dim reduce_sum in the EST's
 //      executor variant (model.py:183-192) -> EST gradient slot; per-EST loss,
 //      TrackedStat update and dropout-RNG advance (model.py:173, 99-104);
@@ -15,11 +15,14 @@
 // Layout: CTA c owns ESTs [c*epc, (c+1)*epc).  Everything a step touches is
 // staged in shared memory for the whole launch (parameters, velocity, EST
 // RNG/stat slots, the rotation table, the EST gradient slots, and -- when they
-// fit -- the dataset and this launch's index lists), so a step costs its
-// dependent fp64 chain plus four CTA barriers.  With several CTAs, stage F is
-// computed by EVERY CTA redundantly (bit-identical: same inputs, same order)
-// after one grid barrier; global gradient slots are double-buffered by step
-// parity so a fast CTA's step s+1 writes never race a slow CTA's step s reads.
+// fit -- the dataset and this launch's index lists).
+// Exchange: on a thread-block cluster every CTA pushes its EST slots into
+// every CTA's step-parity slot array with st.async (DSMEM store + mbarrier
+// complete_tx); a CTA waits on its own mbarrier for all E_total*P*8 bytes, so
+// there is no cluster-wide barrier and no release fence per step.  Stage F is
+// computed by EVERY CTA redundantly (bit-identical: same inputs, same order).
+// Parameters/velocity are double-buffered so a step commits with one CTA
+// barrier (and only when every synchronized gradient is finite).
 // Every binary64 op is an explicit _rn intrinsic (no FMA contraction) and tanh
 // is glibc's (bt_libm.cuh): results are bit-identical to the reference.
 #include "bt_common.cuh"
@@ -64,21 +67,25 @@ __device__ __forceinline__ bool grid_sync(uint32_t* bar, uint32_t target, int32_
   return s_ok != 0;
 }
 
-// reduce_sum over the B rows of one EST in its executor's variant.  With a
-// compile-time B the common fanins get a fully unrolled register tree.
-template <int BT, class Gen>
+// reduce_sum over the B rows of one EST in its executor's variant.  FB >= 0:
+// every EST's variant is known at compile time; otherwise `fan` (run time).
+template <int BT, int FB, class Gen>
 __device__ __forceinline__ double fold_rows(int nb, int fan, Gen gen) {
   if constexpr (BT > 0) {
     double v[BT];
 #pragma unroll
     for (int r = 0; r < BT; ++r) v[r] = gen(r);
-    if (fan == 0 || fan >= BT) return TreeLevel<BT, 0>::run(v);  // Tree(f >= n) folds like Sequential
-    if (fan == 2) return TreeLevel<BT, 2>::run(v);
-    StreamFold<double, FOLD_LEVELS> f;
-    f.init(fan);
+    if constexpr (FB >= 0) {
+      return TreeLevel<BT, FB>::run(v);
+    } else {
+      if (fan == 0 || fan >= BT) return TreeLevel<BT, 0>::run(v);  // Tree(f >= n) folds like Sequential
+      if (fan == 2) return TreeLevel<BT, 2>::run(v);
+      StreamFold<double, FOLD_LEVELS> f;
+      f.init(fan);
 #pragma unroll
-    for (int r = 0; r < BT; ++r) f.push(v[r]);
-    return f.finish();
+      for (int r = 0; r < BT; ++r) f.push(v[r]);
+      return f.finish();
+    }
   } else {
     StreamFold<double, FOLD_LEVELS> f;
     f.init(fan);
@@ -88,10 +95,10 @@ __device__ __forceinline__ double fold_rows(int nb, int fan, Gen gen) {
 }
 
 // The allreduce fold of one parameter over N EST slots (slot of leaf k is
-// (start+k) mod N), register-resident with a compile-time tree shape.
-// `ld(q)` returns EST slot q's value (local shared memory or a cluster peer's).
-template <int N, class Ld>
-__device__ __forceinline__ double fold_ranks_n(int fan, int start, Ld ld) {
+// (start+k) mod N), register-resident with a compile-time tree shape F.
+// `ld(q)` returns EST slot q's value.
+template <int N, int F, class Ld>
+__device__ __forceinline__ double fold_ranks_t(int start, Ld ld) {
   double v[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) {
@@ -99,12 +106,16 @@ __device__ __forceinline__ double fold_ranks_n(int fan, int start, Ld ld) {
     q -= q >= N ? N : 0;
     v[k] = ld(q);
   }
-  return fan == 0 ? TreeLevel<N, 0>::run(v) : TreeLevel<N, 2>::run(v);  // caller: fan in {0, 2}
+  return TreeLevel<N, F>::run(v);
+}
+
+template <int N, class Ld>
+__device__ __forceinline__ double fold_ranks_n(int fan, int start, Ld ld) {  // fan in {0, 2}
+  return fan == 0 ? fold_ranks_t<N, 0>(start, ld) : fold_ranks_t<N, 2>(start, ld);
 }
 
 // Register tree for the common shapes (power-of-two E, Sequential / Tree(2));
-// everything else takes the (compact) register StreamFold.  Few variants keep
-// the persistent kernel's loop small enough for the instruction cache.
+// everything else takes the (compact) register StreamFold.
 template <class Ld>
 __device__ __forceinline__ bool fold_ranks_ct(int n, int fan, int start, Ld ld, double* out) {
   if (!(fan == 0 || fan == 2)) return false;
@@ -139,22 +150,46 @@ struct MlpLaunch {  // launcher-computed shared-memory plan
   int stage_data;   // dataset copied into shared memory
   int stage_idx;    // this launch's index lists copied into shared memory
   int grads_smem;   // EST gradient slots [E_total][P] in shared memory (fused, non-cluster mode)
-  int cluster;      // fused mode on a thread-block cluster: slots exchanged through DSMEM
-  unsigned long long* timing;  // optional [8] per-stage clock64 sums (bt_mlp_step_profiled)
+  int cluster;      // fused mode on a thread-block cluster: slots pushed through DSMEM
+  unsigned long long* timing;  // optional [9] per-stage clock64 sums (bt_mlp_step_profiled)
 };
 
+// ---- cluster plumbing (PTX) -------------------------------------------------
 __device__ __forceinline__ void cluster_barrier() {  // all threads of all CTAs; release/acquire
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// shared::cluster window address of `p` (this CTA's shared memory) in CTA `rank`
-__device__ __forceinline__ uint32_t cluster_map32(const double* p, int rank) {
-  const uint32_t local = (uint32_t)__cvta_generic_to_shared(p);
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// shared::cluster window address of this CTA's shared address `local` in CTA `rank`
+__device__ __forceinline__ uint32_t cluster_map32(uint32_t local, int rank) {
   uint32_t out;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(local), "r"(rank));
   return out;
 }
-__device__ __forceinline__ void st_dsmem(uint32_t addr, double v) {  // DSMEM store (fire and forget)
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {  // make mbarrier.init visible to cluster peers
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// DSMEM store into a cluster peer that also counts 8 bytes on the peer's mbarrier
+__device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(addr), "d"(v),
+               "r"(remote_bar)
+               : "memory");
 }
 
 // Per-stage cycle accounting for profiling builds of a launch (thread 0's view
@@ -166,11 +201,17 @@ __device__ __forceinline__ void st_dsmem(uint32_t addr, double v) {  // DSMEM st
     tlast = now_;                                      \
   }
 
-template <int BT>
+// BT: compile-time rows per EST (0 = run time).  ET > 0 selects a specialised
+// build for E_total == ET with every EST's batch variant FB and the allreduce
+// variant FC known at compile time, staged dataset/index lists, and the
+// cluster (or single-CTA) exchange -- the launcher only picks it then.  The
+// generic build (ET = 0, FB = FC = -1) handles every other job.
+template <int BT, int ET, int FB, int FC>
 __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_constant__ bt_mlp_args a,
                                                                const MlpLaunch L) {
+  constexpr bool SPEC = ET > 0;
   extern __shared__ __align__(16) double sm[];
-  const int tid = threadIdx.x, T = blockDim.x;
+  const int tid = threadIdx.x, T = blockDim.x;  // T >= BT_P (launcher): thread p owns parameter p in stage F
   const int cta = blockIdx.x, G = gridDim.x;
   const int nb = BT > 0 ? BT : a.B;
   const int epc = a.est_per_cta;
@@ -178,12 +219,14 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
   const int ne = min(epc, a.E - e0);
   const int nrows = ne * nb;
   const int rows_cap = epc * nb;
-  const int Et = a.E_total;
+  const int Et = SPEC ? ET : a.E_total;
+  const bool staged = SPEC || (L.stage_idx && L.stage_data);
 
-  double* s_par = sm;
+  double* s_par = sm;                            // current parameters / velocity ...
   double* s_vel = s_par + PAD_P;
-  double* s_g = s_vel + PAD_P;
-  double* s_x = s_g + PAD_P;                     // [rows][8] jittered inputs
+  double* s_par_n = s_vel + PAD_P;               // ... and the next step's (double buffer)
+  double* s_vel_n = s_par_n + PAD_P;
+  double* s_x = s_vel_n + PAD_P;                 // [rows][8] jittered inputs
   double* s_y = s_x + rows_cap * BT_INPUT_DIM;   // [rows]
   double* s_act = s_y + rows_cap;                // [rows][16] tanh outputs
   double* s_msk = s_act + rows_cap * BT_HIDDEN;  // [rows][16] dropout masks
@@ -195,17 +238,29 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
   double* s_mean = s_rm + rows_cap;              // [epc]
   uint64_t* s_rng = (uint64_t*)(s_mean + epc);   // [epc]
   uint64_t* s_cnt = s_rng + epc;                 // [epc]
-  double* s_grad = (double*)(s_cnt + epc);  // [E_total][P] when L.grads_smem; [2][epc][P] when L.cluster
+  double* s_grad = (double*)(s_cnt + epc);  // [E_total][P] when L.grads_smem; [2][E_total][P] when L.cluster
   double* s_data = s_grad + (L.cluster ? (size_t)2 * Et * BT_P : (L.grads_smem ? (size_t)Et * BT_P : 0));
   double* s_jit = s_data + (L.stage_data ? (size_t)a.dataset_rows * BT_ROW : 0);  // [K][epc][B] when L.stage_idx
   int32_t* s_rot = (int32_t*)(s_jit + (L.stage_idx ? (size_t)a.K * rows_cap : 0));  // [P]
   int32_t* s_fan = s_rot + PAD_P;                // [epc] batch-reduction fanin per local EST
   int32_t* s_idx = s_fan + ((epc + 1) & ~1);     // [K][epc][B] when L.stage_idx
 
-  __shared__ uint32_t s_peer[MAX_CLUSTER_CTAS];  // cluster mode: CTA r's slot array (shared::cluster)
+  __shared__ uint32_t s_peer[MAX_CLUSTER_CTAS];     // cluster: CTA r's slot array (shared::cluster)
+  __shared__ uint32_t s_peerbar[MAX_CLUSTER_CTAS];  // cluster: CTA r's mbarrier pair
+  __shared__ __align__(8) uint64_t s_mbar[2];       // cluster: "all slots of step parity q arrived"
 
-  if (a.flags[FLAG_STATUS] != 0) return;  // sticky error from an earlier launch
-  for (int r = tid; r < G && L.cluster; r += T) s_peer[r] = cluster_map32(s_grad, r);
+  if (a.flags[FLAG_STATUS] != 0) return;  // sticky error from an earlier launch (same for every CTA)
+  if (L.cluster) {
+    if (tid == 0) {
+      mbar_init(smem_u32(&s_mbar[0]), 1);
+      mbar_init(smem_u32(&s_mbar[1]), 1);
+      mbar_init_fence();
+    }
+    for (int r = tid; r < G; r += T) {
+      s_peer[r] = cluster_map32(smem_u32(s_grad), r);
+      s_peerbar[r] = cluster_map32(smem_u32(&s_mbar[0]), r);
+    }
+  }
 
   // ---- launch prologue: stage state in shared memory -----------------------
   const double* rep0 = a.replicas;
@@ -222,11 +277,13 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
       if (a.fuse_reduce) bad |= d2u(rx[BT_P + i]) != d2u(v0);
     }
   }
+  int hint_bad = 0;
   for (int el = tid; el < ne; el += T) {
     s_rng[el] = a.rng[e0 + el];
     s_mean[el] = a.stat_mean[e0 + el];
     s_cnt[el] = a.stat_count[e0 + el];
     s_fan[el] = a.est_fanin[e0 + el];
+    if (SPEC) hint_bad |= s_fan[el] != FB;
   }
   if (L.stage_data) {
     const int64_t nd = a.dataset_rows * BT_ROW;
@@ -249,13 +306,16 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
       s_jit[q] = ju;
     }
   }
-  if (__syncthreads_or(bad)) {
+  // every CTA reads the same replicas / fanins, so all CTAs take the same exit
+  const int prologue = __syncthreads_or(bad | (hint_bad << 1));
+  if (prologue) {
     if (cta == 0 && tid == 0) {
-      a.flags[FLAG_STATUS] = ERR_CORRUPTION;
+      a.flags[FLAG_STATUS] = (prologue & 1) ? ERR_CORRUPTION : ERR_INPUT;
       a.flags[FLAG_STEP] = 0;
     }
     return;
   }
+  if (L.cluster) cluster_barrier();  // every peer's mbarriers are initialised before the first push
 
   const double rate = a.rate;
   const double keep = rate >= 1.0 ? 0.0 : ddiv(1.0, dsub(1.0, rate));  // model.py:150
@@ -263,6 +323,8 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
   const IntDivisor divB = IntDivisor::of(nb), divH = IntDivisor::of(BT_HIDDEN), divE = IntDivisor::of(Et);
   const double* data = L.stage_data ? s_data : a.dataset;
   const bool jit = !a.rows && a.jitter != 0.0;
+  const uint32_t slot_bytes = (uint32_t)Et * BT_P * (uint32_t)sizeof(double);  // one step's arrivals per CTA
+  uint32_t phases = 0;  // cluster: bit q = parity of the next completion of s_mbar[q]
   int s = 0;
   int64_t epoch = a.rows ? 0 : a.step0 / a.spe, local = a.rows ? 0 : a.step0 % a.spe;
 
@@ -270,110 +332,106 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
   long long tlast = clock64();
   for (; s < a.K; ++s) {
     const int64_t gstep = a.step0 + s;
+    const int par = (int)(gstep & 1);
     if (s > 0 && !a.rows && ++local == a.spe) {  // incremental (no 64-bit division per step)
       local = 0;
       ++epoch;
     }
 
-    // ---- B: rows + hidden pre-activation, tanh, dropout ------------------
-#pragma unroll 1
-    for (int it = tid; it < nrows * BT_HIDDEN; it += T) {
-      const int row = it >> 4, j = it & 15;
-      const int el = row / nb, r = row - el * nb;
-      const int eg = a.est_base + e0 + el;  // global virtual rank
-      double x[BT_ROW];  // 8 inputs, then y
-      double ju = 0.0;
-      if (L.stage_idx && L.stage_data) {  // the common path: shared-memory rows (LDS), staged index + jitter
-        const int q = (s * epc + el) * nb + r;
-        const double* srcs = s_data + (size_t)s_idx[q] * BT_ROW;
-        ju = s_jit[q];
-#pragma unroll
-        for (int i = 0; i < BT_ROW; ++i) x[i] = srcs[i];
-      } else {
-        const double* src;
-        if (a.rows) {  // split_by_rank: row r of rank k is global row r*E+k
-          src = a.rows + ((size_t)s * nb * Et + (size_t)r * Et + eg) * BT_ROW;
-        } else if (L.stage_idx) {
-          const int q = (s * epc + el) * nb + r;
-          src = data + (size_t)s_idx[q] * BT_ROW;
-          ju = s_jit[q];
-        } else {
-          const int32_t* lst = a.lists + ((size_t)(epoch - a.epoch_base) * Et + eg) * (size_t)(a.spe * nb);
-          src = data + (size_t)lst[local * nb + r] * BT_ROW;
-          if (jit) {  // one uniform per row (sampling.py:168-170)
-            const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)epoch, (uint64_t)local, (uint64_t)eg);
-            ju = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), a.jitter);
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < BT_ROW; ++i) x[i] = src[i];
-      }
-      const long long tb0 = L.timing ? clock64() : 0;
-#pragma unroll
-      for (int i = 0; i < BT_INPUT_DIM; ++i) x[i] = jit ? dadd(x[i], ju) : x[i];
-      {  // lane j < 8 keeps input j, lane 8 keeps y: a select chain, no divergent stores
-        double keepv = x[0];
-#pragma unroll
-        for (int i = 1; i < BT_ROW; ++i) keepv = j == i ? x[i] : keepv;
-        if (j < BT_INPUT_DIM) s_x[row * BT_INPUT_DIM + j] = keepv;
-        else if (j == BT_INPUT_DIM) s_y[row] = keepv;
-      }
-      double acc = dmul(s_par[BT_W1 + j], x[0]);
-#pragma unroll
-      for (int i = 1; i < BT_INPUT_DIM; ++i) acc = dadd(acc, dmul(s_par[BT_W1 + i * BT_HIDDEN + j], x[i]));
-      const double pre = dadd(acc, s_par[BT_B1 + j]);
-      long long tb1 = 0;
-      if (L.timing && tid == 0) {  // profiling: keep `pre` live before the clock read
-        asm volatile("" ::"d"(pre));
-        tb1 = clock64();
-      }
-      const double act = glibc_tanh_simt(pre);
-      if (L.timing && tid == 0) {
-        asm volatile("" ::"d"(act));
-        const long long tb2 = clock64();
-        tacc[6] += (unsigned long long)(tb1 - tb0);
-        tacc[7] += (unsigned long long)(tb2 - tb1);
-        tacc[8] += (unsigned long long)(tb0 - tlast);
-      }
-      double m = 1.0;
-      if (rate > 0.0) {  // draw n = r*16+j of this EST's stream (rows outer, units inner)
-        const double ud = unit_float(draw_raw(s_rng[el], (uint64_t)(r * BT_HIDDEN + j)));
-        m = ud < rate ? 0.0 : keep;
-      }
-      s_act[it] = act;
-      s_msk[it] = m;
-      s_hid[it] = dmul(act, m);
-    }
-    __syncthreads();
-    BT_TICK(0)
-
-    // ---- C: per row, a 16-lane group (lane j = hidden unit j) ------------
-    // Every lane of the group gathers the 16 products w2[j]*h[j] and the 16
-    // activations by shuffle and runs the two sequential 16-term folds (output
-    // and row mean, model.py:168-171, 194) -- identical bits on every lane, no
-    // divergence -- then lane j writes its own dz[r][j] = ((gy*w2[j])*mask)*(1-a*a)
-    // (model.py:179).
+    // ---- B+C: one 16-lane group per row (lane j = hidden unit j) ----------
+    // B: row gather + jitter, pre-activation, tanh, dropout (model.py:141-163).
+    // C: every lane of the group reads the row's 16 products w2[j]*h[j] and 16
+    // activations (shared-memory broadcast) and runs the two sequential
+    // 16-term folds (output and row mean, model.py:168-171, 194) -- identical
+    // bits on every lane -- then lane j writes dz[r][j] = ((gy*w2[j])*mask)*(1-a*a)
+    // (model.py:179).  A row's lanes share a warp, so B -> C is a __syncwarp.
     {
       const int span = ((nrows * BT_HIDDEN + 31) / 32) * 32;
 #pragma unroll 1
       for (int it = tid; it < span; it += T) {
         const bool valid = it < nrows * BT_HIDDEN;
         const int row = valid ? it >> 4 : 0, j = it & 15;
-        // all 16 lanes of the group read the same addresses: shared-memory broadcast
+        const int el = row / nb, r = row - el * nb;
+        const int eg = a.est_base + e0 + el;  // global virtual rank
+        double x[BT_ROW];  // 8 inputs, then y
+        double ju = 0.0;
+        if (staged) {  // the common path: shared-memory rows (LDS), staged index + jitter
+          const int q = (s * epc + el) * nb + r;
+          const double* srcs = s_data + (size_t)s_idx[q] * BT_ROW;
+          ju = s_jit[q];
+#pragma unroll
+          for (int i = 0; i < BT_ROW; ++i) x[i] = srcs[i];
+        } else {
+          const double* src;
+          if (a.rows) {  // split_by_rank: row r of rank k is global row r*E+k
+            src = a.rows + ((size_t)s * nb * Et + (size_t)r * Et + eg) * BT_ROW;
+          } else if (L.stage_idx) {
+            const int q = (s * epc + el) * nb + r;
+            src = data + (size_t)s_idx[q] * BT_ROW;
+            ju = s_jit[q];
+          } else {
+            const int32_t* lst = a.lists + ((size_t)(epoch - a.epoch_base) * Et + eg) * (size_t)(a.spe * nb);
+            src = data + (size_t)lst[local * nb + r] * BT_ROW;
+            if (jit) {  // one uniform per row (sampling.py:168-170)
+              const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)epoch, (uint64_t)local, (uint64_t)eg);
+              ju = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), a.jitter);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < BT_ROW; ++i) x[i] = src[i];
+        }
+        const long long tb0 = L.timing ? clock64() : 0;
+#pragma unroll
+        for (int i = 0; i < BT_INPUT_DIM; ++i) x[i] = jit ? dadd(x[i], ju) : x[i];
+        {  // lane j < 8 keeps input j, lane 8 keeps y: a select chain, no divergent stores
+          double keepv = x[0];
+#pragma unroll
+          for (int i = 1; i < BT_ROW; ++i) keepv = j == i ? x[i] : keepv;
+          if (valid && j < BT_INPUT_DIM) s_x[row * BT_INPUT_DIM + j] = keepv;
+          else if (valid && j == BT_INPUT_DIM) s_y[row] = keepv;
+        }
+        double acc = dmul(s_par[BT_W1 + j], x[0]);
+#pragma unroll
+        for (int i = 1; i < BT_INPUT_DIM; ++i) acc = dadd(acc, dmul(s_par[BT_W1 + i * BT_HIDDEN + j], x[i]));
+        const double pre = dadd(acc, s_par[BT_B1 + j]);
+        long long tb1 = 0;
+        if (L.timing && tid == 0) {  // profiling: keep `pre` live before the clock read
+          asm volatile("" ::"d"(pre));
+          tb1 = clock64();
+        }
+        const double act = glibc_tanh_simt(pre);
+        if (L.timing && tid == 0) {
+          asm volatile("" ::"d"(act));
+          const long long tb2 = clock64();
+          tacc[6] += (unsigned long long)(tb1 - tb0);
+          tacc[7] += (unsigned long long)(tb2 - tb1);
+          tacc[8] += (unsigned long long)(tb0 - tlast);
+        }
+        double m = 1.0;
+        if (rate > 0.0) {  // draw n = r*16+j of this EST's stream (rows outer, units inner)
+          const double ud = unit_float(draw_raw(s_rng[el], (uint64_t)(r * BT_HIDDEN + j)));
+          m = ud < rate ? 0.0 : keep;
+        }
+        const double hj = dmul(act, m);
+        if (valid) {
+          s_act[it] = act;
+          s_hid[it] = hj;
+        }
+        __syncwarp();
+        // C (lanes of invalid rows recompute row 0 and store nothing)
         const double* h = s_hid + row * BT_HIDDEN;
         const double* ar = s_act + row * BT_HIDDEN;
-        const double actj = ar[j];
-        double acc = dmul(s_par[BT_W2], h[0]);
+        double acc2 = dmul(s_par[BT_W2], h[0]);
         double msum = ar[0];
 #pragma unroll
         for (int q = 1; q < BT_HIDDEN; ++q) {
-          acc = dadd(acc, dmul(s_par[BT_W2 + q], h[q]));
+          acc2 = dadd(acc2, dmul(s_par[BT_W2 + q], h[q]));
           msum = dadd(msum, ar[q]);
         }
         if (valid) {
-          const double err = dsub(dadd(acc, s_par[BT_B2]), s_y[row]);
+          const double err = dsub(dadd(acc2, s_par[BT_B2]), s_y[row]);
           const double gy = divB.apply(dmul(2.0, err));
-          s_dz[it] = dmul(dmul(dmul(gy, s_par[BT_W2 + j]), s_msk[it]), dsub(1.0, dmul(actj, actj)));
+          s_dz[it] = dmul(dmul(dmul(gy, s_par[BT_W2 + j]), m), dsub(1.0, dmul(act, act)));
           if (j == 0) {
             s_e2[row] = dmul(err, err);
             s_gy[row] = gy;
@@ -383,7 +441,7 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
       }
     }
     __syncthreads();
-    BT_TICK(1)
+    BT_TICK(0)
 
     // ---- E: per-EST gradients -> EST slot; loss, TrackedStat, RNG ---------
     // One thread per (EST, parameter): a batch-dim reduce_sum in the EST's
@@ -391,16 +449,16 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
     // independent chains, because with a few warps per SM the step is
     // latency-bound and per-thread instruction count is the cost.  One more
     // thread per EST folds the loss and updates TrackedStat and the RNG.
-    double* gbuf = a.grads + (a.fuse_reduce ? (size_t)(gstep & 1) * (size_t)a.E * BT_P : 0);
+    double* gbuf = a.grads + (a.fuse_reduce ? (size_t)par * (size_t)a.E * BT_P : 0);
     const bool to_global = !a.fuse_reduce || G > 1;
-    const int par = (int)(gstep & 1);
+    if (L.cluster && tid == 0) mbar_arrive_expect_tx(smem_u32(&s_mbar[par]), slot_bytes);
     constexpr int ITEMS = BT_P + 1;
 #pragma unroll 1
     for (int it = tid; it < ne * ITEMS; it += T) {
       const int el = it / ITEMS, p = it - el * ITEMS;
       const int rb = el * nb;
-      const int fan = s_fan[el];
-      const double g = fold_rows<BT>(nb, fan, [&](int r) {
+      const int fan = FB >= 0 ? FB : s_fan[el];
+      const double g = fold_rows<BT, FB>(nb, fan, [&](int r) {
         const int row = rb + r;
         if (p < BT_B1) return dmul(s_dz[row * BT_HIDDEN + (p & 15)], s_x[row * BT_INPUT_DIM + (p >> 4)]);  // w1
         if (p < BT_W2) return s_dz[row * BT_HIDDEN + (p - BT_B1)];                                         // b1
@@ -409,12 +467,14 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
         return s_e2[row];                                                                                  // loss
       });
       if (p < BT_P) {
-        if (to_global && !L.cluster) gbuf[(size_t)(e0 + el) * BT_P + p] = g;
         if (L.cluster) {  // push this EST's slot into every CTA's copy of the step-parity slot array
           const uint32_t off = (uint32_t)((((size_t)par * Et + e0 + el) * BT_P + p) * sizeof(double));
-          for (int r = 0; r < G; ++r) st_dsmem(s_peer[r] + off, g);
+          for (int rk = 0; rk < G; ++rk) st_async_f64(s_peer[rk] + off, g, s_peerbar[rk] + par * 8);
+        } else if (to_global) {
+          gbuf[(size_t)(e0 + el) * BT_P + p] = g;
+        } else if (L.grads_smem) {
+          s_grad[(size_t)(e0 + el) * BT_P + p] = g;
         }
-        else if (L.grads_smem) s_grad[(size_t)(e0 + el) * BT_P + p] = g;
       } else {
         const int e = e0 + el;
         const double loss = divB.apply(g);
@@ -433,14 +493,27 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
       ++s;
       break;
     }
+    BT_TICK(1)
 
-    // ---- F: fixed-order allreduce + /E + momentum SGD --------------------
+    // ---- exchange: every EST slot of this step in local shared memory -----
     if (L.cluster) {
-      // One cluster barrier: every CTA's step-parity slots are complete and
-      // visible (release/acquire); each CTA then folds all E slots -- its own
-      // and its peers' through DSMEM -- in the same rank order, bit-identically.
-      // A CTA can be at most one step ahead, and it writes the other parity.
-      cluster_barrier();
+      // Wait for all E_total*P*8 bytes of step parity `par` (peers' st.async
+      // complete_tx; acquire).  A CTA is at most one step ahead of any peer:
+      // its step s+1 pushes need every peer's step s+1 slots, which each
+      // peer only pushes after finishing its step-s fold -- so the parity
+      // double buffer is never overwritten while being read.
+      const uint32_t bar = smem_u32(&s_mbar[par]);
+      const uint32_t want = (phases >> par) & 1u;
+      if (!mbar_try_wait(bar, want)) {
+        const long long t0 = clock64();
+        while (!mbar_try_wait(bar, want)) {
+          if (clock64() - t0 > (1ll << 34)) {  // ~9 s: a lost arrival is a bug; fail instead of hanging
+            atomicCAS(a.flags + FLAG_STATUS, 0, (int)ERR_CUDA);
+            __trap();
+          }
+        }
+      }
+      phases ^= 1u << par;
     } else {
       if (G > 1) {
         if (!grid_sync(a.bar, (uint32_t)(s + 1) * (uint32_t)G, a.flags)) break;
@@ -449,17 +522,27 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
       __syncthreads();
     }
     BT_TICK(2)
+
+    // ---- F: fixed-order allreduce + /E + momentum SGD into the next buffers
+    // Leaf k of parameter p is EST slot (rot[p] + k) mod E: ascending virtual
+    // rank, rotated by the parameter's ring chunk under Tree (buckets.py:115-123).
     int ok = 1;
-    for (int p = tid; p < BT_P; p += T) {
-      // Leaf k of parameter p is EST slot (rot[p] + k) mod E: ascending virtual
-      // rank, rotated by the parameter's ring chunk under Tree (buckets.py:115-123).
-      // every slot is local: cluster peers pushed theirs before the barrier
+    double np = 0.0;
+    const int p = tid;
+    if (p < BT_P) {
       const double* col = s_grad + (L.cluster ? (size_t)par * Et * BT_P : 0) + p;
-      const double sum = fold_ranks_any(Et, a.comm_fanin, s_rot[p], [&](int q) { return col[(size_t)q * BT_P]; });
+      auto ld = [&](int q) { return col[(size_t)q * BT_P]; };
+      double sum;
+      if constexpr (SPEC) sum = fold_ranks_t<ET, FC>(s_rot[p], ld);
+      else sum = fold_ranks_any(Et, a.comm_fanin, s_rot[p], ld);
       const double g = divE.apply(sum);
-      s_g[p] = g;
-      ok &= finite_d(g) ? 1 : 0;
+      ok = finite_d(g) ? 1 : 0;
+      const double v = dadd(dmul(a.mu, s_vel[p]), g);
+      np = dsub(s_par[p], dmul(a.lr, v));
+      s_vel_n[p] = v;
+      s_par_n[p] = np;
     }
+    BT_TICK(3)
     if (!__syncthreads_and(ok)) {  // sgd_step raises before mutating (model.py:207-209)
       if (cta == 0 && tid == 0) {
         a.flags[FLAG_STATUS] = ERR_NUMERIC;
@@ -467,15 +550,15 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
       }
       break;  // this mini-batch's EST contexts already advanced (engine.py:301-302)
     }
-    BT_TICK(3)
-    for (int p = tid; p < BT_P; p += T) {
-      const double v = dadd(dmul(a.mu, s_vel[p]), s_g[p]);
-      const double np = dsub(s_par[p], dmul(a.lr, v));
-      s_vel[p] = v;
-      s_par[p] = np;
-      if (a.param_trace && cta == 0) a.param_trace[(size_t)s * BT_P + p] = np;
+    {  // commit: the next buffers become current
+      double* t = s_par;
+      s_par = s_par_n;
+      s_par_n = t;
+      t = s_vel;
+      s_vel = s_vel_n;
+      s_vel_n = t;
     }
-    __syncthreads();
+    if (a.param_trace && cta == 0 && p < BT_P) a.param_trace[(size_t)s * BT_P + p] = np;
     BT_TICK(4)
   }
   if (L.timing && tid == 0 && cta == 0) {
@@ -485,7 +568,7 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
   }
 
   // ---- epilogue: EST slots back to HBM; mirror the update to every replica
-  if (L.cluster) cluster_barrier();  // peers may still be reading this CTA's slots
+  if (L.cluster) cluster_barrier();  // no CTA leaves while a peer may still address it
   else __syncthreads();
   for (int el = tid; el < ne; el += T) {
     a.rng[e0 + el] = s_rng[el];
@@ -508,7 +591,7 @@ static constexpr size_t SMEM_LIMIT = 220 * 1024;
 
 static size_t base_smem_bytes(const bt_mlp_args& a) {
   const size_t rows = (size_t)a.est_per_cta * a.B;
-  return sizeof(double) * (3 * PAD_P + rows * (BT_INPUT_DIM + 1 + 4 * BT_HIDDEN + 3) + 3 * (size_t)a.est_per_cta) +
+  return sizeof(double) * (4 * PAD_P + rows * (BT_INPUT_DIM + 1 + 4 * BT_HIDDEN + 3) + 3 * (size_t)a.est_per_cta) +
          sizeof(int32_t) * (PAD_P + (((size_t)a.est_per_cta + 1) & ~(size_t)1));
 }
 
@@ -551,7 +634,7 @@ static MlpLaunch plan(const bt_mlp_args& a, size_t* smem) {
   return L;
 }
 
-size_t mlp_smem_bytes(int nrows) { return sizeof(double) * (3 * PAD_P + (size_t)nrows * 76); }
+size_t mlp_smem_bytes(int nrows) { return sizeof(double) * (4 * PAD_P + (size_t)nrows * 76); }
 
 bool mlp_fused_fits(const bt_mlp_args& a) {
   if (a.E_total > BT_MAX_FUSED_E) return false;
@@ -559,12 +642,12 @@ bool mlp_fused_fits(const bt_mlp_args& a) {
   return base_smem_bytes(a) + sizeof(double) * slots * BT_P <= SMEM_LIMIT;
 }
 
-template <int BT>
-static cudaError_t launch_bt(const bt_mlp_args& a, const MlpLaunch& L, size_t smem, int grid, cudaStream_t stream) {
-  static bool attr_set = false;
+template <int BT, int ET, int FB, int FC>
+static cudaError_t launch_k(const bt_mlp_args& a, const MlpLaunch& L, size_t smem, int grid, cudaStream_t stream) {
+  auto kern = mlp_step_kernel<BT, ET, FB, FC>;
+  static bool attr_set = false;  // one per instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(mlp_step_kernel<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SMEM_LIMIT);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -585,34 +668,58 @@ static cudaError_t launch_bt(const bt_mlp_args& a, const MlpLaunch& L, size_t sm
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, mlp_step_kernel<BT>, a, L);
+    return cudaLaunchKernelEx(&cfg, kern, a, L);
   }
   if (grid > 1 && a.fuse_reduce) {
     if (cudaMemsetAsync(a.bar, 0, sizeof(uint32_t), stream) != cudaSuccess) return cudaGetLastError();
     void* params[] = {(void*)&a, (void*)&L};
-    return cudaLaunchCooperativeKernel((const void*)mlp_step_kernel<BT>, dim3(grid), dim3(MLP_THREADS), params,
-                                       smem, stream);
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(MLP_THREADS), params, smem, stream);
   }
-  mlp_step_kernel<BT><<<grid, MLP_THREADS, smem, stream>>>(a, L);
+  kern<<<grid, MLP_THREADS, smem, stream>>>(a, L);
   return cudaGetLastError();
 }
 
+// Specialised builds: B = 4 rows, E_total in {4, 8, 16}, one variant for every
+// EST and the allreduce (Sequential: d1d2 / d2, or Tree(2): the gpu_fast kind).
+template <int ET>
+static bool launch_spec(const bt_mlp_args& a, const MlpLaunch& L, size_t smem, int grid, cudaStream_t stream,
+                        int fan, cudaError_t* err) {
+  if (fan == 0) *err = launch_k<4, ET, 0, 0>(a, L, smem, grid, stream);
+  else if (fan == 2) *err = launch_k<4, ET, 2, 2>(a, L, smem, grid, stream);
+  else return false;
+  return true;
+}
+
 int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* timing) {
-  const int grid = (a.E + a.est_per_cta - 1) / a.est_per_cta;
+  const int grid = grid_of(a);
   size_t smem = 0;
   MlpLaunch L = plan(a, &smem);
   L.timing = timing;
   if (a.fuse_reduce && !L.grads_smem && !L.cluster) return ERR_INPUT;  // too many ESTs for the fused path
   if (smem > SMEM_LIMIT) return ERR_INPUT;
-  cudaError_t err;
-  switch (a.B) {
-    case 1: err = launch_bt<1>(a, L, smem, grid, stream); break;
-    case 2: err = launch_bt<2>(a, L, smem, grid, stream); break;
-    case 4: err = launch_bt<4>(a, L, smem, grid, stream); break;
-    case 8: err = launch_bt<8>(a, L, smem, grid, stream); break;
-    case 16: err = launch_bt<16>(a, L, smem, grid, stream); break;
-    case 32: err = launch_bt<32>(a, L, smem, grid, stream); break;
-    default: err = launch_bt<0>(a, L, smem, grid, stream); break;
+  cudaError_t err = cudaSuccess;
+  const int fan = a.est_fanin_uniform - 1;  // every EST's batch variant, when the caller knows it
+  const bool spec_ok = a.fuse_reduce && a.B == 4 && a.E == a.E_total && !a.rows && L.stage_idx && L.stage_data &&
+                       (L.cluster || (grid == 1 && L.grads_smem)) && fan >= 0 && fan == a.comm_fanin;
+  bool done = false;
+  if (spec_ok) {
+    switch (a.E_total) {
+      case 4: done = launch_spec<4>(a, L, smem, grid, stream, fan, &err); break;
+      case 8: done = launch_spec<8>(a, L, smem, grid, stream, fan, &err); break;
+      case 16: done = launch_spec<16>(a, L, smem, grid, stream, fan, &err); break;
+      default: break;
+    }
+  }
+  if (!done) {
+    switch (a.B) {
+      case 1: err = launch_k<1, 0, -1, -1>(a, L, smem, grid, stream); break;
+      case 2: err = launch_k<2, 0, -1, -1>(a, L, smem, grid, stream); break;
+      case 4: err = launch_k<4, 0, -1, -1>(a, L, smem, grid, stream); break;
+      case 8: err = launch_k<8, 0, -1, -1>(a, L, smem, grid, stream); break;
+      case 16: err = launch_k<16, 0, -1, -1>(a, L, smem, grid, stream); break;
+      case 32: err = launch_k<32, 0, -1, -1>(a, L, smem, grid, stream); break;
+      default: err = launch_k<0, 0, -1, -1>(a, L, smem, grid, stream); break;
+    }
   }
   return err == cudaSuccess ? OK : ERR_CUDA;
 }

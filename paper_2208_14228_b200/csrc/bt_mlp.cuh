@@ -29,7 +29,8 @@ typedef struct bt_mlp_args {
   int32_t fuse_reduce; /* 1: allreduce + sgd in-kernel (E must equal E_total); 0: grads only */
   int32_t est_per_cta; /* ESTs per CTA (grid = ceil(E / est_per_cta)) */
   int32_t comm_fanin;  /* executor 0's variant for the allreduce (engine.py:309); 0 = Sequential */
-  int32_t pad0;
+  int32_t est_fanin_uniform; /* 0: per-EST est_fanin only; f+1: every est_fanin[] is f (a hint that lets
+                                the launcher pick a specialised kernel; a wrong hint is reported as InputError) */
   int64_t rank_override; /* >= 0: TrackedStat rank of EST 0 (pure forward_backward seam) */
   double rate, lr, mu, jitter;
   /* state */

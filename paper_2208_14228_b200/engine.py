@@ -376,6 +376,8 @@ def _step_args(ts: TrainingState, K: int, B: int, rows: torch.Tensor | None, los
     a.fuse_reduce = int(fuse)
     a.est_per_cta = _native.lib().bt_mlp_pick_est_per_cta(cfg.max_workers, B)
     a.comm_fanin = fanin_code(_comm_variant(ts))
+    fans = {fanin_code(ex.kernel_profile.reduce_variant) for ex in ts.executors}
+    a.est_fanin_uniform = fans.pop() + 1 if len(fans) == 1 else 0  # lets the launcher specialise
     a.rank_override = -1
     a.rate, a.lr, a.mu, a.jitter = float(cfg.dropout_rate), float(ex0._lr), float(ex0._mu), float(cfg.jitter)
     a.replicas, a.est_fanin, a.rng = ptr(dev.replicas), ptr(dev.est_fanin), ptr(dev.rng)

@@ -1,0 +1,16 @@
+#!/bin/bash
+# Round profiling recipe (run under gpurun): bench line, reference arm, ncu launch list,
+# one `ncu --set full` capture each of the step kernel and the reducer.
+#   gpurun -- 'bash tools/profile_round.sh r01'   then   python tools/summarize_ncu.py r01
+tag=${1:-r01}
+O=gpurun_out
+mkdir -p $O
+python bench.py > $O/bench.json 2> $O/bench.err; echo bench_rc=$?
+python bench.py --impl reference --steps 3200 --warmup 64 > $O/bench_ref.json 2>&1; echo ref_rc=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
+  python bench.py --steps 320 --warmup 32 --cpu-seconds 0 > $O/ncu_list.out 2>&1; echo list_rc=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:mlp_step -s 3 -c 1 -f -o $O/prof_mlp_$tag \
+  python bench.py --steps 64 --warmup 32 --cpu-seconds 0 --no-reducer > $O/ncu_mlp.out 2>&1; echo mlp_rc=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:reduce_fast -s 2 -c 1 -f -o $O/prof_reduce_$tag \
+  python bench.py --steps 64 --warmup 32 --cpu-seconds 0 > $O/ncu_red.out 2>&1; echo red_rc=$?
+cat $O/bench.json; tail -3 $O/bench.err

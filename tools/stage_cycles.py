@@ -33,7 +33,7 @@ for shape in SHAPES:
     ev1.synchronize()
     t = timing.tolist()
     n = max(t[5], 1)
-    names = ["B rows+tanh", "C out chain", "E grads(+gsync)", "F fold", "F update"]
+    names = ["B+C rows..dz", "E grads+push", "exchange wait", "F fold+sgd", "commit barrier"]
     per = [x / n for x in t[:5]]
     print(f"E={E} B={B} K={K} epc={a.est_per_cta}: launch {ev0.elapsed_time(ev1) * 1e3:.1f} us, "
           f"{sum(per):.0f} cyc/step: " + ", ".join(f"{nm} {v:.0f}" for nm, v in zip(names, per))

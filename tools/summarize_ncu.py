@@ -84,8 +84,8 @@ def summarize(rep, name):
 
 PROF.mkdir(exist_ok=True)
 launches()
-t_mlp = summarize(OUT / "prof_mlp_r1.ncu-rep", "ncu_mlp_step")
-t_red = summarize(OUT / "prof_reduce_r1.ncu-rep", "ncu_reducer")
+t_mlp = summarize(OUT / f"prof_mlp_{tag}.ncu-rep", "ncu_mlp_step")
+t_red = summarize(OUT / f"prof_reduce_{tag}.ncu-rep", "ncu_reducer")
 traffic = {"mlp_step_kernel": t_mlp[0] if t_mlp else None, "reduce_fast_kernel": t_red[0] if t_red else None,
            "source": f"profiles/{tag}_ncu_*.txt (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"}
 (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
