@@ -201,15 +201,14 @@ __device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t r
     tlast = now_;                                      \
   }
 
-// BT: compile-time rows per EST (0 = run time).  ET > 0 selects a specialised
-// build for E_total == ET with every EST's batch variant FB and the allreduce
-// variant FC known at compile time, staged dataset/index lists, and the
-// cluster (or single-CTA) exchange -- the launcher only picks it then.  The
-// generic build (ET = 0, FB = FC = -1) handles every other job.
-template <int BT, int ET, int FB, int FC>
+// Generic build: BT = compile-time rows per EST (0 = run time); any E_total,
+// per-EST variants, explicit or sampled rows, cluster / grid / single-CTA.
+// (mlp_step_spec_kernel below is the compact build for the common shapes.)
+template <int BT>
 __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_constant__ bt_mlp_args a,
                                                                const MlpLaunch L) {
-  constexpr bool SPEC = ET > 0;
+  constexpr bool SPEC = false;
+  constexpr int ET = 0, FB = -1, FC = -1;
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, T = blockDim.x;  // T >= BT_P (launcher): thread p owns parameter p in stage F
   const int cta = blockIdx.x, G = gridDim.x;
@@ -587,6 +586,311 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// Compact build for the common shapes: B = 4 rows per EST, E_total = ET in
+// {4, 8, 16} ESTs on one thread-block cluster of G = min(ET, 8) CTAs (EPC =
+// ET / G ESTs each), one reduction variant F (0 = Sequential, 2 = Tree(2))
+// for every EST's batch reductions and for the allreduce, dataset and index
+// lists staged in shared memory.  Same arithmetic, same order as the generic
+// build; what changes is the bookkeeping: the shared-memory layout and every
+// thread's role are compile-time, each thread's addresses (rows, gradient
+// operands, DSMEM push targets, allreduce leaves) are computed once per
+// launch, and the next mini-batch's row gather, jitter and dropout mask are
+// prefetched while the slot exchange is in flight.
+template <int ET>
+struct SpecShape {
+  static constexpr int G = ET < MAX_CLUSTER_CTAS ? ET : MAX_CLUSTER_CTAS;  // CTAs = cluster size
+  static constexpr int EPC = ET / G;                                     // ESTs per CTA
+  static constexpr int NB = 4;                                           // rows per EST
+  static constexpr int R = NB * EPC;                                     // rows per CTA
+  static constexpr int LANES = R * BT_HIDDEN;                            // stage B+C lanes
+  static constexpr int T = LANES > 192 ? LANES : 192;                    // >= BT_P + 1
+  static constexpr int ITEMS = EPC * (BT_P + 1);                         // stage E items
+  static constexpr int NIT = (ITEMS + T - 1) / T;
+  // shared-memory layout, in doubles
+  static constexpr int PAR = 0;                    // [2][PAD_P] parameters (step-parity buffers)
+  static constexpr int VEL = PAR + 2 * PAD_P;      // [2][PAD_P] velocity
+  static constexpr int X = VEL + 2 * PAD_P;        // [R][8] jittered inputs
+  static constexpr int Y = X + R * BT_INPUT_DIM;   // [R]
+  static constexpr int ACT = Y + R;                // [R][16]
+  static constexpr int HID = ACT + R * BT_HIDDEN;  // [R][16]
+  static constexpr int DZ = HID + R * BT_HIDDEN;   // [R][16]
+  static constexpr int GY = DZ + R * BT_HIDDEN;    // [R]
+  static constexpr int E2 = GY + R;                // [R]
+  static constexpr int RM = E2 + R;                // [R]
+  static constexpr int MEAN = RM + R;              // [EPC]
+  static constexpr int RNG = MEAN + EPC;           // [EPC] u64
+  static constexpr int CNT = RNG + EPC;            // [EPC] u64
+  static constexpr int GRAD = (CNT + EPC + 1) & ~1;  // [2][ET][BT_P] slot arrays (16-byte aligned)
+  static constexpr int ROT = GRAD + 2 * ET * BT_P;   // int32 [PAD_P]
+  static constexpr int DATA = ROT + PAD_P / 2;       // [dataset_rows][9], then jit [K][R], idx int32 [K][R]
+  static constexpr size_t fixed_bytes() { return sizeof(double) * DATA; }
+};
+
+template <int ET, int F>
+__global__ void __launch_bounds__(SpecShape<ET>::T) mlp_step_spec_kernel(const __grid_constant__ bt_mlp_args a,
+                                                                          const MlpLaunch L) {
+  using S = SpecShape<ET>;
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x;
+  const int cta = blockIdx.x;  // the grid is one cluster: blockIdx.x is the cluster rank
+  const int e0 = cta * S::EPC;
+  double* const s_data = sm + S::DATA;
+  double* const s_jit = s_data + (size_t)a.dataset_rows * BT_ROW;
+  int32_t* const s_idx = (int32_t*)(s_jit + (size_t)a.K * S::R);
+  int32_t* const s_rot = (int32_t*)(sm + S::ROT);
+  uint64_t* const s_rng = (uint64_t*)(sm + S::RNG);
+  uint64_t* const s_cnt = (uint64_t*)(sm + S::CNT);
+  __shared__ __align__(8) uint64_t s_mbar[2];
+
+  if (a.flags[FLAG_STATUS] != 0) return;
+  if (tid == 0) {
+    mbar_init(smem_u32(&s_mbar[0]), 1);
+    mbar_init(smem_u32(&s_mbar[1]), 1);
+    mbar_init_fence();
+  }
+  // ---- prologue ---------------------------------------------------------
+  int bad = 0;
+  for (int i = tid; i < BT_P; i += S::T) {
+    const double p0 = a.replicas[i], v0 = a.replicas[BT_P + i];
+    sm[S::PAR + i] = p0;
+    sm[S::VEL + i] = v0;
+    s_rot[i] = a.rot ? a.rot[i] : 0;
+    for (int x = 1; x < a.X; ++x) {  // replica agreement, bytewise (engine.py:246-258)
+      const double* rx = a.replicas + (size_t)x * 2 * BT_P;
+      bad |= (d2u(rx[i]) != d2u(p0)) | (d2u(rx[BT_P + i]) != d2u(v0));
+    }
+  }
+  for (int el = tid; el < S::EPC; el += S::T) {
+    s_rng[el] = a.rng[e0 + el];
+    sm[S::MEAN + el] = a.stat_mean[e0 + el];
+    s_cnt[el] = a.stat_count[e0 + el];
+    bad |= (a.est_fanin[e0 + el] != F) << 1;  // the launcher's variant hint must hold
+  }
+  {
+    const int64_t nd = a.dataset_rows * BT_ROW;
+    for (int64_t i = tid; i < nd; i += S::T) s_data[i] = a.dataset[i];
+  }
+  for (int it = tid; it < a.K * S::R; it += S::T) {
+    const int s = it / S::R, rem = it - s * S::R;
+    const int el = rem / S::NB, r = rem - el * S::NB;
+    const int64_t gstep = a.step0 + s, epoch = gstep / a.spe, local = gstep % a.spe;
+    const int eg = e0 + el;
+    const int32_t* lst = a.lists + ((size_t)(epoch - a.epoch_base) * ET + eg) * (size_t)(a.spe * S::NB);
+    s_idx[it] = lst[local * S::NB + r];
+    double ju = 0.0;
+    if (a.jitter != 0.0) {  // one uniform per row of worker_rng(seed, epoch, local, est) (sampling.py:99-170)
+      const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)epoch, (uint64_t)local, (uint64_t)eg);
+      ju = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), a.jitter);
+    }
+    s_jit[it] = ju;
+  }
+  const int prologue = __syncthreads_or(bad);
+  if (prologue) {
+    if (cta == 0 && tid == 0) {
+      a.flags[FLAG_STATUS] = (prologue & 1) ? ERR_CORRUPTION : ERR_INPUT;
+      a.flags[FLAG_STEP] = 0;
+    }
+    return;
+  }
+  cluster_barrier();  // every peer's mbarriers are initialised before the first push
+
+  // ---- per-thread constants ----------------------------------------------
+  const double rate = a.rate, lr = a.lr, mu = a.mu;
+  const double keep = rate >= 1.0 ? 0.0 : ddiv(1.0, dsub(1.0, rate));  // model.py:150
+  const bool jit = a.jitter != 0.0;
+  const IntDivisor divB = IntDivisor::of(S::NB), divH = IntDivisor::of(BT_HIDDEN), divE = IntDivisor::of(ET);
+  // B+C lane: row = tid / 16 of this CTA, hidden unit j = tid % 16
+  const bool lane = tid < S::LANES;
+  const int row = lane ? tid >> 4 : 0, j = tid & 15;
+  const int lel = row / S::NB, lr_ = row - lel * S::NB;
+  uint64_t lrng = s_rng[lel];  // this row's EST dropout stream, advanced in registers
+  // E items: (EST, parameter or loss) pairs
+  uint32_t push_off[S::NIT];  // byte offset of the item's slot entry in a parity-0 slot array
+  uint32_t peer[S::G], peerbar[S::G];
+#pragma unroll
+  for (int k = 0; k < S::NIT; ++k) {
+    const int it = tid + k * S::T;
+    const int el = it / (BT_P + 1), p = it - el * (BT_P + 1);
+    push_off[k] = (uint32_t)(((e0 + el) * BT_P + p) * sizeof(double));
+  }
+#pragma unroll
+  for (int rk = 0; rk < S::G; ++rk) {
+    peer[rk] = cluster_map32(smem_u32(sm + S::GRAD), rk);
+    peerbar[rk] = cluster_map32(smem_u32(&s_mbar[0]), rk);
+  }
+  const int rot_p = tid < BT_P ? s_rot[tid] : 0;
+  uint32_t phases = 0;
+
+  // prefetched inputs of the next mini-batch (lane threads)
+  double x[BT_ROW], msk = 1.0;
+  auto prefetch = [&](int s) {
+    const int q = s * S::R + row;
+    const double* src = s_data + (size_t)s_idx[q] * BT_ROW;
+    const double ju = s_jit[q];
+#pragma unroll
+    for (int i = 0; i < BT_INPUT_DIM; ++i) x[i] = jit ? dadd(src[i], ju) : src[i];
+    x[BT_INPUT_DIM] = src[BT_INPUT_DIM];
+    msk = 1.0;
+    if (rate > 0.0) {  // draw n = r*16+j of this EST's stream (rows outer, units inner)
+      const double ud = unit_float(draw_raw(lrng, (uint64_t)(lr_ * BT_HIDDEN + j)));
+      msk = ud < rate ? 0.0 : keep;
+    }
+  };
+  if (lane) prefetch(0);
+
+  unsigned long long tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+  int cur = 0, s = 0;
+  for (; s < a.K; ++s) {
+    const int par = (int)((a.step0 + s) & 1);
+    const double* P = sm + S::PAR + cur * PAD_P;
+
+    // ---- B+C (model.py:141-179, 194) --------------------------------------
+    if (lane) {
+      {  // lane j < 8 keeps input j, lane 8 keeps y
+        double keepv = x[0];
+#pragma unroll
+        for (int i = 1; i < BT_ROW; ++i) keepv = j == i ? x[i] : keepv;
+        if (j < BT_INPUT_DIM) sm[S::X + row * BT_INPUT_DIM + j] = keepv;
+        else if (j == BT_INPUT_DIM) sm[S::Y + row] = keepv;
+      }
+      double acc = dmul(P[BT_W1 + j], x[0]);
+#pragma unroll
+      for (int i = 1; i < BT_INPUT_DIM; ++i) acc = dadd(acc, dmul(P[BT_W1 + i * BT_HIDDEN + j], x[i]));
+      const double act = glibc_tanh_simt(dadd(acc, P[BT_B1 + j]));
+      const double hj = dmul(act, msk);
+      sm[S::ACT + tid] = act;
+      sm[S::HID + tid] = hj;
+      __syncwarp();
+      const double* h = sm + S::HID + row * BT_HIDDEN;
+      const double* ar = sm + S::ACT + row * BT_HIDDEN;
+      double o = dmul(P[BT_W2], h[0]);
+      double msum = ar[0];
+#pragma unroll
+      for (int q = 1; q < BT_HIDDEN; ++q) {
+        o = dadd(o, dmul(P[BT_W2 + q], h[q]));
+        msum = dadd(msum, ar[q]);
+      }
+      const double err = dsub(dadd(o, P[BT_B2]), x[BT_INPUT_DIM]);
+      const double gy = divB.apply(dmul(2.0, err));
+      sm[S::DZ + tid] = dmul(dmul(dmul(gy, P[BT_W2 + j]), msk), dsub(1.0, dmul(act, act)));
+      if (j == 0) {
+        sm[S::E2 + row] = dmul(err, err);
+        sm[S::GY + row] = gy;
+        sm[S::RM + row] = divH.apply(msum);
+      }
+    }
+    __syncthreads();
+    BT_TICK(0)
+
+    // ---- E: gradients -> every CTA's slot array (model.py:183-192) --------
+    if (tid == 0) mbar_arrive_expect_tx(smem_u32(&s_mbar[par]), (uint32_t)(ET * BT_P * sizeof(double)));
+#pragma unroll
+    for (int k = 0; k < S::NIT; ++k) {
+      const int it = tid + k * S::T;
+      if (it < S::ITEMS) {
+        const int el = it / (BT_P + 1), p = it - el * (BT_P + 1);
+        const int rb = el * S::NB;
+        const double g = fold_rows<S::NB, F>(S::NB, F, [&](int r) {
+          const int rw = rb + r;
+          if (p < BT_B1) return dmul(sm[S::DZ + rw * BT_HIDDEN + (p & 15)], sm[S::X + rw * BT_INPUT_DIM + (p >> 4)]);
+          if (p < BT_W2) return sm[S::DZ + rw * BT_HIDDEN + (p - BT_B1)];
+          if (p < BT_B2) return dmul(sm[S::GY + rw], sm[S::HID + rw * BT_HIDDEN + (p - BT_W2)]);
+          if (p == BT_B2) return sm[S::GY + rw];
+          return sm[S::E2 + rw];
+        });
+        if (p < BT_P) {
+          const uint32_t off = push_off[k] + (uint32_t)(par * ET * BT_P * sizeof(double));
+#pragma unroll
+          for (int rk = 0; rk < S::G; ++rk) st_async_f64(peer[rk] + off, g, peerbar[rk] + par * 8);
+        } else {  // loss, TrackedStat, dropout stream of EST e0+el (model.py:173, 99-104)
+          const int e = e0 + el;
+          a.losses[(size_t)s * ET + e] = divB.apply(g);
+          double bm = sm[S::RM + rb];
+#pragma unroll
+          for (int r = 1; r < S::NB; ++r) bm = dadd(bm, sm[S::RM + rb + r]);
+          bm = divB.apply(bm);
+          const int64_t rank = a.rank_override >= 0 ? a.rank_override : (int64_t)e;
+          const double mixed = dadd(bm, dmul((double)rank, 0x1p-40));
+          sm[S::MEAN + el] = dadd(dmul(sm[S::MEAN + el], 0.9), dmul(0.1, mixed));
+          s_cnt[el] += 1;
+          if (rate > 0.0) s_rng[el] = advance(s_rng[el], (uint64_t)S::NB * BT_HIDDEN);
+        }
+      }
+    }
+    BT_TICK(1)
+    // the next mini-batch's rows and masks while the exchange is in flight
+    if (lane && s + 1 < a.K) {
+      if (rate > 0.0) lrng = advance(lrng, (uint64_t)S::NB * BT_HIDDEN);
+      prefetch(s + 1);
+    }
+
+    // ---- exchange: all ET*P*8 slot bytes of this step parity --------------
+    {
+      const uint32_t bar = smem_u32(&s_mbar[par]);
+      const uint32_t want = (phases >> par) & 1u;
+      if (!mbar_try_wait(bar, want)) {
+        const long long t0 = clock64();
+        while (!mbar_try_wait(bar, want)) {
+          if (clock64() - t0 > (1ll << 34)) {  // a lost arrival is a bug: fail instead of hanging
+            atomicCAS(a.flags + FLAG_STATUS, 0, (int)ERR_CUDA);
+            __trap();
+          }
+        }
+      }
+      phases ^= 1u << par;
+    }
+    BT_TICK(2)
+
+    // ---- F: allreduce + /E + momentum SGD into the other buffer -----------
+    int ok = 1;
+    double np = 0.0;
+    if (tid < BT_P) {
+      const double* col = sm + S::GRAD + par * ET * BT_P + tid;
+      const double sum = fold_ranks_t<ET, F>(rot_p, [&](int q) { return col[q * BT_P]; });
+      const double g = divE.apply(sum);
+      ok = finite_d(g) ? 1 : 0;
+      const double v = dadd(dmul(mu, sm[S::VEL + cur * PAD_P + tid]), g);
+      np = dsub(P[tid], dmul(lr, v));
+      sm[S::VEL + (cur ^ 1) * PAD_P + tid] = v;
+      sm[S::PAR + (cur ^ 1) * PAD_P + tid] = np;
+    }
+    BT_TICK(3)
+    if (!__syncthreads_and(ok)) {  // sgd_step raises before mutating (model.py:207-209)
+      if (cta == 0 && tid == 0) {
+        a.flags[FLAG_STATUS] = ERR_NUMERIC;
+        a.flags[FLAG_STEP] = s;
+      }
+      break;
+    }
+    cur ^= 1;
+    if (a.param_trace && cta == 0 && tid < BT_P) a.param_trace[(size_t)s * BT_P + tid] = np;
+    BT_TICK(4)
+  }
+  if (L.timing && tid == 0 && cta == 0) {
+    for (int k = 0; k < 5; ++k) L.timing[k] += tacc[k];
+    L.timing[5] += (unsigned long long)s;
+  }
+
+  // ---- epilogue -----------------------------------------------------------
+  cluster_barrier();
+  for (int el = tid; el < S::EPC; el += S::T) {
+    a.rng[e0 + el] = s_rng[el];
+    a.stat_mean[e0 + el] = sm[S::MEAN + el];
+    a.stat_count[e0 + el] = s_cnt[el];
+  }
+  if (cta == 0) {  // engine.py:313-315
+    for (int x = 0; x < a.X; ++x) {
+      double* rx = a.replicas + (size_t)x * 2 * BT_P;
+      for (int i = tid; i < BT_P; i += S::T) {
+        rx[i] = sm[S::PAR + cur * PAD_P + i];
+        rx[BT_P + i] = sm[S::VEL + cur * PAD_P + i];
+      }
+    }
+  }
+}
+
 static constexpr size_t SMEM_LIMIT = 220 * 1024;
 
 static size_t base_smem_bytes(const bt_mlp_args& a) {
@@ -642,12 +946,30 @@ bool mlp_fused_fits(const bt_mlp_args& a) {
   return base_smem_bytes(a) + sizeof(double) * slots * BT_P <= SMEM_LIMIT;
 }
 
-template <int BT, int ET, int FB, int FC>
+template <class Kern>
+static cudaError_t launch_cluster(Kern kern, const bt_mlp_args& a, size_t smem, int grid, int threads,
+                                  cudaStream_t stream, const MlpLaunch& L) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = grid;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, L);
+}
+
+template <int BT>
 static cudaError_t launch_k(const bt_mlp_args& a, const MlpLaunch& L, size_t smem, int grid, cudaStream_t stream) {
-  auto kern = mlp_step_kernel<BT, ET, FB, FC>;
   static bool attr_set = false;  // one per instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
+    cudaError_t e =
+        cudaFuncSetAttribute(mlp_step_kernel<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -656,38 +978,39 @@ static cudaError_t launch_k(const bt_mlp_args& a, const MlpLaunch& L, size_t sme
     // (stage B: one thread per (row, unit)), at least one per parameter.
     int threads = ((a.est_per_cta * a.B * BT_HIDDEN + 31) / 32) * 32;
     threads = threads < 192 ? 192 : (threads > MLP_THREADS ? MLP_THREADS : threads);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = grid;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, a, L);
+    return launch_cluster(mlp_step_kernel<BT>, a, smem, grid, threads, stream, L);
   }
   if (grid > 1 && a.fuse_reduce) {
     if (cudaMemsetAsync(a.bar, 0, sizeof(uint32_t), stream) != cudaSuccess) return cudaGetLastError();
     void* params[] = {(void*)&a, (void*)&L};
-    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(MLP_THREADS), params, smem, stream);
+    return cudaLaunchCooperativeKernel((const void*)mlp_step_kernel<BT>, dim3(grid), dim3(MLP_THREADS), params,
+                                       smem, stream);
   }
-  kern<<<grid, MLP_THREADS, smem, stream>>>(a, L);
+  mlp_step_kernel<BT><<<grid, MLP_THREADS, smem, stream>>>(a, L);
   return cudaGetLastError();
 }
 
-// Specialised builds: B = 4 rows, E_total in {4, 8, 16}, one variant for every
-// EST and the allreduce (Sequential: d1d2 / d2, or Tree(2): the gpu_fast kind).
+template <int ET, int F>
+static cudaError_t launch_spec(const bt_mlp_args& a, size_t smem, cudaStream_t stream, const MlpLaunch& L) {
+  using S = SpecShape<ET>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(mlp_step_spec_kernel<ET, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  return launch_cluster(mlp_step_spec_kernel<ET, F>, a, smem, S::G, S::T, stream, L);
+}
+
+// Shared memory of the compact build, or 0 when it does not apply.
 template <int ET>
-static bool launch_spec(const bt_mlp_args& a, const MlpLaunch& L, size_t smem, int grid, cudaStream_t stream,
-                        int fan, cudaError_t* err) {
-  if (fan == 0) *err = launch_k<4, ET, 0, 0>(a, L, smem, grid, stream);
-  else if (fan == 2) *err = launch_k<4, ET, 2, 2>(a, L, smem, grid, stream);
-  else return false;
-  return true;
+static size_t spec_smem(const bt_mlp_args& a) {
+  using S = SpecShape<ET>;
+  if (a.est_per_cta != S::EPC) return 0;
+  const size_t bytes = S::fixed_bytes() + sizeof(double) * (size_t)a.dataset_rows * BT_ROW +
+                       (sizeof(double) + sizeof(int32_t)) * (size_t)a.K * S::R;
+  return bytes <= SMEM_LIMIT ? bytes : 0;
 }
 
 int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* timing) {
@@ -697,29 +1020,35 @@ int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* ti
   L.timing = timing;
   if (a.fuse_reduce && !L.grads_smem && !L.cluster) return ERR_INPUT;  // too many ESTs for the fused path
   if (smem > SMEM_LIMIT) return ERR_INPUT;
-  cudaError_t err = cudaSuccess;
   const int fan = a.est_fanin_uniform - 1;  // every EST's batch variant, when the caller knows it
-  const bool spec_ok = a.fuse_reduce && a.B == 4 && a.E == a.E_total && !a.rows && L.stage_idx && L.stage_data &&
-                       (L.cluster || (grid == 1 && L.grads_smem)) && fan >= 0 && fan == a.comm_fanin;
-  bool done = false;
-  if (spec_ok) {
+  if (a.fuse_reduce && a.B == 4 && a.E == a.E_total && !a.rows && a.dataset_rows > 0 && a.rank_override < 0 &&
+      (fan == 0 || fan == 2) && fan == a.comm_fanin) {
+    size_t ss = 0;
+    cudaError_t err = cudaErrorNotSupported;
     switch (a.E_total) {
-      case 4: done = launch_spec<4>(a, L, smem, grid, stream, fan, &err); break;
-      case 8: done = launch_spec<8>(a, L, smem, grid, stream, fan, &err); break;
-      case 16: done = launch_spec<16>(a, L, smem, grid, stream, fan, &err); break;
+      case 4:
+        if ((ss = spec_smem<4>(a))) err = fan ? launch_spec<4, 2>(a, ss, stream, L) : launch_spec<4, 0>(a, ss, stream, L);
+        break;
+      case 8:
+        if ((ss = spec_smem<8>(a))) err = fan ? launch_spec<8, 2>(a, ss, stream, L) : launch_spec<8, 0>(a, ss, stream, L);
+        break;
+      case 16:
+        if ((ss = spec_smem<16>(a)))
+          err = fan ? launch_spec<16, 2>(a, ss, stream, L) : launch_spec<16, 0>(a, ss, stream, L);
+        break;
       default: break;
     }
+    if (ss) return err == cudaSuccess ? OK : ERR_CUDA;
   }
-  if (!done) {
-    switch (a.B) {
-      case 1: err = launch_k<1, 0, -1, -1>(a, L, smem, grid, stream); break;
-      case 2: err = launch_k<2, 0, -1, -1>(a, L, smem, grid, stream); break;
-      case 4: err = launch_k<4, 0, -1, -1>(a, L, smem, grid, stream); break;
-      case 8: err = launch_k<8, 0, -1, -1>(a, L, smem, grid, stream); break;
-      case 16: err = launch_k<16, 0, -1, -1>(a, L, smem, grid, stream); break;
-      case 32: err = launch_k<32, 0, -1, -1>(a, L, smem, grid, stream); break;
-      default: err = launch_k<0, 0, -1, -1>(a, L, smem, grid, stream); break;
-    }
+  cudaError_t err;
+  switch (a.B) {
+    case 1: err = launch_k<1>(a, L, smem, grid, stream); break;
+    case 2: err = launch_k<2>(a, L, smem, grid, stream); break;
+    case 4: err = launch_k<4>(a, L, smem, grid, stream); break;
+    case 8: err = launch_k<8>(a, L, smem, grid, stream); break;
+    case 16: err = launch_k<16>(a, L, smem, grid, stream); break;
+    case 32: err = launch_k<32>(a, L, smem, grid, stream); break;
+    default: err = launch_k<0>(a, L, smem, grid, stream); break;
   }
   return err == cudaSuccess ? OK : ERR_CUDA;
 }
