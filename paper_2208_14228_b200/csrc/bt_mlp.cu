@@ -174,6 +174,12 @@ __device__ __forceinline__ void mbar_init_fence() {  // make mbarrier.init visib
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void st_shared_f64(uint32_t addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -588,29 +594,39 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
 
 // ---------------------------------------------------------------------------
 // Compact build for the common shapes: B = 4 rows per EST, E_total = ET in
-// {4, 8, 16} ESTs on one thread-block cluster of G = min(ET, 8) CTAs (EPC =
-// ET / G ESTs each), one reduction variant F (0 = Sequential, 2 = Tree(2))
-// for every EST's batch reductions and for the allreduce, dataset and index
-// lists staged in shared memory.  Same arithmetic, same order as the generic
-// build; what changes is the bookkeeping: the shared-memory layout and every
-// thread's role are compile-time, each thread's addresses (rows, gradient
-// operands, DSMEM push targets, allreduce leaves) are computed once per
-// launch, and the next mini-batch's row gather, jitter and dropout mask are
-// prefetched while the slot exchange is in flight.
-template <int ET>
+// {4, 8, 16} ESTs on one thread-block cluster of G CTAs (EPC = ET / G ESTs
+// each), one reduction variant F (0 = Sequential, 2 = Tree(2)) for every EST's
+// batch reductions and for the allreduce, dataset and index lists staged in
+// shared memory.  Same arithmetic, same order as the generic build; what
+// changes is the data movement and the bookkeeping:
+//  * the allreduce is owner-computes: parameter p belongs to CTA p / CH.  Each
+//    CTA pushes gradient p of its ESTs only to p's owner (reduce-scatter, one
+//    DSMEM store per value); the owner folds all ET leaves in the reference
+//    order, applies /E and momentum SGD, and pushes the new parameter to every
+//    CTA (all-gather) together with a per-warp "all finite" flag.  Both
+//    exchanges are st.async stores counted on the receiver's mbarrier, so a
+//    step has one CTA barrier and two mbarrier waits, and moves ~2.5 KB per
+//    CTA over DSMEM instead of ET * 1.3 KB;
+//  * the shared-memory layout and every thread's role are compile-time; each
+//    thread's addresses are computed once per launch; the next mini-batch's
+//    row gather, jitter and dropout mask are prefetched during the exchange.
+template <int ET, int GG>
 struct SpecShape {
-  static constexpr int G = ET < MAX_CLUSTER_CTAS ? ET : MAX_CLUSTER_CTAS;  // CTAs = cluster size
-  static constexpr int EPC = ET / G;                                     // ESTs per CTA
-  static constexpr int NB = 4;                                           // rows per EST
-  static constexpr int R = NB * EPC;                                     // rows per CTA
-  static constexpr int LANES = R * BT_HIDDEN;                            // stage B+C lanes
-  static constexpr int T = LANES > 192 ? LANES : 192;                    // >= BT_P + 1
-  static constexpr int ITEMS = EPC * (BT_P + 1);                         // stage E items
+  static constexpr int G = GG;                            // CTAs = cluster size
+  static constexpr int EPC = ET / G;                      // ESTs per CTA
+  static constexpr int NB = 4;                            // rows per EST
+  static constexpr int R = NB * EPC;                      // rows per CTA
+  static constexpr int LANES = R * BT_HIDDEN;             // stage B+C lanes
+  static constexpr int T = LANES > 192 ? LANES : 192;     // >= BT_P + 1
+  static constexpr int ITEMS = EPC * (BT_P + 1);          // stage E items
   static constexpr int NIT = (ITEMS + T - 1) / T;
+  static constexpr int CH = (BT_P + G - 1) / G;           // parameters per owner
+  static constexpr int NW = (CH + 31) / 32;               // owner warps (one finite flag each)
+  static constexpr int chunk(int c) { return (c + 1) * CH <= BT_P ? CH : BT_P - c * CH; }
   // shared-memory layout, in doubles
   static constexpr int PAR = 0;                    // [2][PAD_P] parameters (step-parity buffers)
-  static constexpr int VEL = PAR + 2 * PAD_P;      // [2][PAD_P] velocity
-  static constexpr int X = VEL + 2 * PAD_P;        // [R][8] jittered inputs
+  static constexpr int VEL = PAR + 2 * PAD_P;      // [2][CH] velocity of the owned chunk
+  static constexpr int X = VEL + 2 * CH;           // [R][8] jittered inputs
   static constexpr int Y = X + R * BT_INPUT_DIM;   // [R]
   static constexpr int ACT = Y + R;                // [R][16]
   static constexpr int HID = ACT + R * BT_HIDDEN;  // [R][16]
@@ -621,32 +637,45 @@ struct SpecShape {
   static constexpr int MEAN = RM + R;              // [EPC]
   static constexpr int RNG = MEAN + EPC;           // [EPC] u64
   static constexpr int CNT = RNG + EPC;            // [EPC] u64
-  static constexpr int GRAD = (CNT + EPC + 1) & ~1;  // [2][ET][BT_P] slot arrays (16-byte aligned)
-  static constexpr int ROT = GRAD + 2 * ET * BT_P;   // int32 [PAD_P]
-  static constexpr int DATA = ROT + PAD_P / 2;       // [dataset_rows][9], then jit [K][R], idx int32 [K][R]
+  static constexpr int RS = CNT + EPC;             // [2][ET][CH] gradients of the owned chunk
+  static constexpr int OK = RS + 2 * ET * CH;      // [2][G * NW] owners' finite flags
+  static constexpr int ROT = OK + 2 * G * NW;      // int32 [CH] rotation starts of the owned chunk
+  static constexpr int DATA = (ROT + CH / 2 + 2) & ~1;  // [dataset_rows][9], jit [K][R], idx int32 [K][R]
   static constexpr size_t fixed_bytes() { return sizeof(double) * DATA; }
 };
 
-template <int ET, int F>
-__global__ void __launch_bounds__(SpecShape<ET>::T) mlp_step_spec_kernel(const __grid_constant__ bt_mlp_args a,
-                                                                          const MlpLaunch L) {
-  using S = SpecShape<ET>;
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int32_t* flags) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > (1ll << 34)) {  // a lost arrival is a bug: fail instead of hanging
+      atomicCAS(flags + FLAG_STATUS, 0, (int)ERR_CUDA);
+      __trap();
+    }
+  }
+}
+
+template <int ET, int G, int F>
+__global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(const __grid_constant__ bt_mlp_args a,
+                                                                             const MlpLaunch L) {
+  using S = SpecShape<ET, G>;
+  static_assert(G > 1 && ET % G == 0, "compact build: a cluster of G > 1 CTAs");
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
   const int cta = blockIdx.x;  // the grid is one cluster: blockIdx.x is the cluster rank
   const int e0 = cta * S::EPC;
+  const int own0 = cta * S::CH, own_n = S::chunk(cta);  // owned parameters [own0, own0 + own_n)
   double* const s_data = sm + S::DATA;
   double* const s_jit = s_data + (size_t)a.dataset_rows * BT_ROW;
   int32_t* const s_idx = (int32_t*)(s_jit + (size_t)a.K * S::R);
   int32_t* const s_rot = (int32_t*)(sm + S::ROT);
   uint64_t* const s_rng = (uint64_t*)(sm + S::RNG);
   uint64_t* const s_cnt = (uint64_t*)(sm + S::CNT);
-  __shared__ __align__(8) uint64_t s_mbar[2];
+  __shared__ __align__(8) uint64_t s_mbar[4];  // [0..1] reduce-scatter, [2..3] all-gather, by step parity
 
   if (a.flags[FLAG_STATUS] != 0) return;
-  if (tid == 0) {
-    mbar_init(smem_u32(&s_mbar[0]), 1);
-    mbar_init(smem_u32(&s_mbar[1]), 1);
+  if (tid == 0) {  // a phase completes when every local thread arrived and every remote byte landed
+    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&s_mbar[i]), S::T);
     mbar_init_fence();
   }
   // ---- prologue ---------------------------------------------------------
@@ -654,8 +683,10 @@ __global__ void __launch_bounds__(SpecShape<ET>::T) mlp_step_spec_kernel(const _
   for (int i = tid; i < BT_P; i += S::T) {
     const double p0 = a.replicas[i], v0 = a.replicas[BT_P + i];
     sm[S::PAR + i] = p0;
-    sm[S::VEL + i] = v0;
-    s_rot[i] = a.rot ? a.rot[i] : 0;
+    if (i >= own0 && i < own0 + own_n) {
+      sm[S::VEL + (i - own0)] = v0;
+      s_rot[i - own0] = a.rot ? a.rot[i] : 0;
+    }
     for (int x = 1; x < a.X; ++x) {  // replica agreement, bytewise (engine.py:246-258)
       const double* rx = a.replicas + (size_t)x * 2 * BT_P;
       bad |= (d2u(rx[i]) != d2u(p0)) | (d2u(rx[BT_P + i]) != d2u(v0));
@@ -705,22 +736,31 @@ __global__ void __launch_bounds__(SpecShape<ET>::T) mlp_step_spec_kernel(const _
   const int row = lane ? tid >> 4 : 0, j = tid & 15;
   const int lel = row / S::NB, lr_ = row - lel * S::NB;
   uint64_t lrng = s_rng[lel];  // this row's EST dropout stream, advanced in registers
-  // E items: (EST, parameter or loss) pairs
-  uint32_t push_off[S::NIT];  // byte offset of the item's slot entry in a parity-0 slot array
-  uint32_t peer[S::G], peerbar[S::G];
+  uint32_t peer[G], peerbar[G];
+#pragma unroll
+  for (int rk = 0; rk < G; ++rk) {
+    peer[rk] = cluster_map32(smem_u32(sm), rk);
+    peerbar[rk] = cluster_map32(smem_u32(&s_mbar[0]), rk);
+  }
+  // E items: gradient p of local EST el goes to owner p / CH, leaf slot e0 + el
+  uint32_t rs_dst[S::NIT], rs_bar[S::NIT];
+  bool rs_local[S::NIT];
 #pragma unroll
   for (int k = 0; k < S::NIT; ++k) {
     const int it = tid + k * S::T;
     const int el = it / (BT_P + 1), p = it - el * (BT_P + 1);
-    push_off[k] = (uint32_t)(((e0 + el) * BT_P + p) * sizeof(double));
+    const int o = p < BT_P ? p / S::CH : 0;
+    rs_local[k] = o == cta;
+    const uint32_t off = (uint32_t)((S::RS + (e0 + el) * S::CH + (p - o * S::CH)) * sizeof(double));
+    rs_dst[k] = (rs_local[k] ? smem_u32(sm) : peer[o]) + off;
+    rs_bar[k] = rs_local[k] ? smem_u32(&s_mbar[0]) : peerbar[o];
   }
-#pragma unroll
-  for (int rk = 0; rk < S::G; ++rk) {
-    peer[rk] = cluster_map32(smem_u32(sm + S::GRAD), rk);
-    peerbar[rk] = cluster_map32(smem_u32(&s_mbar[0]), rk);
-  }
-  const int rot_p = tid < BT_P ? s_rot[tid] : 0;
-  uint32_t phases = 0;
+  // F: owner thread t < own_n handles parameter own0 + t
+  const bool owner = tid < own_n;
+  const int rot_t = owner ? s_rot[tid] : 0;
+  const uint32_t rs_bytes = (uint32_t)((ET - S::EPC) * own_n * sizeof(double));
+  const uint32_t ag_bytes = (uint32_t)(((BT_P - own_n) + (G - 1) * S::NW) * sizeof(double));
+  uint32_t phases = 0;  // bit b: parity of the next completion of s_mbar[b]
 
   // prefetched inputs of the next mini-batch (lane threads)
   double x[BT_ROW], msk = 1.0;
@@ -741,9 +781,10 @@ __global__ void __launch_bounds__(SpecShape<ET>::T) mlp_step_spec_kernel(const _
 
   unsigned long long tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tlast = clock64();
-  int cur = 0, s = 0;
+  int s = 0;
   for (; s < a.K; ++s) {
     const int par = (int)((a.step0 + s) & 1);
+    const int cur = s & 1;  // parameter buffer of this step
     const double* P = sm + S::PAR + cur * PAD_P;
 
     // ---- B+C (model.py:141-179, 194) --------------------------------------
@@ -784,8 +825,7 @@ __global__ void __launch_bounds__(SpecShape<ET>::T) mlp_step_spec_kernel(const _
     __syncthreads();
     BT_TICK(0)
 
-    // ---- E: gradients -> every CTA's slot array (model.py:183-192) --------
-    if (tid == 0) mbar_arrive_expect_tx(smem_u32(&s_mbar[par]), (uint32_t)(ET * BT_P * sizeof(double)));
+    // ---- E: gradients -> their owners (reduce-scatter, model.py:183-192) --
 #pragma unroll
     for (int k = 0; k < S::NIT; ++k) {
       const int it = tid + k * S::T;
@@ -801,9 +841,9 @@ __global__ void __launch_bounds__(SpecShape<ET>::T) mlp_step_spec_kernel(const _
           return sm[S::E2 + rw];
         });
         if (p < BT_P) {
-          const uint32_t off = push_off[k] + (uint32_t)(par * ET * BT_P * sizeof(double));
-#pragma unroll
-          for (int rk = 0; rk < S::G; ++rk) st_async_f64(peer[rk] + off, g, peerbar[rk] + par * 8);
+          const uint32_t dst = rs_dst[k] + (uint32_t)(par * ET * S::CH * sizeof(double));
+          if (rs_local[k]) st_shared_f64(dst, g);
+          else st_async_f64(dst, g, rs_bar[k] + par * 8);
         } else {  // loss, TrackedStat, dropout stream of EST e0+el (model.py:173, 99-104)
           const int e = e0 + el;
           a.losses[(size_t)s * ET + e] = divB.apply(g);
@@ -819,53 +859,71 @@ __global__ void __launch_bounds__(SpecShape<ET>::T) mlp_step_spec_kernel(const _
         }
       }
     }
+    {  // local slot stores ordered before the arrival (release); thread 0 adds the remote bytes
+      const uint32_t bar = smem_u32(&s_mbar[par]);
+      if (tid == 0) mbar_arrive_expect_tx(bar, rs_bytes);
+      else mbar_arrive(bar);
+    }
     BT_TICK(1)
-    // the next mini-batch's rows and masks while the exchange is in flight
-    if (lane && s + 1 < a.K) {
+    if (lane && s + 1 < a.K) {  // the next mini-batch's rows and masks while the exchange is in flight
       if (rate > 0.0) lrng = advance(lrng, (uint64_t)S::NB * BT_HIDDEN);
       prefetch(s + 1);
     }
-
-    // ---- exchange: all ET*P*8 slot bytes of this step parity --------------
-    {
-      const uint32_t bar = smem_u32(&s_mbar[par]);
-      const uint32_t want = (phases >> par) & 1u;
-      if (!mbar_try_wait(bar, want)) {
-        const long long t0 = clock64();
-        while (!mbar_try_wait(bar, want)) {
-          if (clock64() - t0 > (1ll << 34)) {  // a lost arrival is a bug: fail instead of hanging
-            atomicCAS(a.flags + FLAG_STATUS, 0, (int)ERR_CUDA);
-            __trap();
-          }
-        }
-      }
-      phases ^= 1u << par;
-    }
+    mbar_wait(smem_u32(&s_mbar[par]), (phases >> par) & 1u, a.flags);
+    phases ^= 1u << par;
     BT_TICK(2)
 
-    // ---- F: allreduce + /E + momentum SGD into the other buffer -----------
+    // ---- F: owner-computes allreduce + /E + momentum SGD, then all-gather --
+    // Leaf k of parameter p is EST slot (rot[p] + k) mod E: ascending virtual
+    // rank, rotated by the parameter's ring chunk under Tree (buckets.py:115-123).
     int ok = 1;
     double np = 0.0;
-    if (tid < BT_P) {
-      const double* col = sm + S::GRAD + par * ET * BT_P + tid;
-      const double sum = fold_ranks_t<ET, F>(rot_p, [&](int q) { return col[q * BT_P]; });
+    const uint32_t nxt_off = (uint32_t)((S::PAR + (cur ^ 1) * PAD_P + own0 + tid) * sizeof(double));
+    if (owner) {
+      const double* col = sm + S::RS + par * ET * S::CH + tid;
+      const double sum = fold_ranks_t<ET, F>(rot_t, [&](int q) { return col[q * S::CH]; });
       const double g = divE.apply(sum);
       ok = finite_d(g) ? 1 : 0;
-      const double v = dadd(dmul(mu, sm[S::VEL + cur * PAD_P + tid]), g);
-      np = dsub(P[tid], dmul(lr, v));
-      sm[S::VEL + (cur ^ 1) * PAD_P + tid] = v;
-      sm[S::PAR + (cur ^ 1) * PAD_P + tid] = np;
+      const double v = dadd(dmul(mu, sm[S::VEL + cur * S::CH + tid]), g);
+      np = dsub(P[own0 + tid], dmul(lr, v));
+      sm[S::VEL + (cur ^ 1) * S::CH + tid] = v;
+#pragma unroll
+      for (int rk = 0; rk < G; ++rk) {
+        if (rk == cta) st_shared_f64(smem_u32(sm) + nxt_off, np);
+        else st_async_f64(peer[rk] + nxt_off, np, peerbar[rk] + (2 + par) * 8);
+      }
+    }
+    if (tid < S::NW * 32) {  // one "every g of this warp's parameters is finite" flag per owner warp
+      const int all_ok = __all_sync(0xffffffffu, ok);
+      if ((tid & 31) == 0) {
+        const uint32_t foff = (uint32_t)((S::OK + par * G * S::NW + cta * S::NW + (tid >> 5)) * sizeof(double));
+        const double fv = all_ok ? 1.0 : 0.0;
+#pragma unroll
+        for (int rk = 0; rk < G; ++rk) {
+          if (rk == cta) st_shared_f64(smem_u32(sm) + foff, fv);
+          else st_async_f64(peer[rk] + foff, fv, peerbar[rk] + (2 + par) * 8);
+        }
+      }
+    }
+    if (a.param_trace && owner) a.param_trace[(size_t)s * BT_P + own0 + tid] = np;
+    {
+      const uint32_t bar = smem_u32(&s_mbar[2 + par]);
+      if (tid == 0) mbar_arrive_expect_tx(bar, ag_bytes);
+      else mbar_arrive(bar);
     }
     BT_TICK(3)
-    if (!__syncthreads_and(ok)) {  // sgd_step raises before mutating (model.py:207-209)
+    mbar_wait(smem_u32(&s_mbar[2 + par]), (phases >> (2 + par)) & 1u, a.flags);
+    phases ^= 1u << (2 + par);
+    bool all = true;
+#pragma unroll
+    for (int w = 0; w < G * S::NW; ++w) all &= sm[S::OK + par * G * S::NW + w] != 0.0;
+    if (!all) {  // sgd_step raises before mutating (model.py:207-209): nobody commits this step
       if (cta == 0 && tid == 0) {
         a.flags[FLAG_STATUS] = ERR_NUMERIC;
         a.flags[FLAG_STEP] = s;
       }
       break;
     }
-    cur ^= 1;
-    if (a.param_trace && cta == 0 && tid < BT_P) a.param_trace[(size_t)s * BT_P + tid] = np;
     BT_TICK(4)
   }
   if (L.timing && tid == 0 && cta == 0) {
@@ -873,20 +931,19 @@ __global__ void __launch_bounds__(SpecShape<ET>::T) mlp_step_spec_kernel(const _
     L.timing[5] += (unsigned long long)s;
   }
 
-  // ---- epilogue -----------------------------------------------------------
+  // ---- epilogue: EST slots; each owner mirrors its chunk to every replica --
   cluster_barrier();
   for (int el = tid; el < S::EPC; el += S::T) {
     a.rng[e0 + el] = s_rng[el];
     a.stat_mean[e0 + el] = sm[S::MEAN + el];
     a.stat_count[e0 + el] = s_cnt[el];
   }
-  if (cta == 0) {  // engine.py:313-315
+  if (owner) {  // engine.py:313-315 (after a NumericError: the last committed step)
+    const int fin = s & 1;
     for (int x = 0; x < a.X; ++x) {
       double* rx = a.replicas + (size_t)x * 2 * BT_P;
-      for (int i = tid; i < BT_P; i += S::T) {
-        rx[i] = sm[S::PAR + cur * PAD_P + i];
-        rx[BT_P + i] = sm[S::VEL + cur * PAD_P + i];
-      }
+      rx[own0 + tid] = sm[S::PAR + fin * PAD_P + own0 + tid];
+      rx[BT_P + own0 + tid] = sm[S::VEL + fin * S::CH + tid];
     }
   }
 }
@@ -990,27 +1047,45 @@ static cudaError_t launch_k(const bt_mlp_args& a, const MlpLaunch& L, size_t sme
   return cudaGetLastError();
 }
 
-template <int ET, int F>
+template <int ET, int G, int F>
 static cudaError_t launch_spec(const bt_mlp_args& a, size_t smem, cudaStream_t stream, const MlpLaunch& L) {
-  using S = SpecShape<ET>;
+  using S = SpecShape<ET, G>;
+  auto kern = mlp_step_spec_kernel<ET, G, F>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(mlp_step_spec_kernel<ET, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  return launch_cluster(mlp_step_spec_kernel<ET, F>, a, smem, S::G, S::T, stream, L);
+  return launch_cluster(kern, a, smem, G, S::T, stream, L);
 }
 
-// Shared memory of the compact build, or 0 when it does not apply.
-template <int ET>
+// Shared memory of the compact build, or 0 when it does not fit.
+template <int ET, int G>
 static size_t spec_smem(const bt_mlp_args& a) {
-  using S = SpecShape<ET>;
-  if (a.est_per_cta != S::EPC) return 0;
+  using S = SpecShape<ET, G>;
   const size_t bytes = S::fixed_bytes() + sizeof(double) * (size_t)a.dataset_rows * BT_ROW +
                        (sizeof(double) + sizeof(int32_t)) * (size_t)a.K * S::R;
   return bytes <= SMEM_LIMIT ? bytes : 0;
+}
+
+template <int ET, int G>
+static bool try_spec(const bt_mlp_args& a, int fan, cudaStream_t stream, const MlpLaunch& L, cudaError_t* err) {
+  const size_t ss = spec_smem<ET, G>(a);
+  if (!ss) return false;
+  *err = fan ? launch_spec<ET, G, 2>(a, ss, stream, L) : launch_spec<ET, G, 0>(a, ss, stream, L);
+  return true;
+}
+
+// CTAs per cluster for the compact build (BT_SPEC_G overrides, for measurements).
+static int spec_g(int et) {
+  static int env = -1;
+  if (env < 0) {
+    const char* v = getenv("BT_SPEC_G");
+    env = v ? atoi(v) : 0;
+  }
+  if (env > 0) return env;
+  return et < 8 ? et : 8;
 }
 
 int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* timing) {
@@ -1023,22 +1098,19 @@ int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* ti
   const int fan = a.est_fanin_uniform - 1;  // every EST's batch variant, when the caller knows it
   if (a.fuse_reduce && a.B == 4 && a.E == a.E_total && !a.rows && a.dataset_rows > 0 && a.rank_override < 0 &&
       (fan == 0 || fan == 2) && fan == a.comm_fanin) {
-    size_t ss = 0;
-    cudaError_t err = cudaErrorNotSupported;
-    switch (a.E_total) {
-      case 4:
-        if ((ss = spec_smem<4>(a))) err = fan ? launch_spec<4, 2>(a, ss, stream, L) : launch_spec<4, 0>(a, ss, stream, L);
-        break;
-      case 8:
-        if ((ss = spec_smem<8>(a))) err = fan ? launch_spec<8, 2>(a, ss, stream, L) : launch_spec<8, 0>(a, ss, stream, L);
-        break;
-      case 16:
-        if ((ss = spec_smem<16>(a)))
-          err = fan ? launch_spec<16, 2>(a, ss, stream, L) : launch_spec<16, 0>(a, ss, stream, L);
-        break;
+    cudaError_t err = cudaSuccess;
+    bool ran = false;
+    const int g = spec_g(a.E_total);
+    switch (a.E_total * 16 + g) {
+      case 4 * 16 + 2: ran = try_spec<4, 2>(a, fan, stream, L, &err); break;
+      case 4 * 16 + 4: ran = try_spec<4, 4>(a, fan, stream, L, &err); break;
+      case 8 * 16 + 4: ran = try_spec<8, 4>(a, fan, stream, L, &err); break;
+      case 8 * 16 + 8: ran = try_spec<8, 8>(a, fan, stream, L, &err); break;
+      case 16 * 16 + 4: ran = try_spec<16, 4>(a, fan, stream, L, &err); break;
+      case 16 * 16 + 8: ran = try_spec<16, 8>(a, fan, stream, L, &err); break;
       default: break;
     }
-    if (ss) return err == cudaSuccess ? OK : ERR_CUDA;
+    if (ran) return err == cudaSuccess ? OK : ERR_CUDA;
   }
   cudaError_t err;
   switch (a.B) {
