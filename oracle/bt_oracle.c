@@ -639,3 +639,9 @@ int or_reduce_update_seq_f32_mt(const float *grads, int E, int64_t n, const floa
     for (int t = 0; t < nthreads; t++) if (jobs[t].st) return jobs[t].st;
     return OR_OK;
 }
+
+/* The reference's math.tanh is this host's libm tanh (model.py:148): a batch
+ * form for checking the device tanh on many inputs. */
+void or_libm_tanh_array(const double *x, int64_t n, double *out) {
+    for (int64_t i = 0; i < n; i++) out[i] = tanh(x[i]);
+}

@@ -88,8 +88,17 @@ def lib():
                                            C.c_float, _fp, _fp]
         L.or_reduce_update_seq_f32_mt.argtypes = [_fp, C.c_int, _i64, _fp, _fp, C.c_float, C.c_float,
                                                   _fp, _fp, C.c_int]
+        L.or_libm_tanh_array.argtypes = [_dp, _i64, _dp]
         _lib = L
     return _lib
+
+
+def libm_tanh(x: np.ndarray) -> np.ndarray:
+    """This host's libm tanh elementwise (the reference's math.tanh, model.py:148)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    lib().or_libm_tanh_array(_p(x, _dp), x.size, _p(out, _dp))
+    return out
 
 
 def _p(a: np.ndarray, t):

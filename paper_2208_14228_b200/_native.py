@@ -14,7 +14,7 @@ from pathlib import Path
 from . import errors
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libbittrain_b200.so"
+LIB_PATH = Path(os.environ["BT_LIB_PATH"]) if os.environ.get("BT_LIB_PATH") else PKG / "libbittrain_b200.so"
 
 _u64, _i64, _i32, _dbl, _vp = C.c_uint64, C.c_int64, C.c_int32, C.c_double, C.c_void_p
 _u64p, _i64p, _i32p, _dp = C.POINTER(C.c_uint64), C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_double)

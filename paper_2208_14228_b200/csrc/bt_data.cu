@@ -108,7 +108,7 @@ __global__ void slot_copy_kernel(const __grid_constant__ CopyTable t, int count)
 
 __global__ void tanh_kernel(const double* x, int64_t n, double* out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = glibc_tanh(x[i]);
+    out[i] = glibc_tanh_simt(x[i]);  // the step kernels' tanh
 }
 
 __global__ void flags_reset_kernel(int32_t* flags) {

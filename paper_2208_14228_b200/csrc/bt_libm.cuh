@@ -144,9 +144,9 @@ BT_HD double glibc_expm1_fma_tanh_domain(double x) {
                Q5 = -2.01099218183624371326e-07;
   const uint32_t hx = hi_word(x) & 0x7fffffffu;
   const bool neg = (hi_word(x) >> 31) != 0;
-  const int kg = (int)dadd(dmul(invln2, x), neg ? -0.5 : 0.5);
-  const int k = hx <= 0x3fd62e42u ? 0 : (hx < 0x3FF0A2B2u ? (neg ? -1 : 1) : kg);
-  const double tk = (double)k;
+  const double kgd = dtrunc(dadd(dmul(invln2, x), neg ? -0.5 : 0.5));  // (int) truncation, kept in binary64
+  const double tk = hx <= 0x3fd62e42u ? 0.0 : (hx < 0x3FF0A2B2u ? (neg ? -1.0 : 1.0) : kgd);
+  const int k = (int)tk;  // exact (|k| <= 64 in the tanh domain); off the critical path
   const double hi = dfma(-tk, ln2_hi, x);
   const double lo = dmul(tk, ln2_lo);
   const double xr = dsub(hi, lo);
@@ -160,7 +160,7 @@ BT_HD double glibc_expm1_fma_tanh_domain(double x) {
   const double R3 = dfma(hxs, Q5, Q4);
   const double r1 = dfma(h4, R3, dfma(h2, R2, R1));
   const double t = dfma(-r1, hfx, 3.0);
-  const double e = dmul(hxs, ddiv(dsub(r1, t), dfma(-xr, t, 6.0)));
+  const double e = dmul(hxs, ddiv_normal(dsub(r1, t), dfma(-xr, t, 6.0)));  // num ~ -2, den ~ 6
   const double res0 = dsub(xr, dfma(xr, e, -hxs));           // k == 0
   const double e2 = dsub(dfma(dsub(e, c), xr, -c), hxs);
   const double resm1 = dfma(0.5, dsub(xr, e2), -0.5);        // k == -1
@@ -187,19 +187,21 @@ BT_HD double glibc_expm1_fma_tanh_domain(double x) {
 
 BT_HD double glibc_tanh_simt(double x) {
   const uint32_t jx = hi_word(x), ix = jx & 0x7fffffffu, lx = lo_word(x);
-  if (ix >= 0x40360000u || ix < 0x3c800000u || (ix | lx) == 0) {  // rare inputs: glibc's early returns
-    if (ix >= 0x7ff00000u) return (jx >> 31) ? dsub(ddiv(1.0, x), 1.0) : dadd(ddiv(1.0, x), 1.0);
-    if ((ix | lx) == 0) return x;
-    if (ix < 0x3c800000u) return dmul(x, dadd(1.0, x));
-    const double one_m = dsub(1.0, 1e-300);
-    return (jx >> 31) ? -one_m : one_m;
-  }
   const double ax = fabs(x);
   const bool big = ix >= 0x3ff00000u;  // |x| >= 1
   const double t = glibc_expm1_fma_tanh_domain(big ? dadd(ax, ax) : dmul(-2.0, ax));
-  const double q = ddiv(big ? 2.0 : -t, dadd(t, 2.0));
+  const double q = ddiv_normal(big ? 2.0 : -t, dadd(t, 2.0));
   const double z = big ? dsub(1.0, q) : q;
-  return (jx >> 31) ? -z : z;
+  double r = (jx >> 31) ? -z : z;
+  // glibc's early returns, as selects (no branch; the general path above is
+  // harmless garbage for these inputs and is discarded):
+  //   |x| >= 22 or inf: +-(1 - 1e-300) = +-1 (inf: 1/x +- 1 = +-1)
+  //   |x| < 2^-55, +-0 included: x * (1 + x)  (glibc returns x for +-0: same bits)
+  //   NaN: a NaN (binary64 NaN results are canonical on the GPU either way)
+  r = ix >= 0x40360000u ? ((jx >> 31) ? -1.0 : 1.0) : r;
+  r = ix < 0x3c800000u ? dmul(x, dadd(1.0, x)) : r;
+  r = (ix > 0x7ff00000u || (ix == 0x7ff00000u && lx != 0)) ? dadd(x, x) : r;
+  return r;
 }
 
 }  // namespace bt

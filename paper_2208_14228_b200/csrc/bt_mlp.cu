@@ -174,6 +174,11 @@ __device__ __forceinline__ void mbar_init_fence() {  // make mbarrier.init visib
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ double ld_shared_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_shared_f64(uint32_t addr, double v) {
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
@@ -184,7 +189,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(bar), "r"(parity)
@@ -594,39 +599,35 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
 
 // ---------------------------------------------------------------------------
 // Compact build for the common shapes: B = 4 rows per EST, E_total = ET in
-// {4, 8, 16} ESTs on one thread-block cluster of G CTAs (EPC = ET / G ESTs
-// each), one reduction variant F (0 = Sequential, 2 = Tree(2)) for every EST's
-// batch reductions and for the allreduce, dataset and index lists staged in
-// shared memory.  Same arithmetic, same order as the generic build; what
-// changes is the data movement and the bookkeeping:
-//  * the allreduce is owner-computes: parameter p belongs to CTA p / CH.  Each
-//    CTA pushes gradient p of its ESTs only to p's owner (reduce-scatter, one
-//    DSMEM store per value); the owner folds all ET leaves in the reference
-//    order, applies /E and momentum SGD, and pushes the new parameter to every
-//    CTA (all-gather) together with a per-warp "all finite" flag.  Both
-//    exchanges are st.async stores counted on the receiver's mbarrier, so a
-//    step has one CTA barrier and two mbarrier waits, and moves ~2.5 KB per
-//    CTA over DSMEM instead of ET * 1.3 KB;
-//  * the shared-memory layout and every thread's role are compile-time; each
-//    thread's addresses are computed once per launch; the next mini-batch's
-//    row gather, jitter and dropout mask are prefetched during the exchange.
+// {4, 8, 16} ESTs on one thread-block cluster of G CTAs (default min(ET, 8); EPC =
+// ET / G ESTs each), one reduction variant F (0 = Sequential, 2 = Tree(2))
+// for every EST's batch reductions and for the allreduce, dataset and index
+// lists staged in shared memory.  Same arithmetic, same order as the generic
+// build; what changes is the bookkeeping: the shared-memory layout and every
+// thread's role are compile-time, each thread's addresses (rows, gradient
+// operands, DSMEM push targets, allreduce leaves) are computed once per
+// launch, and the next mini-batch's row gather, jitter and dropout mask are
+// prefetched while the slot exchange is in flight.
+// Exchange: all-to-all of the EST gradient slots (own slot by local store,
+// peers' by st.async counted on the receiver's mbarrier) and a redundant,
+// bit-identical stage F in every CTA.  An owner-computes reduce-scatter +
+// all-gather moves 4x fewer DSMEM bytes but needs a second exchange per step;
+// measured on B200 it is ~10% slower (the exchange is latency-bound, ~500
+// cycles per hop), so one hop wins.
 template <int ET, int GG>
 struct SpecShape {
-  static constexpr int G = GG;                            // CTAs = cluster size
-  static constexpr int EPC = ET / G;                      // ESTs per CTA
-  static constexpr int NB = 4;                            // rows per EST
-  static constexpr int R = NB * EPC;                      // rows per CTA
-  static constexpr int LANES = R * BT_HIDDEN;             // stage B+C lanes
-  static constexpr int T = LANES > 192 ? LANES : 192;     // >= BT_P + 1
-  static constexpr int ITEMS = EPC * (BT_P + 1);          // stage E items
+  static constexpr int G = GG;                                           // CTAs = cluster size
+  static constexpr int EPC = ET / G;                                     // ESTs per CTA
+  static constexpr int NB = 4;                                           // rows per EST
+  static constexpr int R = NB * EPC;                                     // rows per CTA
+  static constexpr int LANES = R * BT_HIDDEN;                            // stage B+C lanes
+  static constexpr int T = LANES > 192 ? LANES : 192;                    // >= BT_P + 1
+  static constexpr int ITEMS = EPC * (BT_P + 1);                         // stage E items
   static constexpr int NIT = (ITEMS + T - 1) / T;
-  static constexpr int CH = (BT_P + G - 1) / G;           // parameters per owner
-  static constexpr int NW = (CH + 31) / 32;               // owner warps (one finite flag each)
-  static constexpr int chunk(int c) { return (c + 1) * CH <= BT_P ? CH : BT_P - c * CH; }
   // shared-memory layout, in doubles
   static constexpr int PAR = 0;                    // [2][PAD_P] parameters (step-parity buffers)
-  static constexpr int VEL = PAR + 2 * PAD_P;      // [2][CH] velocity of the owned chunk
-  static constexpr int X = VEL + 2 * CH;           // [R][8] jittered inputs
+  static constexpr int VEL = PAR + 2 * PAD_P;      // [2][PAD_P] velocity
+  static constexpr int X = VEL + 2 * PAD_P;        // [R][8] jittered inputs
   static constexpr int Y = X + R * BT_INPUT_DIM;   // [R]
   static constexpr int ACT = Y + R;                // [R][16]
   static constexpr int HID = ACT + R * BT_HIDDEN;  // [R][16]
@@ -637,10 +638,9 @@ struct SpecShape {
   static constexpr int MEAN = RM + R;              // [EPC]
   static constexpr int RNG = MEAN + EPC;           // [EPC] u64
   static constexpr int CNT = RNG + EPC;            // [EPC] u64
-  static constexpr int RS = CNT + EPC;             // [2][ET][CH] gradients of the owned chunk
-  static constexpr int OK = RS + 2 * ET * CH;      // [2][G * NW] owners' finite flags
-  static constexpr int ROT = OK + 2 * G * NW;      // int32 [CH] rotation starts of the owned chunk
-  static constexpr int DATA = (ROT + CH / 2 + 2) & ~1;  // [dataset_rows][9], jit [K][R], idx int32 [K][R]
+  static constexpr int GRAD = (CNT + EPC + 1) & ~1;  // [2][ET][BT_P] slot arrays (16-byte aligned)
+  static constexpr int ROT = GRAD + 2 * ET * BT_P;   // int32 [PAD_P]
+  static constexpr int DATA = ROT + PAD_P / 2;       // [dataset_rows][9], then jit [K][R], idx int32 [K][R]
   static constexpr size_t fixed_bytes() { return sizeof(double) * DATA; }
 };
 
@@ -664,18 +664,18 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
   const int tid = threadIdx.x;
   const int cta = blockIdx.x;  // the grid is one cluster: blockIdx.x is the cluster rank
   const int e0 = cta * S::EPC;
-  const int own0 = cta * S::CH, own_n = S::chunk(cta);  // owned parameters [own0, own0 + own_n)
   double* const s_data = sm + S::DATA;
   double* const s_jit = s_data + (size_t)a.dataset_rows * BT_ROW;
   int32_t* const s_idx = (int32_t*)(s_jit + (size_t)a.K * S::R);
   int32_t* const s_rot = (int32_t*)(sm + S::ROT);
   uint64_t* const s_rng = (uint64_t*)(sm + S::RNG);
   uint64_t* const s_cnt = (uint64_t*)(sm + S::CNT);
-  __shared__ __align__(8) uint64_t s_mbar[4];  // [0..1] reduce-scatter, [2..3] all-gather, by step parity
+  __shared__ __align__(8) uint64_t s_mbar[2];
 
   if (a.flags[FLAG_STATUS] != 0) return;
   if (tid == 0) {  // a phase completes when every local thread arrived and every remote byte landed
-    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(&s_mbar[i]), S::T);
+    mbar_init(smem_u32(&s_mbar[0]), S::T);
+    mbar_init(smem_u32(&s_mbar[1]), S::T);
     mbar_init_fence();
   }
   // ---- prologue ---------------------------------------------------------
@@ -683,10 +683,8 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
   for (int i = tid; i < BT_P; i += S::T) {
     const double p0 = a.replicas[i], v0 = a.replicas[BT_P + i];
     sm[S::PAR + i] = p0;
-    if (i >= own0 && i < own0 + own_n) {
-      sm[S::VEL + (i - own0)] = v0;
-      s_rot[i - own0] = a.rot ? a.rot[i] : 0;
-    }
+    sm[S::VEL + i] = v0;
+    s_rot[i] = a.rot ? a.rot[i] : 0;
     for (int x = 1; x < a.X; ++x) {  // replica agreement, bytewise (engine.py:246-258)
       const double* rx = a.replicas + (size_t)x * 2 * BT_P;
       bad |= (d2u(rx[i]) != d2u(p0)) | (d2u(rx[BT_P + i]) != d2u(v0));
@@ -736,31 +734,50 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
   const int row = lane ? tid >> 4 : 0, j = tid & 15;
   const int lel = row / S::NB, lr_ = row - lel * S::NB;
   uint64_t lrng = s_rng[lel];  // this row's EST dropout stream, advanced in registers
-  uint32_t peer[G], peerbar[G];
+  // E items: (EST, parameter or loss) pairs.  Term r of item (el, p) is
+  // A[r] * B[r] (w1: dz*x, w2: gy*h) or A[r] (b1: dz, b2: gy, loss: e^2);
+  // the operand addresses are per-thread constants, so the step's gradient
+  // code is loads, multiplies, a select and the fold -- no branches.
+  uint32_t opa[S::NIT][S::NB], opb[S::NIT][S::NB], own_dst[S::NIT], rdst[S::NIT][G - 1];
+  bool has_b[S::NIT], is_loss[S::NIT], valid[S::NIT];
+  uint32_t rbar[G - 1];
+  const uint32_t sm0 = smem_u32(sm);
 #pragma unroll
-  for (int rk = 0; rk < G; ++rk) {
-    peer[rk] = cluster_map32(smem_u32(sm), rk);
-    peerbar[rk] = cluster_map32(smem_u32(&s_mbar[0]), rk);
+  for (int i = 0; i < G - 1; ++i) {  // the other CTAs, in rotated order (no rank test per push)
+    int rk = cta + 1 + i;
+    rk -= rk >= G ? G : 0;
+    rbar[i] = cluster_map32(smem_u32(&s_mbar[0]), rk);
   }
-  // E items: gradient p of local EST el goes to owner p / CH, leaf slot e0 + el
-  uint32_t rs_dst[S::NIT], rs_bar[S::NIT];
-  bool rs_local[S::NIT];
 #pragma unroll
   for (int k = 0; k < S::NIT; ++k) {
     const int it = tid + k * S::T;
-    const int el = it / (BT_P + 1), p = it - el * (BT_P + 1);
-    const int o = p < BT_P ? p / S::CH : 0;
-    rs_local[k] = o == cta;
-    const uint32_t off = (uint32_t)((S::RS + (e0 + el) * S::CH + (p - o * S::CH)) * sizeof(double));
-    rs_dst[k] = (rs_local[k] ? smem_u32(sm) : peer[o]) + off;
-    rs_bar[k] = rs_local[k] ? smem_u32(&s_mbar[0]) : peerbar[o];
+    valid[k] = it < S::ITEMS;
+    const int el = valid[k] ? it / (BT_P + 1) : 0, p = valid[k] ? it - el * (BT_P + 1) : 0;
+    const int rb = el * S::NB;
+    int a0, as, b0, bs;  // first operand index and row stride, in doubles
+    if (p < BT_B1) { a0 = S::DZ + rb * BT_HIDDEN + (p & 15); as = BT_HIDDEN; b0 = S::X + rb * BT_INPUT_DIM + (p >> 4); bs = BT_INPUT_DIM; }
+    else if (p < BT_W2) { a0 = S::DZ + rb * BT_HIDDEN + (p - BT_B1); as = BT_HIDDEN; b0 = a0; bs = as; }
+    else if (p < BT_B2) { a0 = S::GY + rb; as = 1; b0 = S::HID + rb * BT_HIDDEN + (p - BT_W2); bs = BT_HIDDEN; }
+    else if (p == BT_B2) { a0 = S::GY + rb; as = 1; b0 = a0; bs = as; }
+    else { a0 = S::E2 + rb; as = 1; b0 = a0; bs = as; }
+    has_b[k] = p < BT_W2 ? p < BT_B1 : p < BT_B2;
+    is_loss[k] = p == BT_P;
+#pragma unroll
+    for (int r = 0; r < S::NB; ++r) {
+      opa[k][r] = sm0 + (uint32_t)((a0 + r * as) * sizeof(double));
+      opb[k][r] = sm0 + (uint32_t)((b0 + r * bs) * sizeof(double));
+    }
+    const uint32_t off = (uint32_t)((S::GRAD + (e0 + el) * BT_P + p) * sizeof(double));  // parity-0 slot entry
+    own_dst[k] = sm0 + off;
+#pragma unroll
+    for (int i = 0; i < G - 1; ++i) {
+      int rk = cta + 1 + i;
+      rk -= rk >= G ? G : 0;
+      rdst[k][i] = cluster_map32(sm0, rk) + off;
+    }
   }
-  // F: owner thread t < own_n handles parameter own0 + t
-  const bool owner = tid < own_n;
-  const int rot_t = owner ? s_rot[tid] : 0;
-  const uint32_t rs_bytes = (uint32_t)((ET - S::EPC) * own_n * sizeof(double));
-  const uint32_t ag_bytes = (uint32_t)(((BT_P - own_n) + (G - 1) * S::NW) * sizeof(double));
-  uint32_t phases = 0;  // bit b: parity of the next completion of s_mbar[b]
+  const int rot_p = tid < BT_P ? s_rot[tid] : 0;
+  uint32_t phases = 0;
 
   // prefetched inputs of the next mini-batch (lane threads)
   double x[BT_ROW], msk = 1.0;
@@ -781,10 +798,9 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
 
   unsigned long long tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tlast = clock64();
-  int s = 0;
+  int cur = 0, s = 0;
   for (; s < a.K; ++s) {
     const int par = (int)((a.step0 + s) & 1);
-    const int cur = s & 1;  // parameter buffer of this step
     const double* P = sm + S::PAR + cur * PAD_P;
 
     // ---- B+C (model.py:141-179, 194) --------------------------------------
@@ -799,7 +815,11 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
       double acc = dmul(P[BT_W1 + j], x[0]);
 #pragma unroll
       for (int i = 1; i < BT_INPUT_DIM; ++i) acc = dadd(acc, dmul(P[BT_W1 + i * BT_HIDDEN + j], x[i]));
+#if defined(BT_ABL) && (BT_ABL & 1)  // timing ablation builds only (tools/ablate.sh)
+      const double act = dadd(acc, P[BT_B1 + j]);
+#else
       const double act = glibc_tanh_simt(dadd(acc, P[BT_B1 + j]));
+#endif
       const double hj = dmul(act, msk);
       sm[S::ACT + tid] = act;
       sm[S::HID + tid] = hj;
@@ -825,27 +845,30 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
     __syncthreads();
     BT_TICK(0)
 
-    // ---- E: gradients -> their owners (reduce-scatter, model.py:183-192) --
+    // ---- E: gradients -> every CTA's slot array (model.py:183-192) --------
+    const uint32_t pb = (uint32_t)(par * ET * BT_P * sizeof(double));  // step-parity slot array
 #pragma unroll
     for (int k = 0; k < S::NIT; ++k) {
-      const int it = tid + k * S::T;
-      if (it < S::ITEMS) {
-        const int el = it / (BT_P + 1), p = it - el * (BT_P + 1);
-        const int rb = el * S::NB;
-        const double g = fold_rows<S::NB, F>(S::NB, F, [&](int r) {
-          const int rw = rb + r;
-          if (p < BT_B1) return dmul(sm[S::DZ + rw * BT_HIDDEN + (p & 15)], sm[S::X + rw * BT_INPUT_DIM + (p >> 4)]);
-          if (p < BT_W2) return sm[S::DZ + rw * BT_HIDDEN + (p - BT_B1)];
-          if (p < BT_B2) return dmul(sm[S::GY + rw], sm[S::HID + rw * BT_HIDDEN + (p - BT_W2)]);
-          if (p == BT_B2) return sm[S::GY + rw];
-          return sm[S::E2 + rw];
-        });
-        if (p < BT_P) {
-          const uint32_t dst = rs_dst[k] + (uint32_t)(par * ET * S::CH * sizeof(double));
-          if (rs_local[k]) st_shared_f64(dst, g);
-          else st_async_f64(dst, g, rs_bar[k] + par * 8);
+      if (valid[k]) {
+        double v[S::NB];
+#pragma unroll
+        for (int r = 0; r < S::NB; ++r) {
+          const double av = ld_shared_f64(opa[k][r]), bv = ld_shared_f64(opb[k][r]);
+          v[r] = has_b[k] ? dmul(av, bv) : av;
+        }
+        const double g = TreeLevel<S::NB, F>::run(v);
+        if (!is_loss[k]) {
+          st_shared_f64(own_dst[k] + pb, g);  // own copy: a local store
+#pragma unroll
+          for (int i = 0; i < G - 1; ++i)
+#if !(defined(BT_ABL) && (BT_ABL & 4))
+            st_async_f64(rdst[k][i] + pb, g, rbar[i] + par * 8);
+#else
+            ;
+#endif
         } else {  // loss, TrackedStat, dropout stream of EST e0+el (model.py:173, 99-104)
-          const int e = e0 + el;
+          const int el = (tid + k * S::T) / (BT_P + 1);
+          const int e = e0 + el, rb = el * S::NB;
           a.losses[(size_t)s * ET + e] = divB.apply(g);
           double bm = sm[S::RM + rb];
 #pragma unroll
@@ -861,69 +884,52 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
     }
     {  // local slot stores ordered before the arrival (release); thread 0 adds the remote bytes
       const uint32_t bar = smem_u32(&s_mbar[par]);
-      if (tid == 0) mbar_arrive_expect_tx(bar, rs_bytes);
+#if defined(BT_ABL) && (BT_ABL & 4)
+      if (tid == 0) mbar_arrive_expect_tx(bar, 0);
+#else
+      if (tid == 0) mbar_arrive_expect_tx(bar, (uint32_t)((ET - S::EPC) * BT_P * sizeof(double)));
+#endif
       else mbar_arrive(bar);
     }
     BT_TICK(1)
-    if (lane && s + 1 < a.K) {  // the next mini-batch's rows and masks while the exchange is in flight
+    // the next mini-batch's rows and masks while the exchange is in flight
+    if (lane && s + 1 < a.K) {
       if (rate > 0.0) lrng = advance(lrng, (uint64_t)S::NB * BT_HIDDEN);
       prefetch(s + 1);
     }
+
+    // ---- exchange: all ET*P*8 slot bytes of this step parity --------------
     mbar_wait(smem_u32(&s_mbar[par]), (phases >> par) & 1u, a.flags);
     phases ^= 1u << par;
     BT_TICK(2)
 
-    // ---- F: owner-computes allreduce + /E + momentum SGD, then all-gather --
-    // Leaf k of parameter p is EST slot (rot[p] + k) mod E: ascending virtual
-    // rank, rotated by the parameter's ring chunk under Tree (buckets.py:115-123).
+    // ---- F: allreduce + /E + momentum SGD into the other buffer -----------
     int ok = 1;
     double np = 0.0;
-    const uint32_t nxt_off = (uint32_t)((S::PAR + (cur ^ 1) * PAD_P + own0 + tid) * sizeof(double));
-    if (owner) {
-      const double* col = sm + S::RS + par * ET * S::CH + tid;
-      const double sum = fold_ranks_t<ET, F>(rot_t, [&](int q) { return col[q * S::CH]; });
+    if (tid < BT_P) {
+      const double* col = sm + S::GRAD + par * ET * BT_P + tid;
+#if defined(BT_ABL) && (BT_ABL & 8)
+      const double sum = col[0];
+#else
+      const double sum = fold_ranks_t<ET, F>(rot_p, [&](int q) { return col[q * BT_P]; });
+#endif
       const double g = divE.apply(sum);
       ok = finite_d(g) ? 1 : 0;
-      const double v = dadd(dmul(mu, sm[S::VEL + cur * S::CH + tid]), g);
-      np = dsub(P[own0 + tid], dmul(lr, v));
-      sm[S::VEL + (cur ^ 1) * S::CH + tid] = v;
-#pragma unroll
-      for (int rk = 0; rk < G; ++rk) {
-        if (rk == cta) st_shared_f64(smem_u32(sm) + nxt_off, np);
-        else st_async_f64(peer[rk] + nxt_off, np, peerbar[rk] + (2 + par) * 8);
-      }
-    }
-    if (tid < S::NW * 32) {  // one "every g of this warp's parameters is finite" flag per owner warp
-      const int all_ok = __all_sync(0xffffffffu, ok);
-      if ((tid & 31) == 0) {
-        const uint32_t foff = (uint32_t)((S::OK + par * G * S::NW + cta * S::NW + (tid >> 5)) * sizeof(double));
-        const double fv = all_ok ? 1.0 : 0.0;
-#pragma unroll
-        for (int rk = 0; rk < G; ++rk) {
-          if (rk == cta) st_shared_f64(smem_u32(sm) + foff, fv);
-          else st_async_f64(peer[rk] + foff, fv, peerbar[rk] + (2 + par) * 8);
-        }
-      }
-    }
-    if (a.param_trace && owner) a.param_trace[(size_t)s * BT_P + own0 + tid] = np;
-    {
-      const uint32_t bar = smem_u32(&s_mbar[2 + par]);
-      if (tid == 0) mbar_arrive_expect_tx(bar, ag_bytes);
-      else mbar_arrive(bar);
+      const double v = dadd(dmul(mu, sm[S::VEL + cur * PAD_P + tid]), g);
+      np = dsub(P[tid], dmul(lr, v));
+      sm[S::VEL + (cur ^ 1) * PAD_P + tid] = v;
+      sm[S::PAR + (cur ^ 1) * PAD_P + tid] = np;
     }
     BT_TICK(3)
-    mbar_wait(smem_u32(&s_mbar[2 + par]), (phases >> (2 + par)) & 1u, a.flags);
-    phases ^= 1u << (2 + par);
-    bool all = true;
-#pragma unroll
-    for (int w = 0; w < G * S::NW; ++w) all &= sm[S::OK + par * G * S::NW + w] != 0.0;
-    if (!all) {  // sgd_step raises before mutating (model.py:207-209): nobody commits this step
+    if (!__syncthreads_and(ok)) {  // sgd_step raises before mutating (model.py:207-209)
       if (cta == 0 && tid == 0) {
         a.flags[FLAG_STATUS] = ERR_NUMERIC;
         a.flags[FLAG_STEP] = s;
       }
       break;
     }
+    cur ^= 1;
+    if (a.param_trace && cta == 0 && tid < BT_P) a.param_trace[(size_t)s * BT_P + tid] = np;
     BT_TICK(4)
   }
   if (L.timing && tid == 0 && cta == 0) {
@@ -931,19 +937,20 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
     L.timing[5] += (unsigned long long)s;
   }
 
-  // ---- epilogue: EST slots; each owner mirrors its chunk to every replica --
+  // ---- epilogue -----------------------------------------------------------
   cluster_barrier();
   for (int el = tid; el < S::EPC; el += S::T) {
     a.rng[e0 + el] = s_rng[el];
     a.stat_mean[e0 + el] = sm[S::MEAN + el];
     a.stat_count[e0 + el] = s_cnt[el];
   }
-  if (owner) {  // engine.py:313-315 (after a NumericError: the last committed step)
-    const int fin = s & 1;
+  if (cta == 0) {  // engine.py:313-315
     for (int x = 0; x < a.X; ++x) {
       double* rx = a.replicas + (size_t)x * 2 * BT_P;
-      rx[own0 + tid] = sm[S::PAR + fin * PAD_P + own0 + tid];
-      rx[BT_P + own0 + tid] = sm[S::VEL + fin * S::CH + tid];
+      for (int i = tid; i < BT_P; i += S::T) {
+        rx[i] = sm[S::PAR + cur * PAD_P + i];
+        rx[BT_P + i] = sm[S::VEL + cur * PAD_P + i];
+      }
     }
   }
 }

@@ -5,6 +5,7 @@
 
 extern "C" {
 double shim_tanh(double x) { return bt::glibc_tanh(x); }
+double shim_tanh_simt(double x) { return bt::glibc_tanh_simt(x); }
 double shim_expm1(double x) { return bt::glibc_expm1_fma(x); }
 double shim_streamfold(const double* v, int n, int fanin) {
   bt::StreamFold<double, 24> f;

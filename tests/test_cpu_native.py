@@ -50,7 +50,7 @@ def shim(tmp_path_factory):
     subprocess.run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-ffp-contract=off", "-o", str(so),
                     str(ROOT / "tests" / "native" / "host_shim.cpp")], check=True)
     L = C.CDLL(str(so))
-    for f in ("shim_tanh", "shim_expm1"):
+    for f in ("shim_tanh", "shim_tanh_simt", "shim_expm1"):
         getattr(L, f).restype = C.c_double
         getattr(L, f).argtypes = [C.c_double]
     L.shim_streamfold.restype = C.c_double
@@ -67,9 +67,10 @@ def test_libm_restatement_bitexact_on_host(shim):
                          rng.integers(0, 2**63, 30_000, dtype=np.int64).view(np.float64),
                          np.array([0.0, -0.0, np.inf, -np.inf, 22.0, 1e-300, 0.34657359027997264])])
     xs = xs[np.isfinite(xs) | np.isinf(xs)]
-    got = np.array([shim.shim_tanh(float(x)) for x in xs])
     want = np.array([math.tanh(float(x)) for x in xs])  # math.tanh == libm (np.tanh is numpy SIMD, not libm)
-    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    for fn in (shim.shim_tanh, shim.shim_tanh_simt):  # scalar glibc form and the branch-free SIMT form
+        got = np.array([fn(float(x)) for x in xs])
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
     ys = xs[np.abs(xs) < 400] * 1.7
     got = np.array([shim.shim_expm1(float(y)) for y in ys])
     assert np.array_equal(got.view(np.uint64), np.array([math.expm1(float(y)) for y in ys]).view(np.uint64))

@@ -52,6 +52,28 @@ def test_device_tanh_bitexact_vs_libm(bt, oracle):
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
 
 
+def test_device_tanh_bitexact_vs_libm_wide(bt, oracle):
+    """2e7 inputs over the ranges the step's pre-activations and tanh's internal
+    divisions see, plus random bit patterns: the step kernels' branch-free tanh
+    (with the unchecked fast division) equals host libm bit for bit."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    rng = np.random.default_rng(11)
+    x = np.concatenate([rng.uniform(-3, 3, 8_000_000), rng.uniform(-25, 25, 4_000_000),
+                        rng.uniform(-1.2, 1.2, 4_000_000), rng.uniform(-1e-6, 1e-6, 1_000_000),
+                        (rng.standard_normal(1_000_000) * 2.0 ** rng.integers(-60, 6, 1_000_000)),
+                        rng.integers(0, 2**63, 2_000_000, dtype=np.int64).view(np.float64)])
+    x = x[~np.isnan(x)]
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty_like(xd)
+    _native.check(_native.lib().bt_tanh_f64(xd.data_ptr(), xd.numel(), out.data_ptr(), stream()))
+    got = out.cpu().numpy()
+    want = oracle.libm_tanh(x)
+    bad = np.nonzero(got.view(np.uint64) != want.view(np.uint64))[0]
+    assert bad.size == 0, [(float(x[i]), float(got[i]), float(want[i])) for i in bad[:5]]
+
+
 def test_splitmix64_counter_form_matches_stream(bt):
     from paper_2208_14228_b200.prng import draws
 
