@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
 // {4, 8, 16} ESTs on one thread-block cluster of G CTAs (default min(ET, 8); EPC =
 // ET / G ESTs each), one reduction variant F (0 = Sequential, 2 = Tree(2))
 // for every EST's batch reductions and for the allreduce, dataset and index
-// lists staged in shared memory.  Same arithmetic, same order as the generic
+// lists (or, for an explicit global batch, this CTA's rows) staged in shared memory.  Same arithmetic, same order as the generic
 // build; what changes is the bookkeeping: the shared-memory layout and every
 // thread's role are compile-time, each thread's addresses (rows, gradient
 // operands, DSMEM push targets, allreduce leaves) are computed once per
@@ -664,8 +664,12 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
   const int tid = threadIdx.x;
   const int cta = blockIdx.x;  // the grid is one cluster: blockIdx.x is the cluster rank
   const int e0 = cta * S::EPC;
+  // sampler mode: the resident dataset + this launch's (index, jitter) per row;
+  // explicit-batch mode (split_by_rank rows, engine.py:261-268): this CTA's own
+  // rows of every mini-batch, index = position, jitter = 0 (rows are final)
+  const int64_t data_rows = a.rows ? (int64_t)a.K * S::R : a.dataset_rows;
   double* const s_data = sm + S::DATA;
-  double* const s_jit = s_data + (size_t)a.dataset_rows * BT_ROW;
+  double* const s_jit = s_data + (size_t)data_rows * BT_ROW;
   int32_t* const s_idx = (int32_t*)(s_jit + (size_t)a.K * S::R);
   int32_t* const s_rot = (int32_t*)(sm + S::ROT);
   uint64_t* const s_rng = (uint64_t*)(sm + S::RNG);
@@ -696,11 +700,21 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
     s_cnt[el] = a.stat_count[e0 + el];
     bad |= (a.est_fanin[e0 + el] != F) << 1;  // the launcher's variant hint must hold
   }
-  {
+  if (a.rows) {
+    for (int it = tid; it < a.K * S::R; it += S::T) {
+      const int s = it / S::R, rem = it - s * S::R;
+      const int el = rem / S::NB, r = rem - el * S::NB;
+      const double* src = a.rows + ((size_t)s * S::NB * ET + (size_t)r * ET + (e0 + el)) * BT_ROW;
+#pragma unroll
+      for (int i = 0; i < BT_ROW; ++i) s_data[(size_t)it * BT_ROW + i] = src[i];
+      s_idx[it] = it;
+      s_jit[it] = 0.0;
+    }
+  } else {
     const int64_t nd = a.dataset_rows * BT_ROW;
     for (int64_t i = tid; i < nd; i += S::T) s_data[i] = a.dataset[i];
   }
-  for (int it = tid; it < a.K * S::R; it += S::T) {
+  for (int it = tid; !a.rows && it < a.K * S::R; it += S::T) {
     const int s = it / S::R, rem = it - s * S::R;
     const int el = rem / S::NB, r = rem - el * S::NB;
     const int64_t gstep = a.step0 + s, epoch = gstep / a.spe, local = gstep % a.spe;
@@ -727,7 +741,7 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
   // ---- per-thread constants ----------------------------------------------
   const double rate = a.rate, lr = a.lr, mu = a.mu;
   const double keep = rate >= 1.0 ? 0.0 : ddiv(1.0, dsub(1.0, rate));  // model.py:150
-  const bool jit = a.jitter != 0.0;
+  const bool jit = !a.rows && a.jitter != 0.0;
   const IntDivisor divB = IntDivisor::of(S::NB), divH = IntDivisor::of(BT_HIDDEN), divE = IntDivisor::of(ET);
   // B+C lane: row = tid / 16 of this CTA, hidden unit j = tid % 16
   const bool lane = tid < S::LANES;
@@ -1071,7 +1085,8 @@ static cudaError_t launch_spec(const bt_mlp_args& a, size_t smem, cudaStream_t s
 template <int ET, int G>
 static size_t spec_smem(const bt_mlp_args& a) {
   using S = SpecShape<ET, G>;
-  const size_t bytes = S::fixed_bytes() + sizeof(double) * (size_t)a.dataset_rows * BT_ROW +
+  const size_t data_rows = a.rows ? (size_t)a.K * S::R : (size_t)a.dataset_rows;
+  const size_t bytes = S::fixed_bytes() + sizeof(double) * data_rows * BT_ROW +
                        (sizeof(double) + sizeof(int32_t)) * (size_t)a.K * S::R;
   return bytes <= SMEM_LIMIT ? bytes : 0;
 }
@@ -1103,7 +1118,7 @@ int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* ti
   if (a.fuse_reduce && !L.grads_smem && !L.cluster) return ERR_INPUT;  // too many ESTs for the fused path
   if (smem > SMEM_LIMIT) return ERR_INPUT;
   const int fan = a.est_fanin_uniform - 1;  // every EST's batch variant, when the caller knows it
-  if (a.fuse_reduce && a.B == 4 && a.E == a.E_total && !a.rows && a.dataset_rows > 0 && a.rank_override < 0 &&
+  if (a.fuse_reduce && a.B == 4 && a.E == a.E_total && (a.rows || a.dataset_rows > 0) && a.rank_override < 0 &&
       (fan == 0 || fan == 2) && fan == a.comm_fanin) {
     cudaError_t err = cudaSuccess;
     bool ran = false;
