@@ -408,10 +408,76 @@ def gen_ladder():
     dump("ladder.json", doc)
 
 
+def gen_cli():
+    """The reference's own command line (cli.py:38-78): run logs (JSON lines), checkpoint bytes, and
+    the reprocheck / bitdiff reports, byte for byte, for small configs and the train_d1 fixture."""
+    import contextlib
+    import io
+    import tempfile
+
+    import yaml
+    from bittrain import cli
+
+    def small(**over):
+        doc = {"seed": 7, "max_workers": 4, "micro_batch": 4, "dataset_size": 128, "minibatches": 12,
+               "determinism": "d1", "devices": {"gpu_fast": 2, "gpu_mid": 3},
+               "layout": [{"device": "gpu_fast"}, {"device": "gpu_fast"}]}
+        doc.update(over)
+        return doc
+
+    fixture = yaml.safe_load(open("/root/reference/pkg/fixtures/train_d1.yaml", encoding="utf-8"))
+    out = {"train": [], "reprocheck": []}
+    with tempfile.TemporaryDirectory() as td:
+        def run(argv):
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                rc = cli.main(argv)
+            return rc, buf.getvalue()
+
+        cases = [("small_fast2", small()), ("small_mid2", small(layout=[{"device": "gpu_mid"}] * 2)),
+                 ("small_fast1", small(layout=[{"device": "gpu_fast"}])),
+                 ("small_e2", small(max_workers=2, layout=[{"device": "gpu_fast"}])),
+                 ("small_dump", small(dump_params_every=4, minibatches=8)),
+                 ("train_d1_fixture", fixture)]
+        for name, doc in cases:
+            cfg_path, log_path, ck_path = f"{td}/{name}.yaml", f"{td}/{name}.log", f"{td}/{name}.ckpt"
+            with open(cfg_path, "w", encoding="utf-8") as fh:
+                yaml.safe_dump(doc, fh)
+            rc, text = run(["train", "--config", cfg_path, "--out", log_path, "--ckpt", ck_path])
+            out["train"].append({"name": name, "doc": doc, "rc": rc, "stdout": text,
+                                 "log": open(log_path, encoding="utf-8").read(),
+                                 "ckpt": open(ck_path, "rb").read().hex()})
+        logs = {c["name"]: f"{td}/{c['name']}.log" for c in out["train"]}
+        out["bitdiff"] = []
+        for a, b in (("small_fast2", "small_fast1"), ("small_fast2", "small_mid2"), ("small_fast2", "small_e2")):
+            rc, text = run(["bitdiff", logs[a], logs[b]])
+            out["bitdiff"].append({"a": a, "b": b, "rc": rc, "stdout": text})
+        matrix = {"steps": 12,
+                  "config": {"seed": 3, "max_workers": 4, "micro_batch": 4, "dataset_size": 128,
+                             "devices": {"gpu_fast": 2, "gpu_mid": 3}},
+                  "scenarios": [{"level": "S1", "run_a": {"layout": [{"device": "gpu_fast"}]},
+                                 "run_b": {"layout": [{"device": "gpu_fast"}]}},
+                                {"level": "S3", "run_a": {"layout": [{"device": "gpu_fast"}]},
+                                 "run_b": {"layout": [{"device": "gpu_mid"}]}},
+                                {"level": "S4", "run_a": {"layout": [{"device": "gpu_fast"}] * 4},
+                                 "run_b": {"layout": [{"device": "gpu_fast"}] * 2,
+                                           "restarts": [{"after_step": 6, "layout": [{"device": "gpu_fast"}] * 3}]}}]}
+        mpath = f"{td}/matrix.yaml"
+        with open(mpath, "w", encoding="utf-8") as fh:
+            yaml.safe_dump(matrix, fh)
+        for mode in ("d0", "d1", "d1d2"):
+            rc, text = run(["reprocheck", "--mode", mode, "--matrix", mpath])
+            out["reprocheck"].append({"mode": mode, "matrix": matrix, "rc": rc, "stdout": text})
+    dump("cli.json", out)
+
+
 if __name__ == "__main__":
     assert os.path.isdir(REF_SRC), "needs the read-only reference at /root/reference"
     if sys.argv[1:] == ["ladder"]:
         gen_ladder()
+        sys.exit(0)
+    if sys.argv[1:] == ["cli"]:
+        gen_cli()
         sys.exit(0)
     gen_prng()
     gen_reduction()
@@ -422,3 +488,4 @@ if __name__ == "__main__":
     gen_checkpoint()
     gen_global_batch()
     gen_ladder()
+    gen_cli()
