@@ -105,6 +105,16 @@ int bt_sgd_step_f64(const double *params_dev, const double *vel_dev, const doubl
                     double lr, double mu, double *params_out_dev, double *vel_out_dev, int32_t *flags_dev,
                     void *stream);
 
+/* ---------------- deterministic tensor-core GEMM (C3/C4 model stack) ------
+ * C[M][N] = A[M][K] * B[N][K]^T, bf16 inputs (K contiguous), fp32 accumulate
+ * in TMEM, C fp32 (out_dtype 0) or bf16 (1).  tcgen05 + TMA, one CTA per
+ * output tile, fixed K order: the bits depend only on the inputs and the
+ * shape, never on `grid` (0 = one CTA per SM) or the GPU.  Requires
+ * M % 128 == 0, N % 128 == 0, K % 64 == 0, 16-byte aligned pointers.
+ *                                         analogue of model.py:141-192's dense products */
+int bt_gemm_bf16_tn(const void *a_dev, const void *b_dev, void *c_dev, int32_t M, int32_t N, int32_t K,
+                    int32_t out_dtype, int32_t grid, void *stream);
+
 /* ---------------- L3 data ------------------------------------------------- */
 /* make_dataset(seed, n, dim): [n][dim+1], x then y                       sampling.py:24-35 */
 int bt_make_dataset(uint64_t seed, int64_t n, int32_t dim, double *out_dev, void *stream);

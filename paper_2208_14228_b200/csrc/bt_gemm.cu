@@ -1,0 +1,328 @@
+// bt_gemm.cu -- deterministic bf16 GEMM on the 5th-generation tensor cores.
+//
+// C[M][N] = A[M][K] * B[N][K]^T   (A, B bf16 K-contiguous -- the nn.Linear
+// layout x @ W^T; C fp32 or bf16; fp32 accumulation in TMEM).
+//
+// SURVEY.md §8f row 2 / north_star "deterministic model kernels": the dense
+// layers of the C3/C4 model stack (ResNet-18, BERT-base) run as tcgen05
+// kernels whose result is a pure function of the inputs:
+//   * every C tile is owned by exactly one CTA (no split-K, no atomics);
+//   * its K loop runs in ascending order, 16-wide UMMA steps in ascending
+//     order, accumulating into one TMEM tile;
+// so the bits do not depend on the grid size, the SM count, the tile
+// schedule or the GPU count -- the property the elastic step needs (an EST's
+// gradients must not change when it moves to another GPU).
+//
+// Structure (one CTA per SM, persistent, static round-robin tile schedule):
+//   warp 0   TMA producer: A/B k-blocks (128B swizzle) into a STAGES-deep
+//            shared-memory ring (full/empty mbarriers);
+//   warp 1   TMEM allocator + MMA issuer: one elected thread issues
+//            tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN, K=16) and
+//            tcgen05.commit's the stage back to the producer; two TMEM
+//            accumulators (2 x BN fp32 columns) so the epilogue of tile i
+//            overlaps the MMAs of tile i+1;
+//   warps 2-5 epilogue: tcgen05.ld 32 lanes x 32 columns -> registers ->
+//            st.global (row-contiguous 128 B per thread).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bt_common.cuh"
+
+namespace bt {
+namespace gemm {
+
+constexpr int BM = 128, BK = 64, UK = 16;  // tile M, k-block (128 B of bf16), UMMA K
+constexpr int THREADS = 192;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Bounded wait: a pipeline bug traps (a launch error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity))
+    if (clock64() - t0 > (1ll << 33)) __trap();
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(map), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, int acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// K-major, 128-byte-swizzled operand tile: rows of 64 bf16 (128 B), 8-row
+// swizzle atoms 1024 B apart.  UMMA shared-memory descriptor (sm_100):
+// start>>4 [0,14), LBO>>4 [16,30) = 1 (unused for swizzled K-major),
+// SBO>>4 [32,46) = 1024>>4, version [46,48) = 1, base offset 0,
+// layout type [61,64) = 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// Instruction descriptor: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
+// both K-major, N>>3 at [17,23), M>>4 at [24,29).
+template <int BN>
+__device__ __forceinline__ constexpr uint32_t instr_desc() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int BAR = STAGES * STAGE;  // full[S], empty[S], tfull[2], tempty[2], tmem addr
+  static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
+};
+
+template <int BN, int STAGES, bool OUT_BF16>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                        void* __restrict__ c, int M, int N, int K) {
+  using L = Smem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;  // SW128 tiles need 1024-byte alignment
+  uint8_t* const gbase = smem_raw + (base - raw);
+  const uint32_t bar0 = base + L::BAR;
+  auto full = [&](int s) { return bar0 + 8u * s; };
+  auto empty = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto tfull = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
+  auto tempty = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
+  uint32_t* const tmem_slot = (uint32_t*)(gbase + L::BAR + (2 * STAGES + 4) * 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = M / BM, nt = N / BN, kb_n = K / BK;
+  const int tiles = mt * nt;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), 4);  // one arrival per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // 2 x BN fp32 accumulator columns (power of two >= 32)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(2 * BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer ------------------------------------------------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(empty(stage), phase ^ 1u);
+          const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
+          mbar_arrive_expect_tx(full(stage), L::STAGE);
+          tma_load_2d(sa, &map_a, kb * BK, m0, full(stage));
+          tma_load_2d(sb, &map_b, kb * BK, n0, full(stage));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer --------------------------------------------------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = instr_desc<BN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int acc = i & 1;
+        mbar_wait(tempty(acc), ((i >> 1) & 1) ^ 1u);  // the epilogue drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(full(stage), phase);
+          tc_fence_after();
+          const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
+          const uint64_t da = kmajor_sw128_desc(sa), db = kmajor_sw128_desc(sb);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)  // +32 B per UMMA step inside the swizzled 128 B row
+            tc_mma(d, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (kb | k) != 0);
+          tc_commit(empty(stage));  // frees the smem stage when these MMAs complete
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        tc_commit(tfull(acc));  // accumulator complete
+      }
+    }
+  } else {
+    // ---- epilogue: TMEM -> registers -> global -------------------------------
+    const int lg = warp & 3;  // TMEM lane group this warp may access (lanes 32*lg ...)
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int acc = i & 1;
+      const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      mbar_wait(tfull(acc), (i >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + lg * 32 + lane;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * BN + cc);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (OUT_BF16) {
+          uint4* dst = (uint4*)((__nv_bfloat16*)c + (size_t)row * N + n0 + cc);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t w[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const __nv_bfloat162 b2 =
+                  __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * h]), __uint_as_float(v[q * 8 + 2 * h + 1]));
+              w[h] = *(const uint32_t*)&b2;
+            }
+            dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        } else {
+          uint4* dst = (uint4*)((float*)c + (size_t)row * N + n0 + cc);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty(acc));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN) : "memory");
+  }
+}
+
+}  // namespace gemm
+
+// ---------------------------------------------------------------- launcher
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)p;
+  }
+  return fn;
+}
+
+// rows x K bf16, K contiguous; box = box_rows x 64 (128 B), 128-byte swizzle
+static bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)gemm::BK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, int STAGES, bool OUT_BF16>
+static int launch_gemm(const void* a, const void* b, void* c, int M, int N, int K, int grid, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, a, M, K, gemm::BM) || !make_map(&mb, b, N, K, BN)) return ERR_CUDA;
+  auto kern = gemm::gemm_bf16_tn_kernel<BN, STAGES, OUT_BF16>;
+  const int smem = gemm::Smem<BN, STAGES>::TOTAL + 1024;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return ERR_CUDA;
+    attr = true;
+  }
+  const int tiles = (M / gemm::BM) * (N / BN);
+  if (grid <= 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = sms;
+  }
+  if (grid > tiles) grid = tiles;
+  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, c, M, N, K);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+
+// tile N = 256 when N allows it, else 128 (both deterministic, same per-element order)
+int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int M, int N, int K, int out_bf16, int grid,
+                        cudaStream_t s) {
+  if (N % 256 == 0)
+    return out_bf16 ? launch_gemm<256, 4, true>(a, b, c, M, N, K, grid, s)
+                    : launch_gemm<256, 4, false>(a, b, c, M, N, K, grid, s);
+  return out_bf16 ? launch_gemm<128, 6, true>(a, b, c, M, N, K, grid, s)
+                  : launch_gemm<128, 6, false>(a, b, c, M, N, K, grid, s);
+}
+
+}  // namespace bt

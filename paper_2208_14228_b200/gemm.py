@@ -1,0 +1,35 @@
+"""Deterministic tensor-core GEMM (csrc/bt_gemm.cu) -- the dense-layer brick of
+the C3/C4 model stack.
+
+`gemm_bf16(a, b)` = a @ b.T for bf16 `a` [M, K] and `b` [N, K] (the nn.Linear
+layout), fp32 accumulation on the tcgen05 tensor cores, fp32 or bf16 out.
+One CTA owns each output tile and walks K in ascending order, so the result's
+bits depend only on the inputs and the shape -- not on the grid size, the SM
+count or the GPU: an EST's gradients do not change when it is remapped.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native
+from .device import require_cuda, stream
+from .errors import InputError
+
+
+def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype = torch.float32, grid: int = 0) -> torch.Tensor:
+    require_cuda()
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or not (a.is_cuda and b.is_cuda):
+        raise InputError("gemm_bf16 takes CUDA bfloat16 tensors")
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[1]:
+        raise InputError(f"gemm_bf16 shapes {tuple(a.shape)} x {tuple(b.shape)}^T")
+    if out_dtype not in (torch.float32, torch.bfloat16):
+        raise InputError("out_dtype must be float32 or bfloat16")
+    a, b = a.contiguous(), b.contiguous()
+    M, K = a.shape
+    N = b.shape[0]
+    c = torch.empty((M, N), dtype=out_dtype, device=a.device)
+    _native.check(_native.lib().bt_gemm_bf16_tn(a.data_ptr(), b.data_ptr(), c.data_ptr(), M, N, K,
+                                                 1 if out_dtype == torch.bfloat16 else 0, grid, stream()),
+                  "gemm_bf16")
+    return c

@@ -1,0 +1,68 @@
+"""Deterministic tcgen05 GEMM (csrc/bt_gemm.cu) vs a float64 reference (needs a B200).
+
+Numerics: bf16 inputs, fp32 accumulation -> |C - C64| <= K * 2^-23 * sum_k |a_ik b_jk|
+(the fp32-accumulation bound, stated here as the test tolerance).  Determinism:
+bit-identical across repeats and across grid sizes (1 CTA ... one per SM),
+which is the property the elastic step needs from its model kernels.
+"""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(128, 128, 64), (256, 384, 512), (512, 512, 1024), (384, 1024, 768), (1024, 256, 4096)]
+
+
+@pytest.fixture(scope="module")
+def gemm():
+    assert torch.cuda.is_available()
+    from paper_2208_14228_b200.gemm import gemm_bf16
+
+    return gemm_bf16
+
+
+def _inputs(M, N, K, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    a = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    b = (torch.randn(N, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    return a, b
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_gemm_matches_float64(gemm, M, N, K):
+    a, b = _inputs(M, N, K, M + N + K)
+    c = gemm(a, b)
+    ref = a.double() @ b.double().T
+    bound = K * 2.0 ** -23 * (a.double().abs() @ b.double().abs().T)
+    err = (c.double() - ref).abs()
+    assert bool((err <= bound + 1e-30).all()), float((err / (bound + 1e-30)).max())
+    # and it agrees with cuBLAS (torch) to fp32-accumulation accuracy
+    cub = torch.matmul(a.float(), b.float().T)
+    assert bool(((c - cub).abs().double() <= 2 * bound + 1e-30).all())
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 512, 1024), (384, 1024, 768)])
+def test_gemm_bitwise_deterministic_across_grids(gemm, M, N, K):
+    a, b = _inputs(M, N, K, 7)
+    ref = gemm(a, b)
+    for grid in (0, 1, 3, 7, 37, 148):
+        c = gemm(a, b, grid=grid)
+        assert torch.equal(c.view(torch.int32), ref.view(torch.int32)), grid
+
+
+def test_gemm_bf16_output_is_rounded_fp32(gemm):
+    a, b = _inputs(256, 512, 640, 3)
+    c32 = gemm(a, b)
+    c16 = gemm(a, b, out_dtype=torch.bfloat16)
+    assert torch.equal(c16.view(torch.int16), c32.to(torch.bfloat16).view(torch.int16))
+
+
+def test_gemm_rejects_bad_shapes(gemm):
+    from paper_2208_14228_b200.errors import InputError
+
+    a, b = _inputs(128, 128, 64, 1)
+    with pytest.raises(InputError):
+        gemm(a[:, :32].contiguous(), b[:, :32].contiguous())
+    with pytest.raises(InputError):
+        gemm(a[:100].contiguous(), b)
