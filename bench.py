@@ -14,7 +14,8 @@ dataset, d1, Tree(2) device kind, momentum SGD; a "step" is one mini-batch.
   launch's global batches (split_by_rank rows) are copied from pinned host
   memory and its per-EST losses copied back inside the timed span.
 * roofline -- the step kernel (latency-bound: 32 samples/step), plus the
-  deterministic reducer (bt_reduce.cu, C5 shape) measured against HBM.
+  deterministic reducer (bt_reduce.cu, C5 shape) measured against HBM, and the
+  deterministic tcgen05 GEMM (bt_gemm.cu, 8192^3 bf16) against the tensor peak.
 * cpu_baseline -- the CPU oracle (a C restatement of the reference) on a
   bounded sample of the same workload, on this box's host cores.
 N > 1 (torchrun): the 8 ESTs are split into contiguous rank blocks; each rank
@@ -303,6 +304,44 @@ def bench_reducer(flush, peaks, E=8, S_MB=256, iters=10):
             "variants": {k: {kk: round(vv, 4) for kk, vv in d.items()} for k, d in out.items()}}
 
 
+def bench_gemm(flush, peaks, M=8192, N=8192, K=8192, iters=10):
+    """SURVEY §8f row 2 brick: the deterministic tcgen05 GEMM (bt_gemm.cu) at 8192^3 bf16 -> bf16,
+    against the measured bf16 tensor peak, with cuBLAS (torch.matmul) on the same shape beside it."""
+    from paper_2208_14228_b200.gemm import gemm_bf16
+
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    s = torch.cuda.current_stream()
+
+    def med(fn):
+        for _ in range(2):
+            fn()
+        times = []
+        for _ in range(iters):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fn()
+            e1.record(s)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        return statistics.median(times)
+
+    ms = med(lambda: gemm_bf16(a, b, torch.bfloat16))
+    ms_cublas = med(lambda: torch.matmul(a, b.T))
+    again = gemm_bf16(a, b, torch.bfloat16, grid=37)  # bits independent of the grid (determinism)
+    same = bool(torch.equal(gemm_bf16(a, b, torch.bfloat16).view(torch.int16), again.view(torch.int16)))
+    fl = 2.0 * M * N * K
+    del a, b, again
+    torch.cuda.empty_cache()
+    tf = fl / ms / 1e9
+    return {"kernel": "gemm_bf16_tn_kernel<256,4,bf16> (bt_gemm.cu: tcgen05 + TMA, 1 CTA per tile, fixed K order)",
+            "shape": [M, N, K], "bound": "tensor", "achieved": round(tf, 1), "peak": peaks["bf16_tflops"],
+            "unit": "TFLOP/s", "frac": round(tf / peaks["bf16_tflops"], 4), "ms": round(ms, 4),
+            "traffic": ncu_traffic("gemm_bf16_tn_kernel"), "cublas_tflops": round(fl / ms_cublas / 1e9, 1),
+            "grid_invariant_bits": same}
+
+
 def cpu_baseline(seconds: float, threads: int = 1):
     """The CPU oracle (C restatement of the reference) on the same C2 workload, bounded in time."""
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -428,8 +467,10 @@ def main():
     value = args.steps * SAMPLES_PER_STEP / (ms / 1e3)
     e2e = args.steps * SAMPLES_PER_STEP / (ms_e2e / 1e3)
     reducer = None
+    gemm = None
     if not args.no_reducer and rank == 0:
         reducer = bench_reducer(flush, peaks)
+        gemm = bench_gemm(flush, peaks)
     clk = clocks.stop()
 
     # Roofline of the step kernel: algorithmic HBM bytes per mini-batch = the 32 rows read
@@ -458,6 +499,8 @@ def main():
         line["config"]["exchange"] = exchange
     if reducer is not None:
         line["reducer"] = reducer
+    if gemm is not None:
+        line["gemm"] = gemm
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         v, steps, el, run = cpu_baseline(args.cpu_seconds)
         sys.path.insert(0, str(ROOT / "oracle"))

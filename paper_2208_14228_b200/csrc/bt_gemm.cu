@@ -103,6 +103,20 @@ __device__ __forceinline__ constexpr uint32_t instr_desc() {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
+// Tile t -> (m0, n0): groups of GROUP_M row-blocks walked column by column, so
+// one wave of CTAs touches GROUP_M A row-blocks and a few B column-blocks
+// (L2-resident) instead of streaming A once per B column.  The order only
+// affects which CTA computes a tile, never a tile's bits.
+constexpr int GROUP_M = 16;
+template <int BN>
+__device__ __forceinline__ void tile_coords_bn(int t, int mt, int nt, int* m0, int* n0) {
+  const int per_group = GROUP_M * nt;
+  const int g = t / per_group, r = t - g * per_group;
+  const int gm = min(GROUP_M, mt - g * GROUP_M);  // rows in this (possibly short) last group
+  *m0 = (g * GROUP_M + r % gm) * BM;
+  *n0 = (r / gm) * BN;
+}
+
 template <int BN, int STAGES>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
@@ -129,6 +143,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = M / BM, nt = N / BN, kb_n = K / BK;
+  auto tile_coords = [](int t, int mt_, int nt_, int* m0, int* n0) { tile_coords_bn<BN>(t, mt_, nt_, m0, n0); };
   const int tiles = mt * nt;
 
   if (warp == 0 && lane == 0) {
@@ -161,7 +176,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+        int m0, n0;
+        tile_coords(t, mt, nt, &m0, &n0);
         for (int kb = 0; kb < kb_n; ++kb) {
           mbar_wait(empty(stage), phase ^ 1u);
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
@@ -210,7 +226,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int acc = i & 1;
-      const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      int m0, n0;
+      tile_coords(t, mt, nt, &m0, &n0);
       mbar_wait(tfull(acc), (i >> 1) & 1);
       tc_fence_after();
       const int row = m0 + lg * 32 + lane;

@@ -12,9 +12,11 @@ from paper_2208_14228_b200.gemm import gemm_bf16  # noqa: E402
 
 SHAPES = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]] or [
     (8192, 8192, 8192), (4096, 4096, 4096), (32768, 768, 768), (32768, 3072, 768), (32768, 768, 3072)]
+ITERS = 3 if len(sys.argv) > 1 else 20
 
 
-def timeit(fn, iters=20):
+def timeit(fn, iters=None):
+    iters = iters or ITERS
     for _ in range(3):
         fn()
     torch.cuda.synchronize()

@@ -13,4 +13,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:mlp_
   python bench.py --steps 64 --warmup 32 --cpu-seconds 0 --no-reducer > $O/ncu_mlp.out 2>&1; echo mlp_rc=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:reduce_fast -s 2 -c 1 -f -o $O/prof_reduce_$tag \
   python bench.py --steps 64 --warmup 32 --cpu-seconds 0 > $O/ncu_red.out 2>&1; echo red_rc=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16 -s 2 -c 1 -f -o $O/prof_gemm_$tag \
+  python tools/gemm_bench.py 8192,8192,8192 > $O/ncu_gemm.out 2>&1; echo gemm_rc=$?
 cat $O/bench.json; tail -3 $O/bench.err

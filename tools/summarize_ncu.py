@@ -58,14 +58,15 @@ KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__shared_mem_per_block_dynamic"]
 
 
-def summarize(rep, name):
+def summarize(rep, name, extra=()):
     if not rep.exists():
         return None
     recs = raw(rep)
     lines = [f"# ncu --set full summary of {rep.name}", ""]
     traffic = []
     for d in recs:
-        for k in KEYS:
+        keys = KEYS + sorted(k for k in d if any(x in k for x in extra) and "pct" in k)
+        for k in keys:
             if k in d:
                 v, u = d[k]
                 lines.append(f"{k:70s} {v} {u}")
@@ -86,7 +87,9 @@ PROF.mkdir(exist_ok=True)
 launches()
 t_mlp = summarize(OUT / f"prof_mlp_{tag}.ncu-rep", "ncu_mlp_step")
 t_red = summarize(OUT / f"prof_reduce_{tag}.ncu-rep", "ncu_reducer")
+t_gemm = summarize(OUT / f"prof_gemm_{tag}.ncu-rep", "ncu_gemm", extra=("pipe_tensor", "pipe_tc", "tmem", "utc"))
 traffic = {"mlp_step_kernel": t_mlp[0] if t_mlp else None, "reduce_fast_kernel": t_red[0] if t_red else None,
+           "gemm_bf16_tn_kernel": t_gemm[0] if t_gemm else None,
            "source": f"profiles/{tag}_ncu_*.txt (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"}
 (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
 print(json.dumps(traffic))
