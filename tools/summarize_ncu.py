@@ -31,11 +31,16 @@ def launches():
         agg[name][0] += 1
         agg[name][1] += float(r[v_i].replace(",", ""))
     tot = sum(v[1] for v in agg.values())
+    setup = ("jitter_gather", "make_dataset", "init_random", "flags_reset", "at::", "dropout_mask")
+    step_tot = sum(v[1] for k, v in agg.items() if not any(x in k for x in setup)) or 1.0
     lines = [f"# ncu launch list ({path.name}): gpu__time_duration.sum per kernel, --clock-control none",
-             f"# cold-cache, serialised launches: compare SHARES, not absolute times", "",
-             f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'share':>7s}"]
+             f"# cold-cache, serialised launches: compare SHARES, not absolute times",
+             f"# 'setup' = input generation / buffer fills outside the timed spans (the e2e leg builds its",
+             f"# host batches with one jitter_gather launch per mini-batch before timing)", "",
+             f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'share':>7s} {'of step':>8s}"]
     for name, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        lines.append(f"{name[:70]:70s} {n:8d} {t / 1e3:12.1f} {t / tot * 100:6.1f}%")
+        tag = "   setup" if any(x in name for x in setup) else f"{t / step_tot * 100:7.1f}%"
+        lines.append(f"{name[:70]:70s} {n:8d} {t / 1e3:12.1f} {t / tot * 100:6.1f}% {tag}")
     (PROF / f"{tag}_launches.txt").write_text("\n".join(lines) + "\n")
     return agg
 
