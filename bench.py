@@ -335,7 +335,7 @@ def bench_gemm(flush, peaks, M=8192, N=8192, K=8192, iters=10):
     del a, b, again
     torch.cuda.empty_cache()
     tf = fl / ms / 1e9
-    return {"kernel": "gemm_bf16_tn_kernel<256,4,bf16> (bt_gemm.cu: tcgen05 + TMA, 1 CTA per tile, fixed K order)",
+    return {"kernel": "gemm_bf16_tn_pair_kernel<6,bf16> (bt_gemm.cu: tcgen05 cta_group::2 + TMA, 256x256 tile per CTA pair, fixed K order)",
             "shape": [M, N, K], "bound": "tensor", "achieved": round(tf, 1), "peak": peaks["bf16_tflops"],
             "unit": "TFLOP/s", "frac": round(tf / peaks["bf16_tflops"], 4), "ms": round(ms, 4),
             "traffic": ncu_traffic("gemm_bf16_tn_kernel"), "cublas_tflops": round(fl / ms_cublas / 1e9, 1),

@@ -27,6 +27,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "bt_common.cuh"
 
@@ -276,6 +277,223 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair form (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256 x 256 tile with M = 256 UMMAs issued by the leader.  Each CTA loads its
+// 128 rows of A and 128 rows of B (half the operand traffic of two 1-CTA
+// tiles); both CTAs' TMA bytes complete on the leader's full barrier; the
+// leader's commits multicast to both CTAs' empty / accumulator barriers; each
+// CTA drains its own 128 TMEM lanes.  Same per-element order as the 1-CTA
+// kernel (one tile owner, ascending K), so the same determinism guarantee.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                                 uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, int acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {  // arrive on this offset in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t local, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(local), "r"(rank));
+  return out;
+}
+
+constexpr int PAIR_BN = 256, PAIR_M = 256;
+
+template <int STAGES>
+struct PairSmem {
+  static constexpr int A_BYTES = BM * BK * 2, B_BYTES = (PAIR_BN / 2) * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int BAR = STAGES * STAGE;
+  static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
+};
+
+template <int STAGES, bool OUT_BF16>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                             void* __restrict__ c, int M, int N, int K) {
+  using L = PairSmem<STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* const gbase = smem_raw + (base - raw);
+  const uint32_t bar0 = base + L::BAR;
+  auto full = [&](int s) { return bar0 + 8u * s; };
+  auto empty = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto tfull = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
+  auto tempty = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
+  uint32_t* const tmem_slot = (uint32_t*)(gbase + L::BAR + (2 * STAGES + 4) * 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int mt = M / PAIR_M, nt = N / PAIR_BN, kb_n = K / BK;
+  const int tiles = mt * nt;
+  const int pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
+  auto coords = [&](int t, int* m0, int* n0) {  // grouped raster, as the 1-CTA kernel
+    constexpr int GM = GROUP_M / 2;
+    const int per_group = GM * nt;
+    const int g = t / per_group, r = t - g * per_group;
+    const int gm = min(GM, mt - g * GM);
+    *m0 = (g * GM + r % gm) * PAIR_M;
+    *n0 = (r / gm) * PAIR_BN;
+  };
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full(s), 1);   // leader: its expect_tx arrival; the bytes come from both CTAs
+      mbar_init(empty(s), 1);  // each CTA: the leader's multicast commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), 8);  // leader: 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(2 * PAIR_BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs: own A half, own B half) ----
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < tiles; t += pairs) {
+        int m0, n0;
+        coords(t, &m0, &n0);
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(empty(stage), phase ^ 1u);
+          const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
+          const uint32_t lb = full(stage) & 0xFEFFFFFFu;  // the leader CTA's barrier
+          if (leader) mbar_arrive_expect_tx(full(stage), 2 * L::STAGE);
+          tma_load_2d_pair(sa, &map_a, kb * BK, m0 + (int)rank * BM, lb);
+          tma_load_2d_pair(sb, &map_b, kb * BK, n0 + (int)rank * (PAIR_BN / 2), lb);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ---- MMA issuer (leader only) ----
+      constexpr uint32_t idesc =
+          (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(PAIR_BN >> 3) << 17) | ((uint32_t)(PAIR_M >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int i = 0;
+      for (int t = pair; t < tiles; t += pairs, ++i) {
+        const int acc = i & 1;
+        mbar_wait(tempty(acc), ((i >> 1) & 1) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(acc * PAIR_BN);
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(full(stage), phase);
+          tc_fence_after();
+          const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
+          const uint64_t da = kmajor_sw128_desc(sa), db = kmajor_sw128_desc(sb);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            tc_mma_pair(d, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (kb | k) != 0);
+          tc_commit_pair(empty(stage));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        tc_commit_pair(tfull(acc));
+      }
+    }
+  } else {  // ---- epilogue (both CTAs: own 128 rows) ----
+    const int lg = warp & 3;
+    const uint32_t leader_tempty0 = map_to_rank(tempty(0), 0), leader_tempty1 = map_to_rank(tempty(1), 0);
+    int i = 0;
+    for (int t = pair; t < tiles; t += pairs, ++i) {
+      const int acc = i & 1;
+      int m0, n0;
+      coords(t, &m0, &n0);
+      mbar_wait(tfull(acc), (i >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + (int)rank * BM + lg * 32 + lane;
+#pragma unroll 1
+      for (int cc = 0; cc < PAIR_BN; cc += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * PAIR_BN + cc);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (OUT_BF16) {
+          uint4* dst = (uint4*)((__nv_bfloat16*)c + (size_t)row * N + n0 + cc);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t w[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const __nv_bfloat162 b2 =
+                  __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * h]), __uint_as_float(v[q * 8 + 2 * h + 1]));
+              w[h] = *(const uint32_t*)&b2;
+            }
+            dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        } else {
+          uint4* dst = (uint4*)((float*)c + (size_t)row * N + n0 + cc);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(acc ? leader_tempty1 : leader_tempty0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * PAIR_BN) : "memory");
+  }
+}
+
 }  // namespace gemm
 
 // ---------------------------------------------------------------- launcher
@@ -332,9 +550,54 @@ static int launch_gemm(const void* a, const void* b, void* c, int M, int N, int 
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
-// tile N = 256 when N allows it, else 128 (both deterministic, same per-element order)
+template <int STAGES, bool OUT_BF16>
+static int launch_gemm_pair(const void* a, const void* b, void* c, int M, int N, int K, int grid, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, a, M, K, gemm::BM) || !make_map(&mb, b, N, K, gemm::PAIR_BN / 2)) return ERR_CUDA;
+  auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16>;
+  const int smem = gemm::PairSmem<STAGES>::TOTAL + 1024;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return ERR_CUDA;
+    attr = true;
+  }
+  const int tiles = (M / gemm::PAIR_M) * (N / gemm::PAIR_BN);
+  if (grid <= 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = sms;
+  }
+  grid &= ~1;  // CTA pairs
+  if (grid < 2) grid = 2;
+  if (grid > 2 * tiles) grid = 2 * tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(gemm::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr_[1];
+  attr_[0].id = cudaLaunchAttributeClusterDimension;
+  attr_[0].val.clusterDim.x = 2;
+  attr_[0].val.clusterDim.y = 1;
+  attr_[0].val.clusterDim.z = 1;
+  cfg.attrs = attr_;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, c, M, N, K) == cudaSuccess ? OK : ERR_CUDA;
+}
+
+static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests, measurements)
+  const char* e = getenv("BT_GEMM_VARIANT");
+  return e ? atoi(e) : 0;
+}
+
+// 256 x 256 CTA-pair tiles when M and N allow it, else 128 x {256, 128} tiles (all deterministic)
 int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int M, int N, int K, int out_bf16, int grid,
                         cudaStream_t s) {
+  if (M % 256 == 0 && N % 256 == 0 && gemm_variant() != 1)
+    return out_bf16 ? launch_gemm_pair<6, true>(a, b, c, M, N, K, grid, s)
+                    : launch_gemm_pair<6, false>(a, b, c, M, N, K, grid, s);
   if (N % 256 == 0)
     return out_bf16 ? launch_gemm<256, 4, true>(a, b, c, M, N, K, grid, s)
                     : launch_gemm<256, 4, false>(a, b, c, M, N, K, grid, s);

@@ -66,3 +66,14 @@ def test_gemm_rejects_bad_shapes(gemm):
         gemm(a[:, :32].contiguous(), b[:, :32].contiguous())
     with pytest.raises(InputError):
         gemm(a[:100].contiguous(), b)
+
+
+def test_cta_pair_and_single_cta_kernels_agree_bitwise(gemm, monkeypatch):
+    """The 256x256 CTA-pair kernel (cta_group::2) and the 128x256 1-CTA kernel give the same bits:
+    the per-element accumulation order does not depend on the tile shape or the SM pairing."""
+    a, b = _inputs(512, 768, 1536, 11)
+    pair = gemm(a, b)
+    monkeypatch.setenv("BT_GEMM_VARIANT", "1")
+    single = gemm(a, b)
+    monkeypatch.delenv("BT_GEMM_VARIANT")
+    assert torch.equal(pair.view(torch.int32), single.view(torch.int32))

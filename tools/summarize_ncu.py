@@ -39,8 +39,8 @@ def launches():
              f"# host batches with one jitter_gather launch per mini-batch before timing)", "",
              f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'share':>7s} {'of step':>8s}"]
     for name, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        tag = "   setup" if any(x in name for x in setup) else f"{t / step_tot * 100:7.1f}%"
-        lines.append(f"{name[:70]:70s} {n:8d} {t / 1e3:12.1f} {t / tot * 100:6.1f}% {tag}")
+        share = "   setup" if any(x in name for x in setup) else f"{t / step_tot * 100:7.1f}%"
+        lines.append(f"{name[:70]:70s} {n:8d} {t / 1e3:12.1f} {t / tot * 100:6.1f}% {share}")
     (PROF / f"{tag}_launches.txt").write_text("\n".join(lines) + "\n")
     return agg
 
