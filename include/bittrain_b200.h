@@ -114,6 +114,12 @@ int bt_sgd_step_f64(const double *params_dev, const double *vel_dev, const doubl
  *                                         analogue of model.py:141-192's dense products */
 int bt_gemm_bf16_tn(const void *a_dev, const void *b_dev, void *c_dev, int32_t M, int32_t N, int32_t K,
                     int32_t out_dtype, int32_t grid, void *stream);
+/* Batched form: C[e] = A[e] * B[e]^T for e < batch; A[e] at a_dev + e*stride_a elements, B[e] at
+ * b_dev + e*stride_b, C[e] at c_dev + e*M*N (e.g. one weight gradient per EST, each its own GEMM,
+ * reduced afterwards by bt_reduce_update in EST-rank order). */
+int bt_gemm_bf16_tn_batched(const void *a_dev, const void *b_dev, void *c_dev, int32_t batch, int32_t M, int32_t N,
+                            int32_t K, int64_t stride_a, int64_t stride_b, int32_t out_dtype, int32_t grid,
+                            void *stream);
 
 /* ---------------- L3 data ------------------------------------------------- */
 /* make_dataset(seed, n, dim): [n][dim+1], x then y                       sampling.py:24-35 */

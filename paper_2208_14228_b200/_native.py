@@ -86,6 +86,7 @@ EXPORTS = {
     "bt_mlp_pick_est_per_cta": (C.c_int, [_i32, _i32]),
     "bt_reduce_update": (C.c_int, [C.POINTER(ReduceArgs), _vp]),
     "bt_gemm_bf16_tn": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
+    "bt_gemm_bf16_tn_batched": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i64, _i32, _i32, _vp]),
     "bt_sgd_step_f64": (C.c_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp, _vp, _vp]),
     "bt_make_dataset": (C.c_int, [_u64, _i64, _i32, _vp, _vp]),
     "bt_jitter_gather": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i64, _u64, _i64, _i64, _dbl, _vp, _vp]),

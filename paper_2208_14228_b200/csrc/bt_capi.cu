@@ -30,8 +30,8 @@ int replica_check_launch(const void* const* ptrs, int R, int64_t nbytes, int32_t
 int slot_copy_launch(void* const* dst, const void* const* src, const int64_t* bytes, int count, cudaStream_t s);
 int flags_reset_launch(int32_t* flags, cudaStream_t s);
 int tanh_launch(const double* x, int64_t n, double* out, cudaStream_t s);
-int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int M, int N, int K, int out_bf16, int grid,
-                        cudaStream_t s);
+int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
+                        int64_t sb, int out_bf16, int grid, cudaStream_t s);
 }  // namespace bt
 
 static thread_local char g_err[512];
@@ -259,16 +259,26 @@ int bt_fwd_bwd_mlp_f64(const double* params_dev, const double* rows_dev, int32_t
 }
 
 // ------------------------------------------------------ tensor-core GEMM
-int bt_gemm_bf16_tn(const void* a_dev, const void* b_dev, void* c_dev, int32_t M, int32_t N, int32_t K,
-                    int32_t out_dtype, int32_t grid, void* stream) {
+int bt_gemm_bf16_tn_batched(const void* a_dev, const void* b_dev, void* c_dev, int32_t batch, int32_t M, int32_t N,
+                            int32_t K, int64_t stride_a, int64_t stride_b, int32_t out_dtype, int32_t grid,
+                            void* stream) {
   if (!a_dev || !b_dev || !c_dev) return fail(bt::ERR_INPUT, "null pointer");
-  if (M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 128 || K % 64)
-    return fail(bt::ERR_INPUT, "gemm shape %dx%dx%d: need M %% 128 == 0, N %% 128 == 0, K %% 64 == 0", M, N, K);
+  if (batch < 1 || M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 128 || K % 64)
+    return fail(bt::ERR_INPUT, "gemm shape %dx%dx%d x%d: need M %% 128 == 0, N %% 128 == 0, K %% 64 == 0", M, N, K,
+                batch);
   if (((uintptr_t)a_dev | (uintptr_t)b_dev | (uintptr_t)c_dev) & 15)
     return fail(bt::ERR_INPUT, "gemm operands must be 16-byte aligned");
+  if (batch > 1 && (stride_a < (int64_t)M * K || stride_b < (int64_t)N * K || (stride_a | stride_b) % 8))
+    return fail(bt::ERR_INPUT, "gemm batch strides must cover a matrix and be multiples of 8 elements");
   if (out_dtype != 0 && out_dtype != 1) return fail(bt::ERR_INPUT, "gemm out_dtype must be 0 (f32) or 1 (bf16)");
-  return done(bt::gemm_bf16_tn_launch(a_dev, b_dev, c_dev, M, N, K, out_dtype, grid, STREAM(stream)),
+  return done(bt::gemm_bf16_tn_launch(a_dev, b_dev, c_dev, batch, M, N, K, batch > 1 ? stride_a : (int64_t)M * K,
+                                      batch > 1 ? stride_b : (int64_t)N * K, out_dtype, grid, STREAM(stream)),
               "bt_gemm_bf16_tn");
+}
+
+int bt_gemm_bf16_tn(const void* a_dev, const void* b_dev, void* c_dev, int32_t M, int32_t N, int32_t K,
+                    int32_t out_dtype, int32_t grid, void* stream) {
+  return bt_gemm_bf16_tn_batched(a_dev, b_dev, c_dev, 1, M, N, K, 0, 0, out_dtype, grid, stream);
 }
 
 // ------------------------------------------------------------- device: L2

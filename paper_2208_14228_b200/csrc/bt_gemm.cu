@@ -66,11 +66,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint32_t bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          dst),
-      "l"(map), "r"(x), "r"(y), "r"(bar)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -129,7 +130,7 @@ struct Smem {
 template <int BN, int STAGES, bool OUT_BF16>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                        void* __restrict__ c, int M, int N, int K) {
+                        void* __restrict__ c, int M, int N, int K, int batch) {
   using L = Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
@@ -144,8 +145,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = M / BM, nt = N / BN, kb_n = K / BK;
-  auto tile_coords = [](int t, int mt_, int nt_, int* m0, int* n0) { tile_coords_bn<BN>(t, mt_, nt_, m0, n0); };
-  const int tiles = mt * nt;
+  const int per_batch = mt * nt;
+  auto tile_coords = [&](int t, int mt_, int nt_, int* m0, int* n0) {  // t -> (batch entry, m0, n0)
+    tile_coords_bn<BN>(t % per_batch, mt_, nt_, m0, n0);
+  };
+  const int tiles = per_batch * batch;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
@@ -183,8 +187,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(empty(stage), phase ^ 1u);
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
           mbar_arrive_expect_tx(full(stage), L::STAGE);
-          tma_load_2d(sa, &map_a, kb * BK, m0, full(stage));
-          tma_load_2d(sb, &map_b, kb * BK, n0, full(stage));
+          tma_load_3d(sa, &map_a, kb * BK, m0, t / per_batch, full(stage));
+          tma_load_3d(sb, &map_b, kb * BK, n0, t / per_batch, full(stage));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tile_coords(t, mt, nt, &m0, &n0);
       mbar_wait(tfull(acc), (i >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + lg * 32 + lane;
+      const size_t row = (size_t)(t / per_batch) * M + m0 + lg * 32 + lane;  // batch entries stacked in C
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 32) {
         uint32_t v[32];
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (OUT_BF16) {
-          uint4* dst = (uint4*)((__nv_bfloat16*)c + (size_t)row * N + n0 + cc);
+          uint4* dst = (uint4*)((__nv_bfloat16*)c + row * N + n0 + cc);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint32_t w[4];
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
           }
         } else {
-          uint4* dst = (uint4*)((float*)c + (size_t)row * N + n0 + cc);
+          uint4* dst = (uint4*)((float*)c + row * N + n0 + cc);
 #pragma unroll
           for (int q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
@@ -291,12 +295,12 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y,
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, int x, int y, int z,
                                                  uint32_t leader_bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];" ::"r"(dst),
-      "l"(map), "r"(x), "r"(y), "r"(leader_bar)
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(leader_bar)
       : "memory");
 }
 __device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, int acc) {
@@ -335,7 +339,7 @@ struct PairSmem {
 template <int STAGES, bool OUT_BF16>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                             void* __restrict__ c, int M, int N, int K) {
+                             void* __restrict__ c, int M, int N, int K, int batch) {
   using L = PairSmem<STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
@@ -352,9 +356,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int mt = M / PAIR_M, nt = N / PAIR_BN, kb_n = K / BK;
-  const int tiles = mt * nt;
+  const int per_batch = mt * nt;
+  const int tiles = per_batch * batch;
   const int pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
   auto coords = [&](int t, int* m0, int* n0) {  // grouped raster, as the 1-CTA kernel
+    t %= per_batch;
     constexpr int GM = GROUP_M / 2;
     const int per_group = GM * nt;
     const int g = t / per_group, r = t - g * per_group;
@@ -399,8 +405,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
           const uint32_t lb = full(stage) & 0xFEFFFFFFu;  // the leader CTA's barrier
           if (leader) mbar_arrive_expect_tx(full(stage), 2 * L::STAGE);
-          tma_load_2d_pair(sa, &map_a, kb * BK, m0 + (int)rank * BM, lb);
-          tma_load_2d_pair(sb, &map_b, kb * BK, n0 + (int)rank * (PAIR_BN / 2), lb);
+          tma_load_3d_pair(sa, &map_a, kb * BK, m0 + (int)rank * BM, t / per_batch, lb);
+          tma_load_3d_pair(sb, &map_b, kb * BK, n0 + (int)rank * (PAIR_BN / 2), t / per_batch, lb);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -447,7 +453,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       coords(t, &m0, &n0);
       mbar_wait(tfull(acc), (i >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + (int)rank * BM + lg * 32 + lane;
+      const size_t row = (size_t)(t / per_batch) * M + m0 + (int)rank * BM + lg * 32 + lane;
 #pragma unroll 1
       for (int cc = 0; cc < PAIR_BN; cc += 32) {
         uint32_t v[32];
@@ -462,7 +468,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (OUT_BF16) {
-          uint4* dst = (uint4*)((__nv_bfloat16*)c + (size_t)row * N + n0 + cc);
+          uint4* dst = (uint4*)((__nv_bfloat16*)c + row * N + n0 + cc);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint32_t w[4];
@@ -475,7 +481,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
           }
         } else {
-          uint4* dst = (uint4*)((float*)c + (size_t)row * N + n0 + cc);
+          uint4* dst = (uint4*)((float*)c + row * N + n0 + cc);
 #pragma unroll
           for (int q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
@@ -513,23 +519,33 @@ static PFN_encodeTiled encode_fn() {
   return fn;
 }
 
-// rows x K bf16, K contiguous; box = box_rows x 64 (128 B), 128-byte swizzle
-static bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows) {
+// [batch][rows][K] bf16, K contiguous, batch entries `bstride` elements apart;
+// box = 64 (128 B) x box_rows x 1, 128-byte swizzle
+static bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows, int batch, int64_t bstride) {
   PFN_encodeTiled enc = encode_fn();
   if (!enc) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)gemm::BK, (cuuint32_t)box_rows};
-  const cuuint32_t estr[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+  const cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)bstride * 2};
+  const cuuint32_t box[3] = {(cuuint32_t)gemm::BK, (cuuint32_t)box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+struct GemmShape {
+  const void *a, *b;
+  void* c;
+  int M, N, K, batch;
+  int64_t sa, sb;  // batch strides of A and B in elements (C is [batch][M][N] contiguous)
+};
+
 template <int BN, int STAGES, bool OUT_BF16>
-static int launch_gemm(const void* a, const void* b, void* c, int M, int N, int K, int grid, cudaStream_t s) {
+static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
+  const int M = g.M, N = g.N, K = g.K;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, a, M, K, gemm::BM) || !make_map(&mb, b, N, K, BN)) return ERR_CUDA;
+  if (!make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) || !make_map(&mb, g.b, N, K, BN, g.batch, g.sb))
+    return ERR_CUDA;
   auto kern = gemm::gemm_bf16_tn_kernel<BN, STAGES, OUT_BF16>;
   const int smem = gemm::Smem<BN, STAGES>::TOTAL + 1024;
   static bool attr = false;
@@ -538,7 +554,7 @@ static int launch_gemm(const void* a, const void* b, void* c, int M, int N, int 
       return ERR_CUDA;
     attr = true;
   }
-  const int tiles = (M / gemm::BM) * (N / BN);
+  const int tiles = (M / gemm::BM) * (N / BN) * g.batch;
   if (grid <= 0) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -546,14 +562,17 @@ static int launch_gemm(const void* a, const void* b, void* c, int M, int N, int 
     grid = sms;
   }
   if (grid > tiles) grid = tiles;
-  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, c, M, N, K);
+  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, g.c, M, N, K, g.batch);
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
 template <int STAGES, bool OUT_BF16>
-static int launch_gemm_pair(const void* a, const void* b, void* c, int M, int N, int K, int grid, cudaStream_t s) {
+static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
+  const int M = g.M, N = g.N, K = g.K;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, a, M, K, gemm::BM) || !make_map(&mb, b, N, K, gemm::PAIR_BN / 2)) return ERR_CUDA;
+  if (!make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) ||
+      !make_map(&mb, g.b, N, K, gemm::PAIR_BN / 2, g.batch, g.sb))
+    return ERR_CUDA;
   auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16>;
   const int smem = gemm::PairSmem<STAGES>::TOTAL + 1024;
   static bool attr = false;
@@ -562,7 +581,7 @@ static int launch_gemm_pair(const void* a, const void* b, void* c, int M, int N,
       return ERR_CUDA;
     attr = true;
   }
-  const int tiles = (M / gemm::PAIR_M) * (N / gemm::PAIR_BN);
+  const int tiles = (M / gemm::PAIR_M) * (N / gemm::PAIR_BN) * g.batch;
   if (grid <= 0) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -584,7 +603,7 @@ static int launch_gemm_pair(const void* a, const void* b, void* c, int M, int N,
   attr_[0].val.clusterDim.z = 1;
   cfg.attrs = attr_;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb, c, M, N, K) == cudaSuccess ? OK : ERR_CUDA;
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, g.c, M, N, K, g.batch) == cudaSuccess ? OK : ERR_CUDA;
 }
 
 static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests, measurements)
@@ -593,16 +612,14 @@ static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests
 }
 
 // 256 x 256 CTA-pair tiles when M and N allow it, else 128 x {256, 128} tiles (all deterministic)
-int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int M, int N, int K, int out_bf16, int grid,
-                        cudaStream_t s) {
+int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
+                        int64_t sb, int out_bf16, int grid, cudaStream_t s) {
+  const GemmShape g{a, b, c, M, N, K, batch, sa, sb};
   if (M % 256 == 0 && N % 256 == 0 && gemm_variant() != 1)
-    return out_bf16 ? launch_gemm_pair<6, true>(a, b, c, M, N, K, grid, s)
-                    : launch_gemm_pair<6, false>(a, b, c, M, N, K, grid, s);
+    return out_bf16 ? launch_gemm_pair<6, true>(g, grid, s) : launch_gemm_pair<6, false>(g, grid, s);
   if (N % 256 == 0)
-    return out_bf16 ? launch_gemm<256, 4, true>(a, b, c, M, N, K, grid, s)
-                    : launch_gemm<256, 4, false>(a, b, c, M, N, K, grid, s);
-  return out_bf16 ? launch_gemm<128, 6, true>(a, b, c, M, N, K, grid, s)
-                  : launch_gemm<128, 6, false>(a, b, c, M, N, K, grid, s);
+    return out_bf16 ? launch_gemm<256, 4, true>(g, grid, s) : launch_gemm<256, 4, false>(g, grid, s);
+  return out_bf16 ? launch_gemm<128, 6, true>(g, grid, s) : launch_gemm<128, 6, false>(g, grid, s);
 }
 
 }  // namespace bt

@@ -33,3 +33,22 @@ def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype = torch.f
                                                  1 if out_dtype == torch.bfloat16 else 0, grid, stream()),
                   "gemm_bf16")
     return c
+
+
+def gemm_bf16_batched(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype = torch.float32,
+                      grid: int = 0) -> torch.Tensor:
+    """c[e] = a[e] @ b[e].T for bf16 a [E, M, K], b [E, N, K] (one launch; per-entry bits equal the
+    single-GEMM bits -- e.g. one weight gradient per EST, reduced afterwards in EST-rank order)."""
+    require_cuda()
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or not (a.is_cuda and b.is_cuda):
+        raise InputError("gemm_bf16_batched takes CUDA bfloat16 tensors")
+    if a.dim() != 3 or b.dim() != 3 or a.shape[0] != b.shape[0] or a.shape[2] != b.shape[2]:
+        raise InputError(f"gemm_bf16_batched shapes {tuple(a.shape)} x {tuple(b.shape)}^T")
+    a, b = a.contiguous(), b.contiguous()
+    E, M, K = a.shape
+    N = b.shape[1]
+    c = torch.empty((E, M, N), dtype=out_dtype, device=a.device)
+    _native.check(_native.lib().bt_gemm_bf16_tn_batched(a.data_ptr(), b.data_ptr(), c.data_ptr(), E, M, N, K,
+                                                         M * K, N * K, 1 if out_dtype == torch.bfloat16 else 0,
+                                                         grid, stream()), "gemm_bf16_batched")
+    return c

@@ -77,3 +77,18 @@ def test_cta_pair_and_single_cta_kernels_agree_bitwise(gemm, monkeypatch):
     single = gemm(a, b)
     monkeypatch.delenv("BT_GEMM_VARIANT")
     assert torch.equal(pair.view(torch.int32), single.view(torch.int32))
+
+
+@pytest.mark.parametrize("E,M,N,K", [(4, 256, 256, 512), (3, 128, 384, 256), (8, 256, 768, 1024)])
+def test_batched_gemm_equals_per_entry_gemms(gemm, E, M, N, K):
+    from paper_2208_14228_b200.gemm import gemm_bf16_batched
+
+    g = torch.Generator(device="cuda").manual_seed(E * 1000 + M)
+    a = torch.randn(E, M, K, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(E, N, K, device="cuda", generator=g).to(torch.bfloat16)
+    c = gemm_bf16_batched(a, b)
+    for e in range(E):
+        assert torch.equal(c[e].view(torch.int32), gemm(a[e], b[e]).view(torch.int32)), e
+    ref = torch.einsum("emk,enk->emn", a.double(), b.double())
+    bound = K * 2.0 ** -23 * torch.einsum("emk,enk->emn", a.double().abs(), b.double().abs())
+    assert bool(((c.double() - ref).abs() <= bound + 1e-30).all())
