@@ -121,6 +121,27 @@ int bt_gemm_bf16_tn_batched(const void *a_dev, const void *b_dev, void *c_dev, i
                             int32_t K, int64_t stride_a, int64_t stride_b, int32_t out_dtype, int32_t grid,
                             void *stream);
 
+/* ---------------- per-EST transformer FFN step (C4 slice, no reference) ----
+ * The kernels between the GEMMs of a BERT-style FFN sublayer trained by E ESTs
+ * (tokens of local EST e are rows [e*Te, (e+1)*Te)); all randomness is keyed
+ * by (seed, est_base + e, step, element) and all sums have a fixed shape.
+ * Activations bf16, GEMM outputs fp32.                  analogue of model.py:141-196 */
+int bt_ffn_data(uint64_t seed, int64_t step, int32_t est_base, int32_t E, int32_t Te, int32_t D, void *x_dev,
+                float *target_dev, void *stream);
+int bt_ffn_fwd_act(const float *h_dev, const float *b1_dev, uint64_t seed, int64_t step, int32_t est_base, int32_t E,
+                   int32_t Te, int32_t F, float p, void *hpre_dev, void *d_dev, void *stream);
+/* partials_dev: E*64 floats of scratch; loss_dev[E] = sum 0.5*(y-target)^2 / Te; dy = (y-target)/Te */
+int bt_ffn_out(const float *y_dev, const float *b2_dev, const float *target_dev, int32_t E, int32_t Te, int32_t D,
+               void *dy_dev, float *partials_dev, float *loss_dev, void *stream);
+int bt_ffn_bwd_act(const float *dd_dev, const void *hpre_dev, uint64_t seed, int64_t step, int32_t est_base,
+                   int32_t E, int32_t Te, int32_t F, float p, void *dh_dev, void *stream);
+/* out[e][c] = sum_r in[e][r][c] (bf16 in, fp32 out, r ascending) */
+int bt_colsum_bf16(const void *in_dev, int32_t E, int32_t R, int32_t C, float *out_dev, void *stream);
+/* out[e][c][r] = bf16(in[e][r][c]); in is bf16 (in_f32 = 0) or fp32 (1) */
+int bt_transpose_to_bf16(const void *in_dev, int32_t in_f32, int32_t E, int32_t R, int32_t C, void *out_dev,
+                         void *stream);
+int bt_cast_f32_bf16(const float *in_dev, int64_t n, void *out_dev, void *stream);
+
 /* ---------------- L3 data ------------------------------------------------- */
 /* make_dataset(seed, n, dim): [n][dim+1], x then y                       sampling.py:24-35 */
 int bt_make_dataset(uint64_t seed, int64_t n, int32_t dim, double *out_dev, void *stream);

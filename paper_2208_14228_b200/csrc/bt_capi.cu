@@ -32,6 +32,17 @@ int flags_reset_launch(int32_t* flags, cudaStream_t s);
 int tanh_launch(const double* x, int64_t n, double* out, cudaStream_t s);
 int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                         int64_t sb, int out_bf16, int grid, cudaStream_t s);
+int ffn_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, void* X, float* target,
+                    cudaStream_t s);
+int ffn_fwd_act_launch(const float* H, const float* b1, uint64_t seed, int64_t step, int est_base, int E, int Te,
+                       int F, float p, void* Hpre, void* Dout, cudaStream_t s);
+int ffn_out_launch(const float* Y, const float* b2, const float* target, int E, int Te, int D, void* dY, float* part,
+                   float* loss, cudaStream_t s);
+int ffn_bwd_act_launch(const float* dD, const void* Hpre, uint64_t seed, int64_t step, int est_base, int E, int Te,
+                       int F, float p, void* dH, cudaStream_t s);
+int colsum_bf16_launch(const void* in, int E, int R, int C, float* out, cudaStream_t s);
+int transpose_launch(const void* in, int in_f32, int E, int R, int C, void* out, cudaStream_t s);
+int cast_f32_bf16_launch(const float* in, int64_t n, void* out, cudaStream_t s);
 }  // namespace bt
 
 static thread_local char g_err[512];
@@ -279,6 +290,51 @@ int bt_gemm_bf16_tn_batched(const void* a_dev, const void* b_dev, void* c_dev, i
 int bt_gemm_bf16_tn(const void* a_dev, const void* b_dev, void* c_dev, int32_t M, int32_t N, int32_t K,
                     int32_t out_dtype, int32_t grid, void* stream) {
   return bt_gemm_bf16_tn_batched(a_dev, b_dev, c_dev, 1, M, N, K, 0, 0, out_dtype, grid, stream);
+}
+
+// ------------------------------------------ per-EST FFN step (C4 slice)
+static int ffn_check(int E, int Te, int D) {
+  if (E < 1 || Te < 1 || D < 1) return fail(bt::ERR_INPUT, "ffn shape E=%d Te=%d D=%d", E, Te, D);
+  return 0;
+}
+int bt_ffn_data(uint64_t seed, int64_t step, int32_t est_base, int32_t E, int32_t Te, int32_t D, void* x_dev,
+                float* target_dev, void* stream) {
+  if (int st = ffn_check(E, Te, D)) return st;
+  return done(bt::ffn_data_launch(seed, step, est_base, E, Te, D, x_dev, target_dev, STREAM(stream)), "bt_ffn_data");
+}
+int bt_ffn_fwd_act(const float* h_dev, const float* b1_dev, uint64_t seed, int64_t step, int32_t est_base, int32_t E,
+                   int32_t Te, int32_t F, float p, void* hpre_dev, void* d_dev, void* stream) {
+  if (int st = ffn_check(E, Te, F)) return st;
+  if (!(p >= 0.f && p < 1.f)) return fail(bt::ERR_CONFIG, "dropout rate %g not in [0, 1)", (double)p);
+  return done(bt::ffn_fwd_act_launch(h_dev, b1_dev, seed, step, est_base, E, Te, F, p, hpre_dev, d_dev,
+                                     STREAM(stream)),
+              "bt_ffn_fwd_act");
+}
+int bt_ffn_out(const float* y_dev, const float* b2_dev, const float* target_dev, int32_t E, int32_t Te, int32_t D,
+               void* dy_dev, float* partials_dev, float* loss_dev, void* stream) {
+  if (int st = ffn_check(E, Te, D)) return st;
+  return done(bt::ffn_out_launch(y_dev, b2_dev, target_dev, E, Te, D, dy_dev, partials_dev, loss_dev, STREAM(stream)),
+              "bt_ffn_out");
+}
+int bt_ffn_bwd_act(const float* dd_dev, const void* hpre_dev, uint64_t seed, int64_t step, int32_t est_base, int32_t E,
+                   int32_t Te, int32_t F, float p, void* dh_dev, void* stream) {
+  if (int st = ffn_check(E, Te, F)) return st;
+  if (!(p >= 0.f && p < 1.f)) return fail(bt::ERR_CONFIG, "dropout rate %g not in [0, 1)", (double)p);
+  return done(bt::ffn_bwd_act_launch(dd_dev, hpre_dev, seed, step, est_base, E, Te, F, p, dh_dev, STREAM(stream)),
+              "bt_ffn_bwd_act");
+}
+int bt_colsum_bf16(const void* in_dev, int32_t E, int32_t R, int32_t C, float* out_dev, void* stream) {
+  if (int st = ffn_check(E, R, C)) return st;
+  return done(bt::colsum_bf16_launch(in_dev, E, R, C, out_dev, STREAM(stream)), "bt_colsum_bf16");
+}
+int bt_transpose_to_bf16(const void* in_dev, int32_t in_f32, int32_t E, int32_t R, int32_t C, void* out_dev,
+                         void* stream) {
+  if (int st = ffn_check(E, R, C)) return st;
+  return done(bt::transpose_launch(in_dev, in_f32, E, R, C, out_dev, STREAM(stream)), "bt_transpose_to_bf16");
+}
+int bt_cast_f32_bf16(const float* in_dev, int64_t n, void* out_dev, void* stream) {
+  if (n < 0) return fail(bt::ERR_INPUT, "negative length");
+  return done(bt::cast_f32_bf16_launch(in_dev, n, out_dev, STREAM(stream)), "bt_cast_f32_bf16");
 }
 
 // ------------------------------------------------------------- device: L2

@@ -1,0 +1,155 @@
+"""Per-EST transformer FFN training step -- the C4 model-stack slice.
+
+A BERT-base FFN sublayer (d_model 768 -> d_ff 3072 -> 768, erf-GELU, dropout)
+trained data-parallel by E virtual workers (ESTs), EasyScale-style:
+
+* every EST's randomness (its synthetic tokens and targets, its dropout masks)
+  is keyed by (seed, EST rank, step), never by the launch or the GPU
+  (the reference keys dropout the same way, model.py:151-161);
+* the dense products run on the deterministic tcgen05 GEMM (csrc/bt_gemm.cu):
+  row-independent products (forward, dD) for a whole group of ESTs at once --
+  a row's bits do not depend on which rows share the launch -- and one weight
+  gradient per EST (batched GEMM over the EST's own tokens);
+* the per-EST gradients are summed by the fixed-order reducer (csrc/bt_reduce.cu,
+  EST-rank order, fused /E and momentum SGD on fp32 master weights).
+
+So the trained weights are bit-identical however the ESTs are grouped into
+launches (`groups=`) -- the same property the multi-GPU mapping needs: a GPU
+holding a contiguous EST block runs exactly one such group.
+
+There is no reference implementation of this model: parity is
+against a float64 restatement with the same bf16 rounding points
+(tests/test_gpu_ffn.py), at a stated tolerance.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native
+from .device import Flags, require_cuda, stream
+from .errors import ConfigError, NumericError
+from .gemm import gemm_bf16, gemm_bf16_batched
+
+_P = 64  # partial loss sums per EST (bt_ffn_out)
+
+
+def _init_uniform(seed: int, n: int, scale: float) -> torch.Tensor:
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().bt_init_random(seed & (2**64 - 1), scale, n, out.data_ptr(), stream()))
+    return out.float()
+
+
+class FFNJob:
+    """E ESTs x `tokens` tokens each, one FFN sublayer, momentum SGD on fp32 master weights."""
+
+    def __init__(self, ests: int, tokens: int, d_model: int = 768, d_ff: int = 3072, seed: int = 42,
+                 lr: float = 1e-2, momentum: float = 0.9, dropout: float = 0.1, fanin: int = 0):
+        require_cuda()
+        if tokens % 128 or d_model % 128 or d_ff % 128:
+            raise ConfigError("tokens, d_model and d_ff must be multiples of 128")
+        if fanin not in (0, 2) or (fanin == 2 and ests & (ests - 1)):
+            raise ConfigError("allreduce variant: Sequential (0) or Tree(2) with a power-of-two EST count")
+        self.E, self.Te, self.D, self.F = ests, tokens, d_model, d_ff
+        self.seed, self.lr, self.mu, self.p, self.fanin = seed, lr, momentum, dropout, fanin
+        D, F = d_model, d_ff
+        self.W1 = _init_uniform(seed, F * D, D ** -0.5).view(F, D)
+        self.b1 = torch.zeros(F, device="cuda")
+        self.W2 = _init_uniform(seed + 1, D * F, F ** -0.5).view(D, F)
+        self.b2 = torch.zeros(D, device="cuda")
+        self.params = [self.W1, self.b1, self.W2, self.b2]
+        self.vel = [torch.zeros_like(t) for t in self.params]
+        self.step_idx = 0
+        self.flags = Flags()
+        self._refresh_bf16()
+
+    # -- bf16 operand copies of the master weights (W2^T for the dD product)
+    def _refresh_bf16(self):
+        L, s = _native.lib(), stream()
+        self.W1h = torch.empty(self.F, self.D, dtype=torch.bfloat16, device="cuda")
+        self.W2h = torch.empty(self.D, self.F, dtype=torch.bfloat16, device="cuda")
+        self.W2t = torch.empty(self.F, self.D, dtype=torch.bfloat16, device="cuda")
+        _native.check(L.bt_cast_f32_bf16(self.W1.data_ptr(), self.W1.numel(), self.W1h.data_ptr(), s))
+        _native.check(L.bt_cast_f32_bf16(self.W2.data_ptr(), self.W2.numel(), self.W2h.data_ptr(), s))
+        _native.check(L.bt_transpose_to_bf16(self.W2.data_ptr(), 1, 1, self.D, self.F, self.W2t.data_ptr(), s))
+
+    def _group(self, base: int, n: int, grads: list, losses: torch.Tensor, capture: dict | None = None):
+        """Forward/backward of ESTs [base, base+n): per-EST gradients into grads[*][base:base+n]."""
+        L, s = _native.lib(), stream()
+        D, F, Te, T = self.D, self.F, self.Te, n * self.Te
+        seed, step, p = self.seed & (2**64 - 1), self.step_idx, self.p
+        X = torch.empty(T, D, dtype=torch.bfloat16, device="cuda")
+        tgt = torch.empty(T, D, dtype=torch.float32, device="cuda")
+        _native.check(L.bt_ffn_data(seed, step, base, n, Te, D, X.data_ptr(), tgt.data_ptr(), s))
+        H = gemm_bf16(X, self.W1h)                                     # [T][F] = X W1^T
+        Hpre = torch.empty(T, F, dtype=torch.bfloat16, device="cuda")
+        Dact = torch.empty(T, F, dtype=torch.bfloat16, device="cuda")
+        _native.check(L.bt_ffn_fwd_act(H.data_ptr(), self.b1.data_ptr(), seed, step, base, n, Te, F, p,
+                                       Hpre.data_ptr(), Dact.data_ptr(), s))
+        del H
+        Y = gemm_bf16(Dact, self.W2h)                                  # [T][D] = dropout(gelu) W2^T
+        dY = torch.empty(T, D, dtype=torch.bfloat16, device="cuda")
+        part = torch.empty(n * _P, dtype=torch.float32, device="cuda")
+        _native.check(L.bt_ffn_out(Y.data_ptr(), self.b2.data_ptr(), tgt.data_ptr(), n, Te, D, dY.data_ptr(),
+                                   part.data_ptr(), losses[base:].data_ptr(), s))
+        del Y, tgt
+        dD = gemm_bf16(dY, self.W2t)                                   # [T][F] = dY W2
+        dH = torch.empty(T, F, dtype=torch.bfloat16, device="cuda")
+        _native.check(L.bt_ffn_bwd_act(dD.data_ptr(), Hpre.data_ptr(), seed, step, base, n, Te, F, p,
+                                       dH.data_ptr(), s))
+        del dD, Hpre
+        # per-EST weight gradients: K = the EST's own tokens (transposed, token-contiguous operands)
+        dYt = torch.empty(n, D, Te, dtype=torch.bfloat16, device="cuda")
+        Dt = torch.empty(n, F, Te, dtype=torch.bfloat16, device="cuda")
+        dHt = torch.empty(n, F, Te, dtype=torch.bfloat16, device="cuda")
+        Xt = torch.empty(n, D, Te, dtype=torch.bfloat16, device="cuda")
+        for src, dst, cols in ((dY, dYt, D), (Dact, Dt, F), (dH, dHt, F), (X, Xt, D)):
+            _native.check(L.bt_transpose_to_bf16(src.data_ptr(), 0, n, Te, cols, dst.data_ptr(), s))
+        if capture is not None:
+            capture.update(X=X, D=Dact, dY=dY, dH=dH)
+        gW1, gb1, gW2, gb2 = grads
+        gemm_bf16_batched(dHt, Xt, out=gW1[base:base + n])     # dW1_e = dH_e^T X_e   [n][F][D]
+        gemm_bf16_batched(dYt, Dt, out=gW2[base:base + n])     # dW2_e = dY_e^T D_e   [n][D][F]
+        _native.check(L.bt_colsum_bf16(dH.data_ptr(), n, Te, F, gb1[base:].data_ptr(), s))
+        _native.check(L.bt_colsum_bf16(dY.data_ptr(), n, Te, D, gb2[base:].data_ptr(), s))
+
+    def step(self, groups: list[int] | None = None, capture: dict | None = None) -> torch.Tensor:
+        """One mini-batch of all E ESTs; `groups` = EST counts per launch group (default: one group).
+        Returns the per-EST losses [E] (fp32, on device)."""
+        groups = groups or [self.E]
+        if sum(groups) != self.E or min(groups) < 1:
+            raise ConfigError(f"groups {groups} must partition {self.E} ESTs")
+        E = self.E
+        grads = [torch.empty(E, t.numel(), dtype=torch.float32, device="cuda") for t in self.params]
+        losses = torch.empty(E, dtype=torch.float32, device="cuda")
+        base = 0
+        for n in groups:
+            self._group(base, n, grads, losses, capture if len(groups) == 1 else None)
+            base += n
+        if capture is not None:
+            capture["grads"] = [g.clone() for g in grads]
+        self._reduce_update(grads)
+        self.step_idx += 1
+        self._refresh_bf16()
+        return losses
+
+    def _reduce_update(self, grads):
+        """Fixed EST-rank-order sum, /E, momentum SGD (bt_reduce_update, f32, strided slots)."""
+        L, s = _native.lib(), stream()
+        for g, prm, vel in zip(grads, self.params, self.vel):
+            a = _native.ReduceArgs()
+            a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, self.E, self.fanin, prm.numel()
+            a.grads[0], a.grads_ld = g.data_ptr(), prm.numel()
+            a.param, a.vel, a.param_out, a.vel_out = prm.data_ptr(), vel.data_ptr(), prm.data_ptr(), vel.data_ptr()
+            a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
+            _native.check(L.bt_reduce_update(C.byref(a), s), "ffn reduce_update")
+        st, _, _ = self.flags.status()
+        if st:
+            self.flags.reset()
+            raise NumericError("ffn: non-finite synchronized gradient")
+
+    def flops_per_step(self) -> float:
+        """5 GEMMs of 2*T*D*F flops each (forward x2, dD, dW1, dW2; no dX for the first layer)."""
+        return 5 * 2.0 * self.E * self.Te * self.D * self.F

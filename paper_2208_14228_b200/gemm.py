@@ -17,7 +17,16 @@ from .device import require_cuda, stream
 from .errors import InputError
 
 
-def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype = torch.float32, grid: int = 0) -> torch.Tensor:
+def _out(out, shape, dtype, device):
+    if out is None:
+        return torch.empty(shape, dtype=dtype, device=device)
+    if out.dtype != dtype or out.numel() != int(torch.Size(shape).numel()) or not out.is_contiguous():
+        raise InputError(f"out must be a contiguous {dtype} tensor of {shape}")
+    return out
+
+
+def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype = torch.float32, grid: int = 0,
+              out: torch.Tensor | None = None) -> torch.Tensor:
     require_cuda()
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or not (a.is_cuda and b.is_cuda):
         raise InputError("gemm_bf16 takes CUDA bfloat16 tensors")
@@ -28,7 +37,7 @@ def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype = torch.f
     a, b = a.contiguous(), b.contiguous()
     M, K = a.shape
     N = b.shape[0]
-    c = torch.empty((M, N), dtype=out_dtype, device=a.device)
+    c = _out(out, (M, N), out_dtype, a.device)
     _native.check(_native.lib().bt_gemm_bf16_tn(a.data_ptr(), b.data_ptr(), c.data_ptr(), M, N, K,
                                                  1 if out_dtype == torch.bfloat16 else 0, grid, stream()),
                   "gemm_bf16")
@@ -36,7 +45,7 @@ def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype = torch.f
 
 
 def gemm_bf16_batched(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype = torch.float32,
-                      grid: int = 0) -> torch.Tensor:
+                      grid: int = 0, out: torch.Tensor | None = None) -> torch.Tensor:
     """c[e] = a[e] @ b[e].T for bf16 a [E, M, K], b [E, N, K] (one launch; per-entry bits equal the
     single-GEMM bits -- e.g. one weight gradient per EST, reduced afterwards in EST-rank order)."""
     require_cuda()
@@ -47,7 +56,7 @@ def gemm_bf16_batched(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype =
     a, b = a.contiguous(), b.contiguous()
     E, M, K = a.shape
     N = b.shape[1]
-    c = torch.empty((E, M, N), dtype=out_dtype, device=a.device)
+    c = _out(out, (E, M, N), out_dtype, a.device)
     _native.check(_native.lib().bt_gemm_bf16_tn_batched(a.data_ptr(), b.data_ptr(), c.data_ptr(), E, M, N, K,
                                                          M * K, N * K, 1 if out_dtype == torch.bfloat16 else 0,
                                                          grid, stream()), "gemm_bf16_batched")
