@@ -130,13 +130,22 @@ int bt_ffn_data(uint64_t seed, int64_t step, int32_t est_base, int32_t E, int32_
                 float *target_dev, void *stream);
 int bt_ffn_fwd_act(const float *h_dev, const float *b1_dev, uint64_t seed, int64_t step, int32_t est_base, int32_t E,
                    int32_t Te, int32_t F, float p, void *hpre_dev, void *d_dev, void *stream);
+/* The FFN's GEMMs with the element ops fused into the epilogue (no fp32 round trip):
+ * kind 1 (forward):  h = A*B^T + bias -> c = bf16(h), out2 = bf16(dropout(gelu(h)))
+ * kind 2 (backward): c = bf16((A*B^T) * dropout_scale * gelu'(aux))   (aux = bf16 pre-activations)
+ * rows are tokens, row r belongs to EST est_base + r / Te; same determinism as bt_gemm_bf16_tn. */
+int bt_gemm_bf16_ffn(const void *a_dev, const void *b_dev, void *c_dev, int32_t M, int32_t N, int32_t K, int32_t kind,
+                     const float *bias_dev, const void *aux_dev, void *out2_dev, uint64_t seed, int64_t step,
+                     int32_t est_base, int32_t Te, float p, int32_t grid, void *stream);
 /* partials_dev: E*64 floats of scratch; loss_dev[E] = sum 0.5*(y-target)^2 / Te; dy = (y-target)/Te */
 int bt_ffn_out(const float *y_dev, const float *b2_dev, const float *target_dev, int32_t E, int32_t Te, int32_t D,
                void *dy_dev, float *partials_dev, float *loss_dev, void *stream);
 int bt_ffn_bwd_act(const float *dd_dev, const void *hpre_dev, uint64_t seed, int64_t step, int32_t est_base,
                    int32_t E, int32_t Te, int32_t F, float p, void *dh_dev, void *stream);
-/* out[e][c] = sum_r in[e][r][c] (bf16 in, fp32 out, r ascending) */
-int bt_colsum_bf16(const void *in_dev, int32_t E, int32_t R, int32_t C, float *out_dev, void *stream);
+/* out[e][c] = sum_r in[e][r][c] (bf16 in, fp32 out): 16 ascending row chunks summed ascending, then
+ * the chunk sums in order (fixed association).  scratch_dev: E*16*C floats, or NULL (allocated). */
+int bt_colsum_bf16(const void *in_dev, int32_t E, int32_t R, int32_t C, float *out_dev, float *scratch_dev,
+                   void *stream);
 /* out[e][c][r] = bf16(in[e][r][c]); in is bf16 (in_f32 = 0) or fp32 (1) */
 int bt_transpose_to_bf16(const void *in_dev, int32_t in_f32, int32_t E, int32_t R, int32_t C, void *out_dev,
                          void *stream);

@@ -87,11 +87,13 @@ EXPORTS = {
     "bt_reduce_update": (C.c_int, [C.POINTER(ReduceArgs), _vp]),
     "bt_gemm_bf16_tn": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
     "bt_gemm_bf16_tn_batched": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i64, _i32, _i32, _vp]),
+    "bt_gemm_bf16_ffn": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _u64, _i64, _i32, _i32,
+                                   C.c_float, _i32, _vp]),
     "bt_ffn_data": (C.c_int, [_u64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "bt_ffn_fwd_act": (C.c_int, [_vp, _vp, _u64, _i64, _i32, _i32, _i32, _i32, C.c_float, _vp, _vp, _vp]),
     "bt_ffn_out": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "bt_ffn_bwd_act": (C.c_int, [_vp, _vp, _u64, _i64, _i32, _i32, _i32, _i32, C.c_float, _vp, _vp]),
-    "bt_colsum_bf16": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),
+    "bt_colsum_bf16": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _vp]),
     "bt_transpose_to_bf16": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "bt_cast_f32_bf16": (C.c_int, [_vp, _i64, _vp, _vp]),
     "bt_sgd_step_f64": (C.c_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp, _vp, _vp]),

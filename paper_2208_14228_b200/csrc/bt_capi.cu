@@ -10,6 +10,7 @@
 
 #include "../../include/bittrain_b200.h"
 #include "bt_common.cuh"
+#include "bt_ffn.cuh"
 
 namespace bt {
 int mlp_launch(const bt_mlp_args& a, cudaStream_t s, unsigned long long* timing = nullptr);
@@ -32,6 +33,8 @@ int flags_reset_launch(int32_t* flags, cudaStream_t s);
 int tanh_launch(const double* x, int64_t n, double* out, cudaStream_t s);
 int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                         int64_t sb, int out_bf16, int grid, cudaStream_t s);
+int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
+                            int64_t sb, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s);
 int ffn_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, void* X, float* target,
                     cudaStream_t s);
 int ffn_fwd_act_launch(const float* H, const float* b1, uint64_t seed, int64_t step, int est_base, int E, int Te,
@@ -40,7 +43,7 @@ int ffn_out_launch(const float* Y, const float* b2, const float* target, int E, 
                    float* loss, cudaStream_t s);
 int ffn_bwd_act_launch(const float* dD, const void* Hpre, uint64_t seed, int64_t step, int est_base, int E, int Te,
                        int F, float p, void* dH, cudaStream_t s);
-int colsum_bf16_launch(const void* in, int E, int R, int C, float* out, cudaStream_t s);
+int colsum_bf16_launch(const void* in, int E, int R, int C, float* out, float* scratch, cudaStream_t s);
 int transpose_launch(const void* in, int in_f32, int E, int R, int C, void* out, cudaStream_t s);
 int cast_f32_bf16_launch(const float* in, int64_t n, void* out, cudaStream_t s);
 }  // namespace bt
@@ -292,6 +295,33 @@ int bt_gemm_bf16_tn(const void* a_dev, const void* b_dev, void* c_dev, int32_t M
   return bt_gemm_bf16_tn_batched(a_dev, b_dev, c_dev, 1, M, N, K, 0, 0, out_dtype, grid, stream);
 }
 
+int bt_gemm_bf16_ffn(const void* a_dev, const void* b_dev, void* c_dev, int32_t M, int32_t N, int32_t K, int32_t kind,
+                     const float* bias_dev, const void* aux_dev, void* out2_dev, uint64_t seed, int64_t step,
+                     int32_t est_base, int32_t Te, float p, int32_t grid, void* stream) {
+  if (!a_dev || !b_dev || !c_dev) return fail(bt::ERR_INPUT, "null pointer");
+  if (M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 128 || K % 64)
+    return fail(bt::ERR_INPUT, "gemm shape %dx%dx%d: need M %% 128 == 0, N %% 128 == 0, K %% 64 == 0", M, N, K);
+  if (kind != bt::EPI_FFN_FWD && kind != bt::EPI_FFN_BWD) return fail(bt::ERR_INPUT, "bad epilogue kind %d", kind);
+  if (kind == bt::EPI_FFN_FWD && (!bias_dev || !out2_dev)) return fail(bt::ERR_INPUT, "FFN_FWD needs bias and out2");
+  if (kind == bt::EPI_FFN_BWD && !aux_dev) return fail(bt::ERR_INPUT, "FFN_BWD needs the pre-activations");
+  if (Te < 1 || M % Te || !(p >= 0.f && p < 1.f)) return fail(bt::ERR_CONFIG, "bad Te %d / dropout %g", Te, (double)p);
+  if (((uintptr_t)a_dev | (uintptr_t)b_dev | (uintptr_t)c_dev | (uintptr_t)aux_dev | (uintptr_t)out2_dev) & 15)
+    return fail(bt::ERR_INPUT, "gemm operands must be 16-byte aligned");
+  bt::GemmEpi epi{};
+  epi.kind = kind;
+  epi.bias = bias_dev;
+  epi.aux = (const __nv_bfloat16*)aux_dev;
+  epi.out2 = (__nv_bfloat16*)out2_dev;
+  epi.seed = seed;
+  epi.step = step;
+  epi.est_base = est_base;
+  epi.Te = Te;
+  epi.p = p;
+  return done(bt::gemm_bf16_tn_launch_epi(a_dev, b_dev, c_dev, 1, M, N, K, (int64_t)M * K, (int64_t)N * K, 1, grid,
+                                          epi, STREAM(stream)),
+              "bt_gemm_bf16_ffn");
+}
+
 // ------------------------------------------ per-EST FFN step (C4 slice)
 static int ffn_check(int E, int Te, int D) {
   if (E < 1 || Te < 1 || D < 1) return fail(bt::ERR_INPUT, "ffn shape E=%d Te=%d D=%d", E, Te, D);
@@ -323,9 +353,10 @@ int bt_ffn_bwd_act(const float* dd_dev, const void* hpre_dev, uint64_t seed, int
   return done(bt::ffn_bwd_act_launch(dd_dev, hpre_dev, seed, step, est_base, E, Te, F, p, dh_dev, STREAM(stream)),
               "bt_ffn_bwd_act");
 }
-int bt_colsum_bf16(const void* in_dev, int32_t E, int32_t R, int32_t C, float* out_dev, void* stream) {
+int bt_colsum_bf16(const void* in_dev, int32_t E, int32_t R, int32_t C, float* out_dev, float* scratch_dev,
+                   void* stream) {
   if (int st = ffn_check(E, R, C)) return st;
-  return done(bt::colsum_bf16_launch(in_dev, E, R, C, out_dev, STREAM(stream)), "bt_colsum_bf16");
+  return done(bt::colsum_bf16_launch(in_dev, E, R, C, out_dev, scratch_dev, STREAM(stream)), "bt_colsum_bf16");
 }
 int bt_transpose_to_bf16(const void* in_dev, int32_t in_f32, int32_t E, int32_t R, int32_t C, void* out_dev,
                          void* stream) {

@@ -14,56 +14,85 @@
 #include <stdint.h>
 
 #include "bt_common.cuh"
+#include "bt_ffn.cuh"
 
 namespace bt {
 namespace ffn {
 
-constexpr uint64_t TAG_FFN_X = 0x4646'4e5f'5844'4154ull;     // "FFN_XDAT"
-constexpr uint64_t TAG_FFN_Y = 0x4646'4e5f'5944'4154ull;     // "FFN_YDAT"
-constexpr uint64_t TAG_FFN_DROP = 0x4646'4e5f'4452'4f50ull;  // "FFN_DROP"
+// Row-oriented kernels: a block walks whole token rows (grid-stride), so the
+// EST's counter stream is derived once per row, and each thread moves 8
+// consecutive features with 16-byte loads/stores (dims are multiples of 128).
+constexpr int ROW_THREADS = 128;
 
-__device__ __forceinline__ float uniform_pm1(uint64_t stream, uint64_t n) {  // [-1, 1)
-  return (float)(unit_float(draw_raw(stream, n)) * 2.0 - 1.0);
+__device__ __forceinline__ void load8(const float* p, float* v) {
+  const float4 a = *(const float4*)p, b = *(const float4*)(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float* v) {
+  const uint4 u = *(const uint4*)p;
+  const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __bfloat1622float2(h[k]);
+    v[2 * k] = f.x;
+    v[2 * k + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* v) {
+  uint4 u;
+  __nv_bfloat162* h = (__nv_bfloat162*)&u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+  *(uint4*)p = u;
 }
 
-// keep-scale of element (token tl, unit j) of EST eg at `step` (inverted dropout)
-__device__ __forceinline__ float drop_scale(uint64_t stream, int64_t step, int Te, int F, int tl, int j, float p,
-                                            float keep) {
-  if (p <= 0.f) return 1.f;
-  const uint64_t n = ((uint64_t)step * (uint64_t)Te + (uint64_t)tl) * (uint64_t)F + (uint64_t)j;
-  return unit_float(draw_raw(stream, n)) < (double)p ? 0.f : keep;
-}
-
-__device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
-__device__ __forceinline__ float gelu_grad(float x) {
-  return 0.5f * (1.f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * expf(-0.5f * x * x);
-}
-
-__global__ void data_kernel(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, __nv_bfloat16* X,
-                            float* target) {
-  const int64_t n = (int64_t)E * Te * D;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(i / D), d = (int)(i - (int64_t)t * D);
+__global__ void __launch_bounds__(ROW_THREADS) data_kernel(uint64_t seed, int64_t step, int est_base, int Te, int D,
+                                                           int rows, __nv_bfloat16* X, float* target) {
+  for (int t = blockIdx.x; t < rows; t += gridDim.x) {
     const int e = t / Te, tl = t - e * Te;
-    const uint64_t idx = ((uint64_t)step * Te + tl) * (uint64_t)D + d;
-    X[i] = __float2bfloat16_rn(uniform_pm1(derive3(TAG_FFN_X, seed, (uint64_t)(est_base + e)), idx));
-    target[i] = 0.5f * uniform_pm1(derive3(TAG_FFN_Y, seed, (uint64_t)(est_base + e)), idx);
+    const uint64_t sx = derive3(TAG_FFN_X, seed, (uint64_t)(est_base + e));
+    const uint64_t sy = derive3(TAG_FFN_Y, seed, (uint64_t)(est_base + e));
+    const uint64_t row0 = ((uint64_t)step * Te + tl) * (uint64_t)D;
+    for (int d0 = threadIdx.x * 8; d0 < D; d0 += ROW_THREADS * 8) {
+      float xv[8], yv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        xv[k] = uniform_pm1(sx, row0 + d0 + k);
+        yv[k] = 0.5f * uniform_pm1(sy, row0 + d0 + k);
+      }
+      store8(X + (size_t)t * D + d0, xv);
+      float4* tp = (float4*)(target + (size_t)t * D + d0);
+      tp[0] = make_float4(yv[0], yv[1], yv[2], yv[3]);
+      tp[1] = make_float4(yv[4], yv[5], yv[6], yv[7]);
+    }
   }
 }
 
 // h = H32 + b1 -> Hpre (bf16, kept for backward); D = dropout(gelu(h)) (bf16)
-__global__ void fwd_act_kernel(const float* __restrict__ H, const float* __restrict__ b1, uint64_t seed, int64_t step,
-                               int est_base, int E, int Te, int F, float p, __nv_bfloat16* __restrict__ Hpre,
-                               __nv_bfloat16* __restrict__ Dout) {
+__global__ void __launch_bounds__(ROW_THREADS) fwd_act_kernel(const float* __restrict__ H, const float* __restrict__ b1,
+                                                              uint64_t seed, int64_t step, int est_base, int Te,
+                                                              int F, int rows, float p, __nv_bfloat16* __restrict__ Hpre,
+                                                              __nv_bfloat16* __restrict__ Dout) {
   const float keep = p < 1.f ? 1.f / (1.f - p) : 0.f;
-  const int64_t n = (int64_t)E * Te * F;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(i / F), j = (int)(i - (int64_t)t * F);
+  for (int t = blockIdx.x; t < rows; t += gridDim.x) {
     const int e = t / Te, tl = t - e * Te;
-    const float h = H[i] + b1[j];
-    Hpre[i] = __float2bfloat16_rn(h);
-    const float m = drop_scale(derive3(TAG_FFN_DROP, seed, (uint64_t)(est_base + e)), step, Te, F, tl, j, p, keep);
-    Dout[i] = __float2bfloat16_rn(gelu(h) * m);
+    const uint64_t sd = derive3(TAG_FFN_DROP, seed, (uint64_t)(est_base + e));
+    for (int j0 = threadIdx.x * 8; j0 < F; j0 += ROW_THREADS * 8) {
+      float h[8], b[8], d[8];
+      load8(H + (size_t)t * F + j0, h);
+      load8(b1 + j0, b);
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        float m0, m1;
+        drop_scale2(sd, step, Te, F, tl, j0 + k, p, keep, &m0, &m1);
+        h[k] += b[k];
+        h[k + 1] += b[k + 1];
+        d[k] = gelu(h[k]) * m0;
+        d[k + 1] = gelu(h[k + 1]) * m1;
+      }
+      store8(Hpre + (size_t)t * F + j0, h);
+      store8(Dout + (size_t)t * F + j0, d);
+    }
   }
 }
 
@@ -104,47 +133,94 @@ __global__ void loss_final_kernel(const float* __restrict__ part, int E, int Te,
 }
 
 // dH = dropout'(dD32) * gelu'(Hpre)   (bf16)
-__global__ void bwd_act_kernel(const float* __restrict__ dD, const __nv_bfloat16* __restrict__ Hpre, uint64_t seed,
-                               int64_t step, int est_base, int E, int Te, int F, float p,
-                               __nv_bfloat16* __restrict__ dH) {
+__global__ void __launch_bounds__(ROW_THREADS) bwd_act_kernel(const float* __restrict__ dD,
+                                                              const __nv_bfloat16* __restrict__ Hpre, uint64_t seed,
+                                                              int64_t step, int est_base, int Te, int F, int rows,
+                                                              float p, __nv_bfloat16* __restrict__ dH) {
   const float keep = p < 1.f ? 1.f / (1.f - p) : 0.f;
-  const int64_t n = (int64_t)E * Te * F;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(i / F), j = (int)(i - (int64_t)t * F);
+  for (int t = blockIdx.x; t < rows; t += gridDim.x) {
     const int e = t / Te, tl = t - e * Te;
-    const float m = drop_scale(derive3(TAG_FFN_DROP, seed, (uint64_t)(est_base + e)), step, Te, F, tl, j, p, keep);
-    dH[i] = __float2bfloat16_rn(dD[i] * m * gelu_grad(__bfloat162float(Hpre[i])));
+    const uint64_t sd = derive3(TAG_FFN_DROP, seed, (uint64_t)(est_base + e));
+    for (int j0 = threadIdx.x * 8; j0 < F; j0 += ROW_THREADS * 8) {
+      float g[8], h[8];
+      load8(dD + (size_t)t * F + j0, g);
+      load8(Hpre + (size_t)t * F + j0, h);
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        float m0, m1;
+        drop_scale2(sd, step, Te, F, tl, j0 + k, p, keep, &m0, &m1);
+        g[k] = g[k] * m0 * gelu_grad(h[k]);
+        g[k + 1] = g[k + 1] * m1 * gelu_grad(h[k + 1]);
+      }
+      store8(dH + (size_t)t * F + j0, g);
+    }
   }
 }
 
-// out[e][c] = sum over r ascending of in[e][r][c]  (per-EST bias gradients)
-__global__ void colsum_kernel(const __nv_bfloat16* __restrict__ in, int E, int R, int C, float* __restrict__ out) {
+// out[e][c] = sum over r of in[e][r][c] (per-EST bias gradients), in a fixed
+// association: COLSUM_CHUNKS ascending row ranges are summed ascending into
+// partials (pass 1, parallel over chunks x columns), then the partials are
+// summed in chunk order (pass 2).  Same bits for any grid.
+constexpr int COLSUM_CHUNKS = 16;
+__global__ void colsum_part_kernel(const __nv_bfloat16* __restrict__ in, int E, int R, int C,
+                                   float* __restrict__ part) {
+  const int cpt = C / 8;
+  const int64_t n = (int64_t)E * COLSUM_CHUNKS * cpt;
+  const int rows = (R + COLSUM_CHUNKS - 1) / COLSUM_CHUNKS;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % cpt) * 8;
+    const int64_t ek = i / cpt;
+    const int k = (int)(ek % COLSUM_CHUNKS), e = (int)(ek / COLSUM_CHUNKS);
+    const int r0 = k * rows, r1 = min(R, r0 + rows);
+    const __nv_bfloat16* p = in + (size_t)e * R * C + c0;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = r0; r < r1; ++r) {
+      float v[8];
+      load8(p + (size_t)r * C, v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] += v[q];
+    }
+    float4* o = (float4*)(part + ((size_t)e * COLSUM_CHUNKS + k) * C + c0);
+    o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+__global__ void colsum_final_kernel(const float* __restrict__ part, int E, int C, float* __restrict__ out) {
   const int64_t n = (int64_t)E * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int e = (int)(i / C), c = (int)(i - (int64_t)e * C);
-    const __nv_bfloat16* p = in + (size_t)e * R * C + c;
-    float acc = 0.f;
-    for (int r = 0; r < R; ++r) acc += __bfloat162float(p[(size_t)r * C]);
+    float acc = part[((size_t)e * COLSUM_CHUNKS) * C + c];
+    for (int k = 1; k < COLSUM_CHUNKS; ++k) acc += part[((size_t)e * COLSUM_CHUNKS + k) * C + c];
     out[i] = acc;
   }
 }
 
-// out[e][c][r] = in[e][r][c]: 32x32 tiles through shared memory
+// out[e][c][r] = in[e][r][c]: 64x64 tiles through shared memory, 4-byte
+// (two-element) accesses on both sides
 template <class Tin>
-__global__ void transpose_kernel(const Tin* __restrict__ in, int R, int C, __nv_bfloat16* __restrict__ out) {
-  __shared__ float tile[32][33];
+__global__ void __launch_bounds__(256) transpose_kernel(const Tin* __restrict__ in, int R, int C,
+                                                        __nv_bfloat16* __restrict__ out) {
+  __shared__ float tile[64][65];
   const int e = blockIdx.z;
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
   const Tin* src = in + (size_t)e * R * C;
   __nv_bfloat16* dst = out + (size_t)e * R * C;
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    const int r = r0 + k, c = c0 + threadIdx.x;
-    if (r < R && c < C) tile[k][threadIdx.x] = (float)src[(size_t)r * C + c];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int k = ty; k < 64; k += 8) {
+    const int r = r0 + k, c = c0 + 2 * tx;
+    if (r < R && c + 1 < C) {
+      float2 v;
+      if constexpr (sizeof(Tin) == 4) v = *(const float2*)(src + (size_t)r * C + c);
+      else v = __bfloat1622float2(*(const __nv_bfloat162*)(src + (size_t)r * C + c));
+      tile[k][2 * tx] = v.x;
+      tile[k][2 * tx + 1] = v.y;
+    }
   }
   __syncthreads();
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    const int c = c0 + k, r = r0 + threadIdx.x;
-    if (r < R && c < C) dst[(size_t)c * R + r] = __float2bfloat16_rn(tile[threadIdx.x][k]);
+  for (int k = ty; k < 64; k += 8) {
+    const int c = c0 + k, r = r0 + 2 * tx;
+    if (c < C && r + 1 < R)
+      *(__nv_bfloat162*)(dst + (size_t)c * R + r) = __floats2bfloat162_rn(tile[2 * tx][k], tile[2 * tx + 1][k]);
   }
 }
 
@@ -161,16 +237,20 @@ static int grid_for(int64_t n) {
 }
 static int ok_or_cuda() { return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA; }
 
+static int row_grid(int rows) { return rows < 148 * 16 ? rows : 148 * 16; }
+
 int ffn_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, void* X, float* target,
                     cudaStream_t s) {
-  ffn::data_kernel<<<grid_for((int64_t)E * Te * D), 256, 0, s>>>(seed, step, est_base, E, Te, D,
-                                                                   (__nv_bfloat16*)X, target);
+  if (D % 8) return ERR_INPUT;
+  ffn::data_kernel<<<row_grid(E * Te), ffn::ROW_THREADS, 0, s>>>(seed, step, est_base, Te, D, E * Te,
+                                                                    (__nv_bfloat16*)X, target);
   return ok_or_cuda();
 }
 int ffn_fwd_act_launch(const float* H, const float* b1, uint64_t seed, int64_t step, int est_base, int E, int Te,
                        int F, float p, void* Hpre, void* Dout, cudaStream_t s) {
-  ffn::fwd_act_kernel<<<grid_for((int64_t)E * Te * F), 256, 0, s>>>(H, b1, seed, step, est_base, E, Te, F, p,
-                                                                      (__nv_bfloat16*)Hpre, (__nv_bfloat16*)Dout);
+  if (F % 8) return ERR_INPUT;
+  ffn::fwd_act_kernel<<<row_grid(E * Te), ffn::ROW_THREADS, 0, s>>>(H, b1, seed, step, est_base, Te, F, E * Te, p,
+                                                                       (__nv_bfloat16*)Hpre, (__nv_bfloat16*)Dout);
   return ok_or_cuda();
 }
 int ffn_out_launch(const float* Y, const float* b2, const float* target, int E, int Te, int D, void* dY, float* part,
@@ -182,20 +262,33 @@ int ffn_out_launch(const float* Y, const float* b2, const float* target, int E, 
 }
 int ffn_bwd_act_launch(const float* dD, const void* Hpre, uint64_t seed, int64_t step, int est_base, int E, int Te,
                        int F, float p, void* dH, cudaStream_t s) {
-  ffn::bwd_act_kernel<<<grid_for((int64_t)E * Te * F), 256, 0, s>>>(dD, (const __nv_bfloat16*)Hpre, seed, step,
-                                                                      est_base, E, Te, F, p, (__nv_bfloat16*)dH);
+  if (F % 8) return ERR_INPUT;
+  ffn::bwd_act_kernel<<<row_grid(E * Te), ffn::ROW_THREADS, 0, s>>>(dD, (const __nv_bfloat16*)Hpre, seed, step,
+                                                                       est_base, Te, F, E * Te, p, (__nv_bfloat16*)dH);
   return ok_or_cuda();
 }
-int colsum_bf16_launch(const void* in, int E, int R, int C, float* out, cudaStream_t s) {
-  ffn::colsum_kernel<<<grid_for((int64_t)E * C), 256, 0, s>>>((const __nv_bfloat16*)in, E, R, C, out);
+int colsum_bf16_launch(const void* in, int E, int R, int C, float* out, float* scratch, cudaStream_t s) {
+  if (C % 8) return ERR_INPUT;
+  float* part = scratch;  // E * COLSUM_CHUNKS * C partials
+  bool own = false;
+  if (!part) {
+    if (cudaMallocAsync((void**)&part, sizeof(float) * (size_t)E * ffn::COLSUM_CHUNKS * C, s) != cudaSuccess)
+      return ERR_CUDA;
+    own = true;
+  }
+  ffn::colsum_part_kernel<<<grid_for((int64_t)E * ffn::COLSUM_CHUNKS * C / 8), 256, 0, s>>>(
+      (const __nv_bfloat16*)in, E, R, C, part);
+  ffn::colsum_final_kernel<<<grid_for((int64_t)E * C), 256, 0, s>>>(part, E, C, out);
+  if (own) cudaFreeAsync(part, s);
   return ok_or_cuda();
 }
 int transpose_launch(const void* in, int in_f32, int E, int R, int C, void* out, cudaStream_t s) {
-  const dim3 grid((C + 31) / 32, (R + 31) / 32, E), block(32, 8);
+  if (R % 2 || C % 2) return ERR_INPUT;
+  const dim3 grid((C + 63) / 64, (R + 63) / 64, E);
   if (in_f32)
-    ffn::transpose_kernel<float><<<grid, block, 0, s>>>((const float*)in, R, C, (__nv_bfloat16*)out);
+    ffn::transpose_kernel<float><<<grid, 256, 0, s>>>((const float*)in, R, C, (__nv_bfloat16*)out);
   else
-    ffn::transpose_kernel<__nv_bfloat16><<<grid, block, 0, s>>>((const __nv_bfloat16*)in, R, C, (__nv_bfloat16*)out);
+    ffn::transpose_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)in, R, C, (__nv_bfloat16*)out);
   return ok_or_cuda();
 }
 int cast_f32_bf16_launch(const float* in, int64_t n, void* out, cudaStream_t s) {

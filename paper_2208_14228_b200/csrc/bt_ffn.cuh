@@ -1,0 +1,65 @@
+// bt_ffn.cuh -- element math of the per-EST FFN step, shared by the fused
+// GEMM epilogues (bt_gemm.cu) and the standalone kernels (bt_ffn.cu).
+// All randomness is counter-form splitmix64 keyed by (seed, global EST rank,
+// step, element) -- never by the launch, tile or GPU.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "bt_common.cuh"
+
+namespace bt {
+namespace ffn {
+
+constexpr uint64_t TAG_FFN_X = 0x4646'4e5f'5844'4154ull;     // "FFN_XDAT"
+constexpr uint64_t TAG_FFN_Y = 0x4646'4e5f'5944'4154ull;     // "FFN_YDAT"
+constexpr uint64_t TAG_FFN_DROP = 0x4646'4e5f'4452'4f50ull;  // "FFN_DROP"
+
+__device__ __forceinline__ float uniform_pm1(uint64_t stream, uint64_t n) {  // [-1, 1)
+  return (float)(unit_float(draw_raw(stream, n)) * 2.0 - 1.0);
+}
+
+// Dropout masks: one splitmix64 draw per PAIR of units (j even, j+1): the low
+// and high 32-bit halves decide units j and j+1; a unit is dropped iff its
+// half < ceil(p * 2^32).  Keyed by (EST stream, step, token, unit pair).
+__device__ __forceinline__ uint32_t drop_threshold32(float p) { return (uint32_t)ceil((double)p * 0x1p32); }
+__device__ __forceinline__ void drop_scale2(uint64_t stream, int64_t step, int Te, int F, int tl, int j, float p,
+                                            float keep, float* m0, float* m1) {  // j even
+  if (p <= 0.f) {
+    *m0 = *m1 = 1.f;
+    return;
+  }
+  const uint64_t n = (((uint64_t)step * (uint64_t)Te + (uint64_t)tl) * (uint64_t)F + (uint64_t)j) >> 1;
+  const uint64_t r = draw_raw(stream, n);
+  const uint32_t t = drop_threshold32(p);
+  *m0 = (uint32_t)r < t ? 0.f : keep;
+  *m1 = (uint32_t)(r >> 32) < t ? 0.f : keep;
+}
+
+__device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_grad(float x) {
+  return 0.5f * (1.f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * expf(-0.5f * x * x);
+}
+
+}  // namespace ffn
+
+// GEMM epilogue selector (bt_gemm.cu): what the epilogue warps do with a
+// row-chunk of fp32 accumulators instead of storing them.
+enum GemmEpiKind : int {
+  EPI_STORE = 0,    // C = acc (fp32 or bf16)
+  EPI_FFN_FWD = 1,  // h = acc + bias[j]: C = bf16(h) (pre-activation), out2 = bf16(dropout(gelu(h)))
+  EPI_FFN_BWD = 2,  // C = bf16(acc * dropout_scale * gelu'(aux[row][j]))   (aux = pre-activation, bf16)
+};
+struct GemmEpi {
+  int kind;
+  const float* bias;          // [N] (FFN_FWD)
+  const __nv_bfloat16* aux;   // [M][N] (FFN_BWD)
+  __nv_bfloat16* out2;        // [M][N] (FFN_FWD)
+  uint64_t seed;
+  int64_t step;
+  int est_base, Te;           // row r belongs to EST est_base + r / Te
+  float p;
+};
+
+}  // namespace bt

@@ -30,12 +30,15 @@
 #include <stdlib.h>
 
 #include "bt_common.cuh"
+#include "bt_ffn.cuh"
 
 namespace bt {
 namespace gemm {
 
 constexpr int BM = 128, BK = 64, UK = 16;  // tile M, k-block (128 B of bf16), UMMA K
-constexpr int THREADS = 192;
+constexpr int EPI_WARPS = 16;  // four per TMEM lane group, each draining a quarter of the tile's columns
+constexpr int EPI_SPLIT = EPI_WARPS / 4;
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -119,6 +122,71 @@ __device__ __forceinline__ void tile_coords_bn(int t, int mt, int nt, int* m0, i
   *n0 = (r / gm) * BN;
 }
 
+
+// Store one epilogue chunk: 32 consecutive fp32 accumulators of row `row`,
+// columns [col, col+32) -- plain (fp32 / bf16) or an FFN element op fused in.
+template <bool OUT_BF16>
+__device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, int col, int N, void* c,
+                                               const GemmEpi& epi) {
+  float f[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
+  if (epi.kind == EPI_STORE && !OUT_BF16) {
+    uint4* dst = (uint4*)((float*)c + row * N + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    return;
+  }
+  float g[32];  // second output (FFN_FWD)
+  if (epi.kind != EPI_STORE) {
+    const int e = (int)(row / (size_t)epi.Te), tl = (int)(row - (size_t)e * epi.Te);
+    const uint64_t sd = derive3(ffn::TAG_FFN_DROP, epi.seed, (uint64_t)(epi.est_base + e));
+    const float keep = epi.p < 1.f ? 1.f / (1.f - epi.p) : 0.f;
+    if (epi.kind == EPI_FFN_FWD) {
+#pragma unroll
+      for (int q = 0; q < 32; q += 2) {
+        float m0, m1;
+        ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
+        f[q] += epi.bias[col + q];
+        f[q + 1] += epi.bias[col + q + 1];
+        g[q] = ffn::gelu(f[q]) * m0;
+        g[q + 1] = ffn::gelu(f[q + 1]) * m1;
+      }
+    } else {
+      const uint4* ap = (const uint4*)(epi.aux + row * N + col);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const uint4 u = ap[q4];
+        const __nv_bfloat162* h2 = (const __nv_bfloat162*)&u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 hp = __bfloat1622float2(h2[k]);
+          const int q = q4 * 8 + 2 * k;
+          float m0, m1;
+          ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
+          f[q] = f[q] * m0 * ffn::gelu_grad(hp.x);
+          f[q + 1] = f[q + 1] * m1 * ffn::gelu_grad(hp.y);
+        }
+      }
+    }
+  }
+  auto store_bf16 = [&](__nv_bfloat16* base, const float* x) {
+    uint4* dst = (uint4*)(base + row * N + col);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t w[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const __nv_bfloat162 b2 = __floats2bfloat162_rn(x[q * 8 + 2 * h], x[q * 8 + 2 * h + 1]);
+        w[h] = *(const uint32_t*)&b2;
+      }
+      dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  };
+  store_bf16((__nv_bfloat16*)c, f);
+  if (epi.kind == EPI_FFN_FWD) store_bf16(epi.out2, g);
+}
+
 template <int BN, int STAGES>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
@@ -130,7 +198,7 @@ struct Smem {
 template <int BN, int STAGES, bool OUT_BF16>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                        void* __restrict__ c, int M, int N, int K, int batch) {
+                        void* __restrict__ c, int M, int N, int K, int batch, const GemmEpi epi) {
   using L = Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
@@ -160,7 +228,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 4);  // one arrival per epilogue warp
+      mbar_init(tempty(a), EPI_WARPS);  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -228,6 +296,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {
     // ---- epilogue: TMEM -> registers -> global -------------------------------
     const int lg = warp & 3;  // TMEM lane group this warp may access (lanes 32*lg ...)
+    const int half = (warp - 2) >> 2;  // which column slice (of EPI_SPLIT)
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int acc = i & 1;
@@ -237,7 +306,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const size_t row = (size_t)(t / per_batch) * M + m0 + lg * 32 + lane;  // batch entries stacked in C
 #pragma unroll 1
-      for (int cc = 0; cc < BN; cc += 32) {
+      for (int cc = half * (BN / EPI_SPLIT); cc < (half + 1) * (BN / EPI_SPLIT); cc += 32) {
         uint32_t v[32];
         const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * BN + cc);
         asm volatile(
@@ -249,24 +318,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (OUT_BF16) {
-          uint4* dst = (uint4*)((__nv_bfloat16*)c + row * N + n0 + cc);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t w[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              const __nv_bfloat162 b2 =
-                  __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * h]), __uint_as_float(v[q * 8 + 2 * h + 1]));
-              w[h] = *(const uint32_t*)&b2;
-            }
-            dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        } else {
-          uint4* dst = (uint4*)((float*)c + row * N + n0 + cc);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        }
+        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, c, epi);
       }
       tc_fence_before();
       __syncwarp();
@@ -339,7 +391,7 @@ struct PairSmem {
 template <int STAGES, bool OUT_BF16>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                             void* __restrict__ c, int M, int N, int K, int batch) {
+                             void* __restrict__ c, int M, int N, int K, int batch, const GemmEpi epi) {
   using L = PairSmem<STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
@@ -378,7 +430,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 8);  // leader: 4 epilogue warps x 2 CTAs
+      mbar_init(tempty(a), 2 * EPI_WARPS);  // leader: every epilogue warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -445,6 +497,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {  // ---- epilogue (both CTAs: own 128 rows) ----
     const int lg = warp & 3;
+    const int half = (warp - 2) >> 2;
     const uint32_t leader_tempty0 = map_to_rank(tempty(0), 0), leader_tempty1 = map_to_rank(tempty(1), 0);
     int i = 0;
     for (int t = pair; t < tiles; t += pairs, ++i) {
@@ -455,7 +508,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const size_t row = (size_t)(t / per_batch) * M + m0 + (int)rank * BM + lg * 32 + lane;
 #pragma unroll 1
-      for (int cc = 0; cc < PAIR_BN; cc += 32) {
+      for (int cc = half * (PAIR_BN / EPI_SPLIT); cc < (half + 1) * (PAIR_BN / EPI_SPLIT); cc += 32) {
         uint32_t v[32];
         const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * PAIR_BN + cc);
         asm volatile(
@@ -467,24 +520,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (OUT_BF16) {
-          uint4* dst = (uint4*)((__nv_bfloat16*)c + row * N + n0 + cc);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t w[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              const __nv_bfloat162 b2 =
-                  __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * h]), __uint_as_float(v[q * 8 + 2 * h + 1]));
-              w[h] = *(const uint32_t*)&b2;
-            }
-            dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        } else {
-          uint4* dst = (uint4*)((float*)c + row * N + n0 + cc);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        }
+        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, c, epi);
       }
       tc_fence_before();
       __syncwarp();
@@ -538,6 +574,7 @@ struct GemmShape {
   void* c;
   int M, N, K, batch;
   int64_t sa, sb;  // batch strides of A and B in elements (C is [batch][M][N] contiguous)
+  GemmEpi epi;
 };
 
 template <int BN, int STAGES, bool OUT_BF16>
@@ -562,7 +599,7 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
     grid = sms;
   }
   if (grid > tiles) grid = tiles;
-  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, g.c, M, N, K, g.batch);
+  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, g.c, M, N, K, g.batch, g.epi);
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
@@ -603,7 +640,7 @@ static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
   attr_[0].val.clusterDim.z = 1;
   cfg.attrs = attr_;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb, g.c, M, N, K, g.batch) == cudaSuccess ? OK : ERR_CUDA;
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, g.c, M, N, K, g.batch, g.epi) == cudaSuccess ? OK : ERR_CUDA;
 }
 
 static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests, measurements)
@@ -612,14 +649,21 @@ static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests
 }
 
 // 256 x 256 CTA-pair tiles when M and N allow it, else 128 x {256, 128} tiles (all deterministic)
-int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
-                        int64_t sb, int out_bf16, int grid, cudaStream_t s) {
-  const GemmShape g{a, b, c, M, N, K, batch, sa, sb};
+int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
+                            int64_t sb, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s) {
+  const GemmShape g{a, b, c, M, N, K, batch, sa, sb, epi};
+  if (epi.kind != EPI_STORE) out_bf16 = 1;
   if (M % 256 == 0 && N % 256 == 0 && gemm_variant() != 1)
     return out_bf16 ? launch_gemm_pair<6, true>(g, grid, s) : launch_gemm_pair<6, false>(g, grid, s);
   if (N % 256 == 0)
     return out_bf16 ? launch_gemm<256, 4, true>(g, grid, s) : launch_gemm<256, 4, false>(g, grid, s);
   return out_bf16 ? launch_gemm<128, 6, true>(g, grid, s) : launch_gemm<128, 6, false>(g, grid, s);
+}
+int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
+                        int64_t sb, int out_bf16, int grid, cudaStream_t s) {
+  GemmEpi epi{};
+  epi.kind = EPI_STORE;
+  return gemm_bf16_tn_launch_epi(a, b, c, batch, M, N, K, sa, sb, out_bf16, grid, epi, s);
 }
 
 }  // namespace bt

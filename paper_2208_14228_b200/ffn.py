@@ -46,14 +46,17 @@ class FFNJob:
     """E ESTs x `tokens` tokens each, one FFN sublayer, momentum SGD on fp32 master weights."""
 
     def __init__(self, ests: int, tokens: int, d_model: int = 768, d_ff: int = 3072, seed: int = 42,
-                 lr: float = 1e-2, momentum: float = 0.9, dropout: float = 0.1, fanin: int = 0):
+                 lr: float = 1e-2, momentum: float = 0.9, dropout: float = 0.1, fanin: int = 0, fused: bool = True):
         require_cuda()
         if tokens % 128 or d_model % 128 or d_ff % 128:
             raise ConfigError("tokens, d_model and d_ff must be multiples of 128")
+        if ests > _native.BT_MAX_TABLE:
+            raise ConfigError(f"at most {_native.BT_MAX_TABLE} ESTs per job")
         if fanin not in (0, 2) or (fanin == 2 and ests & (ests - 1)):
             raise ConfigError("allreduce variant: Sequential (0) or Tree(2) with a power-of-two EST count")
         self.E, self.Te, self.D, self.F = ests, tokens, d_model, d_ff
         self.seed, self.lr, self.mu, self.p, self.fanin = seed, lr, momentum, dropout, fanin
+        self.fused = fused  # element ops in the GEMM epilogues (False: standalone kernels, same math)
         D, F = d_model, d_ff
         self.W1 = _init_uniform(seed, F * D, D ** -0.5).view(F, D)
         self.b1 = torch.zeros(F, device="cuda")
@@ -63,57 +66,75 @@ class FFNJob:
         self.vel = [torch.zeros_like(t) for t in self.params]
         self.step_idx = 0
         self.flags = Flags()
+        self._ws = {}
+        self._grads = [torch.empty(ests, t.numel(), dtype=torch.float32, device="cuda") for t in self.params]
         self._refresh_bf16()
 
     # -- bf16 operand copies of the master weights (W2^T for the dD product)
     def _refresh_bf16(self):
         L, s = _native.lib(), stream()
-        self.W1h = torch.empty(self.F, self.D, dtype=torch.bfloat16, device="cuda")
-        self.W2h = torch.empty(self.D, self.F, dtype=torch.bfloat16, device="cuda")
-        self.W2t = torch.empty(self.F, self.D, dtype=torch.bfloat16, device="cuda")
+        if not hasattr(self, "W1h"):
+            self.W1h = torch.empty(self.F, self.D, dtype=torch.bfloat16, device="cuda")
+            self.W2h = torch.empty(self.D, self.F, dtype=torch.bfloat16, device="cuda")
+            self.W2t = torch.empty(self.F, self.D, dtype=torch.bfloat16, device="cuda")
         _native.check(L.bt_cast_f32_bf16(self.W1.data_ptr(), self.W1.numel(), self.W1h.data_ptr(), s))
         _native.check(L.bt_cast_f32_bf16(self.W2.data_ptr(), self.W2.numel(), self.W2h.data_ptr(), s))
         _native.check(L.bt_transpose_to_bf16(self.W2.data_ptr(), 1, 1, self.D, self.F, self.W2t.data_ptr(), s))
+
+    def _workspace(self, n: int) -> dict:
+        """Activation / scratch buffers of an n-EST group, allocated once and reused every step."""
+        ws = self._ws.get(n)
+        if ws is None:
+            D, F, Te, T = self.D, self.F, self.Te, n * self.Te
+            bf, f32 = dict(dtype=torch.bfloat16, device="cuda"), dict(dtype=torch.float32, device="cuda")
+            ws = {"X": torch.empty(T, D, **bf), "tgt": torch.empty(T, D, **f32), "Hpre": torch.empty(T, F, **bf),
+                  "D": torch.empty(T, F, **bf), "Y": torch.empty(T, D, **f32), "dY": torch.empty(T, D, **bf),
+                  "dH": torch.empty(T, F, **bf), "part": torch.empty(n * _P, **f32),
+                  "dYt": torch.empty(n, D, Te, **bf), "Dt": torch.empty(n, F, Te, **bf),
+                  "dHt": torch.empty(n, F, Te, **bf), "Xt": torch.empty(n, D, Te, **bf),
+                  "colsum": torch.empty(n * 16 * F, **f32)}
+            if not self.fused:
+                ws["H"] = torch.empty(T, F, **f32)
+            self._ws[n] = ws
+        return ws
 
     def _group(self, base: int, n: int, grads: list, losses: torch.Tensor, capture: dict | None = None):
         """Forward/backward of ESTs [base, base+n): per-EST gradients into grads[*][base:base+n]."""
         L, s = _native.lib(), stream()
         D, F, Te, T = self.D, self.F, self.Te, n * self.Te
         seed, step, p = self.seed & (2**64 - 1), self.step_idx, self.p
-        X = torch.empty(T, D, dtype=torch.bfloat16, device="cuda")
-        tgt = torch.empty(T, D, dtype=torch.float32, device="cuda")
+        w = self._workspace(n)
+        X, tgt, Hpre, Dact, dY, dH = w["X"], w["tgt"], w["Hpre"], w["D"], w["dY"], w["dH"]
         _native.check(L.bt_ffn_data(seed, step, base, n, Te, D, X.data_ptr(), tgt.data_ptr(), s))
-        H = gemm_bf16(X, self.W1h)                                     # [T][F] = X W1^T
-        Hpre = torch.empty(T, F, dtype=torch.bfloat16, device="cuda")
-        Dact = torch.empty(T, F, dtype=torch.bfloat16, device="cuda")
-        _native.check(L.bt_ffn_fwd_act(H.data_ptr(), self.b1.data_ptr(), seed, step, base, n, Te, F, p,
-                                       Hpre.data_ptr(), Dact.data_ptr(), s))
-        del H
-        Y = gemm_bf16(Dact, self.W2h)                                  # [T][D] = dropout(gelu) W2^T
-        dY = torch.empty(T, D, dtype=torch.bfloat16, device="cuda")
-        part = torch.empty(n * _P, dtype=torch.float32, device="cuda")
-        _native.check(L.bt_ffn_out(Y.data_ptr(), self.b2.data_ptr(), tgt.data_ptr(), n, Te, D, dY.data_ptr(),
-                                   part.data_ptr(), losses[base:].data_ptr(), s))
-        del Y, tgt
-        dD = gemm_bf16(dY, self.W2t)                                   # [T][F] = dY W2
-        dH = torch.empty(T, F, dtype=torch.bfloat16, device="cuda")
-        _native.check(L.bt_ffn_bwd_act(dD.data_ptr(), Hpre.data_ptr(), seed, step, base, n, Te, F, p,
-                                       dH.data_ptr(), s))
-        del dD, Hpre
+        if self.fused:  # X W1^T with bias + GELU + dropout in the GEMM epilogue
+            _native.check(L.bt_gemm_bf16_ffn(X.data_ptr(), self.W1h.data_ptr(), Hpre.data_ptr(), T, F, D, 1,
+                                             self.b1.data_ptr(), None, Dact.data_ptr(), seed, step, base, Te, p, 0,
+                                             s), "ffn forward GEMM")
+        else:
+            gemm_bf16(X, self.W1h, out=w["H"])                         # [T][F] = X W1^T
+            _native.check(L.bt_ffn_fwd_act(w["H"].data_ptr(), self.b1.data_ptr(), seed, step, base, n, Te, F, p,
+                                           Hpre.data_ptr(), Dact.data_ptr(), s))
+        gemm_bf16(Dact, self.W2h, out=w["Y"])                          # [T][D] = dropout(gelu) W2^T
+        _native.check(L.bt_ffn_out(w["Y"].data_ptr(), self.b2.data_ptr(), tgt.data_ptr(), n, Te, D, dY.data_ptr(),
+                                   w["part"].data_ptr(), losses[base:].data_ptr(), s))
+        if self.fused:  # dY W2 with dropout' and GELU' in the GEMM epilogue
+            _native.check(L.bt_gemm_bf16_ffn(dY.data_ptr(), self.W2t.data_ptr(), dH.data_ptr(), T, F, D, 2, None,
+                                             Hpre.data_ptr(), None, seed, step, base, Te, p, 0, s),
+                          "ffn backward GEMM")
+        else:
+            gemm_bf16(dY, self.W2t, out=w["H"])                        # [T][F] = dY W2
+            _native.check(L.bt_ffn_bwd_act(w["H"].data_ptr(), Hpre.data_ptr(), seed, step, base, n, Te, F, p,
+                                           dH.data_ptr(), s))
         # per-EST weight gradients: K = the EST's own tokens (transposed, token-contiguous operands)
-        dYt = torch.empty(n, D, Te, dtype=torch.bfloat16, device="cuda")
-        Dt = torch.empty(n, F, Te, dtype=torch.bfloat16, device="cuda")
-        dHt = torch.empty(n, F, Te, dtype=torch.bfloat16, device="cuda")
-        Xt = torch.empty(n, D, Te, dtype=torch.bfloat16, device="cuda")
-        for src, dst, cols in ((dY, dYt, D), (Dact, Dt, F), (dH, dHt, F), (X, Xt, D)):
+        for src, dst, cols in ((dY, w["dYt"], D), (Dact, w["Dt"], F), (dH, w["dHt"], F), (X, w["Xt"], D)):
             _native.check(L.bt_transpose_to_bf16(src.data_ptr(), 0, n, Te, cols, dst.data_ptr(), s))
         if capture is not None:
-            capture.update(X=X, D=Dact, dY=dY, dH=dH)
+            capture.update(X=X.clone(), D=Dact.clone(), dY=dY.clone(), dH=dH.clone())
         gW1, gb1, gW2, gb2 = grads
-        gemm_bf16_batched(dHt, Xt, out=gW1[base:base + n])     # dW1_e = dH_e^T X_e   [n][F][D]
-        gemm_bf16_batched(dYt, Dt, out=gW2[base:base + n])     # dW2_e = dY_e^T D_e   [n][D][F]
-        _native.check(L.bt_colsum_bf16(dH.data_ptr(), n, Te, F, gb1[base:].data_ptr(), s))
-        _native.check(L.bt_colsum_bf16(dY.data_ptr(), n, Te, D, gb2[base:].data_ptr(), s))
+        gemm_bf16_batched(w["dHt"], w["Xt"], out=gW1[base:base + n])     # dW1_e = dH_e^T X_e   [n][F][D]
+        gemm_bf16_batched(w["dYt"], w["Dt"], out=gW2[base:base + n])     # dW2_e = dY_e^T D_e   [n][D][F]
+        _native.check(L.bt_colsum_bf16(dH.data_ptr(), n, Te, F, gb1[base:].data_ptr(), w["colsum"].data_ptr(), s))
+        _native.check(L.bt_colsum_bf16(dY.data_ptr(), n, Te, D, gb2[base:].data_ptr(), w["colsum"].data_ptr(), s))
 
     def step(self, groups: list[int] | None = None, capture: dict | None = None) -> torch.Tensor:
         """One mini-batch of all E ESTs; `groups` = EST counts per launch group (default: one group).
@@ -122,7 +143,7 @@ class FFNJob:
         if sum(groups) != self.E or min(groups) < 1:
             raise ConfigError(f"groups {groups} must partition {self.E} ESTs")
         E = self.E
-        grads = [torch.empty(E, t.numel(), dtype=torch.float32, device="cuda") for t in self.params]
+        grads = self._grads
         losses = torch.empty(E, dtype=torch.float32, device="cuda")
         base = 0
         for n in groups:
@@ -141,7 +162,8 @@ class FFNJob:
         for g, prm, vel in zip(grads, self.params, self.vel):
             a = _native.ReduceArgs()
             a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, self.E, self.fanin, prm.numel()
-            a.grads[0], a.grads_ld = g.data_ptr(), prm.numel()
+            for k in range(self.E):  # a pointer table (the 16-byte-vector fast path), EST-rank order
+                a.grads[k] = g[k].data_ptr()
             a.param, a.vel, a.param_out, a.vel_out = prm.data_ptr(), vel.data_ptr(), prm.data_ptr(), vel.data_ptr()
             a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
             _native.check(L.bt_reduce_update(C.byref(a), s), "ffn reduce_update")
