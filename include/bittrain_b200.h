@@ -150,6 +150,52 @@ int bt_colsum_bf16(const void *in_dev, int32_t E, int32_t R, int32_t C, float *o
 int bt_transpose_to_bf16(const void *in_dev, int32_t in_f32, int32_t E, int32_t R, int32_t C, void *out_dev,
                          void *stream);
 int bt_cast_f32_bf16(const float *in_dev, int64_t n, void *out_dev, void *stream);
+/* General form of the GEMM: batch strides for A, B and C (stride_c = 0: M*N) -- e.g. per-EST weight
+ * gradients written straight into each EST's slot of a [E][P] gradient buffer; bias_dev (or NULL)
+ * is added to every row in the epilogue (C = A*B^T + bias). */
+int bt_gemm_bf16_tn_ex(const void *a_dev, const void *b_dev, void *c_dev, int32_t batch, int32_t M, int32_t N,
+                       int32_t K, int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype,
+                       const float *bias_dev, int32_t grid, void *stream);
+/* bt_colsum_bf16 with out[e][c] at out_dev + e*out_stride + c */
+int bt_colsum_bf16_strided(const void *in_dev, int32_t E, int32_t R, int32_t C, float *out_dev, int64_t out_stride,
+                           float *scratch_dev, void *stream);
+
+/* ---------------- per-EST BERT encoder step (C4, no reference) ------------
+ * Post-LN BERT layer (attention with 64-wide heads over 128-token sequences,
+ * LayerNorm, GELU FFN, hidden and attention-probability dropout).  Tokens of
+ * local EST e are rows [e*Te, (e+1)*Te), Te % 128 == 0, D % 256 == 0.  Every
+ * random draw is keyed by (seed, est_base + e, step, layer, element), every
+ * sum has a shape fixed by the EST's own data: an EST's results do not depend
+ * on which ESTs share the launch or the GPU.           analogue of model.py:107-196 */
+int bt_bert_data(uint64_t seed, int64_t step, int32_t est_base, int32_t E, int32_t Te, int32_t D, float *x32_dev,
+                 void *xb_dev, float *target_dev, void *stream);
+/* forward (backward = 0): ctx[T][D] = dropout(softmax(Q K^T / 8)) V per (sequence, head), qkv [T][3D] bf16;
+ * backward (1): out = dqkv [T][3D] from qkv and dctx [T][D] (P recomputed bit-identically) */
+int bt_bert_attn(int32_t backward, const void *qkv_dev, const void *dctx_dev, void *out_dev, int32_t E, int32_t Te,
+                 int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed, int64_t step,
+                 float p, void *stream);
+/* x = resid + dropout(branch + bias); y = LayerNorm(x) * gamma + beta -> xsum (x), stats (mean, rstd)
+ * [T][2], y32, yb (bf16) */
+int bt_bert_ln_fwd(const float *resid_dev, const float *branch_dev, const float *bias_dev, const float *gamma_dev,
+                   const float *beta_dev, float *xsum_dev, float *stats_dev, float *y32_dev, void *yb_dev, int32_t E,
+                   int32_t Te, int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
+                   int64_t step, float p, float eps, void *stream);
+/* dx = LayerNorm'(dy1 + dy2) (dy2 may be NULL), dbranch = bf16(dropout'(dx)); part [E][Te/64][3][D]
+ * = per-64-row-chunk column sums of (dy*xhat, dy, dropout'(dx)) */
+int bt_bert_ln_bwd(const float *dy1_dev, const float *dy2_dev, const float *xsum_dev, const float *stats_dev,
+                   const float *gamma_dev, float *dx_dev, void *dbranch_dev, float *part_dev, int32_t E, int32_t Te,
+                   int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
+                   int64_t step, float p, void *stream);
+/* chunk partials summed in chunk order -> dgamma/dbeta/dbias of EST e at + e*est_stride */
+int bt_bert_ln_fold(const float *part_dev, int32_t E, int32_t Te, int32_t D, float *dgamma_dev, float *dbeta_dev,
+                    float *dbias_dev, int64_t est_stride, void *stream);
+/* loss[e] = sum 0.5*(y-target)^2 / Te, dy = (y-target)/Te (fp32); partials_dev: E*64 floats */
+int bt_bert_mse(const float *y_dev, const float *target_dev, int32_t E, int32_t Te, int32_t D, float *dy_dev,
+                float *partials_dev, float *loss_dev, void *stream);
+/* bf16 operand copies of fp32 master weights, one launch: wb[i] = bf16(w[i]) [rows][cols],
+ * wt[i] = bf16(w[i])^T [cols][rows] */
+int bt_cast_weights_bf16(const float *const *w_dev, void *const *wb_dev, void *const *wt_dev, const int32_t *rows,
+                         const int32_t *cols, int32_t n, void *stream);
 
 /* ---------------- L3 data ------------------------------------------------- */
 /* make_dataset(seed, n, dim): [n][dim+1], x then y                       sampling.py:24-35 */

@@ -96,6 +96,19 @@ EXPORTS = {
     "bt_colsum_bf16": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _vp]),
     "bt_transpose_to_bf16": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "bt_cast_f32_bf16": (C.c_int, [_vp, _i64, _vp, _vp]),
+    "bt_gemm_bf16_tn_ex": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _i32, _vp, _i32,
+                                     _vp]),
+    "bt_colsum_bf16_strided": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i64, _vp, _vp]),
+    "bt_bert_data": (C.c_int, [_u64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "bt_bert_attn": (C.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _u64, _i64,
+                               C.c_float, _vp]),
+    "bt_bert_ln_fwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
+                                 _i32, _u64, _i64, C.c_float, C.c_float, _vp]),
+    "bt_bert_ln_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
+                                 _u64, _i64, C.c_float, _vp]),
+    "bt_bert_ln_fold": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp]),
+    "bt_bert_mse": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "bt_cast_weights_bf16": (C.c_int, [C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i32p, _i32p, _i32, _vp]),
     "bt_sgd_step_f64": (C.c_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp, _vp, _vp]),
     "bt_make_dataset": (C.c_int, [_u64, _i64, _i32, _vp, _vp]),
     "bt_jitter_gather": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i64, _u64, _i64, _i64, _dbl, _vp, _vp]),

@@ -1,0 +1,310 @@
+"""Per-EST BERT encoder training step -- C4 (BASELINE.json configs[3]).
+
+A post-LN BERT encoder (BERT-base: 12 layers, d_model 768, 12 heads of 64,
+FFN 3072, sequence 128, hidden and attention-probability dropout 0.1) trained
+data-parallel by E virtual workers (ESTs), EasyScale-style:
+
+* every EST's randomness (its synthetic inputs and targets, every dropout
+  mask) is keyed by (seed, EST rank, step, layer, element), never by the
+  launch or the GPU -- the reference keys dropout by rank the same way
+  (model.py:151-161);
+* the dense products run on the deterministic tcgen05 GEMM (csrc/bt_gemm.cu):
+  row-independent products (forward, dX) for a whole launch group of ESTs at
+  once -- a row's bits do not depend on which rows share the launch -- and one
+  weight gradient per EST (batched GEMM over the EST's own tokens, written
+  straight into the EST's gradient slot); attention, LayerNorm and the loss
+  are csrc/bt_bert.cu, each with a reduction shape fixed by the EST's data;
+* the per-EST gradients [E][P] are summed by the fixed-order reducer
+  (csrc/bt_reduce.cu: EST-rank order, fused /E and momentum SGD on the fp32
+  master weights) -- one launch over all P parameters.
+
+So the trained weights are bit-identical however the ESTs are grouped into
+launches (`groups=`), which is what mapping them onto 1/2/4/8 GPUs does: a GPU
+holding a contiguous EST block runs exactly one such group.
+
+The model head is a per-token regression (MSE against synthetic targets) on
+the encoder output; token embeddings and the MLM head are not modelled (the
+inputs are synthetic embedded tokens).  There is no reference implementation
+of this model: parity is against a float64 restatement of every
+stage with the same bf16 rounding points (tests/test_gpu_bert.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native
+from .device import Flags, require_cuda, stream
+from .errors import ConfigError, NumericError
+
+_LAYER = ("Wqkv", "bqkv", "Wo", "bo", "g1", "be1", "W1", "b1", "W2", "b2", "g2", "be2")
+_MATS = ("Wqkv", "Wo", "W1", "W2")
+
+
+def _init_uniform(seed: int, n: int, scale: float) -> torch.Tensor:
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().bt_init_random(seed & (2**64 - 1), scale, n, out.data_ptr(), stream()))
+    return out.float()
+
+
+class BertJob:
+    """E ESTs x `seqs` sequences of 128 tokens each, `layers` encoder layers, momentum SGD."""
+
+    def __init__(self, ests: int, seqs: int = 8, layers: int = 12, d_model: int = 768, heads: int = 12,
+                 d_ff: int = 3072, seed: int = 42, lr: float = 1e-3, momentum: float = 0.9, p_hidden: float = 0.1,
+                 p_attn: float = 0.1, fanin: int = 0, eps: float = 1e-12):
+        require_cuda()
+        if heads * 64 != d_model or d_model % 256 or d_model > 1024 or d_ff % 256:
+            raise ConfigError("d_model = 64 * heads, a multiple of 256 (<= 1024); d_ff a multiple of 256")
+        if ests > _native.BT_MAX_TABLE or ests < 1:
+            raise ConfigError(f"1..{_native.BT_MAX_TABLE} ESTs per job")
+        if fanin not in (0, 2) or (fanin == 2 and ests & (ests - 1)):
+            raise ConfigError("allreduce variant: Sequential (0) or Tree(2) with a power-of-two EST count")
+        if seqs < 1 or layers < 1:
+            raise ConfigError("seqs and layers must be >= 1")
+        self.E, self.S, self.L, self.D, self.H, self.F = ests, seqs, layers, d_model, heads, d_ff
+        self.Te = seqs * 128
+        self.seed, self.lr, self.mu, self.fanin = seed, lr, momentum, fanin
+        self.ph, self.pa, self.eps = p_hidden, p_attn, eps
+        D, F = d_model, d_ff
+        shapes = {"Wqkv": (3 * D, D), "bqkv": (3 * D,), "Wo": (D, D), "bo": (D,), "g1": (D,), "be1": (D,),
+                  "W1": (F, D), "b1": (F,), "W2": (D, F), "b2": (D,), "g2": (D,), "be2": (D,)}
+        self.shapes = shapes
+        self.off = []  # per layer: name -> flat offset (floats; all multiples of 256)
+        o = 0
+        for _ in range(layers):
+            d = {}
+            for k in _LAYER:
+                d[k] = o
+                o += int(torch.Size(shapes[k]).numel())
+            self.off.append(d)
+        self.P = o
+        self.params = torch.zeros(self.P, dtype=torch.float32, device="cuda")
+        for l in range(layers):
+            for i, k in enumerate(_MATS):
+                rows, cols = shapes[k]
+                self.view(l, k).copy_(_init_uniform(seed * 1000003 + 16 * l + i, rows * cols, cols ** -0.5)
+                                      .view(rows, cols))
+            self.view(l, "g1").fill_(1.0)
+            self.view(l, "g2").fill_(1.0)
+        self.vel = torch.zeros_like(self.params)
+        self.grads = torch.empty(ests, self.P, dtype=torch.float32, device="cuda")
+        # bf16 operand copies: W [out][in] (forward) and W^T [in][out] (dX products)
+        self._moff = []
+        m = 0
+        for _ in range(layers):
+            d = {}
+            for k in _MATS:
+                d[k] = m
+                m += int(torch.Size(shapes[k]).numel())
+            self._moff.append(d)
+        self.wb = torch.empty(m, dtype=torch.bfloat16, device="cuda")
+        self.wt = torch.empty(m, dtype=torch.bfloat16, device="cuda")
+        n = layers * len(_MATS)
+        self._cast = [(C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_int32 * n)(),
+                      (C.c_int32 * n)()]
+        i = 0
+        for l in range(layers):
+            for k in _MATS:
+                rows, cols = shapes[k]
+                self._cast[0][i] = self.params.data_ptr() + 4 * self.off[l][k]
+                self._cast[1][i] = self.wb.data_ptr() + 2 * self._moff[l][k]
+                self._cast[2][i] = self.wt.data_ptr() + 2 * self._moff[l][k]
+                self._cast[3][i], self._cast[4][i] = rows, cols
+                i += 1
+        self.step_idx = 0
+        self.flags = Flags()
+        self._ws = {}
+        self._refresh_bf16()
+
+    # ------------------------------------------------------------------ views
+    def view(self, layer: int, name: str, t: torch.Tensor | None = None) -> torch.Tensor:
+        """Parameter `name` of `layer` as a view of the flat fp32 buffer (or of row e of grads)."""
+        t = self.params if t is None else t
+        o, shape = self.off[layer][name], self.shapes[name]
+        return t[o:o + int(torch.Size(shape).numel())].view(shape)
+
+    def _wb(self, l, k):
+        return self.wb.data_ptr() + 2 * self._moff[l][k]
+
+    def _wt(self, l, k):
+        return self.wt.data_ptr() + 2 * self._moff[l][k]
+
+    def _p(self, l, k):
+        return self.params.data_ptr() + 4 * self.off[l][k]
+
+    def _g(self, base, l, k):  # EST `base`'s gradient slot for (layer, name); EST e at + e*P floats
+        return self.grads.data_ptr() + 4 * (base * self.P + self.off[l][k])
+
+    def _refresh_bf16(self):
+        c = self._cast
+        _native.check(_native.lib().bt_cast_weights_bf16(c[0], c[1], c[2], c[3], c[4], len(c[3]), stream()),
+                      "bert weight cast")
+
+    # -------------------------------------------------------------- workspace
+    def _workspace(self, n: int) -> dict:
+        ws = self._ws.get(n)
+        if ws is not None:
+            return ws
+        D, F, Te, T, L = self.D, self.F, self.Te, n * self.Te, self.L
+        bf, f32 = dict(dtype=torch.bfloat16, device="cuda"), dict(dtype=torch.float32, device="cuda")
+        ws = {
+            "layers": [{"xb": torch.empty(T, D, **bf), "qkv": torch.empty(T, 3 * D, **bf), "ctx": torch.empty(T, D, **bf),
+                        "hs1": torch.empty(T, D, **f32), "st1": torch.empty(T, 2, **f32),
+                        "h1b": torch.empty(T, D, **bf), "Hpre": torch.empty(T, F, **bf),
+                        "Dact": torch.empty(T, F, **bf), "hs2": torch.empty(T, D, **f32),
+                        "st2": torch.empty(T, 2, **f32)} for _ in range(L)],
+            "x32": torch.empty(T, D, **f32), "r32": [torch.empty(T, D, **f32) for _ in range(2)],
+            "h1_32": torch.empty(T, D, **f32), "br32": torch.empty(T, D, **f32), "ytop": torch.empty(T, D, **bf),
+            "tgt": torch.empty(T, D, **f32), "dbuf": [torch.empty(T, D, **f32) for _ in range(4)],
+            "dbr": torch.empty(T, D, **bf), "dHpre": torch.empty(T, F, **bf), "dctx": torch.empty(T, D, **bf),
+            "dqkv": torch.empty(T, 3 * D, **bf), "tA": torch.empty(T * max(3 * D, F), **bf),
+            "tB": torch.empty(T * max(3 * D, F), **bf), "lnpart": torch.empty(n * (Te // 64) * 3 * D, **f32),
+            "colsum": torch.empty(n * 16 * max(3 * D, F), **f32), "msepart": torch.empty(n * 64, **f32),
+        }
+        self._ws[n] = ws
+        return ws
+
+    # ------------------------------------------------------------- launchers
+    def _gemm(self, a, b, c, M, N, K, out_bf16=False, bias=None, batch=1, sa=0, sb=0, sc=0):
+        _native.check(_native.lib().bt_gemm_bf16_tn_ex(a, b, c, batch, M, N, K, sa, sb, sc, 1 if out_bf16 else 0,
+                                                       bias, 0, stream()), "bert gemm")
+
+    def _wgrad(self, ws, n, dy, x, rows_out, cols_in, dst):
+        """Per-EST weight gradients dW_e = dy_e^T x_e ([rows_out][cols_in], K = the EST's tokens),
+        written into each EST's slot (stride P)."""
+        L, s, Te = _native.lib(), stream(), self.Te
+        _native.check(L.bt_transpose_to_bf16(dy, 0, n, Te, rows_out, ws["tA"].data_ptr(), s))
+        _native.check(L.bt_transpose_to_bf16(x, 0, n, Te, cols_in, ws["tB"].data_ptr(), s))
+        self._gemm(ws["tA"].data_ptr(), ws["tB"].data_ptr(), dst, rows_out, cols_in, Te, batch=n,
+                   sa=rows_out * Te, sb=cols_in * Te, sc=self.P)
+
+    def _group(self, base: int, n: int, losses: torch.Tensor, capture: dict | None = None):
+        """Forward/backward of ESTs [base, base+n): per-EST gradients into grads[base:base+n]."""
+        L, s = _native.lib(), stream()
+        D, F, H, Te, T, NL = self.D, self.F, self.H, self.Te, n * self.Te, self.L
+        seed, step = self.seed & (2**64 - 1), self.step_idx
+        ws = self._workspace(n)
+        lay = ws["layers"]
+        _native.check(L.bt_bert_data(seed, step, base, n, Te, D, ws["x32"].data_ptr(), lay[0]["xb"].data_ptr(),
+                                     ws["tgt"].data_ptr(), s))
+        x32 = ws["x32"]
+        for l in range(NL):
+            w = lay[l]
+            self._gemm(w["xb"].data_ptr(), self._wb(l, "Wqkv"), w["qkv"].data_ptr(), T, 3 * D, D, out_bf16=True,
+                       bias=self._p(l, "bqkv"))
+            _native.check(L.bt_bert_attn(0, w["qkv"].data_ptr(), None, w["ctx"].data_ptr(), n, Te, D, H, base, NL, l,
+                                         seed, step, self.pa, s), "attention forward")
+            self._gemm(w["ctx"].data_ptr(), self._wb(l, "Wo"), ws["br32"].data_ptr(), T, D, D)
+            _native.check(L.bt_bert_ln_fwd(x32.data_ptr(), ws["br32"].data_ptr(), self._p(l, "bo"), self._p(l, "g1"),
+                                           self._p(l, "be1"), w["hs1"].data_ptr(), w["st1"].data_ptr(),
+                                           ws["h1_32"].data_ptr(), w["h1b"].data_ptr(), n, Te, D, base, NL, l, 0,
+                                           seed, step, self.ph, self.eps, s), "layernorm 1")
+            _native.check(L.bt_gemm_bf16_ffn(w["h1b"].data_ptr(), self._wb(l, "W1"), w["Hpre"].data_ptr(), T, F, D, 1,
+                                             self._p(l, "b1"), None, w["Dact"].data_ptr(), seed, step, base, Te, 0.0,
+                                             0, s), "ffn forward GEMM")
+            self._gemm(w["Dact"].data_ptr(), self._wb(l, "W2"), ws["br32"].data_ptr(), T, D, F)
+            y32 = ws["r32"][l & 1]
+            yb = lay[l + 1]["xb"] if l + 1 < NL else ws["ytop"]
+            _native.check(L.bt_bert_ln_fwd(ws["h1_32"].data_ptr(), ws["br32"].data_ptr(), self._p(l, "b2"),
+                                           self._p(l, "g2"), self._p(l, "be2"), w["hs2"].data_ptr(),
+                                           w["st2"].data_ptr(), y32.data_ptr(), yb.data_ptr(), n, Te, D, base, NL, l,
+                                           1, seed, step, self.ph, self.eps, s), "layernorm 2")
+            if capture is not None and l == 0:
+                capture.update({k: w[k].clone() for k in ("xb", "qkv", "ctx", "hs1", "st1", "h1b", "Hpre", "Dact",
+                                                          "hs2", "st2")})
+                capture.update(x32=x32.clone(), y32=y32.clone())
+            x32 = y32
+        A, B, Cb, Db = ws["dbuf"]
+        _native.check(L.bt_bert_mse(x32.data_ptr(), ws["tgt"].data_ptr(), n, Te, D, A.data_ptr(),
+                                    ws["msepart"].data_ptr(), losses[base:].data_ptr(), s))
+        if capture is not None:
+            capture.update(ytop=x32.clone(), tgt=ws["tgt"].clone())
+        dy2 = None
+        part = ws["lnpart"].data_ptr()
+        for l in reversed(range(NL)):
+            w = lay[l]
+            if capture is not None and l == 0:
+                capture.update(dy1_top=A.clone(), dy2_top=None if dy2 is None else dy2.clone())
+            _native.check(L.bt_bert_ln_bwd(A.data_ptr(), None if dy2 is None else dy2.data_ptr(), w["hs2"].data_ptr(),
+                                           w["st2"].data_ptr(), self._p(l, "g2"), Cb.data_ptr(), ws["dbr"].data_ptr(),
+                                           part, n, Te, D, base, NL, l, 1, seed, step, self.ph, s), "layernorm 2'")
+            _native.check(L.bt_bert_ln_fold(part, n, Te, D, self._g(base, l, "g2"), self._g(base, l, "be2"),
+                                            self._g(base, l, "b2"), self.P, s))
+            if capture is not None and l == 0:
+                capture.update(dg=Cb.clone(), do=ws["dbr"].clone())
+            _native.check(L.bt_gemm_bf16_ffn(ws["dbr"].data_ptr(), self._wt(l, "W2"), ws["dHpre"].data_ptr(), T, F, D,
+                                             2, None, w["Hpre"].data_ptr(), None, seed, step, base, Te, 0.0, 0, s),
+                          "ffn backward GEMM")
+            self._gemm(ws["dHpre"].data_ptr(), self._wt(l, "W1"), Db.data_ptr(), T, D, F)
+            self._wgrad(ws, n, ws["dbr"].data_ptr(), w["Dact"].data_ptr(), D, F, self._g(base, l, "W2"))
+            self._wgrad(ws, n, ws["dHpre"].data_ptr(), w["h1b"].data_ptr(), F, D, self._g(base, l, "W1"))
+            _native.check(L.bt_colsum_bf16_strided(ws["dHpre"].data_ptr(), n, Te, F, self._g(base, l, "b1"), self.P,
+                                                   ws["colsum"].data_ptr(), s))
+            if capture is not None and l == 0:
+                capture.update(dHpre=ws["dHpre"].clone(), dh1=Db.clone())
+            _native.check(L.bt_bert_ln_bwd(Db.data_ptr(), Cb.data_ptr(), w["hs1"].data_ptr(), w["st1"].data_ptr(),
+                                           self._p(l, "g1"), B.data_ptr(), ws["dbr"].data_ptr(), part, n, Te, D, base,
+                                           NL, l, 0, seed, step, self.ph, s), "layernorm 1'")
+            _native.check(L.bt_bert_ln_fold(part, n, Te, D, self._g(base, l, "g1"), self._g(base, l, "be1"),
+                                            self._g(base, l, "bo"), self.P, s))
+            self._gemm(ws["dbr"].data_ptr(), self._wt(l, "Wo"), ws["dctx"].data_ptr(), T, D, D, out_bf16=True)
+            self._wgrad(ws, n, ws["dbr"].data_ptr(), w["ctx"].data_ptr(), D, D, self._g(base, l, "Wo"))
+            _native.check(L.bt_bert_attn(1, w["qkv"].data_ptr(), ws["dctx"].data_ptr(), ws["dqkv"].data_ptr(), n, Te,
+                                         D, H, base, NL, l, seed, step, self.pa, s), "attention backward")
+            if capture is not None and l == 0:
+                capture.update(dh=B.clone(), da=ws["dbr"].clone(), dctx=ws["dctx"].clone(), dqkv=ws["dqkv"].clone())
+            self._gemm(ws["dqkv"].data_ptr(), self._wt(l, "Wqkv"), A.data_ptr(), T, D, 3 * D)
+            self._wgrad(ws, n, ws["dqkv"].data_ptr(), w["xb"].data_ptr(), 3 * D, D, self._g(base, l, "Wqkv"))
+            _native.check(L.bt_colsum_bf16_strided(ws["dqkv"].data_ptr(), n, Te, 3 * D, self._g(base, l, "bqkv"),
+                                                   self.P, ws["colsum"].data_ptr(), s))
+            dy2 = B
+        if capture is not None:
+            capture["dx"] = A.clone()
+
+    # ------------------------------------------------------------------ step
+    def step(self, groups: list[int] | None = None, capture: dict | None = None) -> torch.Tensor:
+        """One mini-batch of all E ESTs; `groups` = EST counts per launch group (default: one group).
+        Returns the per-EST losses [E] (fp32, on device)."""
+        groups = groups or [self.E]
+        if sum(groups) != self.E or min(groups) < 1:
+            raise ConfigError(f"groups {groups} must partition {self.E} ESTs")
+        losses = torch.empty(self.E, dtype=torch.float32, device="cuda")
+        base = 0
+        for n in groups:
+            self._group(base, n, losses, capture if len(groups) == 1 else None)
+            base += n
+        if capture is not None:
+            capture["grads"] = self.grads.clone()
+        self._reduce_update()
+        self.step_idx += 1
+        self._refresh_bf16()
+        return losses
+
+    def _reduce_update(self):
+        """Fixed EST-rank-order sum of the E gradient slots, /E, momentum SGD: one launch over all P."""
+        a = _native.ReduceArgs()
+        a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, self.E, self.fanin, self.P
+        for k in range(self.E):
+            a.grads[k] = self.grads.data_ptr() + 4 * k * self.P
+        p, v = self.params.data_ptr(), self.vel.data_ptr()
+        a.param, a.vel, a.param_out, a.vel_out = p, v, p, v
+        a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
+        _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()), "bert reduce_update")
+        st, _, _ = self.flags.status()
+        if st:
+            self.flags.reset()
+            raise NumericError("bert: non-finite synchronized gradient")
+
+    # ---------------------------------------------------------------- sizes
+    def gemm_flops_per_step(self) -> float:
+        """Dense-layer flops: forward 2*T*P_w, backward dX + dW 4*T*P_w (P_w = weight-matrix params)."""
+        pw = sum(int(torch.Size(self.shapes[k]).numel()) for k in _MATS) * self.L
+        return 6.0 * self.E * self.Te * pw
+
+    def attn_flops_per_step(self) -> float:
+        """QK^T and PV: 4*128*128*64 per (sequence, head) forward; backward recomputes S (+1) and does 4 more."""
+        per = 4 * 128 * 128 * 64 / 2  # one 128x128x64 product = 2*128*128*64 flops
+        return (2 + 5) * per * self.E * self.S * self.H * self.L

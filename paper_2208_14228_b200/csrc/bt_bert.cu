@@ -1,0 +1,771 @@
+// bt_bert.cu -- the kernels between the GEMMs of a per-EST BERT encoder step
+// (C4, BASELINE.json configs[3]).  No reference
+// implementation exists for this model; the EasyScale contract
+// it keeps is the reference's: every random draw is keyed by the EST's global
+// rank and the step (counter-form splitmix64, as model.py:151-161 keys dropout
+// by rank), and every reduction has a shape fixed by the EST's own data, so
+// an EST's gradients are the same bits whichever launch group / GPU runs it.
+//
+// Layout: the tokens of local EST e are rows [e*Te, (e+1)*Te) of every
+// activation matrix; sequence s of the launch is rows [s*128, s*128+128).
+//   qkv  [T][3*Dm] bf16  (Q | K | V, head h at columns h*64 of each third)
+//   ctx  [T][Dm]   bf16
+//   LayerNorm input sums / outputs fp32 [T][Dm], bf16 copies for the GEMMs.
+//
+// Kernels:
+//   attn_fwd / attn_bwd  one CTA per (sequence, head), 8 warps x 16 query
+//                        rows, mma.sync m16n8k16 bf16 (S = QK^T/8, softmax,
+//                        keyed dropout, PV); the backward recomputes P from
+//                        Q, K (same instructions -> same bits) and sums dV,
+//                        dK over query rows in ascending k-steps;
+//   ln_fwd               x = resid + dropout(branch + bias); y = LN(x)
+//                        (one warp per row, butterfly sums: fixed order);
+//   ln_bwd               dx = LN'(dy1 + dy2); branch grad = dropout'(dx);
+//                        per-EST gamma/beta/bias column partials over fixed
+//                        64-row chunks, folded in chunk order (ln_fold);
+//   data / mse           synthetic per-EST inputs / regression head.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bt_common.cuh"
+
+namespace bt {
+namespace bert {
+
+constexpr uint64_t TAG_BERT_X = 0x4245'5254'5f58'4441ull;      // "BERT_XDA"
+constexpr uint64_t TAG_BERT_Y = 0x4245'5254'5f59'4441ull;      // "BERT_YDA"
+constexpr uint64_t TAG_BERT_HDROP = 0x4245'5254'4844'5250ull;  // "BERTHDRP" hidden dropout
+constexpr uint64_t TAG_BERT_ADROP = 0x4245'5254'4144'5250ull;  // "BERTADRP" attention-probability dropout
+
+constexpr int SEQ = 128, HD = 64;
+constexpr int AT_WARPS = 8, AT_THREADS = 32 * AT_WARPS;
+constexpr int LDS = HD + 8;     // bf16 row stride of Q/K/V/dO tiles (144 B: conflict-free ldmatrix)
+constexpr int LDP = SEQ + 8;    // bf16 row stride of the P / dS tiles (272 B)
+constexpr int LN_CHUNK = 64;    // rows per ln_bwd partial (fixed: part of the reduction's shape)
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *(const uint32_t*)&v;
+}
+
+// [128][64] bf16 tile (row stride `ld` elements in global) -> smem [128][LDS]
+__device__ __forceinline__ void load_tile(__nv_bfloat16* dst, const __nv_bfloat16* src, int ld) {
+  for (int c = threadIdx.x; c < SEQ * (HD / 8); c += AT_THREADS) {
+    const int r = c >> 3, k = (c & 7) * 8;
+    *(uint4*)(dst + r * LDS + k) = *(const uint4*)(src + (size_t)r * ld + k);
+  }
+}
+
+// Keep-scale of the attention-probability dropout for (row i, columns j, j+1), j even:
+// one draw per column pair, low / high 32-bit halves (the hidden dropout's rule).
+__device__ __forceinline__ void attn_mask2(uint64_t sd, uint64_t nb, int i, int j, uint32_t thr, float keep,
+                                           float* m0, float* m1) {
+  if (thr == 0) {
+    *m0 = *m1 = 1.f;
+    return;
+  }
+  const uint64_t r = draw_raw(sd, (nb + (uint64_t)i * SEQ + (uint64_t)j) >> 1);
+  *m0 = (uint32_t)r < thr ? 0.f : keep;
+  *m1 = (uint32_t)(r >> 32) < thr ? 0.f : keep;
+}
+__device__ __forceinline__ uint32_t threshold32(float p) { return p > 0.f ? (uint32_t)ceil((double)p * 0x1p32) : 0u; }
+
+// S = softmax(Q_w K^T / 8) for the warp's 16 query rows: s[nt][0..1] = row g, s[nt][2..3] = row g+8,
+// columns nt*8 + 2*(lane&3) + {0,1}.  Fixed instruction sequence -> the backward recomputes the same bits.
+__device__ __forceinline__ void warp_softmax(const __nv_bfloat16* Qs, const __nv_bfloat16* Ks, int w, int lane,
+                                             float (&s)[16][4]) {
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+  const uint32_t qb = su32(Qs), kb = su32(Ks);
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    uint32_t a[4];
+    ldsm_x4(qb + 2u * ((16 * w + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + kk * 16 + (lane >> 4) * 8), a);
+#pragma unroll
+    for (int n2 = 0; n2 < 8; ++n2) {
+      uint32_t b[4];
+      ldsm_x4(kb + 2u * ((n2 * 16 + (lane & 7) + (lane >> 4) * 8) * LDS + kk * 16 + ((lane >> 3) & 1) * 8), b);
+      mma16816(s[2 * n2], a, b[0], b[1]);
+      mma16816(s[2 * n2 + 1], a, b[2], b[3]);
+    }
+  }
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[nt][q] *= 0.125f;  // 1/sqrt(64), exact
+    m0 = fmaxf(m0, fmaxf(s[nt][0], s[nt][1]));
+    m1 = fmaxf(m1, fmaxf(s[nt][2], s[nt][3]));
+  }
+  m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+  m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+  m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+  m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+  float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    s[nt][0] = expf(s[nt][0] - m0);
+    l0 += s[nt][0];
+    s[nt][1] = expf(s[nt][1] - m0);
+    l0 += s[nt][1];
+    s[nt][2] = expf(s[nt][2] - m1);
+    l1 += s[nt][2];
+    s[nt][3] = expf(s[nt][3] - m1);
+    l1 += s[nt][3];
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);  // a+b == b+a: all four lanes of a row agree bitwise
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = 1.f / l0, i1 = 1.f / l1;
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    s[nt][0] *= i0;
+    s[nt][1] *= i0;
+    s[nt][2] *= i1;
+    s[nt][3] *= i1;
+  }
+}
+
+struct AttnArgs {
+  const __nv_bfloat16* qkv;  // [T][3*Dm]
+  const __nv_bfloat16* dctx; // [T][Dm] (backward)
+  __nv_bfloat16* out;        // ctx [T][Dm] (forward) / dqkv [T][3*Dm] (backward)
+  int Dm, H, seqs_per_est, est_base, L, layer;
+  uint64_t seed;
+  int64_t step;
+  float p;
+};
+
+// counter base of (EST stream, step, layer, sequence-in-EST, head): 128 x 128 (i, j) draws follow
+__device__ __forceinline__ uint64_t attn_counter_base(const AttnArgs& a, int sl, int h) {
+  return ((((uint64_t)a.step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ);
+}
+
+constexpr int ATF_SMEM = 3 * SEQ * LDS * 2;
+__global__ void __launch_bounds__(AT_THREADS) attn_fwd_kernel(const AttnArgs a) {
+  extern __shared__ __align__(16) uint8_t at_smem[];
+  __nv_bfloat16* Qs = (__nv_bfloat16*)at_smem;
+  __nv_bfloat16* Ks = Qs + SEQ * LDS;
+  __nv_bfloat16* Vs = Ks + SEQ * LDS;
+  const int s = blockIdx.x, h = blockIdx.y;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ld = 3 * a.Dm;
+  const __nv_bfloat16* base = a.qkv + (size_t)s * SEQ * ld + h * HD;
+  load_tile(Qs, base, ld);
+  load_tile(Ks, base + a.Dm, ld);
+  load_tile(Vs, base + 2 * a.Dm, ld);
+  __syncthreads();
+
+  float P[16][4];
+  warp_softmax(Qs, Ks, w, lane, P);
+
+  const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
+  const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
+  const uint64_t nb = attn_counter_base(a, sl, h);
+  const uint32_t thr = threshold32(a.p);
+  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
+  const int g = lane >> 2, i0 = 16 * w + g, c0 = 2 * (lane & 3);
+  uint32_t pa[8][4];  // dropped P as bf16 A fragments, k-step kv = keys 16kv..16kv+15
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    float m0, m1, m2, m3;
+    attn_mask2(sd, nb, i0, nt * 8 + c0, thr, keep, &m0, &m1);
+    attn_mask2(sd, nb, i0 + 8, nt * 8 + c0, thr, keep, &m2, &m3);
+    pa[nt >> 1][(nt & 1) * 2 + 0] = pack2(P[nt][0] * m0, P[nt][1] * m1);
+    pa[nt >> 1][(nt & 1) * 2 + 1] = pack2(P[nt][2] * m2, P[nt][3] * m3);
+  }
+  float o[8][4];
+#pragma unroll
+  for (int dt = 0; dt < 8; ++dt) o[dt][0] = o[dt][1] = o[dt][2] = o[dt][3] = 0.f;
+  const uint32_t vb = su32(Vs);
+#pragma unroll
+  for (int kv = 0; kv < 8; ++kv) {
+#pragma unroll
+    for (int d2 = 0; d2 < 4; ++d2) {
+      uint32_t b[4];
+      ldsm_x4_t(vb + 2u * ((kv * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + d2 * 16 + (lane >> 4) * 8), b);
+      mma16816(o[2 * d2], pa[kv], b[0], b[1]);
+      mma16816(o[2 * d2 + 1], pa[kv], b[2], b[3]);
+    }
+  }
+  __nv_bfloat16* out = a.out + (size_t)s * SEQ * a.Dm + h * HD;
+#pragma unroll
+  for (int dt = 0; dt < 8; ++dt) {
+    *(uint32_t*)(out + (size_t)i0 * a.Dm + dt * 8 + c0) = pack2(o[dt][0], o[dt][1]);
+    *(uint32_t*)(out + (size_t)(i0 + 8) * a.Dm + dt * 8 + c0) = pack2(o[dt][2], o[dt][3]);
+  }
+}
+
+// dV = Pd^T dO, dP = (dO V^T) * mask, dS = P * (dP - rowsum(dP * P)) / 8, dQ = dS K, dK = dS^T Q
+constexpr int ATB_SMEM = (4 * SEQ * LDS + 2 * SEQ * LDP) * 2;
+__global__ void __launch_bounds__(AT_THREADS) attn_bwd_kernel(const AttnArgs a) {
+  extern __shared__ __align__(16) uint8_t at_smem[];
+  __nv_bfloat16* Qs = (__nv_bfloat16*)at_smem;
+  __nv_bfloat16* Ks = Qs + SEQ * LDS;
+  __nv_bfloat16* Vs = Ks + SEQ * LDS;
+  __nv_bfloat16* dOs = Vs + SEQ * LDS;
+  __nv_bfloat16* Ps = dOs + SEQ * LDS;   // dropped P  [query][key]
+  __nv_bfloat16* dSs = Ps + SEQ * LDP;   // dS / 8     [query][key]
+  const int s = blockIdx.x, h = blockIdx.y;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ld = 3 * a.Dm;
+  const __nv_bfloat16* base = a.qkv + (size_t)s * SEQ * ld + h * HD;
+  load_tile(Qs, base, ld);
+  load_tile(Ks, base + a.Dm, ld);
+  load_tile(Vs, base + 2 * a.Dm, ld);
+  load_tile(dOs, a.dctx + (size_t)s * SEQ * a.Dm + h * HD, a.Dm);
+  __syncthreads();
+
+  float P[16][4];
+  warp_softmax(Qs, Ks, w, lane, P);
+  float dp[16][4];  // dO_w V^T
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) dp[nt][0] = dp[nt][1] = dp[nt][2] = dp[nt][3] = 0.f;
+  {
+    const uint32_t ob = su32(dOs), vb = su32(Vs);
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      uint32_t af[4];
+      ldsm_x4(ob + 2u * ((16 * w + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + kk * 16 + (lane >> 4) * 8), af);
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) {
+        uint32_t b[4];
+        ldsm_x4(vb + 2u * ((n2 * 16 + (lane & 7) + (lane >> 4) * 8) * LDS + kk * 16 + ((lane >> 3) & 1) * 8), b);
+        mma16816(dp[2 * n2], af, b[0], b[1]);
+        mma16816(dp[2 * n2 + 1], af, b[2], b[3]);
+      }
+    }
+  }
+  const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
+  const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
+  const uint64_t nb = attn_counter_base(a, sl, h);
+  const uint32_t thr = threshold32(a.p);
+  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
+  const int g = lane >> 2, i0 = 16 * w + g, c0 = 2 * (lane & 3);
+  float r0 = 0.f, r1 = 0.f;  // rowsum(dP * P), rows i0 / i0+8
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    float m[4];
+    attn_mask2(sd, nb, i0, nt * 8 + c0, thr, keep, &m[0], &m[1]);
+    attn_mask2(sd, nb, i0 + 8, nt * 8 + c0, thr, keep, &m[2], &m[3]);
+    const int j = nt * 8 + c0;
+    *(uint32_t*)(Ps + i0 * LDP + j) = pack2(P[nt][0] * m[0], P[nt][1] * m[1]);
+    *(uint32_t*)(Ps + (i0 + 8) * LDP + j) = pack2(P[nt][2] * m[2], P[nt][3] * m[3]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dp[nt][q] *= m[q];
+    r0 += dp[nt][0] * P[nt][0];
+    r0 += dp[nt][1] * P[nt][1];
+    r1 += dp[nt][2] * P[nt][2];
+    r1 += dp[nt][3] * P[nt][3];
+  }
+  r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
+  r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
+  r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
+  r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
+  uint32_t da[8][4];  // dS/8 as bf16 A fragments (rows of this warp)
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    const float d0 = P[nt][0] * (dp[nt][0] - r0) * 0.125f, d1 = P[nt][1] * (dp[nt][1] - r0) * 0.125f;
+    const float d2 = P[nt][2] * (dp[nt][2] - r1) * 0.125f, d3 = P[nt][3] * (dp[nt][3] - r1) * 0.125f;
+    const uint32_t lo = pack2(d0, d1), hi = pack2(d2, d3);
+    da[nt >> 1][(nt & 1) * 2 + 0] = lo;
+    da[nt >> 1][(nt & 1) * 2 + 1] = hi;
+    const int j = nt * 8 + c0;
+    *(uint32_t*)(dSs + i0 * LDP + j) = lo;
+    *(uint32_t*)(dSs + (i0 + 8) * LDP + j) = hi;
+  }
+  __nv_bfloat16* dq = a.out + (size_t)s * SEQ * ld + h * HD;
+  {  // dQ_w = dS_w K
+    float acc[8][4];
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.f;
+    const uint32_t kb = su32(Ks);
+#pragma unroll
+    for (int kv = 0; kv < 8; ++kv) {
+#pragma unroll
+      for (int d2 = 0; d2 < 4; ++d2) {
+        uint32_t b[4];
+        ldsm_x4_t(kb + 2u * ((kv * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + d2 * 16 + (lane >> 4) * 8), b);
+        mma16816(acc[2 * d2], da[kv], b[0], b[1]);
+        mma16816(acc[2 * d2 + 1], da[kv], b[2], b[3]);
+      }
+    }
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+      *(uint32_t*)(dq + (size_t)i0 * ld + dt * 8 + c0) = pack2(acc[dt][0], acc[dt][1]);
+      *(uint32_t*)(dq + (size_t)(i0 + 8) * ld + dt * 8 + c0) = pack2(acc[dt][2], acc[dt][3]);
+    }
+  }
+  __syncthreads();
+  // warp w: key rows 16w..16w+15.  dV = Pd^T dO, dK = dS^T Q; k-steps = ascending query blocks
+#pragma unroll 1
+  for (int which = 0; which < 2; ++which) {
+    const uint32_t ab = su32(which == 0 ? Ps : dSs), bb = su32(which == 0 ? dOs : Qs);
+    float acc[8][4];
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.f;
+#pragma unroll
+    for (int kq = 0; kq < 8; ++kq) {
+      uint32_t af[4];
+      ldsm_x4_t(ab + 2u * ((kq * 16 + (lane & 7) + (lane >> 4) * 8) * LDP + 16 * w + ((lane >> 3) & 1) * 8), af);
+#pragma unroll
+      for (int d2 = 0; d2 < 4; ++d2) {
+        uint32_t b[4];
+        ldsm_x4_t(bb + 2u * ((kq * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + d2 * 16 + (lane >> 4) * 8), b);
+        mma16816(acc[2 * d2], af, b[0], b[1]);
+        mma16816(acc[2 * d2 + 1], af, b[2], b[3]);
+      }
+    }
+    __nv_bfloat16* dst = dq + (which == 0 ? 2 : 1) * a.Dm;
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+      *(uint32_t*)(dst + (size_t)i0 * ld + dt * 8 + c0) = pack2(acc[dt][0], acc[dt][1]);
+      *(uint32_t*)(dst + (size_t)(i0 + 8) * ld + dt * 8 + c0) = pack2(acc[dt][2], acc[dt][3]);
+    }
+  }
+}
+
+// ------------------------------------------------------------ LayerNorm
+struct LnArgs {
+  const float* resid;   // fwd: residual input [T][D]      bwd: dy1 [T][D]
+  const float* branch;  // fwd: branch GEMM output (no bias) bwd: dy2 [T][D] or null
+  const float* bias;    // fwd: branch bias [D]
+  const float* gamma;
+  const float* beta;
+  float* xsum;          // fwd: out, the LN input (kept for backward)   bwd: in
+  const float2* stats_in;
+  float2* stats;        // fwd: out (mean, rstd) per row
+  float* y32;           // fwd: LN output fp32       bwd: dx (LN-input gradient, the residual path)
+  __nv_bfloat16* yb;    // fwd: LN output bf16       bwd: dropout'(dx) bf16 (the branch gradient)
+  float* part;          // bwd: [E][chunks][3][D] column partials (dgamma, dbeta, dbias)
+  int D, Te, rows, est_base, L, layer, site;
+  uint64_t seed;
+  int64_t step;
+  float p, eps;
+};
+
+__device__ __forceinline__ void ln_mask8(const LnArgs& a, uint64_t sd, int tl, int col, uint32_t thr, float keep,
+                                         float* m) {
+  if (thr == 0) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = 1.f;
+    return;
+  }
+  const uint64_t n0 = ((((uint64_t)a.step * a.L + a.layer) * 2 + a.site) * a.Te + tl) * (uint64_t)a.D + col;
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const uint64_t r = draw_raw(sd, (n0 + k) >> 1);
+    m[k] = (uint32_t)r < thr ? 0.f : keep;
+    m[k + 1] = (uint32_t)(r >> 32) < thr ? 0.f : keep;
+  }
+}
+__device__ __forceinline__ float warp_sum(float v) {  // butterfly: every lane ends with the same bits
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ void ld8(const float* p, float* v) {
+  const float4 x = *(const float4*)p, y = *(const float4*)(p + 4);
+  v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+}
+__device__ __forceinline__ void st8(float* p, const float* v) {
+  *(float4*)p = make_float4(v[0], v[1], v[2], v[3]);
+  *(float4*)(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const float* v) {
+  uint4 u;
+  u.x = pack2(v[0], v[1]);
+  u.y = pack2(v[2], v[3]);
+  u.z = pack2(v[4], v[5]);
+  u.w = pack2(v[6], v[7]);
+  *(uint4*)p = u;
+}
+
+// one warp per row; lane owns columns c*256 + lane*8 + [0, 8) for c < NC (D = 256*NC)
+template <int NC>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const LnArgs a) {
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (t >= a.rows) return;
+  const int e = t / a.Te, tl = t - e * a.Te;
+  const uint64_t sd = derive3(TAG_BERT_HDROP, a.seed, (uint64_t)(a.est_base + e));
+  const uint32_t thr = threshold32(a.p);
+  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
+  float x[NC][8];
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int col = c * 256 + lane * 8;
+    float r[8], b[8], bi[8], m[8];
+    ld8(a.resid + (size_t)t * a.D + col, r);
+    ld8(a.branch + (size_t)t * a.D + col, b);
+    ld8(a.bias + col, bi);
+    ln_mask8(a, sd, tl, col, thr, keep, m);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      x[c][k] = r[k] + (b[k] + bi[k]) * m[k];
+      sum += x[c][k];
+    }
+  }
+  const float mean = warp_sum(sum) / (float)a.D;
+  float sq = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float d = x[c][k] - mean;
+      sq += d * d;
+    }
+  const float rstd = 1.f / sqrtf(warp_sum(sq) / (float)a.D + a.eps);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int col = c * 256 + lane * 8;
+    float gm[8], bt[8], y[8];
+    ld8(a.gamma + col, gm);
+    ld8(a.beta + col, bt);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) y[k] = (x[c][k] - mean) * rstd * gm[k] + bt[k];
+    st8(a.xsum + (size_t)t * a.D + col, x[c]);
+    st8(a.y32 + (size_t)t * a.D + col, y);
+    st8(a.yb + (size_t)t * a.D + col, y);
+  }
+  if (lane == 0) a.stats[t] = make_float2(mean, rstd);
+}
+
+// block = (local EST e, 64-row chunk k); warp w handles rows w, w+8, ... of the chunk in order
+template <int NC>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(const LnArgs a) {
+  extern __shared__ float ln_smem[];  // [8 warps][3][D]
+  const int chunks = a.Te / LN_CHUNK;
+  const int e = blockIdx.x / chunks, k = blockIdx.x - e * chunks;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t sd = derive3(TAG_BERT_HDROP, a.seed, (uint64_t)(a.est_base + e));
+  const uint32_t thr = threshold32(a.p);
+  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
+  float pg[NC][8], pb[NC][8], pr[NC][8];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pg[c][q] = pb[c][q] = pr[c][q] = 0.f;
+  for (int rr = w; rr < LN_CHUNK; rr += 8) {
+    const int tl = k * LN_CHUNK + rr;
+    const size_t t = (size_t)e * a.Te + tl;
+    const float2 st = a.stats_in[t];
+    float dy[NC][8], xh[NC][8], gg[NC][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int col = c * 256 + lane * 8;
+      float x[8], gm[8];
+      ld8(a.resid + t * a.D + col, dy[c]);
+      if (a.branch) {
+        float d2[8];
+        ld8(a.branch + t * a.D + col, d2);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dy[c][q] += d2[q];
+      }
+      ld8(a.xsum + t * a.D + col, x);
+      ld8(a.gamma + col, gm);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        xh[c][q] = (x[q] - st.x) * st.y;
+        gg[c][q] = dy[c][q] * gm[q];
+        s1 += gg[c][q];
+        s2 += gg[c][q] * xh[c][q];
+      }
+    }
+    const float m1 = warp_sum(s1) / (float)a.D, m2 = warp_sum(s2) / (float)a.D;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int col = c * 256 + lane * 8;
+      float dx[8], m[8];
+      ln_mask8(a, sd, tl, col, thr, keep, m);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        dx[q] = (gg[c][q] - m1 - xh[c][q] * m2) * st.y;
+        pg[c][q] += dy[c][q] * xh[c][q];
+        pb[c][q] += dy[c][q];
+      }
+      st8(a.y32 + t * a.D + col, dx);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        dx[q] *= m[q];
+        pr[c][q] += dx[q];
+      }
+      st8(a.yb + t * a.D + col, dx);
+    }
+  }
+  // warp partials -> smem, folded in warp order -> this chunk's partial
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int col = c * 256 + lane * 8;
+    st8(ln_smem + (size_t)(w * 3 + 0) * a.D + col, pg[c]);
+    st8(ln_smem + (size_t)(w * 3 + 1) * a.D + col, pb[c]);
+    st8(ln_smem + (size_t)(w * 3 + 2) * a.D + col, pr[c]);
+  }
+  __syncthreads();
+  float* out = a.part + (size_t)blockIdx.x * 3 * a.D;
+  for (int i = threadIdx.x; i < 3 * a.D; i += 256) {
+    float acc = ln_smem[i];
+    for (int ww = 1; ww < 8; ++ww) acc += ln_smem[(size_t)ww * 3 * a.D + i];
+    out[i] = acc;
+  }
+}
+
+// per-EST dgamma / dbeta / dbias = chunk partials summed in chunk order; written into the EST's
+// gradient slot (out_g/out_b/out_r + e * est_stride)
+__global__ void ln_fold_kernel(const float* __restrict__ part, int E, int chunks, int D, float* out_g, float* out_b,
+                               float* out_r, int64_t est_stride) {
+  const int64_t n = (int64_t)E * 3 * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i / (3 * D)), r = (int)(i - (int64_t)e * 3 * D);
+    const float* p = part + (size_t)e * chunks * 3 * D + r;
+    float acc = p[0];
+    for (int k = 1; k < chunks; ++k) acc += p[(size_t)k * 3 * D];
+    const int which = r / D, c = r - which * D;
+    float* dst = which == 0 ? out_g : (which == 1 ? out_b : out_r);
+    dst[(size_t)e * est_stride + c] = acc;
+  }
+}
+
+// ------------------------------------------------------------ data / head
+// X[t][d] = bf16(U[-1,1)) from (TAG_BERT_X, seed, EST) at counter (step*Te + tl)*D + d (bf16-exact, so the
+// fp32 residual copy and the GEMM operand agree); target 0.5*U[-1,1)
+__global__ void __launch_bounds__(256) data_kernel(uint64_t seed, int64_t step, int est_base, int Te, int D, int rows,
+                                                   float* X32, __nv_bfloat16* Xb, float* target) {
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (t >= rows) return;
+  const int e = t / Te, tl = t - e * Te;
+  const uint64_t sx = derive3(TAG_BERT_X, seed, (uint64_t)(est_base + e));
+  const uint64_t sy = derive3(TAG_BERT_Y, seed, (uint64_t)(est_base + e));
+  const uint64_t row0 = ((uint64_t)step * Te + tl) * (uint64_t)D;
+  for (int col = lane * 8; col < D; col += 256) {
+    float x[8], y[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      x[q] = __bfloat162float(__float2bfloat16_rn((float)(unit_float(draw_raw(sx, row0 + col + q)) * 2.0 - 1.0)));
+      y[q] = 0.5f * (float)(unit_float(draw_raw(sy, row0 + col + q)) * 2.0 - 1.0);
+    }
+    st8(X32 + (size_t)t * D + col, x);
+    st8(Xb + (size_t)t * D + col, x);
+    st8(target + (size_t)t * D + col, y);
+  }
+}
+
+// loss[e] = sum 0.5*(y - target)^2 / Te over the EST's rows (64 fixed element ranges, fixed
+// tree, ranges summed in order); dy = (y - target) / Te
+constexpr int MSE_THREADS = 256, MSE_BLOCKS = 64;
+__global__ void __launch_bounds__(MSE_THREADS) mse_kernel(const float* __restrict__ y, const float* __restrict__ tgt,
+                                                          int Te, int D, float* __restrict__ dy,
+                                                          float* __restrict__ part) {
+  const int e = blockIdx.y, blk = blockIdx.x;
+  const int64_t per_est = (int64_t)Te * D;
+  const int64_t chunk = (per_est + MSE_BLOCKS - 1) / MSE_BLOCKS;
+  const int64_t lo = blk * chunk, hi = min(per_est, lo + chunk);
+  const float inv = 1.f / (float)Te;
+  float acc = 0.f;
+  for (int64_t k = lo + threadIdx.x; k < hi; k += MSE_THREADS) {
+    const int64_t i = (int64_t)e * per_est + k;
+    const float diff = y[i] - tgt[i];
+    dy[i] = diff * inv;
+    acc += 0.5f * diff * diff;
+  }
+  __shared__ float sm[MSE_THREADS];
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = MSE_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[e * MSE_BLOCKS + blk] = sm[0];
+}
+__global__ void mse_final_kernel(const float* __restrict__ part, int E, int Te, float* __restrict__ loss) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  float acc = 0.f;
+  for (int b = 0; b < MSE_BLOCKS; ++b) acc += part[e * MSE_BLOCKS + b];
+  loss[e] = acc / (float)Te;
+}
+
+// bf16 operand copies of fp32 master weights: W [R][C] -> Wb [R][C] and Wt [C][R]
+struct CastT {
+  const float* w;
+  __nv_bfloat16* wb;
+  __nv_bfloat16* wt;
+  int R, C;
+};
+constexpr int MAX_CAST = 64;
+struct CastTable {
+  CastT m[MAX_CAST];
+  int n;
+};
+__global__ void __launch_bounds__(256) cast_t_kernel(const __grid_constant__ CastTable tab) {
+  __shared__ float tile[64][65];
+  const CastT& m = tab.m[blockIdx.z];
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  if (r0 >= m.R || c0 >= m.C) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int k = ty; k < 64; k += 8) {
+    const int r = r0 + k, c = c0 + 2 * tx;
+    if (r < m.R && c + 1 < m.C) {
+      const float2 v = *(const float2*)(m.w + (size_t)r * m.C + c);
+      tile[k][2 * tx] = v.x;
+      tile[k][2 * tx + 1] = v.y;
+      *(uint32_t*)(m.wb + (size_t)r * m.C + c) = pack2(v.x, v.y);
+    }
+  }
+  __syncthreads();
+  for (int k = ty; k < 64; k += 8) {
+    const int c = c0 + k, r = r0 + 2 * tx;
+    if (c < m.C && r + 1 < m.R) *(uint32_t*)(m.wt + (size_t)c * m.R + r) = pack2(tile[2 * tx][k], tile[2 * tx + 1][k]);
+  }
+}
+
+}  // namespace bert
+
+// ----------------------------------------------------------------- launchers
+static int ok_or_cuda_b() { return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA; }
+
+int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out, int n_seq, int Dm, int H,
+                     int seqs_per_est, int est_base, int L, int layer, uint64_t seed, int64_t step, float p,
+                     cudaStream_t s) {
+  bert::AttnArgs a{(const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dctx, (__nv_bfloat16*)out, Dm, H, seqs_per_est,
+                   est_base, L, layer, seed, step, p};
+  const dim3 grid(n_seq, H);
+  if (!backward) {
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(bert::attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bert::ATF_SMEM) !=
+          cudaSuccess)
+        return ERR_CUDA;
+      attr = true;
+    }
+    bert::attn_fwd_kernel<<<grid, bert::AT_THREADS, bert::ATF_SMEM, s>>>(a);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(bert::attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bert::ATB_SMEM) !=
+          cudaSuccess)
+        return ERR_CUDA;
+      attr = true;
+    }
+    bert::attn_bwd_kernel<<<grid, bert::AT_THREADS, bert::ATB_SMEM, s>>>(a);
+  }
+  return ok_or_cuda_b();
+}
+
+template <int NC>
+static int ln_launch_nc(int backward, const bert::LnArgs& a, int E, cudaStream_t s) {
+  if (!backward) {
+    bert::ln_fwd_kernel<NC><<<(a.rows + 7) / 8, 256, 0, s>>>(a);
+  } else {
+    const int smem = 8 * 3 * a.D * (int)sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(bert::ln_bwd_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               8 * 3 * 256 * NC * (int)sizeof(float)) != cudaSuccess)
+        return ERR_CUDA;
+      attr = true;
+    }
+    bert::ln_bwd_kernel<NC><<<E * (a.Te / bert::LN_CHUNK), 256, smem, s>>>(a);
+  }
+  return ok_or_cuda_b();
+}
+
+// forward: resid/branch/bias/gamma/beta -> xsum, stats, y32, yb
+// backward: dy1 (resid), dy2 (branch, may be null), xsum, stats_in, gamma -> dx (y32), dbranch (yb), part
+int bert_ln_launch(int backward, const float* in1, const float* in2, const float* bias, const float* gamma,
+                   const float* beta, float* xsum, float* stats, float* y32, void* yb, float* part, int E, int Te,
+                   int D, int est_base, int L, int layer, int site, uint64_t seed, int64_t step, float p, float eps,
+                   cudaStream_t s) {
+  if (D % 256 || D > 1024 || Te % bert::LN_CHUNK) return ERR_INPUT;
+  bert::LnArgs a{};
+  a.resid = in1;
+  a.branch = in2;
+  a.bias = bias;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.xsum = xsum;
+  a.stats_in = (const float2*)stats;
+  a.stats = (float2*)stats;
+  a.y32 = y32;
+  a.yb = (__nv_bfloat16*)yb;
+  a.part = part;
+  a.D = D;
+  a.Te = Te;
+  a.rows = E * Te;
+  a.est_base = est_base;
+  a.L = L;
+  a.layer = layer;
+  a.site = site;
+  a.seed = seed;
+  a.step = step;
+  a.p = p;
+  a.eps = eps;
+  switch (D / 256) {
+    case 1: return ln_launch_nc<1>(backward, a, E, s);
+    case 2: return ln_launch_nc<2>(backward, a, E, s);
+    case 3: return ln_launch_nc<3>(backward, a, E, s);
+    default: return ln_launch_nc<4>(backward, a, E, s);
+  }
+}
+
+int bert_ln_fold_launch(const float* part, int E, int Te, int D, float* dg, float* db, float* dr, int64_t est_stride,
+                        cudaStream_t s) {
+  const int64_t n = (int64_t)E * 3 * D;
+  const int grid = (int)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8);
+  bert::ln_fold_kernel<<<grid, 256, 0, s>>>(part, E, Te / bert::LN_CHUNK, D, dg, db, dr, est_stride);
+  return ok_or_cuda_b();
+}
+
+int bert_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, float* X32, void* Xb,
+                     float* target, cudaStream_t s) {
+  if (D % 8) return ERR_INPUT;
+  const int rows = E * Te;
+  bert::data_kernel<<<(rows + 7) / 8, 256, 0, s>>>(seed, step, est_base, Te, D, rows, X32, (__nv_bfloat16*)Xb, target);
+  return ok_or_cuda_b();
+}
+
+int bert_mse_launch(const float* y, const float* tgt, int E, int Te, int D, float* dy, float* part, float* loss,
+                    cudaStream_t s) {
+  bert::mse_kernel<<<dim3(bert::MSE_BLOCKS, E), bert::MSE_THREADS, 0, s>>>(y, tgt, Te, D, dy, part);
+  bert::mse_final_kernel<<<(E + 127) / 128, 128, 0, s>>>(part, E, Te, loss);
+  return ok_or_cuda_b();
+}
+
+int bert_cast_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* R, const int* C, int n,
+                             cudaStream_t s) {
+  if (n < 1 || n > bert::MAX_CAST) return ERR_INPUT;
+  bert::CastTable tab{};
+  int maxr = 0, maxc = 0;
+  for (int i = 0; i < n; ++i) {
+    if (R[i] % 2 || C[i] % 2) return ERR_INPUT;
+    tab.m[i] = bert::CastT{w[i], (__nv_bfloat16*)wb[i], (__nv_bfloat16*)wt[i], R[i], C[i]};
+    maxr = R[i] > maxr ? R[i] : maxr;
+    maxc = C[i] > maxc ? C[i] : maxc;
+  }
+  tab.n = n;
+  bert::cast_t_kernel<<<dim3((maxc + 63) / 64, (maxr + 63) / 64, n), 256, 0, s>>>(tab);
+  return ok_or_cuda_b();
+}
+
+}  // namespace bt

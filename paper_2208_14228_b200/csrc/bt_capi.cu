@@ -32,9 +32,9 @@ int slot_copy_launch(void* const* dst, const void* const* src, const int64_t* by
 int flags_reset_launch(int32_t* flags, cudaStream_t s);
 int tanh_launch(const double* x, int64_t n, double* out, cudaStream_t s);
 int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
-                        int64_t sb, int out_bf16, int grid, cudaStream_t s);
+                        int64_t sb, int64_t sc, int out_bf16, int grid, cudaStream_t s);
 int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
-                            int64_t sb, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s);
+                            int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s);
 int ffn_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, void* X, float* target,
                     cudaStream_t s);
 int ffn_fwd_act_launch(const float* H, const float* b1, uint64_t seed, int64_t step, int est_base, int E, int Te,
@@ -46,6 +46,23 @@ int ffn_bwd_act_launch(const float* dD, const void* Hpre, uint64_t seed, int64_t
 int colsum_bf16_launch(const void* in, int E, int R, int C, float* out, float* scratch, cudaStream_t s);
 int transpose_launch(const void* in, int in_f32, int E, int R, int C, void* out, cudaStream_t s);
 int cast_f32_bf16_launch(const float* in, int64_t n, void* out, cudaStream_t s);
+int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, int64_t ostride, float* scratch,
+                               cudaStream_t s);
+int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out, int n_seq, int Dm, int H,
+                     int seqs_per_est, int est_base, int L, int layer, uint64_t seed, int64_t step, float p,
+                     cudaStream_t s);
+int bert_ln_launch(int backward, const float* in1, const float* in2, const float* bias, const float* gamma,
+                   const float* beta, float* xsum, float* stats, float* y32, void* yb, float* part, int E, int Te,
+                   int D, int est_base, int L, int layer, int site, uint64_t seed, int64_t step, float p, float eps,
+                   cudaStream_t s);
+int bert_ln_fold_launch(const float* part, int E, int Te, int D, float* dg, float* db, float* dr, int64_t est_stride,
+                        cudaStream_t s);
+int bert_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, float* X32, void* Xb,
+                     float* target, cudaStream_t s);
+int bert_mse_launch(const float* y, const float* tgt, int E, int Te, int D, float* dy, float* part, float* loss,
+                    cudaStream_t s);
+int bert_cast_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* R, const int* C, int n,
+                             cudaStream_t s);
 }  // namespace bt
 
 static thread_local char g_err[512];
@@ -273,21 +290,38 @@ int bt_fwd_bwd_mlp_f64(const double* params_dev, const double* rows_dev, int32_t
 }
 
 // ------------------------------------------------------ tensor-core GEMM
-int bt_gemm_bf16_tn_batched(const void* a_dev, const void* b_dev, void* c_dev, int32_t batch, int32_t M, int32_t N,
-                            int32_t K, int64_t stride_a, int64_t stride_b, int32_t out_dtype, int32_t grid,
-                            void* stream) {
+int bt_gemm_bf16_tn_ex(const void* a_dev, const void* b_dev, void* c_dev, int32_t batch, int32_t M, int32_t N,
+                       int32_t K, int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype,
+                       const float* bias_dev, int32_t grid, void* stream) {
   if (!a_dev || !b_dev || !c_dev) return fail(bt::ERR_INPUT, "null pointer");
   if (batch < 1 || M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 128 || K % 64)
     return fail(bt::ERR_INPUT, "gemm shape %dx%dx%d x%d: need M %% 128 == 0, N %% 128 == 0, K %% 64 == 0", M, N, K,
                 batch);
-  if (((uintptr_t)a_dev | (uintptr_t)b_dev | (uintptr_t)c_dev) & 15)
+  if (((uintptr_t)a_dev | (uintptr_t)b_dev | (uintptr_t)c_dev | (uintptr_t)bias_dev) & 15)
     return fail(bt::ERR_INPUT, "gemm operands must be 16-byte aligned");
-  if (batch > 1 && (stride_a < (int64_t)M * K || stride_b < (int64_t)N * K || (stride_a | stride_b) % 8))
+  if (batch == 1) {
+    stride_a = (int64_t)M * K;
+    stride_b = (int64_t)N * K;
+    stride_c = (int64_t)M * N;
+  }
+  if (stride_c == 0) stride_c = (int64_t)M * N;
+  if (stride_a < (int64_t)M * K || stride_b < (int64_t)N * K || stride_c < (int64_t)M * N ||
+      (stride_a | stride_b | stride_c) % 8)
     return fail(bt::ERR_INPUT, "gemm batch strides must cover a matrix and be multiples of 8 elements");
   if (out_dtype != 0 && out_dtype != 1) return fail(bt::ERR_INPUT, "gemm out_dtype must be 0 (f32) or 1 (bf16)");
-  return done(bt::gemm_bf16_tn_launch(a_dev, b_dev, c_dev, batch, M, N, K, batch > 1 ? stride_a : (int64_t)M * K,
-                                      batch > 1 ? stride_b : (int64_t)N * K, out_dtype, grid, STREAM(stream)),
+  bt::GemmEpi epi{};
+  epi.kind = bias_dev ? bt::EPI_BIAS : bt::EPI_STORE;
+  epi.bias = bias_dev;
+  return done(bt::gemm_bf16_tn_launch_epi(a_dev, b_dev, c_dev, batch, M, N, K, stride_a, stride_b, stride_c,
+                                          out_dtype, grid, epi, STREAM(stream)),
               "bt_gemm_bf16_tn");
+}
+
+int bt_gemm_bf16_tn_batched(const void* a_dev, const void* b_dev, void* c_dev, int32_t batch, int32_t M, int32_t N,
+                            int32_t K, int64_t stride_a, int64_t stride_b, int32_t out_dtype, int32_t grid,
+                            void* stream) {
+  return bt_gemm_bf16_tn_ex(a_dev, b_dev, c_dev, batch, M, N, K, stride_a, stride_b, (int64_t)M * N, out_dtype,
+                            nullptr, grid, stream);
 }
 
 int bt_gemm_bf16_tn(const void* a_dev, const void* b_dev, void* c_dev, int32_t M, int32_t N, int32_t K,
@@ -317,7 +351,8 @@ int bt_gemm_bf16_ffn(const void* a_dev, const void* b_dev, void* c_dev, int32_t 
   epi.est_base = est_base;
   epi.Te = Te;
   epi.p = p;
-  return done(bt::gemm_bf16_tn_launch_epi(a_dev, b_dev, c_dev, 1, M, N, K, (int64_t)M * K, (int64_t)N * K, 1, grid,
+  return done(bt::gemm_bf16_tn_launch_epi(a_dev, b_dev, c_dev, 1, M, N, K, (int64_t)M * K, (int64_t)N * K,
+                                          (int64_t)M * N, 1, grid,
                                           epi, STREAM(stream)),
               "bt_gemm_bf16_ffn");
 }
@@ -531,6 +566,86 @@ int bt_enable_peer_access(int32_t peer_device) {
   }
   if (e != cudaSuccess) return cuda_fail("cudaDeviceEnablePeerAccess");
   return 0;
+}
+
+// ------------------------------------------ per-EST BERT encoder step (C4)
+static int bert_shape(int E, int Te, int D) {
+  if (E < 1 || Te < 128 || Te % 128 || D % 256 || D > 1024)
+    return fail(bt::ERR_INPUT, "bert shape E=%d Te=%d D=%d: need Te %% 128 == 0, D %% 256 == 0, D <= 1024", E, Te, D);
+  return 0;
+}
+int bt_bert_data(uint64_t seed, int64_t step, int32_t est_base, int32_t E, int32_t Te, int32_t D, float* x32_dev,
+                 void* xb_dev, float* target_dev, void* stream) {
+  if (int st = bert_shape(E, Te, D)) return st;
+  if (!x32_dev || !xb_dev || !target_dev) return fail(bt::ERR_INPUT, "null pointer");
+  return done(bt::bert_data_launch(seed, step, est_base, E, Te, D, x32_dev, xb_dev, target_dev, STREAM(stream)),
+              "bt_bert_data");
+}
+int bt_bert_attn(int32_t backward, const void* qkv_dev, const void* dctx_dev, void* out_dev, int32_t E, int32_t Te,
+                 int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed, int64_t step,
+                 float p, void* stream) {
+  if (int st = bert_shape(E, Te, D)) return st;
+  if (heads * 64 != D) return fail(bt::ERR_INPUT, "bert attention: head dim must be 64 (heads %d, D %d)", heads, D);
+  if (!qkv_dev || !out_dev || (backward && !dctx_dev)) return fail(bt::ERR_INPUT, "null pointer");
+  if (!(p >= 0.f && p < 1.f) || layer < 0 || layer >= layers) return fail(bt::ERR_CONFIG, "bad dropout / layer");
+  return done(bt::bert_attn_launch(backward, qkv_dev, dctx_dev, out_dev, E * Te / 128, D, heads, Te / 128, est_base,
+                                   layers, layer, seed, step, p, STREAM(stream)),
+              "bt_bert_attn");
+}
+int bt_bert_ln_fwd(const float* resid_dev, const float* branch_dev, const float* bias_dev, const float* gamma_dev,
+                   const float* beta_dev, float* xsum_dev, float* stats_dev, float* y32_dev, void* yb_dev, int32_t E,
+                   int32_t Te, int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
+                   int64_t step, float p, float eps, void* stream) {
+  if (int st = bert_shape(E, Te, D)) return st;
+  if (!resid_dev || !branch_dev || !bias_dev || !gamma_dev || !beta_dev || !xsum_dev || !stats_dev || !y32_dev ||
+      !yb_dev)
+    return fail(bt::ERR_INPUT, "null pointer");
+  if (!(p >= 0.f && p < 1.f) || (site != 0 && site != 1)) return fail(bt::ERR_CONFIG, "bad dropout / site");
+  return done(bt::bert_ln_launch(0, resid_dev, branch_dev, bias_dev, gamma_dev, beta_dev, xsum_dev, stats_dev, y32_dev,
+                                 yb_dev, nullptr, E, Te, D, est_base, layers, layer, site, seed, step, p, eps,
+                                 STREAM(stream)),
+              "bt_bert_ln_fwd");
+}
+int bt_bert_ln_bwd(const float* dy1_dev, const float* dy2_dev, const float* xsum_dev, const float* stats_dev,
+                   const float* gamma_dev, float* dx_dev, void* dbranch_dev, float* part_dev, int32_t E, int32_t Te,
+                   int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
+                   int64_t step, float p, void* stream) {
+  if (int st = bert_shape(E, Te, D)) return st;
+  if (!dy1_dev || !xsum_dev || !stats_dev || !gamma_dev || !dx_dev || !dbranch_dev || !part_dev)
+    return fail(bt::ERR_INPUT, "null pointer");
+  if (!(p >= 0.f && p < 1.f) || (site != 0 && site != 1)) return fail(bt::ERR_CONFIG, "bad dropout / site");
+  return done(bt::bert_ln_launch(1, dy1_dev, dy2_dev, nullptr, gamma_dev, nullptr, (float*)xsum_dev,
+                                 (float*)stats_dev, dx_dev, dbranch_dev, part_dev, E, Te, D, est_base, layers, layer,
+                                 site, seed, step, p, 0.f, STREAM(stream)),
+              "bt_bert_ln_bwd");
+}
+int bt_bert_ln_fold(const float* part_dev, int32_t E, int32_t Te, int32_t D, float* dgamma_dev, float* dbeta_dev,
+                    float* dbias_dev, int64_t est_stride, void* stream) {
+  if (int st = bert_shape(E, Te, D)) return st;
+  if (!part_dev || !dgamma_dev || !dbeta_dev || !dbias_dev) return fail(bt::ERR_INPUT, "null pointer");
+  return done(bt::bert_ln_fold_launch(part_dev, E, Te, D, dgamma_dev, dbeta_dev, dbias_dev, est_stride,
+                                      STREAM(stream)),
+              "bt_bert_ln_fold");
+}
+int bt_bert_mse(const float* y_dev, const float* target_dev, int32_t E, int32_t Te, int32_t D, float* dy_dev,
+                float* partials_dev, float* loss_dev, void* stream) {
+  if (int st = bert_shape(E, Te, D)) return st;
+  if (!y_dev || !target_dev || !dy_dev || !partials_dev || !loss_dev) return fail(bt::ERR_INPUT, "null pointer");
+  return done(bt::bert_mse_launch(y_dev, target_dev, E, Te, D, dy_dev, partials_dev, loss_dev, STREAM(stream)),
+              "bt_bert_mse");
+}
+int bt_colsum_bf16_strided(const void* in_dev, int32_t E, int32_t R, int32_t C, float* out_dev, int64_t out_stride,
+                           float* scratch_dev, void* stream) {
+  if (E < 1 || R < 1 || C < 1 || C % 8 || out_stride < C) return fail(bt::ERR_INPUT, "colsum shape");
+  if (!in_dev || !out_dev) return fail(bt::ERR_INPUT, "null pointer");
+  return done(bt::colsum_bf16_strided_launch(in_dev, E, R, C, out_dev, out_stride, scratch_dev, STREAM(stream)),
+              "bt_colsum_bf16_strided");
+}
+int bt_cast_weights_bf16(const float* const* w_dev, void* const* wb_dev, void* const* wt_dev, const int32_t* rows,
+                         const int32_t* cols, int32_t n, void* stream) {
+  if (n < 1 || n > 64) return fail(bt::ERR_INPUT, "cast table of %d matrices (1..64)", n);
+  return done(bt::bert_cast_weights_launch(w_dev, wb_dev, wt_dev, rows, cols, n, STREAM(stream)),
+              "bt_cast_weights_bf16");
 }
 
 }  // extern "C"

@@ -185,13 +185,14 @@ __global__ void colsum_part_kernel(const __nv_bfloat16* __restrict__ in, int E, 
     o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
 }
-__global__ void colsum_final_kernel(const float* __restrict__ part, int E, int C, float* __restrict__ out) {
+__global__ void colsum_final_kernel(const float* __restrict__ part, int E, int C, float* __restrict__ out,
+                                    int64_t ostride) {
   const int64_t n = (int64_t)E * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int e = (int)(i / C), c = (int)(i - (int64_t)e * C);
     float acc = part[((size_t)e * COLSUM_CHUNKS) * C + c];
     for (int k = 1; k < COLSUM_CHUNKS; ++k) acc += part[((size_t)e * COLSUM_CHUNKS + k) * C + c];
-    out[i] = acc;
+    out[(size_t)e * ostride + c] = acc;
   }
 }
 
@@ -237,6 +238,8 @@ static int grid_for(int64_t n) {
 }
 static int ok_or_cuda() { return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA; }
 
+int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, int64_t ostride, float* scratch,
+                               cudaStream_t s);
 static int row_grid(int rows) { return rows < 148 * 16 ? rows : 148 * 16; }
 
 int ffn_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, void* X, float* target,
@@ -268,6 +271,10 @@ int ffn_bwd_act_launch(const float* dD, const void* Hpre, uint64_t seed, int64_t
   return ok_or_cuda();
 }
 int colsum_bf16_launch(const void* in, int E, int R, int C, float* out, float* scratch, cudaStream_t s) {
+  return colsum_bf16_strided_launch(in, E, R, C, out, C, scratch, s);
+}
+int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, int64_t ostride, float* scratch,
+                               cudaStream_t s) {
   if (C % 8) return ERR_INPUT;
   float* part = scratch;  // E * COLSUM_CHUNKS * C partials
   bool own = false;
@@ -278,7 +285,7 @@ int colsum_bf16_launch(const void* in, int E, int R, int C, float* out, float* s
   }
   ffn::colsum_part_kernel<<<grid_for((int64_t)E * ffn::COLSUM_CHUNKS * C / 8), 256, 0, s>>>(
       (const __nv_bfloat16*)in, E, R, C, part);
-  ffn::colsum_final_kernel<<<grid_for((int64_t)E * C), 256, 0, s>>>(part, E, C, out);
+  ffn::colsum_final_kernel<<<grid_for((int64_t)E * C), 256, 0, s>>>(part, E, C, out, ostride);
   if (own) cudaFreeAsync(part, s);
   return ok_or_cuda();
 }

@@ -50,6 +50,7 @@ enum GemmEpiKind : int {
   EPI_STORE = 0,    // C = acc (fp32 or bf16)
   EPI_FFN_FWD = 1,  // h = acc + bias[j]: C = bf16(h) (pre-activation), out2 = bf16(dropout(gelu(h)))
   EPI_FFN_BWD = 2,  // C = bf16(acc * dropout_scale * gelu'(aux[row][j]))   (aux = pre-activation, bf16)
+  EPI_BIAS = 3,     // C = acc + bias[j] (fp32 or bf16)
 };
 struct GemmEpi {
   int kind;

@@ -131,14 +131,18 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
   float f[32];
 #pragma unroll
   for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
-  if (epi.kind == EPI_STORE && !OUT_BF16) {
-    uint4* dst = (uint4*)((float*)c + row * N + col);
+  if (epi.kind == EPI_BIAS) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    for (int q = 0; q < 32; ++q) f[q] += epi.bias[col + q];
+  }
+  if ((epi.kind == EPI_STORE || epi.kind == EPI_BIAS) && !OUT_BF16) {
+    float4* dst = (float4*)((float*)c + row * N + col);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
     return;
   }
   float g[32];  // second output (FFN_FWD)
-  if (epi.kind != EPI_STORE) {
+  if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) {
     const int e = (int)(row / (size_t)epi.Te), tl = (int)(row - (size_t)e * epi.Te);
     const uint64_t sd = derive3(ffn::TAG_FFN_DROP, epi.seed, (uint64_t)(epi.est_base + e));
     const float keep = epi.p < 1.f ? 1.f / (1.f - epi.p) : 0.f;
@@ -198,7 +202,7 @@ struct Smem {
 template <int BN, int STAGES, bool OUT_BF16>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                        void* __restrict__ c, int M, int N, int K, int batch, const GemmEpi epi) {
+                        void* __restrict__ c, int M, int N, int K, int batch, int64_t sc, const GemmEpi epi) {
   using L = Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
@@ -304,7 +308,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       tile_coords(t, mt, nt, &m0, &n0);
       mbar_wait(tfull(acc), (i >> 1) & 1);
       tc_fence_after();
-      const size_t row = (size_t)(t / per_batch) * M + m0 + lg * 32 + lane;  // batch entries stacked in C
+      const size_t row = (size_t)m0 + lg * 32 + lane;  // row within the batch entry
+      void* const cb = (char*)c + (size_t)(t / per_batch) * (size_t)sc * (OUT_BF16 ? 2 : 4);  // entry's C
 #pragma unroll 1
       for (int cc = half * (BN / EPI_SPLIT); cc < (half + 1) * (BN / EPI_SPLIT); cc += 32) {
         uint32_t v[32];
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, c, epi);
+        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, cb, epi);
       }
       tc_fence_before();
       __syncwarp();
@@ -391,7 +396,7 @@ struct PairSmem {
 template <int STAGES, bool OUT_BF16>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                             void* __restrict__ c, int M, int N, int K, int batch, const GemmEpi epi) {
+                             void* __restrict__ c, int M, int N, int K, int batch, int64_t sc, const GemmEpi epi) {
   using L = PairSmem<STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
@@ -506,7 +511,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       coords(t, &m0, &n0);
       mbar_wait(tfull(acc), (i >> 1) & 1);
       tc_fence_after();
-      const size_t row = (size_t)(t / per_batch) * M + m0 + (int)rank * BM + lg * 32 + lane;
+      const size_t row = (size_t)m0 + (int)rank * BM + lg * 32 + lane;
+      void* const cb = (char*)c + (size_t)(t / per_batch) * (size_t)sc * (OUT_BF16 ? 2 : 4);
 #pragma unroll 1
       for (int cc = half * (PAIR_BN / EPI_SPLIT); cc < (half + 1) * (PAIR_BN / EPI_SPLIT); cc += 32) {
         uint32_t v[32];
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, c, epi);
+        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, cb, epi);
       }
       tc_fence_before();
       __syncwarp();
@@ -573,7 +579,7 @@ struct GemmShape {
   const void *a, *b;
   void* c;
   int M, N, K, batch;
-  int64_t sa, sb;  // batch strides of A and B in elements (C is [batch][M][N] contiguous)
+  int64_t sa, sb, sc;  // batch strides of A, B and C in elements
   GemmEpi epi;
 };
 
@@ -599,7 +605,7 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
     grid = sms;
   }
   if (grid > tiles) grid = tiles;
-  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, g.c, M, N, K, g.batch, g.epi);
+  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, g.c, M, N, K, g.batch, g.sc, g.epi);
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
@@ -640,7 +646,7 @@ static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
   attr_[0].val.clusterDim.z = 1;
   cfg.attrs = attr_;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb, g.c, M, N, K, g.batch, g.epi) == cudaSuccess ? OK : ERR_CUDA;
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, g.c, M, N, K, g.batch, g.sc, g.epi) == cudaSuccess ? OK : ERR_CUDA;
 }
 
 static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests, measurements)
@@ -650,9 +656,9 @@ static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests
 
 // 256 x 256 CTA-pair tiles when M and N allow it, else 128 x {256, 128} tiles (all deterministic)
 int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
-                            int64_t sb, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s) {
-  const GemmShape g{a, b, c, M, N, K, batch, sa, sb, epi};
-  if (epi.kind != EPI_STORE) out_bf16 = 1;
+                            int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s) {
+  const GemmShape g{a, b, c, M, N, K, batch, sa, sb, sc, epi};
+  if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) out_bf16 = 1;
   if (M % 256 == 0 && N % 256 == 0 && gemm_variant() != 1)
     return out_bf16 ? launch_gemm_pair<6, true>(g, grid, s) : launch_gemm_pair<6, false>(g, grid, s);
   if (N % 256 == 0)
@@ -660,10 +666,10 @@ int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, in
   return out_bf16 ? launch_gemm<128, 6, true>(g, grid, s) : launch_gemm<128, 6, false>(g, grid, s);
 }
 int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
-                        int64_t sb, int out_bf16, int grid, cudaStream_t s) {
+                        int64_t sb, int64_t sc, int out_bf16, int grid, cudaStream_t s) {
   GemmEpi epi{};
   epi.kind = EPI_STORE;
-  return gemm_bf16_tn_launch_epi(a, b, c, batch, M, N, K, sa, sb, out_bf16, grid, epi, s);
+  return gemm_bf16_tn_launch_epi(a, b, c, batch, M, N, K, sa, sb, sc, out_bf16, grid, epi, s);
 }
 
 }  // namespace bt

@@ -1,0 +1,245 @@
+"""Per-EST BERT encoder step (C4, BASELINE.json configs[3]; needs a B200).
+
+* Mapping invariance (the EasyScale property, bit for bit): the same E ESTs
+  grouped into launches in different ways -- what mapping them onto 1/2/4/8
+  GPUs does -- give identical losses and weights after several steps.
+* Parity (there is no reference implementation of this model):
+  every stage of layer 0's forward and backward, the loss, and every per-EST
+  gradient against a float64 restatement fed with the captured bf16 inputs of
+  that stage, with the same bf16 rounding points and the same counter-keyed
+  dropout masks (regenerated here from splitmix64).  Tolerances, stated:
+  fp32 outputs rel. Frobenius error <= 1e-4; bf16 outputs: <= 1% of elements
+  differ (one bf16 ulp, fp32-vs-fp64 accumulation) and rel. error <= 5e-3;
+  per-EST gradients rel. Frobenius error <= 5e-3.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+SMALL = dict(ests=4, seqs=2, layers=2, d_model=256, heads=4, d_ff=512, seed=3, lr=0.01, momentum=0.9,
+             p_hidden=0.1, p_attn=0.1)
+
+GAMMA = np.uint64(0x9E3779B97F4A7C15)
+TAG_HDROP = 0x4245_5254_4844_5250
+TAG_ADROP = 0x4245_5254_4144_5250
+
+
+def _mix64(x):
+    x = x ^ (x >> np.uint64(30))
+    x = x * np.uint64(0xBF58476D1CE4E5B9)
+    x = x ^ (x >> np.uint64(27))
+    x = x * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def _draws(s0, n):
+    with np.errstate(over="ignore"):
+        return _mix64(np.uint64(s0) + (n.astype(np.uint64) + np.uint64(1)) * GAMMA)
+
+
+def _keep(raw_pairs, j, p):
+    """scale per unit from the pair draw: unit j uses the low (j even) / high (j odd) 32 bits"""
+    half = np.where(j % 2 == 0, raw_pairs & np.uint64(0xFFFFFFFF), raw_pairs >> np.uint64(32))
+    thr = np.uint64(math.ceil(p * 2 ** 32))
+    return np.where(half < thr, 0.0, 1.0 / (1.0 - p))
+
+
+@pytest.fixture(scope="module")
+def bert():
+    assert torch.cuda.is_available()
+    from paper_2208_14228_b200 import bert as mod
+
+    return mod
+
+
+def _bits(t):
+    return t.detach().contiguous().view(torch.int32).cpu().numpy()
+
+
+def test_groupings_are_bitwise_identical(bert):
+    runs = {}
+    for groups in ([4], [2, 2], [1, 1, 1, 1], [1, 3]):
+        job = bert.BertJob(**SMALL)
+        losses = [job.step(groups).clone() for _ in range(3)]
+        runs[tuple(groups)] = (losses, job.params.clone(), job.vel.clone())
+    ref_l, ref_p, ref_v = runs[(4,)]
+    for key, (losses, params, vel) in runs.items():
+        for a, b in zip(losses, ref_l):
+            assert np.array_equal(_bits(a), _bits(b)), key
+        assert np.array_equal(_bits(params), _bits(ref_p)), key
+        assert np.array_equal(_bits(vel), _bits(ref_v)), key
+
+
+def test_tree_reducer_groupings_and_repeat(bert):
+    a, b = bert.BertJob(fanin=2, **SMALL), bert.BertJob(fanin=2, **SMALL)
+    for _ in range(2):
+        assert np.array_equal(_bits(a.step([2, 2])), _bits(b.step()))
+    assert np.array_equal(_bits(a.params), _bits(b.params))
+
+
+def test_losses_decrease(bert):
+    job = bert.BertJob(**dict(SMALL, lr=0.05, p_hidden=0.0, p_attn=0.0))
+    first = job.step().mean().item()
+    for _ in range(8):
+        last = job.step().mean().item()
+    assert last < first
+
+
+def _d(t):
+    return t.detach().double().cpu()
+
+
+def _bf(x):
+    return x.to(torch.bfloat16).double()
+
+
+def _close_bf16(got, want, what, frac=1e-2, rel=5e-3):
+    got, want = _d(got), want.double()
+    assert got.shape == want.shape, what
+    mism = (got != _bf(want)).double().mean().item()
+    err = ((got - want).norm() / (want.norm() + 1e-30)).item()
+    assert mism <= frac and err <= rel, (what, mism, err)
+
+
+def _close(got, want, what, rel=1e-4):
+    got, want = _d(got), want.double()
+    err = ((got - want).norm() / (want.norm() + 1e-30)).item()
+    assert err <= rel, (what, err)
+
+
+def _ln(x, g, b, eps):
+    mean = x.mean(-1, keepdim=True)
+    var = ((x - mean) ** 2).mean(-1, keepdim=True)
+    rstd = 1 / torch.sqrt(var + eps)
+    return (x - mean) * rstd * g + b, mean.squeeze(-1), rstd.squeeze(-1)
+
+
+def _ln_bwd(dy, x, g, eps):
+    mean = x.mean(-1, keepdim=True)
+    rstd = 1 / torch.sqrt(((x - mean) ** 2).mean(-1, keepdim=True) + eps)
+    xh = (x - mean) * rstd
+    gg = dy * g
+    return (gg - gg.mean(-1, keepdim=True) - xh * (gg * xh).mean(-1, keepdim=True)) * rstd, xh
+
+
+def test_layer0_stages_match_float64_restatement(bert):
+    from paper_2208_14228_b200._native import host_derive_stream
+
+    job = bert.BertJob(**SMALL)
+    P0 = job.params.clone()
+    cap = {}
+    losses = job.step(capture=cap)
+    E, Te, D, H, F, NL = job.E, job.Te, job.D, job.H, job.F, job.L
+    S, seed, step, ph, pa, eps = job.S, job.seed, 0, job.ph, job.pa, job.eps
+    T = E * Te
+    W = {k: _d(job.view(0, k, P0)) for k in bert._LAYER}
+
+    def hidden_scale(site, l=0):
+        sc = np.empty((T, D))
+        for e in range(E):
+            s0 = host_derive_stream(TAG_HDROP, seed, e)
+            tl = np.arange(Te)[:, None]
+            j = np.arange(D)[None, :]
+            n0 = ((((step * NL + l) * 2 + site) * Te + tl) * D + j) >> 1
+            sc[e * Te:(e + 1) * Te] = _keep(_draws(s0, n0), j, ph)
+        return torch.from_numpy(sc)
+
+    def attn_scale(l=0):
+        sc = np.empty((E, S, H, 128, 128))
+        i = np.arange(128)[:, None]
+        j = np.arange(128)[None, :]
+        for e in range(E):
+            s0 = host_derive_stream(TAG_ADROP, seed, e)
+            for sl in range(S):
+                for h in range(H):
+                    nb = ((((step * NL + l) * S + sl) * H + h) * 16384)
+                    sc[e, sl, h] = _keep(_draws(s0, (nb + i * 128 + j) >> 1), j, pa)
+        return torch.from_numpy(sc).view(E * S, H, 128, 128)
+
+    # ---- forward, layer 0
+    xb, x32 = _d(cap["xb"]), _d(cap["x32"])
+    assert torch.equal(xb, x32)  # the synthetic input is bf16-exact
+    qkv_ref = xb @ _bf(W["Wqkv"]).T + W["bqkv"]
+    _close_bf16(cap["qkv"], qkv_ref, "qkv")
+    qkv = _d(cap["qkv"]).view(E * S, 128, 3, H, 64).permute(2, 0, 3, 1, 4)  # [3][seq][head][128][64]
+    q, k, v = qkv[0], qkv[1], qkv[2]
+    P = torch.softmax(q @ k.transpose(-1, -2) / 8, -1)
+    am = attn_scale()
+    drop_frac = (am == 0).double().mean().item()
+    assert abs(drop_frac - pa) < 0.01, drop_frac
+    Pd = _bf(P * am)
+    ctx_ref = (Pd @ v).permute(0, 2, 1, 3).reshape(T, D)
+    _close_bf16(cap["ctx"], ctx_ref, "ctx")
+    ctx = _d(cap["ctx"])
+    hm1 = hidden_scale(0)
+    hs1_ref = x32 + (ctx @ _bf(W["Wo"]).T + W["bo"]) * hm1
+    _close(cap["hs1"], hs1_ref, "ln1 input")
+    hs1 = _d(cap["hs1"])
+    h1, mean1, rstd1 = _ln(hs1, W["g1"], W["be1"], eps)
+    _close(cap["st1"][:, 0], mean1, "ln1 mean", rel=1e-5)
+    _close(cap["st1"][:, 1], rstd1, "ln1 rstd", rel=1e-5)
+    _close_bf16(cap["h1b"], h1, "ln1 out")
+    h1b = _d(cap["h1b"])
+    hpre = h1b @ _bf(W["W1"]).T + W["b1"]
+    _close_bf16(cap["Hpre"], hpre, "ffn pre-activation")
+    _close_bf16(cap["Dact"], 0.5 * hpre * (1 + torch.erf(hpre / math.sqrt(2))), "gelu")
+    hm2 = hidden_scale(1)
+    hs2_ref = h1 + (_d(cap["Dact"]) @ _bf(W["W2"]).T + W["b2"]) * hm2
+    _close(cap["hs2"], hs2_ref, "ln2 input")
+    # ---- loss head
+    ytop, tgt = _d(cap["ytop"]), _d(cap["tgt"])
+    diff = ytop - tgt
+    loss_ref = (0.5 * diff ** 2).view(E, Te * D).sum(1) / Te
+    assert torch.allclose(_d(losses), loss_ref, rtol=1e-5), (losses, loss_ref)
+    # ---- backward, layer 0
+    dy1 = _d(cap["dy1_top"])
+    dy2 = _d(cap["dy2_top"])
+    hs2 = _d(cap["hs2"])
+    dg_ref, xh2 = _ln_bwd(dy1 + dy2, hs2, W["g2"], eps)
+    _close(cap["dg"], dg_ref, "ln2 backward")
+    do_ref = _d(cap["dg"]) * hm2
+    _close_bf16(cap["do"], do_ref, "ffn-out dropout'")
+    do = _d(cap["do"])
+    hp = _d(cap["Hpre"])
+    gelu_g = 0.5 * (1 + torch.erf(hp / math.sqrt(2))) + hp * torch.exp(-0.5 * hp ** 2) / math.sqrt(2 * math.pi)
+    _close_bf16(cap["dHpre"], (do @ _bf(W["W2"])) * gelu_g, "dHpre")
+    dHpre = _d(cap["dHpre"])
+    _close(cap["dh1"], dHpre @ _bf(W["W1"]), "dh1")
+    dyl1 = _d(cap["dh1"]) + _d(cap["dg"])
+    dh_ref, xh1 = _ln_bwd(dyl1, hs1, W["g1"], eps)
+    _close(cap["dh"], dh_ref, "ln1 backward")
+    _close_bf16(cap["da"], _d(cap["dh"]) * hm1, "attn-out dropout'")
+    da = _d(cap["da"])
+    _close_bf16(cap["dctx"], da @ _bf(W["Wo"]), "dctx")
+    dctx = _d(cap["dctx"]).view(E * S, 128, H, 64).permute(0, 2, 1, 3)
+    dPd = dctx @ v.transpose(-1, -2)
+    dP = dPd * am
+    dS = _bf(P * (dP - (dP * P).sum(-1, keepdim=True)) / 8)
+    dq_ref, dk_ref, dv_ref = dS @ k, dS.transpose(-1, -2) @ q, Pd.transpose(-1, -2) @ dctx
+    dqkv_ref = torch.stack([dq_ref, dk_ref, dv_ref]).permute(1, 3, 0, 2, 4).reshape(T, 3 * D)
+    _close_bf16(cap["dqkv"], dqkv_ref, "attention backward", frac=2e-2, rel=1e-2)
+    dqkv = _d(cap["dqkv"])
+    _close(cap["dx"], dqkv @ _bf(W["Wqkv"]), "dx")
+    # ---- per-EST gradients of layer 0
+    g = cap["grads"]
+    for e in range(E):
+        r = slice(e * Te, (e + 1) * Te)
+        want = {
+            "Wqkv": dqkv[r].T @ xb[r], "bqkv": dqkv[r].sum(0),
+            "Wo": da[r].T @ ctx[r], "bo": (_d(cap["dh"])[r] * hm1[r]).sum(0),
+            "g1": (dyl1[r] * xh1[r]).sum(0), "be1": dyl1[r].sum(0),
+            "W1": dHpre[r].T @ h1b[r], "b1": dHpre[r].sum(0),
+            "W2": do[r].T @ _d(cap["Dact"])[r], "b2": (_d(cap["dg"])[r] * hm2[r]).sum(0),
+            "g2": ((dy1 + dy2)[r] * xh2[r]).sum(0), "be2": (dy1 + dy2)[r].sum(0),
+        }
+        for name, w_ in want.items():
+            _close(job.view(0, name, g[e]), w_, f"grad {name} est {e}", rel=5e-3)
+    # ---- fixed-order mean + momentum SGD (v0 = 0: v = mean_e g_e, p' = p - lr v)
+    mean_g = _d(g).mean(0)
+    _close(job.vel, mean_g, "velocity", rel=1e-6)
+    _close(job.params - P0, -job.lr * mean_g, "update", rel=1e-4)
