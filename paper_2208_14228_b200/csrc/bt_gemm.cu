@@ -123,26 +123,55 @@ __device__ __forceinline__ void tile_coords_bn(int t, int mt, int nt, int* m0, i
 }
 
 
-// Store one epilogue chunk: 32 consecutive fp32 accumulators of row `row`,
-// columns [col, col+32) -- plain (fp32 / bf16) or an FFN element op fused in.
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map), "r"(src),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Epilogue staging: each epilogue warp owns EPI_STAGE bytes of shared memory, holding one
+// 32-row x 32-column box of C (and of the second output) in the TMA swizzled layout:
+// fp32 rows of 128 B (SWIZZLE_128B: 16-byte chunk q of row r at q ^ (r & 7)), bf16 rows of
+// 64 B (SWIZZLE_64B: chunk q at q ^ ((r >> 1) & 3)) -- conflict-free row-per-lane writes;
+// one elected lane then issues a TMA bulk-tensor store (full 128-byte lines to L2/HBM).
+constexpr int EPI_STAGE = 4096;
+__device__ __forceinline__ void stage_f32(uint8_t* st, const float* f, int lane) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    *(float4*)(st + lane * 128 + ((q ^ (lane & 7)) << 4)) = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+}
+__device__ __forceinline__ void stage_bf16(uint8_t* st, const float* f, int lane) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const __nv_bfloat162 b2 = __floats2bfloat162_rn(f[q * 8 + 2 * h], f[q * 8 + 2 * h + 1]);
+      w[h] = *(const uint32_t*)&b2;
+    }
+    *(uint4*)(st + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// One epilogue chunk: 32 consecutive fp32 accumulators of row `row` (lane = row - row0),
+// columns [col, col+32) -- plain (fp32 / bf16), + bias, or an FFN element op fused in --
+// staged in shared memory and stored by TMA at (col, row0, batch entry z).
 template <bool OUT_BF16>
-__device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, int col, int N, void* c,
-                                               const GemmEpi& epi) {
+__device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, int col, int N, const GemmEpi& epi,
+                                               uint8_t* st, int lane, const CUtensorMap* mc, const CUtensorMap* mc2,
+                                               int row0, int z) {
   float f[32];
 #pragma unroll
   for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
+  float g[32];  // second output (FFN_FWD)
   if (epi.kind == EPI_BIAS) {
 #pragma unroll
     for (int q = 0; q < 32; ++q) f[q] += epi.bias[col + q];
-  }
-  if ((epi.kind == EPI_STORE || epi.kind == EPI_BIAS) && !OUT_BF16) {
-    float4* dst = (float4*)((float*)c + row * N + col);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) dst[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
-    return;
-  }
-  float g[32];  // second output (FFN_FWD)
-  if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) {
+  } else if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) {
     const int e = (int)(row / (size_t)epi.Te), tl = (int)(row - (size_t)e * epi.Te);
     const uint64_t sd = derive3(ffn::TAG_FFN_DROP, epi.seed, (uint64_t)(epi.est_base + e));
     const float keep = epi.p < 1.f ? 1.f / (1.f - epi.p) : 0.f;
@@ -174,35 +203,37 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
       }
     }
   }
-  auto store_bf16 = [&](__nv_bfloat16* base, const float* x) {
-    uint4* dst = (uint4*)(base + row * N + col);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t w[4];
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const __nv_bfloat162 b2 = __floats2bfloat162_rn(x[q * 8 + 2 * h], x[q * 8 + 2 * h + 1]);
-        w[h] = *(const uint32_t*)&b2;
-      }
-      dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-  };
-  store_bf16((__nv_bfloat16*)c, f);
-  if (epi.kind == EPI_FFN_FWD) store_bf16(epi.out2, g);
+  if (lane == 0) bulk_wait_read0();  // the previous chunk's store has finished reading the staging box
+  __syncwarp();
+  if (OUT_BF16) {
+    stage_bf16(st, f, lane);
+    if (epi.kind == EPI_FFN_FWD) stage_bf16(st + EPI_STAGE / 2, g, lane);
+  } else {
+    stage_f32(st, f, lane);
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_3d(mc, su32(st), col, row0, z);
+    if (epi.kind == EPI_FFN_FWD) tma_store_3d(mc2, su32(st + EPI_STAGE / 2), col, row0, z);
+    bulk_commit();
+  }
 }
 
 template <int BN, int STAGES>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int BAR = STAGES * STAGE;  // full[S], empty[S], tfull[2], tempty[2], tmem addr
+  static constexpr int EPI = STAGES * STAGE;           // epilogue staging, EPI_STAGE per epilogue warp
+  static constexpr int BAR = EPI + EPI_WARPS * EPI_STAGE;  // full[S], empty[S], tfull[2], tempty[2], tmem addr
   static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
 };
 
 template <int BN, int STAGES, bool OUT_BF16>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                        void* __restrict__ c, int M, int N, int K, int batch, int64_t sc, const GemmEpi epi) {
+                        const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2, int M,
+                        int N, int K, int batch, const GemmEpi epi) {
   using L = Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
@@ -301,6 +332,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---- epilogue: TMEM -> registers -> global -------------------------------
     const int lg = warp & 3;  // TMEM lane group this warp may access (lanes 32*lg ...)
     const int half = (warp - 2) >> 2;  // which column slice (of EPI_SPLIT)
+    uint8_t* const est = gbase + L::EPI + (warp - 2) * EPI_STAGE;
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int acc = i & 1;
@@ -308,8 +340,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       tile_coords(t, mt, nt, &m0, &n0);
       mbar_wait(tfull(acc), (i >> 1) & 1);
       tc_fence_after();
-      const size_t row = (size_t)m0 + lg * 32 + lane;  // row within the batch entry
-      void* const cb = (char*)c + (size_t)(t / per_batch) * (size_t)sc * (OUT_BF16 ? 2 : 4);  // entry's C
+      const int row0 = m0 + lg * 32;  // this warp's 32 rows (lane = row - row0) within the batch entry
+      const size_t row = (size_t)row0 + lane;
 #pragma unroll 1
       for (int cc = half * (BN / EPI_SPLIT); cc < (half + 1) * (BN / EPI_SPLIT); cc += 32) {
         uint32_t v[32];
@@ -323,12 +355,13 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, cb, epi);
+        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, epi, est, lane, &map_c, &map_c2, row0, t / per_batch);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty(acc));
     }
+    if (lane == 0) bulk_wait0();  // this warp's stores complete before the CTA exits
   }
   tc_fence_before();
   __syncthreads();
@@ -389,14 +422,16 @@ template <int STAGES>
 struct PairSmem {
   static constexpr int A_BYTES = BM * BK * 2, B_BYTES = (PAIR_BN / 2) * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int BAR = STAGES * STAGE;
+  static constexpr int EPI = STAGES * STAGE;
+  static constexpr int BAR = EPI + EPI_WARPS * EPI_STAGE;
   static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
 };
 
 template <int STAGES, bool OUT_BF16>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                             void* __restrict__ c, int M, int N, int K, int batch, int64_t sc, const GemmEpi epi) {
+                             const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2,
+                             int M, int N, int K, int batch, const GemmEpi epi) {
   using L = PairSmem<STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
@@ -503,6 +538,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {  // ---- epilogue (both CTAs: own 128 rows) ----
     const int lg = warp & 3;
     const int half = (warp - 2) >> 2;
+    uint8_t* const est = gbase + L::EPI + (warp - 2) * EPI_STAGE;
     const uint32_t leader_tempty0 = map_to_rank(tempty(0), 0), leader_tempty1 = map_to_rank(tempty(1), 0);
     int i = 0;
     for (int t = pair; t < tiles; t += pairs, ++i) {
@@ -511,8 +547,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       coords(t, &m0, &n0);
       mbar_wait(tfull(acc), (i >> 1) & 1);
       tc_fence_after();
-      const size_t row = (size_t)m0 + (int)rank * BM + lg * 32 + lane;
-      void* const cb = (char*)c + (size_t)(t / per_batch) * (size_t)sc * (OUT_BF16 ? 2 : 4);
+      const int row0 = m0 + (int)rank * BM + lg * 32;
+      const size_t row = (size_t)row0 + lane;
 #pragma unroll 1
       for (int cc = half * (PAIR_BN / EPI_SPLIT); cc < (half + 1) * (PAIR_BN / EPI_SPLIT); cc += 32) {
         uint32_t v[32];
@@ -526,12 +562,13 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, cb, epi);
+        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, epi, est, lane, &map_c, &map_c2, row0, t / per_batch);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(acc ? leader_tempty1 : leader_tempty0);
     }
+    if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -575,6 +612,23 @@ static bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// C [batch][rows][cols] (fp32 or bf16), entries `bstride` elements apart; box = 32 x 32 x 1 --
+// the epilogue's staging box (fp32: 128-byte rows, SWIZZLE_128B; bf16: 64-byte rows, SWIZZLE_64B)
+static bool make_store_map(CUtensorMap* map, const void* ptr, int rows, int cols, int batch, int64_t bstride,
+                           bool bf16) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const int eb = bf16 ? 2 : 4;
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)cols * eb, (cuuint64_t)bstride * eb};
+  const cuuint32_t box[3] = {32, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr),
+             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct GemmShape {
   const void *a, *b;
   void* c;
@@ -586,8 +640,10 @@ struct GemmShape {
 template <int BN, int STAGES, bool OUT_BF16>
 static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
   const int M = g.M, N = g.N, K = g.K;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) || !make_map(&mb, g.b, N, K, BN, g.batch, g.sb))
+  CUtensorMap ma, mb, mc, mc2;
+  if (!make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) || !make_map(&mb, g.b, N, K, BN, g.batch, g.sb) ||
+      !make_store_map(&mc, g.c, M, N, g.batch, g.sc, OUT_BF16) ||
+      !make_store_map(&mc2, g.epi.out2 ? (const void*)g.epi.out2 : g.c, M, N, g.batch, g.sc, OUT_BF16))
     return ERR_CUDA;
   auto kern = gemm::gemm_bf16_tn_kernel<BN, STAGES, OUT_BF16>;
   const int smem = gemm::Smem<BN, STAGES>::TOTAL + 1024;
@@ -605,16 +661,18 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
     grid = sms;
   }
   if (grid > tiles) grid = tiles;
-  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, g.c, M, N, K, g.batch, g.sc, g.epi);
+  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, mc, mc2, M, N, K, g.batch, g.epi);
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
 template <int STAGES, bool OUT_BF16>
 static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
   const int M = g.M, N = g.N, K = g.K;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc, mc2;
   if (!make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) ||
-      !make_map(&mb, g.b, N, K, gemm::PAIR_BN / 2, g.batch, g.sb))
+      !make_map(&mb, g.b, N, K, gemm::PAIR_BN / 2, g.batch, g.sb) ||
+      !make_store_map(&mc, g.c, M, N, g.batch, g.sc, OUT_BF16) ||
+      !make_store_map(&mc2, g.epi.out2 ? (const void*)g.epi.out2 : g.c, M, N, g.batch, g.sc, OUT_BF16))
     return ERR_CUDA;
   auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16>;
   const int smem = gemm::PairSmem<STAGES>::TOTAL + 1024;
@@ -646,7 +704,7 @@ static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
   attr_[0].val.clusterDim.z = 1;
   cfg.attrs = attr_;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb, g.c, M, N, K, g.batch, g.sc, g.epi) == cudaSuccess ? OK : ERR_CUDA;
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mc2, M, N, K, g.batch, g.epi) == cudaSuccess ? OK : ERR_CUDA;
 }
 
 static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests, measurements)
@@ -660,10 +718,10 @@ int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, in
   const GemmShape g{a, b, c, M, N, K, batch, sa, sb, sc, epi};
   if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) out_bf16 = 1;
   if (M % 256 == 0 && N % 256 == 0 && gemm_variant() != 1)
-    return out_bf16 ? launch_gemm_pair<6, true>(g, grid, s) : launch_gemm_pair<6, false>(g, grid, s);
+    return out_bf16 ? launch_gemm_pair<5, true>(g, grid, s) : launch_gemm_pair<5, false>(g, grid, s);
   if (N % 256 == 0)
-    return out_bf16 ? launch_gemm<256, 4, true>(g, grid, s) : launch_gemm<256, 4, false>(g, grid, s);
-  return out_bf16 ? launch_gemm<128, 6, true>(g, grid, s) : launch_gemm<128, 6, false>(g, grid, s);
+    return out_bf16 ? launch_gemm<256, 3, true>(g, grid, s) : launch_gemm<256, 3, false>(g, grid, s);
+  return out_bf16 ? launch_gemm<128, 5, true>(g, grid, s) : launch_gemm<128, 5, false>(g, grid, s);
 }
 int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                         int64_t sb, int64_t sc, int out_bf16, int grid, cudaStream_t s) {
