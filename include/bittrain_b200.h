@@ -156,6 +156,12 @@ int bt_cast_f32_bf16(const float *in_dev, int64_t n, void *out_dev, void *stream
 int bt_gemm_bf16_tn_ex(const void *a_dev, const void *b_dev, void *c_dev, int32_t batch, int32_t M, int32_t N,
                        int32_t K, int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype,
                        const float *bias_dev, int32_t grid, void *stream);
+/* mn_major = 1: both operands MN-major, C[e] = A[e]^T * B[e] with A[e] stored [K][M] and B[e] stored
+ * [K][N] (M / N contiguous) -- e.g. a per-EST weight gradient dW_e = dY_e^T X_e read straight from the
+ * token-major activations dY [T][M], X [T][N] (stride_a = Te*M, stride_b = Te*N; no transposes). */
+int bt_gemm_bf16_ex(const void *a_dev, const void *b_dev, void *c_dev, int32_t batch, int32_t M, int32_t N, int32_t K,
+                    int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype, const float *bias_dev,
+                    int32_t mn_major, int32_t grid, void *stream);
 /* bt_colsum_bf16 with out[e][c] at out_dev + e*out_stride + c */
 int bt_colsum_bf16_strided(const void *in_dev, int32_t E, int32_t R, int32_t C, float *out_dev, int64_t out_stride,
                            float *scratch_dev, void *stream);

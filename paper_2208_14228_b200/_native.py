@@ -98,6 +98,8 @@ EXPORTS = {
     "bt_cast_f32_bf16": (C.c_int, [_vp, _i64, _vp, _vp]),
     "bt_gemm_bf16_tn_ex": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _i32, _vp, _i32,
                                      _vp]),
+    "bt_gemm_bf16_ex": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _i32, _vp, _i32, _i32,
+                                  _vp]),
     "bt_colsum_bf16_strided": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i64, _vp, _vp]),
     "bt_bert_data": (C.c_int, [_u64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "bt_bert_attn": (C.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _u64, _i64,

@@ -160,8 +160,7 @@ class BertJob:
             "h1_32": torch.empty(T, D, **f32), "br32": torch.empty(T, D, **f32), "ytop": torch.empty(T, D, **bf),
             "tgt": torch.empty(T, D, **f32), "dbuf": [torch.empty(T, D, **f32) for _ in range(4)],
             "dbr": torch.empty(T, D, **bf), "dHpre": torch.empty(T, F, **bf), "dctx": torch.empty(T, D, **bf),
-            "dqkv": torch.empty(T, 3 * D, **bf), "tA": torch.empty(T * max(3 * D, F), **bf),
-            "tB": torch.empty(T * max(3 * D, F), **bf), "lnpart": torch.empty(n * (Te // 64) * 3 * D, **f32),
+            "dqkv": torch.empty(T, 3 * D, **bf), "lnpart": torch.empty(n * (Te // 64) * 3 * D, **f32),
             "colsum": torch.empty(n * 16 * max(3 * D, F), **f32), "msepart": torch.empty(n * 64, **f32),
         }
         self._ws[n] = ws
@@ -174,12 +173,11 @@ class BertJob:
 
     def _wgrad(self, ws, n, dy, x, rows_out, cols_in, dst):
         """Per-EST weight gradients dW_e = dy_e^T x_e ([rows_out][cols_in], K = the EST's tokens),
-        written into each EST's slot (stride P)."""
-        L, s, Te = _native.lib(), stream(), self.Te
-        _native.check(L.bt_transpose_to_bf16(dy, 0, n, Te, rows_out, ws["tA"].data_ptr(), s))
-        _native.check(L.bt_transpose_to_bf16(x, 0, n, Te, cols_in, ws["tB"].data_ptr(), s))
-        self._gemm(ws["tA"].data_ptr(), ws["tB"].data_ptr(), dst, rows_out, cols_in, Te, batch=n,
-                   sa=rows_out * Te, sb=cols_in * Te, sc=self.P)
+        read MN-major straight from the token-major activations and written into each EST's slot
+        (stride P): one batched launch, no transposed copies."""
+        Te = self.Te
+        _native.check(_native.lib().bt_gemm_bf16_ex(dy, x, dst, n, rows_out, cols_in, Te, rows_out * Te, cols_in * Te,
+                                                     self.P, 0, None, 1, 0, stream()), "bert weight-gradient gemm")
 
     def _group(self, base: int, n: int, losses: torch.Tensor, capture: dict | None = None):
         """Forward/backward of ESTs [base, base+n): per-EST gradients into grads[base:base+n]."""

@@ -35,6 +35,8 @@ int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M,
                         int64_t sb, int64_t sc, int out_bf16, int grid, cudaStream_t s);
 int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                             int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s);
+int gemm_bf16_launch_any(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
+                         int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, bool mn, cudaStream_t s);
 int ffn_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, void* X, float* target,
                     cudaStream_t s);
 int ffn_fwd_act_launch(const float* H, const float* b1, uint64_t seed, int64_t step, int est_base, int E, int Te,
@@ -290,9 +292,9 @@ int bt_fwd_bwd_mlp_f64(const double* params_dev, const double* rows_dev, int32_t
 }
 
 // ------------------------------------------------------ tensor-core GEMM
-int bt_gemm_bf16_tn_ex(const void* a_dev, const void* b_dev, void* c_dev, int32_t batch, int32_t M, int32_t N,
-                       int32_t K, int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype,
-                       const float* bias_dev, int32_t grid, void* stream) {
+int bt_gemm_bf16_ex(const void* a_dev, const void* b_dev, void* c_dev, int32_t batch, int32_t M, int32_t N, int32_t K,
+                    int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype, const float* bias_dev,
+                    int32_t mn_major, int32_t grid, void* stream) {
   if (!a_dev || !b_dev || !c_dev) return fail(bt::ERR_INPUT, "null pointer");
   if (batch < 1 || M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 128 || K % 64)
     return fail(bt::ERR_INPUT, "gemm shape %dx%dx%d x%d: need M %% 128 == 0, N %% 128 == 0, K %% 64 == 0", M, N, K,
@@ -312,9 +314,15 @@ int bt_gemm_bf16_tn_ex(const void* a_dev, const void* b_dev, void* c_dev, int32_
   bt::GemmEpi epi{};
   epi.kind = bias_dev ? bt::EPI_BIAS : bt::EPI_STORE;
   epi.bias = bias_dev;
-  return done(bt::gemm_bf16_tn_launch_epi(a_dev, b_dev, c_dev, batch, M, N, K, stride_a, stride_b, stride_c,
-                                          out_dtype, grid, epi, STREAM(stream)),
-              "bt_gemm_bf16_tn");
+  return done(bt::gemm_bf16_launch_any(a_dev, b_dev, c_dev, batch, M, N, K, stride_a, stride_b, stride_c, out_dtype,
+                                       grid, epi, mn_major != 0, STREAM(stream)),
+              "bt_gemm_bf16");
+}
+int bt_gemm_bf16_tn_ex(const void* a_dev, const void* b_dev, void* c_dev, int32_t batch, int32_t M, int32_t N,
+                       int32_t K, int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype,
+                       const float* bias_dev, int32_t grid, void* stream) {
+  return bt_gemm_bf16_ex(a_dev, b_dev, c_dev, batch, M, N, K, stride_a, stride_b, stride_c, out_dtype, bias_dev, 0,
+                         grid, stream);
 }
 
 int bt_gemm_bf16_tn_batched(const void* a_dev, const void* b_dev, void* c_dev, int32_t batch, int32_t M, int32_t N,

@@ -101,11 +101,32 @@ __device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
+// MN-major, 128-byte-swizzled operand tile (A^T / B^T stored token-major, e.g. an activation
+// matrix X[k][m] read as the K x M operand): TMA boxes of 64 MN-elements (128 B) x 64 k-rows,
+// one box per 64-wide MN block, 8 KB apart.  Canonical UMMA MN-major SW128 layout
+// ((8,n),(8,k)) : ((1,LBO),(8,SBO)) in 16-byte units: LBO = 8192 B between MN blocks,
+// SBO = 1024 B between 8-row k groups; a 16-deep UMMA k step advances 2 groups (2048 B).
+constexpr int MN_BLOCK_BYTES = 64 * BK * 2;
+__device__ __forceinline__ uint64_t mnmajor_sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(MN_BLOCK_BYTES >> 4) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+template <bool MN>
+__device__ __forceinline__ uint64_t op_desc(uint32_t saddr) {
+  return MN ? mnmajor_sw128_desc(saddr) : kmajor_sw128_desc(saddr);
+}
+template <bool MN>
+constexpr uint64_t k_step() {  // descriptor increment per UMMA K step (16-byte units)
+  return MN ? 2048 >> 4 : 32 >> 4;
+}
+
 // Instruction descriptor: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
 // both K-major, N>>3 at [17,23), M>>4 at [24,29).
-template <int BN>
+// a_major [15] / b_major [16] = 1 for MN-major operands.
+template <int BN, bool MN = false>
 __device__ __forceinline__ constexpr uint32_t instr_desc() {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  return (1u << 4) | (1u << 7) | (1u << 10) | (MN ? (3u << 15) : 0u) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
 }
 
 // Tile t -> (m0, n0): groups of GROUP_M row-blocks walked column by column, so
@@ -229,7 +250,7 @@ struct Smem {
   static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
 };
 
-template <int BN, int STAGES, bool OUT_BF16>
+template <int BN, int STAGES, bool OUT_BF16, bool MN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2, int M,
@@ -290,8 +311,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(empty(stage), phase ^ 1u);
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
           mbar_arrive_expect_tx(full(stage), L::STAGE);
-          tma_load_3d(sa, &map_a, kb * BK, m0, t / per_batch, full(stage));
-          tma_load_3d(sb, &map_b, kb * BK, n0, t / per_batch, full(stage));
+          if constexpr (MN) {  // [k][mn] operands: one 64 x 64 box per 64-wide MN block
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_3d(sa + j * MN_BLOCK_BYTES, &map_a, m0 + 64 * j, kb * BK, t / per_batch, full(stage));
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_3d(sb + j * MN_BLOCK_BYTES, &map_b, n0 + 64 * j, kb * BK, t / per_batch, full(stage));
+          } else {
+            tma_load_3d(sa, &map_a, kb * BK, m0, t / per_batch, full(stage));
+            tma_load_3d(sb, &map_b, kb * BK, n0, t / per_batch, full(stage));
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -302,7 +332,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     // ---- MMA issuer --------------------------------------------------------
     if (lane == 0) {
-      constexpr uint32_t idesc = instr_desc<BN>();
+      constexpr uint32_t idesc = instr_desc<BN, MN>();
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
@@ -315,10 +345,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(full(stage), phase);
           tc_fence_after();
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
-          const uint64_t da = kmajor_sw128_desc(sa), db = kmajor_sw128_desc(sb);
+          const uint64_t da = op_desc<MN>(sa), db = op_desc<MN>(sb);
 #pragma unroll
-          for (int k = 0; k < BK / UK; ++k)  // +32 B per UMMA step inside the swizzled 128 B row
-            tc_mma(d, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / UK; ++k)  // K-major: +32 B inside the swizzled row; MN-major: +2 k groups
+            tc_mma(d, da + k * k_step<MN>(), db + k * k_step<MN>(), idesc, (kb | k) != 0);
           tc_commit(empty(stage));  // frees the smem stage when these MMAs complete
           if (++stage == STAGES) {
             stage = 0;
@@ -427,7 +457,7 @@ struct PairSmem {
   static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
 };
 
-template <int STAGES, bool OUT_BF16>
+template <int STAGES, bool OUT_BF16, bool MN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                              const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2,
@@ -497,8 +527,19 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
           const uint32_t lb = full(stage) & 0xFEFFFFFFu;  // the leader CTA's barrier
           if (leader) mbar_arrive_expect_tx(full(stage), 2 * L::STAGE);
-          tma_load_3d_pair(sa, &map_a, kb * BK, m0 + (int)rank * BM, t / per_batch, lb);
-          tma_load_3d_pair(sb, &map_b, kb * BK, n0 + (int)rank * (PAIR_BN / 2), t / per_batch, lb);
+          if constexpr (MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_3d_pair(sa + j * MN_BLOCK_BYTES, &map_a, m0 + (int)rank * BM + 64 * j, kb * BK, t / per_batch,
+                               lb);
+#pragma unroll
+            for (int j = 0; j < PAIR_BN / 128; ++j)
+              tma_load_3d_pair(sb + j * MN_BLOCK_BYTES, &map_b, n0 + (int)rank * (PAIR_BN / 2) + 64 * j, kb * BK,
+                               t / per_batch, lb);
+          } else {
+            tma_load_3d_pair(sa, &map_a, kb * BK, m0 + (int)rank * BM, t / per_batch, lb);
+            tma_load_3d_pair(sb, &map_b, kb * BK, n0 + (int)rank * (PAIR_BN / 2), t / per_batch, lb);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -508,8 +549,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {  // ---- MMA issuer (leader only) ----
-      constexpr uint32_t idesc =
-          (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(PAIR_BN >> 3) << 17) | ((uint32_t)(PAIR_M >> 4) << 24);
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (MN ? (3u << 15) : 0u) |
+                                 ((uint32_t)(PAIR_BN >> 3) << 17) | ((uint32_t)(PAIR_M >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
@@ -522,10 +563,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(full(stage), phase);
           tc_fence_after();
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
-          const uint64_t da = kmajor_sw128_desc(sa), db = kmajor_sw128_desc(sb);
+          const uint64_t da = op_desc<MN>(sa), db = op_desc<MN>(sb);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)
-            tc_mma_pair(d, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (kb | k) != 0);
+            tc_mma_pair(d, da + k * k_step<MN>(), db + k * k_step<MN>(), idesc, (kb | k) != 0);
           tc_commit_pair(empty(stage));
           if (++stage == STAGES) {
             stage = 0;
@@ -629,23 +670,40 @@ static bool make_store_map(CUtensorMap* map, const void* ptr, int rows, int cols
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// MN-major operand: stored [batch][K][rows] (rows contiguous); box = 64 (128 B) x 64 k-rows x 1
+static bool make_map_mn(CUtensorMap* map, const void* ptr, int rows, int K, int batch, int64_t bstride) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)K, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)rows * 2, (cuuint64_t)bstride * 2};
+  const cuuint32_t box[3] = {64, (cuuint32_t)gemm::BK, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct GemmShape {
   const void *a, *b;
   void* c;
   int M, N, K, batch;
   int64_t sa, sb, sc;  // batch strides of A, B and C in elements
   GemmEpi epi;
+  bool mn;  // A, B MN-major: C[e] = A[e]^T B[e] with A[e] stored [K][M], B[e] stored [K][N]
 };
 
-template <int BN, int STAGES, bool OUT_BF16>
+template <int BN, int STAGES, bool OUT_BF16, bool MN>
 static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
   const int M = g.M, N = g.N, K = g.K;
   CUtensorMap ma, mb, mc, mc2;
-  if (!make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) || !make_map(&mb, g.b, N, K, BN, g.batch, g.sb) ||
+  const bool in_ok = MN ? make_map_mn(&ma, g.a, M, K, g.batch, g.sa) && make_map_mn(&mb, g.b, N, K, g.batch, g.sb)
+                        : make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) &&
+                              make_map(&mb, g.b, N, K, BN, g.batch, g.sb);
+  if (!in_ok ||
       !make_store_map(&mc, g.c, M, N, g.batch, g.sc, OUT_BF16) ||
       !make_store_map(&mc2, g.epi.out2 ? (const void*)g.epi.out2 : g.c, M, N, g.batch, g.sc, OUT_BF16))
     return ERR_CUDA;
-  auto kern = gemm::gemm_bf16_tn_kernel<BN, STAGES, OUT_BF16>;
+  auto kern = gemm::gemm_bf16_tn_kernel<BN, STAGES, OUT_BF16, MN>;
   const int smem = gemm::Smem<BN, STAGES>::TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
@@ -665,16 +723,18 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
-template <int STAGES, bool OUT_BF16>
+template <int STAGES, bool OUT_BF16, bool MN>
 static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
   const int M = g.M, N = g.N, K = g.K;
   CUtensorMap ma, mb, mc, mc2;
-  if (!make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) ||
-      !make_map(&mb, g.b, N, K, gemm::PAIR_BN / 2, g.batch, g.sb) ||
+  const bool in_ok = MN ? make_map_mn(&ma, g.a, M, K, g.batch, g.sa) && make_map_mn(&mb, g.b, N, K, g.batch, g.sb)
+                        : make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) &&
+                              make_map(&mb, g.b, N, K, gemm::PAIR_BN / 2, g.batch, g.sb);
+  if (!in_ok ||
       !make_store_map(&mc, g.c, M, N, g.batch, g.sc, OUT_BF16) ||
       !make_store_map(&mc2, g.epi.out2 ? (const void*)g.epi.out2 : g.c, M, N, g.batch, g.sc, OUT_BF16))
     return ERR_CUDA;
-  auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16>;
+  auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16, MN>;
   const int smem = gemm::PairSmem<STAGES>::TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
@@ -713,15 +773,23 @@ static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests
 }
 
 // 256 x 256 CTA-pair tiles when M and N allow it, else 128 x {256, 128} tiles (all deterministic)
+template <bool MN>
+static int launch_any(const GemmShape& g, int out_bf16, int grid, cudaStream_t s) {
+  if (g.M % 256 == 0 && g.N % 256 == 0 && gemm_variant() != 1)
+    return out_bf16 ? launch_gemm_pair<5, true, MN>(g, grid, s) : launch_gemm_pair<5, false, MN>(g, grid, s);
+  if (g.N % 256 == 0)
+    return out_bf16 ? launch_gemm<256, 3, true, MN>(g, grid, s) : launch_gemm<256, 3, false, MN>(g, grid, s);
+  return out_bf16 ? launch_gemm<128, 5, true, MN>(g, grid, s) : launch_gemm<128, 5, false, MN>(g, grid, s);
+}
+int gemm_bf16_launch_any(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
+                         int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, bool mn, cudaStream_t s) {
+  const GemmShape g{a, b, c, M, N, K, batch, sa, sb, sc, epi, mn};
+  if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) out_bf16 = 1;
+  return mn ? launch_any<true>(g, out_bf16, grid, s) : launch_any<false>(g, out_bf16, grid, s);
+}
 int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                             int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s) {
-  const GemmShape g{a, b, c, M, N, K, batch, sa, sb, sc, epi};
-  if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) out_bf16 = 1;
-  if (M % 256 == 0 && N % 256 == 0 && gemm_variant() != 1)
-    return out_bf16 ? launch_gemm_pair<5, true>(g, grid, s) : launch_gemm_pair<5, false>(g, grid, s);
-  if (N % 256 == 0)
-    return out_bf16 ? launch_gemm<256, 3, true>(g, grid, s) : launch_gemm<256, 3, false>(g, grid, s);
-  return out_bf16 ? launch_gemm<128, 5, true>(g, grid, s) : launch_gemm<128, 5, false>(g, grid, s);
+  return gemm_bf16_launch_any(a, b, c, batch, M, N, K, sa, sb, sc, out_bf16, grid, epi, false, s);
 }
 int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                         int64_t sb, int64_t sc, int out_bf16, int grid, cudaStream_t s) {

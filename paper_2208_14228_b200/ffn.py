@@ -31,7 +31,7 @@ import torch
 from . import _native
 from .device import Flags, require_cuda, stream
 from .errors import ConfigError, NumericError
-from .gemm import gemm_bf16, gemm_bf16_batched
+from .gemm import gemm_bf16, gemm_bf16_at_b
 
 _P = 64  # partial loss sums per EST (bt_ffn_out)
 
@@ -90,8 +90,6 @@ class FFNJob:
             ws = {"X": torch.empty(T, D, **bf), "tgt": torch.empty(T, D, **f32), "Hpre": torch.empty(T, F, **bf),
                   "D": torch.empty(T, F, **bf), "Y": torch.empty(T, D, **f32), "dY": torch.empty(T, D, **bf),
                   "dH": torch.empty(T, F, **bf), "part": torch.empty(n * _P, **f32),
-                  "dYt": torch.empty(n, D, Te, **bf), "Dt": torch.empty(n, F, Te, **bf),
-                  "dHt": torch.empty(n, F, Te, **bf), "Xt": torch.empty(n, D, Te, **bf),
                   "colsum": torch.empty(n * 16 * F, **f32)}
             if not self.fused:
                 ws["H"] = torch.empty(T, F, **f32)
@@ -125,14 +123,12 @@ class FFNJob:
             gemm_bf16(dY, self.W2t, out=w["H"])                        # [T][F] = dY W2
             _native.check(L.bt_ffn_bwd_act(w["H"].data_ptr(), Hpre.data_ptr(), seed, step, base, n, Te, F, p,
                                            dH.data_ptr(), s))
-        # per-EST weight gradients: K = the EST's own tokens (transposed, token-contiguous operands)
-        for src, dst, cols in ((dY, w["dYt"], D), (Dact, w["Dt"], F), (dH, w["dHt"], F), (X, w["Xt"], D)):
-            _native.check(L.bt_transpose_to_bf16(src.data_ptr(), 0, n, Te, cols, dst.data_ptr(), s))
         if capture is not None:
             capture.update(X=X.clone(), D=Dact.clone(), dY=dY.clone(), dH=dH.clone())
         gW1, gb1, gW2, gb2 = grads
-        gemm_bf16_batched(w["dHt"], w["Xt"], out=gW1[base:base + n])     # dW1_e = dH_e^T X_e   [n][F][D]
-        gemm_bf16_batched(w["dYt"], w["Dt"], out=gW2[base:base + n])     # dW2_e = dY_e^T D_e   [n][D][F]
+        # per-EST weight gradients, K = the EST's own tokens, operands read MN-major from the activations
+        gemm_bf16_at_b(dH.view(n, Te, F), X.view(n, Te, D), out=gW1[base:base + n])      # dW1_e = dH_e^T X_e
+        gemm_bf16_at_b(dY.view(n, Te, D), Dact.view(n, Te, F), out=gW2[base:base + n])   # dW2_e = dY_e^T D_e
         _native.check(L.bt_colsum_bf16(dH.data_ptr(), n, Te, F, gb1[base:].data_ptr(), w["colsum"].data_ptr(), s))
         _native.check(L.bt_colsum_bf16(dY.data_ptr(), n, Te, D, gb2[base:].data_ptr(), w["colsum"].data_ptr(), s))
 

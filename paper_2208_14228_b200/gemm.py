@@ -61,3 +61,25 @@ def gemm_bf16_batched(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype =
                                                          M * K, N * K, 1 if out_dtype == torch.bfloat16 else 0,
                                                          grid, stream()), "gemm_bf16_batched")
     return c
+
+
+def gemm_bf16_at_b(a: torch.Tensor, b: torch.Tensor, out_dtype: torch.dtype = torch.float32, grid: int = 0,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
+    """c[e] = a[e].T @ b[e] for bf16 a [E, K, M], b [E, K, N] (M, N contiguous: token-major
+    activations): both operands are loaded MN-major by TMA, so e.g. a per-EST weight gradient
+    dW_e = dY_e^T X_e needs no transposed copies.  Same determinism as gemm_bf16."""
+    require_cuda()
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or not (a.is_cuda and b.is_cuda):
+        raise InputError("gemm_bf16_at_b takes CUDA bfloat16 tensors")
+    if a.dim() == 2:
+        a, b = a.unsqueeze(0), b.unsqueeze(0)
+    if a.dim() != 3 or b.dim() != 3 or a.shape[0] != b.shape[0] or a.shape[1] != b.shape[1]:
+        raise InputError(f"gemm_bf16_at_b shapes {tuple(a.shape)}^T x {tuple(b.shape)}")
+    a, b = a.contiguous(), b.contiguous()
+    E, K, M = a.shape
+    N = b.shape[2]
+    c = _out(out, (E, M, N), out_dtype, a.device)
+    _native.check(_native.lib().bt_gemm_bf16_ex(a.data_ptr(), b.data_ptr(), c.data_ptr(), E, M, N, K, K * M, K * N,
+                                                 M * N, 1 if out_dtype == torch.bfloat16 else 0, None, 1, grid,
+                                                 stream()), "gemm_bf16_at_b")
+    return c

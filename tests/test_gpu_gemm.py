@@ -92,3 +92,25 @@ def test_batched_gemm_equals_per_entry_gemms(gemm, E, M, N, K):
     ref = torch.einsum("emk,enk->emn", a.double(), b.double())
     bound = K * 2.0 ** -23 * torch.einsum("emk,enk->emn", a.double().abs(), b.double().abs())
     assert bool(((c.double() - ref).abs() <= bound + 1e-30).all())
+
+
+@pytest.mark.parametrize("E,M,N,K,variant", [(4, 256, 256, 512, "0"), (3, 128, 384, 256, "0"),
+                                             (2, 768, 3072, 1024, "0"), (2, 256, 512, 256, "1")])
+def test_mn_major_gemm(gemm, monkeypatch, E, M, N, K, variant):
+    """c[e] = a[e]^T b[e] from token-major operands (MN-major TMA/UMMA): within the fp32-accumulation
+    bound of a float64 reference, identical bits for every batch entry alone and in the batch, and
+    (the accumulation order is the K order) the same bits as the K-major GEMM of the transposes."""
+    from paper_2208_14228_b200.gemm import gemm_bf16_at_b, gemm_bf16_batched
+
+    monkeypatch.setenv("BT_GEMM_VARIANT", variant)
+    g = torch.Generator(device="cuda").manual_seed(E * 7 + N)
+    a = torch.randn(E, K, M, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(E, K, N, device="cuda", generator=g).to(torch.bfloat16)
+    c = gemm_bf16_at_b(a, b)
+    ref = torch.einsum("ekm,ekn->emn", a.double(), b.double())
+    bound = K * 2.0 ** -23 * torch.einsum("ekm,ekn->emn", a.double().abs(), b.double().abs())
+    assert bool(((c.double() - ref).abs() <= bound + 1e-30).all())
+    for e in range(E):
+        assert torch.equal(c[e].view(torch.int32), gemm_bf16_at_b(a[e], b[e])[0].view(torch.int32)), e
+    kmaj = gemm_bf16_batched(a.transpose(1, 2).contiguous(), b.transpose(1, 2).contiguous())
+    assert torch.equal(c.view(torch.int32), kmaj.view(torch.int32))
