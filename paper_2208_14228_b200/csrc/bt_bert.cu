@@ -13,11 +13,12 @@
 //   LayerNorm input sums / outputs fp32 [T][Dm], bf16 copies for the GEMMs.
 //
 // Kernels:
-//   attn_fwd / attn_bwd  one CTA per (sequence, head), 8 warps x 16 query
-//                        rows, mma.sync m16n8k16 bf16 (S = QK^T/8, softmax,
-//                        keyed dropout, PV); the backward recomputes P from
-//                        Q, K (same instructions -> same bits) and sums dV,
-//                        dK over query rows in ascending k-steps;
+//   attn_fwd / attn_bwd  persistent CTAs walking (sequence, head) items with
+//                        cp.async double buffering; 8 warps x 16 query rows,
+//                        mma.sync m16n8k16 bf16 (S = QK^T/8, softmax, keyed
+//                        dropout, PV); the backward recomputes P from Q, K
+//                        (same instructions -> same bits) and sums dV, dK over
+//                        query rows in ascending k-steps;
 //   ln_fwd               x = resid + dropout(branch + bias); y = LN(x)
 //                        (one warp per row, butterfly sums: fixed order);
 //   ln_bwd               dx = LN'(dy1 + dy2); branch grad = dropout'(dx);
@@ -67,27 +68,41 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *(const uint32_t*)&v;
 }
 
-// [128][64] bf16 tile (row stride `ld` elements in global) -> smem [128][LDS]
-__device__ __forceinline__ void load_tile(__nv_bfloat16* dst, const __nv_bfloat16* src, int ld) {
+// [128][64] bf16 tile (row stride `ld` elements in global) -> smem [128][LDS], asynchronously
+// (cp.async 16 B; the persistent attention kernels prefetch the next (sequence, head) item's
+// tiles while computing the current one)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void load_tile_async(__nv_bfloat16* dst, const __nv_bfloat16* src, int ld) {
+  const uint32_t d = su32(dst);
   for (int c = threadIdx.x; c < SEQ * (HD / 8); c += AT_THREADS) {
     const int r = c >> 3, k = (c & 7) * 8;
-    *(uint4*)(dst + r * LDS + k) = *(const uint4*)(src + (size_t)r * ld + k);
+    cp_async16(d + 2u * (r * LDS + k), src + (size_t)r * ld + k);
   }
 }
 
-// Keep-scale of the attention-probability dropout for (row i, columns j, j+1), j even:
-// one draw per column pair, low / high 32-bit halves (the hidden dropout's rule).
-__device__ __forceinline__ void attn_mask2(uint64_t sd, uint64_t nb, int i, int j, uint32_t thr, float keep,
-                                           float* m0, float* m1) {
+// Attention-probability dropout.  One splitmix64 draw per (16-row block, row g < 8, column pair)
+// covers 4 units as 16-bit fields: field (hi*2 + lo) is (row 16*r16 + g + 8*hi, column 2*jp + lo);
+// a unit is dropped iff its field < ceil(p * 2^16).  Counter of the draw: nb + (r16*8 + g)*64 + jp,
+// nb = 4096 draws per (EST, step, layer, sequence, head).  In the mma fragment layout this is one
+// draw per thread per 8-column tile, covering the thread's rows g and g+8, columns 2c, 2c+1.
+__device__ __forceinline__ uint32_t threshold32(float p) { return p > 0.f ? (uint32_t)ceil((double)p * 0x1p32) : 0u; }
+__device__ __forceinline__ uint32_t threshold16(float p) { return p > 0.f ? (uint32_t)ceil((double)p * 65536.0) : 0u; }
+__device__ __forceinline__ void attn_mask4(uint64_t sd, uint64_t n, uint32_t thr, float keep, float* m) {
   if (thr == 0) {
-    *m0 = *m1 = 1.f;
+    m[0] = m[1] = m[2] = m[3] = 1.f;
     return;
   }
-  const uint64_t r = draw_raw(sd, (nb + (uint64_t)i * SEQ + (uint64_t)j) >> 1);
-  *m0 = (uint32_t)r < thr ? 0.f : keep;
-  *m1 = (uint32_t)(r >> 32) < thr ? 0.f : keep;
+  const uint64_t r = draw_raw(sd, n);
+  const uint32_t lo = (uint32_t)r, hi = (uint32_t)(r >> 32);
+  m[0] = (lo & 0xFFFFu) < thr ? 0.f : keep;
+  m[1] = (lo >> 16) < thr ? 0.f : keep;
+  m[2] = (hi & 0xFFFFu) < thr ? 0.f : keep;
+  m[3] = (hi >> 16) < thr ? 0.f : keep;
 }
-__device__ __forceinline__ uint32_t threshold32(float p) { return p > 0.f ? (uint32_t)ceil((double)p * 0x1p32) : 0u; }
 
 // S = softmax(Q_w K^T / 8) for the warp's 16 query rows: s[nt][0..1] = row g, s[nt][2..3] = row g+8,
 // columns nt*8 + 2*(lane&3) + {0,1}.  Fixed instruction sequence -> the backward recomputes the same bits.
@@ -108,11 +123,13 @@ __device__ __forceinline__ void warp_softmax(const __nv_bfloat16* Qs, const __nv
       mma16816(s[2 * n2 + 1], a, b[2], b[3]);
     }
   }
+  // scores in log2 units: S/8 * log2(e), so exp(S/8 - max) = exp2(s - max2) (ex2.approx)
+  constexpr float SC = 0.125f * 1.4426950408889634f;
   float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
   for (int nt = 0; nt < 16; ++nt) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) s[nt][q] *= 0.125f;  // 1/sqrt(64), exact
+    for (int q = 0; q < 4; ++q) s[nt][q] *= SC;
     m0 = fmaxf(m0, fmaxf(s[nt][0], s[nt][1]));
     m1 = fmaxf(m1, fmaxf(s[nt][2], s[nt][3]));
   }
@@ -123,20 +140,20 @@ __device__ __forceinline__ void warp_softmax(const __nv_bfloat16* Qs, const __nv
   float l0 = 0.f, l1 = 0.f;
 #pragma unroll
   for (int nt = 0; nt < 16; ++nt) {
-    s[nt][0] = expf(s[nt][0] - m0);
+    s[nt][0] = exp2f(s[nt][0] - m0);
     l0 += s[nt][0];
-    s[nt][1] = expf(s[nt][1] - m0);
+    s[nt][1] = exp2f(s[nt][1] - m0);
     l0 += s[nt][1];
-    s[nt][2] = expf(s[nt][2] - m1);
+    s[nt][2] = exp2f(s[nt][2] - m1);
     l1 += s[nt][2];
-    s[nt][3] = expf(s[nt][3] - m1);
+    s[nt][3] = exp2f(s[nt][3] - m1);
     l1 += s[nt][3];
   }
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);  // a+b == b+a: all four lanes of a row agree bitwise
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  const float i0 = 1.f / l0, i1 = 1.f / l1;
+  const float i0 = __frcp_rn(l0), i1 = __frcp_rn(l1);
 #pragma unroll
   for (int nt = 0; nt < 16; ++nt) {
     s[nt][0] *= i0;
@@ -150,198 +167,224 @@ struct AttnArgs {
   const __nv_bfloat16* qkv;  // [T][3*Dm]
   const __nv_bfloat16* dctx; // [T][Dm] (backward)
   __nv_bfloat16* out;        // ctx [T][Dm] (forward) / dqkv [T][3*Dm] (backward)
-  int Dm, H, seqs_per_est, est_base, L, layer;
+  int Dm, H, seqs_per_est, est_base, L, layer, n_items;
   uint64_t seed;
   int64_t step;
   float p;
 };
 
-// counter base of (EST stream, step, layer, sequence-in-EST, head): 128 x 128 (i, j) draws follow
+// counter base of (EST stream, step, layer, sequence-in-EST, head): 4096 draws (16384 units) follow
 __device__ __forceinline__ uint64_t attn_counter_base(const AttnArgs& a, int sl, int h) {
-  return ((((uint64_t)a.step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ);
+  return ((((uint64_t)a.step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4);
 }
 
-constexpr int ATF_SMEM = 3 * SEQ * LDS * 2;
+// Persistent: CTA walks items (sequence s, head h) = (it / H, it % H), it += gridDim.x; the next
+// item's tiles stream into the other buffer (cp.async) while this one computes.
+constexpr int ATF_BUF = 3 * SEQ * LDS;  // bf16 elements per buffer (Q, K, V)
+constexpr int ATF_SMEM = 2 * ATF_BUF * 2;
 __global__ void __launch_bounds__(AT_THREADS) attn_fwd_kernel(const AttnArgs a) {
   extern __shared__ __align__(16) uint8_t at_smem[];
-  __nv_bfloat16* Qs = (__nv_bfloat16*)at_smem;
-  __nv_bfloat16* Ks = Qs + SEQ * LDS;
-  __nv_bfloat16* Vs = Ks + SEQ * LDS;
-  const int s = blockIdx.x, h = blockIdx.y;
+  __nv_bfloat16* const buf0 = (__nv_bfloat16*)at_smem;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ld = 3 * a.Dm;
-  const __nv_bfloat16* base = a.qkv + (size_t)s * SEQ * ld + h * HD;
-  load_tile(Qs, base, ld);
-  load_tile(Ks, base + a.Dm, ld);
-  load_tile(Vs, base + 2 * a.Dm, ld);
-  __syncthreads();
-
-  float P[16][4];
-  warp_softmax(Qs, Ks, w, lane, P);
-
-  const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
-  const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
-  const uint64_t nb = attn_counter_base(a, sl, h);
-  const uint32_t thr = threshold32(a.p);
+  auto issue = [&](int it, __nv_bfloat16* bq) {
+    if (it < a.n_items) {
+      const __nv_bfloat16* base = a.qkv + (size_t)(it / a.H) * SEQ * ld + (it % a.H) * HD;
+      load_tile_async(bq, base, ld);
+      load_tile_async(bq + SEQ * LDS, base + a.Dm, ld);
+      load_tile_async(bq + 2 * SEQ * LDS, base + 2 * a.Dm, ld);
+    }
+    cp_commit();
+  };
+  const uint32_t thr = threshold16(a.p);
   const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
   const int g = lane >> 2, i0 = 16 * w + g, c0 = 2 * (lane & 3);
-  uint32_t pa[8][4];  // dropped P as bf16 A fragments, k-step kv = keys 16kv..16kv+15
+  int cur = 0;
+  issue(blockIdx.x, buf0);
+  for (int it = blockIdx.x; it < a.n_items; it += gridDim.x, cur ^= 1) {
+    __nv_bfloat16* const Qs = buf0 + cur * ATF_BUF;
+    __nv_bfloat16* const Ks = Qs + SEQ * LDS;
+    __nv_bfloat16* const Vs = Ks + SEQ * LDS;
+    issue(it + gridDim.x, buf0 + (cur ^ 1) * ATF_BUF);
+    cp_wait1();
+    __syncthreads();
+    const int s = it / a.H, h = it % a.H;
+    float P[16][4];
+    warp_softmax(Qs, Ks, w, lane, P);
+    const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
+    const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
+    const uint64_t nb = attn_counter_base(a, sl, h) + (uint64_t)(w * 8 + g) * 64 + (lane & 3);
+    uint32_t pa[8][4];  // dropped P as bf16 A fragments, k-step kv = keys 16kv..16kv+15
 #pragma unroll
-  for (int nt = 0; nt < 16; ++nt) {
-    float m0, m1, m2, m3;
-    attn_mask2(sd, nb, i0, nt * 8 + c0, thr, keep, &m0, &m1);
-    attn_mask2(sd, nb, i0 + 8, nt * 8 + c0, thr, keep, &m2, &m3);
-    pa[nt >> 1][(nt & 1) * 2 + 0] = pack2(P[nt][0] * m0, P[nt][1] * m1);
-    pa[nt >> 1][(nt & 1) * 2 + 1] = pack2(P[nt][2] * m2, P[nt][3] * m3);
-  }
-  float o[8][4];
-#pragma unroll
-  for (int dt = 0; dt < 8; ++dt) o[dt][0] = o[dt][1] = o[dt][2] = o[dt][3] = 0.f;
-  const uint32_t vb = su32(Vs);
-#pragma unroll
-  for (int kv = 0; kv < 8; ++kv) {
-#pragma unroll
-    for (int d2 = 0; d2 < 4; ++d2) {
-      uint32_t b[4];
-      ldsm_x4_t(vb + 2u * ((kv * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + d2 * 16 + (lane >> 4) * 8), b);
-      mma16816(o[2 * d2], pa[kv], b[0], b[1]);
-      mma16816(o[2 * d2 + 1], pa[kv], b[2], b[3]);
+    for (int nt = 0; nt < 16; ++nt) {
+      float m[4];
+      attn_mask4(sd, nb + nt * 4, thr, keep, m);
+      pa[nt >> 1][(nt & 1) * 2 + 0] = pack2(P[nt][0] * m[0], P[nt][1] * m[1]);
+      pa[nt >> 1][(nt & 1) * 2 + 1] = pack2(P[nt][2] * m[2], P[nt][3] * m[3]);
     }
-  }
-  __nv_bfloat16* out = a.out + (size_t)s * SEQ * a.Dm + h * HD;
+    float o[8][4];
 #pragma unroll
-  for (int dt = 0; dt < 8; ++dt) {
-    *(uint32_t*)(out + (size_t)i0 * a.Dm + dt * 8 + c0) = pack2(o[dt][0], o[dt][1]);
-    *(uint32_t*)(out + (size_t)(i0 + 8) * a.Dm + dt * 8 + c0) = pack2(o[dt][2], o[dt][3]);
-  }
-}
-
-// dV = Pd^T dO, dP = (dO V^T) * mask, dS = P * (dP - rowsum(dP * P)) / 8, dQ = dS K, dK = dS^T Q
-constexpr int ATB_SMEM = (4 * SEQ * LDS + 2 * SEQ * LDP) * 2;
-__global__ void __launch_bounds__(AT_THREADS) attn_bwd_kernel(const AttnArgs a) {
-  extern __shared__ __align__(16) uint8_t at_smem[];
-  __nv_bfloat16* Qs = (__nv_bfloat16*)at_smem;
-  __nv_bfloat16* Ks = Qs + SEQ * LDS;
-  __nv_bfloat16* Vs = Ks + SEQ * LDS;
-  __nv_bfloat16* dOs = Vs + SEQ * LDS;
-  __nv_bfloat16* Ps = dOs + SEQ * LDS;   // dropped P  [query][key]
-  __nv_bfloat16* dSs = Ps + SEQ * LDP;   // dS / 8     [query][key]
-  const int s = blockIdx.x, h = blockIdx.y;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ld = 3 * a.Dm;
-  const __nv_bfloat16* base = a.qkv + (size_t)s * SEQ * ld + h * HD;
-  load_tile(Qs, base, ld);
-  load_tile(Ks, base + a.Dm, ld);
-  load_tile(Vs, base + 2 * a.Dm, ld);
-  load_tile(dOs, a.dctx + (size_t)s * SEQ * a.Dm + h * HD, a.Dm);
-  __syncthreads();
-
-  float P[16][4];
-  warp_softmax(Qs, Ks, w, lane, P);
-  float dp[16][4];  // dO_w V^T
-#pragma unroll
-  for (int nt = 0; nt < 16; ++nt) dp[nt][0] = dp[nt][1] = dp[nt][2] = dp[nt][3] = 0.f;
-  {
-    const uint32_t ob = su32(dOs), vb = su32(Vs);
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      uint32_t af[4];
-      ldsm_x4(ob + 2u * ((16 * w + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + kk * 16 + (lane >> 4) * 8), af);
-#pragma unroll
-      for (int n2 = 0; n2 < 8; ++n2) {
-        uint32_t b[4];
-        ldsm_x4(vb + 2u * ((n2 * 16 + (lane & 7) + (lane >> 4) * 8) * LDS + kk * 16 + ((lane >> 3) & 1) * 8), b);
-        mma16816(dp[2 * n2], af, b[0], b[1]);
-        mma16816(dp[2 * n2 + 1], af, b[2], b[3]);
-      }
-    }
-  }
-  const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
-  const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
-  const uint64_t nb = attn_counter_base(a, sl, h);
-  const uint32_t thr = threshold32(a.p);
-  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
-  const int g = lane >> 2, i0 = 16 * w + g, c0 = 2 * (lane & 3);
-  float r0 = 0.f, r1 = 0.f;  // rowsum(dP * P), rows i0 / i0+8
-#pragma unroll
-  for (int nt = 0; nt < 16; ++nt) {
-    float m[4];
-    attn_mask2(sd, nb, i0, nt * 8 + c0, thr, keep, &m[0], &m[1]);
-    attn_mask2(sd, nb, i0 + 8, nt * 8 + c0, thr, keep, &m[2], &m[3]);
-    const int j = nt * 8 + c0;
-    *(uint32_t*)(Ps + i0 * LDP + j) = pack2(P[nt][0] * m[0], P[nt][1] * m[1]);
-    *(uint32_t*)(Ps + (i0 + 8) * LDP + j) = pack2(P[nt][2] * m[2], P[nt][3] * m[3]);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) dp[nt][q] *= m[q];
-    r0 += dp[nt][0] * P[nt][0];
-    r0 += dp[nt][1] * P[nt][1];
-    r1 += dp[nt][2] * P[nt][2];
-    r1 += dp[nt][3] * P[nt][3];
-  }
-  r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
-  r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
-  r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
-  r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
-  uint32_t da[8][4];  // dS/8 as bf16 A fragments (rows of this warp)
-#pragma unroll
-  for (int nt = 0; nt < 16; ++nt) {
-    const float d0 = P[nt][0] * (dp[nt][0] - r0) * 0.125f, d1 = P[nt][1] * (dp[nt][1] - r0) * 0.125f;
-    const float d2 = P[nt][2] * (dp[nt][2] - r1) * 0.125f, d3 = P[nt][3] * (dp[nt][3] - r1) * 0.125f;
-    const uint32_t lo = pack2(d0, d1), hi = pack2(d2, d3);
-    da[nt >> 1][(nt & 1) * 2 + 0] = lo;
-    da[nt >> 1][(nt & 1) * 2 + 1] = hi;
-    const int j = nt * 8 + c0;
-    *(uint32_t*)(dSs + i0 * LDP + j) = lo;
-    *(uint32_t*)(dSs + (i0 + 8) * LDP + j) = hi;
-  }
-  __nv_bfloat16* dq = a.out + (size_t)s * SEQ * ld + h * HD;
-  {  // dQ_w = dS_w K
-    float acc[8][4];
-#pragma unroll
-    for (int dt = 0; dt < 8; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.f;
-    const uint32_t kb = su32(Ks);
+    for (int dt = 0; dt < 8; ++dt) o[dt][0] = o[dt][1] = o[dt][2] = o[dt][3] = 0.f;
+    const uint32_t vb = su32(Vs);
 #pragma unroll
     for (int kv = 0; kv < 8; ++kv) {
 #pragma unroll
       for (int d2 = 0; d2 < 4; ++d2) {
         uint32_t b[4];
-        ldsm_x4_t(kb + 2u * ((kv * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + d2 * 16 + (lane >> 4) * 8), b);
-        mma16816(acc[2 * d2], da[kv], b[0], b[1]);
-        mma16816(acc[2 * d2 + 1], da[kv], b[2], b[3]);
+        ldsm_x4_t(vb + 2u * ((kv * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + d2 * 16 + (lane >> 4) * 8), b);
+        mma16816(o[2 * d2], pa[kv], b[0], b[1]);
+        mma16816(o[2 * d2 + 1], pa[kv], b[2], b[3]);
       }
     }
+    __nv_bfloat16* out = a.out + (size_t)s * SEQ * a.Dm + h * HD;
 #pragma unroll
     for (int dt = 0; dt < 8; ++dt) {
-      *(uint32_t*)(dq + (size_t)i0 * ld + dt * 8 + c0) = pack2(acc[dt][0], acc[dt][1]);
-      *(uint32_t*)(dq + (size_t)(i0 + 8) * ld + dt * 8 + c0) = pack2(acc[dt][2], acc[dt][3]);
+      *(uint32_t*)(out + (size_t)i0 * a.Dm + dt * 8 + c0) = pack2(o[dt][0], o[dt][1]);
+      *(uint32_t*)(out + (size_t)(i0 + 8) * a.Dm + dt * 8 + c0) = pack2(o[dt][2], o[dt][3]);
     }
+    __syncthreads();  // all warps are done with this buffer before it is refilled
   }
-  __syncthreads();
-  // warp w: key rows 16w..16w+15.  dV = Pd^T dO, dK = dS^T Q; k-steps = ascending query blocks
-#pragma unroll 1
-  for (int which = 0; which < 2; ++which) {
-    const uint32_t ab = su32(which == 0 ? Ps : dSs), bb = su32(which == 0 ? dOs : Qs);
-    float acc[8][4];
+}
+
+// dV = Pd^T dO, dP = (dO V^T) * mask, dS = P * (dP - rowsum(dP * P)) / 8, dQ = dS K, dK = dS^T Q
+constexpr int ATB_BUF = 4 * SEQ * LDS;  // Q, K, V, dO
+constexpr int ATB_SMEM = (2 * ATB_BUF + 2 * SEQ * LDP) * 2;
+__global__ void __launch_bounds__(AT_THREADS) attn_bwd_kernel(const AttnArgs a) {
+  extern __shared__ __align__(16) uint8_t at_smem[];
+  __nv_bfloat16* const buf0 = (__nv_bfloat16*)at_smem;
+  __nv_bfloat16* const Ps = buf0 + 2 * ATB_BUF;  // dropped P  [query][key]
+  __nv_bfloat16* const dSs = Ps + SEQ * LDP;     // dS / 8     [query][key]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ld = 3 * a.Dm;
+  auto issue = [&](int it, __nv_bfloat16* bq) {
+    if (it < a.n_items) {
+      const int s = it / a.H, h = it % a.H;
+      const __nv_bfloat16* base = a.qkv + (size_t)s * SEQ * ld + h * HD;
+      load_tile_async(bq, base, ld);
+      load_tile_async(bq + SEQ * LDS, base + a.Dm, ld);
+      load_tile_async(bq + 2 * SEQ * LDS, base + 2 * a.Dm, ld);
+      load_tile_async(bq + 3 * SEQ * LDS, a.dctx + (size_t)s * SEQ * a.Dm + h * HD, a.Dm);
+    }
+    cp_commit();
+  };
+  const uint32_t thr = threshold16(a.p);
+  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
+  const int g = lane >> 2, i0 = 16 * w + g, c0 = 2 * (lane & 3);
+  int cur = 0;
+  issue(blockIdx.x, buf0);
+  for (int it = blockIdx.x; it < a.n_items; it += gridDim.x, cur ^= 1) {
+    __nv_bfloat16* const Qs = buf0 + cur * ATB_BUF;
+    __nv_bfloat16* const Ks = Qs + SEQ * LDS;
+    __nv_bfloat16* const Vs = Ks + SEQ * LDS;
+    __nv_bfloat16* const dOs = Vs + SEQ * LDS;
+    issue(it + gridDim.x, buf0 + (cur ^ 1) * ATB_BUF);
+    cp_wait1();
+    __syncthreads();
+    const int s = it / a.H, h = it % a.H;
+    float P[16][4];
+    warp_softmax(Qs, Ks, w, lane, P);
+    float dp[16][4];  // dO_w V^T
 #pragma unroll
-    for (int dt = 0; dt < 8; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.f;
+    for (int nt = 0; nt < 16; ++nt) dp[nt][0] = dp[nt][1] = dp[nt][2] = dp[nt][3] = 0.f;
+    {
+      const uint32_t ob = su32(dOs), vb = su32(Vs);
 #pragma unroll
-    for (int kq = 0; kq < 8; ++kq) {
-      uint32_t af[4];
-      ldsm_x4_t(ab + 2u * ((kq * 16 + (lane & 7) + (lane >> 4) * 8) * LDP + 16 * w + ((lane >> 3) & 1) * 8), af);
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        uint32_t af[4];
+        ldsm_x4(ob + 2u * ((16 * w + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + kk * 16 + (lane >> 4) * 8), af);
 #pragma unroll
-      for (int d2 = 0; d2 < 4; ++d2) {
-        uint32_t b[4];
-        ldsm_x4_t(bb + 2u * ((kq * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + d2 * 16 + (lane >> 4) * 8), b);
-        mma16816(acc[2 * d2], af, b[0], b[1]);
-        mma16816(acc[2 * d2 + 1], af, b[2], b[3]);
+        for (int n2 = 0; n2 < 8; ++n2) {
+          uint32_t b[4];
+          ldsm_x4(vb + 2u * ((n2 * 16 + (lane & 7) + (lane >> 4) * 8) * LDS + kk * 16 + ((lane >> 3) & 1) * 8), b);
+          mma16816(dp[2 * n2], af, b[0], b[1]);
+          mma16816(dp[2 * n2 + 1], af, b[2], b[3]);
+        }
       }
     }
-    __nv_bfloat16* dst = dq + (which == 0 ? 2 : 1) * a.Dm;
+    const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
+    const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
+    const uint64_t nb = attn_counter_base(a, sl, h) + (uint64_t)(w * 8 + g) * 64 + (lane & 3);
+    float r0 = 0.f, r1 = 0.f;  // rowsum(dP * P), rows i0 / i0+8
 #pragma unroll
-    for (int dt = 0; dt < 8; ++dt) {
-      *(uint32_t*)(dst + (size_t)i0 * ld + dt * 8 + c0) = pack2(acc[dt][0], acc[dt][1]);
-      *(uint32_t*)(dst + (size_t)(i0 + 8) * ld + dt * 8 + c0) = pack2(acc[dt][2], acc[dt][3]);
+    for (int nt = 0; nt < 16; ++nt) {
+      float m[4];
+      attn_mask4(sd, nb + nt * 4, thr, keep, m);
+      const int j = nt * 8 + c0;
+      *(uint32_t*)(Ps + i0 * LDP + j) = pack2(P[nt][0] * m[0], P[nt][1] * m[1]);
+      *(uint32_t*)(Ps + (i0 + 8) * LDP + j) = pack2(P[nt][2] * m[2], P[nt][3] * m[3]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dp[nt][q] *= m[q];
+      r0 += dp[nt][0] * P[nt][0];
+      r0 += dp[nt][1] * P[nt][1];
+      r1 += dp[nt][2] * P[nt][2];
+      r1 += dp[nt][3] * P[nt][3];
     }
+    r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
+    r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
+    r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
+    r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
+    uint32_t da[8][4];  // dS/8 as bf16 A fragments (rows of this warp)
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const float d0 = P[nt][0] * (dp[nt][0] - r0) * 0.125f, d1 = P[nt][1] * (dp[nt][1] - r0) * 0.125f;
+      const float d2 = P[nt][2] * (dp[nt][2] - r1) * 0.125f, d3 = P[nt][3] * (dp[nt][3] - r1) * 0.125f;
+      const uint32_t lo = pack2(d0, d1), hi = pack2(d2, d3);
+      da[nt >> 1][(nt & 1) * 2 + 0] = lo;
+      da[nt >> 1][(nt & 1) * 2 + 1] = hi;
+      const int j = nt * 8 + c0;
+      *(uint32_t*)(dSs + i0 * LDP + j) = lo;
+      *(uint32_t*)(dSs + (i0 + 8) * LDP + j) = hi;
+    }
+    __nv_bfloat16* dq = a.out + (size_t)s * SEQ * ld + h * HD;
+    {  // dQ_w = dS_w K
+      float acc[8][4];
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.f;
+      const uint32_t kb = su32(Ks);
+#pragma unroll
+      for (int kv = 0; kv < 8; ++kv) {
+#pragma unroll
+        for (int d2 = 0; d2 < 4; ++d2) {
+          uint32_t b[4];
+          ldsm_x4_t(kb + 2u * ((kv * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + d2 * 16 + (lane >> 4) * 8), b);
+          mma16816(acc[2 * d2], da[kv], b[0], b[1]);
+          mma16816(acc[2 * d2 + 1], da[kv], b[2], b[3]);
+        }
+      }
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) {
+        *(uint32_t*)(dq + (size_t)i0 * ld + dt * 8 + c0) = pack2(acc[dt][0], acc[dt][1]);
+        *(uint32_t*)(dq + (size_t)(i0 + 8) * ld + dt * 8 + c0) = pack2(acc[dt][2], acc[dt][3]);
+      }
+    }
+    __syncthreads();
+    // warp w: key rows 16w..16w+15.  dV = Pd^T dO, dK = dS^T Q; k-steps = ascending query blocks
+#pragma unroll 1
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t ab = su32(which == 0 ? Ps : dSs), bb = su32(which == 0 ? dOs : Qs);
+      float acc[8][4];
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.f;
+#pragma unroll
+      for (int kq = 0; kq < 8; ++kq) {
+        uint32_t af[4];
+        ldsm_x4_t(ab + 2u * ((kq * 16 + (lane & 7) + (lane >> 4) * 8) * LDP + 16 * w + ((lane >> 3) & 1) * 8), af);
+#pragma unroll
+        for (int d2 = 0; d2 < 4; ++d2) {
+          uint32_t b[4];
+          ldsm_x4_t(bb + 2u * ((kq * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + d2 * 16 + (lane >> 4) * 8), b);
+          mma16816(acc[2 * d2], af, b[0], b[1]);
+          mma16816(acc[2 * d2 + 1], af, b[2], b[3]);
+        }
+      }
+      __nv_bfloat16* dst = dq + (which == 0 ? 2 : 1) * a.Dm;
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) {
+        *(uint32_t*)(dst + (size_t)i0 * ld + dt * 8 + c0) = pack2(acc[dt][0], acc[dt][1]);
+        *(uint32_t*)(dst + (size_t)(i0 + 8) * ld + dt * 8 + c0) = pack2(acc[dt][2], acc[dt][3]);
+      }
+    }
+    __syncthreads();  // Ps / dSs / this buffer free before the next item
   }
 }
 
@@ -649,25 +692,33 @@ int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out,
                      int seqs_per_est, int est_base, int L, int layer, uint64_t seed, int64_t step, float p,
                      cudaStream_t s) {
   bert::AttnArgs a{(const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dctx, (__nv_bfloat16*)out, Dm, H, seqs_per_est,
-                   est_base, L, layer, seed, step, p};
-  const dim3 grid(n_seq, H);
+                   est_base, L, layer, n_seq * H, seed, step, p};
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (!backward) {
     static bool attr = false;
     if (!attr) {
       if (cudaFuncSetAttribute(bert::attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bert::ATF_SMEM) !=
-          cudaSuccess)
+              cudaSuccess ||
+          cudaFuncSetAttribute(bert::attn_fwd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100) !=
+              cudaSuccess)
         return ERR_CUDA;
       attr = true;
     }
+    const int grid = a.n_items < 2 * sms ? a.n_items : 2 * sms;
     bert::attn_fwd_kernel<<<grid, bert::AT_THREADS, bert::ATF_SMEM, s>>>(a);
   } else {
     static bool attr = false;
     if (!attr) {
       if (cudaFuncSetAttribute(bert::attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bert::ATB_SMEM) !=
-          cudaSuccess)
+              cudaSuccess ||
+          cudaFuncSetAttribute(bert::attn_bwd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100) !=
+              cudaSuccess)
         return ERR_CUDA;
       attr = true;
     }
+    const int grid = a.n_items < sms ? a.n_items : sms;
     bert::attn_bwd_kernel<<<grid, bert::AT_THREADS, bert::ATB_SMEM, s>>>(a);
   }
   return ok_or_cuda_b();

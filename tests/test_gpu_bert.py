@@ -150,15 +150,22 @@ def test_layer0_stages_match_float64_restatement(bert):
         return torch.from_numpy(sc)
 
     def attn_scale(l=0):
+        """one draw per (16-row block, row g < 8, column pair): four 16-bit fields, field
+        ((i >> 3) & 1) * 2 + (j & 1) decides (i, j); dropped iff field < ceil(p * 2^16)"""
         sc = np.empty((E, S, H, 128, 128))
         i = np.arange(128)[:, None]
         j = np.arange(128)[None, :]
+        cnt = ((i >> 4) * 8 + (i & 7)) * 64 + (j >> 1)
+        field = ((i >> 3) & 1) * 2 + (j & 1)
+        thr = np.uint64(math.ceil(pa * 65536))
         for e in range(E):
             s0 = host_derive_stream(TAG_ADROP, seed, e)
             for sl in range(S):
                 for h in range(H):
-                    nb = ((((step * NL + l) * S + sl) * H + h) * 16384)
-                    sc[e, sl, h] = _keep(_draws(s0, (nb + i * 128 + j) >> 1), j, pa)
+                    nb = ((((step * NL + l) * S + sl) * H + h) * 4096)
+                    raw = _draws(s0, nb + cnt)
+                    f = (raw >> (np.uint64(16) * field.astype(np.uint64))) & np.uint64(0xFFFF)
+                    sc[e, sl, h] = np.where(f < thr, 0.0, 1.0 / (1.0 - pa))
         return torch.from_numpy(sc).view(E * S, H, 128, 128)
 
     # ---- forward, layer 0
