@@ -335,11 +335,69 @@ def bench_gemm(flush, peaks, M=8192, N=8192, K=8192, iters=10):
     del a, b, again
     torch.cuda.empty_cache()
     tf = fl / ms / 1e9
-    return {"kernel": "gemm_bf16_tn_pair_kernel<6,bf16> (bt_gemm.cu: tcgen05 cta_group::2 + TMA, 256x256 tile per CTA pair, fixed K order)",
+    return {"kernel": "gemm_bf16_tn_pair_kernel<5,bf16> (bt_gemm.cu: tcgen05 cta_group::2 + TMA, 256x256 tile per CTA pair, fixed K order)",
             "shape": [M, N, K], "bound": "tensor", "achieved": round(tf, 1), "peak": peaks["bf16_tflops"],
             "unit": "TFLOP/s", "frac": round(tf / peaks["bf16_tflops"], 4), "ms": round(ms, 4),
             "traffic": ncu_traffic("gemm_bf16_tn_kernel"), "cublas_tflops": round(fl / ms_cublas / 1e9, 1),
             "grid_invariant_bits": same}
+
+
+def bench_bert(peaks, ests=32, steps=5, warmup=3):
+    """C4 (BASELINE.json configs[3]): BERT-base encoder (12 x 768, 12 heads, FFN 3072, seq 128, dropout 0.1),
+    32 ESTs x 8 sequences, deterministic tcgen05 GEMMs + fixed-order reducer (paper_2208_14228_b200/bert.py).
+    Step time by CUDA events; per-kernel split of one step by CUPTI (torch.profiler); the same 32 ESTs as
+    4 launch groups of 8 (the 4-GPU mapping's per-GPU work) must give bit-identical weights."""
+    from torch.profiler import ProfilerActivity, profile
+
+    from paper_2208_14228_b200.bert import BertJob
+
+    job = BertJob(ests=ests)
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        job.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        losses = job.step()
+    e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        job.step()
+        torch.cuda.synchronize()
+    split = {}
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA:
+            key = next((k for k in ("gemm_bf16", "attn_fwd", "attn_bwd", "ln_fwd", "ln_bwd", "reduce", "colsum")
+                        if k in ev.name), "other")
+            split[key] = split.get(key, 0.0) + ev.device_time_total / 1e3
+    fnv_one = job.params.view(torch.int32).sum().item()
+    flops = job.gemm_flops_per_step()
+    del job
+    torch.cuda.empty_cache()
+    a, b = BertJob(ests=ests, layers=2), BertJob(ests=ests, layers=2)
+    for _ in range(2):
+        a.step()
+        b.step([ests // 4] * 4)
+    same = bool(torch.equal(a.params.view(torch.int32), b.params.view(torch.int32)))
+    del a, b
+    torch.cuda.empty_cache()
+    gemm_ms = split.get("gemm_bf16", 0.0)
+    seqs = ests * 8
+    return {"workload": "C4: BERT-base encoder bf16 (12 layers, d 768, 12 heads, FFN 3072, seq 128, dropout 0.1 "
+                        "hidden + attention), 32 ESTs x 8 sequences, MSE head, momentum SGD (BASELINE.json configs[3])",
+            "samples_per_s": round(seqs / (ms / 1e3), 1), "unit": "sequences/s", "ms_per_step": round(ms, 3),
+            "tokens_per_s": round(seqs * 128 / (ms / 1e3), 1), "loss": round(losses.mean().item(), 5),
+            "roofline": {"kernel": "gemm_bf16_tn_pair_kernel (bt_gemm.cu, all dense products of the step)",
+                         "bound": "tensor", "achieved": round(flops / gemm_ms / 1e9, 1) if gemm_ms else None,
+                         "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                         "frac": round(flops / gemm_ms / 1e9 / peaks["bf16_tflops"], 4) if gemm_ms else None,
+                         "step_level_tflops": round(flops / ms / 1e9, 1), "dense_flops_per_step": flops,
+                         "traffic": None},
+            "kernel_ms_per_step": {k: round(v, 3) for k, v in sorted(split.items(), key=lambda kv: -kv[1])},
+            "bit_identical_groupings": {"groups": [[ests], [ests // 4] * 4], "layers": 2, "steps": 2, "equal": same},
+            "params_checksum": fnv_one}
 
 
 def cpu_baseline(seconds: float, threads: int = 1):
@@ -408,6 +466,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-reducer", action="store_true")
+    ap.add_argument("--no-bert", action="store_true", help="skip the C4 BERT-base step measurement")
     ap.add_argument("--exchange", default="ipc", choices=["ipc", "allgather"],
                     help="N>1: peer-memory reducer over CUDA IPC, or NCCL all-gather of EST slots")
     args = ap.parse_args()
@@ -468,9 +527,12 @@ def main():
     e2e = args.steps * SAMPLES_PER_STEP / (ms_e2e / 1e3)
     reducer = None
     gemm = None
+    bert = None
     if not args.no_reducer and rank == 0:
         reducer = bench_reducer(flush, peaks)
         gemm = bench_gemm(flush, peaks)
+    if not args.no_bert and rank == 0:
+        bert = bench_bert(peaks)
     clk = clocks.stop()
 
     # Roofline of the step kernel: algorithmic HBM bytes per mini-batch = the 32 rows read
@@ -501,6 +563,8 @@ def main():
         line["reducer"] = reducer
     if gemm is not None:
         line["gemm"] = gemm
+    if bert is not None:
+        line["c4_bert"] = bert
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         v, steps, el, run = cpu_baseline(args.cpu_seconds)
         sys.path.insert(0, str(ROOT / "oracle"))
