@@ -181,22 +181,23 @@ int bt_bert_attn(int32_t backward, const void *qkv_dev, const void *dctx_dev, vo
                  int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed, int64_t step,
                  float p, void *stream);
 /* x = resid + dropout(branch + bias); y = LayerNorm(x) * gamma + beta -> xsum (x), stats (mean, rstd)
- * [T][2], y32, yb (bf16) */
-int bt_bert_ln_fwd(const float *resid_dev, const float *branch_dev, const float *bias_dev, const float *gamma_dev,
+ * [T][2], y32, yb (bf16).  resid fp32 (the residual stream), branch bf16 (a GEMM output). */
+int bt_bert_ln_fwd(const float *resid_dev, const void *branch_dev, const float *bias_dev, const float *gamma_dev,
                    const float *beta_dev, float *xsum_dev, float *stats_dev, float *y32_dev, void *yb_dev, int32_t E,
                    int32_t Te, int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
                    int64_t step, float p, float eps, void *stream);
-/* dx = LayerNorm'(dy1 + dy2) (dy2 may be NULL), dbranch = bf16(dropout'(dx)); part [E][Te/64][3][D]
- * = per-64-row-chunk column sums of (dy*xhat, dy, dropout'(dx)) */
-int bt_bert_ln_bwd(const float *dy1_dev, const float *dy2_dev, const float *xsum_dev, const float *stats_dev,
+/* dx = LayerNorm'(dy1 + dy2) (dy1 bf16 from a GEMM, dy2 fp32 residual-path gradient or NULL),
+ * dbranch = bf16(dropout'(dx)); part [E][Te/64][3][D] = per-64-row-chunk column sums of
+ * (dy*xhat, dy, dropout'(dx)) */
+int bt_bert_ln_bwd(const void *dy1_dev, const float *dy2_dev, const float *xsum_dev, const float *stats_dev,
                    const float *gamma_dev, float *dx_dev, void *dbranch_dev, float *part_dev, int32_t E, int32_t Te,
                    int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
                    int64_t step, float p, void *stream);
 /* chunk partials summed in chunk order -> dgamma/dbeta/dbias of EST e at + e*est_stride */
 int bt_bert_ln_fold(const float *part_dev, int32_t E, int32_t Te, int32_t D, float *dgamma_dev, float *dbeta_dev,
                     float *dbias_dev, int64_t est_stride, void *stream);
-/* loss[e] = sum 0.5*(y-target)^2 / Te, dy = (y-target)/Te (fp32); partials_dev: E*64 floats */
-int bt_bert_mse(const float *y_dev, const float *target_dev, int32_t E, int32_t Te, int32_t D, float *dy_dev,
+/* loss[e] = sum 0.5*(y-target)^2 / Te, dy = bf16((y-target)/Te); partials_dev: E*64 floats */
+int bt_bert_mse(const float *y_dev, const float *target_dev, int32_t E, int32_t Te, int32_t D, void *dy_dev,
                 float *partials_dev, float *loss_dev, void *stream);
 /* bf16 operand copies of fp32 master weights, one launch: wb[i] = bf16(w[i]) [rows][cols],
  * wt[i] = bf16(w[i])^T [cols][rows] */

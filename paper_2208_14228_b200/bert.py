@@ -157,8 +157,9 @@ class BertJob:
                         "Dact": torch.empty(T, F, **bf), "hs2": torch.empty(T, D, **f32),
                         "st2": torch.empty(T, 2, **f32)} for _ in range(L)],
             "x32": torch.empty(T, D, **f32), "r32": [torch.empty(T, D, **f32) for _ in range(2)],
-            "h1_32": torch.empty(T, D, **f32), "br32": torch.empty(T, D, **f32), "ytop": torch.empty(T, D, **bf),
-            "tgt": torch.empty(T, D, **f32), "dbuf": [torch.empty(T, D, **f32) for _ in range(4)],
+            "h1_32": torch.empty(T, D, **f32), "brb": torch.empty(T, D, **bf), "ytop": torch.empty(T, D, **bf),
+            "tgt": torch.empty(T, D, **f32), "dy1": [torch.empty(T, D, **bf) for _ in range(2)],
+            "dres": [torch.empty(T, D, **f32) for _ in range(2)],
             "dbr": torch.empty(T, D, **bf), "dHpre": torch.empty(T, F, **bf), "dctx": torch.empty(T, D, **bf),
             "dqkv": torch.empty(T, 3 * D, **bf), "lnpart": torch.empty(n * (Te // 64) * 3 * D, **f32),
             "colsum": torch.empty(n * 16 * max(3 * D, F), **f32), "msepart": torch.empty(n * 64, **f32),
@@ -195,18 +196,18 @@ class BertJob:
                        bias=self._p(l, "bqkv"))
             _native.check(L.bt_bert_attn(0, w["qkv"].data_ptr(), None, w["ctx"].data_ptr(), n, Te, D, H, base, NL, l,
                                          seed, step, self.pa, s), "attention forward")
-            self._gemm(w["ctx"].data_ptr(), self._wb(l, "Wo"), ws["br32"].data_ptr(), T, D, D)
-            _native.check(L.bt_bert_ln_fwd(x32.data_ptr(), ws["br32"].data_ptr(), self._p(l, "bo"), self._p(l, "g1"),
+            self._gemm(w["ctx"].data_ptr(), self._wb(l, "Wo"), ws["brb"].data_ptr(), T, D, D, out_bf16=True)
+            _native.check(L.bt_bert_ln_fwd(x32.data_ptr(), ws["brb"].data_ptr(), self._p(l, "bo"), self._p(l, "g1"),
                                            self._p(l, "be1"), w["hs1"].data_ptr(), w["st1"].data_ptr(),
                                            ws["h1_32"].data_ptr(), w["h1b"].data_ptr(), n, Te, D, base, NL, l, 0,
                                            seed, step, self.ph, self.eps, s), "layernorm 1")
             _native.check(L.bt_gemm_bf16_ffn(w["h1b"].data_ptr(), self._wb(l, "W1"), w["Hpre"].data_ptr(), T, F, D, 1,
                                              self._p(l, "b1"), None, w["Dact"].data_ptr(), seed, step, base, Te, 0.0,
                                              0, s), "ffn forward GEMM")
-            self._gemm(w["Dact"].data_ptr(), self._wb(l, "W2"), ws["br32"].data_ptr(), T, D, F)
+            self._gemm(w["Dact"].data_ptr(), self._wb(l, "W2"), ws["brb"].data_ptr(), T, D, F, out_bf16=True)
             y32 = ws["r32"][l & 1]
             yb = lay[l + 1]["xb"] if l + 1 < NL else ws["ytop"]
-            _native.check(L.bt_bert_ln_fwd(ws["h1_32"].data_ptr(), ws["br32"].data_ptr(), self._p(l, "b2"),
+            _native.check(L.bt_bert_ln_fwd(ws["h1_32"].data_ptr(), ws["brb"].data_ptr(), self._p(l, "b2"),
                                            self._p(l, "g2"), self._p(l, "be2"), w["hs2"].data_ptr(),
                                            w["st2"].data_ptr(), y32.data_ptr(), yb.data_ptr(), n, Te, D, base, NL, l,
                                            1, seed, step, self.ph, self.eps, s), "layernorm 2")
@@ -215,7 +216,8 @@ class BertJob:
                                                           "hs2", "st2")})
                 capture.update(x32=x32.clone(), y32=y32.clone())
             x32 = y32
-        A, B, Cb, Db = ws["dbuf"]
+        # gradients between GEMMs bf16 (A: into LN2', Db: into LN1'), residual-path gradients fp32 (B, Cb)
+        (A, Db), (B, Cb) = ws["dy1"], ws["dres"]
         _native.check(L.bt_bert_mse(x32.data_ptr(), ws["tgt"].data_ptr(), n, Te, D, A.data_ptr(),
                                     ws["msepart"].data_ptr(), losses[base:].data_ptr(), s))
         if capture is not None:
@@ -236,7 +238,7 @@ class BertJob:
             _native.check(L.bt_gemm_bf16_ffn(ws["dbr"].data_ptr(), self._wt(l, "W2"), ws["dHpre"].data_ptr(), T, F, D,
                                              2, None, w["Hpre"].data_ptr(), None, seed, step, base, Te, 0.0, 0, s),
                           "ffn backward GEMM")
-            self._gemm(ws["dHpre"].data_ptr(), self._wt(l, "W1"), Db.data_ptr(), T, D, F)
+            self._gemm(ws["dHpre"].data_ptr(), self._wt(l, "W1"), Db.data_ptr(), T, D, F, out_bf16=True)
             self._wgrad(ws, n, ws["dbr"].data_ptr(), w["Dact"].data_ptr(), D, F, self._g(base, l, "W2"))
             self._wgrad(ws, n, ws["dHpre"].data_ptr(), w["h1b"].data_ptr(), F, D, self._g(base, l, "W1"))
             _native.check(L.bt_colsum_bf16_strided(ws["dHpre"].data_ptr(), n, Te, F, self._g(base, l, "b1"), self.P,
@@ -254,7 +256,7 @@ class BertJob:
                                          D, H, base, NL, l, seed, step, self.pa, s), "attention backward")
             if capture is not None and l == 0:
                 capture.update(dh=B.clone(), da=ws["dbr"].clone(), dctx=ws["dctx"].clone(), dqkv=ws["dqkv"].clone())
-            self._gemm(ws["dqkv"].data_ptr(), self._wt(l, "Wqkv"), A.data_ptr(), T, D, 3 * D)
+            self._gemm(ws["dqkv"].data_ptr(), self._wt(l, "Wqkv"), A.data_ptr(), T, D, 3 * D, out_bf16=True)
             self._wgrad(ws, n, ws["dqkv"].data_ptr(), w["xb"].data_ptr(), 3 * D, D, self._g(base, l, "Wqkv"))
             _native.check(L.bt_colsum_bf16_strided(ws["dqkv"].data_ptr(), n, Te, 3 * D, self._g(base, l, "bqkv"),
                                                    self.P, ws["colsum"].data_ptr(), s))

@@ -20,6 +20,8 @@
 //                        (same instructions -> same bits) and sums dV, dK over
 //                        query rows in ascending k-steps;
 //   ln_fwd               x = resid + dropout(branch + bias); y = LN(x)
+//                        (residual stream fp32; GEMM outputs and gradients
+//                        between GEMMs bf16, as mixed-precision training keeps them)
 //                        (one warp per row, butterfly sums: fixed order);
 //   ln_bwd               dx = LN'(dy1 + dy2); branch grad = dropout'(dx);
 //                        per-EST gamma/beta/bias column partials over fixed
@@ -390,8 +392,8 @@ __global__ void __launch_bounds__(AT_THREADS) attn_bwd_kernel(const AttnArgs a) 
 
 // ------------------------------------------------------------ LayerNorm
 struct LnArgs {
-  const float* resid;   // fwd: residual input [T][D]      bwd: dy1 [T][D]
-  const float* branch;  // fwd: branch GEMM output (no bias) bwd: dy2 [T][D] or null
+  const float* resid;         // fwd: residual input [T][D] fp32     bwd: dy2 (residual-path grad) fp32 or null
+  const __nv_bfloat16* bin;  // fwd: branch GEMM output (no bias)   bwd: dy1 (branch-path grad), both bf16
   const float* bias;    // fwd: branch bias [D]
   const float* gamma;
   const float* beta;
@@ -431,6 +433,16 @@ __device__ __forceinline__ void ld8(const float* p, float* v) {
   const float4 x = *(const float4*)p, y = *(const float4*)(p + 4);
   v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
 }
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* v) {
+  const uint4 u = *(const uint4*)p;
+  const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __bfloat1622float2(h[k]);
+    v[2 * k] = f.x;
+    v[2 * k + 1] = f.y;
+  }
+}
 __device__ __forceinline__ void st8(float* p, const float* v) {
   *(float4*)p = make_float4(v[0], v[1], v[2], v[3]);
   *(float4*)(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
@@ -460,7 +472,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const LnArgs a) {
     const int col = c * 256 + lane * 8;
     float r[8], b[8], bi[8], m[8];
     ld8(a.resid + (size_t)t * a.D + col, r);
-    ld8(a.branch + (size_t)t * a.D + col, b);
+    ld8(a.bin + (size_t)t * a.D + col, b);
     ld8(a.bias + col, bi);
     ln_mask8(a, sd, tl, col, thr, keep, m);
 #pragma unroll
@@ -519,10 +531,10 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const LnArgs a) {
     for (int c = 0; c < NC; ++c) {
       const int col = c * 256 + lane * 8;
       float x[8], gm[8];
-      ld8(a.resid + t * a.D + col, dy[c]);
-      if (a.branch) {
+      ld8(a.bin + t * a.D + col, dy[c]);
+      if (a.resid) {
         float d2[8];
-        ld8(a.branch + t * a.D + col, d2);
+        ld8(a.resid + t * a.D + col, d2);
 #pragma unroll
         for (int q = 0; q < 8; ++q) dy[c][q] += d2[q];
       }
@@ -615,10 +627,10 @@ __global__ void __launch_bounds__(256) data_kernel(uint64_t seed, int64_t step, 
 }
 
 // loss[e] = sum 0.5*(y - target)^2 / Te over the EST's rows (64 fixed element ranges, fixed
-// tree, ranges summed in order); dy = (y - target) / Te
+// tree, ranges summed in order); dy = bf16((y - target) / Te)
 constexpr int MSE_THREADS = 256, MSE_BLOCKS = 64;
 __global__ void __launch_bounds__(MSE_THREADS) mse_kernel(const float* __restrict__ y, const float* __restrict__ tgt,
-                                                          int Te, int D, float* __restrict__ dy,
+                                                          int Te, int D, __nv_bfloat16* __restrict__ dy,
                                                           float* __restrict__ part) {
   const int e = blockIdx.y, blk = blockIdx.x;
   const int64_t per_est = (int64_t)Te * D;
@@ -629,7 +641,7 @@ __global__ void __launch_bounds__(MSE_THREADS) mse_kernel(const float* __restric
   for (int64_t k = lo + threadIdx.x; k < hi; k += MSE_THREADS) {
     const int64_t i = (int64_t)e * per_est + k;
     const float diff = y[i] - tgt[i];
-    dy[i] = diff * inv;
+    dy[i] = __float2bfloat16_rn(diff * inv);
     acc += 0.5f * diff * diff;
   }
   __shared__ float sm[MSE_THREADS];
@@ -742,16 +754,16 @@ static int ln_launch_nc(int backward, const bert::LnArgs& a, int E, cudaStream_t
   return ok_or_cuda_b();
 }
 
-// forward: resid/branch/bias/gamma/beta -> xsum, stats, y32, yb
-// backward: dy1 (resid), dy2 (branch, may be null), xsum, stats_in, gamma -> dx (y32), dbranch (yb), part
-int bert_ln_launch(int backward, const float* in1, const float* in2, const float* bias, const float* gamma,
+// forward: resid (fp32) / branch (bf16) / bias / gamma / beta -> xsum, stats, y32, yb
+// backward: dy2 (in1, fp32, may be null), dy1 (in2, bf16), xsum, stats_in, gamma -> dx (y32), dbranch (yb), part
+int bert_ln_launch(int backward, const float* in1, const void* in2, const float* bias, const float* gamma,
                    const float* beta, float* xsum, float* stats, float* y32, void* yb, float* part, int E, int Te,
                    int D, int est_base, int L, int layer, int site, uint64_t seed, int64_t step, float p, float eps,
                    cudaStream_t s) {
   if (D % 256 || D > 1024 || Te % bert::LN_CHUNK) return ERR_INPUT;
   bert::LnArgs a{};
   a.resid = in1;
-  a.branch = in2;
+  a.bin = (const __nv_bfloat16*)in2;
   a.bias = bias;
   a.gamma = gamma;
   a.beta = beta;
@@ -796,9 +808,9 @@ int bert_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, i
   return ok_or_cuda_b();
 }
 
-int bert_mse_launch(const float* y, const float* tgt, int E, int Te, int D, float* dy, float* part, float* loss,
+int bert_mse_launch(const float* y, const float* tgt, int E, int Te, int D, void* dy, float* part, float* loss,
                     cudaStream_t s) {
-  bert::mse_kernel<<<dim3(bert::MSE_BLOCKS, E), bert::MSE_THREADS, 0, s>>>(y, tgt, Te, D, dy, part);
+  bert::mse_kernel<<<dim3(bert::MSE_BLOCKS, E), bert::MSE_THREADS, 0, s>>>(y, tgt, Te, D, (__nv_bfloat16*)dy, part);
   bert::mse_final_kernel<<<(E + 127) / 128, 128, 0, s>>>(part, E, Te, loss);
   return ok_or_cuda_b();
 }

@@ -53,7 +53,7 @@ int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, 
 int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out, int n_seq, int Dm, int H,
                      int seqs_per_est, int est_base, int L, int layer, uint64_t seed, int64_t step, float p,
                      cudaStream_t s);
-int bert_ln_launch(int backward, const float* in1, const float* in2, const float* bias, const float* gamma,
+int bert_ln_launch(int backward, const float* in1, const void* in2, const float* bias, const float* gamma,
                    const float* beta, float* xsum, float* stats, float* y32, void* yb, float* part, int E, int Te,
                    int D, int est_base, int L, int layer, int site, uint64_t seed, int64_t step, float p, float eps,
                    cudaStream_t s);
@@ -61,7 +61,7 @@ int bert_ln_fold_launch(const float* part, int E, int Te, int D, float* dg, floa
                         cudaStream_t s);
 int bert_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, float* X32, void* Xb,
                      float* target, cudaStream_t s);
-int bert_mse_launch(const float* y, const float* tgt, int E, int Te, int D, float* dy, float* part, float* loss,
+int bert_mse_launch(const float* y, const float* tgt, int E, int Te, int D, void* dy, float* part, float* loss,
                     cudaStream_t s);
 int bert_cast_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* R, const int* C, int n,
                              cudaStream_t s);
@@ -600,7 +600,7 @@ int bt_bert_attn(int32_t backward, const void* qkv_dev, const void* dctx_dev, vo
                                    layers, layer, seed, step, p, STREAM(stream)),
               "bt_bert_attn");
 }
-int bt_bert_ln_fwd(const float* resid_dev, const float* branch_dev, const float* bias_dev, const float* gamma_dev,
+int bt_bert_ln_fwd(const float* resid_dev, const void* branch_dev, const float* bias_dev, const float* gamma_dev,
                    const float* beta_dev, float* xsum_dev, float* stats_dev, float* y32_dev, void* yb_dev, int32_t E,
                    int32_t Te, int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
                    int64_t step, float p, float eps, void* stream) {
@@ -614,7 +614,7 @@ int bt_bert_ln_fwd(const float* resid_dev, const float* branch_dev, const float*
                                  STREAM(stream)),
               "bt_bert_ln_fwd");
 }
-int bt_bert_ln_bwd(const float* dy1_dev, const float* dy2_dev, const float* xsum_dev, const float* stats_dev,
+int bt_bert_ln_bwd(const void* dy1_dev, const float* dy2_dev, const float* xsum_dev, const float* stats_dev,
                    const float* gamma_dev, float* dx_dev, void* dbranch_dev, float* part_dev, int32_t E, int32_t Te,
                    int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
                    int64_t step, float p, void* stream) {
@@ -622,7 +622,7 @@ int bt_bert_ln_bwd(const float* dy1_dev, const float* dy2_dev, const float* xsum
   if (!dy1_dev || !xsum_dev || !stats_dev || !gamma_dev || !dx_dev || !dbranch_dev || !part_dev)
     return fail(bt::ERR_INPUT, "null pointer");
   if (!(p >= 0.f && p < 1.f) || (site != 0 && site != 1)) return fail(bt::ERR_CONFIG, "bad dropout / site");
-  return done(bt::bert_ln_launch(1, dy1_dev, dy2_dev, nullptr, gamma_dev, nullptr, (float*)xsum_dev,
+  return done(bt::bert_ln_launch(1, dy2_dev, dy1_dev, nullptr, gamma_dev, nullptr, (float*)xsum_dev,
                                  (float*)stats_dev, dx_dev, dbranch_dev, part_dev, E, Te, D, est_base, layers, layer,
                                  site, seed, step, p, 0.f, STREAM(stream)),
               "bt_bert_ln_bwd");
@@ -635,7 +635,7 @@ int bt_bert_ln_fold(const float* part_dev, int32_t E, int32_t Te, int32_t D, flo
                                       STREAM(stream)),
               "bt_bert_ln_fold");
 }
-int bt_bert_mse(const float* y_dev, const float* target_dev, int32_t E, int32_t Te, int32_t D, float* dy_dev,
+int bt_bert_mse(const float* y_dev, const float* target_dev, int32_t E, int32_t Te, int32_t D, void* dy_dev,
                 float* partials_dev, float* loss_dev, void* stream) {
   if (int st = bert_shape(E, Te, D)) return st;
   if (!y_dev || !target_dev || !dy_dev || !partials_dev || !loss_dev) return fail(bt::ERR_INPUT, "null pointer");

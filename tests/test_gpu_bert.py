@@ -8,7 +8,8 @@
   gradient against a float64 restatement fed with the captured bf16 inputs of
   that stage, with the same bf16 rounding points and the same counter-keyed
   dropout masks (regenerated here from splitmix64).  Tolerances, stated:
-  fp32 outputs rel. Frobenius error <= 1e-4; bf16 outputs: <= 1% of elements
+  fp32 outputs rel. Frobenius error <= 1e-4 (2e-3 where a bf16 GEMM output
+  feeds them: a rounding flip there moves one input by one bf16 ulp); bf16 outputs: <= 1% of elements
   differ (one bf16 ulp, fp32-vs-fp64 accumulation) and rel. error <= 5e-3;
   per-EST gradients rel. Frobenius error <= 5e-3.
 """
@@ -184,8 +185,8 @@ def test_layer0_stages_match_float64_restatement(bert):
     _close_bf16(cap["ctx"], ctx_ref, "ctx")
     ctx = _d(cap["ctx"])
     hm1 = hidden_scale(0)
-    hs1_ref = x32 + (ctx @ _bf(W["Wo"]).T + W["bo"]) * hm1
-    _close(cap["hs1"], hs1_ref, "ln1 input")
+    hs1_ref = x32 + (_bf(ctx @ _bf(W["Wo"]).T) + W["bo"]) * hm1  # branch GEMM output rounded to bf16
+    _close(cap["hs1"], hs1_ref, "ln1 input", rel=2e-3)
     hs1 = _d(cap["hs1"])
     h1, mean1, rstd1 = _ln(hs1, W["g1"], W["be1"], eps)
     _close(cap["st1"][:, 0], mean1, "ln1 mean", rel=1e-5)
@@ -196,8 +197,8 @@ def test_layer0_stages_match_float64_restatement(bert):
     _close_bf16(cap["Hpre"], hpre, "ffn pre-activation")
     _close_bf16(cap["Dact"], 0.5 * hpre * (1 + torch.erf(hpre / math.sqrt(2))), "gelu")
     hm2 = hidden_scale(1)
-    hs2_ref = h1 + (_d(cap["Dact"]) @ _bf(W["W2"]).T + W["b2"]) * hm2
-    _close(cap["hs2"], hs2_ref, "ln2 input")
+    hs2_ref = h1 + (_bf(_d(cap["Dact"]) @ _bf(W["W2"]).T) + W["b2"]) * hm2
+    _close(cap["hs2"], hs2_ref, "ln2 input", rel=2e-3)
     # ---- loss head
     ytop, tgt = _d(cap["ytop"]), _d(cap["tgt"])
     diff = ytop - tgt
@@ -216,7 +217,7 @@ def test_layer0_stages_match_float64_restatement(bert):
     gelu_g = 0.5 * (1 + torch.erf(hp / math.sqrt(2))) + hp * torch.exp(-0.5 * hp ** 2) / math.sqrt(2 * math.pi)
     _close_bf16(cap["dHpre"], (do @ _bf(W["W2"])) * gelu_g, "dHpre")
     dHpre = _d(cap["dHpre"])
-    _close(cap["dh1"], dHpre @ _bf(W["W1"]), "dh1")
+    _close_bf16(cap["dh1"], dHpre @ _bf(W["W1"]), "dh1")
     dyl1 = _d(cap["dh1"]) + _d(cap["dg"])
     dh_ref, xh1 = _ln_bwd(dyl1, hs1, W["g1"], eps)
     _close(cap["dh"], dh_ref, "ln1 backward")
@@ -231,7 +232,7 @@ def test_layer0_stages_match_float64_restatement(bert):
     dqkv_ref = torch.stack([dq_ref, dk_ref, dv_ref]).permute(1, 3, 0, 2, 4).reshape(T, 3 * D)
     _close_bf16(cap["dqkv"], dqkv_ref, "attention backward", frac=2e-2, rel=1e-2)
     dqkv = _d(cap["dqkv"])
-    _close(cap["dx"], dqkv @ _bf(W["Wqkv"]), "dx")
+    _close_bf16(cap["dx"], dqkv @ _bf(W["Wqkv"]), "dx")
     # ---- per-EST gradients of layer 0
     g = cap["grads"]
     for e in range(E):
