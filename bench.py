@@ -374,6 +374,28 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
             split[key] = split.get(key, 0.0) + ev.device_time_total / 1e3
     fnv_one = job.params.view(torch.int32).sum().item()
     flops = job.gemm_flops_per_step()
+    # the dominant kernel, per launch: the FFN forward GEMM (T x 3072 x 768, bias + GELU epilogue), timed
+    # alone on its stream with CUDA events (inputs: layer 0's activations of the last step)
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream as cur_stream
+
+    w, L = job._workspace(ests)["layers"][0], _native.lib()
+    T, D, F = ests * job.Te, job.D, job.F
+
+    def ffn_gemm():
+        _native.check(L.bt_gemm_bf16_ffn(w["h1b"].data_ptr(), job._wb(0, "W1"), w["Hpre"].data_ptr(), T, F, D, 1,
+                                         job._p(0, "b1"), None, w["Dact"].data_ptr(), 42, 0, 0, job.Te, 0.0, 0,
+                                         cur_stream()))
+    for _ in range(3):
+        ffn_gemm()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(s)
+    for _ in range(20):
+        ffn_gemm()
+    g1.record(s)
+    g1.synchronize()
+    ffn_ms = g0.elapsed_time(g1) / 20
+    ffn_tf = 2.0 * T * F * D / ffn_ms / 1e9
     del job
     torch.cuda.empty_cache()
     a, b = BertJob(ests=ests, layers=2), BertJob(ests=ests, layers=2)
@@ -389,12 +411,14 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
                         "hidden + attention), 32 ESTs x 8 sequences, MSE head, momentum SGD (BASELINE.json configs[3])",
             "samples_per_s": round(seqs / (ms / 1e3), 1), "unit": "sequences/s", "ms_per_step": round(ms, 3),
             "tokens_per_s": round(seqs * 128 / (ms / 1e3), 1), "loss": round(losses.mean().item(), 5),
-            "roofline": {"kernel": "gemm_bf16_tn_pair_kernel (bt_gemm.cu, all dense products of the step)",
-                         "bound": "tensor", "achieved": round(flops / gemm_ms / 1e9, 1) if gemm_ms else None,
-                         "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                         "frac": round(flops / gemm_ms / 1e9 / peaks["bf16_tflops"], 4) if gemm_ms else None,
+            "roofline": {"kernel": "gemm_bf16_tn_pair_kernel<5,bf16> FFN forward (bt_gemm.cu: 32768x3072x768, "
+                                   "bias+GELU epilogue, TMA-store), one launch",
+                         "bound": "tensor", "achieved": round(ffn_tf, 1), "peak": peaks["bf16_tflops"],
+                         "unit": "TFLOP/s", "frac": round(ffn_tf / peaks["bf16_tflops"], 4),
+                         "ms": round(ffn_ms, 4), "traffic": ncu_traffic("bert_ffn_gemm"),
+                         "all_step_gemms_tflops": round(flops / gemm_ms / 1e9, 1) if gemm_ms else None,
                          "step_level_tflops": round(flops / ms / 1e9, 1), "dense_flops_per_step": flops,
-                         "traffic": None},
+                         "note": "L2 not flushed between the 20 back-to-back launches (55 MB of operands)"},
             "kernel_ms_per_step": {k: round(v, 3) for k, v in sorted(split.items(), key=lambda kv: -kv[1])},
             "bit_identical_groupings": {"groups": [[ests], [ests // 4] * 4], "layers": 2, "steps": 2, "equal": same},
             "params_checksum": fnv_one}

@@ -37,9 +37,19 @@ __device__ __forceinline__ void drop_scale2(uint64_t stream, int64_t step, int T
   *m1 = (uint32_t)(r >> 32) < t ? 0.f : keep;
 }
 
-__device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+// GELU in its tanh form -- the activation of the original BERT code:
+//   gelu(x) = 0.5 x (1 + tanh(c (x + 0.044715 x^3))),  c = sqrt(2/pi).
+// tanh(u) = 1 - 2 / (1 + 2^(2u log2 e)) with the MUFU exp2 / fast reciprocal: absolute error ~1e-7,
+// which is what 1 + tanh needs (no erf polynomial in the GEMM epilogue).
+__device__ __forceinline__ float tanh_fast(float u) {
+  return 1.f - __fdividef(2.f, 1.f + exp2f(2.8853900817779268f * u));
+}
+__device__ __forceinline__ float gelu(float x) {
+  return 0.5f * x * (1.f + tanh_fast(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+}
 __device__ __forceinline__ float gelu_grad(float x) {
-  return 0.5f * (1.f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * expf(-0.5f * x * x);
+  const float t = tanh_fast(0.7978845608028654f * (x + 0.044715f * x * x * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * 0.7978845608028654f * (1.f + 0.134145f * x * x);
 }
 
 }  // namespace ffn

@@ -1,6 +1,6 @@
 """Per-EST transformer FFN training step -- the C4 model-stack slice.
 
-A BERT-base FFN sublayer (d_model 768 -> d_ff 3072 -> 768, erf-GELU, dropout)
+A BERT-base FFN sublayer (d_model 768 -> d_ff 3072 -> 768, GELU (tanh form, as BERT), dropout)
 trained data-parallel by E virtual workers (ESTs), EasyScale-style:
 
 * every EST's randomness (its synthetic tokens and targets, its dropout masks)

@@ -22,6 +22,18 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
+C_GELU = math.sqrt(2 / math.pi)
+
+
+def _gelu(x):
+    """GELU, tanh form (the original BERT code's activation)"""
+    return 0.5 * x * (1 + torch.tanh(C_GELU * (x + 0.044715 * x ** 3)))
+
+
+def _gelu_grad(x):
+    t = torch.tanh(C_GELU * (x + 0.044715 * x ** 3))
+    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * C_GELU * (1 + 3 * 0.044715 * x * x)
+
 SMALL = dict(ests=4, seqs=2, layers=2, d_model=256, heads=4, d_ff=512, seed=3, lr=0.01, momentum=0.9,
              p_hidden=0.1, p_attn=0.1)
 
@@ -195,7 +207,7 @@ def test_layer0_stages_match_float64_restatement(bert):
     h1b = _d(cap["h1b"])
     hpre = h1b @ _bf(W["W1"]).T + W["b1"]
     _close_bf16(cap["Hpre"], hpre, "ffn pre-activation")
-    _close_bf16(cap["Dact"], 0.5 * hpre * (1 + torch.erf(hpre / math.sqrt(2))), "gelu")
+    _close_bf16(cap["Dact"], _gelu(hpre), "gelu")
     hm2 = hidden_scale(1)
     hs2_ref = h1 + (_bf(_d(cap["Dact"]) @ _bf(W["W2"]).T) + W["b2"]) * hm2
     _close(cap["hs2"], hs2_ref, "ln2 input", rel=2e-3)
@@ -214,7 +226,7 @@ def test_layer0_stages_match_float64_restatement(bert):
     _close_bf16(cap["do"], do_ref, "ffn-out dropout'")
     do = _d(cap["do"])
     hp = _d(cap["Hpre"])
-    gelu_g = 0.5 * (1 + torch.erf(hp / math.sqrt(2))) + hp * torch.exp(-0.5 * hp ** 2) / math.sqrt(2 * math.pi)
+    gelu_g = _gelu_grad(hp)
     _close_bf16(cap["dHpre"], (do @ _bf(W["W2"])) * gelu_g, "dHpre")
     dHpre = _d(cap["dHpre"])
     _close_bf16(cap["dh1"], dHpre @ _bf(W["W1"]), "dh1")

@@ -2,6 +2,7 @@
 
     python tools/bert_bench.py [ests] [groups] [layers] [seqs]
 """
+import os
 import sys
 from pathlib import Path
 
@@ -16,11 +17,11 @@ NL = int(sys.argv[3]) if len(sys.argv) > 3 else 12
 S = int(sys.argv[4]) if len(sys.argv) > 4 else 8
 job = BertJob(ests=E, seqs=S, layers=NL)
 groups = [E // G] * G
-for _ in range(3):
+W, K = int(os.environ.get("BT_BENCH_WARMUP", "3")), int(os.environ.get("BT_BENCH_STEPS", "5"))
+for _ in range(W):
     job.step(groups)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-K = 5
 e0.record()
 for _ in range(K):
     losses = job.step(groups)

@@ -15,8 +15,8 @@ PROF = ROOT / "profiles"
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 
 
-def launches():
-    path = OUT / "launches.csv"
+def launches(src="launches.csv", dst="launches"):
+    path = OUT / src
     if not path.exists():
         return None
     rows = [r for r in csv.reader(open(path)) if r]
@@ -41,7 +41,7 @@ def launches():
     for name, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         share = "   setup" if any(x in name for x in setup) else f"{t / step_tot * 100:7.1f}%"
         lines.append(f"{name[:70]:70s} {n:8d} {t / 1e3:12.1f} {t / tot * 100:6.1f}% {share}")
-    (PROF / f"{tag}_launches.txt").write_text("\n".join(lines) + "\n")
+    (PROF / f"{tag}_{dst}.txt").write_text("\n".join(lines) + "\n")
     return agg
 
 
@@ -90,11 +90,17 @@ def summarize(rep, name, extra=()):
 
 PROF.mkdir(exist_ok=True)
 launches()
+launches("bert_launches.csv", "bert_launches")
+t_bg = summarize(OUT / f"prof_bert_gemm_{tag}.ncu-rep", "ncu_bert_gemm", extra=("pipe_tensor", "pipe_tc", "tmem", "utc"))
+t_ba = summarize(OUT / f"prof_bert_attn_{tag}.ncu-rep", "ncu_bert_attn_bwd", extra=("pipe_tensor", "pipe_tc"))
+t_bl = summarize(OUT / f"prof_bert_ln_{tag}.ncu-rep", "ncu_bert_ln_bwd")
 t_mlp = summarize(OUT / f"prof_mlp_{tag}.ncu-rep", "ncu_mlp_step")
 t_red = summarize(OUT / f"prof_reduce_{tag}.ncu-rep", "ncu_reducer")
 t_gemm = summarize(OUT / f"prof_gemm_{tag}.ncu-rep", "ncu_gemm", extra=("pipe_tensor", "pipe_tc", "tmem", "utc"))
 traffic = {"mlp_step_kernel": t_mlp[0] if t_mlp else None, "reduce_fast_kernel": t_red[0] if t_red else None,
            "gemm_bf16_tn_kernel": t_gemm[0] if t_gemm else None,
+           "bert_ffn_gemm": t_bg[0] if t_bg else None, "attn_bwd_kernel": t_ba[0] if t_ba else None,
+           "ln_bwd_kernel": t_bl[0] if t_bl else None,
            "source": f"profiles/{tag}_ncu_*.txt (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"}
 (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
 print(json.dumps(traffic))
