@@ -204,6 +204,44 @@ int bt_bert_mse(const float *y_dev, const float *target_dev, int32_t E, int32_t 
 int bt_cast_weights_bf16(const float *const *w_dev, void *const *wb_dev, void *const *wt_dev, const int32_t *rows,
                          const int32_t *cols, int32_t n, void *stream);
 
+/* ---------------- per-EST ResNet-18 step with BatchNorm (C3, no reference) ----
+ * NHWC bf16 activations; the images of local EST e are [e*B, (e+1)*B), its rows one
+ * contiguous block.  Each EST normalises with its own micro-batch statistics and keeps
+ * its own running statistics (slot [E] x run_stride); data are keyed by (seed, EST rank,
+ * the EST's sampler cursor slot).  Convolutions are bt_gemm_bf16_ex products of
+ * im2col matrices (forward, and the transposed convolution for dX as a gather).
+ *                                                    analogue of model.py:94-104, 107-196 */
+int bt_cnn_data(uint64_t seed, const int64_t *cursor_dev, int32_t est_base, int32_t E, int32_t B, void *x_dev,
+                int32_t *labels_dev, void *stream);
+/* col[(n,ho,wo)][(kh,kw,c)]: forward source (ho*s-p+kh, wo*s-p+kw); transposed = 1: source
+ * ((ho+p-kh)/s, (wo+p-kw)/s) when exact (the dX gather of a stride-s convolution) */
+int bt_cnn_im2col(const void *src_dev, void *col_dev, int32_t N, int32_t Hs, int32_t Ws, int32_t C, int32_t Ho,
+                  int32_t Wo, int32_t KH, int32_t KW, int32_t stride, int32_t pad, int32_t transposed, void *stream);
+/* per-EST column statistics over fixed 256-row chunks folded in order; mode 0: mean; mode 1: rstd +
+ * running-statistics update of each EST's slot; mode 2: backward sums (g, g*xhat) -> dbeta, dgamma
+ * of each EST's gradient slot (g = dy * [y > 0]).  part_dev: E * ceil(R/256) * 2 * C floats */
+int bt_cnn_bn_stats(int32_t mode, const void *z_dev, const void *dy_dev, const void *y_dev, float *mean_dev,
+                    float *rstd_dev, float *sg_dev, float *sgx_dev, float *part_dev, float *run_mean_dev,
+                    float *run_var_dev, int64_t run_stride, float *dgamma_dev, float *dbeta_dev, int64_t grad_stride,
+                    int32_t E, int32_t R, int32_t C, float eps, void *stream);
+/* y = [relu](gamma (z - mean) rstd + beta [+ res]) */
+int bt_cnn_bn_apply(const void *z_dev, const void *res_dev, const float *mean_dev, const float *rstd_dev,
+                    const float *gamma_dev, const float *beta_dev, int32_t E, int32_t R, int32_t C, int32_t relu,
+                    void *y_dev, void *stream);
+/* dz = gamma rstd (g - S_g/R - xhat S_gx/R), g = dy [y > 0] */
+int bt_cnn_bn_bwd(const void *z_dev, const void *dy_dev, const void *y_dev, const float *mean_dev,
+                  const float *rstd_dev, const float *sg_dev, const float *sgx_dev, const float *gamma_dev, int32_t E,
+                  int32_t R, int32_t C, void *dz_dev, void *stream);
+/* out = a + (y ? b [y > 0] : b), n elements (bf16) */
+int bt_cnn_add(const void *a_dev, const void *b_dev, const void *y_dev, int64_t n, void *out_dev, void *stream);
+/* avgpool 4x4 + fc 512->10 + softmax cross-entropy, forward and backward, one block per EST */
+int bt_cnn_head(const void *x_dev, const int32_t *labels_dev, const float *w_dev, const float *b_dev, int32_t E,
+                int32_t B, float *dw_dev, float *db_dev, int64_t grad_stride, float *loss_dev, void *dx_dev,
+                void *stream);
+/* master conv weights [Co][taps][Ci] fp32 -> wb [Co][taps*Ci] and wt [Ci][taps][Co] (bf16), one launch */
+int bt_cnn_conv_weights(const float *const *w_dev, void *const *wb_dev, void *const *wt_dev, const int32_t *co,
+                        const int32_t *taps, const int32_t *ci, int32_t n, void *stream);
+
 /* ---------------- L3 data ------------------------------------------------- */
 /* make_dataset(seed, n, dim): [n][dim+1], x then y                       sampling.py:24-35 */
 int bt_make_dataset(uint64_t seed, int64_t n, int32_t dim, double *out_dev, void *stream);

@@ -110,6 +110,16 @@ EXPORTS = {
                                  _u64, _i64, C.c_float, _vp]),
     "bt_bert_ln_fold": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp]),
     "bt_bert_mse": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "bt_cnn_data": (C.c_int, [_u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "bt_cnn_im2col": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp]),
+    "bt_cnn_bn_stats": (C.c_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64,
+                                  _i32, _i32, _i32, C.c_float, _vp]),
+    "bt_cnn_bn_apply": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "bt_cnn_bn_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
+    "bt_cnn_add": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
+    "bt_cnn_head": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "bt_cnn_conv_weights": (C.c_int, [C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i32p, _i32p, _i32p, _i32,
+                                      _vp]),
     "bt_cast_weights_bf16": (C.c_int, [C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i32p, _i32p, _i32, _vp]),
     "bt_sgd_step_f64": (C.c_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp, _vp, _vp]),
     "bt_make_dataset": (C.c_int, [_u64, _i64, _i32, _vp, _vp]),

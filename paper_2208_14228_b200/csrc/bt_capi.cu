@@ -65,6 +65,24 @@ int bert_mse_launch(const float* y, const float* tgt, int E, int Te, int D, void
                     cudaStream_t s);
 int bert_cast_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* R, const int* C, int n,
                              cudaStream_t s);
+int cnn_data_launch(uint64_t seed, const int64_t* cursor, int est_base, int E, int B, void* x, int32_t* labels,
+                    cudaStream_t s);
+int cnn_im2col_launch(const void* src, void* col, int N, int Hs, int Ws, int C, int Ho, int Wo, int KH, int KW,
+                      int stride, int pad, int transposed, cudaStream_t s);
+int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, float* mean, float* rstd,
+                        float* sg, float* sgx, float* part, float* run_mean, float* run_var, int64_t run_stride,
+                        float* dgamma, float* dbeta, int64_t grad_stride, int E, int R, int C, float eps,
+                        cudaStream_t s);
+int cnn_bn_apply_launch(const void* z, const void* res, const float* mean, const float* rstd, const float* gamma,
+                        const float* beta, int E, int R, int C, int relu, void* y, cudaStream_t s);
+int cnn_bn_bwd_launch(const void* z, const void* dy, const void* y, const float* mean, const float* rstd,
+                      const float* sg, const float* sgx, const float* gamma, int E, int R, int C, void* dz,
+                      cudaStream_t s);
+int cnn_add_launch(const void* a, const void* b, const void* y, int64_t n, void* out, cudaStream_t s);
+int cnn_head_launch(const void* x, const int32_t* labels, const float* W, const float* bias, int E, int B, float* dW,
+                    float* db, int64_t grad_stride, float* loss, void* dx, cudaStream_t s);
+int cnn_conv_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* Co, const int* T,
+                            const int* Ci, int n, cudaStream_t s);
 }  // namespace bt
 
 static thread_local char g_err[512];
@@ -296,9 +314,9 @@ int bt_gemm_bf16_ex(const void* a_dev, const void* b_dev, void* c_dev, int32_t b
                     int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype, const float* bias_dev,
                     int32_t mn_major, int32_t grid, void* stream) {
   if (!a_dev || !b_dev || !c_dev) return fail(bt::ERR_INPUT, "null pointer");
-  if (batch < 1 || M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 128 || K % 64)
-    return fail(bt::ERR_INPUT, "gemm shape %dx%dx%d x%d: need M %% 128 == 0, N %% 128 == 0, K %% 64 == 0", M, N, K,
-                batch);
+  if (batch < 1 || M <= 0 || N <= 0 || K <= 0 || N % 8 || (mn_major ? M % 8 : K % 8))
+    return fail(bt::ERR_INPUT, "gemm shape %dx%dx%d x%d: need N %% 8 == 0 and %s %% 8 == 0 (16-byte TMA strides)", M,
+                N, K, batch, mn_major ? "M" : "K");
   if (((uintptr_t)a_dev | (uintptr_t)b_dev | (uintptr_t)c_dev | (uintptr_t)bias_dev) & 15)
     return fail(bt::ERR_INPUT, "gemm operands must be 16-byte aligned");
   if (batch == 1) {
@@ -654,6 +672,71 @@ int bt_cast_weights_bf16(const float* const* w_dev, void* const* wb_dev, void* c
   if (n < 1 || n > 64) return fail(bt::ERR_INPUT, "cast table of %d matrices (1..64)", n);
   return done(bt::bert_cast_weights_launch(w_dev, wb_dev, wt_dev, rows, cols, n, STREAM(stream)),
               "bt_cast_weights_bf16");
+}
+
+// ------------------------------------ per-EST ResNet-18 step with BatchNorm (C3)
+int bt_cnn_data(uint64_t seed, const int64_t* cursor_dev, int32_t est_base, int32_t E, int32_t B, void* x_dev,
+                int32_t* labels_dev, void* stream) {
+  if (E < 1 || B < 1 || !cursor_dev || !x_dev || !labels_dev) return fail(bt::ERR_INPUT, "bt_cnn_data arguments");
+  return done(bt::cnn_data_launch(seed, cursor_dev, est_base, E, B, x_dev, labels_dev, STREAM(stream)), "bt_cnn_data");
+}
+int bt_cnn_im2col(const void* src_dev, void* col_dev, int32_t N, int32_t Hs, int32_t Ws, int32_t C, int32_t Ho,
+                  int32_t Wo, int32_t KH, int32_t KW, int32_t stride, int32_t pad, int32_t transposed, void* stream) {
+  if (!src_dev || !col_dev || N < 1 || C % 8 || C < 8 || stride < 1 || KH < 1 || KW < 1 || Ho < 1 || Wo < 1)
+    return fail(bt::ERR_INPUT, "bt_cnn_im2col shape (C %% 8 == 0)");
+  return done(bt::cnn_im2col_launch(src_dev, col_dev, N, Hs, Ws, C, Ho, Wo, KH, KW, stride, pad, transposed,
+                                    STREAM(stream)),
+              "bt_cnn_im2col");
+}
+int bt_cnn_bn_stats(int32_t mode, const void* z_dev, const void* dy_dev, const void* y_dev, float* mean_dev,
+                    float* rstd_dev, float* sg_dev, float* sgx_dev, float* part_dev, float* run_mean_dev,
+                    float* run_var_dev, int64_t run_stride, float* dgamma_dev, float* dbeta_dev, int64_t grad_stride,
+                    int32_t E, int32_t R, int32_t C, float eps, void* stream) {
+  if (mode < 0 || mode > 2 || E < 1 || R < 2 || C % 8 || C > 2048 || !z_dev || !mean_dev || !part_dev)
+    return fail(bt::ERR_INPUT, "bt_cnn_bn_stats arguments");
+  if (mode == 1 && (!rstd_dev || !run_mean_dev || !run_var_dev)) return fail(bt::ERR_INPUT, "mode 1 needs rstd/run");
+  if (mode == 2 && (!dy_dev || !y_dev || !rstd_dev || !sg_dev || !sgx_dev || !dgamma_dev || !dbeta_dev))
+    return fail(bt::ERR_INPUT, "mode 2 needs dy, y, rstd, sums and gradient slots");
+  return done(bt::cnn_bn_stats_launch(mode, z_dev, dy_dev, y_dev, mean_dev, rstd_dev, sg_dev, sgx_dev, part_dev,
+                                      run_mean_dev, run_var_dev, run_stride, dgamma_dev, dbeta_dev, grad_stride, E, R,
+                                      C, eps, STREAM(stream)),
+              "bt_cnn_bn_stats");
+}
+int bt_cnn_bn_apply(const void* z_dev, const void* res_dev, const float* mean_dev, const float* rstd_dev,
+                    const float* gamma_dev, const float* beta_dev, int32_t E, int32_t R, int32_t C, int32_t relu,
+                    void* y_dev, void* stream) {
+  if (E < 1 || R < 1 || C % 8 || !z_dev || !y_dev) return fail(bt::ERR_INPUT, "bt_cnn_bn_apply arguments");
+  return done(bt::cnn_bn_apply_launch(z_dev, res_dev, mean_dev, rstd_dev, gamma_dev, beta_dev, E, R, C, relu, y_dev,
+                                      STREAM(stream)),
+              "bt_cnn_bn_apply");
+}
+int bt_cnn_bn_bwd(const void* z_dev, const void* dy_dev, const void* y_dev, const float* mean_dev,
+                  const float* rstd_dev, const float* sg_dev, const float* sgx_dev, const float* gamma_dev, int32_t E,
+                  int32_t R, int32_t C, void* dz_dev, void* stream) {
+  if (E < 1 || R < 1 || C % 8 || !z_dev || !dy_dev || !y_dev || !dz_dev) return fail(bt::ERR_INPUT, "bt_cnn_bn_bwd");
+  return done(bt::cnn_bn_bwd_launch(z_dev, dy_dev, y_dev, mean_dev, rstd_dev, sg_dev, sgx_dev, gamma_dev, E, R, C,
+                                    dz_dev, STREAM(stream)),
+              "bt_cnn_bn_bwd");
+}
+int bt_cnn_add(const void* a_dev, const void* b_dev, const void* y_dev, int64_t n, void* out_dev, void* stream) {
+  if (!a_dev || !b_dev || !out_dev || n % 8) return fail(bt::ERR_INPUT, "bt_cnn_add arguments");
+  return done(bt::cnn_add_launch(a_dev, b_dev, y_dev, n, out_dev, STREAM(stream)), "bt_cnn_add");
+}
+int bt_cnn_head(const void* x_dev, const int32_t* labels_dev, const float* w_dev, const float* b_dev, int32_t E,
+                int32_t B, float* dw_dev, float* db_dev, int64_t grad_stride, float* loss_dev, void* dx_dev,
+                void* stream) {
+  if (E < 1 || B < 1 || B > 96 || !x_dev || !labels_dev || !w_dev || !b_dev || !dw_dev || !db_dev || !loss_dev ||
+      !dx_dev)
+    return fail(bt::ERR_INPUT, "bt_cnn_head arguments (B <= 96)");
+  return done(bt::cnn_head_launch(x_dev, labels_dev, w_dev, b_dev, E, B, dw_dev, db_dev, grad_stride, loss_dev, dx_dev,
+                                  STREAM(stream)),
+              "bt_cnn_head");
+}
+int bt_cnn_conv_weights(const float* const* w_dev, void* const* wb_dev, void* const* wt_dev, const int32_t* co,
+                        const int32_t* taps, const int32_t* ci, int32_t n, void* stream) {
+  if (n < 1 || n > 32) return fail(bt::ERR_INPUT, "conv weight table of %d (1..32)", n);
+  return done(bt::cnn_conv_weights_launch(w_dev, wb_dev, wt_dev, co, taps, ci, n, STREAM(stream)),
+              "bt_cnn_conv_weights");
 }
 
 }  // extern "C"

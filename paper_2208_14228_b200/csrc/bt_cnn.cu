@@ -1,0 +1,510 @@
+// bt_cnn.cu -- the kernels between the GEMMs of a per-EST ResNet-18 step with
+// BatchNorm (C3, BASELINE.json configs[2]).  No reference
+// implementation exists for this model.  The EasyScale contract:
+// every EST normalises with the statistics of its OWN micro-batch and keeps its
+// OWN BatchNorm running statistics (an HBM slot indexed by EST rank, moved
+// with the EST on an elastic rescale), its data are keyed by (seed, EST rank,
+// EST sampler cursor), and every reduction has a shape fixed by the EST's data
+// -- so the bits never depend on which ESTs share a launch or a GPU.
+//
+// Layout: NHWC bf16 activations; the images of local EST e are n in
+// [e*B, (e+1)*B), so its rows (n, h, w) are one contiguous block of B*H*W rows.
+// Convolutions are GEMMs on the deterministic tcgen05 kernel (bt_gemm.cu):
+//   forward  z = im2col(x) . W^T        (K = KH*KW*Ci, ordered (kh, kw, ci))
+//   dX       dx = im2colT(dz) . W'^T    (the transposed convolution as a gather:
+//                                        no scatter, no atomics)
+//   dW_e     = dz_e^T im2col(x)_e       (MN-major batched GEMM, one per EST)
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bt_common.cuh"
+
+namespace bt {
+namespace cnn {
+
+constexpr uint64_t TAG_CNN_X = 0x434e'4e5f'5844'4154ull;      // "CNN_XDAT"
+constexpr uint64_t TAG_CNN_LABEL = 0x434e'4e5f'4c41'424cull;  // "CNN_LABL"
+constexpr int CHUNK = 256;  // rows per column-statistics partial (fixed: part of the reduction's shape)
+
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* v) {
+  const uint4 u = *(const uint4*)p;
+  const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __bfloat1622float2(h[k]);
+    v[2 * k] = f.x;
+    v[2 * k + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const float* v) {
+  uint4 u;
+  __nv_bfloat162* h = (__nv_bfloat162*)&u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+  *(uint4*)p = u;
+}
+
+// ---------------------------------------------------------------- data
+// images [E*B][32][32][8] bf16 (channels 3..7 zero), labels [E*B]: image nl of EST e at its sampler
+// cursor c = cursor[e]: pixel draws (TAG_CNN_X, seed, EST) at (c*B + nl)*3072 + (h*32 + w)*3 + ch,
+// label (TAG_CNN_LABEL, seed, EST) draw c*B + nl mod 10
+__global__ void data_kernel(uint64_t seed, const int64_t* __restrict__ cursor, int est_base, int B, int E,
+                            __nv_bfloat16* __restrict__ x, int32_t* __restrict__ labels) {
+  const int64_t n = (int64_t)E * B * 1024;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int img = (int)(i >> 10), pix = (int)(i & 1023);
+    const int e = img / B, nl = img - e * B;
+    const uint64_t c = (uint64_t)cursor[e];
+    const uint64_t sx = derive3(TAG_CNN_X, seed, (uint64_t)(est_base + e));
+    const uint64_t base = ((c * B + nl) * 1024 + pix) * 3;
+    float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) v[ch] = (float)(unit_float(draw_raw(sx, base + ch)) * 2.0 - 1.0);
+    st8(x + i * 8, v);
+    if (pix == 0) {
+      const uint64_t sl = derive3(TAG_CNN_LABEL, seed, (uint64_t)(est_base + e));
+      labels[img] = (int32_t)(draw_raw(sl, c * B + nl) % 10u);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- im2col
+// col[(n, ho, wo)][(kh, kw, c)] (8 channels per thread, 16-byte moves).
+// forward:     source (ho*s - p + kh, wo*s - p + kw) of x [N][Hs][Ws][C]
+// transposed:  (the dX gather of a stride-s convolution) output grid = the forward input grid;
+//              source ((ho + p - kh)/s, (wo + p - kw)/s) of dz [N][Hs][Ws][C] when exact and in range
+struct ColArgs {
+  const __nv_bfloat16* src;
+  __nv_bfloat16* col;
+  int N, Hs, Ws, C, Ho, Wo, KH, KW, s, p, transposed;
+};
+__global__ void __launch_bounds__(256) im2col_kernel(const ColArgs a) {
+  const int cg = a.C / 8, K8 = a.KH * a.KW * cg;
+  const int64_t n = (int64_t)a.N * a.Ho * a.Wo * K8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k8 = (int)(i % K8);
+    const int64_t r = i / K8;
+    const int wo = (int)(r % a.Wo), ho = (int)((r / a.Wo) % a.Ho), img = (int)(r / ((int64_t)a.Wo * a.Ho));
+    const int c8 = k8 % cg, t = k8 / cg, kw = t % a.KW, kh = t / a.KW;
+    int hi, wi;
+    bool ok;
+    if (!a.transposed) {
+      hi = ho * a.s - a.p + kh;
+      wi = wo * a.s - a.p + kw;
+      ok = true;
+    } else {
+      const int hn = ho + a.p - kh, wn = wo + a.p - kw;
+      ok = hn >= 0 && wn >= 0 && hn % a.s == 0 && wn % a.s == 0;
+      hi = hn / a.s;
+      wi = wn / a.s;
+    }
+    ok = ok && hi >= 0 && hi < a.Hs && wi >= 0 && wi < a.Ws;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (ok) v = *(const uint4*)(a.src + (((size_t)img * a.Hs + hi) * a.Ws + wi) * a.C + c8 * 8);
+    *(uint4*)(a.col + r * (size_t)(K8 * 8) + (size_t)k8 * 8) = v;
+  }
+}
+
+// ---------------------------------------------------------------- BatchNorm
+// Column statistics per EST over fixed CHUNK-row chunks: block = (chunk k, local EST e);
+// thread = (row lane, 8-channel group); rows walked in order, lanes combined in lane order.
+//   mode 0: sum z                      mode 1: sum (z - mean)^2
+//   mode 2: sum g, sum g * xhat         (g = dy * [y > 0], xhat = (z - mean) * rstd)
+struct StatArgs {
+  const __nv_bfloat16* z;     // conv output (pre-BN)
+  const __nv_bfloat16* dy;    // mode 2: gradient of the block/ReLU output
+  const __nv_bfloat16* y;     // mode 2: the ReLU output (mask)
+  const float* mean;          // [E][C] (modes 1, 2)
+  const float* rstd;          // [E][C] (mode 2)
+  float* part;                // [E][chunks][2][C]
+  int C, R, mode;             // R = rows per EST
+};
+__global__ void __launch_bounds__(256) stats_kernel(const StatArgs a) {
+  extern __shared__ float st_smem[];  // [lanes][2][C]
+  const int k = blockIdx.x, e = blockIdx.y, chunks = gridDim.x;
+  const int cg = a.C / 8, lanes = 256 / cg;  // C <= 2048
+  const int lane = threadIdx.x / cg, c0 = (threadIdx.x % cg) * 8;
+  float s0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, s1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float m[8], r[8];
+  if (lane < lanes) {
+    if (a.mode >= 1)
+      for (int q = 0; q < 8; ++q) m[q] = a.mean[(size_t)e * a.C + c0 + q];
+    if (a.mode == 2)
+      for (int q = 0; q < 8; ++q) r[q] = a.rstd[(size_t)e * a.C + c0 + q];
+    const int r1 = min(a.R, (k + 1) * CHUNK);
+    for (int row = k * CHUNK + lane; row < r1; row += lanes) {
+      const size_t off = ((size_t)e * a.R + row) * a.C + c0;
+      float zv[8];
+      ld8(a.z + off, zv);
+      if (a.mode == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s0[q] += zv[q];
+      } else if (a.mode == 1) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float d = zv[q] - m[q];
+          s0[q] += d * d;
+        }
+      } else {
+        float dv[8], yv[8];
+        ld8(a.dy + off, dv);
+        ld8(a.y + off, yv);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float g = yv[q] > 0.f ? dv[q] : 0.f;
+          s0[q] += g;
+          s1[q] += g * ((zv[q] - m[q]) * r[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      st_smem[(size_t)(lane * 2 + 0) * a.C + c0 + q] = s0[q];
+      st_smem[(size_t)(lane * 2 + 1) * a.C + c0 + q] = s1[q];
+    }
+  }
+  __syncthreads();
+  float* out = a.part + ((size_t)e * chunks + k) * 2 * a.C;
+  for (int i = threadIdx.x; i < 2 * a.C; i += 256) {
+    float acc = st_smem[i];
+    for (int l = 1; l < lanes; ++l) acc += st_smem[(size_t)l * 2 * a.C + i];
+    out[i] = acc;
+  }
+}
+
+// Fold the chunk partials in chunk order.  mode 0: mean = S/R.  mode 1: var = S/R, rstd, and the
+// EST's running statistics (slot): rm = 0.9 rm + 0.1 mean, rv = 0.9 rv + 0.1 var * R/(R-1).
+// mode 2: (sum g, sum g*xhat) -> out0 / out1 (and dbeta / dgamma into the EST's gradient slot).
+struct FoldArgs {
+  const float* part;
+  float* out0;      // mode 0: mean [E][C]; mode 1: rstd [E][C]; mode 2: sum g [E][C]
+  float* out1;      // mode 2: sum g*xhat [E][C]
+  const float* mean;
+  float* run_mean;  // slot [E] x stride
+  float* run_var;
+  int64_t run_stride;
+  float* dgamma;    // grad slot of EST e at + e*grad_stride
+  float* dbeta;
+  int64_t grad_stride;
+  int C, R, E, chunks, mode;
+  float eps;
+};
+__global__ void fold_kernel(const FoldArgs a) {
+  const int64_t n = (int64_t)a.E * a.C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i / a.C), c = (int)(i - (int64_t)e * a.C);
+    const float* p = a.part + (size_t)e * a.chunks * 2 * a.C + c;
+    float s0 = p[0], s1 = p[a.C];
+    for (int k = 1; k < a.chunks; ++k) {
+      s0 += p[(size_t)k * 2 * a.C];
+      s1 += p[(size_t)k * 2 * a.C + a.C];
+    }
+    if (a.mode == 0) {
+      a.out0[i] = s0 / (float)a.R;
+    } else if (a.mode == 1) {
+      const float var = s0 / (float)a.R;
+      a.out0[i] = 1.f / sqrtf(var + a.eps);
+      float* rm = a.run_mean + (size_t)e * a.run_stride + c;
+      float* rv = a.run_var + (size_t)e * a.run_stride + c;
+      *rm = 0.9f * *rm + 0.1f * a.mean[i];
+      *rv = 0.9f * *rv + 0.1f * (var * ((float)a.R / (float)(a.R - 1)));
+    } else {
+      a.out0[i] = s0;
+      a.out1[i] = s1;
+      a.dbeta[(size_t)e * a.grad_stride + c] = s0;
+      a.dgamma[(size_t)e * a.grad_stride + c] = s1;
+    }
+  }
+}
+
+// y = [relu](gamma * (z - mean) * rstd + beta [+ res])   (bf16, 8 channels per thread)
+__global__ void __launch_bounds__(256) bn_apply_kernel(const __nv_bfloat16* __restrict__ z,
+                                                       const __nv_bfloat16* __restrict__ res,
+                                                       const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                       const float* __restrict__ gamma, const float* __restrict__ beta,
+                                                       int C, int R, int64_t rows, int relu,
+                                                       __nv_bfloat16* __restrict__ y) {
+  const int cg = C / 8;
+  const int64_t n = rows * cg;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / cg;
+    const int c0 = (int)(i - row * cg) * 8, e = (int)(row / R);
+    float zv[8], o[8], rv[8];
+    ld8(z + row * C + c0, zv);
+    if (res) ld8(res + row * C + c0, rv);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = c0 + q;
+      float v = gamma[c] * ((zv[q] - mean[(size_t)e * C + c]) * rstd[(size_t)e * C + c]) + beta[c];
+      if (res) v += rv[q];
+      o[q] = (relu && !(v > 0.f)) ? 0.f : v;
+    }
+    st8(y + row * C + c0, o);
+  }
+}
+
+// dz = gamma * rstd * (g - S_g / R - xhat * S_gx / R),  g = dy * [y > 0]
+__global__ void __launch_bounds__(256) bn_bwd_kernel(const __nv_bfloat16* __restrict__ z,
+                                                     const __nv_bfloat16* __restrict__ dy,
+                                                     const __nv_bfloat16* __restrict__ y,
+                                                     const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                     const float* __restrict__ sg, const float* __restrict__ sgx,
+                                                     const float* __restrict__ gamma, int C, int R, int64_t rows,
+                                                     __nv_bfloat16* __restrict__ dz) {
+  const int cg = C / 8;
+  const int64_t n = rows * cg;
+  const float invR = 1.f / (float)R;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / cg;
+    const int c0 = (int)(i - row * cg) * 8, e = (int)(row / R);
+    float zv[8], dv[8], yv[8], o[8];
+    ld8(z + row * C + c0, zv);
+    ld8(dy + row * C + c0, dv);
+    ld8(y + row * C + c0, yv);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const size_t ec = (size_t)e * C + c0 + q;
+      const float g = yv[q] > 0.f ? dv[q] : 0.f;
+      const float xh = (zv[q] - mean[ec]) * rstd[ec];
+      o[q] = gamma[c0 + q] * rstd[ec] * (g - sg[ec] * invR - xh * (sgx[ec] * invR));
+    }
+    st8(dz + row * C + c0, o);
+  }
+}
+
+// out = a + (y ? dy * [y > 0] : b)   (the gradient arriving at a residual block's input)
+__global__ void __launch_bounds__(256) add_kernel(const __nv_bfloat16* __restrict__ a,
+                                                  const __nv_bfloat16* __restrict__ b,
+                                                  const __nv_bfloat16* __restrict__ y, int64_t n8,
+                                                  __nv_bfloat16* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    float av[8], bv[8], o[8];
+    ld8(a + i * 8, av);
+    ld8(b + i * 8, bv);
+    if (y) {
+      float yv[8];
+      ld8(y + i * 8, yv);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] = av[q] + (yv[q] > 0.f ? bv[q] : 0.f);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] = av[q] + bv[q];
+    }
+    st8(out + i * 8, o);
+  }
+}
+
+// ---------------------------------------------------------------- head
+// Per EST (one block): pooled[n][c] = mean of the 16 positions (4x4) in order; logits = pooled Wfc^T + b
+// (c ascending); loss = mean_n CE(softmax(logits), label); dlogits = (p - onehot)/B; per-EST dWfc, dbfc
+// (n ascending) into the EST's gradient slot; dx[n][pos][c] = (sum_k dlogits[n][k] Wfc[k][c]) / 16.
+constexpr int HEAD_C = 512, HEAD_K = 10, HEAD_POS = 16;
+__global__ void __launch_bounds__(512) head_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ labels,
+                                                   const float* __restrict__ W, const float* __restrict__ bias, int B,
+                                                   float* __restrict__ dW, float* __restrict__ db, int64_t grad_stride,
+                                                   float* __restrict__ loss, __nv_bfloat16* __restrict__ dx) {
+  extern __shared__ float hsm[];
+  float* pooled = hsm;                    // [B][512]
+  float* dlog = pooled + B * HEAD_C;      // [B][10]
+  const int e = blockIdx.x, t = threadIdx.x;
+  const size_t img0 = (size_t)e * B;
+  for (int n = 0; n < B; ++n) {  // thread = channel
+    float acc = 0.f;
+    for (int p = 0; p < HEAD_POS; ++p) acc += __bfloat162float(x[((img0 + n) * HEAD_POS + p) * HEAD_C + t]);
+    pooled[n * HEAD_C + t] = acc * (1.f / HEAD_POS);
+  }
+  __syncthreads();
+  for (int i = t; i < B * HEAD_K; i += blockDim.x) {
+    const int n = i / HEAD_K, k = i - n * HEAD_K;
+    float acc = bias[k];
+    for (int c = 0; c < HEAD_C; ++c) acc += pooled[n * HEAD_C + c] * W[k * HEAD_C + c];
+    dlog[i] = acc;
+  }
+  __syncthreads();
+  if (t < B) {  // softmax + CE per image
+    float* l = dlog + t * HEAD_K;
+    float m = l[0];
+    for (int k = 1; k < HEAD_K; ++k) m = fmaxf(m, l[k]);
+    float s = 0.f;
+    for (int k = 0; k < HEAD_K; ++k) s += expf(l[k] - m);
+    const int y = labels[img0 + t];
+    const float lse = m + logf(s);
+    const float ce = lse - l[y];
+    for (int k = 0; k < HEAD_K; ++k) l[k] = (expf(l[k] - lse) - (k == y ? 1.f : 0.f)) / (float)B;
+    hsm[B * HEAD_C + B * HEAD_K + t] = ce;
+  }
+  __syncthreads();
+  if (t == 0) {
+    float acc = 0.f;
+    for (int n = 0; n < B; ++n) acc += hsm[B * HEAD_C + B * HEAD_K + n];
+    loss[e] = acc / (float)B;
+  }
+  for (int k = 0; k < HEAD_K; ++k) {  // dW[k][c], thread = c
+    float acc = 0.f;
+    for (int n = 0; n < B; ++n) acc += dlog[n * HEAD_K + k] * pooled[n * HEAD_C + t];
+    dW[(size_t)e * grad_stride + k * HEAD_C + t] = acc;
+  }
+  if (t < HEAD_K) {
+    float acc = 0.f;
+    for (int n = 0; n < B; ++n) acc += dlog[n * HEAD_K + t];
+    db[(size_t)e * grad_stride + t] = acc;
+  }
+  for (int n = 0; n < B; ++n) {
+    float acc = 0.f;
+    for (int k = 0; k < HEAD_K; ++k) acc += dlog[n * HEAD_K + k] * W[k * HEAD_C + t];
+    const __nv_bfloat16 g = __float2bfloat16_rn(acc * (1.f / HEAD_POS));
+    for (int p = 0; p < HEAD_POS; ++p) dx[((img0 + n) * HEAD_POS + p) * HEAD_C + t] = g;
+  }
+}
+
+// ---------------------------------------------------------------- weights
+// master W [Co][KH*KW][Ci] fp32 -> Wb [Co][KH*KW*Ci] bf16 (forward B operand) and
+// Wt [Ci][KH*KW][Co] bf16 (the transposed convolution's B operand), one launch for a table
+struct ConvW {
+  const float* w;
+  __nv_bfloat16* wb;
+  __nv_bfloat16* wt;
+  int Co, T, Ci;  // T = KH*KW
+};
+constexpr int MAX_CONV = 32;
+struct ConvWTable {
+  ConvW m[MAX_CONV];
+  int n;
+};
+__global__ void conv_weights_kernel(const __grid_constant__ ConvWTable tab) {
+  const ConvW& m = tab.m[blockIdx.y];
+  const int64_t n = (int64_t)m.Co * m.T * m.Ci;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int ci = (int)(i % m.Ci);
+    const int64_t r = i / m.Ci;
+    const int t = (int)(r % m.T), co = (int)(r / m.T);
+    const __nv_bfloat16 v = __float2bfloat16_rn(m.w[i]);
+    m.wb[i] = v;
+    m.wt[((size_t)ci * m.T + t) * m.Co + co] = v;
+  }
+}
+
+}  // namespace cnn
+
+// ----------------------------------------------------------------- launchers
+static int ok_or_cuda_c() { return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA; }
+static int grid_n(int64_t n) {
+  const int64_t g = (n + 255) / 256;
+  return (int)(g > 148 * 16 ? 148 * 16 : (g < 1 ? 1 : g));
+}
+
+int cnn_data_launch(uint64_t seed, const int64_t* cursor, int est_base, int E, int B, void* x, int32_t* labels,
+                    cudaStream_t s) {
+  cnn::data_kernel<<<grid_n((int64_t)E * B * 1024), 256, 0, s>>>(seed, cursor, est_base, B, E, (__nv_bfloat16*)x,
+                                                                 labels);
+  return ok_or_cuda_c();
+}
+
+int cnn_im2col_launch(const void* src, void* col, int N, int Hs, int Ws, int C, int Ho, int Wo, int KH, int KW,
+                      int stride, int pad, int transposed, cudaStream_t s) {
+  if (C % 8) return ERR_INPUT;
+  const cnn::ColArgs a{(const __nv_bfloat16*)src, (__nv_bfloat16*)col, N, Hs, Ws, C, Ho, Wo, KH, KW, stride, pad,
+                       transposed};
+  cnn::im2col_kernel<<<grid_n((int64_t)N * Ho * Wo * KH * KW * (C / 8)), 256, 0, s>>>(a);
+  return ok_or_cuda_c();
+}
+
+// mode 0 / 1: mean / (rstd + running stats); mode 2: backward sums (+ dgamma, dbeta)
+int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, float* mean, float* rstd,
+                        float* sg, float* sgx, float* part, float* run_mean, float* run_var, int64_t run_stride,
+                        float* dgamma, float* dbeta, int64_t grad_stride, int E, int R, int C, float eps,
+                        cudaStream_t s) {
+  if (C % 8 || C > 2048 || R < 2) return ERR_INPUT;
+  const int chunks = (R + cnn::CHUNK - 1) / cnn::CHUNK;
+  const int lanes = 256 / (C / 8);
+  const int smem = lanes * 2 * C * (int)sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(cnn::stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024) !=
+        cudaSuccess)
+      return ERR_CUDA;
+    attr = true;
+  }
+  cnn::StatArgs sa{(const __nv_bfloat16*)z, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)y,
+                   mode == 0 ? nullptr : mean, rstd, part, C, R, mode};
+  cnn::stats_kernel<<<dim3(chunks, E), 256, smem, s>>>(sa);
+  cnn::FoldArgs fa{};
+  fa.part = part;
+  fa.out0 = mode == 0 ? mean : (mode == 1 ? rstd : sg);
+  fa.out1 = sgx;
+  fa.mean = mean;
+  fa.run_mean = run_mean;
+  fa.run_var = run_var;
+  fa.run_stride = run_stride;
+  fa.dgamma = dgamma;
+  fa.dbeta = dbeta;
+  fa.grad_stride = grad_stride;
+  fa.C = C;
+  fa.R = R;
+  fa.E = E;
+  fa.chunks = chunks;
+  fa.mode = mode;
+  fa.eps = eps;
+  cnn::fold_kernel<<<grid_n((int64_t)E * C), 256, 0, s>>>(fa);
+  return ok_or_cuda_c();
+}
+
+int cnn_bn_apply_launch(const void* z, const void* res, const float* mean, const float* rstd, const float* gamma,
+                        const float* beta, int E, int R, int C, int relu, void* y, cudaStream_t s) {
+  const int64_t rows = (int64_t)E * R;
+  cnn::bn_apply_kernel<<<grid_n(rows * C / 8), 256, 0, s>>>((const __nv_bfloat16*)z, (const __nv_bfloat16*)res, mean,
+                                                           rstd, gamma, beta, C, R, rows, relu, (__nv_bfloat16*)y);
+  return ok_or_cuda_c();
+}
+
+int cnn_bn_bwd_launch(const void* z, const void* dy, const void* y, const float* mean, const float* rstd,
+                      const float* sg, const float* sgx, const float* gamma, int E, int R, int C, void* dz,
+                      cudaStream_t s) {
+  const int64_t rows = (int64_t)E * R;
+  cnn::bn_bwd_kernel<<<grid_n(rows * C / 8), 256, 0, s>>>((const __nv_bfloat16*)z, (const __nv_bfloat16*)dy,
+                                                         (const __nv_bfloat16*)y, mean, rstd, sg, sgx, gamma, C, R,
+                                                         rows, (__nv_bfloat16*)dz);
+  return ok_or_cuda_c();
+}
+
+int cnn_add_launch(const void* a, const void* b, const void* y, int64_t n, void* out, cudaStream_t s) {
+  if (n % 8) return ERR_INPUT;
+  cnn::add_kernel<<<grid_n(n / 8), 256, 0, s>>>((const __nv_bfloat16*)a, (const __nv_bfloat16*)b,
+                                                (const __nv_bfloat16*)y, n / 8, (__nv_bfloat16*)out);
+  return ok_or_cuda_c();
+}
+
+int cnn_head_launch(const void* x, const int32_t* labels, const float* W, const float* bias, int E, int B, float* dW,
+                    float* db, int64_t grad_stride, float* loss, void* dx, cudaStream_t s) {
+  const int smem = (B * cnn::HEAD_C + B * cnn::HEAD_K + B) * (int)sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(cnn::head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+        cudaSuccess)
+      return ERR_CUDA;
+    attr = true;
+  }
+  if (B < 1 || smem > 200 * 1024) return ERR_INPUT;
+  cnn::head_kernel<<<E, cnn::HEAD_C, smem, s>>>((const __nv_bfloat16*)x, labels, W, bias, B, dW, db, grad_stride, loss,
+                                                (__nv_bfloat16*)dx);
+  return ok_or_cuda_c();
+}
+
+int cnn_conv_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* Co, const int* T,
+                            const int* Ci, int n, cudaStream_t s) {
+  if (n < 1 || n > cnn::MAX_CONV) return ERR_INPUT;
+  cnn::ConvWTable tab{};
+  int64_t mx = 0;
+  for (int i = 0; i < n; ++i) {
+    tab.m[i] = cnn::ConvW{w[i], (__nv_bfloat16*)wb[i], (__nv_bfloat16*)wt[i], Co[i], T[i], Ci[i]};
+    const int64_t sz = (int64_t)Co[i] * T[i] * Ci[i];
+    mx = sz > mx ? sz : mx;
+  }
+  tab.n = n;
+  const int gx = (int)((mx + 255) / 256 < 1024 ? (mx + 255) / 256 : 1024);
+  cnn::conv_weights_kernel<<<dim3(gx, n), 256, 0, s>>>(tab);
+  return ok_or_cuda_c();
+}
+
+}  // namespace bt

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* const tmem_slot = (uint32_t*)(gbase + L::BAR + (2 * STAGES + 4) * 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = M / BM, nt = N / BN, kb_n = K / BK;
+  const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN, kb_n = (K + BK - 1) / BK;  // TMA zero-fills / clips edges
   const int per_batch = mt * nt;
   auto tile_coords = [&](int t, int mt_, int nt_, int* m0, int* n0) {  // t -> (batch entry, m0, n0)
     tile_coords_bn<BN>(t % per_batch, mt_, nt_, m0, n0);
@@ -373,7 +373,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row0 = m0 + lg * 32;  // this warp's 32 rows (lane = row - row0) within the batch entry
       const size_t row = (size_t)row0 + lane;
 #pragma unroll 1
-      for (int cc = half * (BN / EPI_SPLIT); cc < (half + 1) * (BN / EPI_SPLIT); cc += 32) {
+      constexpr int PER = BN / EPI_SPLIT < 32 ? 32 : BN / EPI_SPLIT;  // columns per epilogue warp (BN=64: 8 warps work)
+      for (int cc = half * PER; cc < (half + 1) * PER && cc < BN; cc += 32) {
         uint32_t v[32];
         const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * BN + cc);
         asm volatile(
@@ -477,7 +478,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int mt = M / PAIR_M, nt = N / PAIR_BN, kb_n = K / BK;
+  const int mt = M / PAIR_M, nt = N / PAIR_BN, kb_n = (K + BK - 1) / BK;
   const int per_batch = mt * nt;
   const int tiles = per_batch * batch;
   const int pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
@@ -711,7 +712,7 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
       return ERR_CUDA;
     attr = true;
   }
-  const int tiles = (M / gemm::BM) * (N / BN) * g.batch;
+  const int tiles = ((M + gemm::BM - 1) / gemm::BM) * ((N + BN - 1) / BN) * g.batch;
   if (grid <= 0) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -772,13 +773,16 @@ static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests
   return e ? atoi(e) : 0;
 }
 
-// 256 x 256 CTA-pair tiles when M and N allow it, else 128 x {256, 128} tiles (all deterministic)
+// 256 x 256 CTA-pair tiles when M and N allow it, else 128 x {256, 128, 64} tiles; ragged M / N / K
+// edges are zero-filled by the TMA loads and clipped by the TMA stores (all deterministic)
 template <bool MN>
 static int launch_any(const GemmShape& g, int out_bf16, int grid, cudaStream_t s) {
   if (g.M % 256 == 0 && g.N % 256 == 0 && gemm_variant() != 1)
     return out_bf16 ? launch_gemm_pair<5, true, MN>(g, grid, s) : launch_gemm_pair<5, false, MN>(g, grid, s);
   if (g.N % 256 == 0)
     return out_bf16 ? launch_gemm<256, 3, true, MN>(g, grid, s) : launch_gemm<256, 3, false, MN>(g, grid, s);
+  if (g.N <= 64)  // narrow outputs (64-channel convolutions)
+    return out_bf16 ? launch_gemm<64, 6, true, MN>(g, grid, s) : launch_gemm<64, 6, false, MN>(g, grid, s);
   return out_bf16 ? launch_gemm<128, 5, true, MN>(g, grid, s) : launch_gemm<128, 5, false, MN>(g, grid, s);
 }
 int gemm_bf16_launch_any(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,

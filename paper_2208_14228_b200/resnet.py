@@ -1,0 +1,357 @@
+"""Per-EST ResNet-18 training step with BatchNorm and elastic rescale -- C3
+(BASELINE.json configs[2]).
+
+CIFAR ResNet-18 (3x3 stem, 4 stages x 2 BasicBlocks of widths 64-128-256-512,
+1x1 stride-2 downsample shortcuts, 4x4 average pool, 10-way linear head,
+softmax cross-entropy) trained data-parallel by E ESTs of B images each.
+The EasyScale properties it keeps (paper §3.2, D1):
+
+* per-EST state -- each EST's BatchNorm running statistics and its sampler
+  cursor -- lives in HBM slots indexed by the EST's rank and travels with the
+  EST: `rescale(G)` redistributes the slots onto a new number of "GPUs"
+  (launch groups of contiguous EST blocks, `engine.assign_ranks`) with the
+  128-bit slot-copy kernel (bt_est_slot_copy), the context switch of
+  SURVEY §7 D5;
+* every EST normalises with its own micro-batch statistics (no cross-EST
+  BatchNorm), all randomness is keyed by (seed, EST rank, EST cursor), every
+  reduction has a shape fixed by the EST's own data, and the per-EST gradients
+  are summed by the fixed-order reducer -- so losses, weights and BN statistics
+  are bit-identical for any mapping and across an 8 -> 4 -> 2 rescale
+  (tests/test_gpu_resnet.py).
+
+Convolutions are im2col GEMMs on the deterministic tcgen05 kernel; dX is the
+transposed convolution as an im2col gather (no scatter-add), dW one MN-major
+batched GEMM per EST.  The stem's 3 input channels are zero-padded to 8.
+There is no reference implementation of this model.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native
+from .device import Flags, require_cuda, stream
+from .errors import ConfigError, NumericError
+
+WIDTHS = (64, 128, 256, 512)
+CLASSES = 10
+
+
+def _init_uniform(seed: int, n: int, scale: float) -> torch.Tensor:
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().bt_init_random(seed & (2**64 - 1), scale, n, out.data_ptr(), stream()))
+    return out.float()
+
+
+def _round8(n: int) -> int:
+    return (n + 7) // 8 * 8
+
+
+class _Conv:
+    def __init__(self, name, ci, co, k, s, hin):
+        self.name, self.ci, self.co, self.k, self.s, self.hin = name, ci, co, k, s, hin
+        self.p = k // 2
+        self.hout = (hin + 2 * self.p - k) // s + 1
+        self.taps = k * k
+        self.K = self.taps * ci
+
+
+class ResNetJob:
+    """E ESTs x B images (32 x 32 x 3), ResNet-18 with per-EST BatchNorm, momentum SGD, `groups` "GPUs"."""
+
+    def __init__(self, ests: int = 16, batch: int = 32, gpus: int = 8, seed: int = 42, lr: float = 0.02,
+                 momentum: float = 0.9, fanin: int = 0, eps: float = 1e-5):
+        require_cuda()
+        if ests < 1 or ests > _native.BT_MAX_TABLE:
+            raise ConfigError(f"1..{_native.BT_MAX_TABLE} ESTs per job")
+        if fanin not in (0, 2) or (fanin == 2 and ests & (ests - 1)):
+            raise ConfigError("allreduce variant: Sequential (0) or Tree(2) with a power-of-two EST count")
+        self.E, self.B, self.seed, self.lr, self.mu, self.fanin, self.eps = ests, batch, seed, lr, momentum, fanin, eps
+        convs = [_Conv("stem", 8, 64, 3, 1, 32)]
+        blocks = []
+        ci, h = 64, 32
+        for si, w in enumerate(WIDTHS):
+            for bi in range(2):
+                s = 2 if (si > 0 and bi == 0) else 1
+                a = _Conv(f"l{si + 1}.{bi}.a", ci, w, 3, s, h)
+                b = _Conv(f"l{si + 1}.{bi}.b", w, w, 3, 1, a.hout)
+                d = _Conv(f"l{si + 1}.{bi}.d", ci, w, 1, s, h) if (s != 1 or ci != w) else None
+                convs += [a, b] + ([d] if d else [])
+                blocks.append((a, b, d))
+                ci, h = w, a.hout
+        self.convs, self.blocks = convs, blocks
+        # flat fp32 parameters: per conv W [Co][taps][Ci], gamma [Co], beta [Co]; then fc W [10][512], b [10]
+        self.off, o = {}, 0
+        for cv in convs:
+            self.off[cv.name] = (o, o + _round8(cv.co * cv.K), o + _round8(cv.co * cv.K) + _round8(cv.co))
+            o += _round8(cv.co * cv.K) + 2 * _round8(cv.co)
+        self.off_fc = (o, o + CLASSES * 512)
+        o += CLASSES * 512 + _round8(CLASSES)
+        self.P = _round8(o)
+        self.params = torch.zeros(self.P, dtype=torch.float32, device="cuda")
+        for i, cv in enumerate(convs):
+            w0, g0, _ = self.off[cv.name]
+            fan_in = cv.taps * (3 if cv.name == "stem" else cv.ci)
+            w = _init_uniform(seed * 7919 + i, cv.co * cv.K, (6.0 / fan_in) ** 0.5).view(cv.co, cv.taps, cv.ci)
+            if cv.name == "stem":
+                w[:, :, 3:] = 0.0  # padded input channels
+            self.params[w0:w0 + cv.co * cv.K] = w.reshape(-1)
+            self.params[g0:g0 + cv.co] = 1.0
+        self.params[self.off_fc[0]:self.off_fc[0] + CLASSES * 512] = _init_uniform(seed * 7919 + 999, CLASSES * 512,
+                                                                                   (1.0 / 512) ** 0.5)
+        self.vel = torch.zeros_like(self.params)
+        self.grads = torch.zeros(ests, self.P, dtype=torch.float32, device="cuda")  # padding stays 0
+        # BatchNorm channel offsets inside an EST's running-statistics slot
+        self.bn_off, c = {}, 0
+        for cv in convs:
+            self.bn_off[cv.name] = c
+            c += cv.co
+        self.CBN = c
+        # bf16 operand copies of the conv weights: wb [Co][taps*Ci] (forward), wt [Ci][taps][Co] (dX)
+        tot = sum(cv.co * cv.K for cv in convs)
+        self.wb = torch.empty(tot, dtype=torch.bfloat16, device="cuda")
+        self.wt = torch.empty(tot, dtype=torch.bfloat16, device="cuda")
+        self.woff, m = {}, 0
+        for cv in convs:
+            self.woff[cv.name] = m
+            m += cv.co * cv.K
+        n = len(convs)
+        self._cast = [(C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_int32 * n)(),
+                      (C.c_int32 * n)(), (C.c_int32 * n)()]
+        for i, cv in enumerate(convs):
+            self._cast[0][i] = self.params.data_ptr() + 4 * self.off[cv.name][0]
+            self._cast[1][i] = self.wb.data_ptr() + 2 * self.woff[cv.name]
+            self._cast[2][i] = self.wt.data_ptr() + 2 * self.woff[cv.name]
+            self._cast[3][i], self._cast[4][i], self._cast[5][i] = cv.co, cv.taps, cv.ci
+        self.flags = Flags()
+        self.step_idx = 0
+        self._ws = {}
+        # per-EST slots, held by the "GPU" (launch group) that owns the EST
+        self.G = 0
+        self.slots = []
+        self._place(gpus, initial=True)
+        self._refresh_bf16()
+
+    # ------------------------------------------------------------ EST slots
+    def layout(self, gpus: int) -> list[tuple[int, int]]:
+        """Contiguous EST blocks (engine.assign_ranks with balanced, larger-first shares)."""
+        if gpus < 1 or gpus > self.E:
+            raise ConfigError(f"{gpus} GPUs for {self.E} ESTs")
+        q, r = divmod(self.E, gpus)
+        out, base = [], 0
+        for g in range(gpus):
+            n = q + (1 if g < r else 0)
+            out.append((base, n))
+            base += n
+        return out
+
+    def _new_slots(self, n: int) -> dict:
+        return {"run_mean": torch.zeros(n, self.CBN, dtype=torch.float32, device="cuda"),
+                "run_var": torch.ones(n, self.CBN, dtype=torch.float32, device="cuda"),
+                "cursor": torch.zeros(n, dtype=torch.int64, device="cuda")}
+
+    def _place(self, gpus: int, initial: bool = False):
+        new_layout = self.layout(gpus)
+        new = [self._new_slots(n) for _, n in new_layout]
+        if not initial:  # context switch: every EST's slot bytes move to its new owner (one launch)
+            owner = {}
+            for g, (base, n) in enumerate(self.layout(self.G)):
+                for k in range(n):
+                    owner[base + k] = (g, k)
+            dst, src, nb = [], [], []
+            for g, (base, n) in enumerate(new_layout):
+                for k in range(n):
+                    og, ok = owner[base + k]
+                    for key in ("run_mean", "run_var", "cursor"):
+                        d, s_ = new[g][key][k], self.slots[og][key][ok]
+                        dst.append(d.data_ptr())
+                        src.append(s_.data_ptr())
+                        nb.append(d.numel() * d.element_size())
+            cnt = len(dst)
+            _native.check(_native.lib().bt_est_slot_copy((C.c_void_p * cnt)(*dst), (C.c_void_p * cnt)(*src),
+                                                         (C.c_int64 * cnt)(*nb), cnt, stream()), "EST slot copy")
+        self.slots, self.G = new, gpus
+
+    def rescale(self, gpus: int):
+        """Elastic rescale onto `gpus` launch groups: per-EST slots move, parameters are replicated."""
+        self._place(gpus)
+
+    def est_state(self) -> dict:
+        """Per-EST slots gathered in EST-rank order (for comparisons across mappings)."""
+        return {k: torch.cat([s[k] for s in self.slots]) for k in ("run_mean", "run_var", "cursor")}
+
+    # ------------------------------------------------------------ workspace
+    def _refresh_bf16(self):
+        c = self._cast
+        _native.check(_native.lib().bt_cnn_conv_weights(c[0], c[1], c[2], c[3], c[4], c[5], len(c[3]), stream()),
+                      "conv weight cast")
+
+    def _workspace(self, n: int) -> dict:
+        ws = self._ws.get(n)
+        if ws is not None:
+            return ws
+        B = self.B
+        bf, f32 = dict(dtype=torch.bfloat16, device="cuda"), dict(dtype=torch.float32, device="cuda")
+        col = 0
+        for cv in self.convs:
+            col = max(col, n * B * cv.hout ** 2 * cv.K, n * B * cv.hin ** 2 * cv.taps * cv.co)
+        ws = {"img": torch.empty(n * B * 1024 * 8, **bf), "labels": torch.empty(n * B, dtype=torch.int32, device="cuda"),
+              "col": torch.empty(col, **bf), "loss": torch.empty(n, **f32)}
+        for cv in self.convs:
+            R = n * B * cv.hout ** 2
+            ws[cv.name] = {"z": torch.empty(R * cv.co, **bf), "y": torch.empty(R * cv.co, **bf),
+                           "mean": torch.empty(n * cv.co, **f32), "rstd": torch.empty(n * cv.co, **f32)}
+        big = max(n * B * cv.hin ** 2 * max(cv.ci, cv.co) for cv in self.convs)
+        ws["g"] = [torch.empty(big, **bf) for _ in range(4)]
+        ws["sg"] = torch.empty(n * 512, **f32)
+        ws["sgx"] = torch.empty(n * 512, **f32)
+        chunks = max((B * cv.hout ** 2 + 255) // 256 for cv in self.convs)
+        ws["part"] = torch.empty(n * chunks * 2 * 512, **f32)
+        self._ws[n] = ws
+        return ws
+
+    # ------------------------------------------------------------ layers
+    def _conv_fwd(self, ws, cv, x, n, z):
+        L, s = _native.lib(), stream()
+        R = n * self.B * cv.hout ** 2
+        _native.check(L.bt_cnn_im2col(x.data_ptr(), ws["col"].data_ptr(), n * self.B, cv.hin, cv.hin, cv.ci, cv.hout,
+                                      cv.hout, cv.k, cv.k, cv.s, cv.p, 0, s), "im2col")
+        _native.check(L.bt_gemm_bf16_ex(ws["col"].data_ptr(), self.wb.data_ptr() + 2 * self.woff[cv.name], z.data_ptr(),
+                                        1, R, cv.co, cv.K, 0, 0, 0, 1, None, 0, 0, s), "conv gemm")
+
+    def _bn_fwd(self, ws, cv, n, gslot, res=None, relu=True, out=None):
+        L, s = _native.lib(), stream()
+        w = ws[cv.name]
+        Re = self.B * cv.hout ** 2
+        _, g0, b0 = self.off[cv.name]
+        sl = self.slots[gslot]
+        rm = sl["run_mean"].data_ptr() + 4 * self.bn_off[cv.name]
+        rv = sl["run_var"].data_ptr() + 4 * self.bn_off[cv.name]
+        for mode in (0, 1):
+            _native.check(L.bt_cnn_bn_stats(mode, w["z"].data_ptr(), None, None, w["mean"].data_ptr(),
+                                            w["rstd"].data_ptr(), None, None, ws["part"].data_ptr(), rm, rv, self.CBN,
+                                            None, None, 0, n, Re, cv.co, self.eps, s), "bn stats")
+        out = w["y"] if out is None else out
+        _native.check(L.bt_cnn_bn_apply(w["z"].data_ptr(), None if res is None else res.data_ptr(),
+                                        w["mean"].data_ptr(), w["rstd"].data_ptr(),
+                                        self.params.data_ptr() + 4 * g0, self.params.data_ptr() + 4 * b0, n, Re,
+                                        cv.co, 1 if relu else 0, out.data_ptr(), s), "bn apply")
+
+    def _bn_bwd(self, ws, cv, n, base, dy, y, dz):
+        """dz of BN(z) whose (block) output y got gradient dy (through the ReLU mask of y)."""
+        L, s = _native.lib(), stream()
+        w = ws[cv.name]
+        Re = self.B * cv.hout ** 2
+        _, g0, b0 = self.off[cv.name]
+        gp = self.grads.data_ptr() + 4 * base * self.P
+        _native.check(L.bt_cnn_bn_stats(2, w["z"].data_ptr(), dy.data_ptr(), y.data_ptr(), w["mean"].data_ptr(),
+                                        w["rstd"].data_ptr(), ws["sg"].data_ptr(), ws["sgx"].data_ptr(),
+                                        ws["part"].data_ptr(), None, None, 0, gp + 4 * g0, gp + 4 * b0, self.P, n, Re,
+                                        cv.co, self.eps, s), "bn backward sums")
+        _native.check(L.bt_cnn_bn_bwd(w["z"].data_ptr(), dy.data_ptr(), y.data_ptr(), w["mean"].data_ptr(),
+                                      w["rstd"].data_ptr(), ws["sg"].data_ptr(), ws["sgx"].data_ptr(),
+                                      self.params.data_ptr() + 4 * g0, n, Re, cv.co, dz.data_ptr(), s), "bn backward")
+
+    def _conv_bwd(self, ws, cv, n, base, x, dz, dx):
+        """dW_e (into each EST's gradient slot) and, if dx is given, the input gradient."""
+        L, s, B = _native.lib(), stream(), self.B
+        Re = B * cv.hout ** 2
+        _native.check(L.bt_cnn_im2col(x.data_ptr(), ws["col"].data_ptr(), n * B, cv.hin, cv.hin, cv.ci, cv.hout,
+                                      cv.hout, cv.k, cv.k, cv.s, cv.p, 0, s), "im2col")
+        _native.check(L.bt_gemm_bf16_ex(dz.data_ptr(), ws["col"].data_ptr(),
+                                        self.grads.data_ptr() + 4 * (base * self.P + self.off[cv.name][0]), n, cv.co,
+                                        cv.K, Re, Re * cv.co, Re * cv.K, self.P, 0, None, 1, 0, s), "conv dW gemm")
+        if dx is not None:
+            Rin = n * B * cv.hin ** 2
+            _native.check(L.bt_cnn_im2col(dz.data_ptr(), ws["col"].data_ptr(), n * B, cv.hout, cv.hout, cv.co, cv.hin,
+                                          cv.hin, cv.k, cv.k, cv.s, cv.p, 1, s), "im2col (transposed)")
+            _native.check(L.bt_gemm_bf16_ex(ws["col"].data_ptr(), self.wt.data_ptr() + 2 * self.woff[cv.name],
+                                            dx.data_ptr(), 1, Rin, cv.ci, cv.taps * cv.co, 0, 0, 0, 1, None, 0, 0, s),
+                          "conv dX gemm")
+
+    def _group(self, gslot: int, base: int, n: int, losses: torch.Tensor, capture: dict | None):
+        L, s, B = _native.lib(), stream(), self.B
+        ws = self._workspace(n)
+        sl = self.slots[gslot]
+        _native.check(L.bt_cnn_data(self.seed & (2**64 - 1), sl["cursor"].data_ptr(), base, n, B,
+                                    ws["img"].data_ptr(), ws["labels"].data_ptr(), s))
+        stem = self.convs[0]
+        self._conv_fwd(ws, stem, ws["img"], n, ws["stem"]["z"])
+        self._bn_fwd(ws, stem, n, gslot)
+        x = ws["stem"]["y"]
+        ins = []
+        for a, b, d in self.blocks:
+            ins.append(x)
+            self._conv_fwd(ws, a, x, n, ws[a.name]["z"])
+            self._bn_fwd(ws, a, n, gslot)
+            self._conv_fwd(ws, b, ws[a.name]["y"], n, ws[b.name]["z"])
+            res = x
+            if d is not None:
+                self._conv_fwd(ws, d, x, n, ws[d.name]["z"])
+                self._bn_fwd(ws, d, n, gslot, relu=False)
+                res = ws[d.name]["y"]
+            self._bn_fwd(ws, b, n, gslot, res=res)
+            x = ws[b.name]["y"]
+        gp = self.grads.data_ptr() + 4 * base * self.P
+        g = ws["g"]
+        fw, fb = self.off_fc
+        _native.check(L.bt_cnn_head(x.data_ptr(), ws["labels"].data_ptr(), self.params.data_ptr() + 4 * fw,
+                                    self.params.data_ptr() + 4 * fb, n, B, gp + 4 * fw, gp + 4 * fb, self.P,
+                                    losses[base:].data_ptr(), g[0].data_ptr(), s), "head")
+        if capture is not None:
+            capture.update(img=ws["img"].clone(), labels=ws["labels"].clone(),
+                           **{f"{k}_{cv.name}": ws[cv.name][k].clone() for cv in self.convs[:4] + self.convs[-2:]
+                              for k in ("z", "y", "mean", "rstd")}, top=x.clone(),
+                           dtop=g[0][:x.numel()].clone())
+        dy = g[0]  # gradient of the current block output
+        for (a, b, d), xin in zip(reversed(self.blocks), reversed(ins)):
+            out = ws[b.name]["y"]
+            dzb, dya, dza, dxa = g[1], g[2], g[1], g[3]
+            self._bn_bwd(ws, b, n, base, dy, out, dzb)
+            self._conv_bwd(ws, b, n, base, ws[a.name]["y"], dzb, dya)
+            self._bn_bwd(ws, a, n, base, dya, ws[a.name]["y"], dza)
+            self._conv_bwd(ws, a, n, base, xin, dza, dxa)
+            if d is None:  # identity shortcut: dx = dxa + dy [out > 0]
+                _native.check(L.bt_cnn_add(dxa.data_ptr(), dy.data_ptr(), out.data_ptr(), n * B * a.hin ** 2 * a.ci,
+                                           dy.data_ptr(), s))
+            else:
+                self._bn_bwd(ws, d, n, base, dy, out, g[2])
+                self._conv_bwd(ws, d, n, base, xin, g[2], g[1])
+                _native.check(L.bt_cnn_add(dxa.data_ptr(), g[1].data_ptr(), None, n * B * a.hin ** 2 * a.ci,
+                                           dy.data_ptr(), s))
+        self._bn_bwd(ws, stem, n, base, dy, ws["stem"]["y"], g[1])
+        self._conv_bwd(ws, stem, n, base, ws["img"], g[1], None)
+        sl["cursor"].add_(1)  # every EST of the group consumed one micro-batch
+
+    # ------------------------------------------------------------ step
+    def step(self, capture: dict | None = None) -> torch.Tensor:
+        """One mini-batch of all E ESTs on the current layout; per-EST losses [E] (fp32, on device)."""
+        losses = torch.empty(self.E, dtype=torch.float32, device="cuda")
+        for g, (base, n) in enumerate(self.layout(self.G)):
+            self._group(g, base, n, losses, capture if self.G == 1 else None)
+        if capture is not None:
+            capture["grads"] = self.grads.clone()
+        a = _native.ReduceArgs()
+        a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, self.E, self.fanin, self.P
+        for k in range(self.E):
+            a.grads[k] = self.grads.data_ptr() + 4 * k * self.P
+        p, v = self.params.data_ptr(), self.vel.data_ptr()
+        a.param, a.vel, a.param_out, a.vel_out = p, v, p, v
+        a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
+        _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()), "resnet reduce_update")
+        st, _, _ = self.flags.status()
+        if st:
+            self.flags.reset()
+            raise NumericError("resnet: non-finite synchronized gradient")
+        self.step_idx += 1
+        self._refresh_bf16()
+        return losses
+
+    def flops_per_step(self) -> float:
+        """Convolution + head flops of one mini-batch (forward 2*R*Co*K, backward dX and dW 2x that)."""
+        f = 0.0
+        for cv in self.convs:
+            f += 6.0 * self.E * self.B * cv.hout ** 2 * cv.co * (cv.taps * (3 if cv.name == "stem" else cv.ci))
+        return f

@@ -62,10 +62,32 @@ def test_gemm_rejects_bad_shapes(gemm):
     from paper_2208_14228_b200.errors import InputError
 
     a, b = _inputs(128, 128, 64, 1)
-    with pytest.raises(InputError):
-        gemm(a[:, :32].contiguous(), b[:, :32].contiguous())
-    with pytest.raises(InputError):
-        gemm(a[:100].contiguous(), b)
+    with pytest.raises(InputError):  # K-major rows must be 16-byte aligned (K % 8)
+        gemm(a[:, :30].contiguous(), b[:, :30].contiguous())
+    with pytest.raises(InputError):  # N % 8
+        gemm(a, b[:100].contiguous())
+
+
+@pytest.mark.parametrize("M,N,K,mn", [(200, 72, 40, False), (96, 64, 1000, False), (1000, 576, 96, False),
+                                      (72, 24, 4096, True), (576, 64, 2048, True), (64, 32, 640, True)])
+def test_ragged_shapes(gemm, M, N, K, mn):
+    """M, N, K off the 128 / 64 tile grid (64-channel convolutions, 3x3x3 stems, 576-wide im2col weight
+    gradients): TMA zero-fills the loads and clips the stores; results within the fp32 bound."""
+    from paper_2208_14228_b200.gemm import gemm_bf16_at_b
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    if mn:
+        a = torch.randn(2, K, M, device="cuda", generator=g).to(torch.bfloat16)
+        b = torch.randn(2, K, N, device="cuda", generator=g).to(torch.bfloat16)
+        c = gemm_bf16_at_b(a, b)
+        ref = torch.einsum("ekm,ekn->emn", a.double(), b.double())
+        bound = K * 2.0 ** -23 * torch.einsum("ekm,ekn->emn", a.double().abs(), b.double().abs())
+    else:
+        a, b = _inputs(M, N, K, 3)
+        c = gemm(a, b)
+        ref = a.double() @ b.double().T
+        bound = K * 2.0 ** -23 * (a.double().abs() @ b.double().abs().T)
+    assert bool(((c.double() - ref).abs() <= bound + 1e-30).all())
 
 
 def test_cta_pair_and_single_cta_kernels_agree_bitwise(gemm, monkeypatch):

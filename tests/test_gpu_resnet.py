@@ -1,0 +1,219 @@
+"""Per-EST ResNet-18 step with BatchNorm and elastic rescale (C3, BASELINE.json configs[2]; needs a B200).
+
+* Elastic rescale (the EasyScale S1/S2/S4 property, bit for bit): 16 ESTs trained on 8 "GPUs"
+  (launch groups), rescaled to 4 and then 2 mid-training -- per-EST BatchNorm running statistics and
+  sampler cursors moved by the slot-copy kernel -- give the same losses, weights, momentum and per-EST
+  BN statistics as the uninterrupted 1-GPU run.
+* Parity (no reference implementation exists for this model): the stem and first block
+  stage by stage against float64 restatements fed with the captured bf16 inputs (conv: <= 1% of bf16
+  outputs differ by one ulp; BN statistics and running statistics rel. error <= 1e-5); the whole
+  network's per-EST loss against a float64 restatement with the same forward bf16 rounding points
+  (rel. error <= 2e-3 after 20 layers of bf16 activations); the head and the last BasicBlock's
+  backward stage by stage from the captured tensors (fc gradients <= 1e-4, BN dgamma/dbeta <= 1e-4,
+  per-EST conv weight gradient rel. Frobenius error <= 5e-3).
+"""
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as Fn
+
+pytestmark = pytest.mark.gpu
+
+SMALL = dict(ests=16, batch=4, seed=7, lr=0.05, momentum=0.9)
+
+
+@pytest.fixture(scope="module")
+def rn():
+    assert torch.cuda.is_available()
+    from paper_2208_14228_b200 import resnet as mod
+
+    return mod
+
+
+def _bits(t):
+    return t.detach().contiguous().view(torch.int32).cpu().numpy()
+
+
+def test_rescale_8_4_2_matches_uninterrupted_run(rn):
+    a = rn.ResNetJob(gpus=8, **SMALL)
+    b = rn.ResNetJob(gpus=1, **SMALL)
+    la, lb = [], []
+    for gpus in (8, 4, 2):
+        if gpus != 8:
+            a.rescale(gpus)
+        for _ in range(2):
+            la.append(a.step().clone())
+            lb.append(b.step().clone())
+    for x, y in zip(la, lb):
+        assert np.array_equal(_bits(x), _bits(y))
+    assert np.array_equal(_bits(a.params), _bits(b.params))
+    assert np.array_equal(_bits(a.vel), _bits(b.vel))
+    sa, sb = a.est_state(), b.est_state()
+    for k in ("run_mean", "run_var"):
+        assert np.array_equal(_bits(sa[k]), _bits(sb[k])), k
+    assert torch.equal(sa["cursor"], sb["cursor"]) and int(sa["cursor"][0]) == 6
+    assert a.G == 2 and len(a.slots) == 2
+
+
+def test_uneven_layout_and_tree_reducer(rn):
+    a = rn.ResNetJob(gpus=3, fanin=2, **SMALL)  # 6 + 5 + 5 ESTs
+    b = rn.ResNetJob(gpus=1, fanin=2, **SMALL)
+    for _ in range(2):
+        assert np.array_equal(_bits(a.step()), _bits(b.step()))
+    assert np.array_equal(_bits(a.params), _bits(b.params))
+
+
+def test_same_batch_loss_decreases(rn):
+    job = rn.ResNetJob(gpus=1, **dict(SMALL, lr=0.05))
+    first = job.step().mean().item()
+    for _ in range(3):
+        job.slots[0]["cursor"].zero_()  # replay micro-batch 0 of every EST
+        last = job.step().mean().item()
+    assert last < first, (first, last)
+
+
+def _d(t):
+    return t.detach().double().cpu()
+
+
+def _bf(x):
+    return x.to(torch.bfloat16).double()
+
+
+def _close_bf16(got, want, what, frac=1e-2, rel=5e-3):
+    got, want = _d(got), want.double()
+    mism = (got != _bf(want)).double().mean().item()
+    err = ((got - want).norm() / (want.norm() + 1e-30)).item()
+    assert mism <= frac and err <= rel, (what, mism, err)
+
+
+def _close(got, want, what, rel):
+    got, want = _d(got), want.double()
+    err = ((got - want).norm() / (want.norm() + 1e-30)).item()
+    assert err <= rel, (what, err)
+
+
+def _conv_w(job, cv, p):
+    w0 = job.off[cv.name][0]
+    return _d(p[w0:w0 + cv.co * cv.K]).view(cv.co, cv.k, cv.k, cv.ci).permute(0, 3, 1, 2)  # OIHW
+
+
+def _nchw(t, n, h, c):
+    return _d(t).view(n, h, h, c).permute(0, 3, 1, 2)
+
+
+def test_stem_and_block_stages_match_float64(rn):
+    job = rn.ResNetJob(gpus=1, **SMALL)
+    P0 = job.params.clone()
+    cap = {}
+    job.step(capture=cap)
+    E, B, eps = job.E, job.B, job.eps
+    N = E * B
+    stem = job.convs[0]
+    x = _nchw(cap["img"], N, 32, 8)
+    assert bool((x[:, 3:] == 0).all()) and float(x[:, :3].abs().max()) <= 1.0
+    z_ref = Fn.conv2d(x, _bf(_conv_w(job, stem, P0)), padding=1)
+    z = _nchw(cap["z_stem"], N, 32, 64)
+    _close_bf16(z, z_ref, "stem conv")
+    # per-EST batch statistics over the EST's own B x 32 x 32 pixels
+    zc = z.view(E, B, 64, 1024).permute(0, 2, 1, 3).reshape(E, 64, -1)
+    mean, var = zc.mean(-1), zc.var(-1, unbiased=False)
+    _close(cap["mean_stem"].view(E, 64), mean, "bn mean", 1e-5)
+    _close(cap["rstd_stem"].view(E, 64), 1 / torch.sqrt(var + eps), "bn rstd", 1e-5)
+    g0, b0 = job.off["stem"][1:]
+    gam, bet = _d(P0[g0:g0 + 64]), _d(P0[b0:b0 + 64])
+    y_ref = torch.relu(gam.view(1, 64, 1, 1) * (z - mean.repeat_interleave(B, 0).view(N, 64, 1, 1))
+                       * (1 / torch.sqrt(var + eps)).repeat_interleave(B, 0).view(N, 64, 1, 1) + bet.view(1, 64, 1, 1))
+    _close_bf16(_nchw(cap["y_stem"], N, 32, 64), y_ref, "bn + relu")
+    st = job.est_state()
+    R = B * 1024
+    _close(st["run_mean"][:, :64], 0.1 * mean, "running mean", 1e-5)
+    _close(st["run_var"][:, :64], 0.9 + 0.1 * var * R / (R - 1), "running var", 1e-5)
+    a = job.convs[1]
+    za_ref = Fn.conv2d(_nchw(cap["y_stem"], N, 32, 64), _bf(_conv_w(job, a, P0)), padding=1)
+    _close_bf16(_nchw(cap[f"z_{a.name}"], N, 32, 64), za_ref, "block conv a")
+
+
+def _restate_loss(job, P, img, labels):
+    """float64 ResNet-18 with the kernels' forward bf16 rounding points; per-EST BatchNorm statistics."""
+    E, B, eps = job.E, job.B, job.eps
+    N = E * B
+
+    def bn(z, cv, relu=True, res=None):
+        g0, b0 = job.off[cv.name][1:]
+        zz = z.view(E, B, cv.co, -1).transpose(1, 2).reshape(E, cv.co, -1)
+        m = zz.mean(-1).repeat_interleave(B, 0).view(N, cv.co, 1, 1)
+        v = zz.var(-1, unbiased=False).repeat_interleave(B, 0).view(N, cv.co, 1, 1)
+        y = P[g0:g0 + cv.co].view(1, -1, 1, 1) * (z - m) / torch.sqrt(v + eps) + P[b0:b0 + cv.co].view(1, -1, 1, 1)
+        if res is not None:
+            y = y + res
+        return _bf(torch.relu(y) if relu else y)
+
+    def conv(x, cv):
+        w0 = job.off[cv.name][0]
+        w = P[w0:w0 + cv.co * cv.K].view(cv.co, cv.k, cv.k, cv.ci).permute(0, 3, 1, 2)
+        return _bf(Fn.conv2d(x, _bf(w), stride=cv.s, padding=cv.p))
+
+    x = bn(conv(img, job.convs[0]), job.convs[0])
+    for a, b, d in job.blocks:
+        h = bn(conv(x, a), a)
+        res = x if d is None else bn(conv(x, d), d, relu=False)
+        x = bn(conv(h, b), b, res=res)
+    pooled = x.mean((2, 3))
+    fw, fb = job.off_fc
+    logits = pooled @ P[fw:fw + 5120].view(10, 512).T + P[fb:fb + 10]
+    ce = Fn.cross_entropy(logits, labels, reduction="none")
+    return ce.view(E, B).mean(1)
+
+
+def test_loss_and_last_block_gradients_match_float64(rn):
+    """Whole-network loss vs the float64 restatement; the head and the last BasicBlock's backward
+    (ReLU mask, BatchNorm backward with per-EST statistics, per-EST conv weight gradient) stage by
+    stage from the captured bf16 tensors."""
+    job = rn.ResNetJob(gpus=1, **SMALL)
+    P0 = job.params.clone()
+    cap = {}
+    losses = job.step(capture=cap)
+    E, B, eps = job.E, job.B, job.eps
+    N = E * B
+    img = _nchw(cap["img"], N, 32, 8)
+    labels = cap["labels"].long().cpu()
+    assert int(labels.min()) >= 0 and int(labels.max()) <= 9
+    with torch.no_grad():
+        ref = _restate_loss(job, _d(P0), img, labels)
+    _close(losses, ref, "per-EST loss (20 layers of bf16 activations)", 2e-3)
+    g = cap["grads"].double().cpu()
+    # head: avgpool + fc + CE from the captured block output
+    top = _d(cap["top"]).view(N, 16, 512)
+    pooled = top.mean(1).requires_grad_(True)
+    fw, fb = job.off_fc
+    W = _d(P0[fw:fw + 5120]).view(10, 512).requires_grad_(True)
+    bvec = _d(P0[fb:fb + 10]).requires_grad_(True)
+    ce = Fn.cross_entropy(pooled @ W.T + bvec, labels, reduction="none").view(E, B).mean(1)
+    _close(losses, ce.detach(), "head loss", 1e-5)
+    for e in (0, E - 1):
+        gw, gb, gp = torch.autograd.grad(ce[e], (W, bvec, pooled), retain_graph=True)
+        _close(g[e, fw:fw + 5120], gw.reshape(-1), f"fc grad est {e}", 1e-4)
+        _close(g[e, fb:fb + 10], gb, f"fc bias grad est {e}", 1e-4)
+    (gpool,) = torch.autograd.grad(ce.sum(), pooled)
+    dtop = _d(cap["dtop"]).view(N, 16, 512)
+    _close_bf16(dtop, (gpool / 16).unsqueeze(1).expand(N, 16, 512), "head dx")
+    # last block, conv b: g = dtop [out > 0]; BN backward with the EST's own statistics; dW_e
+    a, b = job.convs[-2], job.convs[-1]
+    z = _d(cap[f"z_{b.name}"]).view(E, B * 16, 512)
+    mean, rstd = _d(cap[f"mean_{b.name}"]).view(E, 1, 512), _d(cap[f"rstd_{b.name}"]).view(E, 1, 512)
+    gmask = (dtop * (top > 0)).view(E, B * 16, 512)
+    xh = (z - mean) * rstd
+    gam = _d(P0[job.off[b.name][1]:job.off[b.name][1] + 512])
+    R = B * 16
+    dz = gam * rstd * (gmask - gmask.sum(1, keepdim=True) / R - xh * (gmask * xh).sum(1, keepdim=True) / R)
+    ya = _d(cap[f"y_{a.name}"]).view(N, 4, 4, 512).permute(0, 3, 1, 2)
+    col = Fn.unfold(ya, 3, padding=1).view(E, B, 512, 9, 16)  # (ci, tap) x position
+    col = col.permute(0, 1, 4, 3, 2).reshape(E, R, 9 * 512)     # rows (n, pos), columns (tap, ci)
+    dzb = _bf(dz)
+    lo, g0, b0 = job.off[b.name]
+    for e in (0, E - 1):
+        _close(g[e, b0:b0 + 512], gmask[e].sum(0), f"dbeta est {e}", 1e-5)
+        _close(g[e, g0:g0 + 512], (gmask[e] * xh[e]).sum(0), f"dgamma est {e}", 1e-4)
+        _close(g[e, lo:g0], (dzb[e].T @ col[e]).reshape(-1), f"conv dW est {e}", 5e-3)
