@@ -424,6 +424,56 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
             "params_checksum": fnv_one}
 
 
+def bench_resnet(peaks, ests=16, batch=32, steps=10, warmup=3):
+    """C3 (BASELINE.json configs[2]): ResNet-18 with per-EST BatchNorm, 16 ESTs x 32 CIFAR-shaped images
+    (paper_2208_14228_b200/resnet.py).  Throughput with all 16 ESTs on this GPU (CUDA events); the C3
+    schedule itself -- 2 steps on 8 launch groups ("GPUs"), rescale to 4, 2 steps, rescale to 2, 2 steps,
+    per-EST BN statistics and cursors moved by the slot-copy kernel -- checked bit-identical against
+    the uninterrupted run, with the context-switch time of each rescale."""
+    from paper_2208_14228_b200.resnet import ResNetJob
+
+    job = ResNetJob(ests=ests, batch=batch, gpus=1)
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        job.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        losses = job.step()
+    e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    flops = job.flops_per_step()
+    del job
+    torch.cuda.empty_cache()
+    a, b = ResNetJob(ests=ests, batch=batch, gpus=8), ResNetJob(ests=ests, batch=batch, gpus=1)
+    switch_us = []
+    for gpus in (8, 4, 2):
+        if gpus != 8:
+            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            r0.record(s)
+            a.rescale(gpus)
+            r1.record(s)
+            r1.synchronize()
+            switch_us.append(round(r0.elapsed_time(r1) * 1e3, 1))
+        for _ in range(2):
+            a.step()
+            b.step()
+    sa, sb = a.est_state(), b.est_state()
+    same = bool(torch.equal(a.params.view(torch.int32), b.params.view(torch.int32)) and
+                torch.equal(sa["run_mean"].view(torch.int32), sb["run_mean"].view(torch.int32)) and
+                torch.equal(sa["run_var"].view(torch.int32), sb["run_var"].view(torch.int32)))
+    del a, b
+    torch.cuda.empty_cache()
+    return {"workload": "C3: ResNet-18 (CIFAR layout, widths 64-512) with per-EST BatchNorm, 16 ESTs x 32 "
+                        "synthetic 32x32x3 images, softmax CE, momentum SGD (BASELINE.json configs[2])",
+            "samples_per_s": round(ests * batch / (ms / 1e3), 1), "unit": "images/s", "ms_per_step": round(ms, 3),
+            "conv_tflops_step_level": round(flops / ms / 1e9, 1), "loss": round(losses.mean().item(), 5),
+            "rescale_8_4_2": {"schedule": "2 steps @8, rescale, 2 @4, rescale, 2 @2 vs 6 steps @1",
+                              "bit_identical_weights_and_bn_stats": same, "context_switch_us": switch_us}}
+
+
 def cpu_baseline(seconds: float, threads: int = 1):
     """The CPU oracle (C restatement of the reference) on the same C2 workload, bounded in time."""
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -490,7 +540,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-reducer", action="store_true")
-    ap.add_argument("--no-bert", action="store_true", help="skip the C4 BERT-base step measurement")
+    ap.add_argument("--no-bert", action="store_true", help="skip the C3 ResNet-18 and C4 BERT-base step measurements")
     ap.add_argument("--exchange", default="ipc", choices=["ipc", "allgather"],
                     help="N>1: peer-memory reducer over CUDA IPC, or NCCL all-gather of EST slots")
     args = ap.parse_args()
@@ -555,8 +605,10 @@ def main():
     if not args.no_reducer and rank == 0:
         reducer = bench_reducer(flush, peaks)
         gemm = bench_gemm(flush, peaks)
+    resnet = None
     if not args.no_bert and rank == 0:
         bert = bench_bert(peaks)
+        resnet = bench_resnet(peaks)
     clk = clocks.stop()
 
     # Roofline of the step kernel: algorithmic HBM bytes per mini-batch = the 32 rows read
@@ -589,6 +641,8 @@ def main():
         line["gemm"] = gemm
     if bert is not None:
         line["c4_bert"] = bert
+    if resnet is not None:
+        line["c3_resnet"] = resnet
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         v, steps, el, run = cpu_baseline(args.cpu_seconds)
         sys.path.insert(0, str(ROOT / "oracle"))

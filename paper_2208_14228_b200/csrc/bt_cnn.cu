@@ -79,30 +79,38 @@ struct ColArgs {
   __nv_bfloat16* col;
   int N, Hs, Ws, C, Ho, Wo, KH, KW, s, p, transposed;
 };
-__global__ void __launch_bounds__(256) im2col_kernel(const ColArgs a) {
-  const int cg = a.C / 8, K8 = a.KH * a.KW * cg;
-  const int64_t n = (int64_t)a.N * a.Ho * a.Wo * K8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int k8 = (int)(i % K8);
-    const int64_t r = i / K8;
-    const int wo = (int)(r % a.Wo), ho = (int)((r / a.Wo) % a.Ho), img = (int)(r / ((int64_t)a.Wo * a.Ho));
-    const int c8 = k8 % cg, t = k8 / cg, kw = t % a.KW, kh = t / a.KW;
-    int hi, wi;
-    bool ok;
-    if (!a.transposed) {
-      hi = ho * a.s - a.p + kh;
-      wi = wo * a.s - a.p + kw;
-      ok = true;
-    } else {
-      const int hn = ho + a.p - kh, wn = wo + a.p - kw;
-      ok = hn >= 0 && wn >= 0 && hn % a.s == 0 && wn % a.s == 0;
-      hi = hn / a.s;
-      wi = wn / a.s;
+// One warp per output row (its (image, ho, wo) decoded once); lanes walk the row's K8 16-byte
+// chunks -- coalesced stores, contiguous 16-byte reads per tap -- with shift/mask decoding (C/8 a
+// power of two, KW in {1, 3}): the kernel is store-bandwidth-bound rather than integer-bound.
+__global__ void __launch_bounds__(256) im2col_kernel(const ColArgs a, int lcg) {
+  const int cg = 1 << lcg, K8 = a.KH * a.KW * cg;
+  const int rows = a.N * a.Ho * a.Wo, HoWo = a.Ho * a.Wo;
+  const int lane = threadIdx.x & 31;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+    const int img = r / HoWo, pix = r - img * HoWo;
+    const int ho = pix / a.Wo, wo = pix - ho * a.Wo;
+    const __nv_bfloat16* src = a.src + (size_t)img * a.Hs * a.Ws * a.C;
+    uint4* dst = (uint4*)(a.col + (size_t)r * K8 * 8);
+    for (int k8 = lane; k8 < K8; k8 += 32) {
+      const int t = k8 >> lcg, c8 = k8 & (cg - 1);
+      const int kh = a.KW == 3 ? (t * 11) >> 5 : t, kw = t - kh * a.KW;  // t / 3 for t < 9
+      int hi, wi;
+      bool ok;
+      if (!a.transposed) {
+        hi = ho * a.s - a.p + kh;
+        wi = wo * a.s - a.p + kw;
+        ok = true;
+      } else {
+        const int hn = ho + a.p - kh, wn = wo + a.p - kw;
+        ok = hn >= 0 && wn >= 0 && ((hn | wn) & (a.s - 1)) == 0;  // s in {1, 2}
+        hi = hn >> (a.s - 1);
+        wi = wn >> (a.s - 1);
+      }
+      ok = ok && hi >= 0 && hi < a.Hs && wi >= 0 && wi < a.Ws;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (ok) v = *(const uint4*)(src + ((size_t)hi * a.Ws + wi) * a.C + c8 * 8);
+      dst[k8] = v;
     }
-    ok = ok && hi >= 0 && hi < a.Hs && wi >= 0 && wi < a.Ws;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (ok) v = *(const uint4*)(a.src + (((size_t)img * a.Hs + hi) * a.Ws + wi) * a.C + c8 * 8);
-    *(uint4*)(a.col + r * (size_t)(K8 * 8) + (size_t)k8 * 8) = v;
   }
 }
 
@@ -226,13 +234,14 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(const __nv_bfloat16* __re
                                                        int C, int R, int64_t rows, int relu,
                                                        __nv_bfloat16* __restrict__ y) {
   const int cg = C / 8;
-  const int64_t n = rows * cg;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / cg;
-    const int c0 = (int)(i - row * cg) * 8, e = (int)(row / R);
+  const int n = (int)(rows * cg);  // < 2^31 (launcher)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int row = i / cg;
+    const int c0 = (i - row * cg) * 8, e = row / R;
     float zv[8], o[8], rv[8];
-    ld8(z + row * C + c0, zv);
-    if (res) ld8(res + row * C + c0, rv);
+    const size_t off = (size_t)row * C + c0;
+    ld8(z + off, zv);
+    if (res) ld8(res + off, rv);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int c = c0 + q;
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(const __nv_bfloat16* __re
       if (res) v += rv[q];
       o[q] = (relu && !(v > 0.f)) ? 0.f : v;
     }
-    st8(y + row * C + c0, o);
+    st8(y + off, o);
   }
 }
 
@@ -253,15 +262,16 @@ __global__ void __launch_bounds__(256) bn_bwd_kernel(const __nv_bfloat16* __rest
                                                      const float* __restrict__ gamma, int C, int R, int64_t rows,
                                                      __nv_bfloat16* __restrict__ dz) {
   const int cg = C / 8;
-  const int64_t n = rows * cg;
+  const int n = (int)(rows * cg);  // < 2^31 (launcher)
   const float invR = 1.f / (float)R;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / cg;
-    const int c0 = (int)(i - row * cg) * 8, e = (int)(row / R);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int row = i / cg;
+    const int c0 = (i - row * cg) * 8, e = row / R;
     float zv[8], dv[8], yv[8], o[8];
-    ld8(z + row * C + c0, zv);
-    ld8(dy + row * C + c0, dv);
-    ld8(y + row * C + c0, yv);
+    const size_t off = (size_t)row * C + c0;
+    ld8(z + off, zv);
+    ld8(dy + off, dv);
+    ld8(y + off, yv);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const size_t ec = (size_t)e * C + c0 + q;
@@ -269,7 +279,7 @@ __global__ void __launch_bounds__(256) bn_bwd_kernel(const __nv_bfloat16* __rest
       const float xh = (zv[q] - mean[ec]) * rstd[ec];
       o[q] = gamma[c0 + q] * rstd[ec] * (g - sg[ec] * invR - xh * (sgx[ec] * invR));
     }
-    st8(dz + row * C + c0, o);
+    st8(dz + off, o);
   }
 }
 
@@ -404,9 +414,15 @@ int cnn_data_launch(uint64_t seed, const int64_t* cursor, int est_base, int E, i
 int cnn_im2col_launch(const void* src, void* col, int N, int Hs, int Ws, int C, int Ho, int Wo, int KH, int KW,
                       int stride, int pad, int transposed, cudaStream_t s) {
   if (C % 8) return ERR_INPUT;
+  const int cg = C / 8;
+  if ((int64_t)N * Ho * Wo >= (int64_t)1 << 31 || (cg & (cg - 1)) || (KW != 1 && KW != 3) || KH > 3 ||
+      (stride != 1 && stride != 2))
+    return ERR_INPUT;
+  int lcg = 0;
+  while ((1 << lcg) < cg) ++lcg;
   const cnn::ColArgs a{(const __nv_bfloat16*)src, (__nv_bfloat16*)col, N, Hs, Ws, C, Ho, Wo, KH, KW, stride, pad,
                        transposed};
-  cnn::im2col_kernel<<<grid_n((int64_t)N * Ho * Wo * KH * KW * (C / 8)), 256, 0, s>>>(a);
+  cnn::im2col_kernel<<<grid_n((int64_t)N * Ho * Wo * 32), 256, 0, s>>>(a, lcg);
   return ok_or_cuda_c();
 }
 
@@ -453,6 +469,7 @@ int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, 
 int cnn_bn_apply_launch(const void* z, const void* res, const float* mean, const float* rstd, const float* gamma,
                         const float* beta, int E, int R, int C, int relu, void* y, cudaStream_t s) {
   const int64_t rows = (int64_t)E * R;
+  if (rows * C / 8 >= (int64_t)1 << 31) return ERR_INPUT;
   cnn::bn_apply_kernel<<<grid_n(rows * C / 8), 256, 0, s>>>((const __nv_bfloat16*)z, (const __nv_bfloat16*)res, mean,
                                                            rstd, gamma, beta, C, R, rows, relu, (__nv_bfloat16*)y);
   return ok_or_cuda_c();
@@ -462,6 +479,7 @@ int cnn_bn_bwd_launch(const void* z, const void* dy, const void* y, const float*
                       const float* sg, const float* sgx, const float* gamma, int E, int R, int C, void* dz,
                       cudaStream_t s) {
   const int64_t rows = (int64_t)E * R;
+  if (rows * C / 8 >= (int64_t)1 << 31) return ERR_INPUT;
   cnn::bn_bwd_kernel<<<grid_n(rows * C / 8), 256, 0, s>>>((const __nv_bfloat16*)z, (const __nv_bfloat16*)dy,
                                                          (const __nv_bfloat16*)y, mean, rstd, sg, sgx, gamma, C, R,
                                                          rows, (__nv_bfloat16*)dz);

@@ -194,15 +194,16 @@ class ResNetJob:
             return ws
         B = self.B
         bf, f32 = dict(dtype=torch.bfloat16, device="cuda"), dict(dtype=torch.float32, device="cuda")
-        col = 0
+        col = 0  # the transposed-convolution gather (dX)
         for cv in self.convs:
-            col = max(col, n * B * cv.hout ** 2 * cv.K, n * B * cv.hin ** 2 * cv.taps * cv.co)
+            col = max(col, n * B * cv.hin ** 2 * cv.taps * cv.co)
         ws = {"img": torch.empty(n * B * 1024 * 8, **bf), "labels": torch.empty(n * B, dtype=torch.int32, device="cuda"),
               "col": torch.empty(col, **bf), "loss": torch.empty(n, **f32)}
         for cv in self.convs:
             R = n * B * cv.hout ** 2
             ws[cv.name] = {"z": torch.empty(R * cv.co, **bf), "y": torch.empty(R * cv.co, **bf),
-                           "mean": torch.empty(n * cv.co, **f32), "rstd": torch.empty(n * cv.co, **f32)}
+                           "mean": torch.empty(n * cv.co, **f32), "rstd": torch.empty(n * cv.co, **f32),
+                           "col": torch.empty(R * cv.K, **bf)}  # forward im2col, kept for the dW product
         big = max(n * B * cv.hin ** 2 * max(cv.ci, cv.co) for cv in self.convs)
         ws["g"] = [torch.empty(big, **bf) for _ in range(4)]
         ws["sg"] = torch.empty(n * 512, **f32)
@@ -216,9 +217,10 @@ class ResNetJob:
     def _conv_fwd(self, ws, cv, x, n, z):
         L, s = _native.lib(), stream()
         R = n * self.B * cv.hout ** 2
-        _native.check(L.bt_cnn_im2col(x.data_ptr(), ws["col"].data_ptr(), n * self.B, cv.hin, cv.hin, cv.ci, cv.hout,
+        col = ws[cv.name]["col"]
+        _native.check(L.bt_cnn_im2col(x.data_ptr(), col.data_ptr(), n * self.B, cv.hin, cv.hin, cv.ci, cv.hout,
                                       cv.hout, cv.k, cv.k, cv.s, cv.p, 0, s), "im2col")
-        _native.check(L.bt_gemm_bf16_ex(ws["col"].data_ptr(), self.wb.data_ptr() + 2 * self.woff[cv.name], z.data_ptr(),
+        _native.check(L.bt_gemm_bf16_ex(col.data_ptr(), self.wb.data_ptr() + 2 * self.woff[cv.name], z.data_ptr(),
                                         1, R, cv.co, cv.K, 0, 0, 0, 1, None, 0, 0, s), "conv gemm")
 
     def _bn_fwd(self, ws, cv, n, gslot, res=None, relu=True, out=None):
@@ -255,12 +257,11 @@ class ResNetJob:
                                       self.params.data_ptr() + 4 * g0, n, Re, cv.co, dz.data_ptr(), s), "bn backward")
 
     def _conv_bwd(self, ws, cv, n, base, x, dz, dx):
-        """dW_e (into each EST's gradient slot) and, if dx is given, the input gradient."""
+        """dW_e from the forward's im2col (into each EST's gradient slot) and, if dx is given, the input
+        gradient (transposed-convolution gather + GEMM)."""
         L, s, B = _native.lib(), stream(), self.B
         Re = B * cv.hout ** 2
-        _native.check(L.bt_cnn_im2col(x.data_ptr(), ws["col"].data_ptr(), n * B, cv.hin, cv.hin, cv.ci, cv.hout,
-                                      cv.hout, cv.k, cv.k, cv.s, cv.p, 0, s), "im2col")
-        _native.check(L.bt_gemm_bf16_ex(dz.data_ptr(), ws["col"].data_ptr(),
+        _native.check(L.bt_gemm_bf16_ex(dz.data_ptr(), ws[cv.name]["col"].data_ptr(),
                                         self.grads.data_ptr() + 4 * (base * self.P + self.off[cv.name][0]), n, cv.co,
                                         cv.K, Re, Re * cv.co, Re * cv.K, self.P, 0, None, 1, 0, s), "conv dW gemm")
         if dx is not None:
