@@ -107,10 +107,11 @@ int bt_sgd_step_f64(const double *params_dev, const double *vel_dev, const doubl
 
 /* ---------------- deterministic tensor-core GEMM (C3/C4 model stack) ------
  * C[M][N] = A[M][K] * B[N][K]^T, bf16 inputs (K contiguous), fp32 accumulate
- * in TMEM, C fp32 (out_dtype 0) or bf16 (1).  tcgen05 + TMA, one CTA per
- * output tile, fixed K order: the bits depend only on the inputs and the
- * shape, never on `grid` (0 = one CTA per SM) or the GPU.  Requires
- * M % 128 == 0, N % 128 == 0, K % 64 == 0, 16-byte aligned pointers.
+ * in TMEM, C fp32 (out_dtype 0) or bf16 (1).  tcgen05 + TMA, one CTA (pair)
+ * per output tile, fixed K order: the bits depend only on the inputs and the
+ * shape, never on `grid` (0 = one CTA per SM) or the GPU.  Ragged M / N / K
+ * are zero-filled by the TMA loads and clipped by the TMA stores; rows must be
+ * 16-byte aligned (K % 8 == 0, N % 8 == 0), pointers 16-byte aligned.
  *                                         analogue of model.py:141-192's dense products */
 int bt_gemm_bf16_tn(const void *a_dev, const void *b_dev, void *c_dev, int32_t M, int32_t N, int32_t K,
                     int32_t out_dtype, int32_t grid, void *stream);
