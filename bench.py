@@ -424,6 +424,45 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
             "params_checksum": fnv_one}
 
 
+def bench_bert_dist(rank, world, dist, ests=32, steps=5, warmup=3):
+    """C4 on N GPUs: rank r holds ESTs [r*E/N, (r+1)*E/N) and exchanges through the peer-memory reducer
+    (RankTree(2): subtree partials + NVLink owner fold, fused /E + SGD, updated shards stored into every
+    replica).  Step time = max over ranks (CUDA events); replicas must agree bitwise."""
+    from paper_2208_14228_b200.bert import BertJob
+
+    n = ests // world
+    job = BertJob(ests=ests, est_base=rank * n, est_count=n, fanin=2)
+    job.attach_peer()
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        job.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        job.step()
+    e1.record(s)
+    e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    chk = torch.tensor([float(job.params.view(torch.int32).to(torch.int64).sum().item())], dtype=torch.float64,
+                       device="cuda")
+    lo, hi = chk.clone(), chk.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+    torch.cuda.synchronize()
+    dist.barrier()
+    job.peer.close()
+    del job
+    torch.cuda.empty_cache()
+    return {"workload": "C4: BERT-base encoder bf16, 32 ESTs x 8 sequences, EST blocks per GPU, peer-memory "
+                        "RankTree(2) reducer (BASELINE.json configs[3])",
+            "samples_per_s": round(ests * 8 / (ms / 1e3), 1), "unit": "sequences/s", "ms_per_step": round(ms, 3),
+            "n_gpus": world, "ests_per_gpu": n, "replicas_bit_identical": bool(lo.item() == hi.item())}
+
+
 def bench_resnet(peaks, ests=16, batch=32, steps=10, warmup=3):
     """C3 (BASELINE.json configs[2]): ResNet-18 with per-EST BatchNorm, 16 ESTs x 32 CIFAR-shaped images
     (paper_2208_14228_b200/resnet.py).  Throughput with all 16 ESTs on this GPU (CUDA events); the C3
@@ -606,9 +645,14 @@ def main():
         reducer = bench_reducer(flush, peaks)
         gemm = bench_gemm(flush, peaks)
     resnet = None
-    if not args.no_bert and rank == 0:
+    if not args.no_bert and world == 1:
         bert = bench_bert(peaks)
         resnet = bench_resnet(peaks)
+    elif not args.no_bert:
+        try:
+            bert = bench_bert_dist(rank, world, dist)
+        except Exception as exc:  # keep the headline line if the model-stack leg fails on this box
+            bert = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     clk = clocks.stop()
 
     # Roofline of the step kernel: algorithmic HBM bytes per mini-batch = the 32 rows read

@@ -54,7 +54,10 @@ class BertJob:
 
     def __init__(self, ests: int, seqs: int = 8, layers: int = 12, d_model: int = 768, heads: int = 12,
                  d_ff: int = 3072, seed: int = 42, lr: float = 1e-3, momentum: float = 0.9, p_hidden: float = 0.1,
-                 p_attn: float = 0.1, fanin: int = 0, eps: float = 1e-12):
+                 p_attn: float = 0.1, fanin: int = 0, eps: float = 1e-12, est_base: int = 0,
+                 est_count: int | None = None):
+        """`est_base` / `est_count`: this process computes ESTs [est_base, est_base + est_count) of the E
+        (one rank of a multi-GPU job, `attach_peer`); default all E."""
         require_cuda()
         if heads * 64 != d_model or d_model % 256 or d_model > 1024 or d_ff % 256:
             raise ConfigError("d_model = 64 * heads, a multiple of 256 (<= 1024); d_ff a multiple of 256")
@@ -65,6 +68,10 @@ class BertJob:
         if seqs < 1 or layers < 1:
             raise ConfigError("seqs and layers must be >= 1")
         self.E, self.S, self.L, self.D, self.H, self.F = ests, seqs, layers, d_model, heads, d_ff
+        self.est0, self.En = est_base, ests if est_count is None else est_count
+        if self.est0 < 0 or self.En < 1 or self.est0 + self.En > ests:
+            raise ConfigError(f"local EST block [{est_base}, +{est_count}) outside the {ests} ESTs")
+        self.peer = None
         self.Te = seqs * 128
         self.seed, self.lr, self.mu, self.fanin = seed, lr, momentum, fanin
         self.ph, self.pa, self.eps = p_hidden, p_attn, eps
@@ -90,7 +97,7 @@ class BertJob:
             self.view(l, "g1").fill_(1.0)
             self.view(l, "g2").fill_(1.0)
         self.vel = torch.zeros_like(self.params)
-        self.grads = torch.empty(ests, self.P, dtype=torch.float32, device="cuda")
+        self.grads = torch.empty(self.En, self.P, dtype=torch.float32, device="cuda")  # this rank's EST slots
         # bf16 operand copies: W [out][in] (forward) and W^T [in][out] (dX products)
         self._moff = []
         m = 0
@@ -180,9 +187,11 @@ class BertJob:
         _native.check(_native.lib().bt_gemm_bf16_ex(dy, x, dst, n, rows_out, cols_in, Te, rows_out * Te, cols_in * Te,
                                                      self.P, 0, None, 1, 0, stream()), "bert weight-gradient gemm")
 
-    def _group(self, base: int, n: int, losses: torch.Tensor, capture: dict | None = None):
-        """Forward/backward of ESTs [base, base+n): per-EST gradients into grads[base:base+n]."""
+    def _group(self, lb: int, n: int, losses: torch.Tensor, capture: dict | None = None):
+        """Forward/backward of local ESTs [lb, lb+n) (global ranks est0 + lb ...): per-EST gradients into
+        grads[lb:lb+n]; every random draw keyed by the GLOBAL rank."""
         L, s = _native.lib(), stream()
+        base = self.est0 + lb
         D, F, H, Te, T, NL = self.D, self.F, self.H, self.Te, n * self.Te, self.L
         seed, step = self.seed & (2**64 - 1), self.step_idx
         ws = self._workspace(n)
@@ -219,7 +228,7 @@ class BertJob:
         # gradients between GEMMs bf16 (A: into LN2', Db: into LN1'), residual-path gradients fp32 (B, Cb)
         (A, Db), (B, Cb) = ws["dy1"], ws["dres"]
         _native.check(L.bt_bert_mse(x32.data_ptr(), ws["tgt"].data_ptr(), n, Te, D, A.data_ptr(),
-                                    ws["msepart"].data_ptr(), losses[base:].data_ptr(), s))
+                                    ws["msepart"].data_ptr(), losses[lb:].data_ptr(), s))
         if capture is not None:
             capture.update(ytop=x32.clone(), tgt=ws["tgt"].clone())
         dy2 = None
@@ -231,34 +240,34 @@ class BertJob:
             _native.check(L.bt_bert_ln_bwd(A.data_ptr(), None if dy2 is None else dy2.data_ptr(), w["hs2"].data_ptr(),
                                            w["st2"].data_ptr(), self._p(l, "g2"), Cb.data_ptr(), ws["dbr"].data_ptr(),
                                            part, n, Te, D, base, NL, l, 1, seed, step, self.ph, s), "layernorm 2'")
-            _native.check(L.bt_bert_ln_fold(part, n, Te, D, self._g(base, l, "g2"), self._g(base, l, "be2"),
-                                            self._g(base, l, "b2"), self.P, s))
+            _native.check(L.bt_bert_ln_fold(part, n, Te, D, self._g(lb, l, "g2"), self._g(lb, l, "be2"),
+                                            self._g(lb, l, "b2"), self.P, s))
             if capture is not None and l == 0:
                 capture.update(dg=Cb.clone(), do=ws["dbr"].clone())
             _native.check(L.bt_gemm_bf16_ffn(ws["dbr"].data_ptr(), self._wt(l, "W2"), ws["dHpre"].data_ptr(), T, F, D,
                                              2, None, w["Hpre"].data_ptr(), None, seed, step, base, Te, 0.0, 0, s),
                           "ffn backward GEMM")
             self._gemm(ws["dHpre"].data_ptr(), self._wt(l, "W1"), Db.data_ptr(), T, D, F, out_bf16=True)
-            self._wgrad(ws, n, ws["dbr"].data_ptr(), w["Dact"].data_ptr(), D, F, self._g(base, l, "W2"))
-            self._wgrad(ws, n, ws["dHpre"].data_ptr(), w["h1b"].data_ptr(), F, D, self._g(base, l, "W1"))
-            _native.check(L.bt_colsum_bf16_strided(ws["dHpre"].data_ptr(), n, Te, F, self._g(base, l, "b1"), self.P,
+            self._wgrad(ws, n, ws["dbr"].data_ptr(), w["Dact"].data_ptr(), D, F, self._g(lb, l, "W2"))
+            self._wgrad(ws, n, ws["dHpre"].data_ptr(), w["h1b"].data_ptr(), F, D, self._g(lb, l, "W1"))
+            _native.check(L.bt_colsum_bf16_strided(ws["dHpre"].data_ptr(), n, Te, F, self._g(lb, l, "b1"), self.P,
                                                    ws["colsum"].data_ptr(), s))
             if capture is not None and l == 0:
                 capture.update(dHpre=ws["dHpre"].clone(), dh1=Db.clone())
             _native.check(L.bt_bert_ln_bwd(Db.data_ptr(), Cb.data_ptr(), w["hs1"].data_ptr(), w["st1"].data_ptr(),
                                            self._p(l, "g1"), B.data_ptr(), ws["dbr"].data_ptr(), part, n, Te, D, base,
                                            NL, l, 0, seed, step, self.ph, s), "layernorm 1'")
-            _native.check(L.bt_bert_ln_fold(part, n, Te, D, self._g(base, l, "g1"), self._g(base, l, "be1"),
-                                            self._g(base, l, "bo"), self.P, s))
+            _native.check(L.bt_bert_ln_fold(part, n, Te, D, self._g(lb, l, "g1"), self._g(lb, l, "be1"),
+                                            self._g(lb, l, "bo"), self.P, s))
             self._gemm(ws["dbr"].data_ptr(), self._wt(l, "Wo"), ws["dctx"].data_ptr(), T, D, D, out_bf16=True)
-            self._wgrad(ws, n, ws["dbr"].data_ptr(), w["ctx"].data_ptr(), D, D, self._g(base, l, "Wo"))
+            self._wgrad(ws, n, ws["dbr"].data_ptr(), w["ctx"].data_ptr(), D, D, self._g(lb, l, "Wo"))
             _native.check(L.bt_bert_attn(1, w["qkv"].data_ptr(), ws["dctx"].data_ptr(), ws["dqkv"].data_ptr(), n, Te,
                                          D, H, base, NL, l, seed, step, self.pa, s), "attention backward")
             if capture is not None and l == 0:
                 capture.update(dh=B.clone(), da=ws["dbr"].clone(), dctx=ws["dctx"].clone(), dqkv=ws["dqkv"].clone())
             self._gemm(ws["dqkv"].data_ptr(), self._wt(l, "Wqkv"), A.data_ptr(), T, D, 3 * D, out_bf16=True)
-            self._wgrad(ws, n, ws["dqkv"].data_ptr(), w["xb"].data_ptr(), 3 * D, D, self._g(base, l, "Wqkv"))
-            _native.check(L.bt_colsum_bf16_strided(ws["dqkv"].data_ptr(), n, Te, 3 * D, self._g(base, l, "bqkv"),
+            self._wgrad(ws, n, ws["dqkv"].data_ptr(), w["xb"].data_ptr(), 3 * D, D, self._g(lb, l, "Wqkv"))
+            _native.check(L.bt_colsum_bf16_strided(ws["dqkv"].data_ptr(), n, Te, 3 * D, self._g(lb, l, "bqkv"),
                                                    self.P, ws["colsum"].data_ptr(), s))
             dy2 = B
         if capture is not None:
@@ -266,12 +275,12 @@ class BertJob:
 
     # ------------------------------------------------------------------ step
     def step(self, groups: list[int] | None = None, capture: dict | None = None) -> torch.Tensor:
-        """One mini-batch of all E ESTs; `groups` = EST counts per launch group (default: one group).
-        Returns the per-EST losses [E] (fp32, on device)."""
-        groups = groups or [self.E]
-        if sum(groups) != self.E or min(groups) < 1:
-            raise ConfigError(f"groups {groups} must partition {self.E} ESTs")
-        losses = torch.empty(self.E, dtype=torch.float32, device="cuda")
+        """One mini-batch of this process's ESTs; `groups` = EST counts per launch group (default: one group).
+        Returns the local per-EST losses [est_count] (fp32, on device)."""
+        groups = groups or [self.En]
+        if sum(groups) != self.En or min(groups) < 1:
+            raise ConfigError(f"groups {groups} must partition {self.En} ESTs")
+        losses = torch.empty(self.En, dtype=torch.float32, device="cuda")
         base = 0
         for n in groups:
             self._group(base, n, losses, capture if len(groups) == 1 else None)
@@ -283,8 +292,28 @@ class BertJob:
         self._refresh_bf16()
         return losses
 
+    def attach_peer(self, group=None):
+        """Multi-GPU (one process per GPU, torch.distributed initialised, rank r holding the r-th contiguous
+        EST block): the exchange becomes paper_2208_14228_b200.peer.PeerGroupReducer over CUDA IPC --
+        Tree(2): each rank's subtree partial, then the owner of each parameter shard folds the G partials
+        with NVLink peer loads (the same association as the flat tree); Sequential: the owner reads all E
+        slots in rank order.  Fused /E + momentum SGD, updated shard stored into every replica."""
+        from .hier import RankBuffers
+        from .peer import PeerGroupReducer
+
+        loc = RankBuffers(self.grads, self.params, self.vel, torch.cuda.current_stream())
+        self.peer = PeerGroupReducer(loc, self.E, "rank_tree2" if self.fanin == 2 else "sequential", None, self.lr,
+                                     self.mu, group)
+
     def _reduce_update(self):
-        """Fixed EST-rank-order sum of the E gradient slots, /E, momentum SGD: one launch over all P."""
+        """Fixed EST-rank-order sum of the E gradient slots, /E, momentum SGD: one launch over all P
+        (or, across processes, the peer-memory reducer)."""
+        if self.peer is not None:
+            self.peer.step()
+            self.peer.check()
+            return
+        if self.En != self.E:
+            raise ConfigError("a partial EST block needs attach_peer() for the exchange")
         a = _native.ReduceArgs()
         a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, self.E, self.fanin, self.P
         for k in range(self.E):
@@ -302,9 +331,9 @@ class BertJob:
     def gemm_flops_per_step(self) -> float:
         """Dense-layer flops: forward 2*T*P_w, backward dX + dW 4*T*P_w (P_w = weight-matrix params)."""
         pw = sum(int(torch.Size(self.shapes[k]).numel()) for k in _MATS) * self.L
-        return 6.0 * self.E * self.Te * pw
+        return 6.0 * self.En * self.Te * pw
 
     def attn_flops_per_step(self) -> float:
         """QK^T and PV: 4*128*128*64 per (sequence, head) forward; backward recomputes S (+1) and does 4 more."""
         per = 4 * 128 * 128 * 64 / 2  # one 128x128x64 product = 2*128*128*64 flops
-        return (2 + 5) * per * self.E * self.S * self.H * self.L
+        return (2 + 5) * per * self.En * self.S * self.H * self.L
