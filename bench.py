@@ -424,14 +424,15 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
             "params_checksum": fnv_one}
 
 
-def bench_bert_dist(rank, world, dist, ests=32, steps=5, warmup=3):
+def bench_bert_dist(rank, world, dist, ests=32, steps=5, warmup=3, **model):
     """C4 on N GPUs: rank r holds ESTs [r*E/N, (r+1)*E/N) and exchanges through the peer-memory reducer
     (RankTree(2): subtree partials + NVLink owner fold, fused /E + SGD, updated shards stored into every
     replica).  Step time = max over ranks (CUDA events); replicas must agree bitwise."""
     from paper_2208_14228_b200.bert import BertJob
 
     n = ests // world
-    job = BertJob(ests=ests, est_base=rank * n, est_count=n, fanin=2)
+    job = BertJob(ests=ests, est_base=rank * n, est_count=n, fanin=2, **model)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"  # gloo: host tensors (tests)
     job.attach_peer()
     s = torch.cuda.current_stream()
     for _ in range(warmup):
@@ -444,11 +445,11 @@ def bench_bert_dist(rank, world, dist, ests=32, steps=5, warmup=3):
         job.step()
     e1.record(s)
     e1.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device="cuda")
+    t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = t.item()
     chk = torch.tensor([float(job.params.view(torch.int32).to(torch.int64).sum().item())], dtype=torch.float64,
-                       device="cuda")
+                       device=dev)
     lo, hi = chk.clone(), chk.clone()
     dist.all_reduce(lo, op=dist.ReduceOp.MIN)
     dist.all_reduce(hi, op=dist.ReduceOp.MAX)
@@ -459,8 +460,8 @@ def bench_bert_dist(rank, world, dist, ests=32, steps=5, warmup=3):
     torch.cuda.empty_cache()
     return {"workload": "C4: BERT-base encoder bf16, 32 ESTs x 8 sequences, EST blocks per GPU, peer-memory "
                         "RankTree(2) reducer (BASELINE.json configs[3])",
-            "samples_per_s": round(ests * 8 / (ms / 1e3), 1), "unit": "sequences/s", "ms_per_step": round(ms, 3),
-            "n_gpus": world, "ests_per_gpu": n, "replicas_bit_identical": bool(lo.item() == hi.item())}
+            "samples_per_s": round(ests * model.get("seqs", 8) / (ms / 1e3), 1), "unit": "sequences/s",
+            "ms_per_step": round(ms, 3), "n_gpus": world, "ests_per_gpu": n, "replicas_bit_identical": bool(lo.item() == hi.item())}
 
 
 def bench_resnet(peaks, ests=16, batch=32, steps=10, warmup=3):

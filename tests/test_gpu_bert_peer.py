@@ -87,3 +87,50 @@ def test_two_process_bert_matches_one_process(fanin):
         for step in range(3):
             got = np.frombuffer(res[r][1][step], dtype=np.float32)
             assert got.tobytes() == ref_losses[step][2 * r:2 * r + 2].tobytes(), (r, step)
+
+
+def _bench_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root))
+    import torch.distributed as dist
+
+    import bench
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        out = bench.bench_bert_dist(rank, world, dist, ests=4, steps=2, warmup=1, seqs=1, layers=2, d_model=256,
+                                    heads=4, d_ff=512)
+        q.put((rank, out))
+    except Exception:
+        import traceback
+
+        q.put((rank, {"error": traceback.format_exc()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_multi_gpu_c4_leg():
+    """bench.py's N>1 C4 leg (what the driver's scaling run executes), on 2 processes here."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        outs = [q.get(timeout=240) for _ in procs]
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for r, out in outs:
+        assert "error" not in out, out
+        assert out["replicas_bit_identical"] and out["ests_per_gpu"] == 2 and out["samples_per_s"] > 0
