@@ -36,7 +36,10 @@ namespace bt {
 namespace gemm {
 
 constexpr int BM = 128, BK = 64, UK = 16;  // tile M, k-block (128 B of bf16), UMMA K
-constexpr int EPI_WARPS = 16;  // four per TMEM lane group, each draining a quarter of the tile's columns
+#ifndef BT_EPI_WARPS
+#define BT_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = BT_EPI_WARPS;  // EPI_WARPS/4 per TMEM lane group, each draining a column slice
 constexpr int EPI_SPLIT = EPI_WARPS / 4;
 constexpr int THREADS = 64 + 32 * EPI_WARPS;
 
@@ -150,7 +153,7 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sr
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -159,7 +162,8 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // fp32 rows of 128 B (SWIZZLE_128B: 16-byte chunk q of row r at q ^ (r & 7)), bf16 rows of
 // 64 B (SWIZZLE_64B: chunk q at q ^ ((r >> 1) & 3)) -- conflict-free row-per-lane writes;
 // one elected lane then issues a TMA bulk-tensor store (full 128-byte lines to L2/HBM).
-constexpr int EPI_STAGE = 4096;
+constexpr int EPI_BOX = 4096;              // one 32 x 32 staging box (fp32, or two bf16 outputs)
+constexpr int EPI_STAGE = 2 * EPI_BOX;     // double-buffered: chunk i stages in box i & 1
 __device__ __forceinline__ void stage_f32(uint8_t* st, const float* f, int lane) {
 #pragma unroll
   for (int q = 0; q < 8; ++q)
@@ -224,11 +228,11 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
       }
     }
   }
-  if (lane == 0) bulk_wait_read0();  // the previous chunk's store has finished reading the staging box
+  if (lane == 0) bulk_wait_read1();  // the store that last used this box (two chunks ago) has read it
   __syncwarp();
   if (OUT_BF16) {
     stage_bf16(st, f, lane);
-    if (epi.kind == EPI_FFN_FWD) stage_bf16(st + EPI_STAGE / 2, g, lane);
+    if (epi.kind == EPI_FFN_FWD) stage_bf16(st + EPI_BOX / 2, g, lane);
   } else {
     stage_f32(st, f, lane);
   }
@@ -236,7 +240,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
   __syncwarp();
   if (lane == 0) {
     tma_store_3d(mc, su32(st), col, row0, z);
-    if (epi.kind == EPI_FFN_FWD) tma_store_3d(mc2, su32(st + EPI_STAGE / 2), col, row0, z);
+    if (epi.kind == EPI_FFN_FWD) tma_store_3d(mc2, su32(st + EPI_BOX / 2), col, row0, z);
     bulk_commit();
   }
 }
@@ -363,6 +367,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int lg = warp & 3;  // TMEM lane group this warp may access (lanes 32*lg ...)
     const int half = (warp - 2) >> 2;  // which column slice (of EPI_SPLIT)
     uint8_t* const est = gbase + L::EPI + (warp - 2) * EPI_STAGE;
+    int chunk = 0;  // alternates the two staging boxes
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int acc = i & 1;
@@ -386,7 +391,8 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, epi, est, lane, &map_c, &map_c2, row0, t / per_batch);
+        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, epi, est + (chunk++ & 1) * EPI_BOX, lane, &map_c, &map_c2, row0,
+                                  t / per_batch);
       }
       tc_fence_before();
       __syncwarp();
@@ -581,6 +587,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int lg = warp & 3;
     const int half = (warp - 2) >> 2;
     uint8_t* const est = gbase + L::EPI + (warp - 2) * EPI_STAGE;
+    int chunk = 0;
     const uint32_t leader_tempty0 = map_to_rank(tempty(0), 0), leader_tempty1 = map_to_rank(tempty(1), 0);
     int i = 0;
     for (int t = pair; t < tiles; t += pairs, ++i) {
@@ -604,7 +611,8 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, epi, est, lane, &map_c, &map_c2, row0, t / per_batch);
+        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, epi, est + (chunk++ & 1) * EPI_BOX, lane, &map_c, &map_c2, row0,
+                                  t / per_batch);
       }
       tc_fence_before();
       __syncwarp();
@@ -777,13 +785,15 @@ static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests
 // edges are zero-filled by the TMA loads and clipped by the TMA stores (all deterministic)
 template <bool MN>
 static int launch_any(const GemmShape& g, int out_bf16, int grid, cudaStream_t s) {
+  constexpr int SP = gemm::EPI_WARPS == 8 ? 5 : 3, S256 = gemm::EPI_WARPS == 8 ? 3 : 2,
+                S64 = gemm::EPI_WARPS == 8 ? 6 : 4, S128 = gemm::EPI_WARPS == 8 ? 5 : 3;
   if (g.M % 256 == 0 && g.N % 256 == 0 && gemm_variant() != 1)
-    return out_bf16 ? launch_gemm_pair<5, true, MN>(g, grid, s) : launch_gemm_pair<5, false, MN>(g, grid, s);
+    return out_bf16 ? launch_gemm_pair<SP, true, MN>(g, grid, s) : launch_gemm_pair<SP, false, MN>(g, grid, s);
   if (g.N % 256 == 0)
-    return out_bf16 ? launch_gemm<256, 3, true, MN>(g, grid, s) : launch_gemm<256, 3, false, MN>(g, grid, s);
+    return out_bf16 ? launch_gemm<256, S256, true, MN>(g, grid, s) : launch_gemm<256, S256, false, MN>(g, grid, s);
   if (g.N <= 64)  // narrow outputs (64-channel convolutions)
-    return out_bf16 ? launch_gemm<64, 6, true, MN>(g, grid, s) : launch_gemm<64, 6, false, MN>(g, grid, s);
-  return out_bf16 ? launch_gemm<128, 5, true, MN>(g, grid, s) : launch_gemm<128, 5, false, MN>(g, grid, s);
+    return out_bf16 ? launch_gemm<64, S64, true, MN>(g, grid, s) : launch_gemm<64, S64, false, MN>(g, grid, s);
+  return out_bf16 ? launch_gemm<128, S128, true, MN>(g, grid, s) : launch_gemm<128, S128, false, MN>(g, grid, s);
 }
 int gemm_bf16_launch_any(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                          int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, bool mn, cudaStream_t s) {
