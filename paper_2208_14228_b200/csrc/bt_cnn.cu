@@ -117,13 +117,14 @@ __global__ void __launch_bounds__(256) im2col_kernel(const ColArgs a, int lcg) {
 // ---------------------------------------------------------------- BatchNorm
 // Column statistics per EST over fixed CHUNK-row chunks: block = (chunk k, local EST e);
 // thread = (row lane, 8-channel group); rows walked in order, lanes combined in lane order.
-//   mode 0: sum z                      mode 1: sum (z - mean)^2
+//   mode 0: sum (z - k), sum (z - k)^2   (one pass; k = the EST's first row, a per-channel shift
+//           that keeps the variance free of cancellation)
 //   mode 2: sum g, sum g * xhat         (g = dy * [y > 0], xhat = (z - mean) * rstd)
 struct StatArgs {
   const __nv_bfloat16* z;     // conv output (pre-BN)
   const __nv_bfloat16* dy;    // mode 2: gradient of the block/ReLU output
   const __nv_bfloat16* y;     // mode 2: the ReLU output (mask)
-  const float* mean;          // [E][C] (modes 1, 2)
+  const float* mean;          // [E][C] (mode 2)
   const float* rstd;          // [E][C] (mode 2)
   float* part;                // [E][chunks][2][C]
   int C, R, mode;             // R = rows per EST
@@ -136,7 +137,8 @@ __global__ void __launch_bounds__(256) stats_kernel(const StatArgs a) {
   float s0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, s1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   float m[8], r[8];
   if (lane < lanes) {
-    if (a.mode >= 1)
+    if (a.mode == 0) ld8(a.z + (size_t)e * a.R * a.C + c0, m);  // shift k = row 0 of the EST
+    else
       for (int q = 0; q < 8; ++q) m[q] = a.mean[(size_t)e * a.C + c0 + q];
     if (a.mode == 2)
       for (int q = 0; q < 8; ++q) r[q] = a.rstd[(size_t)e * a.C + c0 + q];
@@ -147,12 +149,10 @@ __global__ void __launch_bounds__(256) stats_kernel(const StatArgs a) {
       ld8(a.z + off, zv);
       if (a.mode == 0) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s0[q] += zv[q];
-      } else if (a.mode == 1) {
-#pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float d = zv[q] - m[q];
-          s0[q] += d * d;
+          s0[q] += d;
+          s1[q] += d * d;
         }
       } else {
         float dv[8], yv[8];
@@ -181,14 +181,14 @@ __global__ void __launch_bounds__(256) stats_kernel(const StatArgs a) {
   }
 }
 
-// Fold the chunk partials in chunk order.  mode 0: mean = S/R.  mode 1: var = S/R, rstd, and the
-// EST's running statistics (slot): rm = 0.9 rm + 0.1 mean, rv = 0.9 rv + 0.1 var * R/(R-1).
+// Fold the chunk partials in chunk order.  mode 0: d = S/R, mean = k + d, var = Q/R - d^2, rstd, and
+// the EST's running statistics (slot): rm = 0.9 rm + 0.1 mean, rv = 0.9 rv + 0.1 var * R/(R-1).
 // mode 2: (sum g, sum g*xhat) -> out0 / out1 (and dbeta / dgamma into the EST's gradient slot).
 struct FoldArgs {
   const float* part;
-  float* out0;      // mode 0: mean [E][C]; mode 1: rstd [E][C]; mode 2: sum g [E][C]
-  float* out1;      // mode 2: sum g*xhat [E][C]
-  const float* mean;
+  float* out0;      // mode 0: mean [E][C]; mode 2: sum g [E][C]
+  float* out1;      // mode 0: rstd [E][C]; mode 2: sum g*xhat [E][C]
+  const __nv_bfloat16* z;  // mode 0: the shift rows
   float* run_mean;  // slot [E] x stride
   float* run_var;
   int64_t run_stride;
@@ -209,13 +209,14 @@ __global__ void fold_kernel(const FoldArgs a) {
       s1 += p[(size_t)k * 2 * a.C + a.C];
     }
     if (a.mode == 0) {
-      a.out0[i] = s0 / (float)a.R;
-    } else if (a.mode == 1) {
-      const float var = s0 / (float)a.R;
-      a.out0[i] = 1.f / sqrtf(var + a.eps);
+      const float k = __bfloat162float(a.z[(size_t)e * a.R * a.C + c]);
+      const float d = s0 / (float)a.R;
+      const float mean = k + d, var = fmaxf(s1 / (float)a.R - d * d, 0.f);
+      a.out0[i] = mean;
+      a.out1[i] = 1.f / sqrtf(var + a.eps);
       float* rm = a.run_mean + (size_t)e * a.run_stride + c;
       float* rv = a.run_var + (size_t)e * a.run_stride + c;
-      *rm = 0.9f * *rm + 0.1f * a.mean[i];
+      *rm = 0.9f * *rm + 0.1f * mean;
       *rv = 0.9f * *rv + 0.1f * (var * ((float)a.R / (float)(a.R - 1)));
     } else {
       a.out0[i] = s0;
@@ -426,12 +427,12 @@ int cnn_im2col_launch(const void* src, void* col, int N, int Hs, int Ws, int C, 
   return ok_or_cuda_c();
 }
 
-// mode 0 / 1: mean / (rstd + running stats); mode 2: backward sums (+ dgamma, dbeta)
+// mode 0: mean, rstd, running stats (one pass); mode 2: backward sums (+ dgamma, dbeta)
 int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, float* mean, float* rstd,
                         float* sg, float* sgx, float* part, float* run_mean, float* run_var, int64_t run_stride,
                         float* dgamma, float* dbeta, int64_t grad_stride, int E, int R, int C, float eps,
                         cudaStream_t s) {
-  if (C % 8 || C > 2048 || R < 2) return ERR_INPUT;
+  if (C % 8 || C > 2048 || R < 2 || mode == 1) return ERR_INPUT;
   const int chunks = (R + cnn::CHUNK - 1) / cnn::CHUNK;
   const int lanes = 256 / (C / 8);
   const int smem = lanes * 2 * C * (int)sizeof(float);
@@ -443,13 +444,13 @@ int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, 
     attr = true;
   }
   cnn::StatArgs sa{(const __nv_bfloat16*)z, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)y,
-                   mode == 0 ? nullptr : mean, rstd, part, C, R, mode};
+                   mean, rstd, part, C, R, mode};
   cnn::stats_kernel<<<dim3(chunks, E), 256, smem, s>>>(sa);
   cnn::FoldArgs fa{};
   fa.part = part;
-  fa.out0 = mode == 0 ? mean : (mode == 1 ? rstd : sg);
-  fa.out1 = sgx;
-  fa.mean = mean;
+  fa.out0 = mode == 0 ? mean : sg;
+  fa.out1 = mode == 0 ? rstd : sgx;
+  fa.z = (const __nv_bfloat16*)z;
   fa.run_mean = run_mean;
   fa.run_var = run_var;
   fa.run_stride = run_stride;

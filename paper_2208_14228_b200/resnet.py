@@ -49,6 +49,16 @@ def _round8(n: int) -> int:
     return (n + 7) // 8 * 8
 
 
+def est_blocks(ests: int, gpus: int) -> list[tuple[int, int]]:
+    """(first EST, count) per GPU: the reference's EST -> executor mapper (engine.assign_ranks,
+    engine.py:169-199: contiguous blocks, balanced, larger shares first)."""
+    from .engine import ExecutorSpec, assign_ranks
+
+    if gpus < 1:
+        raise ConfigError(f"{gpus} GPUs")
+    return [(ranks[0], len(ranks)) for _, ranks in assign_ranks([ExecutorSpec("gpu")] * gpus, ests)]
+
+
 class _Conv:
     def __init__(self, name, ci, co, k, s, hin):
         self.name, self.ci, self.co, self.k, self.s, self.hin = name, ci, co, k, s, hin
@@ -136,16 +146,7 @@ class ResNetJob:
 
     # ------------------------------------------------------------ EST slots
     def layout(self, gpus: int) -> list[tuple[int, int]]:
-        """Contiguous EST blocks (engine.assign_ranks with balanced, larger-first shares)."""
-        if gpus < 1 or gpus > self.E:
-            raise ConfigError(f"{gpus} GPUs for {self.E} ESTs")
-        q, r = divmod(self.E, gpus)
-        out, base = [], 0
-        for g in range(gpus):
-            n = q + (1 if g < r else 0)
-            out.append((base, n))
-            base += n
-        return out
+        return est_blocks(self.E, gpus)
 
     def _new_slots(self, n: int) -> dict:
         return {"run_mean": torch.zeros(n, self.CBN, dtype=torch.float32, device="cuda"),
@@ -231,10 +232,9 @@ class ResNetJob:
         sl = self.slots[gslot]
         rm = sl["run_mean"].data_ptr() + 4 * self.bn_off[cv.name]
         rv = sl["run_var"].data_ptr() + 4 * self.bn_off[cv.name]
-        for mode in (0, 1):
-            _native.check(L.bt_cnn_bn_stats(mode, w["z"].data_ptr(), None, None, w["mean"].data_ptr(),
-                                            w["rstd"].data_ptr(), None, None, ws["part"].data_ptr(), rm, rv, self.CBN,
-                                            None, None, 0, n, Re, cv.co, self.eps, s), "bn stats")
+        _native.check(L.bt_cnn_bn_stats(0, w["z"].data_ptr(), None, None, w["mean"].data_ptr(), w["rstd"].data_ptr(),
+                                        None, None, ws["part"].data_ptr(), rm, rv, self.CBN, None, None, 0, n, Re,
+                                        cv.co, self.eps, s), "bn stats")
         out = w["y"] if out is None else out
         _native.check(L.bt_cnn_bn_apply(w["z"].data_ptr(), None if res is None else res.data_ptr(),
                                         w["mean"].data_ptr(), w["rstd"].data_ptr(),

@@ -192,3 +192,18 @@ def test_memory_model():
 
     assert len({executor_peak_mu(t, 1.0) for t in range(1, 17)}) == 1
     assert packing_peak_mu(16, 1.0) > 16 > executor_peak_mu(16, 1.0)
+
+
+def test_model_stack_est_blocks_follow_assign_ranks():
+    """C3/C4 drivers place ESTs on GPUs with the reference's mapper (engine.py:169-199)."""
+    import pytest
+
+    from paper_2208_14228_b200.errors import ConfigError
+    from paper_2208_14228_b200.resnet import est_blocks
+
+    assert est_blocks(16, 8) == [(2 * g, 2) for g in range(8)]
+    assert est_blocks(16, 4) == [(0, 4), (4, 4), (8, 4), (12, 4)]
+    assert est_blocks(16, 3) == [(0, 6), (6, 5), (11, 5)]
+    assert est_blocks(32, 1) == [(0, 32)]
+    with pytest.raises(ConfigError):
+        est_blocks(4, 5)
