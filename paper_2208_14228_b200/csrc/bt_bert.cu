@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const LnArgs a) {
 // block = (local EST e, 64-row chunk k); warp w handles rows w, w+8, ... of the chunk in order
 template <int NC>
 __global__ void __launch_bounds__(256) ln_bwd_kernel(const LnArgs a) {
-  extern __shared__ float ln_smem[];  // [8 warps][3][D]
+  extern __shared__ float ln_smem[];  // [8 warps][D]
   const int chunks = a.Te / LN_CHUNK;
   const int e = blockIdx.x / chunks, k = blockIdx.x - e * chunks;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -569,20 +569,21 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const LnArgs a) {
       st8(a.yb + t * a.D + col, dx);
     }
   }
-  // warp partials -> smem, folded in warp order -> this chunk's partial
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int col = c * 256 + lane * 8;
-    st8(ln_smem + (size_t)(w * 3 + 0) * a.D + col, pg[c]);
-    st8(ln_smem + (size_t)(w * 3 + 1) * a.D + col, pb[c]);
-    st8(ln_smem + (size_t)(w * 3 + 2) * a.D + col, pr[c]);
-  }
-  __syncthreads();
+  // warp partials -> smem ([8][D], one quantity at a time: 8*D floats keep several blocks per SM
+  // resident), folded in warp order -> this chunk's partial
   float* out = a.part + (size_t)blockIdx.x * 3 * a.D;
-  for (int i = threadIdx.x; i < 3 * a.D; i += 256) {
-    float acc = ln_smem[i];
-    for (int ww = 1; ww < 8; ++ww) acc += ln_smem[(size_t)ww * 3 * a.D + i];
-    out[i] = acc;
+#pragma unroll
+  for (int qi = 0; qi < 3; ++qi) {
+    if (qi) __syncthreads();  // the previous quantity's fold has read the buffer
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      st8(ln_smem + (size_t)w * a.D + c * 256 + lane * 8, qi == 0 ? pg[c] : (qi == 1 ? pb[c] : pr[c]));
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.D; i += 256) {
+      float acc = ln_smem[i];
+      for (int ww = 1; ww < 8; ++ww) acc += ln_smem[(size_t)ww * a.D + i];
+      out[(size_t)qi * a.D + i] = acc;
+    }
   }
 }
 
@@ -741,11 +742,11 @@ static int ln_launch_nc(int backward, const bert::LnArgs& a, int E, cudaStream_t
   if (!backward) {
     bert::ln_fwd_kernel<NC><<<(a.rows + 7) / 8, 256, 0, s>>>(a);
   } else {
-    const int smem = 8 * 3 * a.D * (int)sizeof(float);
+    const int smem = 8 * a.D * (int)sizeof(float);
     static bool attr = false;
     if (!attr) {
       if (cudaFuncSetAttribute(bert::ln_bwd_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               8 * 3 * 256 * NC * (int)sizeof(float)) != cudaSuccess)
+                               8 * 256 * NC * (int)sizeof(float)) != cudaSuccess)
         return ERR_CUDA;
       attr = true;
     }
