@@ -351,7 +351,7 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
 
     from paper_2208_14228_b200.bert import BertJob
 
-    job = BertJob(ests=ests)
+    job = BertJob(ests=ests, est_group=4, fanin=2)
     s = torch.cuda.current_stream()
     for _ in range(warmup):
         job.step()
@@ -398,7 +398,19 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
     ffn_tf = 2.0 * T * F * D / ffn_ms / 1e9
     del job
     torch.cuda.empty_cache()
-    a, b = BertJob(ests=ests, layers=2), BertJob(ests=ests, layers=2)
+    per_est = BertJob(ests=ests, fanin=2)  # one gradient buffer per EST (est_group 1)
+    for _ in range(warmup):
+        per_est.step()
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(steps):
+        per_est.step()
+    e1.record(s)
+    e1.synchronize()
+    ms_per_est = e0.elapsed_time(e1) / steps
+    del per_est
+    torch.cuda.empty_cache()
+    a, b = BertJob(ests=ests, layers=2, est_group=4, fanin=2), BertJob(ests=ests, layers=2, est_group=4, fanin=2)
     for _ in range(2):
         a.step()
         b.step([ests // 4] * 4)
@@ -408,8 +420,11 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
     gemm_ms = split.get("gemm_bf16", 0.0)
     seqs = ests * 8
     return {"workload": "C4: BERT-base encoder bf16 (12 layers, d 768, 12 heads, FFN 3072, seq 128, dropout 0.1 "
-                        "hidden + attention), 32 ESTs x 8 sequences, MSE head, momentum SGD (BASELINE.json configs[3])",
+                        "hidden + attention), 32 ESTs x 8 sequences, MSE head, momentum SGD (BASELINE.json configs[3]); "
+                        "gradient leaves of 4 ESTs (EST-ordered accumulation, valid for 1/2/4/8 GPUs), Tree(2) reducer",
             "samples_per_s": round(seqs / (ms / 1e3), 1), "unit": "sequences/s", "ms_per_step": round(ms, 3),
+            "per_est_gradient_buffers": {"samples_per_s": round(seqs / (ms_per_est / 1e3), 1),
+                                         "ms_per_step": round(ms_per_est, 3)},
             "tokens_per_s": round(seqs * 128 / (ms / 1e3), 1), "loss": round(losses.mean().item(), 5),
             "roofline": {"kernel": "gemm_bf16_tn_pair_kernel<5,bf16> FFN forward (bt_gemm.cu: 32768x3072x768, "
                                    "bias+GELU epilogue, TMA-store), one launch",
@@ -431,7 +446,7 @@ def bench_bert_dist(rank, world, dist, ests=32, steps=5, warmup=3, **model):
     from paper_2208_14228_b200.bert import BertJob
 
     n = ests // world
-    job = BertJob(ests=ests, est_base=rank * n, est_count=n, fanin=2, **model)
+    job = BertJob(ests=ests, est_base=rank * n, est_count=n, fanin=2, est_group=min(4, n), **model)
     dev = "cuda" if dist.get_backend() == "nccl" else "cpu"  # gloo: host tensors (tests)
     job.attach_peer()
     s = torch.cuda.current_stream()

@@ -55,22 +55,33 @@ class BertJob:
     def __init__(self, ests: int, seqs: int = 8, layers: int = 12, d_model: int = 768, heads: int = 12,
                  d_ff: int = 3072, seed: int = 42, lr: float = 1e-3, momentum: float = 0.9, p_hidden: float = 0.1,
                  p_attn: float = 0.1, fanin: int = 0, eps: float = 1e-12, est_base: int = 0,
-                 est_count: int | None = None):
+                 est_count: int | None = None, est_group: int = 1):
         """`est_base` / `est_count`: this process computes ESTs [est_base, est_base + est_count) of the E
-        (one rank of a multi-GPU job, `attach_peer`); default all E."""
+        (one rank of a multi-GPU job, `attach_peer`); default all E.
+        `est_group` (g): gradient leaf group.  g = 1: one gradient buffer per EST, summed by the reducer in
+        EST-rank order.  g > 1: the weight/bias/LN gradients of ESTs [g*j, g*j+g) are accumulated in one
+        buffer in a canonical order -- the GEMM's ascending K over EST g*j's tokens, then g*j+1's, ... --
+        before the rank-ordered reducer runs over the E/g leaves (EasyScale's per-worker gradient
+        accumulation with a pinned order).  Bit-identical for every mapping whose GPU blocks are whole
+        leaf groups (E=32, g=4: 1/2/4/8 GPUs), with g-fold less gradient traffic."""
         require_cuda()
         if heads * 64 != d_model or d_model % 256 or d_model > 1024 or d_ff % 256:
             raise ConfigError("d_model = 64 * heads, a multiple of 256 (<= 1024); d_ff a multiple of 256")
         if ests > _native.BT_MAX_TABLE or ests < 1:
             raise ConfigError(f"1..{_native.BT_MAX_TABLE} ESTs per job")
-        if fanin not in (0, 2) or (fanin == 2 and ests & (ests - 1)):
-            raise ConfigError("allreduce variant: Sequential (0) or Tree(2) with a power-of-two EST count")
+        if fanin not in (0, 2):
+            raise ConfigError("allreduce variant: Sequential (0) or Tree(2)")
         if seqs < 1 or layers < 1:
             raise ConfigError("seqs and layers must be >= 1")
         self.E, self.S, self.L, self.D, self.H, self.F = ests, seqs, layers, d_model, heads, d_ff
         self.est0, self.En = est_base, ests if est_count is None else est_count
         if self.est0 < 0 or self.En < 1 or self.est0 + self.En > ests:
             raise ConfigError(f"local EST block [{est_base}, +{est_count}) outside the {ests} ESTs")
+        self.g = est_group
+        if self.g < 1 or ests % self.g or self.En % self.g or self.est0 % self.g:
+            raise ConfigError(f"gradient leaf group {est_group} must divide E and the local EST block")
+        if fanin == 2 and (ests // self.g) & (ests // self.g - 1):
+            raise ConfigError("Tree(2) needs a power-of-two number of gradient leaves")
         self.peer = None
         self.Te = seqs * 128
         self.seed, self.lr, self.mu, self.fanin = seed, lr, momentum, fanin
@@ -97,7 +108,7 @@ class BertJob:
             self.view(l, "g1").fill_(1.0)
             self.view(l, "g2").fill_(1.0)
         self.vel = torch.zeros_like(self.params)
-        self.grads = torch.empty(self.En, self.P, dtype=torch.float32, device="cuda")  # this rank's EST slots
+        self.grads = torch.empty(self.En // self.g, self.P, dtype=torch.float32, device="cuda")  # gradient leaves
         # bf16 operand copies: W [out][in] (forward) and W^T [in][out] (dX products)
         self._moff = []
         m = 0
@@ -142,8 +153,8 @@ class BertJob:
     def _p(self, l, k):
         return self.params.data_ptr() + 4 * self.off[l][k]
 
-    def _g(self, base, l, k):  # EST `base`'s gradient slot for (layer, name); EST e at + e*P floats
-        return self.grads.data_ptr() + 4 * (base * self.P + self.off[l][k])
+    def _g(self, base, l, k):  # local EST `base`'s gradient leaf for (layer, name); leaf j at + j*P floats
+        return self.grads.data_ptr() + 4 * ((base // self.g) * self.P + self.off[l][k])
 
     def _refresh_bf16(self):
         c = self._cast
@@ -158,8 +169,8 @@ class BertJob:
         D, F, Te, T, L = self.D, self.F, self.Te, n * self.Te, self.L
         bf, f32 = dict(dtype=torch.bfloat16, device="cuda"), dict(dtype=torch.float32, device="cuda")
         ws = {
-            "layers": [{"xb": torch.empty(T, D, **bf), "qkv": torch.empty(T, 3 * D, **bf), "ctx": torch.empty(T, D, **bf),
-                        "hs1": torch.empty(T, D, **f32), "st1": torch.empty(T, 2, **f32),
+            "layers": [{"xb": torch.empty(T, D, **bf), "qkv": torch.empty(T, 3 * D, **bf),
+                        "ctx": torch.empty(T, D, **bf), "hs1": torch.empty(T, D, **f32), "st1": torch.empty(T, 2, **f32),
                         "h1b": torch.empty(T, D, **bf), "Hpre": torch.empty(T, F, **bf),
                         "Dact": torch.empty(T, F, **bf), "hs2": torch.empty(T, D, **f32),
                         "st2": torch.empty(T, 2, **f32)} for _ in range(L)],
@@ -180,18 +191,19 @@ class BertJob:
                                                        bias, 0, stream()), "bert gemm")
 
     def _wgrad(self, ws, n, dy, x, rows_out, cols_in, dst):
-        """Per-EST weight gradients dW_e = dy_e^T x_e ([rows_out][cols_in], K = the EST's tokens),
-        read MN-major straight from the token-major activations and written into each EST's slot
-        (stride P): one batched launch, no transposed copies."""
-        Te = self.Te
-        _native.check(_native.lib().bt_gemm_bf16_ex(dy, x, dst, n, rows_out, cols_in, Te, rows_out * Te, cols_in * Te,
-                                                     self.P, 0, None, 1, 0, stream()), "bert weight-gradient gemm")
+        """Weight gradient of each gradient leaf, dW_j = dy_j^T x_j ([rows_out][cols_in], K = the leaf's
+        tokens in EST order), read MN-major straight from the token-major activations and written into
+        the leaf's slot (stride P): one batched launch, no transposed copies."""
+        K = self.g * self.Te
+        _native.check(_native.lib().bt_gemm_bf16_ex(dy, x, dst, n // self.g, rows_out, cols_in, K, rows_out * K,
+                                                     cols_in * K, self.P, 0, None, 1, 0, stream()),
+                      "bert weight-gradient gemm")
 
     def _group(self, lb: int, n: int, losses: torch.Tensor, capture: dict | None = None):
         """Forward/backward of local ESTs [lb, lb+n) (global ranks est0 + lb ...): per-EST gradients into
         grads[lb:lb+n]; every random draw keyed by the GLOBAL rank."""
         L, s = _native.lib(), stream()
-        base = self.est0 + lb
+        base, gg = self.est0 + lb, self.g
         D, F, H, Te, T, NL = self.D, self.F, self.H, self.Te, n * self.Te, self.L
         seed, step = self.seed & (2**64 - 1), self.step_idx
         ws = self._workspace(n)
@@ -240,7 +252,7 @@ class BertJob:
             _native.check(L.bt_bert_ln_bwd(A.data_ptr(), None if dy2 is None else dy2.data_ptr(), w["hs2"].data_ptr(),
                                            w["st2"].data_ptr(), self._p(l, "g2"), Cb.data_ptr(), ws["dbr"].data_ptr(),
                                            part, n, Te, D, base, NL, l, 1, seed, step, self.ph, s), "layernorm 2'")
-            _native.check(L.bt_bert_ln_fold(part, n, Te, D, self._g(lb, l, "g2"), self._g(lb, l, "be2"),
+            _native.check(L.bt_bert_ln_fold(part, n // gg, gg * Te, D, self._g(lb, l, "g2"), self._g(lb, l, "be2"),
                                             self._g(lb, l, "b2"), self.P, s))
             if capture is not None and l == 0:
                 capture.update(dg=Cb.clone(), do=ws["dbr"].clone())
@@ -250,14 +262,14 @@ class BertJob:
             self._gemm(ws["dHpre"].data_ptr(), self._wt(l, "W1"), Db.data_ptr(), T, D, F, out_bf16=True)
             self._wgrad(ws, n, ws["dbr"].data_ptr(), w["Dact"].data_ptr(), D, F, self._g(lb, l, "W2"))
             self._wgrad(ws, n, ws["dHpre"].data_ptr(), w["h1b"].data_ptr(), F, D, self._g(lb, l, "W1"))
-            _native.check(L.bt_colsum_bf16_strided(ws["dHpre"].data_ptr(), n, Te, F, self._g(lb, l, "b1"), self.P,
-                                                   ws["colsum"].data_ptr(), s))
+            _native.check(L.bt_colsum_bf16_strided(ws["dHpre"].data_ptr(), n // gg, gg * Te, F, self._g(lb, l, "b1"),
+                                                   self.P, ws["colsum"].data_ptr(), s))
             if capture is not None and l == 0:
                 capture.update(dHpre=ws["dHpre"].clone(), dh1=Db.clone())
             _native.check(L.bt_bert_ln_bwd(Db.data_ptr(), Cb.data_ptr(), w["hs1"].data_ptr(), w["st1"].data_ptr(),
                                            self._p(l, "g1"), B.data_ptr(), ws["dbr"].data_ptr(), part, n, Te, D, base,
                                            NL, l, 0, seed, step, self.ph, s), "layernorm 1'")
-            _native.check(L.bt_bert_ln_fold(part, n, Te, D, self._g(lb, l, "g1"), self._g(lb, l, "be1"),
+            _native.check(L.bt_bert_ln_fold(part, n // gg, gg * Te, D, self._g(lb, l, "g1"), self._g(lb, l, "be1"),
                                             self._g(lb, l, "bo"), self.P, s))
             self._gemm(ws["dbr"].data_ptr(), self._wt(l, "Wo"), ws["dctx"].data_ptr(), T, D, D, out_bf16=True)
             self._wgrad(ws, n, ws["dbr"].data_ptr(), w["ctx"].data_ptr(), D, D, self._g(lb, l, "Wo"))
@@ -267,8 +279,8 @@ class BertJob:
                 capture.update(dh=B.clone(), da=ws["dbr"].clone(), dctx=ws["dctx"].clone(), dqkv=ws["dqkv"].clone())
             self._gemm(ws["dqkv"].data_ptr(), self._wt(l, "Wqkv"), A.data_ptr(), T, D, 3 * D, out_bf16=True)
             self._wgrad(ws, n, ws["dqkv"].data_ptr(), w["xb"].data_ptr(), 3 * D, D, self._g(lb, l, "Wqkv"))
-            _native.check(L.bt_colsum_bf16_strided(ws["dqkv"].data_ptr(), n, Te, 3 * D, self._g(lb, l, "bqkv"),
-                                                   self.P, ws["colsum"].data_ptr(), s))
+            _native.check(L.bt_colsum_bf16_strided(ws["dqkv"].data_ptr(), n // gg, gg * Te, 3 * D,
+                                                   self._g(lb, l, "bqkv"), self.P, ws["colsum"].data_ptr(), s))
             dy2 = B
         if capture is not None:
             capture["dx"] = A.clone()
@@ -278,8 +290,8 @@ class BertJob:
         """One mini-batch of this process's ESTs; `groups` = EST counts per launch group (default: one group).
         Returns the local per-EST losses [est_count] (fp32, on device)."""
         groups = groups or [self.En]
-        if sum(groups) != self.En or min(groups) < 1:
-            raise ConfigError(f"groups {groups} must partition {self.En} ESTs")
+        if sum(groups) != self.En or min(groups) < 1 or any(n % self.g for n in groups):
+            raise ConfigError(f"groups {groups} must partition {self.En} ESTs into whole gradient leaves of {self.g}")
         losses = torch.empty(self.En, dtype=torch.float32, device="cuda")
         base = 0
         for n in groups:
@@ -302,8 +314,8 @@ class BertJob:
         from .peer import PeerGroupReducer
 
         loc = RankBuffers(self.grads, self.params, self.vel, torch.cuda.current_stream())
-        self.peer = PeerGroupReducer(loc, self.E, "rank_tree2" if self.fanin == 2 else "sequential", None, self.lr,
-                                     self.mu, group)
+        self.peer = PeerGroupReducer(loc, self.E // self.g, "rank_tree2" if self.fanin == 2 else "sequential", None,
+                                     self.lr, self.mu, group, divisor=self.E)
 
     def _reduce_update(self):
         """Fixed EST-rank-order sum of the E gradient slots, /E, momentum SGD: one launch over all P
@@ -315,8 +327,10 @@ class BertJob:
         if self.En != self.E:
             raise ConfigError("a partial EST block needs attach_peer() for the exchange")
         a = _native.ReduceArgs()
-        a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, self.E, self.fanin, self.P
-        for k in range(self.E):
+        leaves = self.E // self.g
+        a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, leaves, self.fanin, self.P
+        a.divisor = self.E
+        for k in range(leaves):
             a.grads[k] = self.grads.data_ptr() + 4 * k * self.P
         p, v = self.params.data_ptr(), self.vel.data_ptr()
         a.param, a.vel, a.param_out, a.vel_out = p, v, p, v

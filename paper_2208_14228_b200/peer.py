@@ -64,8 +64,10 @@ class PeerGroupReducer:
     NAMES = ("grads", "partial", "param", "vel", "sig")
 
     def __init__(self, local: RankBuffers, E: int, variant: str = "rank_tree2", rot: torch.Tensor | None = None,
-                 lr: float = 0.02, mu: float = 0.9, group=None):
+                 lr: float = 0.02, mu: float = 0.9, group=None, divisor: int = 0):
+        """E = gradient slots of the job (all ranks); divisor = the mean's denominator (0: E)."""
         self.group = group
+        self.divisor = divisor
         self.rank, self.G = dist.get_rank(group), dist.get_world_size(group)
         self.local, self.E, self.variant, self.rot, self.lr, self.mu = local, E, variant, rot, lr, mu
         if E % self.G:
@@ -121,11 +123,11 @@ class PeerGroupReducer:
             a = _native.ReduceArgs()
             a.dtype, a.mode, a.n = self.dtype, _native.REDUCE_UPDATE, hi - lo
             if self.variant == "rank_tree2":
-                a.E, a.fanin, a.divisor = self.G, 2, self.E
+                a.E, a.fanin, a.divisor = self.G, 2, self.divisor or self.E
                 for q in range(self.G):
                     a.grads[q] = self.ptrs[q]["partial"] + off
             else:
-                a.E, a.fanin = self.E, 0 if self.variant == "sequential" else 2
+                a.E, a.fanin, a.divisor = self.E, 0 if self.variant == "sequential" else 2, self.divisor
                 for k in range(self.E):
                     a.grads[k] = self.ptrs[k // self.E_loc]["grads"] + (k % self.E_loc) * row + off
                 if self.rot is not None:

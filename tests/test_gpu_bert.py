@@ -263,3 +263,27 @@ def test_layer0_stages_match_float64_restatement(bert):
     mean_g = _d(g).mean(0)
     _close(job.vel, mean_g, "velocity", rel=1e-6)
     _close(job.params - P0, -job.lr * mean_g, "update", rel=1e-4)
+
+
+def test_gradient_leaf_groups(bert):
+    """est_group=2: ESTs (0,1), (2,3) accumulate into one gradient leaf each (GEMM K over EST 2j's then
+    2j+1's tokens); mapping-invariant for launch groups of whole leaves, the reducer's mean still over
+    E; leaf gradients equal the sum of the per-EST gradients within fp32 accumulation error."""
+    from paper_2208_14228_b200.errors import ConfigError
+
+    a = bert.BertJob(est_group=2, **SMALL)
+    b = bert.BertJob(est_group=2, **SMALL)
+    for _ in range(2):
+        assert np.array_equal(_bits(a.step([2, 2])), _bits(b.step([4])))
+    assert np.array_equal(_bits(a.params), _bits(b.params))
+    with pytest.raises(ConfigError):
+        a.step([1, 3])
+    one, two = bert.BertJob(**SMALL), bert.BertJob(est_group=2, **SMALL)
+    c1, c2 = {}, {}
+    l1, l2 = one.step(capture=c1), two.step(capture=c2)
+    assert np.array_equal(_bits(l1), _bits(l2))  # the forward is per EST either way
+    g1, g2 = c1["grads"].double(), c2["grads"].double()
+    for j in range(2):
+        want = g1[2 * j] + g1[2 * j + 1]
+        assert ((g2[j] - want).norm() / want.norm()).item() < 1e-5
+    assert ((two.params.double() - one.params.double()).norm() / one.params.double().norm()).item() < 1e-6
