@@ -163,6 +163,15 @@ int bt_gemm_bf16_tn_ex(const void *a_dev, const void *b_dev, void *c_dev, int32_
 int bt_gemm_bf16_ex(const void *a_dev, const void *b_dev, void *c_dev, int32_t batch, int32_t M, int32_t N, int32_t K,
                     int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype, const float *bias_dev,
                     int32_t mn_major, int32_t grid, void *stream);
+/* Implicit-GEMM convolution on the tcgen05 GEMM with TMA im2col-mode loads (no im2col matrix in HBM).
+ * x: NHWC bf16 [xN][xH][xW][Ci], Ci % 64 == 0; filter KH x KW, stride, pad; output grid Ho x Wo.
+ * wgrad = 0: c[xN*Ho*Wo][Co] = im2col(x) . W^T, other = W [Co][KH*KW*Ci] (K order (kh, kw, ci)).
+ * wgrad = 1: c[e] (e < batch, stride_c apart) [Co][KH*KW*Ci] = dz[e]^T im2col(x)[e], other = dz
+ *            [xN*Ho*Wo][Co]; each batch entry is rows_per_batch (% 64 == 0) output pixels (one EST).
+ * Same tiles, same K order -- the same bits -- as the explicit im2col + bt_gemm_bf16_ex. */
+int bt_gemm_conv(int32_t wgrad, const void *x_dev, int32_t xN, int32_t xH, int32_t xW, int32_t Ci, int32_t Ho,
+                 int32_t Wo, int32_t KH, int32_t KW, int32_t stride, int32_t pad, const void *other_dev, void *c_dev,
+                 int32_t Co, int32_t batch, int32_t rows_per_batch, int64_t stride_c, int32_t out_dtype, void *stream);
 /* bt_colsum_bf16 with out[e][c] at out_dev + e*out_stride + c */
 int bt_colsum_bf16_strided(const void *in_dev, int32_t E, int32_t R, int32_t C, float *out_dev, int64_t out_stride,
                            float *scratch_dev, void *stream);
@@ -240,9 +249,14 @@ int bt_cnn_add(const void *a_dev, const void *b_dev, const void *y_dev, int64_t 
 int bt_cnn_head(const void *x_dev, const int32_t *labels_dev, const float *w_dev, const float *b_dev, int32_t E,
                 int32_t B, float *dw_dev, float *db_dev, int64_t grad_stride, float *loss_dev, void *dx_dev,
                 void *stream);
-/* master conv weights [Co][taps][Ci] fp32 -> wb [Co][taps*Ci] and wt [Ci][taps][Co] (bf16), one launch */
+/* out[e] (at out_dev + e*out_stride, n floats) = sum over sp ascending of part[e*splits + sp]: the fixed
+ * split-K fold of per-EST weight gradients computed in pinned pixel splits */
+int bt_fold_splits(const float *part_dev, int32_t E, int32_t splits, int64_t n, float *out_dev, int64_t out_stride,
+                   void *stream);
+/* master conv weights [Co][taps][Ci] fp32 -> wb [Co][taps*Ci] and wt [Ci][taps][Co] (bf16; taps reversed
+ * where flip[i], for a stride-1 dX computed as a forward convolution of dz), one launch */
 int bt_cnn_conv_weights(const float *const *w_dev, void *const *wb_dev, void *const *wt_dev, const int32_t *co,
-                        const int32_t *taps, const int32_t *ci, int32_t n, void *stream);
+                        const int32_t *taps, const int32_t *ci, const int32_t *flip, int32_t n, void *stream);
 
 /* ---------------- L3 data ------------------------------------------------- */
 /* make_dataset(seed, n, dim): [n][dim+1], x then y                       sampling.py:24-35 */

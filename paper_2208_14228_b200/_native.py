@@ -100,6 +100,8 @@ EXPORTS = {
                                      _vp]),
     "bt_gemm_bf16_ex": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _i32, _vp, _i32, _i32,
                                   _vp]),
+    "bt_gemm_conv": (C.c_int, [_i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp,
+                               _i32, _i32, _i32, _i64, _i32, _vp]),
     "bt_colsum_bf16_strided": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i64, _vp, _vp]),
     "bt_bert_data": (C.c_int, [_u64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "bt_bert_attn": (C.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _u64, _i64,
@@ -118,8 +120,9 @@ EXPORTS = {
     "bt_cnn_bn_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
     "bt_cnn_add": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "bt_cnn_head": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp]),
-    "bt_cnn_conv_weights": (C.c_int, [C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i32p, _i32p, _i32p, _i32,
-                                      _vp]),
+    "bt_fold_splits": (C.c_int, [_vp, _i32, _i32, _i64, _vp, _i64, _vp]),
+    "bt_cnn_conv_weights": (C.c_int, [C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i32p, _i32p, _i32p, _i32p,
+                                      _i32, _vp]),
     "bt_cast_weights_bf16": (C.c_int, [C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i32p, _i32p, _i32, _vp]),
     "bt_sgd_step_f64": (C.c_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp, _vp, _vp]),
     "bt_make_dataset": (C.c_int, [_u64, _i64, _i32, _vp, _vp]),

@@ -35,6 +35,9 @@ int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M,
                         int64_t sb, int64_t sc, int out_bf16, int grid, cudaStream_t s);
 int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                             int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s);
+int gemm_conv_launch(int wgrad, const void* x, int xN, int xH, int xW, int Ci, int Ho, int Wo, int KH, int KW,
+                     int stride, int pad, const void* other, void* c, int Co, int batch, int rows_per_batch,
+                     int64_t sc, int out_bf16, cudaStream_t s);
 int gemm_bf16_launch_any(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                          int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, bool mn, cudaStream_t s);
 int ffn_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, void* X, float* target,
@@ -67,6 +70,8 @@ int bert_cast_weights_launch(const float* const* w, void* const* wb, void* const
                              cudaStream_t s);
 int cnn_data_launch(uint64_t seed, const int64_t* cursor, int est_base, int E, int B, void* x, int32_t* labels,
                     cudaStream_t s);
+int cnn_fold_splits_launch(const float* part, int E, int splits, int64_t n, float* out, int64_t out_stride,
+                           cudaStream_t s);
 int cnn_im2col_launch(const void* src, void* col, int N, int Hs, int Ws, int C, int Ho, int Wo, int KH, int KW,
                       int stride, int pad, int transposed, cudaStream_t s);
 int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, float* mean, float* rstd,
@@ -82,7 +87,7 @@ int cnn_add_launch(const void* a, const void* b, const void* y, int64_t n, void*
 int cnn_head_launch(const void* x, const int32_t* labels, const float* W, const float* bias, int E, int B, float* dW,
                     float* db, int64_t grad_stride, float* loss, void* dx, cudaStream_t s);
 int cnn_conv_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* Co, const int* T,
-                            const int* Ci, int n, cudaStream_t s);
+                            const int* Ci, const int* flip, int n, cudaStream_t s);
 }  // namespace bt
 
 static thread_local char g_err[512];
@@ -336,6 +341,23 @@ int bt_gemm_bf16_ex(const void* a_dev, const void* b_dev, void* c_dev, int32_t b
                                        grid, epi, mn_major != 0, STREAM(stream)),
               "bt_gemm_bf16");
 }
+int bt_gemm_conv(int32_t wgrad, const void* x_dev, int32_t xN, int32_t xH, int32_t xW, int32_t Ci, int32_t Ho,
+                 int32_t Wo, int32_t KH, int32_t KW, int32_t stride, int32_t pad, const void* other_dev, void* c_dev,
+                 int32_t Co, int32_t batch, int32_t rows_per_batch, int64_t stride_c, int32_t out_dtype, void* stream) {
+  if (!x_dev || !other_dev || !c_dev) return fail(bt::ERR_INPUT, "null pointer");
+  if (Ci % 64 || Ci > 4096 || Co % 8 || Co < 8 || xN < 1 || xH < 1 || xW < 1 || Ho < 1 || Wo < 1 || KH < 1 || KW < 1 ||
+      stride < 1 || stride > 8 || pad < 0 || pad > 16 || (out_dtype != 0 && out_dtype != 1))
+    return fail(bt::ERR_INPUT, "bt_gemm_conv geometry (Ci %% 64 == 0, Co %% 8 == 0)");
+  if (wgrad && (batch < 1 || rows_per_batch < 64 || rows_per_batch % 64 || (int64_t)batch * rows_per_batch !=
+                (int64_t)xN * Ho * Wo || stride_c < (int64_t)Co * KH * KW * Ci || stride_c % 8))
+    return fail(bt::ERR_INPUT, "bt_gemm_conv wgrad: rows_per_batch %% 64 == 0, batches covering the output");
+  if (((uintptr_t)x_dev | (uintptr_t)other_dev | (uintptr_t)c_dev) & 15)
+    return fail(bt::ERR_INPUT, "operands must be 16-byte aligned");
+  return done(bt::gemm_conv_launch(wgrad, x_dev, xN, xH, xW, Ci, Ho, Wo, KH, KW, stride, pad, other_dev, c_dev, Co,
+                                   batch, rows_per_batch, stride_c, out_dtype, STREAM(stream)),
+              "bt_gemm_conv");
+}
+
 int bt_gemm_bf16_tn_ex(const void* a_dev, const void* b_dev, void* c_dev, int32_t batch, int32_t M, int32_t N,
                        int32_t K, int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype,
                        const float* bias_dev, int32_t grid, void* stream) {
@@ -732,10 +754,17 @@ int bt_cnn_head(const void* x_dev, const int32_t* labels_dev, const float* w_dev
                                   STREAM(stream)),
               "bt_cnn_head");
 }
+int bt_fold_splits(const float* part_dev, int32_t E, int32_t splits, int64_t n, float* out_dev, int64_t out_stride,
+                   void* stream) {
+  if (!part_dev || !out_dev || E < 1 || splits < 1 || n < 4 || n % 4 || out_stride < n || out_stride % 4)
+    return fail(bt::ERR_INPUT, "bt_fold_splits arguments");
+  return done(bt::cnn_fold_splits_launch(part_dev, E, splits, n, out_dev, out_stride, STREAM(stream)),
+              "bt_fold_splits");
+}
 int bt_cnn_conv_weights(const float* const* w_dev, void* const* wb_dev, void* const* wt_dev, const int32_t* co,
-                        const int32_t* taps, const int32_t* ci, int32_t n, void* stream) {
+                        const int32_t* taps, const int32_t* ci, const int32_t* flip, int32_t n, void* stream) {
   if (n < 1 || n > 32) return fail(bt::ERR_INPUT, "conv weight table of %d (1..32)", n);
-  return done(bt::cnn_conv_weights_launch(w_dev, wb_dev, wt_dev, co, taps, ci, n, STREAM(stream)),
+  return done(bt::cnn_conv_weights_launch(w_dev, wb_dev, wt_dev, co, taps, ci, flip, n, STREAM(stream)),
               "bt_cnn_conv_weights");
 }
 

@@ -371,12 +371,13 @@ __global__ void __launch_bounds__(512) head_kernel(const __nv_bfloat16* __restri
 
 // ---------------------------------------------------------------- weights
 // master W [Co][KH*KW][Ci] fp32 -> Wb [Co][KH*KW*Ci] bf16 (forward B operand) and
-// Wt [Ci][KH*KW][Co] bf16 (the transposed convolution's B operand), one launch for a table
+// Wt [Ci][KH*KW][Co] bf16 (the dX product's B operand; taps reversed when flip), one launch for a table
 struct ConvW {
   const float* w;
   __nv_bfloat16* wb;
   __nv_bfloat16* wt;
   int Co, T, Ci;  // T = KH*KW
+  int flip;       // wt taps reversed (stride-1 dX as a forward convolution of dz with the flipped filter)
 };
 constexpr int MAX_CONV = 32;
 struct ConvWTable {
@@ -392,13 +393,42 @@ __global__ void conv_weights_kernel(const __grid_constant__ ConvWTable tab) {
     const int t = (int)(r % m.T), co = (int)(r / m.T);
     const __nv_bfloat16 v = __float2bfloat16_rn(m.w[i]);
     m.wb[i] = v;
-    m.wt[((size_t)ci * m.T + t) * m.Co + co] = v;
+    m.wt[((size_t)ci * m.T + (m.flip ? m.T - 1 - t : t)) * m.Co + co] = v;
+  }
+}
+
+// Weight gradients computed in fixed pixel splits (split-K with a pinned order): out[e] = sum over
+// sp ascending of part[e*splits + sp]  (n floats each), written at out + e*out_stride.
+__global__ void fold_splits_kernel(const float* __restrict__ part, int E, int splits, int64_t n,
+                                   float* __restrict__ out, int64_t out_stride) {
+  const int64_t total = (int64_t)E * (n / 4);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i / (n / 4));
+    const int64_t j = (i - (int64_t)e * (n / 4)) * 4;
+    const float* p = part + (size_t)e * splits * n + j;
+    float4 acc = *(const float4*)p;
+    for (int sp = 1; sp < splits; ++sp) {
+      const float4 v = *(const float4*)(p + (size_t)sp * n);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    *(float4*)(out + (size_t)e * out_stride + j) = acc;
   }
 }
 
 }  // namespace cnn
 
 // ----------------------------------------------------------------- launchers
+static int ok_or_cuda_c();
+static int grid_n(int64_t n);
+int cnn_fold_splits_launch(const float* part, int E, int splits, int64_t n, float* out, int64_t out_stride,
+                           cudaStream_t s) {
+  if (n % 4 || out_stride % 4) return ERR_INPUT;
+  cnn::fold_splits_kernel<<<grid_n((int64_t)E * n / 4), 256, 0, s>>>(part, E, splits, n, out, out_stride);
+  return ok_or_cuda_c();
+}
 static int ok_or_cuda_c() { return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA; }
 static int grid_n(int64_t n) {
   const int64_t g = (n + 255) / 256;
@@ -511,12 +541,12 @@ int cnn_head_launch(const void* x, const int32_t* labels, const float* W, const 
 }
 
 int cnn_conv_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* Co, const int* T,
-                            const int* Ci, int n, cudaStream_t s) {
+                            const int* Ci, const int* flip, int n, cudaStream_t s) {
   if (n < 1 || n > cnn::MAX_CONV) return ERR_INPUT;
   cnn::ConvWTable tab{};
   int64_t mx = 0;
   for (int i = 0; i < n; ++i) {
-    tab.m[i] = cnn::ConvW{w[i], (__nv_bfloat16*)wb[i], (__nv_bfloat16*)wt[i], Co[i], T[i], Ci[i]};
+    tab.m[i] = cnn::ConvW{w[i], (__nv_bfloat16*)wb[i], (__nv_bfloat16*)wt[i], Co[i], T[i], Ci[i], flip ? flip[i] : 0};
     const int64_t sz = (int64_t)Co[i] * T[i] * Ci[i];
     mx = sz > mx ? sz : mx;
   }

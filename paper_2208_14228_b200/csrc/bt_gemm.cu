@@ -245,6 +245,34 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
   }
 }
 
+// Implicit-GEMM convolution (TMA im2col mode).  The activation is NHWC [N][H][W][Ci] (Ci % 64 == 0);
+// GEMM row / K index q of an operand is the output pixel (n, ho, wo) in row-major order; a K block
+// (forward) or N block (weight gradient) of 64 is one filter tap (kh, kw) x 64 input channels, in the
+// order (tap, channel) -- the explicit im2col's column order, so the tiles (and the bits) are the same.
+// The tensor map's pixel box is [-p, (Wo-1)s - p] x [-p, (Ho-1)s - p] with traversal stride s, so a
+// column of consecutive output pixels wraps rows and images exactly as the GEMM rows do; the load
+// starts at input (wo*s - p, ho*s - p, n) and adds the tap offset (kw, kh).
+struct ConvGeom {
+  int Ho, Wo, s, p, KW, cblocks;  // cblocks = Ci / 64
+  int rows_per_batch;             // output pixels per batch entry (weight gradient: one EST's pixels)
+};
+__device__ __forceinline__ void tma_load_im2col(uint32_t dst, const CUtensorMap* map, int c, int w, int h, int n,
+                                                int ow, int oh, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6], {%7, %8};" ::"r"(dst),
+      "l"(map), "r"(c), "r"(w), "r"(h), "r"(n), "r"(bar), "h"((uint16_t)ow), "h"((uint16_t)oh)
+      : "memory");
+}
+// im2col load of the 64 channels of tap `t`, channel block `cb`, for the column starting at output pixel q
+__device__ __forceinline__ void conv_load(uint32_t dst, const CUtensorMap* map, const ConvGeom& g, int q, int t,
+                                          int cb, uint32_t bar) {
+  const int hw = g.Ho * g.Wo;
+  const int n = q / hw, r = q - n * hw, ho = r / g.Wo, wo = r - ho * g.Wo;
+  const int kh = t / g.KW, kw = t - kh * g.KW;
+  tma_load_im2col(dst, map, cb * 64, wo * g.s - g.p, ho * g.s - g.p, n, kw, kh, bar);
+}
+
 template <int BN, int STAGES>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
@@ -254,11 +282,13 @@ struct Smem {
   static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
 };
 
-template <int BN, int STAGES, bool OUT_BF16, bool MN>
+// AIM: 0 = tiled operands; 1 = A is im2col(x) (forward convolution, K-major); 2 = B is im2col(x)
+// (weight gradient dW = dz^T im2col(x), MN-major, K = output pixels of one batch entry)
+template <int BN, int STAGES, bool OUT_BF16, bool MN, int AIM = 0>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2, int M,
-                        int N, int K, int batch, const GemmEpi epi) {
+                        int N, int K, int batch, const GemmEpi epi, const ConvGeom cg) {
   using L = Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
@@ -315,7 +345,21 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(empty(stage), phase ^ 1u);
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
           mbar_arrive_expect_tx(full(stage), L::STAGE);
-          if constexpr (MN) {  // [k][mn] operands: one 64 x 64 box per 64-wide MN block
+          if constexpr (AIM == 1) {  // 128 output pixels x (tap, 64 channels); weights K-major
+            const int tap = kb / cg.cblocks;
+            conv_load(sa, &map_a, cg, m0, tap, kb - tap * cg.cblocks, full(stage));
+            tma_load_3d(sb, &map_b, kb * BK, n0, t / per_batch, full(stage));
+          } else if constexpr (AIM == 2) {  // dz MN-major; im2col columns of 64 pixels per 64-wide N block
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_3d(sa + j * MN_BLOCK_BYTES, &map_a, m0 + 64 * j, kb * BK, t / per_batch, full(stage));
+            const int q = (t / per_batch) * cg.rows_per_batch + kb * BK;
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) {
+              const int nb = (n0 >> 6) + j, tap = nb / cg.cblocks;
+              conv_load(sb + j * MN_BLOCK_BYTES, &map_b, cg, q, tap, nb - tap * cg.cblocks, full(stage));
+            }
+          } else if constexpr (MN) {  // [k][mn] operands: one 64 x 64 box per 64-wide MN block
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
               tma_load_3d(sa + j * MN_BLOCK_BYTES, &map_a, m0 + 64 * j, kb * BK, t / per_batch, full(stage));
@@ -692,6 +736,32 @@ static bool make_map_mn(CUtensorMap* map, const void* ptr, int rows, int K, int 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// NHWC activation [N][H][W][C] for the im2col loads: `pixels` output pixels x 64 channels per load
+static bool make_im2col_map(CUtensorMap* map, const void* x, int N, int H, int W, int C, const gemm::ConvGeom& g,
+                            int pixels) {
+  typedef CUresult (*PFN_encodeIm2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                       const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                       CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static PFN_encodeIm2col enc = nullptr;
+  if (!enc) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = (PFN_encodeIm2col)p;
+  }
+  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  const int lower[2] = {-g.p, -g.p};
+  const int upper[2] = {(g.Wo - 1) * g.s - g.p - (W - 1), (g.Ho - 1) * g.s - g.p - (H - 1)};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)g.s, (cuuint32_t)g.s, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper, 64,
+             (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 struct GemmShape {
   const void *a, *b;
   void* c;
@@ -699,20 +769,29 @@ struct GemmShape {
   int64_t sa, sb, sc;  // batch strides of A, B and C in elements
   GemmEpi epi;
   bool mn;  // A, B MN-major: C[e] = A[e]^T B[e] with A[e] stored [K][M], B[e] stored [K][N]
+  int aim = 0;  // implicit convolution operand (see AIM); x / geometry below
+  gemm::ConvGeom cg{};
+  int xN = 0, xH = 0, xW = 0, xC = 0;
 };
 
-template <int BN, int STAGES, bool OUT_BF16, bool MN>
+template <int BN, int STAGES, bool OUT_BF16, bool MN, int AIM = 0>
 static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
   const int M = g.M, N = g.N, K = g.K;
   CUtensorMap ma, mb, mc, mc2;
-  const bool in_ok = MN ? make_map_mn(&ma, g.a, M, K, g.batch, g.sa) && make_map_mn(&mb, g.b, N, K, g.batch, g.sb)
-                        : make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) &&
-                              make_map(&mb, g.b, N, K, BN, g.batch, g.sb);
+  bool in_ok;
+  if (AIM == 1)
+    in_ok = make_im2col_map(&ma, g.a, g.xN, g.xH, g.xW, g.xC, g.cg, gemm::BM) &&
+            make_map(&mb, g.b, N, K, BN, g.batch, g.sb);
+  else if (AIM == 2)
+    in_ok = make_map_mn(&ma, g.a, M, K, g.batch, g.sa) && make_im2col_map(&mb, g.b, g.xN, g.xH, g.xW, g.xC, g.cg, 64);
+  else
+    in_ok = MN ? make_map_mn(&ma, g.a, M, K, g.batch, g.sa) && make_map_mn(&mb, g.b, N, K, g.batch, g.sb)
+               : make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) && make_map(&mb, g.b, N, K, BN, g.batch, g.sb);
   if (!in_ok ||
       !make_store_map(&mc, g.c, M, N, g.batch, g.sc, OUT_BF16) ||
       !make_store_map(&mc2, g.epi.out2 ? (const void*)g.epi.out2 : g.c, M, N, g.batch, g.sc, OUT_BF16))
     return ERR_CUDA;
-  auto kern = gemm::gemm_bf16_tn_kernel<BN, STAGES, OUT_BF16, MN>;
+  auto kern = gemm::gemm_bf16_tn_kernel<BN, STAGES, OUT_BF16, MN, AIM>;
   const int smem = gemm::Smem<BN, STAGES>::TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
@@ -728,7 +807,7 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
     grid = sms;
   }
   if (grid > tiles) grid = tiles;
-  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, mc, mc2, M, N, K, g.batch, g.epi);
+  kern<<<grid, gemm::THREADS, smem, s>>>(ma, mb, mc, mc2, M, N, K, g.batch, g.epi, g.cg);
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
@@ -801,6 +880,49 @@ int gemm_bf16_launch_any(const void* a, const void* b, void* c, int batch, int M
   if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) out_bf16 = 1;
   return mn ? launch_any<true>(g, out_bf16, grid, s) : launch_any<false>(g, out_bf16, grid, s);
 }
+// Implicit-GEMM convolution products (1-CTA tiles).  fwd: C[Ho*Wo*N][Co] = im2col(x) . W^T with W [Co][K],
+// K = taps * Ci.  wgrad: C[e][Co][K] = dz[e]^T im2col(x)[e], dz [rows][Co], rows_per_batch output pixels per
+// batch entry (one EST), batch entries `batch`, C entries sc apart.
+int gemm_conv_launch(int wgrad, const void* x, int xN, int xH, int xW, int Ci, int Ho, int Wo, int KH, int KW,
+                     int stride, int pad, const void* other, void* c, int Co, int batch, int rows_per_batch,
+                     int64_t sc, int out_bf16, cudaStream_t s) {
+  GemmShape g{};
+  g.cg = gemm::ConvGeom{Ho, Wo, stride, pad, KW, Ci / 64, rows_per_batch};
+  g.xN = xN;
+  g.xH = xH;
+  g.xW = xW;
+  g.xC = Ci;
+  g.epi.kind = EPI_STORE;
+  g.c = c;
+  const int K = KH * KW * Ci;
+  constexpr int S64 = gemm::EPI_WARPS == 8 ? 6 : 4, S128 = gemm::EPI_WARPS == 8 ? 5 : 3;
+  if (!wgrad) {
+    g.a = x;
+    g.b = other;
+    g.M = xN * Ho * Wo;
+    g.N = Co;
+    g.K = K;
+    g.batch = 1;
+    g.sb = (int64_t)Co * K;
+    g.sc = (int64_t)g.M * Co;
+    g.aim = 1;
+    if (Co <= 64)
+      return out_bf16 ? launch_gemm<64, S64, true, false, 1>(g, 0, s) : launch_gemm<64, S64, false, false, 1>(g, 0, s);
+    return out_bf16 ? launch_gemm<128, S128, true, false, 1>(g, 0, s) : launch_gemm<128, S128, false, false, 1>(g, 0, s);
+  }
+  g.a = other;  // dz [batch * rows_per_batch][Co]
+  g.b = x;
+  g.M = Co;
+  g.N = K;
+  g.K = rows_per_batch;
+  g.batch = batch;
+  g.sa = (int64_t)rows_per_batch * Co;
+  g.sc = sc;
+  g.mn = true;
+  g.aim = 2;
+  return out_bf16 ? launch_gemm<128, S128, true, true, 2>(g, 0, s) : launch_gemm<128, S128, false, true, 2>(g, 0, s);
+}
+
 int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                             int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s) {
   return gemm_bf16_launch_any(a, b, c, batch, M, N, K, sa, sb, sc, out_bf16, grid, epi, false, s);

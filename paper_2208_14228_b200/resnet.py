@@ -28,6 +28,7 @@ There is no reference implementation of this model.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -129,12 +130,13 @@ class ResNetJob:
             m += cv.co * cv.K
         n = len(convs)
         self._cast = [(C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_int32 * n)(),
-                      (C.c_int32 * n)(), (C.c_int32 * n)()]
+                      (C.c_int32 * n)(), (C.c_int32 * n)(), (C.c_int32 * n)()]
         for i, cv in enumerate(convs):
             self._cast[0][i] = self.params.data_ptr() + 4 * self.off[cv.name][0]
             self._cast[1][i] = self.wb.data_ptr() + 2 * self.woff[cv.name]
             self._cast[2][i] = self.wt.data_ptr() + 2 * self.woff[cv.name]
             self._cast[3][i], self._cast[4][i], self._cast[5][i] = cv.co, cv.taps, cv.ci
+            self._cast[6][i] = 1 if cv.s == 1 else 0  # stride-1 dX = forward convolution with the flipped filter
         self.flags = Flags()
         self.step_idx = 0
         self._ws = {}
@@ -183,10 +185,20 @@ class ResNetJob:
         """Per-EST slots gathered in EST-rank order (for comparisons across mappings)."""
         return {k: torch.cat([s[k] for s in self.slots]) for k in ("run_mean", "run_var", "cursor")}
 
+    def implicit(self, cv) -> bool:
+        """Convolution as an implicit GEMM (TMA im2col loads, bt_gemm_conv): 64-channel-block inputs and
+        64-pixel EST blocks; the stem (3 -> 8 padded channels) keeps the explicit im2col.  BT_CONV_EXPLICIT=1
+        forces the explicit im2col path (the same tiles and K order: the same bits)."""
+        return cv.ci % 64 == 0 and (self.B * cv.hout ** 2) % 64 == 0 and os.environ.get("BT_CONV_EXPLICIT") != "1"
+
+    def splits(self, cv) -> int:
+        """Pinned pixel splits of an EST's weight-gradient reduction (a function of the shape only)."""
+        return max(1, (self.B * cv.hout ** 2) // 2048)
+
     # ------------------------------------------------------------ workspace
     def _refresh_bf16(self):
         c = self._cast
-        _native.check(_native.lib().bt_cnn_conv_weights(c[0], c[1], c[2], c[3], c[4], c[5], len(c[3]), stream()),
+        _native.check(_native.lib().bt_cnn_conv_weights(c[0], c[1], c[2], c[3], c[4], c[5], c[6], len(c[3]), stream()),
                       "conv weight cast")
 
     def _workspace(self, n: int) -> dict:
@@ -195,18 +207,21 @@ class ResNetJob:
             return ws
         B = self.B
         bf, f32 = dict(dtype=torch.bfloat16, device="cuda"), dict(dtype=torch.float32, device="cuda")
-        col = 0  # the transposed-convolution gather (dX)
+        col = 0  # the dX gathers: stride-2 transposed convolutions, explicit stride-1 fallbacks
         for cv in self.convs:
-            col = max(col, n * B * cv.hin ** 2 * cv.taps * cv.co)
+            if cv.name != "stem" and (cv.s != 1 or not self.implicit(cv)):
+                col = max(col, n * B * cv.hin ** 2 * cv.taps * cv.co)
         ws = {"img": torch.empty(n * B * 1024 * 8, **bf), "labels": torch.empty(n * B, dtype=torch.int32, device="cuda"),
               "col": torch.empty(col, **bf), "loss": torch.empty(n, **f32)}
         for cv in self.convs:
             R = n * B * cv.hout ** 2
             ws[cv.name] = {"z": torch.empty(R * cv.co, **bf), "y": torch.empty(R * cv.co, **bf),
-                           "mean": torch.empty(n * cv.co, **f32), "rstd": torch.empty(n * cv.co, **f32),
-                           "col": torch.empty(R * cv.K, **bf)}  # forward im2col, kept for the dW product
+                           "mean": torch.empty(n * cv.co, **f32), "rstd": torch.empty(n * cv.co, **f32)}
+            if not self.implicit(cv):  # explicit forward im2col, kept for the dW product
+                ws[cv.name]["col"] = torch.empty(R * cv.K, **bf)
         big = max(n * B * cv.hin ** 2 * max(cv.ci, cv.co) for cv in self.convs)
         ws["g"] = [torch.empty(big, **bf) for _ in range(4)]
+        ws["wpart"] = torch.empty(max(n * self.splits(cv) * cv.co * cv.K for cv in self.convs), **f32)
         ws["sg"] = torch.empty(n * 512, **f32)
         ws["sgx"] = torch.empty(n * 512, **f32)
         chunks = max((B * cv.hout ** 2 + 255) // 256 for cv in self.convs)
@@ -218,11 +233,16 @@ class ResNetJob:
     def _conv_fwd(self, ws, cv, x, n, z):
         L, s = _native.lib(), stream()
         R = n * self.B * cv.hout ** 2
+        wb = self.wb.data_ptr() + 2 * self.woff[cv.name]
+        if self.implicit(cv):
+            _native.check(L.bt_gemm_conv(0, x.data_ptr(), n * self.B, cv.hin, cv.hin, cv.ci, cv.hout, cv.hout, cv.k,
+                                         cv.k, cv.s, cv.p, wb, z.data_ptr(), cv.co, 1, 0, 0, 1, s), "conv (implicit)")
+            return
         col = ws[cv.name]["col"]
         _native.check(L.bt_cnn_im2col(x.data_ptr(), col.data_ptr(), n * self.B, cv.hin, cv.hin, cv.ci, cv.hout,
                                       cv.hout, cv.k, cv.k, cv.s, cv.p, 0, s), "im2col")
-        _native.check(L.bt_gemm_bf16_ex(col.data_ptr(), self.wb.data_ptr() + 2 * self.woff[cv.name], z.data_ptr(),
-                                        1, R, cv.co, cv.K, 0, 0, 0, 1, None, 0, 0, s), "conv gemm")
+        _native.check(L.bt_gemm_bf16_ex(col.data_ptr(), wb, z.data_ptr(), 1, R, cv.co, cv.K, 0, 0, 0, 1, None, 0, 0, s),
+                      "conv gemm")
 
     def _bn_fwd(self, ws, cv, n, gslot, res=None, relu=True, out=None):
         L, s = _native.lib(), stream()
@@ -257,20 +277,37 @@ class ResNetJob:
                                       self.params.data_ptr() + 4 * g0, n, Re, cv.co, dz.data_ptr(), s), "bn backward")
 
     def _conv_bwd(self, ws, cv, n, base, x, dz, dx):
-        """dW_e from the forward's im2col (into each EST's gradient slot) and, if dx is given, the input
-        gradient (transposed-convolution gather + GEMM)."""
+        """dW_e into each EST's gradient slot (implicit GEMM over the EST's output pixels, or the forward's
+        explicit im2col) and, if dx is given, the input gradient: stride 1 = a forward convolution of dz
+        with the flipped filter; stride 2 = the transposed-convolution gather + GEMM."""
         L, s, B = _native.lib(), stream(), self.B
         Re = B * cv.hout ** 2
-        _native.check(L.bt_gemm_bf16_ex(dz.data_ptr(), ws[cv.name]["col"].data_ptr(),
-                                        self.grads.data_ptr() + 4 * (base * self.P + self.off[cv.name][0]), n, cv.co,
-                                        cv.K, Re, Re * cv.co, Re * cv.K, self.P, 0, None, 1, 0, s), "conv dW gemm")
-        if dx is not None:
-            Rin = n * B * cv.hin ** 2
-            _native.check(L.bt_cnn_im2col(dz.data_ptr(), ws["col"].data_ptr(), n * B, cv.hout, cv.hout, cv.co, cv.hin,
-                                          cv.hin, cv.k, cv.k, cv.s, cv.p, 1, s), "im2col (transposed)")
-            _native.check(L.bt_gemm_bf16_ex(ws["col"].data_ptr(), self.wt.data_ptr() + 2 * self.woff[cv.name],
-                                            dx.data_ptr(), 1, Rin, cv.ci, cv.taps * cv.co, 0, 0, 0, 1, None, 0, 0, s),
-                          "conv dX gemm")
+        gdst = self.grads.data_ptr() + 4 * (base * self.P + self.off[cv.name][0])
+        # fixed split-K: the EST's pixels in `sp` pinned splits of >= 2048 (more output tiles in flight),
+        # partials folded in split order
+        sp = self.splits(cv)
+        Rs, part = Re // sp, ws["wpart"].data_ptr()
+        if self.implicit(cv):
+            _native.check(L.bt_gemm_conv(1, x.data_ptr(), n * B, cv.hin, cv.hin, cv.ci, cv.hout, cv.hout, cv.k, cv.k,
+                                         cv.s, cv.p, dz.data_ptr(), part, cv.co, n * sp, Rs, cv.co * cv.K, 0, s),
+                          "conv dW (implicit)")
+        else:
+            _native.check(L.bt_gemm_bf16_ex(dz.data_ptr(), ws[cv.name]["col"].data_ptr(), part, n * sp, cv.co, cv.K,
+                                            Rs, Rs * cv.co, Rs * cv.K, cv.co * cv.K, 0, None, 1, 0, s), "conv dW gemm")
+        _native.check(L.bt_fold_splits(part, n, sp, cv.co * cv.K, gdst, self.P, s), "dW split fold")
+        if dx is None:
+            return
+        Rin = n * B * cv.hin ** 2
+        wt = self.wt.data_ptr() + 2 * self.woff[cv.name]
+        if cv.s == 1 and self.implicit(cv):
+            _native.check(L.bt_gemm_conv(0, dz.data_ptr(), n * B, cv.hout, cv.hout, cv.co, cv.hin, cv.hin, cv.k, cv.k,
+                                         1, cv.p, wt, dx.data_ptr(), cv.ci, 1, 0, 0, 1, s), "conv dX (implicit)")
+            return
+        # stride 1: forward im2col of dz (flipped filter); stride 2: the transposed gather
+        _native.check(L.bt_cnn_im2col(dz.data_ptr(), ws["col"].data_ptr(), n * B, cv.hout, cv.hout, cv.co, cv.hin,
+                                      cv.hin, cv.k, cv.k, cv.s, cv.p, 0 if cv.s == 1 else 1, s), "dX im2col")
+        _native.check(L.bt_gemm_bf16_ex(ws["col"].data_ptr(), wt, dx.data_ptr(), 1, Rin, cv.ci, cv.taps * cv.co, 0, 0,
+                                        0, 1, None, 0, 0, s), "conv dX gemm")
 
     def _group(self, gslot: int, base: int, n: int, losses: torch.Tensor, capture: dict | None):
         L, s, B = _native.lib(), stream(), self.B

@@ -217,3 +217,17 @@ def test_loss_and_last_block_gradients_match_float64(rn):
         _close(g[e, b0:b0 + 512], gmask[e].sum(0), f"dbeta est {e}", 1e-5)
         _close(g[e, g0:g0 + 512], (gmask[e] * xh[e]).sum(0), f"dgamma est {e}", 1e-4)
         _close(g[e, lo:g0], (dzb[e].T @ col[e]).reshape(-1), f"conv dW est {e}", 5e-3)
+
+
+def test_implicit_gemm_convolutions_equal_explicit_im2col(rn, monkeypatch):
+    """TMA im2col-mode convolutions (bt_gemm_conv: forward, weight gradient, stride-1 dX) load the same
+    tiles in the same K order as the explicit im2col + GEMM path: identical bits over several steps."""
+    a = rn.ResNetJob(gpus=2, **SMALL)
+    la = [a.step().clone() for _ in range(2)]
+    monkeypatch.setenv("BT_CONV_EXPLICIT", "1")
+    b = rn.ResNetJob(gpus=2, **SMALL)
+    lb = [b.step().clone() for _ in range(2)]
+    monkeypatch.delenv("BT_CONV_EXPLICIT")
+    for x, y in zip(la, lb):
+        assert np.array_equal(_bits(x), _bits(y))
+    assert np.array_equal(_bits(a.params), _bits(b.params))
