@@ -479,6 +479,45 @@ def bench_bert_dist(rank, world, dist, ests=32, steps=5, warmup=3, **model):
             "ms_per_step": round(ms, 3), "n_gpus": world, "ests_per_gpu": n, "replicas_bit_identical": bool(lo.item() == hi.item())}
 
 
+def bench_resnet_dist(rank, world, dist, ests=16, batch=32, steps=10, warmup=3):
+    """C3 on N GPUs: rank r holds ESTs [r*E/N, (r+1)*E/N) (their BN slots and cursors), peer-memory
+    Tree(2) reducer; step time = max over ranks; replicas must agree bitwise."""
+    from paper_2208_14228_b200.resnet import ResNetJob
+
+    n = ests // world
+    job = ResNetJob(ests=ests, batch=batch, gpus=1, est_base=rank * n, est_count=n, fanin=2)
+    job.attach_peer()
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        job.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        job.step()
+    e1.record(s)
+    e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    chk = torch.tensor([float(job.params.view(torch.int32).to(torch.int64).sum().item())], dtype=torch.float64,
+                       device=dev)
+    lo, hi = chk.clone(), chk.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+    torch.cuda.synchronize()
+    dist.barrier()
+    job.peer.close()
+    del job
+    torch.cuda.empty_cache()
+    return {"workload": "C3: ResNet-18 with per-EST BatchNorm, 16 ESTs x 32 images, EST blocks (and their BN slots) "
+                        "per GPU, peer-memory RankTree(2) reducer (BASELINE.json configs[2])",
+            "samples_per_s": round(ests * batch / (ms / 1e3), 1), "unit": "images/s", "ms_per_step": round(ms, 3),
+            "n_gpus": world, "ests_per_gpu": n, "replicas_bit_identical": bool(lo.item() == hi.item())}
+
+
 def bench_resnet(peaks, ests=16, batch=32, steps=10, warmup=3):
     """C3 (BASELINE.json configs[2]): ResNet-18 with per-EST BatchNorm, 16 ESTs x 32 CIFAR-shaped images
     (paper_2208_14228_b200/resnet.py).  Throughput with all 16 ESTs on this GPU (CUDA events); the C3
@@ -669,6 +708,10 @@ def main():
             bert = bench_bert_dist(rank, world, dist)
         except Exception as exc:  # keep the headline line if the model-stack leg fails on this box
             bert = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        try:
+            resnet = bench_resnet_dist(rank, world, dist)
+        except Exception as exc:
+            resnet = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     clk = clocks.stop()
 
     # Roofline of the step kernel: algorithmic HBM bytes per mini-batch = the 32 rows read

@@ -73,13 +73,20 @@ class ResNetJob:
     """E ESTs x B images (32 x 32 x 3), ResNet-18 with per-EST BatchNorm, momentum SGD, `groups` "GPUs"."""
 
     def __init__(self, ests: int = 16, batch: int = 32, gpus: int = 8, seed: int = 42, lr: float = 0.02,
-                 momentum: float = 0.9, fanin: int = 0, eps: float = 1e-5):
+                 momentum: float = 0.9, fanin: int = 0, eps: float = 1e-5, est_base: int = 0,
+                 est_count: int | None = None):
+        """`gpus`: launch groups ("GPUs") of this process's ESTs.  `est_base` / `est_count`: this process
+        holds ESTs [est_base, est_base + est_count) of the E (one rank of a multi-GPU job, `attach_peer`)."""
         require_cuda()
         if ests < 1 or ests > _native.BT_MAX_TABLE:
             raise ConfigError(f"1..{_native.BT_MAX_TABLE} ESTs per job")
         if fanin not in (0, 2) or (fanin == 2 and ests & (ests - 1)):
             raise ConfigError("allreduce variant: Sequential (0) or Tree(2) with a power-of-two EST count")
         self.E, self.B, self.seed, self.lr, self.mu, self.fanin, self.eps = ests, batch, seed, lr, momentum, fanin, eps
+        self.est0, self.En = est_base, ests if est_count is None else est_count
+        if self.est0 < 0 or self.En < 1 or self.est0 + self.En > ests:
+            raise ConfigError(f"local EST block [{est_base}, +{est_count}) outside the {ests} ESTs")
+        self.peer = None
         convs = [_Conv("stem", 8, 64, 3, 1, 32)]
         blocks = []
         ci, h = 64, 32
@@ -113,7 +120,7 @@ class ResNetJob:
         self.params[self.off_fc[0]:self.off_fc[0] + CLASSES * 512] = _init_uniform(seed * 7919 + 999, CLASSES * 512,
                                                                                    (1.0 / 512) ** 0.5)
         self.vel = torch.zeros_like(self.params)
-        self.grads = torch.zeros(ests, self.P, dtype=torch.float32, device="cuda")  # padding stays 0
+        self.grads = torch.zeros(self.En, self.P, dtype=torch.float32, device="cuda")  # padding stays 0
         # BatchNorm channel offsets inside an EST's running-statistics slot
         self.bn_off, c = {}, 0
         for cv in convs:
@@ -148,7 +155,7 @@ class ResNetJob:
 
     # ------------------------------------------------------------ EST slots
     def layout(self, gpus: int) -> list[tuple[int, int]]:
-        return est_blocks(self.E, gpus)
+        return est_blocks(self.En, gpus)
 
     def _new_slots(self, n: int) -> dict:
         return {"run_mean": torch.zeros(n, self.CBN, dtype=torch.float32, device="cuda"),
@@ -313,7 +320,7 @@ class ResNetJob:
         L, s, B = _native.lib(), stream(), self.B
         ws = self._workspace(n)
         sl = self.slots[gslot]
-        _native.check(L.bt_cnn_data(self.seed & (2**64 - 1), sl["cursor"].data_ptr(), base, n, B,
+        _native.check(L.bt_cnn_data(self.seed & (2**64 - 1), sl["cursor"].data_ptr(), self.est0 + base, n, B,
                                     ws["img"].data_ptr(), ws["labels"].data_ptr(), s))
         stem = self.convs[0]
         self._conv_fwd(ws, stem, ws["img"], n, ws["stem"]["z"])
@@ -365,12 +372,20 @@ class ResNetJob:
 
     # ------------------------------------------------------------ step
     def step(self, capture: dict | None = None) -> torch.Tensor:
-        """One mini-batch of all E ESTs on the current layout; per-EST losses [E] (fp32, on device)."""
-        losses = torch.empty(self.E, dtype=torch.float32, device="cuda")
+        """One mini-batch of this process's ESTs on the current layout; per-EST losses [est_count]."""
+        losses = torch.empty(self.En, dtype=torch.float32, device="cuda")
         for g, (base, n) in enumerate(self.layout(self.G)):
             self._group(g, base, n, losses, capture if self.G == 1 else None)
         if capture is not None:
             capture["grads"] = self.grads.clone()
+        if self.peer is not None:  # across processes: the peer-memory reducer
+            self.peer.step()
+            self.peer.check()
+            self.step_idx += 1
+            self._refresh_bf16()
+            return losses
+        if self.En != self.E:
+            raise ConfigError("a partial EST block needs attach_peer() for the exchange")
         a = _native.ReduceArgs()
         a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, self.E, self.fanin, self.P
         for k in range(self.E):
@@ -391,5 +406,16 @@ class ResNetJob:
         """Convolution + head flops of one mini-batch (forward 2*R*Co*K, backward dX and dW 2x that)."""
         f = 0.0
         for cv in self.convs:
-            f += 6.0 * self.E * self.B * cv.hout ** 2 * cv.co * (cv.taps * (3 if cv.name == "stem" else cv.ci))
+            f += 6.0 * self.En * self.B * cv.hout ** 2 * cv.co * (cv.taps * (3 if cv.name == "stem" else cv.ci))
         return f
+
+    def attach_peer(self, group=None):
+        """Multi-GPU (one process per GPU, torch.distributed initialised, rank r holding the r-th contiguous
+        EST block): the exchange becomes paper_2208_14228_b200.peer.PeerGroupReducer over CUDA IPC (Tree(2):
+        hierarchical partials + owner fold over NVLink; Sequential: owner reads all E slots in rank order)."""
+        from .hier import RankBuffers
+        from .peer import PeerGroupReducer
+
+        loc = RankBuffers(self.grads, self.params, self.vel, torch.cuda.current_stream())
+        self.peer = PeerGroupReducer(loc, self.E, "rank_tree2" if self.fanin == 2 else "sequential", None, self.lr,
+                                     self.mu, group)

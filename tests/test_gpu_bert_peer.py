@@ -105,7 +105,8 @@ def _bench_worker(rank, world, port, q):
         torch.cuda.set_device(0)
         out = bench.bench_bert_dist(rank, world, dist, ests=4, steps=2, warmup=1, seqs=1, layers=2, d_model=256,
                                     heads=4, d_ff=512)
-        q.put((rank, out))
+        out2 = bench.bench_resnet_dist(rank, world, dist, ests=4, batch=2, steps=2, warmup=1)
+        q.put((rank, {"bert": out, "resnet": out2}))
     except Exception:
         import traceback
 
@@ -114,8 +115,8 @@ def _bench_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_bench_multi_gpu_c4_leg():
-    """bench.py's N>1 C4 leg (what the driver's scaling run executes), on 2 processes here."""
+def test_bench_multi_gpu_model_stack_legs():
+    """bench.py's N>1 C4 and C3 legs (what the driver's scaling run executes), on 2 processes here."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -131,6 +132,7 @@ def test_bench_multi_gpu_c4_leg():
             p.join(timeout=30)
             if p.is_alive():
                 p.kill()
-    for r, out in outs:
-        assert "error" not in out, out
-        assert out["replicas_bit_identical"] and out["ests_per_gpu"] == 2 and out["samples_per_s"] > 0
+    for r, outd in outs:
+        assert "error" not in outd, outd
+        for out in outd.values():
+            assert out["replicas_bit_identical"] and out["ests_per_gpu"] == 2 and out["samples_per_s"] > 0
