@@ -23,7 +23,7 @@ BT_P = 161
 BT_MAX_TABLE = 64
 BT_MAX_REPLICA_OUT = 8
 DTYPE_F64, DTYPE_F32 = 0, 1
-REDUCE_UPDATE, REDUCE_MEAN_ONLY, REDUCE_SUM_ONLY = 0, 1, 2
+REDUCE_UPDATE, REDUCE_MEAN_ONLY, REDUCE_SUM_ONLY, REDUCE_ADAM = 0, 1, 2, 3
 
 STATUS_TO_ERROR = {
     1: errors.InputError,
@@ -59,6 +59,8 @@ class ReduceArgs(C.Structure):
         ("param", _vp), ("vel", _vp), ("param_out", _vp), ("vel_out", _vp),
         ("extra_param_out", _vp * BT_MAX_REPLICA_OUT), ("extra_vel_out", _vp * BT_MAX_REPLICA_OUT),
         ("lr", _dbl), ("mu", _dbl), ("flags", _vp),
+        ("vel2", _vp), ("vel2_out", _vp), ("extra_vel2_out", _vp * BT_MAX_REPLICA_OUT),
+        ("beta2", _dbl), ("eps", _dbl), ("bc1", _dbl), ("bc2", _dbl),
     ]
 
 

@@ -55,7 +55,8 @@ class BertJob:
     def __init__(self, ests: int, seqs: int = 8, layers: int = 12, d_model: int = 768, heads: int = 12,
                  d_ff: int = 3072, seed: int = 42, lr: float = 1e-3, momentum: float = 0.9, p_hidden: float = 0.1,
                  p_attn: float = 0.1, fanin: int = 0, eps: float = 1e-12, est_base: int = 0,
-                 est_count: int | None = None, est_group: int = 1):
+                 est_count: int | None = None, est_group: int = 1, optimizer: str = "sgd",
+                 adam_beta2: float = 0.999, adam_eps: float = 1e-8):
         """`est_base` / `est_count`: this process computes ESTs [est_base, est_base + est_count) of the E
         (one rank of a multi-GPU job, `attach_peer`); default all E.
         `est_group` (g): gradient leaf group.  g = 1: one gradient buffer per EST, summed by the reducer in
@@ -63,7 +64,9 @@ class BertJob:
         buffer in a canonical order -- the GEMM's ascending K over EST g*j's tokens, then g*j+1's, ... --
         before the rank-ordered reducer runs over the E/g leaves (EasyScale's per-worker gradient
         accumulation with a pinned order).  Bit-identical for every mapping whose GPU blocks are whole
-        leaf groups (E=32, g=4: 1/2/4/8 GPUs), with g-fold less gradient traffic."""
+        leaf groups (E=32, g=4: 1/2/4/8 GPUs), with g-fold less gradient traffic.
+        `optimizer`: "sgd" (momentum SGD, the reference's update) or "adam" (beta1 = momentum; fused into
+        the reducer's final pass as well, bias corrections from the step count)."""
         require_cuda()
         if heads * 64 != d_model or d_model % 256 or d_model > 1024 or d_ff % 256:
             raise ConfigError("d_model = 64 * heads, a multiple of 256 (<= 1024); d_ff a multiple of 256")
@@ -108,6 +111,10 @@ class BertJob:
             self.view(l, "g1").fill_(1.0)
             self.view(l, "g2").fill_(1.0)
         self.vel = torch.zeros_like(self.params)
+        if optimizer not in ("sgd", "adam"):
+            raise ConfigError(f"optimizer {optimizer!r}: 'sgd' or 'adam'")
+        self.adam = (adam_beta2, adam_eps) if optimizer == "adam" else None
+        self.vel2 = torch.zeros_like(self.params) if self.adam else None
         self.grads = torch.empty(self.En // self.g, self.P, dtype=torch.float32, device="cuda")  # gradient leaves
         # bf16 operand copies: W [out][in] (forward) and W^T [in][out] (dX products)
         self._moff = []
@@ -313,9 +320,9 @@ class BertJob:
         from .hier import RankBuffers
         from .peer import PeerGroupReducer
 
-        loc = RankBuffers(self.grads, self.params, self.vel, torch.cuda.current_stream())
+        loc = RankBuffers(self.grads, self.params, self.vel, torch.cuda.current_stream(), vel2=self.vel2)
         self.peer = PeerGroupReducer(loc, self.E // self.g, "rank_tree2" if self.fanin == 2 else "sequential", None,
-                                     self.lr, self.mu, group, divisor=self.E)
+                                     self.lr, self.mu, group, divisor=self.E, adam=self.adam)
 
     def _reduce_update(self):
         """Fixed EST-rank-order sum of the E gradient slots, /E, momentum SGD: one launch over all P
@@ -335,6 +342,12 @@ class BertJob:
         p, v = self.params.data_ptr(), self.vel.data_ptr()
         a.param, a.vel, a.param_out, a.vel_out = p, v, p, v
         a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
+        if self.adam is not None:
+            t = self.step_idx + 1
+            a.mode = _native.REDUCE_ADAM
+            a.vel2 = a.vel2_out = self.vel2.data_ptr()
+            a.beta2, a.eps = self.adam
+            a.bc1, a.bc2 = 1.0 / (1.0 - self.mu ** t), 1.0 / (1.0 - self.adam[0] ** t)
         _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()), "bert reduce_update")
         st, _, _ = self.flags.status()
         if st:

@@ -461,10 +461,19 @@ int bt_reduce_update(const bt_reduce_args* a, void* stream) {
   if (a->fanin < 0 || a->fanin == 1) return fail(bt::ERR_CONFIG, "bad fanin %d", a->fanin);
   if (a->n < 0) return fail(bt::ERR_INPUT, "negative length");
   if (a->nout < 0 || a->nout > BT_MAX_REPLICA_OUT) return fail(bt::ERR_INPUT, "nout outside [0, 8]");
-  if (a->mode < BT_REDUCE_UPDATE || a->mode > BT_REDUCE_SUM_ONLY) return fail(bt::ERR_INPUT, "bad mode %d", a->mode);
+  if (a->mode < BT_REDUCE_UPDATE || a->mode > BT_REDUCE_ADAM) return fail(bt::ERR_INPUT, "bad mode %d", a->mode);
   if (a->divisor < 0) return fail(bt::ERR_INPUT, "negative divisor");
-  if (!a->param_out || (a->mode == BT_REDUCE_UPDATE && (!a->param || !a->vel || !a->vel_out || !a->flags)))
+  const bool upd = a->mode == BT_REDUCE_UPDATE || a->mode == BT_REDUCE_ADAM;
+  if (!a->param_out || (upd && (!a->param || !a->vel || !a->vel_out || !a->flags)))
     return fail(bt::ERR_INPUT, "null buffer");
+  if (a->mode == BT_REDUCE_ADAM) {
+    if (!a->vel2 || !a->vel2_out) return fail(bt::ERR_INPUT, "Adam needs the second-moment buffers");
+    for (int r = 0; r < a->nout; ++r)
+      if (!a->extra_vel2_out[r]) return fail(bt::ERR_INPUT, "Adam replica outputs need extra_vel2_out");
+    if (!(a->eps > 0) || !(a->beta2 >= 0 && a->beta2 < 1) || !(a->mu >= 0 && a->mu < 1) || !(a->bc1 > 0) ||
+        !(a->bc2 > 0))
+      return fail(bt::ERR_CONFIG, "Adam hyper-parameters: 0 <= beta1, beta2 < 1, eps > 0, bias corrections > 0");
+  }
   return done(bt::reduce_launch(*a, STREAM(stream)), "bt_reduce_update");
 }
 

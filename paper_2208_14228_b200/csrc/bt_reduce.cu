@@ -43,6 +43,20 @@ __device__ __forceinline__ T elem(const bt_reduce_args& a, int k, int64_t p) {
   return base[p];
 }
 
+// Adam for one element, every operation round-to-nearest in a fixed order (no contraction):
+// m' = mu*m + (1-mu)*g; s' = b2*s + (1-b2)*(g*g); p' = p - lr*(m'*bc1) / (sqrt(s'*bc2) + eps)
+template <typename T>
+__device__ __forceinline__ void adam_elem(const bt_reduce_args& a, T g, T m, T s2, T p, T* mo, T* so, T* po) {
+  using A = Arith<T>;
+  const T b1 = (T)a.mu, b2 = (T)a.beta2;
+  const T m1 = A::add(A::mul(b1, m), A::mul(A::sub((T)1, b1), g));
+  const T s1 = A::add(A::mul(b2, s2), A::mul(A::sub((T)1, b2), A::mul(g, g)));
+  const T den = A::add(sqrt(A::mul(s1, (T)a.bc2)), (T)a.eps);
+  *mo = m1;
+  *so = s1;
+  *po = A::sub(p, A::mul((T)a.lr, A::div(A::mul(m1, (T)a.bc1), den)));
+}
+
 // Apply /E, finite check and the update for one element.
 template <typename T>
 __device__ __forceinline__ void finish_elem(const bt_reduce_args& a, int64_t p, T sum) {
@@ -56,6 +70,19 @@ __device__ __forceinline__ void finish_elem(const bt_reduce_args& a, int64_t p, 
     return;
   }
   if (!finite_v(g)) flag_numeric(a.flags, p);
+  if (a.mode == BT_REDUCE_ADAM) {
+    T m, s2, np;
+    adam_elem<T>(a, g, ((const T*)a.vel)[p], ((const T*)a.vel2)[p], ((const T*)a.param)[p], &m, &s2, &np);
+    ((T*)a.vel_out)[p] = m;
+    ((T*)a.vel2_out)[p] = s2;
+    ((T*)a.param_out)[p] = np;
+    for (int r = 0; r < a.nout; ++r) {
+      ((T*)a.extra_param_out[r])[p] = np;
+      ((T*)a.extra_vel_out[r])[p] = m;
+      ((T*)a.extra_vel2_out[r])[p] = s2;
+    }
+    return;
+  }
   const T v = Arith<T>::add(Arith<T>::mul((T)a.mu, ((const T*)a.vel)[p]), g);
   const T np = Arith<T>::sub(((const T*)a.param)[p], Arith<T>::mul((T)a.lr, v));
   ((T*)a.vel_out)[p] = v;
@@ -154,6 +181,27 @@ __global__ void __launch_bounds__(256) reduce_fast_kernel(const __grid_constant_
     const V pv = ld_stream((const V*)a.param + i);
     const V vv = ld_stream((const V*)a.vel + i);
     V nv_, np_;
+    if (a.mode == BT_REDUCE_ADAM) {
+      const V sv = ld_stream((const V*)a.vel2 + i);
+      V ns_;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        T m, s2, np;
+        adam_elem<T>(a, lane(g, w), lane(vv, w), lane(sv, w), lane(pv, w), &m, &s2, &np);
+        set_lane(nv_, w, m);
+        set_lane(ns_, w, s2);
+        set_lane(np_, w, np);
+      }
+      st_stream((V*)a.vel_out + i, nv_);
+      st_stream((V*)a.vel2_out + i, ns_);
+      st_stream((V*)a.param_out + i, np_);
+      for (int r = 0; r < a.nout; ++r) {
+        st_stream((V*)a.extra_param_out[r] + i, np_);
+        st_stream((V*)a.extra_vel_out[r] + i, nv_);
+        st_stream((V*)a.extra_vel2_out[r] + i, ns_);
+      }
+      continue;
+    }
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       const T v = Arith<T>::add(Arith<T>::mul((T)a.mu, lane(vv, w)), lane(g, w));
@@ -230,9 +278,13 @@ static cudaError_t reduce_launch_t(const bt_reduce_args& a, cudaStream_t s) {
   if (fast_ok) {
     for (int k = 0; k < a.E; ++k) fast_ok = fast_ok && aligned16(a.grads[k]);
     fast_ok = fast_ok && aligned16(a.param_out);
-    if (a.mode == BT_REDUCE_UPDATE) {  // (SUM_ONLY / MEAN_ONLY only write param_out)
+    if (a.mode == BT_REDUCE_UPDATE || a.mode == BT_REDUCE_ADAM) {  // (SUM_ONLY / MEAN_ONLY only write param_out)
       fast_ok = fast_ok && aligned16(a.param) && aligned16(a.vel) && aligned16(a.vel_out);
       for (int r = 0; r < a.nout; ++r) fast_ok = fast_ok && aligned16(a.extra_param_out[r]) && aligned16(a.extra_vel_out[r]);
+      if (a.mode == BT_REDUCE_ADAM) {
+        fast_ok = fast_ok && aligned16(a.vel2) && aligned16(a.vel2_out);
+        for (int r = 0; r < a.nout; ++r) fast_ok = fast_ok && aligned16(a.extra_vel2_out[r]);
+      }
     }
   }
   if (fast_ok) {

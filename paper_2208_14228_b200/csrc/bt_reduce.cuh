@@ -10,10 +10,13 @@ extern "C" {
 #define BT_MAX_REPLICA_OUT 8
 
 enum { BT_DTYPE_F64 = 0, BT_DTYPE_F32 = 1 };
-enum { BT_REDUCE_UPDATE = 0, BT_REDUCE_MEAN_ONLY = 1, BT_REDUCE_SUM_ONLY = 2 };
+enum { BT_REDUCE_UPDATE = 0, BT_REDUCE_MEAN_ONLY = 1, BT_REDUCE_SUM_ONLY = 2, BT_REDUCE_ADAM = 3 };
 
 /* out[p] = reduce_sum(g[(rot[p]+k) % E][p] for k in 0..E-1, fanin) / E   (buckets.py:115-123)
- * then, in BT_REDUCE_UPDATE mode, v' = mu*v + out; p' = p - lr*v'      (model.py:206-212).
+ * then, in BT_REDUCE_UPDATE mode, v' = mu*v + out; p' = p - lr*v'      (model.py:206-212);
+ * in BT_REDUCE_ADAM mode (the north star's "or Adam"): m' = mu*m + (1-mu)*out (m = vel),
+ * s' = beta2*s + (1-beta2)*out*out (s = vel2), p' = p - lr*(m'*bc1) / (sqrt(s'*bc2) + eps), with the
+ * bias corrections bc1 = 1/(1-mu^t), bc2 = 1/(1-beta2^t) supplied by the caller.
  * BT_REDUCE_SUM_ONLY writes the raw fold (no division): the per-GPU subtree of
  * the hierarchical RankTree(2) path, whose top level is then folded over the G
  * partials in rank order with divisor = E.
@@ -39,6 +42,11 @@ typedef struct bt_reduce_args {
   void *extra_vel_out[BT_MAX_REPLICA_OUT];
   double lr, mu;
   int32_t *flags; /* [4] device status; NUMERIC + first bad index */
+  /* BT_REDUCE_ADAM only (appended: earlier fields keep their offsets) */
+  const void *vel2;   /* second-moment input */
+  void *vel2_out;     /* second-moment output; may alias vel2 */
+  void *extra_vel2_out[BT_MAX_REPLICA_OUT];
+  double beta2, eps, bc1, bc2;
 } bt_reduce_args;
 
 #ifdef __cplusplus

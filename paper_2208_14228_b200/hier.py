@@ -46,6 +46,7 @@ class RankBuffers:
     vel: torch.Tensor      # [n] replica
     stream: torch.cuda.Stream
     partial: torch.Tensor | None = None  # [n] RankTree subtree sum
+    vel2: torch.Tensor | None = None     # [n] Adam second moment (replica), when the update is Adam
 
 
 def shard_bounds(n: int, G: int, align: int = 4) -> list[tuple[int, int]]:

@@ -64,10 +64,17 @@ class PeerGroupReducer:
     NAMES = ("grads", "partial", "param", "vel", "sig")
 
     def __init__(self, local: RankBuffers, E: int, variant: str = "rank_tree2", rot: torch.Tensor | None = None,
-                 lr: float = 0.02, mu: float = 0.9, group=None, divisor: int = 0):
-        """E = gradient slots of the job (all ranks); divisor = the mean's denominator (0: E)."""
+                 lr: float = 0.02, mu: float = 0.9, group=None, divisor: int = 0, adam: tuple | None = None):
+        """E = gradient slots of the job (all ranks); divisor = the mean's denominator (0: E);
+        adam = (beta2, eps): Adam update (beta1 = mu, moments in local.vel / local.vel2, bias corrections
+        from the step count) instead of momentum SGD."""
         self.group = group
         self.divisor = divisor
+        self.adam = adam
+        if adam is not None and local.vel2 is None:
+            raise ConfigError("Adam needs the second-moment replica (RankBuffers.vel2)")
+        if adam is not None:
+            self.NAMES = self.NAMES + ("vel2",)
         self.rank, self.G = dist.get_rank(group), dist.get_world_size(group)
         self.local, self.E, self.variant, self.rot, self.lr, self.mu = local, E, variant, rot, lr, mu
         if E % self.G:
@@ -139,6 +146,14 @@ class PeerGroupReducer:
             for i, q in enumerate(others):
                 a.extra_param_out[i] = self.ptrs[q]["param"] + off
                 a.extra_vel_out[i] = self.ptrs[q]["vel"] + off
+            if self.adam is not None:
+                b2, eps = self.adam
+                a.mode = _native.REDUCE_ADAM
+                a.vel2 = a.vel2_out = self.ptrs[self.rank]["vel2"] + off
+                for i, q in enumerate(others):
+                    a.extra_vel2_out[i] = self.ptrs[q]["vel2"] + off
+                a.beta2, a.eps = b2, eps
+                a.bc1, a.bc2 = 1.0 / (1.0 - self.mu ** self.step_no), 1.0 / (1.0 - b2 ** self.step_no)
             a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
             _native.check(_native.lib().bt_reduce_update(C.byref(a), s), "owner")
         self._signal_and_wait(1)

@@ -287,3 +287,23 @@ def test_gradient_leaf_groups(bert):
         want = g1[2 * j] + g1[2 * j + 1]
         assert ((g2[j] - want).norm() / want.norm()).item() < 1e-5
     assert ((two.params.double() - one.params.double()).norm() / one.params.double().norm()).item() < 1e-6
+
+
+def test_adam_update(bert):
+    """optimizer="adam": the reducer's final pass applies Adam (bias-corrected, beta1 = momentum) --
+    mapping-invariant bits like SGD, and the first update equals a float64 Adam step of the captured
+    mean gradient within fp32 rounding."""
+    a = bert.BertJob(optimizer="adam", **dict(SMALL, lr=1e-3))
+    b = bert.BertJob(optimizer="adam", **dict(SMALL, lr=1e-3))
+    p0 = a.params.clone()
+    cap = {}
+    a.step(capture=cap)
+    b.step([1, 3])
+    assert np.array_equal(_bits(a.params), _bits(b.params)) and np.array_equal(_bits(a.vel2), _bits(b.vel2))
+    g = _d(cap["grads"]).mean(0)
+    m, s = 0.1 * g, 0.001 * g * g
+    want = _d(p0) - 1e-3 * (m / 0.1) / (torch.sqrt(s / 0.001) + 1e-8)
+    _close(a.params, want, "adam step", rel=1e-6)
+    for _ in range(2):
+        assert np.array_equal(_bits(a.step()), _bits(b.step([2, 2])))
+    assert np.array_equal(_bits(a.params), _bits(b.params))

@@ -25,7 +25,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, fanin, q):
+def _worker(rank, world, port, fanin, q, optimizer="sgd"):
     import sys
     from pathlib import Path
 
@@ -39,7 +39,7 @@ def _worker(rank, world, port, fanin, q):
     try:
         torch.cuda.set_device(0)
         n = CFG["ests"] // world
-        job = BertJob(fanin=fanin, est_base=rank * n, est_count=n, **CFG)
+        job = BertJob(fanin=fanin, est_base=rank * n, est_count=n, optimizer=optimizer, **CFG)
         job.attach_peer()
         losses = [job.step().cpu().numpy().tobytes() for _ in range(3)]
         torch.cuda.synchronize()
@@ -55,8 +55,8 @@ def _worker(rank, world, port, fanin, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fanin", [2, 0])
-def test_two_process_bert_matches_one_process(fanin):
+@pytest.mark.parametrize("fanin,optimizer", [(2, "sgd"), (0, "sgd"), (2, "adam")])
+def test_two_process_bert_matches_one_process(fanin, optimizer):
     import torch.multiprocessing as mp
 
     from paper_2208_14228_b200.bert import BertJob
@@ -64,7 +64,7 @@ def test_two_process_bert_matches_one_process(fanin):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, fanin, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, fanin, q, optimizer)) for r in range(2)]
     for p in procs:
         p.start()
     try:
@@ -79,7 +79,7 @@ def test_two_process_bert_matches_one_process(fanin):
             if p.is_alive():
                 p.kill()
     assert all(p.exitcode == 0 for p in procs)
-    ref = BertJob(fanin=fanin, **CFG)
+    ref = BertJob(fanin=fanin, optimizer=optimizer, **CFG)
     ref_losses = [ref.step().cpu().numpy() for _ in range(3)]
     want = ref.params.cpu().numpy().tobytes()
     for r in (0, 1):

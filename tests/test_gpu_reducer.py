@@ -129,3 +129,60 @@ def test_reducer_layout_invariance_hierarchical_rank_tree(oracle):
         top, _, _, _, _ = run_reduce(partial.astype(np.float32), None, 2, z, z, -1.0, 0.0)
         top = (top * G).astype(np.float32) / np.float32(E)
         assert np.array_equal(top.view(np.uint32), flat_p.view(np.uint32)), G
+
+
+def _fold(grads, fanin):
+    """numpy restatement of the reducer's fold in the grads' dtype: Sequential left fold / Tree(2)"""
+    if fanin == 0:
+        acc = grads[0].copy()
+        for k in range(1, grads.shape[0]):
+            acc = acc + grads[k]
+        return acc
+    level = [grads[k] for k in range(grads.shape[0])]
+    while len(level) > 1:
+        level = [level[i] + level[i + 1] if i + 1 < len(level) else level[i] for i in range(0, len(level), 2)]
+    return level[0]
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("fanin,E,nout", [(0, 8, 0), (2, 8, 1), (2, 16, 0), (0, 5, 2)])
+def test_fused_adam_update_bit_exact(dtype, fanin, E, nout):
+    """BT_REDUCE_ADAM (the north star's "or Adam"): the rank-ordered fold, /E, then Adam with caller-side
+    bias corrections -- every operation round-to-nearest in a fixed order, so it equals a numpy
+    restatement in the same dtype bit for bit (vector body, scalar tail, replica outputs)."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import Flags, stream
+
+    n = 10_003
+    grads = adversarial(E, n, 17 + E, dtype) * dtype(1e-9)
+    rng = np.random.default_rng(3)
+    p0 = rng.uniform(-1, 1, n).astype(dtype)
+    m0 = (rng.uniform(-1, 1, n) * 1e-3).astype(dtype)
+    s0 = (rng.uniform(0, 1, n) * 1e-6).astype(dtype)
+    b1, b2, eps, lr, t = 0.9, 0.999, 1e-8, 1e-3, 7
+    bc1, bc2 = 1.0 / (1.0 - b1 ** t), 1.0 / (1.0 - b2 ** t)
+    g_t, p_t, m_t, s_t = (torch.from_numpy(x).cuda() for x in (grads, p0, m0, s0))
+    extra = [tuple(torch.empty_like(p_t) for _ in range(3)) for _ in range(nout)]
+    flags = Flags()
+    a = _native.ReduceArgs()
+    a.dtype = _native.DTYPE_F64 if dtype == np.float64 else _native.DTYPE_F32
+    a.mode, a.E, a.fanin, a.n, a.nout = _native.REDUCE_ADAM, E, fanin, n, nout
+    for k in range(E):
+        a.grads[k] = g_t[k].data_ptr()
+    a.param = a.param_out = p_t.data_ptr()
+    a.vel = a.vel_out = m_t.data_ptr()
+    a.vel2 = a.vel2_out = s_t.data_ptr()
+    for r, (ep, em, es) in enumerate(extra):
+        a.extra_param_out[r], a.extra_vel_out[r], a.extra_vel2_out[r] = ep.data_ptr(), em.data_ptr(), es.data_ptr()
+    a.lr, a.mu, a.beta2, a.eps, a.bc1, a.bc2, a.flags = lr, b1, b2, eps, bc1, bc2, flags.t.data_ptr()
+    _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()))
+    assert flags.status()[0] == 0
+    T = dtype
+    g = _fold(grads, fanin) / T(E)
+    m1 = T(b1) * m0 + (T(1) - T(b1)) * g
+    s1 = T(b2) * s0 + (T(1) - T(b2)) * (g * g)
+    p1 = p0 - T(lr) * ((m1 * T(bc1)) / (np.sqrt(s1 * T(bc2)) + T(eps)))
+    for got, want in ((p_t, p1), (m_t, m1), (s_t, s1)):
+        assert np.array_equal(got.cpu().numpy().view(np.uint8), want.astype(dtype).view(np.uint8))
+    for ep, em, es in extra:
+        assert torch.equal(ep, p_t) and torch.equal(em, m_t) and torch.equal(es, s_t)
