@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(ROW_THREADS) data_kernel(uint64_t seed, int64_
   }
 }
 
-// h = H32 + b1 -> Hpre (bf16, kept for backward); D = dropout(gelu(h)) (bf16)
+// h = H32 + b1 -> Hpre = gelu'(h) (bf16, kept for backward); D = dropout(gelu(h)) (bf16)
 __global__ void __launch_bounds__(ROW_THREADS) fwd_act_kernel(const float* __restrict__ H, const float* __restrict__ b1,
                                                               uint64_t seed, int64_t step, int est_base, int Te,
                                                               int F, int rows, float p, __nv_bfloat16* __restrict__ Hpre,
@@ -85,10 +85,11 @@ __global__ void __launch_bounds__(ROW_THREADS) fwd_act_kernel(const float* __res
       for (int k = 0; k < 8; k += 2) {
         float m0, m1;
         drop_scale2(sd, step, Te, F, tl, j0 + k, p, keep, &m0, &m1);
-        h[k] += b[k];
-        h[k + 1] += b[k + 1];
-        d[k] = gelu(h[k]) * m0;
-        d[k + 1] = gelu(h[k + 1]) * m1;
+        float g0, g1;
+        gelu_and_grad(h[k] + b[k], &g0, &h[k]);
+        gelu_and_grad(h[k + 1] + b[k + 1], &g1, &h[k + 1]);
+        d[k] = g0 * m0;
+        d[k + 1] = g1 * m1;
       }
       store8(Hpre + (size_t)t * F + j0, h);
       store8(Dout + (size_t)t * F + j0, d);
@@ -132,7 +133,7 @@ __global__ void loss_final_kernel(const float* __restrict__ part, int E, int Te,
   loss[e] = acc / (float)Te;
 }
 
-// dH = dropout'(dD32) * gelu'(Hpre)   (bf16)
+// dH = dropout'(dD32) * Hpre   (Hpre = the stored gelu'(h); bf16)
 __global__ void __launch_bounds__(ROW_THREADS) bwd_act_kernel(const float* __restrict__ dD,
                                                               const __nv_bfloat16* __restrict__ Hpre, uint64_t seed,
                                                               int64_t step, int est_base, int Te, int F, int rows,
@@ -149,8 +150,8 @@ __global__ void __launch_bounds__(ROW_THREADS) bwd_act_kernel(const float* __res
       for (int k = 0; k < 8; k += 2) {
         float m0, m1;
         drop_scale2(sd, step, Te, F, tl, j0 + k, p, keep, &m0, &m1);
-        g[k] = g[k] * m0 * gelu_grad(h[k]);
-        g[k + 1] = g[k + 1] * m1 * gelu_grad(h[k + 1]);
+        g[k] = g[k] * m0 * h[k];
+        g[k + 1] = g[k + 1] * m1 * h[k + 1];
       }
       store8(dH + (size_t)t * F + j0, g);
     }

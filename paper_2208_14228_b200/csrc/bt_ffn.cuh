@@ -51,6 +51,27 @@ __device__ __forceinline__ float gelu_grad(float x) {
   const float t = tanh_fast(0.7978845608028654f * (x + 0.044715f * x * x * x));
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * 0.7978845608028654f * (1.f + 0.134145f * x * x);
 }
+// Both from one tanh: the forward stores gelu'(h) for the backward (which then needs no transcendental).
+// Written with explicit fused multiply-adds (the library builds with -fmad=false for the reference's
+// fp64 path; here contraction is a deliberate, fixed choice) and the MUFU exp2 / reciprocal:
+//   u = x (c + c k x^2),  t = 1 - 2 / (1 + 2^(2 log2(e) u)),  g = hx + hx t  (hx = x / 2),
+//   g' = (1/2 + t/2) + hx (1 - t^2) (c + 3 c k x^2)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void gelu_and_grad(float x, float* g, float* gd) {
+  constexpr float C = 0.7978845608028654f, CK = C * 0.044715f, CK3 = 3.f * CK;
+  const float x2 = __fmul_rn(x, x);
+  const float u = __fmul_rn(x, __fmaf_rn(CK, x2, C));
+  const float e = ex2_approx(__fmul_rn(2.8853900817779268f, u));
+  const float t = __fsub_rn(1.f, __fdividef(2.f, __fadd_rn(1.f, e)));
+  const float hx = __fmul_rn(0.5f, x);
+  *g = __fmaf_rn(hx, t, hx);
+  const float w = __fmul_rn(__fmul_rn(hx, __fmaf_rn(-t, t, 1.f)), __fmaf_rn(CK3, x2, C));
+  *gd = __fmaf_rn(0.5f, t, __fadd_rn(0.5f, w));
+}
 
 }  // namespace ffn
 
@@ -58,14 +79,14 @@ __device__ __forceinline__ float gelu_grad(float x) {
 // row-chunk of fp32 accumulators instead of storing them.
 enum GemmEpiKind : int {
   EPI_STORE = 0,    // C = acc (fp32 or bf16)
-  EPI_FFN_FWD = 1,  // h = acc + bias[j]: C = bf16(h) (pre-activation), out2 = bf16(dropout(gelu(h)))
-  EPI_FFN_BWD = 2,  // C = bf16(acc * dropout_scale * gelu'(aux[row][j]))   (aux = pre-activation, bf16)
+  EPI_FFN_FWD = 1,  // h = acc + bias[j]: C = bf16(gelu'(h)) (kept for backward), out2 = bf16(dropout(gelu(h)))
+  EPI_FFN_BWD = 2,  // C = bf16(acc * dropout_scale * aux[row][j])   (aux = the stored gelu'(h), bf16)
   EPI_BIAS = 3,     // C = acc + bias[j] (fp32 or bf16)
 };
 struct GemmEpi {
   int kind;
   const float* bias;          // [N] (FFN_FWD)
-  const __nv_bfloat16* aux;   // [M][N] (FFN_BWD)
+  const __nv_bfloat16* aux;   // [M][N] (FFN_BWD: gelu'(h))
   __nv_bfloat16* out2;        // [M][N] (FFN_FWD)
   uint64_t seed;
   int64_t step;

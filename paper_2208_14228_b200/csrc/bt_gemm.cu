@@ -203,27 +203,38 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
     if (epi.kind == EPI_FFN_FWD) {
 #pragma unroll
       for (int q = 0; q < 32; q += 2) {
-        float m0, m1;
+        float m0, m1, g0, g1;
         ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
-        f[q] += epi.bias[col + q];
-        f[q + 1] += epi.bias[col + q + 1];
-        g[q] = ffn::gelu(f[q]) * m0;
-        g[q + 1] = ffn::gelu(f[q + 1]) * m1;
+        ffn::gelu_and_grad(f[q] + epi.bias[col + q], &g0, &f[q]);  // C = gelu'(h) for the backward
+        ffn::gelu_and_grad(f[q + 1] + epi.bias[col + q + 1], &g1, &f[q + 1]);
+        g[q] = g0 * m0;
+        g[q + 1] = g1 * m1;
       }
     } else {
-      const uint4* ap = (const uint4*)(epi.aux + row * N + col);
+      // aux box (32 rows x 32 bf16 = 64 B per row) staged through the second half of this warp's staging
+      // box with coalesced 16-byte loads (4 lanes per row), then read back row-per-lane (SW64 pattern)
+      uint8_t* const ab = st + EPI_BOX / 2;
+      if (lane == 0) bulk_wait_read1();  // (the box's previous store read only its first half; order anyway)
+      __syncwarp();
+#pragma unroll
+      for (int pass = 0; pass < 4; ++pass) {
+        const int rr = pass * 8 + (lane >> 2), qq = lane & 3;
+        const uint4 v = *(const uint4*)(epi.aux + ((size_t)row0 + rr) * N + col + qq * 8);
+        *(uint4*)(ab + rr * 64 + ((qq ^ ((rr >> 1) & 3)) << 4)) = v;
+      }
+      __syncwarp();
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
-        const uint4 u = ap[q4];
+        const uint4 u = *(const uint4*)(ab + lane * 64 + ((q4 ^ ((lane >> 1) & 3)) << 4));
         const __nv_bfloat162* h2 = (const __nv_bfloat162*)&u;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float2 hp = __bfloat1622float2(h2[k]);
+          const float2 gp = __bfloat1622float2(h2[k]);
           const int q = q4 * 8 + 2 * k;
           float m0, m1;
           ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
-          f[q] = f[q] * m0 * ffn::gelu_grad(hp.x);
-          f[q + 1] = f[q + 1] * m1 * ffn::gelu_grad(hp.y);
+          f[q] = f[q] * m0 * gp.x;
+          f[q + 1] = f[q + 1] * m1 * gp.y;
         }
       }
     }

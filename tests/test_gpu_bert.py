@@ -206,7 +206,7 @@ def test_layer0_stages_match_float64_restatement(bert):
     _close_bf16(cap["h1b"], h1, "ln1 out")
     h1b = _d(cap["h1b"])
     hpre = h1b @ _bf(W["W1"]).T + W["b1"]
-    _close_bf16(cap["Hpre"], hpre, "ffn pre-activation")
+    _close_bf16(cap["Hpre"], _gelu_grad(hpre), "gelu' kept for the backward")
     _close_bf16(cap["Dact"], _gelu(hpre), "gelu")
     hm2 = hidden_scale(1)
     hs2_ref = h1 + (_bf(_d(cap["Dact"]) @ _bf(W["W2"]).T) + W["b2"]) * hm2
@@ -225,8 +225,7 @@ def test_layer0_stages_match_float64_restatement(bert):
     do_ref = _d(cap["dg"]) * hm2
     _close_bf16(cap["do"], do_ref, "ffn-out dropout'")
     do = _d(cap["do"])
-    hp = _d(cap["Hpre"])
-    gelu_g = _gelu_grad(hp)
+    gelu_g = _d(cap["Hpre"])  # the stored gelu'(h)
     _close_bf16(cap["dHpre"], (do @ _bf(W["W2"])) * gelu_g, "dHpre")
     dHpre = _d(cap["dHpre"])
     _close_bf16(cap["dh1"], dHpre @ _bf(W["W1"]), "dh1")
