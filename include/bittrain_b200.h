@@ -182,27 +182,29 @@ int bt_colsum_bf16_strided(const void *in_dev, int32_t E, int32_t R, int32_t C, 
  * local EST e are rows [e*Te, (e+1)*Te), Te % 128 == 0, D % 256 == 0.  Every
  * random draw is keyed by (seed, est_base + e, step, layer, element), every
  * sum has a shape fixed by the EST's own data: an EST's results do not depend
- * on which ESTs share the launch or the GPU.           analogue of model.py:107-196 */
+ * on which ESTs share the launch or the GPU.  step_dev (or NULL): read the step from device memory
+ * instead of `step` (a CUDA graph of the whole step replays with an advancing counter).
+ *                                                       analogue of model.py:107-196 */
 int bt_bert_data(uint64_t seed, int64_t step, int32_t est_base, int32_t E, int32_t Te, int32_t D, float *x32_dev,
-                 void *xb_dev, float *target_dev, void *stream);
+                 void *xb_dev, float *target_dev, const int64_t *step_dev, void *stream);
 /* forward (backward = 0): ctx[T][D] = dropout(softmax(Q K^T / 8)) V per (sequence, head), qkv [T][3D] bf16;
  * backward (1): out = dqkv [T][3D] from qkv and dctx [T][D] (P recomputed bit-identically) */
 int bt_bert_attn(int32_t backward, const void *qkv_dev, const void *dctx_dev, void *out_dev, int32_t E, int32_t Te,
                  int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed, int64_t step,
-                 float p, void *stream);
+                 float p, const int64_t *step_dev, void *stream);
 /* x = resid + dropout(branch + bias); y = LayerNorm(x) * gamma + beta -> xsum (x), stats (mean, rstd)
  * [T][2], y32, yb (bf16).  resid fp32 (the residual stream), branch bf16 (a GEMM output). */
 int bt_bert_ln_fwd(const float *resid_dev, const void *branch_dev, const float *bias_dev, const float *gamma_dev,
                    const float *beta_dev, float *xsum_dev, float *stats_dev, float *y32_dev, void *yb_dev, int32_t E,
                    int32_t Te, int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
-                   int64_t step, float p, float eps, void *stream);
+                   int64_t step, float p, float eps, const int64_t *step_dev, void *stream);
 /* dx = LayerNorm'(dy1 + dy2) (dy1 bf16 from a GEMM, dy2 fp32 residual-path gradient or NULL),
  * dbranch = bf16(dropout'(dx)); part [E][Te/64][3][D] = per-64-row-chunk column sums of
  * (dy*xhat, dy, dropout'(dx)) */
 int bt_bert_ln_bwd(const void *dy1_dev, const float *dy2_dev, const float *xsum_dev, const float *stats_dev,
                    const float *gamma_dev, float *dx_dev, void *dbranch_dev, float *part_dev, int32_t E, int32_t Te,
                    int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
-                   int64_t step, float p, void *stream);
+                   int64_t step, float p, const int64_t *step_dev, void *stream);
 /* chunk partials summed in chunk order -> dgamma/dbeta/dbias of EST e at + e*est_stride */
 int bt_bert_ln_fold(const float *part_dev, int32_t E, int32_t Te, int32_t D, float *dgamma_dev, float *dbeta_dev,
                     float *dbias_dev, int64_t est_stride, void *stream);

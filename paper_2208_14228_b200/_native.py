@@ -105,13 +105,13 @@ EXPORTS = {
     "bt_gemm_conv": (C.c_int, [_i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp,
                                _i32, _i32, _i32, _i64, _i32, _vp]),
     "bt_colsum_bf16_strided": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i64, _vp, _vp]),
-    "bt_bert_data": (C.c_int, [_u64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "bt_bert_data": (C.c_int, [_u64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "bt_bert_attn": (C.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _u64, _i64,
-                               C.c_float, _vp]),
+                               C.c_float, _vp, _vp]),
     "bt_bert_ln_fwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
-                                 _i32, _u64, _i64, C.c_float, C.c_float, _vp]),
+                                 _i32, _u64, _i64, C.c_float, C.c_float, _vp, _vp]),
     "bt_bert_ln_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
-                                 _u64, _i64, C.c_float, _vp]),
+                                 _u64, _i64, C.c_float, _vp, _vp]),
     "bt_bert_ln_fold": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp]),
     "bt_bert_mse": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "bt_cnn_data": (C.c_int, [_u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),

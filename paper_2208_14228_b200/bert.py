@@ -56,7 +56,7 @@ class BertJob:
                  d_ff: int = 3072, seed: int = 42, lr: float = 1e-3, momentum: float = 0.9, p_hidden: float = 0.1,
                  p_attn: float = 0.1, fanin: int = 0, eps: float = 1e-12, est_base: int = 0,
                  est_count: int | None = None, est_group: int = 1, optimizer: str = "sgd",
-                 adam_beta2: float = 0.999, adam_eps: float = 1e-8):
+                 adam_beta2: float = 0.999, adam_eps: float = 1e-8, graph: bool = True):
         """`est_base` / `est_count`: this process computes ESTs [est_base, est_base + est_count) of the E
         (one rank of a multi-GPU job, `attach_peer`); default all E.
         `est_group` (g): gradient leaf group.  g = 1: one gradient buffer per EST, summed by the reducer in
@@ -66,7 +66,10 @@ class BertJob:
         accumulation with a pinned order).  Bit-identical for every mapping whose GPU blocks are whole
         leaf groups (E=32, g=4: 1/2/4/8 GPUs), with g-fold less gradient traffic.
         `optimizer`: "sgd" (momentum SGD, the reference's update) or "adam" (beta1 = momentum; fused into
-        the reducer's final pass as well, bias corrections from the step count)."""
+        the reducer's final pass as well, bias corrections from the step count).
+        `graph`: after one eager step, the whole step (all launch groups, the reducer, the bf16 weight
+        refresh, the device step counter) is captured once as a CUDA graph and replayed -- no per-kernel
+        host launches; every kernel reads the step from the device counter, so replays are exact."""
         require_cuda()
         if heads * 64 != d_model or d_model % 256 or d_model > 1024 or d_ff % 256:
             raise ConfigError("d_model = 64 * heads, a multiple of 256 (<= 1024); d_ff a multiple of 256")
@@ -140,8 +143,11 @@ class BertJob:
                 self._cast[3][i], self._cast[4][i] = rows, cols
                 i += 1
         self.step_idx = 0
+        self._step_dev = torch.zeros(1, dtype=torch.int64, device="cuda")  # == step_idx, read by the kernels
         self.flags = Flags()
         self._ws = {}
+        self.graph = graph and est_count is None  # CUDA-graph replay of the whole step (single process)
+        self._graph, self._gwarm = None, False
         self._refresh_bf16()
 
     # ------------------------------------------------------------------ views
@@ -211,24 +217,25 @@ class BertJob:
         grads[lb:lb+n]; every random draw keyed by the GLOBAL rank."""
         L, s = _native.lib(), stream()
         base, gg = self.est0 + lb, self.g
+        sp = self._step_dev.data_ptr()  # the step counter lives on the device (CUDA-graph replays)
         D, F, H, Te, T, NL = self.D, self.F, self.H, self.Te, n * self.Te, self.L
         seed, step = self.seed & (2**64 - 1), self.step_idx
         ws = self._workspace(n)
         lay = ws["layers"]
         _native.check(L.bt_bert_data(seed, step, base, n, Te, D, ws["x32"].data_ptr(), lay[0]["xb"].data_ptr(),
-                                     ws["tgt"].data_ptr(), s))
+                                     ws["tgt"].data_ptr(), sp, s))
         x32 = ws["x32"]
         for l in range(NL):
             w = lay[l]
             self._gemm(w["xb"].data_ptr(), self._wb(l, "Wqkv"), w["qkv"].data_ptr(), T, 3 * D, D, out_bf16=True,
                        bias=self._p(l, "bqkv"))
             _native.check(L.bt_bert_attn(0, w["qkv"].data_ptr(), None, w["ctx"].data_ptr(), n, Te, D, H, base, NL, l,
-                                         seed, step, self.pa, s), "attention forward")
+                                         seed, step, self.pa, sp, s), "attention forward")
             self._gemm(w["ctx"].data_ptr(), self._wb(l, "Wo"), ws["brb"].data_ptr(), T, D, D, out_bf16=True)
             _native.check(L.bt_bert_ln_fwd(x32.data_ptr(), ws["brb"].data_ptr(), self._p(l, "bo"), self._p(l, "g1"),
                                            self._p(l, "be1"), w["hs1"].data_ptr(), w["st1"].data_ptr(),
                                            ws["h1_32"].data_ptr(), w["h1b"].data_ptr(), n, Te, D, base, NL, l, 0,
-                                           seed, step, self.ph, self.eps, s), "layernorm 1")
+                                           seed, step, self.ph, self.eps, sp, s), "layernorm 1")
             _native.check(L.bt_gemm_bf16_ffn(w["h1b"].data_ptr(), self._wb(l, "W1"), w["Hpre"].data_ptr(), T, F, D, 1,
                                              self._p(l, "b1"), None, w["Dact"].data_ptr(), seed, step, base, Te, 0.0,
                                              0, s), "ffn forward GEMM")
@@ -238,7 +245,7 @@ class BertJob:
             _native.check(L.bt_bert_ln_fwd(ws["h1_32"].data_ptr(), ws["brb"].data_ptr(), self._p(l, "b2"),
                                            self._p(l, "g2"), self._p(l, "be2"), w["hs2"].data_ptr(),
                                            w["st2"].data_ptr(), y32.data_ptr(), yb.data_ptr(), n, Te, D, base, NL, l,
-                                           1, seed, step, self.ph, self.eps, s), "layernorm 2")
+                                           1, seed, step, self.ph, self.eps, sp, s), "layernorm 2")
             if capture is not None and l == 0:
                 capture.update({k: w[k].clone() for k in ("xb", "qkv", "ctx", "hs1", "st1", "h1b", "Hpre", "Dact",
                                                           "hs2", "st2")})
@@ -258,7 +265,7 @@ class BertJob:
                 capture.update(dy1_top=A.clone(), dy2_top=None if dy2 is None else dy2.clone())
             _native.check(L.bt_bert_ln_bwd(A.data_ptr(), None if dy2 is None else dy2.data_ptr(), w["hs2"].data_ptr(),
                                            w["st2"].data_ptr(), self._p(l, "g2"), Cb.data_ptr(), ws["dbr"].data_ptr(),
-                                           part, n, Te, D, base, NL, l, 1, seed, step, self.ph, s), "layernorm 2'")
+                                           part, n, Te, D, base, NL, l, 1, seed, step, self.ph, sp, s), "layernorm 2'")
             _native.check(L.bt_bert_ln_fold(part, n // gg, gg * Te, D, self._g(lb, l, "g2"), self._g(lb, l, "be2"),
                                             self._g(lb, l, "b2"), self.P, s))
             if capture is not None and l == 0:
@@ -275,13 +282,13 @@ class BertJob:
                 capture.update(dHpre=ws["dHpre"].clone(), dh1=Db.clone())
             _native.check(L.bt_bert_ln_bwd(Db.data_ptr(), Cb.data_ptr(), w["hs1"].data_ptr(), w["st1"].data_ptr(),
                                            self._p(l, "g1"), B.data_ptr(), ws["dbr"].data_ptr(), part, n, Te, D, base,
-                                           NL, l, 0, seed, step, self.ph, s), "layernorm 1'")
+                                           NL, l, 0, seed, step, self.ph, sp, s), "layernorm 1'")
             _native.check(L.bt_bert_ln_fold(part, n // gg, gg * Te, D, self._g(lb, l, "g1"), self._g(lb, l, "be1"),
                                             self._g(lb, l, "bo"), self.P, s))
             self._gemm(ws["dbr"].data_ptr(), self._wt(l, "Wo"), ws["dctx"].data_ptr(), T, D, D, out_bf16=True)
             self._wgrad(ws, n, ws["dbr"].data_ptr(), w["ctx"].data_ptr(), D, D, self._g(lb, l, "Wo"))
             _native.check(L.bt_bert_attn(1, w["qkv"].data_ptr(), ws["dctx"].data_ptr(), ws["dqkv"].data_ptr(), n, Te,
-                                         D, H, base, NL, l, seed, step, self.pa, s), "attention backward")
+                                         D, H, base, NL, l, seed, step, self.pa, sp, s), "attention backward")
             if capture is not None and l == 0:
                 capture.update(dh=B.clone(), da=ws["dbr"].clone(), dctx=ws["dctx"].clone(), dqkv=ws["dqkv"].clone())
             self._gemm(ws["dqkv"].data_ptr(), self._wt(l, "Wqkv"), A.data_ptr(), T, D, 3 * D, out_bf16=True)
@@ -299,7 +306,25 @@ class BertJob:
         groups = groups or [self.En]
         if sum(groups) != self.En or min(groups) < 1 or any(n % self.g for n in groups):
             raise ConfigError(f"groups {groups} must partition {self.En} ESTs into whole gradient leaves of {self.g}")
+        replay = self.graph and capture is None and self.peer is None and self.adam is None and groups == [self.En]
+        if replay and self._gwarm:
+            if self._graph is None:  # capture once (the captured work runs at the first replay)
+                self._gloss = torch.empty(self.En, dtype=torch.float32, device="cuda")
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._body(groups, self._gloss)
+                self._graph = g
+            self._graph.replay()
+            self._post()
+            return self._gloss.clone()
         losses = torch.empty(self.En, dtype=torch.float32, device="cuda")
+        self._body(groups, losses, capture)
+        self._post()
+        self._gwarm = self._gwarm or replay
+        return losses
+
+    def _body(self, groups, losses, capture=None):
+        """Everything a step puts on the stream (capturable: no host synchronisation, no allocation)."""
         base = 0
         for n in groups:
             self._group(base, n, losses, capture if len(groups) == 1 else None)
@@ -307,9 +332,19 @@ class BertJob:
         if capture is not None:
             capture["grads"] = self.grads.clone()
         self._reduce_update()
-        self.step_idx += 1
         self._refresh_bf16()
-        return losses
+        self._step_dev.add_(1)
+
+    def _post(self):
+        """Host side of a step: the non-finite check (one status read) and the step count."""
+        self.step_idx += 1
+        if self.peer is not None:
+            self.peer.check()
+            return
+        st, _, _ = self.flags.status()
+        if st:
+            self.flags.reset()
+            raise NumericError("bert: non-finite synchronized gradient")
 
     def attach_peer(self, group=None):
         """Multi-GPU (one process per GPU, torch.distributed initialised, rank r holding the r-th contiguous
@@ -329,7 +364,6 @@ class BertJob:
         (or, across processes, the peer-memory reducer)."""
         if self.peer is not None:
             self.peer.step()
-            self.peer.check()
             return
         if self.En != self.E:
             raise ConfigError("a partial EST block needs attach_peer() for the exchange")
@@ -349,10 +383,6 @@ class BertJob:
             a.beta2, a.eps = self.adam
             a.bc1, a.bc2 = 1.0 / (1.0 - self.mu ** t), 1.0 / (1.0 - self.adam[0] ** t)
         _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()), "bert reduce_update")
-        st, _, _ = self.flags.status()
-        if st:
-            self.flags.reset()
-            raise NumericError("bert: non-finite synchronized gradient")
 
     # ---------------------------------------------------------------- sizes
     def gemm_flops_per_step(self) -> float:

@@ -173,11 +173,15 @@ struct AttnArgs {
   uint64_t seed;
   int64_t step;
   float p;
+  const int64_t* step_dev;  // when set, the step is read from device memory (CUDA-graph replays)
 };
+__device__ __forceinline__ int64_t cur_step(int64_t step, const int64_t* step_dev) {
+  return step_dev ? *step_dev : step;
+}
 
 // counter base of (EST stream, step, layer, sequence-in-EST, head): 4096 draws (16384 units) follow
-__device__ __forceinline__ uint64_t attn_counter_base(const AttnArgs& a, int sl, int h) {
-  return ((((uint64_t)a.step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4);
+__device__ __forceinline__ uint64_t attn_counter_base(const AttnArgs& a, int64_t step, int sl, int h) {
+  return ((((uint64_t)step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4);
 }
 
 // Persistent: CTA walks items (sequence s, head h) = (it / H, it % H), it += gridDim.x; the next
@@ -189,6 +193,7 @@ __global__ void __launch_bounds__(AT_THREADS) attn_fwd_kernel(const AttnArgs a) 
   __nv_bfloat16* const buf0 = (__nv_bfloat16*)at_smem;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ld = 3 * a.Dm;
+  const int64_t step = cur_step(a.step, a.step_dev);
   auto issue = [&](int it, __nv_bfloat16* bq) {
     if (it < a.n_items) {
       const __nv_bfloat16* base = a.qkv + (size_t)(it / a.H) * SEQ * ld + (it % a.H) * HD;
@@ -215,7 +220,7 @@ __global__ void __launch_bounds__(AT_THREADS) attn_fwd_kernel(const AttnArgs a) 
     warp_softmax(Qs, Ks, w, lane, P);
     const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
     const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
-    const uint64_t nb = attn_counter_base(a, sl, h) + (uint64_t)(w * 8 + g) * 64 + (lane & 3);
+    const uint64_t nb = attn_counter_base(a, step, sl, h) + (uint64_t)(w * 8 + g) * 64 + (lane & 3);
     uint32_t pa[8][4];  // dropped P as bf16 A fragments, k-step kv = keys 16kv..16kv+15
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) {
@@ -258,6 +263,7 @@ __global__ void __launch_bounds__(AT_THREADS) attn_bwd_kernel(const AttnArgs a) 
   __nv_bfloat16* const dSs = Ps + SEQ * LDP;     // dS / 8     [query][key]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ld = 3 * a.Dm;
+  const int64_t step = cur_step(a.step, a.step_dev);
   auto issue = [&](int it, __nv_bfloat16* bq) {
     if (it < a.n_items) {
       const int s = it / a.H, h = it % a.H;
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(AT_THREADS) attn_bwd_kernel(const AttnArgs a) 
     }
     const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
     const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
-    const uint64_t nb = attn_counter_base(a, sl, h) + (uint64_t)(w * 8 + g) * 64 + (lane & 3);
+    const uint64_t nb = attn_counter_base(a, step, sl, h) + (uint64_t)(w * 8 + g) * 64 + (lane & 3);
     float r0 = 0.f, r1 = 0.f;  // rowsum(dP * P), rows i0 / i0+8
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) {
@@ -407,16 +413,17 @@ struct LnArgs {
   uint64_t seed;
   int64_t step;
   float p, eps;
+  const int64_t* step_dev;  // when set, the step is read from device memory (CUDA-graph replays)
 };
 
-__device__ __forceinline__ void ln_mask8(const LnArgs& a, uint64_t sd, int tl, int col, uint32_t thr, float keep,
-                                         float* m) {
+__device__ __forceinline__ void ln_mask8(const LnArgs& a, int64_t step, uint64_t sd, int tl, int col, uint32_t thr,
+                                         float keep, float* m) {
   if (thr == 0) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) m[k] = 1.f;
     return;
   }
-  const uint64_t n0 = ((((uint64_t)a.step * a.L + a.layer) * 2 + a.site) * a.Te + tl) * (uint64_t)a.D + col;
+  const uint64_t n0 = ((((uint64_t)step * a.L + a.layer) * 2 + a.site) * a.Te + tl) * (uint64_t)a.D + col;
 #pragma unroll
   for (int k = 0; k < 8; k += 2) {
     const uint64_t r = draw_raw(sd, (n0 + k) >> 1);
@@ -464,6 +471,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const LnArgs a) {
   const int e = t / a.Te, tl = t - e * a.Te;
   const uint64_t sd = derive3(TAG_BERT_HDROP, a.seed, (uint64_t)(a.est_base + e));
   const uint32_t thr = threshold32(a.p);
+  const int64_t step = cur_step(a.step, a.step_dev);
   const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
   float x[NC][8];
   float sum = 0.f;
@@ -474,7 +482,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const LnArgs a) {
     ld8(a.resid + (size_t)t * a.D + col, r);
     ld8(a.bin + (size_t)t * a.D + col, b);
     ld8(a.bias + col, bi);
-    ln_mask8(a, sd, tl, col, thr, keep, m);
+    ln_mask8(a, step, sd, tl, col, thr, keep, m);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       x[c][k] = r[k] + (b[k] + bi[k]) * m[k];
@@ -515,6 +523,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const LnArgs a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t sd = derive3(TAG_BERT_HDROP, a.seed, (uint64_t)(a.est_base + e));
   const uint32_t thr = threshold32(a.p);
+  const int64_t step = cur_step(a.step, a.step_dev);
   const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
   float pg[NC][8], pb[NC][8], pr[NC][8];
 #pragma unroll
@@ -553,7 +562,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const LnArgs a) {
     for (int c = 0; c < NC; ++c) {
       const int col = c * 256 + lane * 8;
       float dx[8], m[8];
-      ln_mask8(a, sd, tl, col, thr, keep, m);
+      ln_mask8(a, step, sd, tl, col, thr, keep, m);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         dx[q] = (gg[c][q] - m1 - xh[c][q] * m2) * st.y;
@@ -606,8 +615,10 @@ __global__ void ln_fold_kernel(const float* __restrict__ part, int E, int chunks
 // ------------------------------------------------------------ data / head
 // X[t][d] = bf16(U[-1,1)) from (TAG_BERT_X, seed, EST) at counter (step*Te + tl)*D + d (bf16-exact, so the
 // fp32 residual copy and the GEMM operand agree); target 0.5*U[-1,1)
-__global__ void __launch_bounds__(256) data_kernel(uint64_t seed, int64_t step, int est_base, int Te, int D, int rows,
-                                                   float* X32, __nv_bfloat16* Xb, float* target) {
+__global__ void __launch_bounds__(256) data_kernel(uint64_t seed, int64_t step_h, const int64_t* step_dev, int est_base,
+                                                   int Te, int D, int rows, float* X32, __nv_bfloat16* Xb,
+                                                   float* target) {
+  const int64_t step = cur_step(step_h, step_dev);
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (t >= rows) return;
   const int e = t / Te, tl = t - e * Te;
@@ -703,9 +714,9 @@ static int ok_or_cuda_b() { return cudaGetLastError() == cudaSuccess ? OK : ERR_
 
 int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out, int n_seq, int Dm, int H,
                      int seqs_per_est, int est_base, int L, int layer, uint64_t seed, int64_t step, float p,
-                     cudaStream_t s) {
+                     const int64_t* step_dev, cudaStream_t s) {
   bert::AttnArgs a{(const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dctx, (__nv_bfloat16*)out, Dm, H, seqs_per_est,
-                   est_base, L, layer, n_seq * H, seed, step, p};
+                   est_base, L, layer, n_seq * H, seed, step, p, step_dev};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -760,7 +771,7 @@ static int ln_launch_nc(int backward, const bert::LnArgs& a, int E, cudaStream_t
 int bert_ln_launch(int backward, const float* in1, const void* in2, const float* bias, const float* gamma,
                    const float* beta, float* xsum, float* stats, float* y32, void* yb, float* part, int E, int Te,
                    int D, int est_base, int L, int layer, int site, uint64_t seed, int64_t step, float p, float eps,
-                   cudaStream_t s) {
+                   const int64_t* step_dev, cudaStream_t s) {
   if (D % 256 || D > 1024 || Te % bert::LN_CHUNK) return ERR_INPUT;
   bert::LnArgs a{};
   a.resid = in1;
@@ -783,6 +794,7 @@ int bert_ln_launch(int backward, const float* in1, const void* in2, const float*
   a.site = site;
   a.seed = seed;
   a.step = step;
+  a.step_dev = step_dev;
   a.p = p;
   a.eps = eps;
   switch (D / 256) {
@@ -802,10 +814,11 @@ int bert_ln_fold_launch(const float* part, int E, int Te, int D, float* dg, floa
 }
 
 int bert_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, float* X32, void* Xb,
-                     float* target, cudaStream_t s) {
+                     float* target, const int64_t* step_dev, cudaStream_t s) {
   if (D % 8) return ERR_INPUT;
   const int rows = E * Te;
-  bert::data_kernel<<<(rows + 7) / 8, 256, 0, s>>>(seed, step, est_base, Te, D, rows, X32, (__nv_bfloat16*)Xb, target);
+  bert::data_kernel<<<(rows + 7) / 8, 256, 0, s>>>(seed, step, step_dev, est_base, Te, D, rows, X32,
+                                                   (__nv_bfloat16*)Xb, target);
   return ok_or_cuda_b();
 }
 

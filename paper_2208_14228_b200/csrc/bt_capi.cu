@@ -55,15 +55,15 @@ int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, 
                                cudaStream_t s);
 int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out, int n_seq, int Dm, int H,
                      int seqs_per_est, int est_base, int L, int layer, uint64_t seed, int64_t step, float p,
-                     cudaStream_t s);
+                     const int64_t* step_dev, cudaStream_t s);
 int bert_ln_launch(int backward, const float* in1, const void* in2, const float* bias, const float* gamma,
                    const float* beta, float* xsum, float* stats, float* y32, void* yb, float* part, int E, int Te,
                    int D, int est_base, int L, int layer, int site, uint64_t seed, int64_t step, float p, float eps,
-                   cudaStream_t s);
+                   const int64_t* step_dev, cudaStream_t s);
 int bert_ln_fold_launch(const float* part, int E, int Te, int D, float* dg, float* db, float* dr, int64_t est_stride,
                         cudaStream_t s);
 int bert_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, float* X32, void* Xb,
-                     float* target, cudaStream_t s);
+                     float* target, const int64_t* step_dev, cudaStream_t s);
 int bert_mse_launch(const float* y, const float* tgt, int E, int Te, int D, void* dy, float* part, float* loss,
                     cudaStream_t s);
 int bert_cast_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* R, const int* C, int n,
@@ -632,27 +632,28 @@ static int bert_shape(int E, int Te, int D) {
   return 0;
 }
 int bt_bert_data(uint64_t seed, int64_t step, int32_t est_base, int32_t E, int32_t Te, int32_t D, float* x32_dev,
-                 void* xb_dev, float* target_dev, void* stream) {
+                 void* xb_dev, float* target_dev, const int64_t* step_dev, void* stream) {
   if (int st = bert_shape(E, Te, D)) return st;
   if (!x32_dev || !xb_dev || !target_dev) return fail(bt::ERR_INPUT, "null pointer");
-  return done(bt::bert_data_launch(seed, step, est_base, E, Te, D, x32_dev, xb_dev, target_dev, STREAM(stream)),
+  return done(bt::bert_data_launch(seed, step, est_base, E, Te, D, x32_dev, xb_dev, target_dev, step_dev,
+                                   STREAM(stream)),
               "bt_bert_data");
 }
 int bt_bert_attn(int32_t backward, const void* qkv_dev, const void* dctx_dev, void* out_dev, int32_t E, int32_t Te,
                  int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed, int64_t step,
-                 float p, void* stream) {
+                 float p, const int64_t* step_dev, void* stream) {
   if (int st = bert_shape(E, Te, D)) return st;
   if (heads * 64 != D) return fail(bt::ERR_INPUT, "bert attention: head dim must be 64 (heads %d, D %d)", heads, D);
   if (!qkv_dev || !out_dev || (backward && !dctx_dev)) return fail(bt::ERR_INPUT, "null pointer");
   if (!(p >= 0.f && p < 1.f) || layer < 0 || layer >= layers) return fail(bt::ERR_CONFIG, "bad dropout / layer");
   return done(bt::bert_attn_launch(backward, qkv_dev, dctx_dev, out_dev, E * Te / 128, D, heads, Te / 128, est_base,
-                                   layers, layer, seed, step, p, STREAM(stream)),
+                                   layers, layer, seed, step, p, step_dev, STREAM(stream)),
               "bt_bert_attn");
 }
 int bt_bert_ln_fwd(const float* resid_dev, const void* branch_dev, const float* bias_dev, const float* gamma_dev,
                    const float* beta_dev, float* xsum_dev, float* stats_dev, float* y32_dev, void* yb_dev, int32_t E,
                    int32_t Te, int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
-                   int64_t step, float p, float eps, void* stream) {
+                   int64_t step, float p, float eps, const int64_t* step_dev, void* stream) {
   if (int st = bert_shape(E, Te, D)) return st;
   if (!resid_dev || !branch_dev || !bias_dev || !gamma_dev || !beta_dev || !xsum_dev || !stats_dev || !y32_dev ||
       !yb_dev)
@@ -660,20 +661,20 @@ int bt_bert_ln_fwd(const float* resid_dev, const void* branch_dev, const float* 
   if (!(p >= 0.f && p < 1.f) || (site != 0 && site != 1)) return fail(bt::ERR_CONFIG, "bad dropout / site");
   return done(bt::bert_ln_launch(0, resid_dev, branch_dev, bias_dev, gamma_dev, beta_dev, xsum_dev, stats_dev, y32_dev,
                                  yb_dev, nullptr, E, Te, D, est_base, layers, layer, site, seed, step, p, eps,
-                                 STREAM(stream)),
+                                 step_dev, STREAM(stream)),
               "bt_bert_ln_fwd");
 }
 int bt_bert_ln_bwd(const void* dy1_dev, const float* dy2_dev, const float* xsum_dev, const float* stats_dev,
                    const float* gamma_dev, float* dx_dev, void* dbranch_dev, float* part_dev, int32_t E, int32_t Te,
                    int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
-                   int64_t step, float p, void* stream) {
+                   int64_t step, float p, const int64_t* step_dev, void* stream) {
   if (int st = bert_shape(E, Te, D)) return st;
   if (!dy1_dev || !xsum_dev || !stats_dev || !gamma_dev || !dx_dev || !dbranch_dev || !part_dev)
     return fail(bt::ERR_INPUT, "null pointer");
   if (!(p >= 0.f && p < 1.f) || (site != 0 && site != 1)) return fail(bt::ERR_CONFIG, "bad dropout / site");
   return done(bt::bert_ln_launch(1, dy2_dev, dy1_dev, nullptr, gamma_dev, nullptr, (float*)xsum_dev,
                                  (float*)stats_dev, dx_dev, dbranch_dev, part_dev, E, Te, D, est_base, layers, layer,
-                                 site, seed, step, p, 0.f, STREAM(stream)),
+                                 site, seed, step, p, 0.f, step_dev, STREAM(stream)),
               "bt_bert_ln_bwd");
 }
 int bt_bert_ln_fold(const float* part_dev, int32_t E, int32_t Te, int32_t D, float* dgamma_dev, float* dbeta_dev,

@@ -306,3 +306,14 @@ def test_adam_update(bert):
     for _ in range(2):
         assert np.array_equal(_bits(a.step()), _bits(b.step([2, 2])))
     assert np.array_equal(_bits(a.params), _bits(b.params))
+
+
+def test_cuda_graph_replay_equals_eager(bert):
+    """The captured step (one CUDA graph: every launch group, the reducer, the weight refresh, the device
+    step counter) replays bit-identically to eager execution, step after step."""
+    a = bert.BertJob(graph=True, **SMALL)
+    b = bert.BertJob(graph=False, **SMALL)
+    for _ in range(4):
+        assert np.array_equal(_bits(a.step()), _bits(b.step()))
+    assert a._graph is not None and b._graph is None
+    assert np.array_equal(_bits(a.params), _bits(b.params)) and int(a._step_dev.item()) == 4
