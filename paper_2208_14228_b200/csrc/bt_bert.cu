@@ -514,10 +514,13 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const LnArgs a) {
   if (lane == 0) a.stats[t] = make_float2(mean, rstd);
 }
 
-// block = (local EST e, 64-row chunk k); warp w handles rows w, w+8, ... of the chunk in order
+// block = (local EST e, 64-row chunk k); warp w handles rows w, w+8, ... of the chunk in order.
+// Each warp's column partials (dgamma, dbeta, dbias terms) accumulate in its own shared-memory rows
+// (same per-lane columns, same row order as a register accumulator would -- the registers are what
+// limited residency), then the 8 warps' partials are folded in warp order.
 template <int NC>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(const LnArgs a) {
-  extern __shared__ float ln_smem[];  // [8 warps][D]
+__global__ void __launch_bounds__(256, 2) ln_bwd_kernel(const LnArgs a) {
+  extern __shared__ float ln_smem[];  // [8 warps][3][D]
   const int chunks = a.Te / LN_CHUNK;
   const int e = blockIdx.x / chunks, k = blockIdx.x - e * chunks;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -525,11 +528,9 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const LnArgs a) {
   const uint32_t thr = threshold32(a.p);
   const int64_t step = cur_step(a.step, a.step_dev);
   const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
-  float pg[NC][8], pb[NC][8], pr[NC][8];
-#pragma unroll
-  for (int c = 0; c < NC; ++c)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) pg[c][q] = pb[c][q] = pr[c][q] = 0.f;
+  float* const pw = ln_smem + (size_t)w * 3 * a.D;  // this warp's [3][D] partials
+  for (int i = lane * 4; i < 3 * a.D; i += 128) *(float4*)(pw + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();
   for (int rr = w; rr < LN_CHUNK; rr += 8) {
     const int tl = k * LN_CHUNK + rr;
     const size_t t = (size_t)e * a.Te + tl;
@@ -561,38 +562,35 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const LnArgs a) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int col = c * 256 + lane * 8;
-      float dx[8], m[8];
+      float dx[8], m[8], pg[8], pb[8], pr[8];
       ln_mask8(a, step, sd, tl, col, thr, keep, m);
+      ld8(pw + col, pg);
+      ld8(pw + a.D + col, pb);
+      ld8(pw + 2 * a.D + col, pr);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         dx[q] = (gg[c][q] - m1 - xh[c][q] * m2) * st.y;
-        pg[c][q] += dy[c][q] * xh[c][q];
-        pb[c][q] += dy[c][q];
+        pg[q] += dy[c][q] * xh[c][q];
+        pb[q] += dy[c][q];
       }
       st8(a.y32 + t * a.D + col, dx);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         dx[q] *= m[q];
-        pr[c][q] += dx[q];
+        pr[q] += dx[q];
       }
       st8(a.yb + t * a.D + col, dx);
+      st8(pw + col, pg);
+      st8(pw + a.D + col, pb);
+      st8(pw + 2 * a.D + col, pr);
     }
   }
-  // warp partials -> smem ([8][D], one quantity at a time: 8*D floats keep several blocks per SM
-  // resident), folded in warp order -> this chunk's partial
+  __syncthreads();
   float* out = a.part + (size_t)blockIdx.x * 3 * a.D;
-#pragma unroll
-  for (int qi = 0; qi < 3; ++qi) {
-    if (qi) __syncthreads();  // the previous quantity's fold has read the buffer
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-      st8(ln_smem + (size_t)w * a.D + c * 256 + lane * 8, qi == 0 ? pg[c] : (qi == 1 ? pb[c] : pr[c]));
-    __syncthreads();
-    for (int i = threadIdx.x; i < a.D; i += 256) {
-      float acc = ln_smem[i];
-      for (int ww = 1; ww < 8; ++ww) acc += ln_smem[(size_t)ww * a.D + i];
-      out[(size_t)qi * a.D + i] = acc;
-    }
+  for (int i = threadIdx.x; i < 3 * a.D; i += 256) {
+    float acc = ln_smem[i];
+    for (int ww = 1; ww < 8; ++ww) acc += ln_smem[(size_t)ww * 3 * a.D + i];
+    out[i] = acc;
   }
 }
 
@@ -753,11 +751,11 @@ static int ln_launch_nc(int backward, const bert::LnArgs& a, int E, cudaStream_t
   if (!backward) {
     bert::ln_fwd_kernel<NC><<<(a.rows + 7) / 8, 256, 0, s>>>(a);
   } else {
-    const int smem = 8 * a.D * (int)sizeof(float);
+    const int smem = 8 * 3 * a.D * (int)sizeof(float);
     static bool attr = false;
     if (!attr) {
       if (cudaFuncSetAttribute(bert::ln_bwd_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               8 * 256 * NC * (int)sizeof(float)) != cudaSuccess)
+                               8 * 3 * 256 * NC * (int)sizeof(float)) != cudaSuccess)
         return ERR_CUDA;
       attr = true;
     }
