@@ -510,21 +510,21 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t local, uint32_t rank) {
 
 constexpr int PAIR_BN = 256, PAIR_M = 256;
 
-template <int STAGES>
+template <int STAGES, int EW = EPI_WARPS>
 struct PairSmem {
   static constexpr int A_BYTES = BM * BK * 2, B_BYTES = (PAIR_BN / 2) * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int EPI = STAGES * STAGE;
-  static constexpr int BAR = EPI + EPI_WARPS * EPI_STAGE;
+  static constexpr int BAR = EPI + EW * EPI_STAGE;
   static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
 };
 
-template <int STAGES, bool OUT_BF16, bool MN>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int STAGES, bool OUT_BF16, bool MN, int EW = EPI_WARPS>  // EW epilogue warps (16 for ALU-heavy epilogues)
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
     gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                              const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2,
                              int M, int N, int K, int batch, const GemmEpi epi) {
-  using L = PairSmem<STAGES>;
+  using L = PairSmem<STAGES, EW>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 2 * EPI_WARPS);  // leader: every epilogue warp of both CTAs
+      mbar_init(tempty(a), 2 * EW);  // leader: every epilogue warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row0 = m0 + (int)rank * BM + lg * 32;
       const size_t row = (size_t)row0 + lane;
 #pragma unroll 1
-      for (int cc = half * (PAIR_BN / EPI_SPLIT); cc < (half + 1) * (PAIR_BN / EPI_SPLIT); cc += 32) {
+      for (int cc = half * (PAIR_BN / (EW / 4)); cc < (half + 1) * (PAIR_BN / (EW / 4)); cc += 32) {
         uint32_t v[32];
         const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * PAIR_BN + cc);
         asm volatile(
@@ -822,7 +822,7 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
-template <int STAGES, bool OUT_BF16, bool MN>
+template <int STAGES, bool OUT_BF16, bool MN, int EW = gemm::EPI_WARPS>
 static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
   const int M = g.M, N = g.N, K = g.K;
   CUtensorMap ma, mb, mc, mc2;
@@ -833,8 +833,8 @@ static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
       !make_store_map(&mc, g.c, M, N, g.batch, g.sc, OUT_BF16) ||
       !make_store_map(&mc2, g.epi.out2 ? (const void*)g.epi.out2 : g.c, M, N, g.batch, g.sc, OUT_BF16))
     return ERR_CUDA;
-  auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16, MN>;
-  const int smem = gemm::PairSmem<STAGES>::TOTAL + 1024;
+  auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16, MN, EW>;
+  const int smem = gemm::PairSmem<STAGES, EW>::TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -853,7 +853,7 @@ static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
   if (grid > 2 * tiles) grid = 2 * tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(gemm::THREADS);
+  cfg.blockDim = dim3(64 + 32 * EW);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr_[1];
@@ -877,8 +877,11 @@ template <bool MN>
 static int launch_any(const GemmShape& g, int out_bf16, int grid, cudaStream_t s) {
   constexpr int SP = gemm::EPI_WARPS == 8 ? 5 : 3, S256 = gemm::EPI_WARPS == 8 ? 3 : 2,
                 S64 = gemm::EPI_WARPS == 8 ? 6 : 4, S128 = gemm::EPI_WARPS == 8 ? 5 : 3;
-  if (g.M % 256 == 0 && g.N % 256 == 0 && gemm_variant() != 1)
+  if (g.M % 256 == 0 && g.N % 256 == 0 && gemm_variant() != 1) {
+    if (g.epi.kind == EPI_FFN_FWD)  // the ALU-heavy GELU epilogue: 16 epilogue warps
+      return launch_gemm_pair<3, true, MN, 16>(g, grid, s);
     return out_bf16 ? launch_gemm_pair<SP, true, MN>(g, grid, s) : launch_gemm_pair<SP, false, MN>(g, grid, s);
+  }
   if (g.N % 256 == 0)
     return out_bf16 ? launch_gemm<256, S256, true, MN>(g, grid, s) : launch_gemm<256, S256, false, MN>(g, grid, s);
   if (g.N <= 64)  // narrow outputs (64-channel convolutions)
