@@ -1,0 +1,243 @@
+// bt_attn_tc.cu -- BERT attention forward on the 5th-generation tensor cores (C4).
+//
+// One (sequence, head) item per iteration of a persistent CTA of 4 warps; thread i owns query row i:
+//   TMA      Q, K [128][64] (K-major, 128 B swizzle) and V as two MN-major 64x64 boxes;
+//   tcgen05  S = Q K^T (M = 128, N = 128, K = 64) into TMEM columns [0, 128);
+//   softmax  each thread loads ITS row of S from TMEM (tcgen05.ld: max, exp2 row sum in column order,
+//            then P -- three passes, few registers), applies the attention-probability dropout keyed
+//            exactly as the mma.sync kernel keys it (bt_bert.cu: one splitmix64 draw per (16-row
+//            block, row, column pair), 16-bit fields; rows i and i^8 share a draw, computed by one
+//            of the two lanes and exchanged by shuffle), and writes the bf16 row of P into a K-major
+//            swizzled shared tile;
+//   tcgen05  O = P V (M = 128, N = 64, K = 128; V MN-major) into TMEM columns [0, 64) (S's, consumed);
+//   store    each thread its row of O (bf16).
+// Every output element is produced by a fixed instruction sequence over its own inputs: the bits do
+// not depend on the grid, the item order or which ESTs share the launch.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bt_common.cuh"
+#include "bt_tc.cuh"
+
+namespace bt {
+bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows, int batch, int64_t bstride);
+bool make_map_mn(CUtensorMap* map, const void* ptr, int rows, int K, int batch, int64_t bstride);
+
+namespace attn_tc {
+using namespace tc;
+
+constexpr uint64_t TAG_BERT_ADROP = 0x4245'5254'4144'5250ull;  // == bt_bert.cu (same masks)
+constexpr int SEQ = 128, HD = 64, THREADS = 128;
+// P (bf16, two K-major k-blocks) reuses the Q/K tiles once the S product has consumed them; O reuses
+// S's TMEM columns once every thread holds its row statistics: 48 KB + 128 TMEM columns per CTA, so
+// four CTAs (16 warps) share an SM and hide each other's load / MMA / softmax latency.
+constexpr int OFF_Q = 0, OFF_K = 16384, OFF_P = 0, OFF_V = 32768, OFF_BAR = 49152;
+constexpr int SMEM = OFF_BAR + 64 + 1024;  // + alignment slack
+constexpr int TMEM_COLS = 128;             // S: [0, 128); then O: [0, 64)
+
+struct Args {
+  __nv_bfloat16* out;  // ctx [T][Dm]
+  int Dm, H, seqs_per_est, est_base, L, layer, n_items;
+  uint64_t seed;
+  int64_t step;
+  float p;
+  const int64_t* step_dev;
+};
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *(const uint32_t*)&v;
+}
+
+__global__ void __launch_bounds__(THREADS, 4)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mqk, const __grid_constant__ CUtensorMap mv, const Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw), base = (raw + 1023u) & ~1023u;
+  uint8_t* const gbase = smem_raw + (base - raw);
+  const uint32_t bar_ld = base + OFF_BAR, bar_s = bar_ld + 8, bar_o = bar_ld + 16;
+  uint32_t* const tmem_slot = (uint32_t*)(gbase + OFF_BAR + 32);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mqk) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mv) : "memory");
+    mbar_init(bar_ld, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_o, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's TMEM lane quarter
+  const int64_t step = a.step_dev ? *a.step_dev : a.step;
+  const uint32_t thr = a.p > 0.f ? (uint32_t)ceil((double)a.p * 65536.0) : 0u;
+  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
+  constexpr float SC = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
+  const int hi = (tid >> 3) & 1;                       // rows i, i^8 share draws (lanes l, l^8)
+  int n = 0;
+  for (int it = blockIdx.x; it < a.n_items; it += gridDim.x, ++n) {
+    const int s = it / a.H, h = it - (it / a.H) * a.H;
+    const uint32_t ph = n & 1;
+    if (tid == 0) {
+      mbar_arrive_expect_tx(bar_ld, 3 * 16384);
+      tma_load_3d(base + OFF_Q, &mqk, h * HD, s * SEQ, 0, bar_ld);
+      tma_load_3d(base + OFF_K, &mqk, a.Dm + h * HD, s * SEQ, 0, bar_ld);
+      tma_load_3d(base + OFF_V, &mv, 2 * a.Dm + h * HD, s * SEQ, 0, bar_ld);
+      tma_load_3d(base + OFF_V + 8192, &mv, 2 * a.Dm + h * HD, s * SEQ + 64, 0, bar_ld);
+      mbar_wait(bar_ld, ph);
+      tc_fence_after();
+      constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
+      const uint64_t dq = kmajor_sw128_desc(base + OFF_Q), dk = kmajor_sw128_desc(base + OFF_K);
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k) tc_mma(tmem, dq + 2 * k, dk + 2 * k, idS, k != 0);
+      tc_commit(bar_s);
+    }
+    mbar_wait(bar_s, ph);
+    tc_fence_after();
+    // this thread's row of S, three passes over TMEM (row max; exp2 row sum in column order; P)
+    // (exp2 arguments x*SC - m as one FMA; MUFU ex2 directly: arguments are <= 0)
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < SEQ / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(lane_base + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 32; ++q) mx = fmaxf(mx, __uint_as_float(v[q]));
+    }
+    const float nm = -__fmul_rn(mx, SC);  // -max(x*SC), SC > 0
+    float l = 0.f;
+#pragma unroll
+    for (int c = 0; c < SEQ / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(lane_base + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 32; ++q) l += ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm));
+    }
+    const float inv = 1.f / l;
+    // dropout keyed by (EST, step, layer, sequence, head, row, column pair) -- bt_bert.cu's layout
+    const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
+    const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
+    const uint64_t nb = ((((uint64_t)step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4) +
+                        (uint64_t)((tid >> 4) * 8 + (tid & 7)) * 64;
+    const int fsh = hi * 32;  // this row's two 16-bit fields of each draw
+    uint8_t* const prow = gbase + OFF_P + tid * 128;
+#pragma unroll
+    for (int c = 0; c < SEQ / 32; ++c) {  // 32 columns = 16 column pairs; this lane draws 8, its partner 8
+      uint32_t v[32];
+      tmem_ld32(lane_base + c * 32, v);
+      tmem_ld_wait();
+      uint32_t f[16];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        uint64_t r = 0;
+        if (thr) r = draw_raw(sd, nb + (uint64_t)(c * 16 + 2 * t + hi));
+        const uint64_t o = __shfl_xor_sync(0xffffffffu, r, 8);  // the partner row's draw: pair 2t + !hi
+        const uint64_t r_even = hi ? o : r, r_odd = hi ? r : o;
+        f[2 * t] = (uint32_t)(r_even >> fsh);
+        f[2 * t + 1] = (uint32_t)(r_odd >> fsh);
+      }
+      const int kb = c >> 1;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {  // four 16-byte chunks (8 columns each) of this 32-column slice
+        uint32_t w[4];
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+          const int q = cc * 8 + 2 * hh;  // column c*32 + q, pair index q / 2
+          const float p0 = ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm)) * inv;
+          const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(v[q + 1]), SC, nm)) * inv;
+          float m0 = 1.f, m1 = 1.f;
+          if (thr) {
+            m0 = (f[q >> 1] & 0xFFFFu) < thr ? 0.f : keep;
+            m1 = (f[q >> 1] >> 16) < thr ? 0.f : keep;
+          }
+          w[hh] = pack2(p0 * m0, p1 * m1);
+        }
+        const int chunk = (c & 1) * 4 + cc;  // 16-byte chunk within the 128-byte row of k-block kb
+        *(uint4*)(prow + kb * 16384 + ((chunk ^ (tid & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      constexpr uint32_t idO = idesc_bf16(128, HD, false, true);
+      const uint64_t dv = mnmajor_sw128_desc(base + OFF_V);
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb) {
+        const uint64_t dp = kmajor_sw128_desc(base + OFF_P + kb * 16384);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma(tmem, dp + 2 * k, dv + (uint64_t)(kb * 4 + k) * (2048 >> 4), idO, (kb | k) != 0);
+      }
+      tc_commit(bar_o);
+    }
+    mbar_wait(bar_o, ph);
+    tc_fence_after();
+    uint4* const orow = (uint4*)(a.out + ((size_t)s * SEQ + tid) * a.Dm + h * HD);
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(lane_base + c * 32, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        orow[c * 4 + q] =
+            make_uint4(pack2(__uint_as_float(v[8 * q]), __uint_as_float(v[8 * q + 1])),
+                       pack2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3])),
+                       pack2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
+                       pack2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
+    }
+    tc_fence_before();
+    __syncthreads();  // TMEM and the shared tiles are free for the next item
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+}  // namespace attn_tc
+
+int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int seqs_per_est, int est_base, int L,
+                       int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev, cudaStream_t s) {
+  const int T = n_seq * attn_tc::SEQ;
+  CUtensorMap mqk, mv;
+  if (!make_map(&mqk, qkv, T, 3 * Dm, attn_tc::SEQ, 1, (int64_t)T * 3 * Dm) ||
+      !make_map_mn(&mv, qkv, 3 * Dm, T, 1, (int64_t)T * 3 * Dm))
+    return ERR_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(attn_tc::attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             attn_tc::SMEM) != cudaSuccess)
+      return ERR_CUDA;
+    attr = true;
+  }
+  attn_tc::Args a{(__nv_bfloat16*)out, Dm, H, seqs_per_est, est_base, L, layer, n_seq * H, seed, step, p, step_dev};
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = a.n_items < 4 * sms ? a.n_items : 4 * sms;
+  attn_tc::attn_fwd_tc_kernel<<<grid, attn_tc::THREADS, attn_tc::SMEM, s>>>(mqk, mv, a);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+
+}  // namespace bt

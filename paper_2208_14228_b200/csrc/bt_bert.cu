@@ -30,6 +30,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "bt_common.cuh"
 
@@ -708,6 +709,12 @@ __global__ void __launch_bounds__(256) cast_t_kernel(const __grid_constant__ Cas
 }  // namespace bert
 
 // ----------------------------------------------------------------- launchers
+int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int seqs_per_est, int est_base, int L,
+                       int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev, cudaStream_t s);
+static bool attn_tc_enabled() {  // BT_ATTN_TC=0: the mma.sync forward (bt_bert.cu) instead of bt_attn_tc.cu
+  const char* e = getenv("BT_ATTN_TC");
+  return !(e && e[0] == '0');
+}
 static int ok_or_cuda_b() { return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA; }
 
 int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out, int n_seq, int Dm, int H,
@@ -718,6 +725,8 @@ int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out,
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (!backward && attn_tc_enabled())
+    return attn_fwd_tc_launch(qkv, out, n_seq, Dm, H, seqs_per_est, est_base, L, layer, seed, step, p, step_dev, s);
   if (!backward) {
     static bool attr = false;
     if (!attr) {

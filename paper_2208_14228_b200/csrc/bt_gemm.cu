@@ -31,6 +31,7 @@
 
 #include "bt_common.cuh"
 #include "bt_ffn.cuh"
+#include "bt_tc.cuh"
 
 namespace bt {
 namespace gemm {
@@ -43,77 +44,8 @@ constexpr int EPI_WARPS = BT_EPI_WARPS;  // EPI_WARPS/4 per TMEM lane group, eac
 constexpr int EPI_SPLIT = EPI_WARPS / 4;
 constexpr int THREADS = 64 + 32 * EPI_WARPS;
 
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+using namespace tc;  // bt_tc.cuh: mbarriers, TMA, tcgen05, UMMA descriptors
 
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// Bounded wait: a pipeline bug traps (a launch error) instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  if (mbar_try(bar, parity)) return;
-  const long long t0 = clock64();
-  while (!mbar_try(bar, parity))
-    if (clock64() - t0 > (1ll << 33)) __trap();
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z,
-                                            uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-          "r"(dst),
-      "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, int acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
-// K-major, 128-byte-swizzled operand tile: rows of 64 bf16 (128 B), 8-row
-// swizzle atoms 1024 B apart.  UMMA shared-memory descriptor (sm_100):
-// start>>4 [0,14), LBO>>4 [16,30) = 1 (unused for swizzled K-major),
-// SBO>>4 [32,46) = 1024>>4, version [46,48) = 1, base offset 0,
-// layout type [61,64) = 2 (SWIZZLE_128B).
-__device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-
-// MN-major, 128-byte-swizzled operand tile (A^T / B^T stored token-major, e.g. an activation
-// matrix X[k][m] read as the K x M operand): TMA boxes of 64 MN-elements (128 B) x 64 k-rows,
-// one box per 64-wide MN block, 8 KB apart.  Canonical UMMA MN-major SW128 layout
-// ((8,n),(8,k)) : ((1,LBO),(8,SBO)) in 16-byte units: LBO = 8192 B between MN blocks,
-// SBO = 1024 B between 8-row k groups; a 16-deep UMMA k step advances 2 groups (2048 B).
-constexpr int MN_BLOCK_BYTES = 64 * BK * 2;
-__device__ __forceinline__ uint64_t mnmajor_sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(MN_BLOCK_BYTES >> 4) << 16) |
-         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
 template <bool MN>
 __device__ __forceinline__ uint64_t op_desc(uint32_t saddr) {
   return MN ? mnmajor_sw128_desc(saddr) : kmajor_sw128_desc(saddr);
@@ -705,7 +637,7 @@ static PFN_encodeTiled encode_fn() {
 
 // [batch][rows][K] bf16, K contiguous, batch entries `bstride` elements apart;
 // box = 64 (128 B) x box_rows x 1, 128-byte swizzle
-static bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows, int batch, int64_t bstride) {
+bool make_map(CUtensorMap* map, const void* ptr, int rows, int K, int box_rows, int batch, int64_t bstride) {
   PFN_encodeTiled enc = encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
@@ -735,7 +667,7 @@ static bool make_store_map(CUtensorMap* map, const void* ptr, int rows, int cols
 }
 
 // MN-major operand: stored [batch][K][rows] (rows contiguous); box = 64 (128 B) x 64 k-rows x 1
-static bool make_map_mn(CUtensorMap* map, const void* ptr, int rows, int K, int batch, int64_t bstride) {
+bool make_map_mn(CUtensorMap* map, const void* ptr, int rows, int K, int batch, int64_t bstride) {
   PFN_encodeTiled enc = encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)K, (cuuint64_t)batch};

@@ -317,3 +317,34 @@ def test_cuda_graph_replay_equals_eager(bert):
         assert np.array_equal(_bits(a.step()), _bits(b.step()))
     assert a._graph is not None and b._graph is None
     assert np.array_equal(_bits(a.params), _bits(b.params)) and int(a._step_dev.item()) == 4
+
+
+def test_tcgen05_attention_forward_matches_mma_sync(bert, monkeypatch):
+    """The tcgen05 attention forward (bt_attn_tc.cu: S and PV on the 5th-gen tensor cores, one softmax
+    row per thread) and the mma.sync forward apply the same keyed dropout masks to the same softmax:
+    their ctx agree to bf16 rounding (<= 1% of elements one ulp apart), each is run-to-run bitwise
+    stable, and the tcgen05 path keeps the grouping invariance."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    job = bert.BertJob(**SMALL)
+    cap = {}
+    job.step(capture=cap)
+    qkv = cap["qkv"]
+    E, Te, D, H = job.E, job.Te, job.D, job.H
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("BT_ATTN_TC", mode)
+        o = torch.empty(E * Te, D, dtype=torch.bfloat16, device="cuda")
+        _native.check(_native.lib().bt_bert_attn(0, qkv.data_ptr(), None, o.data_ptr(), E, Te, D, H, 0, job.L, 0,
+                                                 job.seed, 0, job.pa, None, stream()))
+        o2 = torch.empty_like(o)
+        _native.check(_native.lib().bt_bert_attn(0, qkv.data_ptr(), None, o2.data_ptr(), E, Te, D, H, 0, job.L, 0,
+                                                 job.seed, 0, job.pa, None, stream()))
+        assert torch.equal(o.view(torch.int16), o2.view(torch.int16))
+        outs[mode] = o
+    monkeypatch.delenv("BT_ATTN_TC")
+    a, b = _d(outs["1"]), _d(outs["0"])
+    assert torch.equal(a, _d(cap["ctx"]))  # the step used the tcgen05 path
+    assert (a != b).double().mean().item() <= 1e-2
+    assert ((a - b).norm() / b.norm()).item() <= 5e-3
