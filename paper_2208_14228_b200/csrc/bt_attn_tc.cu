@@ -56,6 +56,48 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *(const uint32_t*)&v;
 }
 
+// This thread's softmax row statistics from S in TMEM columns [0, 128) of its lane: nm = -max(x*SC)
+// and inv = 1 / sum exp2(x*SC + nm), the sum in column order (exp2 arguments as one FMA; MUFU ex2
+// directly: arguments are <= 0).  The forward and the backward call this same sequence: same bits.
+constexpr float SC = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
+__device__ __forceinline__ void row_stats(uint32_t lane_base, float* nm_out, float* inv_out) {
+  float mx = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < SEQ / 32; ++c) {
+    uint32_t v[32];
+    tmem_ld32(lane_base + c * 32, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q = 0; q < 32; ++q) mx = fmaxf(mx, __uint_as_float(v[q]));
+  }
+  const float nm = -__fmul_rn(mx, SC);
+  float l = 0.f;
+#pragma unroll
+  for (int c = 0; c < SEQ / 32; ++c) {
+    uint32_t v[32];
+    tmem_ld32(lane_base + c * 32, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q = 0; q < 32; ++q) l += ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm));
+  }
+  *nm_out = nm;
+  *inv_out = 1.f / l;
+}
+// The 16 mask fields (one per column pair) of this row's 32-column slice c: rows i and i^8 share a
+// draw; each of the two lanes computes half of the slice's draws and they exchange by shuffle.
+__device__ __forceinline__ void row_fields(uint64_t sd, uint64_t nb, int c, int hi, uint32_t thr, uint32_t* f) {
+  const int fsh = hi * 32;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    uint64_t r = 0;
+    if (thr) r = draw_raw(sd, nb + (uint64_t)(c * 16 + 2 * t + hi));
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, r, 8);  // the partner row's draw: pair 2t + !hi
+    const uint64_t r_even = hi ? o : r, r_odd = hi ? r : o;
+    f[2 * t] = (uint32_t)(r_even >> fsh);
+    f[2 * t + 1] = (uint32_t)(r_odd >> fsh);
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 4)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mqk, const __grid_constant__ CUtensorMap mv, const Args a) {
   extern __shared__ uint8_t smem_raw[];
@@ -86,7 +128,6 @@ __global__ void __launch_bounds__(THREADS, 4)
   const int64_t step = a.step_dev ? *a.step_dev : a.step;
   const uint32_t thr = a.p > 0.f ? (uint32_t)ceil((double)a.p * 65536.0) : 0u;
   const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
-  constexpr float SC = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
   const int hi = (tid >> 3) & 1;                       // rows i, i^8 share draws (lanes l, l^8)
   int n = 0;
   for (int it = blockIdx.x; it < a.n_items; it += gridDim.x, ++n) {
@@ -109,33 +150,13 @@ __global__ void __launch_bounds__(THREADS, 4)
     mbar_wait(bar_s, ph);
     tc_fence_after();
     // this thread's row of S, three passes over TMEM (row max; exp2 row sum in column order; P)
-    // (exp2 arguments x*SC - m as one FMA; MUFU ex2 directly: arguments are <= 0)
-    float mx = -INFINITY;
-#pragma unroll
-    for (int c = 0; c < SEQ / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld32(lane_base + c * 32, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 32; ++q) mx = fmaxf(mx, __uint_as_float(v[q]));
-    }
-    const float nm = -__fmul_rn(mx, SC);  // -max(x*SC), SC > 0
-    float l = 0.f;
-#pragma unroll
-    for (int c = 0; c < SEQ / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld32(lane_base + c * 32, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 32; ++q) l += ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm));
-    }
-    const float inv = 1.f / l;
+    float nm, inv;
+    row_stats(lane_base, &nm, &inv);
     // dropout keyed by (EST, step, layer, sequence, head, row, column pair) -- bt_bert.cu's layout
     const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
     const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
     const uint64_t nb = ((((uint64_t)step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4) +
                         (uint64_t)((tid >> 4) * 8 + (tid & 7)) * 64;
-    const int fsh = hi * 32;  // this row's two 16-bit fields of each draw
     uint8_t* const prow = gbase + OFF_P + tid * 128;
 #pragma unroll
     for (int c = 0; c < SEQ / 32; ++c) {  // 32 columns = 16 column pairs; this lane draws 8, its partner 8
@@ -143,15 +164,7 @@ __global__ void __launch_bounds__(THREADS, 4)
       tmem_ld32(lane_base + c * 32, v);
       tmem_ld_wait();
       uint32_t f[16];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        uint64_t r = 0;
-        if (thr) r = draw_raw(sd, nb + (uint64_t)(c * 16 + 2 * t + hi));
-        const uint64_t o = __shfl_xor_sync(0xffffffffu, r, 8);  // the partner row's draw: pair 2t + !hi
-        const uint64_t r_even = hi ? o : r, r_odd = hi ? r : o;
-        f[2 * t] = (uint32_t)(r_even >> fsh);
-        f[2 * t + 1] = (uint32_t)(r_odd >> fsh);
-      }
+      row_fields(sd, nb, c, hi, thr, f);
       const int kb = c >> 1;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {  // four 16-byte chunks (8 columns each) of this 32-column slice
@@ -215,6 +228,235 @@ __global__ void __launch_bounds__(THREADS, 4)
   }
 }
 
+
+// ---------------------------------------------------------------------------------------- backward
+// Per (sequence, head) item, thread i owns query row i for the row work and key row i for dK / dV:
+//   TMA      Q, K, V, dO [128][64] K-major tiles (each tile is also read MN-major by the products
+//            that need its transpose: the bytes of a K-major [r][64] tile are the MN-major layout of
+//            its [64][r] view);
+//   tcgen05  S = Q K^T -> TMEM [0,128), dPd = dO V^T -> TMEM [128,256);
+//   rows     P recomputed by the forward's exact sequence (row_stats), masks, dP = dPd * mask,
+//            D = sum dP*P (column order), dS = P (dP - D) / 8 -> shared (K-major [q][key]);
+//            the dropped P kept packed in registers;
+//   tcgen05  dQ = dS K -> [0,64), dK = dS^T Q -> [64,128); then Pd (from registers) replaces dS in
+//            shared memory and dV = Pd^T dO -> [128,192);
+//   store    dq / dk / dv rows into dqkv (bf16).
+constexpr int B_OFF_Q = 0, B_OFF_K = 16384, B_OFF_V = 32768, B_OFF_DO = 49152, B_OFF_S = 65536, B_OFF_BAR = 98304;
+constexpr int B_SMEM = B_OFF_BAR + 64 + 1024;
+constexpr int B_TMEM_COLS = 256;
+
+// MN-major SW128 descriptor with an explicit distance between 64-wide MN blocks
+__device__ __forceinline__ uint64_t mn_desc(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+struct BwdArgs {
+  __nv_bfloat16* dqkv;  // [T][3*Dm]
+  int Dm, H, seqs_per_est, est_base, L, layer, n_items;
+  uint64_t seed;
+  int64_t step;
+  float p;
+  const int64_t* step_dev;
+};
+
+__device__ __forceinline__ void store_row64(__nv_bfloat16* dst, uint32_t taddr) {
+  uint4* const o = (uint4*)dst;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t v[32];
+    tmem_ld32(taddr + c * 32, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      o[c * 4 + q] = make_uint4(pack2(__uint_as_float(v[8 * q]), __uint_as_float(v[8 * q + 1])),
+                                pack2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3])),
+                                pack2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
+                                pack2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 2)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap mqk, const __grid_constant__ CUtensorMap mdo,
+                       const BwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw), base = (raw + 1023u) & ~1023u;
+  uint8_t* const gbase = smem_raw + (base - raw);
+  const uint32_t bar_ld = base + B_OFF_BAR, bar_s = bar_ld + 8, bar_a = bar_ld + 16, bar_v = bar_ld + 24;
+  uint32_t* const tmem_slot = (uint32_t*)(gbase + B_OFF_BAR + 40);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mqk) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mdo) : "memory");
+    mbar_init(bar_ld, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_a, 1);
+    mbar_init(bar_v, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(B_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  const int64_t step = a.step_dev ? *a.step_dev : a.step;
+  const uint32_t thr = a.p > 0.f ? (uint32_t)ceil((double)a.p * 65536.0) : 0u;
+  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
+  const int hi = (tid >> 3) & 1;
+  const int ld = 3 * a.Dm;
+  int n = 0;
+  for (int it = blockIdx.x; it < a.n_items; it += gridDim.x, ++n) {
+    const int s = it / a.H, h = it - (it / a.H) * a.H;
+    const uint32_t ph = n & 1;
+    if (tid == 0) {
+      mbar_arrive_expect_tx(bar_ld, 4 * 16384);
+      tma_load_3d(base + B_OFF_Q, &mqk, h * HD, s * SEQ, 0, bar_ld);
+      tma_load_3d(base + B_OFF_K, &mqk, a.Dm + h * HD, s * SEQ, 0, bar_ld);
+      tma_load_3d(base + B_OFF_V, &mqk, 2 * a.Dm + h * HD, s * SEQ, 0, bar_ld);
+      tma_load_3d(base + B_OFF_DO, &mdo, h * HD, s * SEQ, 0, bar_ld);
+      mbar_wait(bar_ld, ph);
+      tc_fence_after();
+      constexpr uint32_t id128 = idesc_bf16(128, 128, false, false);
+      const uint64_t dq = kmajor_sw128_desc(base + B_OFF_Q), dk = kmajor_sw128_desc(base + B_OFF_K);
+      const uint64_t dv = kmajor_sw128_desc(base + B_OFF_V), ddo = kmajor_sw128_desc(base + B_OFF_DO);
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k) tc_mma(tmem, dq + 2 * k, dk + 2 * k, id128, k != 0);         // S
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k) tc_mma(tmem + 128, ddo + 2 * k, dv + 2 * k, id128, k != 0);  // dPd
+      tc_commit(bar_s);
+    }
+    mbar_wait(bar_s, ph);
+    tc_fence_after();
+    float nm, inv;
+    row_stats(lane_base, &nm, &inv);
+    const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
+    const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
+    const uint64_t nb = ((((uint64_t)step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4) +
+                        (uint64_t)((tid >> 4) * 8 + (tid & 7)) * 64;
+    // pass 3: dropped P (packed, registers), mask bits, D = sum dP * P in column order
+    uint32_t pd[SEQ / 2], mbits[SEQ / 32];
+    float D = 0.f;
+#pragma unroll
+    for (int c = 0; c < SEQ / 32; ++c) {
+      uint32_t v[32], g[32], f[16];
+      tmem_ld32(lane_base + c * 32, v);
+      tmem_ld32(lane_base + 128 + c * 32, g);
+      tmem_ld_wait();
+      row_fields(sd, nb, c, hi, thr, f);
+      uint32_t bits = 0;
+#pragma unroll
+      for (int q = 0; q < 32; q += 2) {
+        const float p0 = ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm)) * inv;
+        const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(v[q + 1]), SC, nm)) * inv;
+        float m0 = 1.f, m1 = 1.f;
+        if (thr) {
+          const bool k0 = !((f[q >> 1] & 0xFFFFu) < thr), k1 = !((f[q >> 1] >> 16) < thr);
+          m0 = k0 ? keep : 0.f;
+          m1 = k1 ? keep : 0.f;
+          bits |= (k0 ? 1u : 0u) << q;
+          bits |= (k1 ? 1u : 0u) << (q + 1);
+        }
+        pd[c * 16 + (q >> 1)] = pack2(p0 * m0, p1 * m1);
+        D += __uint_as_float(g[q]) * m0 * p0;
+        D += __uint_as_float(g[q + 1]) * m1 * p1;
+      }
+      mbits[c] = bits;
+    }
+    // pass 4: dS = P (dP - D) / 8 -> shared, K-major [q][key] (two 64-key k-blocks, 128 B swizzle)
+    uint8_t* const srow = gbase + B_OFF_S + tid * 128;
+#pragma unroll
+    for (int c = 0; c < SEQ / 32; ++c) {
+      uint32_t v[32], g[32];
+      tmem_ld32(lane_base + c * 32, v);
+      tmem_ld32(lane_base + 128 + c * 32, g);
+      tmem_ld_wait();
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t w[4];
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+          const int q = cc * 8 + 2 * hh;
+          const float p0 = ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm)) * inv;
+          const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(v[q + 1]), SC, nm)) * inv;
+          const float m0 = thr ? (((mbits[c] >> q) & 1u) ? keep : 0.f) : 1.f;
+          const float m1 = thr ? (((mbits[c] >> (q + 1)) & 1u) ? keep : 0.f) : 1.f;
+          w[hh] = pack2(p0 * (__uint_as_float(g[q]) * m0 - D) * 0.125f,
+                        p1 * (__uint_as_float(g[q + 1]) * m1 - D) * 0.125f);
+        }
+        const int chunk = (c & 1) * 4 + cc;
+        *(uint4*)(srow + (c >> 1) * 16384 + ((chunk ^ (tid & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      // dQ = dS K: A = dS K-major [q][key], B = K viewed MN-major ([d][key], d contiguous)
+      constexpr uint32_t idQ = idesc_bf16(128, HD, false, true);
+      const uint64_t dK_mn = mn_desc(base + B_OFF_K, 8192);
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb) {
+        const uint64_t ds = kmajor_sw128_desc(base + B_OFF_S + kb * 16384);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma(tmem, ds + 2 * k, dK_mn + (uint64_t)(kb * 4 + k) * (2048 >> 4), idQ, (kb | k) != 0);
+      }
+      // dK = dS^T Q: A = dS viewed MN-major ([key][q]: two 64-key blocks 16 KB apart), B = Q MN-major
+      constexpr uint32_t idK = idesc_bf16(128, HD, true, true);
+      const uint64_t ds_mn = mn_desc(base + B_OFF_S, 16384), q_mn = mn_desc(base + B_OFF_Q, 8192);
+#pragma unroll
+      for (int k = 0; k < SEQ / 16; ++k)
+        tc_mma(tmem + 64, ds_mn + (uint64_t)k * (2048 >> 4), q_mn + (uint64_t)k * (2048 >> 4), idK, k != 0);
+      tc_commit(bar_a);
+    }
+    mbar_wait(bar_a, ph);  // dS consumed: Pd takes its place
+    tc_fence_after();
+#pragma unroll
+    for (int c = 0; c < SEQ / 32; ++c) {
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int chunk = (c & 1) * 4 + cc, j = c * 16 + cc * 4;
+        *(uint4*)(srow + (c >> 1) * 16384 + ((chunk ^ (tid & 7)) << 4)) =
+            make_uint4(pd[j], pd[j + 1], pd[j + 2], pd[j + 3]);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      // dV = Pd^T dO: A = Pd viewed MN-major ([key][q]), B = dO MN-major ([d][q])
+      constexpr uint32_t idV = idesc_bf16(128, HD, true, true);
+      const uint64_t p_mn = mn_desc(base + B_OFF_S, 16384), do_mn = mn_desc(base + B_OFF_DO, 8192);
+#pragma unroll
+      for (int k = 0; k < SEQ / 16; ++k)
+        tc_mma(tmem + 128, p_mn + (uint64_t)k * (2048 >> 4), do_mn + (uint64_t)k * (2048 >> 4), idV, k != 0);
+      tc_commit(bar_v);
+    }
+    __nv_bfloat16* const row = a.dqkv + ((size_t)s * SEQ + tid) * ld + h * HD;
+    store_row64(row, lane_base);            // dq (query row tid)
+    store_row64(row + a.Dm, lane_base + 64);  // dk (key row tid)
+    mbar_wait(bar_v, ph);
+    tc_fence_after();
+    store_row64(row + 2 * a.Dm, lane_base + 128);  // dv (key row tid)
+    tc_fence_before();
+    __syncthreads();  // TMEM and the shared tiles are free for the next item
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(B_TMEM_COLS) : "memory");
+  }
+}
+
 }  // namespace attn_tc
 
 int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int seqs_per_est, int est_base, int L,
@@ -237,6 +479,31 @@ int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = a.n_items < 4 * sms ? a.n_items : 4 * sms;
   attn_tc::attn_fwd_tc_kernel<<<grid, attn_tc::THREADS, attn_tc::SMEM, s>>>(mqk, mv, a);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+
+int attn_bwd_tc_launch(const void* qkv, const void* dctx, void* dqkv, int n_seq, int Dm, int H, int seqs_per_est,
+                       int est_base, int L, int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev,
+                       cudaStream_t s) {
+  const int T = n_seq * attn_tc::SEQ;
+  CUtensorMap mqk, mdo;
+  if (!make_map(&mqk, qkv, T, 3 * Dm, attn_tc::SEQ, 1, (int64_t)T * 3 * Dm) ||
+      !make_map(&mdo, dctx, T, Dm, attn_tc::SEQ, 1, (int64_t)T * Dm))
+    return ERR_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(attn_tc::attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             attn_tc::B_SMEM) != cudaSuccess)
+      return ERR_CUDA;
+    attr = true;
+  }
+  attn_tc::BwdArgs a{(__nv_bfloat16*)dqkv, Dm, H, seqs_per_est, est_base, L, layer, n_seq * H, seed, step, p,
+                     step_dev};
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = a.n_items < 2 * sms ? a.n_items : 2 * sms;
+  attn_tc::attn_bwd_tc_kernel<<<grid, attn_tc::THREADS, attn_tc::B_SMEM, s>>>(mqk, mdo, a);
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 

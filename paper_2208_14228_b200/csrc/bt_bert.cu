@@ -711,6 +711,9 @@ __global__ void __launch_bounds__(256) cast_t_kernel(const __grid_constant__ Cas
 // ----------------------------------------------------------------- launchers
 int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int seqs_per_est, int est_base, int L,
                        int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev, cudaStream_t s);
+int attn_bwd_tc_launch(const void* qkv, const void* dctx, void* dqkv, int n_seq, int Dm, int H, int seqs_per_est,
+                       int est_base, int L, int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev,
+                       cudaStream_t s);
 static bool attn_tc_enabled() {  // BT_ATTN_TC=0: the mma.sync forward (bt_bert.cu) instead of bt_attn_tc.cu
   const char* e = getenv("BT_ATTN_TC");
   return !(e && e[0] == '0');
@@ -725,8 +728,11 @@ int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out,
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (!backward && attn_tc_enabled())
-    return attn_fwd_tc_launch(qkv, out, n_seq, Dm, H, seqs_per_est, est_base, L, layer, seed, step, p, step_dev, s);
+  if (attn_tc_enabled())
+    return backward ? attn_bwd_tc_launch(qkv, dctx, out, n_seq, Dm, H, seqs_per_est, est_base, L, layer, seed, step, p,
+                                         step_dev, s)
+                    : attn_fwd_tc_launch(qkv, out, n_seq, Dm, H, seqs_per_est, est_base, L, layer, seed, step, p,
+                                         step_dev, s);
   if (!backward) {
     static bool attr = false;
     if (!attr) {

@@ -348,3 +348,35 @@ def test_tcgen05_attention_forward_matches_mma_sync(bert, monkeypatch):
     assert torch.equal(a, _d(cap["ctx"]))  # the step used the tcgen05 path
     assert (a != b).double().mean().item() <= 1e-2
     assert ((a - b).norm() / b.norm()).item() <= 5e-3
+
+
+def test_tcgen05_attention_backward_matches_mma_sync(bert, monkeypatch):
+    """The tcgen05 attention backward (bt_attn_tc.cu: S, dP, dQ, dK, dV as UMMAs, the forward's exact
+    softmax recomputation, K-major tiles read MN-major for the transposed products) agrees with the
+    mma.sync backward to bf16 rounding and is run-to-run bitwise stable."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    job = bert.BertJob(**SMALL)
+    cap = {}
+    job.step(capture=cap)
+    qkv, dctx = cap["qkv"], cap["dctx"]
+    E, Te, D, H = job.E, job.Te, job.D, job.H
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("BT_ATTN_TC", mode)
+        res = []
+        for _ in range(2):
+            o = torch.empty(E * Te, 3 * D, dtype=torch.bfloat16, device="cuda")
+            _native.check(_native.lib().bt_bert_attn(1, qkv.data_ptr(), dctx.data_ptr(), o.data_ptr(), E, Te, D, H,
+                                                     0, job.L, 0, job.seed, 0, job.pa, None, stream()))
+            res.append(o)
+        assert torch.equal(res[0].view(torch.int16), res[1].view(torch.int16))
+        outs[mode] = res[0]
+    monkeypatch.delenv("BT_ATTN_TC")
+    a, b = _d(outs["1"]), _d(outs["0"])
+    assert torch.equal(a, _d(cap["dqkv"]))  # the step used the tcgen05 path
+    for part in range(3):
+        x, y = a[:, part * D:(part + 1) * D], b[:, part * D:(part + 1) * D]
+        assert (x != y).double().mean().item() <= 3e-2, part
+        assert ((x - y).norm() / y.norm()).item() <= 1e-2, part
