@@ -368,16 +368,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr int PER = BN / EPI_SPLIT < 32 ? 32 : BN / EPI_SPLIT;  // columns per epilogue warp (BN=64: 8 warps work)
       for (int cc = half * PER; cc < (half + 1) * PER && cc < BN; cc += 32) {
         uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * BN + cc);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * BN + cc), v);
+        tmem_ld_wait();
         epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, epi, est + (chunk++ & 1) * EPI_BOX, lane, &map_c, &map_c2, row0,
                                   t / per_batch);
       }
@@ -588,16 +580,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
 #pragma unroll 1
       for (int cc = half * (PAIR_BN / (EW / 4)); cc < (half + 1) * (PAIR_BN / (EW / 4)); cc += 32) {
         uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * PAIR_BN + cc);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * PAIR_BN + cc), v);
+        tmem_ld_wait();
         epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, epi, est + (chunk++ & 1) * EPI_BOX, lane, &map_c, &map_c2, row0,
                                   t / per_batch);
       }
