@@ -71,17 +71,49 @@ __device__ __forceinline__ void row_stats(uint32_t lane_base, float* nm_out, flo
     for (int q = 0; q < 32; ++q) mx = fmaxf(mx, __uint_as_float(v[q]));
   }
   const float nm = -__fmul_rn(mx, SC);
-  float l = 0.f;
+  float l[2] = {0.f, 0.f};  // the two 64-column halves, each in column order, then added
 #pragma unroll
   for (int c = 0; c < SEQ / 32; ++c) {
     uint32_t v[32];
     tmem_ld32(lane_base + c * 32, v);
     tmem_ld_wait();
 #pragma unroll
-    for (int q = 0; q < 32; ++q) l += ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm));
+    for (int q = 0; q < 32; ++q) l[c >> 1] += ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm));
   }
   *nm_out = nm;
-  *inv_out = 1.f / l;
+  *inv_out = 1.f / (l[0] + l[1]);
+}
+// The same statistics from one 64-column half (cols [64*hf, 64*hf + 64)) per thread, the halves of a
+// row combined through shared memory: identical bits to row_stats (max is exact; sum = half0 + half1).
+__device__ __forceinline__ void row_stats_half(uint32_t lane_base, int hf, int row, float* red, float* nm_out,
+                                               float* inv_out) {
+  float mx = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t v[32];
+    tmem_ld32(lane_base + hf * 64 + c * 32, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q = 0; q < 32; ++q) mx = fmaxf(mx, __uint_as_float(v[q]));
+  }
+  red[hf * SEQ + row] = mx;
+  __syncthreads();
+  mx = fmaxf(red[row], red[SEQ + row]);
+  const float nm = -__fmul_rn(mx, SC);
+  float l = 0.f;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t v[32];
+    tmem_ld32(lane_base + hf * 64 + c * 32, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q = 0; q < 32; ++q) l += ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm));
+  }
+  __syncthreads();  // everyone has read the max slots
+  red[hf * SEQ + row] = l;
+  __syncthreads();
+  *nm_out = nm;
+  *inv_out = 1.f / (red[row] + red[SEQ + row]);
 }
 // The 16 mask fields (one per column pair) of this row's 32-column slice c: rows i and i^8 share a
 // draw; each of the two lanes computes half of the slice's draws and they exchange by shuffle.
@@ -230,7 +262,8 @@ __global__ void __launch_bounds__(THREADS, 4)
 
 
 // ---------------------------------------------------------------------------------------- backward
-// Per (sequence, head) item, thread i owns query row i for the row work and key row i for dK / dV:
+// Per (sequence, head) item; 8 warps, thread (row i, half hf) owns columns [64 hf, 64 hf + 64) of query
+// row i for the row work and of key row i for dK / dV (row reductions combined through shared memory):
 //   TMA      Q, K, V, dO [128][64] K-major tiles (each tile is also read MN-major by the products
 //            that need its transpose: the bytes of a K-major [r][64] tile are the MN-major layout of
 //            its [64][r] view);
@@ -241,9 +274,11 @@ __global__ void __launch_bounds__(THREADS, 4)
 //   tcgen05  dQ = dS K -> [0,64), dK = dS^T Q -> [64,128); then Pd (from registers) replaces dS in
 //            shared memory and dV = Pd^T dO -> [128,192);
 //   store    dq / dk / dv rows into dqkv (bf16).
-constexpr int B_OFF_Q = 0, B_OFF_K = 16384, B_OFF_V = 32768, B_OFF_DO = 49152, B_OFF_S = 65536, B_OFF_BAR = 98304;
+constexpr int B_OFF_Q = 0, B_OFF_K = 16384, B_OFF_V = 32768, B_OFF_DO = 49152, B_OFF_S = 65536, B_OFF_RED = 98304,
+              B_OFF_BAR = B_OFF_RED + 2 * SEQ * 4;
 constexpr int B_SMEM = B_OFF_BAR + 64 + 1024;
 constexpr int B_TMEM_COLS = 256;
+constexpr int B_THREADS = 256;  // thread (row, half): row = 32 * (warp % 4) + lane, columns [64*half, +64)
 
 // MN-major SW128 descriptor with an explicit distance between 64-wide MN blocks
 __device__ __forceinline__ uint64_t mn_desc(uint32_t saddr, uint32_t lbo) {
@@ -260,31 +295,31 @@ struct BwdArgs {
   const int64_t* step_dev;
 };
 
-__device__ __forceinline__ void store_row64(__nv_bfloat16* dst, uint32_t taddr) {
+// 32 TMEM columns of this lane's row -> 32 bf16 (64 bytes) at dst
+__device__ __forceinline__ void store_row32(__nv_bfloat16* dst, uint32_t taddr) {
   uint4* const o = (uint4*)dst;
+  uint32_t v[32];
+  tmem_ld32(taddr, v);
+  tmem_ld_wait();
 #pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    uint32_t v[32];
-    tmem_ld32(taddr + c * 32, v);
-    tmem_ld_wait();
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      o[c * 4 + q] = make_uint4(pack2(__uint_as_float(v[8 * q]), __uint_as_float(v[8 * q + 1])),
-                                pack2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3])),
-                                pack2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
-                                pack2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
-  }
+  for (int q = 0; q < 4; ++q)
+    o[q] = make_uint4(pack2(__uint_as_float(v[8 * q]), __uint_as_float(v[8 * q + 1])),
+                      pack2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3])),
+                      pack2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
+                      pack2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
 }
 
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(B_THREADS, 2)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap mqk, const __grid_constant__ CUtensorMap mdo,
                        const BwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw), base = (raw + 1023u) & ~1023u;
   uint8_t* const gbase = smem_raw + (base - raw);
+  float* const red = (float*)(gbase + B_OFF_RED);  // [2 halves][128 rows] row-reduction exchange
   const uint32_t bar_ld = base + B_OFF_BAR, bar_s = bar_ld + 8, bar_a = bar_ld + 16, bar_v = bar_ld + 24;
   uint32_t* const tmem_slot = (uint32_t*)(gbase + B_OFF_BAR + 40);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int hf = warp >> 2, row = (warp & 3) * 32 + lane;
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mqk) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mdo) : "memory");
@@ -304,11 +339,11 @@ __global__ void __launch_bounds__(THREADS, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's TMEM lane quarter
   const int64_t step = a.step_dev ? *a.step_dev : a.step;
   const uint32_t thr = a.p > 0.f ? (uint32_t)ceil((double)a.p * 65536.0) : 0u;
   const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
-  const int hi = (tid >> 3) & 1;
+  const int hi = (row >> 3) & 1;  // rows i, i^8 (lanes l, l^8 of one warp) share draws
   const int ld = 3 * a.Dm;
   int n = 0;
   for (int it = blockIdx.x; it < a.n_items; it += gridDim.x, ++n) {
@@ -334,16 +369,17 @@ __global__ void __launch_bounds__(THREADS, 2)
     mbar_wait(bar_s, ph);
     tc_fence_after();
     float nm, inv;
-    row_stats(lane_base, &nm, &inv);
+    row_stats_half(lane_base, hf, row, red, &nm, &inv);
     const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
     const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
     const uint64_t nb = ((((uint64_t)step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4) +
-                        (uint64_t)((tid >> 4) * 8 + (tid & 7)) * 64;
-    // pass 3: dropped P (packed, registers), mask bits, D = sum dP * P in column order
-    uint32_t pd[SEQ / 2], mbits[SEQ / 32];
+                        (uint64_t)((row >> 4) * 8 + (row & 7)) * 64;
+    // pass 3 (this half): dropped P (packed, registers), mask bits, partial D = sum dP * P
+    uint32_t pd[32], mbits[2];
     float D = 0.f;
 #pragma unroll
-    for (int c = 0; c < SEQ / 32; ++c) {
+    for (int c2 = 0; c2 < 2; ++c2) {
+      const int c = hf * 2 + c2;  // 32-column slice
       uint32_t v[32], g[32], f[16];
       tmem_ld32(lane_base + c * 32, v);
       tmem_ld32(lane_base + 128 + c * 32, g);
@@ -362,16 +398,21 @@ __global__ void __launch_bounds__(THREADS, 2)
           bits |= (k0 ? 1u : 0u) << q;
           bits |= (k1 ? 1u : 0u) << (q + 1);
         }
-        pd[c * 16 + (q >> 1)] = pack2(p0 * m0, p1 * m1);
+        pd[c2 * 16 + (q >> 1)] = pack2(p0 * m0, p1 * m1);
         D += __uint_as_float(g[q]) * m0 * p0;
         D += __uint_as_float(g[q + 1]) * m1 * p1;
       }
-      mbits[c] = bits;
+      mbits[c2] = bits;
     }
-    // pass 4: dS = P (dP - D) / 8 -> shared, K-major [q][key] (two 64-key k-blocks, 128 B swizzle)
-    uint8_t* const srow = gbase + B_OFF_S + tid * 128;
+    __syncthreads();  // the sum slots of row_stats_half are read
+    red[hf * SEQ + row] = D;
+    __syncthreads();
+    D = red[row] + red[SEQ + row];  // (half 0 + half 1)
+    // pass 4: dS = P (dP - D) / 8 -> shared, K-major [q][key]: this half is k-block hf
+    uint8_t* const srow = gbase + B_OFF_S + hf * 16384 + row * 128;
 #pragma unroll
-    for (int c = 0; c < SEQ / 32; ++c) {
+    for (int c2 = 0; c2 < 2; ++c2) {
+      const int c = hf * 2 + c2;
       uint32_t v[32], g[32];
       tmem_ld32(lane_base + c * 32, v);
       tmem_ld32(lane_base + 128 + c * 32, g);
@@ -384,13 +425,13 @@ __global__ void __launch_bounds__(THREADS, 2)
           const int q = cc * 8 + 2 * hh;
           const float p0 = ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm)) * inv;
           const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(v[q + 1]), SC, nm)) * inv;
-          const float m0 = thr ? (((mbits[c] >> q) & 1u) ? keep : 0.f) : 1.f;
-          const float m1 = thr ? (((mbits[c] >> (q + 1)) & 1u) ? keep : 0.f) : 1.f;
+          const float m0 = thr ? (((mbits[c2] >> q) & 1u) ? keep : 0.f) : 1.f;
+          const float m1 = thr ? (((mbits[c2] >> (q + 1)) & 1u) ? keep : 0.f) : 1.f;
           w[hh] = pack2(p0 * (__uint_as_float(g[q]) * m0 - D) * 0.125f,
                         p1 * (__uint_as_float(g[q + 1]) * m1 - D) * 0.125f);
         }
-        const int chunk = (c & 1) * 4 + cc;
-        *(uint4*)(srow + (c >> 1) * 16384 + ((chunk ^ (tid & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        const int chunk = c2 * 4 + cc;
+        *(uint4*)(srow + ((chunk ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -419,12 +460,11 @@ __global__ void __launch_bounds__(THREADS, 2)
     mbar_wait(bar_a, ph);  // dS consumed: Pd takes its place
     tc_fence_after();
 #pragma unroll
-    for (int c = 0; c < SEQ / 32; ++c) {
+    for (int c2 = 0; c2 < 2; ++c2) {
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
-        const int chunk = (c & 1) * 4 + cc, j = c * 16 + cc * 4;
-        *(uint4*)(srow + (c >> 1) * 16384 + ((chunk ^ (tid & 7)) << 4)) =
-            make_uint4(pd[j], pd[j + 1], pd[j + 2], pd[j + 3]);
+        const int chunk = c2 * 4 + cc, j = c2 * 16 + cc * 4;
+        *(uint4*)(srow + ((chunk ^ (row & 7)) << 4)) = make_uint4(pd[j], pd[j + 1], pd[j + 2], pd[j + 3]);
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -440,14 +480,14 @@ __global__ void __launch_bounds__(THREADS, 2)
         tc_mma(tmem + 128, p_mn + (uint64_t)k * (2048 >> 4), do_mn + (uint64_t)k * (2048 >> 4), idV, k != 0);
       tc_commit(bar_v);
     }
-    __nv_bfloat16* const row = a.dqkv + ((size_t)s * SEQ + tid) * ld + h * HD;
-    store_row64(row, lane_base);            // dq (query row tid)
-    store_row64(row + a.Dm, lane_base + 64);  // dk (key row tid)
+    __nv_bfloat16* const out = a.dqkv + ((size_t)s * SEQ + row) * ld + h * HD + hf * 32;
+    store_row32(out, lane_base + hf * 32);               // dq (query row), this half's 32 columns
+    store_row32(out + a.Dm, lane_base + 64 + hf * 32);   // dk (key row)
     mbar_wait(bar_v, ph);
     tc_fence_after();
-    store_row64(row + 2 * a.Dm, lane_base + 128);  // dv (key row tid)
+    store_row32(out + 2 * a.Dm, lane_base + 128 + hf * 32);  // dv (key row)
     tc_fence_before();
-    __syncthreads();  // TMEM and the shared tiles are free for the next item
+    __syncthreads();  // TMEM, the shared tiles and the exchange slots are free for the next item
   }
   tc_fence_before();
   __syncthreads();
@@ -503,7 +543,7 @@ int attn_bwd_tc_launch(const void* qkv, const void* dctx, void* dqkv, int n_seq,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = a.n_items < 2 * sms ? a.n_items : 2 * sms;
-  attn_tc::attn_bwd_tc_kernel<<<grid, attn_tc::THREADS, attn_tc::B_SMEM, s>>>(mqk, mdo, a);
+  attn_tc::attn_bwd_tc_kernel<<<grid, attn_tc::B_THREADS, attn_tc::B_SMEM, s>>>(mqk, mdo, a);
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
