@@ -231,3 +231,54 @@ def test_implicit_gemm_convolutions_equal_explicit_im2col(rn, monkeypatch):
     for x, y in zip(la, lb):
         assert np.array_equal(_bits(x), _bits(y))
     assert np.array_equal(_bits(a.params), _bits(b.params))
+
+
+@pytest.mark.parametrize("ci,co,k,s,hw", [(64, 64, 3, 1, 8), (64, 128, 3, 2, 8), (128, 256, 1, 2, 8)])
+def test_convolution_products_match_float64(rn, ci, co, k, s, hw):
+    """The implicit-GEMM convolution (bt_gemm_conv: TMA im2col loads), its weight gradient and the dX
+    paths (stride 1: forward convolution of dz with the tap-reversed filter; stride 2: the transposed
+    gather) against torch's float64 conv2d / conv2d_weight / conv2d_input on the same bf16 values:
+    fp32-accumulation error only (rel. Frobenius <= 1e-5 for fp32 outputs, bf16 rounding for bf16)."""
+    from torch.nn.grad import conv2d_input, conv2d_weight
+
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    L = _native.lib()
+    N, p = 4, k // 2
+    ho = (hw + 2 * p - k) // s + 1
+    g = torch.Generator(device="cuda").manual_seed(ci + co + k)
+    x = torch.randn(N, hw, hw, ci, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(co, k, k, ci, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    dz = torch.randn(N, ho, ho, co, device="cuda", generator=g).to(torch.bfloat16)
+    wt = w.permute(3, 1, 2, 0).contiguous()  # [Ci][kh][kw][Co]
+    x64, w64, dz64 = (t.double().cpu() for t in (x.permute(0, 3, 1, 2), w.permute(0, 3, 1, 2), dz.permute(0, 3, 1, 2)))
+    # forward (fp32 out)
+    z = torch.empty(N * ho * ho, co, device="cuda")
+    _native.check(L.bt_gemm_conv(0, x.data_ptr(), N, hw, hw, ci, ho, ho, k, k, s, p, w.data_ptr(), z.data_ptr(), co,
+                                 1, 0, 0, 0, stream()))
+    zref = torch.nn.functional.conv2d(x64, w64, stride=s, padding=p).permute(0, 2, 3, 1).reshape(-1, co)
+    _close(z, zref, "conv forward", 1e-5)
+    # weight gradient, one batch entry per 2 images (an "EST"), fp32 out
+    R = 2 * ho * ho
+    if R % 64 == 0:
+        dw = torch.empty(2, co, k * k * ci, device="cuda")
+        _native.check(L.bt_gemm_conv(1, x.data_ptr(), N, hw, hw, ci, ho, ho, k, k, s, p, dz.data_ptr(), dw.data_ptr(),
+                                     co, 2, R, co * k * k * ci, 0, stream()))
+        for e in range(2):
+            sl = slice(2 * e, 2 * e + 2)
+            ref = conv2d_weight(x64[sl], w64.shape, dz64[sl], stride=s, padding=p).permute(0, 2, 3, 1).reshape(co, -1)
+            _close(dw[e], ref, f"conv dW entry {e}", 1e-5)
+    # dX
+    dxref = conv2d_input(x64.shape, w64, dz64, stride=s, padding=p).permute(0, 2, 3, 1).reshape(-1, ci)
+    dx = torch.empty(N * hw * hw, ci, device="cuda")
+    if s == 1:  # forward convolution of dz with the tap-reversed filter
+        wflip = torch.flip(w.view(co, k, k, ci), dims=(1, 2)).permute(3, 1, 2, 0).contiguous()
+        _native.check(L.bt_gemm_conv(0, dz.data_ptr(), N, ho, ho, co, hw, hw, k, k, 1, p, wflip.data_ptr(),
+                                     dx.data_ptr(), ci, 1, 0, 0, 0, stream()))
+    else:  # transposed-convolution gather + GEMM
+        col = torch.empty(N * hw * hw, k * k * co, dtype=torch.bfloat16, device="cuda")
+        _native.check(L.bt_cnn_im2col(dz.data_ptr(), col.data_ptr(), N, ho, ho, co, hw, hw, k, k, s, p, 1, stream()))
+        _native.check(L.bt_gemm_bf16_ex(col.data_ptr(), wt.data_ptr(), dx.data_ptr(), 1, N * hw * hw, ci, k * k * co,
+                                        0, 0, 0, 0, None, 0, 0, stream()))
+    _close(dx, dxref, "conv dX", 1e-5)
