@@ -74,7 +74,7 @@ class ResNetJob:
 
     def __init__(self, ests: int = 16, batch: int = 32, gpus: int = 8, seed: int = 42, lr: float = 0.02,
                  momentum: float = 0.9, fanin: int = 0, eps: float = 1e-5, est_base: int = 0,
-                 est_count: int | None = None):
+                 est_count: int | None = None, graph: bool = True):
         """`gpus`: launch groups ("GPUs") of this process's ESTs.  `est_base` / `est_count`: this process
         holds ESTs [est_base, est_base + est_count) of the E (one rank of a multi-GPU job, `attach_peer`)."""
         require_cuda()
@@ -87,6 +87,7 @@ class ResNetJob:
         if self.est0 < 0 or self.En < 1 or self.est0 + self.En > ests:
             raise ConfigError(f"local EST block [{est_base}, +{est_count}) outside the {ests} ESTs")
         self.peer = None
+        self.graph = graph
         convs = [_Conv("stem", 8, 64, 3, 1, 32)]
         blocks = []
         ci, h = 64, 32
@@ -183,6 +184,7 @@ class ResNetJob:
             _native.check(_native.lib().bt_est_slot_copy((C.c_void_p * cnt)(*dst), (C.c_void_p * cnt)(*src),
                                                          (C.c_int64 * cnt)(*nb), cnt, stream()), "EST slot copy")
         self.slots, self.G = new, gpus
+        self._graph, self._gwarm = None, False  # a new layout (slot buffers, launch groups): capture again
 
     def rescale(self, gpus: int):
         """Elastic rescale onto `gpus` launch groups: per-EST slots move, parameters are replicated."""
@@ -372,35 +374,57 @@ class ResNetJob:
 
     # ------------------------------------------------------------ step
     def step(self, capture: dict | None = None) -> torch.Tensor:
-        """One mini-batch of this process's ESTs on the current layout; per-EST losses [est_count]."""
+        """One mini-batch of this process's ESTs on the current layout; per-EST losses [est_count].
+        After one eager step on a layout, the whole step (every launch group, the reducer, the weight
+        refresh, the cursor advance) is captured as a CUDA graph and replayed until the next rescale."""
+        replay = self.graph and capture is None and self.peer is None
+        if replay and self._gwarm:
+            if self._graph is None:  # capture once per layout (the captured work runs at the first replay)
+                self._gloss = torch.empty(self.En, dtype=torch.float32, device="cuda")
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._body(self._gloss)
+                self._graph = g
+            self._graph.replay()
+            self._post()
+            return self._gloss.clone()
         losses = torch.empty(self.En, dtype=torch.float32, device="cuda")
+        self._body(losses, capture)
+        self._post()
+        self._gwarm = self._gwarm or replay
+        return losses
+
+    def _body(self, losses, capture=None):
+        """Everything a step puts on the stream (capturable: no host synchronisation, no allocation)."""
         for g, (base, n) in enumerate(self.layout(self.G)):
             self._group(g, base, n, losses, capture if self.G == 1 else None)
         if capture is not None:
             capture["grads"] = self.grads.clone()
         if self.peer is not None:  # across processes: the peer-memory reducer
             self.peer.step()
+        else:
+            if self.En != self.E:
+                raise ConfigError("a partial EST block needs attach_peer() for the exchange")
+            a = _native.ReduceArgs()
+            a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, self.E, self.fanin, self.P
+            for k in range(self.E):
+                a.grads[k] = self.grads.data_ptr() + 4 * k * self.P
+            p, v = self.params.data_ptr(), self.vel.data_ptr()
+            a.param, a.vel, a.param_out, a.vel_out = p, v, p, v
+            a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
+            _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()), "resnet reduce_update")
+        self._refresh_bf16()
+
+    def _post(self):
+        """Host side of a step: the non-finite check (one status read) and the step count."""
+        self.step_idx += 1
+        if self.peer is not None:
             self.peer.check()
-            self.step_idx += 1
-            self._refresh_bf16()
-            return losses
-        if self.En != self.E:
-            raise ConfigError("a partial EST block needs attach_peer() for the exchange")
-        a = _native.ReduceArgs()
-        a.dtype, a.mode, a.E, a.fanin, a.n = _native.DTYPE_F32, _native.REDUCE_UPDATE, self.E, self.fanin, self.P
-        for k in range(self.E):
-            a.grads[k] = self.grads.data_ptr() + 4 * k * self.P
-        p, v = self.params.data_ptr(), self.vel.data_ptr()
-        a.param, a.vel, a.param_out, a.vel_out = p, v, p, v
-        a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
-        _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()), "resnet reduce_update")
+            return
         st, _, _ = self.flags.status()
         if st:
             self.flags.reset()
             raise NumericError("resnet: non-finite synchronized gradient")
-        self.step_idx += 1
-        self._refresh_bf16()
-        return losses
 
     def flops_per_step(self) -> float:
         """Convolution + head flops of one mini-batch (forward 2*R*Co*K, backward dX and dW 2x that)."""

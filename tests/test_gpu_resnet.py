@@ -282,3 +282,19 @@ def test_convolution_products_match_float64(rn, ci, co, k, s, hw):
         _native.check(L.bt_gemm_bf16_ex(col.data_ptr(), wt.data_ptr(), dx.data_ptr(), 1, N * hw * hw, ci, k * k * co,
                                         0, 0, 0, 0, None, 0, 0, stream()))
     _close(dx, dxref, "conv dX", 1e-5)
+
+
+def test_cuda_graph_replay_equals_eager_across_rescale(rn):
+    """The captured ResNet step replays bit-identically to eager execution, and a rescale (new slot
+    buffers and launch groups) re-captures: graph runs through 4 -> 2 GPUs equal the eager run."""
+    a = rn.ResNetJob(gpus=4, graph=True, **SMALL)
+    b = rn.ResNetJob(gpus=4, graph=False, **SMALL)
+    for gpus in (4, 2):
+        if gpus != 4:
+            a.rescale(gpus)
+            b.rescale(gpus)
+        for _ in range(3):
+            assert np.array_equal(_bits(a.step()), _bits(b.step()))
+    assert a._graph is not None and np.array_equal(_bits(a.params), _bits(b.params))
+    sa, sb = a.est_state(), b.est_state()
+    assert np.array_equal(_bits(sa["run_var"]), _bits(sb["run_var"])) and torch.equal(sa["cursor"], sb["cursor"])
