@@ -127,18 +127,34 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
   float g[32];  // second output (FFN_FWD)
   if (epi.kind == EPI_BIAS) {
 #pragma unroll
-    for (int q = 0; q < 32; ++q) f[q] += epi.bias[col + q];
+    for (int q4 = 0; q4 < 8; ++q4) {
+      const float4 bv = *(const float4*)(epi.bias + col + 4 * q4);
+      f[4 * q4] += bv.x;
+      f[4 * q4 + 1] += bv.y;
+      f[4 * q4 + 2] += bv.z;
+      f[4 * q4 + 3] += bv.w;
+    }
   } else if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) {
     const int e = (int)(row / (size_t)epi.Te), tl = (int)(row - (size_t)e * epi.Te);
-    const uint64_t sd = derive3(ffn::TAG_FFN_DROP, epi.seed, (uint64_t)(epi.est_base + e));
+    // the EST's dropout stream only when there is dropout (p == 0: every scale is 1, no draw)
+    const uint64_t sd = epi.p > 0.f ? derive3(ffn::TAG_FFN_DROP, epi.seed, (uint64_t)(epi.est_base + e)) : 0;
     const float keep = epi.p < 1.f ? 1.f / (1.f - epi.p) : 0.f;
     if (epi.kind == EPI_FFN_FWD) {
+      float b[32];  // the chunk's 32 biases, 8 vector loads
+#pragma unroll
+      for (int q4 = 0; q4 < 8; ++q4) {
+        const float4 bv = *(const float4*)(epi.bias + col + 4 * q4);
+        b[4 * q4] = bv.x;
+        b[4 * q4 + 1] = bv.y;
+        b[4 * q4 + 2] = bv.z;
+        b[4 * q4 + 3] = bv.w;
+      }
 #pragma unroll
       for (int q = 0; q < 32; q += 2) {
         float m0, m1, g0, g1;
         ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
-        ffn::gelu_and_grad(f[q] + epi.bias[col + q], &g0, &f[q]);  // C = gelu'(h) for the backward
-        ffn::gelu_and_grad(f[q + 1] + epi.bias[col + q + 1], &g1, &f[q + 1]);
+        ffn::gelu_and_grad(f[q] + b[q], &g0, &f[q]);  // C = gelu'(h) for the backward
+        ffn::gelu_and_grad(f[q + 1] + b[q + 1], &g1, &f[q + 1]);
         g[q] = g0 * m0;
         g[q + 1] = g1 * m1;
       }
