@@ -143,8 +143,8 @@ int bt_ffn_out(const float *y_dev, const float *b2_dev, const float *target_dev,
                void *dy_dev, float *partials_dev, float *loss_dev, void *stream);
 int bt_ffn_bwd_act(const float *dd_dev, const void *hpre_dev, uint64_t seed, int64_t step, int32_t est_base,
                    int32_t E, int32_t Te, int32_t F, float p, void *dh_dev, void *stream);
-/* out[e][c] = sum_r in[e][r][c] (bf16 in, fp32 out): 16 ascending row chunks summed ascending, then
- * the chunk sums in order (fixed association).  scratch_dev: E*16*C floats, or NULL (allocated). */
+/* out[e][c] = sum_r in[e][r][c] (bf16 in, fp32 out): ascending 64-row chunks summed ascending, then
+ * the chunk sums in order (fixed association).  scratch_dev: E*ceil(R/64)*C floats, or NULL. */
 int bt_colsum_bf16(const void *in_dev, int32_t E, int32_t R, int32_t C, float *out_dev, float *scratch_dev,
                    void *stream);
 /* out[e][c][r] = bf16(in[e][r][c]); in is bf16 (in_f32 = 0) or fp32 (1) */

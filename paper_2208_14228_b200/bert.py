@@ -193,7 +193,7 @@ class BertJob:
             "dres": [torch.empty(T, D, **f32) for _ in range(2)],
             "dbr": torch.empty(T, D, **bf), "dHpre": torch.empty(T, F, **bf), "dctx": torch.empty(T, D, **bf),
             "dqkv": torch.empty(T, 3 * D, **bf), "lnpart": torch.empty(n * (Te // 64) * 3 * D, **f32),
-            "colsum": torch.empty(n * 16 * max(3 * D, F), **f32), "msepart": torch.empty(n * 64, **f32),
+            "colsum": torch.empty(n * -(-Te // 64) * max(3 * D, F), **f32), "msepart": torch.empty(n * 64, **f32),
         }
         self._ws[n] = ws
         return ws

@@ -158,41 +158,41 @@ __global__ void __launch_bounds__(ROW_THREADS) bwd_act_kernel(const float* __res
   }
 }
 
-// out[e][c] = sum over r of in[e][r][c] (per-EST bias gradients), in a fixed
-// association: COLSUM_CHUNKS ascending row ranges are summed ascending into
-// partials (pass 1, parallel over chunks x columns), then the partials are
-// summed in chunk order (pass 2).  Same bits for any grid.
-constexpr int COLSUM_CHUNKS = 16;
+// out[e][c] = sum over r of in[e][r][c] (per-EST / per-leaf bias gradients), in a fixed association:
+// ascending 64-row chunks (COLSUM_ROWS, fixed: part of the reduction's shape) are summed ascending into
+// partials (pass 1, parallel over chunks x columns), then the partials are summed in chunk order
+// (pass 2).  Same bits for any grid.
+constexpr int COLSUM_ROWS = 64;
 __global__ void colsum_part_kernel(const __nv_bfloat16* __restrict__ in, int E, int R, int C,
                                    float* __restrict__ part) {
-  const int cpt = C / 8;
-  const int64_t n = (int64_t)E * COLSUM_CHUNKS * cpt;
-  const int rows = (R + COLSUM_CHUNKS - 1) / COLSUM_CHUNKS;
+  const int cpt = C / 8, chunks = (R + COLSUM_ROWS - 1) / COLSUM_ROWS;
+  const int64_t n = (int64_t)E * chunks * cpt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int c0 = (int)(i % cpt) * 8;
     const int64_t ek = i / cpt;
-    const int k = (int)(ek % COLSUM_CHUNKS), e = (int)(ek / COLSUM_CHUNKS);
-    const int r0 = k * rows, r1 = min(R, r0 + rows);
+    const int k = (int)(ek % chunks), e = (int)(ek / chunks);
+    const int r0 = k * COLSUM_ROWS, r1 = min(R, r0 + COLSUM_ROWS);
     const __nv_bfloat16* p = in + (size_t)e * R * C + c0;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
     for (int r = r0; r < r1; ++r) {
       float v[8];
       load8(p + (size_t)r * C, v);
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] += v[q];
     }
-    float4* o = (float4*)(part + ((size_t)e * COLSUM_CHUNKS + k) * C + c0);
+    float4* o = (float4*)(part + ((size_t)e * chunks + k) * C + c0);
     o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
     o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
 }
-__global__ void colsum_final_kernel(const float* __restrict__ part, int E, int C, float* __restrict__ out,
+__global__ void colsum_final_kernel(const float* __restrict__ part, int E, int chunks, int C, float* __restrict__ out,
                                     int64_t ostride) {
   const int64_t n = (int64_t)E * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int e = (int)(i / C), c = (int)(i - (int64_t)e * C);
-    float acc = part[((size_t)e * COLSUM_CHUNKS) * C + c];
-    for (int k = 1; k < COLSUM_CHUNKS; ++k) acc += part[((size_t)e * COLSUM_CHUNKS + k) * C + c];
+    float acc = part[((size_t)e * chunks) * C + c];
+    for (int k = 1; k < chunks; ++k) acc += part[((size_t)e * chunks + k) * C + c];
     out[(size_t)e * ostride + c] = acc;
   }
 }
@@ -277,16 +277,16 @@ int colsum_bf16_launch(const void* in, int E, int R, int C, float* out, float* s
 int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, int64_t ostride, float* scratch,
                                cudaStream_t s) {
   if (C % 8) return ERR_INPUT;
-  float* part = scratch;  // E * COLSUM_CHUNKS * C partials
+  const int chunks = (R + ffn::COLSUM_ROWS - 1) / ffn::COLSUM_ROWS;
+  float* part = scratch;  // E * ceil(R / 64) * C partials
   bool own = false;
   if (!part) {
-    if (cudaMallocAsync((void**)&part, sizeof(float) * (size_t)E * ffn::COLSUM_CHUNKS * C, s) != cudaSuccess)
-      return ERR_CUDA;
+    if (cudaMallocAsync((void**)&part, sizeof(float) * (size_t)E * chunks * C, s) != cudaSuccess) return ERR_CUDA;
     own = true;
   }
-  ffn::colsum_part_kernel<<<grid_for((int64_t)E * ffn::COLSUM_CHUNKS * C / 8), 256, 0, s>>>(
-      (const __nv_bfloat16*)in, E, R, C, part);
-  ffn::colsum_final_kernel<<<grid_for((int64_t)E * C), 256, 0, s>>>(part, E, C, out, ostride);
+  ffn::colsum_part_kernel<<<grid_for((int64_t)E * chunks * C / 8), 256, 0, s>>>((const __nv_bfloat16*)in, E, R, C,
+                                                                               part);
+  ffn::colsum_final_kernel<<<grid_for((int64_t)E * C), 256, 0, s>>>(part, E, chunks, C, out, ostride);
   if (own) cudaFreeAsync(part, s);
   return ok_or_cuda();
 }

@@ -90,7 +90,7 @@ class FFNJob:
             ws = {"X": torch.empty(T, D, **bf), "tgt": torch.empty(T, D, **f32), "Hpre": torch.empty(T, F, **bf),
                   "D": torch.empty(T, F, **bf), "Y": torch.empty(T, D, **f32), "dY": torch.empty(T, D, **bf),
                   "dH": torch.empty(T, F, **bf), "part": torch.empty(n * _P, **f32),
-                  "colsum": torch.empty(n * 16 * F, **f32)}
+                  "colsum": torch.empty(n * -(-Te // 64) * F, **f32)}
             if not self.fused:
                 ws["H"] = torch.empty(T, F, **f32)
             self._ws[n] = ws
