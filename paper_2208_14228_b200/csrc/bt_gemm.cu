@@ -121,6 +121,43 @@ template <bool OUT_BF16>
 __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, int col, int N, const GemmEpi& epi,
                                                uint8_t* st, int lane, const CUtensorMap* mc, const CUtensorMap* mc2,
                                                int row0, int z) {
+  if (epi.kind == EPI_FFN_FWD) {
+    // bias + GELU' (C) and dropout(GELU) (out2), produced and staged 8 columns at a time (few live
+    // registers: the 16-epilogue-warp kernel has ~96 per thread)
+    const int e = (int)(row / (size_t)epi.Te), tl = (int)(row - (size_t)e * epi.Te);
+    const uint64_t sd = epi.p > 0.f ? derive3(ffn::TAG_FFN_DROP, epi.seed, (uint64_t)(epi.est_base + e)) : 0;
+    const float keep = epi.p < 1.f ? 1.f / (1.f - epi.p) : 0.f;
+    if (lane == 0) bulk_wait_read1();  // the store that last used this box (two chunks ago) has read it
+    __syncwarp();
+#pragma unroll
+    for (int q8 = 0; q8 < 4; ++q8) {
+      const float4 b0 = *(const float4*)(epi.bias + col + 8 * q8), b1 = *(const float4*)(epi.bias + col + 8 * q8 + 4);
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      uint32_t wc[4], wo[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int q = 8 * q8 + 2 * h;
+        float m0, m1, g0, g1, d0, d1;
+        ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
+        ffn::gelu_and_grad(__uint_as_float(v[q]) + bb[2 * h], &g0, &d0);
+        ffn::gelu_and_grad(__uint_as_float(v[q + 1]) + bb[2 * h + 1], &g1, &d1);
+        const __nv_bfloat162 c2 = __floats2bfloat162_rn(d0, d1), o2 = __floats2bfloat162_rn(g0 * m0, g1 * m1);
+        wc[h] = *(const uint32_t*)&c2;
+        wo[h] = *(const uint32_t*)&o2;
+      }
+      const int off = lane * 64 + ((q8 ^ ((lane >> 1) & 3)) << 4);  // SW64 box layout
+      *(uint4*)(st + off) = make_uint4(wc[0], wc[1], wc[2], wc[3]);
+      *(uint4*)(st + EPI_BOX / 2 + off) = make_uint4(wo[0], wo[1], wo[2], wo[3]);
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(mc, su32(st), col, row0, z);
+      tma_store_3d(mc2, su32(st + EPI_BOX / 2), col, row0, z);
+      bulk_commit();
+    }
+    return;
+  }
   float f[32];
 #pragma unroll
   for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
