@@ -158,10 +158,51 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
     }
     return;
   }
+  if (epi.kind == EPI_FFN_BWD) {
+    // C = acc * dropout_scale * gelu'(h): the aux box (32 rows x 32 bf16) staged in the second half of
+    // this warp's staging box with coalesced loads, consumed and the output staged 8 columns at a time
+    const int e = (int)(row / (size_t)epi.Te), tl = (int)(row - (size_t)e * epi.Te);
+    const uint64_t sd = epi.p > 0.f ? derive3(ffn::TAG_FFN_DROP, epi.seed, (uint64_t)(epi.est_base + e)) : 0;
+    const float keep = epi.p < 1.f ? 1.f / (1.f - epi.p) : 0.f;
+    uint8_t* const ab = st + EPI_BOX / 2;
+    if (lane == 0) bulk_wait_read1();
+    __syncwarp();
+#pragma unroll
+    for (int pass = 0; pass < 4; ++pass) {
+      const int rr = pass * 8 + (lane >> 2), qq = lane & 3;
+      const uint4 a4 = *(const uint4*)(epi.aux + ((size_t)row0 + rr) * N + col + qq * 8);
+      *(uint4*)(ab + rr * 64 + ((qq ^ ((rr >> 1) & 3)) << 4)) = a4;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q8 = 0; q8 < 4; ++q8) {
+      const int off = lane * 64 + ((q8 ^ ((lane >> 1) & 3)) << 4);
+      const uint4 u = *(const uint4*)(ab + off);
+      const __nv_bfloat162* h2 = (const __nv_bfloat162*)&u;
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 gp = __bfloat1622float2(h2[k]);
+        const int q = 8 * q8 + 2 * k;
+        float m0, m1;
+        ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
+        const __nv_bfloat162 o2 = __floats2bfloat162_rn(__uint_as_float(v[q]) * m0 * gp.x,
+                                                        __uint_as_float(v[q + 1]) * m1 * gp.y);
+        w[k] = *(const uint32_t*)&o2;
+      }
+      *(uint4*)(st + off) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(mc, su32(st), col, row0, z);
+      bulk_commit();
+    }
+    return;
+  }
   float f[32];
 #pragma unroll
   for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
-  float g[32];  // second output (FFN_FWD)
   if (epi.kind == EPI_BIAS) {
 #pragma unroll
     for (int q4 = 0; q4 < 8; ++q4) {
@@ -171,64 +212,11 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
       f[4 * q4 + 2] += bv.z;
       f[4 * q4 + 3] += bv.w;
     }
-  } else if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) {
-    const int e = (int)(row / (size_t)epi.Te), tl = (int)(row - (size_t)e * epi.Te);
-    // the EST's dropout stream only when there is dropout (p == 0: every scale is 1, no draw)
-    const uint64_t sd = epi.p > 0.f ? derive3(ffn::TAG_FFN_DROP, epi.seed, (uint64_t)(epi.est_base + e)) : 0;
-    const float keep = epi.p < 1.f ? 1.f / (1.f - epi.p) : 0.f;
-    if (epi.kind == EPI_FFN_FWD) {
-      float b[32];  // the chunk's 32 biases, 8 vector loads
-#pragma unroll
-      for (int q4 = 0; q4 < 8; ++q4) {
-        const float4 bv = *(const float4*)(epi.bias + col + 4 * q4);
-        b[4 * q4] = bv.x;
-        b[4 * q4 + 1] = bv.y;
-        b[4 * q4 + 2] = bv.z;
-        b[4 * q4 + 3] = bv.w;
-      }
-#pragma unroll
-      for (int q = 0; q < 32; q += 2) {
-        float m0, m1, g0, g1;
-        ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
-        ffn::gelu_and_grad(f[q] + b[q], &g0, &f[q]);  // C = gelu'(h) for the backward
-        ffn::gelu_and_grad(f[q + 1] + b[q + 1], &g1, &f[q + 1]);
-        g[q] = g0 * m0;
-        g[q + 1] = g1 * m1;
-      }
-    } else {
-      // aux box (32 rows x 32 bf16 = 64 B per row) staged through the second half of this warp's staging
-      // box with coalesced 16-byte loads (4 lanes per row), then read back row-per-lane (SW64 pattern)
-      uint8_t* const ab = st + EPI_BOX / 2;
-      if (lane == 0) bulk_wait_read1();  // (the box's previous store read only its first half; order anyway)
-      __syncwarp();
-#pragma unroll
-      for (int pass = 0; pass < 4; ++pass) {
-        const int rr = pass * 8 + (lane >> 2), qq = lane & 3;
-        const uint4 v = *(const uint4*)(epi.aux + ((size_t)row0 + rr) * N + col + qq * 8);
-        *(uint4*)(ab + rr * 64 + ((qq ^ ((rr >> 1) & 3)) << 4)) = v;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const uint4 u = *(const uint4*)(ab + lane * 64 + ((q4 ^ ((lane >> 1) & 3)) << 4));
-        const __nv_bfloat162* h2 = (const __nv_bfloat162*)&u;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 gp = __bfloat1622float2(h2[k]);
-          const int q = q4 * 8 + 2 * k;
-          float m0, m1;
-          ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
-          f[q] = f[q] * m0 * gp.x;
-          f[q + 1] = f[q + 1] * m1 * gp.y;
-        }
-      }
-    }
   }
   if (lane == 0) bulk_wait_read1();  // the store that last used this box (two chunks ago) has read it
   __syncwarp();
   if (OUT_BF16) {
     stage_bf16(st, f, lane);
-    if (epi.kind == EPI_FFN_FWD) stage_bf16(st + EPI_BOX / 2, g, lane);
   } else {
     stage_f32(st, f, lane);
   }
@@ -236,7 +224,6 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
   __syncwarp();
   if (lane == 0) {
     tma_store_3d(mc, su32(st), col, row0, z);
-    if (epi.kind == EPI_FFN_FWD) tma_store_3d(mc2, su32(st + EPI_BOX / 2), col, row0, z);
     bulk_commit();
   }
 }
@@ -847,7 +834,7 @@ static int launch_any(const GemmShape& g, int out_bf16, int grid, cudaStream_t s
   constexpr int SP = gemm::EPI_WARPS == 8 ? 5 : 3, S256 = gemm::EPI_WARPS == 8 ? 3 : 2,
                 S64 = gemm::EPI_WARPS == 8 ? 6 : 4, S128 = gemm::EPI_WARPS == 8 ? 5 : 3;
   if (g.M % 256 == 0 && g.N % 256 == 0 && gemm_variant() != 1) {
-    if (g.epi.kind == EPI_FFN_FWD)  // the ALU-heavy GELU epilogue: 16 epilogue warps
+    if (g.epi.kind == EPI_FFN_FWD || g.epi.kind == EPI_FFN_BWD)  // ALU-heavy epilogues: 16 epilogue warps
       return launch_gemm_pair<3, true, MN, 16>(g, grid, s);
     return out_bf16 ? launch_gemm_pair<SP, true, MN>(g, grid, s) : launch_gemm_pair<SP, false, MN>(g, grid, s);
   }
