@@ -247,6 +247,10 @@ int bt_cnn_bn_bwd(const void *z_dev, const void *dy_dev, const void *y_dev, cons
                   int32_t R, int32_t C, void *dz_dev, void *stream);
 /* out = a + (y ? b [y > 0] : b), n elements (bf16) */
 int bt_cnn_add(const void *a_dev, const void *b_dev, const void *y_dev, int64_t n, void *out_dev, void *stream);
+/* zero insertion: up [N][s*Hs][s*Ws][C] = src [N][Hs][Ws][C] at multiples of s, else 0 (bf16): the dX of a
+ * stride-s convolution as a stride-1 convolution of `up` with the flipped filter */
+int bt_cnn_upsample(const void *src_dev, int64_t N, int32_t Hs, int32_t Ws, int32_t C, int32_t s, void *up_dev,
+                    void *stream);
 /* avgpool 4x4 + fc 512->10 + softmax cross-entropy, forward and backward, one block per EST */
 int bt_cnn_head(const void *x_dev, const int32_t *labels_dev, const float *w_dev, const float *b_dev, int32_t E,
                 int32_t B, float *dw_dev, float *db_dev, int64_t grad_stride, float *loss_dev, void *dx_dev,

@@ -84,6 +84,7 @@ int cnn_bn_bwd_launch(const void* z, const void* dy, const void* y, const float*
                       const float* sg, const float* sgx, const float* gamma, int E, int R, int C, void* dz,
                       cudaStream_t s);
 int cnn_add_launch(const void* a, const void* b, const void* y, int64_t n, void* out, cudaStream_t s);
+int cnn_upsample_launch(const void* src, int64_t N, int Hs, int Ws, int C, int s, void* up, cudaStream_t st);
 int cnn_head_launch(const void* x, const int32_t* labels, const float* W, const float* bias, int E, int B, float* dW,
                     float* db, int64_t grad_stride, float* loss, void* dx, cudaStream_t s);
 int cnn_conv_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* Co, const int* T,
@@ -753,6 +754,12 @@ int bt_cnn_bn_bwd(const void* z_dev, const void* dy_dev, const void* y_dev, cons
 int bt_cnn_add(const void* a_dev, const void* b_dev, const void* y_dev, int64_t n, void* out_dev, void* stream) {
   if (!a_dev || !b_dev || !out_dev || n % 8) return fail(bt::ERR_INPUT, "bt_cnn_add arguments");
   return done(bt::cnn_add_launch(a_dev, b_dev, y_dev, n, out_dev, STREAM(stream)), "bt_cnn_add");
+}
+int bt_cnn_upsample(const void* src_dev, int64_t N, int32_t Hs, int32_t Ws, int32_t C, int32_t s, void* up_dev,
+                    void* stream) {
+  if (!src_dev || !up_dev || N < 1 || Hs < 1 || Ws < 1) return fail(bt::ERR_INPUT, "bt_cnn_upsample arguments");
+  return done(bt::cnn_upsample_launch(src_dev, N, Hs, Ws, C, s, up_dev, STREAM(stream)),
+              "bt_cnn_upsample (C a power of two >= 8, s in {1, 2})");
 }
 int bt_cnn_head(const void* x_dev, const int32_t* labels_dev, const float* w_dev, const float* b_dev, int32_t E,
                 int32_t B, float* dw_dev, float* db_dev, int64_t grad_stride, float* loss_dev, void* dx_dev,

@@ -306,6 +306,26 @@ __global__ void __launch_bounds__(256) add_kernel(const __nv_bfloat16* __restric
   }
 }
 
+// ---------------------------------------------------------------- zero insertion
+// up[n][y][x][c] = src[n][y/s][x/s][c] when y and x are multiples of s, else 0 ([N][s*Hs][s*Ws][C]):
+// the dX of a stride-s convolution becomes a stride-1 convolution of `up` with the flipped filter
+// (the transposed convolution's gather with its zero taps made explicit), so it runs as an implicit GEMM.
+__global__ void __launch_bounds__(256) upsample_kernel(const __nv_bfloat16* __restrict__ src, int64_t rows, int Hs,
+                                                       int Ws, int lc8, int s, __nv_bfloat16* __restrict__ up) {
+  const int Hu = Hs * s, Wu = Ws * s;
+  const int64_t n = rows * ((int64_t)Hu * Wu) << lc8;  // 16-byte chunks of up
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pix = i >> lc8;
+    const int c8 = (int)(i & ((1 << lc8) - 1));
+    const int64_t img = pix / ((int64_t)Hu * Wu);
+    const int r = (int)(pix - img * Hu * Wu), y = r / Wu, x = r - y * Wu;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if ((y % s) == 0 && (x % s) == 0)
+      v = *(const uint4*)(src + ((((size_t)img * Hs + y / s) * Ws + x / s) << lc8) * 8 + c8 * 8);
+    ((uint4*)up)[i] = v;
+  }
+}
+
 // ---------------------------------------------------------------- head
 // Per EST (one block): pooled[n][c] = mean of the 16 positions (4x4) in order; logits = pooled Wfc^T + b
 // (c ascending); loss = mean_n CE(softmax(logits), label); dlogits = (p - onehot)/B; per-EST dWfc, dbfc
@@ -521,6 +541,15 @@ int cnn_add_launch(const void* a, const void* b, const void* y, int64_t n, void*
   if (n % 8) return ERR_INPUT;
   cnn::add_kernel<<<grid_n(n / 8), 256, 0, s>>>((const __nv_bfloat16*)a, (const __nv_bfloat16*)b,
                                                 (const __nv_bfloat16*)y, n / 8, (__nv_bfloat16*)out);
+  return ok_or_cuda_c();
+}
+
+int cnn_upsample_launch(const void* src, int64_t N, int Hs, int Ws, int C, int s, void* up, cudaStream_t st) {
+  int lc8 = 0;
+  while ((8 << lc8) < C) ++lc8;
+  if ((8 << lc8) != C || (s != 1 && s != 2)) return ERR_INPUT;
+  cnn::upsample_kernel<<<grid_n(N * Hs * Ws * s * s * (C / 8)), 256, 0, st>>>((const __nv_bfloat16*)src, N, Hs, Ws, lc8,
+                                                                              s, (__nv_bfloat16*)up);
   return ok_or_cuda_c();
 }
 

@@ -144,7 +144,7 @@ class ResNetJob:
             self._cast[1][i] = self.wb.data_ptr() + 2 * self.woff[cv.name]
             self._cast[2][i] = self.wt.data_ptr() + 2 * self.woff[cv.name]
             self._cast[3][i], self._cast[4][i], self._cast[5][i] = cv.co, cv.taps, cv.ci
-            self._cast[6][i] = 1 if cv.s == 1 else 0  # stride-1 dX = forward convolution with the flipped filter
+            self._cast[6][i] = 1  # dX = a stride-1 convolution (of dz, or of its zero insertion) with the flipped filter
         self.flags = Flags()
         self.step_idx = 0
         self._ws = {}
@@ -200,6 +200,11 @@ class ResNetJob:
         forces the explicit im2col path (the same tiles and K order: the same bits)."""
         return cv.ci % 64 == 0 and (self.B * cv.hout ** 2) % 64 == 0 and os.environ.get("BT_CONV_EXPLICIT") != "1"
 
+    def implicit_dx(self, cv) -> bool:
+        """The input gradient as an implicit GEMM: a stride-1 convolution over dz (stride 1) or over its zero
+        insertion (stride 2), whose input channels are cv.co and output pixels the forward input grid."""
+        return cv.co % 64 == 0 and (self.B * cv.hin ** 2) % 64 == 0 and os.environ.get("BT_CONV_EXPLICIT") != "1"
+
     def splits(self, cv) -> int:
         """Pinned pixel splits of an EST's weight-gradient reduction (a function of the shape only)."""
         return max(1, (self.B * cv.hout ** 2) // 2048)
@@ -216,12 +221,14 @@ class ResNetJob:
             return ws
         B = self.B
         bf, f32 = dict(dtype=torch.bfloat16, device="cuda"), dict(dtype=torch.float32, device="cuda")
-        col = 0  # the dX gathers: stride-2 transposed convolutions, explicit stride-1 fallbacks
+        col = up = 0  # the dX gathers of explicit fallbacks; the zero insertions of stride-2 dz
         for cv in self.convs:
-            if cv.name != "stem" and (cv.s != 1 or not self.implicit(cv)):
+            if cv.name != "stem" and not self.implicit_dx(cv):
                 col = max(col, n * B * cv.hin ** 2 * cv.taps * cv.co)
+            if cv.name != "stem" and cv.s != 1:
+                up = max(up, n * B * cv.hin ** 2 * cv.co)
         ws = {"img": torch.empty(n * B * 1024 * 8, **bf), "labels": torch.empty(n * B, dtype=torch.int32, device="cuda"),
-              "col": torch.empty(col, **bf), "loss": torch.empty(n, **f32)}
+              "col": torch.empty(col, **bf), "up": torch.empty(up, **bf), "loss": torch.empty(n, **f32)}
         for cv in self.convs:
             R = n * B * cv.hout ** 2
             ws[cv.name] = {"z": torch.empty(R * cv.co, **bf), "y": torch.empty(R * cv.co, **bf),
@@ -288,7 +295,7 @@ class ResNetJob:
     def _conv_bwd(self, ws, cv, n, base, x, dz, dx):
         """dW_e into each EST's gradient slot (implicit GEMM over the EST's output pixels, or the forward's
         explicit im2col) and, if dx is given, the input gradient: stride 1 = a forward convolution of dz
-        with the flipped filter; stride 2 = the transposed-convolution gather + GEMM."""
+        with the flipped filter; stride 2 = the same over the zero insertion of dz (bt_cnn_upsample)."""
         L, s, B = _native.lib(), stream(), self.B
         Re = B * cv.hout ** 2
         gdst = self.grads.data_ptr() + 4 * (base * self.P + self.off[cv.name][0])
@@ -308,13 +315,18 @@ class ResNetJob:
             return
         Rin = n * B * cv.hin ** 2
         wt = self.wt.data_ptr() + 2 * self.woff[cv.name]
-        if cv.s == 1 and self.implicit(cv):
-            _native.check(L.bt_gemm_conv(0, dz.data_ptr(), n * B, cv.hout, cv.hout, cv.co, cv.hin, cv.hin, cv.k, cv.k,
-                                         1, cv.p, wt, dx.data_ptr(), cv.ci, 1, 0, 0, 1, s), "conv dX (implicit)")
+        pad = cv.k - 1 - cv.p
+        src, hs = dz, cv.hout
+        if cv.s != 1:  # zero insertion: the transposed convolution becomes a stride-1 convolution of `up`
+            src, hs = ws["up"], cv.hin
+            _native.check(L.bt_cnn_upsample(dz.data_ptr(), n * B, cv.hout, cv.hout, cv.co, cv.s, src.data_ptr(), s),
+                          "dz zero insertion")
+        if self.implicit_dx(cv):
+            _native.check(L.bt_gemm_conv(0, src.data_ptr(), n * B, hs, hs, cv.co, cv.hin, cv.hin, cv.k, cv.k, 1, pad,
+                                         wt, dx.data_ptr(), cv.ci, 1, 0, 0, 1, s), "conv dX (implicit)")
             return
-        # stride 1: forward im2col of dz (flipped filter); stride 2: the transposed gather
-        _native.check(L.bt_cnn_im2col(dz.data_ptr(), ws["col"].data_ptr(), n * B, cv.hout, cv.hout, cv.co, cv.hin,
-                                      cv.hin, cv.k, cv.k, cv.s, cv.p, 0 if cv.s == 1 else 1, s), "dX im2col")
+        _native.check(L.bt_cnn_im2col(src.data_ptr(), ws["col"].data_ptr(), n * B, hs, hs, cv.co, cv.hin, cv.hin, cv.k,
+                                      cv.k, 1, pad, 0, s), "dX im2col")
         _native.check(L.bt_gemm_bf16_ex(ws["col"].data_ptr(), wt, dx.data_ptr(), 1, Rin, cv.ci, cv.taps * cv.co, 0, 0,
                                         0, 1, None, 0, 0, s), "conv dX gemm")
 

@@ -237,7 +237,7 @@ def test_implicit_gemm_convolutions_equal_explicit_im2col(rn, monkeypatch):
 def test_convolution_products_match_float64(rn, ci, co, k, s, hw):
     """The implicit-GEMM convolution (bt_gemm_conv: TMA im2col loads), its weight gradient and the dX
     paths (stride 1: forward convolution of dz with the tap-reversed filter; stride 2: the transposed
-    gather) against torch's float64 conv2d / conv2d_weight / conv2d_input on the same bf16 values:
+    gather, and the zero insertion of dz convolved at stride 1) against torch's float64 conv2d / conv2d_weight / conv2d_input on the same bf16 values:
     fp32-accumulation error only (rel. Frobenius <= 1e-5 for fp32 outputs, bf16 rounding for bf16)."""
     from torch.nn.grad import conv2d_input, conv2d_weight
 
@@ -282,6 +282,17 @@ def test_convolution_products_match_float64(rn, ci, co, k, s, hw):
         _native.check(L.bt_gemm_bf16_ex(col.data_ptr(), wt.data_ptr(), dx.data_ptr(), 1, N * hw * hw, ci, k * k * co,
                                         0, 0, 0, 0, None, 0, 0, stream()))
     _close(dx, dxref, "conv dX", 1e-5)
+    if s != 1:  # the step's path: zero insertion of dz, then a stride-1 implicit convolution (flipped filter)
+        up = torch.empty(N, hw, hw, co, dtype=torch.bfloat16, device="cuda")
+        _native.check(L.bt_cnn_upsample(dz.data_ptr(), N, ho, ho, co, s, up.data_ptr(), stream()))
+        upref = torch.zeros_like(up)
+        upref[:, ::s, ::s, :] = dz
+        assert torch.equal(up, upref)
+        wflip = torch.flip(w.view(co, k, k, ci), dims=(1, 2)).permute(3, 1, 2, 0).contiguous()
+        dx2 = torch.empty(N * hw * hw, ci, device="cuda")
+        _native.check(L.bt_gemm_conv(0, up.data_ptr(), N, hw, hw, co, hw, hw, k, k, 1, k - 1 - p, wflip.data_ptr(),
+                                     dx2.data_ptr(), ci, 1, 0, 0, 0, stream()))
+        _close(dx2, dxref, "conv dX (zero insertion)", 1e-5)
 
 
 def test_cuda_graph_replay_equals_eager_across_rescale(rn):

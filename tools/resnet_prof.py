@@ -32,3 +32,8 @@ all_us = sum(tot.values())
 for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
     print(f"{v / 1e3:9.3f} ms  {100 * v / all_us:5.1f}%  x{cnt[k]:4d}  {k}")
 print(f"total kernel time {all_us / 1e3:.3f} ms")
+if "--seq" in sys.argv:
+    evs = [ev for ev in prof.events() if ev.device_type == torch.autograd.DeviceType.CUDA]
+    evs.sort(key=lambda e: e.time_range.start)
+    for ev in evs:
+        print(f"{ev.device_time_total:9.1f} us  {ev.name.split('(')[0][:90]}")
