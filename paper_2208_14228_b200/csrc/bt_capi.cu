@@ -738,7 +738,9 @@ int bt_cnn_bn_stats(int32_t mode, const void* z_dev, const void* dy_dev, const v
 int bt_cnn_bn_apply(const void* z_dev, const void* res_dev, const float* mean_dev, const float* rstd_dev,
                     const float* gamma_dev, const float* beta_dev, int32_t E, int32_t R, int32_t C, int32_t relu,
                     void* y_dev, void* stream) {
-  if (E < 1 || R < 1 || C % 8 || !z_dev || !y_dev) return fail(bt::ERR_INPUT, "bt_cnn_bn_apply arguments");
+  if (E < 1 || R < 1 || C % 8 || !z_dev || !y_dev || !mean_dev || !rstd_dev || !gamma_dev || !beta_dev ||
+      (((uintptr_t)mean_dev | (uintptr_t)rstd_dev | (uintptr_t)gamma_dev | (uintptr_t)beta_dev) & 15))
+    return fail(bt::ERR_INPUT, "bt_cnn_bn_apply arguments (per-channel vectors 16-byte aligned)");
   return done(bt::cnn_bn_apply_launch(z_dev, res_dev, mean_dev, rstd_dev, gamma_dev, beta_dev, E, R, C, relu, y_dev,
                                       STREAM(stream)),
               "bt_cnn_bn_apply");
@@ -746,7 +748,10 @@ int bt_cnn_bn_apply(const void* z_dev, const void* res_dev, const float* mean_de
 int bt_cnn_bn_bwd(const void* z_dev, const void* dy_dev, const void* y_dev, const float* mean_dev,
                   const float* rstd_dev, const float* sg_dev, const float* sgx_dev, const float* gamma_dev, int32_t E,
                   int32_t R, int32_t C, void* dz_dev, void* stream) {
-  if (E < 1 || R < 1 || C % 8 || !z_dev || !dy_dev || !y_dev || !dz_dev) return fail(bt::ERR_INPUT, "bt_cnn_bn_bwd");
+  if (E < 1 || R < 1 || C % 8 || !z_dev || !dy_dev || !y_dev || !dz_dev || !mean_dev || !rstd_dev || !sg_dev ||
+      !sgx_dev || !gamma_dev ||
+      (((uintptr_t)mean_dev | (uintptr_t)rstd_dev | (uintptr_t)sg_dev | (uintptr_t)sgx_dev | (uintptr_t)gamma_dev) & 15))
+    return fail(bt::ERR_INPUT, "bt_cnn_bn_bwd arguments (per-channel vectors 16-byte aligned)");
   return done(bt::cnn_bn_bwd_launch(z_dev, dy_dev, y_dev, mean_dev, rstd_dev, sg_dev, sgx_dev, gamma_dev, E, R, C,
                                     dz_dev, STREAM(stream)),
               "bt_cnn_bn_bwd");

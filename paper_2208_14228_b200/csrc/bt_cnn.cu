@@ -25,7 +25,9 @@ namespace cnn {
 
 constexpr uint64_t TAG_CNN_X = 0x434e'4e5f'5844'4154ull;      // "CNN_XDAT"
 constexpr uint64_t TAG_CNN_LABEL = 0x434e'4e5f'4c41'424cull;  // "CNN_LABL"
-constexpr int CHUNK = 256;  // rows per column-statistics partial (fixed: part of the reduction's shape)
+// rows per column-statistics partial: a function of the channel count only (part of the reduction's
+// shape, so the same for every EST mapping); ~128 KB of bf16 per block
+__host__ __device__ inline int chunk_rows(int C) { return C >= 256 ? 256 : 65536 / C; }
 
 __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* v) {
   const uint4 u = *(const uint4*)p;
@@ -36,6 +38,10 @@ __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* v) {
     v[2 * k] = f.x;
     v[2 * k + 1] = f.y;
   }
+}
+__device__ __forceinline__ void ldf8(const float* p, float* v) {  // 32-byte aligned
+  const float4 a = __ldg((const float4*)p), b = __ldg((const float4*)p + 1);
+  v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
 }
 __device__ __forceinline__ void st8(__nv_bfloat16* p, const float* v) {
   uint4 u;
@@ -115,7 +121,7 @@ __global__ void __launch_bounds__(256) im2col_kernel(const ColArgs a, int lcg) {
 }
 
 // ---------------------------------------------------------------- BatchNorm
-// Column statistics per EST over fixed CHUNK-row chunks: block = (chunk k, local EST e);
+// Column statistics per EST over fixed chunk_rows(C)-row chunks: block = (chunk k, local EST e);
 // thread = (row lane, 8-channel group); rows walked in order, lanes combined in lane order.
 //   mode 0: sum (z - k), sum (z - k)^2   (one pass; k = the EST's first row, a per-channel shift
 //           that keeps the variance free of cancellation)
@@ -127,7 +133,7 @@ struct StatArgs {
   const float* mean;          // [E][C] (mode 2)
   const float* rstd;          // [E][C] (mode 2)
   float* part;                // [E][chunks][2][C]
-  int C, R, mode;             // R = rows per EST
+  int C, R, mode, chunk;      // R = rows per EST, chunk = chunk_rows(C)
 };
 __global__ void __launch_bounds__(256) stats_kernel(const StatArgs a) {
   extern __shared__ float st_smem[];  // [lanes][2][C]
@@ -142,8 +148,9 @@ __global__ void __launch_bounds__(256) stats_kernel(const StatArgs a) {
       for (int q = 0; q < 8; ++q) m[q] = a.mean[(size_t)e * a.C + c0 + q];
     if (a.mode == 2)
       for (int q = 0; q < 8; ++q) r[q] = a.rstd[(size_t)e * a.C + c0 + q];
-    const int r1 = min(a.R, (k + 1) * CHUNK);
-    for (int row = k * CHUNK + lane; row < r1; row += lanes) {
+    const int r1 = min(a.R, (k + 1) * a.chunk);
+#pragma unroll 4
+    for (int row = k * a.chunk + lane; row < r1; row += lanes) {
       const size_t off = ((size_t)e * a.R + row) * a.C + c0;
       float zv[8];
       ld8(a.z + off, zv);
@@ -204,6 +211,7 @@ __global__ void fold_kernel(const FoldArgs a) {
     const int e = (int)(i / a.C), c = (int)(i - (int64_t)e * a.C);
     const float* p = a.part + (size_t)e * a.chunks * 2 * a.C + c;
     float s0 = p[0], s1 = p[a.C];
+#pragma unroll 4
     for (int k = 1; k < a.chunks; ++k) {
       s0 += p[(size_t)k * 2 * a.C];
       s1 += p[(size_t)k * 2 * a.C + a.C];
@@ -239,14 +247,17 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(const __nv_bfloat16* __re
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int row = i / cg;
     const int c0 = (i - row * cg) * 8, e = row / R;
-    float zv[8], o[8], rv[8];
+    float zv[8], o[8], rv[8], mv[8], sv[8], gv[8], bv[8];
     const size_t off = (size_t)row * C + c0;
     ld8(z + off, zv);
     if (res) ld8(res + off, rv);
+    ldf8(mean + (size_t)e * C + c0, mv);
+    ldf8(rstd + (size_t)e * C + c0, sv);
+    ldf8(gamma + c0, gv);
+    ldf8(beta + c0, bv);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int c = c0 + q;
-      float v = gamma[c] * ((zv[q] - mean[(size_t)e * C + c]) * rstd[(size_t)e * C + c]) + beta[c];
+      float v = gv[q] * ((zv[q] - mv[q]) * sv[q]) + bv[q];
       if (res) v += rv[q];
       o[q] = (relu && !(v > 0.f)) ? 0.f : v;
     }
@@ -268,17 +279,21 @@ __global__ void __launch_bounds__(256) bn_bwd_kernel(const __nv_bfloat16* __rest
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int row = i / cg;
     const int c0 = (i - row * cg) * 8, e = row / R;
-    float zv[8], dv[8], yv[8], o[8];
-    const size_t off = (size_t)row * C + c0;
+    float zv[8], dv[8], yv[8], o[8], mv[8], sv[8], gv[8], av[8], bv[8];
+    const size_t off = (size_t)row * C + c0, ec = (size_t)e * C + c0;
     ld8(z + off, zv);
     ld8(dy + off, dv);
     ld8(y + off, yv);
+    ldf8(mean + ec, mv);
+    ldf8(rstd + ec, sv);
+    ldf8(sg + ec, av);
+    ldf8(sgx + ec, bv);
+    ldf8(gamma + c0, gv);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const size_t ec = (size_t)e * C + c0 + q;
       const float g = yv[q] > 0.f ? dv[q] : 0.f;
-      const float xh = (zv[q] - mean[ec]) * rstd[ec];
-      o[q] = gamma[c0 + q] * rstd[ec] * (g - sg[ec] * invR - xh * (sgx[ec] * invR));
+      const float xh = (zv[q] - mv[q]) * sv[q];
+      o[q] = gv[q] * sv[q] * (g - av[q] * invR - xh * (bv[q] * invR));
     }
     st8(dz + off, o);
   }
@@ -483,7 +498,7 @@ int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, 
                         float* dgamma, float* dbeta, int64_t grad_stride, int E, int R, int C, float eps,
                         cudaStream_t s) {
   if (C % 8 || C > 2048 || R < 2 || mode == 1) return ERR_INPUT;
-  const int chunks = (R + cnn::CHUNK - 1) / cnn::CHUNK;
+  const int chunk = cnn::chunk_rows(C), chunks = (R + chunk - 1) / chunk;
   const int lanes = 256 / (C / 8);
   const int smem = lanes * 2 * C * (int)sizeof(float);
   static bool attr = false;
@@ -494,7 +509,7 @@ int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, 
     attr = true;
   }
   cnn::StatArgs sa{(const __nv_bfloat16*)z, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)y,
-                   mean, rstd, part, C, R, mode};
+                   mean, rstd, part, C, R, mode, chunk};
   cnn::stats_kernel<<<dim3(chunks, E), 256, smem, s>>>(sa);
   cnn::FoldArgs fa{};
   fa.part = part;
