@@ -229,7 +229,8 @@ int bt_cnn_data(uint64_t seed, const int64_t *cursor_dev, int32_t est_base, int3
  * ((ho+p-kh)/s, (wo+p-kw)/s) when exact (the dX gather of a stride-s convolution) */
 int bt_cnn_im2col(const void *src_dev, void *col_dev, int32_t N, int32_t Hs, int32_t Ws, int32_t C, int32_t Ho,
                   int32_t Wo, int32_t KH, int32_t KW, int32_t stride, int32_t pad, int32_t transposed, void *stream);
-/* per-EST column statistics over fixed 256-row chunks folded in order; mode 0 (one pass over z, shifted
+/* per-EST column statistics over fixed 256-row chunks (1024 for mode 0 with C <= 64; C in {8, 16, 32, 64} or a multiple of 64), the
+ * chunk partials folded in a fixed shape (32 lanes in chunk order, then a butterfly); mode 0 (one pass over z, shifted
  * by the EST's first row): mean, rstd and the running-statistics update of each EST's slot; mode 2:
  * backward sums (g, g*xhat) -> dbeta, dgamma of each EST's gradient slot (g = dy * [y > 0]).
  * part_dev: E * ceil(R/256) * 2 * C floats */

@@ -25,9 +25,9 @@ namespace cnn {
 
 constexpr uint64_t TAG_CNN_X = 0x434e'4e5f'5844'4154ull;      // "CNN_XDAT"
 constexpr uint64_t TAG_CNN_LABEL = 0x434e'4e5f'4c41'424cull;  // "CNN_LABL"
-// rows per column-statistics partial: a function of the channel count only (part of the reduction's
-// shape, so the same for every EST mapping); ~128 KB of bf16 per block
-__host__ __device__ inline int chunk_rows(int C) { return C >= 256 ? 256 : 65536 / C; }
+// rows per column-statistics partial: a function of the channel count and the mode only (part of the
+// reduction's shape, the same for every EST mapping); sized for the HBM pass at ResNet-18 shapes
+inline int chunk_rows(int C, int mode) { return mode == 0 && C <= 64 ? 1024 : 256; }
 
 __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* v) {
   const uint4 u = *(const uint4*)p;
@@ -121,8 +121,8 @@ __global__ void __launch_bounds__(256) im2col_kernel(const ColArgs a, int lcg) {
 }
 
 // ---------------------------------------------------------------- BatchNorm
-// Column statistics per EST over fixed chunk_rows(C)-row chunks: block = (chunk k, local EST e);
-// thread = (row lane, 8-channel group); rows walked in order, lanes combined in lane order.
+// Column statistics per EST over fixed chunk_rows(C, mode)-row chunks: block = (chunk k, 64-channel slice, local EST
+// e); thread = (row lane, 8-channel group); rows walked in order, lanes combined in lane order.
 //   mode 0: sum (z - k), sum (z - k)^2   (one pass; k = the EST's first row, a per-channel shift
 //           that keeps the variance free of cancellation)
 //   mode 2: sum g, sum g * xhat         (g = dy * [y > 0], xhat = (z - mean) * rstd)
@@ -135,56 +135,66 @@ struct StatArgs {
   float* part;                // [E][chunks][2][C]
   int C, R, mode, chunk;      // R = rows per EST, chunk = chunk_rows(C)
 };
-__global__ void __launch_bounds__(256) stats_kernel(const StatArgs a) {
-  extern __shared__ float st_smem[];  // [lanes][2][C]
-  const int k = blockIdx.x, e = blockIdx.y, chunks = gridDim.x;
-  const int cg = a.C / 8, lanes = 256 / cg;  // C <= 2048
-  const int lane = threadIdx.x / cg, c0 = (threadIdx.x % cg) * 8;
+template <int MODE>
+__global__ void __launch_bounds__(256, 4) stats_kernel(const StatArgs a) {
+  __shared__ float st_smem[8 * 2 * 64];  // [warps][2][SW]
+  const int k = blockIdx.x, e = blockIdx.z, chunks = gridDim.x;
+  const int SW = min(a.C, 64), cg = SW / 8, lanes = 256 / cg;
+  const int lane = threadIdx.x / cg, cl = (threadIdx.x % cg) * 8, c0 = blockIdx.y * 64 + cl;
   float s0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, s1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   float m[8], r[8];
-  if (lane < lanes) {
-    if (a.mode == 0) ld8(a.z + (size_t)e * a.R * a.C + c0, m);  // shift k = row 0 of the EST
-    else
-      for (int q = 0; q < 8; ++q) m[q] = a.mean[(size_t)e * a.C + c0 + q];
-    if (a.mode == 2)
-      for (int q = 0; q < 8; ++q) r[q] = a.rstd[(size_t)e * a.C + c0 + q];
-    const int r1 = min(a.R, (k + 1) * a.chunk);
+  if (MODE == 0) ld8(a.z + (size_t)e * a.R * a.C + c0, m);  // shift k = row 0 of the EST
+  else
+    for (int q = 0; q < 8; ++q) m[q] = a.mean[(size_t)e * a.C + c0 + q];
+  if (MODE == 2)
+    for (int q = 0; q < 8; ++q) r[q] = a.rstd[(size_t)e * a.C + c0 + q];
+  const int r1 = min(a.R, (k + 1) * a.chunk);
 #pragma unroll 4
-    for (int row = k * a.chunk + lane; row < r1; row += lanes) {
-      const size_t off = ((size_t)e * a.R + row) * a.C + c0;
-      float zv[8];
-      ld8(a.z + off, zv);
-      if (a.mode == 0) {
+  for (int row = k * a.chunk + lane; row < r1; row += lanes) {
+    const size_t off = ((size_t)e * a.R + row) * a.C + c0;
+    float zv[8];
+    ld8(a.z + off, zv);
+    if (MODE == 0) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float d = zv[q] - m[q];
-          s0[q] += d;
-          s1[q] += d * d;
-        }
-      } else {
-        float dv[8], yv[8];
-        ld8(a.dy + off, dv);
-        ld8(a.y + off, yv);
+      for (int q = 0; q < 8; ++q) {
+        const float d = zv[q] - m[q];
+        s0[q] += d;
+        s1[q] += d * d;
+      }
+    } else {
+      float dv[8], yv[8];
+      ld8(a.dy + off, dv);
+      ld8(a.y + off, yv);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float g = yv[q] > 0.f ? dv[q] : 0.f;
-          s0[q] += g;
-          s1[q] += g * ((zv[q] - m[q]) * r[q]);
-        }
+      for (int q = 0; q < 8; ++q) {
+        const float g = yv[q] > 0.f ? dv[q] : 0.f;
+        s0[q] += g;
+        s1[q] += g * ((zv[q] - m[q]) * r[q]);
       }
     }
+  }
+  // lanes of a warp (32 / cg row lanes) combined by a fixed butterfly, then the 8 warps in order
+  for (int o = cg; o < 32; o <<= 1)
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      st_smem[(size_t)(lane * 2 + 0) * a.C + c0 + q] = s0[q];
-      st_smem[(size_t)(lane * 2 + 1) * a.C + c0 + q] = s1[q];
+      s0[q] += __shfl_xor_sync(0xffffffffu, s0[q], o);
+      s1[q] += __shfl_xor_sync(0xffffffffu, s1[q], o);
     }
-  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) < cg)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      st_smem[(warp * 2 + 0) * SW + cl + q] = s0[q];
+      st_smem[(warp * 2 + 1) * SW + cl + q] = s1[q];
+    }
   __syncthreads();
-  float* out = a.part + ((size_t)e * chunks + k) * 2 * a.C;
-  for (int i = threadIdx.x; i < 2 * a.C; i += 256) {
-    float acc = st_smem[i];
-    for (int l = 1; l < lanes; ++l) acc += st_smem[(size_t)l * 2 * a.C + i];
-    out[i] = acc;
+  float* out = a.part + ((size_t)e * chunks + k) * 2 * a.C + blockIdx.y * 64;
+  for (int i = threadIdx.x; i < 2 * SW; i += 256) {
+    const int j = i / SW, c = i - j * SW;
+    float acc = st_smem[j * SW + c];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) acc += st_smem[(w * 2 + j) * SW + c];
+    out[(size_t)j * a.C + c] = acc;
   }
 }
 
@@ -205,17 +215,26 @@ struct FoldArgs {
   int C, R, E, chunks, mode;
   float eps;
 };
+// One warp per (EST, channel): lane l sums chunks l, l+32, ... in order, then a fixed xor butterfly
+// (every lane ends with the same bits: IEEE addition commutes).
 __global__ void fold_kernel(const FoldArgs a) {
   const int64_t n = (int64_t)a.E * a.C;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int e = (int)(i / a.C), c = (int)(i - (int64_t)e * a.C);
     const float* p = a.part + (size_t)e * a.chunks * 2 * a.C + c;
-    float s0 = p[0], s1 = p[a.C];
-#pragma unroll 4
-    for (int k = 1; k < a.chunks; ++k) {
+    float s0 = 0.f, s1 = 0.f;
+    for (int k = lane; k < a.chunks; k += 32) {
       s0 += p[(size_t)k * 2 * a.C];
       s1 += p[(size_t)k * 2 * a.C + a.C];
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (lane) continue;
     if (a.mode == 0) {
       const float k = __bfloat162float(a.z[(size_t)e * a.R * a.C + c]);
       const float d = s0 / (float)a.R;
@@ -442,7 +461,20 @@ __global__ void fold_splits_kernel(const float* __restrict__ part, int E, int sp
     const int64_t j = (i - (int64_t)e * (n / 4)) * 4;
     const float* p = part + (size_t)e * splits * n + j;
     float4 acc = *(const float4*)p;
-    for (int sp = 1; sp < splits; ++sp) {
+    int sp = 1;
+    for (; sp + 3 < splits; sp += 4) {  // four loads in flight, added in split order
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = *(const float4*)(p + (size_t)(sp + u) * n);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
+    }
+    for (; sp < splits; ++sp) {
       const float4 v = *(const float4*)(p + (size_t)sp * n);
       acc.x += v.x;
       acc.y += v.y;
@@ -497,20 +529,14 @@ int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, 
                         float* sg, float* sgx, float* part, float* run_mean, float* run_var, int64_t run_stride,
                         float* dgamma, float* dbeta, int64_t grad_stride, int E, int R, int C, float eps,
                         cudaStream_t s) {
-  if (C % 8 || C > 2048 || R < 2 || mode == 1) return ERR_INPUT;
-  const int chunk = cnn::chunk_rows(C), chunks = (R + chunk - 1) / chunk;
-  const int lanes = 256 / (C / 8);
-  const int smem = lanes * 2 * C * (int)sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(cnn::stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024) !=
-        cudaSuccess)
-      return ERR_CUDA;
-    attr = true;
-  }
+  // C in {8, 16, 32, 64} or a multiple of 64 (64-channel slices per block)
+  if (!(C == 8 || C == 16 || C == 32 || C % 64 == 0) || C > 2048 || R < 2 || mode == 1) return ERR_INPUT;
+  const int chunk = cnn::chunk_rows(C, mode), chunks = (R + chunk - 1) / chunk;
   cnn::StatArgs sa{(const __nv_bfloat16*)z, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)y,
                    mean, rstd, part, C, R, mode, chunk};
-  cnn::stats_kernel<<<dim3(chunks, E), 256, smem, s>>>(sa);
+  const dim3 grid(chunks, C > 64 ? C / 64 : 1, E);
+  if (mode == 0) cnn::stats_kernel<0><<<grid, 256, 0, s>>>(sa);
+  else cnn::stats_kernel<2><<<grid, 256, 0, s>>>(sa);
   cnn::FoldArgs fa{};
   fa.part = part;
   fa.out0 = mode == 0 ? mean : sg;
@@ -528,7 +554,7 @@ int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, 
   fa.chunks = chunks;
   fa.mode = mode;
   fa.eps = eps;
-  cnn::fold_kernel<<<grid_n((int64_t)E * C), 256, 0, s>>>(fa);
+  cnn::fold_kernel<<<grid_n((int64_t)E * C * 32), 256, 0, s>>>(fa);
   return ok_or_cuda_c();
 }
 

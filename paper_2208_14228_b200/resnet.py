@@ -302,15 +302,18 @@ class ResNetJob:
         # fixed split-K: the EST's pixels in `sp` pinned splits of >= 2048 (more output tiles in flight),
         # partials folded in split order
         sp = self.splits(cv)
-        Rs, part = Re // sp, ws["wpart"].data_ptr()
+        Rs = Re // sp
+        # one split: the product lands in the EST's gradient slot directly (batch stride P)
+        part, pst = (ws["wpart"].data_ptr(), cv.co * cv.K) if sp > 1 else (gdst, self.P)
         if self.implicit(cv):
             _native.check(L.bt_gemm_conv(1, x.data_ptr(), n * B, cv.hin, cv.hin, cv.ci, cv.hout, cv.hout, cv.k, cv.k,
-                                         cv.s, cv.p, dz.data_ptr(), part, cv.co, n * sp, Rs, cv.co * cv.K, 0, s),
+                                         cv.s, cv.p, dz.data_ptr(), part, cv.co, n * sp, Rs, pst, 0, s),
                           "conv dW (implicit)")
         else:
             _native.check(L.bt_gemm_bf16_ex(dz.data_ptr(), ws[cv.name]["col"].data_ptr(), part, n * sp, cv.co, cv.K,
-                                            Rs, Rs * cv.co, Rs * cv.K, cv.co * cv.K, 0, None, 1, 0, s), "conv dW gemm")
-        _native.check(L.bt_fold_splits(part, n, sp, cv.co * cv.K, gdst, self.P, s), "dW split fold")
+                                            Rs, Rs * cv.co, Rs * cv.K, pst, 0, None, 1, 0, s), "conv dW gemm")
+        if sp > 1:
+            _native.check(L.bt_fold_splits(part, n, sp, cv.co * cv.K, gdst, self.P, s), "dW split fold")
         if dx is None:
             return
         Rin = n * B * cv.hin ** 2
