@@ -256,23 +256,27 @@ __device__ __forceinline__ void conv_load(uint32_t dst, const CUtensorMap* map, 
   tma_load_im2col(dst, map, cb * 64, wo * g.s - g.p, ho * g.s - g.p, n, kw, kh, bar);
 }
 
-template <int BN, int STAGES>
+constexpr int RB_KB = 9;  // resident-weight form (AIM 3): up to 9 k-blocks (K <= 576) of a BN = 64 B operand
+template <int BN, int STAGES, int RB = 0>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int EPI = STAGES * STAGE;           // epilogue staging, EPI_STAGE per epilogue warp
-  static constexpr int BAR = EPI + EPI_WARPS * EPI_STAGE;  // full[S], empty[S], tfull[2], tempty[2], tmem addr
-  static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
+  static constexpr int STAGE = A_BYTES + (RB ? 0 : B_BYTES);  // RB: only A streams through the stages
+  static constexpr int RES = STAGES * STAGE;                  // resident B: RB k-blocks
+  static constexpr int EPI = RES + RB * B_BYTES;              // epilogue staging, EPI_STAGE per epilogue warp
+  static constexpr int BAR = EPI + EPI_WARPS * EPI_STAGE;     // full[S], empty[S], tfull[2], tempty[2], bres, tmem addr
+  static constexpr int TOTAL = BAR + (2 * STAGES + 5) * 8 + 16;
 };
 
 // AIM: 0 = tiled operands; 1 = A is im2col(x) (forward convolution, K-major); 2 = B is im2col(x)
-// (weight gradient dW = dz^T im2col(x), MN-major, K = output pixels of one batch entry)
+// (weight gradient dW = dz^T im2col(x), MN-major, K = output pixels of one batch entry); 3 = AIM 1 with
+// the whole B operand (N <= 64, K <= 576: the filter) loaded once per CTA and kept resident in shared
+// memory, so only the im2col A tiles stream (the same UMMAs in the same order: the same bits)
 template <int BN, int STAGES, bool OUT_BF16, bool MN, int AIM = 0>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2, int M,
                         int N, int K, int batch, const GemmEpi epi, const ConvGeom cg) {
-  using L = Smem<BN, STAGES>;
+  using L = Smem<BN, STAGES, AIM == 3 ? RB_KB : 0>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SW128 tiles need 1024-byte alignment
@@ -282,7 +286,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   auto empty = [&](int s) { return bar0 + 8u * (STAGES + s); };
   auto tfull = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
   auto tempty = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
-  uint32_t* const tmem_slot = (uint32_t*)(gbase + L::BAR + (2 * STAGES + 4) * 8);
+  const uint32_t bres = bar0 + 8u * (2 * STAGES + 4);  // AIM 3: the resident B operand landed
+  uint32_t* const tmem_slot = (uint32_t*)(gbase + L::BAR + (2 * STAGES + 5) * 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN, kb_n = (K + BK - 1) / BK;  // TMA zero-fills / clips edges
@@ -303,6 +308,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(tfull(a), 1);
       mbar_init(tempty(a), EPI_WARPS);  // one arrival per epilogue warp
     }
+    mbar_init(bres, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {  // 2 x BN fp32 accumulator columns (power of two >= 32)
@@ -321,6 +327,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      if constexpr (AIM == 3) {  // the filter, once (one N tile, batch 1)
+        mbar_arrive_expect_tx(bres, kb_n * L::B_BYTES);
+        for (int kb = 0; kb < kb_n; ++kb) tma_load_3d(base + L::RES + kb * L::B_BYTES, &map_b, kb * BK, 0, 0, bres);
+      }
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         int m0, n0;
         tile_coords(t, mt, nt, &m0, &n0);
@@ -328,7 +338,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(empty(stage), phase ^ 1u);
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
           mbar_arrive_expect_tx(full(stage), L::STAGE);
-          if constexpr (AIM == 1) {  // 128 output pixels x (tap, 64 channels); weights K-major
+          if constexpr (AIM == 3) {
+            const int tap = kb / cg.cblocks;
+            conv_load(sa, &map_a, cg, m0, tap, kb - tap * cg.cblocks, full(stage));
+          } else if constexpr (AIM == 1) {  // 128 output pixels x (tap, 64 channels); weights K-major
             const int tap = kb / cg.cblocks;
             conv_load(sa, &map_a, cg, m0, tap, kb - tap * cg.cblocks, full(stage));
             tma_load_3d(sb, &map_b, kb * BK, n0, t / per_batch, full(stage));
@@ -367,6 +380,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
+      if constexpr (AIM == 3) mbar_wait(bres, 0);
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
         const int acc = i & 1;
         mbar_wait(tempty(acc), ((i >> 1) & 1) ^ 1u);  // the epilogue drained this accumulator
@@ -375,7 +389,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kb = 0; kb < kb_n; ++kb) {
           mbar_wait(full(stage), phase);
           tc_fence_after();
-          const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
+          const uint32_t sa = base + stage * L::STAGE;
+          const uint32_t sb = AIM == 3 ? base + L::RES + kb * L::B_BYTES : sa + L::A_BYTES;
           const uint64_t da = op_desc<MN>(sa), db = op_desc<MN>(sb);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)  // K-major: +32 B inside the swizzled row; MN-major: +2 k groups
@@ -746,7 +761,7 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
   const int M = g.M, N = g.N, K = g.K;
   CUtensorMap ma, mb, mc, mc2;
   bool in_ok;
-  if (AIM == 1)
+  if (AIM == 1 || AIM == 3)
     in_ok = make_im2col_map(&ma, g.a, g.xN, g.xH, g.xW, g.xC, g.cg, gemm::BM) &&
             make_map(&mb, g.b, N, K, BN, g.batch, g.sb);
   else if (AIM == 2)
@@ -759,7 +774,7 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
       !make_store_map(&mc2, g.epi.out2 ? (const void*)g.epi.out2 : g.c, M, N, g.batch, g.sc, OUT_BF16))
     return ERR_CUDA;
   auto kern = gemm::gemm_bf16_tn_kernel<BN, STAGES, OUT_BF16, MN, AIM>;
-  const int smem = gemm::Smem<BN, STAGES>::TOTAL + 1024;
+  const int smem = gemm::Smem<BN, STAGES, AIM == 3 ? gemm::RB_KB : 0>::TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -876,6 +891,9 @@ int gemm_conv_launch(int wgrad, const void* x, int xN, int xH, int xW, int Ci, i
     g.sb = (int64_t)Co * K;
     g.sc = (int64_t)g.M * Co;
     g.aim = 1;
+    constexpr int SRB = gemm::EPI_WARPS == 8 ? 5 : 7;  // A-only stages beside the 72 KB resident filter
+    if (Co <= 64 && K <= 64 * gemm::RB_KB && getenv("BT_CONV_RB0") == nullptr)
+      return out_bf16 ? launch_gemm<64, SRB, true, false, 3>(g, 0, s) : launch_gemm<64, SRB, false, false, 3>(g, 0, s);
     if (Co <= 64)
       return out_bf16 ? launch_gemm<64, S64, true, false, 1>(g, 0, s) : launch_gemm<64, S64, false, false, 1>(g, 0, s);
     return out_bf16 ? launch_gemm<128, S128, true, false, 1>(g, 0, s) : launch_gemm<128, S128, false, false, 1>(g, 0, s);
