@@ -25,9 +25,10 @@ BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --set full --clock-control no
   -f -o $O/prof_bert_attn_$tag python tools/bert_bench.py 32 1 1 8 > $O/ncu_bert_attn.out 2>&1; echo bert_attn_rc=$?
 BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ln_bwd -c 1 \
   -f -o $O/prof_bert_ln_$tag python tools/bert_bench.py 32 1 1 8 > $O/ncu_bert_ln.out 2>&1; echo bert_ln_rc=$?
-# C3 (ResNet-18 per-EST BN step): launch list of one step, ncu of the BN statistics kernel and im2col
+# C3 (ResNet-18 per-EST BN step): launch list of one step, ncu of the layer-1 convolution
 BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 400 \
   --csv --log-file $O/resnet_launches.csv python tools/resnet_bench.py > $O/ncu_resnet_list.out 2>&1; echo resnet_list_rc=$?
-BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:im2col -s 1 -c 1 \
-  -f -o $O/prof_resnet_im2col_$tag python tools/resnet_bench.py > $O/ncu_resnet_im2col.out 2>&1; echo resnet_im2col_rc=$?
+# the layer-1 3x3 convolution (2nd GEMM launch of the first step: implicit GEMM, resident filter)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16_tn_kernel -s 1 -c 1 \
+  -f -o $O/prof_resnet_conv_$tag python tools/resnet_prof.py 16 32 1 > $O/ncu_resnet_conv.out 2>&1; echo resnet_conv_rc=$?
 cat $O/bench.json; tail -3 $O/bench.err

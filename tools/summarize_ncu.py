@@ -92,7 +92,7 @@ PROF.mkdir(exist_ok=True)
 launches()
 launches("bert_launches.csv", "bert_launches")
 launches("resnet_launches.csv", "resnet_launches")
-t_ri = summarize(OUT / f"prof_resnet_im2col_{tag}.ncu-rep", "ncu_resnet_im2col")
+t_ri = summarize(OUT / f"prof_resnet_conv_{tag}.ncu-rep", "ncu_resnet_conv", extra=("pipe_tensor", "pipe_tc", "tma"))
 t_bg = summarize(OUT / f"prof_bert_gemm_{tag}.ncu-rep", "ncu_bert_gemm", extra=("pipe_tensor", "pipe_tc", "tmem", "utc"))
 t_ba = summarize(OUT / f"prof_bert_attn_{tag}.ncu-rep", "ncu_bert_attn_bwd", extra=("pipe_tensor", "pipe_tc"))
 t_bl = summarize(OUT / f"prof_bert_ln_{tag}.ncu-rep", "ncu_bert_ln_bwd")
@@ -102,7 +102,7 @@ t_gemm = summarize(OUT / f"prof_gemm_{tag}.ncu-rep", "ncu_gemm", extra=("pipe_te
 traffic = {"mlp_step_kernel": t_mlp[0] if t_mlp else None, "reduce_fast_kernel": t_red[0] if t_red else None,
            "gemm_bf16_tn_kernel": t_gemm[0] if t_gemm else None,
            "bert_ffn_gemm": t_bg[0] if t_bg else None, "attn_bwd_kernel": t_ba[0] if t_ba else None,
-           "ln_bwd_kernel": t_bl[0] if t_bl else None, "im2col_kernel": t_ri[0] if t_ri else None,
+           "ln_bwd_kernel": t_bl[0] if t_bl else None, "resnet_conv_layer1": t_ri[0] if t_ri else None,
            "source": f"profiles/{tag}_ncu_*.txt (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"}
 (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
 print(json.dumps(traffic))
