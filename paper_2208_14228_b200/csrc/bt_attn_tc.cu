@@ -161,16 +161,20 @@ __global__ void __launch_bounds__(THREADS, 4)
   const uint32_t thr = a.p > 0.f ? (uint32_t)ceil((double)a.p * 65536.0) : 0u;
   const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
   const int hi = (tid >> 3) & 1;                       // rows i, i^8 share draws (lanes l, l^8)
+  auto load_item = [&](int it) {  // Q, K, V of item `it` (thread 0)
+    const int s = it / a.H, h = it - (it / a.H) * a.H;
+    mbar_arrive_expect_tx(bar_ld, 3 * 16384);
+    tma_load_3d(base + OFF_Q, &mqk, h * HD, s * SEQ, 0, bar_ld);
+    tma_load_3d(base + OFF_K, &mqk, a.Dm + h * HD, s * SEQ, 0, bar_ld);
+    tma_load_3d(base + OFF_V, &mv, 2 * a.Dm + h * HD, s * SEQ, 0, bar_ld);
+    tma_load_3d(base + OFF_V + 8192, &mv, 2 * a.Dm + h * HD, s * SEQ + 64, 0, bar_ld);
+  };
+  if (tid == 0 && (int)blockIdx.x < a.n_items) load_item(blockIdx.x);
   int n = 0;
   for (int it = blockIdx.x; it < a.n_items; it += gridDim.x, ++n) {
     const int s = it / a.H, h = it - (it / a.H) * a.H;
     const uint32_t ph = n & 1;
     if (tid == 0) {
-      mbar_arrive_expect_tx(bar_ld, 3 * 16384);
-      tma_load_3d(base + OFF_Q, &mqk, h * HD, s * SEQ, 0, bar_ld);
-      tma_load_3d(base + OFF_K, &mqk, a.Dm + h * HD, s * SEQ, 0, bar_ld);
-      tma_load_3d(base + OFF_V, &mv, 2 * a.Dm + h * HD, s * SEQ, 0, bar_ld);
-      tma_load_3d(base + OFF_V + 8192, &mv, 2 * a.Dm + h * HD, s * SEQ + 64, 0, bar_ld);
       mbar_wait(bar_ld, ph);
       tc_fence_after();
       constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
@@ -235,6 +239,9 @@ __global__ void __launch_bounds__(THREADS, 4)
     }
     mbar_wait(bar_o, ph);
     tc_fence_after();
+    // the O product has consumed P and V: the shared tiles are free, so the next item's loads overlap
+    // this item's output drain
+    if (tid == 0 && it + (int)gridDim.x < a.n_items) load_item(it + gridDim.x);
     uint4* const orow = (uint4*)(a.out + ((size_t)s * SEQ + tid) * a.Dm + h * HD);
 #pragma unroll
     for (int c = 0; c < HD / 32; ++c) {
@@ -345,16 +352,29 @@ __global__ void __launch_bounds__(B_THREADS, 2)
   const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
   const int hi = (row >> 3) & 1;  // rows i, i^8 (lanes l, l^8 of one warp) share draws
   const int ld = 3 * a.Dm;
+  // the next item's Q, K, V load as soon as the dQ / dK products have consumed this item's (bar_a), its
+  // dO once dV has (bar_v): one expect_tx of all four tiles per item (thread 0)
+  auto load_qkv = [&](int it) {
+    const int s = it / a.H, h = it - (it / a.H) * a.H;
+    mbar_arrive_expect_tx(bar_ld, 4 * 16384);
+    tma_load_3d(base + B_OFF_Q, &mqk, h * HD, s * SEQ, 0, bar_ld);
+    tma_load_3d(base + B_OFF_K, &mqk, a.Dm + h * HD, s * SEQ, 0, bar_ld);
+    tma_load_3d(base + B_OFF_V, &mqk, 2 * a.Dm + h * HD, s * SEQ, 0, bar_ld);
+  };
+  auto load_do = [&](int it) {
+    const int s = it / a.H, h = it - (it / a.H) * a.H;
+    tma_load_3d(base + B_OFF_DO, &mdo, h * HD, s * SEQ, 0, bar_ld);
+  };
+  if (tid == 0 && (int)blockIdx.x < a.n_items) {
+    load_qkv(blockIdx.x);
+    load_do(blockIdx.x);
+  }
   int n = 0;
   for (int it = blockIdx.x; it < a.n_items; it += gridDim.x, ++n) {
     const int s = it / a.H, h = it - (it / a.H) * a.H;
     const uint32_t ph = n & 1;
+    const bool more = it + (int)gridDim.x < a.n_items;
     if (tid == 0) {
-      mbar_arrive_expect_tx(bar_ld, 4 * 16384);
-      tma_load_3d(base + B_OFF_Q, &mqk, h * HD, s * SEQ, 0, bar_ld);
-      tma_load_3d(base + B_OFF_K, &mqk, a.Dm + h * HD, s * SEQ, 0, bar_ld);
-      tma_load_3d(base + B_OFF_V, &mqk, 2 * a.Dm + h * HD, s * SEQ, 0, bar_ld);
-      tma_load_3d(base + B_OFF_DO, &mdo, h * HD, s * SEQ, 0, bar_ld);
       mbar_wait(bar_ld, ph);
       tc_fence_after();
       constexpr uint32_t id128 = idesc_bf16(128, 128, false, false);
@@ -459,6 +479,7 @@ __global__ void __launch_bounds__(B_THREADS, 2)
     }
     mbar_wait(bar_a, ph);  // dS consumed: Pd takes its place
     tc_fence_after();
+    if (tid == 0 && more) load_qkv(it + gridDim.x);
 #pragma unroll
     for (int c2 = 0; c2 < 2; ++c2) {
 #pragma unroll
@@ -485,6 +506,7 @@ __global__ void __launch_bounds__(B_THREADS, 2)
     store_row32(out + a.Dm, lane_base + 64 + hf * 32);   // dk (key row)
     mbar_wait(bar_v, ph);
     tc_fence_after();
+    if (tid == 0 && more) load_do(it + gridDim.x);
     store_row32(out + 2 * a.Dm, lane_base + 128 + hf * 32);  // dv (key row)
     tc_fence_before();
     __syncthreads();  // TMEM, the shared tiles and the exchange slots are free for the next item
