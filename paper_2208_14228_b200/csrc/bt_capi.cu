@@ -725,7 +725,8 @@ int bt_cnn_bn_stats(int32_t mode, const void* z_dev, const void* dy_dev, const v
                     float* rstd_dev, float* sg_dev, float* sgx_dev, float* part_dev, float* run_mean_dev,
                     float* run_var_dev, int64_t run_stride, float* dgamma_dev, float* dbeta_dev, int64_t grad_stride,
                     int32_t E, int32_t R, int32_t C, float eps, void* stream) {
-  if ((mode != 0 && mode != 2) || E < 1 || R < 2 || !(C == 8 || C == 16 || C == 32 || C % 64 == 0) || C > 2048 || !z_dev || !mean_dev || !part_dev)
+  if ((mode != 0 && mode != 2) || E < 1 || R < 2 || !(C == 8 || C == 16 || C == 32 || C % 64 == 0) || C > 2048 ||
+      !z_dev || !mean_dev || !part_dev)
     return fail(bt::ERR_INPUT, "bt_cnn_bn_stats arguments (mode 0 or 2; C in {8, 16, 32} or a multiple of 64)");
   if (mode == 0 && (!rstd_dev || !run_mean_dev || !run_var_dev)) return fail(bt::ERR_INPUT, "mode 0 needs rstd/run");
   if (mode == 2 && (!dy_dev || !y_dev || !rstd_dev || !sg_dev || !sgx_dev || !dgamma_dev || !dbeta_dev))

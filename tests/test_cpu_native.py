@@ -140,3 +140,27 @@ def test_rotation_table_matches_oracle(oracle):
         bm = bt.BucketMap(c["capacity"], tuple(tuple(b) for b in c["buckets"]))
         nrep = len(c["replicas"])
         assert rotation_table(bm, nrep).tolist() == oracle.rotation_table(c["buckets"], nrep, bm.param_count).tolist()
+
+
+def test_model_stack_entry_points_validate_before_the_device():
+    """The C3/C4 entry points reject malformed shapes with InputError (status 1) before any device call,
+    so the checks run here without a GPU (the pointers are never dereferenced)."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.errors import InputError
+
+    L = _native.lib()
+    P, Q = 0x10000, 0x20000  # 16-byte aligned, never touched
+    cases = [
+        ("bt_gemm_conv", L.bt_gemm_conv(0, P, 1, 8, 8, 24, 8, 8, 3, 3, 1, 1, Q, P, 64, 1, 0, 0, 1, None)),  # Ci % 64
+        ("bt_gemm_conv", L.bt_gemm_conv(1, P, 2, 8, 8, 64, 8, 8, 3, 3, 1, 1, Q, P, 64, 2, 100, 64 * 576, 0, None)),
+        ("bt_cnn_upsample", L.bt_cnn_upsample(P, 1, 4, 4, 24, 2, Q, None)),  # C not a power of two
+        ("bt_cnn_upsample", L.bt_cnn_upsample(P, 1, 4, 4, 64, 3, Q, None)),  # stride 3
+        ("bt_cnn_bn_stats", L.bt_cnn_bn_stats(0, P, None, None, Q, Q, None, None, P, None, None, 0, None, None, 0,
+                                              1, 64, 96, 1e-5, None)),  # C = 96
+        ("bt_cnn_bn_apply", L.bt_cnn_bn_apply(P, None, Q, Q, Q + 4, Q, 1, 64, 64, 1, P, None)),  # misaligned gamma
+        ("bt_fold_splits", L.bt_fold_splits(P, 1, 2, 6, Q, 6, None)),  # n % 4
+    ]
+    for name, status in cases:
+        assert status == 1, (name, status)
+        with pytest.raises(InputError):
+            _native.check(status, name)
