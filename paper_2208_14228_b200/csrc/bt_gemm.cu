@@ -655,6 +655,156 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Halo form of the 3x3 / stride-1 / pad-1 convolution with 64 input channels and the filter resident
+// (Co <= 64): a 128-pixel tile is 128/W whole output rows of one image, and every tap's A operand is a
+// 128-row view of one of three halo boxes {64 ch, W px starting at kw-1, 128/W+2 rows starting at
+// ho0-1} (TMA zero-fills the padding).  The kh taps are the views at row offsets kh*W (multiples of
+// 1024 bytes, so the SW128 pattern is unchanged): 3 boxes per tile instead of 9 im2col boxes, while
+// the UMMAs are exactly the im2col path's (tap order (kh, kw), the same rows, the same filter blocks):
+// the same bits.  Two tiles of halo boxes in flight; the epilogue stores rows straight from registers
+// (no staging), which is what leaves room for the resident filter.
+constexpr int HALO_THREADS = 64 + 256;
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
+  return *(const uint32_t*)&b2;
+}
+template <int W>
+struct HaloSmem {
+  static constexpr int ROWS = BM / W + 2;                       // halo rows per box
+  static constexpr int BOX = ROWS * W * 128;                    // one kw box (64 channels x 2 bytes per pixel)
+  static constexpr int SLOT = 3 * BOX;                          // one tile's three boxes
+  static constexpr int RES = 2 * SLOT;                          // the resident filter: 9 k-blocks x 64 x 64
+  static constexpr int BAR = RES + 9 * 8192;                    // afull[2], aempty[2], bres, tfull[2], tempty[2]
+  static constexpr int TOTAL = BAR + 9 * 8 + 16;
+};
+__device__ __forceinline__ void tma_load_4d_tile(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                                 uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+template <int W, bool OUT_BF16>
+__global__ void __launch_bounds__(HALO_THREADS, 1)
+    conv_halo_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                     void* __restrict__ out, int M, int Co, int H) {
+  using L = HaloSmem<W>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw), base = (raw + 1023u) & ~1023u;
+  uint8_t* const gbase = smem_raw + (base - raw);
+  const uint32_t bar0 = base + L::BAR;
+  auto afull = [&](int i) { return bar0 + 8u * i; };
+  auto aempty = [&](int i) { return bar0 + 8u * (2 + i); };
+  const uint32_t bres = bar0 + 32u;
+  auto tfull = [&](int i) { return bar0 + 8u * (5 + i); };
+  auto tempty = [&](int i) { return bar0 + 8u * (7 + i); };
+  uint32_t* const tmem_slot = (uint32_t*)(gbase + L::BAR + 9 * 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles = (M + BM - 1) / BM, tpi = (H * W) / BM;  // tiles per image
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(afull(i), 1);
+      mbar_init(aempty(i), 1);
+      mbar_init(tfull(i), 1);
+      mbar_init(tempty(i), 8);  // one arrival per epilogue warp
+    }
+    mbar_init(bres, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)), "r"(128)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer: the filter once, then three halo boxes per tile
+      mbar_arrive_expect_tx(bres, 9 * 8192);
+      for (int kb = 0; kb < 9; ++kb) tma_load_3d(base + L::RES + kb * 8192, &map_w, kb * BK, 0, 0, bres);
+      int i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int sl = i & 1;
+        mbar_wait(aempty(sl), ((i >> 1) & 1) ^ 1u);
+        const int n = t / tpi, ho0 = (t - n * tpi) * (BM / W);
+        mbar_arrive_expect_tx(afull(sl), L::SLOT);
+        for (int kw = 0; kw < 3; ++kw)
+          tma_load_4d_tile(base + sl * L::SLOT + kw * L::BOX, &map_x, 0, kw - 1, ho0 - 1, n, afull(sl));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer: the im2col path's UMMA sequence, A from the halo views
+      constexpr uint32_t idesc = idesc_bf16(BM, 64, false, false);
+      mbar_wait(bres, 0);
+      int i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int sl = i & 1, acc = i & 1;
+        mbar_wait(tempty(acc), ((i >> 1) & 1) ^ 1u);
+        mbar_wait(afull(sl), (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(acc * 64);
+        for (int kb = 0; kb < 9; ++kb) {
+          const int kh = kb / 3, kw = kb - kh * 3;
+          const uint64_t da = kmajor_sw128_desc(base + sl * L::SLOT + kw * L::BOX + kh * W * 128);
+          const uint64_t db = kmajor_sw128_desc(base + L::RES + kb * 8192);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k) tc_mma(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+        }
+        tc_commit(aempty(sl));
+        tc_commit(tfull(acc));
+      }
+    }
+  } else {  // ---- epilogue: 8 warps = 4 TMEM lane groups x 2 column halves; rows stored from registers
+    const int lg = warp & 3, half = (warp - 2) >> 2;  // a warp may only read TMEM lanes 32*(warp % 4)..
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int acc = i & 1;
+      mbar_wait(tfull(acc), (i >> 1) & 1);
+      tc_fence_after();
+      const int row = t * BM + lg * 32 + lane, c0 = half * 32;
+      uint32_t v[32];
+      tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 64 + c0), v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty(acc));
+      if (row < M && c0 < Co) {
+        if constexpr (OUT_BF16) {
+          uint4* o = (uint4*)((__nv_bfloat16*)out + (size_t)row * Co + c0);
+          const int nq = min(4, (Co - c0) / 8);
+          for (int q = 0; q < nq; ++q) {
+            uint4 u;
+            u.x = pack_bf16(__uint_as_float(v[8 * q]), __uint_as_float(v[8 * q + 1]));
+            u.y = pack_bf16(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
+            u.z = pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
+            u.w = pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+            o[q] = u;
+          }
+        } else {
+          float4* o = (float4*)((float*)out + (size_t)row * Co + c0);
+          const int nq = min(8, (Co - c0) / 4);
+          for (int q = 0; q < nq; ++q)
+            o[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                               __uint_as_float(v[4 * q + 3]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
+  }
+}
+
 }  // namespace gemm
 
 // ---------------------------------------------------------------- launcher
@@ -742,6 +892,37 @@ static bool make_im2col_map(CUtensorMap* map, const void* x, int N, int H, int W
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper, 64,
              (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the halo form's activation map: [N][H][W][64] bf16, box {64, W, 128/W + 2, 1}, SW128, zero fill
+static bool make_halo_map(CUtensorMap* map, const void* x, int N, int H, int W) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 128};
+  const cuuint32_t box[4] = {64, (cuuint32_t)W, (cuuint32_t)(gemm::BM / W + 2), 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <int W, bool OUT_BF16>
+static int launch_conv_halo(const void* x, int N, int H, const void* w, void* c, int Co, cudaStream_t s) {
+  CUtensorMap mx, mw;
+  if (!make_halo_map(&mx, x, N, H, W) || !make_map(&mw, w, Co, 9 * 64, 64, 1, (int64_t)Co * 9 * 64)) return ERR_CUDA;
+  auto kern = gemm::conv_halo_kernel<W, OUT_BF16>;
+  const int smem = gemm::HaloSmem<W>::TOTAL + 1024;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return ERR_CUDA;
+    attr = true;
+  }
+  const int M = N * H * W, tiles = (M + gemm::BM - 1) / gemm::BM;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  kern<<<tiles < sms ? tiles : sms, gemm::HALO_THREADS, smem, s>>>(mx, mw, c, M, Co, H);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
 struct GemmShape {
@@ -891,6 +1072,15 @@ int gemm_conv_launch(int wgrad, const void* x, int xN, int xH, int xW, int Ci, i
     g.sb = (int64_t)Co * K;
     g.sc = (int64_t)g.M * Co;
     g.aim = 1;
+    // 3x3 / stride 1 / pad 1, 64 input channels, Co <= 64, whole-row 128-pixel tiles: the halo form
+    if (Ci == 64 && KH == 3 && KW == 3 && stride == 1 && pad == 1 && Ho == xH && Wo == xW && Co <= 64 &&
+        (Co % 8) == 0 && (xW == 32 || xW == 16) && (xH * xW) % gemm::BM == 0 && getenv("BT_CONV_HALO0") == nullptr) {
+      if (xW == 32)
+        return out_bf16 ? launch_conv_halo<32, true>(x, xN, xH, other, c, Co, s)
+                        : launch_conv_halo<32, false>(x, xN, xH, other, c, Co, s);
+      return out_bf16 ? launch_conv_halo<16, true>(x, xN, xH, other, c, Co, s)
+                      : launch_conv_halo<16, false>(x, xN, xH, other, c, Co, s);
+    }
     constexpr int SRB = gemm::EPI_WARPS == 8 ? 5 : 7;  // A-only stages beside the 72 KB resident filter
     if (Co <= 64 && K <= 64 * gemm::RB_KB && getenv("BT_CONV_RB0") == nullptr)
       return out_bf16 ? launch_gemm<64, SRB, true, false, 3>(g, 0, s) : launch_gemm<64, SRB, false, false, 3>(g, 0, s);

@@ -233,7 +233,7 @@ def test_implicit_gemm_convolutions_equal_explicit_im2col(rn, monkeypatch):
     assert np.array_equal(_bits(a.params), _bits(b.params))
 
 
-@pytest.mark.parametrize("ci,co,k,s,hw", [(64, 64, 3, 1, 8), (64, 128, 3, 2, 8), (128, 256, 1, 2, 8)])
+@pytest.mark.parametrize("ci,co,k,s,hw", [(64, 64, 3, 1, 8), (64, 128, 3, 2, 8), (128, 256, 1, 2, 8), (64, 64, 3, 1, 32)])
 def test_convolution_products_match_float64(rn, ci, co, k, s, hw):
     """The implicit-GEMM convolution (bt_gemm_conv: TMA im2col loads), its weight gradient and the dX
     paths (stride 1: forward convolution of dz with the tap-reversed filter; stride 2: the transposed
@@ -293,6 +293,35 @@ def test_convolution_products_match_float64(rn, ci, co, k, s, hw):
         _native.check(L.bt_gemm_conv(0, up.data_ptr(), N, hw, hw, co, hw, hw, k, k, 1, k - 1 - p, wflip.data_ptr(),
                                      dx2.data_ptr(), ci, 1, 0, 0, 0, stream()))
         _close(dx2, dxref, "conv dX (zero insertion)", 1e-5)
+
+
+@pytest.mark.parametrize("co,hw,out_bf16", [(64, 32, 1), (64, 32, 0), (32, 16, 1), (64, 16, 0)])
+def test_halo_convolution_equals_im2col_path(co, hw, out_bf16, monkeypatch):
+    """The halo form (three row-halo boxes per tile, the kh taps as views) issues the im2col path's
+    UMMAs on the same rows: identical bits, bf16 and fp32 outputs, Co = 64 and Co < 64."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    L = _native.lib()
+    N = 6
+    g = torch.Generator(device="cuda").manual_seed(co + hw)
+    x = torch.randn(N, hw, hw, 64, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(co, 9 * 64, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    dt = torch.bfloat16 if out_bf16 else torch.float32
+    outs = []
+    for halo in (True, False):
+        if halo:
+            monkeypatch.delenv("BT_CONV_HALO0", raising=False)
+        else:
+            monkeypatch.setenv("BT_CONV_HALO0", "1")
+        z = torch.full((N * hw * hw, co), float("nan"), device="cuda", dtype=dt)
+        _native.check(L.bt_gemm_conv(0, x.data_ptr(), N, hw, hw, 64, hw, hw, 3, 3, 1, 1, w.data_ptr(), z.data_ptr(),
+                                     co, 1, 0, 0, out_bf16, stream()))
+        outs.append(z)
+    torch.cuda.synchronize()
+    assert not torch.isnan(outs[0]).any()
+    assert torch.equal(outs[0].view(torch.int16 if out_bf16 else torch.int32),
+                       outs[1].view(torch.int16 if out_bf16 else torch.int32))
 
 
 def test_cuda_graph_replay_equals_eager_across_rescale(rn):
