@@ -28,7 +28,7 @@ BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --set full --clock-control no
 # C3 (ResNet-18 per-EST BN step): launch list of one step, ncu of the layer-1 convolution
 BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 400 \
   --csv --log-file $O/resnet_launches.csv python tools/resnet_bench.py > $O/ncu_resnet_list.out 2>&1; echo resnet_list_rc=$?
-# the layer-1 3x3 convolution (2nd GEMM launch of the first step: implicit GEMM, resident filter)
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16_tn_kernel -s 1 -c 1 \
+# the layer-1 3x3 convolution (first halo-tile launch of the first step: implicit GEMM, resident filter)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_halo -s 0 -c 1 \
   -f -o $O/prof_resnet_conv_$tag python tools/resnet_prof.py 16 32 1 > $O/ncu_resnet_conv.out 2>&1; echo resnet_conv_rc=$?
 cat $O/bench.json; tail -3 $O/bench.err
