@@ -464,6 +464,18 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
       "l"(map), "r"(x), "r"(y), "r"(z), "r"(leader_bar)
       : "memory");
 }
+__device__ __forceinline__ void conv_load_pair(uint32_t dst, const CUtensorMap* map, const ConvGeom& g, int q, int t,
+                                               int cb, uint32_t leader_bar) {  // conv_load, bytes to the leader
+  const int hw = g.Ho * g.Wo;
+  const int n = q / hw, r = q - n * hw, ho = r / g.Wo, wo = r - ho * g.Wo;
+  const int kh = t / g.KW, kw = t - kh * g.KW;
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+      "l"(map), "r"(cb * 64), "r"(wo * g.s - g.p), "r"(ho * g.s - g.p), "r"(n), "r"(leader_bar), "h"((uint16_t)kw),
+      "h"((uint16_t)kh)
+      : "memory");
+}
 __device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, int acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -498,11 +510,13 @@ struct PairSmem {
   static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
 };
 
-template <int STAGES, bool OUT_BF16, bool MN, int EW = EPI_WARPS>  // EW epilogue warps (16 for ALU-heavy epilogues)
+// EW epilogue warps (16 for ALU-heavy epilogues); AIM 1: A = im2col(x) K-major (the forward convolution);
+// AIM 2: B = im2col(x) MN-major (the weight gradient)
+template <int STAGES, bool OUT_BF16, bool MN, int EW = EPI_WARPS, int AIM = 0>
 __global__ void __launch_bounds__(64 + 32 * EW, 1)
     gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                              const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2,
-                             int M, int N, int K, int batch, const GemmEpi epi) {
+                             int M, int N, int K, int batch, const GemmEpi epi, const ConvGeom cg) {
   using L = PairSmem<STAGES, EW>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
@@ -573,12 +587,26 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             for (int j = 0; j < BM / 64; ++j)
               tma_load_3d_pair(sa + j * MN_BLOCK_BYTES, &map_a, m0 + (int)rank * BM + 64 * j, kb * BK, t / per_batch,
                                lb);
+            if constexpr (AIM == 2) {  // 64-pixel x 64-channel im2col blocks of this CTA's N half
+              const int q = (t / per_batch) * cg.rows_per_batch + kb * BK;
 #pragma unroll
-            for (int j = 0; j < PAIR_BN / 128; ++j)
-              tma_load_3d_pair(sb + j * MN_BLOCK_BYTES, &map_b, n0 + (int)rank * (PAIR_BN / 2) + 64 * j, kb * BK,
-                               t / per_batch, lb);
+              for (int j = 0; j < PAIR_BN / 128; ++j) {
+                const int nb = ((n0 + (int)rank * (PAIR_BN / 2)) >> 6) + j, tap = nb / cg.cblocks;
+                conv_load_pair(sb + j * MN_BLOCK_BYTES, &map_b, cg, q, tap, nb - tap * cg.cblocks, lb);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < PAIR_BN / 128; ++j)
+                tma_load_3d_pair(sb + j * MN_BLOCK_BYTES, &map_b, n0 + (int)rank * (PAIR_BN / 2) + 64 * j, kb * BK,
+                                 t / per_batch, lb);
+            }
           } else {
-            tma_load_3d_pair(sa, &map_a, kb * BK, m0 + (int)rank * BM, t / per_batch, lb);
+            if constexpr (AIM == 1) {  // this CTA's 128 output pixels x (tap, 64 channels)
+              const int tap = kb / cg.cblocks;
+              conv_load_pair(sa, &map_a, cg, m0 + (int)rank * BM, tap, kb - tap * cg.cblocks, lb);
+            } else {
+              tma_load_3d_pair(sa, &map_a, kb * BK, m0 + (int)rank * BM, t / per_batch, lb);
+            }
             tma_load_3d_pair(sb, &map_b, kb * BK, n0 + (int)rank * (PAIR_BN / 2), t / per_batch, lb);
           }
           if (++stage == STAGES) {
@@ -974,18 +1002,23 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
-template <int STAGES, bool OUT_BF16, bool MN, int EW = gemm::EPI_WARPS>
+template <int STAGES, bool OUT_BF16, bool MN, int EW = gemm::EPI_WARPS, int AIM = 0>
 static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
   const int M = g.M, N = g.N, K = g.K;
   CUtensorMap ma, mb, mc, mc2;
-  const bool in_ok = MN ? make_map_mn(&ma, g.a, M, K, g.batch, g.sa) && make_map_mn(&mb, g.b, N, K, g.batch, g.sb)
-                        : make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) &&
-                              make_map(&mb, g.b, N, K, gemm::PAIR_BN / 2, g.batch, g.sb);
+  const bool in_ok =
+      AIM == 1   ? make_im2col_map(&ma, g.a, g.xN, g.xH, g.xW, g.xC, g.cg, gemm::BM) &&
+                     make_map(&mb, g.b, N, K, gemm::PAIR_BN / 2, g.batch, g.sb)
+      : AIM == 2 ? make_map_mn(&ma, g.a, M, K, g.batch, g.sa) &&
+                     make_im2col_map(&mb, g.b, g.xN, g.xH, g.xW, g.xC, g.cg, 64)
+      : MN     ? make_map_mn(&ma, g.a, M, K, g.batch, g.sa) && make_map_mn(&mb, g.b, N, K, g.batch, g.sb)
+               : make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) &&
+                     make_map(&mb, g.b, N, K, gemm::PAIR_BN / 2, g.batch, g.sb);
   if (!in_ok ||
       !make_store_map(&mc, g.c, M, N, g.batch, g.sc, OUT_BF16) ||
       !make_store_map(&mc2, g.epi.out2 ? (const void*)g.epi.out2 : g.c, M, N, g.batch, g.sc, OUT_BF16))
     return ERR_CUDA;
-  auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16, MN, EW>;
+  auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16, MN, EW, AIM>;
   const int smem = gemm::PairSmem<STAGES, EW>::TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
@@ -1015,7 +1048,7 @@ static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
   attr_[0].val.clusterDim.z = 1;
   cfg.attrs = attr_;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mc2, M, N, K, g.batch, g.epi) == cudaSuccess ? OK : ERR_CUDA;
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mc2, M, N, K, g.batch, g.epi, g.cg) == cudaSuccess ? OK : ERR_CUDA;
 }
 
 static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests, measurements)
@@ -1086,6 +1119,11 @@ int gemm_conv_launch(int wgrad, const void* x, int xN, int xH, int xW, int Ci, i
       return out_bf16 ? launch_gemm<64, SRB, true, false, 3>(g, 0, s) : launch_gemm<64, SRB, false, false, 3>(g, 0, s);
     if (Co <= 64)
       return out_bf16 ? launch_gemm<64, S64, true, false, 1>(g, 0, s) : launch_gemm<64, S64, false, false, 1>(g, 0, s);
+    if (Co % gemm::PAIR_BN == 0 && g.M % gemm::PAIR_M == 0 && getenv("BT_CONV_FWD_PAIR0") == nullptr) {
+      constexpr int SP = gemm::EPI_WARPS == 8 ? 5 : 3;
+      return out_bf16 ? launch_gemm_pair<SP, true, false, gemm::EPI_WARPS, 1>(g, 0, s)
+                      : launch_gemm_pair<SP, false, false, gemm::EPI_WARPS, 1>(g, 0, s);
+    }
     return out_bf16 ? launch_gemm<128, S128, true, false, 1>(g, 0, s) : launch_gemm<128, S128, false, false, 1>(g, 0, s);
   }
   g.a = other;  // dz [batch * rows_per_batch][Co]
@@ -1098,6 +1136,12 @@ int gemm_conv_launch(int wgrad, const void* x, int xN, int xH, int xW, int Ci, i
   g.sc = sc;
   g.mn = true;
   g.aim = 2;
+  // whole 256 x 256 CTA-pair tiles (Co, KH*KW*Ci multiples of 256): half the operand bytes per flop
+  if (Co % gemm::PAIR_M == 0 && K % gemm::PAIR_BN == 0 && getenv("BT_CONV_WG_PAIR0") == nullptr) {
+    constexpr int SP = gemm::EPI_WARPS == 8 ? 5 : 3;
+    return out_bf16 ? launch_gemm_pair<SP, true, true, gemm::EPI_WARPS, 2>(g, 0, s)
+                    : launch_gemm_pair<SP, false, true, gemm::EPI_WARPS, 2>(g, 0, s);
+  }
   return out_bf16 ? launch_gemm<128, S128, true, true, 2>(g, 0, s) : launch_gemm<128, S128, false, true, 2>(g, 0, s);
 }
 

@@ -233,7 +233,7 @@ def test_implicit_gemm_convolutions_equal_explicit_im2col(rn, monkeypatch):
     assert np.array_equal(_bits(a.params), _bits(b.params))
 
 
-@pytest.mark.parametrize("ci,co,k,s,hw", [(64, 64, 3, 1, 8), (64, 128, 3, 2, 8), (128, 256, 1, 2, 8), (64, 64, 3, 1, 32)])
+@pytest.mark.parametrize("ci,co,k,s,hw", [(64, 64, 3, 1, 8), (64, 128, 3, 2, 8), (128, 256, 1, 2, 8), (64, 64, 3, 1, 32), (256, 256, 3, 1, 8)])
 def test_convolution_products_match_float64(rn, ci, co, k, s, hw):
     """The implicit-GEMM convolution (bt_gemm_conv: TMA im2col loads), its weight gradient and the dX
     paths (stride 1: forward convolution of dz with the tap-reversed filter; stride 2: the transposed
@@ -322,6 +322,67 @@ def test_halo_convolution_equals_im2col_path(co, hw, out_bf16, monkeypatch):
     assert not torch.isnan(outs[0]).any()
     assert torch.equal(outs[0].view(torch.int16 if out_bf16 else torch.int32),
                        outs[1].view(torch.int16 if out_bf16 else torch.int32))
+
+
+@pytest.mark.parametrize("ci,co,k,s", [(256, 256, 3, 1), (256, 512, 3, 2), (128, 256, 1, 2)])
+def test_weight_gradient_pair_tiles_equal_single_cta(ci, co, k, s, monkeypatch):
+    """The weight gradient on 256 x 256 CTA-pair tiles (im2col B halves loaded by each CTA of the pair)
+    equals the 1-CTA form bit for bit (same per-element K order); shapes that do not tile fall back."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    L = _native.lib()
+    N, hw, p = 8, 8, k // 2
+    ho = (hw + 2 * p - k) // s + 1
+    g = torch.Generator(device="cuda").manual_seed(ci + co)
+    x = torch.randn(N, hw, hw, ci, device="cuda", generator=g).to(torch.bfloat16)
+    dz = torch.randn(N, ho, ho, co, device="cuda", generator=g).to(torch.bfloat16)
+    R = 4 * ho * ho
+    if R % 64:
+        pytest.skip("rows per entry not a multiple of 64")
+    outs = []
+    for pair in (True, False):
+        if pair:
+            monkeypatch.delenv("BT_CONV_WG_PAIR0", raising=False)
+        else:
+            monkeypatch.setenv("BT_CONV_WG_PAIR0", "1")
+        dw = torch.full((2, co, k * k * ci), float("nan"), device="cuda")
+        _native.check(L.bt_gemm_conv(1, x.data_ptr(), N, hw, hw, ci, ho, ho, k, k, s, p, dz.data_ptr(), dw.data_ptr(),
+                                     co, 2, R, co * k * k * ci, 0, stream()))
+        outs.append(dw)
+    torch.cuda.synchronize()
+    assert not torch.isnan(outs[0]).any()
+    assert torch.equal(outs[0].view(torch.int32), outs[1].view(torch.int32))
+
+
+@pytest.mark.parametrize("ci,co,k,s,out_bf16", [(256, 256, 3, 1, 1), (128, 256, 3, 2, 0), (512, 512, 3, 1, 1)])
+def test_forward_convolution_pair_tiles_equal_single_cta(ci, co, k, s, out_bf16, monkeypatch):
+    """The forward implicit convolution on CTA-pair tiles (each CTA loads its 128 pixels' im2col boxes and
+    its half of the filter rows) equals the 1-CTA form bit for bit."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    L = _native.lib()
+    N, hw, p = 16, 8, k // 2
+    ho = (hw + 2 * p - k) // s + 1
+    g = torch.Generator(device="cuda").manual_seed(ci + co + s)
+    x = torch.randn(N, hw, hw, ci, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(co, k * k * ci, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    dt = torch.bfloat16 if out_bf16 else torch.float32
+    outs = []
+    for pair in (True, False):
+        if pair:
+            monkeypatch.delenv("BT_CONV_FWD_PAIR0", raising=False)
+        else:
+            monkeypatch.setenv("BT_CONV_FWD_PAIR0", "1")
+        z = torch.full((N * ho * ho, co), float("nan"), device="cuda", dtype=dt)
+        _native.check(L.bt_gemm_conv(0, x.data_ptr(), N, hw, hw, ci, ho, ho, k, k, s, p, w.data_ptr(), z.data_ptr(),
+                                     co, 1, 0, 0, out_bf16, stream()))
+        outs.append(z)
+    torch.cuda.synchronize()
+    assert not torch.isnan(outs[0]).any()
+    iv = torch.int16 if out_bf16 else torch.int32
+    assert torch.equal(outs[0].view(iv), outs[1].view(iv))
 
 
 def test_cuda_graph_replay_equals_eager_across_rescale(rn):
