@@ -252,6 +252,14 @@ int bt_cnn_add(const void *a_dev, const void *b_dev, const void *y_dev, int64_t 
  * stride-s convolution as a stride-1 convolution of `up` with the flipped filter */
 int bt_cnn_upsample(const void *src_dev, int64_t N, int32_t Hs, int32_t Ws, int32_t C, int32_t s, void *up_dev,
                     void *stream);
+/* stride-2 dX by output parity class (a, b): class filters out[i] [Ci][class_taps[i]][Co] (bf16) =
+ * w[i] [Co][taps[i]][Ci] (fp32) at source taps tap_map[9*i + t], one launch for n <= 16 filters */
+int bt_cnn_filter_taps(const float *const *w_dev, void *const *out_dev, const int32_t *co, const int32_t *taps,
+                       const int32_t *ci, const int32_t *class_taps, const int32_t *tap_map, int32_t n, void *stream);
+/* out [N][2Hs][2Ws][C] = a[2(y%2) + x%2][n][y/2][x/2] + b[...] (4 class pointers each, null = zero; bf16):
+ * the parity classes of a stride-2 dX interleaved back, plus the shortcut's classes */
+int bt_cnn_add_s2(const void *const *a_dev, const void *const *b_dev, void *out_dev, int64_t N, int32_t Hs, int32_t Ws,
+                  int32_t C, void *stream);
 /* avgpool 4x4 + fc 512->10 + softmax cross-entropy, forward and backward, one block per EST */
 int bt_cnn_head(const void *x_dev, const int32_t *labels_dev, const float *w_dev, const float *b_dev, int32_t E,
                 int32_t B, float *dw_dev, float *db_dev, int64_t grad_stride, float *loss_dev, void *dx_dev,

@@ -122,6 +122,8 @@ EXPORTS = {
     "bt_cnn_bn_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
     "bt_cnn_add": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "bt_cnn_upsample": (C.c_int, [_vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "bt_cnn_filter_taps": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "bt_cnn_add_s2": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp]),
     "bt_cnn_head": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp]),
     "bt_fold_splits": (C.c_int, [_vp, _i32, _i32, _i64, _vp, _i64, _vp]),
     "bt_cnn_conv_weights": (C.c_int, [C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _i32p, _i32p, _i32p, _i32p,

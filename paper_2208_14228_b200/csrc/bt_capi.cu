@@ -85,6 +85,10 @@ int cnn_bn_bwd_launch(const void* z, const void* dy, const void* y, const float*
                       cudaStream_t s);
 int cnn_add_launch(const void* a, const void* b, const void* y, int64_t n, void* out, cudaStream_t s);
 int cnn_upsample_launch(const void* src, int64_t N, int Hs, int Ws, int C, int s, void* up, cudaStream_t st);
+int cnn_filter_taps_launch(const float* const* w, void* const* out, const int* Co, const int* T, const int* Ci,
+                           const int* Tc, const int* src, int n, cudaStream_t s);
+int cnn_add_s2_launch(const void* const* a, const void* const* b, void* out, int64_t N, int Hs, int Ws, int C,
+                      cudaStream_t s);
 int cnn_head_launch(const void* x, const int32_t* labels, const float* W, const float* bias, int E, int B, float* dW,
                     float* db, int64_t grad_stride, float* loss, void* dx, cudaStream_t s);
 int cnn_conv_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* Co, const int* T,
@@ -766,6 +770,19 @@ int bt_cnn_upsample(const void* src_dev, int64_t N, int32_t Hs, int32_t Ws, int3
   if (!src_dev || !up_dev || N < 1 || Hs < 1 || Ws < 1) return fail(bt::ERR_INPUT, "bt_cnn_upsample arguments");
   return done(bt::cnn_upsample_launch(src_dev, N, Hs, Ws, C, s, up_dev, STREAM(stream)),
               "bt_cnn_upsample (C a power of two >= 8, s in {1, 2})");
+}
+int bt_cnn_filter_taps(const float* const* w_dev, void* const* out_dev, const int32_t* co, const int32_t* taps,
+                       const int32_t* ci, const int32_t* class_taps, const int32_t* tap_map, int32_t n, void* stream) {
+  if (!w_dev || !out_dev || !co || !taps || !ci || !class_taps || !tap_map || n < 1 || n > 16)
+    return fail(bt::ERR_INPUT, "bt_cnn_filter_taps arguments (1 <= n <= 16)");
+  return done(bt::cnn_filter_taps_launch(w_dev, out_dev, co, taps, ci, class_taps, tap_map, n, STREAM(stream)),
+              "bt_cnn_filter_taps (1 <= class taps <= 9, map entries < taps)");
+}
+int bt_cnn_add_s2(const void* const* a_dev, const void* const* b_dev, void* out_dev, int64_t N, int32_t Hs, int32_t Ws,
+                  int32_t C, void* stream) {
+  if (!out_dev || N < 1 || Hs < 1 || Ws < 1) return fail(bt::ERR_INPUT, "bt_cnn_add_s2 arguments");
+  return done(bt::cnn_add_s2_launch(a_dev, b_dev, out_dev, N, Hs, Ws, C, STREAM(stream)),
+              "bt_cnn_add_s2 (C a power of two >= 8)");
 }
 int bt_cnn_head(const void* x_dev, const int32_t* labels_dev, const float* w_dev, const float* b_dev, int32_t E,
                 int32_t B, float* dw_dev, float* db_dev, int64_t grad_stride, float* loss_dev, void* dx_dev,

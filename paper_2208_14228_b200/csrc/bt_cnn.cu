@@ -87,7 +87,7 @@ struct ColArgs {
 };
 // One warp per output row (its (image, ho, wo) decoded once); lanes walk the row's K8 16-byte
 // chunks -- coalesced stores, contiguous 16-byte reads per tap -- with shift/mask decoding (C/8 a
-// power of two, KW in {1, 3}): the kernel is store-bandwidth-bound rather than integer-bound.
+// power of two, KW <= 3): the kernel is store-bandwidth-bound rather than integer-bound.
 __global__ void __launch_bounds__(256) im2col_kernel(const ColArgs a, int lcg) {
   const int cg = 1 << lcg, K8 = a.KH * a.KW * cg;
   const int rows = a.N * a.Ho * a.Wo, HoWo = a.Ho * a.Wo;
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) im2col_kernel(const ColArgs a, int lcg) {
     uint4* dst = (uint4*)(a.col + (size_t)r * K8 * 8);
     for (int k8 = lane; k8 < K8; k8 += 32) {
       const int t = k8 >> lcg, c8 = k8 & (cg - 1);
-      const int kh = a.KW == 3 ? (t * 11) >> 5 : t, kw = t - kh * a.KW;  // t / 3 for t < 9
+      const int kh = a.KW == 3 ? (t * 11) >> 5 : (a.KW == 2 ? t >> 1 : t), kw = t - kh * a.KW;  // t / 3 for t < 9
       int hi, wi;
       bool ok;
       if (!a.transposed) {
@@ -340,6 +340,58 @@ __global__ void __launch_bounds__(256) add_kernel(const __nv_bfloat16* __restric
   }
 }
 
+// ---------------------------------------------------------------- stride-2 dX by parity class
+// The dX of a stride-2 convolution splits by output parity (a, b) = (y % 2, x % 2): only the taps with
+// (a + p - kh) and (b + p - kw) even reach class (a, b), each a stride-1 convolution of dz at row /
+// column offsets (a + p - kh) / 2 -- no zero products.  filter_taps_kernel builds a class filter
+// [Ci][Tc][Co] (bf16) from the master [Co][T][Ci] (fp32) through a tap map; add_s2_kernel interleaves
+// the classes back into the [N][2Hs][2Ws][C] gradient while adding the shortcut's classes.
+struct TapMap {
+  const float* w;
+  __nv_bfloat16* out;
+  int Co, T, Ci, Tc;
+  int src[9];  // source tap of class tap tc
+};
+struct TapTable {
+  TapMap m[16];
+  int n;
+};
+__global__ void filter_taps_kernel(const __grid_constant__ TapTable tab) {
+  const TapMap& m = tab.m[blockIdx.y];
+  const int64_t n = (int64_t)m.Ci * m.Tc * m.Co;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int co = (int)(i % m.Co);
+    const int64_t r = i / m.Co;
+    const int tc = (int)(r % m.Tc), ci = (int)(r / m.Tc);
+    m.out[i] = __float2bfloat16_rn(m.w[((size_t)co * m.T + m.src[tc]) * m.Ci + ci]);
+  }
+}
+struct S2Args {
+  const __nv_bfloat16* a[4];  // class (y%2, x%2) = 2a+b of the first gradient, [N][Hs][Ws][C] (null: zero)
+  const __nv_bfloat16* b[4];  // the same for the second (the shortcut's dX), null: zero
+  __nv_bfloat16* out;         // [N][2Hs][2Ws][C]
+  int64_t N;
+  int Hs, Ws, lc8;
+};
+__global__ void __launch_bounds__(256) add_s2_kernel(const __grid_constant__ S2Args g) {
+  const int Ho = 2 * g.Hs, Wo = 2 * g.Ws;
+  const int64_t n = (g.N * Ho * Wo) << g.lc8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pix = i >> g.lc8;
+    const int c8 = (int)(i & ((1 << g.lc8) - 1));
+    const int64_t img = pix / (Ho * Wo);
+    const int r = (int)(pix - img * Ho * Wo), y = r / Wo, x = r - y * Wo;
+    const int cls = (y & 1) * 2 + (x & 1);
+    const size_t src = ((((size_t)img * g.Hs + (y >> 1)) * g.Ws + (x >> 1)) << g.lc8) * 8 + c8 * 8;
+    float va[8] = {0, 0, 0, 0, 0, 0, 0, 0}, vb[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o[8];
+    if (g.a[cls]) ld8(g.a[cls] + src, va);
+    if (g.b[cls]) ld8(g.b[cls] + src, vb);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = va[q] + vb[q];
+    st8(g.out + i * 8, o);
+  }
+}
+
 // ---------------------------------------------------------------- zero insertion
 // up[n][y][x][c] = src[n][y/s][x/s][c] when y and x are multiples of s, else 0 ([N][s*Hs][s*Ws][C]):
 // the dX of a stride-s convolution becomes a stride-1 convolution of `up` with the flipped filter
@@ -513,7 +565,7 @@ int cnn_im2col_launch(const void* src, void* col, int N, int Hs, int Ws, int C, 
                       int stride, int pad, int transposed, cudaStream_t s) {
   if (C % 8) return ERR_INPUT;
   const int cg = C / 8;
-  if ((int64_t)N * Ho * Wo >= (int64_t)1 << 31 || (cg & (cg - 1)) || (KW != 1 && KW != 3) || KH > 3 ||
+  if ((int64_t)N * Ho * Wo >= (int64_t)1 << 31 || (cg & (cg - 1)) || KW > 3 || KH > 3 ||
       (stride != 1 && stride != 2))
     return ERR_INPUT;
   int lcg = 0;
@@ -582,6 +634,52 @@ int cnn_add_launch(const void* a, const void* b, const void* y, int64_t n, void*
   if (n % 8) return ERR_INPUT;
   cnn::add_kernel<<<grid_n(n / 8), 256, 0, s>>>((const __nv_bfloat16*)a, (const __nv_bfloat16*)b,
                                                 (const __nv_bfloat16*)y, n / 8, (__nv_bfloat16*)out);
+  return ok_or_cuda_c();
+}
+
+int cnn_filter_taps_launch(const float* const* w, void* const* out, const int* Co, const int* T, const int* Ci,
+                           const int* Tc, const int* src, int n, cudaStream_t s) {
+  if (n < 1 || n > 16) return ERR_INPUT;
+  cnn::TapTable tab{};
+  int64_t mx = 0;
+  for (int i = 0; i < n; ++i) {
+    if (Tc[i] < 1 || Tc[i] > 9) return ERR_INPUT;
+    cnn::TapMap& m = tab.m[i];
+    m.w = w[i];
+    m.out = (__nv_bfloat16*)out[i];
+    m.Co = Co[i];
+    m.T = T[i];
+    m.Ci = Ci[i];
+    m.Tc = Tc[i];
+    for (int t = 0; t < Tc[i]; ++t) {
+      if (src[i * 9 + t] < 0 || src[i * 9 + t] >= T[i]) return ERR_INPUT;
+      m.src[t] = src[i * 9 + t];
+    }
+    const int64_t sz = (int64_t)Co[i] * Tc[i] * Ci[i];
+    mx = sz > mx ? sz : mx;
+  }
+  tab.n = n;
+  const int gx = (int)((mx + 255) / 256 < 1024 ? (mx + 255) / 256 : 1024);
+  cnn::filter_taps_kernel<<<dim3(gx, n), 256, 0, s>>>(tab);
+  return ok_or_cuda_c();
+}
+
+int cnn_add_s2_launch(const void* const* a, const void* const* b, void* out, int64_t N, int Hs, int Ws, int C,
+                      cudaStream_t s) {
+  int lc8 = 0;
+  while ((8 << lc8) < C) ++lc8;
+  if ((8 << lc8) != C) return ERR_INPUT;
+  cnn::S2Args g{};
+  for (int k = 0; k < 4; ++k) {
+    g.a[k] = a ? (const __nv_bfloat16*)a[k] : nullptr;
+    g.b[k] = b ? (const __nv_bfloat16*)b[k] : nullptr;
+  }
+  g.out = (__nv_bfloat16*)out;
+  g.N = N;
+  g.Hs = Hs;
+  g.Ws = Ws;
+  g.lc8 = lc8;
+  cnn::add_s2_kernel<<<grid_n(N * 4 * Hs * Ws * (C / 8)), 256, 0, s>>>(g);
   return ok_or_cuda_c();
 }
 

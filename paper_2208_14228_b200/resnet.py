@@ -144,7 +144,38 @@ class ResNetJob:
             self._cast[1][i] = self.wb.data_ptr() + 2 * self.woff[cv.name]
             self._cast[2][i] = self.wt.data_ptr() + 2 * self.woff[cv.name]
             self._cast[3][i], self._cast[4][i], self._cast[5][i] = cv.co, cv.taps, cv.ci
-            self._cast[6][i] = 1  # dX = a stride-1 convolution (of dz, or of its zero insertion) with the flipped filter
+            self._cast[6][i] = 1  # stride-1 dX = a forward convolution of dz with the flipped filter
+        # stride-2 dX by output parity class: per (conv, class) the taps that reach it, as a stride-1
+        # convolution of dz (offsets (a + p - kh) / 2 from 0) with a class filter [Ci][Tc][Co] (bf16)
+        self.cls, ents, m = {}, [], 0
+        for cv in convs:
+            if cv.s != 2:
+                continue
+            lst = []
+            for a in (0, 1):
+                for b in (0, 1):
+                    th = sorted((kh for kh in range(cv.k) if (a + cv.p - kh) % 2 == 0), key=lambda kh: -kh)
+                    tw = sorted((kw for kw in range(cv.k) if (b + cv.p - kw) % 2 == 0), key=lambda kw: -kw)
+                    if not th or not tw:
+                        lst.append(None)
+                        continue
+                    assert [(a + cv.p - kh) // 2 for kh in th] == list(range(len(th)))
+                    assert [(b + cv.p - kw) // 2 for kw in tw] == list(range(len(tw)))
+                    src = [kh * cv.k + kw for kh in th for kw in tw]
+                    lst.append((len(th), len(tw), m))
+                    ents.append((cv, src, m))
+                    m += cv.ci * len(src) * cv.co
+            self.cls[cv.name] = lst
+        self.wcls = torch.empty(max(m, 1), dtype=torch.bfloat16, device="cuda")
+        k = len(ents)
+        self._taps = [(C.c_void_p * k)(), (C.c_void_p * k)(), (C.c_int32 * k)(), (C.c_int32 * k)(),
+                      (C.c_int32 * k)(), (C.c_int32 * k)(), (C.c_int32 * (9 * k))(), k]
+        for i, (cv, src, off) in enumerate(ents):
+            self._taps[0][i] = self.params.data_ptr() + 4 * self.off[cv.name][0]
+            self._taps[1][i] = self.wcls.data_ptr() + 2 * off
+            self._taps[2][i], self._taps[3][i], self._taps[4][i], self._taps[5][i] = cv.co, cv.taps, cv.ci, len(src)
+            for t, v in enumerate(src):
+                self._taps[6][9 * i + t] = v
         self.flags = Flags()
         self.step_idx = 0
         self._ws = {}
@@ -201,9 +232,9 @@ class ResNetJob:
         return cv.ci % 64 == 0 and (self.B * cv.hout ** 2) % 64 == 0 and os.environ.get("BT_CONV_EXPLICIT") != "1"
 
     def implicit_dx(self, cv) -> bool:
-        """The input gradient as an implicit GEMM: a stride-1 convolution over dz (stride 1) or over its zero
-        insertion (stride 2), whose input channels are cv.co and output pixels the forward input grid."""
-        return cv.co % 64 == 0 and (self.B * cv.hin ** 2) % 64 == 0 and os.environ.get("BT_CONV_EXPLICIT") != "1"
+        """The input gradient as an implicit GEMM: a stride-1 convolution over dz (stride 1: the whole
+        gradient; stride 2: one output parity class), input channels cv.co, output pixels dz's grid."""
+        return cv.co % 64 == 0 and (self.B * cv.hout ** 2) % 64 == 0 and os.environ.get("BT_CONV_EXPLICIT") != "1"
 
     def splits(self, cv) -> int:
         """Pinned pixel splits of an EST's weight-gradient reduction (a function of the shape only)."""
@@ -211,9 +242,12 @@ class ResNetJob:
 
     # ------------------------------------------------------------ workspace
     def _refresh_bf16(self):
-        c = self._cast
+        c, t = self._cast, self._taps
         _native.check(_native.lib().bt_cnn_conv_weights(c[0], c[1], c[2], c[3], c[4], c[5], c[6], len(c[3]), stream()),
                       "conv weight cast")
+        if t[7]:
+            _native.check(_native.lib().bt_cnn_filter_taps(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], stream()),
+                          "class filters")
 
     def _workspace(self, n: int) -> dict:
         ws = self._ws.get(n)
@@ -221,14 +255,12 @@ class ResNetJob:
             return ws
         B = self.B
         bf, f32 = dict(dtype=torch.bfloat16, device="cuda"), dict(dtype=torch.float32, device="cuda")
-        col = up = 0  # the dX gathers of explicit fallbacks; the zero insertions of stride-2 dz
+        col = 0  # the dX gathers of explicit fallbacks (stride 1: 9 taps; stride 2: a class's <= 4 taps)
         for cv in self.convs:
             if cv.name != "stem" and not self.implicit_dx(cv):
-                col = max(col, n * B * cv.hin ** 2 * cv.taps * cv.co)
-            if cv.name != "stem" and cv.s != 1:
-                up = max(up, n * B * cv.hin ** 2 * cv.co)
+                col = max(col, n * B * cv.hout ** 2 * cv.taps * cv.co)
         ws = {"img": torch.empty(n * B * 1024 * 8, **bf), "labels": torch.empty(n * B, dtype=torch.int32, device="cuda"),
-              "col": torch.empty(col, **bf), "up": torch.empty(up, **bf), "loss": torch.empty(n, **f32)}
+              "col": torch.empty(col, **bf), "loss": torch.empty(n, **f32)}
         for cv in self.convs:
             R = n * B * cv.hout ** 2
             ws[cv.name] = {"z": torch.empty(R * cv.co, **bf), "y": torch.empty(R * cv.co, **bf),
@@ -294,8 +326,8 @@ class ResNetJob:
 
     def _conv_bwd(self, ws, cv, n, base, x, dz, dx):
         """dW_e into each EST's gradient slot (implicit GEMM over the EST's output pixels, or the forward's
-        explicit im2col) and, if dx is given, the input gradient: stride 1 = a forward convolution of dz
-        with the flipped filter; stride 2 = the same over the zero insertion of dz (bt_cnn_upsample)."""
+        explicit im2col) and, if dx is given, the input gradient (`_dx`: stride 2 returns its parity
+        classes)."""
         L, s, B = _native.lib(), stream(), self.B
         Re = B * cv.hout ** 2
         gdst = self.grads.data_ptr() + 4 * (base * self.P + self.off[cv.name][0])
@@ -315,22 +347,39 @@ class ResNetJob:
         if sp > 1:
             _native.check(L.bt_fold_splits(part, n, sp, cv.co * cv.K, gdst, self.P, s), "dW split fold")
         if dx is None:
-            return
-        Rin = n * B * cv.hin ** 2
-        wt = self.wt.data_ptr() + 2 * self.woff[cv.name]
-        pad = cv.k - 1 - cv.p
-        src, hs = dz, cv.hout
-        if cv.s != 1:  # zero insertion: the transposed convolution becomes a stride-1 convolution of `up`
-            src, hs = ws["up"], cv.hin
-            _native.check(L.bt_cnn_upsample(dz.data_ptr(), n * B, cv.hout, cv.hout, cv.co, cv.s, src.data_ptr(), s),
-                          "dz zero insertion")
+            return None
+        return self._dx(ws, cv, n, dz, dx)
+
+    def _dx(self, ws, cv, n, dz, dx):
+        """Stride 1: dx = a forward convolution of dz with the flipped filter.  Stride 2: the four output
+        parity classes, each a stride-1 convolution of dz with its class filter, into the four quarters
+        of `dx`'s buffer; returns their pointers (None for a class no tap reaches) for bt_cnn_add_s2."""
+        if cv.s == 1:
+            wt = self.wt.data_ptr() + 2 * self.woff[cv.name]
+            self._conv_s1(ws, cv, n, dz.data_ptr(), cv.k, cv.k, cv.k - 1 - cv.p, wt, dx.data_ptr())
+            return None
+        q = n * self.B * cv.hout ** 2 * cv.ci  # one class's elements
+        out = []
+        for i, c in enumerate(self.cls[cv.name]):
+            if c is None:
+                out.append(None)
+                continue
+            kh, kw, off = c
+            dst = dx.data_ptr() + 2 * i * q
+            self._conv_s1(ws, cv, n, dz.data_ptr(), kh, kw, 0, self.wcls.data_ptr() + 2 * off, dst)
+            out.append(dst)
+        return out
+
+    def _conv_s1(self, ws, cv, n, src, kh, kw, pad, w, dst):
+        """A stride-1 convolution over dz's grid (cv.hout square, cv.co channels) into cv.ci channels."""
+        L, s, B, h = _native.lib(), stream(), self.B, cv.hout
         if self.implicit_dx(cv):
-            _native.check(L.bt_gemm_conv(0, src.data_ptr(), n * B, hs, hs, cv.co, cv.hin, cv.hin, cv.k, cv.k, 1, pad,
-                                         wt, dx.data_ptr(), cv.ci, 1, 0, 0, 1, s), "conv dX (implicit)")
+            _native.check(L.bt_gemm_conv(0, src, n * B, h, h, cv.co, h, h, kh, kw, 1, pad, w, dst, cv.ci, 1, 0, 0, 1, s),
+                          "conv dX (implicit)")
             return
-        _native.check(L.bt_cnn_im2col(src.data_ptr(), ws["col"].data_ptr(), n * B, hs, hs, cv.co, cv.hin, cv.hin, cv.k,
-                                      cv.k, 1, pad, 0, s), "dX im2col")
-        _native.check(L.bt_gemm_bf16_ex(ws["col"].data_ptr(), wt, dx.data_ptr(), 1, Rin, cv.ci, cv.taps * cv.co, 0, 0,
+        _native.check(L.bt_cnn_im2col(src, ws["col"].data_ptr(), n * B, h, h, cv.co, h, h, kh, kw, 1, pad, 0, s),
+                      "dX im2col")
+        _native.check(L.bt_gemm_bf16_ex(ws["col"].data_ptr(), w, dst, 1, n * B * h * h, cv.ci, kh * kw * cv.co, 0, 0,
                                         0, 1, None, 0, 0, s), "conv dX gemm")
 
     def _group(self, gslot: int, base: int, n: int, losses: torch.Tensor, capture: dict | None):
@@ -374,15 +423,19 @@ class ResNetJob:
             self._bn_bwd(ws, b, n, base, dy, out, dzb)
             self._conv_bwd(ws, b, n, base, ws[a.name]["y"], dzb, dya)
             self._bn_bwd(ws, a, n, base, dya, ws[a.name]["y"], dza)
-            self._conv_bwd(ws, a, n, base, xin, dza, dxa)
+            ca = self._conv_bwd(ws, a, n, base, xin, dza, dxa)
             if d is None:  # identity shortcut: dx = dxa + dy [out > 0]
                 _native.check(L.bt_cnn_add(dxa.data_ptr(), dy.data_ptr(), out.data_ptr(), n * B * a.hin ** 2 * a.ci,
                                            dy.data_ptr(), s))
-            else:
+            else:  # stride-2 block: both gradients arrive as parity classes, interleaved by the add
                 self._bn_bwd(ws, d, n, base, dy, out, g[2])
-                self._conv_bwd(ws, d, n, base, xin, g[2], g[1])
-                _native.check(L.bt_cnn_add(dxa.data_ptr(), g[1].data_ptr(), None, n * B * a.hin ** 2 * a.ci,
-                                           dy.data_ptr(), s))
+                cd = self._conv_bwd(ws, d, n, base, xin, g[2], g[1])
+                if a.s == 2:
+                    _native.check(L.bt_cnn_add_s2((C.c_void_p * 4)(*ca), (C.c_void_p * 4)(*cd), dy.data_ptr(), n * B,
+                                                  a.hout, a.hout, a.ci, s), "stride-2 dX classes + shortcut")
+                else:
+                    _native.check(L.bt_cnn_add(dxa.data_ptr(), g[1].data_ptr(), None, n * B * a.hin ** 2 * a.ci,
+                                               dy.data_ptr(), s))
         self._bn_bwd(ws, stem, n, base, dy, ws["stem"]["y"], g[1])
         self._conv_bwd(ws, stem, n, base, ws["img"], g[1], None)
         sl["cursor"].add_(1)  # every EST of the group consumed one micro-batch

@@ -13,6 +13,8 @@
   per-EST conv weight gradient rel. Frobenius error <= 5e-3).
 """
 
+import ctypes as C
+
 import numpy as np
 import pytest
 import torch
@@ -282,7 +284,34 @@ def test_convolution_products_match_float64(rn, ci, co, k, s, hw):
         _native.check(L.bt_gemm_bf16_ex(col.data_ptr(), wt.data_ptr(), dx.data_ptr(), 1, N * hw * hw, ci, k * k * co,
                                         0, 0, 0, 0, None, 0, 0, stream()))
     _close(dx, dxref, "conv dX", 1e-5)
-    if s != 1:  # the step's path: zero insertion of dz, then a stride-1 implicit convolution (flipped filter)
+    if s != 1:  # the step's path: four output parity classes, each a stride-1 convolution of dz
+        wf = w.float().reshape(co, k * k, ci).contiguous()  # master layout [Co][taps][Ci]
+        cls, outs = [], []
+        for a in (0, 1):
+            for b in (0, 1):
+                th = sorted((t for t in range(k) if (a + p - t) % 2 == 0), key=lambda t: -t)
+                tw = sorted((t for t in range(k) if (b + p - t) % 2 == 0), key=lambda t: -t)
+                if not th or not tw:
+                    cls.append(None)
+                    continue
+                src = [u * k + v for u in th for v in tw]
+                wc = torch.empty(ci, len(src), co, dtype=torch.bfloat16, device="cuda")
+                tm = (C.c_int32 * 9)(*(src + [0] * (9 - len(src))))
+                _native.check(L.bt_cnn_filter_taps((C.c_void_p * 1)(wf.data_ptr()), (C.c_void_p * 1)(wc.data_ptr()),
+                                                   (C.c_int32 * 1)(co), (C.c_int32 * 1)(k * k), (C.c_int32 * 1)(ci),
+                                                   (C.c_int32 * 1)(len(src)), tm, 1, stream()))
+                ref = w.view(co, k * k, ci)[:, src, :].permute(2, 1, 0)
+                torch.cuda.synchronize()
+                assert torch.equal(wc, ref)
+                o = torch.empty(N, ho, ho, ci, dtype=torch.bfloat16, device="cuda")
+                _native.check(L.bt_gemm_conv(0, dz.data_ptr(), N, ho, ho, co, ho, ho, len(th), len(tw), 1, 0,
+                                             wc.data_ptr(), o.data_ptr(), ci, 1, 0, 0, 1, stream()))
+                outs.append(o)
+                cls.append(o.data_ptr())
+        dxc = torch.empty(N, hw, hw, ci, dtype=torch.bfloat16, device="cuda")
+        _native.check(L.bt_cnn_add_s2((C.c_void_p * 4)(*cls), None, dxc.data_ptr(), N, ho, ho, ci, stream()))
+        _close_bf16(dxc.reshape(-1, ci), dxref, "conv dX (parity classes)")
+    if s != 1:  # the zero-insertion alternative: a stride-1 implicit convolution of the zero-inserted dz
         up = torch.empty(N, hw, hw, co, dtype=torch.bfloat16, device="cuda")
         _native.check(L.bt_cnn_upsample(dz.data_ptr(), N, ho, ho, co, s, up.data_ptr(), stream()))
         upref = torch.zeros_like(up)
