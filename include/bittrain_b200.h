@@ -193,11 +193,19 @@ int bt_bert_attn(int32_t backward, const void *qkv_dev, const void *dctx_dev, vo
                  int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed, int64_t step,
                  float p, const int64_t *step_dev, void *stream);
 /* x = resid + dropout(branch + bias); y = LayerNorm(x) * gamma + beta -> xsum (x), stats (mean, rstd)
- * [T][2], y32, yb (bf16).  resid fp32 (the residual stream), branch bf16 (a GEMM output). */
+ * [T][2], y32 (may be NULL), yb (bf16).  resid fp32 (the residual stream), branch bf16 (a GEMM output). */
 int bt_bert_ln_fwd(const float *resid_dev, const void *branch_dev, const float *bias_dev, const float *gamma_dev,
                    const float *beta_dev, float *xsum_dev, float *stats_dev, float *y32_dev, void *yb_dev, int32_t E,
                    int32_t Te, int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
                    int64_t step, float p, float eps, const int64_t *step_dev, void *stream);
+/* bt_bert_ln_fwd whose residual input is the previous LayerNorm's output recomputed from that LayerNorm's
+ * input, (mean, rstd) and affine parameters -- the expression that produced its fp32 output, so the same
+ * bits -- instead of a stored fp32 copy; y32_dev may be NULL (no fp32 output written) */
+int bt_bert_ln_fwd_rc(const float *prev_xsum_dev, const float *prev_stats_dev, const float *prev_gamma_dev,
+                      const float *prev_beta_dev, const void *branch_dev, const float *bias_dev, const float *gamma_dev,
+                      const float *beta_dev, float *xsum_dev, float *stats_dev, float *y32_dev, void *yb_dev, int32_t E,
+                      int32_t Te, int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site,
+                      uint64_t seed, int64_t step, float p, float eps, const int64_t *step_dev, void *stream);
 /* dx = LayerNorm'(dy1 + dy2) (dy1 bf16 from a GEMM, dy2 fp32 residual-path gradient or NULL),
  * dbranch = bf16(dropout'(dx)); part [E][Te/64][3][D] = per-64-row-chunk column sums of
  * (dy*xhat, dy, dropout'(dx)) */

@@ -187,8 +187,8 @@ class BertJob:
                         "h1b": torch.empty(T, D, **bf), "Hpre": torch.empty(T, F, **bf),
                         "Dact": torch.empty(T, F, **bf), "hs2": torch.empty(T, D, **f32),
                         "st2": torch.empty(T, 2, **f32)} for _ in range(L)],
-            "x32": torch.empty(T, D, **f32), "r32": [torch.empty(T, D, **f32) for _ in range(2)],
-            "h1_32": torch.empty(T, D, **f32), "brb": torch.empty(T, D, **bf), "ytop": torch.empty(T, D, **bf),
+            "x32": torch.empty(T, D, **f32), "y32": torch.empty(T, D, **f32),
+            "brb": torch.empty(T, D, **bf), "ytop": torch.empty(T, D, **bf),
             "tgt": torch.empty(T, D, **f32), "dy1": [torch.empty(T, D, **bf) for _ in range(2)],
             "dres": [torch.empty(T, D, **f32) for _ in range(2)],
             "dbr": torch.empty(T, D, **bf), "dHpre": torch.empty(T, F, **bf), "dctx": torch.empty(T, D, **bf),
@@ -232,20 +232,32 @@ class BertJob:
             _native.check(L.bt_bert_attn(0, w["qkv"].data_ptr(), None, w["ctx"].data_ptr(), n, Te, D, H, base, NL, l,
                                          seed, step, self.pa, sp, s), "attention forward")
             self._gemm(w["ctx"].data_ptr(), self._wb(l, "Wo"), ws["brb"].data_ptr(), T, D, D, out_bf16=True)
-            _native.check(L.bt_bert_ln_fwd(x32.data_ptr(), ws["brb"].data_ptr(), self._p(l, "bo"), self._p(l, "g1"),
-                                           self._p(l, "be1"), w["hs1"].data_ptr(), w["st1"].data_ptr(),
-                                           ws["h1_32"].data_ptr(), w["h1b"].data_ptr(), n, Te, D, base, NL, l, 0,
-                                           seed, step, self.ph, self.eps, sp, s), "layernorm 1")
+            if l == 0:  # the embedding input is stored fp32; later residuals are recomputed (bt_bert_ln_fwd_rc)
+                _native.check(L.bt_bert_ln_fwd(x32.data_ptr(), ws["brb"].data_ptr(), self._p(l, "bo"),
+                                               self._p(l, "g1"), self._p(l, "be1"), w["hs1"].data_ptr(),
+                                               w["st1"].data_ptr(), None, w["h1b"].data_ptr(), n, Te,
+                                               D, base, NL, l, 0, seed, step, self.ph, self.eps, sp, s), "layernorm 1")
+            else:
+                pw = lay[l - 1]
+                _native.check(L.bt_bert_ln_fwd_rc(pw["hs2"].data_ptr(), pw["st2"].data_ptr(), self._p(l - 1, "g2"),
+                                                  self._p(l - 1, "be2"), ws["brb"].data_ptr(), self._p(l, "bo"),
+                                                  self._p(l, "g1"), self._p(l, "be1"), w["hs1"].data_ptr(),
+                                                  w["st1"].data_ptr(), None, w["h1b"].data_ptr(), n, Te, D, base, NL, l,
+                                                  0, seed, step, self.ph, self.eps, sp, s), "layernorm 1")
             _native.check(L.bt_gemm_bf16_ffn(w["h1b"].data_ptr(), self._wb(l, "W1"), w["Hpre"].data_ptr(), T, F, D, 1,
                                              self._p(l, "b1"), None, w["Dact"].data_ptr(), seed, step, base, Te, 0.0,
                                              0, s), "ffn forward GEMM")
             self._gemm(w["Dact"].data_ptr(), self._wb(l, "W2"), ws["brb"].data_ptr(), T, D, F, out_bf16=True)
-            y32 = ws["r32"][l & 1]
+            # the fp32 LayerNorm-2 output is kept only where it is read: the loss (last layer), captures
+            keep = l == NL - 1 or (capture is not None and l == 0)
+            y32 = ws["y32"]
             yb = lay[l + 1]["xb"] if l + 1 < NL else ws["ytop"]
-            _native.check(L.bt_bert_ln_fwd(ws["h1_32"].data_ptr(), ws["brb"].data_ptr(), self._p(l, "b2"),
-                                           self._p(l, "g2"), self._p(l, "be2"), w["hs2"].data_ptr(),
-                                           w["st2"].data_ptr(), y32.data_ptr(), yb.data_ptr(), n, Te, D, base, NL, l,
-                                           1, seed, step, self.ph, self.eps, sp, s), "layernorm 2")
+            _native.check(L.bt_bert_ln_fwd_rc(w["hs1"].data_ptr(), w["st1"].data_ptr(), self._p(l, "g1"),
+                                              self._p(l, "be1"), ws["brb"].data_ptr(), self._p(l, "b2"),
+                                              self._p(l, "g2"), self._p(l, "be2"), w["hs2"].data_ptr(),
+                                              w["st2"].data_ptr(), y32.data_ptr() if keep else None, yb.data_ptr(), n,
+                                              Te, D, base, NL, l, 1, seed, step, self.ph, self.eps, sp, s),
+                          "layernorm 2")
             if capture is not None and l == 0:
                 capture.update({k: w[k].clone() for k in ("xb", "qkv", "ctx", "hs1", "st1", "h1b", "Hpre", "Dact",
                                                           "hs2", "st2")})

@@ -410,6 +410,13 @@ struct LnArgs {
   float* y32;           // fwd: LN output fp32       bwd: dx (LN-input gradient, the residual path)
   __nv_bfloat16* yb;    // fwd: LN output bf16       bwd: dropout'(dx) bf16 (the branch gradient)
   float* part;          // bwd: [E][chunks][3][D] column partials (dgamma, dbeta, dbias)
+  // fwd, when rx is set: the residual is the previous LayerNorm's output recomputed from its input rx,
+  // statistics rst and affine rg / rb -- the same expression that produced its y32, hence the same bits
+  // (-fmad=false) -- so that LayerNorm need not write y32
+  const float* rx;
+  const float2* rst;
+  const float* rg;
+  const float* rb;
   int D, Te, rows, est_base, L, layer, site;
   uint64_t seed;
   int64_t step;
@@ -480,7 +487,17 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const LnArgs a) {
   for (int c = 0; c < NC; ++c) {
     const int col = c * 256 + lane * 8;
     float r[8], b[8], bi[8], m[8];
-    ld8(a.resid + (size_t)t * a.D + col, r);
+    if (a.rx) {
+      const float2 rs = a.rst[t];
+      float rgm[8], rbt[8];
+      ld8(a.rx + (size_t)t * a.D + col, r);
+      ld8(a.rg + col, rgm);
+      ld8(a.rb + col, rbt);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = (r[k] - rs.x) * rs.y * rgm[k] + rbt[k];
+    } else {
+      ld8(a.resid + (size_t)t * a.D + col, r);
+    }
     ld8(a.bin + (size_t)t * a.D + col, b);
     ld8(a.bias + col, bi);
     ln_mask8(a, step, sd, tl, col, thr, keep, m);
@@ -509,7 +526,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const LnArgs a) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) y[k] = (x[c][k] - mean) * rstd * gm[k] + bt[k];
     st8(a.xsum + (size_t)t * a.D + col, x[c]);
-    st8(a.y32 + (size_t)t * a.D + col, y);
+    if (a.y32) st8(a.y32 + (size_t)t * a.D + col, y);
     st8(a.yb + (size_t)t * a.D + col, y);
   }
   if (lane == 0) a.stats[t] = make_float2(mean, rstd);
@@ -784,10 +801,15 @@ static int ln_launch_nc(int backward, const bert::LnArgs& a, int E, cudaStream_t
 int bert_ln_launch(int backward, const float* in1, const void* in2, const float* bias, const float* gamma,
                    const float* beta, float* xsum, float* stats, float* y32, void* yb, float* part, int E, int Te,
                    int D, int est_base, int L, int layer, int site, uint64_t seed, int64_t step, float p, float eps,
-                   const int64_t* step_dev, cudaStream_t s) {
+                   const int64_t* step_dev, cudaStream_t s, const float* rx, const float* rst, const float* rg,
+                   const float* rb) {
   if (D % 256 || D > 1024 || Te % bert::LN_CHUNK) return ERR_INPUT;
   bert::LnArgs a{};
   a.resid = in1;
+  a.rx = rx;
+  a.rst = (const float2*)rst;
+  a.rg = rg;
+  a.rb = rb;
   a.bin = (const __nv_bfloat16*)in2;
   a.bias = bias;
   a.gamma = gamma;

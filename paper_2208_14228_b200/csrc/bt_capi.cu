@@ -59,7 +59,8 @@ int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out,
 int bert_ln_launch(int backward, const float* in1, const void* in2, const float* bias, const float* gamma,
                    const float* beta, float* xsum, float* stats, float* y32, void* yb, float* part, int E, int Te,
                    int D, int est_base, int L, int layer, int site, uint64_t seed, int64_t step, float p, float eps,
-                   const int64_t* step_dev, cudaStream_t s);
+                   const int64_t* step_dev, cudaStream_t s, const float* rx = nullptr,
+                   const float* rst = nullptr, const float* rg = nullptr, const float* rb = nullptr);
 int bert_ln_fold_launch(const float* part, int E, int Te, int D, float* dg, float* db, float* dr, int64_t est_stride,
                         cudaStream_t s);
 int bert_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, float* X32, void* Xb,
@@ -660,14 +661,29 @@ int bt_bert_ln_fwd(const float* resid_dev, const void* branch_dev, const float* 
                    int32_t Te, int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site, uint64_t seed,
                    int64_t step, float p, float eps, const int64_t* step_dev, void* stream) {
   if (int st = bert_shape(E, Te, D)) return st;
-  if (!resid_dev || !branch_dev || !bias_dev || !gamma_dev || !beta_dev || !xsum_dev || !stats_dev || !y32_dev ||
-      !yb_dev)
+  if (!resid_dev || !branch_dev || !bias_dev || !gamma_dev || !beta_dev || !xsum_dev || !stats_dev || !yb_dev)
     return fail(bt::ERR_INPUT, "null pointer");
   if (!(p >= 0.f && p < 1.f) || (site != 0 && site != 1)) return fail(bt::ERR_CONFIG, "bad dropout / site");
   return done(bt::bert_ln_launch(0, resid_dev, branch_dev, bias_dev, gamma_dev, beta_dev, xsum_dev, stats_dev, y32_dev,
                                  yb_dev, nullptr, E, Te, D, est_base, layers, layer, site, seed, step, p, eps,
                                  step_dev, STREAM(stream)),
               "bt_bert_ln_fwd");
+}
+int bt_bert_ln_fwd_rc(const float* prev_xsum_dev, const float* prev_stats_dev, const float* prev_gamma_dev,
+                      const float* prev_beta_dev, const void* branch_dev, const float* bias_dev, const float* gamma_dev,
+                      const float* beta_dev, float* xsum_dev, float* stats_dev, float* y32_dev, void* yb_dev, int32_t E,
+                      int32_t Te, int32_t D, int32_t est_base, int32_t layers, int32_t layer, int32_t site,
+                      uint64_t seed, int64_t step, float p, float eps, const int64_t* step_dev, void* stream) {
+  if (int st = bert_shape(E, Te, D)) return st;
+  if (!prev_xsum_dev || !prev_stats_dev || !prev_gamma_dev || !prev_beta_dev || !branch_dev || !bias_dev ||
+      !gamma_dev || !beta_dev || !xsum_dev || !stats_dev || !yb_dev)
+    return fail(bt::ERR_INPUT, "null pointer");
+  if (!(p >= 0.f && p < 1.f) || (site != 0 && site != 1)) return fail(bt::ERR_CONFIG, "bad dropout / site");
+  return done(bt::bert_ln_launch(0, nullptr, branch_dev, bias_dev, gamma_dev, beta_dev, xsum_dev, stats_dev, y32_dev,
+                                 yb_dev, nullptr, E, Te, D, est_base, layers, layer, site, seed, step, p, eps,
+                                 step_dev, STREAM(stream), prev_xsum_dev, prev_stats_dev, prev_gamma_dev,
+                                 prev_beta_dev),
+              "bt_bert_ln_fwd_rc");
 }
 int bt_bert_ln_bwd(const void* dy1_dev, const float* dy2_dev, const float* xsum_dev, const float* stats_dev,
                    const float* gamma_dev, float* dx_dev, void* dbranch_dev, float* part_dev, int32_t E, int32_t Te,
