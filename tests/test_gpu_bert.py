@@ -380,3 +380,46 @@ def test_tcgen05_attention_backward_matches_mma_sync(bert, monkeypatch):
         x, y = a[:, part * D:(part + 1) * D], b[:, part * D:(part + 1) * D]
         assert (x != y).double().mean().item() <= 3e-2, part
         assert ((x - y).norm() / y.norm()).item() <= 1e-2, part
+
+
+def test_layernorm_residual_recompute_equals_stored(bert):
+    """bt_bert_ln_fwd_rc (the residual recomputed from the previous LayerNorm's input, statistics and
+    affine parameters) gives the bits of bt_bert_ln_fwd fed the previous LayerNorm's stored fp32 output."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    L = _native.lib()
+    E, Te, D = 2, 128, 768
+    T = E * Te
+    g = torch.Generator(device="cuda").manual_seed(5)
+    f32 = dict(device="cuda", dtype=torch.float32)
+
+    def rnd(*shape, scale=1.0):
+        return torch.randn(*shape, generator=g, **f32) * scale
+
+    x0, b0 = rnd(T, D), rnd(T, D).to(torch.bfloat16)
+    bias0, g0, be0 = rnd(D, scale=0.1), 1 + rnd(D, scale=0.1), rnd(D, scale=0.1)
+    bias1, g1, be1 = rnd(D, scale=0.1), 1 + rnd(D, scale=0.1), rnd(D, scale=0.1)
+    b1 = rnd(T, D).to(torch.bfloat16)
+    hs0, st0, y0, yb0 = torch.empty(T, D, **f32), torch.empty(T, 2, **f32), torch.empty(T, D, **f32), \
+        torch.empty(T, D, device="cuda", dtype=torch.bfloat16)
+    args = (E, Te, D, 0, 2, 0, 1, 42, 3, 0.1, 1e-5, None, stream())
+    _native.check(L.bt_bert_ln_fwd(x0.data_ptr(), b0.data_ptr(), bias0.data_ptr(), g0.data_ptr(), be0.data_ptr(),
+                                   hs0.data_ptr(), st0.data_ptr(), y0.data_ptr(), yb0.data_ptr(), *args))
+    outs = []
+    for rc in (False, True):
+        hs, st = torch.empty(T, D, **f32), torch.empty(T, 2, **f32)
+        y, yb = torch.empty(T, D, **f32), torch.empty(T, D, device="cuda", dtype=torch.bfloat16)
+        if rc:
+            _native.check(L.bt_bert_ln_fwd_rc(hs0.data_ptr(), st0.data_ptr(), g0.data_ptr(), be0.data_ptr(),
+                                              b1.data_ptr(), bias1.data_ptr(), g1.data_ptr(), be1.data_ptr(),
+                                              hs.data_ptr(), st.data_ptr(), y.data_ptr(), yb.data_ptr(), *args))
+        else:
+            _native.check(L.bt_bert_ln_fwd(y0.data_ptr(), b1.data_ptr(), bias1.data_ptr(), g1.data_ptr(),
+                                           be1.data_ptr(), hs.data_ptr(), st.data_ptr(), y.data_ptr(), yb.data_ptr(),
+                                           *args))
+        outs.append((hs, st, y, yb))
+    torch.cuda.synchronize()
+    for a, b in zip(*outs):
+        assert torch.equal(a.view(torch.int16 if a.dtype == torch.bfloat16 else torch.int32),
+                           b.view(torch.int16 if b.dtype == torch.bfloat16 else torch.int32))
