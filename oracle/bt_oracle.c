@@ -35,6 +35,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <pthread.h>
+#include <stdatomic.h>
 
 #define OR_INPUT_DIM 8
 #define OR_HIDDEN 16
@@ -338,8 +339,9 @@ typedef struct {
     int64_t global_step, epoch;
     int spe;
     double *grads; /* [E][P] */
-    /* worker pool (bench cpu baseline only) */
+    /* worker pool (bench cpu baseline / reference arm only) */
     int nthreads;
+    struct or_pool *pool;
 } or_run;
 
 /* assign_ranks (engine.py:169-199).  threads may be NULL (balanced, larger shares first). */
@@ -428,8 +430,10 @@ or_run *or_run_create(const or_cfg *cfg, int nexec, const uint64_t *kind_fnv, co
     return R;
 }
 
+static void or_pool_stop(or_run *R);
 void or_run_free(or_run *R) {
     if (!R) return;
+    or_pool_stop(R);
     free(R->rng); free(R->stat_count); free(R->stat_mean); free(R->dataset); free(R->lists); free(R->grads);
     free(R);
 }
@@ -500,6 +504,60 @@ static void *or_thread_main(void *arg) {
     return NULL;
 }
 
+/* Persistent spinning workers (the per-step cost of pthread_create would exceed a mini-batch's
+ * work): the main thread publishes a generation, each worker runs its EST range and counts in. */
+typedef struct or_pool {
+    int n; /* workers besides the main thread */
+    pthread_t th[64];
+    or_job jobs[64];
+    atomic_int gen, done, quit;
+    struct or_worker { struct or_pool *pool; int id; } w[64];
+} or_pool;
+
+static inline void or_relax(void) {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+}
+
+static void *or_pool_main(void *arg) {
+    struct or_worker *w = (struct or_worker *)arg;
+    or_pool *P = w->pool;
+    int seen = 0;
+    for (;;) {
+        int g;
+        while ((g = atomic_load(&P->gen)) == seen && !atomic_load(&P->quit)) or_relax();
+        if (atomic_load(&P->quit)) return NULL;
+        seen = g;
+        or_est_range(&P->jobs[w->id]);
+        atomic_fetch_add(&P->done, 1);
+    }
+}
+
+static void or_pool_stop(or_run *R) {
+    or_pool *P = R->pool;
+    if (!P) return;
+    atomic_store(&P->quit, 1);
+    for (int t = 1; t <= P->n; t++) pthread_join(P->th[t], NULL);
+    free(P);
+    R->pool = NULL;
+}
+
+static void or_pool_start(or_run *R, int n) {
+    or_pool_stop(R);
+    if (n < 1) return;
+    or_pool *P = (or_pool *)calloc(1, sizeof(or_pool));
+    P->n = n;
+    atomic_init(&P->gen, 0);
+    atomic_init(&P->done, 0);
+    atomic_init(&P->quit, 0);
+    for (int t = 1; t <= n; t++) {
+        P->w[t] = (struct or_worker){P, t};
+        pthread_create(&P->th[t], NULL, or_pool_main, &P->w[t]);
+    }
+    R->pool = P;
+}
+
 /* run_minibatch (engine.py:271-329).  gx/gy: optional explicit global batch
  * ([E*B][8], [E*B]); losses_out: [E]. */
 int or_run_step(or_run *R, const double *gx, const double *gy, double *losses_out) {
@@ -512,15 +570,25 @@ int or_run_step(or_run *R, const double *gx, const double *gy, double *losses_ou
     if (nt > 64) nt = 64;
     or_job jobs[64];
     pthread_t th[64];
-    for (int t = 0; t < nt; t++) {
-        jobs[t] = (or_job){R, gx, gy, losses_out, (E * t) / nt, (E * (t + 1)) / nt, 0};
-    }
-    if (nt == 1) {
-        or_est_range(&jobs[0]);
+    or_pool *P = R->pool;
+    if (P && P->n + 1 == nt) { /* persistent workers */
+        for (int t = 0; t < nt; t++) P->jobs[t] = (or_job){R, gx, gy, losses_out, (E * t) / nt, (E * (t + 1)) / nt, 0};
+        atomic_store(&P->done, 0);
+        atomic_fetch_add(&P->gen, 1);
+        or_est_range(&P->jobs[0]);
+        while (atomic_load(&P->done) != P->n) or_relax();
+        for (int t = 0; t < nt; t++) jobs[t] = P->jobs[t];
     } else {
-        for (int t = 1; t < nt; t++) pthread_create(&th[t], NULL, or_thread_main, &jobs[t]);
-        or_est_range(&jobs[0]);
-        for (int t = 1; t < nt; t++) pthread_join(th[t], NULL);
+        for (int t = 0; t < nt; t++) {
+            jobs[t] = (or_job){R, gx, gy, losses_out, (E * t) / nt, (E * (t + 1)) / nt, 0};
+        }
+        if (nt == 1) {
+            or_est_range(&jobs[0]);
+        } else {
+            for (int t = 1; t < nt; t++) pthread_create(&th[t], NULL, or_thread_main, &jobs[t]);
+            or_est_range(&jobs[0]);
+            for (int t = 1; t < nt; t++) pthread_join(th[t], NULL);
+        }
     }
     for (int t = 0; t < nt; t++) if (jobs[t].status) return jobs[t].status;
     double synced[OR_P], np[OR_P], nv[OR_P];
@@ -544,7 +612,20 @@ int or_run_step(or_run *R, const double *gx, const double *gy, double *losses_ou
     return OR_OK;
 }
 
-void or_run_set_threads(or_run *R, int n) { R->nthreads = n; }
+void or_run_set_threads(or_run *R, int n) {
+    R->nthreads = n;
+    const int nt = n > R->cfg.max_workers ? R->cfg.max_workers : n;
+    or_pool_start(R, nt > 1 ? (nt > 64 ? 63 : nt - 1) : 0);
+}
+
+/* n pipeline-fed steps in C (the bench's reference arm: no per-step interpreter overhead) */
+int or_run_steps(or_run *R, int64_t n, double *losses_out) {
+    for (int64_t i = 0; i < n; i++) {
+        int st = or_run_step(R, NULL, NULL, losses_out);
+        if (st) return st;
+    }
+    return OR_OK;
+}
 
 void or_run_get_state(const or_run *R, double *params, double *vel, double *stat_mean, uint64_t *stat_count,
                       uint64_t *rng, int64_t *global_step, int64_t *epoch) {

@@ -80,6 +80,7 @@ def lib():
         L.or_run_relayout.argtypes = [C.c_void_p, C.c_int, _u64p, _i32p, _i64p]
         L.or_run_step.argtypes = [C.c_void_p, _dp, _dp, _dp]
         L.or_run_set_threads.argtypes = [C.c_void_p, C.c_int]
+        L.or_run_steps.argtypes = [C.c_void_p, _i64, _dp]
         L.or_run_get_state.argtypes = [C.c_void_p, _dp, _dp, _dp, _u64p, _u64p, _i64p, _i64p]
         L.or_run_get_buckets.argtypes = [C.c_void_p, _i32p, _i32p]
         L.or_reduce_update_f64.argtypes = [_dp, C.c_int, _i64, _i32p, C.c_int, _dp, _dp, C.c_double,
@@ -287,6 +288,14 @@ class Run:
 
     def set_threads(self, n: int):
         lib().or_run_set_threads(self._h, n)
+
+    def steps(self, n: int) -> np.ndarray:
+        """n pipeline-fed mini-batches in one native call; the last step's per-EST losses."""
+        losses = np.zeros(self.E)
+        st = lib().or_run_steps(self._h, n, losses.ctypes.data_as(_dp))
+        if st:
+            raise RuntimeError(f"oracle status {st}")
+        return losses
 
     def step(self, global_batch=None) -> np.ndarray:
         losses = np.zeros(self.E)
