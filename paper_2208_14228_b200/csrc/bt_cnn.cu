@@ -9,11 +9,14 @@
 //
 // Layout: NHWC bf16 activations; the images of local EST e are n in
 // [e*B, (e+1)*B), so its rows (n, h, w) are one contiguous block of B*H*W rows.
-// Convolutions are GEMMs on the deterministic tcgen05 kernel (bt_gemm.cu):
+// Convolutions are GEMMs on the deterministic tcgen05 kernels (bt_gemm.cu; implicit im2col
+// operands by TMA, or the explicit im2col below -- the same tiles and K order):
 //   forward  z = im2col(x) . W^T        (K = KH*KW*Ci, ordered (kh, kw, ci))
-//   dX       dx = im2colT(dz) . W'^T    (the transposed convolution as a gather:
-//                                        no scatter, no atomics)
-//   dW_e     = dz_e^T im2col(x)_e       (MN-major batched GEMM, one per EST)
+//   dX       stride 1: a forward convolution of dz with the tap-reversed filter;
+//            stride 2: four output parity classes, each a stride-1 convolution of
+//            dz with its class filter (filter_taps_kernel), interleaved by
+//            add_s2_kernel (no scatter, no atomics, no zero products)
+//   dW_e     = dz_e^T im2col(x)_e       (MN-major batched GEMM, one per EST split)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
