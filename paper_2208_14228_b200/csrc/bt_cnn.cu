@@ -91,16 +91,25 @@ struct ColArgs {
 // One warp per output row (its (image, ho, wo) decoded once); lanes walk the row's K8 16-byte
 // chunks -- coalesced stores, contiguous 16-byte reads per tap -- with shift/mask decoding (C/8 a
 // power of two, KW <= 3): the kernel is store-bandwidth-bound rather than integer-bound.
+// ROWPACK (K8 < 32, e.g. the 8-channel stem): thread per (row, chunk) item instead, so short rows do
+// not leave most of a warp idle; the stores stay contiguous across rows.
+template <bool ROWPACK>
 __global__ void __launch_bounds__(256) im2col_kernel(const ColArgs a, int lcg) {
   const int cg = 1 << lcg, K8 = a.KH * a.KW * cg;
   const int rows = a.N * a.Ho * a.Wo, HoWo = a.Ho * a.Wo;
   const int lane = threadIdx.x & 31;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+  const int64_t items = ROWPACK ? (int64_t)rows * K8 : rows;
+  const int64_t first = ROWPACK ? blockIdx.x * (int64_t)blockDim.x + threadIdx.x
+                                : (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t stride = ROWPACK ? (int64_t)gridDim.x * blockDim.x : ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = first; it < items; it += stride) {
+    const int r = ROWPACK ? (int)(it / K8) : (int)it;
     const int img = r / HoWo, pix = r - img * HoWo;
     const int ho = pix / a.Wo, wo = pix - ho * a.Wo;
     const __nv_bfloat16* src = a.src + (size_t)img * a.Hs * a.Ws * a.C;
     uint4* dst = (uint4*)(a.col + (size_t)r * K8 * 8);
-    for (int k8 = lane; k8 < K8; k8 += 32) {
+    const int kb = ROWPACK ? (int)(it - (int64_t)r * K8) : lane;
+    for (int k8 = kb; k8 < K8; k8 += ROWPACK ? K8 : 32) {
       const int t = k8 >> lcg, c8 = k8 & (cg - 1);
       const int kh = a.KW == 3 ? (t * 11) >> 5 : (a.KW == 2 ? t >> 1 : t), kw = t - kh * a.KW;  // t / 3 for t < 9
       int hi, wi;
@@ -575,7 +584,11 @@ int cnn_im2col_launch(const void* src, void* col, int N, int Hs, int Ws, int C, 
   while ((1 << lcg) < cg) ++lcg;
   const cnn::ColArgs a{(const __nv_bfloat16*)src, (__nv_bfloat16*)col, N, Hs, Ws, C, Ho, Wo, KH, KW, stride, pad,
                        transposed};
-  cnn::im2col_kernel<<<grid_n((int64_t)N * Ho * Wo * 32), 256, 0, s>>>(a, lcg);
+  const int K8 = KH * KW * cg;
+  if (K8 < 32)
+    cnn::im2col_kernel<true><<<grid_n((int64_t)N * Ho * Wo * K8), 256, 0, s>>>(a, lcg);
+  else
+    cnn::im2col_kernel<false><<<grid_n((int64_t)N * Ho * Wo * 32), 256, 0, s>>>(a, lcg);
   return ok_or_cuda_c();
 }
 
