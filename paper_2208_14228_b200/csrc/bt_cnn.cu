@@ -368,14 +368,23 @@ struct TapTable {
   TapMap m[16];
   int n;
 };
-__global__ void filter_taps_kernel(const __grid_constant__ TapTable tab) {
-  const TapMap& m = tab.m[blockIdx.y];
-  const int64_t n = (int64_t)m.Ci * m.Tc * m.Co;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int co = (int)(i % m.Co);
-    const int64_t r = i / m.Co;
-    const int tc = (int)(r % m.Tc), ci = (int)(r / m.Tc);
-    m.out[i] = __float2bfloat16_rn(m.w[((size_t)co * m.T + m.src[tc]) * m.Ci + ci]);
+// block = (32 x 32 tile of (ci, co), class tap tc, filter): read along ci, written along co
+__global__ void __launch_bounds__(256) filter_taps_kernel(const __grid_constant__ TapTable tab) {
+  __shared__ float tile[32][33];
+  const TapMap& m = tab.m[blockIdx.z];
+  const int tc = blockIdx.y;
+  const int tci = (m.Ci + 31) / 32;
+  const int ci0 = (blockIdx.x % tci) * 32, co0 = (blockIdx.x / tci) * 32;
+  if (tc >= m.Tc || co0 >= m.Co) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int k = ty; k < 32; k += 8) {
+    const int co = co0 + k, ci = ci0 + tx;
+    if (co < m.Co && ci < m.Ci) tile[k][tx] = m.w[((size_t)co * m.T + m.src[tc]) * m.Ci + ci];
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int ci = ci0 + k, co = co0 + tx;
+    if (ci < m.Ci && co < m.Co) m.out[((size_t)ci * m.Tc + tc) * m.Co + co] = __float2bfloat16_rn(tile[tx][k]);
   }
 }
 struct S2Args {
@@ -675,8 +684,14 @@ int cnn_filter_taps_launch(const float* const* w, void* const* out, const int* C
     mx = sz > mx ? sz : mx;
   }
   tab.n = n;
-  const int gx = (int)((mx + 255) / 256 < 1024 ? (mx + 255) / 256 : 1024);
-  cnn::filter_taps_kernel<<<dim3(gx, n), 256, 0, s>>>(tab);
+  int tiles = 0, tcmax = 0;
+  for (int i = 0; i < n; ++i) {
+    const int t = ((Ci[i] + 31) / 32) * ((Co[i] + 31) / 32);
+    tiles = t > tiles ? t : tiles;
+    tcmax = Tc[i] > tcmax ? Tc[i] : tcmax;
+  }
+  (void)mx;
+  cnn::filter_taps_kernel<<<dim3(tiles, tcmax, n), 256, 0, s>>>(tab);
   return ok_or_cuda_c();
 }
 
