@@ -511,16 +511,30 @@ struct ConvWTable {
   ConvW m[MAX_CONV];
   int n;
 };
-__global__ void conv_weights_kernel(const __grid_constant__ ConvWTable tab) {
-  const ConvW& m = tab.m[blockIdx.y];
-  const int64_t n = (int64_t)m.Co * m.T * m.Ci;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int ci = (int)(i % m.Ci);
-    const int64_t r = i / m.Ci;
-    const int t = (int)(r % m.T), co = (int)(r / m.T);
-    const __nv_bfloat16 v = __float2bfloat16_rn(m.w[i]);
-    m.wb[i] = v;
-    m.wt[((size_t)ci * m.T + (m.flip ? m.T - 1 - t : t)) * m.Co + co] = v;
+// block = (32 x 32 tile of (ci, co), tap t, conv): wb written along ci as read; wt through a shared-
+// memory transpose, written along co
+__global__ void __launch_bounds__(256) conv_weights_kernel(const __grid_constant__ ConvWTable tab) {
+  __shared__ float tile[32][33];
+  const ConvW& m = tab.m[blockIdx.z];
+  const int t = blockIdx.y;
+  const int tci = (m.Ci + 31) / 32;
+  const int ci0 = (blockIdx.x % tci) * 32, co0 = (blockIdx.x / tci) * 32;
+  if (t >= m.T || co0 >= m.Co) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int k = ty; k < 32; k += 8) {
+    const int co = co0 + k, ci = ci0 + tx;
+    if (co < m.Co && ci < m.Ci) {
+      const size_t i = ((size_t)co * m.T + t) * m.Ci + ci;
+      const float v = m.w[i];
+      m.wb[i] = __float2bfloat16_rn(v);
+      tile[k][tx] = v;
+    }
+  }
+  __syncthreads();
+  const int tt = m.flip ? m.T - 1 - t : t;
+  for (int k = ty; k < 32; k += 8) {
+    const int ci = ci0 + k, co = co0 + tx;
+    if (ci < m.Ci && co < m.Co) m.wt[((size_t)ci * m.T + tt) * m.Co + co] = __float2bfloat16_rn(tile[tx][k]);
   }
 }
 
@@ -750,8 +764,14 @@ int cnn_conv_weights_launch(const float* const* w, void* const* wb, void* const*
     mx = sz > mx ? sz : mx;
   }
   tab.n = n;
-  const int gx = (int)((mx + 255) / 256 < 1024 ? (mx + 255) / 256 : 1024);
-  cnn::conv_weights_kernel<<<dim3(gx, n), 256, 0, s>>>(tab);
+  int tiles = 0, tmax = 0;
+  for (int i = 0; i < n; ++i) {
+    const int tl = ((Ci[i] + 31) / 32) * ((Co[i] + 31) / 32);
+    tiles = tl > tiles ? tl : tiles;
+    tmax = T[i] > tmax ? T[i] : tmax;
+  }
+  (void)mx;
+  cnn::conv_weights_kernel<<<dim3(tiles, tmax, n), 256, 0, s>>>(tab);
   return ok_or_cuda_c();
 }
 
