@@ -77,6 +77,13 @@ class ClockSampler:
         except OSError:
             self.proc = None
         self.busy = []
+        self.first = ""
+        if self.proc is not None:  # let nvidia-smi finish starting up (driver queries) before anything is timed
+            import select
+
+            if select.select([self.proc.stdout], [], [], 15.0)[0]:
+                self.first = self.proc.stdout.readline()
+            time.sleep(0.2)
 
     def mark(self):
         self.busy.append(time.time())
@@ -86,6 +93,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
+        out = self.first + out
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
@@ -115,6 +123,27 @@ def ncu_traffic(kernel: str):
         return None
 
 
+class HostGate:
+    """Holds a stream at a device-side wait on a pinned host word until the host has enqueued the
+    whole timed region, so the CUDA-event span holds the kernels only -- not host scheduling jitter
+    between the first event and the launch (cuStreamWaitValue32 on mapped host memory)."""
+
+    def __init__(self):
+        self.word = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.np = self.word.numpy()
+        self.n = 0
+
+    def close(self, stream) -> None:
+        from paper_2208_14228_b200 import _native
+
+        self.n += 1
+        _native.check(_native.lib().bt_stream_wait_u32_geq(self.word.data_ptr(), self.n, stream.cuda_stream),
+                      "host gate")
+
+    def open(self) -> None:
+        self.np[0] = self.n
+
+
 # ------------------------------------------------------------------ b200 arm
 def make_cfg(bt):
     return bt.TrainRunConfig(seed=SEED, max_workers=E_TOTAL, micro_batch=MICRO, dataset_size=NROWS, lr=0.02,
@@ -132,28 +161,36 @@ def chunks(K: int, spe: int):
 
 
 def bench_device_single(bt, K: int, W: int, flush):
-    """N=1: persistent fused kernel, one launch per epoch-sized chunk."""
+    """N=1, inputs resident in HBM: the fused persistent kernel, one launch per chunk of at most
+    LAUNCH mini-batches (the prepared launch of run_steps, engine._FastStep), CUDA events on its
+    stream around each launch, L2 flushed before each launch (outside the span)."""
     from paper_2208_14228_b200 import _native, engine
-    from paper_2208_14228_b200.device import stream
 
     cfg = make_cfg(bt)
     ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")])
     for n in chunks(W, LAUNCH):
         engine.run_steps(ts, n)
     torch.cuda.synchronize()
+    fs = engine._fast(ts)
+    gate = HostGate()
     spans = []
     launches = 0
     s = torch.cuda.current_stream()
     for n in chunks(K, LAUNCH):
-        for st in range(n):
-            ts.pipeline.advance_all(ts.global_step + st)
-        losses = torch.empty((n, E_TOTAL), dtype=torch.float64, device="cuda")
-        a, keep = engine._step_args(ts, n, MICRO, None, losses, None)
+        ts.pipeline.advance_range(ts.global_step, n)
+        gs, spe = ts.global_step, ts.pipeline.steps_per_epoch
+        lists, base = ts.pipeline.device_lists(gs // spe, (gs + n - 1) // spe)
+        a = fs.a
+        a.K, a.step0, a.lists, a.epoch_base = n, gs, lists.data_ptr(), base
         flush()
+        gate.close(s)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()))
-        e1.record(s)
+        try:
+            e0.record(s)
+            _native.check(_native.lib().bt_mlp_step(C.byref(a), s.cuda_stream))
+            e1.record(s)
+        finally:
+            gate.open()
         launches += 1
         e1.synchronize()
         spans.append(e0.elapsed_time(e1))
@@ -165,65 +202,51 @@ def bench_device_single(bt, K: int, W: int, flush):
 
 
 def bench_e2e_single(bt, K: int, W: int, flush):
-    """N=1 end to end: host global batches -> pinned H2D -> fused kernel -> D2H losses, per launch.
-    The next launch's rows are copied on a second stream while the current launch computes (double-
-    buffered device rows); each timed span runs from before the wait on that launch's copy to after
-    its losses are back on the host, so every step's H2D and D2H is inside the timed region."""
-    from paper_2208_14228_b200 import _native, engine
-    from paper_2208_14228_b200.device import stream
+    """N=1 end to end through the public API (engine.run_steps, the K-mini-batch form of
+    run_minibatch), timed on the host clock: every launch starts from HOST inputs -- the epoch
+    index lists are recomputed (native Fisher-Yates, the reference's sampling.py:63-82) and copied
+    host->device inside the span -- and returns HOST outputs (per-EST losses + status, device->host,
+    stream synchronised) inside the span.  L2 flushed before each launch (outside the span)."""
+    from paper_2208_14228_b200 import engine
 
     cfg = make_cfg(bt)
     ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")])
-    # The user-side data: the reference pipeline's jittered rows for every step,
-    # laid out as split_by_rank global batches (row r of EST k at r*E+k).
-    total = W + K
-    host_rows = torch.empty((total, MICRO * E_TOTAL, 9), dtype=torch.float64).pin_memory()
-    pipe = bt.DataPipeline(SEED, NROWS, E_TOTAL, MICRO, 0.1, 2, 2)
-    for step in range(total):
-        for k in range(E_TOTAL):
-            for r, (x, y) in enumerate(pipe.batch(k, step)):
-                host_rows[step, r * E_TOTAL + k, :8] = torch.tensor(x, dtype=torch.float64)
-                host_rows[step, r * E_TOTAL + k, 8] = y
-    host_losses = torch.empty((total, E_TOTAL), dtype=torch.float64).pin_memory()
-    dev_rows = [torch.empty((LAUNCH, MICRO * E_TOTAL, 9), dtype=torch.float64, device="cuda") for _ in range(2)]
-    dev_losses = torch.empty((LAUNCH, E_TOTAL), dtype=torch.float64, device="cuda")
-    s = torch.cuda.current_stream()
-    cs = torch.cuda.Stream()
-    ready = [torch.cuda.Event() for _ in range(2)]
+    for n in chunks(W, LAUNCH):
+        engine.run_steps(ts, n)
+    torch.cuda.synchronize()
+    pipe = ts.pipeline
     spans, launches, h2d, d2h = [], 0, 0, 0
-    plan = [(False, n) for n in chunks(W, LAUNCH)] + [(True, n) for n in chunks(K, LAUNCH)]
-    starts = [sum(n for _, n in plan[:i]) for i in range(len(plan))]
+    losses = []
+    for n in chunks(K, LAUNCH):
+        flush()
+        pipe._lists_dev = None   # nothing of the inputs stays resident between launches
+        pipe._lists_host.clear()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out, _ = engine.run_steps(ts, n)
+        spans.append((time.perf_counter() - t0) * 1e3)
+        launches += 1
+        h2d += pipe._lists_dev.numel() * 4
+        d2h += out.size * 8 + 16
+        losses.append(out)
+    return ts, sum(spans), launches, h2d / K, d2h / K, np.concatenate(losses)
 
-    def prefetch(i):
-        if i < len(plan):
-            n, b = plan[i][1], i & 1
-            with torch.cuda.stream(cs):
-                dev_rows[b][:n].copy_(host_rows[starts[i]:starts[i] + n], non_blocking=True)
-                ready[b].record(cs)
 
-    prefetch(0)
-    for i, (timed, n) in enumerate(plan):
-        step0, b = starts[i], i & 1
-        if timed:
-            flush()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s)
-        s.wait_event(ready[b])
-        a, keep = engine._step_args(ts, n, MICRO, dev_rows[b], dev_losses, None)
-        _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()))
-        prefetch(i + 1)  # the next launch's rows stream in while this one computes
-        host_losses[step0:step0 + n].copy_(dev_losses[:n], non_blocking=True)
-        if timed:
-            e1.record(s)
-            e1.synchronize()
-            spans.append(e0.elapsed_time(e1))
-            launches += 1
-            h2d += host_rows[step0:step0 + n].numel() * 8
-            d2h += n * E_TOTAL * 8
-        else:
-            s.synchronize()
-        engine._finish_steps(ts, n)
-    return ts, sum(spans), launches, h2d / K, d2h / K, host_losses
+def bench_run_minibatch(bt, calls: int = 300, warm: int = 30):
+    """The reference API's per-step call (run_minibatch: one mini-batch, host losses back), wall
+    clock per call, median over `calls` calls."""
+    cfg = make_cfg(bt)
+    ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")])
+    for _ in range(warm):
+        bt.run_minibatch(ts)
+    times = []
+    for _ in range(calls):
+        t0 = time.perf_counter()
+        bt.run_minibatch(ts)
+        times.append((time.perf_counter() - t0) * 1e6)
+    return {"us_per_call": round(statistics.median(times), 2), "p10_us": round(sorted(times)[calls // 10], 2),
+            "p90_us": round(sorted(times)[calls * 9 // 10], 2), "calls": calls,
+            "samples_per_s": round(SAMPLES_PER_STEP / (statistics.median(times) / 1e6), 1)}
 
 
 def bench_device_dist(bt, K: int, W: int, rank: int, world: int, flush, e2e: bool, exchange: str):
@@ -379,7 +402,9 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
             key = next((k for k in ("gemm_bf16", "attn_fwd", "attn_bwd", "ln_fwd", "ln_bwd", "reduce", "colsum")
                         if k in ev.name), "other")
             split[key] = split.get(key, 0.0) + ev.device_time_total / 1e3
-    fnv_one = job.params.view(torch.int32).sum().item()
+    import paper_2208_14228_b200 as bt
+
+    fnv_one = f"{bt.fnv1a64(job.params.cpu().numpy().tobytes()):016x}"
     flops = job.gemm_flops_per_step()
     # the dominant kernel, per launch: the FFN forward GEMM (T x 3072 x 768, bias + GELU epilogue), timed
     # alone on its stream with CUDA events (inputs: layer 0's activations of the last step)
@@ -443,7 +468,20 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
                          "note": "L2 not flushed between the 20 back-to-back launches (55 MB of operands)"},
             "kernel_ms_per_step": {k: round(v, 3) for k, v in sorted(split.items(), key=lambda kv: -kv[1])},
             "bit_identical_groupings": {"groups": [[ests], [ests // 4] * 4], "layers": 2, "steps": 2, "equal": same},
-            "params_checksum": fnv_one}
+            "params_fnv": fnv_one}
+
+
+def replicas_identical(dist, data: bytes) -> tuple[bool, str]:
+    """Byte-level agreement of every rank's replica: FNV-1a of the bytes gathered from every rank
+    and the bytes themselves compared against rank 0's (no checksum that cancels)."""
+    import paper_2208_14228_b200 as bt
+
+    h = f"{bt.fnv1a64(data):016x}"
+    hs = [None] * dist.get_world_size()
+    dist.all_gather_object(hs, h)
+    blobs = [None] * dist.get_world_size()
+    dist.all_gather_object(blobs, data)
+    return len(set(hs)) == 1 and all(b == blobs[0] for b in blobs), h
 
 
 def bench_bert_dist(rank, world, dist, ests=32, steps=5, warmup=3, **model):
@@ -470,11 +508,7 @@ def bench_bert_dist(rank, world, dist, ests=32, steps=5, warmup=3, **model):
     t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = t.item()
-    chk = torch.tensor([float(job.params.view(torch.int32).to(torch.int64).sum().item())], dtype=torch.float64,
-                       device=dev)
-    lo, hi = chk.clone(), chk.clone()
-    dist.all_reduce(lo, op=dist.ReduceOp.MIN)
-    dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+    same, h = replicas_identical(dist, job.params.cpu().numpy().tobytes())
     torch.cuda.synchronize()
     dist.barrier()
     job.peer.close()
@@ -483,7 +517,7 @@ def bench_bert_dist(rank, world, dist, ests=32, steps=5, warmup=3, **model):
     return {"workload": "C4: BERT-base encoder bf16, 32 ESTs x 8 sequences, EST blocks per GPU, peer-memory "
                         "RankTree(2) reducer (BASELINE.json configs[3])",
             "samples_per_s": round(ests * model.get("seqs", 8) / (ms / 1e3), 1), "unit": "sequences/s",
-            "ms_per_step": round(ms, 3), "n_gpus": world, "ests_per_gpu": n, "replicas_bit_identical": bool(lo.item() == hi.item())}
+            "ms_per_step": round(ms, 3), "n_gpus": world, "ests_per_gpu": n, "replicas_bit_identical": same, "params_fnv": h}
 
 
 def bench_resnet_dist(rank, world, dist, ests=16, batch=32, steps=10, warmup=3):
@@ -509,11 +543,7 @@ def bench_resnet_dist(rank, world, dist, ests=16, batch=32, steps=10, warmup=3):
     t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = t.item()
-    chk = torch.tensor([float(job.params.view(torch.int32).to(torch.int64).sum().item())], dtype=torch.float64,
-                       device=dev)
-    lo, hi = chk.clone(), chk.clone()
-    dist.all_reduce(lo, op=dist.ReduceOp.MIN)
-    dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+    same, h = replicas_identical(dist, job.params.cpu().numpy().tobytes())
     torch.cuda.synchronize()
     dist.barrier()
     job.peer.close()
@@ -522,7 +552,7 @@ def bench_resnet_dist(rank, world, dist, ests=16, batch=32, steps=10, warmup=3):
     return {"workload": "C3: ResNet-18 with per-EST BatchNorm, 16 ESTs x 32 images, EST blocks (and their BN slots) "
                         "per GPU, peer-memory RankTree(2) reducer (BASELINE.json configs[2])",
             "samples_per_s": round(ests * batch / (ms / 1e3), 1), "unit": "images/s", "ms_per_step": round(ms, 3),
-            "n_gpus": world, "ests_per_gpu": n, "replicas_bit_identical": bool(lo.item() == hi.item())}
+            "n_gpus": world, "ests_per_gpu": n, "replicas_bit_identical": same, "params_fnv": h}
 
 
 def bench_resnet(peaks, ests=16, batch=32, steps=10, warmup=3):
@@ -657,6 +687,51 @@ def config_block(n):
                 f"each launch = {LAUNCH} mini-batches" if n == 1 else "each timed span = one epoch of 32 mini-batches")}
 
 
+# Critical-path (latency) floor of one C2 mini-batch in the fused step kernel: the dependent
+# chain every mini-batch must traverse, priced with latencies measured on the B200
+# (tools/ubench*.cu), in SM cycles.
+LATENCY_FLOOR_CYCLES = {
+    "pre-activation chain (1 DMUL + 8 dependent DADD)": 72,
+    "glibc tanh (branch-free form)": 550,
+    "hidden -> shared -> warp (store, syncwarp, load)": 60,
+    "output fold (16 dependent DADD) + error + gy": 152,
+    "dz (3 DMUL + DSUB) + CTA barrier": 82,
+    "gradient fold (loads + DMUL + 2-level tree)": 54,
+    "one DSMEM slot exchange hop (st.async + mbarrier)": 500,
+    "allreduce fold (loads + 3-level tree) + /E": 62,
+    "momentum SGD (2 DMUL + DADD + DSUB) + commit barrier": 82,
+}
+
+
+def latency_floor(us_per_step: float, sm_mhz: float | None) -> dict:
+    cyc = sum(LATENCY_FLOOR_CYCLES.values())
+    mhz = sm_mhz or 1965.0
+    floor_us = cyc / mhz
+    return {"bound": "latency", "floor_us_per_step": round(floor_us, 3), "achieved_us_per_step": round(us_per_step, 3),
+            "frac": round(floor_us / us_per_step, 4), "floor_cycles": cyc, "sm_mhz": mhz,
+            "chain": LATENCY_FLOOR_CYCLES}
+
+
+def _spawn_ranks(n: int) -> int:
+    """`--gpus N` without a launcher: re-run this command under torch.distributed.run with N
+    local ranks (127.0.0.1 rendezvous); rank 0 prints the line."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def _rank_device(local: int) -> tuple[int, bool]:
+    """(device index, shared): ranks beyond the visible GPU count share devices (tests on one GPU)."""
+    n = torch.cuda.device_count()
+    return local % n, n < int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -671,6 +746,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -679,25 +756,34 @@ def main():
 
     import paper_2208_14228_b200 as bt
 
-    torch.cuda.set_device(local)
+    devidx, shared = _rank_device(local)
+    torch.cuda.set_device(devidx)
     dist = None
+    hdev = "cuda"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:  # several ranks on one GPU (tests): NCCL refuses duplicate GPUs, gloo carries the host values
+            dist.init_process_group("gloo")
+            hdev = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", devidx))
     peaks, peak_src = load_peaks()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(devidx)
     flush_buf = torch.zeros(64 * 2**20, dtype=torch.float32, device="cuda")
 
     def flush():
         flush_buf.add_(1)
 
+    rmb = None
     if world == 1:
         ts, ms, spans, launches, epc = bench_device_single(bt, args.steps, args.warmup, flush)
         final = np.array(ts.executors[0].model.values.tolist())
         ts_e, ms_e2e, launches_e, h2d, d2h, _ = bench_e2e_single(bt, args.steps, args.warmup, flush)
         final_e = np.array(ts_e.executors[0].model.values.tolist())
         assert np.array_equal(final.view(np.uint64), final_e.view(np.uint64)), "e2e and device runs diverged"
+        rmb = bench_run_minibatch(bt)
+        exchange = None
     else:
         exchange = args.exchange
         try:
@@ -713,14 +799,13 @@ def main():
                                                                    True, exchange)
         epc = E_TOTAL // world
     if world > 1:
-        t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=hdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, ms_e2e = t.tolist()
     weights_fnv = f"{bt.fnv1a64(final.astype('<f8').tobytes()):016x}"
     if world > 1:
-        allh = [None] * world
-        dist.all_gather_object(allh, weights_fnv)
-        assert len(set(allh)) == 1, f"ranks disagree: {allh}"
+        same, _ = replicas_identical(dist, final.astype("<f8").tobytes())
+        assert same, "ranks hold different weights"
 
     value = args.steps * SAMPLES_PER_STEP / (ms / 1e3)
     e2e = args.steps * SAMPLES_PER_STEP / (ms_e2e / 1e3)
@@ -751,23 +836,30 @@ def main():
     per_launch_ms = ms / launches
     steps_per_launch = args.steps / launches
     achieved = alg_step * steps_per_launch / (per_launch_ms / 1e3) / 1e9
+    us_step = ms * 1e3 / args.steps
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 42)",
         "config": config_block(world),
-        "e2e": {"value": round(e2e, 1), "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": round(e2e, 1), "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "timing": "host clock around engine.run_steps (epoch lists recomputed on the host and copied "
+                          "H2D, losses + status copied D2H, stream synchronised, all inside the span)"
+                          if world == 1 else "CUDA events around the distributed steps"},
         "gpu_launches": launches,
         "roofline": {"kernel": "mlp_step_spec_kernel<8,8,2> (bt_mlp.cu: E=8, 8-CTA cluster, Tree(2))", "bound": "hbm", "achieved": round(achieved, 3),
                      "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 6),
                      "traffic": ncu_traffic("mlp_step_kernel"), "peak_source": peak_src,
                      "note": "latency-bound: one mini-batch is a ~1 kflop/sample dependent fp64 chain over 32 "
-                             "samples; HBM and tensor rooflines do not bind (DESIGN.md section 5)",
-                     "us_per_step": round(ms * 1e3 / args.steps, 3), "est_per_cta": epc},
+                             "samples; HBM and tensor rooflines do not bind -- see `latency` (DESIGN.md section 3.1)",
+                     "us_per_step": round(us_step, 3), "est_per_cta": epc,
+                     "latency": latency_floor(us_step, clk.get("sm_mhz"))},
         "weights_fnv": weights_fnv,  # FNV-1a of the final weights: equal for every N (bit-identical mappings)
         "clocks": clk,
     }
-    if world > 1:
+    if rmb is not None:
+        line["run_minibatch"] = rmb
+    if exchange is not None:
         line["config"]["exchange"] = exchange
     if reducer is not None:
         line["reducer"] = reducer

@@ -86,9 +86,14 @@ int bt_fwd_bwd_mlp_f64(const double *params_dev, const double *rows_dev, int32_t
  * variant, rank-keyed) -> /E -> momentum SGD -> mirror to every replica.
  *                                                           engine.py:271-329 */
 int bt_mlp_step(const bt_mlp_args *args, void *stream);
+/* bt_mlp_step, then the K x E_total per-EST losses and the 4-word status block copied into
+ * caller-owned HOST buffers and the stream synchronised: the whole of one run_minibatch /
+ * run_steps call in one entry point (losses_host may be NULL).         engine.py:271-329 */
+int bt_mlp_run(const bt_mlp_args *args, double *losses_host, int32_t *status_host, void *stream);
 /* Same launch with per-stage clock64 sums accumulated into timing_dev[0..4]
  * (rows+tanh, output chain, gradients, allreduce fold, update) and the step
- * count into timing_dev[5] (profiling; thread 0 of CTA 0's view). */
+ * count into timing_dev[5]; the compact build also adds its prologue, epilogue and whole-CTA
+ * cycles into timing_dev[9..11] (profiling; thread 0 of CTA 0's view; 16 words). */
 int bt_mlp_step_profiled(const bt_mlp_args *args, uint64_t *timing_dev, void *stream);
 /* 1 when the fused (fuse_reduce = 1) step fits on chip for these args (E_total
  * slots in shared memory), else 0: use grads-only + bt_reduce_update. */

@@ -83,6 +83,7 @@ EXPORTS = {
     "bt_fwd_bwd_mlp_f64": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _dbl, _i64, _vp, _vp, _vp, _vp,
                                      _vp, _vp, _vp]),
     "bt_mlp_step": (C.c_int, [C.POINTER(MlpArgs), _vp]),
+    "bt_mlp_run": (C.c_int, [C.POINTER(MlpArgs), _vp, _vp, _vp]),
     "bt_mlp_step_profiled": (C.c_int, [C.POINTER(MlpArgs), _vp, _vp]),
     "bt_mlp_fused_fits": (C.c_int, [C.POINTER(MlpArgs)]),
     "bt_mlp_pick_est_per_cta": (C.c_int, [_i32, _i32]),

@@ -285,6 +285,23 @@ int bt_mlp_step(const bt_mlp_args* args, void* stream) {
   return done(bt::mlp_launch(*args, STREAM(stream)), "bt_mlp_step");
 }
 
+int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_host, void* stream) {
+  int st = validate_mlp(args);
+  if (st) return st;
+  if (!status_host) return fail(bt::ERR_INPUT, "bt_mlp_run needs a status buffer");
+  st = bt::mlp_launch(*args, STREAM(stream));
+  if (st) return done(st, "bt_mlp_run");
+  cudaStream_t s = STREAM(stream);
+  if (losses_host && cudaMemcpyAsync(losses_host, args->losses, sizeof(double) * (size_t)args->K * args->E_total,
+                                     cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return cuda_fail("bt_mlp_run losses");
+  if (cudaMemcpyAsync(status_host, args->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return cuda_fail("bt_mlp_run status");
+  if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail("bt_mlp_run sync");
+  g_err[0] = 0;
+  return 0;
+}
+
 int bt_mlp_step_profiled(const bt_mlp_args* args, uint64_t* timing_dev, void* stream) {
   int st = validate_mlp(args);
   if (st) return st;

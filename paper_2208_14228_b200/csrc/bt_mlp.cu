@@ -196,6 +196,28 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Bulk copy global -> this CTA's shared memory, counted on its mbarrier (16-byte aligned sizes).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+// Bulk copy global -> the same shared offset in every CTA of `mask`, counted on each CTA's mbarrier
+// (the same offset too).  bytes and both addresses 16-byte aligned.
+__device__ __forceinline__ void bulk_multicast(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "h"(mask)
+      : "memory");
+}
 // DSMEM store into a cluster peer that also counts 8 bytes on the peer's mbarrier
 __device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t remote_bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(addr), "d"(v),
@@ -674,16 +696,31 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
   int32_t* const s_rot = (int32_t*)(sm + S::ROT);
   uint64_t* const s_rng = (uint64_t*)(sm + S::RNG);
   uint64_t* const s_cnt = (uint64_t*)(sm + S::CNT);
-  __shared__ __align__(8) uint64_t s_mbar[2];
+  __shared__ __align__(8) uint64_t s_mbar[3];  // [0], [1]: slot exchange by step parity; [2]: dataset
+  const long long t_entry = clock64();
 
-  if (a.flags[FLAG_STATUS] != 0) return;
+  // ---- prologue: everything below is issued at once and overlaps ---------
+  // Sampler mode: the resident dataset arrives in one bulk copy per CTA (the copy engine streams
+  // it while the threads fetch the parameters, slots and index lists); the cluster barrier that
+  // orders every CTA's mbarrier initialisation before the first DSMEM push is split around the
+  // prologue (arrive now, wait before the loop), so it costs nothing on the critical path.
+  const int64_t nd_bytes = a.rows ? 0 : a.dataset_rows * BT_ROW * (int64_t)sizeof(double);
+  const bool bulk = nd_bytes > 0 && (nd_bytes & 15) == 0 && (((uintptr_t)a.dataset) & 15) == 0 &&
+                    nd_bytes < (1 << 20);
   if (tid == 0) {  // a phase completes when every local thread arrived and every remote byte landed
     mbar_init(smem_u32(&s_mbar[0]), S::T);
     mbar_init(smem_u32(&s_mbar[1]), S::T);
+    mbar_init(smem_u32(&s_mbar[2]), 1);
     mbar_init_fence();
+    if (bulk) {
+      const uint32_t bar = smem_u32(&s_mbar[2]);
+      mbar_arrive_expect_tx(bar, (uint32_t)nd_bytes);
+      bulk_g2s(smem_u32(s_data), a.dataset, (uint32_t)nd_bytes, bar);
+    }
   }
-  // ---- prologue ---------------------------------------------------------
-  int bad = 0;
+  cluster_arrive();
+  const long long t_p0 = clock64();
+  int bad = a.flags[FLAG_STATUS] != 0 ? 4 : 0;  // a sticky earlier failure: do nothing
   for (int i = tid; i < BT_P; i += S::T) {
     const double p0 = a.replicas[i], v0 = a.replicas[BT_P + i];
     sm[S::PAR + i] = p0;
@@ -698,8 +735,12 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
     s_rng[el] = a.rng[e0 + el];
     sm[S::MEAN + el] = a.stat_mean[e0 + el];
     s_cnt[el] = a.stat_count[e0 + el];
-    bad |= (a.est_fanin[e0 + el] != F) << 1;  // the launcher's variant hint must hold
   }
+  // the launcher's variant hint must hold -- checked for every EST in every CTA, so the whole
+  // cluster takes the same exit
+  for (int e = tid; e < ET; e += S::T) bad |= (a.est_fanin[e] != F) << 1;
+  const long long t_p1 = clock64();
+  long long t_p2 = t_p1;
   if (a.rows) {
     for (int it = tid; it < a.K * S::R; it += S::T) {
       const int s = it / S::R, rem = it - s * S::R;
@@ -711,32 +752,49 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
       s_jit[it] = 0.0;
     }
   } else {
-    const int64_t nd = a.dataset_rows * BT_ROW;
-    for (int64_t i = tid; i < nd; i += S::T) s_data[i] = a.dataset[i];
-  }
-  for (int it = tid; !a.rows && it < a.K * S::R; it += S::T) {
-    const int s = it / S::R, rem = it - s * S::R;
-    const int el = rem / S::NB, r = rem - el * S::NB;
-    const int64_t gstep = a.step0 + s, epoch = gstep / a.spe, local = gstep % a.spe;
-    const int eg = e0 + el;
-    const int32_t* lst = a.lists + ((size_t)(epoch - a.epoch_base) * ET + eg) * (size_t)(a.spe * S::NB);
-    s_idx[it] = lst[local * S::NB + r];
-    double ju = 0.0;
-    if (a.jitter != 0.0) {  // one uniform per row of worker_rng(seed, epoch, local, est) (sampling.py:99-170)
-      const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)epoch, (uint64_t)local, (uint64_t)eg);
-      ju = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), a.jitter);
+    if (!bulk) {
+      const int64_t nd = a.dataset_rows * BT_ROW;
+      for (int64_t i = tid; i < nd; i += S::T) s_data[i] = a.dataset[i];
     }
-    s_jit[it] = ju;
+    // (epoch, local step) of mini-batch s: one 64-bit division per thread, then 32-bit steps
+    const int64_t ep0 = a.step0 / a.spe;
+    const int spe = (int)a.spe, loc0 = (int)(a.step0 - ep0 * a.spe);
+#pragma unroll 4
+    for (int it = tid; it < a.K * S::R; it += S::T) {  // index loads only: independent, batched
+      const int s = it / S::R, rem = it - s * S::R;
+      const int el = rem / S::NB, r = rem - el * S::NB;
+      const int q = loc0 + s, de = q / spe, local = q - de * spe;
+      const int32_t* lst = a.lists + ((size_t)(ep0 + de - a.epoch_base) * ET + (e0 + el)) * (size_t)(spe * S::NB);
+      s_idx[it] = lst[local * S::NB + r];
+    }
+    t_p2 = clock64();
+    for (int it = tid; it < a.K * S::EPC; it += S::T) {  // one worker stream per (mini-batch, EST)
+      const int s = it / S::EPC, el = it - s * S::EPC;
+      const int q = loc0 + s, de = q / spe, local = q - de * spe;
+      double* jd = s_jit + (size_t)s * S::R + el * S::NB;
+      if (a.jitter != 0.0) {  // one uniform per row of worker_rng(seed, epoch, local, est) (sampling.py:99-170)
+        const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)(ep0 + de), (uint64_t)local, (uint64_t)(e0 + el));
+#pragma unroll
+        for (int r = 0; r < S::NB; ++r) jd[r] = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), a.jitter);
+      } else {
+#pragma unroll
+        for (int r = 0; r < S::NB; ++r) jd[r] = 0.0;
+      }
+    }
   }
+  const long long t_p3 = clock64();
+  if (bulk) mbar_wait(smem_u32(&s_mbar[2]), 0, a.flags);  // the dataset has landed (also before any exit)
+  const long long t_p4 = clock64();
   const int prologue = __syncthreads_or(bad);
-  if (prologue) {
-    if (cta == 0 && tid == 0) {
+  const long long t_p5 = clock64();
+  cluster_wait();  // every CTA's mbarriers are initialised (and every CTA took the same branch below)
+  if (prologue) {  // identical in every CTA of the cluster
+    if (cta == 0 && tid == 0 && !(prologue & 4)) {
       a.flags[FLAG_STATUS] = (prologue & 1) ? ERR_CORRUPTION : ERR_INPUT;
       a.flags[FLAG_STEP] = 0;
     }
     return;
   }
-  cluster_barrier();  // every peer's mbarriers are initialised before the first push
 
   // ---- per-thread constants ----------------------------------------------
   const double rate = a.rate, lr = a.lr, mu = a.mu;
@@ -812,6 +870,7 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
 
   unsigned long long tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tlast = clock64();
+  const long long t_loop = tlast;
   int cur = 0, s = 0;
   for (; s < a.K; ++s) {
     const int par = (int)((a.step0 + s) & 1);
@@ -946,13 +1005,12 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
     if (a.param_trace && cta == 0 && tid < BT_P) a.param_trace[(size_t)s * BT_P + tid] = np;
     BT_TICK(4)
   }
-  if (L.timing && tid == 0 && cta == 0) {
-    for (int k = 0; k < 5; ++k) L.timing[k] += tacc[k];
-    L.timing[5] += (unsigned long long)s;
-  }
+  const long long t_loop_end = clock64();
 
   // ---- epilogue -----------------------------------------------------------
-  cluster_barrier();
+  // (every DSMEM push addressed to this CTA has landed -- its own mbarrier said so; the split
+  // cluster barrier keeps each CTA resident until its peers are past their last push as well)
+  cluster_arrive();
   for (int el = tid; el < S::EPC; el += S::T) {
     a.rng[e0 + el] = s_rng[el];
     a.stat_mean[e0 + el] = sm[S::MEAN + el];
@@ -967,9 +1025,28 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
       }
     }
   }
+  cluster_wait();
+  if (L.timing && tid == 0 && cta == 0) {  // [9] prologue, [10] epilogue, [11] whole CTA (cycles)
+    for (int k = 0; k < 5; ++k) L.timing[k] += tacc[k];
+    L.timing[5] += (unsigned long long)s;
+    const long long t_exit = clock64();
+    L.timing[9] += (unsigned long long)(t_loop - t_entry);
+    L.timing[10] += (unsigned long long)(t_exit - t_loop_end);
+    L.timing[11] += (unsigned long long)(t_exit - t_entry);
+    // prologue detail: [6] init+issue, [7] params/slots loads, [8] index loads, [12] jitter,
+    // [13] dataset wait, [14] CTA barrier, [15] cluster wait
+    L.timing[6] += (unsigned long long)(t_p0 - t_entry);
+    L.timing[7] += (unsigned long long)(t_p1 - t_p0);
+    L.timing[8] += (unsigned long long)(t_p2 - t_p1);
+    L.timing[12] += (unsigned long long)(t_p3 - t_p2);
+    L.timing[13] += (unsigned long long)(t_p4 - t_p3);
+    L.timing[14] += (unsigned long long)(t_p5 - t_p4);
+    L.timing[15] += (unsigned long long)(t_loop - t_p5);
+  }
 }
 
 static constexpr size_t SMEM_LIMIT = 220 * 1024;
+static constexpr int SPEC_KCAP = 128;
 
 static size_t base_smem_bytes(const bt_mlp_args& a) {
   const size_t rows = (size_t)a.est_per_cta * a.B;
@@ -1086,9 +1163,15 @@ template <int ET, int G>
 static size_t spec_smem(const bt_mlp_args& a) {
   using S = SpecShape<ET, G>;
   const size_t data_rows = a.rows ? (size_t)a.K * S::R : (size_t)a.dataset_rows;
+  // sampler mode: the per-launch (index, jitter) staging is sized for at least SPEC_KCAP
+  // mini-batches, so launches of different lengths share one shared-memory configuration
+  const size_t kst = a.rows ? (size_t)a.K : (size_t)(a.K > SPEC_KCAP ? a.K : SPEC_KCAP);
   const size_t bytes = S::fixed_bytes() + sizeof(double) * data_rows * BT_ROW +
+                       (sizeof(double) + sizeof(int32_t)) * kst * S::R;
+  if (bytes <= SMEM_LIMIT) return bytes;
+  const size_t exact = S::fixed_bytes() + sizeof(double) * data_rows * BT_ROW +
                        (sizeof(double) + sizeof(int32_t)) * (size_t)a.K * S::R;
-  return bytes <= SMEM_LIMIT ? bytes : 0;
+  return exact <= SMEM_LIMIT ? exact : 0;
 }
 
 template <int ET, int G>

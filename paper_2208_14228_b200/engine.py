@@ -242,6 +242,7 @@ class TrainingState:
     epoch: int = 0
     rebuild_pending: bool = False
     dev: DeviceState | None = None
+    _fast: object = field(default=None, repr=False, compare=False)  # prepared launch (_FastStep)
 
     @property
     def max_workers(self) -> int:
@@ -434,6 +435,55 @@ def _finish_steps(ts: TrainingState, nsteps: int) -> None:
         ts.rebuild_pending = False
 
 
+def _raw_stream() -> int:
+    return torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())
+
+
+class _FastStep:
+    """The sampler-mode launch of run_minibatch / run_steps, prepared once per TrainingState:
+    the argument block with its fixed pointers, and pinned host buffers that bt_mlp_run fills
+    with the per-EST losses and the status words (one C-ABI call and one sync per call)."""
+
+    KMAX = 128
+
+    def __init__(self, ts: TrainingState):
+        cfg = ts.cfg
+        self.E = cfg.max_workers
+        self.fits = _fused_fits(cfg)
+        self.losses = torch.empty((self.KMAX, self.E), dtype=torch.float64, device="cuda")
+        self.host_losses = torch.empty((self.KMAX, self.E), dtype=torch.float64).pin_memory()
+        self.host_status = torch.zeros(4, dtype=torch.int32).pin_memory()
+        self.status_np = self.host_status.numpy()
+        self.losses_np = self.host_losses.numpy()
+        self.a, self.keep = _step_args(ts, 1, cfg.micro_batch, None, self.losses, None) if self.fits else (None, [])
+        self.dev = ts.dev
+
+    def run(self, ts: TrainingState, K: int) -> int:
+        """Launch K mini-batches from ts.global_step; returns the device status word."""
+        a = self.a
+        gs = ts.global_step
+        spe = ts.pipeline.steps_per_epoch
+        lists, base = ts.pipeline.device_lists(gs // spe, (gs + K - 1) // spe)
+        self.keep = [lists]
+        rot = _rot_tensor(ts)
+        ex0 = ts.executors[0]
+        a.K, a.step0, a.lists, a.epoch_base = K, gs, lists.data_ptr(), base
+        a.rot = ptr(rot)
+        a.lr, a.mu = float(ex0._lr), float(ex0._mu)
+        st = _native.lib().bt_mlp_run(C.byref(a), self.host_losses.data_ptr(), self.host_status.data_ptr(),
+                                      _raw_stream())
+        _native.check(st, "run_minibatch")
+        self.dev.invalidate()
+        return int(self.status_np[0])
+
+
+def _fast(ts: TrainingState) -> _FastStep:
+    fs = ts._fast
+    if fs is None or fs.dev is not ts.dev:
+        fs = ts._fast = _FastStep(ts)
+    return fs
+
+
 def run_minibatch(ts: TrainingState, global_batch: Batch | None = None) -> list[float]:
     """One mini-batch; returns per-EST losses by ascending rank (engine.py:271-329)."""
     cfg = ts.cfg
@@ -446,6 +496,15 @@ def run_minibatch(ts: TrainingState, global_batch: Batch | None = None) -> list[
     else:
         B = cfg.micro_batch
         ts.pipeline.advance_all(ts.global_step)
+        if globals()["allreduce"] is _DEVICE_ALLREDUCE:
+            fs = _fast(ts)
+            if fs.fits:
+                st = fs.run(ts, 1)
+                if st:
+                    _raise_step_error(ts, st, int(fs.status_np[1]), "run_minibatch")
+                out = fs.losses_np[0].tolist()
+                _finish_steps(ts, 1)
+                return out
     if globals()["allreduce"] is not _DEVICE_ALLREDUCE or not _fused_fits(cfg, B):
         # spied allreduce seam, or too many ESTs for on-chip slots: kernels per seam
         return _run_minibatch_unfused(ts, B, rows)
@@ -512,6 +571,21 @@ def run_steps(ts: TrainingState, K: int, trace: bool = False):
     E = cfg.max_workers
     gs = ts.global_step
     ts.pipeline.advance_all(gs)  # progress check (ProgressError) before anything runs
+    if not trace and K <= _FastStep.KMAX:
+        fs = _fast(ts)
+        st = fs.run(ts, K)
+        failed = int(fs.status_np[2])
+        out = fs.losses_np[:K].copy()
+    else:
+        out, st, failed = None, None, 0
+    if st is not None:
+        done = K if not st else (failed if st == 5 else 0)
+        ts.pipeline.advance_range(gs + 1, min(K, done + (1 if st == 5 else 0)) - 1)
+        if st:
+            _finish_steps(ts, done)
+            _raise_step_error(ts, st, int(fs.status_np[1]), f"run_steps (mini-batch {ts.global_step})")
+        _finish_steps(ts, K)
+        return out, None
     losses = torch.empty((K, E), dtype=torch.float64, device="cuda")
     tr = torch.empty((K, P), dtype=torch.float64, device="cuda") if trace else None
     a, keep = _step_args(ts, K, cfg.micro_batch, None, losses, tr)

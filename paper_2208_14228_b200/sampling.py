@@ -99,7 +99,7 @@ def worker_rng(seed: int, epoch: int, local_step: int, worker_index: int) -> int
 class DataPipeline:
     """Shared data-worker pool with a progress-ordered queuing buffer."""
 
-    EPOCH_WINDOW = 4  # epochs of index lists kept resident on the device
+    EPOCH_WINDOW = 2  # epochs of index lists uploaded together (the current one and the next)
 
     def __init__(self, seed: int, dataset_size: int, total_workers: int, micro_batch: int, jitter: float = 0.0,
                  worker_slots: int = 1, prefetch_depth: int = 2, shuffle: bool = True):
@@ -119,8 +119,13 @@ class DataPipeline:
         if self.steps_per_epoch < 1:
             raise ConfigError("dataset smaller than one global batch")
         self._dataset_dev = None
-        self._queue: dict[tuple[int, int], WorkerState] = {}
+        # The queuing buffer (sampling.py:138-144, 188-197), kept lazily: the states a worker
+        # prefetched itself are a pure function of their key, so only their extent is stored
+        # (`_ahead[w]`: last prefetched mini-batch); states restored from a checkpoint are kept
+        # verbatim in `_explicit` (they may be foreign and are checked when consumed).
+        self._explicit: dict[tuple[int, int], WorkerState] = {}
         self._next_step = [0] * total_workers
+        self._ahead = [-1] * total_workers
         self._lists_host: dict[int, np.ndarray] = {}
         self._lists_dev: torch.Tensor | None = None
         self._lists_dev_base = -1
@@ -151,9 +156,9 @@ class DataPipeline:
         """Resident [n_epochs][workers][spe*B] lists covering [first, last]; returns (tensor, base epoch)."""
         if not (self._lists_dev is not None and self._lists_dev_base <= first_epoch
                 and last_epoch < self._lists_dev_base + self._lists_dev_count):
-            count = max(last_epoch - first_epoch + 1, min(self.EPOCH_WINDOW, last_epoch - first_epoch + 1))
-            host = np.stack([self._lists_for_epoch(e) for e in range(first_epoch, first_epoch + count)])
-            self._lists_dev = torch.from_numpy(host).to("cuda")
+            count = max(last_epoch - first_epoch + 1, self.EPOCH_WINDOW)  # the next epoch rides along
+            host = torch.from_numpy(np.stack([self._lists_for_epoch(e) for e in range(first_epoch, first_epoch + count)]))
+            self._lists_dev = host.pin_memory().to("cuda", non_blocking=True)  # stream-ordered, no host sync
             self._lists_dev_base, self._lists_dev_count = first_epoch, count
         return self._lists_dev, self._lists_dev_base
 
@@ -169,14 +174,14 @@ class DataPipeline:
             raise ProgressError(f"mini-batch {minibatch_idx} of worker {worker} was already consumed")
         if minibatch_idx > expected:
             raise ProgressError(f"worker {worker} must consume mini-batch {expected} before {minibatch_idx}")
-        ws = self._queue.pop((minibatch_idx, worker), None)
-        if ws is None:
+        ws = self._explicit.pop((minibatch_idx, worker), None)
+        if ws is not None:
+            self._check_state(ws)
+        else:  # prefetched earlier or made now: the same state either way
             ws = self._make_state(minibatch_idx, worker)
         self._next_step[worker] = minibatch_idx + 1
-        for ahead in range(1, self.prefetch_depth + 1):
-            key = (minibatch_idx + ahead, worker)
-            if key not in self._queue:
-                self._queue[key] = self._make_state(*key)
+        if minibatch_idx + self.prefetch_depth > self._ahead[worker]:
+            self._ahead[worker] = minibatch_idx + self.prefetch_depth
         return ws
 
     def _check_state(self, ws: WorkerState) -> None:
@@ -188,8 +193,7 @@ class DataPipeline:
 
     def batch(self, worker: int, minibatch_idx: int) -> list[Row]:
         """Produce and consume the micro-batch for (minibatch_idx, worker) (sampling.py:174-198)."""
-        ws = self._consume(worker, minibatch_idx)
-        self._check_state(ws)
+        self._consume(worker, minibatch_idx)
         epoch, local = divmod(minibatch_idx, self.steps_per_epoch)
         lists, base = self.device_lists(epoch, epoch)
         rows = torch.empty((self.micro_batch, INPUT_DIM + 1), dtype=torch.float64, device="cuda")
@@ -202,15 +206,38 @@ class DataPipeline:
     def advance_all(self, minibatch_idx: int) -> None:
         """Consume (minibatch_idx, w) for every worker without producing host rows:
         the step kernel gathers them on the device.  Same progress/queue semantics as batch()."""
+        nxt = self._next_step
         for w in range(self.total_workers):  # validate first so a failure leaves no partial progress
-            if self._next_step[w] != minibatch_idx:
+            if nxt[w] != minibatch_idx:
                 self._consume(w, minibatch_idx)  # raises the reference's ProgressError
-        for w in range(self.total_workers):
-            self._check_state(self._consume(w, minibatch_idx))
+        if self._explicit:
+            for w in range(self.total_workers):
+                self._consume(w, minibatch_idx)
+            return
+        self._next_step = [minibatch_idx + 1] * self.total_workers
+        ahead = minibatch_idx + self.prefetch_depth
+        self._ahead = [a if a > ahead else ahead for a in self._ahead]
+
+    def advance_range(self, first: int, count: int) -> None:
+        """advance_all for mini-batches first .. first+count-1 (one persistent launch's worth)."""
+        if self._explicit or count < 1 or any(n != first for n in self._next_step):
+            for k in range(count):
+                self.advance_all(first + k)
+            return
+        self._next_step = [first + count] * self.total_workers
+        ahead = first + count - 1 + self.prefetch_depth
+        self._ahead = [a if a > ahead else ahead for a in self._ahead]
 
     def drain_for_checkpoint(self) -> list[WorkerState]:
-        return [self._queue[k] for k in sorted(self._queue)]
+        """Every queued state in (mini-batch, worker) order (sampling.py:200-202)."""
+        q = dict(self._explicit)
+        for w in range(self.total_workers):
+            for step in range(self._next_step[w], self._ahead[w] + 1):
+                if (step, w) not in q:
+                    q[(step, w)] = self._make_state(step, w)
+        return [q[k] for k in sorted(q)]
 
     def restore_queue(self, states: list[WorkerState], next_step: int) -> None:
-        self._queue = {(ws.minibatch_idx, ws.worker_index): ws for ws in states}
+        self._explicit = {(ws.minibatch_idx, ws.worker_index): ws for ws in states}
         self._next_step = [next_step] * self.total_workers
+        self._ahead = [-1] * self.total_workers

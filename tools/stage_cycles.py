@@ -37,4 +37,5 @@ for shape in SHAPES:
     per = [x / n for x in t[:5]]
     print(f"E={E} B={B} K={K} epc={a.est_per_cta}: launch {ev0.elapsed_time(ev1) * 1e3:.1f} us, "
           f"{sum(per):.0f} cyc/step: " + ", ".join(f"{nm} {v:.0f}" for nm, v in zip(names, per))
-          + f" | B detail (thread 0): idx {t[8] / n:.0f}, loads+preact {t[6] / n:.0f}, tanh {t[7] / n:.0f}")
+          + f" | prologue detail: init {t[6]}, params {t[7]}, idx {t[8]}, jitter {t[12]}, data wait {t[13]}, bar {t[14]}, cluster {t[15]}"
+          + f" | prologue {t[9]} cyc, epilogue {t[10]} cyc, CTA total {t[11]} cyc = {t[11] / 1965:.2f} us @1965")
