@@ -23,7 +23,8 @@ BT_P = 161
 BT_MAX_TABLE = 64
 BT_MAX_REPLICA_OUT = 8
 DTYPE_F64, DTYPE_F32 = 0, 1
-REDUCE_UPDATE, REDUCE_MEAN_ONLY, REDUCE_SUM_ONLY, REDUCE_ADAM = 0, 1, 2, 3
+REDUCE_UPDATE, REDUCE_MEAN_ONLY, REDUCE_SUM_ONLY, REDUCE_ADAM, REDUCE_MEAN_CHECK = 0, 1, 2, 3, 4
+REDUCE_APPLY_SGD, REDUCE_APPLY_ADAM = 5, 6
 
 STATUS_TO_ERROR = {
     1: errors.InputError,
@@ -61,6 +62,7 @@ class ReduceArgs(C.Structure):
         ("lr", _dbl), ("mu", _dbl), ("flags", _vp),
         ("vel2", _vp), ("vel2_out", _vp), ("extra_vel2_out", _vp * BT_MAX_REPLICA_OUT),
         ("beta2", _dbl), ("eps", _dbl), ("bc1", _dbl), ("bc2", _dbl),
+        ("stage", _vp), ("gate", _vp), ("ngate", _i32), ("pad_", _i32),
     ]
 
 
@@ -139,6 +141,7 @@ EXPORTS = {
     "bt_replica_check": (C.c_int, [C.POINTER(_vp), _i32, _i64, _vp, _vp]),
     "bt_est_slot_copy": (C.c_int, [C.POINTER(_vp), C.POINTER(_vp), _i64p, _i32, _vp]),
     "bt_allgather_params": (C.c_int, [_i32, _vp, C.POINTER(_vp), _i32, _i64, _vp]),
+    "bt_memcpy_async": (C.c_int, [_vp, _vp, _i64, _vp]),
     "bt_flags_reset": (C.c_int, [_vp, _vp]),
     "bt_step_status": (C.c_int, [_vp, _i32p, _i32p, _vp]),
     "bt_ipc_handle_size": (C.c_int, []),

@@ -358,6 +358,13 @@ class BertJob:
             self.flags.reset()
             raise NumericError("bert: non-finite synchronized gradient")
 
+    def _stage(self) -> torch.Tensor:
+        """Staging buffer of the guarded update (the synchronized gradients, checked before any write)."""
+        st = getattr(self, "_stage_buf", None)
+        if st is None or st.numel() != self.P:
+            st = self._stage_buf = torch.empty(self.P, dtype=torch.float32, device="cuda")
+        return st
+
     def attach_peer(self, group=None):
         """Multi-GPU (one process per GPU, torch.distributed initialised, rank r holding the r-th contiguous
         EST block): the exchange becomes paper_2208_14228_b200.peer.PeerGroupReducer over CUDA IPC --
@@ -388,6 +395,7 @@ class BertJob:
         p, v = self.params.data_ptr(), self.vel.data_ptr()
         a.param, a.vel, a.param_out, a.vel_out = p, v, p, v
         a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
+        a.stage = self._stage().data_ptr()  # guarded: a non-finite step changes nothing (model.py:207-209)
         if self.adam is not None:
             t = self.step_idx + 1
             a.mode = _native.REDUCE_ADAM

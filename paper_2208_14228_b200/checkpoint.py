@@ -69,8 +69,10 @@ class _Cursor:
         return out
 
 
-def decode_esck(data: bytes) -> dict:
-    """Parse and validate ESCK bytes; FormatError carries the defect's byte offset."""
+def decode_esck(data: bytes, cfg: TrainRunConfig | None = None) -> dict:
+    """Parse and validate ESCK bytes; FormatError carries the defect's byte offset.  With `cfg`, the
+    run-configuration checks fire where the reference's reader makes them (checkpoint.py:152-177):
+    the determinism flags right after they are read, the context count right after it is read."""
     cur = _Cursor(bytes(data))
     (magic,) = cur.read("<4s")
     if magic != MAGIC:
@@ -88,6 +90,8 @@ def decode_esck(data: bytes) -> dict:
         raise FormatError(f"velocity count {nv} != parameter count", cur.pos - 4)
     velocity = list(cur.read(f"<{nv}d"))
     flags = tuple(bool(f) for f in cur.read("<BBB"))
+    if cfg is not None and flags != (cfg.determinism.d0, cfg.determinism.d1, cfg.determinism.d2):
+        raise ConfigError("checkpoint determinism flags do not match the run configuration")
     bucket_map = None
     if flags[1]:
         capacity, nb = cur.read("<II")
@@ -99,6 +103,8 @@ def decode_esck(data: bytes) -> dict:
         if not bucket_map.covered_exactly_once():
             raise FormatError("bucket map does not partition the parameters", cur.pos)
     (nctx,) = cur.read("<I")
+    if cfg is not None and nctx != cfg.max_workers:
+        raise ConfigError(f"checkpoint holds {nctx} worker contexts, run expects {cfg.max_workers}")
     contexts = [cur.read("<IQdQQ") for _ in range(nctx)]
     contexts_pos = cur.pos
     (nq,) = cur.read("<I")
@@ -137,7 +143,7 @@ def checkpoint_save(ts: TrainingState) -> bytes:
 
 def checkpoint_restore(data: bytes, layout: list[ExecutorSpec], cfg: TrainRunConfig) -> TrainingState:
     """Rebuild a device training state on a (possibly different) layout (checkpoint.py:122-238)."""
-    doc = decode_esck(data)
+    doc = decode_esck(data, cfg)
     mode = cfg.determinism
     if doc["flags"] != (mode.d0, mode.d1, mode.d2):
         raise ConfigError("checkpoint determinism flags do not match the run configuration")

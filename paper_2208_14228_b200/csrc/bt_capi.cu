@@ -484,7 +484,14 @@ int bt_reduce_update(const bt_reduce_args* a, void* stream) {
   if (a->fanin < 0 || a->fanin == 1) return fail(bt::ERR_CONFIG, "bad fanin %d", a->fanin);
   if (a->n < 0) return fail(bt::ERR_INPUT, "negative length");
   if (a->nout < 0 || a->nout > BT_MAX_REPLICA_OUT) return fail(bt::ERR_INPUT, "nout outside [0, 8]");
-  if (a->mode < BT_REDUCE_UPDATE || a->mode > BT_REDUCE_ADAM) return fail(bt::ERR_INPUT, "bad mode %d", a->mode);
+  if (a->mode < BT_REDUCE_UPDATE || a->mode > BT_REDUCE_APPLY_ADAM) return fail(bt::ERR_INPUT, "bad mode %d", a->mode);
+  if (a->mode == BT_REDUCE_MEAN_CHECK && !a->flags) return fail(bt::ERR_INPUT, "MEAN_CHECK needs the flags");
+  if ((a->mode == BT_REDUCE_APPLY_SGD || a->mode == BT_REDUCE_APPLY_ADAM) &&
+      (!a->stage || !a->param || !a->vel || !a->vel_out || !a->flags))
+    return fail(bt::ERR_INPUT, "APPLY needs stage, param, vel and flags");
+  if (a->mode == BT_REDUCE_APPLY_ADAM && (!a->vel2 || !a->vel2_out))
+    return fail(bt::ERR_INPUT, "Adam needs the second-moment buffers");
+  if (a->ngate < 0 || (a->ngate > 0 && !a->gate)) return fail(bt::ERR_INPUT, "bad gate table");
   if (a->divisor < 0) return fail(bt::ERR_INPUT, "negative divisor");
   const bool upd = a->mode == BT_REDUCE_UPDATE || a->mode == BT_REDUCE_ADAM;
   if (!a->param_out || (upd && (!a->param || !a->vel || !a->vel_out || !a->flags)))
@@ -559,6 +566,14 @@ int bt_allgather_params(int32_t dtype, const void* src_dev, void* const* dst_dev
   return bt_est_slot_copy(dst_dev, srcs, bytes, ndst, stream);
 }
 
+int bt_memcpy_async(void* dst, const void* src, int64_t nbytes, void* stream) {
+  if (nbytes < 0) return fail(bt::ERR_INPUT, "negative byte count");
+  if (nbytes == 0) return 0;
+  if (cudaMemcpyAsync(dst, src, (size_t)nbytes, cudaMemcpyDefault, STREAM(stream)) != cudaSuccess)
+    return cuda_fail("bt_memcpy_async");
+  return 0;
+}
+
 int bt_flags_reset(int32_t* flags_dev, void* stream) {
   return done(bt::flags_reset_launch(flags_dev, STREAM(stream)), "bt_flags_reset");
 }
@@ -620,10 +635,21 @@ int bt_stream_write_u32(void* dev_ptr, uint32_t value, void* stream) {
     return fail(bt::ERR_CUDA, "cuStreamWriteValue32 failed");
   return 0;
 }
+typedef int (*PFN_deviceGetAttribute)(int*, int, int);
 int bt_stream_wait_u32_geq(void* dev_ptr, uint32_t value, void* stream) {
   static PFN_streamWaitValue32 fn = driver_fn<PFN_streamWaitValue32>("cuStreamWaitValue32");
+  static PFN_deviceGetAttribute attr = driver_fn<PFN_deviceGetAttribute>("cuDeviceGetAttribute");
   if (!fn) return fail(bt::ERR_CUDA, "cuStreamWaitValue32 unavailable");
-  if (fn(stream, (unsigned long long)dev_ptr, value, 0 /*CU_STREAM_WAIT_VALUE_GEQ*/) != 0)
+  // The wait is followed by reads of data other GPUs wrote to this one (peer stores, IPC): where
+  // the device supports it, CU_STREAM_WAIT_VALUE_FLUSH makes those remote writes visible first.
+  static int flush = -1;
+  if (flush < 0) {
+    int dev = 0, can = 0;
+    cudaGetDevice(&dev);
+    flush = (attr && attr(&can, 98 /*CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES*/, dev) == 0 && can) ? 1 : 0;
+  }
+  const unsigned flags = 0u /*CU_STREAM_WAIT_VALUE_GEQ*/ | (flush ? (1u << 30) /*CU_STREAM_WAIT_VALUE_FLUSH*/ : 0u);
+  if (fn(stream, (unsigned long long)dev_ptr, value, flags) != 0)
     return fail(bt::ERR_CUDA, "cuStreamWaitValue32 failed");
   return 0;
 }

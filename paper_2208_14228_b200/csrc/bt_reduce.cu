@@ -57,6 +57,9 @@ __device__ __forceinline__ void adam_elem(const bt_reduce_args& a, T g, T m, T s
   *po = A::sub(p, A::mul((T)a.lr, A::div(A::mul(m1, (T)a.bc1), den)));
 }
 
+template <typename T>
+__device__ __forceinline__ void update_elem(const bt_reduce_args& a, int64_t p, T g);
+
 // Apply /E, finite check and the update for one element.
 template <typename T>
 __device__ __forceinline__ void finish_elem(const bt_reduce_args& a, int64_t p, T sum) {
@@ -65,11 +68,18 @@ __device__ __forceinline__ void finish_elem(const bt_reduce_args& a, int64_t p, 
     return;
   }
   const T g = Arith<T>::div(sum, (T)(a.divisor > 0 ? a.divisor : a.E));
-  if (a.mode == BT_REDUCE_MEAN_ONLY) {
+  if (a.mode == BT_REDUCE_MEAN_ONLY || a.mode == BT_REDUCE_MEAN_CHECK) {
+    if (a.mode == BT_REDUCE_MEAN_CHECK && !finite_v(g)) flag_numeric(a.flags, p);
     ((T*)a.param_out)[p] = g;
     return;
   }
   if (!finite_v(g)) flag_numeric(a.flags, p);
+  update_elem<T>(a, p, g);
+}
+
+// The update of one element from its synchronized gradient g (momentum SGD or Adam) + replicas.
+template <typename T>
+__device__ __forceinline__ void update_elem(const bt_reduce_args& a, int64_t p, T g) {
   if (a.mode == BT_REDUCE_ADAM) {
     T m, s2, np;
     adam_elem<T>(a, g, ((const T*)a.vel)[p], ((const T*)a.vel2)[p], ((const T*)a.param)[p], &m, &s2, &np);
@@ -113,6 +123,9 @@ template <typename V>
 __device__ __forceinline__ V ld_stream(const V* p) { return __ldcs(p); }
 template <typename V>
 __device__ __forceinline__ void st_stream(V* p, const V& v) { __stcs(p, v); }
+
+template <typename T>
+__device__ __forceinline__ void update_vec(const bt_reduce_args& a, int64_t i, const typename Vec16<T>::type& g);
 
 // E in {1,2,4,...,64}; F == 0 (Sequential) or F == 2 (unrotated Tree(2)).
 template <typename T, int E, int F>
@@ -173,11 +186,37 @@ __global__ void __launch_bounds__(256) reduce_fast_kernel(const __grid_constant_
       set_lane(g, w, gw);
       fin = fin && finite_v(gw);
     }
-    if (a.mode == BT_REDUCE_MEAN_ONLY) {
+    if (a.mode == BT_REDUCE_MEAN_ONLY || a.mode == BT_REDUCE_MEAN_CHECK) {
+      if (a.mode == BT_REDUCE_MEAN_CHECK && !fin) flag_numeric(a.flags, i * W);
       st_stream((V*)a.param_out + i, g);
       continue;
     }
     if (!fin) flag_numeric(a.flags, i * W);
+    update_vec<T>(a, i, g);
+  }
+  // scalar tail (n % W elements)
+  if (blockIdx.x == 0) {
+    for (int64_t p = nv * W + threadIdx.x; p < a.n; p += blockDim.x) {
+      T acc = ((const T*)a.grads[0])[p];
+      if (F == 0) {
+        for (int k = 1; k < E; ++k) acc = Arith<T>::add(acc, ((const T*)a.grads[k])[p]);
+      } else {
+        T v[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) v[k] = ((const T*)a.grads[k])[p];
+        acc = TreeLevel<E, 2>::run(v);
+      }
+      finish_elem<T>(a, p, acc);
+    }
+  }
+}
+
+// The update of 16 bytes of elements from their synchronized gradients g, + replicas.
+template <typename T>
+__device__ __forceinline__ void update_vec(const bt_reduce_args& a, int64_t i, const typename Vec16<T>::type& g) {
+  using V = typename Vec16<T>::type;
+  constexpr int W = Vec16<T>::W;
+  {
     const V pv = ld_stream((const V*)a.param + i);
     const V vv = ld_stream((const V*)a.vel + i);
     V nv_, np_;
@@ -200,7 +239,7 @@ __global__ void __launch_bounds__(256) reduce_fast_kernel(const __grid_constant_
         st_stream((V*)a.extra_vel_out[r] + i, nv_);
         st_stream((V*)a.extra_vel2_out[r] + i, ns_);
       }
-      continue;
+      return;
     }
 #pragma unroll
     for (int w = 0; w < W; ++w) {
@@ -215,20 +254,38 @@ __global__ void __launch_bounds__(256) reduce_fast_kernel(const __grid_constant_
       st_stream((V*)a.extra_vel_out[r] + i, nv_);
     }
   }
-  // scalar tail (n % W elements)
-  if (blockIdx.x == 0) {
-    for (int64_t p = nv * W + threadIdx.x; p < a.n; p += blockDim.x) {
-      T acc = ((const T*)a.grads[0])[p];
-      if (F == 0) {
-        for (int k = 1; k < E; ++k) acc = Arith<T>::add(acc, ((const T*)a.grads[k])[p]);
-      } else {
-        T v[E];
-#pragma unroll
-        for (int k = 0; k < E; ++k) v[k] = ((const T*)a.grads[k])[p];
-        acc = TreeLevel<E, 2>::run(v);
-      }
-      finish_elem<T>(a, p, acc);
-    }
+}
+
+// Pass 2 of a guarded update: the update from the staged synchronized gradients, applied only
+// when this update's status (and every other rank's published status) is clean.
+__device__ __forceinline__ bool gate_open(const bt_reduce_args& a) {
+  if (a.flags[FLAG_STATUS] != 0) return false;
+  for (int i = 0; i < a.ngate; ++i)
+    if (((volatile const int32_t*)a.gate)[i] != 0) return false;
+  return true;
+}
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(256) reduce_apply_kernel(const __grid_constant__ bt_reduce_args a) {
+  __shared__ int s_open;
+  if (threadIdx.x == 0) {
+    s_open = gate_open(a);
+    if (!s_open && blockIdx.x == 0 && a.flags[FLAG_STATUS] == 0)
+      atomicCAS(a.flags + FLAG_STATUS, 0, (int)ERR_NUMERIC);  // another rank's shard was not finite
+  }
+  __syncthreads();
+  if (!s_open) return;
+  using V = typename Vec16<T>::type;
+  constexpr int W = Vec16<T>::W;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (VEC) {
+    const int64_t nv = a.n / W;
+    for (int64_t i = t0; i < nv; i += stride) update_vec<T>(a, i, ld_stream((const V*)a.stage + i));
+    if (blockIdx.x == 0)
+      for (int64_t p = nv * W + threadIdx.x; p < a.n; p += blockDim.x) update_elem<T>(a, p, ((const T*)a.stage)[p]);
+  } else {
+    for (int64_t p = t0; p < a.n; p += stride) update_elem<T>(a, p, ((const T*)a.stage)[p]);
   }
 }
 
@@ -300,9 +357,44 @@ static cudaError_t reduce_launch_t(const bt_reduce_args& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <typename T>
+static cudaError_t apply_launch_t(const bt_reduce_args& a, cudaStream_t s) {
+  bool vec = aligned16(a.stage) && aligned16(a.param) && aligned16(a.vel) && aligned16(a.param_out) &&
+             aligned16(a.vel_out);
+  for (int r = 0; r < a.nout; ++r) vec = vec && aligned16(a.extra_param_out[r]) && aligned16(a.extra_vel_out[r]);
+  if (a.mode == BT_REDUCE_ADAM) {
+    vec = vec && aligned16(a.vel2) && aligned16(a.vel2_out);
+    for (int r = 0; r < a.nout; ++r) vec = vec && aligned16(a.extra_vel2_out[r]);
+  }
+  int64_t blocks = (a.n / (vec ? Vec16<T>::W : 1) + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  if (vec) reduce_apply_kernel<T, true><<<(unsigned)blocks, 256, 0, s>>>(a);
+  else reduce_apply_kernel<T, false><<<(unsigned)blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 int reduce_launch(const bt_reduce_args& a, cudaStream_t s) {
   if (a.n == 0) return OK;
-  const cudaError_t e = a.dtype == BT_DTYPE_F64 ? reduce_launch_t<double>(a, s) : reduce_launch_t<float>(a, s);
+  const bool f64 = a.dtype == BT_DTYPE_F64;
+  if (a.mode == BT_REDUCE_APPLY_SGD || a.mode == BT_REDUCE_APPLY_ADAM) {  // pass 2 of a multi-rank guard
+    bt_reduce_args p2 = a;
+    p2.mode = a.mode == BT_REDUCE_APPLY_ADAM ? BT_REDUCE_ADAM : BT_REDUCE_UPDATE;
+    const cudaError_t e = f64 ? apply_launch_t<double>(p2, s) : apply_launch_t<float>(p2, s);
+    return e == cudaSuccess ? OK : ERR_CUDA;
+  }
+  if (a.stage && (a.mode == BT_REDUCE_UPDATE || a.mode == BT_REDUCE_ADAM)) {  // guarded: check, then apply
+    bt_reduce_args p1 = a;
+    p1.mode = BT_REDUCE_MEAN_CHECK;
+    p1.param_out = a.stage;
+    p1.nout = 0;
+    cudaError_t e = f64 ? reduce_launch_t<double>(p1, s) : reduce_launch_t<float>(p1, s);
+    if (e != cudaSuccess) return ERR_CUDA;
+    e = f64 ? apply_launch_t<double>(a, s) : apply_launch_t<float>(a, s);
+    return e == cudaSuccess ? OK : ERR_CUDA;
+  }
+  const cudaError_t e = f64 ? reduce_launch_t<double>(a, s) : reduce_launch_t<float>(a, s);
   return e == cudaSuccess ? OK : ERR_CUDA;
 }
 

@@ -10,7 +10,10 @@ extern "C" {
 #define BT_MAX_REPLICA_OUT 8
 
 enum { BT_DTYPE_F64 = 0, BT_DTYPE_F32 = 1 };
-enum { BT_REDUCE_UPDATE = 0, BT_REDUCE_MEAN_ONLY = 1, BT_REDUCE_SUM_ONLY = 2, BT_REDUCE_ADAM = 3 };
+enum { BT_REDUCE_UPDATE = 0, BT_REDUCE_MEAN_ONLY = 1, BT_REDUCE_SUM_ONLY = 2, BT_REDUCE_ADAM = 3,
+       BT_REDUCE_MEAN_CHECK = 4, /* MEAN_ONLY + the non-finite flag (pass 1 of a guarded update) */
+       BT_REDUCE_APPLY_SGD = 5,  /* pass 2 alone: momentum SGD from `stage`, gated (multi-rank guard) */
+       BT_REDUCE_APPLY_ADAM = 6  /* pass 2 alone: Adam from `stage`, gated */ };
 
 /* out[p] = reduce_sum(g[(rot[p]+k) % E][p] for k in 0..E-1, fanin) / E   (buckets.py:115-123)
  * then, in BT_REDUCE_UPDATE mode, v' = mu*v + out; p' = p - lr*v'      (model.py:206-212);
@@ -47,6 +50,16 @@ typedef struct bt_reduce_args {
   void *vel2_out;     /* second-moment output; may alias vel2 */
   void *extra_vel2_out[BT_MAX_REPLICA_OUT];
   double beta2, eps, bc1, bc2;
+  /* Guarded update (UPDATE / ADAM): when `stage` [n] is non-NULL nothing is written unless every
+   * synchronized gradient of the update is finite -- the reference's sgd_step raises before it
+   * mutates anything (model.py:207-209).  Pass 1 folds, divides and checks into `stage`; pass 2
+   * applies the update only if flags[0] == 0 and every gate[i] (i < ngate) is 0 (gate: the
+   * status words other ranks published for their shards of the same update; NULL when the whole
+   * update is local).  A gated-off pass 2 marks flags NUMERIC so every rank raises. */
+  void *stage;
+  const int32_t *gate;
+  int32_t ngate;
+  int32_t pad_;
 } bt_reduce_args;
 
 #ifdef __cplusplus

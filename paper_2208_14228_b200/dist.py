@@ -92,7 +92,7 @@ class DistributedTrainer:
         self.xchg = SlotExchange(self.E, PARAM_COUNT, group)
         self.params = torch.zeros((2, PARAM_COUNT), dtype=torch.float64, device="cuda")
         self.params[0] = ToyModel.init_random(seed).tensor
-        self.new = torch.empty_like(self.params)
+        self.stage = torch.empty(PARAM_COUNT, dtype=torch.float64, device="cuda")  # guarded update
         self.fan = torch.full((self.count,), fanin, dtype=torch.int32, device="cuda")
         self.rng = torch.tensor([u64_to_i64(derive_stream(TAG_DROPOUT, seed, self.base + k))
                                  for k in range(self.count)], dtype=torch.int64, device="cuda")
@@ -150,10 +150,10 @@ class DistributedTrainer:
         r.grads[0], r.grads_ld = self.grads_all.data_ptr(), PARAM_COUNT
         r.rot = self.rot.data_ptr() if self.rot is not None else None
         r.param, r.vel = self.params[0].data_ptr(), self.params[1].data_ptr()
-        r.param_out, r.vel_out = self.new[0].data_ptr(), self.new[1].data_ptr()
+        r.param_out, r.vel_out = r.param, r.vel  # in place, guarded: nothing changes on a non-finite step
+        r.stage = self.stage.data_ptr()
         r.lr, r.mu, r.flags = self.lr, self.mu, self.flags.t.data_ptr()
         _native.check(_native.lib().bt_reduce_update(C.byref(r), stream()), "reduce_update")
-        self.params.copy_(self.new)
         self.step_idx += 1
         return self.losses
 

@@ -89,7 +89,13 @@ class GroupReducer:
                 if r.partial is None:
                     r.partial = torch.empty_like(r.param)
         self.shards = shard_bounds(self.n, self.G, 16 // ranks[0].param.element_size())
-        self.flags = [Flags() for _ in ranks]
+        self.flags = []
+        self.stage, self.gate = [], []
+        for r, (lo, hi) in zip(ranks, self.shards):  # per rank: status, staged shard gradients, gate table
+            with torch.cuda.device(r.param.device):
+                self.flags.append(Flags())
+                self.stage.append(torch.empty(max(hi - lo, 1), dtype=r.param.dtype, device=r.param.device))
+                self.gate.append(torch.zeros(self.G, dtype=torch.int32, device=r.param.device))
         self.es = ranks[0].param.element_size()
 
     def _dtype_code(self) -> int:
@@ -110,7 +116,7 @@ class GroupReducer:
                     e = torch.cuda.Event()
                     e.record(r.stream)
                     ev1.append(e)
-        ev2 = []
+        evp, pending = [], []
         for g, r in enumerate(self.ranks):  # phase 2: shard owners
             lo, hi = self.shards[g]
             with torch.cuda.stream(r.stream):
@@ -138,12 +144,33 @@ class GroupReducer:
                         a.extra_param_out[i] = self.ranks[q].param.data_ptr() + off
                         a.extra_vel_out[i] = self.ranks[q].vel.data_ptr() + off
                     a.lr, a.mu, a.flags = self.lr, self.mu, self.flags[g].t.data_ptr()
-                    _native.check(_native.lib().bt_reduce_update(C.byref(a), r.stream.cuda_stream), "owner")
+                    # pass 1: fold, /E, finite check of the shard into the staging buffer
+                    a.mode, a.param_out, a.stage = _native.REDUCE_MEAN_CHECK, self.stage[g].data_ptr(), self.stage[g].data_ptr()
+                    nout, a.nout = a.nout, 0
+                    _native.check(_native.lib().bt_reduce_update(C.byref(a), r.stream.cuda_stream), "owner check")
+                    a.mode, a.param_out, a.nout = _native.REDUCE_APPLY_SGD, a.param, nout
+                    a.gate, a.ngate = self.gate[g].data_ptr(), G
+                    pending.append((g, a))
+                for q in range(G):  # publish the shard's status word into every rank's gate table
+                    _native.check(_native.lib().bt_memcpy_async(self.gate[q].data_ptr() + 4 * g,
+                                                                self.flags[g].t.data_ptr(), 4, r.stream.cuda_stream),
+                                  "publish status")
                 e = torch.cuda.Event()
                 e.record(r.stream)
-                ev2.append(e)
+                evp.append(e)
+        for g, a in pending:  # pass 2: the update, only if every shard was finite
+            r = self.ranks[g]
+            with torch.cuda.stream(r.stream):
+                for e in evp:
+                    r.stream.wait_event(e)
+                _native.check(_native.lib().bt_reduce_update(C.byref(a), r.stream.cuda_stream), "owner apply")
+        ev2 = []
+        for r in self.ranks:
+            e = torch.cuda.Event()
+            e.record(r.stream)
+            ev2.append(e)
         for r in self.ranks:  # every replica complete before a rank's next kernels
-            for e in ev2:
+            for e in ev2 + evp:
                 r.stream.wait_event(e)
 
     def check(self) -> None:

@@ -9,8 +9,13 @@ maps every peer's.  A step is then (hier.GroupReducer's schedule, per rank):
   wait     every peer's sig[0] >= step  (cuStreamWaitValue32 -- the GPU front
            end blocks the stream; no host barrier, no spinning kernel)
   phase 2  owner of shard g: peer LOADS of the G partials (or all E slots for
-           owner-computes) over NVLink, fixed rank-order fold, /E, momentum SGD,
-           peer STORES of the updated shard into every replica
+           owner-computes) over NVLink, fixed rank-order fold, /E and the finite
+           check into a staging buffer; the shard's status word is published into
+           every rank's gate table (signal / wait sig[2]); then, only if every
+           shard of the update was finite, momentum SGD (or Adam) from the staged
+           gradients with peer STORES of the updated shard into every replica
+           (the reference raises NumericError before it mutates anything,
+           model.py:207-209, so a non-finite step leaves every replica as it was)
   signal   own sig[1] = step; wait every peer's sig[1] >= step
 
 so the reduce-scatter, update and parameter all-gather are one kernel per rank
@@ -61,7 +66,7 @@ class _Opened:
 class PeerGroupReducer:
     """This rank's side of a G-rank deterministic reduce over CUDA IPC (see module doc)."""
 
-    NAMES = ("grads", "partial", "param", "vel", "sig")
+    NAMES = ("grads", "partial", "param", "vel", "sig", "gate")
 
     def __init__(self, local: RankBuffers, E: int, variant: str = "rank_tree2", rot: torch.Tensor | None = None,
                  lr: float = 0.02, mu: float = 0.9, group=None, divisor: int = 0, adam: tuple | None = None):
@@ -86,18 +91,23 @@ class PeerGroupReducer:
             raise ConfigError(f"owner-computes reads at most {_native.BT_MAX_TABLE} slots per element")
         if local.partial is None:
             local.partial = torch.empty_like(local.param)
-        self.sig = torch.zeros(2, dtype=torch.int32, device=local.param.device)
+        self.sig = torch.zeros(3, dtype=torch.int32, device=local.param.device)
+        self.gate = torch.zeros(self.G, dtype=torch.int32, device=local.param.device)  # every shard's status
         self.n, self.es = local.param.numel(), local.param.element_size()
         self.dtype = _native.DTYPE_F64 if local.param.dtype == torch.float64 else _native.DTYPE_F32
         self.shards = shard_bounds(self.n, self.G, 16 // self.es)
-        mine = {k: _export(getattr(self, k) if k == "sig" else getattr(local, k)) for k in self.NAMES}
+        lo, hi = self.shards[self.rank]
+        self.stage = torch.empty(max(hi - lo, 1), dtype=local.param.dtype, device=local.param.device)
+        own = ("sig", "gate")
+        mine = {k: _export(getattr(self, k) if k in own else getattr(local, k)) for k in self.NAMES}
         table = [None] * self.G
         dist.all_gather_object(table, mine, group=group)
         self.opened = _Opened()
         self.ptrs = []
         for q in range(self.G):
             if q == self.rank:
-                self.ptrs.append({k: (self.sig if k == "sig" else getattr(local, k)).data_ptr() for k in self.NAMES})
+                self.ptrs.append({k: (getattr(self, k) if k in own else getattr(local, k)).data_ptr()
+                                  for k in self.NAMES})
             else:
                 self.ptrs.append({k: self.opened.ptr(*table[q][k]) for k in self.NAMES})
         self.flags = Flags()
@@ -155,7 +165,21 @@ class PeerGroupReducer:
                 a.beta2, a.eps = b2, eps
                 a.bc1, a.bc2 = 1.0 / (1.0 - self.mu ** self.step_no), 1.0 / (1.0 - b2 ** self.step_no)
             a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
-            _native.check(_native.lib().bt_reduce_update(C.byref(a), s), "owner")
+            # pass 1: fold, /E and the finite check of this shard into the staging buffer
+            upd = a.mode
+            a.mode, a.param_out, a.stage = _native.REDUCE_MEAN_CHECK, self.stage.data_ptr(), self.stage.data_ptr()
+            nout, a.nout = a.nout, 0
+            _native.check(_native.lib().bt_reduce_update(C.byref(a), s), "owner check")
+            a.mode = _native.REDUCE_APPLY_ADAM if upd == _native.REDUCE_ADAM else _native.REDUCE_APPLY_SGD
+            a.param_out, a.nout = a.param, nout
+        # publish this shard's status word into every rank's gate table, then wait for every shard's
+        for q in range(self.G):
+            _native.check(_native.lib().bt_memcpy_async(self.ptrs[q]["gate"] + 4 * self.rank, self.flags.t.data_ptr(),
+                                                        4, s), "publish status")
+        self._signal_and_wait(2)
+        if hi > lo:  # pass 2: the update, only if every shard of the update was finite
+            a.gate, a.ngate = self.gate.data_ptr(), self.G
+            _native.check(_native.lib().bt_reduce_update(C.byref(a), s), "owner apply")
         self._signal_and_wait(1)
 
     def check(self) -> None:

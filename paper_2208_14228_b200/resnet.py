@@ -480,6 +480,7 @@ class ResNetJob:
             p, v = self.params.data_ptr(), self.vel.data_ptr()
             a.param, a.vel, a.param_out, a.vel_out = p, v, p, v
             a.lr, a.mu, a.flags = self.lr, self.mu, self.flags.t.data_ptr()
+            a.stage = self._stage().data_ptr()  # guarded: a non-finite step changes nothing (model.py:207-209)
             _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()), "resnet reduce_update")
         self._refresh_bf16()
 
@@ -500,6 +501,13 @@ class ResNetJob:
         for cv in self.convs:
             f += 6.0 * self.En * self.B * cv.hout ** 2 * cv.co * (cv.taps * (3 if cv.name == "stem" else cv.ci))
         return f
+
+    def _stage(self) -> torch.Tensor:
+        """Staging buffer of the guarded update (the synchronized gradients, checked before any write)."""
+        st = getattr(self, "_stage_buf", None)
+        if st is None or st.numel() != self.P:
+            st = self._stage_buf = torch.empty(self.P, dtype=torch.float32, device="cuda")
+        return st
 
     def attach_peer(self, group=None):
         """Multi-GPU (one process per GPU, torch.distributed initialised, rank r holding the r-th contiguous

@@ -107,6 +107,26 @@ def test_esck_errors_carry_offsets():
         ck.decode_esck(bytes(bad))
 
 
+def test_esck_config_errors_fire_where_the_reference_reads_them():
+    """checkpoint.py:152-177: a flag mismatch or a context-count mismatch is a ConfigError even when
+    the bytes after it are malformed (the reference raises before parsing further)."""
+    b = next(x for x in load("checkpoint.json")["blobs"] if x["mode"] != "d0")
+    blob = bytes.fromhex(b["blob"])
+    doc = ck.decode_esck(blob)
+    cfg = bt.TrainRunConfig(seed=42, max_workers=b["workers"], determinism=bt.DeterminismMode.from_label(b["mode"]))
+    other = bt.DeterminismMode.from_label("d0" if b["mode"] != "d0" else "d1")
+    cfg_flags = bt.TrainRunConfig(seed=42, max_workers=b["workers"], determinism=other)
+    cfg_count = bt.TrainRunConfig(seed=42, max_workers=b["workers"] + 1, determinism=cfg.determinism)
+    assert ck.decode_esck(blob, cfg)["global_step"] == doc["global_step"]
+    truncated = blob[: len(blob) - 40]  # a defect after the context count
+    with pytest.raises(bt.FormatError):
+        ck.decode_esck(truncated, cfg)
+    with pytest.raises(bt.ConfigError):
+        ck.decode_esck(truncated, cfg_flags)
+    with pytest.raises(bt.ConfigError):
+        ck.decode_esck(truncated, cfg_count)
+
+
 def test_runlog_roundtrip_and_bitdiff(tmp_path):
     import math
 

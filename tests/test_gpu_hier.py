@@ -65,3 +65,28 @@ def test_group_reducer_repeated_steps_stay_identical(oracle):
     torch.cuda.synchronize()
     for r in ranks:
         assert np.array_equal(r.param.cpu().numpy(), p) and np.array_equal(r.vel.cpu().numpy(), v)
+
+
+@pytest.mark.parametrize("variant", ["rank_tree2", "sequential"])
+def test_group_reducer_non_finite_leaves_every_replica(variant):
+    """A non-finite synchronized gradient in ONE rank's shard: no rank commits its shard (the shard
+    status words are exchanged before the update), every replica keeps its bytes, every rank raises."""
+    from paper_2208_14228_b200.errors import NumericError
+    from paper_2208_14228_b200.hier import GroupReducer, RankBuffers
+
+    E, G, n = 8, 4, 10_000
+    grads = adversarial(E, n, 12, np.float32)
+    grads[5, 9_001] = np.inf  # lands in the last rank's parameter shard
+    p = adversarial(1, n, 13, np.float32)[0]
+    v = adversarial(1, n, 14, np.float32)[0]
+    ranks = [RankBuffers(torch.from_numpy(grads[g * 2:(g + 1) * 2].copy()).cuda(), torch.from_numpy(p.copy()).cuda(),
+                         torch.from_numpy(v.copy()).cuda(), torch.cuda.Stream()) for g in range(G)]
+    red = GroupReducer(ranks, E, variant, None, 0.1, 0.9)
+    red.step()
+    torch.cuda.synchronize()
+    for r in ranks:
+        assert np.array_equal(r.param.cpu().numpy(), p) and np.array_equal(r.vel.cpu().numpy(), v)
+    for f in red.flags:
+        assert f.status()[0] == 5
+    with pytest.raises(NumericError):
+        red.check()

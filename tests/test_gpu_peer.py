@@ -25,7 +25,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, variant, q):
+def _worker(rank, world, port, variant, q, nonfinite=False):
     import sys
     from pathlib import Path
 
@@ -39,7 +39,7 @@ def _worker(rank, world, port, variant, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        _run(rank, world, variant, q, dist, RankBuffers, PeerGroupReducer)
+        _run(rank, world, variant, q, dist, RankBuffers, PeerGroupReducer, nonfinite)
     except Exception:  # report instead of leaving the parent waiting on the queue
         import traceback
 
@@ -48,11 +48,13 @@ def _worker(rank, world, port, variant, q):
         dist.destroy_process_group()
 
 
-def _run(rank, world, variant, q, dist, RankBuffers, PeerGroupReducer):
+def _run(rank, world, variant, q, dist, RankBuffers, PeerGroupReducer, nonfinite=False):
     if True:
         E, n = 8, 20_003
         rng = np.random.default_rng(11)
         grads = (rng.uniform(-1, 1, (E, n)) * 10.0 ** rng.integers(-12, 13, (E, n))).astype(np.float32)
+        if nonfinite:  # rank 1's slot, an element of rank 0's parameter shard
+            grads[6, 100] = np.nan
         p0 = rng.uniform(-1, 1, n).astype(np.float32)
         E_loc = E // world
         torch.cuda.set_device(0)
@@ -60,10 +62,19 @@ def _run(rank, world, variant, q, dist, RankBuffers, PeerGroupReducer):
                           torch.from_numpy(p0.copy()).cuda(), torch.zeros(n, dtype=torch.float32, device="cuda"),
                           torch.cuda.Stream())
         red = PeerGroupReducer(loc, E, variant, None, 0.05, 0.9)
-        for _ in range(3):
+        for _ in range(1 if nonfinite else 3):
             red.step()
         torch.cuda.synchronize()
-        red.check()
+        if nonfinite:
+            from paper_2208_14228_b200.errors import NumericError
+
+            try:
+                red.check()
+                raise AssertionError("no NumericError")
+            except NumericError:
+                pass
+        else:
+            red.check()
         dist.barrier()
         q.put((rank, loc.param.cpu().numpy().tobytes(), loc.vel.cpu().numpy().tobytes()))
         dist.barrier()
@@ -168,3 +179,35 @@ def test_distributed_trainer_over_ipc_matches_reference():
         for step, blob in enumerate(res[k][1]):
             got = [struct.pack("<d", v).hex() for v in struct.unpack(f"<{len(blob) // 8}d", blob)]
             assert got == r["losses"][step][4 * k: 4 * k + 4], (k, step)
+
+
+@pytest.mark.parametrize("variant", ["rank_tree2", "sequential"])
+def test_two_process_ipc_reducer_non_finite_changes_nothing(variant):
+    """NaN in rank 1's EST slot, inside rank 0's parameter shard: rank 0's check fails, its status is
+    published to rank 1 before either commits, and both replicas keep their bytes; both raise."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, variant, q, True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        res = {}
+        for _ in procs:
+            r, pb, vb = q.get(timeout=120)
+            assert pb != "error", vb
+            res[r] = (pb, vb)
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs)
+    rng = np.random.default_rng(11)
+    E, n = 8, 20_003
+    rng.uniform(-1, 1, (E, n)), rng.integers(-12, 13, (E, n))
+    p = rng.uniform(-1, 1, n).astype(np.float32)
+    for r in (0, 1):
+        assert res[r][0] == p.tobytes() and res[r][1] == np.zeros(n, np.float32).tobytes()

@@ -186,3 +186,51 @@ def test_fused_adam_update_bit_exact(dtype, fanin, E, nout):
         assert np.array_equal(got.cpu().numpy().view(np.uint8), want.astype(dtype).view(np.uint8))
     for ep, em, es in extra:
         assert torch.equal(ep, p_t) and torch.equal(em, m_t) and torch.equal(es, s_t)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("fanin,E,nout", [(0, 8, 0), (2, 8, 2), (2, 5, 1)])
+def test_guarded_update_commits_only_finite_steps(oracle, dtype, fanin, E, nout):
+    """`stage` set: a finite update equals the single-pass one bit for bit; a non-finite synchronized
+    gradient anywhere leaves param, velocity and every replica output untouched (the reference's
+    sgd_step raises before it mutates anything, model.py:207-209) and reports NumericError."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import Flags, stream
+
+    n = 10_007
+    grads = adversarial(E, n, 31 + E, dtype)
+    p0 = adversarial(1, n, 5, dtype)[0]
+    v0 = adversarial(1, n, 6, dtype)[0]
+    want_p, want_v, st, _, _ = run_reduce(grads, None, fanin, p0, v0, 0.02, 0.9)
+    assert st == 0
+    for bad in (False, True):
+        g = grads.copy()
+        if bad:
+            g[E - 1, n - 2] = np.nan  # in the scalar tail of the last shard of the vector body
+        g_t = torch.from_numpy(g).cuda()
+        p_t, v_t = torch.from_numpy(p0.copy()).cuda(), torch.from_numpy(v0.copy()).cuda()
+        extra = [(p_t.clone(), v_t.clone()) for _ in range(nout)]
+        stage = torch.empty_like(p_t)
+        flags = Flags()
+        a = _native.ReduceArgs()
+        a.dtype = _native.DTYPE_F64 if dtype == np.float64 else _native.DTYPE_F32
+        a.mode, a.E, a.fanin, a.n, a.nout = _native.REDUCE_UPDATE, E, fanin, n, nout
+        for k in range(E):
+            a.grads[k] = g_t[k].data_ptr()
+        a.param = a.param_out = p_t.data_ptr()
+        a.vel = a.vel_out = v_t.data_ptr()
+        for r, (ep, ev) in enumerate(extra):
+            a.extra_param_out[r], a.extra_vel_out[r] = ep.data_ptr(), ev.data_ptr()
+        a.lr, a.mu, a.flags, a.stage = 0.02, 0.9, flags.t.data_ptr(), stage.data_ptr()
+        _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()))
+        st, detail, _ = flags.status()
+        if bad:
+            assert st == 5 and detail == n - 2
+            wp, wv = p0, v0
+        else:
+            assert st == 0
+            wp, wv = want_p, want_v
+        assert np.array_equal(p_t.cpu().numpy().view(np.uint8), wp.view(np.uint8))
+        assert np.array_equal(v_t.cpu().numpy().view(np.uint8), wv.view(np.uint8))
+        for ep, ev in extra:
+            assert torch.equal(ep, p_t) and torch.equal(ev, v_t)
