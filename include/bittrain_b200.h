@@ -90,6 +90,13 @@ int bt_mlp_step(const bt_mlp_args *args, void *stream);
  * caller-owned HOST buffers and the stream synchronised: the whole of one run_minibatch /
  * run_steps call in one entry point (losses_host may be NULL).         engine.py:271-329 */
 int bt_mlp_run(const bt_mlp_args *args, double *losses_host, int32_t *status_host, void *stream);
+/* The multi-device form (bt_mlp_args.n_dev > 1): the n launches of one lock-step exchange group,
+ * launch i on CUDA device devices[i] / streams[i]; all are queued before any host wait (they
+ * exchange EST slots with each other every mini-batch), then each device's losses (its own EST
+ * columns) and status words are copied to the host buffers and every stream synchronised.
+ * The whole of one multi-GPU run_minibatch / run_steps call.             engine.py:271-329 */
+int bt_mlp_run_group(const bt_mlp_args *const *args, const int32_t *devices, void *const *streams, int32_t n,
+                     double *const *losses_host, int32_t *const *status_host);
 /* Same launch with per-stage clock64 sums accumulated into timing_dev[0..4]
  * (rows+tanh, output chain, gradients, allreduce fold, update) and the step
  * count into timing_dev[5]; the compact build also adds its prologue, epilogue and whole-CTA

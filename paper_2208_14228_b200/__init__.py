@@ -13,7 +13,9 @@ from .engine import (DeterminismMode, ExecutorSpec, TrainingState, TrainRunConfi
                      check_replica_agreement, init_training, reconfigure, run_minibatch, run_steps, split_by_rank)
 from .errors import (BittrainError, ConfigError, CorruptionError, FormatError, InputError, NumericError,
                      ProgressError, StateError, VersionError)
+from . import placement
 from .model import OptState, ToyModel, TrackedStat, forward_backward, sgd_step
+from .placement import set_devices
 from .prng import derive_stream, fnv1a64, rng_uniform01, shuffled_range, splitmix64_next
 from .reduction import KernelProfile, Sequential, Tree, reduce_sum
 from .runlog import RunLog, bitdiff, param_fingerprint
@@ -31,5 +33,5 @@ __all__ = [
     "forward_backward", "sgd_step", "derive_stream", "fnv1a64", "rng_uniform01", "shuffled_range",
     "splitmix64_next", "KernelProfile", "Sequential", "Tree", "reduce_sum", "RunLog", "bitdiff",
     "param_fingerprint", "DataPipeline", "SamplePlan", "epoch_indices", "make_dataset", "RestartEvent", "RunSpec",
-    "run_matrix", "run_scenario", "run_training",
+    "run_matrix", "run_scenario", "run_training", "placement", "set_devices",
 ]

@@ -22,6 +22,7 @@ _u64p, _i64p, _i32p, _dp = C.POINTER(C.c_uint64), C.POINTER(C.c_int64), C.POINTE
 BT_P = 161
 BT_MAX_TABLE = 64
 BT_MAX_REPLICA_OUT = 8
+BT_MAX_XDEV, BT_XSP = 8, 162
 DTYPE_F64, DTYPE_F32 = 0, 1
 REDUCE_UPDATE, REDUCE_MEAN_ONLY, REDUCE_SUM_ONLY, REDUCE_ADAM, REDUCE_MEAN_CHECK = 0, 1, 2, 3, 4
 REDUCE_APPLY_SGD, REDUCE_APPLY_ADAM = 5, 6
@@ -48,6 +49,8 @@ class MlpArgs(C.Structure):
         ("grads", _vp), ("losses", _vp), ("rot", _vp), ("rows", _vp), ("dataset", _vp), ("lists", _vp),
         ("seed", _u64), ("step0", _i64), ("spe", _i64), ("epoch_base", _i64),
         ("flags", _vp), ("bar", _vp), ("param_trace", _vp), ("dataset_rows", _i64),
+        ("n_dev", _i32), ("dev_index", _i32), ("xin", _vp * 8), ("xflag", _vp * 8), ("xbase", C.c_uint32),
+        ("pad_x", _i32), ("xrep", _vp * 8),
     ]
 
 
@@ -86,6 +89,8 @@ EXPORTS = {
                                      _vp, _vp, _vp]),
     "bt_mlp_step": (C.c_int, [C.POINTER(MlpArgs), _vp]),
     "bt_mlp_run": (C.c_int, [C.POINTER(MlpArgs), _vp, _vp, _vp]),
+    "bt_mlp_run_group": (C.c_int, [C.POINTER(C.POINTER(MlpArgs)), _i32p, C.POINTER(_vp), _i32, C.POINTER(_vp),
+                                   C.POINTER(_vp)]),
     "bt_mlp_step_profiled": (C.c_int, [C.POINTER(MlpArgs), _vp, _vp]),
     "bt_mlp_fused_fits": (C.c_int, [C.POINTER(MlpArgs)]),
     "bt_mlp_pick_est_per_cta": (C.c_int, [_i32, _i32]),

@@ -126,7 +126,7 @@ def checkpoint_save(ts: TrainingState) -> bytes:
             raise StateError("checkpoint requested mid-mini-batch (progress skew)")
     check_replica_agreement(ts)
     dev = ts.dev
-    rep0 = dev.replicas[0].cpu().numpy()
+    rep0 = dev.replica(0).cpu().numpy()
     rngs, means, counts = dev.snapshot()
     mode = ts.cfg.determinism
     ex0 = ts.executors[0]
@@ -155,14 +155,10 @@ def checkpoint_restore(data: bytes, layout: list[ExecutorSpec], cfg: TrainRunCon
     for spec in layout:
         cfg.kernel_profile(spec.device_kind)
     ranks = assign_ranks(list(layout), cfg.max_workers)
-    dev = DeviceState(cfg.max_workers, len(ranks))
-    block = torch.tensor([doc["params"], doc["velocity"]], dtype=torch.float64)
-    dev.replicas.copy_(block.unsqueeze(0).expand(dev.X, 2, PARAM_COUNT))
+    dev = DeviceState(cfg.max_workers, ranks)
+    dev.load_replicas(torch.tensor([doc["params"], doc["velocity"]], dtype=torch.float64))
     executors = _build_executors(cfg, layout, dev, doc["lr"], doc["momentum"])
-    dev.rng.copy_(torch.tensor([u64_to_i64(c[1]) for c in ctx_rows], dtype=torch.int64))
-    dev.stat_mean.copy_(torch.tensor([c[2] for c in ctx_rows], dtype=torch.float64))
-    dev.stat_count.copy_(torch.tensor([c[3] for c in ctx_rows], dtype=torch.int64))
-    dev.invalidate()
+    dev.load_contexts([u64_to_i64(c[1]) for c in ctx_rows], [c[2] for c in ctx_rows], [c[3] for c in ctx_rows])
     contexts = []
     for c in ctx_rows:
         wc = WorkerContext(c[0], minibatch_idx=c[4])

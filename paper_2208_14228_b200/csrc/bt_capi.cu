@@ -16,6 +16,7 @@ namespace bt {
 int mlp_launch(const bt_mlp_args& a, cudaStream_t s, unsigned long long* timing = nullptr);
 size_t mlp_smem_bytes(int nrows);
 bool mlp_fused_fits(const bt_mlp_args& a);
+bool mlp_xdev_supported(const bt_mlp_args& a);
 int reduce_launch(const bt_reduce_args& a, cudaStream_t s);
 int reduce_sum_launch(const double* v, int64_t n, int fanin, double* out, cudaStream_t s);
 int sgd_launch(const double* p, const double* v, const double* g, int64_t n, double lr, double mu, double* po,
@@ -258,6 +259,18 @@ static int validate_mlp(const bt_mlp_args* a) {
   if (a->X < 1) return fail(bt::ERR_INPUT, "need at least one replica");
   if (a->est_per_cta < 1 || (int64_t)a->est_per_cta * a->B > 256)
     return fail(bt::ERR_INPUT, "est_per_cta*B must be in [1, 256]");
+  if (a->n_dev < 0 || a->n_dev > BT_MAX_XDEV) return fail(bt::ERR_INPUT, "n_dev %d outside [0, %d]", a->n_dev, BT_MAX_XDEV);
+  if (a->n_dev > 1) {
+    if (a->dev_index < 0 || a->dev_index >= a->n_dev) return fail(bt::ERR_INPUT, "dev_index %d of %d", a->dev_index, a->n_dev);
+    for (int d = 0; d < a->n_dev; ++d)
+      if (!a->xin[d] || !a->xflag[d]) return fail(bt::ERR_INPUT, "null inbox / counter of device %d", d);
+    if (!bt::mlp_xdev_supported(*a))
+      return fail(bt::ERR_INPUT, "multi-device step: E_total in {4,8,16} over 2/4/8 devices in equal blocks, "
+                                 "micro-batch 4, one Sequential/Tree(2) variant");
+    if (!a->replicas || !a->est_fanin || !a->rng || !a->stat_mean || !a->stat_count || !a->losses || !a->flags)
+      return fail(bt::ERR_INPUT, "null device pointer in bt_mlp_args");
+    return 0;
+  }
   if (a->fuse_reduce && a->E != a->E_total)
     return fail(bt::ERR_INPUT, "fused allreduce needs every EST local (E == E_total)");
   if (a->fuse_reduce && !bt::mlp_fused_fits(*a))
@@ -300,6 +313,41 @@ int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_hos
   if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail("bt_mlp_run sync");
   g_err[0] = 0;
   return 0;
+}
+
+int bt_mlp_run_group(const bt_mlp_args* const* args, const int32_t* devices, void* const* streams, int32_t n,
+                     double* const* losses_host, int32_t* const* status_host) {
+  if (n < 1 || n > BT_MAX_XDEV) return fail(bt::ERR_INPUT, "group of %d launches", n);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int i = 0; i < n; ++i) {  // validate everything before anything runs: the launches wait on each other
+    const int st = validate_mlp(args[i]);
+    if (st) return st;
+    if (!status_host[i]) return fail(bt::ERR_INPUT, "bt_mlp_run_group needs status buffers");
+  }
+  int rc = 0;
+  for (int i = 0; i < n && !rc; ++i) {  // every device's launch is queued before any host wait
+    if (cudaSetDevice(devices[i]) != cudaSuccess) rc = cuda_fail("bt_mlp_run_group set device");
+    else rc = done(bt::mlp_launch(*args[i], STREAM(streams[i])), "bt_mlp_run_group");
+  }
+  for (int i = 0; i < n && !rc; ++i) {
+    cudaStream_t s = STREAM(streams[i]);
+    cudaSetDevice(devices[i]);
+    if (losses_host[i] && cudaMemcpyAsync(losses_host[i], args[i]->losses,
+                                          sizeof(double) * (size_t)args[i]->K * args[i]->E_total,
+                                          cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      rc = cuda_fail("bt_mlp_run_group losses");
+    else if (cudaMemcpyAsync(status_host[i], args[i]->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s) !=
+             cudaSuccess)
+      rc = cuda_fail("bt_mlp_run_group status");
+  }
+  for (int i = 0; i < n; ++i) {  // (also after a failed launch: no queued work outlives the call)
+    cudaSetDevice(devices[i]);
+    if (cudaStreamSynchronize(STREAM(streams[i])) != cudaSuccess && !rc) rc = cuda_fail("bt_mlp_run_group sync");
+  }
+  cudaSetDevice(cur);
+  if (!rc) g_err[0] = 0;
+  return rc;
 }
 
 int bt_mlp_step_profiled(const bt_mlp_args* args, uint64_t* timing_dev, void* stream) {

@@ -636,10 +636,13 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_step_kernel(const __grid_cons
 // all-gather moves 4x fewer DSMEM bytes but needs a second exchange per step;
 // measured on B200 it is ~10% slower (the exchange is latency-bound, ~500
 // cycles per hop), so one hop wins.
-template <int ET, int GG>
+template <int ET, int GG, int ND = 1>
 struct SpecShape {
   static constexpr int G = GG;                                           // CTAs = cluster size
-  static constexpr int EPC = ET / G;                                     // ESTs per CTA
+  static constexpr int EL = ET / ND;                                     // ESTs on this device
+  static constexpr int EPC = EL / G;                                     // ESTs per CTA
+  static constexpr int SP = ND > 1 ? BT_XSP : BT_P;                      // slot stride (16-byte rows)
+  static constexpr int GM1 = G > 1 ? G - 1 : 1;                          // (array extents)
   static constexpr int NB = 4;                                           // rows per EST
   static constexpr int R = NB * EPC;                                     // rows per CTA
   static constexpr int LANES = R * BT_HIDDEN;                            // stage B+C lanes
@@ -660,8 +663,8 @@ struct SpecShape {
   static constexpr int MEAN = RM + R;              // [EPC]
   static constexpr int RNG = MEAN + EPC;           // [EPC] u64
   static constexpr int CNT = RNG + EPC;            // [EPC] u64
-  static constexpr int GRAD = (CNT + EPC + 1) & ~1;  // [2][ET][BT_P] slot arrays (16-byte aligned)
-  static constexpr int ROT = GRAD + 2 * ET * BT_P;   // int32 [PAD_P]
+  static constexpr int GRAD = (CNT + EPC + 1) & ~1;  // [2][ET][SP] slot arrays (16-byte aligned)
+  static constexpr int ROT = GRAD + 2 * ET * SP;     // int32 [PAD_P]
   static constexpr int DATA = ROT + PAD_P / 2;       // [dataset_rows][9], then jit [K][R], idx int32 [K][R]
   static constexpr size_t fixed_bytes() { return sizeof(double) * DATA; }
 };
@@ -677,15 +680,26 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int32_t
   }
 }
 
-template <int ET, int G, int F>
-__global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(const __grid_constant__ bt_mlp_args a,
-                                                                             const MlpLaunch L) {
-  using S = SpecShape<ET, G>;
-  static_assert(G > 1 && ET % G == 0, "compact build: a cluster of G > 1 CTAs");
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+template <int ET, int G, int F, int ND = 1>
+__global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(const __grid_constant__ bt_mlp_args a,
+                                                                                 const MlpLaunch L) {
+  using S = SpecShape<ET, G, ND>;
+  static_assert((G > 1 || ND > 1) && ET % (G * ND) == 0, "compact build: a cluster of G CTAs per device");
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
   const int cta = blockIdx.x;  // the grid is one cluster: blockIdx.x is the cluster rank
   const int e0 = cta * S::EPC;
+  const int eb = ND > 1 ? a.est_base : 0;  // global rank of this device's first EST
   // sampler mode: the resident dataset + this launch's (index, jitter) per row;
   // explicit-batch mode (split_by_rank rows, engine.py:261-268): this CTA's own
   // rows of every mini-batch, index = position, jitter = 0 (rows are final)
@@ -731,6 +745,14 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
       bad |= (d2u(rx[i]) != d2u(p0)) | (d2u(rx[BT_P + i]) != d2u(v0));
     }
   }
+  if constexpr (ND > 1) {  // every device's first replica against ours: all devices see the same verdict
+    for (int i = tid; i < 2 * BT_P; i += S::T) {
+      const uint64_t mine = d2u(a.replicas[i]);
+#pragma unroll
+      for (int q = 0; q < ND; ++q)
+        if (a.xrep[q]) bad |= d2u(__ldcg(a.xrep[q] + i)) != mine;
+    }
+  }
   for (int el = tid; el < S::EPC; el += S::T) {
     s_rng[el] = a.rng[e0 + el];
     sm[S::MEAN + el] = a.stat_mean[e0 + el];
@@ -738,14 +760,14 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
   }
   // the launcher's variant hint must hold -- checked for every EST in every CTA, so the whole
   // cluster takes the same exit
-  for (int e = tid; e < ET; e += S::T) bad |= (a.est_fanin[e] != F) << 1;
+  for (int e = tid; e < S::EL; e += S::T) bad |= (a.est_fanin[e] != F) << 1;
   const long long t_p1 = clock64();
   long long t_p2 = t_p1;
   if (a.rows) {
     for (int it = tid; it < a.K * S::R; it += S::T) {
       const int s = it / S::R, rem = it - s * S::R;
       const int el = rem / S::NB, r = rem - el * S::NB;
-      const double* src = a.rows + ((size_t)s * S::NB * ET + (size_t)r * ET + (e0 + el)) * BT_ROW;
+      const double* src = a.rows + ((size_t)s * S::NB * ET + (size_t)r * ET + (eb + e0 + el)) * BT_ROW;
 #pragma unroll
       for (int i = 0; i < BT_ROW; ++i) s_data[(size_t)it * BT_ROW + i] = src[i];
       s_idx[it] = it;
@@ -764,7 +786,7 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
       const int s = it / S::R, rem = it - s * S::R;
       const int el = rem / S::NB, r = rem - el * S::NB;
       const int q = loc0 + s, de = q / spe, local = q - de * spe;
-      const int32_t* lst = a.lists + ((size_t)(ep0 + de - a.epoch_base) * ET + (e0 + el)) * (size_t)(spe * S::NB);
+      const int32_t* lst = a.lists + ((size_t)(ep0 + de - a.epoch_base) * ET + (eb + e0 + el)) * (size_t)(spe * S::NB);
       s_idx[it] = lst[local * S::NB + r];
     }
     t_p2 = clock64();
@@ -773,7 +795,7 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
       const int q = loc0 + s, de = q / spe, local = q - de * spe;
       double* jd = s_jit + (size_t)s * S::R + el * S::NB;
       if (a.jitter != 0.0) {  // one uniform per row of worker_rng(seed, epoch, local, est) (sampling.py:99-170)
-        const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)(ep0 + de), (uint64_t)local, (uint64_t)(e0 + el));
+        const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)(ep0 + de), (uint64_t)local, (uint64_t)(eb + e0 + el));
 #pragma unroll
         for (int r = 0; r < S::NB; ++r) jd[r] = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), a.jitter);
       } else {
@@ -810,9 +832,9 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
   // A[r] * B[r] (w1: dz*x, w2: gy*h) or A[r] (b1: dz, b2: gy, loss: e^2);
   // the operand addresses are per-thread constants, so the step's gradient
   // code is loads, multiplies, a select and the fold -- no branches.
-  uint32_t opa[S::NIT][S::NB], opb[S::NIT][S::NB], own_dst[S::NIT], rdst[S::NIT][G - 1];
+  uint32_t opa[S::NIT][S::NB], opb[S::NIT][S::NB], own_dst[S::NIT], rdst[S::NIT][S::GM1];
   bool has_b[S::NIT], is_loss[S::NIT], valid[S::NIT];
-  uint32_t rbar[G - 1];
+  uint32_t rbar[S::GM1];
   const uint32_t sm0 = smem_u32(sm);
 #pragma unroll
   for (int i = 0; i < G - 1; ++i) {  // the other CTAs, in rotated order (no rank test per push)
@@ -839,7 +861,7 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
       opa[k][r] = sm0 + (uint32_t)((a0 + r * as) * sizeof(double));
       opb[k][r] = sm0 + (uint32_t)((b0 + r * bs) * sizeof(double));
     }
-    const uint32_t off = (uint32_t)((S::GRAD + (e0 + el) * BT_P + p) * sizeof(double));  // parity-0 slot entry
+    const uint32_t off = (uint32_t)((S::GRAD + (eb + e0 + el) * S::SP + p) * sizeof(double));  // parity-0 slot entry
     own_dst[k] = sm0 + off;
 #pragma unroll
     for (int i = 0; i < G - 1; ++i) {
@@ -919,7 +941,7 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
     BT_TICK(0)
 
     // ---- E: gradients -> every CTA's slot array (model.py:183-192) --------
-    const uint32_t pb = (uint32_t)(par * ET * BT_P * sizeof(double));  // step-parity slot array
+    const uint32_t pb = (uint32_t)(par * ET * S::SP * sizeof(double));  // step-parity slot array
 #pragma unroll
     for (int k = 0; k < S::NIT; ++k) {
       if (valid[k]) {
@@ -941,7 +963,7 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
 #endif
         } else {  // loss, TrackedStat, dropout stream of EST e0+el (model.py:173, 99-104)
           const int el = (tid + k * S::T) / (BT_P + 1);
-          const int e = e0 + el, rb = el * S::NB;
+          const int e = eb + e0 + el, rb = el * S::NB;  // global rank
           a.losses[(size_t)s * ET + e] = divB.apply(g);
           double bm = sm[S::RM + rb];
 #pragma unroll
@@ -960,9 +982,25 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
 #if defined(BT_ABL) && (BT_ABL & 4)
       if (tid == 0) mbar_arrive_expect_tx(bar, 0);
 #else
-      if (tid == 0) mbar_arrive_expect_tx(bar, (uint32_t)((ET - S::EPC) * BT_P * sizeof(double)));
+      if (tid == 0) mbar_arrive_expect_tx(bar, (uint32_t)((S::EL - S::EPC) * BT_P * sizeof(double)));
 #endif
       else mbar_arrive(bar);
+    }
+    if constexpr (ND > 1) {  // this CTA's slots -> every other device's inbox (NVLink stores), then signal
+      __syncthreads();
+      const int warp = tid >> 5, ln = tid & 31;
+      constexpr int NW = S::T / 32;
+      constexpr int VEC = S::EPC * S::SP / 2;  // 16-byte vectors of this CTA's slots
+      const double2* src = (const double2*)(sm + S::GRAD + par * ET * S::SP + (eb + e0) * S::SP);
+      for (int r = warp; r < ND - 1; r += NW) {
+        int d = a.dev_index + 1 + r;
+        d -= d >= ND ? ND : 0;
+        double2* dst = (double2*)(a.xin[d] + (size_t)par * ET * S::SP + (size_t)(eb + e0) * S::SP);
+        for (int i = ln; i < VEC; i += 32) dst[i] = src[i];
+        fence_acq_rel_sys();
+        __syncwarp();
+        if (ln == 0) red_release_sys_add(a.xflag[d], 1u);
+      }
     }
     BT_TICK(1)
     // the next mini-batch's rows and masks while the exchange is in flight
@@ -974,17 +1012,46 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
     // ---- exchange: all ET*P*8 slot bytes of this step parity --------------
     mbar_wait(smem_u32(&s_mbar[par]), (phases >> par) & 1u, a.flags);
     phases ^= 1u << par;
+    int xok = 1;
+    if constexpr (ND > 1) {  // every other device's slots of this mini-batch have landed in our inbox
+      __shared__ int s_xok;
+      if (tid == 0) {
+        const uint32_t target = a.xbase + (uint32_t)(s + 1) * (uint32_t)((ND - 1) * G);
+        const uint32_t* fl = a.xflag[a.dev_index];
+        int okw = 1;
+        if ((int32_t)(ld_acquire_sys_u32(fl) - target) < 0) {
+          const long long tw = clock64();
+          while ((int32_t)(ld_acquire_sys_u32(fl) - target) < 0)
+            if (clock64() - tw > (1ll << 32)) {  // a device that never arrives: fail, do not hang
+              atomicCAS(a.flags + FLAG_STATUS, 0, (int)ERR_CUDA);
+              okw = 0;
+              break;
+            }
+        }
+        s_xok = okw;
+      }
+      __syncthreads();
+      xok = s_xok;
+    }
     BT_TICK(2)
 
     // ---- F: allreduce + /E + momentum SGD into the other buffer -----------
-    int ok = 1;
+    int ok = xok;
     double np = 0.0;
-    if (tid < BT_P) {
-      const double* col = sm + S::GRAD + par * ET * BT_P + tid;
+    if (tid < BT_P && xok) {
+      const double* col = sm + S::GRAD + par * ET * S::SP + tid;
 #if defined(BT_ABL) && (BT_ABL & 8)
       const double sum = col[0];
 #else
-      const double sum = fold_ranks_t<ET, F>(rot_p, [&](int q) { return col[q * BT_P]; });
+      double sum;
+      if constexpr (ND > 1) {
+        const double* inb = a.xin[a.dev_index] + (size_t)par * ET * S::SP + tid;
+        sum = fold_ranks_t<ET, F>(rot_p, [&](int q) {
+          return (unsigned)(q - eb) < (unsigned)S::EL ? col[q * S::SP] : __ldcg(inb + (size_t)q * S::SP);
+        });
+      } else {
+        sum = fold_ranks_t<ET, F>(rot_p, [&](int q) { return col[q * BT_P]; });
+      }
 #endif
       const double g = divE.apply(sum);
       ok = finite_d(g) ? 1 : 0;
@@ -995,7 +1062,7 @@ __global__ void __launch_bounds__(SpecShape<ET, G>::T) mlp_step_spec_kernel(cons
     }
     BT_TICK(3)
     if (!__syncthreads_and(ok)) {  // sgd_step raises before mutating (model.py:207-209)
-      if (cta == 0 && tid == 0) {
+      if (cta == 0 && tid == 0 && xok) {
         a.flags[FLAG_STATUS] = ERR_NUMERIC;
         a.flags[FLAG_STEP] = s;
       }
@@ -1145,10 +1212,10 @@ static cudaError_t launch_k(const bt_mlp_args& a, const MlpLaunch& L, size_t sme
   return cudaGetLastError();
 }
 
-template <int ET, int G, int F>
+template <int ET, int G, int F, int ND = 1>
 static cudaError_t launch_spec(const bt_mlp_args& a, size_t smem, cudaStream_t stream, const MlpLaunch& L) {
-  using S = SpecShape<ET, G>;
-  auto kern = mlp_step_spec_kernel<ET, G, F>;
+  using S = SpecShape<ET, G, ND>;
+  auto kern = mlp_step_spec_kernel<ET, G, F, ND>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT);
@@ -1159,9 +1226,9 @@ static cudaError_t launch_spec(const bt_mlp_args& a, size_t smem, cudaStream_t s
 }
 
 // Shared memory of the compact build, or 0 when it does not fit.
-template <int ET, int G>
+template <int ET, int G, int ND = 1>
 static size_t spec_smem(const bt_mlp_args& a) {
-  using S = SpecShape<ET, G>;
+  using S = SpecShape<ET, G, ND>;
   const size_t data_rows = a.rows ? (size_t)a.K * S::R : (size_t)a.dataset_rows;
   // sampler mode: the per-launch (index, jitter) staging is sized for at least SPEC_KCAP
   // mini-batches, so launches of different lengths share one shared-memory configuration
@@ -1174,12 +1241,37 @@ static size_t spec_smem(const bt_mlp_args& a) {
   return exact <= SMEM_LIMIT ? exact : 0;
 }
 
-template <int ET, int G>
+template <int ET, int G, int ND = 1>
 static bool try_spec(const bt_mlp_args& a, int fan, cudaStream_t stream, const MlpLaunch& L, cudaError_t* err) {
-  const size_t ss = spec_smem<ET, G>(a);
+  const size_t ss = spec_smem<ET, G, ND>(a);
   if (!ss) return false;
-  *err = fan ? launch_spec<ET, G, 2>(a, ss, stream, L) : launch_spec<ET, G, 0>(a, ss, stream, L);
+  *err = fan ? launch_spec<ET, G, 2, ND>(a, ss, stream, L) : launch_spec<ET, G, 0, ND>(a, ss, stream, L);
   return true;
+}
+
+// Multi-device exchange group: E_total in {4, 8, 16} over n_dev in {2, 4, 8} devices, equal EST
+// blocks, one cluster of min(E, 8) CTAs per device.
+static bool try_spec_xdev(const bt_mlp_args& a, int fan, cudaStream_t stream, const MlpLaunch& L, cudaError_t* err) {
+  switch (a.E_total * 16 + a.n_dev) {
+    case 4 * 16 + 2: return try_spec<4, 2, 2>(a, fan, stream, L, err);
+    case 4 * 16 + 4: return try_spec<4, 1, 4>(a, fan, stream, L, err);
+    case 8 * 16 + 2: return try_spec<8, 4, 2>(a, fan, stream, L, err);
+    case 8 * 16 + 4: return try_spec<8, 2, 4>(a, fan, stream, L, err);
+    case 8 * 16 + 8: return try_spec<8, 1, 8>(a, fan, stream, L, err);
+    case 16 * 16 + 2: return try_spec<16, 8, 2>(a, fan, stream, L, err);
+    case 16 * 16 + 4: return try_spec<16, 4, 4>(a, fan, stream, L, err);
+    case 16 * 16 + 8: return try_spec<16, 2, 8>(a, fan, stream, L, err);
+    default: return false;
+  }
+}
+
+bool mlp_xdev_supported(const bt_mlp_args& a) {
+  const int fan = a.est_fanin_uniform - 1;
+  const int ed = a.E_total * 16 + a.n_dev;
+  const bool shape = ed == 4 * 16 + 2 || ed == 4 * 16 + 4 || ed == 8 * 16 + 2 || ed == 8 * 16 + 4 ||
+                     ed == 8 * 16 + 8 || ed == 16 * 16 + 2 || ed == 16 * 16 + 4 || ed == 16 * 16 + 8;
+  return shape && a.fuse_reduce && a.B == 4 && a.E * a.n_dev == a.E_total && a.est_base == a.dev_index * a.E &&
+         (a.rows || a.dataset_rows > 0) && a.rank_override < 0 && (fan == 0 || fan == 2) && fan == a.comm_fanin;
 }
 
 // CTAs per cluster for the compact build (BT_SPEC_G overrides, for measurements).
@@ -1194,6 +1286,13 @@ static int spec_g(int et) {
 }
 
 int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* timing) {
+  if (a.n_dev > 1) {  // one device of a lock-step exchange group: the compact build only
+    if (!mlp_xdev_supported(a)) return ERR_INPUT;
+    MlpLaunch L{0, 0, 0, 1, timing};
+    cudaError_t err = cudaSuccess;
+    if (!try_spec_xdev(a, a.est_fanin_uniform - 1, stream, L, &err)) return ERR_INPUT;
+    return err == cudaSuccess ? OK : ERR_CUDA;
+  }
   const int grid = grid_of(a);
   size_t smem = 0;
   MlpLaunch L = plan(a, &smem);

@@ -15,6 +15,8 @@ extern "C" {
 #define BT_B2 (BT_W2 + BT_HIDDEN)
 #define BT_P (BT_B2 + 1) /* 161 */
 #define BT_ROW (BT_INPUT_DIM + 1) /* dataset row: 8 x-values then y (sampling.py:24-35) */
+#define BT_MAX_XDEV 8 /* devices of one multi-device exchange group */
+#define BT_XSP 162    /* inbox slot stride in doubles (161 rounded to 16 bytes) */
 
 /* One launch runs K consecutive mini-batches of the data-parallel step
  * (engine.py:271-329) for the ESTs [est_base, est_base+E) of an E_total-EST job.
@@ -55,6 +57,22 @@ typedef struct bt_mlp_args {
   uint32_t *bar;           /* grid barrier counter, zeroed by the launcher */
   double *param_trace;     /* [K][P] parameters after each mini-batch (RunLog fingerprints) or NULL */
   int64_t dataset_rows;    /* rows in `dataset` (sampler mode); lets the kernel stage it in shared memory */
+  /* Multi-device exchange (n_dev > 1): this launch holds ESTs [est_base, est_base + E) of E_total,
+   * est_base = dev_index * E, and runs K mini-batches in lock step with the other n_dev - 1 devices'
+   * launches: every mini-batch it stores its EST gradient slots into every device's inbox (peer
+   * memory, NVLink) and signals that device's arrival counter; it folds all E_total slots in the
+   * canonical rank order itself (bit-identical on every device).  rng / stat_mean / stat_count /
+   * est_fanin / replicas are this device's (EST pointers offset to est_base); losses is [K][E_total]
+   * and only this device's columns are written. */
+  int32_t n_dev;           /* 1: every EST of the job is local */
+  int32_t dev_index;       /* this device's position in the exchange group */
+  double *xin[BT_MAX_XDEV];     /* every device's slot inbox [2][E_total][BT_XSP] (peer-mapped) */
+  uint32_t *xflag[BT_MAX_XDEV]; /* every device's arrival counter (peer-mapped) */
+  uint32_t xbase;          /* this device's counter value when the launch starts */
+  int32_t pad_x;
+  const double *xrep[BT_MAX_XDEV]; /* every device's first replica (peer-mapped) for the launch-start
+                                      agreement check (engine.py:246-258), or all NULL to skip it --
+                                      only valid when no device is still writing its replicas */
 } bt_mlp_args;
 
 #ifdef __cplusplus

@@ -66,12 +66,17 @@ class Flags:
         self.t = torch.zeros(4, dtype=torch.int32, device=require_cuda())
         self.reset()
 
+    def _stream(self) -> int:  # the current stream of the GPU holding the words
+        return torch.cuda.current_stream(self.t.device).cuda_stream
+
     def reset(self) -> None:
-        _native.check(_native.lib().bt_flags_reset(self.t.data_ptr(), stream()), "flags reset")
+        with torch.cuda.device(self.t.device):
+            _native.check(_native.lib().bt_flags_reset(self.t.data_ptr(), self._stream()), "flags reset")
 
     def status(self) -> tuple[int, int, int]:
         detail, step = C.c_int32(), C.c_int32()
-        st = _native.lib().bt_step_status(self.t.data_ptr(), C.byref(detail), C.byref(step), stream())
+        with torch.cuda.device(self.t.device):
+            st = _native.lib().bt_step_status(self.t.data_ptr(), C.byref(detail), C.byref(step), self._stream())
         return st, detail.value, step.value
 
     def raise_if_set(self, what: str) -> None:

@@ -26,6 +26,7 @@ import torch
 
 from . import _native
 from . import buckets as _buckets
+from . import placement
 from .buckets import (BucketMap, build_buckets_initial, layout_arrival_perm, rebuild_buckets_first_minibatch,
                       rotation_table)
 from .device import DeviceVector, Flags, i64_to_u64, ptr, require_cuda, stream, u64_to_i64
@@ -101,34 +102,134 @@ class TrainRunConfig:
 
 
 # ---------------------------------------------------------------- device state
-class DeviceState:
-    """HBM layout of one job."""
+class Shard:
+    """One GPU's part of a job: the replicas of the executors placed on it and the slots of
+    their ESTs (a contiguous rank block).  Slot arrays are [E] on every shard; only the
+    entries of the shard's own ESTs are meaningful there."""
 
-    def __init__(self, E: int, X: int):
+    def __init__(self, index: int, ordinal: int, execs: list[int], ests: list[int], E: int):
+        self.index, self.ordinal = index, ordinal
+        self.execs, self.ests = list(execs), list(ests)
+        self.base, self.count = (self.ests[0] if self.ests else 0), len(self.ests)
+        with torch.cuda.device(ordinal):
+            self.replicas = torch.zeros((len(execs), 2, P), dtype=torch.float64, device="cuda")  # params | vel
+            self.est_fanin = torch.zeros(E, dtype=torch.int32, device="cuda")
+            self.rng = torch.zeros(E, dtype=torch.int64, device="cuda")         # u64 bit patterns
+            self.stat_mean = torch.zeros(E, dtype=torch.float64, device="cuda")
+            self.stat_count = torch.zeros(E, dtype=torch.int64, device="cuda")
+            self.grads = torch.zeros((2, E, P), dtype=torch.float64, device="cuda")  # step-parity slots
+            self.flags = Flags()
+            self.bar = torch.zeros(1, dtype=torch.int32, device="cuda")
+            # the stream of this shard's lock-step launches: shards sharing one GPU (logical devices)
+            # must run concurrently, so each has its own
+            self.stream = torch.cuda.Stream()
+        self.dataset = None  # this GPU's copy of the resident dataset (multi-GPU jobs)
+        self.lists = (None, None)  # (source tensor, this GPU's copy) of the epoch lists
+        self.rot = (None, None)
+
+    def on(self, t: torch.Tensor | None, cache: str | None = None) -> torch.Tensor | None:
+        """`t` on this shard's GPU (cached per source tensor when `cache` names a slot)."""
+        if t is None or t.device.index == self.ordinal:
+            return t
+        if cache is not None:
+            src, mine = getattr(self, cache)
+            if src is t:
+                return mine
+        with torch.cuda.device(self.ordinal):
+            mine = t.to(torch.device("cuda", self.ordinal))
+        if cache is not None:
+            setattr(self, cache, (t, mine))
+        return mine
+
+
+class DeviceState:
+    """HBM layout of one job over its GPUs: executor x lives on
+    shard `exec_shard[x]` (placement.executor_devices: contiguous blocks over the job's GPUs),
+    EST k's slots on the shard of the executor that hosts it."""
+
+    def __init__(self, E: int, ranks: list[tuple[str, list[int]]]):
         require_cuda()
-        self.E, self.X = E, X
-        self.replicas = torch.zeros((X, 2, P), dtype=torch.float64, device="cuda")  # params | velocity
-        self.est_fanin = torch.zeros(E, dtype=torch.int32, device="cuda")
-        self.rng = torch.zeros(E, dtype=torch.int64, device="cuda")         # u64 bit patterns
-        self.stat_mean = torch.zeros(E, dtype=torch.float64, device="cuda")
-        self.stat_count = torch.zeros(E, dtype=torch.int64, device="cuda")
-        self.grads = torch.zeros((2, E, P), dtype=torch.float64, device="cuda")  # step-parity slots
-        self.flags = Flags()
-        self.bar = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.E, self.X = E, len(ranks)
+        devs = placement.devices()
+        plan = placement.executor_devices(self.X, devs)
+        self.shards: list[Shard] = []
+        self.exec_loc: list[tuple[Shard, int]] = [None] * self.X
+        self.est_owner: list[Shard] = [None] * E
+        for i in range(max(plan) + 1):
+            execs = [x for x in range(self.X) if plan[x] == i]
+            ests = [k for x in execs for k in ranks[x][1]]
+            sh = Shard(i, devs[i], execs, ests, E)
+            self.shards.append(sh)
+            for j, x in enumerate(execs):
+                self.exec_loc[x] = (sh, j)
+            for k in ests:
+                self.est_owner[k] = sh
+        if len(self.shards) > 1:
+            placement.enable_peer_access([sh.ordinal for sh in self.shards])
         self._snap = None
         self.rot = None
         self.rot_key = None
+        self.xstep = None  # the prepared multi-GPU launch (_XdevStep)
+
+    # -- the single-GPU view (one shard: every executor and EST on one device) --------------
+    @property
+    def multi(self) -> bool:
+        return len(self.shards) > 1
+
+    def _one(self) -> Shard:
+        if self.multi:
+            raise RuntimeError("this job spans several GPUs: address its shards")
+        return self.shards[0]
+
+    replicas = property(lambda self: self._one().replicas)
+    est_fanin = property(lambda self: self._one().est_fanin)
+    rng = property(lambda self: self._one().rng)
+    stat_mean = property(lambda self: self._one().stat_mean)
+    stat_count = property(lambda self: self._one().stat_count)
+    grads = property(lambda self: self._one().grads)
+    flags = property(lambda self: self.shards[0].flags)
+    bar = property(lambda self: self._one().bar)
+
+    # -- shard-aware access --------------------------------------------------------------------
+    def replica(self, x: int) -> torch.Tensor:
+        sh, j = self.exec_loc[x]
+        return sh.replicas[j]
+
+    def owner(self, k: int) -> Shard:
+        return self.est_owner[k]
 
     def invalidate(self) -> None:
         self._snap = None
 
     def snapshot(self):
         if self._snap is None:
-            self._snap = (self.rng.tolist(), self.stat_mean.tolist(), self.stat_count.tolist())
+            rng, mean, cnt = [0] * self.E, [0.0] * self.E, [0] * self.E
+            for sh in self.shards:
+                r, m, c = sh.rng.tolist(), sh.stat_mean.tolist(), sh.stat_count.tolist()
+                for k in sh.ests:
+                    rng[k], mean[k], cnt[k] = r[k], m[k], c[k]
+            self._snap = (rng, mean, cnt)
         return self._snap
 
+    def load_contexts(self, rng: list[int], mean: list[float], count: list[int]) -> None:
+        for sh in self.shards:
+            sh.rng.copy_(torch.tensor(rng, dtype=torch.int64))
+            sh.stat_mean.copy_(torch.tensor(mean, dtype=torch.float64))
+            sh.stat_count.copy_(torch.tensor(count, dtype=torch.int64))
+        self.invalidate()
+
+    def load_replicas(self, block: torch.Tensor) -> None:
+        """Every executor's replica <- block [2][P]."""
+        for sh in self.shards:
+            sh.replicas.copy_(block.to(sh.replicas.device).unsqueeze(0).expand_as(sh.replicas))
+
+    def set_fanin(self, fan: np.ndarray) -> None:
+        t = torch.from_numpy(fan)
+        for sh in self.shards:
+            sh.est_fanin.copy_(t)
+
     def replica_ptrs(self) -> list[int]:
-        return [self.replicas[x].data_ptr() for x in range(self.X)]
+        return [self.replica(x).data_ptr() for x in range(self.X)]
 
 
 class WorkerContext:
@@ -148,9 +249,10 @@ class WorkerContext:
 
     def attach(self, dev: DeviceState) -> None:
         k = self.virtual_rank
-        dev.rng[k] = u64_to_i64(self._rng)
-        dev.stat_mean[k] = self._stat.running_mean
-        dev.stat_count[k] = self._stat.update_count
+        sh = dev.owner(k)
+        sh.rng[k] = u64_to_i64(self._rng)
+        sh.stat_mean[k] = self._stat.running_mean
+        sh.stat_count[k] = self._stat.update_count
         dev.invalidate()
         self._dev = dev
 
@@ -165,7 +267,7 @@ class WorkerContext:
         if self._dev is None:
             self._rng = v
         else:
-            self._dev.rng[self.virtual_rank] = u64_to_i64(v)
+            self._dev.owner(self.virtual_rank).rng[self.virtual_rank] = u64_to_i64(v)
             self._dev.invalidate()
 
     @property
@@ -180,8 +282,9 @@ class WorkerContext:
         if self._dev is None:
             self._stat = s
         else:
-            self._dev.stat_mean[self.virtual_rank] = s.running_mean
-            self._dev.stat_count[self.virtual_rank] = s.update_count
+            sh = self._dev.owner(self.virtual_rank)
+            sh.stat_mean[self.virtual_rank] = s.running_mean
+            sh.stat_count[self.virtual_rank] = s.update_count
             self._dev.invalidate()
 
     def _key(self):
@@ -212,21 +315,26 @@ class ExecutorState:
         self._lr, self._mu = lr, momentum
 
     @property
+    def device(self) -> torch.device:
+        """The GPU this executor runs on (placement.executor_devices)."""
+        return self._dev.replica(self._x).device
+
+    @property
     def model(self) -> ToyModel:
-        return ToyModel(self._dev.replicas[self._x, 0])
+        return ToyModel(self._dev.replica(self._x)[0])
 
     @model.setter
     def model(self, m: ToyModel) -> None:
-        self._dev.replicas[self._x, 0].copy_(m.tensor)
+        self._dev.replica(self._x)[0].copy_(m.tensor)
 
     @property
     def opt(self) -> OptState:
-        return OptState(self._lr, self._mu, self._dev.replicas[self._x, 1])
+        return OptState(self._lr, self._mu, self._dev.replica(self._x)[1])
 
     @opt.setter
     def opt(self, o: OptState) -> None:
         self._lr, self._mu = o.lr, o.momentum
-        self._dev.replicas[self._x, 1].copy_(o.tensor)
+        self._dev.replica(self._x)[1].copy_(o.tensor)
 
 
 @dataclass
@@ -292,7 +400,7 @@ def _build_executors(cfg: TrainRunConfig, layout, dev: DeviceState, lr: float, m
         f = fanin_code(prof.reduce_variant)
         fan[ranks] = f
         execs.append(ExecutorState(kind, prof, ranks, dev, x, lr, mu))
-    dev.est_fanin.copy_(torch.from_numpy(fan))
+    dev.set_fanin(fan)
     return execs
 
 
@@ -309,30 +417,32 @@ def init_training(cfg: TrainRunConfig, layout: list[ExecutorSpec]) -> TrainingSt
     for spec in layout:
         cfg.kernel_profile(spec.device_kind)  # ConfigError on unknown kinds before allocating
     ranks = assign_ranks(list(layout), cfg.max_workers)
-    dev = DeviceState(cfg.max_workers, len(ranks))
+    dev = DeviceState(cfg.max_workers, ranks)
     init = ToyModel.init_random(cfg.seed)
-    dev.replicas[:, 0, :] = init.tensor
+    dev.load_replicas(torch.stack([init.tensor, torch.zeros_like(init.tensor)]))
     executors = _build_executors(cfg, layout, dev, cfg.lr, cfg.momentum)
     contexts = []
     for k in range(cfg.max_workers):
         ctx = WorkerContext(k, derive_stream(TAG_DROPOUT, cfg.seed, k), TrackedStat())
         contexts.append(ctx)
-    dev.rng.copy_(torch.tensor([u64_to_i64(c._rng) for c in contexts], dtype=torch.int64))
+    dev.load_contexts([u64_to_i64(c._rng) for c in contexts], [0.0] * cfg.max_workers, [0] * cfg.max_workers)
     for c in contexts:
         c._dev = dev
-    dev.invalidate()
     return TrainingState(cfg, contexts, executors, build_buckets_initial(P, cfg.bucket_capacity),
                          _new_pipeline(cfg), rebuild_pending=not cfg.determinism.d1, dev=dev)
 
 
 def check_replica_agreement(ts: TrainingState) -> None:
-    """Every executor's params+velocity must be bitwise equal (engine.py:246-258), on the device."""
+    """Every executor's params+velocity must be bitwise equal (engine.py:246-258), on the device:
+    one compare kernel on the first GPU reads every replica (peer loads from the other GPUs)."""
     dev = ts.dev
     if dev.X < 2:
         return
     ptrs = (C.c_void_p * dev.X)(*dev.replica_ptrs())
-    _native.check(_native.lib().bt_replica_check(ptrs, dev.X, 2 * P * 8, ptr(dev.flags.t), stream()),
-                  "check_replica_agreement")
+    sh0 = dev.shards[0]
+    with torch.cuda.device(sh0.ordinal):
+        _native.check(_native.lib().bt_replica_check(ptrs, dev.X, 2 * P * 8, ptr(sh0.flags.t), stream()),
+                      "check_replica_agreement")
     st, detail, _ = dev.flags.status()
     if st:
         dev.flags.reset()
@@ -360,7 +470,8 @@ def _rot_tensor(ts: TrainingState):
     key = (ts.bucket_map, ts.cfg.max_workers)
     dev = ts.dev
     if dev.rot_key != key:
-        dev.rot = torch.from_numpy(rotation_table(ts.bucket_map, ts.cfg.max_workers)).to("cuda")
+        with torch.cuda.device(dev.shards[0].ordinal):
+            dev.rot = torch.from_numpy(rotation_table(ts.bucket_map, ts.cfg.max_workers)).to("cuda")
         dev.rot_key = key
     return dev.rot
 
@@ -413,7 +524,8 @@ def _fused_fits(cfg, B: int | None = None) -> bool:
 
 
 def _raise_step_error(ts: TrainingState, st: int, detail: int, what: str) -> None:
-    ts.dev.flags.reset()
+    for sh in ts.dev.shards:
+        sh.flags.reset()
     if st == 6:
         raise CorruptionError(f"{what}: an executor's model/optimizer replica diverged")
     if st == 5:
@@ -477,6 +589,196 @@ class _FastStep:
         return int(self.status_np[0])
 
 
+class _XdevStep:
+    """The lock-step multi-GPU launch (bt_mlp.cu with n_dev > 1) of a job whose executors span
+    several GPUs: every GPU runs the fused step for its EST block, stores its EST gradient slots
+    into every other GPU's inbox over NVLink each mini-batch and folds all E slots in the canonical
+    rank order itself -- the same bits on every GPU and as on one GPU."""
+
+    KMAX = 128
+
+    @staticmethod
+    def eligible(ts: TrainingState) -> bool:
+        dev, cfg = ts.dev, ts.cfg
+        n = len(dev.shards)
+        fans = {fanin_code(ex.kernel_profile.reduce_variant) for ex in ts.executors}
+        return (n in (2, 4, 8) and cfg.max_workers in (4, 8, 16) and cfg.micro_batch == 4
+                and len({sh.count for sh in dev.shards}) == 1 and cfg.max_workers % n == 0
+                and len(fans) == 1 and fans == {fanin_code(_comm_variant(ts))} and fans <= {0, 2})
+
+    def __init__(self, ts: TrainingState):
+        dev, cfg = ts.dev, ts.cfg
+        E, n = cfg.max_workers, len(dev.shards)
+        self.dev, self.n = dev, n
+        self.group = placement.XGroup([sh.ordinal for sh in dev.shards], E)
+        self.G = min(E // n, 8)
+        fan = fanin_code(_comm_variant(ts))
+        xin, xflag = self.group.tables()
+        lib = _native.lib()
+        self.args, self.keep = [], []
+        self.losses_dev, self.host_losses, self.host_status = [], [], []
+        ds = ts.pipeline.dataset_device
+        for i, sh in enumerate(dev.shards):
+            with torch.cuda.device(sh.ordinal):
+                losses = torch.zeros((self.KMAX, E), dtype=torch.float64, device="cuda")
+            sh.dataset = sh.on(ds) if sh.dataset is None else sh.dataset
+            a = _native.MlpArgs()
+            a.E, a.est_base, a.E_total, a.B, a.X, a.K = sh.count, sh.base, E, cfg.micro_batch, len(sh.execs), 1
+            a.fuse_reduce, a.est_per_cta = 1, 1
+            a.comm_fanin, a.est_fanin_uniform, a.rank_override = fan, fan + 1, -1
+            a.rate, a.jitter = float(cfg.dropout_rate), float(cfg.jitter)
+            a.replicas = sh.replicas.data_ptr()
+            a.est_fanin = sh.est_fanin.data_ptr() + 4 * sh.base
+            a.rng, a.stat_mean = sh.rng.data_ptr() + 8 * sh.base, sh.stat_mean.data_ptr() + 8 * sh.base
+            a.stat_count = sh.stat_count.data_ptr() + 8 * sh.base
+            a.grads, a.losses = sh.grads.data_ptr(), losses.data_ptr()
+            a.dataset, a.dataset_rows = sh.dataset.data_ptr(), cfg.dataset_size
+            a.seed, a.spe = cfg.seed & (2**64 - 1), ts.pipeline.steps_per_epoch
+            a.flags, a.bar = sh.flags.t.data_ptr(), sh.bar.data_ptr()
+            a.n_dev, a.dev_index = n, i
+            for q in range(n):
+                a.xin[q], a.xflag[q] = xin[q], xflag[q]
+                a.xrep[q] = dev.shards[q].replicas.data_ptr()  # launch-start agreement of every GPU
+            self.args.append(a)
+            self.losses_dev.append(losses)
+            self.host_losses.append(torch.empty((self.KMAX, E), dtype=torch.float64).pin_memory())
+            self.host_status.append(torch.zeros(4, dtype=torch.int32).pin_memory())
+        self.status_np = [t.numpy() for t in self.host_status]
+        self.losses_np = [t.numpy() for t in self.host_losses]
+        P_ = C.POINTER(_native.MlpArgs)
+        self._argv = (P_ * n)(*[C.pointer(a) for a in self.args])
+        self._devs = (C.c_int32 * n)(*[sh.ordinal for sh in dev.shards])
+        self._lh = (C.c_void_p * n)(*[t.data_ptr() for t in self.host_losses])
+        self._sh = (C.c_void_p * n)(*[t.data_ptr() for t in self.host_status])
+        self.lib = lib
+
+    def run(self, ts: TrainingState, K: int, trace: torch.Tensor | None = None) -> tuple[int, int, int, np.ndarray]:
+        """K mini-batches from ts.global_step on every GPU; returns (status, detail, failed step,
+        losses [K][E]).  trace [K][P] on the first GPU: the parameters after every mini-batch."""
+        gs, spe = ts.global_step, ts.pipeline.steps_per_epoch
+        lists, base = ts.pipeline.device_lists(gs // spe, (gs + K - 1) // spe)
+        rot = _rot_tensor(ts)
+        ex0 = ts.executors[0]
+        xbase = self.group.xbase(self.G)
+        keep = []
+        for a, sh in zip(self.args, self.dev.shards):
+            ls, rt = sh.on(lists, "lists"), sh.on(rot, "rot")
+            keep += [ls, rt]
+            a.K, a.step0, a.lists, a.epoch_base = K, gs, ls.data_ptr(), base
+            a.rot = ptr(rt)
+            a.lr, a.mu, a.xbase = float(ex0._lr), float(ex0._mu), xbase
+            a.param_trace = None
+        self.args[0].param_trace = ptr(trace)
+        for sh in self.dev.shards:  # after everything already queued on the GPU's current stream
+            sh.stream.wait_stream(torch.cuda.current_stream(sh.ordinal))
+        streams = (C.c_void_p * self.n)(*[sh.stream.cuda_stream for sh in self.dev.shards])
+        _native.check(self.lib.bt_mlp_run_group(self._argv, self._devs, streams, self.n, self._lh, self._sh),
+                      "run_minibatch (multi-GPU)")
+        self.dev.invalidate()
+        out = np.empty((K, self.dev.E), dtype=np.float64)
+        for sh, l in zip(self.dev.shards, self.losses_np):
+            out[:, sh.base:sh.base + sh.count] = l[:K, sh.base:sh.base + sh.count]
+        sts = [(int(x[0]), int(x[1]), int(x[2])) for x in self.status_np]
+        bad = [t for t in sts if t[0]]
+        if not bad:
+            self.group.steps += K
+            return 0, 0, 0, out
+        for sh in self.dev.shards:
+            sh.flags.reset()
+        if all(t[0] == 5 for t in sts) and len({t[2] for t in sts}) == 1:
+            self.group.steps += sts[0][2] + 1  # every GPU stopped after the same exchanged mini-batch
+        else:
+            self.dev.xstep = None  # the counters are out of step: a fresh group next time
+        worst = next((t for t in bad if t[0] == 6), None) or next((t for t in bad if t[0] != 9), bad[0])
+        return worst[0], worst[1], worst[2], out
+
+
+def _xdev(ts: TrainingState) -> _XdevStep | None:
+    dev = ts.dev
+    if not dev.multi or not _XdevStep.eligible(ts):
+        return None
+    if dev.xstep is None:
+        dev.xstep = _XdevStep(ts)
+    return dev.xstep
+
+
+def _grads_multi(ts: TrainingState, B: int, rows) -> tuple[torch.Tensor, list[float]]:
+    """Unfused multi-GPU step, part 1: every GPU computes its ESTs' forward/backward (grads-only
+    launch of the step kernel); the EST gradient slots are gathered on the first GPU in rank order
+    (bit copies).  Returns (grads [E][P] on GPU 0, per-EST losses)."""
+    cfg, dev = ts.cfg, ts.dev
+    E = cfg.max_workers
+    spe = ts.pipeline.steps_per_epoch
+    gs = ts.global_step
+    lists, lbase = (None, 0) if rows is not None else ts.pipeline.device_lists(gs // spe, gs // spe)
+    sh0 = dev.shards[0]
+    with torch.cuda.device(sh0.ordinal):
+        gall = torch.empty((E, P), dtype=torch.float64, device="cuda")
+    losses = [0.0] * E
+    for sh in dev.shards:
+        with torch.cuda.device(sh.ordinal):
+            lt = torch.zeros(max(sh.count, 1), dtype=torch.float64, device="cuda")
+            a = _native.MlpArgs()
+            a.E, a.est_base, a.E_total, a.B, a.X, a.K = sh.count, sh.base, E, B, len(sh.execs), 1
+            a.fuse_reduce = 0
+            a.est_per_cta = _native.lib().bt_mlp_pick_est_per_cta(sh.count, B)
+            a.comm_fanin, a.rank_override = fanin_code(_comm_variant(ts)), -1
+            a.rate, a.jitter = float(cfg.dropout_rate), float(cfg.jitter)
+            a.replicas = sh.replicas.data_ptr()
+            a.est_fanin = sh.est_fanin.data_ptr() + 4 * sh.base
+            a.rng, a.stat_mean = sh.rng.data_ptr() + 8 * sh.base, sh.stat_mean.data_ptr() + 8 * sh.base
+            a.stat_count = sh.stat_count.data_ptr() + 8 * sh.base
+            a.grads, a.losses = sh.grads.data_ptr() + 8 * sh.base * P, lt.data_ptr()
+            a.seed, a.step0, a.spe = cfg.seed & (2**64 - 1), gs, spe
+            keep = []
+            if rows is not None:
+                r = sh.on(rows)
+                keep.append(r)
+                a.rows = r.data_ptr()
+            else:
+                if sh.dataset is None:
+                    sh.dataset = sh.on(ts.pipeline.dataset_device)
+                ls = sh.on(lists, "lists")
+                keep.append(ls)
+                a.dataset, a.lists, a.epoch_base, a.dataset_rows = sh.dataset.data_ptr(), ls.data_ptr(), lbase, cfg.dataset_size
+            a.flags, a.bar = sh.flags.t.data_ptr(), sh.bar.data_ptr()
+            _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()), "forward_backward")
+            st, detail, _ = sh.flags.status()
+            if st:
+                _raise_step_error(ts, st, detail, "run_minibatch")
+            vals = lt.tolist()
+            for j in range(sh.count):
+                losses[sh.base + j] = vals[j]
+        gall[sh.base:sh.base + sh.count].copy_(sh.grads[0, sh.base:sh.base + sh.count])
+    dev.invalidate()
+    return gall, losses
+
+
+def _run_minibatch_multi(ts: TrainingState, B: int, rows) -> list[float]:
+    """The same step with its seams exposed across GPUs: per-GPU forward/backward -> the EST slots
+    gathered in rank order -> engine.allreduce -> sgd_step -> mirrored to every executor (the
+    reference's call sequence, engine.py:288-315; also the path of a spied allreduce)."""
+    dev = ts.dev
+    check_replica_agreement(ts)
+    st, detail, _ = dev.shards[0].flags.status()
+    if st:
+        _raise_step_error(ts, st, detail, "run_minibatch")
+    gall, losses = _grads_multi(ts, B, rows)
+    with torch.cuda.device(dev.shards[0].ordinal):
+        for ex in ts.executors:
+            for rank in ex.assigned[:-1]:  # non-final ESTs park their gradients (engine.py:305-307)
+                ts.contexts[rank].pending_grads = DeviceVector(gall[rank].clone())
+        synced = globals()["allreduce"]([DeviceVector(gall[r]) for r in range(ts.cfg.max_workers)], ts.bucket_map,
+                                        _comm_variant(ts))
+        ex0 = ts.executors[0]
+        new_model, new_opt = sgd_step(ex0.model, ex0.opt, synced)
+        for ex in ts.executors:
+            ex.model = new_model
+            ex.opt = new_opt
+    _finish_steps(ts, 1)
+    return losses
+
+
 def _fast(ts: TrainingState) -> _FastStep:
     fs = ts._fast
     if fs is None or fs.dev is not ts.dev:
@@ -496,6 +798,15 @@ def run_minibatch(ts: TrainingState, global_batch: Batch | None = None) -> list[
     else:
         B = cfg.micro_batch
         ts.pipeline.advance_all(ts.global_step)
+        if ts.dev.multi:
+            xs = _xdev(ts) if globals()["allreduce"] is _DEVICE_ALLREDUCE else None
+            if xs is not None:
+                st, detail, _, out = xs.run(ts, 1)
+                if st:
+                    _raise_step_error(ts, st, detail, "run_minibatch")
+                _finish_steps(ts, 1)
+                return out[0].tolist()
+            return _run_minibatch_multi(ts, B, None)
         if globals()["allreduce"] is _DEVICE_ALLREDUCE:
             fs = _fast(ts)
             if fs.fits:
@@ -505,6 +816,8 @@ def run_minibatch(ts: TrainingState, global_batch: Batch | None = None) -> list[
                 out = fs.losses_np[0].tolist()
                 _finish_steps(ts, 1)
                 return out
+    if ts.dev.multi:  # an explicit global batch over several GPUs
+        return _run_minibatch_multi(ts, B, rows)
     if globals()["allreduce"] is not _DEVICE_ALLREDUCE or not _fused_fits(cfg, B):
         # spied allreduce seam, or too many ESTs for on-chip slots: kernels per seam
         return _run_minibatch_unfused(ts, B, rows)
@@ -554,6 +867,8 @@ def run_steps(ts: TrainingState, K: int, trace: bool = False):
     Identical bits to K calls of run_minibatch."""
     if K < 1:
         raise ConfigError("K must be >= 1")
+    if ts.dev.multi:
+        return _run_steps_multi(ts, K, trace)
     if ts.rebuild_pending or globals()["allreduce"] is not _DEVICE_ALLREDUCE or not _fused_fits(ts.cfg):
         # one mini-batch at a time: the d0 rebuild after step 0, a spied seam,
         # or a job too large for the fused launch (run_minibatch goes unfused)
@@ -603,6 +918,69 @@ def run_steps(ts: TrainingState, K: int, trace: bool = False):
     return losses.cpu().numpy(), (tr.cpu().numpy() if trace else None)
 
 
+def _run_steps_multi(ts: TrainingState, K: int, trace: bool):
+    """run_steps over several GPUs: one lock-step launch per GPU for up to _XdevStep.KMAX
+    mini-batches at a time (or mini-batch by mini-batch on the seam path)."""
+    out, tr = [], []
+    while len(out) < K:
+        xs = None
+        if not ts.rebuild_pending and globals()["allreduce"] is _DEVICE_ALLREDUCE:
+            xs = _xdev(ts)
+        if xs is None:
+            out.append(run_minibatch(ts))
+            if trace:
+                tr.append(ts.executors[0].model.values.tolist())
+            continue
+        n = min(K - len(out), _XdevStep.KMAX)
+        gs = ts.global_step
+        ts.pipeline.advance_all(gs)
+        tt = None
+        if trace:
+            with torch.cuda.device(ts.dev.shards[0].ordinal):
+                tt = torch.empty((n, P), dtype=torch.float64, device="cuda")
+        st, detail, failed, losses = xs.run(ts, n, tt)
+        if trace:
+            tr.extend(tt.cpu().numpy()[: (n if not st else failed)])
+        done = n if not st else (failed if st == 5 else 0)
+        ts.pipeline.advance_range(gs + 1, min(n, done + (1 if st == 5 else 0)) - 1)
+        if st:
+            _finish_steps(ts, done)
+            _raise_step_error(ts, st, detail, f"run_steps (mini-batch {ts.global_step})")
+        _finish_steps(ts, n)
+        out.extend(losses)
+    return np.array(out), (np.array(tr) if trace else None)
+
+
+def move_est_slots(old: DeviceState, dev: DeviceState) -> None:
+    """The EST context switch of an elastic rescale: every EST's slots (dropout RNG, TrackedStat)
+    move from the GPU that held it to the GPU that holds it now, and executor 0's replica is copied
+    to every new executor -- one 128-bit vectorised copy launch per destination GPU, reading the
+    sources over NVLink (peer access), then the destinations are synchronised."""
+    placement.enable_peer_access(sorted({sh.ordinal for sh in old.shards + dev.shards}))
+    src0 = old.replica(0)
+    for sh in dev.shards:
+        pairs = []
+        for osh in old.shards:  # the overlap of the old and new contiguous EST blocks
+            lo, hi = max(sh.base, osh.base), min(sh.base + sh.count, osh.base + osh.count)
+            if hi > lo:
+                for name in ("rng", "stat_mean", "stat_count"):
+                    d, o = getattr(sh, name), getattr(osh, name)
+                    pairs.append((d.data_ptr() + 8 * lo, o.data_ptr() + 8 * lo, 8 * (hi - lo)))
+        for j in range(len(sh.execs)):
+            pairs.append((sh.replicas[j].data_ptr(), src0.data_ptr(), 2 * P * 8))
+        for c in range(0, len(pairs), 64):  # (a launch takes up to 64 copy pairs)
+            chunk = pairs[c:c + 64]
+            dsts = (C.c_void_p * len(chunk))(*[d for d, _, _ in chunk])
+            srcs = (C.c_void_p * len(chunk))(*[o for _, o, _ in chunk])
+            nbytes = (C.c_int64 * len(chunk))(*[n for _, _, n in chunk])
+            with torch.cuda.device(sh.ordinal):
+                _native.check(_native.lib().bt_est_slot_copy(dsts, srcs, nbytes, len(chunk), stream()),
+                              "EST slot copy")
+    for sh in dev.shards:  # the old buffers may be freed as soon as this returns
+        torch.cuda.synchronize(sh.ordinal)
+    dev.invalidate()
+
+
 def apply_layout(ts: TrainingState, layout: list[ExecutorSpec]) -> TrainingState:
     """Elastic restart onto a new layout, in device memory.
 
@@ -621,14 +999,8 @@ def apply_layout(ts: TrainingState, layout: list[ExecutorSpec]) -> TrainingState
         cfg.kernel_profile(spec.device_kind)
     ranks = assign_ranks(list(layout), cfg.max_workers)
     old = ts.dev
-    dev = DeviceState(cfg.max_workers, len(ranks))
-    # EST context slots and replica 0 -> every new replica: one slot-copy launch.
-    pairs = [(dev.rng, old.rng), (dev.stat_mean, old.stat_mean), (dev.stat_count, old.stat_count)]
-    pairs += [(dev.replicas[x], old.replicas[0]) for x in range(dev.X)]
-    dsts = (C.c_void_p * len(pairs))(*[d.data_ptr() for d, _ in pairs])
-    srcs = (C.c_void_p * len(pairs))(*[s.data_ptr() for _, s in pairs])
-    nbytes = (C.c_int64 * len(pairs))(*[d.numel() * d.element_size() for d, _ in pairs])
-    _native.check(_native.lib().bt_est_slot_copy(dsts, srcs, nbytes, len(pairs), stream()), "EST slot copy")
+    dev = DeviceState(cfg.max_workers, ranks)
+    move_est_slots(old, dev)
     ex0 = ts.executors[0]
     executors = _build_executors(cfg, layout, dev, ex0._lr, ex0._mu)
     contexts = []

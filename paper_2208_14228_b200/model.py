@@ -35,6 +35,8 @@ def _as_param_tensor(values) -> torch.Tensor:
     if isinstance(values, DeviceVector):
         return values.t
     if isinstance(values, torch.Tensor):
+        if values.is_cuda and values.dtype == torch.float64 and values.is_contiguous():
+            return values  # already a device vector (on whichever GPU holds it): a view, not a copy
         t = values.to(device=require_cuda(), dtype=torch.float64)
         return t if t.is_contiguous() else t.contiguous()
     return to_dev(list(values))
