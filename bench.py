@@ -250,25 +250,74 @@ def bench_run_minibatch(bt, calls: int = 300, warm: int = 30):
 
 
 def bench_device_dist(bt, K: int, W: int, rank: int, world: int, flush, e2e: bool, exchange: str):
-    """N>1: EST blocks per rank (paper_2208_14228_b200.dist.DistributedTrainer): grads-only step
-    kernel, then either (ipc) each rank's owner kernel reads all EST slots of its parameter shard and
-    writes every replica through CUDA IPC peer pointers, ordered by stream memory ops, or (allgather)
-    an NCCL all-gather of the slots (a bit copy) and the same fixed-order reduce+SGD on every rank.
-    e2e: each epoch's index lists are re-uploaded from host memory and every mini-batch's losses are
-    read back inside the timed span."""
+    """N>1: EST blocks per rank (paper_2208_14228_b200.dist.DistributedTrainer).
+
+    exchange "xdev" (default): the persistent lock-step kernel -- each rank runs a chunk of up to
+    LAUNCH mini-batches in one launch and exchanges EST slots every mini-batch through the other
+    ranks' inboxes (CUDA IPC peer memory, device-side counters).  Device spans: every rank holds
+    its stream at a host gate, queues [e0, launch, e1], all ranks meet at a host barrier, then the
+    gates open together -- the span is the lock-step kernel, not launch skew between processes.
+    e2e: host clock around the chunk on every rank (the epoch lists recomputed on the host and
+    uploaded, the launch, the losses and status copied back, the stream synchronised), max over
+    ranks by the caller.
+    exchange "ipc" / "allgather": the per-mini-batch grads-only kernel + reducer paths."""
     import torch.distributed as dist
 
     from paper_2208_14228_b200.dist import DistributedTrainer
 
-    tr = DistributedTrainer(seed=SEED, max_workers=E_TOTAL, micro_batch=MICRO, dataset_size=NROWS, exchange=exchange)
+    tr = DistributedTrainer(seed=SEED, max_workers=E_TOTAL, micro_batch=MICRO, dataset_size=NROWS,
+                            exchange=None if exchange == "xdev" else exchange)
     spe = tr.pipe.steps_per_epoch
+    s = torch.cuda.current_stream()
+    spans, h2d, d2h, launches = [], 0, 0, 0
+    if tr.exchange == "xdev":
+        for n in chunks(W, LAUNCH):
+            tr.run(n)
+        torch.cuda.synchronize()
+        dist.barrier()
+        gate = HostGate()
+        host_out = torch.empty((LAUNCH, E_TOTAL), dtype=torch.float64).pin_memory()
+        host_st = torch.zeros(4, dtype=torch.int32).pin_memory()
+        for n in chunks(K, LAUNCH):
+            flush()
+            if e2e:
+                tr.pipe._lists_dev = None  # nothing of the inputs stays resident between launches
+                tr.pipe._lists_host.clear()
+                torch.cuda.synchronize()
+                dist.barrier()
+                t0 = time.perf_counter()
+                out = tr.run(n)
+                host_out[:n].copy_(out, non_blocking=True)
+                host_st.copy_(tr.flags.t, non_blocking=True)
+                s.synchronize()
+                spans.append((time.perf_counter() - t0) * 1e3)
+                h2d += tr._xlists.numel() * 4
+                d2h += n * tr.count * 8 + 16
+                assert int(host_st[0]) == 0, int(host_st[0])
+            else:
+                gate.close(s)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                try:
+                    e0.record(s)
+                    tr.run(n)
+                    e1.record(s)
+                    dist.barrier()
+                finally:
+                    gate.open()
+                e1.synchronize()
+                spans.append(e0.elapsed_time(e1))
+            launches += 1
+        tr.check()
+        torch.cuda.synchronize()
+        dist.barrier()
+        params = tr.params[0].clone()
+        tr.close()
+        return params, sum(spans), launches, h2d / K, d2h / K
     host_losses = torch.empty((K + W, tr.count), dtype=torch.float64).pin_memory()
     for _ in range(W):
         tr.step()
     torch.cuda.synchronize()
     dist.barrier()
-    s = torch.cuda.current_stream()
-    spans, h2d = [], 0
     for n in chunks(K, spe):
         if e2e:
             tr.pipe._lists_dev = None  # force the epoch's lists through host memory again
@@ -741,8 +790,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-reducer", action="store_true")
     ap.add_argument("--no-bert", action="store_true", help="skip the C3 ResNet-18 and C4 BERT-base step measurements")
-    ap.add_argument("--exchange", default="ipc", choices=["ipc", "allgather"],
-                    help="N>1: peer-memory reducer over CUDA IPC, or NCCL all-gather of EST slots")
+    ap.add_argument("--exchange", default="xdev", choices=["xdev", "ipc", "allgather"],
+                    help="N>1: the lock-step persistent kernel over CUDA IPC peer memory (xdev), the per-step "
+                         "peer-memory reducer (ipc), or an NCCL all-gather of EST slots")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -49,8 +49,7 @@ class MlpArgs(C.Structure):
         ("grads", _vp), ("losses", _vp), ("rot", _vp), ("rows", _vp), ("dataset", _vp), ("lists", _vp),
         ("seed", _u64), ("step0", _i64), ("spe", _i64), ("epoch_base", _i64),
         ("flags", _vp), ("bar", _vp), ("param_trace", _vp), ("dataset_rows", _i64),
-        ("n_dev", _i32), ("dev_index", _i32), ("xin", _vp * 8), ("xflag", _vp * 8), ("xbase", C.c_uint32),
-        ("pad_x", _i32), ("xrep", _vp * 8),
+        ("n_dev", _i32), ("dev_index", _i32), ("xin", _vp * 8), ("xrep", _vp * 8),
     ]
 
 

@@ -263,7 +263,7 @@ static int validate_mlp(const bt_mlp_args* a) {
   if (a->n_dev > 1) {
     if (a->dev_index < 0 || a->dev_index >= a->n_dev) return fail(bt::ERR_INPUT, "dev_index %d of %d", a->dev_index, a->n_dev);
     for (int d = 0; d < a->n_dev; ++d)
-      if (!a->xin[d] || !a->xflag[d]) return fail(bt::ERR_INPUT, "null inbox / counter of device %d", d);
+      if (!a->xin[d]) return fail(bt::ERR_INPUT, "null inbox of device %d", d);
     if (!bt::mlp_xdev_supported(*a))
       return fail(bt::ERR_INPUT, "multi-device step: E_total in {4,8,16} over 2/4/8 devices in equal blocks, "
                                  "micro-batch 4, one Sequential/Tree(2) variant");

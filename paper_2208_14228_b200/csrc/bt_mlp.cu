@@ -689,6 +689,23 @@ __device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// Flag-in-word ("LL") transfer of one binary64 across GPUs: two 8-byte words {32 data bits, 32-bit
+// tag}, each written and read with single-copy-atomic 8-byte accesses, so a reader that sees the
+// expected tag in both words holds the value -- no fence, no counter, no extra barrier.
+__device__ __forceinline__ void ll_store(uint64_t* p, double v, uint32_t tag) {
+  const uint64_t u = d2u(v), t = (uint64_t)tag << 32;
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"((u & 0xffffffffull) | t), "l"((u >> 32) | t)
+               : "memory");
+}
+__device__ __forceinline__ void ll_load_raw(const uint64_t* p, uint64_t* w0, uint64_t* w1) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(*w0), "=l"(*w1) : "l"(p) : "memory");
+}
+__device__ __forceinline__ bool ll_ready(uint64_t w0, uint64_t w1, uint32_t tag) {
+  return (uint32_t)(w0 >> 32) == tag && (uint32_t)(w1 >> 32) == tag;
+}
+__device__ __forceinline__ double ll_value(uint64_t w0, uint64_t w1) {
+  return __longlong_as_double((long long)((w0 & 0xffffffffull) | (w1 << 32)));
+}
 
 template <int ET, int G, int F, int ND = 1>
 __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(const __grid_constant__ bt_mlp_args a,
@@ -896,6 +913,7 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
   int cur = 0, s = 0;
   for (; s < a.K; ++s) {
     const int par = (int)((a.step0 + s) & 1);
+    const uint32_t xtag = (uint32_t)(a.step0 + s + 1);  // (multi-device) tag of this mini-batch's slots
     const double* P = sm + S::PAR + cur * PAD_P;
 
     // ---- B+C (model.py:141-179, 194) --------------------------------------
@@ -961,6 +979,16 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
 #else
             ;
 #endif
+          if constexpr (ND > 1) {  // the same value into every other device's inbox (NVLink stores)
+            const int it = tid + k * S::T, el = it / (BT_P + 1), p = it - el * (BT_P + 1);
+            const size_t off = ((size_t)(par * ET + eb + e0 + el) * S::SP + p) * 2;
+#pragma unroll
+            for (int r = 1; r < ND; ++r) {
+              int d = a.dev_index + r;
+              d -= d >= ND ? ND : 0;
+              ll_store((uint64_t*)a.xin[d] + off, g, xtag);
+            }
+          }
         } else {  // loss, TrackedStat, dropout stream of EST e0+el (model.py:173, 99-104)
           const int el = (tid + k * S::T) / (BT_P + 1);
           const int e = eb + e0 + el, rb = el * S::NB;  // global rank
@@ -986,22 +1014,6 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
 #endif
       else mbar_arrive(bar);
     }
-    if constexpr (ND > 1) {  // this CTA's slots -> every other device's inbox (NVLink stores), then signal
-      __syncthreads();
-      const int warp = tid >> 5, ln = tid & 31;
-      constexpr int NW = S::T / 32;
-      constexpr int VEC = S::EPC * S::SP / 2;  // 16-byte vectors of this CTA's slots
-      const double2* src = (const double2*)(sm + S::GRAD + par * ET * S::SP + (eb + e0) * S::SP);
-      for (int r = warp; r < ND - 1; r += NW) {
-        int d = a.dev_index + 1 + r;
-        d -= d >= ND ? ND : 0;
-        double2* dst = (double2*)(a.xin[d] + (size_t)par * ET * S::SP + (size_t)(eb + e0) * S::SP);
-        for (int i = ln; i < VEC; i += 32) dst[i] = src[i];
-        fence_acq_rel_sys();
-        __syncwarp();
-        if (ln == 0) red_release_sys_add(a.xflag[d], 1u);
-      }
-    }
     BT_TICK(1)
     // the next mini-batch's rows and masks while the exchange is in flight
     if (lane && s + 1 < a.K) {
@@ -1013,42 +1025,44 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
     mbar_wait(smem_u32(&s_mbar[par]), (phases >> par) & 1u, a.flags);
     phases ^= 1u << par;
     int xok = 1;
-    if constexpr (ND > 1) {  // every other device's slots of this mini-batch have landed in our inbox
-      __shared__ int s_xok;
-      if (tid == 0) {
-        const uint32_t target = a.xbase + (uint32_t)(s + 1) * (uint32_t)((ND - 1) * G);
-        const uint32_t* fl = a.xflag[a.dev_index];
-        int okw = 1;
-        if ((int32_t)(ld_acquire_sys_u32(fl) - target) < 0) {
-          const long long tw = clock64();
-          while ((int32_t)(ld_acquire_sys_u32(fl) - target) < 0)
-            if (clock64() - tw > (1ll << 32)) {  // a device that never arrives: fail, do not hang
-              atomicCAS(a.flags + FLAG_STATUS, 0, (int)ERR_CUDA);
-              okw = 0;
-              break;
-            }
-        }
-        s_xok = okw;
-      }
-      __syncthreads();
-      xok = s_xok;
-    }
     BT_TICK(2)
 
     // ---- F: allreduce + /E + momentum SGD into the other buffer -----------
-    int ok = xok;
+    int ok = 1;
     double np = 0.0;
-    if (tid < BT_P && xok) {
+    if (tid < BT_P) {
       const double* col = sm + S::GRAD + par * ET * S::SP + tid;
 #if defined(BT_ABL) && (BT_ABL & 8)
       const double sum = col[0];
 #else
       double sum;
-      if constexpr (ND > 1) {
-        const double* inb = a.xin[a.dev_index] + (size_t)par * ET * S::SP + tid;
-        sum = fold_ranks_t<ET, F>(rot_p, [&](int q) {
-          return (unsigned)(q - eb) < (unsigned)S::EL ? col[q * S::SP] : __ldcg(inb + (size_t)q * S::SP);
-        });
+      if constexpr (ND > 1) {  // the other devices' slots: poll each until its tag is this mini-batch's
+        const uint64_t* inb = (const uint64_t*)a.xin[a.dev_index] + ((size_t)par * ET * S::SP + tid) * 2;
+        double rv[ET];
+        uint64_t w0[ET], w1[ET];
+#pragma unroll
+        for (int q = 0; q < ET; ++q)  // every remote value's first load in flight at once
+          if ((unsigned)(q - eb) >= (unsigned)S::EL) ll_load_raw(inb + (size_t)q * S::SP * 2, &w0[q], &w1[q]);
+#pragma unroll
+        for (int q = 0; q < ET; ++q) {
+          if ((unsigned)(q - eb) < (unsigned)S::EL) {
+            rv[q] = col[q * S::SP];
+            continue;
+          }
+          if (!ll_ready(w0[q], w1[q], xtag)) {  // not yet delivered: poll this one
+            const long long tw = clock64();
+            do {
+              ll_load_raw(inb + (size_t)q * S::SP * 2, &w0[q], &w1[q]);
+              if (clock64() - tw > (1ll << 32)) {  // a device that never delivers: fail, do not hang
+                atomicCAS(a.flags + FLAG_STATUS, 0, (int)ERR_CUDA);
+                xok = 0;
+                break;
+              }
+            } while (!ll_ready(w0[q], w1[q], xtag));
+          }
+          rv[q] = ll_value(w0[q], w1[q]);
+        }
+        sum = fold_ranks_t<ET, F>(rot_p, [&](int q) { return rv[q]; });
       } else {
         sum = fold_ranks_t<ET, F>(rot_p, [&](int q) { return col[q * BT_P]; });
       }
@@ -1061,8 +1075,8 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
       sm[S::PAR + (cur ^ 1) * PAD_P + tid] = np;
     }
     BT_TICK(3)
-    if (!__syncthreads_and(ok)) {  // sgd_step raises before mutating (model.py:207-209)
-      if (cta == 0 && tid == 0 && xok) {
+    if (!__syncthreads_and(ok && xok)) {  // sgd_step raises before mutating (model.py:207-209)
+      if (cta == 0 && tid == 0 && a.flags[FLAG_STATUS] == 0) {
         a.flags[FLAG_STATUS] = ERR_NUMERIC;
         a.flags[FLAG_STEP] = s;
       }

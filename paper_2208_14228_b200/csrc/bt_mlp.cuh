@@ -59,17 +59,16 @@ typedef struct bt_mlp_args {
   int64_t dataset_rows;    /* rows in `dataset` (sampler mode); lets the kernel stage it in shared memory */
   /* Multi-device exchange (n_dev > 1): this launch holds ESTs [est_base, est_base + E) of E_total,
    * est_base = dev_index * E, and runs K mini-batches in lock step with the other n_dev - 1 devices'
-   * launches: every mini-batch it stores its EST gradient slots into every device's inbox (peer
-   * memory, NVLink) and signals that device's arrival counter; it folds all E_total slots in the
-   * canonical rank order itself (bit-identical on every device).  rng / stat_mean / stat_count /
-   * est_fanin / replicas are this device's (EST pointers offset to est_base); losses is [K][E_total]
-   * and only this device's columns are written. */
+   * launches: every mini-batch each of its EST gradient values is stored into every other device's
+   * inbox (peer memory, NVLink) as two 8-byte words {32 data bits, 32-bit mini-batch tag}, and each
+   * device polls its own inbox until the tags match -- no fence, counter or host step; every device
+   * folds all E_total slots in the canonical rank order itself (bit-identical on every device).
+   * rng / stat_mean / stat_count / est_fanin / replicas are this device's (EST pointers offset to
+   * est_base); losses is [K][E_total] and only this device's columns are written. */
   int32_t n_dev;           /* 1: every EST of the job is local */
   int32_t dev_index;       /* this device's position in the exchange group */
-  double *xin[BT_MAX_XDEV];     /* every device's slot inbox [2][E_total][BT_XSP] (peer-mapped) */
-  uint32_t *xflag[BT_MAX_XDEV]; /* every device's arrival counter (peer-mapped) */
-  uint32_t xbase;          /* this device's counter value when the launch starts */
-  int32_t pad_x;
+  double *xin[BT_MAX_XDEV];     /* every device's inbox, 16 bytes per value: [2][E_total][BT_XSP][2] u64
+                                   (peer-mapped; zero-initialised; step parity x EST x parameter) */
   const double *xrep[BT_MAX_XDEV]; /* every device's first replica (peer-mapped) for the launch-start
                                       agreement check (engine.py:246-258), or all NULL to skip it --
                                       only valid when no device is still writing its replicas */

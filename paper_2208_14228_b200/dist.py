@@ -78,11 +78,14 @@ class DistributedTrainer:
 
     def __init__(self, seed=42, max_workers=8, micro_batch=4, dataset_size=1024, lr=0.02, momentum=0.9,
                  dropout_rate=0.5, jitter=0.1, bucket_capacity=64, fanin=2, comm_fanin=2, group=None,
-                 exchange: str = "allgather"):
-        """exchange: "allgather" -- NCCL all-gather of the EST slots, then the reduce kernel on every
-        rank; "ipc" -- no collective at all: each rank owns a parameter shard and its reduce kernel
+                 exchange: str | None = None):
+        """exchange (None: "xdev" where its shape applies, else "allgather"): "xdev" -- the persistent
+        lock-step kernel: K mini-batches per launch,
+        EST slots stored into every rank's inbox over CUDA IPC peer memory with device-side counters
+        (run(K)); "ipc" -- no collective at all: each rank owns a parameter shard and its reduce kernel
         reads every rank's slots and writes every rank's replica through CUDA IPC peer pointers,
-        ordered by stream memory operations (paper_2208_14228_b200.peer)."""
+        ordered by stream memory operations (paper_2208_14228_b200.peer); "allgather" -- NCCL
+        all-gather of the EST slots, then the reduce kernel on every rank."""
         require_cuda()
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.E, self.B = max_workers, micro_batch
@@ -106,6 +109,9 @@ class DistributedTrainer:
         self.pipe = DataPipeline(seed, dataset_size, self.E, micro_batch, jitter, 2, 2)
         self.flags = Flags()
         self.step_idx = 0
+        if exchange is None:  # the lock-step kernel wherever its shape applies
+            exchange = "xdev" if (self.world in (2, 4, 8) and self.E in (4, 8, 16) and self.E % self.world == 0
+                                  and micro_batch == 4 and fanin == comm_fanin and fanin in (0, 2)) else "allgather"
         self.exchange = exchange
         self.peer = None
         if exchange == "ipc":
@@ -119,11 +125,76 @@ class DistributedTrainer:
             self.peer = PeerGroupReducer(
                 RankBuffers(self.grads_loc, self.params[0], self.params[1], torch.cuda.current_stream()), self.E,
                 "sequential" if comm_fanin == 0 else "tree2_rotated", self.rot, lr, momentum, group)
+        elif exchange == "xdev":
+            self._init_xdev(group, fanin)
         elif exchange != "allgather":
             raise ConfigError(f"unknown exchange {exchange!r}")
 
+    # ------------------------------------------------------------------ lock-step (xdev)
+    KMAX = 128
+
+    def _init_xdev(self, group, fanin: int) -> None:
+        """The persistent multi-GPU step: every rank runs K mini-batches in ONE launch of the fused
+        step kernel (bt_mlp.cu, n_dev = world), storing its EST slots into every other rank's inbox
+        (CUDA IPC peer memory over NVLink) as tagged 8-byte words each mini-batch, polled by the
+        receiver; each rank folds all E slots in the canonical order itself.  No host, NCCL or stream operation
+        per mini-batch."""
+        from .peer import _export, _Opened
+
+        if not (self.E in (4, 8, 16) and self.world in (2, 4, 8) and self.E % self.world == 0 and self.B == 4
+                and fanin == self.comm_fanin and fanin in (0, 2)):
+            raise ConfigError("the lock-step exchange needs E in {4,8,16} over 2/4/8 ranks, micro-batch 4 and "
+                              "one Sequential/Tree(2) variant")
+        from .placement import inbox_words
+
+        self.inbox = torch.zeros(inbox_words(self.E), dtype=torch.int64, device="cuda")
+        self.xlosses = torch.zeros((self.KMAX, self.E), dtype=torch.float64, device="cuda")
+        table = [None] * self.world
+        dist.all_gather_object(table, _export(self.inbox), group=group)
+        self.opened = _Opened()
+        self.xin = [self.inbox.data_ptr() if q == self.rank else self.opened.ptr(*table[q]) for q in range(self.world)]
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # every rank's inbox is zero before any launch writes into it
+
+    def xdev_args(self, K: int) -> _native.MlpArgs:
+        """The launch of the next K mini-batches (caller keeps the lists tensor alive)."""
+        spe = self.pipe.steps_per_epoch
+        gs = self.step_idx
+        lists, lbase = self.pipe.device_lists(gs // spe, (gs + K - 1) // spe)
+        self._xlists = lists
+        a = _native.MlpArgs()
+        a.E, a.est_base, a.E_total, a.B, a.X, a.K = self.count, self.base, self.E, self.B, 1, K
+        a.fuse_reduce, a.est_per_cta = 1, 1
+        a.comm_fanin, a.est_fanin_uniform, a.rank_override = self.comm_fanin, self.comm_fanin + 1, -1
+        a.rate, a.lr, a.mu, a.jitter = self.rate, self.lr, self.mu, self.jitter
+        a.replicas, a.est_fanin, a.rng = self.params.data_ptr(), self.fan.data_ptr(), self.rng.data_ptr()
+        a.stat_mean, a.stat_count = self.stat_mean.data_ptr(), self.stat_count.data_ptr()
+        a.grads, a.losses = self.grads_loc.data_ptr(), self.xlosses.data_ptr()
+        a.rot = self.rot.data_ptr() if self.rot is not None else None
+        a.dataset, a.lists, a.dataset_rows = self.pipe.dataset_device.data_ptr(), lists.data_ptr(), self.pipe.dataset_size
+        a.seed, a.step0, a.spe, a.epoch_base = self.seed & (2**64 - 1), gs, spe, lbase
+        a.flags, a.bar = self.flags.t.data_ptr(), None
+        a.n_dev, a.dev_index = self.world, self.rank
+        for q in range(self.world):
+            a.xin[q] = self.xin[q]
+        return a
+
+    def run(self, K: int) -> torch.Tensor:
+        """K mini-batches in one lock-step launch (every rank must call run(K) with the same K);
+        returns the losses [K][E] (this rank's EST columns filled), on the device."""
+        if self.exchange != "xdev":
+            raise ConfigError("run(K) is the lock-step exchange's entry point")
+        if K < 1 or K > self.KMAX:
+            raise ConfigError(f"K must be in [1, {self.KMAX}]")
+        a = self.xdev_args(K)
+        _native.check(_native.lib().bt_mlp_step(C.byref(a), stream()), "lock-step step")
+        self.step_idx += K
+        return self.xlosses[:K]
+
     def step(self) -> torch.Tensor:
         """One mini-batch; returns this rank's per-EST losses (device tensor)."""
+        if self.exchange == "xdev":
+            return self.run(1)[0, self.base:self.base + self.count]
         spe = self.pipe.steps_per_epoch
         epoch, local = divmod(self.step_idx, spe)
         lists, lbase = self.pipe.device_lists(epoch, epoch)
@@ -156,6 +227,13 @@ class DistributedTrainer:
         _native.check(_native.lib().bt_reduce_update(C.byref(r), stream()), "reduce_update")
         self.step_idx += 1
         return self.losses
+
+    def close(self) -> None:
+        torch.cuda.synchronize()
+        if self.peer is not None:
+            self.peer.close()
+        if getattr(self, "opened", None) is not None:
+            self.opened.close()
 
     def check(self) -> None:
         if self.peer is not None:

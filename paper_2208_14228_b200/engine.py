@@ -611,9 +611,8 @@ class _XdevStep:
         E, n = cfg.max_workers, len(dev.shards)
         self.dev, self.n = dev, n
         self.group = placement.XGroup([sh.ordinal for sh in dev.shards], E)
-        self.G = min(E // n, 8)
         fan = fanin_code(_comm_variant(ts))
-        xin, xflag = self.group.tables()
+        xin = self.group.table()
         lib = _native.lib()
         self.args, self.keep = [], []
         self.losses_dev, self.host_losses, self.host_status = [], [], []
@@ -637,7 +636,7 @@ class _XdevStep:
             a.flags, a.bar = sh.flags.t.data_ptr(), sh.bar.data_ptr()
             a.n_dev, a.dev_index = n, i
             for q in range(n):
-                a.xin[q], a.xflag[q] = xin[q], xflag[q]
+                a.xin[q] = xin[q]
                 a.xrep[q] = dev.shards[q].replicas.data_ptr()  # launch-start agreement of every GPU
             self.args.append(a)
             self.losses_dev.append(losses)
@@ -659,14 +658,13 @@ class _XdevStep:
         lists, base = ts.pipeline.device_lists(gs // spe, (gs + K - 1) // spe)
         rot = _rot_tensor(ts)
         ex0 = ts.executors[0]
-        xbase = self.group.xbase(self.G)
         keep = []
         for a, sh in zip(self.args, self.dev.shards):
             ls, rt = sh.on(lists, "lists"), sh.on(rot, "rot")
             keep += [ls, rt]
             a.K, a.step0, a.lists, a.epoch_base = K, gs, ls.data_ptr(), base
             a.rot = ptr(rt)
-            a.lr, a.mu, a.xbase = float(ex0._lr), float(ex0._mu), xbase
+            a.lr, a.mu = float(ex0._lr), float(ex0._mu)
             a.param_trace = None
         self.args[0].param_trace = ptr(trace)
         for sh in self.dev.shards:  # after everything already queued on the GPU's current stream
@@ -681,14 +679,10 @@ class _XdevStep:
         sts = [(int(x[0]), int(x[1]), int(x[2])) for x in self.status_np]
         bad = [t for t in sts if t[0]]
         if not bad:
-            self.group.steps += K
             return 0, 0, 0, out
         for sh in self.dev.shards:
             sh.flags.reset()
-        if all(t[0] == 5 for t in sts) and len({t[2] for t in sts}) == 1:
-            self.group.steps += sts[0][2] + 1  # every GPU stopped after the same exchanged mini-batch
-        else:
-            self.dev.xstep = None  # the counters are out of step: a fresh group next time
+        self.dev.xstep = None  # a retry of the same mini-batch reuses its tags: fresh inboxes next time
         worst = next((t for t in bad if t[0] == 6), None) or next((t for t in bad if t[0] != 9), bad[0])
         return worst[0], worst[1], worst[2], out
 

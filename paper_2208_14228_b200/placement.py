@@ -13,7 +13,8 @@ one process drives every GPU of the box and executor x of a layout runs on a CUD
     load and store the others' memory over NVLink.
 
 `XGroup` holds the per-device exchange buffers of a lock-step multi-device step (bt_mlp.cu,
-n_dev > 1): a slot inbox [2][E][BT_XSP] binary64 and a 32-bit arrival counter per device.
+n_dev > 1): a slot inbox of [2][E][BT_XSP] values per device, 16 bytes per value (two tagged
+8-byte words).
 """
 
 from __future__ import annotations
@@ -67,22 +68,22 @@ def enable_peer_access(ordinals: list[int]) -> None:
 
 
 class XGroup:
-    """Exchange buffers of one lock-step multi-device step: per device an inbox and a counter."""
+    """Exchange buffers of one lock-step multi-device step: one zero-initialised inbox per device."""
 
     def __init__(self, ordinals: list[int], E: int):
         self.ordinals, self.E = list(ordinals), E
-        self.inbox, self.flag = [], []
+        self.inbox = []
         for d in self.ordinals:
             with torch.cuda.device(d):
-                self.inbox.append(torch.zeros(2 * E * _native.BT_XSP, dtype=torch.float64, device="cuda"))
-                self.flag.append(torch.zeros(4, dtype=torch.int32, device="cuda"))
-        self.steps = 0  # mini-batches exchanged since the counters were zero
+                self.inbox.append(torch.zeros(inbox_words(E), dtype=torch.int64, device="cuda"))
 
-    def xbase(self, ctas_per_device: int) -> int:
-        return (self.steps * (len(self.ordinals) - 1) * ctas_per_device) & 0xFFFFFFFF
-
-    def tables(self) -> tuple[list[int], list[int]]:
-        return [t.data_ptr() for t in self.inbox], [t.data_ptr() for t in self.flag]
+    def table(self) -> list[int]:
+        return [t.data_ptr() for t in self.inbox]
 
 
-__all__ = ["set_devices", "devices", "executor_devices", "enable_peer_access", "XGroup"]
+def inbox_words(E: int) -> int:
+    """8-byte words of one device's inbox: [2 parities][E][BT_XSP][2 tagged halves]."""
+    return 2 * E * _native.BT_XSP * 2
+
+
+__all__ = ["set_devices", "devices", "executor_devices", "enable_peer_access", "XGroup", "inbox_words"]

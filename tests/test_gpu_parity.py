@@ -358,7 +358,7 @@ def test_distributed_trainer_single_rank_matches_reference(bt):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
-        tr = DistributedTrainer(seed=42, max_workers=8, micro_batch=4, dataset_size=1024)
+        tr = DistributedTrainer(seed=42, max_workers=8, micro_batch=4, dataset_size=1024, exchange="allgather")
         for step in range(40):
             losses = tr.step()
             assert fhl(losses.tolist()) == r["losses"][step], step

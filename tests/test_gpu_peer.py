@@ -211,3 +211,98 @@ def test_two_process_ipc_reducer_non_finite_changes_nothing(variant):
     p = rng.uniform(-1, 1, n).astype(np.float32)
     for r in (0, 1):
         assert res[r][0] == p.tobytes() and res[r][1] == np.zeros(n, np.float32).tobytes()
+
+
+def _xdev_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root))
+    import torch.distributed as dist
+
+    from paper_2208_14228_b200.dist import DistributedTrainer
+    from paper_2208_14228_b200.runlog import param_fingerprint
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        tr = DistributedTrainer(seed=42, max_workers=8, micro_batch=4, dataset_size=1024)
+        assert tr.exchange == "xdev"
+        losses, hashes = [], []
+        for K in (1, 7, 32, 60):  # 100 mini-batches in lock-step launches of varying length
+            out = tr.run(K).cpu().numpy()
+            losses += [row[tr.base:tr.base + tr.count].tobytes() for row in out]
+            hashes.append(param_fingerprint(tr.params[0].cpu().numpy().tobytes()))
+        tr.check()
+        dist.barrier()
+        q.put((rank, hashes, losses))
+        dist.barrier()
+        tr.close()
+    except Exception:
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_lockstep_multi_process_matches_reference(world):
+    """The persistent lock-step kernel across processes (CUDA IPC inboxes + counters; the processes
+    share this box's GPU): C2's 100 mini-batches in 4 launches per rank reproduce the reference's
+    per-step losses and the fingerprints at every launch boundary, on every rank."""
+    import struct
+
+    import torch.multiprocessing as mp
+
+    from golden_util import load
+
+    r = next(x for x in load("runs.json")["runs"] if x["name"] == "c2_d1")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_xdev_worker, args=(k, world, port, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = {}
+        for _ in procs:
+            k, hashes, losses = q.get(timeout=240)
+            assert hashes != "error", losses
+            res[k] = (hashes, losses)
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    n = 8 // world
+    for k in range(world):
+        assert res[k][0] == [r["param_hash"][i] for i in (0, 7, 39, 99)]
+        for step, blob in enumerate(res[k][1]):
+            got = [struct.pack("<d", v).hex() for v in struct.unpack(f"<{len(blob) // 8}d", blob)]
+            assert got == r["losses"][step][n * k: n * k + n], (k, step)
+
+
+def test_bench_runs_n_ranks_when_asked():
+    """`python bench.py --gpus 2` without a launcher spawns 2 ranks itself: the line reports
+    n_gpus 2 and the same final-weight fingerprint as the 1-GPU run of the same steps."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    args = ["--steps", "20", "--warmup", "5", "--no-bert", "--no-reducer", "--cpu-seconds", "0"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    lines = {}
+    for n in (1, 2):
+        out = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", str(n), *args], cwd=root, env=env,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-3000:]
+        lines[n] = json.loads(out.stdout.strip().splitlines()[-1])
+    assert lines[1]["n_gpus"] == 1 and lines[2]["n_gpus"] == 2
+    assert lines[2]["config"]["exchange"] == "xdev"
+    assert lines[2]["weights_fnv"] == lines[1]["weights_fnv"]
+    assert lines[2]["value"] > 0 and lines[2]["e2e"]["value"] > 0
