@@ -4,6 +4,9 @@ from pathlib import Path
 import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
+# the reference's own tests, vendored by tools/vendor_reference_tests.py, run only through
+# test_gpu_reference_suite.py (they need the GPU and the `bittrain` alias of their own conftest)
+collect_ignore = ["_reference"]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
