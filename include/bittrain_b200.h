@@ -315,10 +315,10 @@ int bt_est_slot_copy(void *const *dst_dev, const void *const *src_dev, const int
  * src_dev to every dst in dst_dev[0..ndst) (bit copies, deterministic).   engine.py:313-315 */
 int bt_allgather_params(int32_t dtype, const void *src_dev, void *const *dst_dev, int32_t ndst, int64_t n,
                         void *stream);
-/* Reset a status block to {0, INT32_MAX, 0, 0}. */
 /* Stream-ordered copy between any two device (or peer / IPC-mapped / pinned host) addresses:
  * the guarded multi-rank reducer publishes each shard's status word with it. */
 int bt_memcpy_async(void *dst, const void *src, int64_t nbytes, void *stream);
+/* Reset a status block to {0, INT32_MAX, 0, 0}. */
 int bt_flags_reset(int32_t *flags_dev, void *stream);
 /* Synchronise `stream`, read the status block; returns its status word. */
 int bt_step_status(const int32_t *flags_dev, int32_t *detail_out, int32_t *step_out, void *stream);

@@ -36,6 +36,10 @@ def _gelu_grad(x):
 
 SMALL = dict(ests=4, seqs=2, layers=2, d_model=256, heads=4, d_ff=512, seed=3, lr=0.01, momentum=0.9,
              p_hidden=0.1, p_attn=0.1)
+# the benched C4 shapes (BERT-base: d 768, 12 heads, FFN 3072, seq 128): the CTA-pair GEMM with the
+# 16-warp GELU epilogue at N = 3072 / K = 768, LayerNorm at D = 768, tcgen05 attention at 12 heads
+BASE = dict(ests=2, seqs=2, layers=2, d_model=768, heads=12, d_ff=3072, seed=3, lr=0.01, momentum=0.9,
+            p_hidden=0.1, p_attn=0.1)
 
 GAMMA = np.uint64(0x9E3779B97F4A7C15)
 TAG_HDROP = 0x4245_5254_4844_5250
@@ -140,10 +144,11 @@ def _ln_bwd(dy, x, g, eps):
     return (gg - gg.mean(-1, keepdim=True) - xh * (gg * xh).mean(-1, keepdim=True)) * rstd, xh
 
 
-def test_layer0_stages_match_float64_restatement(bert):
+@pytest.mark.parametrize("cfg", [SMALL, BASE], ids=["small", "bert_base_dims"])
+def test_layer0_stages_match_float64_restatement(bert, cfg):
     from paper_2208_14228_b200._native import host_derive_stream
 
-    job = bert.BertJob(**SMALL)
+    job = bert.BertJob(**cfg)
     P0 = job.params.clone()
     cap = {}
     losses = job.step(capture=cap)

@@ -366,3 +366,41 @@ def test_distributed_trainer_single_rank_matches_reference(bt):
         tr.check()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("rate", [0.0, 0.1, 0.5, 0.9, 1.0])
+def test_dropout_mask_entry_point_matches_reference_draws(bt, oracle, rate):
+    """bt_dropout_mask (model.py:151-161): one draw per (row, unit), rows outer, u < rate drops,
+    kept units scaled by 1/(1-rate); no draws at rate 0; everything dropped at rate >= 1."""
+    import ctypes as C
+
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    state = derive = oracle.derive_stream(0xD80F0D7A6B15EA5E, 42, 5)
+    rows, units = 37, 16
+    out = torch.empty(rows * units, dtype=torch.float64, device="cuda")
+    _native.check(_native.lib().bt_dropout_mask(state, rows, units, rate, out.data_ptr(), stream()))
+    raw = np.array(oracle.splitmix64_stream(derive, rows * units), dtype=np.uint64)
+    u = (raw >> np.uint64(11)).astype(np.float64) * 2.0**-53
+    keep = 0.0 if rate >= 1.0 else 1.0 / (1.0 - rate)
+    want = np.ones(rows * units) if rate == 0.0 else np.where(u < rate, 0.0, keep)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("dtype,es", [(0, 8), (1, 4)])
+def test_allgather_params_entry_point_copies_bits(bt, dtype, es):
+    """bt_allgather_params: the parameter all-gather as bit copies into every destination
+    (engine.py:313-315), including a length that is not a multiple of the 16-byte vector."""
+    import ctypes as C
+
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    n = 10_003
+    src = torch.randint(-2**31, 2**31 - 1, (n * es // 4,), dtype=torch.int32, device="cuda")
+    dsts = [torch.zeros_like(src) for _ in range(5)]
+    table = (C.c_void_p * 5)(*[d.data_ptr() for d in dsts])
+    _native.check(_native.lib().bt_allgather_params(dtype, src.data_ptr(), table, 5, n, stream()))
+    for d in dsts:
+        assert torch.equal(d, src)

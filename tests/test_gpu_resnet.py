@@ -23,6 +23,7 @@ import torch.nn.functional as Fn
 pytestmark = pytest.mark.gpu
 
 SMALL = dict(ests=16, batch=4, seed=7, lr=0.05, momentum=0.9)
+BENCHED = dict(ests=2, batch=32, seed=7, lr=0.05, momentum=0.9)  # the benched per-EST shape (C3: 32 images)
 
 
 @pytest.fixture(scope="module")
@@ -105,8 +106,9 @@ def _nchw(t, n, h, c):
     return _d(t).view(n, h, h, c).permute(0, 3, 1, 2)
 
 
-def test_stem_and_block_stages_match_float64(rn):
-    job = rn.ResNetJob(gpus=1, **SMALL)
+@pytest.mark.parametrize("cfg", [SMALL, BENCHED], ids=["batch4", "batch32"])
+def test_stem_and_block_stages_match_float64(rn, cfg):
+    job = rn.ResNetJob(gpus=1, **cfg)
     P0 = job.params.clone()
     cap = {}
     job.step(capture=cap)
@@ -169,11 +171,12 @@ def _restate_loss(job, P, img, labels):
     return ce.view(E, B).mean(1)
 
 
-def test_loss_and_last_block_gradients_match_float64(rn):
+@pytest.mark.parametrize("cfg", [SMALL, BENCHED], ids=["batch4", "batch32"])
+def test_loss_and_last_block_gradients_match_float64(rn, cfg):
     """Whole-network loss vs the float64 restatement; the head and the last BasicBlock's backward
     (ReLU mask, BatchNorm backward with per-EST statistics, per-EST conv weight gradient) stage by
     stage from the captured bf16 tensors."""
-    job = rn.ResNetJob(gpus=1, **SMALL)
+    job = rn.ResNetJob(gpus=1, **cfg)
     P0 = job.params.clone()
     cap = {}
     losses = job.step(capture=cap)
