@@ -188,6 +188,33 @@ int bt_gemm_conv(int32_t wgrad, const void *x_dev, int32_t xN, int32_t xH, int32
 int bt_colsum_bf16_strided(const void *in_dev, int32_t E, int32_t R, int32_t C, float *out_dev, int64_t out_stride,
                            float *scratch_dev, void *stream);
 
+/* C4 input / output layers (csrc/bt_embed.cu; synthetic token ids from splitmix64
+ * mod the vocabulary).  Per sequence of 128 tokens: ids from the EST's token stream, `npred` masked
+ * positions by a partial Fisher-Yates of the EST's mask stream (sorted), [MASK] = mask_id at those
+ * inputs; mrow / mlabel: the masked rows of the launch and their original ids. */
+int bt_bert_tokens(uint64_t seed, int64_t step, const int64_t *step_dev, int32_t est_base, int32_t E, int32_t seqs,
+                   int32_t vocab, int32_t npred, int32_t mask_id, int32_t *ids_dev, int32_t *mrow_dev,
+                   int32_t *mlabel_dev, void *stream);
+/* x32[t] = wemb[ids[t]] + pemb[t % 128] (fp32), xb = bf16(x32) */
+int bt_bert_embed_fwd(const int32_t *ids_dev, const float *wemb_dev, const float *pemb_dev, int32_t T, int32_t D,
+                      float *x32_dev, void *xb_dev, void *stream);
+/* bf16 row gather out[r] = in[rows[r]] / scatter dst[rows[r]] = src[r] (other rows of dst zeroed) */
+int bt_rows_gather(const void *in_dev, const int32_t *rows_dev, int32_t R, int32_t D, void *out_dev, void *stream);
+int bt_rows_scatter(const void *src_dev, const int32_t *rows_dev, int32_t R, int32_t npred, int32_t T, int32_t D,
+                    void *dst_dev, void *stream);
+/* Masked-LM cross-entropy: logits [R][vocab_pad] fp32 (columns >= vocab ignored); per-row loss, the
+ * per-EST mean over its rows_per_est rows (row order), dlogits = (softmax - onehot) / rows_per_est
+ * as bf16 [R][vocab_pad] (padding 0). */
+int bt_bert_mlm_ce(const float *logits_dev, const int32_t *labels_dev, int32_t R, int32_t vocab, int32_t vocab_pad,
+                   int32_t E, int32_t rows_per_est, void *dlogits_dev, float *row_loss_dev, float *loss_dev,
+                   void *stream);
+/* Embedding gradient without atomics: per gradient leaf, the (id, token) pairs sorted in shared
+ * memory; per distinct id the rows dx = dxa (bf16) + dxb (fp32) summed in token order and ADDED to
+ * dwemb[leaf][id] (which holds the tied decoder's GEMM gradient); dpemb[leaf][p] = the sum over the
+ * leaf's sequences, in order.  seg_* : scratch [leaves][leaf_tokens] x2 + [leaves]. */
+int bt_bert_embed_grad(const void *dxa_dev, const float *dxb_dev, const int32_t *ids_dev, int32_t leaves,
+                       int32_t leaf_tokens, int32_t D, int32_t *seg_tok_dev, int32_t *seg_first_dev,
+                       int32_t *seg_n_dev, float *dwemb_dev, float *dpemb_dev, int64_t leaf_stride, void *stream);
 /* ---------------- per-EST BERT encoder step (C4, no reference) ------------
  * Post-LN BERT layer (attention with 64-wide heads over 128-token sequences,
  * LayerNorm, GELU FFN, hidden and attention-probability dropout).  Tokens of

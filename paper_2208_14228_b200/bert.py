@@ -22,11 +22,16 @@ So the trained weights are bit-identical however the ESTs are grouped into
 launches (`groups=`), which is what mapping them onto 1/2/4/8 GPUs does: a GPU
 holding a contiguous EST block runs exactly one such group.
 
-The model head is a per-token regression (MSE against synthetic targets) on
-the encoder output; token embeddings and the MLM head are not modelled (the
-inputs are synthetic embedded tokens).  There is no reference implementation
-of this model: parity is against a float64 restatement of every
-stage with the same bf16 rounding points (tests/test_gpu_bert.py).
+Input and output layers (head="mlm", the default; csrc/bt_embed.cu): synthetic token ids from
+splitmix64 mod the vocabulary (30522), word + position embeddings, and BERT's masked-LM
+objective -- `npred` (20) masked positions per 128-token sequence, [MASK] inputs there, a decoder
+tied to the word embedding (logits = y_m W_emb^T + b over the vocabulary, tcgen05 GEMMs) and a
+softmax cross-entropy; the embedding gradient (tied decoder GEMM + a per-leaf sorted segment sum of
+the input-side rows, no atomics) lands in the gradient slot like every other parameter.  (Not
+modelled: token-type embeddings, the embedding LayerNorm and the MLM transform layer.)
+head="mse": a per-token regression on synthetic embedded inputs (the round-1 head).  There is no
+reference implementation of this model: parity is against a float64 restatement of
+every stage with the same bf16 rounding points (tests/test_gpu_bert.py).
 """
 
 from __future__ import annotations
@@ -56,7 +61,8 @@ class BertJob:
                  d_ff: int = 3072, seed: int = 42, lr: float = 1e-3, momentum: float = 0.9, p_hidden: float = 0.1,
                  p_attn: float = 0.1, fanin: int = 0, eps: float = 1e-12, est_base: int = 0,
                  est_count: int | None = None, est_group: int = 1, optimizer: str = "sgd",
-                 adam_beta2: float = 0.999, adam_eps: float = 1e-8, graph: bool = True):
+                 adam_beta2: float = 0.999, adam_eps: float = 1e-8, graph: bool = True, head: str = "mlm",
+                 vocab: int = 30522, npred: int = 20, mask_id: int = 103):
         """`est_base` / `est_count`: this process computes ESTs [est_base, est_base + est_count) of the E
         (one rank of a multi-GPU job, `attach_peer`); default all E.
         `est_group` (g): gradient leaf group.  g = 1: one gradient buffer per EST, summed by the reducer in
@@ -69,7 +75,9 @@ class BertJob:
         the reducer's final pass as well, bias corrections from the step count).
         `graph`: after one eager step, the whole step (all launch groups, the reducer, the bf16 weight
         refresh, the device step counter) is captured once as a CUDA graph and replayed -- no per-kernel
-        host launches; every kernel reads the step from the device counter, so replays are exact."""
+        host launches; every kernel reads the step from the device counter, so replays are exact.
+        `head`: "mlm" (token ids, embeddings, masked-LM cross-entropy over `vocab` with `npred` masked
+        positions per sequence) or "mse" (regression on synthetic embedded inputs)."""
         require_cuda()
         if heads * 64 != d_model or d_model % 256 or d_model > 1024 or d_ff % 256:
             raise ConfigError("d_model = 64 * heads, a multiple of 256 (<= 1024); d_ff a multiple of 256")
@@ -88,6 +96,12 @@ class BertJob:
             raise ConfigError(f"gradient leaf group {est_group} must divide E and the local EST block")
         if fanin == 2 and (ests // self.g) & (ests // self.g - 1):
             raise ConfigError("Tree(2) needs a power-of-two number of gradient leaves")
+        if head not in ("mlm", "mse"):
+            raise ConfigError(f"head {head!r}: 'mlm' or 'mse'")
+        if head == "mlm" and not (2 <= vocab and 1 <= npred <= 32 and 0 <= mask_id < vocab):
+            raise ConfigError("mlm head: vocab >= 2, 1 <= npred <= 32, mask_id in the vocabulary")
+        self.head, self.V, self.NP, self.mask_id = head, vocab, npred, mask_id
+        self.Vp = -(-vocab // 256) * 256  # padded vocabulary (GEMM tiles); the padding rows stay zero
         self.peer = None
         self.Te = seqs * 128
         self.seed, self.lr, self.mu, self.fanin = seed, lr, momentum, fanin
@@ -96,8 +110,14 @@ class BertJob:
         shapes = {"Wqkv": (3 * D, D), "bqkv": (3 * D,), "Wo": (D, D), "bo": (D,), "g1": (D,), "be1": (D,),
                   "W1": (F, D), "b1": (F,), "W2": (D, F), "b2": (D,), "g2": (D,), "be2": (D,)}
         self.shapes = shapes
-        self.off = []  # per layer: name -> flat offset (floats; all multiples of 256)
+        self.eoff = {}  # mlm head: Wemb [Vp][D], Pemb [128][D], bdec [Vp] ahead of the layers
         o = 0
+        if head == "mlm":
+            shapes.update({"Wemb": (self.Vp, D), "Pemb": (128, D), "bdec": (self.Vp,)})
+            for k in ("Wemb", "Pemb", "bdec"):
+                self.eoff[k] = o
+                o += int(torch.Size(shapes[k]).numel())
+        self.off = []  # per layer: name -> flat offset (floats; all multiples of 256)
         for _ in range(layers):
             d = {}
             for k in _LAYER:
@@ -113,6 +133,9 @@ class BertJob:
                                       .view(rows, cols))
             self.view(l, "g1").fill_(1.0)
             self.view(l, "g2").fill_(1.0)
+        if head == "mlm":  # the embeddings (uniform, BERT's 0.02 scale); padding rows and the bias zero
+            self.eview("Wemb")[:vocab].copy_(_init_uniform(seed * 1000003 + 7919, vocab * D, 0.02).view(vocab, D))
+            self.eview("Pemb").copy_(_init_uniform(seed * 1000003 + 7927, 128 * D, 0.02).view(128, D))
         self.vel = torch.zeros_like(self.params)
         if optimizer not in ("sgd", "adam"):
             raise ConfigError(f"optimizer {optimizer!r}: 'sgd' or 'adam'")
@@ -121,7 +144,7 @@ class BertJob:
         self.grads = torch.empty(self.En // self.g, self.P, dtype=torch.float32, device="cuda")  # gradient leaves
         # bf16 operand copies: W [out][in] (forward) and W^T [in][out] (dX products)
         self._moff = []
-        m = 0
+        m = self.Vp * D if head == "mlm" else 0  # the word embedding's bf16 copies come first
         for _ in range(layers):
             d = {}
             for k in _MATS:
@@ -130,10 +153,15 @@ class BertJob:
             self._moff.append(d)
         self.wb = torch.empty(m, dtype=torch.bfloat16, device="cuda")
         self.wt = torch.empty(m, dtype=torch.bfloat16, device="cuda")
-        n = layers * len(_MATS)
+        n = layers * len(_MATS) + (1 if head == "mlm" else 0)
         self._cast = [(C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_int32 * n)(),
                       (C.c_int32 * n)()]
         i = 0
+        if head == "mlm":  # Wemb [Vp][D] -> bf16 [Vp][D] (logits) and [D][Vp] (dy_m)
+            self._cast[0][0] = self.params.data_ptr() + 4 * self.eoff["Wemb"]
+            self._cast[1][0], self._cast[2][0] = self.wb.data_ptr(), self.wt.data_ptr()
+            self._cast[3][0], self._cast[4][0] = self.Vp, D
+            i = 1
         for l in range(layers):
             for k in _MATS:
                 rows, cols = shapes[k]
@@ -156,6 +184,18 @@ class BertJob:
         t = self.params if t is None else t
         o, shape = self.off[layer][name], self.shapes[name]
         return t[o:o + int(torch.Size(shape).numel())].view(shape)
+
+    def eview(self, name: str, t: torch.Tensor | None = None) -> torch.Tensor:
+        """Embedding-layer parameter (Wemb / Pemb / bdec) as a view of the flat buffer (or a gradient row)."""
+        t = self.params if t is None else t
+        o, shape = self.eoff[name], self.shapes[name]
+        return t[o:o + int(torch.Size(shape).numel())].view(shape)
+
+    def _ep(self, k):
+        return self.params.data_ptr() + 4 * self.eoff[k]
+
+    def _eg(self, base, k):  # local EST `base`'s gradient leaf for an embedding-layer parameter
+        return self.grads.data_ptr() + 4 * ((base // self.g) * self.P + self.eoff[k])
 
     def _wb(self, l, k):
         return self.wb.data_ptr() + 2 * self._moff[l][k]
@@ -193,8 +233,17 @@ class BertJob:
             "dres": [torch.empty(T, D, **f32) for _ in range(2)],
             "dbr": torch.empty(T, D, **bf), "dHpre": torch.empty(T, F, **bf), "dctx": torch.empty(T, D, **bf),
             "dqkv": torch.empty(T, 3 * D, **bf), "lnpart": torch.empty(n * (Te // 64) * 3 * D, **f32),
-            "colsum": torch.empty(n * -(-Te // 64) * max(3 * D, F), **f32), "msepart": torch.empty(n * 64, **f32),
+            "colsum": torch.empty(max(n * -(-Te // 64) * max(3 * D, F),
+                                      (n // self.g) * -(-(self.g * self.S * self.NP) // 64) * self.Vp), **f32),
+            "msepart": torch.empty(n * 64, **f32),
         }
+        if self.head == "mlm":
+            R, i32 = n * self.S * self.NP, dict(dtype=torch.int32, device="cuda")
+            ws.update({"ids": torch.empty(T, **i32), "mrow": torch.empty(R, **i32), "mlabel": torch.empty(R, **i32),
+                       "ym": torch.empty(R, D, **bf), "logits": torch.empty(R, self.Vp, **f32),
+                       "dlogits": torch.empty(R, self.Vp, **bf), "rowloss": torch.empty(R, **f32),
+                       "dym": torch.empty(R, D, **bf), "seg_tok": torch.empty(T, **i32),
+                       "seg_first": torch.empty(T, **i32), "seg_n": torch.empty(max(n // self.g, 1), **i32)})
         self._ws[n] = ws
         return ws
 
@@ -222,8 +271,15 @@ class BertJob:
         seed, step = self.seed & (2**64 - 1), self.step_idx
         ws = self._workspace(n)
         lay = ws["layers"]
-        _native.check(L.bt_bert_data(seed, step, base, n, Te, D, ws["x32"].data_ptr(), lay[0]["xb"].data_ptr(),
-                                     ws["tgt"].data_ptr(), sp, s))
+        if self.head == "mlm":  # token ids + masked positions, then word + position embeddings
+            _native.check(L.bt_bert_tokens(seed, step, sp, base, n, self.S, self.V, self.NP, self.mask_id,
+                                           ws["ids"].data_ptr(), ws["mrow"].data_ptr(), ws["mlabel"].data_ptr(), s),
+                          "bert tokens")
+            _native.check(L.bt_bert_embed_fwd(ws["ids"].data_ptr(), self._ep("Wemb"), self._ep("Pemb"), T, D,
+                                              ws["x32"].data_ptr(), lay[0]["xb"].data_ptr(), s), "bert embedding")
+        else:
+            _native.check(L.bt_bert_data(seed, step, base, n, Te, D, ws["x32"].data_ptr(), lay[0]["xb"].data_ptr(),
+                                         ws["tgt"].data_ptr(), sp, s))
         x32 = ws["x32"]
         for l in range(NL):
             w = lay[l]
@@ -265,8 +321,11 @@ class BertJob:
             x32 = y32
         # gradients between GEMMs bf16 (A: into LN2', Db: into LN1'), residual-path gradients fp32 (B, Cb)
         (A, Db), (B, Cb) = ws["dy1"], ws["dres"]
-        _native.check(L.bt_bert_mse(x32.data_ptr(), ws["tgt"].data_ptr(), n, Te, D, A.data_ptr(),
-                                    ws["msepart"].data_ptr(), losses[lb:].data_ptr(), s))
+        if self.head == "mlm":
+            self._mlm_head(ws, n, lb, losses, capture)
+        else:
+            _native.check(L.bt_bert_mse(x32.data_ptr(), ws["tgt"].data_ptr(), n, Te, D, A.data_ptr(),
+                                        ws["msepart"].data_ptr(), losses[lb:].data_ptr(), s))
         if capture is not None:
             capture.update(ytop=x32.clone(), tgt=ws["tgt"].clone())
         dy2 = None
@@ -310,6 +369,38 @@ class BertJob:
             dy2 = B
         if capture is not None:
             capture["dx"] = A.clone()
+            capture["dx_res"] = B.clone()
+        if self.head == "mlm":  # the embedding gradient: dx = A (bf16) + B (fp32 residual path)
+            _native.check(L.bt_bert_embed_grad(A.data_ptr(), B.data_ptr(), ws["ids"].data_ptr(), n // gg, gg * Te, D,
+                                               ws["seg_tok"].data_ptr(), ws["seg_first"].data_ptr(),
+                                               ws["seg_n"].data_ptr(), self._eg(lb, "Wemb"), self._eg(lb, "Pemb"),
+                                               self.P, s), "embedding gradient")
+
+    def _mlm_head(self, ws, n: int, lb: int, losses: torch.Tensor, capture: dict | None) -> None:
+        """Masked-LM head of local ESTs [lb, lb+n): gather the masked rows of the top layer's output, logits
+        against the tied word embedding (+ bias) on the tensor cores, softmax cross-entropy (per-EST mean
+        over its masked rows), then dy_m = dlogits W_emb scattered back to the masked rows (A), the decoder
+        weight gradient dlogits^T y_m and bias column sums into each gradient leaf."""
+        L, s = _native.lib(), stream()
+        D, T, Vp, gg = self.D, n * self.Te, self.Vp, self.g
+        R, per = n * self.S * self.NP, self.S * self.NP
+        A = ws["dy1"][0]
+        ym, lg, dl = ws["ym"], ws["logits"], ws["dlogits"]
+        _native.check(L.bt_rows_gather(ws["ytop"].data_ptr(), ws["mrow"].data_ptr(), R, D, ym.data_ptr(), s), "mlm gather")
+        self._gemm(ym.data_ptr(), self.wb.data_ptr(), lg.data_ptr(), R, Vp, D, bias=self._ep("bdec"))
+        _native.check(L.bt_bert_mlm_ce(lg.data_ptr(), ws["mlabel"].data_ptr(), R, self.V, Vp, n, per, dl.data_ptr(),
+                                       ws["rowloss"].data_ptr(), losses[lb:].data_ptr(), s), "mlm cross-entropy")
+        self._gemm(dl.data_ptr(), self.wt.data_ptr(), ws["dym"].data_ptr(), R, D, Vp, out_bf16=True)
+        _native.check(L.bt_rows_scatter(ws["dym"].data_ptr(), ws["mrow"].data_ptr(), R, self.NP, T, D, A.data_ptr(), s),
+                      "mlm scatter")
+        K = gg * per  # decoder weight gradient per leaf: dlogits_j^T y_m_j (MN-major operands, K = the leaf's rows)
+        _native.check(L.bt_gemm_bf16_ex(dl.data_ptr(), ym.data_ptr(), self._eg(lb, "Wemb"), n // gg, Vp, D, K, Vp * K,
+                                        D * K, self.P, 0, None, 1, 0, s), "mlm decoder weight gradient")
+        _native.check(L.bt_colsum_bf16_strided(dl.data_ptr(), n // gg, K, Vp, self._eg(lb, "bdec"), self.P,
+                                               ws["colsum"].data_ptr(), s), "mlm decoder bias gradient")
+        if capture is not None:
+            capture.update({k: ws[k].clone() for k in ("ids", "mrow", "mlabel", "ym", "logits", "dlogits", "dym")})
+            capture["ytop_b"] = ws["ytop"].clone()
 
     # ------------------------------------------------------------------ step
     def step(self, groups: list[int] | None = None, capture: dict | None = None) -> torch.Tensor:
@@ -406,9 +497,11 @@ class BertJob:
 
     # ---------------------------------------------------------------- sizes
     def gemm_flops_per_step(self) -> float:
-        """Dense-layer flops: forward 2*T*P_w, backward dX + dW 4*T*P_w (P_w = weight-matrix params)."""
+        """Dense-layer flops: forward 2*T*P_w, backward dX + dW 4*T*P_w (P_w = weight-matrix params); the
+        masked-LM decoder adds 6 * R * Vp * D (R = masked rows)."""
         pw = sum(int(torch.Size(self.shapes[k]).numel()) for k in _MATS) * self.L
-        return 6.0 * self.En * self.Te * pw
+        head = 6.0 * self.En * self.S * self.NP * self.Vp * self.D if self.head == "mlm" else 0.0
+        return 6.0 * self.En * self.Te * pw + head
 
     def attn_flops_per_step(self) -> float:
         """QK^T and PV: 4*128*128*64 per (sequence, head) forward; backward recomputes S (+1) and does 4 more."""

@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libbittrain_b200.so"
 BUILD = PKG / "_build"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["bt_capi.cu", "bt_mlp.cu", "bt_reduce.cu", "bt_data.cu", "bt_gemm.cu", "bt_ffn.cu", "bt_bert.cu", "bt_cnn.cu", "bt_attn_tc.cu"]
+SOURCES = ["bt_capi.cu", "bt_mlp.cu", "bt_reduce.cu", "bt_data.cu", "bt_gemm.cu", "bt_ffn.cu", "bt_bert.cu", "bt_cnn.cu", "bt_attn_tc.cu", "bt_embed.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-fmad=false", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr"]
 

@@ -95,6 +95,17 @@ int cnn_head_launch(const void* x, const int32_t* labels, const float* W, const 
                     float* db, int64_t grad_stride, float* loss, void* dx, cudaStream_t s);
 int cnn_conv_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* Co, const int* T,
                             const int* Ci, const int* flip, int n, cudaStream_t s);
+int emb_tokens_launch(uint64_t seed, int64_t step, const int64_t* step_dev, int est_base, int E, int S, int V, int np,
+                      int mask_id, int32_t* ids, int32_t* mrow, int32_t* mlabel, cudaStream_t s);
+int emb_fwd_launch(const int32_t* ids, const float* W, const float* Pe, int T, int D, float* x32, void* xb,
+                   cudaStream_t s);
+int emb_gather_launch(const void* in, const int32_t* rows, int R, int D, void* out, cudaStream_t s);
+int emb_scatter_launch(const void* src, const int32_t* rows, int R, int np, int T, int D, void* dst, cudaStream_t s);
+int emb_ce_launch(const float* logits, const int32_t* labels, int R, int V, int Vp, int E, int rows_per_est,
+                  void* dlogits, float* row_loss, float* loss, cudaStream_t s);
+int emb_grad_launch(const void* dxa, const float* dxb, const int32_t* ids, int leaves, int leaf_tokens, int D,
+                    int32_t* seg_tok, int32_t* seg_first, int32_t* seg_n, float* dW, float* dP, int64_t leaf_stride,
+                    cudaStream_t s);
 }  // namespace bt
 
 static thread_local char g_err[512];
@@ -720,6 +731,50 @@ int bt_enable_peer_access(int32_t peer_device) {
   }
   if (e != cudaSuccess) return cuda_fail("cudaDeviceEnablePeerAccess");
   return 0;
+}
+
+// ------------------------------------------ C4 input / output layers (bt_embed.cu)
+int bt_bert_tokens(uint64_t seed, int64_t step, const int64_t* step_dev, int32_t est_base, int32_t E, int32_t seqs,
+                   int32_t vocab, int32_t npred, int32_t mask_id, int32_t* ids_dev, int32_t* mrow_dev,
+                   int32_t* mlabel_dev, void* stream) {
+  if (!ids_dev || !mrow_dev || !mlabel_dev) return fail(bt::ERR_INPUT, "null buffer");
+  if (mask_id < 0 || mask_id >= vocab) return fail(bt::ERR_INPUT, "mask id %d outside the vocabulary", mask_id);
+  return done(bt::emb_tokens_launch(seed, step, step_dev, est_base, E, seqs, vocab, npred, mask_id, ids_dev, mrow_dev,
+                                    mlabel_dev, STREAM(stream)),
+              "bt_bert_tokens");
+}
+int bt_bert_embed_fwd(const int32_t* ids_dev, const float* wemb_dev, const float* pemb_dev, int32_t T, int32_t D,
+                      float* x32_dev, void* xb_dev, void* stream) {
+  if (T < 1 || D < 4 || D % 8) return fail(bt::ERR_INPUT, "embedding %d x %d", T, D);
+  return done(bt::emb_fwd_launch(ids_dev, wemb_dev, pemb_dev, T, D, x32_dev, xb_dev, STREAM(stream)),
+              "bt_bert_embed_fwd");
+}
+int bt_rows_gather(const void* in_dev, const int32_t* rows_dev, int32_t R, int32_t D, void* out_dev, void* stream) {
+  if (R < 1 || D % 8) return fail(bt::ERR_INPUT, "gather %d rows of %d", R, D);
+  return done(bt::emb_gather_launch(in_dev, rows_dev, R, D, out_dev, STREAM(stream)), "bt_rows_gather");
+}
+int bt_rows_scatter(const void* src_dev, const int32_t* rows_dev, int32_t R, int32_t npred, int32_t T, int32_t D,
+                    void* dst_dev, void* stream) {
+  if (R < 1 || T < 1 || D % 8 || npred < 1) return fail(bt::ERR_INPUT, "scatter %d rows into %d", R, T);
+  return done(bt::emb_scatter_launch(src_dev, rows_dev, R, npred, T, D, dst_dev, STREAM(stream)), "bt_rows_scatter");
+}
+int bt_bert_mlm_ce(const float* logits_dev, const int32_t* labels_dev, int32_t R, int32_t vocab, int32_t vocab_pad,
+                   int32_t E, int32_t rows_per_est, void* dlogits_dev, float* row_loss_dev, float* loss_dev,
+                   void* stream) {
+  if (R < 1 || vocab < 2 || vocab > vocab_pad || R != E * rows_per_est)
+    return fail(bt::ERR_INPUT, "cross-entropy over %d rows x %d classes (padded %d)", R, vocab, vocab_pad);
+  return done(bt::emb_ce_launch(logits_dev, labels_dev, R, vocab, vocab_pad, E, rows_per_est, dlogits_dev, row_loss_dev,
+                                loss_dev, STREAM(stream)),
+              "bt_bert_mlm_ce");
+}
+int bt_bert_embed_grad(const void* dxa_dev, const float* dxb_dev, const int32_t* ids_dev, int32_t leaves,
+                       int32_t leaf_tokens, int32_t D, int32_t* seg_tok_dev, int32_t* seg_first_dev, int32_t* seg_n_dev,
+                       float* dwemb_dev, float* dpemb_dev, int64_t leaf_stride, void* stream) {
+  if (leaves < 1 || leaf_tokens < 128 || leaf_tokens > 16384 || leaf_tokens % 128 || D % 8)
+    return fail(bt::ERR_INPUT, "embedding gradient: %d leaves of %d tokens", leaves, leaf_tokens);
+  return done(bt::emb_grad_launch(dxa_dev, dxb_dev, ids_dev, leaves, leaf_tokens, D, seg_tok_dev, seg_first_dev,
+                                  seg_n_dev, dwemb_dev, dpemb_dev, leaf_stride, STREAM(stream)),
+              "bt_bert_embed_grad");
 }
 
 // ------------------------------------------ per-EST BERT encoder step (C4)

@@ -35,7 +35,7 @@ def _gelu_grad(x):
     return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * C_GELU * (1 + 3 * 0.044715 * x * x)
 
 SMALL = dict(ests=4, seqs=2, layers=2, d_model=256, heads=4, d_ff=512, seed=3, lr=0.01, momentum=0.9,
-             p_hidden=0.1, p_attn=0.1)
+             p_hidden=0.1, p_attn=0.1, vocab=1000)
 # the benched C4 shapes (BERT-base: d 768, 12 heads, FFN 3072, seq 128): the CTA-pair GEMM with the
 # 16-warp GELU epilogue at N = 3072 / K = 768, LayerNorm at D = 768, tcgen05 attention at 12 heads
 BASE = dict(ests=2, seqs=2, layers=2, d_model=768, heads=12, d_ff=3072, seed=3, lr=0.01, momentum=0.9,
@@ -100,7 +100,8 @@ def test_tree_reducer_groupings_and_repeat(bert):
 
 
 def test_losses_decrease(bert):
-    job = bert.BertJob(**dict(SMALL, lr=0.05, p_hidden=0.0, p_attn=0.0))
+    # (the regression head: the masked-LM targets are fresh uniform token ids every step -- nothing to learn)
+    job = bert.BertJob(**dict(SMALL, lr=0.05, p_hidden=0.0, p_attn=0.0, head="mse"))
     first = job.step().mean().item()
     for _ in range(8):
         last = job.step().mean().item()
@@ -148,7 +149,7 @@ def _ln_bwd(dy, x, g, eps):
 def test_layer0_stages_match_float64_restatement(bert, cfg):
     from paper_2208_14228_b200._native import host_derive_stream
 
-    job = bert.BertJob(**cfg)
+    job = bert.BertJob(**dict(cfg, head="mse"))  # the encoder on synthetic embedded inputs (MLM head: below)
     P0 = job.params.clone()
     cap = {}
     losses = job.step(capture=cap)
@@ -428,3 +429,85 @@ def test_layernorm_residual_recompute_equals_stored(bert):
     for a, b in zip(*outs):
         assert torch.equal(a.view(torch.int16 if a.dtype == torch.bfloat16 else torch.int32),
                            b.view(torch.int16 if b.dtype == torch.bfloat16 else torch.int32))
+
+
+TAG_TOK = 0x4245_5254_544F_4B4E
+TAG_MASK = 0x4245_5254_4D41_534B
+
+
+@pytest.mark.parametrize("g", [1, 2])
+def test_mlm_head_and_embeddings_match_float64(bert, g):
+    """Token ids / masked positions regenerated from splitmix64 (bit-exact); the word + position
+    embedding (exact fp32 adds); logits against the tied embedding + bias, the per-EST masked-LM
+    cross-entropy, dlogits, dy at the masked rows; the per-leaf decoder weight and bias gradients;
+    and the embedding gradient (tied decoder part + the sorted segment sum of dx rows, no atomics)
+    and the position-embedding gradient -- against a float64 restatement of the captured tensors."""
+    from paper_2208_14228_b200._native import host_derive_stream
+
+    job = bert.BertJob(est_group=g, **dict(SMALL, vocab=1000, npred=20))
+    P0 = job.params.clone()
+    cap = {}
+    losses = job.step(capture=cap)
+    E, S, Te, D, V, Vp, NPd = job.E, job.S, job.Te, job.D, job.V, job.Vp, job.NP
+    # ---- ids and masked positions (the partial Fisher-Yates + sort), bit for bit
+    ids_want, mrow_want, lab_want = [], [], []
+    for e in range(E):
+        st, sm = host_derive_stream(TAG_TOK, job.seed, e), host_derive_stream(TAG_MASK, job.seed, e)
+        for sl in range(S):
+            ids = [int(x % np.uint64(V)) for x in _draws(st, np.arange(sl * 128, sl * 128 + 128))]
+            pos = list(range(128))
+            raws = _draws(sm, np.arange(sl * NPd, sl * NPd + NPd))
+            for k in range(NPd):
+                j = k + int(raws[k] % np.uint64(128 - k))
+                pos[k], pos[j] = pos[j], pos[k]
+            chosen = sorted(pos[:NPd])
+            seq = e * S + sl
+            mrow_want += [seq * 128 + p for p in chosen]
+            lab_want += [ids[p] for p in chosen]
+            ids_want += [job.mask_id if p in chosen else ids[p] for p in range(128)]
+    assert cap["ids"].tolist() == ids_want
+    assert cap["mrow"].tolist() == mrow_want and cap["mlabel"].tolist() == lab_want
+    # ---- embeddings
+    Wemb, Pemb, bdec = _d(job.eview("Wemb", P0)), _d(job.eview("Pemb", P0)), _d(job.eview("bdec", P0))
+    ids = torch.tensor(ids_want)
+    x32_ref = (job.eview("Wemb", P0)[ids.cuda()] + job.eview("Pemb", P0).repeat(E * S, 1)).cpu()
+    assert torch.equal(cap["x32"].cpu(), x32_ref)
+    # ---- head forward
+    ym = _d(cap["ym"])
+    assert torch.equal(ym, _d(cap["ytop_b"])[torch.tensor(mrow_want)])
+    logits_ref = ym @ _bf(Wemb).T + bdec
+    _close(cap["logits"][:, :V], logits_ref[:, :V], "logits", rel=1e-5)
+    lg = _d(cap["logits"])[:, :V]
+    lab = torch.tensor(lab_want)
+    ce = torch.nn.functional.cross_entropy(lg, lab, reduction="none")
+    per = S * NPd
+    _close(losses, ce.view(E, per).mean(1), "per-EST masked-LM loss", rel=1e-5)
+    sm_ = torch.softmax(lg, -1)
+    dl_ref = (sm_ - torch.nn.functional.one_hot(lab, V).double()) / per
+    dl = _d(cap["dlogits"])
+    _close_bf16(dl[:, :V], dl_ref, "dlogits")
+    assert bool((dl[:, V:] == 0).all())
+    _close_bf16(cap["dym"], dl @ _bf(Wemb), "dy at the masked rows")
+    # ---- gradients per leaf
+    gr = cap["grads"].double().cpu()
+    dx = _d(cap["dx"]) + _d(cap["dx_res"])
+    K = g * per
+    for j in range(E // g):
+        rows = slice(j * K, (j + 1) * K)
+        dec = dl[rows].T @ ym[rows]
+        _close(job.eview("bdec", gr[j])[:V], dl[rows].sum(0)[:V], f"decoder bias leaf {j}", rel=2e-3)
+        toks = slice(j * g * Te, (j + 1) * g * Te)
+        emb = torch.zeros(Vp, D, dtype=torch.float64)
+        emb.index_add_(0, ids[toks], dx[toks])
+        _close(job.eview("Wemb", gr[j]), dec + emb, f"word embedding gradient leaf {j}", rel=5e-3)
+        pos_ref = dx[toks].view(g * S, 128, D).sum(0)
+        _close(job.eview("Pemb", gr[j]), pos_ref, f"position embedding gradient leaf {j}", rel=1e-5)
+
+
+def test_mlm_head_groupings_are_bitwise_identical(bert):
+    """The masked-LM head + embedding gradient keep the mapping invariance (launch groups of whole leaves)."""
+    a = bert.BertJob(est_group=2, **SMALL)
+    b = bert.BertJob(est_group=2, **SMALL)
+    for _ in range(3):
+        assert np.array_equal(_bits(a.step([2, 2])), _bits(b.step()))
+    assert np.array_equal(_bits(a.params), _bits(b.params))

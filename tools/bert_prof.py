@@ -15,7 +15,7 @@ from paper_2208_14228_b200.bert import BertJob  # noqa: E402
 E = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 NL = int(sys.argv[2]) if len(sys.argv) > 2 else 12
 S = int(sys.argv[3]) if len(sys.argv) > 3 else 8
-job = BertJob(ests=E, seqs=S, layers=NL)
+job = BertJob(ests=E, seqs=S, layers=NL, est_group=4 if E % 4 == 0 else 1, fanin=2)
 for _ in range(2):
     job.step()
 torch.cuda.synchronize()
@@ -28,7 +28,9 @@ for ev in prof.events():
     if ev.device_type == torch.autograd.DeviceType.CUDA:
         name = ev.name
         for key in ("gemm_bf16_tn_pair_kernel", "gemm_bf16_tn_kernel", "attn_fwd", "attn_bwd", "ln_fwd", "ln_bwd",
-                    "transpose_kernel", "colsum", "reduce", "cast_t", "ln_fold", "mse", "data_kernel"):
+                    "transpose_kernel", "colsum", "reduce", "cast_t", "ln_fold", "mse", "data_kernel", "tokens_kernel",
+                    "embed_fwd", "gather_rows", "scatter_rows", "ce_kernel", "ce_fold", "sort_segments",
+                    "embed_grad", "pos_grad"):
             if key in name:
                 name = key
                 break
