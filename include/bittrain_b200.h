@@ -146,7 +146,9 @@ int bt_ffn_fwd_act(const float *h_dev, const float *b1_dev, uint64_t seed, int64
 /* The FFN's GEMMs with the element ops fused into the epilogue (no fp32 round trip):
  * kind 1 (forward):  h = A*B^T + bias -> c = bf16(h), out2 = bf16(dropout(gelu(h)))
  * kind 2 (backward): c = bf16((A*B^T) * dropout_scale * gelu'(aux))   (aux = bf16 pre-activations)
- * rows are tokens, row r belongs to EST est_base + r / Te; same determinism as bt_gemm_bf16_tn. */
+ * rows are tokens, row r belongs to EST est_base + r / Te; same determinism as bt_gemm_bf16_tn.
+ * kind | BT_GEMM_B_MN: B is stored [K][N] (C = A*B: the weights as stored, no transposed copy). */
+#define BT_GEMM_B_MN 0x100
 int bt_gemm_bf16_ffn(const void *a_dev, const void *b_dev, void *c_dev, int32_t M, int32_t N, int32_t K, int32_t kind,
                      const float *bias_dev, const void *aux_dev, void *out2_dev, uint64_t seed, int64_t step,
                      int32_t est_base, int32_t Te, float p, int32_t grid, void *stream);
@@ -171,7 +173,9 @@ int bt_gemm_bf16_tn_ex(const void *a_dev, const void *b_dev, void *c_dev, int32_
                        const float *bias_dev, int32_t grid, void *stream);
 /* mn_major = 1: both operands MN-major, C[e] = A[e]^T * B[e] with A[e] stored [K][M] and B[e] stored
  * [K][N] (M / N contiguous) -- e.g. a per-EST weight gradient dW_e = dY_e^T X_e read straight from the
- * token-major activations dY [T][M], X [T][N] (stride_a = Te*M, stride_b = Te*N; no transposes). */
+ * token-major activations dY [T][M], X [T][N] (stride_a = Te*M, stride_b = Te*N; no transposes).
+ * mn_major = 2: A K-major [M][K], B MN-major stored [K][N]: C = A * B -- a dX product dY * W reading the
+ * weight W [out][in] as stored (bit-identical to mode 0 on W^T: the same UMMAs in the same k order). */
 int bt_gemm_bf16_ex(const void *a_dev, const void *b_dev, void *c_dev, int32_t batch, int32_t M, int32_t N, int32_t K,
                     int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype, const float *bias_dev,
                     int32_t mn_major, int32_t grid, void *stream);
@@ -209,12 +213,16 @@ int bt_bert_mlm_ce(const float *logits_dev, const int32_t *labels_dev, int32_t R
                    int32_t E, int32_t rows_per_est, void *dlogits_dev, float *row_loss_dev, float *loss_dev,
                    void *stream);
 /* Embedding gradient without atomics: per gradient leaf, the (id, token) pairs sorted in shared
- * memory; per distinct id the rows dx = dxa (bf16) + dxb (fp32) summed in token order and ADDED to
- * dwemb[leaf][id] (which holds the tied decoder's GEMM gradient); dpemb[leaf][p] = the sum over the
- * leaf's sequences, in order.  seg_* : scratch [leaves][leaf_tokens] x2 + [leaves]. */
+ * memory (a bitonic network); per distinct id the rows dx = dxa (bf16) + dxb (fp32) summed in token
+ * order -- in chunks of 16 rows summed in parallel and folded in chunk order when an id repeats
+ * ([MASK]) -- and ADDED to dwemb[leaf][id] (which holds the tied decoder's GEMM gradient);
+ * dpemb[leaf][p] = the sum over the leaf's sequences, in order.  Scratch sizes from
+ * bt_bert_embed_grad_scratch (int32 and fp32 element counts). */
+int bt_bert_embed_grad_scratch(int32_t leaves, int32_t leaf_tokens, int32_t D, int64_t *ints_out,
+                               int64_t *floats_out);
 int bt_bert_embed_grad(const void *dxa_dev, const float *dxb_dev, const int32_t *ids_dev, int32_t leaves,
-                       int32_t leaf_tokens, int32_t D, int32_t *seg_tok_dev, int32_t *seg_first_dev,
-                       int32_t *seg_n_dev, float *dwemb_dev, float *dpemb_dev, int64_t leaf_stride, void *stream);
+                       int32_t leaf_tokens, int32_t D, int32_t *scratch_dev, float *partial_dev, float *dwemb_dev,
+                       float *dpemb_dev, int64_t leaf_stride, void *stream);
 /* ---------------- per-EST BERT encoder step (C4, no reference) ------------
  * Post-LN BERT layer (attention with 64-wide heads over 128-token sequences,
  * LayerNorm, GELU FFN, hidden and attention-probability dropout).  Tokens of

@@ -118,7 +118,8 @@ EXPORTS = {
     "bt_rows_gather": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp]),
     "bt_rows_scatter": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "bt_bert_mlm_ce": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
-    "bt_bert_embed_grad": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
+    "bt_bert_embed_grad_scratch": (C.c_int, [_i32, _i32, _i32, _i64p, _i64p]),
+    "bt_bert_embed_grad": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bt_bert_attn": (C.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _u64, _i64,
                                C.c_float, _vp, _vp]),
     "bt_bert_ln_fwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,

@@ -142,34 +142,9 @@ class BertJob:
         self.adam = (adam_beta2, adam_eps) if optimizer == "adam" else None
         self.vel2 = torch.zeros_like(self.params) if self.adam else None
         self.grads = torch.empty(self.En // self.g, self.P, dtype=torch.float32, device="cuda")  # gradient leaves
-        # bf16 operand copies: W [out][in] (forward) and W^T [in][out] (dX products)
-        self._moff = []
-        m = self.Vp * D if head == "mlm" else 0  # the word embedding's bf16 copies come first
-        for _ in range(layers):
-            d = {}
-            for k in _MATS:
-                d[k] = m
-                m += int(torch.Size(shapes[k]).numel())
-            self._moff.append(d)
-        self.wb = torch.empty(m, dtype=torch.bfloat16, device="cuda")
-        self.wt = torch.empty(m, dtype=torch.bfloat16, device="cuda")
-        n = layers * len(_MATS) + (1 if head == "mlm" else 0)
-        self._cast = [(C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_void_p * n)(), (C.c_int32 * n)(),
-                      (C.c_int32 * n)()]
-        i = 0
-        if head == "mlm":  # Wemb [Vp][D] -> bf16 [Vp][D] (logits) and [D][Vp] (dy_m)
-            self._cast[0][0] = self.params.data_ptr() + 4 * self.eoff["Wemb"]
-            self._cast[1][0], self._cast[2][0] = self.wb.data_ptr(), self.wt.data_ptr()
-            self._cast[3][0], self._cast[4][0] = self.Vp, D
-            i = 1
-        for l in range(layers):
-            for k in _MATS:
-                rows, cols = shapes[k]
-                self._cast[0][i] = self.params.data_ptr() + 4 * self.off[l][k]
-                self._cast[1][i] = self.wb.data_ptr() + 2 * self._moff[l][k]
-                self._cast[2][i] = self.wt.data_ptr() + 2 * self._moff[l][k]
-                self._cast[3][i], self._cast[4][i] = rows, cols
-                i += 1
+        # bf16 image of every parameter at the same offsets (the GEMM operands: W [out][in] as stored --
+        # K-major for the forward, MN-major (B stored [K][N]) for the dX products, so no transposed copy)
+        self.pb = torch.empty(self.P, dtype=torch.bfloat16, device="cuda")
         self.step_idx = 0
         self._step_dev = torch.zeros(1, dtype=torch.int64, device="cuda")  # == step_idx, read by the kernels
         self.flags = Flags()
@@ -198,10 +173,10 @@ class BertJob:
         return self.grads.data_ptr() + 4 * ((base // self.g) * self.P + self.eoff[k])
 
     def _wb(self, l, k):
-        return self.wb.data_ptr() + 2 * self._moff[l][k]
+        return self.pb.data_ptr() + 2 * self.off[l][k]
 
-    def _wt(self, l, k):
-        return self.wt.data_ptr() + 2 * self._moff[l][k]
+    def _ewb(self, k):
+        return self.pb.data_ptr() + 2 * self.eoff[k]
 
     def _p(self, l, k):
         return self.params.data_ptr() + 4 * self.off[l][k]
@@ -210,8 +185,7 @@ class BertJob:
         return self.grads.data_ptr() + 4 * ((base // self.g) * self.P + self.off[l][k])
 
     def _refresh_bf16(self):
-        c = self._cast
-        _native.check(_native.lib().bt_cast_weights_bf16(c[0], c[1], c[2], c[3], c[4], len(c[3]), stream()),
+        _native.check(_native.lib().bt_cast_f32_bf16(self.params.data_ptr(), self.P, self.pb.data_ptr(), stream()),
                       "bert weight cast")
 
     # -------------------------------------------------------------- workspace
@@ -242,8 +216,11 @@ class BertJob:
             ws.update({"ids": torch.empty(T, **i32), "mrow": torch.empty(R, **i32), "mlabel": torch.empty(R, **i32),
                        "ym": torch.empty(R, D, **bf), "logits": torch.empty(R, self.Vp, **f32),
                        "dlogits": torch.empty(R, self.Vp, **bf), "rowloss": torch.empty(R, **f32),
-                       "dym": torch.empty(R, D, **bf), "seg_tok": torch.empty(T, **i32),
-                       "seg_first": torch.empty(T, **i32), "seg_n": torch.empty(max(n // self.g, 1), **i32)})
+                       "dym": torch.empty(R, D, **bf)})
+            ni, nf = C.c_int64(), C.c_int64()
+            _native.check(_native.lib().bt_bert_embed_grad_scratch(n // self.g, self.g * Te, D, C.byref(ni),
+                                                                   C.byref(nf)), "embedding scratch")
+            ws.update({"eg_int": torch.empty(ni.value, **i32), "eg_part": torch.empty(nf.value, **f32)})
         self._ws[n] = ws
         return ws
 
@@ -251,6 +228,11 @@ class BertJob:
     def _gemm(self, a, b, c, M, N, K, out_bf16=False, bias=None, batch=1, sa=0, sb=0, sc=0):
         _native.check(_native.lib().bt_gemm_bf16_tn_ex(a, b, c, batch, M, N, K, sa, sb, sc, 1 if out_bf16 else 0,
                                                        bias, 0, stream()), "bert gemm")
+
+    def _dx(self, a, w, c, M, N, K):
+        """dX = dY . W with W [K = out][N = in] read as stored (B MN-major: bit-identical to dY . (W^T)^T)."""
+        _native.check(_native.lib().bt_gemm_bf16_ex(a, w, c, 1, M, N, K, 0, 0, 0, 1, None, 2, 0, stream()),
+                      "bert dX gemm")
 
     def _wgrad(self, ws, n, dy, x, rows_out, cols_in, dst):
         """Weight gradient of each gradient leaf, dW_j = dy_j^T x_j ([rows_out][cols_in], K = the leaf's
@@ -341,10 +323,10 @@ class BertJob:
                                             self._g(lb, l, "b2"), self.P, s))
             if capture is not None and l == 0:
                 capture.update(dg=Cb.clone(), do=ws["dbr"].clone())
-            _native.check(L.bt_gemm_bf16_ffn(ws["dbr"].data_ptr(), self._wt(l, "W2"), ws["dHpre"].data_ptr(), T, F, D,
-                                             2, None, w["Hpre"].data_ptr(), None, seed, step, base, Te, 0.0, 0, s),
+            _native.check(L.bt_gemm_bf16_ffn(ws["dbr"].data_ptr(), self._wb(l, "W2"), ws["dHpre"].data_ptr(), T, F, D,
+                                             2 | 0x100, None, w["Hpre"].data_ptr(), None, seed, step, base, Te, 0.0, 0, s),
                           "ffn backward GEMM")
-            self._gemm(ws["dHpre"].data_ptr(), self._wt(l, "W1"), Db.data_ptr(), T, D, F, out_bf16=True)
+            self._dx(ws["dHpre"].data_ptr(), self._wb(l, "W1"), Db.data_ptr(), T, D, F)
             self._wgrad(ws, n, ws["dbr"].data_ptr(), w["Dact"].data_ptr(), D, F, self._g(lb, l, "W2"))
             self._wgrad(ws, n, ws["dHpre"].data_ptr(), w["h1b"].data_ptr(), F, D, self._g(lb, l, "W1"))
             _native.check(L.bt_colsum_bf16_strided(ws["dHpre"].data_ptr(), n // gg, gg * Te, F, self._g(lb, l, "b1"),
@@ -356,13 +338,13 @@ class BertJob:
                                            NL, l, 0, seed, step, self.ph, sp, s), "layernorm 1'")
             _native.check(L.bt_bert_ln_fold(part, n // gg, gg * Te, D, self._g(lb, l, "g1"), self._g(lb, l, "be1"),
                                             self._g(lb, l, "bo"), self.P, s))
-            self._gemm(ws["dbr"].data_ptr(), self._wt(l, "Wo"), ws["dctx"].data_ptr(), T, D, D, out_bf16=True)
+            self._dx(ws["dbr"].data_ptr(), self._wb(l, "Wo"), ws["dctx"].data_ptr(), T, D, D)
             self._wgrad(ws, n, ws["dbr"].data_ptr(), w["ctx"].data_ptr(), D, D, self._g(lb, l, "Wo"))
             _native.check(L.bt_bert_attn(1, w["qkv"].data_ptr(), ws["dctx"].data_ptr(), ws["dqkv"].data_ptr(), n, Te,
                                          D, H, base, NL, l, seed, step, self.pa, sp, s), "attention backward")
             if capture is not None and l == 0:
                 capture.update(dh=B.clone(), da=ws["dbr"].clone(), dctx=ws["dctx"].clone(), dqkv=ws["dqkv"].clone())
-            self._gemm(ws["dqkv"].data_ptr(), self._wt(l, "Wqkv"), A.data_ptr(), T, D, 3 * D, out_bf16=True)
+            self._dx(ws["dqkv"].data_ptr(), self._wb(l, "Wqkv"), A.data_ptr(), T, D, 3 * D)
             self._wgrad(ws, n, ws["dqkv"].data_ptr(), w["xb"].data_ptr(), 3 * D, D, self._g(lb, l, "Wqkv"))
             _native.check(L.bt_colsum_bf16_strided(ws["dqkv"].data_ptr(), n // gg, gg * Te, 3 * D,
                                                    self._g(lb, l, "bqkv"), self.P, ws["colsum"].data_ptr(), s))
@@ -372,9 +354,9 @@ class BertJob:
             capture["dx_res"] = B.clone()
         if self.head == "mlm":  # the embedding gradient: dx = A (bf16) + B (fp32 residual path)
             _native.check(L.bt_bert_embed_grad(A.data_ptr(), B.data_ptr(), ws["ids"].data_ptr(), n // gg, gg * Te, D,
-                                               ws["seg_tok"].data_ptr(), ws["seg_first"].data_ptr(),
-                                               ws["seg_n"].data_ptr(), self._eg(lb, "Wemb"), self._eg(lb, "Pemb"),
-                                               self.P, s), "embedding gradient")
+                                               ws["eg_int"].data_ptr(), ws["eg_part"].data_ptr(),
+                                               self._eg(lb, "Wemb"), self._eg(lb, "Pemb"), self.P, s),
+                          "embedding gradient")
 
     def _mlm_head(self, ws, n: int, lb: int, losses: torch.Tensor, capture: dict | None) -> None:
         """Masked-LM head of local ESTs [lb, lb+n): gather the masked rows of the top layer's output, logits
@@ -387,10 +369,10 @@ class BertJob:
         A = ws["dy1"][0]
         ym, lg, dl = ws["ym"], ws["logits"], ws["dlogits"]
         _native.check(L.bt_rows_gather(ws["ytop"].data_ptr(), ws["mrow"].data_ptr(), R, D, ym.data_ptr(), s), "mlm gather")
-        self._gemm(ym.data_ptr(), self.wb.data_ptr(), lg.data_ptr(), R, Vp, D, bias=self._ep("bdec"))
+        self._gemm(ym.data_ptr(), self._ewb("Wemb"), lg.data_ptr(), R, Vp, D, bias=self._ep("bdec"))
         _native.check(L.bt_bert_mlm_ce(lg.data_ptr(), ws["mlabel"].data_ptr(), R, self.V, Vp, n, per, dl.data_ptr(),
                                        ws["rowloss"].data_ptr(), losses[lb:].data_ptr(), s), "mlm cross-entropy")
-        self._gemm(dl.data_ptr(), self.wt.data_ptr(), ws["dym"].data_ptr(), R, D, Vp, out_bf16=True)
+        self._dx(dl.data_ptr(), self._ewb("Wemb"), ws["dym"].data_ptr(), R, D, Vp)
         _native.check(L.bt_rows_scatter(ws["dym"].data_ptr(), ws["mrow"].data_ptr(), R, self.NP, T, D, A.data_ptr(), s),
                       "mlm scatter")
         K = gg * per  # decoder weight gradient per leaf: dlogits_j^T y_m_j (MN-major operands, K = the leaf's rows)

@@ -40,7 +40,7 @@ int gemm_conv_launch(int wgrad, const void* x, int xN, int xH, int xW, int Ci, i
                      int stride, int pad, const void* other, void* c, int Co, int batch, int rows_per_batch,
                      int64_t sc, int out_bf16, cudaStream_t s);
 int gemm_bf16_launch_any(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
-                         int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, bool mn, cudaStream_t s);
+                         int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, int mn, cudaStream_t s);
 int ffn_data_launch(uint64_t seed, int64_t step, int est_base, int E, int Te, int D, void* X, float* target,
                     cudaStream_t s);
 int ffn_fwd_act_launch(const float* H, const float* b1, uint64_t seed, int64_t step, int est_base, int E, int Te,
@@ -103,9 +103,9 @@ int emb_gather_launch(const void* in, const int32_t* rows, int R, int D, void* o
 int emb_scatter_launch(const void* src, const int32_t* rows, int R, int np, int T, int D, void* dst, cudaStream_t s);
 int emb_ce_launch(const float* logits, const int32_t* labels, int R, int V, int Vp, int E, int rows_per_est,
                   void* dlogits, float* row_loss, float* loss, cudaStream_t s);
+int emb_grad_scratch(int leaves, int leaf_tokens, int D, int64_t* ints, int64_t* floats);
 int emb_grad_launch(const void* dxa, const float* dxb, const int32_t* ids, int leaves, int leaf_tokens, int D,
-                    int32_t* seg_tok, int32_t* seg_first, int32_t* seg_n, float* dW, float* dP, int64_t leaf_stride,
-                    cudaStream_t s);
+                    int32_t* scratch, float* partial, float* dW, float* dP, int64_t leaf_stride, cudaStream_t s);
 }  // namespace bt
 
 static thread_local char g_err[512];
@@ -401,9 +401,10 @@ int bt_gemm_bf16_ex(const void* a_dev, const void* b_dev, void* c_dev, int32_t b
                     int64_t stride_a, int64_t stride_b, int64_t stride_c, int32_t out_dtype, const float* bias_dev,
                     int32_t mn_major, int32_t grid, void* stream) {
   if (!a_dev || !b_dev || !c_dev) return fail(bt::ERR_INPUT, "null pointer");
-  if (batch < 1 || M <= 0 || N <= 0 || K <= 0 || N % 8 || (mn_major ? M % 8 : K % 8))
+  if (mn_major < 0 || mn_major > 2) return fail(bt::ERR_INPUT, "mn_major %d: 0, 1 or 2", mn_major);
+  if (batch < 1 || M <= 0 || N <= 0 || K <= 0 || N % 8 || (mn_major == 1 ? M % 8 : K % 8))
     return fail(bt::ERR_INPUT, "gemm shape %dx%dx%d x%d: need N %% 8 == 0 and %s %% 8 == 0 (16-byte TMA strides)", M,
-                N, K, batch, mn_major ? "M" : "K");
+                N, K, batch, mn_major == 1 ? "M" : "K");
   if (((uintptr_t)a_dev | (uintptr_t)b_dev | (uintptr_t)c_dev | (uintptr_t)bias_dev) & 15)
     return fail(bt::ERR_INPUT, "gemm operands must be 16-byte aligned");
   if (batch == 1) {
@@ -420,7 +421,7 @@ int bt_gemm_bf16_ex(const void* a_dev, const void* b_dev, void* c_dev, int32_t b
   epi.kind = bias_dev ? bt::EPI_BIAS : bt::EPI_STORE;
   epi.bias = bias_dev;
   return done(bt::gemm_bf16_launch_any(a_dev, b_dev, c_dev, batch, M, N, K, stride_a, stride_b, stride_c, out_dtype,
-                                       grid, epi, mn_major != 0, STREAM(stream)),
+                                       grid, epi, mn_major, STREAM(stream)),
               "bt_gemm_bf16");
 }
 int bt_gemm_conv(int32_t wgrad, const void* x_dev, int32_t xN, int32_t xH, int32_t xW, int32_t Ci, int32_t Ho,
@@ -465,6 +466,8 @@ int bt_gemm_bf16_ffn(const void* a_dev, const void* b_dev, void* c_dev, int32_t 
   if (!a_dev || !b_dev || !c_dev) return fail(bt::ERR_INPUT, "null pointer");
   if (M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 128 || K % 64)
     return fail(bt::ERR_INPUT, "gemm shape %dx%dx%d: need M %% 128 == 0, N %% 128 == 0, K %% 64 == 0", M, N, K);
+  const bool b_mn = (kind & BT_GEMM_B_MN) != 0;  // B stored [K][N] (the weights as stored: no transposed copy)
+  kind &= ~BT_GEMM_B_MN;
   if (kind != bt::EPI_FFN_FWD && kind != bt::EPI_FFN_BWD) return fail(bt::ERR_INPUT, "bad epilogue kind %d", kind);
   if (kind == bt::EPI_FFN_FWD && (!bias_dev || !out2_dev)) return fail(bt::ERR_INPUT, "FFN_FWD needs bias and out2");
   if (kind == bt::EPI_FFN_BWD && !aux_dev) return fail(bt::ERR_INPUT, "FFN_BWD needs the pre-activations");
@@ -481,9 +484,8 @@ int bt_gemm_bf16_ffn(const void* a_dev, const void* b_dev, void* c_dev, int32_t 
   epi.est_base = est_base;
   epi.Te = Te;
   epi.p = p;
-  return done(bt::gemm_bf16_tn_launch_epi(a_dev, b_dev, c_dev, 1, M, N, K, (int64_t)M * K, (int64_t)N * K,
-                                          (int64_t)M * N, 1, grid,
-                                          epi, STREAM(stream)),
+  return done(bt::gemm_bf16_launch_any(a_dev, b_dev, c_dev, 1, M, N, K, (int64_t)M * K, (int64_t)N * K,
+                                       (int64_t)M * N, 1, grid, epi, b_mn ? 2 : 0, STREAM(stream)),
               "bt_gemm_bf16_ffn");
 }
 
@@ -767,13 +769,19 @@ int bt_bert_mlm_ce(const float* logits_dev, const int32_t* labels_dev, int32_t R
                                 loss_dev, STREAM(stream)),
               "bt_bert_mlm_ce");
 }
+int bt_bert_embed_grad_scratch(int32_t leaves, int32_t leaf_tokens, int32_t D, int64_t* ints_out,
+                               int64_t* floats_out) {
+  if (leaves < 1 || leaf_tokens < 128 || D < 8 || !ints_out || !floats_out) return fail(bt::ERR_INPUT, "bad shape");
+  return bt::emb_grad_scratch(leaves, leaf_tokens, D, ints_out, floats_out);
+}
 int bt_bert_embed_grad(const void* dxa_dev, const float* dxb_dev, const int32_t* ids_dev, int32_t leaves,
-                       int32_t leaf_tokens, int32_t D, int32_t* seg_tok_dev, int32_t* seg_first_dev, int32_t* seg_n_dev,
-                       float* dwemb_dev, float* dpemb_dev, int64_t leaf_stride, void* stream) {
-  if (leaves < 1 || leaf_tokens < 128 || leaf_tokens > 16384 || leaf_tokens % 128 || D % 8)
-    return fail(bt::ERR_INPUT, "embedding gradient: %d leaves of %d tokens", leaves, leaf_tokens);
-  return done(bt::emb_grad_launch(dxa_dev, dxb_dev, ids_dev, leaves, leaf_tokens, D, seg_tok_dev, seg_first_dev,
-                                  seg_n_dev, dwemb_dev, dpemb_dev, leaf_stride, STREAM(stream)),
+                       int32_t leaf_tokens, int32_t D, int32_t* scratch_dev, float* partial_dev, float* dwemb_dev,
+                       float* dpemb_dev, int64_t leaf_stride, void* stream) {
+  if (leaves < 1 || leaf_tokens < 128 || leaf_tokens > 8192 || leaf_tokens % 128 || D % 8)
+    return fail(bt::ERR_INPUT, "embedding gradient: %d leaves of %d tokens (<= 8192)", leaves, leaf_tokens);
+  if (!scratch_dev || !partial_dev) return fail(bt::ERR_INPUT, "null scratch");
+  return done(bt::emb_grad_launch(dxa_dev, dxb_dev, ids_dev, leaves, leaf_tokens, D, scratch_dev, partial_dev,
+                                  dwemb_dev, dpemb_dev, leaf_stride, STREAM(stream)),
               "bt_bert_embed_grad");
 }
 

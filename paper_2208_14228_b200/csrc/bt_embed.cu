@@ -8,7 +8,7 @@
 // step, position) in counter form, and every reduction has a shape fixed by the EST's own data.  The
 // embedding gradient is the classic nondeterminism site (a scatter-add: atomics in mainstream stacks);
 // here it has NO atomics: each gradient leaf sorts its (token id, position) pairs in shared memory,
-// and one CTA per distinct id sums that id's rows in position order, after the decoder GEMM's
+// and one warp per distinct id sums that id's rows in position order, after the decoder GEMM's
 // contribution, into the leaf's slot -- the same bits whatever the launch grouping or GPU.
 //
 // Layout (launch of n ESTs, Te = S * 128 tokens each, leaves of g ESTs):
@@ -125,42 +125,58 @@ __global__ void __launch_bounds__(128) scatter_rows_kernel(const __nv_bfloat16* 
   for (int c = threadIdx.x; c < D / 8; c += 128) d[c] = s ? s[c] : make_uint4(0, 0, 0, 0);
 }
 
-// Cross-entropy of one masked row over the V classes (columns >= V are padding): row max, then the
-// exp-sum in a fixed order (each thread its strided columns ascending, a fixed tree across threads);
-// loss = log(sum) + max - logit[label]; dlogits = (softmax - onehot) * inv_rows (the EST's loss is the
-// mean over its masked rows), bf16, zero in the padding.
+// Cross-entropy of one masked row over the V classes (columns >= V are padding).  One read of the row
+// for the statistics: each thread keeps an online (max, exp-sum) over its 4-column groups in
+// ascending order, the 256 pairs are combined by a fixed tree; then dlogits = (softmax - onehot) *
+// inv_rows (the EST's loss is the mean over its masked rows), bf16, zero in the padding;
+// loss = log(sum) + max - logit[label].  Vp % 4 == 0.
 constexpr int CE_THREADS = 256;
-__device__ __forceinline__ float block_reduce(float v, float* sm, bool is_max) {
-  sm[threadIdx.x] = v;
-  __syncthreads();
-  for (int w = CE_THREADS / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) sm[threadIdx.x] = is_max ? fmaxf(sm[threadIdx.x], sm[threadIdx.x + w])
-                                                  : sm[threadIdx.x] + sm[threadIdx.x + w];
-    __syncthreads();
-  }
-  const float out = sm[0];
-  __syncthreads();
-  return out;
+__device__ __forceinline__ void ms_combine(float& m, float& s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+  m = mn;
 }
 __global__ void __launch_bounds__(CE_THREADS) ce_kernel(const float* __restrict__ logits,
                                                         const int32_t* __restrict__ labels, int V, int Vp,
                                                         float inv_rows, __nv_bfloat16* __restrict__ dlogits,
                                                         float* __restrict__ row_loss) {
-  __shared__ float sm[CE_THREADS];
+  __shared__ float sm_m[CE_THREADS], sm_s[CE_THREADS];
   const int r = blockIdx.x;
   const float* l = logits + (size_t)r * Vp;
-  float m = -INFINITY;
-  for (int c = threadIdx.x; c < V; c += CE_THREADS) m = fmaxf(m, l[c]);
-  m = block_reduce(m, sm, true);
-  float s = 0.f;
-  for (int c = threadIdx.x; c < V; c += CE_THREADS) s += __expf(l[c] - m);
-  s = block_reduce(s, sm, false);
+  float m = -INFINITY, s = 0.f;
+  for (int c = threadIdx.x * 4; c < V; c += CE_THREADS * 4) {
+    const float4 v = *(const float4*)(l + c);
+    const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (c + q < V) ms_combine(m, s, x[q], 1.f);
+  }
+  sm_m[threadIdx.x] = m;
+  sm_s[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = CE_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      float mm = sm_m[threadIdx.x], ss = sm_s[threadIdx.x];
+      ms_combine(mm, ss, sm_m[threadIdx.x + w], sm_s[threadIdx.x + w]);
+      sm_m[threadIdx.x] = mm;
+      sm_s[threadIdx.x] = ss;
+    }
+    __syncthreads();
+  }
+  m = sm_m[0];
+  s = sm_s[0];
   const int lab = labels[r];
   const float inv_s = 1.f / s;
   __nv_bfloat16* d = dlogits + (size_t)r * Vp;
-  for (int c = threadIdx.x; c < Vp; c += CE_THREADS) {
-    const float g = c < V ? (__expf(l[c] - m) * inv_s - (c == lab ? 1.f : 0.f)) * inv_rows : 0.f;
-    d[c] = __float2bfloat16_rn(g);
+  for (int c = threadIdx.x * 4; c < Vp; c += CE_THREADS * 4) {
+    const float4 v = *(const float4*)(l + c);
+    const float x[4] = {v.x, v.y, v.z, v.w};
+    float g[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      g[q] = c + q < V ? (__expf(x[q] - m) * inv_s - (c + q == lab ? 1.f : 0.f)) * inv_rows : 0.f;
+    *(__nv_bfloat162*)(d + c) = __floats2bfloat162_rn(g[0], g[1]);
+    *(__nv_bfloat162*)(d + c + 2) = __floats2bfloat162_rn(g[2], g[3]);
   }
   if (threadIdx.x == 0) row_loss[r] = __logf(s) + m - l[lab];
 }
@@ -173,19 +189,62 @@ __global__ void ce_fold_kernel(const float* __restrict__ row_loss, int E, int ro
   loss[e] = acc / (float)rows_per_est;
 }
 
-// Embedding gradient, step 1 (one CTA per gradient leaf): sort the leaf's (id, token) pairs by id,
-// then token (a bitonic sort of 64-bit keys in shared memory: a fixed network), and cut the sorted
-// list into per-id segments: seg_tok[leaf][i] = sorted token indices, seg_first[leaf][k] = start of
-// segment k, seg_n[leaf] = number of segments.
-__global__ void __launch_bounds__(1024) sort_segments_kernel(const int32_t* __restrict__ ids, int leaf_tokens,
-                                                             int pow2, int32_t* __restrict__ seg_tok,
-                                                             int32_t* __restrict__ seg_first,
-                                                             int32_t* __restrict__ seg_n) {
-  extern __shared__ uint64_t keys[];
-  const int leaf = blockIdx.x;
-  const int32_t* id = ids + (size_t)leaf * leaf_tokens;
+// Embedding gradient, step 1 (one CTA of 1024 threads per gradient leaf): sort the leaf's (id, token)
+// pairs by id, then token (a bitonic network over 64-bit keys in shared memory), then cut the sorted
+// list into per-id segments and each segment into EG_CH-row chunks -- all with block-wide prefix sums,
+// no serial pass.  Outputs per leaf: seg_tok (sorted token indices), seg_first (segment starts),
+// seg_n; chunks = {cfirst [segment], clo, cseg, cpix [chunk]} (cpix: the chunk's partial slot, -1 when
+// its segment is a single chunk), n_chunks.
+constexpr int EG_CH = 16;  // rows per chunk: a long segment is summed as chunks in parallel, then in order
+constexpr int SORT_THREADS = 1024;
+__device__ int block_scan_inclusive(int* a, int n, int* warp_tot) {  // in place; returns the total
+  const int per = (n + SORT_THREADS - 1) / SORT_THREADS, lo = threadIdx.x * per;
+  int run = 0;
+  for (int i = lo; i < lo + per && i < n; ++i) run += a[i];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = warp_tot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_tot[lane] = t;
+  }
+  __syncthreads();
+  int acc = x - run + (w > 0 ? warp_tot[w - 1] : 0);  // exclusive prefix of this thread's range
+  for (int i = lo; i < lo + per && i < n; ++i) {
+    acc += a[i];
+    a[i] = acc;
+  }
+  const int total = warp_tot[31];
+  __syncthreads();
+  return total;
+}
+__global__ void __launch_bounds__(SORT_THREADS) sort_segments_kernel(const int32_t* __restrict__ ids, int leaf_tokens,
+                                                                     int pow2, int32_t* __restrict__ seg_tok,
+                                                                     int32_t* __restrict__ seg_first,
+                                                                     int32_t* __restrict__ seg_n,
+                                                                     int32_t* __restrict__ chunks,
+                                                                     int32_t* __restrict__ n_chunks) {
+  extern __shared__ uint64_t keys[];  // [pow2] keys, then 4 int arrays of [pow2]
+  __shared__ int warp_tot[32];
+  int* sa = (int*)(keys + pow2);
+  int* sb = sa + pow2;
+  int* sfirst = sb + pow2;
+  int* sc = sfirst + pow2;
+  const int leaf = blockIdx.x, N = leaf_tokens;
+  const int32_t* id = ids + (size_t)leaf * N;
   for (int i = threadIdx.x; i < pow2; i += blockDim.x)
-    keys[i] = i < leaf_tokens ? ((uint64_t)(uint32_t)id[i] << 32) | (uint32_t)i : ~0ull;
+    keys[i] = i < N ? ((uint64_t)(uint32_t)id[i] << 32) | (uint32_t)i : ~0ull;
   __syncthreads();
   for (int k = 2; k <= pow2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
@@ -203,43 +262,141 @@ __global__ void __launch_bounds__(1024) sort_segments_kernel(const int32_t* __re
       __syncthreads();
     }
   }
-  int32_t* tok = seg_tok + (size_t)leaf * leaf_tokens;
-  int32_t* first = seg_first + (size_t)leaf * leaf_tokens;
-  for (int i = threadIdx.x; i < leaf_tokens; i += blockDim.x) tok[i] = (int32_t)(keys[i] & 0xffffffffu);
+  int32_t* tok = seg_tok + (size_t)leaf * N;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    tok[i] = (int32_t)(keys[i] & 0xffffffffu);
+    sa[i] = (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;  // segment heads
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {  // segment starts (sequential: a few thousand compares)
-    int n = 0;
-    for (int i = 0; i < leaf_tokens; ++i)
-      if (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) first[n++] = i;
-    seg_n[leaf] = n;
+  const int nseg = block_scan_inclusive(sa, N, warp_tot);  // sa[i] = heads in [0, i]
+  for (int i = threadIdx.x; i < N; i += blockDim.x)
+    if (i == 0 || sa[i] != sa[i - 1]) sfirst[sa[i] - 1] = i;
+  __syncthreads();
+  for (int k = threadIdx.x; k < nseg; k += blockDim.x) {  // chunks per segment; partial slots per segment
+    const int len = (k + 1 < nseg ? sfirst[k + 1] : N) - sfirst[k], nch = (len + EG_CH - 1) / EG_CH;
+    sb[k] = nch;
+    sc[k] = nch > 1 ? nch : 0;
+  }
+  __syncthreads();
+  const int nc = block_scan_inclusive(sb, nseg, warp_tot);  // sb[k] = chunks of segments 0..k
+  block_scan_inclusive(sc, nseg, warp_tot);
+  int32_t* first = seg_first + (size_t)leaf * N;
+  int32_t* cfirst = chunks + (size_t)leaf * 4 * N;  // [segment] first chunk
+  int32_t* clo = cfirst + N;                        // [chunk] first sorted row
+  int32_t* cseg = clo + N;                          // [chunk] segment
+  int32_t* cpix = cseg + N;                         // [chunk] partial slot or -1
+  for (int k = threadIdx.x; k < nseg; k += blockDim.x) {
+    const int c1 = sb[k], c0 = k > 0 ? sb[k - 1] : 0, p0 = k > 0 ? sc[k - 1] : 0;
+    first[k] = sfirst[k];
+    cfirst[k] = c0;
+    for (int c = c0; c < c1; ++c) {
+      clo[c] = sfirst[k] + (c - c0) * EG_CH;
+      cseg[c] = k;
+      cpix[c] = c1 - c0 > 1 ? p0 + (c - c0) : -1;
+    }
+  }
+  if (threadIdx.x == 0) {
+    seg_n[leaf] = nseg;
+    n_chunks[leaf] = nc;
   }
 }
 
-// Embedding gradient, step 2: CTA (segment k, leaf): dW_leaf[id] += sum over the segment's tokens, in
-// token order, of dx[t] = dxa[t] (bf16) + dxb[t] (fp32) -- added to the decoder GEMM's contribution
-// already in the slot (one addition of the segment sum: a fixed association).
-__global__ void __launch_bounds__(256) embed_grad_kernel(const __nv_bfloat16* __restrict__ dxa,
-                                                         const float* __restrict__ dxb, const int32_t* __restrict__ ids,
-                                                         const int32_t* __restrict__ seg_tok,
-                                                         const int32_t* __restrict__ seg_first,
-                                                         const int32_t* __restrict__ seg_n, int leaf_tokens, int D,
-                                                         float* __restrict__ dW, int64_t leaf_stride) {
-  const int leaf = blockIdx.y, k = blockIdx.x;
-  if (k >= seg_n[leaf]) return;
+// Embedding gradient, step 2: one warp per (chunk c, leaf): the sum, in token order, of the chunk's
+// <= EG_CH rows dx[t] = dxa[t] (bf16) + dxb[t] (fp32) (loads batched 8 rows at a time); a segment of one
+// chunk adds it to dW_leaf[id] (on top of the decoder GEMM's contribution: one addition, a fixed
+// association), a longer segment ([MASK]: every masked position of the leaf) writes it to its partial
+// slot for step 3.  Each lane owns 8-column groups (16-byte bf16 / 2 x 16-byte fp32 loads).
+constexpr int EG_WARPS = 8;
+__device__ __forceinline__ void row8(const __nv_bfloat16* dxa, const float* dxb, size_t t, int D, int c, float* v) {
+  const uint4 ra = *(const uint4*)(dxa + t * D + c);
+  const float4 b0 = *(const float4*)(dxb + t * D + c), b1 = *(const float4*)(dxb + t * D + c + 4);
+  const __nv_bfloat162* a2 = (const __nv_bfloat162*)&ra;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 f = __bfloat1622float2(a2[q]);
+    v[2 * q] = f.x;
+    v[2 * q + 1] = f.y;
+  }
+  v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+  v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+}
+__device__ __forceinline__ void add8(float* w, const float* acc) {
+  float4* wp = (float4*)w;
+  float4 o0 = wp[0], o1 = wp[1];
+  o0.x += acc[0]; o0.y += acc[1]; o0.z += acc[2]; o0.w += acc[3];
+  o1.x += acc[4]; o1.y += acc[5]; o1.z += acc[6]; o1.w += acc[7];
+  wp[0] = o0;
+  wp[1] = o1;
+}
+__global__ void __launch_bounds__(32 * EG_WARPS) embed_chunk_kernel(
+    const __nv_bfloat16* __restrict__ dxa, const float* __restrict__ dxb, const int32_t* __restrict__ ids,
+    const int32_t* __restrict__ seg_tok, const int32_t* __restrict__ seg_first, const int32_t* __restrict__ seg_n,
+    const int32_t* __restrict__ chunks, const int32_t* __restrict__ n_chunks, int leaf_tokens, int D,
+    float* __restrict__ dW, int64_t leaf_stride, float* __restrict__ partial, int pslots) {
+  const int leaf = blockIdx.y, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * EG_WARPS + (threadIdx.x >> 5);
+  if (c >= n_chunks[leaf]) return;
+  const int32_t* cfirst = chunks + (size_t)leaf * 4 * leaf_tokens;
+  const int32_t *clo = cfirst + leaf_tokens, *cseg = clo + leaf_tokens, *cpix = cseg + leaf_tokens;
   const int32_t* tok = seg_tok + (size_t)leaf * leaf_tokens;
   const int32_t* first = seg_first + (size_t)leaf * leaf_tokens;
-  const int lo = first[k], hi = k + 1 < seg_n[leaf] ? first[k + 1] : leaf_tokens;
+  const int k = cseg[c], ns = seg_n[leaf];
+  const int seg_hi = k + 1 < ns ? first[k + 1] : leaf_tokens;
+  const int lo = clo[c], hi = lo + EG_CH < seg_hi ? lo + EG_CH : seg_hi;
   const size_t t0 = (size_t)leaf * leaf_tokens;
-  const int id = ids[t0 + tok[lo]];
-  float* w = dW + (size_t)leaf * leaf_stride + (size_t)id * D;
-  for (int c = threadIdx.x; c < D; c += 256) {
-    float acc = 0.f;
-    for (int i = lo; i < hi; ++i) {
-      const size_t t = t0 + tok[i];
-      const float v = __bfloat162float(dxa[t * D + c]) + dxb[t * D + c];
-      acc = i == lo ? v : acc + v;
+  const int pix = cpix[c];
+  float* out = pix < 0 ? dW + (size_t)leaf * leaf_stride + (size_t)ids[t0 + tok[lo]] * D
+                       : partial + ((size_t)leaf * pslots + pix) * D;
+  constexpr int U = 8;
+  for (int col = lane * 8; col < D; col += 32 * 8) {
+    float acc[8];
+    for (int i0 = lo; i0 < hi; i0 += U) {
+      float v[U][8];
+#pragma unroll
+      for (int j = 0; j < U; ++j) row8(dxa, dxb, t0 + tok[i0 + j < hi ? i0 + j : lo], D, col, v[j]);
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+        if (i0 + j < hi)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = i0 + j == lo ? v[j][q] : acc[q] + v[j][q];
     }
-    w[c] += acc;
+    if (pix < 0) {
+      add8(out + col, acc);
+    } else {
+      *(float4*)(out + col) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      *(float4*)(out + col + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+  }
+}
+// Embedding gradient, step 3: one warp per multi-chunk segment: its chunk partials summed in chunk order,
+// then added to dW_leaf[id] (one addition).
+__global__ void __launch_bounds__(32 * EG_WARPS) embed_fold_kernel(
+    const int32_t* __restrict__ ids, const int32_t* __restrict__ seg_tok, const int32_t* __restrict__ seg_first,
+    const int32_t* __restrict__ seg_n, const int32_t* __restrict__ chunks, const int32_t* __restrict__ n_chunks,
+    int leaf_tokens, int D, float* __restrict__ dW, int64_t leaf_stride, const float* __restrict__ partial,
+    int pslots) {
+  const int leaf = blockIdx.y, lane = threadIdx.x & 31;
+  const int k = blockIdx.x * EG_WARPS + (threadIdx.x >> 5);
+  const int ns = seg_n[leaf];
+  if (k >= ns) return;
+  const int32_t* cfirst = chunks + (size_t)leaf * 4 * leaf_tokens;
+  const int32_t* cpix = cfirst + 3 * leaf_tokens;
+  const int c0 = cfirst[k], c1 = k + 1 < ns ? cfirst[k + 1] : n_chunks[leaf];
+  if (c1 - c0 < 2) return;
+  const int32_t* tok = seg_tok + (size_t)leaf * leaf_tokens;
+  const int32_t* first = seg_first + (size_t)leaf * leaf_tokens;
+  float* w = dW + (size_t)leaf * leaf_stride + (size_t)ids[(size_t)leaf * leaf_tokens + tok[first[k]]] * D;
+  const float* pbase = partial + (size_t)leaf * pslots * D;
+  for (int col = lane * 8; col < D; col += 32 * 8) {
+    float acc[8];
+    for (int c = c0; c < c1; ++c) {
+      const float* p = pbase + (size_t)cpix[c] * D + col;
+      const float4 a = *(const float4*)p, b = *(const float4*)(p + 4);
+      const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = c == c0 ? v[q] : acc[q] + v[q];
+    }
+    add8(w + col, acc);
   }
 }
 
@@ -291,20 +448,26 @@ int emb_scatter_launch(const void* src, const int32_t* rows, int R, int np, int 
 
 int emb_ce_launch(const float* logits, const int32_t* labels, int R, int V, int Vp, int E, int rows_per_est,
                   void* dlogits, float* row_loss, float* loss, cudaStream_t s) {
-  if (R != E * rows_per_est || V > Vp) return ERR_INPUT;
+  if (R != E * rows_per_est || V > Vp || Vp % 4) return ERR_INPUT;
   emb::ce_kernel<<<R, emb::CE_THREADS, 0, s>>>(logits, labels, V, Vp, 1.f / (float)rows_per_est,
                                                (__nv_bfloat16*)dlogits, row_loss);
   emb::ce_fold_kernel<<<(E + 127) / 128, 128, 0, s>>>(row_loss, E, rows_per_est, loss);
   return ok_or_cuda_e();
 }
 
+// int32 scratch: seg_tok, seg_first, chunks (4 arrays) per leaf = 6 * leaf_tokens, + seg_n, n_chunks;
+// fp32 partials: pslots rows of D per leaf (chunks of multi-chunk segments, <= 2 * leaf_tokens / EG_CH + 1)
+int emb_grad_scratch(int leaves, int leaf_tokens, int D, int64_t* ints, int64_t* floats) {
+  *ints = (int64_t)leaves * 6 * leaf_tokens + 2 * (int64_t)leaves;
+  *floats = (int64_t)leaves * (2 * leaf_tokens / emb::EG_CH + 1) * D;
+  return OK;
+}
 int emb_grad_launch(const void* dxa, const float* dxb, const int32_t* ids, int leaves, int leaf_tokens, int D,
-                    int32_t* seg_tok, int32_t* seg_first, int32_t* seg_n, float* dW, float* dP, int64_t leaf_stride,
-                    cudaStream_t s) {
+                    int32_t* scratch, float* partial, float* dW, float* dP, int64_t leaf_stride, cudaStream_t s) {
   if (leaf_tokens % emb::SEQ) return ERR_INPUT;
   int pow2 = 1;
   while (pow2 < leaf_tokens) pow2 <<= 1;
-  const size_t smem = sizeof(uint64_t) * (size_t)pow2;
+  const size_t smem = (sizeof(uint64_t) + 4 * sizeof(int)) * (size_t)pow2;  // keys + 4 int arrays
   if (smem > 200 * 1024) return ERR_INPUT;
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
@@ -313,9 +476,21 @@ int emb_grad_launch(const void* dxa, const float* dxb, const int32_t* ids, int l
       return ERR_CUDA;
     attr = 200 * 1024;
   }
-  emb::sort_segments_kernel<<<leaves, 1024, smem, s>>>(ids, leaf_tokens, pow2, seg_tok, seg_first, seg_n);
-  emb::embed_grad_kernel<<<dim3(leaf_tokens, leaves), 256, 0, s>>>((const __nv_bfloat16*)dxa, dxb, ids, seg_tok,
-                                                                   seg_first, seg_n, leaf_tokens, D, dW, leaf_stride);
+  const size_t T = (size_t)leaves * leaf_tokens;
+  int32_t* seg_tok = scratch;
+  int32_t* seg_first = seg_tok + T;
+  int32_t* chunks = seg_first + T;
+  int32_t* seg_n = chunks + 4 * T;
+  int32_t* n_chunks = seg_n + leaves;
+  const int pslots = 2 * leaf_tokens / emb::EG_CH + 1;
+  emb::sort_segments_kernel<<<leaves, emb::SORT_THREADS, smem, s>>>(ids, leaf_tokens, pow2, seg_tok, seg_first,
+                                                                     seg_n, chunks, n_chunks);
+  const dim3 grid((leaf_tokens + emb::EG_WARPS - 1) / emb::EG_WARPS, leaves);
+  emb::embed_chunk_kernel<<<grid, 32 * emb::EG_WARPS, 0, s>>>((const __nv_bfloat16*)dxa, dxb, ids, seg_tok, seg_first,
+                                                              seg_n, chunks, n_chunks, leaf_tokens, D, dW, leaf_stride,
+                                                              partial, pslots);
+  emb::embed_fold_kernel<<<grid, 32 * emb::EG_WARPS, 0, s>>>(ids, seg_tok, seg_first, seg_n, chunks, n_chunks,
+                                                             leaf_tokens, D, dW, leaf_stride, partial, pslots);
   emb::pos_grad_kernel<<<dim3(emb::SEQ, leaves), 256, 0, s>>>((const __nv_bfloat16*)dxa, dxb,
                                                               leaf_tokens / emb::SEQ, D, dP, leaf_stride);
   return ok_or_cuda_e();

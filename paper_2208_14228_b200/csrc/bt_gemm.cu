@@ -58,10 +58,10 @@ constexpr uint64_t k_step() {  // descriptor increment per UMMA K step (16-byte 
 // Instruction descriptor: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
 // both K-major, N>>3 at [17,23), M>>4 at [24,29).
 // a_major [15] / b_major [16] = 1 for MN-major operands.
-template <int BN, bool MN = false>
+template <int BN, bool MN = false, bool BMN = false>
 __device__ __forceinline__ constexpr uint32_t instr_desc() {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (MN ? (3u << 15) : 0u) | ((uint32_t)(BN >> 3) << 17) |
-         ((uint32_t)(BM >> 4) << 24);
+  return (1u << 4) | (1u << 7) | (1u << 10) | (MN ? (3u << 15) : 0u) | (BMN ? (1u << 16) : 0u) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
 // Tile t -> (m0, n0): groups of GROUP_M row-blocks walked column by column, so
@@ -267,7 +267,8 @@ struct Smem {
   static constexpr int TOTAL = BAR + (2 * STAGES + 5) * 8 + 16;
 };
 
-// AIM: 0 = tiled operands; 1 = A is im2col(x) (forward convolution, K-major); 2 = B is im2col(x)
+// AIM: 0 = tiled operands; 4 = tiled, A K-major and B MN-major (C = A.B with B stored [K][N]: the dX
+// products read the weights as stored, no transposed copy); 1 = A is im2col(x) (forward convolution, K-major); 2 = B is im2col(x)
 // (weight gradient dW = dz^T im2col(x), MN-major, K = output pixels of one batch entry); 3 = AIM 1 with
 // the whole B operand (N <= 64, K <= 576: the filter) loaded once per CTA and kept resident in shared
 // memory, so only the im2col A tiles stream (the same UMMAs in the same order: the same bits)
@@ -362,6 +363,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
               tma_load_3d(sb + j * MN_BLOCK_BYTES, &map_b, n0 + 64 * j, kb * BK, t / per_batch, full(stage));
+          } else if constexpr (AIM == 4) {  // A K-major box; B [k][n]: one 64 x 64 box per 64-wide N block
+            tma_load_3d(sa, &map_a, kb * BK, m0, t / per_batch, full(stage));
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_3d(sb + j * MN_BLOCK_BYTES, &map_b, n0 + 64 * j, kb * BK, t / per_batch, full(stage));
           } else {
             tma_load_3d(sa, &map_a, kb * BK, m0, t / per_batch, full(stage));
             tma_load_3d(sb, &map_b, kb * BK, n0, t / per_batch, full(stage));
@@ -376,7 +382,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     // ---- MMA issuer --------------------------------------------------------
     if (lane == 0) {
-      constexpr uint32_t idesc = instr_desc<BN, MN>();
+      constexpr uint32_t idesc = instr_desc<BN, MN, AIM == 4>();
+      constexpr bool BMJ = MN || AIM == 4;  // B operand MN-major
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
@@ -391,10 +398,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc_fence_after();
           const uint32_t sa = base + stage * L::STAGE;
           const uint32_t sb = AIM == 3 ? base + L::RES + kb * L::B_BYTES : sa + L::A_BYTES;
-          const uint64_t da = op_desc<MN>(sa), db = op_desc<MN>(sb);
+          const uint64_t da = op_desc<MN>(sa), db = op_desc<BMJ>(sb);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)  // K-major: +32 B inside the swizzled row; MN-major: +2 k groups
-            tc_mma(d, da + k * k_step<MN>(), db + k * k_step<MN>(), idesc, (kb | k) != 0);
+            tc_mma(d, da + k * k_step<MN>(), db + k * k_step<BMJ>(), idesc, (kb | k) != 0);
           tc_commit(empty(stage));  // frees the smem stage when these MMAs complete
           if (++stage == STAGES) {
             stage = 0;
@@ -607,7 +614,14 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             } else {
               tma_load_3d_pair(sa, &map_a, kb * BK, m0 + (int)rank * BM, t / per_batch, lb);
             }
-            tma_load_3d_pair(sb, &map_b, kb * BK, n0 + (int)rank * (PAIR_BN / 2), t / per_batch, lb);
+            if constexpr (AIM == 4) {  // B [k][n]: this CTA's N half as 64 x 64 boxes
+#pragma unroll
+              for (int j = 0; j < PAIR_BN / 128; ++j)
+                tma_load_3d_pair(sb + j * MN_BLOCK_BYTES, &map_b, n0 + (int)rank * (PAIR_BN / 2) + 64 * j, kb * BK,
+                                 t / per_batch, lb);
+            } else {
+              tma_load_3d_pair(sb, &map_b, kb * BK, n0 + (int)rank * (PAIR_BN / 2), t / per_batch, lb);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -619,7 +633,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   } else if (warp == 1) {
     if (leader && lane == 0) {  // ---- MMA issuer (leader only) ----
       constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (MN ? (3u << 15) : 0u) |
-                                 ((uint32_t)(PAIR_BN >> 3) << 17) | ((uint32_t)(PAIR_M >> 4) << 24);
+                                 (AIM == 4 ? (1u << 16) : 0u) | ((uint32_t)(PAIR_BN >> 3) << 17) |
+                                 ((uint32_t)(PAIR_M >> 4) << 24);
+      constexpr bool BMJ = MN || AIM == 4;  // B operand MN-major
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
@@ -632,10 +648,10 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           mbar_wait(full(stage), phase);
           tc_fence_after();
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A_BYTES;
-          const uint64_t da = op_desc<MN>(sa), db = op_desc<MN>(sb);
+          const uint64_t da = op_desc<MN>(sa), db = op_desc<BMJ>(sb);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)
-            tc_mma_pair(d, da + k * k_step<MN>(), db + k * k_step<MN>(), idesc, (kb | k) != 0);
+            tc_mma_pair(d, da + k * k_step<MN>(), db + k * k_step<BMJ>(), idesc, (kb | k) != 0);
           tc_commit_pair(empty(stage));
           if (++stage == STAGES) {
             stage = 0;
@@ -975,6 +991,8 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
             make_map(&mb, g.b, N, K, BN, g.batch, g.sb);
   else if (AIM == 2)
     in_ok = make_map_mn(&ma, g.a, M, K, g.batch, g.sa) && make_im2col_map(&mb, g.b, g.xN, g.xH, g.xW, g.xC, g.cg, 64);
+  else if (AIM == 4)
+    in_ok = make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) && make_map_mn(&mb, g.b, N, K, g.batch, g.sb);
   else
     in_ok = MN ? make_map_mn(&ma, g.a, M, K, g.batch, g.sa) && make_map_mn(&mb, g.b, N, K, g.batch, g.sb)
                : make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) && make_map(&mb, g.b, N, K, BN, g.batch, g.sb);
@@ -1011,6 +1029,7 @@ static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
                      make_map(&mb, g.b, N, K, gemm::PAIR_BN / 2, g.batch, g.sb)
       : AIM == 2 ? make_map_mn(&ma, g.a, M, K, g.batch, g.sa) &&
                      make_im2col_map(&mb, g.b, g.xN, g.xH, g.xW, g.xC, g.cg, 64)
+      : AIM == 4 ? make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) && make_map_mn(&mb, g.b, N, K, g.batch, g.sb)
       : MN     ? make_map_mn(&ma, g.a, M, K, g.batch, g.sa) && make_map_mn(&mb, g.b, N, K, g.batch, g.sb)
                : make_map(&ma, g.a, M, K, gemm::BM, g.batch, g.sa) &&
                      make_map(&mb, g.b, N, K, gemm::PAIR_BN / 2, g.batch, g.sb);
@@ -1058,25 +1077,31 @@ static int gemm_variant() {  // BT_GEMM_VARIANT=1 forces the 1-CTA kernel (tests
 
 // 256 x 256 CTA-pair tiles when M and N allow it, else 128 x {256, 128, 64} tiles; ragged M / N / K
 // edges are zero-filled by the TMA loads and clipped by the TMA stores (all deterministic)
-template <bool MN>
+template <bool MN, int AIM = 0>
 static int launch_any(const GemmShape& g, int out_bf16, int grid, cudaStream_t s) {
   constexpr int SP = gemm::EPI_WARPS == 8 ? 5 : 3, S256 = gemm::EPI_WARPS == 8 ? 3 : 2,
                 S64 = gemm::EPI_WARPS == 8 ? 6 : 4, S128 = gemm::EPI_WARPS == 8 ? 5 : 3;
   if (g.M % 256 == 0 && g.N % 256 == 0 && gemm_variant() != 1) {
     if (g.epi.kind == EPI_FFN_FWD || g.epi.kind == EPI_FFN_BWD)  // ALU-heavy epilogues: 16 epilogue warps
-      return launch_gemm_pair<3, true, MN, 16>(g, grid, s);
-    return out_bf16 ? launch_gemm_pair<SP, true, MN>(g, grid, s) : launch_gemm_pair<SP, false, MN>(g, grid, s);
+      return launch_gemm_pair<3, true, MN, 16, AIM>(g, grid, s);
+    return out_bf16 ? launch_gemm_pair<SP, true, MN, gemm::EPI_WARPS, AIM>(g, grid, s)
+                    : launch_gemm_pair<SP, false, MN, gemm::EPI_WARPS, AIM>(g, grid, s);
   }
   if (g.N % 256 == 0)
-    return out_bf16 ? launch_gemm<256, S256, true, MN>(g, grid, s) : launch_gemm<256, S256, false, MN>(g, grid, s);
+    return out_bf16 ? launch_gemm<256, S256, true, MN, AIM>(g, grid, s)
+                    : launch_gemm<256, S256, false, MN, AIM>(g, grid, s);
   if (g.N <= 64)  // narrow outputs (64-channel convolutions)
-    return out_bf16 ? launch_gemm<64, S64, true, MN>(g, grid, s) : launch_gemm<64, S64, false, MN>(g, grid, s);
-  return out_bf16 ? launch_gemm<128, S128, true, MN>(g, grid, s) : launch_gemm<128, S128, false, MN>(g, grid, s);
+    return out_bf16 ? launch_gemm<64, S64, true, MN, AIM>(g, grid, s) : launch_gemm<64, S64, false, MN, AIM>(g, grid, s);
+  return out_bf16 ? launch_gemm<128, S128, true, MN, AIM>(g, grid, s)
+                  : launch_gemm<128, S128, false, MN, AIM>(g, grid, s);
 }
+// mn: 0 = A and B K-major (C = A.B^T); 1 = both MN-major (C = A^T.B); 2 = A K-major, B MN-major (C = A.B
+// with B stored [K][N]) -- the same UMMAs over the same k order, so the same bits as mode 0 on B^T.
 int gemm_bf16_launch_any(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
-                         int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, bool mn, cudaStream_t s) {
-  const GemmShape g{a, b, c, M, N, K, batch, sa, sb, sc, epi, mn};
+                         int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, int mn, cudaStream_t s) {
+  const GemmShape g{a, b, c, M, N, K, batch, sa, sb, sc, epi, mn == 1};
   if (epi.kind == EPI_FFN_FWD || epi.kind == EPI_FFN_BWD) out_bf16 = 1;
+  if (mn == 2) return launch_any<false, 4>(g, out_bf16, grid, s);
   return mn ? launch_any<true>(g, out_bf16, grid, s) : launch_any<false>(g, out_bf16, grid, s);
 }
 // Implicit-GEMM convolution products (1-CTA tiles).  fwd: C[Ho*Wo*N][Co] = im2col(x) . W^T with W [Co][K],
@@ -1147,7 +1172,7 @@ int gemm_conv_launch(int wgrad, const void* x, int xN, int xH, int xW, int Ci, i
 
 int gemm_bf16_tn_launch_epi(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                             int64_t sb, int64_t sc, int out_bf16, int grid, const GemmEpi& epi, cudaStream_t s) {
-  return gemm_bf16_launch_any(a, b, c, batch, M, N, K, sa, sb, sc, out_bf16, grid, epi, false, s);
+  return gemm_bf16_launch_any(a, b, c, batch, M, N, K, sa, sb, sc, out_bf16, grid, epi, 0, s);
 }
 int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                         int64_t sb, int64_t sc, int out_bf16, int grid, cudaStream_t s) {

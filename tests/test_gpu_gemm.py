@@ -136,3 +136,46 @@ def test_mn_major_gemm(gemm, monkeypatch, E, M, N, K, variant):
         assert torch.equal(c[e].view(torch.int32), gemm_bf16_at_b(a[e], b[e])[0].view(torch.int32)), e
     kmaj = gemm_bf16_batched(a.transpose(1, 2).contiguous(), b.transpose(1, 2).contiguous())
     assert torch.equal(c.view(torch.int32), kmaj.view(torch.int32))
+
+
+@pytest.mark.parametrize("M,N,K,bf16", [(512, 768, 3072, True), (512, 3072, 768, False), (384, 256, 768, True),
+                                         (200, 128, 256, False), (128, 64, 192, True)])
+def test_b_mn_major_equals_k_major_on_the_transpose(M, N, K, bf16):
+    """mn_major = 2 (A K-major, B stored [K][N]): C = A.B reading the weight as stored equals the
+    K-major GEMM on B^T bit for bit -- pair tiles, 1-CTA 256/128/64 tiles and ragged M."""
+    import ctypes as C
+
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    a, bt = _inputs(M, N, K, 11)           # bt: [N][K] (K-major B)
+    b_kn = bt.T.contiguous()               # the same matrix stored [K][N]
+    dt = torch.bfloat16 if bf16 else torch.float32
+    c0 = torch.empty(M, N, dtype=dt, device="cuda")
+    c2 = torch.empty(M, N, dtype=dt, device="cuda")
+    L = _native.lib()
+    _native.check(L.bt_gemm_bf16_ex(a.data_ptr(), bt.data_ptr(), c0.data_ptr(), 1, M, N, K, 0, 0, 0, int(bf16), None,
+                                    0, 0, stream()))
+    _native.check(L.bt_gemm_bf16_ex(a.data_ptr(), b_kn.data_ptr(), c2.data_ptr(), 1, M, N, K, 0, 0, 0, int(bf16), None,
+                                    2, 0, stream()))
+    iv = torch.int16 if bf16 else torch.int32
+    assert torch.equal(c0.view(iv), c2.view(iv))
+
+
+def test_ffn_backward_epilogue_with_b_mn_major():
+    """The FFN backward GEMM (dropout' + GELU' epilogue) reading W2 as stored [D][F] == on W2^T."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    T, F, D = 512, 1024, 256
+    g = torch.Generator(device="cuda").manual_seed(5)
+    dy = (torch.randn(T, D, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    w2 = (torch.randn(D, F, device="cuda", generator=g) * 0.1).to(torch.bfloat16)   # [D][F] = [K][N]
+    aux = (torch.randn(T, F, device="cuda", generator=g)).to(torch.bfloat16)
+    outs = []
+    for kind, b in ((2, w2.T.contiguous()), (2 | 0x100, w2)):
+        c = torch.empty(T, F, dtype=torch.bfloat16, device="cuda")
+        _native.check(_native.lib().bt_gemm_bf16_ffn(dy.data_ptr(), b.data_ptr(), c.data_ptr(), T, F, D, kind, None,
+                                                     aux.data_ptr(), None, 42, 3, 0, 128, 0.1, 0, stream()))
+        outs.append(c)
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
