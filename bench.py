@@ -491,11 +491,12 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
     ms_per_est = e0.elapsed_time(e1) / steps
     del per_est
     torch.cuda.empty_cache()
+    from paper_2208_14228_b200.runlog import bitdiff
+
     a, b = BertJob(ests=ests, layers=2, est_group=4, fanin=2), BertJob(ests=ests, layers=2, est_group=4, fanin=2)
-    for _ in range(2):
-        a.step()
-        b.step([ests // 4] * 4)
-    same = bool(torch.equal(a.params.view(torch.int32), b.params.view(torch.int32)))
+    la, lb = a.run_log(2), b.run_log(2, groups=[ests // 4] * 4)  # per-EST losses + weight fingerprints per step
+    same = bool(torch.equal(a.params.view(torch.int32), b.params.view(torch.int32))) and bitdiff(la, lb) is None
+    grouping_fp = la.records[-1].param_hash
     del a, b
     torch.cuda.empty_cache()
     gemm_ms = split.get("gemm_bf16", 0.0)
@@ -518,7 +519,8 @@ def bench_bert(peaks, ests=32, steps=5, warmup=3):
                          "step_level_tflops": round(flops / ms / 1e9, 1), "dense_flops_per_step": flops,
                          "note": "L2 not flushed between the 20 back-to-back launches (55 MB of operands)"},
             "kernel_ms_per_step": {k: round(v, 3) for k, v in sorted(split.items(), key=lambda kv: -kv[1])},
-            "bit_identical_groupings": {"groups": [[ests], [ests // 4] * 4], "layers": 2, "steps": 2, "equal": same},
+            "bit_identical_groupings": {"groups": [[ests], [ests // 4] * 4], "layers": 2, "steps": 2, "equal": same,
+                                        "run_logs": "runlog.bitdiff: no divergence", "weights_fp": grouping_fp},
             "params_fnv": fnv_one}
 
 
@@ -629,8 +631,11 @@ def bench_resnet(peaks, ests=16, batch=32, steps=10, warmup=3):
     flops = job.flops_per_step()
     del job
     torch.cuda.empty_cache()
+    from paper_2208_14228_b200.runlog import bitdiff
+
     a, b = ResNetJob(ests=ests, batch=batch, gpus=8), ResNetJob(ests=ests, batch=batch, gpus=1)
     switch_us = []
+    la = None
     for gpus in (8, 4, 2):
         if gpus != 8:
             r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -639,13 +644,12 @@ def bench_resnet(peaks, ests=16, batch=32, steps=10, warmup=3):
             r1.record(s)
             r1.synchronize()
             switch_us.append(round(r0.elapsed_time(r1) * 1e3, 1))
-        for _ in range(2):
-            a.step()
-            b.step()
+        la = a.run_log(2, la)
+    lb = b.run_log(6)
     sa, sb = a.est_state(), b.est_state()
     same = bool(torch.equal(a.params.view(torch.int32), b.params.view(torch.int32)) and
                 torch.equal(sa["run_mean"].view(torch.int32), sb["run_mean"].view(torch.int32)) and
-                torch.equal(sa["run_var"].view(torch.int32), sb["run_var"].view(torch.int32)))
+                torch.equal(sa["run_var"].view(torch.int32), sb["run_var"].view(torch.int32))) and bitdiff(la, lb) is None
     del a, b
     torch.cuda.empty_cache()
     return {"workload": "C3: ResNet-18 (CIFAR layout, widths 64-512) with per-EST BatchNorm, 16 ESTs x 32 "
@@ -653,7 +657,9 @@ def bench_resnet(peaks, ests=16, batch=32, steps=10, warmup=3):
             "samples_per_s": round(ests * batch / (ms / 1e3), 1), "unit": "images/s", "ms_per_step": round(ms, 3),
             "conv_tflops_step_level": round(flops / ms / 1e9, 1), "loss": round(losses.mean().item(), 5),
             "rescale_8_4_2": {"schedule": "2 steps @8, rescale, 2 @4, rescale, 2 @2 vs 6 steps @1",
-                              "bit_identical_weights_and_bn_stats": same, "context_switch_us": switch_us}}
+                              "bit_identical_weights_and_bn_stats": same, "context_switch_us": switch_us,
+                              "run_logs": "per-EST losses + weight fingerprint per step, runlog.bitdiff: no divergence",
+                              "weights_fp": la.records[-1].param_hash}}
 
 
 def _oracle_run(threads: int):

@@ -239,6 +239,13 @@ int bt_bert_data(uint64_t seed, int64_t step, int32_t est_base, int32_t E, int32
 int bt_bert_attn(int32_t backward, const void *qkv_dev, const void *dctx_dev, void *out_dev, int32_t E, int32_t Te,
                  int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed, int64_t step,
                  float p, const int64_t *step_dev, void *stream);
+/* bt_bert_attn with the softmax row statistics kept between the passes: the forward (tcgen05 path)
+ * writes (-max * scale, 1 / sum) of every query row to stats_dev [E*Te/128 * heads][128] float2, the
+ * backward reads them instead of recomputing (the same instruction sequence on the same S: the same
+ * bits); stats_dev NULL: the backward recomputes them. */
+int bt_bert_attn_ex(int32_t backward, const void *qkv_dev, const void *dctx_dev, void *out_dev, int32_t E,
+                    int32_t Te, int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer,
+                    uint64_t seed, int64_t step, float p, const int64_t *step_dev, float *stats_dev, void *stream);
 /* x = resid + dropout(branch + bias); y = LayerNorm(x) * gamma + beta -> xsum (x), stats (mean, rstd)
  * [T][2], y32 (may be NULL), yb (bf16).  resid fp32 (the residual stream), branch bf16 (a GEMM output). */
 int bt_bert_ln_fwd(const float *resid_dev, const void *branch_dev, const float *bias_dev, const float *gamma_dev,
@@ -353,6 +360,10 @@ int bt_allgather_params(int32_t dtype, const void *src_dev, void *const *dst_dev
 /* Stream-ordered copy between any two device (or peer / IPC-mapped / pinned host) addresses:
  * the guarded multi-rank reducer publishes each shard's status word with it. */
 int bt_memcpy_async(void *dst, const void *src, int64_t nbytes, void *stream);
+/* FNV-1a 64 of every `chunk`-byte slice of a device buffer (chunk % 16 == 0; the last slice may be
+ * short) into out_dev [ceil(nbytes / chunk)]: the parallel half of the model-stack fingerprint
+ * (runlog.device_fingerprint = host FNV-1a of these values).                   runlog.py:30-31 */
+int bt_fnv1a64_chunks(const void *data_dev, int64_t nbytes, int64_t chunk, uint64_t *out_dev, void *stream);
 /* Reset a status block to {0, INT32_MAX, 0, 0}. */
 int bt_flags_reset(int32_t *flags_dev, void *stream);
 /* Synchronise `stream`, read the status block; returns its status word. */

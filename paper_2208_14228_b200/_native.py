@@ -122,6 +122,8 @@ EXPORTS = {
     "bt_bert_embed_grad": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i64, _vp]),
     "bt_bert_attn": (C.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _u64, _i64,
                                C.c_float, _vp, _vp]),
+    "bt_bert_attn_ex": (C.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _u64, _i64,
+                                  C.c_float, _vp, _vp, _vp]),
     "bt_bert_ln_fwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
                                  _i32, _u64, _i64, C.c_float, C.c_float, _vp, _vp]),
     "bt_bert_ln_fwd_rc": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32,
@@ -153,6 +155,7 @@ EXPORTS = {
     "bt_est_slot_copy": (C.c_int, [C.POINTER(_vp), C.POINTER(_vp), _i64p, _i32, _vp]),
     "bt_allgather_params": (C.c_int, [_i32, _vp, C.POINTER(_vp), _i32, _i64, _vp]),
     "bt_memcpy_async": (C.c_int, [_vp, _vp, _i64, _vp]),
+    "bt_fnv1a64_chunks": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
     "bt_flags_reset": (C.c_int, [_vp, _vp]),
     "bt_step_status": (C.c_int, [_vp, _i32p, _i32p, _vp]),
     "bt_ipc_handle_size": (C.c_int, []),

@@ -200,7 +200,8 @@ class BertJob:
                         "ctx": torch.empty(T, D, **bf), "hs1": torch.empty(T, D, **f32), "st1": torch.empty(T, 2, **f32),
                         "h1b": torch.empty(T, D, **bf), "Hpre": torch.empty(T, F, **bf),
                         "Dact": torch.empty(T, F, **bf), "hs2": torch.empty(T, D, **f32),
-                        "st2": torch.empty(T, 2, **f32)} for _ in range(L)],
+                        "st2": torch.empty(T, 2, **f32),
+                        "ast": torch.empty(T * self.H, 2, **f32)} for _ in range(L)],  # attention row statistics
             "x32": torch.empty(T, D, **f32), "y32": torch.empty(T, D, **f32),
             "brb": torch.empty(T, D, **bf), "ytop": torch.empty(T, D, **bf),
             "tgt": torch.empty(T, D, **f32), "dy1": [torch.empty(T, D, **bf) for _ in range(2)],
@@ -267,8 +268,8 @@ class BertJob:
             w = lay[l]
             self._gemm(w["xb"].data_ptr(), self._wb(l, "Wqkv"), w["qkv"].data_ptr(), T, 3 * D, D, out_bf16=True,
                        bias=self._p(l, "bqkv"))
-            _native.check(L.bt_bert_attn(0, w["qkv"].data_ptr(), None, w["ctx"].data_ptr(), n, Te, D, H, base, NL, l,
-                                         seed, step, self.pa, sp, s), "attention forward")
+            _native.check(L.bt_bert_attn_ex(0, w["qkv"].data_ptr(), None, w["ctx"].data_ptr(), n, Te, D, H, base, NL,
+                                            l, seed, step, self.pa, sp, w["ast"].data_ptr(), s), "attention forward")
             self._gemm(w["ctx"].data_ptr(), self._wb(l, "Wo"), ws["brb"].data_ptr(), T, D, D, out_bf16=True)
             if l == 0:  # the embedding input is stored fp32; later residuals are recomputed (bt_bert_ln_fwd_rc)
                 _native.check(L.bt_bert_ln_fwd(x32.data_ptr(), ws["brb"].data_ptr(), self._p(l, "bo"),
@@ -340,8 +341,9 @@ class BertJob:
                                             self._g(lb, l, "bo"), self.P, s))
             self._dx(ws["dbr"].data_ptr(), self._wb(l, "Wo"), ws["dctx"].data_ptr(), T, D, D)
             self._wgrad(ws, n, ws["dbr"].data_ptr(), w["ctx"].data_ptr(), D, D, self._g(lb, l, "Wo"))
-            _native.check(L.bt_bert_attn(1, w["qkv"].data_ptr(), ws["dctx"].data_ptr(), ws["dqkv"].data_ptr(), n, Te,
-                                         D, H, base, NL, l, seed, step, self.pa, sp, s), "attention backward")
+            _native.check(L.bt_bert_attn_ex(1, w["qkv"].data_ptr(), ws["dctx"].data_ptr(), ws["dqkv"].data_ptr(), n,
+                                            Te, D, H, base, NL, l, seed, step, self.pa, sp, w["ast"].data_ptr(), s),
+                          "attention backward")
             if capture is not None and l == 0:
                 capture.update(dh=B.clone(), da=ws["dbr"].clone(), dctx=ws["dctx"].clone(), dqkv=ws["dqkv"].clone())
             self._dx(ws["dqkv"].data_ptr(), self._wb(l, "Wqkv"), A.data_ptr(), T, D, 3 * D)
@@ -437,6 +439,28 @@ class BertJob:
         if st is None or st.numel() != self.P:
             st = self._stage_buf = torch.empty(self.P, dtype=torch.float32, device="cuda")
         return st
+
+    def fingerprint(self) -> str:
+        """FNV fingerprint of the fp32 master weights (runlog.device_fingerprint: 64 KB slices hashed on the
+        GPU, then on the host) -- the model-stack counterpart of the reference's per-step param_hash."""
+        from .runlog import device_fingerprint
+
+        return device_fingerprint(self.params)
+
+    def run_log(self, steps: int, log=None, every: int = 1, groups=None):
+        """`steps` mini-batches recorded like the reference's run_training (scenarios.py:69-80): per step
+        the per-EST losses (binary64 hex on disk) and, every `every` steps (sampled: the weights are
+        hundreds of MB), the weight fingerprint; returns the RunLog (comparable with runlog.bitdiff)."""
+        from .runlog import RunLog, RunRecord
+
+        if log is None:
+            log = RunLog(self.E, "d1", self.seed)
+        for _ in range(steps):
+            losses = self.step(groups) if groups is not None else self.step()
+            n = self.step_idx
+            h = self.fingerprint() if every and n % every == 0 else ""
+            log.add(RunRecord(n, [float(x) for x in losses.tolist()], h))
+        return log
 
     def attach_peer(self, group=None):
         """Multi-GPU (one process per GPU, torch.distributed initialised, rank r holding the r-th contiguous

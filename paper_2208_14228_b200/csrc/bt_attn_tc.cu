@@ -44,6 +44,7 @@ struct Args {
   int64_t step;
   float p;
   const int64_t* step_dev;
+  float2* stats;  // [n_items][128] (nm, inv) of every query row for the backward, or NULL
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(THREADS, 4)
     // this thread's row of S, three passes over TMEM (row max; exp2 row sum in column order; P)
     float nm, inv;
     row_stats(lane_base, &nm, &inv);
+    if (a.stats) a.stats[(size_t)it * SEQ + tid] = make_float2(nm, inv);  // the backward reuses them (same bits)
     // dropout keyed by (EST, step, layer, sequence, head, row, column pair) -- bt_bert.cu's layout
     const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
     const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
@@ -300,6 +302,7 @@ struct BwdArgs {
   int64_t step;
   float p;
   const int64_t* step_dev;
+  const float2* stats;  // the forward's row statistics [n_items][128], or NULL: recompute them
 };
 
 // 32 TMEM columns of this lane's row -> 32 bf16 (64 bytes) at dst
@@ -389,7 +392,13 @@ __global__ void __launch_bounds__(B_THREADS, 2)
     mbar_wait(bar_s, ph);
     tc_fence_after();
     float nm, inv;
-    row_stats_half(lane_base, hf, row, red, &nm, &inv);
+    if (a.stats) {  // the forward's statistics of this row: the same instruction sequence on the same S
+      const float2 st = a.stats[(size_t)it * SEQ + row];
+      nm = st.x;
+      inv = st.y;
+    } else {
+      row_stats_half(lane_base, hf, row, red, &nm, &inv);
+    }
     const int e = s / a.seqs_per_est, sl = s - e * a.seqs_per_est;
     const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
     const uint64_t nb = ((((uint64_t)step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4) +
@@ -424,7 +433,7 @@ __global__ void __launch_bounds__(B_THREADS, 2)
       }
       mbits[c2] = bits;
     }
-    __syncthreads();  // the sum slots of row_stats_half are read
+    if (!a.stats) __syncthreads();  // the sum slots of row_stats_half are read
     red[hf * SEQ + row] = D;
     __syncthreads();
     D = red[row] + red[SEQ + row];  // (half 0 + half 1)
@@ -522,7 +531,8 @@ __global__ void __launch_bounds__(B_THREADS, 2)
 }  // namespace attn_tc
 
 int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int seqs_per_est, int est_base, int L,
-                       int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev, cudaStream_t s) {
+                       int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev, cudaStream_t s,
+                       float* stats) {
   const int T = n_seq * attn_tc::SEQ;
   CUtensorMap mqk, mv;
   if (!make_map(&mqk, qkv, T, 3 * Dm, attn_tc::SEQ, 1, (int64_t)T * 3 * Dm) ||
@@ -535,7 +545,8 @@ int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int
       return ERR_CUDA;
     attr = true;
   }
-  attn_tc::Args a{(__nv_bfloat16*)out, Dm, H, seqs_per_est, est_base, L, layer, n_seq * H, seed, step, p, step_dev};
+  attn_tc::Args a{(__nv_bfloat16*)out, Dm, H, seqs_per_est, est_base, L, layer, n_seq * H, seed, step, p, step_dev,
+                  (float2*)stats};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -546,7 +557,7 @@ int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int
 
 int attn_bwd_tc_launch(const void* qkv, const void* dctx, void* dqkv, int n_seq, int Dm, int H, int seqs_per_est,
                        int est_base, int L, int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev,
-                       cudaStream_t s) {
+                       cudaStream_t s, const float* stats) {
   const int T = n_seq * attn_tc::SEQ;
   CUtensorMap mqk, mdo;
   if (!make_map(&mqk, qkv, T, 3 * Dm, attn_tc::SEQ, 1, (int64_t)T * 3 * Dm) ||
@@ -560,7 +571,7 @@ int attn_bwd_tc_launch(const void* qkv, const void* dctx, void* dqkv, int n_seq,
     attr = true;
   }
   attn_tc::BwdArgs a{(__nv_bfloat16*)dqkv, Dm, H, seqs_per_est, est_base, L, layer, n_seq * H, seed, step, p,
-                     step_dev};
+                     step_dev, (const float2*)stats};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -56,7 +56,7 @@ int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, 
                                cudaStream_t s);
 int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out, int n_seq, int Dm, int H,
                      int seqs_per_est, int est_base, int L, int layer, uint64_t seed, int64_t step, float p,
-                     const int64_t* step_dev, cudaStream_t s);
+                     const int64_t* step_dev, cudaStream_t s, float* stats);
 int bert_ln_launch(int backward, const float* in1, const void* in2, const float* bias, const float* gamma,
                    const float* beta, float* xsum, float* stats, float* y32, void* yb, float* part, int E, int Te,
                    int D, int est_base, int L, int layer, int site, uint64_t seed, int64_t step, float p, float eps,
@@ -95,6 +95,7 @@ int cnn_head_launch(const void* x, const int32_t* labels, const float* W, const 
                     float* db, int64_t grad_stride, float* loss, void* dx, cudaStream_t s);
 int cnn_conv_weights_launch(const float* const* w, void* const* wb, void* const* wt, const int* Co, const int* T,
                             const int* Ci, const int* flip, int n, cudaStream_t s);
+int fnv_chunks_launch(const void* data, int64_t nbytes, int64_t chunk, uint64_t* out, cudaStream_t s);
 int emb_tokens_launch(uint64_t seed, int64_t step, const int64_t* step_dev, int est_base, int E, int S, int V, int np,
                       int mask_id, int32_t* ids, int32_t* mrow, int32_t* mlabel, cudaStream_t s);
 int emb_fwd_launch(const int32_t* ids, const float* W, const float* Pe, int T, int D, float* x32, void* xb,
@@ -635,6 +636,11 @@ int bt_memcpy_async(void* dst, const void* src, int64_t nbytes, void* stream) {
   return 0;
 }
 
+int bt_fnv1a64_chunks(const void* data_dev, int64_t nbytes, int64_t chunk, uint64_t* out_dev, void* stream) {
+  if (!data_dev || !out_dev || nbytes < 1 || chunk < 16 || chunk % 16) return fail(bt::ERR_INPUT, "fnv chunks");
+  return done(bt::fnv_chunks_launch(data_dev, nbytes, chunk, out_dev, STREAM(stream)), "bt_fnv1a64_chunks");
+}
+
 int bt_flags_reset(int32_t* flags_dev, void* stream) {
   return done(bt::flags_reset_launch(flags_dev, STREAM(stream)), "bt_flags_reset");
 }
@@ -799,16 +805,22 @@ int bt_bert_data(uint64_t seed, int64_t step, int32_t est_base, int32_t E, int32
                                    STREAM(stream)),
               "bt_bert_data");
 }
-int bt_bert_attn(int32_t backward, const void* qkv_dev, const void* dctx_dev, void* out_dev, int32_t E, int32_t Te,
-                 int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed, int64_t step,
-                 float p, const int64_t* step_dev, void* stream) {
+int bt_bert_attn_ex(int32_t backward, const void* qkv_dev, const void* dctx_dev, void* out_dev, int32_t E,
+                    int32_t Te, int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed,
+                    int64_t step, float p, const int64_t* step_dev, float* stats_dev, void* stream) {
   if (int st = bert_shape(E, Te, D)) return st;
   if (heads * 64 != D) return fail(bt::ERR_INPUT, "bert attention: head dim must be 64 (heads %d, D %d)", heads, D);
   if (!qkv_dev || !out_dev || (backward && !dctx_dev)) return fail(bt::ERR_INPUT, "null pointer");
   if (!(p >= 0.f && p < 1.f) || layer < 0 || layer >= layers) return fail(bt::ERR_CONFIG, "bad dropout / layer");
   return done(bt::bert_attn_launch(backward, qkv_dev, dctx_dev, out_dev, E * Te / 128, D, heads, Te / 128, est_base,
-                                   layers, layer, seed, step, p, step_dev, STREAM(stream)),
+                                   layers, layer, seed, step, p, step_dev, STREAM(stream), stats_dev),
               "bt_bert_attn");
+}
+int bt_bert_attn(int32_t backward, const void* qkv_dev, const void* dctx_dev, void* out_dev, int32_t E, int32_t Te,
+                 int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed, int64_t step,
+                 float p, const int64_t* step_dev, void* stream) {
+  return bt_bert_attn_ex(backward, qkv_dev, dctx_dev, out_dev, E, Te, D, heads, est_base, layers, layer, seed, step, p,
+                         step_dev, nullptr, stream);
 }
 int bt_bert_ln_fwd(const float* resid_dev, const void* branch_dev, const float* bias_dev, const float* gamma_dev,
                    const float* beta_dev, float* xsum_dev, float* stats_dev, float* y32_dev, void* yb_dev, int32_t E,

@@ -122,6 +122,43 @@ __global__ void flags_reset_kernel(int32_t* flags) {
 
 int tanh_launch(const double* x, int64_t n, double* out, cudaStream_t s);
 
+// FNV-1a 64 (prng.py:72-78) of each `chunk`-byte slice of `data` (the last may be short): thread c hashes
+// slice c byte-serially (reading 16-byte vectors when aligned).  The model-stack fingerprint is the host
+// FNV-1a of these values' little-endian bytes -- byte-exact like the reference's param_fingerprint
+// (runlog.py:30-31) but parallel: a byte-serial hash of hundreds of MB takes seconds on a host core.
+__global__ void fnv_chunks_kernel(const uint8_t* __restrict__ data, int64_t nbytes, int64_t chunk, int64_t nchunks,
+                                  uint64_t* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  const int64_t lo = c * chunk, hi = lo + chunk < nbytes ? lo + chunk : nbytes;
+  uint64_t h = 0xCBF29CE484222325ull;
+  int64_t i = lo;
+  if ((((uintptr_t)data + lo) & 15) == 0) {
+    for (; i + 16 <= hi; i += 16) {
+      const uint4 v = __ldcs((const uint4*)(data + i));
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          h ^= (w[k] >> (8 * b)) & 0xffu;
+          h *= 0x100000001B3ull;
+        }
+    }
+  }
+  for (; i < hi; ++i) {
+    h ^= data[i];
+    h *= 0x100000001B3ull;
+  }
+  out[c] = h;
+}
+
+int fnv_chunks_launch(const void* data, int64_t nbytes, int64_t chunk, uint64_t* out, cudaStream_t s) {
+  const int64_t n = (nbytes + chunk - 1) / chunk;
+  fnv_chunks_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>((const uint8_t*)data, nbytes, chunk, n, out);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
+
 int flags_reset_launch(int32_t* flags, cudaStream_t s) {
   flags_reset_kernel<<<1, 32, 0, s>>>(flags);
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;

@@ -509,6 +509,28 @@ class ResNetJob:
             st = self._stage_buf = torch.empty(self.P, dtype=torch.float32, device="cuda")
         return st
 
+    def fingerprint(self) -> str:
+        """FNV fingerprint of the fp32 master weights (runlog.device_fingerprint: 64 KB slices hashed on the
+        GPU, then on the host) -- the model-stack counterpart of the reference's per-step param_hash."""
+        from .runlog import device_fingerprint
+
+        return device_fingerprint(self.params)
+
+    def run_log(self, steps: int, log=None, every: int = 1):
+        """`steps` mini-batches recorded like the reference's run_training (scenarios.py:69-80): per step
+        the per-EST losses (binary64 hex on disk) and, every `every` steps (sampled: the weights are
+        hundreds of MB), the weight fingerprint; returns the RunLog (comparable with runlog.bitdiff)."""
+        from .runlog import RunLog, RunRecord
+
+        if log is None:
+            log = RunLog(self.E, "d1", self.seed)
+        for _ in range(steps):
+            losses = self.step()
+            n = self.step_idx
+            h = self.fingerprint() if every and n % every == 0 else ""
+            log.add(RunRecord(n, [float(x) for x in losses.tolist()], h))
+        return log
+
     def attach_peer(self, group=None):
         """Multi-GPU (one process per GPU, torch.distributed initialised, rank r holding the r-th contiguous
         EST block): the exchange becomes paper_2208_14228_b200.peer.PeerGroupReducer over CUDA IPC (Tree(2):

@@ -511,3 +511,26 @@ def test_mlm_head_groupings_are_bitwise_identical(bert):
     for _ in range(3):
         assert np.array_equal(_bits(a.step([2, 2])), _bits(b.step()))
     assert np.array_equal(_bits(a.params), _bits(b.params))
+
+
+def test_run_logs_fingerprint_and_bitdiff(bert):
+    """The model stack's run log (runlog.RunLog: per-EST losses + the device weight fingerprint per step):
+    two groupings give identical logs (bitdiff: no divergence); the fingerprint is byte-exact (a
+    one-ULP change of one weight changes it) and equals its host restatement."""
+    import numpy as np
+
+    from paper_2208_14228_b200.prng import fnv1a64
+    from paper_2208_14228_b200.runlog import bitdiff, device_fingerprint
+
+    a = bert.BertJob(est_group=2, **SMALL)
+    b = bert.BertJob(est_group=2, **SMALL)
+    la = a.run_log(3)
+    lb = b.run_log(3, groups=[2, 2])
+    assert bitdiff(la, lb) is None and all(r.param_hash for r in la.records)
+    raw = a.params.cpu().numpy().tobytes()
+    chunks = [raw[i:i + (1 << 16)] for i in range(0, len(raw), 1 << 16)]
+    host = np.array([fnv1a64(c) for c in chunks], dtype=np.uint64).astype("<u8").tobytes()
+    assert device_fingerprint(a.params) == f"{fnv1a64(host):016x}" == la.records[-1].param_hash
+    p = a.params.clone()
+    p[12345] = float(np.nextafter(np.float32(p[12345].item()), np.float32(2.0)))
+    assert device_fingerprint(p) != la.records[-1].param_hash

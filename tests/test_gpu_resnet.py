@@ -431,3 +431,19 @@ def test_cuda_graph_replay_equals_eager_across_rescale(rn):
     assert a._graph is not None and np.array_equal(_bits(a.params), _bits(b.params))
     sa, sb = a.est_state(), b.est_state()
     assert np.array_equal(_bits(sa["run_var"]), _bits(sb["run_var"])) and torch.equal(sa["cursor"], sb["cursor"])
+
+
+def test_run_log_across_rescale(rn):
+    """C3's run log (per-EST losses + weight fingerprint every step) is identical for 8 -> 4 -> 2 launch
+    groups with the EST context switches and for the uninterrupted single group (runlog.bitdiff)."""
+    from paper_2208_14228_b200.runlog import bitdiff
+
+    a = rn.ResNetJob(gpus=8, **SMALL)
+    b = rn.ResNetJob(gpus=1, **SMALL)
+    la = a.run_log(2)
+    a.rescale(4)
+    a.run_log(2, la)
+    a.rescale(2)
+    a.run_log(2, la)
+    lb = b.run_log(6)
+    assert bitdiff(la, lb) is None and len(la.records) == 6 and all(r.param_hash for r in la.records)
