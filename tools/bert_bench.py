@@ -15,7 +15,7 @@ E = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 G = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 NL = int(sys.argv[3]) if len(sys.argv) > 3 else 12
 S = int(sys.argv[4]) if len(sys.argv) > 4 else 8
-job = BertJob(ests=E, seqs=S, layers=NL)
+job = BertJob(ests=E, seqs=S, layers=NL, est_group=4 if E % 4 == 0 else 1, fanin=2)
 groups = [E // G] * G
 W, K = int(os.environ.get("BT_BENCH_WARMUP", "3")), int(os.environ.get("BT_BENCH_STEPS", "5"))
 for _ in range(W):

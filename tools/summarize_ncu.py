@@ -4,6 +4,7 @@
 """
 import csv
 import json
+import os
 import subprocess
 import sys
 from collections import defaultdict
@@ -11,7 +12,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 OUT = ROOT / "gpurun_out"
-PROF = ROOT / "profiles"
+PROF = Path(os.environ.get("BT_PROF_OUT", ROOT / "profiles"))  # on a GPU box: a gpurun_out/ subdirectory
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 
 
