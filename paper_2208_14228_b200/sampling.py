@@ -99,7 +99,7 @@ def worker_rng(seed: int, epoch: int, local_step: int, worker_index: int) -> int
 class DataPipeline:
     """Shared data-worker pool with a progress-ordered queuing buffer."""
 
-    EPOCH_WINDOW = 2  # epochs of index lists uploaded together (the current one and the next)
+    EPOCH_WINDOW = 1  # epochs of index lists uploaded at least (a boundary costs one small async H2D)
 
     def __init__(self, seed: int, dataset_size: int, total_workers: int, micro_batch: int, jitter: float = 0.0,
                  worker_slots: int = 1, prefetch_depth: int = 2, shuffle: bool = True):
@@ -152,13 +152,33 @@ class DataPipeline:
                     del self._lists_host[old]
         return self._lists_host[epoch]
 
+    def _upload(self, host: np.ndarray) -> torch.Tensor:
+        """host lists -> a new device tensor through a reused pinned staging buffer (two, alternating; an
+        event guards each against reuse before its copy has run): stream-ordered, no host sync."""
+        n = host.size
+        if getattr(self, "_stage", None) is None or self._stage[0].numel() < n:
+            self._stage = [torch.empty(max(n, 4096), dtype=torch.int32).pin_memory() for _ in range(2)]
+            self._stage_ev = [None, None]
+            self._stage_i = 0
+        i = self._stage_i = self._stage_i ^ 1
+        if self._stage_ev[i] is not None:
+            self._stage_ev[i].synchronize()
+        buf = self._stage[i][:n]
+        buf.numpy()[:] = host.reshape(-1)
+        dev = torch.empty(host.shape, dtype=torch.int32, device="cuda")
+        dev.view(-1).copy_(buf, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._stage_ev[i] = ev
+        return dev
+
     def device_lists(self, first_epoch: int, last_epoch: int) -> tuple[torch.Tensor, int]:
         """Resident [n_epochs][workers][spe*B] lists covering [first, last]; returns (tensor, base epoch)."""
         if not (self._lists_dev is not None and self._lists_dev_base <= first_epoch
                 and last_epoch < self._lists_dev_base + self._lists_dev_count):
-            count = max(last_epoch - first_epoch + 1, self.EPOCH_WINDOW)  # the next epoch rides along
-            host = torch.from_numpy(np.stack([self._lists_for_epoch(e) for e in range(first_epoch, first_epoch + count)]))
-            self._lists_dev = host.pin_memory().to("cuda", non_blocking=True)  # stream-ordered, no host sync
+            count = max(last_epoch - first_epoch + 1, self.EPOCH_WINDOW)
+            host = np.stack([self._lists_for_epoch(e) for e in range(first_epoch, first_epoch + count)])
+            self._lists_dev = self._upload(host)
             self._lists_dev_base, self._lists_dev_count = first_epoch, count
         return self._lists_dev, self._lists_dev_base
 
