@@ -310,6 +310,24 @@ int bt_mlp_step(const bt_mlp_args* args, void* stream) {
   return done(bt::mlp_launch(*args, STREAM(stream)), "bt_mlp_step");
 }
 
+// Wait for the stream's work by polling an event (a spin, not a blocking wait): a blocking
+// synchronisation costs tens of microseconds of wake-up latency, which is most of a short call.
+static cudaError_t host_wait(cudaStream_t s) {
+  static thread_local cudaEvent_t ev = nullptr;
+  static thread_local int ev_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!ev || ev_dev != dev) {
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return cudaGetLastError();
+    ev_dev = dev;
+  }
+  cudaError_t e = cudaEventRecord(ev, s);
+  if (e != cudaSuccess) return e;
+  while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) {
+  }
+  return e;
+}
+
 int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_host, void* stream) {
   int st = validate_mlp(args);
   if (st) return st;
@@ -322,7 +340,7 @@ int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_hos
     return cuda_fail("bt_mlp_run losses");
   if (cudaMemcpyAsync(status_host, args->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return cuda_fail("bt_mlp_run status");
-  if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail("bt_mlp_run sync");
+  if (host_wait(s) != cudaSuccess) return cuda_fail("bt_mlp_run sync");
   g_err[0] = 0;
   return 0;
 }

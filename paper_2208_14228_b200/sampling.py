@@ -152,33 +152,42 @@ class DataPipeline:
                     del self._lists_host[old]
         return self._lists_host[epoch]
 
-    def _upload(self, host: np.ndarray) -> torch.Tensor:
-        """host lists -> a new device tensor through a reused pinned staging buffer (two, alternating; an
-        event guards each against reuse before its copy has run): stream-ordered, no host sync."""
-        n = host.size
+    def _upload(self, epochs: list) -> torch.Tensor:
+        """Epoch lists (host arrays) -> one device tensor [n_epochs][workers][spe*B], stream-ordered with
+        no host sync: two pinned staging buffers and two device buffers used alternately (an event guards
+        a staging buffer against reuse before its copy ran; a device buffer is rewritten only by a copy
+        queued after every kernel that read it)."""
+        per = epochs[0].size
+        n = per * len(epochs)
         if getattr(self, "_stage", None) is None or self._stage[0].numel() < n:
-            self._stage = [torch.empty(max(n, 4096), dtype=torch.int32).pin_memory() for _ in range(2)]
-            self._stage_ev = [None, None]
+            cap = max(n, 4 * per)
+            self._stage = [torch.empty(cap, dtype=torch.int32).pin_memory() for _ in range(2)]
+            self._stage_np = [t.numpy() for t in self._stage]
+            self._devbuf = [torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(2)]
+            self._devptr = [t.data_ptr() for t in self._devbuf]
+            self._stageptr = [t.data_ptr() for t in self._stage]
+            self._stage_ev = [torch.cuda.Event(), torch.cuda.Event()]
+            self._stage_used = [False, False]
             self._stage_i = 0
         i = self._stage_i = self._stage_i ^ 1
-        if self._stage_ev[i] is not None:
+        if self._stage_used[i]:
             self._stage_ev[i].synchronize()
-        buf = self._stage[i][:n]
-        buf.numpy()[:] = host.reshape(-1)
-        dev = torch.empty(host.shape, dtype=torch.int32, device="cuda")
-        dev.view(-1).copy_(buf, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        self._stage_ev[i] = ev
-        return dev
+        st = self._stage_np[i]
+        for k, arr in enumerate(epochs):
+            st[k * per:(k + 1) * per] = arr.reshape(-1)
+        _native.check(_native.lib().bt_memcpy_async(self._devptr[i], self._stageptr[i], 4 * n,
+                                                    torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())),
+                      "lists upload")
+        self._stage_ev[i].record()
+        self._stage_used[i] = True
+        return self._devbuf[i][:n].view(len(epochs), *epochs[0].shape)
 
     def device_lists(self, first_epoch: int, last_epoch: int) -> tuple[torch.Tensor, int]:
         """Resident [n_epochs][workers][spe*B] lists covering [first, last]; returns (tensor, base epoch)."""
         if not (self._lists_dev is not None and self._lists_dev_base <= first_epoch
                 and last_epoch < self._lists_dev_base + self._lists_dev_count):
             count = max(last_epoch - first_epoch + 1, self.EPOCH_WINDOW)
-            host = np.stack([self._lists_for_epoch(e) for e in range(first_epoch, first_epoch + count)])
-            self._lists_dev = self._upload(host)
+            self._lists_dev = self._upload([self._lists_for_epoch(e) for e in range(first_epoch, first_epoch + count)])
             self._lists_dev_base, self._lists_dev_count = first_epoch, count
         return self._lists_dev, self._lists_dev_base
 

@@ -13,8 +13,8 @@ python bench.py --no-bert > $O/bench_long.json 2> $O/bench_long.err; echo bench_
 python bench.py --gpus 2 --steps 100 --warmup 5 --no-bert --no-reducer --cpu-seconds 0 > $O/bench_n2.json 2> $O/bench_n2.err; echo n2_rc=$?
 python tools/xdev_timing.py > $O/xdev_timing.json 2>&1; python tools/xdev_stages.py 2 4 8 > $O/xdev_stages.txt 2>&1
 python tools/stage_cycles.py 8,4,20 8,4,100 > $O/stage_cycles.txt 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
-  python bench.py --steps 20 --warmup 5 --cpu-seconds 0 --no-bert > $O/ncu_list.out 2>&1; echo list_rc=$?
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches.csv \
+  python bench.py --steps 20 --warmup 5 --cpu-seconds 0 --no-bert --no-reducer > $O/ncu_list.out 2>&1; echo list_rc=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:mlp_step -s 3 -c 1 -f -o $O/prof_mlp_$tag \
   python bench.py --steps 64 --warmup 32 --cpu-seconds 0 --no-reducer --no-bert > $O/ncu_mlp.out 2>&1; echo mlp_rc=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:reduce_fast -s 2 -c 1 -f -o $O/prof_reduce_$tag \
