@@ -152,6 +152,16 @@ int bt_ffn_fwd_act(const float *h_dev, const float *b1_dev, uint64_t seed, int64
 int bt_gemm_bf16_ffn(const void *a_dev, const void *b_dev, void *c_dev, int32_t M, int32_t N, int32_t K, int32_t kind,
                      const float *bias_dev, const void *aux_dev, void *out2_dev, uint64_t seed, int64_t step,
                      int32_t est_base, int32_t Te, float p, int32_t grid, void *stream);
+/* bt_gemm_bf16_ffn with kind FFN_BWD and, when colpart_dev is set, the column sums of the bf16 output over
+ * every 32-row block written to colpart_dev[M/32][N] (fp32; each block: even rows ascending + odd rows
+ * ascending) -- the bias gradient's partials, without re-reading the output (fold: bt_colsum_fold). */
+int bt_gemm_bf16_ffn_cs(const void *a_dev, const void *b_dev, void *c_dev, int32_t M, int32_t N, int32_t K,
+                        int32_t kind, const float *bias_dev, const void *aux_dev, void *out2_dev, float *colpart_dev,
+                        uint64_t seed, int64_t step, int32_t est_base, int32_t Te, float p, int32_t grid,
+                        void *stream);
+/* out[e*out_stride + c] = sum_k part[(e*chunks + k)*C + c], k ascending (per-leaf fold of column partials) */
+int bt_colsum_fold(const float *part_dev, int32_t E, int32_t chunks, int32_t C, float *out_dev, int64_t out_stride,
+                   void *stream);
 /* partials_dev: E*64 floats of scratch; loss_dev[E] = sum 0.5*(y-target)^2 / Te; dy = (y-target)/Te */
 int bt_ffn_out(const float *y_dev, const float *b2_dev, const float *target_dev, int32_t E, int32_t Te, int32_t D,
                void *dy_dev, float *partials_dev, float *loss_dev, void *stream);

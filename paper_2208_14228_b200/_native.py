@@ -98,6 +98,9 @@ EXPORTS = {
     "bt_gemm_bf16_tn_batched": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i64, _i32, _i32, _vp]),
     "bt_gemm_bf16_ffn": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _u64, _i64, _i32, _i32,
                                    C.c_float, _i32, _vp]),
+    "bt_gemm_bf16_ffn_cs": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _u64, _i64, _i32,
+                                      _i32, C.c_float, _i32, _vp]),
+    "bt_colsum_fold": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i64, _vp]),
     "bt_ffn_data": (C.c_int, [_u64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "bt_ffn_fwd_act": (C.c_int, [_vp, _vp, _u64, _i64, _i32, _i32, _i32, _i32, C.c_float, _vp, _vp, _vp]),
     "bt_ffn_out": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),

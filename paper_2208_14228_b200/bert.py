@@ -37,6 +37,7 @@ every stage with the same bf16 rounding points (tests/test_gpu_bert.py).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -46,6 +47,9 @@ from .errors import ConfigError, NumericError
 
 _LAYER = ("Wqkv", "bqkv", "Wo", "bo", "g1", "be1", "W1", "b1", "W2", "b2", "g2", "be2")
 _MATS = ("Wqkv", "Wo", "W1", "W2")
+# b1 gradient partials from the FFN backward GEMM's epilogue (BT_BERT_CS=0: the standalone column-sum pass,
+# kept for A/B measurements)
+_FUSED_CS = os.environ.get("BT_BERT_CS", "1") != "0"
 
 
 def _init_uniform(seed: int, n: int, scale: float) -> torch.Tensor:
@@ -207,8 +211,8 @@ class BertJob:
             "tgt": torch.empty(T, D, **f32), "dy1": [torch.empty(T, D, **bf) for _ in range(2)],
             "dres": [torch.empty(T, D, **f32) for _ in range(2)],
             "dbr": torch.empty(T, D, **bf), "dHpre": torch.empty(T, F, **bf), "dctx": torch.empty(T, D, **bf),
-            "dqkv": torch.empty(T, 3 * D, **bf), "lnpart": torch.empty(n * (Te // 64) * 3 * D, **f32),
-            "colsum": torch.empty(max(n * -(-Te // 64) * max(3 * D, F),
+            "dqkv": torch.empty(T, 3 * D, **bf), "lnpart": torch.empty(n * (Te // 16) * 3 * D, **f32),
+            "colsum": torch.empty(max(n * -(-Te // 32) * max(3 * D, F),
                                       (n // self.g) * -(-(self.g * self.S * self.NP) // 64) * self.Vp), **f32),
             "msepart": torch.empty(n * 64, **f32),
         }
@@ -324,14 +328,21 @@ class BertJob:
                                             self._g(lb, l, "b2"), self.P, s))
             if capture is not None and l == 0:
                 capture.update(dg=Cb.clone(), do=ws["dbr"].clone())
-            _native.check(L.bt_gemm_bf16_ffn(ws["dbr"].data_ptr(), self._wb(l, "W2"), ws["dHpre"].data_ptr(), T, F, D,
-                                             2 | 0x100, None, w["Hpre"].data_ptr(), None, seed, step, base, Te, 0.0, 0, s),
+            # dHpre = (dbr . W2) * gelu'(h), with the b1 gradient's 32-row column partials from the epilogue
+            _native.check(L.bt_gemm_bf16_ffn_cs(ws["dbr"].data_ptr(), self._wb(l, "W2"), ws["dHpre"].data_ptr(), T, F,
+                                                D, 2 | 0x100, None, w["Hpre"].data_ptr(), None,
+                                                ws["colsum"].data_ptr() if _FUSED_CS else None, seed, step, base, Te,
+                                                0.0, 0, s),
                           "ffn backward GEMM")
             self._dx(ws["dHpre"].data_ptr(), self._wb(l, "W1"), Db.data_ptr(), T, D, F)
             self._wgrad(ws, n, ws["dbr"].data_ptr(), w["Dact"].data_ptr(), D, F, self._g(lb, l, "W2"))
             self._wgrad(ws, n, ws["dHpre"].data_ptr(), w["h1b"].data_ptr(), F, D, self._g(lb, l, "W1"))
-            _native.check(L.bt_colsum_bf16_strided(ws["dHpre"].data_ptr(), n // gg, gg * Te, F, self._g(lb, l, "b1"),
-                                                   self.P, ws["colsum"].data_ptr(), s))
+            if _FUSED_CS:
+                _native.check(L.bt_colsum_fold(ws["colsum"].data_ptr(), n // gg, gg * Te // 32, F,
+                                               self._g(lb, l, "b1"), self.P, s), "b1 gradient")
+            else:
+                _native.check(L.bt_colsum_bf16_strided(ws["dHpre"].data_ptr(), n // gg, gg * Te, F,
+                                                       self._g(lb, l, "b1"), self.P, ws["colsum"].data_ptr(), s))
             if capture is not None and l == 0:
                 capture.update(dHpre=ws["dHpre"].clone(), dh1=Db.clone())
             _native.check(L.bt_bert_ln_bwd(Db.data_ptr(), Cb.data_ptr(), w["hs1"].data_ptr(), w["st1"].data_ptr(),

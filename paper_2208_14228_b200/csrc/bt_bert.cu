@@ -46,7 +46,7 @@ constexpr int SEQ = 128, HD = 64;
 constexpr int AT_WARPS = 8, AT_THREADS = 32 * AT_WARPS;
 constexpr int LDS = HD + 8;     // bf16 row stride of Q/K/V/dO tiles (144 B: conflict-free ldmatrix)
 constexpr int LDP = SEQ + 8;    // bf16 row stride of the P / dS tiles (272 B)
-constexpr int LN_CHUNK = 64;    // rows per ln_bwd partial (fixed: part of the reduction's shape)
+constexpr int LN_CHUNK = 16;    // rows per ln_bwd partial (fixed: part of the reduction's shape)
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* r) {
@@ -424,211 +424,380 @@ struct LnArgs {
   const int64_t* step_dev;  // when set, the step is read from device memory (CUDA-graph replays)
 };
 
-__device__ __forceinline__ void ln_mask8(const LnArgs& a, int64_t step, uint64_t sd, int tl, int col, uint32_t thr,
-                                         float keep, float* m) {
+// Hidden dropout: one splitmix64 draw per 4 consecutive units (16-bit fields, field k = bits [16k, 16k+16)
+// decides unit 4q + k; dropped iff field < ceil(p * 2^16)), keyed by (EST stream, step, layer, site, token,
+// unit quad).  The forward and the backward regenerate the same masks.
+__device__ __forceinline__ void ln_mask4(uint64_t sd, uint64_t n, uint32_t thr, float keep, float* m) {
   if (thr == 0) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) m[k] = 1.f;
+    m[0] = m[1] = m[2] = m[3] = 1.f;
     return;
   }
-  const uint64_t n0 = ((((uint64_t)step * a.L + a.layer) * 2 + a.site) * a.Te + tl) * (uint64_t)a.D + col;
+  const uint64_t r = draw_raw(sd, n >> 2);
 #pragma unroll
-  for (int k = 0; k < 8; k += 2) {
-    const uint64_t r = draw_raw(sd, (n0 + k) >> 1);
-    m[k] = (uint32_t)r < thr ? 0.f : keep;
-    m[k + 1] = (uint32_t)(r >> 32) < thr ? 0.f : keep;
-  }
+  for (int k = 0; k < 4; ++k) m[k] = ((uint32_t)(r >> (16 * k)) & 0xFFFFu) < thr ? 0.f : keep;
+}
+__device__ __forceinline__ uint64_t ln_counter(const LnArgs& a, int64_t step, int tl) {  // element counter of (tl, 0)
+  return ((((uint64_t)step * a.L + a.layer) * 2 + a.site) * a.Te + tl) * (uint64_t)a.D;
 }
 __device__ __forceinline__ float warp_sum(float v) {  // butterfly: every lane ends with the same bits
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ void ld8(const float* p, float* v) {
-  const float4 x = *(const float4*)p, y = *(const float4*)(p + 4);
-  v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* v) {
-  const uint4 u = *(const uint4*)p;
-  const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Packed fp32 pairs (sm_100a FADD2 / FMUL2 / FFMA2).  ptxas contracts a packed product feeding a packed
+// addition into FFMA2 even when both are .rn, so every product that feeds an addition is written as an
+// explicit fma: the rounding is then the same wherever the expression appears (the residual recompute of
+// ln_fwd must reproduce the previous LayerNorm's output bit for bit).
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk(f2 r) {
+  float2 f;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(f.x), "=f"(f.y) : "l"(r));
+  return f;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+// 4 consecutive floats as two pairs
+struct f4p { f2 lo, hi; };
+__device__ __forceinline__ f4p ld4f(const void* p) {
+  const float4 v = *(const float4*)p;
+  return {pk(v.x, v.y), pk(v.z, v.w)};
+}
+__device__ __forceinline__ f4p ld4b(const void* p) {  // 4 bf16
+  const uint2 u = *(const uint2*)p;
+  const float2 a = __bfloat1622float2(*(const __nv_bfloat162*)&u.x), b = __bfloat1622float2(*(const __nv_bfloat162*)&u.y);
+  return {pk(a.x, a.y), pk(b.x, b.y)};
+}
+__device__ __forceinline__ void st4f(float* p, f4p v) {
+  const float2 a = upk(v.lo), b = upk(v.hi);
+  *(float4*)p = make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void st4b(__nv_bfloat16* p, f4p v) {
+  const float2 a = upk(v.lo), b = upk(v.hi);
+  *(uint2*)p = make_uint2(pack2(a.x, a.y), pack2(b.x, b.y));
+}
+// the LayerNorm output y = ((x - mean) * rstd) * gamma + beta (one rounding per product, then an fma)
+__device__ __forceinline__ f2 ln_out(f2 x, f2 mean, f2 rstd, f2 g, f2 b) { return fma2(mul2(sub2(x, mean), rstd), g, b); }
+
+// Lane columns: a row of D = 256 NC is G = 2 NC groups of 4 columns; group g of lane l is columns
+// (g >> 1) * 256 + (g & 1) * 128 + 4 l -- 16-byte fp32 / 8-byte bf16 pieces, consecutive across lanes
+// (coalesced loads, conflict-free shared-memory reads).
+template <int NC>
+__device__ __forceinline__ int lcol(int g, int lane) { return (g >> 1) * 256 + (g & 1) * 128 + 4 * lane; }
+
+// Rows stream through a two-slot shared-memory ring per warp (cp.async): each lane copies exactly the pieces
+// it later reads, so a lane waits only on its own copies (no warp synchronisation), and the next row's
+// bytes are in flight while this row computes.
+
+// ---- forward: x = resid + dropout(branch + bias); y = LN(x).  Persistent blocks (grid-stride over rows,
+// one row per warp at a time); bias, gamma, beta (and the previous LayerNorm's gamma / beta when the
+// residual is recomputed from its input rx and statistics rst) staged in shared memory once per block.
+constexpr int LNF_WARPS = 6;
+template <int NC>
+struct LnfSlot {
+  static constexpr int D = 256 * NC, R = 0, B = D * 4, ST = B + D * 2, BYTES = ST + 256;
+  static constexpr int PAR = 5 * D * 4;  // bias, gamma, beta, rg, rb
+};
+template <int NC>
+__global__ void __launch_bounds__(32 * LNF_WARPS) ln_fwd_kernel(const LnArgs a) {
+  using S = LnfSlot<NC>;
+  constexpr int D = S::D, G = 2 * NC;
+  extern __shared__ __align__(16) uint8_t lsm[];
+  float* const par = (float*)lsm;  // [5][D]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* const wr = lsm + S::PAR + (size_t)w * 2 * S::BYTES;
+  const int gw = blockIdx.x * LNF_WARPS + w, nw = gridDim.x * LNF_WARPS;
+  const bool rc = a.rx != nullptr;
+  const float* const rsrc = rc ? a.rx : a.resid;
+  auto issue = [&](int t, int slot) {  // 16-byte pieces, L2 only (.cg); the lanes read each other's pieces
+    const uint32_t sb = su32(wr + slot * S::BYTES);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float2 f = __bfloat1622float2(h[k]);
-    v[2 * k] = f.x;
-    v[2 * k + 1] = f.y;
+    for (int k = lane; k < D / 4; k += 32) cp_async16(sb + S::R + k * 16, rsrc + (size_t)t * D + 4 * k);
+#pragma unroll
+    for (int k = lane; k < D / 8; k += 32) cp_async16(sb + S::B + k * 16, a.bin + (size_t)t * D + 8 * k);
+    if (rc && lane == 0) cp_async8(sb + S::ST, a.rst + t);
+    cp_commit();
+  };
+  if (gw < a.rows) issue(gw, 0);
+  if (gw + nw < a.rows) issue(gw + nw, 1);
+  const float* srcs[5] = {a.bias, a.gamma, a.beta, a.rg, a.rb};
+#pragma unroll
+  for (int q = 0; q < 5; ++q)
+    if (q < 3 || rc)
+      for (int i = threadIdx.x * 4; i < D; i += 32 * LNF_WARPS * 4) *(float4*)(par + q * D + i) = *(const float4*)(srcs[q] + i);
+  __syncthreads();
+  const uint32_t thr = threshold16(a.p);
+  const int64_t step = cur_step(a.step, a.step_dev);
+  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
+  int n = 0;
+  for (int t = gw; t < a.rows; t += nw, ++n) {
+    if (t + nw < a.rows) cp_wait1(); else cp_wait0();
+    __syncwarp();
+    const uint8_t* const sl = wr + (n & 1) * S::BYTES;
+    const int e = t / a.Te, tl = t - e * a.Te;
+    const uint64_t sd = derive3(TAG_BERT_HDROP, a.seed, (uint64_t)(a.est_base + e));
+    const uint64_t n0 = ln_counter(a, step, tl);
+    f2 rm = 0, rs = 0;
+    if (rc) {
+      const float2 q = *(const float2*)(sl + S::ST);
+      rm = pk(q.x, q.x);
+      rs = pk(q.y, q.y);
+    }
+    f4p x[G];
+    f2 sum = pk(0.f, 0.f);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int c = lcol<NC>(g, lane);
+      f4p r = ld4f(sl + S::R + c * 4);
+      if (rc) {
+        const f4p rg = ld4f(par + 3 * D + c), rb = ld4f(par + 4 * D + c);
+        r.lo = ln_out(r.lo, rm, rs, rg.lo, rb.lo);
+        r.hi = ln_out(r.hi, rm, rs, rg.hi, rb.hi);
+      }
+      const f4p b = ld4b(sl + S::B + c * 2), bi = ld4f(par + c);
+      float m[4];
+      ln_mask4(sd, n0 + c, thr, keep, m);
+      x[g].lo = fma2(add2(b.lo, bi.lo), pk(m[0], m[1]), r.lo);
+      x[g].hi = fma2(add2(b.hi, bi.hi), pk(m[2], m[3]), r.hi);
+      sum = add2(sum, add2(x[g].lo, x[g].hi));
+    }
+    __syncwarp();  // every lane has read the slot
+    if (t + 2 * nw < a.rows) issue(t + 2 * nw, n & 1);
+    const float2 sf = upk(sum);
+    const float mean = warp_sum(sf.x + sf.y) / (float)D;
+    const f2 mm = pk(mean, mean);
+    f2 sq = pk(0.f, 0.f);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const f2 d0 = sub2(x[g].lo, mm), d1 = sub2(x[g].hi, mm);
+      sq = fma2(d0, d0, sq);
+      sq = fma2(d1, d1, sq);
+    }
+    const float2 qf = upk(sq);
+    const float rstd = 1.f / sqrtf(warp_sum(qf.x + qf.y) / (float)D + a.eps);
+    const f2 rr = pk(rstd, rstd);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int c = lcol<NC>(g, lane);
+      const f4p gm = ld4f(par + D + c), bt = ld4f(par + 2 * D + c);
+      const f4p y{ln_out(x[g].lo, mm, rr, gm.lo, bt.lo), ln_out(x[g].hi, mm, rr, gm.hi, bt.hi)};
+      st4f(a.xsum + (size_t)t * D + c, x[g]);
+      if (a.y32) st4f(a.y32 + (size_t)t * D + c, y);
+      st4b(a.yb + (size_t)t * D + c, y);
+    }
+    if (lane == 0) a.stats[t] = make_float2(mean, rstd);
   }
 }
+
+// ---- backward: dx = LN'(dy1 + dy2); branch gradient = dropout'(dx); per-chunk column partials.
+// Block = one 16-row chunk (LN_CHUNK, fixed: part of the reduction's shape), 4 warps; warp w takes rows
+// w, w+4, w+8, w+12 of the chunk in order, accumulating its dgamma / dbeta / dbias partials in registers,
+// then the 4 warps' partials are folded in warp order into part[chunk][3][D].
+constexpr int LNB_WARPS = 4;
+template <int NC, bool DY2>
+struct LnbSlot {
+  static constexpr int D = 256 * NC, Y1 = 0, Y2 = D * 2, X = Y2 + (DY2 ? D * 4 : 0), ST = X + D * 4, BYTES = ST + 256;
+};
+template <int NC, bool DY2>
+__global__ void __launch_bounds__(32 * LNB_WARPS, 3) ln_bwd_kernel(const LnArgs a) {
+  using S = LnbSlot<NC, DY2>;
+  constexpr int D = S::D, G = 2 * NC, RPW = LN_CHUNK / LNB_WARPS;
+  static_assert(2 * S::BYTES >= 3 * D * 4, "the ring holds the warp's partials at the end");
+  extern __shared__ __align__(16) uint8_t lsm[];
+  float* const gam = (float*)lsm;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* const wr = lsm + D * 4 + (size_t)w * 2 * S::BYTES;
+  const size_t row0 = (size_t)blockIdx.x * LN_CHUNK;
+  const int e = (int)(row0 / (size_t)a.Te), tl0 = (int)(row0 - (size_t)e * a.Te);
+  auto issue = [&](int i) {  // row w + 4 i of the chunk into slot i & 1 (16-byte pieces, L2 only)
+    const size_t t = row0 + w + LNB_WARPS * i;
+    const uint32_t sb = su32(wr + (i & 1) * S::BYTES);
+#pragma unroll
+    for (int k = lane; k < D / 8; k += 32) cp_async16(sb + S::Y1 + k * 16, a.bin + t * D + 8 * k);
+#pragma unroll
+    for (int k = lane; k < D / 4; k += 32) {
+      if (DY2) cp_async16(sb + S::Y2 + k * 16, a.resid + t * D + 4 * k);
+      cp_async16(sb + S::X + k * 16, a.xsum + t * D + 4 * k);
+    }
+    if (lane == 0) cp_async8(sb + S::ST, a.stats_in + t);
+    cp_commit();
+  };
+  issue(0);
+  issue(1);
+  for (int i = threadIdx.x * 4; i < D; i += 32 * LNB_WARPS * 4) *(float4*)(gam + i) = *(const float4*)(a.gamma + i);
+  __syncthreads();
+  const uint64_t sd = derive3(TAG_BERT_HDROP, a.seed, (uint64_t)(a.est_base + e));
+  const uint32_t thr = threshold16(a.p);
+  const int64_t step = cur_step(a.step, a.step_dev);
+  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
+  f4p pg[G], pb[G], pr[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) pg[g] = pb[g] = pr[g] = f4p{pk(0.f, 0.f), pk(0.f, 0.f)};
+  auto dy_x = [&](const uint8_t* sl, int c, f4p& dy, f4p& xh, f4p& gg, f2 mean, f2 rstd) {
+    dy = ld4b(sl + S::Y1 + c * 2);
+    if (DY2) {
+      const f4p d2 = ld4f(sl + S::Y2 + c * 4);
+      dy.lo = add2(dy.lo, d2.lo);
+      dy.hi = add2(dy.hi, d2.hi);
+    }
+    const f4p x = ld4f(sl + S::X + c * 4), gm = ld4f(gam + c);
+    xh.lo = mul2(sub2(x.lo, mean), rstd);
+    xh.hi = mul2(sub2(x.hi, mean), rstd);
+    gg.lo = mul2(dy.lo, gm.lo);
+    gg.hi = mul2(dy.hi, gm.hi);
+  };
+#pragma unroll 1
+  for (int i = 0; i < RPW; ++i) {
+    if (i + 1 < RPW) cp_wait1(); else cp_wait0();
+    __syncwarp();  // the lanes' copies of this row are visible to the warp
+    const uint8_t* const sl = wr + (i & 1) * S::BYTES;
+    const float2 st = *(const float2*)(sl + S::ST);
+    const f2 mean = pk(st.x, st.x), rstd = pk(st.y, st.y);
+    const int tl = tl0 + w + LNB_WARPS * i;
+    const size_t t = row0 + w + LNB_WARPS * i;
+    f2 s1 = pk(0.f, 0.f), s2 = pk(0.f, 0.f);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      f4p dy, xh, gg;
+      dy_x(sl, lcol<NC>(g, lane), dy, xh, gg, mean, rstd);
+      s1 = add2(s1, add2(gg.lo, gg.hi));
+      s2 = fma2(gg.lo, xh.lo, s2);
+      s2 = fma2(gg.hi, xh.hi, s2);
+    }
+    const float2 a1 = upk(s1), a2 = upk(s2);
+    const float m1 = warp_sum(a1.x + a1.y) / (float)D, m2 = warp_sum(a2.x + a2.y) / (float)D;
+    const f2 M1 = pk(m1, m1), NM2 = pk(-m2, -m2);
+    const uint64_t n0 = ln_counter(a, step, tl);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int c = lcol<NC>(g, lane);
+      f4p dy, xh, gg;
+      dy_x(sl, c, dy, xh, gg, mean, rstd);
+      f4p dx;  // (gg - m1 - xh m2) rstd
+      dx.lo = mul2(fma2(xh.lo, NM2, sub2(gg.lo, M1)), rstd);
+      dx.hi = mul2(fma2(xh.hi, NM2, sub2(gg.hi, M1)), rstd);
+      st4f(a.y32 + t * D + c, dx);
+      float m[4];
+      ln_mask4(sd, n0 + c, thr, keep, m);
+      const f2 mlo = pk(m[0], m[1]), mhi = pk(m[2], m[3]);
+      st4b(a.yb + t * D + c, f4p{mul2(dx.lo, mlo), mul2(dx.hi, mhi)});
+      pg[g].lo = fma2(dy.lo, xh.lo, pg[g].lo);
+      pg[g].hi = fma2(dy.hi, xh.hi, pg[g].hi);
+      pb[g].lo = add2(pb[g].lo, dy.lo);
+      pb[g].hi = add2(pb[g].hi, dy.hi);
+      pr[g].lo = fma2(dx.lo, mlo, pr[g].lo);
+      pr[g].hi = fma2(dx.hi, mhi, pr[g].hi);
+    }
+    __syncwarp();  // every lane has read the slot
+    if (i + 2 < RPW) issue(i + 2);
+  }
+  // this warp's partials into its (now idle) ring, then the warps folded in order
+  float* const pw = (float*)wr;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int c = lcol<NC>(g, lane);
+    st4f(pw + c, pg[g]);
+    st4f(pw + D + c, pb[g]);
+    st4f(pw + 2 * D + c, pr[g]);
+  }
+  __syncthreads();
+  float* const out = a.part + (size_t)blockIdx.x * 3 * D;
+  for (int i = threadIdx.x * 4; i < 3 * D; i += 32 * LNB_WARPS * 4) {
+    f4p acc = ld4f(lsm + D * 4 + i * 4);
+#pragma unroll
+    for (int ww = 1; ww < LNB_WARPS; ++ww) {
+      const f4p v = ld4f(lsm + D * 4 + (size_t)ww * 2 * S::BYTES + i * 4);
+      acc.lo = add2(acc.lo, v.lo);
+      acc.hi = add2(acc.hi, v.hi);
+    }
+    st4f(out + i, acc);
+  }
+}
+
+// per-leaf dgamma / dbeta / dbias = the chunk partials summed in a fixed association: LNF_SEGS segments of
+// consecutive chunks, each summed in order by one thread (4 columns, 16-byte loads, 8 in flight), then the
+// segments in order.  Block = (leaf, 128 of the 3D columns), threads (segment, column quad).
+constexpr int LNF_SEGS = 16;
+__global__ void __launch_bounds__(32 * LNF_SEGS) ln_fold_kernel(const float* __restrict__ part, int chunks, int D,
+                                                                float* out_g, float* out_b, float* out_r,
+                                                                int64_t est_stride) {
+  __shared__ float4 seg[LNF_SEGS][32];
+  const int e = blockIdx.y, q = threadIdx.x & 31, sg = threadIdx.x >> 5, r = blockIdx.x * 128 + 4 * q;
+  const int per = (chunks + LNF_SEGS - 1) / LNF_SEGS, k0 = sg * per, k1 = min(chunks, k0 + per);
+  f4p acc{pk(0.f, 0.f), pk(0.f, 0.f)};
+  if (r < 3 * D && k0 < k1) {
+    const size_t ld = (size_t)3 * D;
+    const float* p = part + ((size_t)e * chunks + k0) * ld + r;
+    acc = ld4f(p);
+    int k = k0 + 1;
+    for (; k + 8 <= k1; k += 8) {  // 8 loads in flight, added in order
+      float4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldg((const float4*)(p + (size_t)(k - k0 + j) * ld));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        acc.lo = add2(acc.lo, pk(v[j].x, v[j].y));
+        acc.hi = add2(acc.hi, pk(v[j].z, v[j].w));
+      }
+    }
+    for (; k < k1; ++k) {
+      const f4p v = ld4f(p + (size_t)(k - k0) * ld);
+      acc.lo = add2(acc.lo, v.lo);
+      acc.hi = add2(acc.hi, v.hi);
+    }
+  }
+  const float2 lo = upk(acc.lo), hi = upk(acc.hi);
+  seg[sg][q] = make_float4(lo.x, lo.y, hi.x, hi.y);
+  __syncthreads();
+  if (sg == 0 && r < 3 * D) {
+    f4p v = ld4f(&seg[0][q]);
+    for (int z = 1; z < LNF_SEGS; ++z)
+      if (z * per < chunks) {
+        const f4p u = ld4f(&seg[z][q]);
+        v.lo = add2(v.lo, u.lo);
+        v.hi = add2(v.hi, u.hi);
+      }
+    const int which = r / D, c = r - which * D;  // D % 128 == 0: a quad never straddles gamma / beta / bias
+    float* dst = which == 0 ? out_g : (which == 1 ? out_b : out_r);
+    st4f(dst + (size_t)e * est_stride + c, v);
+  }
+}
+
+// ------------------------------------------------------------ data / head
 __device__ __forceinline__ void st8(float* p, const float* v) {
   *(float4*)p = make_float4(v[0], v[1], v[2], v[3]);
   *(float4*)(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
 }
 __device__ __forceinline__ void st8(__nv_bfloat16* p, const float* v) {
-  uint4 u;
-  u.x = pack2(v[0], v[1]);
-  u.y = pack2(v[2], v[3]);
-  u.z = pack2(v[4], v[5]);
-  u.w = pack2(v[6], v[7]);
-  *(uint4*)p = u;
+  *(uint4*)p = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
 }
-
-// one warp per row; lane owns columns c*256 + lane*8 + [0, 8) for c < NC (D = 256*NC)
-template <int NC>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const LnArgs a) {
-  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (t >= a.rows) return;
-  const int e = t / a.Te, tl = t - e * a.Te;
-  const uint64_t sd = derive3(TAG_BERT_HDROP, a.seed, (uint64_t)(a.est_base + e));
-  const uint32_t thr = threshold32(a.p);
-  const int64_t step = cur_step(a.step, a.step_dev);
-  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
-  float x[NC][8];
-  float sum = 0.f;
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int col = c * 256 + lane * 8;
-    float r[8], b[8], bi[8], m[8];
-    if (a.rx) {
-      const float2 rs = a.rst[t];
-      float rgm[8], rbt[8];
-      ld8(a.rx + (size_t)t * a.D + col, r);
-      ld8(a.rg + col, rgm);
-      ld8(a.rb + col, rbt);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) r[k] = (r[k] - rs.x) * rs.y * rgm[k] + rbt[k];
-    } else {
-      ld8(a.resid + (size_t)t * a.D + col, r);
-    }
-    ld8(a.bin + (size_t)t * a.D + col, b);
-    ld8(a.bias + col, bi);
-    ln_mask8(a, step, sd, tl, col, thr, keep, m);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      x[c][k] = r[k] + (b[k] + bi[k]) * m[k];
-      sum += x[c][k];
-    }
-  }
-  const float mean = warp_sum(sum) / (float)a.D;
-  float sq = 0.f;
-#pragma unroll
-  for (int c = 0; c < NC; ++c)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float d = x[c][k] - mean;
-      sq += d * d;
-    }
-  const float rstd = 1.f / sqrtf(warp_sum(sq) / (float)a.D + a.eps);
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int col = c * 256 + lane * 8;
-    float gm[8], bt[8], y[8];
-    ld8(a.gamma + col, gm);
-    ld8(a.beta + col, bt);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) y[k] = (x[c][k] - mean) * rstd * gm[k] + bt[k];
-    st8(a.xsum + (size_t)t * a.D + col, x[c]);
-    if (a.y32) st8(a.y32 + (size_t)t * a.D + col, y);
-    st8(a.yb + (size_t)t * a.D + col, y);
-  }
-  if (lane == 0) a.stats[t] = make_float2(mean, rstd);
-}
-
-// block = (local EST e, 64-row chunk k); warp w handles rows w, w+8, ... of the chunk in order.
-// Each warp's column partials (dgamma, dbeta, dbias terms) accumulate in its own shared-memory rows
-// (same per-lane columns, same row order as a register accumulator would -- the registers are what
-// limited residency), then the 8 warps' partials are folded in warp order.
-template <int NC>
-__global__ void __launch_bounds__(256, 2) ln_bwd_kernel(const LnArgs a) {
-  extern __shared__ float ln_smem[];  // [8 warps][3][D]
-  const int chunks = a.Te / LN_CHUNK;
-  const int e = blockIdx.x / chunks, k = blockIdx.x - e * chunks;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t sd = derive3(TAG_BERT_HDROP, a.seed, (uint64_t)(a.est_base + e));
-  const uint32_t thr = threshold32(a.p);
-  const int64_t step = cur_step(a.step, a.step_dev);
-  const float keep = a.p < 1.f ? 1.f / (1.f - a.p) : 0.f;
-  float* const pw = ln_smem + (size_t)w * 3 * a.D;  // this warp's [3][D] partials
-  for (int i = lane * 4; i < 3 * a.D; i += 128) *(float4*)(pw + i) = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncwarp();
-  for (int rr = w; rr < LN_CHUNK; rr += 8) {
-    const int tl = k * LN_CHUNK + rr;
-    const size_t t = (size_t)e * a.Te + tl;
-    const float2 st = a.stats_in[t];
-    float dy[NC][8], xh[NC][8], gg[NC][8];
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int col = c * 256 + lane * 8;
-      float x[8], gm[8];
-      ld8(a.bin + t * a.D + col, dy[c]);
-      if (a.resid) {
-        float d2[8];
-        ld8(a.resid + t * a.D + col, d2);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) dy[c][q] += d2[q];
-      }
-      ld8(a.xsum + t * a.D + col, x);
-      ld8(a.gamma + col, gm);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        xh[c][q] = (x[q] - st.x) * st.y;
-        gg[c][q] = dy[c][q] * gm[q];
-        s1 += gg[c][q];
-        s2 += gg[c][q] * xh[c][q];
-      }
-    }
-    const float m1 = warp_sum(s1) / (float)a.D, m2 = warp_sum(s2) / (float)a.D;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int col = c * 256 + lane * 8;
-      float dx[8], m[8], pg[8], pb[8], pr[8];
-      ln_mask8(a, step, sd, tl, col, thr, keep, m);
-      ld8(pw + col, pg);
-      ld8(pw + a.D + col, pb);
-      ld8(pw + 2 * a.D + col, pr);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        dx[q] = (gg[c][q] - m1 - xh[c][q] * m2) * st.y;
-        pg[q] += dy[c][q] * xh[c][q];
-        pb[q] += dy[c][q];
-      }
-      st8(a.y32 + t * a.D + col, dx);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        dx[q] *= m[q];
-        pr[q] += dx[q];
-      }
-      st8(a.yb + t * a.D + col, dx);
-      st8(pw + col, pg);
-      st8(pw + a.D + col, pb);
-      st8(pw + 2 * a.D + col, pr);
-    }
-  }
-  __syncthreads();
-  float* out = a.part + (size_t)blockIdx.x * 3 * a.D;
-  for (int i = threadIdx.x; i < 3 * a.D; i += 256) {
-    float acc = ln_smem[i];
-    for (int ww = 1; ww < 8; ++ww) acc += ln_smem[(size_t)ww * 3 * a.D + i];
-    out[i] = acc;
-  }
-}
-
-// per-EST dgamma / dbeta / dbias = chunk partials summed in chunk order; written into the EST's
-// gradient slot (out_g/out_b/out_r + e * est_stride)
-__global__ void ln_fold_kernel(const float* __restrict__ part, int E, int chunks, int D, float* out_g, float* out_b,
-                               float* out_r, int64_t est_stride) {
-  const int64_t n = (int64_t)E * 3 * D;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int e = (int)(i / (3 * D)), r = (int)(i - (int64_t)e * 3 * D);
-    const float* p = part + (size_t)e * chunks * 3 * D + r;
-    float acc = p[0];
-    for (int k = 1; k < chunks; ++k) acc += p[(size_t)k * 3 * D];
-    const int which = r / D, c = r - which * D;
-    float* dst = which == 0 ? out_g : (which == 1 ? out_b : out_r);
-    dst[(size_t)e * est_stride + c] = acc;
-  }
-}
-
-// ------------------------------------------------------------ data / head
 // X[t][d] = bf16(U[-1,1)) from (TAG_BERT_X, seed, EST) at counter (step*Te + tl)*D + d (bf16-exact, so the
 // fp32 residual copy and the GEMM operand agree); target 0.5*U[-1,1)
 __global__ void __launch_bounds__(256) data_kernel(uint64_t seed, int64_t step_h, const int64_t* step_dev, int est_base,
@@ -779,20 +948,37 @@ int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out,
   return ok_or_cuda_b();
 }
 
+template <class K>
+static bool smem_attr(K kern, int bytes) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess;
+}
 template <int NC>
-static int ln_launch_nc(int backward, const bert::LnArgs& a, int E, cudaStream_t s) {
+static int ln_launch_nc(int backward, const bert::LnArgs& a, cudaStream_t s) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   if (!backward) {
-    bert::ln_fwd_kernel<NC><<<(a.rows + 7) / 8, 256, 0, s>>>(a);
-  } else {
-    const int smem = 8 * 3 * a.D * (int)sizeof(float);
+    constexpr int smem = bert::LnfSlot<NC>::PAR + 2 * bert::LNF_WARPS * bert::LnfSlot<NC>::BYTES;
     static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(bert::ln_bwd_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               8 * 3 * 256 * NC * (int)sizeof(float)) != cudaSuccess)
-        return ERR_CUDA;
-      attr = true;
-    }
-    bert::ln_bwd_kernel<NC><<<E * (a.Te / bert::LN_CHUNK), 256, smem, s>>>(a);
+    if (!attr && !(attr = smem_attr(bert::ln_fwd_kernel<NC>, smem))) return ERR_CUDA;
+    const int warps = (a.rows + 7) / 8;  // ~8 rows per warp at most, as many blocks as fit resident
+    const int per_sm = (227 * 1024) / (smem + 1024);
+    int grid = (warps + bert::LNF_WARPS - 1) / bert::LNF_WARPS;
+    if (grid > per_sm * sms) grid = per_sm * sms;
+    bert::ln_fwd_kernel<NC><<<grid, 32 * bert::LNF_WARPS, smem, s>>>(a);
+  } else if (a.resid) {
+    constexpr int smem = 256 * NC * 4 + 2 * bert::LNB_WARPS * bert::LnbSlot<NC, true>::BYTES;
+    static bool attr = false;
+    if (!attr && !(attr = smem_attr(bert::ln_bwd_kernel<NC, true>, smem))) return ERR_CUDA;
+    bert::ln_bwd_kernel<NC, true><<<a.rows / bert::LN_CHUNK, 32 * bert::LNB_WARPS, smem, s>>>(a);
+  } else {
+    constexpr int smem = 256 * NC * 4 + 2 * bert::LNB_WARPS * bert::LnbSlot<NC, false>::BYTES;
+    static bool attr = false;
+    if (!attr && !(attr = smem_attr(bert::ln_bwd_kernel<NC, false>, smem))) return ERR_CUDA;
+    bert::ln_bwd_kernel<NC, false><<<a.rows / bert::LN_CHUNK, 32 * bert::LNB_WARPS, smem, s>>>(a);
   }
   return ok_or_cuda_b();
 }
@@ -834,18 +1020,19 @@ int bert_ln_launch(int backward, const float* in1, const void* in2, const float*
   a.p = p;
   a.eps = eps;
   switch (D / 256) {
-    case 1: return ln_launch_nc<1>(backward, a, E, s);
-    case 2: return ln_launch_nc<2>(backward, a, E, s);
-    case 3: return ln_launch_nc<3>(backward, a, E, s);
-    default: return ln_launch_nc<4>(backward, a, E, s);
+    case 1: return ln_launch_nc<1>(backward, a, s);
+    case 2: return ln_launch_nc<2>(backward, a, s);
+    case 3: return ln_launch_nc<3>(backward, a, s);
+    default: return ln_launch_nc<4>(backward, a, s);
   }
 }
 
 int bert_ln_fold_launch(const float* part, int E, int Te, int D, float* dg, float* db, float* dr, int64_t est_stride,
                         cudaStream_t s) {
-  const int64_t n = (int64_t)E * 3 * D;
-  const int grid = (int)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8);
-  bert::ln_fold_kernel<<<grid, 256, 0, s>>>(part, E, Te / bert::LN_CHUNK, D, dg, db, dr, est_stride);
+  if (Te % bert::LN_CHUNK) return ERR_INPUT;
+  if (est_stride % 4 || ((uintptr_t)dg | (uintptr_t)db | (uintptr_t)dr) & 15) return ERR_INPUT;  // 16-byte stores
+  bert::ln_fold_kernel<<<dim3((3 * D + 127) / 128, E), 32 * bert::LNF_SEGS, 0, s>>>(part, Te / bert::LN_CHUNK, D, dg,
+                                                                                   db, dr, est_stride);
   return ok_or_cuda_b();
 }
 

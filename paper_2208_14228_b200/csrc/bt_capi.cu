@@ -52,6 +52,7 @@ int ffn_bwd_act_launch(const float* dD, const void* Hpre, uint64_t seed, int64_t
 int colsum_bf16_launch(const void* in, int E, int R, int C, float* out, float* scratch, cudaStream_t s);
 int transpose_launch(const void* in, int in_f32, int E, int R, int C, void* out, cudaStream_t s);
 int cast_f32_bf16_launch(const float* in, int64_t n, void* out, cudaStream_t s);
+int colsum_fold_launch(const float* part, int E, int chunks, int C, float* out, int64_t ostride, cudaStream_t s);
 int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, int64_t ostride, float* scratch,
                                cudaStream_t s);
 int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out, int n_seq, int Dm, int H,
@@ -482,6 +483,13 @@ int bt_gemm_bf16_tn(const void* a_dev, const void* b_dev, void* c_dev, int32_t M
 int bt_gemm_bf16_ffn(const void* a_dev, const void* b_dev, void* c_dev, int32_t M, int32_t N, int32_t K, int32_t kind,
                      const float* bias_dev, const void* aux_dev, void* out2_dev, uint64_t seed, int64_t step,
                      int32_t est_base, int32_t Te, float p, int32_t grid, void* stream) {
+  return bt_gemm_bf16_ffn_cs(a_dev, b_dev, c_dev, M, N, K, kind, bias_dev, aux_dev, out2_dev, nullptr, seed, step,
+                             est_base, Te, p, grid, stream);
+}
+int bt_gemm_bf16_ffn_cs(const void* a_dev, const void* b_dev, void* c_dev, int32_t M, int32_t N, int32_t K,
+                        int32_t kind, const float* bias_dev, const void* aux_dev, void* out2_dev, float* colpart_dev,
+                        uint64_t seed, int64_t step, int32_t est_base, int32_t Te, float p, int32_t grid,
+                        void* stream) {
   if (!a_dev || !b_dev || !c_dev) return fail(bt::ERR_INPUT, "null pointer");
   if (M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 128 || K % 64)
     return fail(bt::ERR_INPUT, "gemm shape %dx%dx%d: need M %% 128 == 0, N %% 128 == 0, K %% 64 == 0", M, N, K);
@@ -503,6 +511,9 @@ int bt_gemm_bf16_ffn(const void* a_dev, const void* b_dev, void* c_dev, int32_t 
   epi.est_base = est_base;
   epi.Te = Te;
   epi.p = p;
+  if (colpart_dev && kind != bt::EPI_FFN_BWD) return fail(bt::ERR_INPUT, "column partials are an FFN_BWD output");
+  if ((uintptr_t)colpart_dev & 7) return fail(bt::ERR_INPUT, "column partials must be 8-byte aligned");
+  epi.colpart = colpart_dev;
   return done(bt::gemm_bf16_launch_any(a_dev, b_dev, c_dev, 1, M, N, K, (int64_t)M * K, (int64_t)N * K,
                                        (int64_t)M * N, 1, grid, epi, b_mn ? 2 : 0, STREAM(stream)),
               "bt_gemm_bf16_ffn");
@@ -896,6 +907,12 @@ int bt_bert_mse(const float* y_dev, const float* target_dev, int32_t E, int32_t 
   if (!y_dev || !target_dev || !dy_dev || !partials_dev || !loss_dev) return fail(bt::ERR_INPUT, "null pointer");
   return done(bt::bert_mse_launch(y_dev, target_dev, E, Te, D, dy_dev, partials_dev, loss_dev, STREAM(stream)),
               "bt_bert_mse");
+}
+int bt_colsum_fold(const float* part_dev, int32_t E, int32_t chunks, int32_t C, float* out_dev, int64_t out_stride,
+                   void* stream) {
+  if (!part_dev || !out_dev) return fail(bt::ERR_INPUT, "null pointer");
+  if (E < 1 || chunks < 1 || C < 1 || out_stride < C) return fail(bt::ERR_INPUT, "colsum fold shape");
+  return done(bt::colsum_fold_launch(part_dev, E, chunks, C, out_dev, out_stride, STREAM(stream)), "bt_colsum_fold");
 }
 int bt_colsum_bf16_strided(const void* in_dev, int32_t E, int32_t R, int32_t C, float* out_dev, int64_t out_stride,
                            float* scratch_dev, void* stream) {

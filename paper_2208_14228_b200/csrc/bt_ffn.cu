@@ -290,6 +290,10 @@ int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, 
   if (own) cudaFreeAsync(part, s);
   return ok_or_cuda();
 }
+int colsum_fold_launch(const float* part, int E, int chunks, int C, float* out, int64_t ostride, cudaStream_t s) {
+  ffn::colsum_final_kernel<<<grid_for((int64_t)E * C), 256, 0, s>>>(part, E, chunks, C, out, ostride);
+  return ok_or_cuda();
+}
 int transpose_launch(const void* in, int in_f32, int E, int R, int C, void* out, cudaStream_t s) {
   if (R % 2 || C % 2) return ERR_INPUT;
   const dim3 grid((C + 63) / 64, (R + 63) / 64, E);

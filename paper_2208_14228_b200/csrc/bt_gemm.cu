@@ -114,6 +114,25 @@ __device__ __forceinline__ void stage_bf16(uint8_t* st, const float* f, int lane
   }
 }
 
+// Column sums of a staged 32 x 32 bf16 box (SW64 layout, as the TMA store reads it): lane (h, cp) sums
+// columns 2cp, 2cp+1 over the rows of parity h in ascending order (lanes 0-15 read one even row, lanes
+// 16-31 the next odd row: the two 64-byte rows fill all 32 banks), then even + odd -- a fixed association
+// of exactly the stored bf16 values.  out: 32 fp32 partials of this 32-row block.
+__device__ __forceinline__ void colsum_box32(const uint8_t* st, int lane, float* out) {
+  const int h = lane >> 4, cp = lane & 15, q = cp >> 2;
+  ffn::f32x2 acc = ffn::pk2(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = 2 * i + h;
+    const uint32_t w = *(const uint32_t*)(st + r * 64 + ((q ^ ((r >> 1) & 3)) << 4) + (cp & 3) * 4);
+    const float2 f = __bfloat1622float2(*(const __nv_bfloat162*)&w);
+    acc = ffn::add2(acc, ffn::pk2(f.x, f.y));
+  }
+  const float2 a = ffn::upk2(acc);
+  const float ox = __shfl_xor_sync(0xffffffffu, a.x, 16), oy = __shfl_xor_sync(0xffffffffu, a.y, 16);
+  if (h == 0) *(float2*)(out + 2 * cp) = make_float2(__fadd_rn(a.x, ox), __fadd_rn(a.y, oy));
+}
+
 // One epilogue chunk: 32 consecutive fp32 accumulators of row `row` (lane = row - row0),
 // columns [col, col+32) -- plain (fp32 / bf16), + bias, or an FFN element op fused in --
 // staged in shared memory and stored by TMA at (col, row0, batch entry z).
@@ -132,18 +151,21 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
 #pragma unroll
     for (int q8 = 0; q8 < 4; ++q8) {
       const float4 b0 = *(const float4*)(epi.bias + col + 8 * q8), b1 = *(const float4*)(epi.bias + col + 8 * q8 + 4);
-      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const ffn::f32x2 bb[4] = {ffn::pk2(b0.x, b0.y), ffn::pk2(b0.z, b0.w), ffn::pk2(b1.x, b1.y),
+                                ffn::pk2(b1.z, b1.w)};
       uint32_t wc[4], wo[4];
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
+      for (int h = 0; h < 4; ++h) {  // packed pairs: the same operations, bit for bit, at half the issue count
         const int q = 8 * q8 + 2 * h;
-        float m0, m1, g0, g1, d0, d1;
-        ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
-        ffn::gelu_and_grad(__uint_as_float(v[q]) + bb[2 * h], &g0, &d0);
-        ffn::gelu_and_grad(__uint_as_float(v[q + 1]) + bb[2 * h + 1], &g1, &d1);
-        const __nv_bfloat162 c2 = __floats2bfloat162_rn(d0, d1), o2 = __floats2bfloat162_rn(g0 * m0, g1 * m1);
-        wc[h] = *(const uint32_t*)&c2;
-        wo[h] = *(const uint32_t*)&o2;
+        ffn::f32x2 g, d;
+        ffn::gelu_and_grad2(ffn::add2(ffn::pk2(__uint_as_float(v[q]), __uint_as_float(v[q + 1])), bb[h]), &g, &d);
+        if (epi.p > 0.f) {
+          float m0, m1;
+          ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
+          g = ffn::mul2(g, ffn::pk2(m0, m1));
+        }
+        wc[h] = ffn::bf16x2_bits(d);
+        wo[h] = ffn::bf16x2_bits(g);
       }
       const int off = lane * 64 + ((q8 ^ ((lane >> 1) & 3)) << 4);  // SW64 box layout
       *(uint4*)(st + off) = make_uint4(wc[0], wc[1], wc[2], wc[3]);
@@ -184,11 +206,13 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
       for (int k = 0; k < 4; ++k) {
         const float2 gp = __bfloat1622float2(h2[k]);
         const int q = 8 * q8 + 2 * k;
-        float m0, m1;
-        ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
-        const __nv_bfloat162 o2 = __floats2bfloat162_rn(__uint_as_float(v[q]) * m0 * gp.x,
-                                                        __uint_as_float(v[q + 1]) * m1 * gp.y);
-        w[k] = *(const uint32_t*)&o2;
+        ffn::f32x2 a = ffn::pk2(__uint_as_float(v[q]), __uint_as_float(v[q + 1]));
+        if (epi.p > 0.f) {  // (acc * m) * gelu'; without dropout m = 1 and acc * 1 = acc exactly
+          float m0, m1;
+          ffn::drop_scale2(sd, epi.step, epi.Te, N, tl, col + q, epi.p, keep, &m0, &m1);
+          a = ffn::mul2(a, ffn::pk2(m0, m1));
+        }
+        w[k] = ffn::bf16x2_bits(ffn::mul2(a, ffn::pk2(gp.x, gp.y)));
       }
       *(uint4*)(st + off) = make_uint4(w[0], w[1], w[2], w[3]);
     }
@@ -198,6 +222,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
       tma_store_3d(mc, su32(st), col, row0, z);
       bulk_commit();
     }
+    if (epi.colpart) colsum_box32(st, lane, epi.colpart + (size_t)(row0 >> 5) * N + col);
     return;
   }
   float f[32];
@@ -1082,8 +1107,11 @@ static int launch_any(const GemmShape& g, int out_bf16, int grid, cudaStream_t s
   constexpr int SP = gemm::EPI_WARPS == 8 ? 5 : 3, S256 = gemm::EPI_WARPS == 8 ? 3 : 2,
                 S64 = gemm::EPI_WARPS == 8 ? 6 : 4, S128 = gemm::EPI_WARPS == 8 ? 5 : 3;
   if (g.M % 256 == 0 && g.N % 256 == 0 && gemm_variant() != 1) {
-    if (g.epi.kind == EPI_FFN_FWD || g.epi.kind == EPI_FFN_BWD)  // ALU-heavy epilogues: 16 epilogue warps
+    if (g.epi.kind == EPI_FFN_FWD || g.epi.kind == EPI_FFN_BWD) {  // ALU-heavy epilogues: 16 epilogue warps
+      static const int ew = getenv("BT_FFN_EW") ? atoi(getenv("BT_FFN_EW")) : 16;  // A/B measurements
+      if (ew == 8) return launch_gemm_pair<SP, true, MN, gemm::EPI_WARPS, AIM>(g, grid, s);
       return launch_gemm_pair<3, true, MN, 16, AIM>(g, grid, s);
+    }
     return out_bf16 ? launch_gemm_pair<SP, true, MN, gemm::EPI_WARPS, AIM>(g, grid, s)
                     : launch_gemm_pair<SP, false, MN, gemm::EPI_WARPS, AIM>(g, grid, s);
   }

@@ -59,11 +59,11 @@ def _draws(s0, n):
         return _mix64(np.uint64(s0) + (n.astype(np.uint64) + np.uint64(1)) * GAMMA)
 
 
-def _keep(raw_pairs, j, p):
-    """scale per unit from the pair draw: unit j uses the low (j even) / high (j odd) 32 bits"""
-    half = np.where(j % 2 == 0, raw_pairs & np.uint64(0xFFFFFFFF), raw_pairs >> np.uint64(32))
-    thr = np.uint64(math.ceil(p * 2 ** 32))
-    return np.where(half < thr, 0.0, 1.0 / (1.0 - p))
+def _keep(raw_quads, j, p):
+    """scale per unit from the quad draw: unit j uses the 16-bit field j % 4 (bits [16 (j % 4), +16))"""
+    field = (raw_quads >> (np.uint64(16) * (j % 4).astype(np.uint64))) & np.uint64(0xFFFF)
+    thr = np.uint64(math.ceil(p * 2 ** 16))
+    return np.where(field < thr, 0.0, 1.0 / (1.0 - p))
 
 
 @pytest.fixture(scope="module")
@@ -164,7 +164,7 @@ def test_layer0_stages_match_float64_restatement(bert, cfg):
             s0 = host_derive_stream(TAG_HDROP, seed, e)
             tl = np.arange(Te)[:, None]
             j = np.arange(D)[None, :]
-            n0 = ((((step * NL + l) * 2 + site) * Te + tl) * D + j) >> 1
+            n0 = ((((step * NL + l) * 2 + site) * Te + tl) * D + j) >> 2
             sc[e * Te:(e + 1) * Te] = _keep(_draws(s0, n0), j, ph)
         return torch.from_numpy(sc)
 

@@ -6,6 +6,7 @@ bit-identical across repeats and across grid sizes (1 CTA ... one per SM),
 which is the property the elastic step needs from its model kernels.
 """
 
+import numpy as np
 import pytest
 import torch
 
@@ -179,3 +180,43 @@ def test_ffn_backward_epilogue_with_b_mn_major():
                                                      aux.data_ptr(), None, 42, 3, 0, 128, 0.1, 0, stream()))
         outs.append(c)
     assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+
+
+@pytest.mark.parametrize("variant", ["0", "1"])
+def test_ffn_backward_epilogue_column_partials(monkeypatch, variant):
+    """bt_gemm_bf16_ffn_cs: the FFN backward GEMM's epilogue also writes the column sums of its bf16 output
+    over every 32-row block (even rows ascending + odd rows ascending, fp32) -- bit-exact against that
+    association restated in numpy on the stored output, on the CTA-pair and the 1-CTA kernels; the per-leaf
+    fold (bt_colsum_fold) sums the blocks in order, and the output itself is the plain FFN_BWD output."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    monkeypatch.setenv("BT_GEMM_VARIANT", variant)
+    T, F, D = 1024, 768, 256
+    g = torch.Generator(device="cuda").manual_seed(9)
+    dy = (torch.randn(T, D, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    w2 = (torch.randn(D, F, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    aux = (torch.randn(T, F, device="cuda", generator=g)).to(torch.bfloat16)
+    L = _native.lib()
+    c = torch.empty(T, F, dtype=torch.bfloat16, device="cuda")
+    c_ref = torch.empty_like(c)
+    part = torch.full((T // 32, F), float("nan"), device="cuda")
+    _native.check(L.bt_gemm_bf16_ffn_cs(dy.data_ptr(), w2.data_ptr(), c.data_ptr(), T, F, D, 2 | 0x100, None,
+                                        aux.data_ptr(), None, part.data_ptr(), 42, 3, 0, 256, 0.1, 0, stream()))
+    _native.check(L.bt_gemm_bf16_ffn(dy.data_ptr(), w2.data_ptr(), c_ref.data_ptr(), T, F, D, 2 | 0x100, None,
+                                     aux.data_ptr(), None, 42, 3, 0, 256, 0.1, 0, stream()))
+    assert torch.equal(c.view(torch.int16), c_ref.view(torch.int16))
+    x = c.float().cpu().numpy().reshape(T // 32, 16, 2, F)  # [block][i][parity][col]
+    even, odd = np.zeros((T // 32, F), np.float32), np.zeros((T // 32, F), np.float32)
+    for i in range(16):
+        even = even + x[:, i, 0]
+        odd = odd + x[:, i, 1]
+    want = even + odd
+    assert np.array_equal(part.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    leaves, per = 4, T // 32 // 4
+    out = torch.zeros(leaves, F + 8, device="cuda")
+    _native.check(L.bt_colsum_fold(part.data_ptr(), leaves, per, F, out.data_ptr(), F + 8, stream()))
+    acc = want.reshape(leaves, per, F)[:, 0]
+    for k in range(1, per):
+        acc = acc + want.reshape(leaves, per, F)[:, k]
+    assert np.array_equal(out[:, :F].cpu().numpy().view(np.uint32), acc.view(np.uint32))

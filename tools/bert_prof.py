@@ -2,6 +2,7 @@
 
     python tools/bert_prof.py [ests] [layers] [seqs]
 """
+import os
 import sys
 from collections import defaultdict
 from pathlib import Path
@@ -19,8 +20,10 @@ job = BertJob(ests=E, seqs=S, layers=NL, est_group=4 if E % 4 == 0 else 1, fanin
 for _ in range(2):
     job.step()
 torch.cuda.synchronize()
+NS = int(os.environ.get("BT_PROF_STEPS", "1"))  # steps profiled (per-step averages printed)
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    job.step()
+    for _ in range(NS):
+        job.step()
     torch.cuda.synchronize()
 tot = defaultdict(float)
 cnt = defaultdict(int)
@@ -34,9 +37,9 @@ for ev in prof.events():
             if key in name:
                 name = key
                 break
-        tot[name] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
+        tot[name] += (ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total) / NS
         cnt[name] += 1
 all_us = sum(tot.values())
 for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
-    print(f"{v / 1e3:9.3f} ms  {100 * v / all_us:5.1f}%  x{cnt[k]:4d}  {k[:90]}")
+    print(f"{v / 1e3:9.3f} ms  {100 * v / all_us:5.1f}%  x{cnt[k] // NS:4d}  {k[:90]}")
 print(f"total kernel time {all_us / 1e3:.3f} ms")
