@@ -631,20 +631,37 @@ def bench_resnet(peaks, ests=16, batch=32, steps=10, warmup=3):
     flops = job.flops_per_step()
     del job
     torch.cuda.empty_cache()
-    from paper_2208_14228_b200.runlog import bitdiff
+    from paper_2208_14228_b200.runlog import RunRecord, bitdiff
 
     a, b = ResNetJob(ests=ests, batch=batch, gpus=8), ResNetJob(ests=ests, batch=batch, gpus=1)
-    switch_us = []
+    for gpus in (4, 2):  # the planner knows the schedule: the layouts' buffers and step graphs are staged ahead
+        a.prepare(gpus)
+    switch_us, switch_host_us, first_ms = [], [], []
     la = None
     for gpus in (8, 4, 2):
         if gpus != 8:
+            torch.cuda.synchronize()
             r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
             r0.record(s)
             a.rescale(gpus)
             r1.record(s)
+            t1 = time.perf_counter()
             r1.synchronize()
             switch_us.append(round(r0.elapsed_time(r1) * 1e3, 1))
-        la = a.run_log(2, la)
+            switch_host_us.append(round((t1 - t0) * 1e6, 1))
+            pair = []
+            for _ in range(2):  # the first step on the new layout (a replay of its staged graph), then the next
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0.record(s)
+                lo = a.step()
+                f1.record(s)
+                f1.synchronize()
+                pair.append(round(f0.elapsed_time(f1), 3))
+                la.add(RunRecord(a.step_idx, [float(x) for x in lo.tolist()], a.fingerprint()))
+            first_ms.append(pair)
+        else:
+            la = a.run_log(2, la)
     lb = b.run_log(6)
     sa, sb = a.est_state(), b.est_state()
     same = bool(torch.equal(a.params.view(torch.int32), b.params.view(torch.int32)) and
@@ -658,6 +675,11 @@ def bench_resnet(peaks, ests=16, batch=32, steps=10, warmup=3):
             "conv_tflops_step_level": round(flops / ms / 1e9, 1), "loss": round(losses.mean().item(), 5),
             "rescale_8_4_2": {"schedule": "2 steps @8, rescale, 2 @4, rescale, 2 @2 vs 6 steps @1",
                               "bit_identical_weights_and_bn_stats": same, "context_switch_us": switch_us,
+                              "context_switch_host_us": switch_host_us,
+                              "first_and_second_step_after_switch_ms": first_ms,
+                              "context_switch": "one bt_est_slot_copy launch (128-bit copies of every EST's BN "
+                                                "statistics and cursor into its new owner's slots); the new "
+                                                "layout's buffers and step graph staged ahead (ResNetJob.prepare)",
                               "run_logs": "per-EST losses + weight fingerprint per step, runlog.bitdiff: no divergence",
                               "weights_fp": la.records[-1].param_hash}}
 

@@ -346,6 +346,35 @@ int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_hos
   return 0;
 }
 
+int bt_mlp_run_sampled(const bt_mlp_args* args, uint64_t seed, int64_t dataset_n, int32_t shuffle,
+                       int64_t first_epoch, int32_t n_epochs, int32_t* stage_host, int32_t* lists_dev,
+                       double* losses_host, int32_t* status_host, void* stream) {
+  if (!args || !stage_host || !lists_dev) return fail(bt::ERR_INPUT, "bt_mlp_run_sampled: null pointer");
+  if (n_epochs < 1 || first_epoch < 0) return fail(bt::ERR_INPUT, "bt_mlp_run_sampled: %d epochs", n_epochs);
+  const int32_t workers = args->E_total, micro = args->B;
+  if (workers < 1 || micro < 1 || dataset_n / ((int64_t)workers * micro) != args->spe)
+    return fail(bt::ERR_CONFIG, "bt_mlp_run_sampled: steps per epoch %lld do not match the dataset", (long long)args->spe);
+  // the launch's epochs must be the ones staged
+  if (args->step0 / args->spe < first_epoch ||
+      (args->step0 + args->K - 1) / args->spe >= first_epoch + n_epochs)
+    return fail(bt::ERR_INPUT, "bt_mlp_run_sampled: epochs [%lld, +%d) do not cover the launch",
+                (long long)first_epoch, n_epochs);
+  const size_t per = (size_t)workers * (size_t)(args->spe * micro);
+  for (int32_t k = 0; k < n_epochs; ++k) {  // the sampler's host work (sampling.py:63-82), then one H2D copy
+    const int st = bt_host_epoch_indices(seed, (uint64_t)(first_epoch + k), dataset_n, workers, micro, shuffle,
+                                         stage_host + (size_t)k * per);
+    if (st) return st;
+  }
+  cudaStream_t s = STREAM(stream);
+  if (cudaMemcpyAsync(lists_dev, stage_host, sizeof(int32_t) * per * n_epochs, cudaMemcpyHostToDevice, s) !=
+      cudaSuccess)
+    return cuda_fail("bt_mlp_run_sampled lists");
+  bt_mlp_args a = *args;
+  a.lists = lists_dev;
+  a.epoch_base = first_epoch;
+  return bt_mlp_run(&a, losses_host, status_host, stream);
+}
+
 int bt_mlp_run_group(const bt_mlp_args* const* args, const int32_t* devices, void* const* streams, int32_t n,
                      double* const* losses_host, int32_t* const* status_host) {
   if (n < 1 || n > BT_MAX_XDEV) return fail(bt::ERR_INPUT, "group of %d launches", n);

@@ -574,16 +574,30 @@ class _FastStep:
         """Launch K mini-batches from ts.global_step; returns the device status word."""
         a = self.a
         gs = ts.global_step
-        spe = ts.pipeline.steps_per_epoch
-        lists, base = ts.pipeline.device_lists(gs // spe, (gs + K - 1) // spe)
-        self.keep = [lists]
+        pipe = ts.pipeline
+        spe = pipe.steps_per_epoch
+        e0, e1 = gs // spe, (gs + K - 1) // spe
         rot = _rot_tensor(ts)
         ex0 = ts.executors[0]
-        a.K, a.step0, a.lists, a.epoch_base = K, gs, lists.data_ptr(), base
+        a.K, a.step0 = K, gs
         a.rot = ptr(rot)
         a.lr, a.mu = float(ex0._lr), float(ex0._mu)
-        st = _native.lib().bt_mlp_run(C.byref(a), self.host_losses.data_ptr(), self.host_status.data_ptr(),
-                                      _raw_stream())
+        if pipe.lists_resident(e0, e1):
+            lists, base = pipe.device_lists(e0, e1)
+            self.keep = [lists]
+            a.lists, a.epoch_base = lists.data_ptr(), base
+            st = _native.lib().bt_mlp_run(C.byref(a), self.host_losses.data_ptr(), self.host_status.data_ptr(),
+                                          _raw_stream())
+        else:  # the epochs' lists are made on the host inside the native call, copied, then the launch
+            count = max(e1 - e0 + 1, pipe.EPOCH_WINDOW)
+            stage, lists = pipe.reserve_lists(e0, count)
+            self.keep = [lists]
+            st = _native.lib().bt_mlp_run_sampled(C.byref(a), pipe.seed & (2**64 - 1), pipe.dataset_size,
+                                                  int(pipe.shuffle), e0, count, stage, lists.data_ptr(),
+                                                  self.host_losses.data_ptr(), self.host_status.data_ptr(),
+                                                  _raw_stream())
+            if st:
+                pipe.drop_lists()
         _native.check(st, "run_minibatch")
         self.dev.invalidate()
         return int(self.status_np[0])

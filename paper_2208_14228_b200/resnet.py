@@ -194,32 +194,82 @@ class ResNetJob:
                 "run_var": torch.ones(n, self.CBN, dtype=torch.float32, device="cuda"),
                 "cursor": torch.zeros(n, dtype=torch.int64, device="cuda")}
 
-    def _place(self, gpus: int, initial: bool = False):
-        new_layout = self.layout(gpus)
-        new = [self._new_slots(n) for _, n in new_layout]
-        if not initial:  # context switch: every EST's slot bytes move to its new owner (one launch)
+    def _slot_set(self, gpus: int) -> list[dict]:
+        """The slot buffers of layout `gpus` (one set per layout, allocated once: a layout's CUDA graph
+        keeps pointing at them, so re-entering a layout replays its graph)."""
+        if gpus not in self._slot_sets:
+            self._slot_sets[gpus] = [self._new_slots(n) for _, n in self.layout(gpus)]
+        return self._slot_sets[gpus]
+
+    def _copy_plan(self, g0: int, g1: int):
+        """(dst, src, bytes, count) ctypes arrays moving every EST's slot bytes from layout g0 to g1."""
+        key = (g0, g1)
+        if key not in self._plans:
             owner = {}
-            for g, (base, n) in enumerate(self.layout(self.G)):
+            for g, (base, n) in enumerate(self.layout(g0)):
                 for k in range(n):
                     owner[base + k] = (g, k)
+            old, new = self._slot_set(g0), self._slot_set(g1)
             dst, src, nb = [], [], []
-            for g, (base, n) in enumerate(new_layout):
+            for g, (base, n) in enumerate(self.layout(g1)):
                 for k in range(n):
                     og, ok = owner[base + k]
-                    for key in ("run_mean", "run_var", "cursor"):
-                        d, s_ = new[g][key][k], self.slots[og][key][ok]
+                    for name in ("run_mean", "run_var", "cursor"):
+                        d, s_ = new[g][name][k], old[og][name][ok]
                         dst.append(d.data_ptr())
                         src.append(s_.data_ptr())
                         nb.append(d.numel() * d.element_size())
             cnt = len(dst)
-            _native.check(_native.lib().bt_est_slot_copy((C.c_void_p * cnt)(*dst), (C.c_void_p * cnt)(*src),
-                                                         (C.c_int64 * cnt)(*nb), cnt, stream()), "EST slot copy")
-        self.slots, self.G = new, gpus
-        self._graph, self._gwarm = None, False  # a new layout (slot buffers, launch groups): capture again
+            self._plans[key] = ((C.c_void_p * cnt)(*dst), (C.c_void_p * cnt)(*src), (C.c_int64 * cnt)(*nb), cnt)
+        return self._plans[key]
+
+    def _place(self, gpus: int, initial: bool = False):
+        if initial:
+            self._slot_sets, self._plans, self._graphs = {}, {}, {}
+            self.slots, self.G = self._slot_set(gpus), gpus
+            self._graph, self._gwarm = None, False
+            return
+        if gpus == self.G:
+            return
+        # the EST context switch: every EST's slot bytes move to its new owner in ONE launch
+        dst, src, nb, cnt = self._copy_plan(self.G, gpus)
+        _native.check(_native.lib().bt_est_slot_copy(dst, src, nb, cnt, stream()), "EST slot copy")
+        self.slots, self.G = self._slot_set(gpus), gpus
+        self._graph = self._graphs.get(gpus)  # a prepared / previously captured layout replays at once
+        self._gwarm = self._graph is not None
 
     def rescale(self, gpus: int):
         """Elastic rescale onto `gpus` launch groups: per-EST slots move, parameters are replicated."""
         self._place(gpus)
+
+    def prepare(self, gpus: int) -> None:
+        """Stage layout `gpus` before a rescale needs it (EasyScale's planner knows the next layout): its slot
+        buffers, the copy plans from/to the current layout, the launch groups' workspaces and the CUDA graph
+        of its step -- captured, not run, so the training state does not move.  A later rescale(gpus) is then
+        one slot-copy launch and the next step a graph replay."""
+        if not self.graph or self.peer is not None or gpus in self._graphs:
+            return
+        for _, n in self.layout(gpus):
+            self._workspace(n)
+        for g in set(self._slot_sets) | {self.G}:  # copy plans to and from every staged layout
+            if g != gpus:
+                self._copy_plan(g, gpus)
+                self._copy_plan(gpus, g)
+        cur = (self.slots, self.G)
+        self.slots, self.G = self._slot_set(gpus), gpus
+        try:
+            self._capture(gpus)
+        finally:
+            self.slots, self.G = cur
+
+    def _capture(self, gpus: int):
+        self._stage()  # allocated outside the graph's private pool
+        gloss = torch.empty(self.En, dtype=torch.float32, device="cuda")
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._body(gloss)
+        self._graphs[gpus] = (g, gloss)
+        return self._graphs[gpus]
 
     def est_state(self) -> dict:
         """Per-EST slots gathered in EST-rank order (for comparisons across mappings)."""
@@ -448,14 +498,11 @@ class ResNetJob:
         replay = self.graph and capture is None and self.peer is None
         if replay and self._gwarm:
             if self._graph is None:  # capture once per layout (the captured work runs at the first replay)
-                self._gloss = torch.empty(self.En, dtype=torch.float32, device="cuda")
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    self._body(self._gloss)
-                self._graph = g
-            self._graph.replay()
+                self._graph = self._capture(self.G)
+            g, gloss = self._graph
+            g.replay()
             self._post()
-            return self._gloss.clone()
+            return gloss.clone()
         losses = torch.empty(self.En, dtype=torch.float32, device="cuda")
         self._body(losses, capture)
         self._post()

@@ -160,15 +160,7 @@ class DataPipeline:
         per = epochs[0].size
         n = per * len(epochs)
         if getattr(self, "_stage", None) is None or self._stage[0].numel() < n:
-            cap = max(n, 4 * per)
-            self._stage = [torch.empty(cap, dtype=torch.int32).pin_memory() for _ in range(2)]
-            self._stage_np = [t.numpy() for t in self._stage]
-            self._devbuf = [torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(2)]
-            self._devptr = [t.data_ptr() for t in self._devbuf]
-            self._stageptr = [t.data_ptr() for t in self._stage]
-            self._stage_ev = [torch.cuda.Event(), torch.cuda.Event()]
-            self._stage_used = [False, False]
-            self._stage_i = 0
+            self._upload_buffers(max(n, 4 * per))
         i = self._stage_i = self._stage_i ^ 1
         if self._stage_used[i]:
             self._stage_ev[i].synchronize()
@@ -182,10 +174,43 @@ class DataPipeline:
         self._stage_used[i] = True
         return self._devbuf[i][:n].view(len(epochs), *epochs[0].shape)
 
+    def lists_resident(self, first_epoch: int, last_epoch: int) -> bool:
+        return (self._lists_dev is not None and self._lists_dev_base <= first_epoch
+                and last_epoch < self._lists_dev_base + self._lists_dev_count)
+
+    def reserve_lists(self, first_epoch: int, count: int) -> tuple[int, torch.Tensor]:
+        """A pinned staging buffer and the device buffer that a native call (bt_mlp_run_sampled) fills with
+        the lists of epochs [first_epoch, first_epoch + count) -- computed on the host inside that call;
+        the pipeline then treats them as resident.  Returns (staging pointer, device view)."""
+        per = self.total_workers * self.steps_per_epoch * self.micro_batch
+        n = per * count
+        if getattr(self, "_stage", None) is None or self._stage[0].numel() < n:
+            self._stage = None
+            self._upload_buffers(max(n, 4 * per))
+        i = self._stage_i = self._stage_i ^ 1
+        if self._stage_used[i]:
+            self._stage_ev[i].synchronize()
+        self._stage_used[i] = False  # the native call synchronises its stream before returning
+        view = self._devbuf[i][:n].view(count, self.total_workers, self.steps_per_epoch * self.micro_batch)
+        self._lists_dev, self._lists_dev_base, self._lists_dev_count = view, first_epoch, count
+        return self._stageptr[i], view
+
+    def drop_lists(self) -> None:
+        self._lists_dev = None
+
+    def _upload_buffers(self, cap: int) -> None:
+        self._stage = [torch.empty(cap, dtype=torch.int32).pin_memory() for _ in range(2)]
+        self._stage_np = [t.numpy() for t in self._stage]
+        self._devbuf = [torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(2)]
+        self._devptr = [t.data_ptr() for t in self._devbuf]
+        self._stageptr = [t.data_ptr() for t in self._stage]
+        self._stage_ev = [torch.cuda.Event(), torch.cuda.Event()]
+        self._stage_used = [False, False]
+        self._stage_i = 0
+
     def device_lists(self, first_epoch: int, last_epoch: int) -> tuple[torch.Tensor, int]:
         """Resident [n_epochs][workers][spe*B] lists covering [first, last]; returns (tensor, base epoch)."""
-        if not (self._lists_dev is not None and self._lists_dev_base <= first_epoch
-                and last_epoch < self._lists_dev_base + self._lists_dev_count):
+        if not self.lists_resident(first_epoch, last_epoch):
             count = max(last_epoch - first_epoch + 1, self.EPOCH_WINDOW)
             self._lists_dev = self._upload([self._lists_for_epoch(e) for e in range(first_epoch, first_epoch + count)])
             self._lists_dev_base, self._lists_dev_count = first_epoch, count

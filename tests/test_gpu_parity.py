@@ -404,3 +404,38 @@ def test_allgather_params_entry_point_copies_bits(bt, dtype, es):
     _native.check(_native.lib().bt_allgather_params(dtype, src.data_ptr(), table, 5, n, stream()))
     for d in dsts:
         assert torch.equal(d, src)
+
+
+def test_run_steps_sampled_launch_equals_resident_lists(bt):
+    """run_steps with host-made inputs (bt_mlp_run_sampled: the epoch lists computed by the native
+    Fisher-Yates inside the C-ABI call, copied, then the launch) gives the bits of the launch that reads
+    lists already resident on the device -- across epoch boundaries (32 mini-batches per epoch) and
+    launches of 20 / 7 / 33 mini-batches; a launch whose staged epochs do not cover it is rejected."""
+    import ctypes as C
+
+    from paper_2208_14228_b200 import _native, engine
+
+    def cfg():
+        return bt.TrainRunConfig(seed=42, max_workers=8, micro_batch=4, dataset_size=1024, lr=0.02, momentum=0.9,
+                                 dropout_rate=0.5, jitter=0.1, bucket_capacity=64,
+                                 determinism=bt.DeterminismMode.from_label("d1"), device_fanins={"gpu_fast": 2})
+
+    a = bt.init_training(cfg(), [bt.ExecutorSpec("gpu_fast")])
+    b = bt.init_training(cfg(), [bt.ExecutorSpec("gpu_fast")])
+    for k in (20, 7, 33, 20):
+        a.pipeline.drop_lists()  # host inputs every launch: the sampled path
+        la, _ = engine.run_steps(a, k)
+        spe = b.pipeline.steps_per_epoch
+        b.pipeline.device_lists(b.global_step // spe, (b.global_step + k - 1) // spe)  # resident: bt_mlp_run
+        lb, _ = engine.run_steps(b, k)
+        assert np.array_equal(la.view(np.uint64), lb.view(np.uint64))
+    pa = np.array(a.executors[0].model.values.tolist())
+    pb = np.array(b.executors[0].model.values.tolist())
+    assert np.array_equal(pa.view(np.uint64), pb.view(np.uint64))
+    fs = engine._fast(a)
+    fs.a.K, fs.a.step0 = 40, a.global_step  # crosses into an epoch that is not staged
+    stage, lists = a.pipeline.reserve_lists(a.global_step // 32, 1)
+    st = _native.lib().bt_mlp_run_sampled(C.byref(fs.a), 42, 1024, 1, a.global_step // 32, 1, stage, lists.data_ptr(),
+                                          fs.host_losses.data_ptr(), fs.host_status.data_ptr(), None)
+    assert st == 1  # InputError, nothing launched
+    a.pipeline.drop_lists()

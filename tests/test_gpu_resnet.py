@@ -447,3 +447,31 @@ def test_run_log_across_rescale(rn):
     a.run_log(2, la)
     lb = b.run_log(6)
     assert bitdiff(la, lb) is None and len(la.records) == 6 and all(r.param_hash for r in la.records)
+
+
+def test_prepared_rescale_replays_staged_graphs_and_reenters_layouts(rn):
+    """ResNetJob.prepare stages a layout's slot buffers, copy plans and step graph (captured, not run --
+    the training state does not move); the rescale is then one slot-copy launch and the next step a
+    replay.  8 -> 4 -> 2 -> 8 -> 4 with staged graphs (the last two re-enter cached layouts) equals the
+    uninterrupted run bit for bit: weights, momentum, per-EST BN statistics and cursors."""
+    a = rn.ResNetJob(gpus=8, **SMALL)
+    b = rn.ResNetJob(gpus=1, **SMALL)
+    p0 = a.params.clone()
+    for g in (4, 2):
+        a.prepare(g)
+    assert torch.equal(a.params, p0) and set(a._graphs) == {4, 2}
+    la, lb = [], []
+    for gpus in (8, 4, 2, 8, 4):
+        if gpus != a.G:
+            a.rescale(gpus)
+            assert a.G == gpus and (gpus == 8 or a._graph is a._graphs[gpus])
+        for _ in range(2):
+            la.append(a.step().clone())
+            lb.append(b.step().clone())
+    for x, y in zip(la, lb):
+        assert np.array_equal(_bits(x), _bits(y))
+    assert np.array_equal(_bits(a.params), _bits(b.params)) and np.array_equal(_bits(a.vel), _bits(b.vel))
+    sa, sb = a.est_state(), b.est_state()
+    for k in ("run_mean", "run_var"):
+        assert np.array_equal(_bits(sa[k]), _bits(sb[k])), k
+    assert torch.equal(sa["cursor"], sb["cursor"]) and int(sa["cursor"][0]) == 10
