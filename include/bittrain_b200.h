@@ -265,6 +265,13 @@ int bt_bert_attn(int32_t backward, const void *qkv_dev, const void *dctx_dev, vo
 int bt_bert_attn_ex(int32_t backward, const void *qkv_dev, const void *dctx_dev, void *out_dev, int32_t E,
                     int32_t Te, int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer,
                     uint64_t seed, int64_t step, float p, const int64_t *step_dev, float *stats_dev, void *stream);
+/* bt_bert_attn_ex with the attention-dropout keep bits: mbits_dev [E*Te/128*heads][128][4] uint32 (16-byte
+ * aligned; row r of (sequence, head) item i at ((i*128 + r)*4), column c at bit c % 32 of word c / 32) --
+ * written by the forward, read by the backward instead of drawing the masks again; NULL: draw them. */
+int bt_bert_attn_ex2(int32_t backward, const void *qkv_dev, const void *dctx_dev, void *out_dev, int32_t E,
+                     int32_t Te, int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed,
+                     int64_t step, float p, const int64_t *step_dev, float *stats_dev, uint32_t *mbits_dev,
+                     void *stream);
 /* x = resid + dropout(branch + bias); y = LayerNorm(x) * gamma + beta -> xsum (x), stats (mean, rstd)
  * [T][2], y32 (may be NULL), yb (bf16).  resid fp32 (the residual stream), branch bf16 (a GEMM output). */
 int bt_bert_ln_fwd(const float *resid_dev, const void *branch_dev, const float *bias_dev, const float *gamma_dev,

@@ -128,6 +128,8 @@ EXPORTS = {
                                C.c_float, _vp, _vp]),
     "bt_bert_attn_ex": (C.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _u64, _i64,
                                   C.c_float, _vp, _vp, _vp]),
+    "bt_bert_attn_ex2": (C.c_int, [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _u64, _i64,
+                                  C.c_float, _vp, _vp, _vp, _vp]),
     "bt_bert_ln_fwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
                                  _i32, _u64, _i64, C.c_float, C.c_float, _vp, _vp]),
     "bt_bert_ln_fwd_rc": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32,

@@ -50,6 +50,9 @@ _MATS = ("Wqkv", "Wo", "W1", "W2")
 # b1 gradient partials from the FFN backward GEMM's epilogue (BT_BERT_CS=0: the standalone column-sum pass,
 # kept for A/B measurements)
 _FUSED_CS = os.environ.get("BT_BERT_CS", "1") != "0"
+# attention-dropout keep bits written by the forward, read by the backward (BT_ATTN_BITS=0: the backward
+# draws the masks again -- A/B measurements)
+_ATTN_BITS = os.environ.get("BT_ATTN_BITS", "1") != "0"
 
 
 def _init_uniform(seed: int, n: int, scale: float) -> torch.Tensor:
@@ -205,7 +208,9 @@ class BertJob:
                         "h1b": torch.empty(T, D, **bf), "Hpre": torch.empty(T, F, **bf),
                         "Dact": torch.empty(T, F, **bf), "hs2": torch.empty(T, D, **f32),
                         "st2": torch.empty(T, 2, **f32),
-                        "ast": torch.empty(T * self.H, 2, **f32)} for _ in range(L)],  # attention row statistics
+                        "ast": torch.empty(T * self.H, 2, **f32),  # attention row statistics
+                        "amask": torch.empty(T * self.H, 4, dtype=torch.int32, device="cuda")}  # keep bits
+                       for _ in range(L)],
             "x32": torch.empty(T, D, **f32), "y32": torch.empty(T, D, **f32),
             "brb": torch.empty(T, D, **bf), "ytop": torch.empty(T, D, **bf),
             "tgt": torch.empty(T, D, **f32), "dy1": [torch.empty(T, D, **bf) for _ in range(2)],
@@ -272,8 +277,9 @@ class BertJob:
             w = lay[l]
             self._gemm(w["xb"].data_ptr(), self._wb(l, "Wqkv"), w["qkv"].data_ptr(), T, 3 * D, D, out_bf16=True,
                        bias=self._p(l, "bqkv"))
-            _native.check(L.bt_bert_attn_ex(0, w["qkv"].data_ptr(), None, w["ctx"].data_ptr(), n, Te, D, H, base, NL,
-                                            l, seed, step, self.pa, sp, w["ast"].data_ptr(), s), "attention forward")
+            _native.check(L.bt_bert_attn_ex2(0, w["qkv"].data_ptr(), None, w["ctx"].data_ptr(), n, Te, D, H, base, NL,
+                                             l, seed, step, self.pa, sp, w["ast"].data_ptr(),
+                                             w["amask"].data_ptr() if _ATTN_BITS else None, s), "attention forward")
             self._gemm(w["ctx"].data_ptr(), self._wb(l, "Wo"), ws["brb"].data_ptr(), T, D, D, out_bf16=True)
             if l == 0:  # the embedding input is stored fp32; later residuals are recomputed (bt_bert_ln_fwd_rc)
                 _native.check(L.bt_bert_ln_fwd(x32.data_ptr(), ws["brb"].data_ptr(), self._p(l, "bo"),
@@ -352,8 +358,9 @@ class BertJob:
                                             self._g(lb, l, "bo"), self.P, s))
             self._dx(ws["dbr"].data_ptr(), self._wb(l, "Wo"), ws["dctx"].data_ptr(), T, D, D)
             self._wgrad(ws, n, ws["dbr"].data_ptr(), w["ctx"].data_ptr(), D, D, self._g(lb, l, "Wo"))
-            _native.check(L.bt_bert_attn_ex(1, w["qkv"].data_ptr(), ws["dctx"].data_ptr(), ws["dqkv"].data_ptr(), n,
-                                            Te, D, H, base, NL, l, seed, step, self.pa, sp, w["ast"].data_ptr(), s),
+            _native.check(L.bt_bert_attn_ex2(1, w["qkv"].data_ptr(), ws["dctx"].data_ptr(), ws["dqkv"].data_ptr(), n,
+                                             Te, D, H, base, NL, l, seed, step, self.pa, sp, w["ast"].data_ptr(),
+                                             w["amask"].data_ptr() if _ATTN_BITS else None, s),
                           "attention backward")
             if capture is not None and l == 0:
                 capture.update(dh=B.clone(), da=ws["dbr"].clone(), dctx=ws["dctx"].clone(), dqkv=ws["dqkv"].clone())

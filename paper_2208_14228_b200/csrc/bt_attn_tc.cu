@@ -45,6 +45,7 @@ struct Args {
   float p;
   const int64_t* step_dev;
   float2* stats;  // [n_items][128] (nm, inv) of every query row for the backward, or NULL
+  uint32_t* mbits;  // [n_items][128][4] keep bits of every row (column c at word c / 32, bit c % 32), or NULL
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(THREADS, 4)
     const uint64_t nb = ((((uint64_t)step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4) +
                         (uint64_t)((tid >> 4) * 8 + (tid & 7)) * 64;
     uint8_t* const prow = gbase + OFF_P + tid * 128;
+    uint32_t kbits[SEQ / 32];
 #pragma unroll
     for (int c = 0; c < SEQ / 32; ++c) {  // 32 columns = 16 column pairs; this lane draws 8, its partner 8
       uint32_t v[32];
@@ -204,6 +206,7 @@ __global__ void __launch_bounds__(THREADS, 4)
       uint32_t f[16];
       row_fields(sd, nb, c, hi, thr, f);
       const int kb = c >> 1;
+      uint32_t bits = 0;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {  // four 16-byte chunks (8 columns each) of this 32-column slice
         uint32_t w[4];
@@ -214,15 +217,21 @@ __global__ void __launch_bounds__(THREADS, 4)
           const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(v[q + 1]), SC, nm)) * inv;
           float m0 = 1.f, m1 = 1.f;
           if (thr) {
-            m0 = (f[q >> 1] & 0xFFFFu) < thr ? 0.f : keep;
-            m1 = (f[q >> 1] >> 16) < thr ? 0.f : keep;
+            const bool k0 = !((f[q >> 1] & 0xFFFFu) < thr), k1 = !((f[q >> 1] >> 16) < thr);
+            m0 = k0 ? keep : 0.f;
+            m1 = k1 ? keep : 0.f;
+            bits |= (k0 ? 1u : 0u) << q;
+            bits |= (k1 ? 1u : 0u) << (q + 1);
           }
           w[hh] = pack2(p0 * m0, p1 * m1);
         }
         const int chunk = (c & 1) * 4 + cc;  // 16-byte chunk within the 128-byte row of k-block kb
         *(uint4*)(prow + kb * 16384 + ((chunk ^ (tid & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
+      kbits[c] = bits;
     }
+    // the keep bits for the backward (which then draws nothing): 16 bytes per row
+    if (a.mbits) *(uint4*)(a.mbits + ((size_t)it * SEQ + tid) * 4) = make_uint4(kbits[0], kbits[1], kbits[2], kbits[3]);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
     tc_fence_before();
     __syncthreads();
@@ -303,6 +312,7 @@ struct BwdArgs {
   float p;
   const int64_t* step_dev;
   const float2* stats;  // the forward's row statistics [n_items][128], or NULL: recompute them
+  const uint32_t* mbits;  // the forward's keep bits [n_items][128][4], or NULL: draw the masks again
 };
 
 // 32 TMEM columns of this lane's row -> 32 bf16 (64 bytes) at dst
@@ -389,11 +399,15 @@ __global__ void __launch_bounds__(B_THREADS, 2)
       for (int k = 0; k < HD / 16; ++k) tc_mma(tmem + 128, ddo + 2 * k, dv + 2 * k, id128, k != 0);  // dPd
       tc_commit(bar_s);
     }
+    // the forward's statistics and keep bits of this row, in flight while the products run
+    float2 st = make_float2(0.f, 0.f);
+    uint2 mb = make_uint2(0u, 0u);
+    if (a.stats) st = a.stats[(size_t)it * SEQ + row];
+    if (a.mbits) mb = *(const uint2*)(a.mbits + ((size_t)it * SEQ + row) * 4 + hf * 2);
     mbar_wait(bar_s, ph);
     tc_fence_after();
     float nm, inv;
-    if (a.stats) {  // the forward's statistics of this row: the same instruction sequence on the same S
-      const float2 st = a.stats[(size_t)it * SEQ + row];
+    if (a.stats) {  // the same instruction sequence on the same S gave them: the same bits
       nm = st.x;
       inv = st.y;
     } else {
@@ -403,36 +417,47 @@ __global__ void __launch_bounds__(B_THREADS, 2)
     const uint64_t sd = derive3(TAG_BERT_ADROP, a.seed, (uint64_t)(a.est_base + e));
     const uint64_t nb = ((((uint64_t)step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4) +
                         (uint64_t)((row >> 4) * 8 + (row & 7)) * 64;
-    // pass 3 (this half): dropped P (packed, registers), mask bits, partial D = sum dP * P
-    uint32_t pd[32], mbits[2];
+    // pass 3 (this half): dropped P (packed, registers), the keep bits (the forward's, or drawn again),
+    // partial D = sum dP * P; P and dP * mask go back into TMEM in place of S and dPd for pass 4
+    uint32_t pd[32], mbits[2] = {mb.x, mb.y};
     float D = 0.f;
 #pragma unroll
     for (int c2 = 0; c2 < 2; ++c2) {
       const int c = hf * 2 + c2;  // 32-column slice
-      uint32_t v[32], g[32], f[16];
+      uint32_t v[32], g[32];
       tmem_ld32(lane_base + c * 32, v);
       tmem_ld32(lane_base + 128 + c * 32, g);
       tmem_ld_wait();
-      row_fields(sd, nb, c, hi, thr, f);
-      uint32_t bits = 0;
+      if (!a.mbits) {
+        uint32_t f[16];
+        row_fields(sd, nb, c, hi, thr, f);
+        uint32_t bits = 0;
+#pragma unroll
+        for (int q = 0; q < 32; q += 2) {
+          bits |= (!((f[q >> 1] & 0xFFFFu) < thr) ? 1u : 0u) << q;
+          bits |= (!((f[q >> 1] >> 16) < thr) ? 1u : 0u) << (q + 1);
+        }
+        mbits[c2] = bits;
+      }
 #pragma unroll
       for (int q = 0; q < 32; q += 2) {
         const float p0 = ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm)) * inv;
         const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(v[q + 1]), SC, nm)) * inv;
-        float m0 = 1.f, m1 = 1.f;
-        if (thr) {
-          const bool k0 = !((f[q >> 1] & 0xFFFFu) < thr), k1 = !((f[q >> 1] >> 16) < thr);
-          m0 = k0 ? keep : 0.f;
-          m1 = k1 ? keep : 0.f;
-          bits |= (k0 ? 1u : 0u) << q;
-          bits |= (k1 ? 1u : 0u) << (q + 1);
-        }
+        const float m0 = thr ? (((mbits[c2] >> q) & 1u) ? keep : 0.f) : 1.f;
+        const float m1 = thr ? (((mbits[c2] >> (q + 1)) & 1u) ? keep : 0.f) : 1.f;
         pd[c2 * 16 + (q >> 1)] = pack2(p0 * m0, p1 * m1);
-        D += __uint_as_float(g[q]) * m0 * p0;
-        D += __uint_as_float(g[q + 1]) * m1 * p1;
+        const float gm0 = __uint_as_float(g[q]) * m0, gm1 = __uint_as_float(g[q + 1]) * m1;
+        D += gm0 * p0;
+        D += gm1 * p1;
+        v[q] = __float_as_uint(p0);
+        v[q + 1] = __float_as_uint(p1);
+        g[q] = __float_as_uint(gm0);
+        g[q + 1] = __float_as_uint(gm1);
       }
-      mbits[c2] = bits;
+      tmem_st32(lane_base + c * 32, v);
+      tmem_st32(lane_base + 128 + c * 32, g);
     }
+    tmem_st_wait();
     if (!a.stats) __syncthreads();  // the sum slots of row_stats_half are read
     red[hf * SEQ + row] = D;
     __syncthreads();
@@ -443,8 +468,8 @@ __global__ void __launch_bounds__(B_THREADS, 2)
     for (int c2 = 0; c2 < 2; ++c2) {
       const int c = hf * 2 + c2;
       uint32_t v[32], g[32];
-      tmem_ld32(lane_base + c * 32, v);
-      tmem_ld32(lane_base + 128 + c * 32, g);
+      tmem_ld32(lane_base + c * 32, v);        // P
+      tmem_ld32(lane_base + 128 + c * 32, g);  // dP * mask
       tmem_ld_wait();
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
@@ -452,12 +477,8 @@ __global__ void __launch_bounds__(B_THREADS, 2)
 #pragma unroll
         for (int hh = 0; hh < 4; ++hh) {
           const int q = cc * 8 + 2 * hh;
-          const float p0 = ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm)) * inv;
-          const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(v[q + 1]), SC, nm)) * inv;
-          const float m0 = thr ? (((mbits[c2] >> q) & 1u) ? keep : 0.f) : 1.f;
-          const float m1 = thr ? (((mbits[c2] >> (q + 1)) & 1u) ? keep : 0.f) : 1.f;
-          w[hh] = pack2(p0 * (__uint_as_float(g[q]) * m0 - D) * 0.125f,
-                        p1 * (__uint_as_float(g[q + 1]) * m1 - D) * 0.125f);
+          const float p0 = __uint_as_float(v[q]), p1 = __uint_as_float(v[q + 1]);
+          w[hh] = pack2(p0 * (__uint_as_float(g[q]) - D) * 0.125f, p1 * (__uint_as_float(g[q + 1]) - D) * 0.125f);
         }
         const int chunk = c2 * 4 + cc;
         *(uint4*)(srow + ((chunk ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -532,7 +553,7 @@ __global__ void __launch_bounds__(B_THREADS, 2)
 
 int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int seqs_per_est, int est_base, int L,
                        int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev, cudaStream_t s,
-                       float* stats) {
+                       float* stats, uint32_t* mbits) {
   const int T = n_seq * attn_tc::SEQ;
   CUtensorMap mqk, mv;
   if (!make_map(&mqk, qkv, T, 3 * Dm, attn_tc::SEQ, 1, (int64_t)T * 3 * Dm) ||
@@ -546,7 +567,7 @@ int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int
     attr = true;
   }
   attn_tc::Args a{(__nv_bfloat16*)out, Dm, H, seqs_per_est, est_base, L, layer, n_seq * H, seed, step, p, step_dev,
-                  (float2*)stats};
+                  (float2*)stats, mbits};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -557,7 +578,7 @@ int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int
 
 int attn_bwd_tc_launch(const void* qkv, const void* dctx, void* dqkv, int n_seq, int Dm, int H, int seqs_per_est,
                        int est_base, int L, int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev,
-                       cudaStream_t s, const float* stats) {
+                       cudaStream_t s, const float* stats, const uint32_t* mbits) {
   const int T = n_seq * attn_tc::SEQ;
   CUtensorMap mqk, mdo;
   if (!make_map(&mqk, qkv, T, 3 * Dm, attn_tc::SEQ, 1, (int64_t)T * 3 * Dm) ||
@@ -571,7 +592,7 @@ int attn_bwd_tc_launch(const void* qkv, const void* dctx, void* dqkv, int n_seq,
     attr = true;
   }
   attn_tc::BwdArgs a{(__nv_bfloat16*)dqkv, Dm, H, seqs_per_est, est_base, L, layer, n_seq * H, seed, step, p,
-                     step_dev, (const float2*)stats};
+                     step_dev, (const float2*)stats, mbits};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

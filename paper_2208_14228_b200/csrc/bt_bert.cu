@@ -897,10 +897,10 @@ __global__ void __launch_bounds__(256) cast_t_kernel(const __grid_constant__ Cas
 // ----------------------------------------------------------------- launchers
 int attn_fwd_tc_launch(const void* qkv, void* out, int n_seq, int Dm, int H, int seqs_per_est, int est_base, int L,
                        int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev, cudaStream_t s,
-                       float* stats);
+                       float* stats, uint32_t* mbits);
 int attn_bwd_tc_launch(const void* qkv, const void* dctx, void* dqkv, int n_seq, int Dm, int H, int seqs_per_est,
                        int est_base, int L, int layer, uint64_t seed, int64_t step, float p, const int64_t* step_dev,
-                       cudaStream_t s, const float* stats);
+                       cudaStream_t s, const float* stats, const uint32_t* mbits);
 static bool attn_tc_enabled() {  // BT_ATTN_TC=0: the mma.sync forward (bt_bert.cu) instead of bt_attn_tc.cu
   const char* e = getenv("BT_ATTN_TC");
   return !(e && e[0] == '0');
@@ -909,7 +909,7 @@ static int ok_or_cuda_b() { return cudaGetLastError() == cudaSuccess ? OK : ERR_
 
 int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out, int n_seq, int Dm, int H,
                      int seqs_per_est, int est_base, int L, int layer, uint64_t seed, int64_t step, float p,
-                     const int64_t* step_dev, cudaStream_t s, float* stats) {
+                     const int64_t* step_dev, cudaStream_t s, float* stats, uint32_t* mbits) {
   bert::AttnArgs a{(const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dctx, (__nv_bfloat16*)out, Dm, H, seqs_per_est,
                    est_base, L, layer, n_seq * H, seed, step, p, step_dev};
   int dev = 0, sms = 148;
@@ -917,9 +917,9 @@ int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (attn_tc_enabled())
     return backward ? attn_bwd_tc_launch(qkv, dctx, out, n_seq, Dm, H, seqs_per_est, est_base, L, layer, seed, step, p,
-                                         step_dev, s, stats)
+                                         step_dev, s, stats, mbits)
                     : attn_fwd_tc_launch(qkv, out, n_seq, Dm, H, seqs_per_est, est_base, L, layer, seed, step, p,
-                                         step_dev, s, stats);
+                                         step_dev, s, stats, mbits);
   if (!backward) {
     static bool attr = false;
     if (!attr) {

@@ -57,7 +57,7 @@ int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, 
                                cudaStream_t s);
 int bert_attn_launch(int backward, const void* qkv, const void* dctx, void* out, int n_seq, int Dm, int H,
                      int seqs_per_est, int est_base, int L, int layer, uint64_t seed, int64_t step, float p,
-                     const int64_t* step_dev, cudaStream_t s, float* stats);
+                     const int64_t* step_dev, cudaStream_t s, float* stats, uint32_t* mbits);
 int bert_ln_launch(int backward, const float* in1, const void* in2, const float* bias, const float* gamma,
                    const float* beta, float* xsum, float* stats, float* y32, void* yb, float* part, int E, int Te,
                    int D, int est_base, int L, int layer, int site, uint64_t seed, int64_t step, float p, float eps,
@@ -866,12 +866,20 @@ int bt_bert_data(uint64_t seed, int64_t step, int32_t est_base, int32_t E, int32
 int bt_bert_attn_ex(int32_t backward, const void* qkv_dev, const void* dctx_dev, void* out_dev, int32_t E,
                     int32_t Te, int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed,
                     int64_t step, float p, const int64_t* step_dev, float* stats_dev, void* stream) {
+  return bt_bert_attn_ex2(backward, qkv_dev, dctx_dev, out_dev, E, Te, D, heads, est_base, layers, layer, seed, step, p,
+                          step_dev, stats_dev, nullptr, stream);
+}
+int bt_bert_attn_ex2(int32_t backward, const void* qkv_dev, const void* dctx_dev, void* out_dev, int32_t E,
+                     int32_t Te, int32_t D, int32_t heads, int32_t est_base, int32_t layers, int32_t layer, uint64_t seed,
+                     int64_t step, float p, const int64_t* step_dev, float* stats_dev, uint32_t* mbits_dev,
+                     void* stream) {
   if (int st = bert_shape(E, Te, D)) return st;
+  if (((uintptr_t)mbits_dev) & 15) return fail(bt::ERR_INPUT, "attention keep bits must be 16-byte aligned");
   if (heads * 64 != D) return fail(bt::ERR_INPUT, "bert attention: head dim must be 64 (heads %d, D %d)", heads, D);
   if (!qkv_dev || !out_dev || (backward && !dctx_dev)) return fail(bt::ERR_INPUT, "null pointer");
   if (!(p >= 0.f && p < 1.f) || layer < 0 || layer >= layers) return fail(bt::ERR_CONFIG, "bad dropout / layer");
   return done(bt::bert_attn_launch(backward, qkv_dev, dctx_dev, out_dev, E * Te / 128, D, heads, Te / 128, est_base,
-                                   layers, layer, seed, step, p, step_dev, STREAM(stream), stats_dev),
+                                   layers, layer, seed, step, p, step_dev, STREAM(stream), stats_dev, mbits_dev),
               "bt_bert_attn");
 }
 int bt_bert_attn(int32_t backward, const void* qkv_dev, const void* dctx_dev, void* out_dev, int32_t E, int32_t Te,
