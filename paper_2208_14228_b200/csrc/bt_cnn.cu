@@ -266,67 +266,139 @@ __global__ void fold_kernel(const FoldArgs a) {
   }
 }
 
-// y = [relu](gamma * (z - mean) * rstd + beta [+ res])   (bf16, 8 channels per thread)
-__global__ void __launch_bounds__(256) bn_apply_kernel(const __nv_bfloat16* __restrict__ z,
-                                                       const __nv_bfloat16* __restrict__ res,
-                                                       const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                       const float* __restrict__ gamma, const float* __restrict__ beta,
-                                                       int C, int R, int64_t rows, int relu,
-                                                       __nv_bfloat16* __restrict__ y) {
-  const int cg = C / 8;
-  const int n = (int)(rows * cg);  // < 2^31 (launcher)
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int row = i / cg;
-    const int c0 = (i - row * cg) * 8, e = row / R;
-    float zv[8], o[8], rv[8], mv[8], sv[8], gv[8], bv[8];
-    const size_t off = (size_t)row * C + c0;
-    ld8(z + off, zv);
-    if (res) ld8(res + off, rv);
-    ldf8(mean + (size_t)e * C + c0, mv);
-    ldf8(rstd + (size_t)e * C + c0, sv);
-    ldf8(gamma + c0, gv);
-    ldf8(beta + c0, bv);
+// Block = (local EST e, a span of `rows_per` of that EST's rows, sized on the host for ~4 blocks per SM);
+// the EST's per-channel parameters are staged in shared memory once per block and each thread walks its
+// 8-channel group down the span's rows, BN_UNROLL rows' loads in flight at a time.  The per-element
+// arithmetic is unchanged.
+constexpr int BN_THREADS = 256, BN_UNROLL = 4;
+__device__ __forceinline__ void cvt8(const uint4& u, float* v) {
+  const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float v = gv[q] * ((zv[q] - mv[q]) * sv[q]) + bv[q];
-      if (res) v += rv[q];
-      o[q] = (relu && !(v > 0.f)) ? 0.f : v;
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __bfloat1622float2(h[k]);
+    v[2 * k] = f.x;
+    v[2 * k + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void lds8(const float* p, float* v) {
+  const float4 a = *(const float4*)p, b = *(const float4*)(p + 4);
+  v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+}
+
+// y = [relu](gamma * (z - mean) * rstd + beta [+ res])   (bf16, 8 channels per thread)
+__global__ void __launch_bounds__(BN_THREADS, 2) bn_apply_kernel(const __nv_bfloat16* __restrict__ z,
+                                                              const __nv_bfloat16* __restrict__ res,
+                                                              const float* __restrict__ mean,
+                                                              const float* __restrict__ rstd,
+                                                              const float* __restrict__ gamma,
+                                                              const float* __restrict__ beta, int C, int R, int relu,
+                                                              int rows_per, __nv_bfloat16* __restrict__ y) {
+  extern __shared__ __align__(16) float bnp[];  // [4][C]: mean, rstd, gamma, beta of this block's EST
+  const int e = blockIdx.y;
+  for (int i = threadIdx.x; i < C; i += BN_THREADS) {
+    bnp[i] = mean[(size_t)e * C + i];
+    bnp[C + i] = rstd[(size_t)e * C + i];
+    bnp[2 * C + i] = gamma[i];
+    bnp[3 * C + i] = beta[i];
+  }
+  __syncthreads();
+  const int cg = C / 8, lanes = BN_THREADS / cg;  // C in {64 .. 512}: cg divides 256
+  const int c0 = (threadIdx.x % cg) * 8, lane = threadIdx.x / cg;
+  const int r0 = blockIdx.x * rows_per, r1 = min(R, r0 + rows_per);
+  float mv[8], sv[8], gv[8], bv[8];
+  lds8(bnp + c0, mv);
+  lds8(bnp + C + c0, sv);
+  lds8(bnp + 2 * C + c0, gv);
+  lds8(bnp + 3 * C + c0, bv);
+  const size_t base = (size_t)e * R * C + c0;
+  for (int r = r0 + lane; r < r1; r += BN_UNROLL * lanes) {
+    uint4 zr[BN_UNROLL], rr_[BN_UNROLL];  // raw bf16: the loads of all unrolled rows in flight at once
+#pragma unroll
+    for (int u = 0; u < BN_UNROLL; ++u) {
+      const int rr = r + u * lanes;
+      if (rr < r1) {
+        zr[u] = *(const uint4*)(z + base + (size_t)rr * C);
+        if (res) rr_[u] = *(const uint4*)(res + base + (size_t)rr * C);
+      }
     }
-    st8(y + off, o);
+#pragma unroll
+    for (int u = 0; u < BN_UNROLL; ++u) {
+      const int rr = r + u * lanes;
+      if (rr >= r1) continue;
+      float o[8], zv[1][8], rv[1][8];
+      cvt8(zr[u], zv[0]);
+      if (res) cvt8(rr_[u], rv[0]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float v = gv[q] * ((zv[0][q] - mv[q]) * sv[q]) + bv[q];
+        if (res) v += rv[0][q];
+        o[q] = (relu && !(v > 0.f)) ? 0.f : v;
+      }
+      st8(y + base + (size_t)rr * C, o);
+    }
   }
 }
 
 // dz = gamma * rstd * (g - S_g / R - xhat * S_gx / R),  g = dy * [y > 0]
-__global__ void __launch_bounds__(256) bn_bwd_kernel(const __nv_bfloat16* __restrict__ z,
-                                                     const __nv_bfloat16* __restrict__ dy,
-                                                     const __nv_bfloat16* __restrict__ y,
-                                                     const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                     const float* __restrict__ sg, const float* __restrict__ sgx,
-                                                     const float* __restrict__ gamma, int C, int R, int64_t rows,
-                                                     __nv_bfloat16* __restrict__ dz) {
-  const int cg = C / 8;
-  const int n = (int)(rows * cg);  // < 2^31 (launcher)
+__global__ void __launch_bounds__(BN_THREADS, 2) bn_bwd_kernel(const __nv_bfloat16* __restrict__ z,
+                                                            const __nv_bfloat16* __restrict__ dy,
+                                                            const __nv_bfloat16* __restrict__ y,
+                                                            const float* __restrict__ mean,
+                                                            const float* __restrict__ rstd,
+                                                            const float* __restrict__ sg,
+                                                            const float* __restrict__ sgx,
+                                                            const float* __restrict__ gamma, int C, int R,
+                                                            int rows_per, __nv_bfloat16* __restrict__ dz) {
+  extern __shared__ __align__(16) float bnp[];  // [5][C]: mean, rstd, S_g, S_gx, gamma
+  const int e = blockIdx.y;
+  for (int i = threadIdx.x; i < C; i += BN_THREADS) {
+    const size_t ec = (size_t)e * C + i;
+    bnp[i] = mean[ec];
+    bnp[C + i] = rstd[ec];
+    bnp[2 * C + i] = sg[ec];
+    bnp[3 * C + i] = sgx[ec];
+    bnp[4 * C + i] = gamma[i];
+  }
+  __syncthreads();
   const float invR = 1.f / (float)R;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int row = i / cg;
-    const int c0 = (i - row * cg) * 8, e = row / R;
-    float zv[8], dv[8], yv[8], o[8], mv[8], sv[8], gv[8], av[8], bv[8];
-    const size_t off = (size_t)row * C + c0, ec = (size_t)e * C + c0;
-    ld8(z + off, zv);
-    ld8(dy + off, dv);
-    ld8(y + off, yv);
-    ldf8(mean + ec, mv);
-    ldf8(rstd + ec, sv);
-    ldf8(sg + ec, av);
-    ldf8(sgx + ec, bv);
-    ldf8(gamma + c0, gv);
+  const int cg = C / 8, lanes = BN_THREADS / cg;
+  const int c0 = (threadIdx.x % cg) * 8, lane = threadIdx.x / cg;
+  const int r0 = blockIdx.x * rows_per, r1 = min(R, r0 + rows_per);
+  float mv[8], sv[8], av[8], bv[8], gv[8];
+  lds8(bnp + c0, mv);
+  lds8(bnp + C + c0, sv);
+  lds8(bnp + 2 * C + c0, av);
+  lds8(bnp + 3 * C + c0, bv);
+  lds8(bnp + 4 * C + c0, gv);
+  const size_t base = (size_t)e * R * C + c0;
+  for (int r = r0 + lane; r < r1; r += BN_UNROLL * lanes) {
+    uint4 zr[BN_UNROLL], dr[BN_UNROLL], yr[BN_UNROLL];  // raw bf16: all unrolled rows' loads in flight
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float g = yv[q] > 0.f ? dv[q] : 0.f;
-      const float xh = (zv[q] - mv[q]) * sv[q];
-      o[q] = gv[q] * sv[q] * (g - av[q] * invR - xh * (bv[q] * invR));
+    for (int u = 0; u < BN_UNROLL; ++u) {
+      const int rr = r + u * lanes;
+      if (rr < r1) {
+        const size_t off = base + (size_t)rr * C;
+        zr[u] = *(const uint4*)(z + off);
+        dr[u] = *(const uint4*)(dy + off);
+        yr[u] = *(const uint4*)(y + off);
+      }
     }
-    st8(dz + off, o);
+#pragma unroll
+    for (int u = 0; u < BN_UNROLL; ++u) {
+      const int rr = r + u * lanes;
+      if (rr >= r1) continue;
+      float o[8], zv[8], dv[8], yv[8];
+      cvt8(zr[u], zv);
+      cvt8(dr[u], dv);
+      cvt8(yr[u], yv);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float g = yv[q] > 0.f ? dv[q] : 0.f;
+        const float xh = (zv[q] - mv[q]) * sv[q];
+        o[q] = gv[q] * sv[q] * (g - av[q] * invR - xh * (bv[q] * invR));
+      }
+      st8(dz + base + (size_t)rr * C, o);
+    }
   }
 }
 
@@ -649,23 +721,33 @@ int cnn_bn_stats_launch(int mode, const void* z, const void* dy, const void* y, 
   return ok_or_cuda_c();
 }
 
+// rows per BatchNorm block: ~4 blocks per SM over the launch, a whole number of unrolled row steps
+static int bn_rows_per(int E, int R, int C) {
+  const int step = cnn::BN_UNROLL * (cnn::BN_THREADS / (C / 8));
+  const int64_t want = ((int64_t)R * E + 4 * 148 - 1) / (4 * 148);
+  const int64_t rp = (want + step - 1) / step * step;
+  return (int)(rp < R ? rp : R);
+}
 int cnn_bn_apply_launch(const void* z, const void* res, const float* mean, const float* rstd, const float* gamma,
                         const float* beta, int E, int R, int C, int relu, void* y, cudaStream_t s) {
-  const int64_t rows = (int64_t)E * R;
-  if (rows * C / 8 >= (int64_t)1 << 31) return ERR_INPUT;
-  cnn::bn_apply_kernel<<<grid_n(rows * C / 8), 256, 0, s>>>((const __nv_bfloat16*)z, (const __nv_bfloat16*)res, mean,
-                                                           rstd, gamma, beta, C, R, rows, relu, (__nv_bfloat16*)y);
+  if (C % 64 || C > 512 || (int64_t)R * C / 8 >= (int64_t)1 << 31) return ERR_INPUT;
+  const int rows_per = bn_rows_per(E, R, C);
+  const dim3 grid((R + rows_per - 1) / rows_per, E);
+  cnn::bn_apply_kernel<<<grid, cnn::BN_THREADS, 4 * C * sizeof(float), s>>>(
+      (const __nv_bfloat16*)z, (const __nv_bfloat16*)res, mean, rstd, gamma, beta, C, R, relu, rows_per,
+      (__nv_bfloat16*)y);
   return ok_or_cuda_c();
 }
 
 int cnn_bn_bwd_launch(const void* z, const void* dy, const void* y, const float* mean, const float* rstd,
                       const float* sg, const float* sgx, const float* gamma, int E, int R, int C, void* dz,
                       cudaStream_t s) {
-  const int64_t rows = (int64_t)E * R;
-  if (rows * C / 8 >= (int64_t)1 << 31) return ERR_INPUT;
-  cnn::bn_bwd_kernel<<<grid_n(rows * C / 8), 256, 0, s>>>((const __nv_bfloat16*)z, (const __nv_bfloat16*)dy,
-                                                         (const __nv_bfloat16*)y, mean, rstd, sg, sgx, gamma, C, R,
-                                                         rows, (__nv_bfloat16*)dz);
+  if (C % 64 || C > 512 || (int64_t)R * C / 8 >= (int64_t)1 << 31) return ERR_INPUT;
+  const int rows_per = bn_rows_per(E, R, C);
+  const dim3 grid((R + rows_per - 1) / rows_per, E);
+  cnn::bn_bwd_kernel<<<grid, cnn::BN_THREADS, 5 * C * sizeof(float), s>>>(
+      (const __nv_bfloat16*)z, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)y, mean, rstd, sg, sgx, gamma, C, R,
+      rows_per, (__nv_bfloat16*)dz);
   return ok_or_cuda_c();
 }
 
