@@ -128,6 +128,12 @@ class HostGate:
     whole timed region, so the CUDA-event span holds the kernels only -- not host scheduling jitter
     between the first event and the launch (cuStreamWaitValue32 on mapped host memory)."""
 
+    # Under a profiler that serialises launches (Nsight Compute: its injection sets NV_TPS_LAUNCH_TOKEN /
+    # NV_NSIGHT_INJECTION_*) a kernel queued behind the gate would wait for a host write that only comes
+    # after its launch call returns: the gate is then a no-op (profiled runs are never bench values).
+    PASS = any(k in os.environ for k in ("NV_TPS_LAUNCH_TOKEN", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE",
+                                         "CUDA_INJECTION64_PATH")) or os.environ.get("BT_BENCH_GATE") == "0"
+
     def __init__(self):
         self.word = torch.zeros(1, dtype=torch.int32).pin_memory()
         self.np = self.word.numpy()
@@ -136,6 +142,8 @@ class HostGate:
     def close(self, stream) -> None:
         from paper_2208_14228_b200 import _native
 
+        if self.PASS:
+            return
         self.n += 1
         _native.check(_native.lib().bt_stream_wait_u32_geq(self.word.data_ptr(), self.n, stream.cuda_stream),
                       "host gate")

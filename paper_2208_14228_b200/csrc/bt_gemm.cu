@@ -692,6 +692,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     uint8_t* const est = gbase + L::EPI + (warp - 2) * EPI_STAGE;
     int chunk = 0;
     const uint32_t leader_tempty0 = map_to_rank(tempty(0), 0), leader_tempty1 = map_to_rank(tempty(1), 0);
+    const int c_lo = half * (PAIR_BN / (EW / 4)), c_hi = c_lo + PAIR_BN / (EW / 4);
     int i = 0;
     for (int t = pair; t < tiles; t += pairs, ++i) {
       const int acc = i & 1;
@@ -702,7 +703,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
       const int row0 = m0 + (int)rank * BM + lg * 32;
       const size_t row = (size_t)row0 + lane;
 #pragma unroll 1
-      for (int cc = half * (PAIR_BN / (EW / 4)); cc < (half + 1) * (PAIR_BN / (EW / 4)); cc += 32) {
+      for (int cc = c_lo; cc < c_hi; cc += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * PAIR_BN + cc), v);
         tmem_ld_wait();

@@ -467,9 +467,12 @@ def _rot_tensor(ts: TrainingState):
     variant = _comm_variant(ts)
     if fanin_code(variant) == 0:
         return None
-    key = (ts.bucket_map, ts.cfg.max_workers)
     dev = ts.dev
-    if dev.rot_key != key:
+    rk = dev.rot_key
+    if rk is not None and rk[0] is ts.bucket_map and rk[1] == ts.cfg.max_workers:  # the per-call case
+        return dev.rot
+    key = (ts.bucket_map, ts.cfg.max_workers)
+    if rk != key:
         with torch.cuda.device(dev.shards[0].ordinal):
             dev.rot = torch.from_numpy(rotation_table(ts.bucket_map, ts.cfg.max_workers)).to("cuda")
         dev.rot_key = key
@@ -513,14 +516,23 @@ def _step_args(ts: TrainingState, K: int, B: int, rows: torch.Tensor | None, los
     return a, keep
 
 
+_FITS: dict = {}
+
+
 def _fused_fits(cfg, B: int | None = None) -> bool:
-    """Whether one fused launch holds the whole step on chip (bt_mlp_fused_fits)."""
+    """Whether one fused launch holds the whole step on chip (bt_mlp_fused_fits); a pure function of
+    (E, B), cached (it is asked on every run_minibatch / run_steps call)."""
+    key = (cfg.max_workers, cfg.micro_batch if B is None else B)
+    hit = _FITS.get(key)
+    if hit is not None:
+        return hit
     a = _native.MlpArgs()
     a.E = a.E_total = cfg.max_workers
     a.B = cfg.micro_batch if B is None else B
     a.K, a.fuse_reduce = 1, 1
     a.est_per_cta = _native.lib().bt_mlp_pick_est_per_cta(a.E, a.B)
-    return bool(_native.lib().bt_mlp_fused_fits(C.byref(a)))
+    _FITS[key] = ok = bool(_native.lib().bt_mlp_fused_fits(C.byref(a)))
+    return ok
 
 
 def _raise_step_error(ts: TrainingState, st: int, detail: int, what: str) -> None:
@@ -568,6 +580,7 @@ class _FastStep:
         self.status_np = self.host_status.numpy()
         self.losses_np = self.host_losses.numpy()
         self.a, self.keep = _step_args(ts, 1, cfg.micro_batch, None, self.losses, None) if self.fits else (None, [])
+        self._lh = self.host_losses.data_ptr()
         self.dev = ts.dev
 
     def run(self, ts: TrainingState, K: int) -> int:
@@ -586,16 +599,14 @@ class _FastStep:
             lists, base = pipe.device_lists(e0, e1)
             self.keep = [lists]
             a.lists, a.epoch_base = lists.data_ptr(), base
-            st = _native.lib().bt_mlp_run(C.byref(a), self.host_losses.data_ptr(), self.host_status.data_ptr(),
-                                          _raw_stream())
+            st = _native.lib().bt_mlp_run(C.byref(a), self._lh, self.host_status.data_ptr(), _raw_stream())
         else:  # the epochs' lists are made on the host inside the native call, copied, then the launch
             count = max(e1 - e0 + 1, pipe.EPOCH_WINDOW)
             stage, lists = pipe.reserve_lists(e0, count)
             self.keep = [lists]
             st = _native.lib().bt_mlp_run_sampled(C.byref(a), pipe.seed & (2**64 - 1), pipe.dataset_size,
                                                   int(pipe.shuffle), e0, count, stage, lists.data_ptr(),
-                                                  self.host_losses.data_ptr(), self.host_status.data_ptr(),
-                                                  _raw_stream())
+                                                  self._lh, self.host_status.data_ptr(), _raw_stream())
             if st:
                 pipe.drop_lists()
         _native.check(st, "run_minibatch")

@@ -220,3 +220,4 @@ def test_ffn_backward_epilogue_column_partials(monkeypatch, variant):
     for k in range(1, per):
         acc = acc + want.reshape(leaves, per, F)[:, k]
     assert np.array_equal(out[:, :F].cpu().numpy().view(np.uint32), acc.view(np.uint32))
+

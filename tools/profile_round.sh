@@ -28,9 +28,19 @@ BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --metrics gpu__time_duration.
 BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16 -s 2 -c 1 \
   -f -o $O/prof_bert_gemm_$tag python tools/bert_bench.py 32 1 1 8 > $O/ncu_bert_gemm.out 2>&1; echo bert_gemm_rc=$?
 BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_bwd -c 1 \
-  -f -o $O/prof_bert_attn_$tag python tools/bert_bench.py 32 1 1 8 > $O/ncu_bert_attn.out 2>&1; echo bert_attn_rc=$?
-BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ln_bwd -c 1 \
-  -f -o $O/prof_bert_ln_$tag python tools/bert_bench.py 32 1 1 8 > $O/ncu_bert_ln.out 2>&1; echo bert_ln_rc=$?
+  -s 2 -f -o $O/prof_bert_attn_$tag python tools/bert_bench.py 32 1 2 8 > $O/ncu_bert_attn.out 2>&1; echo bert_attn_rc=$?
+BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ln_bwd -s 2 -c 1 \
+  -f -o $O/prof_bert_ln_$tag python tools/bert_bench.py 32 1 2 8 > $O/ncu_bert_ln.out 2>&1; echo bert_ln_rc=$?
+BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ln_fwd -s 2 -c 1 \
+  -f -o $O/prof_bert_lnf_$tag python tools/bert_bench.py 32 1 2 8 > $O/ncu_bert_lnf.out 2>&1; echo bert_lnf_rc=$?
+BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 2 -c 1 \
+  -f -o $O/prof_bert_attnf_$tag python tools/bert_bench.py 32 1 2 8 > $O/ncu_bert_attnf.out 2>&1; echo bert_attnf_rc=$?
+# C3 BatchNorm kernels (statistics pass, apply, backward: the 3rd launch of each)
+for k in stats_kernel bn_apply_kernel bn_bwd_kernel; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -f -o $O/prof_resnet_${k}_$tag \
+    python tools/resnet_prof.py 16 32 1 > $O/ncu_resnet_$k.out 2>&1; echo resnet_${k}_rc=$?
+done
+python tools/resnet_prof.py 16 32 1 > $O/resnet_prof.txt 2>&1
 python tools/bert_prof.py 32 12 8 > $O/bert_prof.txt 2>&1; python tools/gemm_list.py 2 > $O/gemm_list.txt 2>&1
 # C3 (ResNet-18 per-EST BN step): launch list of one step, ncu of the layer-1 convolution
 BT_BENCH_WARMUP=1 BT_BENCH_STEPS=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 400 \

@@ -97,13 +97,19 @@ t_ri = summarize(OUT / f"prof_resnet_conv_{tag}.ncu-rep", "ncu_resnet_conv", ext
 t_bg = summarize(OUT / f"prof_bert_gemm_{tag}.ncu-rep", "ncu_bert_gemm", extra=("pipe_tensor", "pipe_tc", "tmem", "utc"))
 t_ba = summarize(OUT / f"prof_bert_attn_{tag}.ncu-rep", "ncu_bert_attn_bwd", extra=("pipe_tensor", "pipe_tc"))
 t_bl = summarize(OUT / f"prof_bert_ln_{tag}.ncu-rep", "ncu_bert_ln_bwd")
+t_blf = summarize(OUT / f"prof_bert_lnf_{tag}.ncu-rep", "ncu_bert_ln_fwd")
+t_baf = summarize(OUT / f"prof_bert_attnf_{tag}.ncu-rep", "ncu_bert_attn_fwd", extra=("pipe_tensor", "pipe_tc"))
+t_bn = {k: summarize(OUT / f"prof_resnet_{k}_{tag}.ncu-rep", f"ncu_resnet_{k}")
+        for k in ("stats_kernel", "bn_apply_kernel", "bn_bwd_kernel")}
 t_mlp = summarize(OUT / f"prof_mlp_{tag}.ncu-rep", "ncu_mlp_step")
 t_red = summarize(OUT / f"prof_reduce_{tag}.ncu-rep", "ncu_reducer")
 t_gemm = summarize(OUT / f"prof_gemm_{tag}.ncu-rep", "ncu_gemm", extra=("pipe_tensor", "pipe_tc", "tmem", "utc"))
 traffic = {"mlp_step_kernel": t_mlp[0] if t_mlp else None, "reduce_fast_kernel": t_red[0] if t_red else None,
            "gemm_bf16_tn_kernel": t_gemm[0] if t_gemm else None,
            "bert_ffn_gemm": t_bg[0] if t_bg else None, "attn_bwd_kernel": t_ba[0] if t_ba else None,
-           "ln_bwd_kernel": t_bl[0] if t_bl else None, "resnet_conv_layer1": t_ri[0] if t_ri else None,
+           "ln_bwd_kernel": t_bl[0] if t_bl else None, "ln_fwd_kernel": t_blf[0] if t_blf else None,
+           "attn_fwd_kernel": t_baf[0] if t_baf else None, "resnet_conv_layer1": t_ri[0] if t_ri else None,
+           **{f"resnet_{k}": (v[0] if v else None) for k, v in t_bn.items()},
            "source": f"profiles/{tag}_ncu_*.txt (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"}
 (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
 print(json.dumps(traffic))
