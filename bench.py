@@ -190,6 +190,7 @@ def bench_device_single(bt, K: int, W: int, flush):
         lists, base = ts.pipeline.device_lists(gs // spe, (gs + n - 1) // spe)
         a = fs.a
         a.K, a.step0, a.lists, a.epoch_base = n, gs, lists.data_ptr(), base
+        a.losses = fs.io_ptr + 8 * (fs.KMAX - n) * fs.E  # the launch's rows of the shard's I/O block
         flush()
         gate.close(s)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -88,8 +88,10 @@ int bt_fwd_bwd_mlp_f64(const double *params_dev, const double *rows_dev, int32_t
 int bt_mlp_step(const bt_mlp_args *args, void *stream);
 /* bt_mlp_step, then the K x E_total per-EST losses and the 4-word status block copied into
  * caller-owned HOST buffers and the stream synchronised: the whole of one run_minibatch /
- * run_steps call in one entry point (losses_host may be NULL: e.g. when args->losses is itself pinned
- * host memory, which the kernel then writes directly -- zero-copy under UVA).   engine.py:271-329 */
+ * run_steps call in one entry point (losses_host may be NULL).  status_host may be NULL when the
+ * device status block directly follows the K x E_total losses (args->flags == args->losses + K*E_total):
+ * then ONE copy of the losses and the 4 status words lands in losses_host, the words at its tail.
+ *                                                                      engine.py:271-329 */
 int bt_mlp_run(const bt_mlp_args *args, double *losses_host, int32_t *status_host, void *stream);
 /* bt_mlp_run with the sampler's host work inside the call: the index lists of epochs [first_epoch,
  * first_epoch + n_epochs) are computed on the host (native Fisher-Yates seeded seed ^ epoch, dealt

@@ -332,15 +332,25 @@ static cudaError_t host_wait(cudaStream_t s) {
 int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_host, void* stream) {
   int st = validate_mlp(args);
   if (st) return st;
-  if (!status_host) return fail(bt::ERR_INPUT, "bt_mlp_run needs a status buffer");
+  const size_t lbytes = sizeof(double) * (size_t)args->K * args->E_total;
+  // status_host == NULL: the status block directly follows the losses in device memory, and ONE copy
+  // brings both (status words at the tail of losses_host)
+  const bool one_copy = !status_host && losses_host && (const char*)args->flags == (const char*)args->losses + lbytes;
+  if (!status_host && !one_copy)
+    return fail(bt::ERR_INPUT, "bt_mlp_run needs a status buffer (or the status block right after the losses)");
   st = bt::mlp_launch(*args, STREAM(stream));
   if (st) return done(st, "bt_mlp_run");
   cudaStream_t s = STREAM(stream);
-  if (losses_host && cudaMemcpyAsync(losses_host, args->losses, sizeof(double) * (size_t)args->K * args->E_total,
-                                     cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    return cuda_fail("bt_mlp_run losses");
-  if (cudaMemcpyAsync(status_host, args->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    return cuda_fail("bt_mlp_run status");
+  if (one_copy) {
+    if (cudaMemcpyAsync(losses_host, args->losses, lbytes + 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s) !=
+        cudaSuccess)
+      return cuda_fail("bt_mlp_run losses + status");
+  } else {
+    if (losses_host && cudaMemcpyAsync(losses_host, args->losses, lbytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      return cuda_fail("bt_mlp_run losses");
+    if (cudaMemcpyAsync(status_host, args->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      return cuda_fail("bt_mlp_run status");
+  }
   if (host_wait(s) != cudaSuccess) return cuda_fail("bt_mlp_run sync");
   g_err[0] = 0;
   return 0;

@@ -62,8 +62,9 @@ def ptr(t: torch.Tensor | None) -> int | None:
 class Flags:
     """The 4-word device status block {status, detail, step, spare}."""
 
-    def __init__(self):
-        self.t = torch.zeros(4, dtype=torch.int32, device=require_cuda())
+    def __init__(self, t: torch.Tensor | None = None):
+        """`t`: an int32[4] device view to hold the words (e.g. the tail of a shard's I/O block)."""
+        self.t = torch.zeros(4, dtype=torch.int32, device=require_cuda()) if t is None else t
         self.reset()
 
     def _stream(self) -> int:  # the current stream of the GPU holding the words

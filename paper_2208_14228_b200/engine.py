@@ -102,6 +102,9 @@ class TrainRunConfig:
 
 
 # ---------------------------------------------------------------- device state
+IO_ROWS = 128  # mini-batches of losses a shard's I/O block holds (the prepared launch's KMAX)
+
+
 class Shard:
     """One GPU's part of a job: the replicas of the executors placed on it and the slots of
     their ESTs (a contiguous rank block).  Slot arrays are [E] on every shard; only the
@@ -118,7 +121,10 @@ class Shard:
             self.stat_mean = torch.zeros(E, dtype=torch.float64, device="cuda")
             self.stat_count = torch.zeros(E, dtype=torch.int64, device="cuda")
             self.grads = torch.zeros((2, E, P), dtype=torch.float64, device="cuda")  # step-parity slots
-            self.flags = Flags()
+            # I/O block: IO_ROWS x E per-EST losses, then the 4-word status block -- a launch of K
+            # mini-batches writes its losses into the last K rows, so one copy brings losses + status
+            self.io = torch.zeros(IO_ROWS * E + 2, dtype=torch.float64, device="cuda")
+            self.flags = Flags(self.io[IO_ROWS * E:].view(torch.int32))
             self.bar = torch.zeros(1, dtype=torch.int32, device="cuda")
             # the stream of this shard's lock-step launches: shards sharing one GPU (logical devices)
             # must run concurrently, so each has its own
@@ -568,19 +574,23 @@ class _FastStep:
     the argument block with its fixed pointers, and pinned host buffers that bt_mlp_run fills
     with the per-EST losses and the status words (one C-ABI call and one sync per call)."""
 
-    KMAX = 128
+    KMAX = IO_ROWS
 
     def __init__(self, ts: TrainingState):
         cfg = ts.cfg
         self.E = cfg.max_workers
         self.fits = _fused_fits(cfg)
-        self.losses = torch.empty((self.KMAX, self.E), dtype=torch.float64, device="cuda")
-        self.host_losses = torch.empty((self.KMAX, self.E), dtype=torch.float64).pin_memory()
-        self.host_status = torch.zeros(4, dtype=torch.int32).pin_memory()
-        self.status_np = self.host_status.numpy()
-        self.losses_np = self.host_losses.numpy()
-        self.a, self.keep = _step_args(ts, 1, cfg.micro_batch, None, self.losses, None) if self.fits else (None, [])
-        self._lh = self.host_losses.data_ptr()
+        # the shard's I/O block: a K-mini-batch launch writes its losses into the last K rows, which the
+        # status words follow -- so bt_mlp_run brings both back in one copy into the same layout on the host
+        io = ts.dev.shards[0].io
+        self.io_ptr = io.data_ptr()
+        self.host_io = torch.zeros(io.numel(), dtype=torch.float64).pin_memory()
+        self.host_io_ptr = self.host_io.data_ptr()
+        io_np = self.host_io.numpy()
+        self.rows_np = io_np[:self.KMAX * self.E].reshape(self.KMAX, self.E)
+        self.status_np = io_np[self.KMAX * self.E:].view(np.int32)
+        self.losses_np = self.rows_np
+        self.a, self.keep = _step_args(ts, 1, cfg.micro_batch, None, io, None) if self.fits else (None, [])
         self.dev = ts.dev
 
     def run(self, ts: TrainingState, K: int) -> int:
@@ -595,21 +605,25 @@ class _FastStep:
         a.K, a.step0 = K, gs
         a.rot = ptr(rot)
         a.lr, a.mu = float(ex0._lr), float(ex0._mu)
+        off = 8 * (self.KMAX - K) * self.E  # the launch's losses end where the status words begin
+        a.losses = self.io_ptr + off
+        lh = self.host_io_ptr + off
         if pipe.lists_resident(e0, e1):
             lists, base = pipe.device_lists(e0, e1)
             self.keep = [lists]
             a.lists, a.epoch_base = lists.data_ptr(), base
-            st = _native.lib().bt_mlp_run(C.byref(a), self._lh, self.host_status.data_ptr(), _raw_stream())
+            st = _native.lib().bt_mlp_run(C.byref(a), lh, None, _raw_stream())
         else:  # the epochs' lists are made on the host inside the native call, copied, then the launch
             count = max(e1 - e0 + 1, pipe.EPOCH_WINDOW)
             stage, lists = pipe.reserve_lists(e0, count)
             self.keep = [lists]
             st = _native.lib().bt_mlp_run_sampled(C.byref(a), pipe.seed & (2**64 - 1), pipe.dataset_size,
-                                                  int(pipe.shuffle), e0, count, stage, lists.data_ptr(),
-                                                  self._lh, self.host_status.data_ptr(), _raw_stream())
+                                                  int(pipe.shuffle), e0, count, stage, lists.data_ptr(), lh, None,
+                                                  _raw_stream())
             if st:
                 pipe.drop_lists()
         _native.check(st, "run_minibatch")
+        self.losses_np = self.rows_np[self.KMAX - K:]
         self.dev.invalidate()
         return int(self.status_np[0])
 

@@ -434,8 +434,9 @@ def test_run_steps_sampled_launch_equals_resident_lists(bt):
     assert np.array_equal(pa.view(np.uint64), pb.view(np.uint64))
     fs = engine._fast(a)
     fs.a.K, fs.a.step0 = 40, a.global_step  # crosses into an epoch that is not staged
+    fs.a.losses = fs.io_ptr + 8 * (fs.KMAX - 40) * fs.E
     stage, lists = a.pipeline.reserve_lists(a.global_step // 32, 1)
     st = _native.lib().bt_mlp_run_sampled(C.byref(fs.a), 42, 1024, 1, a.global_step // 32, 1, stage, lists.data_ptr(),
-                                          fs.host_losses.data_ptr(), fs.host_status.data_ptr(), None)
+                                          fs.host_io_ptr + 8 * (fs.KMAX - 40) * fs.E, None, None)
     assert st == 1  # InputError, nothing launched
     a.pipeline.drop_lists()

@@ -54,18 +54,19 @@ from paper_2208_14228_b200 import _native  # noqa: E402
 
 a = fs.a
 a.K = K
+a.losses = fs.io_ptr + 8 * (fs.KMAX - K) * fs.E
 L = _native.lib()
 s = torch.cuda.current_stream()
 res = {}
 res["step_launch_then_sync_us"] = med(lambda: (L.bt_mlp_step(C.byref(a), s.cuda_stream), s.synchronize()))
-res["bt_mlp_run_only_us"] = med(lambda: L.bt_mlp_run(C.byref(a), fs.host_losses.data_ptr(), fs.host_status.data_ptr(),
+res["bt_mlp_run_only_us"] = med(lambda: L.bt_mlp_run(C.byref(a), fs.host_io_ptr + 8 * (fs.KMAX - K) * fs.E, None,
                                                       s.cuda_stream))
 res["empty_sync_us"] = med(lambda: s.synchronize())
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 sp = []
 for _ in range(20):
     e0.record(s)
-    L.bt_mlp_run(C.byref(a), fs.host_losses.data_ptr(), fs.host_status.data_ptr(), s.cuda_stream)
+    L.bt_mlp_run(C.byref(a), fs.host_io_ptr + 8 * (fs.KMAX - K) * fs.E, None, s.cuda_stream)
     e1.record(s)
     e1.synchronize()
     sp.append(e0.elapsed_time(e1) * 1e3)
