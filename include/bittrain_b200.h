@@ -394,6 +394,9 @@ int bt_memcpy_async(void *dst, const void *src, int64_t nbytes, void *stream);
  * (runlog.device_fingerprint = host FNV-1a of these values).                   runlog.py:30-31 */
 int bt_fnv1a64_chunks(const void *data_dev, int64_t nbytes, int64_t chunk, uint64_t *out_dev, void *stream);
 /* Reset a status block to {0, INT32_MAX, 0, 0}. */
+/* measurement helper: write `value` over bytes of buf_dev (16-byte aligned) -- the L2 flush between timed
+ * launches, launched with the step kernels' shared-memory carveout preference */
+int bt_l2_flush(void *buf_dev, int64_t bytes, uint32_t value, void *stream);
 int bt_flags_reset(int32_t *flags_dev, void *stream);
 /* Synchronise `stream`, read the status block; returns its status word. */
 int bt_step_status(const int32_t *flags_dev, int32_t *detail_out, int32_t *step_out, void *stream);

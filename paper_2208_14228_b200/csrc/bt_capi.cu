@@ -31,6 +31,7 @@ int dropout_mask_launch(uint64_t state, int64_t rows, int units, double rate, do
 int replica_check_launch(const void* const* ptrs, int R, int64_t nbytes, int32_t* flags, cudaStream_t s);
 int slot_copy_launch(void* const* dst, const void* const* src, const int64_t* bytes, int count, cudaStream_t s);
 int flags_reset_launch(int32_t* flags, cudaStream_t s);
+int l2_flush_launch(void* buf, int64_t bytes, uint32_t v, cudaStream_t s);
 int tanh_launch(const double* x, int64_t n, double* out, cudaStream_t s);
 int gemm_bf16_tn_launch(const void* a, const void* b, void* c, int batch, int M, int N, int K, int64_t sa,
                         int64_t sb, int64_t sc, int out_bf16, int grid, cudaStream_t s);
@@ -709,6 +710,10 @@ int bt_fnv1a64_chunks(const void* data_dev, int64_t nbytes, int64_t chunk, uint6
   return done(bt::fnv_chunks_launch(data_dev, nbytes, chunk, out_dev, STREAM(stream)), "bt_fnv1a64_chunks");
 }
 
+int bt_l2_flush(void* buf_dev, int64_t bytes, uint32_t value, void* stream) {
+  if (!buf_dev || bytes < 16 || ((uintptr_t)buf_dev & 15)) return fail(bt::ERR_INPUT, "l2 flush buffer");
+  return done(bt::l2_flush_launch(buf_dev, bytes, value, STREAM(stream)), "bt_l2_flush");
+}
 int bt_flags_reset(int32_t* flags_dev, void* stream) {
   return done(bt::flags_reset_launch(flags_dev, STREAM(stream)), "bt_flags_reset");
 }

@@ -111,6 +111,14 @@ __global__ void tanh_kernel(const double* x, int64_t n, double* out) {
     out[i] = glibc_tanh_simt(x[i]);  // the step kernels' tanh
 }
 
+// Measurement helper: overwrite an L2-sized-or-larger buffer (16-byte stores) so the next launch starts
+// with a cold L2.  Launched with the maximum shared-memory carveout preference, the configuration of the
+// step kernels that follow it, so their launch does not also pay an SM shared-memory reconfiguration.
+__global__ void __launch_bounds__(256) l2_flush_kernel(uint4* buf, int64_t n16, uint32_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = make_uint4(v, v, v, v);
+}
+
 __global__ void flags_reset_kernel(int32_t* flags) {
   if (threadIdx.x == 0) {
     flags[FLAG_STATUS] = 0;
@@ -159,6 +167,16 @@ int fnv_chunks_launch(const void* data, int64_t nbytes, int64_t chunk, uint64_t*
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
+int l2_flush_launch(void* buf, int64_t bytes, uint32_t v, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(l2_flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
+      return ERR_CUDA;
+    attr = true;
+  }
+  l2_flush_kernel<<<148 * 8, 256, 0, s>>>((uint4*)buf, bytes / 16, v);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
+}
 int flags_reset_launch(int32_t* flags, cudaStream_t s) {
   flags_reset_kernel<<<1, 32, 0, s>>>(flags);
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
