@@ -751,15 +751,59 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
   }
   cluster_arrive();
   const long long t_p0 = clock64();
-  int bad = a.flags[FLAG_STATUS] != 0 ? 4 : 0;  // a sticky earlier failure: do nothing
-  for (int i = tid; i < BT_P; i += S::T) {
-    const double p0 = a.replicas[i], v0 = a.replicas[BT_P + i];
-    sm[S::PAR + i] = p0;
-    sm[S::VEL + i] = v0;
-    s_rot[i] = a.rot ? a.rot[i] : 0;
-    for (int x = 1; x < a.X; ++x) {  // replica agreement, bytewise (engine.py:246-258)
-      const double* rx = a.replicas + (size_t)x * 2 * BT_P;
-      bad |= (d2u(rx[i]) != d2u(p0)) | (d2u(rx[BT_P + i]) != d2u(v0));
+  // Every global load of the prologue is issued before any is consumed (one HBM round trip after the
+  // L2 is cold, not three): the status word, this thread's parameters / velocity / rotation entries, its
+  // EST-slot and variant-hint words and (sampler mode) its first IPT index-list entries.
+  const int flag0 = a.flags[FLAG_STATUS];
+  constexpr int PPT = (BT_P + S::T - 1) / S::T, IPT = 4;
+  double pp[PPT], pv[PPT];
+  int32_t pr[PPT];
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int i = tid + k * S::T;
+    if (i < BT_P) {
+      pp[k] = a.replicas[i];
+      pv[k] = a.replicas[BT_P + i];
+      pr[k] = a.rot ? a.rot[i] : 0;
+    }
+  }
+  uint64_t l_rng = 0, l_cnt = 0;
+  double l_mean = 0.0;
+  if (tid < S::EPC) {
+    l_rng = a.rng[e0 + tid];
+    l_mean = a.stat_mean[e0 + tid];
+    l_cnt = a.stat_count[e0 + tid];
+  }
+  const int l_fan = tid < S::EL ? a.est_fanin[tid] : F;
+  const int64_t ep0 = a.spe > 0 ? a.step0 / a.spe : 0;
+  const int spe = (int)a.spe, loc0 = (int)(a.step0 - ep0 * a.spe);
+  auto list_entry = [&](int it) -> const int32_t* {  // (mini-batch s, row) -> its index-list entry
+    const int s = it / S::R, rem = it - s * S::R;
+    const int el = rem / S::NB, r = rem - el * S::NB;
+    const int q = loc0 + s, de = q / spe, local = q - de * spe;
+    return a.lists + ((size_t)(ep0 + de - a.epoch_base) * ET + (eb + e0 + el)) * (size_t)(spe * S::NB) +
+           local * S::NB + r;
+  };
+  int32_t iv[IPT];
+  if (!a.rows) {
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int it = tid + k * S::T;
+      if (it < a.K * S::R) iv[k] = *list_entry(it);
+    }
+  }
+  int bad = flag0 != 0 ? 4 : 0;  // a sticky earlier failure: do nothing
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int i = tid + k * S::T;
+    if (i < BT_P) {
+      sm[S::PAR + i] = pp[k];
+      sm[S::VEL + i] = pv[k];
+      s_rot[i] = pr[k];
+      for (int x = 1; x < a.X; ++x) {  // replica agreement, bytewise (engine.py:246-258)
+        const double* rx = a.replicas + (size_t)x * 2 * BT_P;
+        bad |= (d2u(rx[i]) != d2u(pp[k])) | (d2u(rx[BT_P + i]) != d2u(pv[k]));
+      }
     }
   }
   if constexpr (ND > 1) {  // every device's first replica against ours: all devices see the same verdict
@@ -770,14 +814,14 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
         if (a.xrep[q]) bad |= d2u(__ldcg(a.xrep[q] + i)) != mine;
     }
   }
-  for (int el = tid; el < S::EPC; el += S::T) {
-    s_rng[el] = a.rng[e0 + el];
-    sm[S::MEAN + el] = a.stat_mean[e0 + el];
-    s_cnt[el] = a.stat_count[e0 + el];
+  if (tid < S::EPC) {
+    s_rng[tid] = l_rng;
+    sm[S::MEAN + tid] = l_mean;
+    s_cnt[tid] = l_cnt;
   }
   // the launcher's variant hint must hold -- checked for every EST in every CTA, so the whole
   // cluster takes the same exit
-  for (int e = tid; e < S::EL; e += S::T) bad |= (a.est_fanin[e] != F) << 1;
+  bad |= (l_fan != F) << 1;
   const long long t_p1 = clock64();
   long long t_p2 = t_p1;
   if (a.rows) {
@@ -795,17 +839,13 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
       const int64_t nd = a.dataset_rows * BT_ROW;
       for (int64_t i = tid; i < nd; i += S::T) s_data[i] = a.dataset[i];
     }
-    // (epoch, local step) of mini-batch s: one 64-bit division per thread, then 32-bit steps
-    const int64_t ep0 = a.step0 / a.spe;
-    const int spe = (int)a.spe, loc0 = (int)(a.step0 - ep0 * a.spe);
-#pragma unroll 4
-    for (int it = tid; it < a.K * S::R; it += S::T) {  // index loads only: independent, batched
-      const int s = it / S::R, rem = it - s * S::R;
-      const int el = rem / S::NB, r = rem - el * S::NB;
-      const int q = loc0 + s, de = q / spe, local = q - de * spe;
-      const int32_t* lst = a.lists + ((size_t)(ep0 + de - a.epoch_base) * ET + (eb + e0 + el)) * (size_t)(spe * S::NB);
-      s_idx[it] = lst[local * S::NB + r];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int it = tid + k * S::T;
+      if (it < a.K * S::R) s_idx[it] = iv[k];
     }
+#pragma unroll 4
+    for (int it = tid + IPT * S::T; it < a.K * S::R; it += S::T) s_idx[it] = *list_entry(it);  // long launches
     t_p2 = clock64();
     for (int it = tid; it < a.K * S::EPC; it += S::T) {  // one worker stream per (mini-batch, EST)
       const int s = it / S::EPC, el = it - s * S::EPC;
