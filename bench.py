@@ -398,6 +398,55 @@ def bench_reducer(flush, peaks, E=8, S_MB=256, iters=10):
             "variants": {k: {kk: round(vv, 4) for kk, vv in d.items()} for k, d in out.items()}}
 
 
+def bench_reducer_dist(rank: int, world: int, dist, peaks, E=64, S_MB=256, iters=5):
+    """C5 on N GPUs: the guarded peer-memory reducer (paper_2208_14228_b200/peer.py,
+    RankTree(2)) -- each rank folds its E/N EST slots of S MB (f32) into a subtree partial in HBM, the owner
+    of each parameter shard folds the N partials with NVLink peer loads, checks, applies momentum SGD and
+    stores its shard into every replica.  Time = CUDA events on each rank's reducer stream between host
+    barriers, max over ranks.  NVLink_alg = 2 (N-1)/N S per direction per GPU (partials in, shard out);
+    HBM_alg per GPU = (E/N + 1) S (subtree) + ~(N + 6) S/N (owner: partials, param, velocity, staging)."""
+    from paper_2208_14228_b200.hier import RankBuffers
+    from paper_2208_14228_b200.peer import PeerGroupReducer
+
+    n = S_MB * 2**20 // 4
+    E_loc = E // world
+    st = torch.cuda.Stream()
+    g = torch.empty((E_loc, n), dtype=torch.float32, device="cuda").uniform_(-1e-3, 1e-3)
+    loc = RankBuffers(g, torch.zeros(n, dtype=torch.float32, device="cuda"),
+                      torch.zeros(n, dtype=torch.float32, device="cuda"), st)
+    red = PeerGroupReducer(loc, E, "rank_tree2", None, 1e-9, 0.9)
+    times = []
+    for it in range(iters + 2):
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        red.step()
+        e1.record(st)
+        e1.synchronize()
+        if it >= 2:
+            times.append(e0.elapsed_time(e1))
+    red.check()
+    t = torch.tensor([statistics.median(times)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    red.close()
+    del g, loc, red
+    torch.cuda.empty_cache()
+    S = S_MB * 2**20
+    nvl = 2.0 * (world - 1) / world * S
+    hbm = (E_loc + 1) * S + (world + 6) * S / world
+    nvl_peak = 900.0  # GB/s per direction per GPU (NVLink 5 / NVSwitch)
+    t_min = max(hbm / peaks["hbm_gbs"] / 1e6, nvl / nvl_peak / 1e6)
+    return {"kernel": "reduce_fast_kernel (subtree) + owner fold over NVLink peer loads (peer.PeerGroupReducer, "
+                      "RankTree(2), guarded)", "E": E, "S_MB": S_MB, "n_gpus": world, "dtype": "f32",
+            "ms": round(ms, 4), "nvlink_alg_bytes_per_dir": int(nvl), "hbm_alg_bytes": int(hbm),
+            "nvlink_gbs": round(nvl / ms / 1e6, 1), "nvlink_peak_gbs": nvl_peak,
+            "hbm_gbs": round(hbm / ms / 1e6, 1), "hbm_peak_gbs": peaks["hbm_gbs"],
+            "frac_of_roofline": round(t_min / ms, 4), "roofline_ms": round(t_min, 4),
+            "bound": "nvlink" if nvl / nvl_peak > hbm / peaks["hbm_gbs"] else "hbm"}
+
+
 def bench_gemm(flush, peaks, M=8192, N=8192, K=8192, iters=10):
     """SURVEY §8f row 2 brick: the deterministic tcgen05 GEMM (bt_gemm.cu) at 8192^3 bf16 -> bf16,
     against the measured bf16 tensor peak, with cuBLAS (torch.matmul) on the same shape beside it."""
@@ -914,6 +963,12 @@ def main():
     reducer = None
     gemm = None
     bert = None
+    reducer_dist = None
+    if not args.no_reducer and world > 1 and (not shared or os.environ.get("BT_BENCH_C5_SHARED") == "1"):
+        try:  # C5 across the GPUs of this run (NVLink); skipped when ranks share a GPU (no NVLink there)
+            reducer_dist = bench_reducer_dist(rank, world, dist, peaks)
+        except Exception as exc:
+            reducer_dist = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if not args.no_reducer and rank == 0:
         reducer = bench_reducer(flush, peaks)
         gemm = bench_gemm(flush, peaks)
@@ -965,6 +1020,8 @@ def main():
         line["config"]["exchange"] = exchange
     if reducer is not None:
         line["reducer"] = reducer
+    if reducer_dist is not None:
+        line["reducer_nvlink"] = reducer_dist
     if gemm is not None:
         line["gemm"] = gemm
     if bert is not None:
