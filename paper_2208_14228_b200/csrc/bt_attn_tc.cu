@@ -62,9 +62,11 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 // and inv = 1 / sum exp2(x*SC + nm), the sum in column order (exp2 arguments as one FMA; MUFU ex2
 // directly: arguments are <= 0).  The forward and the backward call this same sequence: same bits.
 constexpr float SC = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
+// (The 32-column slice loops are not unrolled: the attention kernels are large and their four CTAs per SM
+// run different phases -- the instruction cache, not the ALU, was the forward's limit.)
 __device__ __forceinline__ void row_stats(uint32_t lane_base, float* nm_out, float* inv_out) {
   float mx = -INFINITY;
-#pragma unroll
+#pragma unroll 1
   for (int c = 0; c < SEQ / 32; ++c) {
     uint32_t v[32];
     tmem_ld32(lane_base + c * 32, v);
@@ -75,12 +77,15 @@ __device__ __forceinline__ void row_stats(uint32_t lane_base, float* nm_out, flo
   const float nm = -__fmul_rn(mx, SC);
   float l[2] = {0.f, 0.f};  // the two 64-column halves, each in column order, then added
 #pragma unroll
-  for (int c = 0; c < SEQ / 32; ++c) {
-    uint32_t v[32];
-    tmem_ld32(lane_base + c * 32, v);
-    tmem_ld_wait();
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll 1
+    for (int c = 2 * h; c < 2 * h + 2; ++c) {
+      uint32_t v[32];
+      tmem_ld32(lane_base + c * 32, v);
+      tmem_ld_wait();
 #pragma unroll
-    for (int q = 0; q < 32; ++q) l[c >> 1] += ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm));
+      for (int q = 0; q < 32; ++q) l[h] += ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm));
+    }
   }
   *nm_out = nm;
   *inv_out = 1.f / (l[0] + l[1]);
@@ -197,8 +202,8 @@ __global__ void __launch_bounds__(THREADS, 4)
     const uint64_t nb = ((((uint64_t)step * a.L + a.layer) * a.seqs_per_est + sl) * a.H + h) * (uint64_t)(SEQ * SEQ / 4) +
                         (uint64_t)((tid >> 4) * 8 + (tid & 7)) * 64;
     uint8_t* const prow = gbase + OFF_P + tid * 128;
-    uint32_t kbits[SEQ / 32];
-#pragma unroll
+    uint32_t* const kbits = a.mbits ? a.mbits + ((size_t)it * SEQ + tid) * 4 : nullptr;
+#pragma unroll 1
     for (int c = 0; c < SEQ / 32; ++c) {  // 32 columns = 16 column pairs; this lane draws 8, its partner 8
       uint32_t v[32];
       tmem_ld32(lane_base + c * 32, v);
@@ -228,10 +233,8 @@ __global__ void __launch_bounds__(THREADS, 4)
         const int chunk = (c & 1) * 4 + cc;  // 16-byte chunk within the 128-byte row of k-block kb
         *(uint4*)(prow + kb * 16384 + ((chunk ^ (tid & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
-      kbits[c] = bits;
+      if (kbits) kbits[c] = bits;  // the keep bits for the backward (which then draws nothing)
     }
-    // the keep bits for the backward (which then draws nothing): 16 bytes per row
-    if (a.mbits) *(uint4*)(a.mbits + ((size_t)it * SEQ + tid) * 4) = make_uint4(kbits[0], kbits[1], kbits[2], kbits[3]);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
     tc_fence_before();
     __syncthreads();
