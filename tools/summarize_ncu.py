@@ -32,7 +32,7 @@ def launches(src="launches.csv", dst="launches"):
         agg[name][0] += 1
         agg[name][1] += float(r[v_i].replace(",", ""))
     tot = sum(v[1] for v in agg.values())
-    setup = ("jitter_gather", "make_dataset", "init_random", "flags_reset", "at::", "dropout_mask")
+    setup = ("jitter_gather", "make_dataset", "init_random", "flags_reset", "at::", "dropout_mask", "l2_flush")
     step_tot = sum(v[1] for k, v in agg.items() if not any(x in k for x in setup)) or 1.0
     lines = [f"# ncu launch list ({path.name}): gpu__time_duration.sum per kernel, --clock-control none",
              f"# cold-cache, serialised launches: compare SHARES, not absolute times",
