@@ -191,7 +191,11 @@ class DataPipeline:
         if self._stage_used[i]:
             self._stage_ev[i].synchronize()
         self._stage_used[i] = False  # the native call synchronises its stream before returning
-        view = self._devbuf[i][:n].view(count, self.total_workers, self.steps_per_epoch * self.micro_batch)
+        key = (i, count)  # the views are cached: a tensor view per call costs microseconds on the e2e path
+        view = self._views.get(key)
+        if view is None:
+            view = self._views[key] = self._devbuf[i][:n].view(count, self.total_workers,
+                                                               self.steps_per_epoch * self.micro_batch)
         self._lists_dev, self._lists_dev_base, self._lists_dev_count = view, first_epoch, count
         return self._stageptr[i], view
 
@@ -207,6 +211,7 @@ class DataPipeline:
         self._stage_ev = [torch.cuda.Event(), torch.cuda.Event()]
         self._stage_used = [False, False]
         self._stage_i = 0
+        self._views = {}
 
     def device_lists(self, first_epoch: int, last_epoch: int) -> tuple[torch.Tensor, int]:
         """Resident [n_epochs][workers][spe*B] lists covering [first, last]; returns (tensor, base epoch)."""
