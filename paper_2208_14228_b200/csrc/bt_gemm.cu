@@ -875,6 +875,158 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
   }
 }
 
+// Weight gradient of the 3x3 / stride-1 / pad-1 convolution with 64 input and 64 output channels at
+// W = 32 (ResNet layer 1) by halo boxes instead of im2col loads.  dW_z[co][(kh, kw, ci)] =
+// sum_pixels dz[pix][co] x[pix + (kh-1, kw-1)][ci] over batch entry z's pixels (an EST's pinned split).
+// A tile is (z, kw): the MMA's B operand for the three kh taps is ONE MN-major view of N = 192 over a
+// {64 ch, 32 px from kw-1, 4 rows from h0-1} halo box -- the kh views are 32 pixel rows (4 KB) apart, a
+// uniform distance between 64-wide N blocks, so one UMMA (M 128, N 192, K 16) per k-step covers the
+// three taps.  Per 64-pixel k-block a tile loads 8 KB of dz and 16 KB of x (the im2col form loaded a
+// 16 KB dz box per 128-column tile and 8 KB per tap: 160 KB per k-block for the nine taps, against
+// 72 KB here).  dz is the A operand with M = 128 (rows 64-127 a zero block written once per stage,
+// as the im2col form's zero-filled half), K ascending in 16-wide steps as there: the same products in
+// the same order per output element.
+constexpr int WGH_THREADS = 64 + 256, WGH_STAGES = 6, WGH_N = 192;
+struct WghSmem {
+  static constexpr int A = 2 * MN_BLOCK_BYTES;  // dz: M block 0 (co 0-63) loaded, block 1 zero
+  static constexpr int B = 4 * 32 * 128;        // one kw box: 4 rows x 32 px x 64 ch bf16
+  static constexpr int STAGE = A + B;
+  static constexpr int BAR = WGH_STAGES * STAGE;  // full[S], empty[S], tfull[2], tempty[2], tmem slot
+  static constexpr int TOTAL = BAR + (2 * WGH_STAGES + 4) * 8 + 16;
+};
+__device__ __forceinline__ uint64_t mn_desc_lbo(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__global__ void __launch_bounds__(WGH_THREADS, 1)
+    conv_wgrad_halo_kernel(const __grid_constant__ CUtensorMap map_dz, const __grid_constant__ CUtensorMap map_x,
+                           float* __restrict__ out, int batch, int rpb, int H, int64_t sc) {
+  using L = WghSmem;
+  constexpr int W = 32, K = 9 * 64;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw), base = (raw + 1023u) & ~1023u;
+  uint8_t* const gbase = smem_raw + (base - raw);
+  const uint32_t bar0 = base + L::BAR;
+  auto full = [&](int st) { return bar0 + 8u * st; };
+  auto empty = [&](int st) { return bar0 + 8u * (WGH_STAGES + st); };
+  auto tfull = [&](int a) { return bar0 + 8u * (2 * WGH_STAGES + a); };
+  auto tempty = [&](int a) { return bar0 + 8u * (2 * WGH_STAGES + 2 + a); };
+  uint32_t* const tmem_slot = (uint32_t*)(gbase + L::BAR + (2 * WGH_STAGES + 4) * 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles = batch * 3, kbn = rpb / 64;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_dz) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+    for (int st = 0; st < WGH_STAGES; ++st) {
+      mbar_init(full(st), 1);
+      mbar_init(empty(st), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), 8);  // one arrival per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp >= 2) {  // the A operand's second M block (output rows 64-127) is zero in every stage
+    for (int st = 0; st < WGH_STAGES; ++st) {
+      uint4* zb = (uint4*)(gbase + st * L::STAGE + MN_BLOCK_BYTES);
+      for (int i = threadIdx.x - 64; i < MN_BLOCK_BYTES / 16; i += 256) zb[i] = make_uint4(0, 0, 0, 0);
+    }
+    fence_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer: per k-block the dz box and the kw halo box
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int z = t / 3, kw = t - z * 3;
+        for (int kb = 0; kb < kbn; ++kb) {
+          mbar_wait(empty(stage), phase ^ 1u);
+          const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A;
+          mbar_arrive_expect_tx(full(stage), MN_BLOCK_BYTES + L::B);
+          tma_load_3d(sa, &map_dz, 0, kb * BK, z, full(stage));
+          const int q0 = z * rpb + kb * BK, n = q0 / (H * W), h0 = (q0 - n * H * W) / W;
+          tma_load_4d_tile(sb, &map_x, 0, kw - 1, h0 - 1, n, full(stage));
+          if (++stage == WGH_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer: one M 128 x N 192 UMMA per 16-pixel k-step (the three kh taps)
+      constexpr uint32_t idesc = idesc_bf16(BM, WGH_N, true, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      int i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int acc = i & 1;
+        mbar_wait(tempty(acc), ((i >> 1) & 1) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(acc * 256);
+        for (int kb = 0; kb < kbn; ++kb) {
+          mbar_wait(full(stage), phase);
+          tc_fence_after();
+          const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A;
+          const uint64_t da = mn_desc_lbo(sa, MN_BLOCK_BYTES), db = mn_desc_lbo(sb, 32 * 128);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            tc_mma(d, da + (uint64_t)k * (2048 >> 4), db + (uint64_t)k * (2048 >> 4), idesc, (kb | k) != 0);
+          tc_commit(empty(stage));
+          if (++stage == WGH_STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        tc_commit(tfull(acc));
+      }
+    }
+  } else {  // ---- epilogue: TMEM lanes 0-63 hold the 64 output channels; 192 columns = (kh, ci)
+    const int lg = warp & 3, half = (warp - 2) >> 2;
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int acc = i & 1, z = t / 3, kw = t - z * 3;
+      mbar_wait(tfull(acc), (i >> 1) & 1);
+      tc_fence_after();
+      if (lg < 2) {
+        const int co = lg * 32 + lane;
+        float* const orow = out + (size_t)z * sc + (size_t)co * K;
+#pragma unroll 1
+        for (int cc = 0; cc < 3; ++cc) {
+          const int col = half * 96 + cc * 32, kh = col >> 6, ci0 = col & 63;
+          uint32_t v[32];
+          tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 256 + col), v);
+          tmem_ld_wait();
+          float4* o = (float4*)(orow + (kh * 3 + kw) * 64 + ci0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            o[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                               __uint_as_float(v[4 * q + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty(acc));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
 }  // namespace gemm
 
 // ---------------------------------------------------------------- launcher
@@ -975,6 +1127,38 @@ static bool make_halo_map(CUtensorMap* map, const void* x, int N, int H, int W) 
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// the weight-gradient halo map: [N][H][32][64] bf16, box {64, 32, 4, 1} (two output rows + the halo rows)
+static bool make_wg_halo_map(CUtensorMap* map, const void* x, int N, int H) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {64, 32, (cuuint64_t)H, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {128, 32 * 128, (cuuint64_t)H * 32 * 128};
+  const cuuint32_t box[4] = {64, 32, 4, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static int launch_conv_wgrad_halo(const void* x, int N, int H, const void* dz, float* c, int batch, int rpb,
+                                  int64_t sc, cudaStream_t s) {
+  CUtensorMap mdz, mx;
+  if (!make_map_mn(&mdz, dz, 64, rpb, batch, (int64_t)rpb * 64) || !make_wg_halo_map(&mx, x, N, H)) return ERR_CUDA;
+  const int smem = gemm::WghSmem::TOTAL + 1024;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gemm::conv_wgrad_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return ERR_CUDA;
+    attr = true;
+  }
+  const int tiles = batch * 3;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  gemm::conv_wgrad_halo_kernel<<<tiles < sms ? tiles : sms, gemm::WGH_THREADS, smem, s>>>(mdz, mx, c, batch, rpb, H,
+                                                                                         sc);
+  return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 template <int W, bool OUT_BF16>
 static int launch_conv_halo(const void* x, int N, int H, const void* w, void* c, int Co, cudaStream_t s) {
@@ -1190,6 +1374,10 @@ int gemm_conv_launch(int wgrad, const void* x, int xN, int xH, int xW, int Ci, i
   g.sc = sc;
   g.mn = true;
   g.aim = 2;
+  // 3x3 / stride 1 / pad 1, 64 -> 64 channels at W = 32 (layer 1): the halo form (three taps per UMMA)
+  if (Ci == 64 && Co == 64 && KH == 3 && KW == 3 && stride == 1 && pad == 1 && xW == 32 && Wo == 32 && Ho == xH &&
+      rows_per_batch % gemm::BK == 0 && !out_bf16 && getenv("BT_CONV_WG_HALO0") == nullptr)
+    return launch_conv_wgrad_halo(x, xN, xH, other, (float*)c, batch, rows_per_batch, sc, s);
   // whole 256 x 256 CTA-pair tiles (Co, KH*KW*Ci multiples of 256): half the operand bytes per flop
   if (Co % gemm::PAIR_M == 0 && K % gemm::PAIR_BN == 0 && getenv("BT_CONV_WG_PAIR0") == nullptr) {
     constexpr int SP = gemm::EPI_WARPS == 8 ? 5 : 3;
