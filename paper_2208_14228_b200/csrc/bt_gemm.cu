@@ -875,21 +875,24 @@ __global__ void __launch_bounds__(HALO_THREADS, 1)
   }
 }
 
-// Weight gradient of the 3x3 / stride-1 / pad-1 convolution with 64 input and 64 output channels at
-// W = 32 (ResNet layer 1) by halo boxes instead of im2col loads.  dW_z[co][(kh, kw, ci)] =
+// Weight gradient of the 3x3 / stride-1 / pad-1 convolution with 64 or 128 input and output channels
+// at W = 32 / 16 (ResNet layers 1 and 2) by halo boxes instead of im2col loads.  dW_z[co][(kh, kw, ci)] =
 // sum_pixels dz[pix][co] x[pix + (kh-1, kw-1)][ci] over batch entry z's pixels (an EST's pinned split).
-// A tile is (z, kw): the MMA's B operand for the three kh taps is ONE MN-major view of N = 192 over a
-// {64 ch, 32 px from kw-1, 4 rows from h0-1} halo box -- the kh views are 32 pixel rows (4 KB) apart, a
-// uniform distance between 64-wide N blocks, so one UMMA (M 128, N 192, K 16) per k-step covers the
-// three taps.  Per 64-pixel k-block a tile loads 8 KB of dz and 16 KB of x (the im2col form loaded a
-// 16 KB dz box per 128-column tile and 8 KB per tap: 160 KB per k-block for the nine taps, against
-// 72 KB here).  dz is the A operand with M = 128 (rows 64-127 a zero block written once per stage,
-// as the im2col form's zero-filled half), K ascending in 16-wide steps as there: the same products in
-// the same order per output element.
+// A tile is (z, kw, 64-channel block cb): the MMA's B operand for the three kh taps is ONE MN-major view
+// of N = 192 over a {64 ch, W px from kw-1, 64/W + 2 rows from h0-1} halo box -- the kh views are W pixel
+// rows (W * 128 bytes, a multiple of 1 KB) apart, a uniform distance between 64-wide N blocks, so one UMMA
+// (M 128, N 192, K 16) per k-step covers the three taps.  Per 64-pixel k-block a tile loads the dz box
+// (8 KB per 64 output channels) and one halo box (8 + 16 KB / W... 16 KB at W = 32, 12 KB at W = 16);
+// the im2col form loaded a 16 KB dz box per 128-column tile and 8 KB per (tap, channel block).  dz is
+// the A operand with M = 128 (with 64 output channels rows 64-127 are a zero block written once per
+// stage, as the im2col form's zero-filled half), K ascending in 16-wide steps as there: the same products
+// in the same order per output element, the same bits (tests/test_gpu_resnet.py).
 constexpr int WGH_THREADS = 64 + 256, WGH_STAGES = 6, WGH_N = 192;
+template <int W>
 struct WghSmem {
-  static constexpr int A = 2 * MN_BLOCK_BYTES;  // dz: M block 0 (co 0-63) loaded, block 1 zero
-  static constexpr int B = 4 * 32 * 128;        // one kw box: 4 rows x 32 px x 64 ch bf16
+  static constexpr int ROWS = BK / W + 2;        // halo rows per box
+  static constexpr int A = 2 * MN_BLOCK_BYTES;  // dz: M blocks 0 / 1 (zero when Co = 64)
+  static constexpr int B = ROWS * W * 128;      // one (kw, channel block) box: ROWS x W px x 64 ch bf16
   static constexpr int STAGE = A + B;
   static constexpr int BAR = WGH_STAGES * STAGE;  // full[S], empty[S], tfull[2], tempty[2], tmem slot
   static constexpr int TOTAL = BAR + (2 * WGH_STAGES + 4) * 8 + 16;
@@ -898,11 +901,11 @@ __device__ __forceinline__ uint64_t mn_desc_lbo(uint32_t saddr, uint32_t lbo) {
   return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+template <int W>
 __global__ void __launch_bounds__(WGH_THREADS, 1)
     conv_wgrad_halo_kernel(const __grid_constant__ CUtensorMap map_dz, const __grid_constant__ CUtensorMap map_x,
-                           float* __restrict__ out, int batch, int rpb, int H, int64_t sc) {
-  using L = WghSmem;
-  constexpr int W = 32, K = 9 * 64;
+                           float* __restrict__ out, int batch, int rpb, int H, int64_t sc, int Ci, int Co) {
+  using L = WghSmem<W>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw), base = (raw + 1023u) & ~1023u;
   uint8_t* const gbase = smem_raw + (base - raw);
@@ -913,7 +916,8 @@ __global__ void __launch_bounds__(WGH_THREADS, 1)
   auto tempty = [&](int a) { return bar0 + 8u * (2 * WGH_STAGES + 2 + a); };
   uint32_t* const tmem_slot = (uint32_t*)(gbase + L::BAR + (2 * WGH_STAGES + 4) * 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles = batch * 3, kbn = rpb / 64;
+  const int cbn = Ci / 64, mbn = Co / 64, K = 9 * Ci;
+  const int tiles = batch * 3 * cbn, kbn = rpb / BK;
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_dz) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
@@ -932,7 +936,7 @@ __global__ void __launch_bounds__(WGH_THREADS, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (warp >= 2) {  // the A operand's second M block (output rows 64-127) is zero in every stage
+  if (warp >= 2 && mbn == 1) {  // 64 output channels: the A operand's second M block is zero in every stage
     for (int st = 0; st < WGH_STAGES; ++st) {
       uint4* zb = (uint4*)(gbase + st * L::STAGE + MN_BLOCK_BYTES);
       for (int i = threadIdx.x - 64; i < MN_BLOCK_BYTES / 16; i += 256) zb[i] = make_uint4(0, 0, 0, 0);
@@ -944,18 +948,18 @@ __global__ void __launch_bounds__(WGH_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer: per k-block the dz box and the kw halo box
+    if (lane == 0) {  // ---- TMA producer: per k-block the dz box(es) and the (kw, channel block) halo box
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int z = t / 3, kw = t - z * 3;
+        const int z = t / (3 * cbn), r = t - z * 3 * cbn, kw = r / cbn, cb = r - kw * cbn;
         for (int kb = 0; kb < kbn; ++kb) {
           mbar_wait(empty(stage), phase ^ 1u);
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A;
-          mbar_arrive_expect_tx(full(stage), MN_BLOCK_BYTES + L::B);
-          tma_load_3d(sa, &map_dz, 0, kb * BK, z, full(stage));
+          mbar_arrive_expect_tx(full(stage), mbn * MN_BLOCK_BYTES + L::B);
+          for (int j = 0; j < mbn; ++j) tma_load_3d(sa + j * MN_BLOCK_BYTES, &map_dz, 64 * j, kb * BK, z, full(stage));
           const int q0 = z * rpb + kb * BK, n = q0 / (H * W), h0 = (q0 - n * H * W) / W;
-          tma_load_4d_tile(sb, &map_x, 0, kw - 1, h0 - 1, n, full(stage));
+          tma_load_4d_tile(sb, &map_x, cb * 64, kw - 1, h0 - 1, n, full(stage));
           if (++stage == WGH_STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -978,7 +982,7 @@ __global__ void __launch_bounds__(WGH_THREADS, 1)
           mbar_wait(full(stage), phase);
           tc_fence_after();
           const uint32_t sa = base + stage * L::STAGE, sb = sa + L::A;
-          const uint64_t da = mn_desc_lbo(sa, MN_BLOCK_BYTES), db = mn_desc_lbo(sb, 32 * 128);
+          const uint64_t da = mn_desc_lbo(sa, MN_BLOCK_BYTES), db = mn_desc_lbo(sb, W * 128);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)
             tc_mma(d, da + (uint64_t)k * (2048 >> 4), db + (uint64_t)k * (2048 >> 4), idesc, (kb | k) != 0);
@@ -991,14 +995,14 @@ __global__ void __launch_bounds__(WGH_THREADS, 1)
         tc_commit(tfull(acc));
       }
     }
-  } else {  // ---- epilogue: TMEM lanes 0-63 hold the 64 output channels; 192 columns = (kh, ci)
+  } else {  // ---- epilogue: TMEM lane = output channel; 192 columns = (kh, ci of block cb)
     const int lg = warp & 3, half = (warp - 2) >> 2;
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-      const int acc = i & 1, z = t / 3, kw = t - z * 3;
+      const int acc = i & 1, z = t / (3 * cbn), r = t - z * 3 * cbn, kw = r / cbn, cb = r - kw * cbn;
       mbar_wait(tfull(acc), (i >> 1) & 1);
       tc_fence_after();
-      if (lg < 2) {
+      if (lg < 2 * mbn) {
         const int co = lg * 32 + lane;
         float* const orow = out + (size_t)z * sc + (size_t)co * K;
 #pragma unroll 1
@@ -1007,7 +1011,7 @@ __global__ void __launch_bounds__(WGH_THREADS, 1)
           uint32_t v[32];
           tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 256 + col), v);
           tmem_ld_wait();
-          float4* o = (float4*)(orow + (kh * 3 + kw) * 64 + ci0);
+          float4* o = (float4*)(orow + (kh * 3 + kw) * Ci + cb * 64 + ci0);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             o[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
@@ -1128,36 +1132,39 @@ static bool make_halo_map(CUtensorMap* map, const void* x, int N, int H, int W) 
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-// the weight-gradient halo map: [N][H][32][64] bf16, box {64, 32, 4, 1} (two output rows + the halo rows)
-static bool make_wg_halo_map(CUtensorMap* map, const void* x, int N, int H) {
+// the weight-gradient halo map: [N][H][W][C] bf16, box {64 ch, W px, 64/W + 2 rows, 1} (the k-block's
+// output rows + the halo rows)
+static bool make_wg_halo_map(CUtensorMap* map, const void* x, int N, int H, int W, int C) {
   PFN_encodeTiled enc = encode_fn();
   if (!enc) return false;
-  const cuuint64_t dims[4] = {64, 32, (cuuint64_t)H, (cuuint64_t)N};
-  const cuuint64_t strides[3] = {128, 32 * 128, (cuuint64_t)H * 32 * 128};
-  const cuuint32_t box[4] = {64, 32, 4, 1};
+  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  const cuuint32_t box[4] = {64, (cuuint32_t)W, (cuuint32_t)(gemm::BK / W + 2), 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-static int launch_conv_wgrad_halo(const void* x, int N, int H, const void* dz, float* c, int batch, int rpb,
-                                  int64_t sc, cudaStream_t s) {
+template <int W>
+static int launch_conv_wgrad_halo(const void* x, int N, int H, int Ci, const void* dz, float* c, int Co, int batch,
+                                  int rpb, int64_t sc, cudaStream_t s) {
   CUtensorMap mdz, mx;
-  if (!make_map_mn(&mdz, dz, 64, rpb, batch, (int64_t)rpb * 64) || !make_wg_halo_map(&mx, x, N, H)) return ERR_CUDA;
-  const int smem = gemm::WghSmem::TOTAL + 1024;
+  if (!make_map_mn(&mdz, dz, Co, rpb, batch, (int64_t)rpb * Co) || !make_wg_halo_map(&mx, x, N, H, W, Ci))
+    return ERR_CUDA;
+  const int smem = gemm::WghSmem<W>::TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(gemm::conv_wgrad_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+    if (cudaFuncSetAttribute(gemm::conv_wgrad_halo_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
         cudaSuccess)
       return ERR_CUDA;
     attr = true;
   }
-  const int tiles = batch * 3;
+  const int tiles = batch * 3 * (Ci / 64);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  gemm::conv_wgrad_halo_kernel<<<tiles < sms ? tiles : sms, gemm::WGH_THREADS, smem, s>>>(mdz, mx, c, batch, rpb, H,
-                                                                                         sc);
+  gemm::conv_wgrad_halo_kernel<W><<<tiles < sms ? tiles : sms, gemm::WGH_THREADS, smem, s>>>(mdz, mx, c, batch, rpb, H,
+                                                                                            sc, Ci, Co);
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 template <int W, bool OUT_BF16>
@@ -1374,10 +1381,13 @@ int gemm_conv_launch(int wgrad, const void* x, int xN, int xH, int xW, int Ci, i
   g.sc = sc;
   g.mn = true;
   g.aim = 2;
-  // 3x3 / stride 1 / pad 1, 64 -> 64 channels at W = 32 (layer 1): the halo form (three taps per UMMA)
-  if (Ci == 64 && Co == 64 && KH == 3 && KW == 3 && stride == 1 && pad == 1 && xW == 32 && Wo == 32 && Ho == xH &&
-      rows_per_batch % gemm::BK == 0 && !out_bf16 && getenv("BT_CONV_WG_HALO0") == nullptr)
-    return launch_conv_wgrad_halo(x, xN, xH, other, (float*)c, batch, rows_per_batch, sc, s);
+  // 3x3 / stride 1 / pad 1, 64 or 128 channels in and out at W = 32 / 16 (layers 1 and 2): the halo form
+  // (three taps per UMMA)
+  if ((Ci == 64 || Ci == 128) && (Co == 64 || Co == 128) && KH == 3 && KW == 3 && stride == 1 && pad == 1 &&
+      (xW == 32 || xW == 16) && Wo == xW && Ho == xH && rows_per_batch % gemm::BK == 0 && !out_bf16 &&
+      getenv("BT_CONV_WG_HALO0") == nullptr)
+    return xW == 32 ? launch_conv_wgrad_halo<32>(x, xN, xH, Ci, other, (float*)c, Co, batch, rows_per_batch, sc, s)
+                    : launch_conv_wgrad_halo<16>(x, xN, xH, Ci, other, (float*)c, Co, batch, rows_per_batch, sc, s);
   // whole 256 x 256 CTA-pair tiles (Co, KH*KW*Ci multiples of 256): half the operand bytes per flop
   if (Co % gemm::PAIR_M == 0 && K % gemm::PAIR_BN == 0 && getenv("BT_CONV_WG_PAIR0") == nullptr) {
     constexpr int SP = gemm::EPI_WARPS == 8 ? 5 : 3;

@@ -477,34 +477,38 @@ def test_prepared_rescale_replays_staged_graphs_and_reenters_layouts(rn):
     assert torch.equal(sa["cursor"], sb["cursor"]) and int(sa["cursor"][0]) == 10
 
 
-@pytest.mark.parametrize("n_img,rpb", [(4, 2048), (2, 1024), (3, 1024)])
-def test_weight_gradient_halo_equals_im2col_path(n_img, rpb, monkeypatch):
-    """The layer-1 weight gradient in halo form (per (split, kw): a {64 ch, 32 px, 4 rows} box whose three
-    kh views, 4 KB apart, are ONE N = 192 MN-major operand) issues the im2col form's products in the same
-    K order per output element: identical fp32 bits, including splits that straddle images."""
+@pytest.mark.parametrize("n_img,rpb,hw,ci,co", [(4, 2048, 32, 64, 64), (2, 1024, 32, 64, 64), (3, 1024, 32, 64, 64),
+                                               (8, 512, 16, 128, 128), (6, 256, 16, 128, 128), (4, 512, 16, 64, 128),
+                                               (2, 1024, 32, 128, 64)])
+def test_weight_gradient_halo_equals_im2col_path(n_img, rpb, hw, ci, co, monkeypatch):
+    """The 3x3 / stride-1 weight gradient in halo form (per (split, kw, 64-channel block): a {64 ch, W px,
+    64/W + 2 rows} box whose three kh views, W rows apart, are ONE N = 192 MN-major operand) issues the
+    im2col form's products in the same K order per output element: identical fp32 bits at W = 32 / 16,
+    64 / 128 channels in and out, including splits that straddle images."""
     from paper_2208_14228_b200 import _native
     from paper_2208_14228_b200.device import stream
 
     L = _native.lib()
-    H = W = 32
-    g = torch.Generator(device="cuda").manual_seed(n_img * 7 + rpb)
-    x = torch.randn(n_img, H, W, 64, device="cuda", generator=g).to(torch.bfloat16)
-    dz = (torch.randn(n_img * H * W, 64, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    H = W = hw
+    g = torch.Generator(device="cuda").manual_seed(n_img * 7 + rpb + ci + co)
+    x = torch.randn(n_img, H, W, ci, device="cuda", generator=g).to(torch.bfloat16)
+    dz = (torch.randn(n_img * H * W, co, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
     batch = n_img * H * W // rpb
+    K = 9 * ci
     outs = []
     for halo in (True, False):
         if halo:
             monkeypatch.delenv("BT_CONV_WG_HALO0", raising=False)
         else:
             monkeypatch.setenv("BT_CONV_WG_HALO0", "1")
-        c = torch.full((batch, 64, 9 * 64), float("nan"), device="cuda")
-        _native.check(L.bt_gemm_conv(1, x.data_ptr(), n_img, H, W, 64, H, W, 3, 3, 1, 1, dz.data_ptr(), c.data_ptr(),
-                                     64, batch, rpb, 64 * 9 * 64, 0, stream()))
+        c = torch.full((batch, co, K), float("nan"), device="cuda")
+        _native.check(L.bt_gemm_conv(1, x.data_ptr(), n_img, H, W, ci, H, W, 3, 3, 1, 1, dz.data_ptr(), c.data_ptr(),
+                                     co, batch, rpb, co * K, 0, stream()))
         outs.append(c)
     torch.cuda.synchronize()
     assert not torch.isnan(outs[0]).any()
-    ref = torch.einsum("bpo,bpk->bok", dz.float().view(batch, rpb, 64),
+    ref = torch.einsum("bpo,bpk->bok", dz.float().view(batch, rpb, co),
                        torch.stack([Fn.pad(x.float(), (0, 0, 1, 1, 1, 1))[:, kh:kh + H, kw:kw + W, :]
-                                    for kh in range(3) for kw in range(3)], 3).view(batch, rpb, 9 * 64))
+                                    for kh in range(3) for kw in range(3)], 3).view(batch, rpb, K))
     assert ((outs[0] - ref).norm() / ref.norm()).item() < 1e-5
     assert torch.equal(outs[0].view(torch.int32), outs[1].view(torch.int32))
