@@ -405,9 +405,11 @@ class BertJob:
             capture["ytop_b"] = ws["ytop"].clone()
 
     # ------------------------------------------------------------------ step
-    def step(self, groups: list[int] | None = None, capture: dict | None = None) -> torch.Tensor:
+    def step(self, groups: list[int] | None = None, capture: dict | None = None, check: bool = True) -> torch.Tensor:
         """One mini-batch of this process's ESTs; `groups` = EST counts per launch group (default: one group).
-        Returns the local per-EST losses [est_count] (fp32, on device)."""
+        Returns the local per-EST losses [est_count] (fp32, on device).  check=False defers the host-side
+        non-finite check (no per-step synchronisation; `check_status()` later): the update is guarded on the
+        device either way -- a non-finite step and every step after it leave the weights unchanged."""
         groups = groups or [self.En]
         if sum(groups) != self.En or min(groups) < 1 or any(n % self.g for n in groups):
             raise ConfigError(f"groups {groups} must partition {self.En} ESTs into whole gradient leaves of {self.g}")
@@ -420,11 +422,11 @@ class BertJob:
                     self._body(groups, self._gloss)
                 self._graph = g
             self._graph.replay()
-            self._post()
+            self._post(check)
             return self._gloss.clone()
         losses = torch.empty(self.En, dtype=torch.float32, device="cuda")
         self._body(groups, losses, capture)
-        self._post()
+        self._post(check)
         self._gwarm = self._gwarm or replay
         return losses
 
@@ -440,9 +442,14 @@ class BertJob:
         self._refresh_bf16()
         self._step_dev.add_(1)
 
-    def _post(self):
+    def _post(self, check: bool = True):
         """Host side of a step: the non-finite check (one status read) and the step count."""
         self.step_idx += 1
+        if check:
+            self.check_status()
+
+    def check_status(self):
+        """The non-finite check of every step since the last one (the status words are sticky)."""
         if self.peer is not None:
             self.peer.check()
             return

@@ -491,7 +491,7 @@ class ResNetJob:
         sl["cursor"].add_(1)  # every EST of the group consumed one micro-batch
 
     # ------------------------------------------------------------ step
-    def step(self, capture: dict | None = None) -> torch.Tensor:
+    def step(self, capture: dict | None = None, check: bool = True) -> torch.Tensor:
         """One mini-batch of this process's ESTs on the current layout; per-EST losses [est_count].
         After one eager step on a layout, the whole step (every launch group, the reducer, the weight
         refresh, the cursor advance) is captured as a CUDA graph and replayed until the next rescale."""
@@ -501,11 +501,11 @@ class ResNetJob:
                 self._graph = self._capture(self.G)
             g, gloss = self._graph
             g.replay()
-            self._post()
+            self._post(check)
             return gloss.clone()
         losses = torch.empty(self.En, dtype=torch.float32, device="cuda")
         self._body(losses, capture)
-        self._post()
+        self._post(check)
         self._gwarm = self._gwarm or replay
         return losses
 
@@ -531,9 +531,14 @@ class ResNetJob:
             _native.check(_native.lib().bt_reduce_update(C.byref(a), stream()), "resnet reduce_update")
         self._refresh_bf16()
 
-    def _post(self):
+    def _post(self, check: bool = True):
         """Host side of a step: the non-finite check (one status read) and the step count."""
         self.step_idx += 1
+        if check:
+            self.check_status()
+
+    def check_status(self):
+        """The non-finite check of every step since the last one (the status words are sticky)."""
         if self.peer is not None:
             self.peer.check()
             return

@@ -534,3 +534,26 @@ def test_run_logs_fingerprint_and_bitdiff(bert):
     p = a.params.clone()
     p[12345] = float(np.nextafter(np.float32(p[12345].item()), np.float32(2.0)))
     assert device_fingerprint(p) != la.records[-1].param_hash
+
+
+def test_deferred_status_check_keeps_weights(bert):
+    """step(check=False) skips the per-step host synchronisation; the update stays guarded on the device: a
+    non-finite step and every step after it leave weights and momentum bit-for-bit unchanged, and the next
+    check_status() raises NumericError (the status words are sticky)."""
+    from paper_2208_14228_b200.errors import NumericError
+
+    job = bert.BertJob(**SMALL)
+    job.step()
+    job.step(check=False)
+    job.check_status()  # finite steps: nothing to report
+    job.view(0, "Wo")[0, 0] = float("nan")
+    job._refresh_bf16()
+    p0, v0 = job.params.clone(), job.vel.clone()
+    for _ in range(3):
+        job.step(check=False)
+    torch.cuda.synchronize()
+    assert torch.equal(job.params.view(torch.int32), p0.view(torch.int32))
+    assert torch.equal(job.vel.view(torch.int32), v0.view(torch.int32))
+    with pytest.raises(NumericError):
+        job.check_status()
+    job.check_status()  # reset by the raise

@@ -9,8 +9,9 @@ import torch  # noqa: E402
 
 from paper_2208_14228_b200.bert import BertJob  # noqa: E402
 
-for E in (8, 4):
-    for graph in (True, False):
+for E, graph, CHECK in ((8, True, True), (8, False, True), (8, False, False), (4, True, True), (4, False, True),
+                        (4, False, False)):
+    if True:
         job = BertJob(ests=E, est_group=4, fanin=2, graph=graph)
         for _ in range(3):
             job.step()
@@ -19,10 +20,12 @@ for E in (8, 4):
         t0 = time.perf_counter()
         e0.record()
         for _ in range(5):
-            job.step()
+            job.step(check=CHECK)
         e1.record()
         host = (time.perf_counter() - t0) / 5 * 1e3
         e1.synchronize()
-        print(f"E={E} graph={graph}: {e0.elapsed_time(e1) / 5:.2f} ms/step (host enqueue {host:.2f} ms/step)")
+        job.check_status()
+        print(f"E={E} graph={graph} per-step check={CHECK}: {e0.elapsed_time(e1) / 5:.2f} ms/step "
+              f"(host enqueue {host:.2f} ms/step)")
         del job
         torch.cuda.empty_cache()
