@@ -53,6 +53,32 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+typedef unsigned long long f32x2;  // packed fp32 pair (sm_100a FADD2 / FMUL2 / FFMA2)
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(f32x2 r) {
+  float2 f;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(f.x), "=f"(f.y) : "l"(r));
+  return f;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *(const uint32_t*)&v;
@@ -423,7 +449,8 @@ __global__ void __launch_bounds__(B_THREADS, 2)
     // pass 3 (this half): dropped P (packed, registers), the keep bits (the forward's, or drawn again),
     // partial D = sum dP * P; P and dP * mask go back into TMEM in place of S and dPd for pass 4
     uint32_t pd[32], mbits[2] = {mb.x, mb.y};
-    float D = 0.f;
+    f32x2 D2 = pk2(0.f, 0.f);
+    const f32x2 SC2 = pk2(SC, SC);
 #pragma unroll
     for (int c2 = 0; c2 < 2; ++c2) {
       const int c = hf * 2 + c2;  // 32-column slice
@@ -442,25 +469,32 @@ __global__ void __launch_bounds__(B_THREADS, 2)
         }
         mbits[c2] = bits;
       }
+      // packed fp32 pairs (FFMA2 / FMUL2: the same per-element operations as the forward's P); D accumulates
+      // as an (even, odd) column pair of FMAs, added at the end
+      const uint32_t mw = mbits[c2];
 #pragma unroll
       for (int q = 0; q < 32; q += 2) {
-        const float p0 = ex2_approx(__fmaf_rn(__uint_as_float(v[q]), SC, nm)) * inv;
-        const float p1 = ex2_approx(__fmaf_rn(__uint_as_float(v[q + 1]), SC, nm)) * inv;
-        const float m0 = thr ? (((mbits[c2] >> q) & 1u) ? keep : 0.f) : 1.f;
-        const float m1 = thr ? (((mbits[c2] >> (q + 1)) & 1u) ? keep : 0.f) : 1.f;
-        pd[c2 * 16 + (q >> 1)] = pack2(p0 * m0, p1 * m1);
-        const float gm0 = __uint_as_float(g[q]) * m0, gm1 = __uint_as_float(g[q + 1]) * m1;
-        D += gm0 * p0;
-        D += gm1 * p1;
-        v[q] = __float_as_uint(p0);
-        v[q + 1] = __float_as_uint(p1);
-        g[q] = __float_as_uint(gm0);
-        g[q + 1] = __float_as_uint(gm1);
+        const float2 t = upk2(fma2(pk2(__uint_as_float(v[q]), __uint_as_float(v[q + 1])), SC2, pk2(nm, nm)));
+        const f32x2 pp = mul2(pk2(ex2_approx(t.x), ex2_approx(t.y)), pk2(inv, inv));
+        const float m0 = thr ? (((mw >> q) & 1u) ? keep : 0.f) : 1.f;
+        const float m1 = thr ? (((mw >> (q + 1)) & 1u) ? keep : 0.f) : 1.f;
+        const f32x2 mm = pk2(m0, m1);
+        const float2 pm = upk2(mul2(pp, mm));
+        pd[c2 * 16 + (q >> 1)] = pack2(pm.x, pm.y);
+        const f32x2 gm = mul2(pk2(__uint_as_float(g[q]), __uint_as_float(g[q + 1])), mm);
+        D2 = fma2(gm, pp, D2);
+        const float2 pf = upk2(pp), gf = upk2(gm);
+        v[q] = __float_as_uint(pf.x);
+        v[q + 1] = __float_as_uint(pf.y);
+        g[q] = __float_as_uint(gf.x);
+        g[q + 1] = __float_as_uint(gf.y);
       }
       tmem_st32(lane_base + c * 32, v);
       tmem_st32(lane_base + 128 + c * 32, g);
     }
     tmem_st_wait();
+    const float2 Dp = upk2(D2);
+    float D = Dp.x + Dp.y;
     if (!a.stats) __syncthreads();  // the sum slots of row_stats_half are read
     red[hf * SEQ + row] = D;
     __syncthreads();
@@ -474,14 +508,16 @@ __global__ void __launch_bounds__(B_THREADS, 2)
       tmem_ld32(lane_base + c * 32, v);        // P
       tmem_ld32(lane_base + 128 + c * 32, g);  // dP * mask
       tmem_ld_wait();
+      const f32x2 DD = pk2(D, D), E8 = pk2(0.125f, 0.125f);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         uint32_t w[4];
 #pragma unroll
-        for (int hh = 0; hh < 4; ++hh) {
+        for (int hh = 0; hh < 4; ++hh) {  // (P (dP m - D)) / 8, packed pairs
           const int q = cc * 8 + 2 * hh;
-          const float p0 = __uint_as_float(v[q]), p1 = __uint_as_float(v[q + 1]);
-          w[hh] = pack2(p0 * (__uint_as_float(g[q]) - D) * 0.125f, p1 * (__uint_as_float(g[q + 1]) - D) * 0.125f);
+          const f32x2 pp = pk2(__uint_as_float(v[q]), __uint_as_float(v[q + 1]));
+          const float2 ds = upk2(mul2(mul2(pp, sub2(pk2(__uint_as_float(g[q]), __uint_as_float(g[q + 1])), DD)), E8));
+          w[hh] = pack2(ds.x, ds.y);
         }
         const int chunk = c2 * 4 + cc;
         *(uint4*)(srow + ((chunk ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
