@@ -4,6 +4,7 @@
 
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -330,18 +331,16 @@ static cudaError_t host_wait(cudaStream_t s) {
   return e;
 }
 
-int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_host, void* stream) {
-  int st = validate_mlp(args);
-  if (st) return st;
+// Everything of bt_mlp_run but the host wait: the launch and the copies back, queued on s.
+static int mlp_run_enqueue(const bt_mlp_args* args, double* losses_host, int32_t* status_host, cudaStream_t s) {
   const size_t lbytes = sizeof(double) * (size_t)args->K * args->E_total;
   // status_host == NULL: the status block directly follows the losses in device memory, and ONE copy
   // brings both (status words at the tail of losses_host)
   const bool one_copy = !status_host && losses_host && (const char*)args->flags == (const char*)args->losses + lbytes;
   if (!status_host && !one_copy)
     return fail(bt::ERR_INPUT, "bt_mlp_run needs a status buffer (or the status block right after the losses)");
-  st = bt::mlp_launch(*args, STREAM(stream));
+  const int st = bt::mlp_launch(*args, s);
   if (st) return done(st, "bt_mlp_run");
-  cudaStream_t s = STREAM(stream);
   if (one_copy) {
     if (cudaMemcpyAsync(losses_host, args->losses, lbytes + 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s) !=
         cudaSuccess)
@@ -352,6 +351,15 @@ int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_hos
     if (cudaMemcpyAsync(status_host, args->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
       return cuda_fail("bt_mlp_run status");
   }
+  return 0;
+}
+
+int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_host, void* stream) {
+  int st = validate_mlp(args);
+  if (st) return st;
+  cudaStream_t s = STREAM(stream);
+  st = mlp_run_enqueue(args, losses_host, status_host, s);
+  if (st) return st;
   if (host_wait(s) != cudaSuccess) return cuda_fail("bt_mlp_run sync");
   g_err[0] = 0;
   return 0;
@@ -363,27 +371,36 @@ int bt_mlp_run_sampled(const bt_mlp_args* args, uint64_t seed, int64_t dataset_n
   if (!args || !stage_host || !lists_dev) return fail(bt::ERR_INPUT, "bt_mlp_run_sampled: null pointer");
   if (n_epochs < 1 || first_epoch < 0) return fail(bt::ERR_INPUT, "bt_mlp_run_sampled: %d epochs", n_epochs);
   const int32_t workers = args->E_total, micro = args->B;
-  if (workers < 1 || micro < 1 || dataset_n / ((int64_t)workers * micro) != args->spe)
+  if (workers < 1 || micro < 1 || args->spe < 1 || dataset_n / ((int64_t)workers * micro) != args->spe)
     return fail(bt::ERR_CONFIG, "bt_mlp_run_sampled: steps per epoch %lld do not match the dataset", (long long)args->spe);
   // the launch's epochs must be the ones staged
   if (args->step0 / args->spe < first_epoch ||
       (args->step0 + args->K - 1) / args->spe >= first_epoch + n_epochs)
     return fail(bt::ERR_INPUT, "bt_mlp_run_sampled: epochs [%lld, +%d) do not cover the launch",
                 (long long)first_epoch, n_epochs);
+  bt_mlp_args a = *args;
+  a.lists = lists_dev;
+  a.epoch_base = first_epoch;
+  int st = validate_mlp(&a);
+  if (st) return st;
   const size_t per = (size_t)workers * (size_t)(args->spe * micro);
   for (int32_t k = 0; k < n_epochs; ++k) {  // the sampler's host work (sampling.py:63-82), then one H2D copy
-    const int st = bt_host_epoch_indices(seed, (uint64_t)(first_epoch + k), dataset_n, workers, micro, shuffle,
-                                         stage_host + (size_t)k * per);
+    st = bt_host_epoch_indices(seed, (uint64_t)(first_epoch + k), dataset_n, workers, micro, shuffle,
+                               stage_host + (size_t)k * per);
     if (st) return st;
   }
+  // (Overlapping this host work with the launch latency -- the stream held on a pinned gate word while
+  // the copy and launch are queued, then opened -- was measured slower: +15 us per call, the device's
+  // poll of host memory costing more than the ~8 us of Fisher-Yates it hides.)
   cudaStream_t s = STREAM(stream);
   if (cudaMemcpyAsync(lists_dev, stage_host, sizeof(int32_t) * per * n_epochs, cudaMemcpyHostToDevice, s) !=
       cudaSuccess)
     return cuda_fail("bt_mlp_run_sampled lists");
-  bt_mlp_args a = *args;
-  a.lists = lists_dev;
-  a.epoch_base = first_epoch;
-  return bt_mlp_run(&a, losses_host, status_host, stream);
+  st = mlp_run_enqueue(&a, losses_host, status_host, s);
+  if (st) return st;
+  if (host_wait(s) != cudaSuccess) return cuda_fail("bt_mlp_run_sampled sync");
+  g_err[0] = 0;
+  return 0;
 }
 
 int bt_mlp_run_group(const bt_mlp_args* const* args, const int32_t* devices, void* const* streams, int32_t n,

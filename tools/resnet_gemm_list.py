@@ -16,7 +16,8 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     job.step()
     torch.cuda.synchronize()
 evs = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA], key=lambda e: e.time_range.start)
+ALL = len(sys.argv) > 1 and sys.argv[1] == "all"  # every kernel, not only the GEMMs
 for e in evs:
-    if "gemm" in e.name or "conv" in e.name:
+    if ALL or "gemm" in e.name or "conv" in e.name:
         print(f"{e.device_time_total:8.1f} us  {e.name[:100]}")
 print("convs:", [(c.name, c.ci, c.co, c.k, c.s, c.hout) for c in job.convs])
