@@ -226,10 +226,16 @@ def bench_e2e_single(bt, K: int, W: int, flush):
 
     cfg = make_cfg(bt)
     ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")])
-    for n in chunks(W, LAUNCH):
-        engine.run_steps(ts, n)
-    torch.cuda.synchronize()
     pipe = ts.pipeline
+    # W warm-up mini-batches, one call each and prepared like a timed call: the host / driver / launch path
+    # of a call is warmed W times (its first calls in a process run 1.5-2x slower: tools/e2e_first_call.py)
+    for _ in range(W):
+        flush()
+        pipe._lists_dev = None
+        pipe._lists_host.clear()
+        torch.cuda.synchronize()
+        engine.run_steps(ts, 1)
+    torch.cuda.synchronize()
     spans, launches, h2d, d2h = [], 0, 0, 0
     losses = []
     for n in chunks(K, LAUNCH):
