@@ -189,7 +189,8 @@ int bt_host_epoch_indices(uint64_t seed, uint64_t epoch, int64_t n, int32_t work
   if (micro < 1) return fail(bt::ERR_CONFIG, "micro_batch must be >= 1");
   const int64_t spe = n / ((int64_t)workers * micro);
   if (spe < 1) return fail(bt::ERR_CONFIG, "dataset smaller than one global batch");
-  std::vector<int32_t> order((size_t)n);
+  static thread_local std::vector<int32_t> order;  // (reused: an allocation per epoch shows on the e2e path)
+  order.resize((size_t)n);
   if (shuffle) bt_host_shuffled_range(n, seed ^ epoch, order.data());
   else for (int64_t i = 0; i < n; ++i) order[(size_t)i] = (int32_t)i;
   const int64_t per = spe * micro;

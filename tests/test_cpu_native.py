@@ -164,3 +164,21 @@ def test_model_stack_entry_points_validate_before_the_device():
         assert status == 1, (name, status)
         with pytest.raises(InputError):
             _native.check(status, name)
+
+
+def test_native_fisher_yates_equals_oracle_across_sizes():
+    """bt_host_shuffled_range equals the oracle's Fisher-Yates (prng.py:81-93) for tiny, typical, odd and
+    large sizes and extreme states (the golden vectors pin a few small cases only)."""
+    import sys
+
+    import paper_2208_14228_b200 as bt
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+
+    rng = np.random.default_rng(11)
+    for n in (0, 1, 2, 3, 7, 64, 1000, 1024, 4097, 65_537, (1 << 20) + 5):
+        for state in [0, 2**64 - 1] + [int(x) for x in rng.integers(0, 2**63, size=2, dtype=np.int64)]:
+            a = bt.shuffled_range(n, state)
+            b = oracle.shuffled_range(n, state) if n else []
+            assert a == list(b), (n, state)
