@@ -91,6 +91,11 @@ int bt_mlp_step(const bt_mlp_args *args, void *stream);
  * run_steps call in one entry point (losses_host may be NULL).  status_host may be NULL when the
  * device status block directly follows the K x E_total losses (args->flags == args->losses + K*E_total):
  * then ONE copy of the losses and the 4 status words lands in losses_host, the words at its tail.
+ * In that layout, with losses_host pinned and the single-device compact build running, there is no copy
+ * at all: the kernel's epilogue writes the losses and status words into losses_host (mapped) and then a
+ * per-thread done word (system-scope release) that the call spins on -- the call returns when the
+ * results are in host memory, without a stream synchronisation (the stream may still be retiring the
+ * kernel: later work on it stays ordered).  BT_HOST_SIGNAL=0 restores copy + synchronise.
  *                                                                      engine.py:271-329 */
 int bt_mlp_run(const bt_mlp_args *args, double *losses_host, int32_t *status_host, void *stream);
 /* bt_mlp_run with the sampler's host work inside the call: the index lists of epochs [first_epoch,

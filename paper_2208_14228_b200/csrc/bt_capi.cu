@@ -14,7 +14,13 @@
 #include "bt_ffn.cuh"
 
 namespace bt {
-int mlp_launch(const bt_mlp_args& a, cudaStream_t s, unsigned long long* timing = nullptr);
+struct MlpHostSignal {
+  double* out;
+  uint32_t* done;
+  uint32_t seq;
+};
+int mlp_launch(const bt_mlp_args& a, cudaStream_t s, unsigned long long* timing = nullptr,
+               const MlpHostSignal* hs = nullptr, bool* signaled = nullptr);
 size_t mlp_smem_bytes(int nrows);
 bool mlp_fused_fits(const bt_mlp_args& a);
 bool mlp_xdev_supported(const bt_mlp_args& a);
@@ -332,14 +338,90 @@ static cudaError_t host_wait(cudaStream_t s) {
   return e;
 }
 
-// Everything of bt_mlp_run but the host wait: the launch and the copies back, queued on s.
-static int mlp_run_enqueue(const bt_mlp_args* args, double* losses_host, int32_t* status_host, cudaStream_t s) {
+// BT_HOST_SIGNAL=0: always copy the results back and synchronise the stream (measurements, tests).
+static bool host_signal_enabled() {
+  static const int on = [] {
+    const char* e = getenv("BT_HOST_SIGNAL");
+    return (e && strcmp(e, "0") == 0) ? 0 : 1;
+  }();
+  return on != 0;
+}
+// The host signal of bt_mlp_run: a mapped pinned done word per host thread, bumped per call.
+static uint32_t* host_done_word(uint32_t** dev) {
+  static thread_local uint32_t* w = nullptr;
+  static thread_local uint32_t* wd = nullptr;
+  if (!w) {
+    void* p = nullptr;
+    void* d = nullptr;
+    if (cudaHostAlloc(&p, 64, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&d, p, 0) != cudaSuccess) {
+      if (p) cudaFreeHost(p);
+      cudaGetLastError();
+      return nullptr;
+    }
+    w = (uint32_t*)p;
+    wd = (uint32_t*)d;
+    *(volatile uint32_t*)w = 0;
+  }
+  *dev = wd;
+  return w;
+}
+// device-accessible address of pinned host memory (null when p is not pinned); the last answer is cached
+static void* mapped_ptr(void* p) {
+  static thread_local void* last = nullptr;
+  static thread_local void* last_dev = nullptr;
+  if (p == last) return last_dev;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+  last = p;
+  last_dev = at.devicePointer;
+  return last_dev;
+}
+
+struct RunWait {  // how bt_mlp_run's results arrive: a host signal (seq on *done) or the stream
+  volatile uint32_t* done = nullptr;
+  uint32_t seq = 0;
+};
+
+// Everything of bt_mlp_run but the host wait: the launch and the results' way back, queued on s.  In the
+// one-copy layout with pinned host buffers the compact build's epilogue writes the losses and status words
+// into host memory itself and signals a done word (no copy, no stream synchronisation); otherwise one or
+// two device-to-host copies follow the launch.
+static int mlp_run_enqueue(const bt_mlp_args* args, double* losses_host, int32_t* status_host, cudaStream_t s,
+                           RunWait* w) {
   const size_t lbytes = sizeof(double) * (size_t)args->K * args->E_total;
   // status_host == NULL: the status block directly follows the losses in device memory, and ONE copy
   // brings both (status words at the tail of losses_host)
   const bool one_copy = !status_host && losses_host && (const char*)args->flags == (const char*)args->losses + lbytes;
   if (!status_host && !one_copy)
     return fail(bt::ERR_INPUT, "bt_mlp_run needs a status buffer (or the status block right after the losses)");
+  w->done = nullptr;
+  if (one_copy && args->n_dev <= 1 && host_signal_enabled()) {
+    void* dev_out = mapped_ptr(losses_host);
+    uint32_t* dw_dev = nullptr;
+    uint32_t* dw = dev_out ? host_done_word(&dw_dev) : nullptr;
+    if (dw) {
+      static thread_local uint32_t seq = 0;
+      const bt::MlpHostSignal hs{(double*)dev_out, dw_dev, ++seq};
+      bool signaled = false;
+      const int st = bt::mlp_launch(*args, s, nullptr, &hs, &signaled);
+      if (st) return done(st, "bt_mlp_run");
+      if (signaled) {
+        w->done = dw;
+        w->seq = hs.seq;
+        return 0;
+      }
+      // (the generic build ran: copy back below)
+      if (cudaMemcpyAsync(losses_host, args->losses, lbytes + 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s) !=
+          cudaSuccess)
+        return cuda_fail("bt_mlp_run losses + status");
+      return 0;
+    }
+  }
   const int st = bt::mlp_launch(*args, s);
   if (st) return done(st, "bt_mlp_run");
   if (one_copy) {
@@ -355,13 +437,34 @@ static int mlp_run_enqueue(const bt_mlp_args* args, double* losses_host, int32_t
   return 0;
 }
 
+// Wait for the results: spin on the done word (checking the stream now and then, so a failed or
+// non-signalling launch is reported instead of waited on forever), or poll the stream's event.
+static int mlp_run_wait(cudaStream_t s, const RunWait& w, const char* what) {
+  if (!w.done) return host_wait(s) == cudaSuccess ? 0 : cuda_fail(what);
+  for (uint32_t it = 1;; ++it) {
+    if (*w.done == w.seq) break;
+    if ((it & 255) == 0) {
+      const cudaError_t q = cudaStreamQuery(s);
+      if (q == cudaSuccess) {
+        if (*w.done == w.seq) break;
+        return fail(bt::ERR_CUDA, "%s: the launch completed without signalling its results", what);
+      }
+      if (q != cudaErrorNotReady) return cuda_fail(what);
+    }
+  }
+  __atomic_thread_fence(__ATOMIC_ACQUIRE);  // the results the done word published
+  return 0;
+}
+
 int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_host, void* stream) {
   int st = validate_mlp(args);
   if (st) return st;
   cudaStream_t s = STREAM(stream);
-  st = mlp_run_enqueue(args, losses_host, status_host, s);
+  RunWait w;
+  st = mlp_run_enqueue(args, losses_host, status_host, s, &w);
   if (st) return st;
-  if (host_wait(s) != cudaSuccess) return cuda_fail("bt_mlp_run sync");
+  st = mlp_run_wait(s, w, "bt_mlp_run sync");
+  if (st) return st;
   g_err[0] = 0;
   return 0;
 }
@@ -397,9 +500,11 @@ int bt_mlp_run_sampled(const bt_mlp_args* args, uint64_t seed, int64_t dataset_n
   if (cudaMemcpyAsync(lists_dev, stage_host, sizeof(int32_t) * per * n_epochs, cudaMemcpyHostToDevice, s) !=
       cudaSuccess)
     return cuda_fail("bt_mlp_run_sampled lists");
-  st = mlp_run_enqueue(&a, losses_host, status_host, s);
+  RunWait w;
+  st = mlp_run_enqueue(&a, losses_host, status_host, s, &w);
   if (st) return st;
-  if (host_wait(s) != cudaSuccess) return cuda_fail("bt_mlp_run_sampled sync");
+  st = mlp_run_wait(s, w, "bt_mlp_run_sampled sync");
+  if (st) return st;
   g_err[0] = 0;
   return 0;
 }

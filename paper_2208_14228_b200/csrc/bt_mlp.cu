@@ -146,12 +146,23 @@ __device__ __forceinline__ double fold_ranks_any(int n, int fan, int start, Ld l
   return f.finish();
 }
 
+struct MlpHostSignal {  // bt_mlp_run's request: results to mapped host memory + a done word (see MlpLaunch)
+  double* out;
+  uint32_t* done;
+  uint32_t seq;
+};
 struct MlpLaunch {  // launcher-computed shared-memory plan
   int stage_data;   // dataset copied into shared memory
   int stage_idx;    // this launch's index lists copied into shared memory
   int grads_smem;   // EST gradient slots [E_total][P] in shared memory (fused, non-cluster mode)
   int cluster;      // fused mode on a thread-block cluster: slots pushed through DSMEM
   unsigned long long* timing;  // optional [9] per-stage clock64 sums (bt_mlp_step_profiled)
+  // Host signal (single-device compact build): the epilogue copies the K x E_total losses and the 4 status
+  // words into mapped pinned host memory and then writes done_seq to host_done (system-scope release), so
+  // the host sees the results without a device-to-host copy and a stream synchronisation.
+  double* host_out;
+  uint32_t* host_done;
+  uint32_t done_seq;
 };
 
 // ---- cluster plumbing (PTX) -------------------------------------------------
@@ -1147,6 +1158,17 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
     }
   }
   cluster_wait();
+  if constexpr (ND == 1) {
+    if (L.host_out && cta == 0) {  // every CTA's losses and status words are in global memory (cluster barrier)
+      const int nw = a.K * a.E_total + 2;  // the losses, then the 4 status words (the one-copy layout)
+      const unsigned long long* src = (const unsigned long long*)a.losses;
+      unsigned long long* dst = (unsigned long long*)L.host_out;
+      for (int i = tid; i < nw; i += S::T) dst[i] = __ldcg(src + i);
+      __threadfence_system();
+      __syncthreads();
+      if (tid == 0) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(L.host_done), "r"(L.done_seq) : "memory");
+    }
+  }
   if (L.timing && tid == 0 && cta == 0) {  // [9] prologue, [10] epilogue, [11] whole CTA (cycles)
     for (int k = 0; k < 5; ++k) L.timing[k] += tacc[k];
     L.timing[5] += (unsigned long long)s;
@@ -1339,7 +1361,9 @@ static int spec_g(int et) {
   return et < 8 ? et : 8;
 }
 
-int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* timing) {
+int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* timing, const MlpHostSignal* hs,
+               bool* signaled) {
+  if (signaled) *signaled = false;
   if (a.n_dev > 1) {  // one device of a lock-step exchange group: the compact build only
     if (!mlp_xdev_supported(a)) return ERR_INPUT;
     MlpLaunch L{0, 0, 0, 1, timing};
@@ -1351,6 +1375,7 @@ int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* ti
   size_t smem = 0;
   MlpLaunch L = plan(a, &smem);
   L.timing = timing;
+  const bool sig = hs && hs->out && hs->done && !timing;
   if (a.fuse_reduce && !L.grads_smem && !L.cluster) return ERR_INPUT;  // too many ESTs for the fused path
   if (smem > SMEM_LIMIT) return ERR_INPUT;
   const int fan = a.est_fanin_uniform - 1;  // every EST's batch variant, when the caller knows it
@@ -1359,6 +1384,11 @@ int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* ti
     cudaError_t err = cudaSuccess;
     bool ran = false;
     const int g = spec_g(a.E_total);
+    if (sig) {
+      L.host_out = hs->out;
+      L.host_done = hs->done;
+      L.done_seq = hs->seq;
+    }
     switch (a.E_total * 16 + g) {
       case 4 * 16 + 2: ran = try_spec<4, 2>(a, fan, stream, L, &err); break;
       case 4 * 16 + 4: ran = try_spec<4, 4>(a, fan, stream, L, &err); break;
@@ -1368,7 +1398,12 @@ int mlp_launch(const bt_mlp_args& a, cudaStream_t stream, unsigned long long* ti
       case 16 * 16 + 8: ran = try_spec<16, 8>(a, fan, stream, L, &err); break;
       default: break;
     }
-    if (ran) return err == cudaSuccess ? OK : ERR_CUDA;
+    if (ran) {
+      if (signaled) *signaled = sig && err == cudaSuccess;
+      return err == cudaSuccess ? OK : ERR_CUDA;
+    }
+    L.host_out = nullptr;  // (the generic build below does not signal)
+    L.host_done = nullptr;
   }
   cudaError_t err;
   switch (a.B) {

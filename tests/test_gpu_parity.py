@@ -440,3 +440,48 @@ def test_run_steps_sampled_launch_equals_resident_lists(bt):
                                           fs.host_io_ptr + 8 * (fs.KMAX - 40) * fs.E, None, None)
     assert st == 1  # InputError, nothing launched
     a.pipeline.drop_lists()
+
+
+_SIGNAL_SCRIPT = r"""
+import hashlib, json, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import paper_2208_14228_b200 as bt
+from paper_2208_14228_b200 import engine
+cfg = bt.TrainRunConfig(seed=42, max_workers=8, micro_batch=4, dataset_size=1024, lr=0.02, momentum=0.9,
+                        dropout_rate=0.5, jitter=0.1, bucket_capacity=64,
+                        determinism=bt.DeterminismMode.from_label("d1"), device_fanins={"gpu_fast": 2})
+ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")])
+h = hashlib.sha256()
+for k in (20, 7, 33, 1, 20):
+    ts.pipeline.drop_lists()
+    out, _ = engine.run_steps(ts, k)
+    h.update(np.ascontiguousarray(out).tobytes())
+for _ in range(3):
+    h.update(repr(bt.run_minibatch(ts)).encode())
+p = np.array(ts.executors[0].model.values.tolist())
+print(json.dumps({"losses": h.hexdigest(), "params": hashlib.sha256(p.tobytes()).hexdigest(), "step": ts.global_step}))
+"""
+
+
+def test_host_signal_results_equal_copied_results(tmp_path):
+    """bt_mlp_run / bt_mlp_run_sampled in the one-copy layout with pinned host buffers: the compact build's
+    epilogue writes the losses and status words into host memory and signals a done word (no device-to-host
+    copy, no stream synchronisation).  The losses of launches of 20 / 7 / 33 / 1 mini-batches and
+    run_minibatch calls, and the final weights, equal the copy-back path (BT_HOST_SIGNAL=0) bit for bit."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parent.parent)
+    script = tmp_path / "sig.py"
+    script.write_text(_SIGNAL_SCRIPT)
+    outs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, BT_HOST_SIGNAL=flag)
+        r = subprocess.run([sys.executable, str(script), root], capture_output=True, text=True, env=env, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
