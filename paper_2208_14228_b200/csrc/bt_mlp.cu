@@ -803,6 +803,21 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
       if (it < a.K * S::R) iv[k] = *list_entry(it);
     }
   }
+  if (!a.rows) {  // the rows' jitter needs only counters: computed while the loads above are in flight
+    for (int it = tid; it < a.K * S::EPC; it += S::T) {  // one worker stream per (mini-batch, EST)
+      const int s = it / S::EPC, el = it - s * S::EPC;
+      const int q = loc0 + s, de = q / spe, local = q - de * spe;
+      double* jd = s_jit + (size_t)s * S::R + el * S::NB;
+      if (a.jitter != 0.0) {  // one uniform per row of worker_rng(seed, epoch, local, est) (sampling.py:99-170)
+        const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)(ep0 + de), (uint64_t)local, (uint64_t)(eb + e0 + el));
+#pragma unroll
+        for (int r = 0; r < S::NB; ++r) jd[r] = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), a.jitter);
+      } else {
+#pragma unroll
+        for (int r = 0; r < S::NB; ++r) jd[r] = 0.0;
+      }
+    }
+  }
   int bad = flag0 != 0 ? 4 : 0;  // a sticky earlier failure: do nothing
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
@@ -858,19 +873,6 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
 #pragma unroll 4
     for (int it = tid + IPT * S::T; it < a.K * S::R; it += S::T) s_idx[it] = *list_entry(it);  // long launches
     t_p2 = clock64();
-    for (int it = tid; it < a.K * S::EPC; it += S::T) {  // one worker stream per (mini-batch, EST)
-      const int s = it / S::EPC, el = it - s * S::EPC;
-      const int q = loc0 + s, de = q / spe, local = q - de * spe;
-      double* jd = s_jit + (size_t)s * S::R + el * S::NB;
-      if (a.jitter != 0.0) {  // one uniform per row of worker_rng(seed, epoch, local, est) (sampling.py:99-170)
-        const uint64_t w = derive5(TAG_DATA_WORKER, a.seed, (uint64_t)(ep0 + de), (uint64_t)local, (uint64_t)(eb + e0 + el));
-#pragma unroll
-        for (int r = 0; r < S::NB; ++r) jd[r] = dmul(dsub(unit_float(draw_raw(w, (uint64_t)r)), 0.5), a.jitter);
-      } else {
-#pragma unroll
-        for (int r = 0; r < S::NB; ++r) jd[r] = 0.0;
-      }
-    }
   }
   const long long t_p3 = clock64();
   if (bulk) mbar_wait(smem_u32(&s_mbar[2]), 0, a.flags);  // the dataset has landed (also before any exit)
