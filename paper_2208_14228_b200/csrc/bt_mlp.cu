@@ -718,6 +718,18 @@ __device__ __forceinline__ double ll_value(uint64_t w0, uint64_t w1) {
   return __longlong_as_double((long long)((w0 & 0xffffffffull) | (w1 << 32)));
 }
 
+// The launch's losses and the 4 status words (the one-copy layout) into mapped host memory, then the done
+// word with a system-scope release (all threads of one CTA; bt_mlp_run spins on the word).
+__device__ __forceinline__ void spec_signal_host(const bt_mlp_args& a, const MlpLaunch& L, int tid, int T) {
+  const int nw = a.K * a.E_total + 2;
+  const unsigned long long* src = (const unsigned long long*)a.losses;
+  unsigned long long* dst = (unsigned long long*)L.host_out;
+  for (int i = tid; i < nw; i += T) dst[i] = __ldcg(src + i);
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(L.host_done), "r"(L.done_seq) : "memory");
+}
+
 template <int ET, int G, int F, int ND = 1>
 __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(const __grid_constant__ bt_mlp_args a,
                                                                                  const MlpLaunch L) {
@@ -884,6 +896,13 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
     if (cta == 0 && tid == 0 && !(prologue & 4)) {
       a.flags[FLAG_STATUS] = (prologue & 1) ? ERR_CORRUPTION : ERR_INPUT;
       a.flags[FLAG_STEP] = 0;
+    }
+    if constexpr (ND == 1) {
+      if (L.host_out && cta == 0) {  // the host waits on the signal: publish the status words
+        __threadfence();
+        __syncthreads();
+        spec_signal_host(a, L, tid, S::T);
+      }
     }
     return;
   }
@@ -1161,15 +1180,8 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
   }
   cluster_wait();
   if constexpr (ND == 1) {
-    if (L.host_out && cta == 0) {  // every CTA's losses and status words are in global memory (cluster barrier)
-      const int nw = a.K * a.E_total + 2;  // the losses, then the 4 status words (the one-copy layout)
-      const unsigned long long* src = (const unsigned long long*)a.losses;
-      unsigned long long* dst = (unsigned long long*)L.host_out;
-      for (int i = tid; i < nw; i += S::T) dst[i] = __ldcg(src + i);
-      __threadfence_system();
-      __syncthreads();
-      if (tid == 0) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(L.host_done), "r"(L.done_seq) : "memory");
-    }
+    // every CTA's losses and status words are in global memory (cluster barrier)
+    if (L.host_out && cta == 0) spec_signal_host(a, L, tid, S::T);
   }
   if (L.timing && tid == 0 && cta == 0) {  // [9] prologue, [10] epilogue, [11] whole CTA (cycles)
     for (int k = 0; k < 5; ++k) L.timing[k] += tacc[k];

@@ -485,3 +485,16 @@ def test_host_signal_results_equal_copied_results(tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert outs[0] == outs[1]
+
+
+def test_tampered_replica_raises_corruption_on_the_signalled_path(bt):
+    """The compact build (micro-batch 4) with pinned results signals the host on its early exit too: a replica
+    mismatch raises CorruptionError (not a launch error), and the sticky status makes the next call fail the
+    same way without running."""
+    cfg = bt.TrainRunConfig(seed=42, max_workers=8, micro_batch=4, dataset_size=1024,
+                            determinism=bt.DeterminismMode.from_label("d1"), device_fanins={"gpu_fast": 2})
+    ts = bt.init_training(cfg, [bt.ExecutorSpec("gpu_fast")] * 2)
+    bt.run_minibatch(ts)
+    ts.executors[1].model.values[0] = math.nextafter(ts.executors[1].model.values[0], math.inf)
+    with pytest.raises(bt.CorruptionError):
+        bt.run_minibatch(ts)
