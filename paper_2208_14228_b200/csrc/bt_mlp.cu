@@ -830,6 +830,57 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
       }
     }
   }
+  // ---- per-thread constants (pure arithmetic: computed while the prologue's loads are in flight) ----
+  const double rate = a.rate, lr = a.lr, mu = a.mu;
+  const double keep = rate >= 1.0 ? 0.0 : ddiv(1.0, dsub(1.0, rate));  // model.py:150
+  const bool jit = !a.rows && a.jitter != 0.0;
+  const IntDivisor divB = IntDivisor::of(S::NB), divH = IntDivisor::of(BT_HIDDEN), divE = IntDivisor::of(ET);
+  // B+C lane: row = tid / 16 of this CTA, hidden unit j = tid % 16
+  const bool lane = tid < S::LANES;
+  const int row = lane ? tid >> 4 : 0, j = tid & 15;
+  const int lel = row / S::NB, lr_ = row - lel * S::NB;
+  // E items: (EST, parameter or loss) pairs.  Term r of item (el, p) is
+  // A[r] * B[r] (w1: dz*x, w2: gy*h) or A[r] (b1: dz, b2: gy, loss: e^2);
+  // the operand addresses are per-thread constants, so the step's gradient
+  // code is loads, multiplies, a select and the fold -- no branches.
+  uint32_t opa[S::NIT][S::NB], opb[S::NIT][S::NB], own_dst[S::NIT], rdst[S::NIT][S::GM1];
+  bool has_b[S::NIT], is_loss[S::NIT], valid[S::NIT];
+  uint32_t rbar[S::GM1];
+  const uint32_t sm0 = smem_u32(sm);
+#pragma unroll
+  for (int i = 0; i < G - 1; ++i) {  // the other CTAs, in rotated order (no rank test per push)
+    int rk = cta + 1 + i;
+    rk -= rk >= G ? G : 0;
+    rbar[i] = cluster_map32(smem_u32(&s_mbar[0]), rk);
+  }
+#pragma unroll
+  for (int k = 0; k < S::NIT; ++k) {
+    const int it = tid + k * S::T;
+    valid[k] = it < S::ITEMS;
+    const int el = valid[k] ? it / (BT_P + 1) : 0, p = valid[k] ? it - el * (BT_P + 1) : 0;
+    const int rb = el * S::NB;
+    int a0, as, b0, bs;  // first operand index and row stride, in doubles
+    if (p < BT_B1) { a0 = S::DZ + rb * BT_HIDDEN + (p & 15); as = BT_HIDDEN; b0 = S::X + rb * BT_INPUT_DIM + (p >> 4); bs = BT_INPUT_DIM; }
+    else if (p < BT_W2) { a0 = S::DZ + rb * BT_HIDDEN + (p - BT_B1); as = BT_HIDDEN; b0 = a0; bs = as; }
+    else if (p < BT_B2) { a0 = S::GY + rb; as = 1; b0 = S::HID + rb * BT_HIDDEN + (p - BT_W2); bs = BT_HIDDEN; }
+    else if (p == BT_B2) { a0 = S::GY + rb; as = 1; b0 = a0; bs = as; }
+    else { a0 = S::E2 + rb; as = 1; b0 = a0; bs = as; }
+    has_b[k] = p < BT_W2 ? p < BT_B1 : p < BT_B2;
+    is_loss[k] = p == BT_P;
+#pragma unroll
+    for (int r = 0; r < S::NB; ++r) {
+      opa[k][r] = sm0 + (uint32_t)((a0 + r * as) * sizeof(double));
+      opb[k][r] = sm0 + (uint32_t)((b0 + r * bs) * sizeof(double));
+    }
+    const uint32_t off = (uint32_t)((S::GRAD + (eb + e0 + el) * S::SP + p) * sizeof(double));  // parity-0 slot entry
+    own_dst[k] = sm0 + off;
+#pragma unroll
+    for (int i = 0; i < G - 1; ++i) {
+      int rk = cta + 1 + i;
+      rk -= rk >= G ? G : 0;
+      rdst[k][i] = cluster_map32(sm0, rk) + off;
+    }
+  }
   int bad = flag0 != 0 ? 4 : 0;  // a sticky earlier failure: do nothing
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
@@ -907,58 +958,7 @@ __global__ void __launch_bounds__(SpecShape<ET, G, ND>::T) mlp_step_spec_kernel(
     return;
   }
 
-  // ---- per-thread constants ----------------------------------------------
-  const double rate = a.rate, lr = a.lr, mu = a.mu;
-  const double keep = rate >= 1.0 ? 0.0 : ddiv(1.0, dsub(1.0, rate));  // model.py:150
-  const bool jit = !a.rows && a.jitter != 0.0;
-  const IntDivisor divB = IntDivisor::of(S::NB), divH = IntDivisor::of(BT_HIDDEN), divE = IntDivisor::of(ET);
-  // B+C lane: row = tid / 16 of this CTA, hidden unit j = tid % 16
-  const bool lane = tid < S::LANES;
-  const int row = lane ? tid >> 4 : 0, j = tid & 15;
-  const int lel = row / S::NB, lr_ = row - lel * S::NB;
   uint64_t lrng = s_rng[lel];  // this row's EST dropout stream, advanced in registers
-  // E items: (EST, parameter or loss) pairs.  Term r of item (el, p) is
-  // A[r] * B[r] (w1: dz*x, w2: gy*h) or A[r] (b1: dz, b2: gy, loss: e^2);
-  // the operand addresses are per-thread constants, so the step's gradient
-  // code is loads, multiplies, a select and the fold -- no branches.
-  uint32_t opa[S::NIT][S::NB], opb[S::NIT][S::NB], own_dst[S::NIT], rdst[S::NIT][S::GM1];
-  bool has_b[S::NIT], is_loss[S::NIT], valid[S::NIT];
-  uint32_t rbar[S::GM1];
-  const uint32_t sm0 = smem_u32(sm);
-#pragma unroll
-  for (int i = 0; i < G - 1; ++i) {  // the other CTAs, in rotated order (no rank test per push)
-    int rk = cta + 1 + i;
-    rk -= rk >= G ? G : 0;
-    rbar[i] = cluster_map32(smem_u32(&s_mbar[0]), rk);
-  }
-#pragma unroll
-  for (int k = 0; k < S::NIT; ++k) {
-    const int it = tid + k * S::T;
-    valid[k] = it < S::ITEMS;
-    const int el = valid[k] ? it / (BT_P + 1) : 0, p = valid[k] ? it - el * (BT_P + 1) : 0;
-    const int rb = el * S::NB;
-    int a0, as, b0, bs;  // first operand index and row stride, in doubles
-    if (p < BT_B1) { a0 = S::DZ + rb * BT_HIDDEN + (p & 15); as = BT_HIDDEN; b0 = S::X + rb * BT_INPUT_DIM + (p >> 4); bs = BT_INPUT_DIM; }
-    else if (p < BT_W2) { a0 = S::DZ + rb * BT_HIDDEN + (p - BT_B1); as = BT_HIDDEN; b0 = a0; bs = as; }
-    else if (p < BT_B2) { a0 = S::GY + rb; as = 1; b0 = S::HID + rb * BT_HIDDEN + (p - BT_W2); bs = BT_HIDDEN; }
-    else if (p == BT_B2) { a0 = S::GY + rb; as = 1; b0 = a0; bs = as; }
-    else { a0 = S::E2 + rb; as = 1; b0 = a0; bs = as; }
-    has_b[k] = p < BT_W2 ? p < BT_B1 : p < BT_B2;
-    is_loss[k] = p == BT_P;
-#pragma unroll
-    for (int r = 0; r < S::NB; ++r) {
-      opa[k][r] = sm0 + (uint32_t)((a0 + r * as) * sizeof(double));
-      opb[k][r] = sm0 + (uint32_t)((b0 + r * bs) * sizeof(double));
-    }
-    const uint32_t off = (uint32_t)((S::GRAD + (eb + e0 + el) * S::SP + p) * sizeof(double));  // parity-0 slot entry
-    own_dst[k] = sm0 + off;
-#pragma unroll
-    for (int i = 0; i < G - 1; ++i) {
-      int rk = cta + 1 + i;
-      rk -= rk >= G ? G : 0;
-      rdst[k][i] = cluster_map32(sm0, rk) + off;
-    }
-  }
   const int rot_p = tid < BT_P ? s_rot[tid] : 0;
   uint32_t phases = 0;
 
