@@ -592,6 +592,13 @@ class _FastStep:
         self.losses_np = self.rows_np
         self.a, self.keep = _step_args(ts, 1, cfg.micro_batch, None, io, None) if self.fits else (None, [])
         self.dev = ts.dev
+        # per-call host work is part of every run_minibatch: the argument block's reference, the entry points
+        # and the device ordinal are looked up once, and fields that rarely change are written only on change
+        self.aref = C.byref(self.a) if self.fits else None
+        lib = _native.lib()
+        self.run_fn, self.run_sampled_fn = lib.bt_mlp_run, lib.bt_mlp_run_sampled
+        self.ordinal = ts.dev.shards[0].ordinal
+        self._set = None  # (rot tensor, lr, mu) last written into the argument block
 
     def run(self, ts: TrainingState, K: int) -> int:
         """Launch K mini-batches from ts.global_step; returns the device status word."""
@@ -603,28 +610,32 @@ class _FastStep:
         rot = _rot_tensor(ts)
         ex0 = ts.executors[0]
         a.K, a.step0 = K, gs
-        a.rot = ptr(rot)
-        a.lr, a.mu = float(ex0._lr), float(ex0._mu)
+        key = (rot, ex0._lr, ex0._mu)
+        if self._set is None or key[0] is not self._set[0] or key[1:] != self._set[1:]:
+            a.rot = ptr(rot)
+            a.lr, a.mu = float(ex0._lr), float(ex0._mu)
+            self._set = key
         off = 8 * (self.KMAX - K) * self.E  # the launch's losses end where the status words begin
         a.losses = self.io_ptr + off
         lh = self.host_io_ptr + off
+        sp = torch._C._cuda_getCurrentRawStream(self.ordinal)
         if pipe.lists_resident(e0, e1):
-            lists, base = pipe.device_lists(e0, e1)
-            self.keep = [lists]
+            lists, base = pipe._lists_dev, pipe._lists_dev_base
+            self.keep = lists
             a.lists, a.epoch_base = lists.data_ptr(), base
-            st = _native.lib().bt_mlp_run(C.byref(a), lh, None, _raw_stream())
+            st = self.run_fn(self.aref, lh, None, sp)
         else:  # the epochs' lists are made on the host inside the native call, copied, then the launch
             count = max(e1 - e0 + 1, pipe.EPOCH_WINDOW)
             stage, lists = pipe.reserve_lists(e0, count)
-            self.keep = [lists]
-            st = _native.lib().bt_mlp_run_sampled(C.byref(a), pipe.seed & (2**64 - 1), pipe.dataset_size,
-                                                  int(pipe.shuffle), e0, count, stage, lists.data_ptr(), lh, None,
-                                                  _raw_stream())
+            self.keep = lists
+            st = self.run_sampled_fn(self.aref, pipe.seed & (2**64 - 1), pipe.dataset_size, int(pipe.shuffle), e0,
+                                     count, stage, lists.data_ptr(), lh, None, sp)
             if st:
                 pipe.drop_lists()
-        _native.check(st, "run_minibatch")
+        if st:
+            _native.check(st, "run_minibatch")
         self.losses_np = self.rows_np[self.KMAX - K:]
-        self.dev.invalidate()
+        self.dev._snap = None  # (DeviceState.invalidate)
         return int(self.status_np[0])
 
 
