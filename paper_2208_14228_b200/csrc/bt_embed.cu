@@ -180,6 +180,73 @@ __global__ void __launch_bounds__(CE_THREADS) ce_kernel(const float* __restrict_
   }
   if (threadIdx.x == 0) row_loss[r] = __logf(s) + m - l[lab];
 }
+// The same cross-entropy with the row held in registers: 1024 threads per row, NV float4s each, so the
+// logits are read from HBM once (the two-pass form above reads every row twice).  Exact row max (a max
+// is order-free), then the exp sum per thread in column order, the warps' sums by a fixed butterfly and
+// the 32 warps in order -- deterministic; then dlogits from the registers.
+constexpr int CE_RT = 1024;
+template <int NV>
+__global__ void __launch_bounds__(CE_RT) ce_reg_kernel(const float* __restrict__ logits,
+                                                      const int32_t* __restrict__ labels, int V, int Vp,
+                                                      float inv_rows, __nv_bfloat16* __restrict__ dlogits,
+                                                      float* __restrict__ row_loss) {
+  __shared__ float sm_w[CE_RT / 32];
+  const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* l = logits + (size_t)r * Vp;
+  float4 x[NV];
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (tid + k * CE_RT) * 4;
+    x[k] = c < Vp ? __ldcs((const float4*)(l + c)) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    if (c + 0 >= V) x[k].x = -INFINITY;
+    if (c + 1 >= V) x[k].y = -INFINITY;
+    if (c + 2 >= V) x[k].z = -INFINITY;
+    if (c + 3 >= V) x[k].w = -INFINITY;
+    m = fmaxf(m, fmaxf(fmaxf(x[k].x, x[k].y), fmaxf(x[k].z, x[k].w)));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) sm_w[warp] = m;
+  __syncthreads();
+  m = sm_w[0];
+#pragma unroll
+  for (int w = 1; w < CE_RT / 32; ++w) m = fmaxf(m, sm_w[w]);
+  __syncthreads();
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {  // exp(-inf - m) = 0 for the padding
+    s += __expf(x[k].x - m);
+    s += __expf(x[k].y - m);
+    s += __expf(x[k].z - m);
+    s += __expf(x[k].w - m);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) sm_w[warp] = s;
+  __syncthreads();
+  s = sm_w[0];
+#pragma unroll
+  for (int w = 1; w < CE_RT / 32; ++w) s += sm_w[w];
+  const int lab = labels[r];
+  const float inv_s = 1.f / s;
+  __nv_bfloat16* d = dlogits + (size_t)r * Vp;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (tid + k * CE_RT) * 4;
+    if (c >= Vp) continue;
+    const float xv[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+    float g[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      g[q] = c + q < V ? (__expf(xv[q] - m) * inv_s - (c + q == lab ? 1.f : 0.f)) * inv_rows : 0.f;
+    uint2 u;
+    *(__nv_bfloat162*)&u.x = __floats2bfloat162_rn(g[0], g[1]);
+    *(__nv_bfloat162*)&u.y = __floats2bfloat162_rn(g[2], g[3]);
+    *(uint2*)(d + c) = u;
+  }
+  if (tid == 0) row_loss[r] = __logf(s) + m - l[lab];
+}
 // loss[e] = (sum of the EST's row losses, in row order) / rows_per_est
 __global__ void ce_fold_kernel(const float* __restrict__ row_loss, int E, int rows_per_est, float* __restrict__ loss) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -449,8 +516,14 @@ int emb_scatter_launch(const void* src, const int32_t* rows, int R, int np, int 
 int emb_ce_launch(const float* logits, const int32_t* labels, int R, int V, int Vp, int E, int rows_per_est,
                   void* dlogits, float* row_loss, float* loss, cudaStream_t s) {
   if (R != E * rows_per_est || V > Vp || Vp % 4) return ERR_INPUT;
-  emb::ce_kernel<<<R, emb::CE_THREADS, 0, s>>>(logits, labels, V, Vp, 1.f / (float)rows_per_est,
-                                               (__nv_bfloat16*)dlogits, row_loss);
+  const int nv = (Vp / 4 + emb::CE_RT - 1) / emb::CE_RT;  // float4s per thread of the register form
+  const float ir = 1.f / (float)rows_per_est;
+  __nv_bfloat16* dl = (__nv_bfloat16*)dlogits;
+  if (nv <= 1) emb::ce_reg_kernel<1><<<R, emb::CE_RT, 0, s>>>(logits, labels, V, Vp, ir, dl, row_loss);
+  else if (nv <= 2) emb::ce_reg_kernel<2><<<R, emb::CE_RT, 0, s>>>(logits, labels, V, Vp, ir, dl, row_loss);
+  else if (nv <= 4) emb::ce_reg_kernel<4><<<R, emb::CE_RT, 0, s>>>(logits, labels, V, Vp, ir, dl, row_loss);
+  else if (nv <= 8) emb::ce_reg_kernel<8><<<R, emb::CE_RT, 0, s>>>(logits, labels, V, Vp, ir, dl, row_loss);
+  else emb::ce_kernel<<<R, emb::CE_THREADS, 0, s>>>(logits, labels, V, Vp, ir, dl, row_loss);
   emb::ce_fold_kernel<<<(E + 127) / 128, 128, 0, s>>>(row_loss, E, rows_per_est, loss);
   return ok_or_cuda_e();
 }
