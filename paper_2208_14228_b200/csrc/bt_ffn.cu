@@ -186,14 +186,41 @@ __global__ void colsum_part_kernel(const __nv_bfloat16* __restrict__ in, int E, 
     o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
 }
-__global__ void colsum_final_kernel(const float* __restrict__ part, int E, int chunks, int C, float* __restrict__ out,
-                                    int64_t ostride) {
-  const int64_t n = (int64_t)E * C;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int e = (int)(i / C), c = (int)(i - (int64_t)e * C);
-    float acc = part[((size_t)e * chunks) * C + c];
-    for (int k = 1; k < chunks; ++k) acc += part[((size_t)e * chunks + k) * C + c];
-    out[(size_t)e * ostride + c] = acc;
+// Fold of the chunk partials per (EST / leaf, column): the chunks in 8 contiguous groups of q = ceil(chunks/8),
+// each group summed in chunk order by its own warp (32 columns per block), then the groups in order -- a fixed
+// association for every grid (for chunks <= 8 exactly the sequential sum).  A sequential sum per column
+// left the fold latency-bound on a chain of loads (~10 us per launch at 128 chunks).
+__global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restrict__ part, int E, int chunks, int C,
+                                                           float* __restrict__ out, int64_t ostride) {
+  __shared__ float sp[8][33];
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t ncb = (C + 31) / 32;
+  const int q = (chunks + 7) / 8, ng = (chunks + q - 1) / q;
+  for (int64_t b = blockIdx.x; b < (int64_t)E * ncb; b += gridDim.x) {
+    const int e = (int)(b / ncb), c = (int)(b - (int64_t)e * ncb) * 32 + cl;
+    const int k0 = g * q, k1 = min(chunks, k0 + q);
+    float acc = 0.f;
+    if (c < C && k0 < k1) {
+      const float* pc = part + ((size_t)e * chunks) * C + c;
+      acc = pc[(size_t)k0 * C];
+      int k = k0 + 1;
+      for (; k + 4 <= k1; k += 4) {
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = pc[(size_t)(k + j) * C];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc += v[j];
+      }
+      for (; k < k1; ++k) acc += pc[(size_t)k * C];
+    }
+    sp[g][cl] = acc;
+    __syncthreads();
+    if (g == 0 && c < C) {
+      float t = sp[0][cl];
+      for (int gg = 1; gg < ng; ++gg) t += sp[gg][cl];
+      out[(size_t)e * ostride + c] = t;
+    }
+    __syncthreads();
   }
 }
 
@@ -286,12 +313,14 @@ int colsum_bf16_strided_launch(const void* in, int E, int R, int C, float* out, 
   }
   ffn::colsum_part_kernel<<<grid_for((int64_t)E * chunks * C / 8), 256, 0, s>>>((const __nv_bfloat16*)in, E, R, C,
                                                                                part);
-  ffn::colsum_final_kernel<<<grid_for((int64_t)E * C), 256, 0, s>>>(part, E, chunks, C, out, ostride);
+  ffn::colsum_final_kernel<<<grid_for((int64_t)E * ((C + 31) / 32) * 256), 256, 0, s>>>(part, E, chunks, C, out,
+                                                                                      ostride);
   if (own) cudaFreeAsync(part, s);
   return ok_or_cuda();
 }
 int colsum_fold_launch(const float* part, int E, int chunks, int C, float* out, int64_t ostride, cudaStream_t s) {
-  ffn::colsum_final_kernel<<<grid_for((int64_t)E * C), 256, 0, s>>>(part, E, chunks, C, out, ostride);
+  ffn::colsum_final_kernel<<<grid_for((int64_t)E * ((C + 31) / 32) * 256), 256, 0, s>>>(part, E, chunks, C, out,
+                                                                                      ostride);
   return ok_or_cuda();
 }
 int transpose_launch(const void* in, int in_f32, int E, int R, int C, void* out, cudaStream_t s) {

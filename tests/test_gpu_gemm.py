@@ -216,8 +216,38 @@ def test_ffn_backward_epilogue_column_partials(monkeypatch, variant):
     leaves, per = 4, T // 32 // 4
     out = torch.zeros(leaves, F + 8, device="cuda")
     _native.check(L.bt_colsum_fold(part.data_ptr(), leaves, per, F, out.data_ptr(), F + 8, stream()))
-    acc = want.reshape(leaves, per, F)[:, 0]
-    for k in range(1, per):
-        acc = acc + want.reshape(leaves, per, F)[:, k]
-    assert np.array_equal(out[:, :F].cpu().numpy().view(np.uint32), acc.view(np.uint32))
+    assert np.array_equal(out[:, :F].cpu().numpy().view(np.uint32), _grouped_fold(want.reshape(leaves, per, F)).view(np.uint32))
+
+
+def _grouped_fold(p):
+    """bt_colsum_fold's association over p [leaves][chunks][C]: 8 contiguous groups of ceil(chunks/8) chunks,
+    each summed in order, then the groups in order (fp32)."""
+    chunks = p.shape[1]
+    q = -(-chunks // 8)
+    sums = []
+    for k0 in range(0, chunks, q):
+        acc = p[:, k0].copy()
+        for k in range(k0 + 1, min(chunks, k0 + q)):
+            acc = acc + p[:, k]
+        sums.append(acc)
+    out = sums[0]
+    for t in sums[1:]:
+        out = out + t
+    return out
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 8, 9, 64, 100, 128])
+def test_colsum_fold_association(chunks):
+    """bt_colsum_fold (the bias-gradient fold of column partials) equals its stated association bit for bit
+    for chunk counts below, at and above the 8 groups, ragged group sizes and a column count that is not a
+    multiple of the 32-column block."""
+    from paper_2208_14228_b200 import _native
+    from paper_2208_14228_b200.device import stream
+
+    leaves, C = 3, 200
+    p = (torch.randn(leaves, chunks, C, device="cuda") * 10).float()
+    out = torch.zeros(leaves, C + 5, device="cuda")
+    _native.check(_native.lib().bt_colsum_fold(p.data_ptr(), leaves, chunks, C, out.data_ptr(), C + 5, stream()))
+    want = _grouped_fold(p.cpu().numpy())
+    assert np.array_equal(out[:, :C].cpu().numpy().view(np.uint32), want.view(np.uint32))
 

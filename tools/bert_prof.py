@@ -1,4 +1,5 @@
-"""Kernel-time breakdown of one per-EST BERT step (torch.profiler / CUPTI), grouped by kernel name.
+"""Kernel-time breakdown of one per-EST BERT step (torch.profiler / CUPTI), grouped by kernel name
+(BT_PROF_RAW=1: every kernel name on its own line).
 
     python tools/bert_prof.py [ests] [layers] [seqs]
 """
@@ -30,7 +31,7 @@ cnt = defaultdict(int)
 for ev in prof.events():
     if ev.device_type == torch.autograd.DeviceType.CUDA:
         name = ev.name
-        for key in ("gemm_bf16_tn_pair_kernel", "gemm_bf16_tn_kernel", "attn_fwd", "attn_bwd", "ln_fwd", "ln_bwd",
+        for key in () if os.environ.get("BT_PROF_RAW") else ("gemm_bf16_tn_pair_kernel", "gemm_bf16_tn_kernel", "attn_fwd", "attn_bwd", "ln_fwd", "ln_bwd",
                     "transpose_kernel", "colsum", "reduce", "cast_t", "ln_fold", "mse", "data_kernel", "tokens_kernel",
                     "embed_fwd", "gather_rows", "scatter_rows", "ce_kernel", "ce_fold", "sort_segments",
                     "embed_grad", "pos_grad"):
