@@ -86,6 +86,13 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sr
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// before re-staging a box: with NB boxes per warp the store that last used this box is NB chunks old
+template <int NB>
+__device__ __forceinline__ void bulk_wait_box() {
+  if (NB == 1) bulk_wait_read0();
+  else bulk_wait_read1();
+}
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -136,7 +143,7 @@ __device__ __forceinline__ void colsum_box32(const uint8_t* st, int lane, float*
 // One epilogue chunk: 32 consecutive fp32 accumulators of row `row` (lane = row - row0),
 // columns [col, col+32) -- plain (fp32 / bf16), + bias, or an FFN element op fused in --
 // staged in shared memory and stored by TMA at (col, row0, batch entry z).
-template <bool OUT_BF16>
+template <bool OUT_BF16, int NB = 2>
 __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, int col, int N, const GemmEpi& epi,
                                                uint8_t* st, int lane, const CUtensorMap* mc, const CUtensorMap* mc2,
                                                int row0, int z) {
@@ -146,7 +153,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
     const int e = (int)(row / (size_t)epi.Te), tl = (int)(row - (size_t)e * epi.Te);
     const uint64_t sd = epi.p > 0.f ? derive3(ffn::TAG_FFN_DROP, epi.seed, (uint64_t)(epi.est_base + e)) : 0;
     const float keep = epi.p < 1.f ? 1.f / (1.f - epi.p) : 0.f;
-    if (lane == 0) bulk_wait_read1();  // the store that last used this box (two chunks ago) has read it
+    if (lane == 0) bulk_wait_box<NB>();  // the store that last used this box (two chunks ago) has read it
     __syncwarp();
 #pragma unroll
     for (int q8 = 0; q8 < 4; ++q8) {
@@ -187,7 +194,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
     const uint64_t sd = epi.p > 0.f ? derive3(ffn::TAG_FFN_DROP, epi.seed, (uint64_t)(epi.est_base + e)) : 0;
     const float keep = epi.p < 1.f ? 1.f / (1.f - epi.p) : 0.f;
     uint8_t* const ab = st + EPI_BOX / 2;
-    if (lane == 0) bulk_wait_read1();
+    if (lane == 0) bulk_wait_box<NB>();
     __syncwarp();
 #pragma unroll
     for (int pass = 0; pass < 4; ++pass) {
@@ -238,7 +245,7 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t* v, size_t row, in
       f[4 * q4 + 3] += bv.w;
     }
   }
-  if (lane == 0) bulk_wait_read1();  // the store that last used this box (two chunks ago) has read it
+  if (lane == 0) bulk_wait_box<NB>();  // the store that last used this box (two chunks ago) has read it
   __syncwarp();
   if (OUT_BF16) {
     stage_bf16(st, f, lane);
@@ -533,23 +540,23 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t local, uint32_t rank) {
 
 constexpr int PAIR_BN = 256, PAIR_M = 256;
 
-template <int STAGES, int EW = EPI_WARPS>
+template <int STAGES, int EW = EPI_WARPS, int NB = 2>
 struct PairSmem {
   static constexpr int A_BYTES = BM * BK * 2, B_BYTES = (PAIR_BN / 2) * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int EPI = STAGES * STAGE;
-  static constexpr int BAR = EPI + EW * EPI_STAGE;
+  static constexpr int BAR = EPI + EW * NB * EPI_BOX;
   static constexpr int TOTAL = BAR + (2 * STAGES + 4) * 8 + 16;
 };
 
 // EW epilogue warps (16 for ALU-heavy epilogues); AIM 1: A = im2col(x) K-major (the forward convolution);
 // AIM 2: B = im2col(x) MN-major (the weight gradient)
-template <int STAGES, bool OUT_BF16, bool MN, int EW = EPI_WARPS, int AIM = 0>
+template <int STAGES, bool OUT_BF16, bool MN, int EW = EPI_WARPS, int AIM = 0, int NB = 2>
 __global__ void __launch_bounds__(64 + 32 * EW, 1)
     gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                              const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2,
                              int M, int N, int K, int batch, const GemmEpi epi, const ConvGeom cg) {
-  using L = PairSmem<STAGES, EW>;
+  using L = PairSmem<STAGES, EW, NB>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -689,7 +696,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   } else {  // ---- epilogue (both CTAs: own 128 rows) ----
     const int lg = warp & 3;
     const int half = (warp - 2) >> 2;
-    uint8_t* const est = gbase + L::EPI + (warp - 2) * EPI_STAGE;
+    uint8_t* const est = gbase + L::EPI + (warp - 2) * NB * EPI_BOX;
     int chunk = 0;
     const uint32_t leader_tempty0 = map_to_rank(tempty(0), 0), leader_tempty1 = map_to_rank(tempty(1), 0);
     const int c_lo = half * (PAIR_BN / (EW / 4)), c_hi = c_lo + PAIR_BN / (EW / 4);
@@ -707,8 +714,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         uint32_t v[32];
         tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * PAIR_BN + cc), v);
         tmem_ld_wait();
-        epilogue_chunk<OUT_BF16>(v, row, n0 + cc, N, epi, est + (chunk++ & 1) * EPI_BOX, lane, &map_c, &map_c2, row0,
-                                  t / per_batch);
+        epilogue_chunk<OUT_BF16, NB>(v, row, n0 + cc, N, epi, est + (NB == 2 ? (chunk++ & 1) : 0) * EPI_BOX, lane,
+                                      &map_c, &map_c2, row0, t / per_batch);
       }
       tc_fence_before();
       __syncwarp();
@@ -1237,7 +1244,7 @@ static int launch_gemm(const GemmShape& g, int grid, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess ? OK : ERR_CUDA;
 }
 
-template <int STAGES, bool OUT_BF16, bool MN, int EW = gemm::EPI_WARPS, int AIM = 0>
+template <int STAGES, bool OUT_BF16, bool MN, int EW = gemm::EPI_WARPS, int AIM = 0, int NB = 2>
 static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
   const int M = g.M, N = g.N, K = g.K;
   CUtensorMap ma, mb, mc, mc2;
@@ -1254,8 +1261,8 @@ static int launch_gemm_pair(const GemmShape& g, int grid, cudaStream_t s) {
       !make_store_map(&mc, g.c, M, N, g.batch, g.sc, OUT_BF16) ||
       !make_store_map(&mc2, g.epi.out2 ? (const void*)g.epi.out2 : g.c, M, N, g.batch, g.sc, OUT_BF16))
     return ERR_CUDA;
-  auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16, MN, EW, AIM>;
-  const int smem = gemm::PairSmem<STAGES, EW>::TOTAL + 1024;
+  auto kern = gemm::gemm_bf16_tn_pair_kernel<STAGES, OUT_BF16, MN, EW, AIM, NB>;
+  const int smem = gemm::PairSmem<STAGES, EW, NB>::TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -1302,8 +1309,18 @@ static int launch_any(const GemmShape& g, int out_bf16, int grid, cudaStream_t s
     if (g.epi.kind == EPI_FFN_FWD || g.epi.kind == EPI_FFN_BWD) {  // ALU-heavy epilogues: 16 epilogue warps
       static const int ew = getenv("BT_FFN_EW") ? atoi(getenv("BT_FFN_EW")) : 16;  // A/B measurements
       if (ew == 8) return launch_gemm_pair<SP, true, MN, gemm::EPI_WARPS, AIM>(g, grid, s);
-      return launch_gemm_pair<3, true, MN, 16, AIM>(g, grid, s);
+      // 16 warps x ONE staging box each (a box is re-staged only after its last store has read it; a chunk's
+      // ALU work is far longer than that read) leaves room for 5 k-block stages instead of 3
+      static const int nb = getenv("BT_FFN_NB") ? atoi(getenv("BT_FFN_NB")) : 1;  // A/B measurements
+      if (nb == 2) return launch_gemm_pair<3, true, MN, 16, AIM>(g, grid, s);
+      return launch_gemm_pair<5, true, MN, 16, AIM, 1>(g, grid, s);
     }
+    // one staging box per epilogue warp makes room for a 6th k-block stage: 1-5% per GEMM at the C4 shapes
+    // (tools/gemm_list.py); BT_PAIR_S6=0 restores 5 stages x 2 boxes (A/B)
+    static const int s6 = getenv("BT_PAIR_S6") ? atoi(getenv("BT_PAIR_S6")) : 1;
+    if (s6 && gemm::EPI_WARPS == 8)
+      return out_bf16 ? launch_gemm_pair<6, true, MN, gemm::EPI_WARPS, AIM, 1>(g, grid, s)
+                      : launch_gemm_pair<6, false, MN, gemm::EPI_WARPS, AIM, 1>(g, grid, s);
     return out_bf16 ? launch_gemm_pair<SP, true, MN, gemm::EPI_WARPS, AIM>(g, grid, s)
                     : launch_gemm_pair<SP, false, MN, gemm::EPI_WARPS, AIM>(g, grid, s);
   }
