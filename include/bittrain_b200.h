@@ -100,13 +100,17 @@ int bt_mlp_step(const bt_mlp_args *args, void *stream);
 int bt_mlp_run(const bt_mlp_args *args, double *losses_host, int32_t *status_host, void *stream);
 /* bt_mlp_run with the sampler's host work inside the call: the index lists of epochs [first_epoch,
  * first_epoch + n_epochs) are computed on the host (native Fisher-Yates seeded seed ^ epoch, dealt
- * round-robin: sampling.py:63-82) into stage_host (pinned, n_epochs * E_total * spe * B int32), copied
- * to lists_dev on the stream, and the launch reads them (args->lists / epoch_base are taken from here).
+ * round-robin: sampling.py:63-82) into stage_host (pinned, n_epochs * E_total * spe * B int32); the
+ * launch reads them from stage_host through its mapped device address (zero-copy, once, in the prologue;
+ * BT_LISTS_ZC=0: copied first) and they are copied to lists_dev on the stream after the launch, for
+ * later calls of the same epochs (args->lists / epoch_base are taken from here).
  * Replaces the reference's per-step DataPipeline.batch + forward_backward + allreduce + sgd_step
  * (engine.py:271-329) for K mini-batches with host inputs and host outputs, one call. */
 int bt_mlp_run_sampled(const bt_mlp_args *args, uint64_t seed, int64_t dataset_n, int32_t shuffle,
                        int64_t first_epoch, int32_t n_epochs, int32_t *stage_host, int32_t *lists_dev,
                        double *losses_host, int32_t *status_host, void *stream);
+/* Blocks until no copy queued by bt_mlp_run_sampled still reads stage_host (call before re-filling it). */
+int bt_stage_wait(const void *stage_host);
 /* The multi-device form (bt_mlp_args.n_dev > 1): the n launches of one lock-step exchange group,
  * launch i on CUDA device devices[i] / streams[i]; all are queued before any host wait (they
  * exchange EST slots with each other every mini-batch), then each device's losses (its own EST

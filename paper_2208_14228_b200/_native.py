@@ -90,6 +90,7 @@ EXPORTS = {
     "bt_mlp_run": (C.c_int, [C.POINTER(MlpArgs), _vp, _vp, _vp]),
     "bt_l2_flush": (C.c_int, [_vp, _i64, C.c_uint32, _vp]),
     "bt_mlp_run_sampled": (C.c_int, [C.POINTER(MlpArgs), _u64, _i64, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "bt_stage_wait": (C.c_int, [_vp]),
     "bt_mlp_run_group": (C.c_int, [C.POINTER(C.POINTER(MlpArgs)), _i32p, C.POINTER(_vp), _i32, C.POINTER(_vp),
                                    C.POINTER(_vp)]),
     "bt_mlp_step_profiled": (C.c_int, [C.POINTER(MlpArgs), _vp, _vp]),

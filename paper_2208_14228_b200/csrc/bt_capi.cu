@@ -368,18 +368,22 @@ static uint32_t* host_done_word(uint32_t** dev) {
 }
 // device-accessible address of pinned host memory (null when p is not pinned); the last answer is cached
 static void* mapped_ptr(void* p) {
-  static thread_local void* last = nullptr;
-  static thread_local void* last_dev = nullptr;
-  if (p == last) return last_dev;
+  // a few recent (host, device) pairs: the result block and the sampler's staging buffers alternate
+  static thread_local void* host[4] = {nullptr, nullptr, nullptr, nullptr};
+  static thread_local void* devp[4] = {nullptr, nullptr, nullptr, nullptr};
+  static thread_local unsigned next = 0;
+  for (int i = 0; i < 4; ++i)
+    if (host[i] == p && p) return devp[i];
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
   if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
-  last = p;
-  last_dev = at.devicePointer;
-  return last_dev;
+  const unsigned i = next++ & 3;
+  host[i] = p;
+  devp[i] = at.devicePointer;
+  return devp[i];
 }
 
 struct RunWait {  // how bt_mlp_run's results arrive: a host signal (seq on *done) or the stream
@@ -469,6 +473,63 @@ int bt_mlp_run(const bt_mlp_args* args, double* losses_host, int32_t* status_hos
   return 0;
 }
 
+static bool lists_zero_copy() {  // BT_LISTS_ZC=0: copy the lists to the device before the launch (A/B)
+  static const int on = [] {
+    const char* e = getenv("BT_LISTS_ZC");
+    return (e && strcmp(e, "0") == 0) ? 0 : 1;
+  }();
+  return on != 0;
+}
+// Staging buffers whose device copy may still be queued: (buffer, device, event after the copy).
+struct StageCopy {
+  const void* host;
+  int dev;
+  cudaEvent_t ev;
+  bool pending;
+};
+static StageCopy g_stage[8];
+static int stage_copy_wait(const void* host) {
+  for (auto& c : g_stage)
+    if (c.host == host && c.pending) {
+      c.pending = false;
+      if (cudaEventSynchronize(c.ev) != cudaSuccess) return cuda_fail("bt_mlp_run_sampled staging reuse");
+    }
+  return 0;
+}
+static void stage_copy_record(const void* host, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  StageCopy* slot = nullptr;
+  for (auto& c : g_stage)
+    if (c.host == host && c.dev == dev) slot = &c;
+  if (!slot)
+    for (auto& c : g_stage)
+      if (!c.host || !c.pending) {
+        if (c.host && c.ev) cudaEventDestroy(c.ev);
+        c = StageCopy{host, dev, nullptr, false};
+        slot = &c;
+        break;
+      }
+  if (!slot) {  // every slot busy: wait for the stream instead (never observed: two buffers per pipeline)
+    cudaStreamSynchronize(s);
+    return;
+  }
+  if (!slot->ev && cudaEventCreateWithFlags(&slot->ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    slot->ev = nullptr;
+    cudaStreamSynchronize(s);
+    return;
+  }
+  if (cudaEventRecord(slot->ev, s) != cudaSuccess) {
+    cudaGetLastError();
+    cudaStreamSynchronize(s);
+    return;
+  }
+  slot->pending = true;
+}
+
+int bt_stage_wait(const void* stage_host) { return stage_copy_wait(stage_host); }
+
 int bt_mlp_run_sampled(const bt_mlp_args* args, uint64_t seed, int64_t dataset_n, int32_t shuffle,
                        int64_t first_epoch, int32_t n_epochs, int32_t* stage_host, int32_t* lists_dev,
                        double* losses_host, int32_t* status_host, void* stream) {
@@ -488,6 +549,8 @@ int bt_mlp_run_sampled(const bt_mlp_args* args, uint64_t seed, int64_t dataset_n
   int st = validate_mlp(&a);
   if (st) return st;
   const size_t per = (size_t)workers * (size_t)(args->spe * micro);
+  st = stage_copy_wait(stage_host);  // a previous call's copy out of this staging buffer has finished
+  if (st) return st;
   for (int32_t k = 0; k < n_epochs; ++k) {  // the sampler's host work (sampling.py:63-82), then one H2D copy
     st = bt_host_epoch_indices(seed, (uint64_t)(first_epoch + k), dataset_n, workers, micro, shuffle,
                                stage_host + (size_t)k * per);
@@ -497,12 +560,27 @@ int bt_mlp_run_sampled(const bt_mlp_args* args, uint64_t seed, int64_t dataset_n
   // the copy and launch are queued, then opened -- was measured slower: +15 us per call, the device's
   // poll of host memory costing more than the ~8 us of Fisher-Yates it hides.)
   cudaStream_t s = STREAM(stream);
-  if (cudaMemcpyAsync(lists_dev, stage_host, sizeof(int32_t) * per * n_epochs, cudaMemcpyHostToDevice, s) !=
-      cudaSuccess)
-    return cuda_fail("bt_mlp_run_sampled lists");
+  const size_t lbytes = sizeof(int32_t) * per * n_epochs;
+  // Zero-copy: the launch reads this call's index lists straight from the pinned staging buffer (the
+  // compact build loads them once, in its prologue, beside its other global loads: one PCIe round trip
+  // instead of a DMA copy the launch has to wait for); the device copy that later calls of the same
+  // epochs use is queued AFTER the launch, off the path to the results (the caller re-fills this staging
+  // buffer only after that copy: bt_stage_reuse_wait).
+  int32_t* zc = lists_zero_copy() ? (int32_t*)mapped_ptr(stage_host) : nullptr;
   RunWait w;
-  st = mlp_run_enqueue(&a, losses_host, status_host, s, &w);
-  if (st) return st;
+  if (zc) {
+    a.lists = zc;
+    st = mlp_run_enqueue(&a, losses_host, status_host, s, &w);
+    if (st) return st;
+    if (cudaMemcpyAsync(lists_dev, stage_host, lbytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return cuda_fail("bt_mlp_run_sampled lists");
+    stage_copy_record(stage_host, s);
+  } else {
+    if (cudaMemcpyAsync(lists_dev, stage_host, lbytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return cuda_fail("bt_mlp_run_sampled lists");
+    st = mlp_run_enqueue(&a, losses_host, status_host, s, &w);
+    if (st) return st;
+  }
   st = mlp_run_wait(s, w, "bt_mlp_run_sampled sync");
   if (st) return st;
   g_err[0] = 0;

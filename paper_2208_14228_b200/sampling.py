@@ -160,10 +160,13 @@ class DataPipeline:
         per = epochs[0].size
         n = per * len(epochs)
         if getattr(self, "_stage", None) is None or self._stage[0].numel() < n:
+            for p in getattr(self, "_stageptr", None) or ():  # no queued copy still reads a buffer being freed
+                _native.check(_native.lib().bt_stage_wait(p), "lists staging")
             self._upload_buffers(max(n, 4 * per))
         i = self._stage_i = self._stage_i ^ 1
         if self._stage_used[i]:
             self._stage_ev[i].synchronize()
+        _native.check(_native.lib().bt_stage_wait(self._stageptr[i]), "lists staging")  # a sampled call's copy
         st = self._stage_np[i]
         for k, arr in enumerate(epochs):
             st[k * per:(k + 1) * per] = arr.reshape(-1)
@@ -185,12 +188,14 @@ class DataPipeline:
         per = self.total_workers * self.steps_per_epoch * self.micro_batch
         n = per * count
         if getattr(self, "_stage", None) is None or self._stage[0].numel() < n:
+            for p in getattr(self, "_stageptr", None) or ():  # no queued copy still reads a buffer being freed
+                _native.check(_native.lib().bt_stage_wait(p), "lists staging")
             self._stage = None
             self._upload_buffers(max(n, 4 * per))
         i = self._stage_i = self._stage_i ^ 1
         if self._stage_used[i]:
             self._stage_ev[i].synchronize()
-        self._stage_used[i] = False  # the native call synchronises its stream before returning
+        self._stage_used[i] = False  # the native call orders its own copy out of the buffer (bt_stage_wait)
         key = (i, count)  # the views are cached: a tensor view per call costs microseconds on the e2e path
         view = self._views.get(key)
         if view is None:

@@ -479,12 +479,14 @@ def test_host_signal_results_equal_copied_results(tmp_path):
     script = tmp_path / "sig.py"
     script.write_text(_SIGNAL_SCRIPT)
     outs = []
-    for flag in ("1", "0"):
-        env = dict(os.environ, BT_HOST_SIGNAL=flag)
+    # host signal on / off; the sampled launches reading their index lists zero-copy from the pinned staging
+    # buffer (the device copy queued after the launch, used by the later run_minibatch calls) / copied first
+    for sig, zc in (("1", "1"), ("0", "1"), ("1", "0")):
+        env = dict(os.environ, BT_HOST_SIGNAL=sig, BT_LISTS_ZC=zc)
         r = subprocess.run([sys.executable, str(script), root], capture_output=True, text=True, env=env, timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
-    assert outs[0] == outs[1]
+    assert outs[0] == outs[1] == outs[2]
 
 
 def test_tampered_replica_raises_corruption_on_the_signalled_path(bt):
