@@ -1309,6 +1309,7 @@ static int launch_any(const GemmShape& g, int out_bf16, int grid, cudaStream_t s
     if (g.epi.kind == EPI_FFN_FWD || g.epi.kind == EPI_FFN_BWD) {  // ALU-heavy epilogues: 16 epilogue warps
       static const int ew = getenv("BT_FFN_EW") ? atoi(getenv("BT_FFN_EW")) : 16;  // A/B measurements
       if (ew == 8) return launch_gemm_pair<SP, true, MN, gemm::EPI_WARPS, AIM>(g, grid, s);
+      if (ew == 81 && gemm::EPI_WARPS == 8) return launch_gemm_pair<6, true, MN, 8, AIM, 1>(g, grid, s);  // A/B
       // 16 warps x ONE staging box each (a box is re-staged only after its last store has read it; a chunk's
       // ALU work is far longer than that read) leaves room for 5 k-block stages instead of 3
       static const int nb = getenv("BT_FFN_NB") ? atoi(getenv("BT_FFN_NB")) : 1;  // A/B measurements
